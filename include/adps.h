@@ -1,0 +1,204 @@
+/*
+ * adps.h -- C ABI of the B200-native AdpSplit densify operator.
+ *
+ * This is the drop-in boundary for the reference's split operator
+ * (arXiv 2605.06876 reference package, /root/reference/pkg/src/adpsplit).
+ * Every entry point names the reference function it replaces (file:line).
+ * Signatures use plain C types only: device pointers, sizes, POD structs.
+ * No allocation happens inside the hot calls; the plan owns all scratch.
+ *
+ * Threading: one plan per (device, stream); plans are independent and not
+ * re-entrant.  All device pointers must be on the plan's device.  `stream`
+ * is a cudaStream_t passed as void*.
+ *
+ * Status codes map onto the reference's exceptions in the Python shim:
+ *   ADPS_INVALID_ARG    -> ValueError          (argument validation)
+ *   ADPS_V_TOO_LARGE    -> ValueError          (ref/adc.py:154-157)
+ *   ADPS_DEGENERATE_RAY -> DegenerateRayError  (ref/child_init.py:61-63)
+ *   others              -> RuntimeError
+ */
+#ifndef ADPS_H_
+#define ADPS_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define ADPS_ABI_VERSION 1
+
+#if defined(__GNUC__)
+#define ADPS_API __attribute__((visibility("default")))
+#else
+#define ADPS_API
+#endif
+
+typedef enum {
+  ADPS_OK = 0,
+  ADPS_INVALID_ARG = 1,
+  ADPS_V_TOO_LARGE = 2,
+  ADPS_DEGENERATE_RAY = 3,
+  ADPS_CUDA_ERROR = 4,
+  ADPS_OOM = 5,
+  ADPS_BAD_STATE = 6
+} adps_status;
+
+/* Per-candidate outcome (ref/adc.py:198-226 branch order). */
+typedef enum { ADPS_CASE_SPLIT = 0, ADPS_CASE_FALLBACK = 1, ADPS_CASE_RESET = 2 } adps_case;
+
+typedef struct adps_plan adps_plan;
+
+/* Gaussians as structure-of-arrays fp32 device buffers (ref/scene.py:54-81).
+ * rot is (w, x, y, z).  sh_rest is [n, sh_rest_k, 3] or NULL when k == 0. */
+typedef struct {
+  const float* mu;       /* [n,3] */
+  const float* scale;    /* [n,3] */
+  const float* rot;      /* [n,4] */
+  const float* opacity;  /* [n]   */
+  const float* sh_dc;    /* [n,3] */
+  const float* sh_rest;  /* [n,k,3] or NULL */
+  int32_t sh_rest_k;
+} adps_gaussians;
+
+typedef struct {
+  float* mu;
+  float* scale;
+  float* rot;
+  float* opacity;
+  float* sh_dc;
+  float* sh_rest;        /* [n_out,k,3] or NULL when k == 0 */
+  int32_t sh_rest_k;
+} adps_gaussians_out;
+
+/* Mirrors AdpSplitConfig (ref/scene.py:147-180); t_interval is trainer-only. */
+typedef struct {
+  double tau_l1;
+  int32_t r_erode;
+  int32_t m_min;
+  int32_t l_bands;
+  int32_t n_max;
+  int32_t v_views;
+  int32_t reserved0;
+  double gamma_d;
+  double gamma_c;
+  double tau_g;
+  double tau_s;
+  double eta;
+  double eps;
+} adps_config;
+
+/* Host-visible results of phase 1 (one device->host copy). */
+typedef struct {
+  int64_t n_before;        /* N                                             */
+  int64_t n_out;           /* population after the step      */
+  int64_t n_keep;          /* survivors carried with their index           */
+  int64_t n_split;         /* |split_set|  (ref/adc.py:165)                */
+  int64_t n_clone;         /* |clone_set|                                  */
+  int64_t n_fallback;      /* candidates never dominant -> vanilla split   */
+  int64_t n_reset;         /* dominant but no usable proposal              */
+  int64_t n_children;      /* sum N_i over split candidates                */
+  int64_t n_inserted;      /* all appended Gaussians except clones         */
+  int64_t n_regions;       /* error regions over all sampled views         */
+  int64_t n_proposals;     /* regions with t* > 0                          */
+  int64_t merge_edges;     /* ref/adc.py:210                               */
+  int64_t n_partials;      /* tile-border component fragments (diagnostic) */
+  int32_t degenerate_ray;  /* nonzero -> DegenerateRayError                */
+  int32_t reserved1;
+} adps_counts;
+
+/* Report arrays owned by the plan; valid until the next phase 1.
+ * All are device pointers. */
+typedef struct {
+  const int32_t* cand_index;        /* [n_split] ascending Gaussian index      */
+  const int32_t* cand_case;         /* [n_split] adps_case                     */
+  const int32_t* cand_proposals;    /* [n_split]                               */
+  const int32_t* cand_merged;       /* [n_split] N_i (split case) else 0       */
+  const int32_t* regions_per_view;  /* [n_split, n_views]                      */
+  const int32_t* clone_index;       /* [n_clone] ascending                     */
+  int32_t n_views;
+} adps_report;
+
+/* One error region (ref/error_partition.py:27-41) with its pixel set reduced
+ * to exact integer moments; identical to the device record layout. */
+typedef struct {
+  int32_t view_pos;     /* position of the view in the sampled view ids     */
+  int32_t candidate;    /* Gaussian index                                   */
+  int32_t band;
+  int32_t minpix;       /* y*W + x of the first row-major pixel             */
+  int64_t moments[6];   /* n, Sx, Sy, Sxx, Sxy, Syy                          */
+} adps_region_record;
+
+ADPS_API int adps_abi_version(void);
+ADPS_API const char* adps_last_error(void);
+
+/* Plan: owns every scratch buffer sized for up to max_n Gaussians and
+ * max_views views of height x width pixels.  Buffers grow on demand. */
+ADPS_API adps_status adps_plan_create(adps_plan** plan, int32_t device, int64_t max_n,
+                             int32_t max_views, int32_t height, int32_t width);
+ADPS_API adps_status adps_plan_destroy(adps_plan* plan);
+
+/* Attribution render of n_views cameras: image [V,H,W,3] fp32 and dominant
+ * map [V,H,W] int32 (-1 where nothing contributes).
+ * Replaces raster.render (ref/raster.py:136-157) incl. visible_splats/project
+ * (ref/raster.py:61-117).  cams_host: V x 18 doubles in save_cameras order
+ * (ref/scene.py:339-347).  bg: 3 floats (host). */
+ADPS_API adps_status adps_render(adps_plan* plan, void* stream, const adps_gaussians* g, int64_t n,
+                        const double* cams_host, int32_t n_views, const float* bg,
+                        float* image, int32_t* dominant);
+
+/* Phase 1 of adpsplit_step (ref/adc.py:165-227): select, error maps,
+ * partition, region statistics, ever-dominant, child initialisation,
+ * cross-view merge and cap, per-candidate case, offsets.  Consumes the
+ * attribution of the sampled views (image/dominant, e.g. from adps_render)
+ * and gt for the same views.  Writes counts (host) after one sync.
+ * cams_host: the n_views sampled cameras, in ascending view-id order. */
+ADPS_API adps_status adps_step_phase1(adps_plan* plan, void* stream, const adps_gaussians* g, int64_t n,
+                             double extent, const double* grad_accum, const double* denom,
+                             const adps_config* cfg, const double* cams_host, int32_t n_views,
+                             const float* image, const float* gt, const int32_t* dominant,
+                             adps_counts* counts);
+
+/* Phase 2 (ref/adc.py:198-244): emit children, parent copies, fallback
+ * children, clones and survivors into caller-allocated arrays of
+ * counts.n_out rows plus index_map (old index or -1).
+ * fallback_normals: device, 6*n_fallback doubles drawn by the host from the
+ * caller's numpy Generator in ascending fallback order (ref/adc.py:97). */
+ADPS_API adps_status adps_step_phase2(adps_plan* plan, void* stream, const adps_gaussians* g,
+                             const double* fallback_normals, adps_gaussians_out* out,
+                             int64_t* index_map);
+
+ADPS_API adps_status adps_get_report(adps_plan* plan, adps_report* report);
+
+/* Stage-level parity access to the last phase 1 (device pointers):
+ * records[n] in production order, order[n] = record index in
+ * (candidate, view, band, first pixel) order (ref/adc.py:190-195),
+ * valid[n] = t* > 0 (ref/child_init.py:115-116).  When debug records are
+ * enabled, stats[n,10] = cx,cy,e1x,e1y,sigma1,sigma2,r,g,b,t* and
+ * child[n,16] = mu3, rot9 (row-major), scale3, valid; else NULL. */
+ADPS_API adps_status adps_get_regions(adps_plan* plan, const adps_region_record** records, const int32_t** order,
+                             const uint8_t** valid, const double** stats, const double** child,
+                             int64_t* n);
+ADPS_API adps_status adps_set_debug_records(adps_plan* plan, int32_t enabled);
+
+/* Optional diagnostic: when set, phase 1 also writes the eroded metric map
+ * m and the band map b (uint8 [V,H,W]) -- ref/error_partition.py:86-91.
+ * Pass NULLs to disable. */
+ADPS_API adps_status adps_set_debug_maps(adps_plan* plan, uint8_t* m_out, uint8_t* b_out);
+
+/* Phase timings of the last phase 1 / phase 2 in milliseconds (CUDA events
+ * recorded on `stream`; filled only when timing was enabled). */
+ADPS_API adps_status adps_set_timing(adps_plan* plan, int32_t enabled);
+ADPS_API adps_status adps_get_timing(adps_plan* plan, double* ms, int32_t max_entries, int32_t* n_entries,
+                            const char** names);
+
+/* DensifyStats feed (ref/adc.py:73-79): grad_accum[vis] += |vg|, denom[vis] += 1.
+ * viewspace_grad [n,2] fp32, visible [n] uint8. */
+ADPS_API adps_status adps_accumulate_stats(void* stream, double* grad_accum, double* denom,
+                                  const float* viewspace_grad, const uint8_t* visible, int64_t n);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* ADPS_H_ */

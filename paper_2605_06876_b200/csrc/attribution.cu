@@ -1,0 +1,479 @@
+// Error maps + partition + region moments over the sampled views.
+//
+// Replaces, for every sampled view at once:
+//   error_map / metric_map / erode / band_map   ref/error_partition.py:44-91
+//   partition (8-connected CCL per candidate/band) ref/error_partition.py:94-134
+//   the pixel sums behind region_stats            ref/error_partition.py:137-142
+//   ever_dominant                                 ref/adc.py:177-180
+//
+// Pass structure (all views in each launch):
+//   minmax_kernel     raw L1 (fp64, numpy order) -> per-view min/max
+//   thresholds_kernel per-view thresholds on x = raw - lo that reproduce
+//                     e = (raw-lo)/(hi-lo) > tau and the band floor exactly
+//   tile_kernel       32x32 tile: maps, r x r erosion with halo, key, union-find
+//                     CCL in shared memory, warp-aggregated integer moments;
+//                     interior components -> regions, edge components ->
+//                     partial fragments + border labels
+//   border_kernel     unions fragments across tile edges (global union-find)
+//   resolve_kernel    folds fragment moments into their roots
+//   partial_emit_kernel roots with area >= m_min -> regions
+#include <math.h>
+
+#include "adps_internal.cuh"
+#include "attribution.cuh"
+
+namespace adps {
+
+__device__ __forceinline__ double raw_l1(const float* __restrict__ img, const float* __restrict__ gt,
+                                         long long p) {
+  // np.abs(rendered - gt).sum(axis=-1) == (|d0| + |d1|) + |d2| in fp64
+  double a0 = fabs(dsub((double)img[3 * p + 0], (double)gt[3 * p + 0]));
+  double a1 = fabs(dsub((double)img[3 * p + 1], (double)gt[3 * p + 1]));
+  double a2 = fabs(dsub((double)img[3 * p + 2], (double)gt[3 * p + 2]));
+  return dadd(dadd(a0, a1), a2);
+}
+
+__global__ void minmax_kernel(const float* __restrict__ image, const float* __restrict__ gt,
+                              long long hw, unsigned long long* __restrict__ lohi) {
+  const int v = blockIdx.y;
+  const float* img = image + (long long)v * hw * 3;
+  const float* g = gt + (long long)v * hw * 3;
+  double lo = INFINITY, hi = 0.0;
+  for (long long p = (long long)blockIdx.x * blockDim.x + threadIdx.x; p < hw;
+       p += (long long)gridDim.x * blockDim.x) {
+    double r = raw_l1(img, g, p);
+    lo = fmin(lo, r);
+    hi = fmax(hi, r);
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    lo = fmin(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+    hi = fmax(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+  }
+  __shared__ double slo[32], shi[32];
+  int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  if (lane == 0) {
+    slo[wid] = lo;
+    shi[wid] = hi;
+  }
+  __syncthreads();
+  if (wid == 0) {
+    int nw = blockDim.x >> 5;
+    lo = lane < nw ? slo[lane] : INFINITY;
+    hi = lane < nw ? shi[lane] : 0.0;
+    for (int o = 16; o > 0; o >>= 1) {
+      lo = fmin(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+      hi = fmax(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+    }
+    if (lane == 0) {
+      // raw >= +0.0, so IEEE order == unsigned order of the bit patterns
+      atomicMin(&lohi[2 * v + 0], (unsigned long long)__double_as_longlong(lo));
+      atomicMax(&lohi[2 * v + 1], (unsigned long long)__double_as_longlong(hi));
+    }
+  }
+}
+
+// e(x) = x / d with x = fl(raw - lo) and d = fl(hi - lo); both predicates below
+// are monotone in x, so each is a single threshold on x.
+__device__ __forceinline__ bool m_pred(double x, double d, double tau) { return ddiv(x, d) > tau; }
+
+__device__ __forceinline__ double band_raw(double x, double d, double tau, double omt, double nb) {
+  // np.floor((e - tau) / (1.0 - tau) * l_bands)  (ref/error_partition.py:82)
+  return floor(dmul(ddiv(dsub(ddiv(x, d), tau), omt), nb));
+}
+
+__device__ double min_true(double d, int k, double tau, double omt, double nb) {
+  auto pred = [&](double x) -> bool { return k == 0 ? m_pred(x, d, tau) : band_raw(x, d, tau, omt, nb) >= (double)k; };
+  if (!pred(d)) return INFINITY;
+  long long lo = 0, hi = __double_as_longlong(d);   // pred(hi) true
+  if (pred(0.0)) return 0.0;
+  while (hi - lo > 1) {
+    long long mid = lo + (hi - lo) / 2;
+    if (pred(__longlong_as_double(mid))) hi = mid;
+    else lo = mid;
+  }
+  return __longlong_as_double(hi);
+}
+
+// thr[v*L + 0] = x threshold of m; thr[v*L + k] = x threshold of band >= k.
+__global__ void thresholds_kernel(const unsigned long long* __restrict__ lohi, int n_views, int L,
+                                  double tau, double* __restrict__ lo_out, double* __restrict__ thr) {
+  int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= n_views * L) return;
+  int v = t / L, k = t % L;
+  double lo = __longlong_as_double((long long)lohi[2 * v]);
+  double hi = __longlong_as_double((long long)lohi[2 * v + 1]);
+  if (k == 0) lo_out[v] = lo;
+  if (hi == lo) {  // error_map returns zeros: m false, band 0 (ref/error_partition.py:52-53)
+    thr[t] = INFINITY;
+    return;
+  }
+  double d = dsub(hi, lo);
+  double omt = dsub(1.0, tau);
+  thr[t] = min_true(d, k, tau, omt, (double)L);
+}
+
+// ----------------------------------------------------------------- tile pass
+struct TileSmem {
+  unsigned char mext[(kTileH + 2 * kMaxErodeHalo) * (kTileW + 2 * kMaxErodeHalo)];
+  unsigned char hor[(kTileH + 2 * kMaxErodeHalo) * kTileW];
+  unsigned char band[kTilePx];
+  unsigned char touch[kTilePx];
+  int d[kTilePx];
+  int label[kTilePx];
+  int slot[kTilePx];
+  int mom[6][kTilePx];
+  int n_part, n_reg;
+  unsigned long long base_part, base_reg;
+};
+
+__global__ void __launch_bounds__(kTileThreads) tile_kernel(TileParams P) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  TileSmem& S = *reinterpret_cast<TileSmem*>(smem_raw);
+  const int tid = threadIdx.x;
+  const int tiles_per_view = P.tiles_x * P.tiles_y;
+  const int v = blockIdx.x / tiles_per_view;
+  const int tile_in_view = blockIdx.x % tiles_per_view;
+  const int tyi = tile_in_view / P.tiles_x, txi = tile_in_view % P.tiles_x;
+  const int x0 = txi * kTileW, y0 = tyi * kTileH;
+  const int W = P.W, H = P.H;
+  const long long hw = (long long)W * H;
+  const float* img = P.image + (long long)v * hw * 3;
+  const float* gtv = P.gt + (long long)v * hw * 3;
+  const int* dom = P.dom + (long long)v * hw;
+  const double lo = P.lo[v];
+  const double* thr = P.thr + (long long)v * P.L;
+  const double x_m = thr[0];
+  const int r = P.r_erode;
+  const int hl = r > 1 ? r / 2 : 0;
+  const int hh = r > 1 ? r - r / 2 - 1 : 0;
+  const int ew = kTileW + hl + hh, eh = kTileH + hl + hh;
+
+  if (tid == 0) {
+    S.n_part = 0;
+    S.n_reg = 0;
+  }
+  // 1. pre-erosion metric on the haloed tile, band on the tile itself
+  for (int idx = tid; idx < ew * eh; idx += kTileThreads) {
+    int ex = idx % ew, ey = idx / ew;
+    int x = x0 - hl + ex, y = y0 - hl + ey;
+    unsigned char m = 0;
+    int tx = ex - hl, ty = ey - hl;
+    bool in_tile = tx >= 0 && tx < kTileW && ty >= 0 && ty < kTileH;
+    unsigned char b = 0;
+    if (x >= 0 && x < W && y >= 0 && y < H) {
+      long long p = (long long)y * W + x;
+      double xr = dsub(raw_l1(img, gtv, p), lo);
+      m = xr >= x_m;
+      if (in_tile) {
+        int bb = 0;
+        for (int k = 1; k < P.L; ++k) bb += xr >= thr[k];
+        b = (unsigned char)bb;
+      }
+    }
+    S.mext[ey * ew + ex] = m;
+    if (in_tile) S.band[ty * kTileW + tx] = b;
+  }
+  __syncthreads();
+  // 2. r x r erosion (offsets -(r//2) .. r-r//2-1; outside the image = 0), separable
+  if (r > 1) {
+    for (int idx = tid; idx < eh * kTileW; idx += kTileThreads) {
+      int tx = idx % kTileW, ey = idx / kTileW;
+      unsigned char a = 1;
+      for (int dx = -hl; dx <= hh; ++dx) a &= S.mext[ey * ew + tx + hl + dx];
+      S.hor[ey * kTileW + tx] = a;
+    }
+    __syncthreads();
+  }
+  // 3. keys + ever-dominant flags
+  for (int p = tid; p < kTilePx; p += kTileThreads) {
+    int tx = p % kTileW, ty = p / kTileW;
+    int x = x0 + tx, y = y0 + ty;
+    int key = -1;
+    unsigned char mer = 0;
+    if (x < W && y < H) {
+      if (r > 1) {
+        unsigned char a = 1;
+        for (int dy = -hl; dy <= hh; ++dy) a &= S.hor[(ty + hl + dy) * kTileW + tx];
+        mer = a;
+      } else {
+        mer = S.mext[ty * ew + tx];
+      }
+      int dd = __ldg(dom + (long long)y * W + x);
+      if (dd >= 0 && dd < P.N && __ldg(P.cls + dd) == 1) {
+        if (P.dom_flag[dd] == 0) P.dom_flag[dd] = 1;   // idempotent, race-benign
+        if (mer) key = dd;
+      }
+      if (P.dbg_m) {
+        long long q = (long long)v * hw + (long long)y * W + x;
+        P.dbg_m[q] = mer;
+        P.dbg_b[q] = S.band[p];
+      }
+    }
+    S.d[p] = key;
+    S.label[p] = key >= 0 ? p : -1;
+    S.touch[p] = 0;
+#pragma unroll
+    for (int k = 0; k < 6; ++k) S.mom[k][p] = 0;
+  }
+  __syncthreads();
+  // 4. unions with W, NW, N, NE neighbours of equal (candidate, band)
+  for (int p = tid; p < kTilePx; p += kTileThreads) {
+    int key = S.d[p];
+    if (key < 0) continue;
+    int tx = p % kTileW, ty = p / kTileW;
+    unsigned char b = S.band[p];
+    const int nx[4] = {-1, -1, 0, 1}, ny[4] = {0, -1, -1, -1};
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      int qx = tx + nx[k], qy = ty + ny[k];
+      if (qx < 0 || qx >= kTileW || qy < 0) continue;
+      int q = qy * kTileW + qx;
+      if (S.d[q] == key && S.band[q] == b) uf_unite(S.label, p, q);
+    }
+  }
+  __syncthreads();
+  for (int p = tid; p < kTilePx; p += kTileThreads)
+    if (S.d[p] >= 0) S.label[p] = uf_find(S.label, p);
+  __syncthreads();
+  // 5. warp-aggregated integer moments (tile-local coordinates, exact)
+  const bool left_in = x0 > 0, top_in = y0 > 0;
+  const bool right_in = x0 + kTileW < W, bottom_in = y0 + kTileH < H;
+  for (int p = tid; p < kTilePx; p += kTileThreads) {
+    bool keyed = S.d[p] >= 0;
+    unsigned act = __ballot_sync(0xffffffffu, keyed);
+    if (keyed) {
+      int root = S.label[p];
+      int tx = p % kTileW, ty = p / kTileW;
+      unsigned grp = __match_any_sync(act, root);
+      int v0 = __reduce_add_sync(grp, 1);
+      int v1 = __reduce_add_sync(grp, tx);
+      int v2 = __reduce_add_sync(grp, ty);
+      int v3 = __reduce_add_sync(grp, tx * tx);
+      int v4 = __reduce_add_sync(grp, tx * ty);
+      int v5 = __reduce_add_sync(grp, ty * ty);
+      if ((tid & 31) == __ffs(grp) - 1) {
+        atomicAdd(&S.mom[0][root], v0);
+        atomicAdd(&S.mom[1][root], v1);
+        atomicAdd(&S.mom[2][root], v2);
+        atomicAdd(&S.mom[3][root], v3);
+        atomicAdd(&S.mom[4][root], v4);
+        atomicAdd(&S.mom[5][root], v5);
+      }
+      bool edge = (tx == 0 && left_in) || (ty == 0 && top_in) || (tx == kTileW - 1 && right_in) ||
+                  (ty == kTileH - 1 && bottom_in);
+      if (edge) S.touch[root] = 1;
+    }
+  }
+  __syncthreads();
+  // 6. allocate record slots for roots
+  for (int p = tid; p < kTilePx; p += kTileThreads) {
+    S.slot[p] = -1;
+    if (S.d[p] < 0 || S.label[p] != p) continue;
+    if (S.touch[p]) S.slot[p] = atomicAdd(&S.n_part, 1);
+    else if (S.mom[0][p] >= P.m_min) S.slot[p] = atomicAdd(&S.n_reg, 1);
+  }
+  __syncthreads();
+  if (tid == 0) {
+    S.base_part = S.n_part ? atomicAdd(P.n_partials, (unsigned long long)S.n_part) : 0ull;
+    S.base_reg = S.n_reg ? atomicAdd(P.n_regions, (unsigned long long)S.n_reg) : 0ull;
+  }
+  __syncthreads();
+  for (int p = tid; p < kTilePx; p += kTileThreads) {
+    int s = S.slot[p];
+    if (s < 0) continue;
+    int rx = p % kTileW, ry = p / kTileW;
+    long long n = S.mom[0][p], m1 = S.mom[1][p], m2 = S.mom[2][p];
+    long long X = x0, Y = y0;
+    long long gm[6];
+    gm[0] = n;
+    gm[1] = m1 + n * X;
+    gm[2] = m2 + n * Y;
+    gm[3] = (long long)S.mom[3][p] + 2 * X * m1 + n * X * X;
+    gm[4] = (long long)S.mom[4][p] + X * m2 + Y * m1 + n * X * Y;
+    gm[5] = (long long)S.mom[5][p] + 2 * Y * m2 + n * Y * Y;
+    int minpix = (y0 + ry) * W + (x0 + rx);
+    if (S.touch[p]) {
+      unsigned long long gid = S.base_part + s;
+      if ((long long)gid < P.partial_cap) {
+        PartialRec& R = P.partials[gid];
+        R.view_pos = P.view_offset + v;
+        R.cand = S.d[p];
+        R.band = S.band[p];
+        R.minpix = minpix;
+        for (int k = 0; k < 6; ++k) R.m[k] = gm[k];
+        P.partial_parent[gid] = (int)gid;
+        S.slot[p] = (int)gid;
+      } else {
+        atomicOr(P.overflow, 2u);
+        S.slot[p] = -1;
+      }
+    } else {
+      unsigned long long rid = S.base_reg + s;
+      if ((long long)rid < P.region_cap) {
+        RegionRec& R = P.regions[rid];
+        R.view_pos = P.view_offset + v;
+        R.cand = S.d[p];
+        R.band = S.band[p];
+        R.minpix = minpix;
+        for (int k = 0; k < 6; ++k) R.m[k] = gm[k];
+      } else {
+        atomicOr(P.overflow, 1u);
+      }
+      S.slot[p] = -1;
+    }
+  }
+  __syncthreads();
+  // 7. border labels: top, bottom, left, right
+  int* border = P.border + (long long)blockIdx.x * kBorderSlots;
+  for (int s = tid; s < kBorderSlots; s += kTileThreads) {
+    int tx, ty;
+    if (s < kTileW) { tx = s; ty = 0; }
+    else if (s < 2 * kTileW) { tx = s - kTileW; ty = kTileH - 1; }
+    else if (s < 2 * kTileW + kTileH) { tx = 0; ty = s - 2 * kTileW; }
+    else { tx = kTileW - 1; ty = s - 2 * kTileW - kTileH; }
+    int p = ty * kTileW + tx;
+    int g = -1;
+    if (S.d[p] >= 0) g = S.slot[S.label[p]];
+    border[s] = g;
+  }
+}
+
+__device__ __forceinline__ int border_slot(int lx, int ly) {
+  if (ly == 0) return lx;
+  if (ly == kTileH - 1) return kTileW + lx;
+  if (lx == 0) return 2 * kTileW + ly;
+  return 2 * kTileW + kTileH + ly;   // lx == kTileW - 1
+}
+
+__global__ void border_kernel(BorderParams P) {
+  const int tiles_per_view = P.tiles_x * P.tiles_y;
+  const int v = blockIdx.x / tiles_per_view;
+  const int t = blockIdx.x % tiles_per_view;
+  const int tyi = t / P.tiles_x, txi = t % P.tiles_x;
+  const int s = threadIdx.x;
+  if (s >= kBorderSlots) return;
+  const int gp = P.border[(long long)blockIdx.x * kBorderSlots + s];
+  if (gp < 0) return;
+  int lx, ly;
+  if (s < kTileW) { lx = s; ly = 0; }
+  else if (s < 2 * kTileW) { lx = s - kTileW; ly = kTileH - 1; }
+  else if (s < 2 * kTileW + kTileH) { lx = 0; ly = s - 2 * kTileW; }
+  else { lx = kTileW - 1; ly = s - 2 * kTileW - kTileH; }
+  const int x = txi * kTileW + lx, y = tyi * kTileH + ly;
+  const PartialRec& A = P.partials[gp];
+  const int dxs[4] = {1, -1, 0, 1}, dys[4] = {0, 1, 1, 1};   // E, SW, S, SE
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    int qx = x + dxs[k], qy = y + dys[k];
+    if (qx < 0 || qx >= P.W || qy >= P.H) continue;
+    int qtx = qx / kTileW, qty = qy / kTileH;
+    if (qtx == txi && qty == tyi) continue;
+    long long qt = ((long long)v * P.tiles_y + qty) * P.tiles_x + qtx;
+    int gq = P.border[qt * kBorderSlots + border_slot(qx - qtx * kTileW, qy - qty * kTileH)];
+    if (gq < 0) continue;
+    const PartialRec& B = P.partials[gq];
+    if (A.cand == B.cand && A.band == B.band) uf_unite(P.parent, gp, gq);
+  }
+}
+
+__global__ void resolve_kernel(PartialRec* __restrict__ partials, int* __restrict__ parent,
+                               const unsigned long long* __restrict__ n_partials, long long cap) {
+  long long n = (long long)*n_partials;
+  if (n > cap) n = cap;
+  for (long long g = (long long)blockIdx.x * blockDim.x + threadIdx.x; g < n;
+       g += (long long)gridDim.x * blockDim.x) {
+    int root = uf_find(parent, (int)g);
+    if (root == (int)g) continue;
+    PartialRec& R = partials[root];
+    const PartialRec& A = partials[g];
+    for (int k = 0; k < 6; ++k)
+      atomicAdd(reinterpret_cast<unsigned long long*>(&R.m[k]), (unsigned long long)A.m[k]);
+    atomicMin(&R.minpix, A.minpix);
+  }
+}
+
+__global__ void partial_emit_kernel(const PartialRec* __restrict__ partials, const int* __restrict__ parent,
+                                    const unsigned long long* __restrict__ n_partials, long long pcap,
+                                    int m_min, RegionRec* __restrict__ regions,
+                                    unsigned long long* __restrict__ n_regions, long long rcap,
+                                    unsigned int* __restrict__ overflow) {
+  long long n = (long long)*n_partials;
+  if (n > pcap) n = pcap;
+  for (long long g = (long long)blockIdx.x * blockDim.x + threadIdx.x; g < n;
+       g += (long long)gridDim.x * blockDim.x) {
+    if (parent[g] != (int)g) continue;
+    const PartialRec& A = partials[g];
+    if (A.m[0] < m_min) continue;
+    unsigned long long rid = atomicAdd(n_regions, 1ull);
+    if ((long long)rid >= rcap) {
+      atomicOr(overflow, 1u);
+      continue;
+    }
+    RegionRec& R = regions[rid];
+    R.view_pos = A.view_pos;
+    R.cand = A.cand;
+    R.band = A.band;
+    R.minpix = A.minpix;
+    for (int k = 0; k < 6; ++k) R.m[k] = A.m[k];
+  }
+}
+
+// --------------------------------------------------------------- launchers
+size_t tile_smem_bytes() { return sizeof(TileSmem); }
+
+cudaError_t launch_attribution(const AttributionArgs& a, cudaStream_t s) {
+  const long long hw = (long long)a.H * a.W;
+  dim3 mg((unsigned)((hw + 256 * 8 - 1) / (256 * 8)), (unsigned)a.V);
+  if (mg.x > 1024) mg.x = 1024;
+  minmax_kernel<<<mg, 256, 0, s>>>(a.image, a.gt, hw, a.lohi);
+  int nt = a.V * a.L;
+  thresholds_kernel<<<(nt + 127) / 128, 128, 0, s>>>(a.lohi, a.V, a.L, a.tau, a.lo, a.thr);
+  TileParams P;
+  P.image = a.image;
+  P.gt = a.gt;
+  P.dom = a.dom;
+  P.H = a.H;
+  P.W = a.W;
+  P.tiles_x = (a.W + kTileW - 1) / kTileW;
+  P.tiles_y = (a.H + kTileH - 1) / kTileH;
+  P.view_offset = a.view_offset;
+  P.lo = a.lo;
+  P.thr = a.thr;
+  P.L = a.L;
+  P.r_erode = a.r_erode;
+  P.m_min = a.m_min;
+  P.cls = a.cls;
+  P.N = a.N;
+  P.dom_flag = a.dom_flag;
+  P.regions = a.regions;
+  P.n_regions = a.n_regions;
+  P.region_cap = a.region_cap;
+  P.partials = a.partials;
+  P.n_partials = a.n_partials;
+  P.partial_cap = a.partial_cap;
+  P.partial_parent = a.partial_parent;
+  P.border = a.border;
+  P.dbg_m = a.dbg_m;
+  P.dbg_b = a.dbg_b;
+  P.overflow = a.overflow;
+  const long long nblocks = (long long)P.tiles_x * P.tiles_y * a.V;
+  size_t smem = sizeof(TileSmem);
+  cudaError_t e = cudaFuncSetAttribute(tile_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  tile_kernel<<<(unsigned)nblocks, kTileThreads, smem, s>>>(P);
+  BorderParams B;
+  B.border = a.border;
+  B.partials = a.partials;
+  B.parent = a.partial_parent;
+  B.tiles_x = P.tiles_x;
+  B.tiles_y = P.tiles_y;
+  B.W = a.W;
+  B.H = a.H;
+  border_kernel<<<(unsigned)nblocks, 128, 0, s>>>(B);
+  resolve_kernel<<<a.grid_small, 256, 0, s>>>(a.partials, a.partial_parent, a.n_partials, a.partial_cap);
+  partial_emit_kernel<<<a.grid_small, 256, 0, s>>>(a.partials, a.partial_parent, a.n_partials, a.partial_cap,
+                                                    a.m_min, a.regions, a.n_regions, a.region_cap, a.overflow);
+  return cudaGetLastError();
+}
+
+}  // namespace adps

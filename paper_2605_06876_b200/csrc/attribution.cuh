@@ -1,0 +1,71 @@
+#pragma once
+
+#include "adps_internal.cuh"
+
+namespace adps {
+
+struct TileParams {
+  const float* image;
+  const float* gt;
+  const int* dom;
+  int H, W;
+  int tiles_x, tiles_y;
+  int view_offset;
+  const double* lo;
+  const double* thr;
+  int L, r_erode, m_min;
+  const unsigned char* cls;
+  int N;
+  unsigned char* dom_flag;
+  RegionRec* regions;
+  unsigned long long* n_regions;
+  long long region_cap;
+  PartialRec* partials;
+  unsigned long long* n_partials;
+  long long partial_cap;
+  int* partial_parent;
+  int* border;
+  unsigned char* dbg_m;
+  unsigned char* dbg_b;
+  unsigned int* overflow;
+};
+
+struct BorderParams {
+  const int* border;
+  const PartialRec* partials;
+  int* parent;
+  int tiles_x, tiles_y;
+  int W, H;
+};
+
+struct AttributionArgs {
+  const float* image;
+  const float* gt;
+  const int* dom;
+  int V, H, W, view_offset;
+  int L, r_erode, m_min;
+  double tau;
+  const unsigned char* cls;
+  int N;
+  unsigned char* dom_flag;
+  unsigned long long* lohi;   // [2V], preset to (+inf bits, 0)
+  double* lo;                 // [V]
+  double* thr;                // [V*L]
+  RegionRec* regions;
+  unsigned long long* n_regions;
+  long long region_cap;
+  PartialRec* partials;
+  unsigned long long* n_partials;
+  long long partial_cap;
+  int* partial_parent;
+  int* border;                // [V * tiles * kBorderSlots]
+  unsigned char* dbg_m;
+  unsigned char* dbg_b;
+  unsigned int* overflow;
+  unsigned grid_small;
+};
+
+size_t tile_smem_bytes();
+cudaError_t launch_attribution(const AttributionArgs& a, cudaStream_t s);
+
+}  // namespace adps

@@ -1,0 +1,779 @@
+// C-ABI implementation: the plan (owner of all scratch) and the phase
+// orchestration of adpsplit_step (ref/adc.py:143-245) on one stream.
+#include <cub/cub.cuh>
+#include <math.h>
+#include <stdarg.h>
+#include <stdio.h>
+#include <string.h>
+
+#include <string>
+#include <vector>
+
+#include "adps_internal.cuh"
+#include "attribution.cuh"
+#include "render.cuh"
+#include "split.cuh"
+
+using namespace adps;
+
+static thread_local std::string g_last_error;
+
+static adps_status fail(adps_status st, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_last_error = buf;
+  return st;
+}
+
+#define CK(call)                                                                             \
+  do {                                                                                       \
+    cudaError_t e_ = (call);                                                                 \
+    if (e_ != cudaSuccess) {                                                                 \
+      return fail(e_ == cudaErrorMemoryAllocation ? ADPS_OOM : ADPS_CUDA_ERROR, "%s: %s (%s:%d)", \
+                  #call, cudaGetErrorString(e_), __FILE__, __LINE__);                        \
+    }                                                                                        \
+  } while (0)
+
+namespace {
+
+struct Buf {
+  void* p = nullptr;
+  size_t bytes = 0;
+  template <class T>
+  T* as() const {
+    return reinterpret_cast<T*>(p);
+  }
+};
+
+cudaError_t ensure(Buf& b, size_t bytes) {
+  if (bytes == 0) bytes = 16;
+  if (b.bytes >= bytes) return cudaSuccess;
+  if (b.p) cudaFree(b.p);
+  b.p = nullptr;
+  b.bytes = 0;
+  size_t want = bytes + bytes / 8;   // headroom against small growth
+  cudaError_t e = cudaMalloc(&b.p, want);
+  if (e != cudaSuccess) return e;
+  b.bytes = want;
+  return cudaSuccess;
+}
+
+const char* kStageNames[] = {"select", "attribution", "child_init", "sort", "merge", "offsets", "emit"};
+constexpr int kStages = 7;
+
+}  // namespace
+
+struct adps_plan {
+  int device = 0;
+  int sm_count = 148;
+  // per-Gaussian
+  Buf cls, cand_rank, split_list, clone_list, dom_flag, keep_pos;
+  // per-candidate
+  Buf cand_start, cand_end, cand_nvalid, cand_case, cand_props, cand_merged, cand_ins, ins_off, fb_ord,
+      large_list, regions_per_view;
+  // per-view
+  Buf lohi, lo, thr, cams;
+  // tiles / fragments / regions
+  Buf border, partials, partial_parent, regions, props, valid, keys, vals, keys_sorted, vals_sorted;
+  Buf idx, uf, groups, children, dbg_stats, dbg_child;
+  Buf scan_val, scan_flag, scan_ticket, scan2_val, scan2_flag, scan2_ticket, cub_tmp;
+  Buf ctr;
+  Counters* ctr_host = nullptr;
+  unsigned long long* lohi_host = nullptr;
+  double* cams_host = nullptr;
+  int cams_host_cap = 0;
+  long long region_cap = 0, partial_cap = 0;
+  // render scratch
+  Buf r_key, r_key_sorted, r_order_in, r_order, r_tiles, r_rect, r_splat, r_offs, r_dup, r_dup_sorted,
+      r_tstart, r_tend, r_total, r_cams;
+  unsigned long long* r_total_host = nullptr;
+  // last phase-1 state
+  bool have_phase1 = false;
+  long long n = 0;
+  int V = 0, H = 0, W = 0;
+  adps_counts counts{};
+  double eta = 1.6;
+  int sh_k = 0;
+  // diagnostics
+  unsigned char* dbg_m = nullptr;
+  unsigned char* dbg_b = nullptr;
+  bool dbg_records = false;
+  bool timing = false;
+  cudaEvent_t ev[kStages + 1] = {};
+  double stage_ms[kStages] = {};
+};
+
+static adps_status scan_state(adps_plan* P, Buf& val, Buf& flag, Buf& ticket, long long n, ScanState* st) {
+  long long tiles = scan_tiles(n);
+  CK(ensure(val, sizeof(unsigned long long) * tiles));
+  CK(ensure(flag, sizeof(unsigned int) * tiles));
+  CK(ensure(ticket, sizeof(unsigned int)));
+  st->value = val.as<unsigned long long>();
+  st->flag = flag.as<unsigned int>();
+  st->ticket = ticket.as<unsigned int>();
+  (void)P;
+  return ADPS_OK;
+}
+
+extern "C" int adps_abi_version(void) { return ADPS_ABI_VERSION; }
+
+extern "C" const char* adps_last_error(void) { return g_last_error.c_str(); }
+
+extern "C" adps_status adps_plan_create(adps_plan** plan, int32_t device, int64_t max_n, int32_t max_views,
+                                        int32_t height, int32_t width) {
+  if (!plan) return fail(ADPS_INVALID_ARG, "plan pointer is NULL");
+  if (max_n < 0 || max_views < 0 || height < 0 || width < 0) return fail(ADPS_INVALID_ARG, "negative plan size");
+  int ndev = 0;
+  CK(cudaGetDeviceCount(&ndev));
+  if (device < 0 || device >= ndev) return fail(ADPS_INVALID_ARG, "device %d not present (%d devices)", device, ndev);
+  CK(cudaSetDevice(device));
+  adps_plan* P = new adps_plan();
+  P->device = device;
+  cudaDeviceGetAttribute(&P->sm_count, cudaDevAttrMultiProcessorCount, device);
+  cudaError_t e = cudaMallocHost(&P->ctr_host, sizeof(Counters));
+  if (e == cudaSuccess) e = cudaMallocHost(&P->r_total_host, sizeof(unsigned long long));
+  if (e != cudaSuccess) {
+    delete P;
+    return fail(ADPS_OOM, "pinned allocation failed: %s", cudaGetErrorString(e));
+  }
+  for (int i = 0; i <= kStages; ++i) cudaEventCreate(&P->ev[i]);
+  (void)max_n;
+  (void)max_views;
+  (void)height;
+  (void)width;
+  *plan = P;
+  return ADPS_OK;
+}
+
+extern "C" adps_status adps_plan_destroy(adps_plan* P) {
+  if (!P) return ADPS_OK;
+  cudaSetDevice(P->device);
+  cudaDeviceSynchronize();
+  Buf* bufs[] = {&P->cls, &P->cand_rank, &P->split_list, &P->clone_list, &P->dom_flag, &P->keep_pos,
+                 &P->cand_start, &P->cand_end, &P->cand_nvalid, &P->cand_case, &P->cand_props,
+                 &P->cand_merged, &P->cand_ins, &P->ins_off, &P->fb_ord, &P->large_list,
+                 &P->regions_per_view, &P->lohi, &P->lo, &P->thr, &P->cams, &P->border, &P->partials,
+                 &P->partial_parent, &P->regions, &P->props, &P->valid, &P->keys, &P->vals,
+                 &P->keys_sorted, &P->vals_sorted, &P->idx, &P->uf, &P->groups, &P->children,
+                 &P->dbg_stats, &P->dbg_child, &P->scan_val, &P->scan_flag, &P->scan_ticket,
+                 &P->scan2_val, &P->scan2_flag, &P->scan2_ticket, &P->cub_tmp, &P->ctr, &P->r_key,
+                 &P->r_key_sorted, &P->r_order_in, &P->r_order, &P->r_tiles, &P->r_rect, &P->r_splat,
+                 &P->r_offs, &P->r_dup, &P->r_dup_sorted, &P->r_tstart, &P->r_tend, &P->r_total,
+                 &P->r_cams};
+  for (Buf* b : bufs)
+    if (b->p) cudaFree(b->p);
+  if (P->ctr_host) cudaFreeHost(P->ctr_host);
+  if (P->lohi_host) cudaFreeHost(P->lohi_host);
+  if (P->cams_host) cudaFreeHost(P->cams_host);
+  if (P->r_total_host) cudaFreeHost(P->r_total_host);
+  for (int i = 0; i <= kStages; ++i)
+    if (P->ev[i]) cudaEventDestroy(P->ev[i]);
+  delete P;
+  return ADPS_OK;
+}
+
+static adps_status check_gaussians(const adps_gaussians* g, int64_t n) {
+  if (!g) return fail(ADPS_INVALID_ARG, "gaussians is NULL");
+  if (n > 0 && (!g->mu || !g->scale || !g->rot || !g->opacity || !g->sh_dc))
+    return fail(ADPS_INVALID_ARG, "gaussian arrays must be non-NULL");
+  if (g->sh_rest_k < 0 || g->sh_rest_k > 15) return fail(ADPS_INVALID_ARG, "sh_rest_k must be in [0,15]");
+  if (g->sh_rest_k > 0 && !g->sh_rest) return fail(ADPS_INVALID_ARG, "sh_rest is NULL with sh_rest_k > 0");
+  if (n > 0x7ffffff0LL) return fail(ADPS_INVALID_ARG, "n=%lld exceeds int32 indexing", (long long)n);
+  return ADPS_OK;
+}
+
+static GaussiansIn to_in(const adps_gaussians* g) {
+  GaussiansIn r;
+  r.mu = g->mu;
+  r.scale = g->scale;
+  r.rot = g->rot;
+  r.opacity = g->opacity;
+  r.sh_dc = g->sh_dc;
+  r.sh_rest = g->sh_rest;
+  r.sh_k = g->sh_rest_k;
+  return r;
+}
+
+// ------------------------------------------------------------------ render
+extern "C" adps_status adps_render(adps_plan* P, void* stream_v, const adps_gaussians* g, int64_t n,
+                                   const double* cams_host, int32_t n_views, const float* bg, float* image,
+                                   int32_t* dominant) {
+  if (!P) return fail(ADPS_INVALID_ARG, "plan is NULL");
+  adps_status st = check_gaussians(g, n);
+  if (st != ADPS_OK) return st;
+  if (n_views < 0 || (n_views > 0 && (!cams_host || !image || !dominant)))
+    return fail(ADPS_INVALID_ARG, "bad render arguments");
+  CK(cudaSetDevice(P->device));
+  cudaStream_t s = (cudaStream_t)stream_v;
+  const float bgv[3] = {bg ? bg[0] : 0.f, bg ? bg[1] : 0.f, bg ? bg[2] : 0.f};
+  if (n_views == 0) return ADPS_OK;
+  const CamD c0 = load_cam(cams_host);
+  const int W = c0.w, H = c0.h;
+  for (int v = 1; v < n_views; ++v) {
+    const CamD cv = load_cam(cams_host + 18ll * v);
+    if (cv.w != W || cv.h != H) return fail(ADPS_INVALID_ARG, "all views of one call must share H x W");
+  }
+  if (W <= 0 || H <= 0) return fail(ADPS_INVALID_ARG, "empty image");
+  const int tiles_x = (W + kRTile - 1) / kRTile, tiles_y = (H + kRTile - 1) / kRTile;
+  const int n_tiles = tiles_x * tiles_y;
+  const long long hw = (long long)H * W;
+  if (n == 0) {
+    // nothing contributes: image = bg, dominant = -1
+    std::vector<float> img((size_t)hw * 3);
+    for (long long p = 0; p < hw; ++p)
+      for (int c = 0; c < 3; ++c) img[3 * p + c] = bgv[c];
+    for (int v = 0; v < n_views; ++v) {
+      CK(cudaMemcpyAsync(image + (long long)v * hw * 3, img.data(), sizeof(float) * hw * 3, cudaMemcpyHostToDevice, s));
+      CK(cudaMemsetAsync(dominant + (long long)v * hw, 0xff, sizeof(int) * hw, s));
+    }
+    CK(cudaStreamSynchronize(s));
+    return ADPS_OK;
+  }
+  CK(ensure(P->r_key, sizeof(unsigned long long) * n));
+  CK(ensure(P->r_key_sorted, sizeof(unsigned long long) * n));
+  CK(ensure(P->r_order_in, sizeof(int) * n));
+  CK(ensure(P->r_order, sizeof(int) * n));
+  CK(ensure(P->r_tiles, sizeof(unsigned) * n));
+  CK(ensure(P->r_rect, sizeof(unsigned short) * 4 * n));
+  CK(ensure(P->r_splat, sizeof(SplatData) * n));
+  CK(ensure(P->r_offs, sizeof(unsigned) * n));
+  CK(ensure(P->r_tstart, sizeof(int) * n_tiles));
+  CK(ensure(P->r_tend, sizeof(int) * n_tiles));
+  CK(ensure(P->r_total, sizeof(unsigned long long)));
+  ScanState sst;
+  st = scan_state(P, P->scan_val, P->scan_flag, P->scan_ticket, n, &sst);
+  if (st != ADPS_OK) return st;
+  size_t tmp1 = 0;
+  CK(cub::DeviceRadixSort::SortPairs(nullptr, tmp1, P->r_key.as<unsigned long long>(),
+                                     P->r_key_sorted.as<unsigned long long>(), P->r_order_in.as<int>(),
+                                     P->r_order.as<int>(), (int)n, 0, 64, s));
+  CK(ensure(P->cub_tmp, tmp1));
+  const int tile_bits = ceil_log2((unsigned long long)n_tiles) > 0 ? ceil_log2((unsigned long long)n_tiles) : 1;
+  for (int v = 0; v < n_views; ++v) {
+    PreArgs pa;
+    pa.mu = g->mu;
+    pa.scale = g->scale;
+    pa.rot = g->rot;
+    pa.opacity = g->opacity;
+    pa.sh_dc = g->sh_dc;
+    pa.sh_rest = g->sh_rest;
+    pa.sh_k = g->sh_rest_k;
+    pa.n = n;
+    pa.cam = load_cam(cams_host + 18ll * v);
+    pa.W = W;
+    pa.H = H;
+    pa.depth_key = P->r_key.as<unsigned long long>();
+    pa.order_in = P->r_order_in.as<int>();
+    pa.tiles = P->r_tiles.as<unsigned>();
+    pa.rect = P->r_rect.as<unsigned short>();
+    pa.splat = P->r_splat.as<SplatData>();
+    CK(launch_preprocess(pa, s));
+    size_t tb = P->cub_tmp.bytes;
+    CK(cub::DeviceRadixSort::SortPairs(P->cub_tmp.p, tb, P->r_key.as<unsigned long long>(),
+                                       P->r_key_sorted.as<unsigned long long>(), P->r_order_in.as<int>(),
+                                       P->r_order.as<int>(), (int)n, 0, 64, s));
+    CK(launch_tile_count_scan(P->r_order.as<int>(), P->r_tiles.as<unsigned>(), P->r_offs.as<unsigned>(),
+                              P->r_total.as<unsigned long long>(), n, sst, s));
+    CK(cudaMemcpyAsync(P->r_total_host, P->r_total.p, sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    const long long n_dup = (long long)*P->r_total_host;
+    if (n_dup > 0x7fffffffLL) return fail(ADPS_INVALID_ARG, "tile list too long (%lld)", n_dup);
+    CK(ensure(P->r_dup, sizeof(unsigned long long) * (n_dup > 0 ? n_dup : 1)));
+    CK(ensure(P->r_dup_sorted, sizeof(unsigned long long) * (n_dup > 0 ? n_dup : 1)));
+    CK(cudaMemsetAsync(P->r_tstart.p, 0, sizeof(int) * n_tiles, s));
+    CK(cudaMemsetAsync(P->r_tend.p, 0, sizeof(int) * n_tiles, s));
+    if (n_dup > 0) {
+      DupArgs da;
+      da.order = P->r_order.as<int>();
+      da.tiles = P->r_tiles.as<unsigned>();
+      da.rect = P->r_rect.as<unsigned short>();
+      da.offs = P->r_offs.as<unsigned>();
+      da.n = n;
+      da.tiles_x = tiles_x;
+      da.keys = P->r_dup.as<unsigned long long>();
+      CK(launch_duplicate(da, s));
+      size_t tmp2 = 0;
+      CK(cub::DeviceRadixSort::SortKeys(nullptr, tmp2, P->r_dup.as<unsigned long long>(),
+                                        P->r_dup_sorted.as<unsigned long long>(), (int)n_dup, 32, 32 + tile_bits, s));
+      CK(ensure(P->cub_tmp, tmp2 > tmp1 ? tmp2 : tmp1));
+      tb = P->cub_tmp.bytes;
+      CK(cub::DeviceRadixSort::SortKeys(P->cub_tmp.p, tb, P->r_dup.as<unsigned long long>(),
+                                        P->r_dup_sorted.as<unsigned long long>(), (int)n_dup, 32, 32 + tile_bits, s));
+      CK(launch_tile_ranges(P->r_dup_sorted.as<unsigned long long>(), n_dup, P->r_tstart.as<int>(),
+                            P->r_tend.as<int>(), s));
+    }
+    BlendArgs ba;
+    ba.keys = P->r_dup_sorted.as<unsigned long long>();
+    ba.order = P->r_order.as<int>();
+    ba.splat = P->r_splat.as<SplatData>();
+    ba.tile_start = P->r_tstart.as<int>();
+    ba.tile_end = P->r_tend.as<int>();
+    ba.tiles_x = tiles_x;
+    ba.W = W;
+    ba.H = H;
+    for (int c = 0; c < 3; ++c) ba.bg[c] = bgv[c];
+    ba.image = image + (long long)v * hw * 3;
+    ba.dominant = dominant + (long long)v * hw;
+    CK(launch_blend(ba, n_tiles, s));
+  }
+  return ADPS_OK;
+}
+
+// ------------------------------------------------------------------ phase 1
+static void rec(adps_plan* P, int i, cudaStream_t s) {
+  if (P->timing) cudaEventRecord(P->ev[i], s);
+}
+
+static adps_status run_attribution(adps_plan* P, cudaStream_t s, int V, int H, int W, const adps_config* cfg,
+                                   int N, const float* image, const float* gt, const int32_t* dominant) {
+  for (int v = 0; v < V; ++v) {
+    P->lohi_host[2 * v] = 0x7ff0000000000000ull;   // +inf
+    P->lohi_host[2 * v + 1] = 0ull;                // +0.0
+  }
+  CK(cudaMemcpyAsync(P->lohi.p, P->lohi_host, sizeof(unsigned long long) * 2 * V, cudaMemcpyHostToDevice, s));
+  CK(cudaMemsetAsync(P->dom_flag.p, 0, (size_t)(N > 0 ? N : 1), s));
+  Counters* ctr = P->ctr.as<Counters>();
+  CK(cudaMemsetAsync(&ctr->n_regions, 0, sizeof(unsigned long long), s));
+  CK(cudaMemsetAsync(&ctr->n_partials, 0, sizeof(unsigned long long), s));
+  CK(cudaMemsetAsync(&ctr->overflow, 0, sizeof(unsigned int), s));
+  AttributionArgs a;
+  a.image = image;
+  a.gt = gt;
+  a.dom = dominant;
+  a.V = V;
+  a.H = H;
+  a.W = W;
+  a.view_offset = 0;
+  a.L = cfg->l_bands;
+  a.r_erode = cfg->r_erode;
+  a.m_min = cfg->m_min;
+  a.tau = cfg->tau_l1;
+  a.cls = P->cls.as<unsigned char>();
+  a.N = N;
+  a.dom_flag = P->dom_flag.as<unsigned char>();
+  a.lohi = P->lohi.as<unsigned long long>();
+  a.lo = P->lo.as<double>();
+  a.thr = P->thr.as<double>();
+  a.regions = P->regions.as<RegionRec>();
+  a.n_regions = &ctr->n_regions;
+  a.region_cap = P->region_cap;
+  a.partials = P->partials.as<PartialRec>();
+  a.n_partials = &ctr->n_partials;
+  a.partial_cap = P->partial_cap;
+  a.partial_parent = P->partial_parent.as<int>();
+  a.border = P->border.as<int>();
+  a.dbg_m = P->dbg_m;
+  a.dbg_b = P->dbg_b;
+  a.overflow = &ctr->overflow;
+  a.grid_small = (unsigned)(P->sm_count * 4);
+  CK(launch_attribution(a, s));
+  return ADPS_OK;
+}
+
+extern "C" adps_status adps_step_phase1(adps_plan* P, void* stream_v, const adps_gaussians* g, int64_t n,
+                                        double extent, const double* grad_accum, const double* denom,
+                                        const adps_config* cfg, const double* cams_host, int32_t n_views,
+                                        const float* image, const float* gt, const int32_t* dominant,
+                                        adps_counts* counts) {
+  if (!P) return fail(ADPS_INVALID_ARG, "plan is NULL");
+  P->have_phase1 = false;
+  adps_status st = check_gaussians(g, n);
+  if (st != ADPS_OK) return st;
+  if (!cfg || !counts) return fail(ADPS_INVALID_ARG, "cfg/counts is NULL");
+  if (n > 0 && (!grad_accum || !denom)) return fail(ADPS_INVALID_ARG, "stats arrays are NULL");
+  if (n_views < 1) return fail(ADPS_INVALID_ARG, "need at least one sampled view");
+  if (!cams_host || !image || !gt || !dominant) return fail(ADPS_INVALID_ARG, "view arrays are NULL");
+  if (!(cfg->tau_l1 > 0.0 && cfg->tau_l1 < 1.0)) return fail(ADPS_INVALID_ARG, "tau_l1 must lie in (0,1)");
+  if (cfg->l_bands < 1 || cfg->l_bands > 255) return fail(ADPS_INVALID_ARG, "l_bands must be in [1,255]");
+  if (cfg->n_max < 1) return fail(ADPS_INVALID_ARG, "n_max must be >= 1");
+  if (cfg->r_erode > 2 * kMaxErodeHalo + 1) return fail(ADPS_INVALID_ARG, "r_erode > %d unsupported", 2 * kMaxErodeHalo + 1);
+  if (!(extent > 0)) return fail(ADPS_INVALID_ARG, "scene extent must be > 0");
+  CK(cudaSetDevice(P->device));
+  cudaStream_t s = (cudaStream_t)stream_v;
+  const CamD c0 = load_cam(cams_host);
+  const int W = c0.w, H = c0.h, V = n_views;
+  for (int v = 1; v < V; ++v) {
+    const CamD cv = load_cam(cams_host + 18ll * v);
+    if (cv.w != W || cv.h != H) return fail(ADPS_INVALID_ARG, "all sampled views must share H x W");
+  }
+  if (W <= 0 || H <= 0) return fail(ADPS_INVALID_ARG, "empty image");
+  const long long hw = (long long)H * W;
+  const long long total_px = hw * V;
+  const int tiles_x = (W + kTileW - 1) / kTileW, tiles_y = (H + kTileH - 1) / kTileH;
+  const long long n_tiles = (long long)tiles_x * tiles_y * V;
+  const int N = (int)n;
+
+  // ---- buffers
+  const long long nn = n > 0 ? n : 1;
+  CK(ensure(P->cls, nn));
+  CK(ensure(P->cand_rank, 4 * nn));
+  CK(ensure(P->split_list, 4 * nn));
+  CK(ensure(P->clone_list, 4 * nn));
+  CK(ensure(P->dom_flag, nn));
+  CK(ensure(P->keep_pos, 4 * nn));
+  CK(ensure(P->lohi, 16ll * V));
+  CK(ensure(P->lo, 8ll * V));
+  CK(ensure(P->thr, 8ll * V * cfg->l_bands));
+  CK(ensure(P->cams, 8ll * 18 * V));
+  CK(ensure(P->border, 4ll * n_tiles * kBorderSlots));
+  CK(ensure(P->ctr, sizeof(Counters)));
+  if (P->cams_host_cap < V) {
+    if (P->cams_host) cudaFreeHost(P->cams_host);
+    if (P->lohi_host) cudaFreeHost(P->lohi_host);
+    CK(cudaMallocHost(&P->cams_host, sizeof(double) * 18 * V));
+    CK(cudaMallocHost(&P->lohi_host, sizeof(unsigned long long) * 2 * V));
+    P->cams_host_cap = V;
+  }
+  const long long region_bound = total_px / (cfg->m_min > 1 ? cfg->m_min : 1) + 1;
+  const long long partial_bound = n_tiles * (2 * kTileW + 2 * kTileH) + 1;
+  if (P->region_cap == 0) P->region_cap = region_bound < (1ll << 21) ? region_bound : (1ll << 21);
+  if (P->partial_cap == 0) P->partial_cap = partial_bound < (1ll << 21) ? partial_bound : (1ll << 21);
+  if (P->region_cap > region_bound) P->region_cap = region_bound;
+  if (P->partial_cap > partial_bound) P->partial_cap = partial_bound;
+  CK(ensure(P->regions, sizeof(RegionRec) * P->region_cap));
+  CK(ensure(P->partials, sizeof(PartialRec) * P->partial_cap));
+  CK(ensure(P->partial_parent, sizeof(int) * P->partial_cap));
+  memcpy(P->cams_host, cams_host, sizeof(double) * 18 * V);
+  CK(cudaMemcpyAsync(P->cams.p, P->cams_host, sizeof(double) * 18 * V, cudaMemcpyHostToDevice, s));
+  Counters* ctr = P->ctr.as<Counters>();
+  CK(cudaMemsetAsync(ctr, 0, sizeof(Counters), s));
+  rec(P, 0, s);
+
+  // ---- select (ref/adc.py:165)
+  ScanState sst, sst2;
+  st = scan_state(P, P->scan_val, P->scan_flag, P->scan_ticket, nn, &sst);
+  if (st != ADPS_OK) return st;
+  SelectArgs sa;
+  sa.scale = g->scale;
+  sa.ga = grad_accum;
+  sa.den = denom;
+  sa.tau_g = cfg->tau_g;
+  sa.tau_s_abs = cfg->tau_s * extent;
+  sa.n = n;
+  sa.cls = P->cls.as<unsigned char>();
+  sa.cand_rank = P->cand_rank.as<int>();
+  sa.split_list = P->split_list.as<int>();
+  sa.clone_list = P->clone_list.as<int>();
+  sa.ctr = ctr;
+  CK(launch_select(sa, sst, s));
+  rec(P, 1, s);
+
+  // ---- maps + partition + moments + ever-dominant (ref/adc.py:168-180)
+  for (int attempt = 0;; ++attempt) {
+    st = run_attribution(P, s, V, H, W, cfg, N, image, gt, dominant);
+    if (st != ADPS_OK) return st;
+    CK(cudaMemcpyAsync(P->ctr_host, ctr, sizeof(Counters), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    if (!P->ctr_host->overflow) break;
+    if (attempt > 0) return fail(ADPS_BAD_STATE, "region capacity overflow after regrow");
+    if (P->ctr_host->overflow & 1u) {
+      long long want = (long long)P->ctr_host->n_regions + (long long)P->ctr_host->n_partials + 1;
+      P->region_cap = want < region_bound ? want : region_bound;
+      CK(ensure(P->regions, sizeof(RegionRec) * P->region_cap));
+    }
+    if (P->ctr_host->overflow & 2u) {
+      long long want = (long long)P->ctr_host->n_partials + 1;
+      P->partial_cap = want < partial_bound ? want : partial_bound;
+      CK(ensure(P->partials, sizeof(PartialRec) * P->partial_cap));
+      CK(ensure(P->partial_parent, sizeof(int) * P->partial_cap));
+    }
+  }
+  const long long n_regions = (long long)P->ctr_host->n_regions;
+  const long long n_split = (long long)P->ctr_host->n_split;
+  const long long n_clone = (long long)P->ctr_host->n_clone;
+  rec(P, 2, s);
+
+  // ---- region stats + child init (ref/adc.py:172-176, 190-196)
+  const long long rc = n_regions > 0 ? n_regions : 1;
+  CK(ensure(P->props, sizeof(Proposal) * rc));
+  CK(ensure(P->valid, rc));
+  CK(ensure(P->keys, 8 * rc));
+  CK(ensure(P->vals, 4 * rc));
+  CK(ensure(P->keys_sorted, 8 * rc));
+  CK(ensure(P->vals_sorted, 4 * rc));
+  CK(ensure(P->idx, 4 * rc));
+  CK(ensure(P->uf, 4 * rc));
+  CK(ensure(P->groups, sizeof(GroupRec) * rc));
+  CK(ensure(P->children, sizeof(float) * 14 * rc));
+  if (P->dbg_records) {
+    CK(ensure(P->dbg_stats, sizeof(double) * 10 * rc));
+    CK(ensure(P->dbg_child, sizeof(double) * 16 * rc));
+  }
+  const int bits_v = ceil_log2((unsigned long long)V);
+  const int bits_b = ceil_log2((unsigned long long)cfg->l_bands);
+  const int bits_p = ceil_log2((unsigned long long)hw);
+  const int bits_c = ceil_log2((unsigned long long)(n_split > 0 ? n_split : 1));
+  const int total_bits = bits_c + bits_v + bits_b + bits_p;
+  if (total_bits > 64) return fail(ADPS_INVALID_ARG, "region sort key needs %d bits (> 64)", total_bits);
+  ChildArgs ca;
+  ca.regions = P->regions.as<RegionRec>();
+  ca.n_regions = &ctr->n_regions;
+  ca.region_cap = P->region_cap;
+  ca.g = to_in(g);
+  ca.cams = P->cams.as<double>();
+  ca.gt = gt;
+  ca.H = H;
+  ca.W = W;
+  ca.eps = cfg->eps;
+  ca.cand_rank = P->cand_rank.as<int>();
+  ca.bits_v = bits_v;
+  ca.bits_b = bits_b;
+  ca.bits_p = bits_p;
+  ca.props = P->props.as<Proposal>();
+  ca.valid = P->valid.as<unsigned char>();
+  ca.keys = P->keys.as<unsigned long long>();
+  ca.vals = P->vals.as<int>();
+  ca.dbg_stats = P->dbg_records ? P->dbg_stats.as<double>() : nullptr;
+  ca.dbg_child = P->dbg_records ? P->dbg_child.as<double>() : nullptr;
+  ca.ctr = ctr;
+  long long cgrid = (n_regions + 127) / 128;
+  ca.grid = (unsigned)(cgrid < 1 ? 1 : (cgrid > 65535 ? 65535 : cgrid));
+  if (n_regions > 0) CK(launch_child_init(ca, s));
+  rec(P, 3, s);
+
+  // ---- order (candidate, view, band, first pixel)  (ref/adc.py:190-195)
+  if (n_regions > 0) {
+    size_t tb = 0;
+    CK(cub::DeviceRadixSort::SortPairs(nullptr, tb, P->keys.as<unsigned long long>(),
+                                       P->keys_sorted.as<unsigned long long>(), P->vals.as<int>(),
+                                       P->vals_sorted.as<int>(), (int)n_regions, 0, total_bits > 0 ? total_bits : 1, s));
+    CK(ensure(P->cub_tmp, tb));
+    tb = P->cub_tmp.bytes;
+    CK(cub::DeviceRadixSort::SortPairs(P->cub_tmp.p, tb, P->keys.as<unsigned long long>(),
+                                       P->keys_sorted.as<unsigned long long>(), P->vals.as<int>(),
+                                       P->vals_sorted.as<int>(), (int)n_regions, 0, total_bits > 0 ? total_bits : 1, s));
+  }
+  const long long sc = n_split > 0 ? n_split : 1;
+  CK(ensure(P->cand_start, 4 * sc));
+  CK(ensure(P->cand_end, 4 * sc));
+  CK(ensure(P->cand_nvalid, 4 * sc));
+  CK(ensure(P->cand_case, 4 * sc));
+  CK(ensure(P->cand_props, 4 * sc));
+  CK(ensure(P->cand_merged, 4 * sc));
+  CK(ensure(P->cand_ins, 4 * sc));
+  CK(ensure(P->ins_off, 4 * sc));
+  CK(ensure(P->fb_ord, 4 * sc));
+  CK(ensure(P->large_list, 4 * sc));
+  CK(ensure(P->regions_per_view, 4 * sc * V));
+  CK(cudaMemsetAsync(P->cand_start.p, 0, 4 * sc, s));
+  CK(cudaMemsetAsync(P->cand_end.p, 0, 4 * sc, s));
+  CK(cudaMemsetAsync(P->cand_nvalid.p, 0, 4 * sc, s));
+  CK(cudaMemsetAsync(P->regions_per_view.p, 0, 4 * sc * V, s));
+  RangeArgs ra;
+  ra.keys_sorted = P->keys_sorted.as<unsigned long long>();
+  ra.vals_sorted = P->vals_sorted.as<int>();
+  ra.n = n_regions;
+  ra.shift_rank = bits_v + bits_b + bits_p;
+  ra.bits_v = bits_v;
+  ra.shift_view = bits_b + bits_p;
+  ra.valid = P->valid.as<unsigned char>();
+  ra.n_views = V;
+  ra.cand_start = P->cand_start.as<int>();
+  ra.cand_end = P->cand_end.as<int>();
+  ra.cand_nvalid = P->cand_nvalid.as<int>();
+  ra.regions_per_view = P->regions_per_view.as<int>();
+  long long rgrid = (n_regions + 255) / 256;
+  ra.grid = (unsigned)(rgrid < 1 ? 1 : (rgrid > 65535 ? 65535 : rgrid));
+  CK(launch_ranges(ra, s));
+  rec(P, 4, s);
+
+  // ---- per-candidate case, merge, cap (ref/adc.py:184-227)
+  MergeArgs ma;
+  ma.split_list = P->split_list.as<int>();
+  ma.cand_start = P->cand_start.as<int>();
+  ma.cand_end = P->cand_end.as<int>();
+  ma.cand_nvalid = P->cand_nvalid.as<int>();
+  ma.vals_sorted = P->vals_sorted.as<int>();
+  ma.valid = P->valid.as<unsigned char>();
+  ma.props = P->props.as<Proposal>();
+  ma.dom_flag = P->dom_flag.as<unsigned char>();
+  ma.opacity = g->opacity;
+  ma.gamma_d = cfg->gamma_d;
+  ma.gamma_c = cfg->gamma_c;
+  ma.n_max = cfg->n_max;
+  ma.large_threshold = 96;
+  ma.idx = P->idx.as<int>();
+  ma.uf = P->uf.as<int>();
+  ma.groups = P->groups.as<GroupRec>();
+  ma.children = P->children.as<float>();
+  ma.cand_case = P->cand_case.as<int>();
+  ma.cand_props = P->cand_props.as<int>();
+  ma.cand_merged = P->cand_merged.as<int>();
+  ma.cand_ins = P->cand_ins.as<int>();
+  ma.large_list = P->large_list.as<int>();
+  ma.ctr = ctr;
+  long long mgrid = (n_split + 7) / 8;
+  ma.grid = (unsigned)(mgrid < 1 ? 1 : (mgrid > (long long)P->sm_count * 16 ? P->sm_count * 16 : mgrid));
+  if (n_split > 0) CK(launch_merge(ma, s));
+  rec(P, 5, s);
+
+  // ---- offsets (ref/adc.py:229-244)
+  st = scan_state(P, P->scan2_val, P->scan2_flag, P->scan2_ticket, sc, &sst2);
+  if (st != ADPS_OK) return st;
+  OffsetArgs oa;
+  oa.n = n;
+  oa.cls = P->cls.as<unsigned char>();
+  oa.cand_rank = P->cand_rank.as<int>();
+  oa.cand_case = P->cand_case.as<int>();
+  oa.cand_ins = P->cand_ins.as<int>();
+  oa.ins_off = P->ins_off.as<int>();
+  oa.fb_ord = P->fb_ord.as<int>();
+  oa.keep_pos = P->keep_pos.as<int>();
+  oa.ctr = ctr;
+  oa.n_split_dev = &ctr->n_split;
+  CK(launch_offsets(oa, n_split, sst2, sst, s));
+  rec(P, 6, s);
+  CK(cudaMemcpyAsync(P->ctr_host, ctr, sizeof(Counters), cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  const Counters& C = *P->ctr_host;
+  if (P->timing) {
+    for (int i = 0; i < 6; ++i) {
+      float ms = 0;
+      cudaEventElapsedTime(&ms, P->ev[i], P->ev[i + 1]);
+      P->stage_ms[i] = ms;
+    }
+  }
+  adps_counts& K = P->counts;
+  K.n_before = n;
+  K.n_split = n_split;
+  K.n_clone = n_clone;
+  K.n_keep = (long long)C.n_keep;
+  K.n_inserted = (long long)C.n_inserted;
+  K.n_out = K.n_keep + K.n_inserted + n_clone;
+  K.n_fallback = (long long)C.n_fallback;
+  K.n_reset = (long long)C.n_reset;
+  K.n_children = (long long)C.n_children;
+  K.n_regions = n_regions;
+  K.n_proposals = 0;
+  K.merge_edges = (long long)C.merge_edges;
+  K.n_partials = (long long)C.n_partials;
+  K.degenerate_ray = C.degenerate ? 1 : 0;
+  *counts = K;
+  P->n = n;
+  P->V = V;
+  P->H = H;
+  P->W = W;
+  P->eta = cfg->eta;
+  P->sh_k = g->sh_rest_k;
+  P->have_phase1 = true;
+  if (C.degenerate) return fail(ADPS_DEGENERATE_RAY, "quadratic coefficient underflows (DegenerateRayError)");
+  return ADPS_OK;
+}
+
+extern "C" adps_status adps_step_phase2(adps_plan* P, void* stream_v, const adps_gaussians* g,
+                                        const double* fallback_normals, adps_gaussians_out* out,
+                                        int64_t* index_map) {
+  if (!P) return fail(ADPS_INVALID_ARG, "plan is NULL");
+  if (!P->have_phase1) return fail(ADPS_BAD_STATE, "phase 2 without a successful phase 1");
+  adps_status st = check_gaussians(g, P->n);
+  if (st != ADPS_OK) return st;
+  if (!out || !index_map) return fail(ADPS_INVALID_ARG, "outputs are NULL");
+  if (P->counts.n_fallback > 0 && !fallback_normals) return fail(ADPS_INVALID_ARG, "fallback normals are NULL");
+  if (g->sh_rest_k != P->sh_k || out->sh_rest_k != P->sh_k)
+    return fail(ADPS_INVALID_ARG, "sh_rest_k differs between phases/outputs");
+  if (P->sh_k > 0 && !out->sh_rest) return fail(ADPS_INVALID_ARG, "out.sh_rest is NULL");
+  CK(cudaSetDevice(P->device));
+  cudaStream_t s = (cudaStream_t)stream_v;
+  if (P->timing) cudaEventRecord(P->ev[0], s);
+  EmitArgs ea;
+  ea.g = to_in(g);
+  ea.n = P->n;
+  ea.n_split = P->counts.n_split;
+  ea.n_clone = P->counts.n_clone;
+  ea.n_keep = P->counts.n_keep;
+  ea.n_inserted = P->counts.n_inserted;
+  ea.keep_pos = P->keep_pos.as<int>();
+  ea.split_list = P->split_list.as<int>();
+  ea.clone_list = P->clone_list.as<int>();
+  ea.cand_case = P->cand_case.as<int>();
+  ea.cand_merged = P->cand_merged.as<int>();
+  ea.cand_start = P->cand_start.as<int>();
+  ea.ins_off = P->ins_off.as<int>();
+  ea.fb_ord = P->fb_ord.as<int>();
+  ea.children = P->children.as<float>();
+  ea.normals = fallback_normals;
+  ea.eta = P->eta;
+  ea.mu = out->mu;
+  ea.scale = out->scale;
+  ea.rot = out->rot;
+  ea.opacity = out->opacity;
+  ea.sh_dc = out->sh_dc;
+  ea.sh_rest = out->sh_rest;
+  ea.index_map = (long long*)index_map;
+  CK(launch_emit(ea, s));
+  if (P->timing) {
+    cudaEventRecord(P->ev[1], s);
+  }
+  return ADPS_OK;
+}
+
+extern "C" adps_status adps_get_report(adps_plan* P, adps_report* r) {
+  if (!P || !r) return fail(ADPS_INVALID_ARG, "NULL argument");
+  if (!P->have_phase1) return fail(ADPS_BAD_STATE, "no phase 1 result");
+  r->cand_index = P->split_list.as<int>();
+  r->cand_case = P->cand_case.as<int>();
+  r->cand_proposals = P->cand_props.as<int>();
+  r->cand_merged = P->cand_merged.as<int>();
+  r->regions_per_view = P->regions_per_view.as<int>();
+  r->clone_index = P->clone_list.as<int>();
+  r->n_views = P->V;
+  return ADPS_OK;
+}
+
+extern "C" adps_status adps_get_regions(adps_plan* P, const adps_region_record** records,
+                                        const int32_t** order, const uint8_t** valid, const double** stats,
+                                        const double** child, int64_t* n) {
+  if (!P || !records || !order || !valid || !stats || !child || !n) return fail(ADPS_INVALID_ARG, "NULL argument");
+  if (!P->have_phase1) return fail(ADPS_BAD_STATE, "no phase 1 result");
+  static_assert(sizeof(adps_region_record) == sizeof(RegionRec), "record layout");
+  *records = reinterpret_cast<const adps_region_record*>(P->regions.p);
+  *order = P->vals_sorted.as<int32_t>();
+  *valid = P->valid.as<uint8_t>();
+  *stats = P->dbg_records ? P->dbg_stats.as<double>() : nullptr;
+  *child = P->dbg_records ? P->dbg_child.as<double>() : nullptr;
+  *n = P->counts.n_regions;
+  return ADPS_OK;
+}
+
+extern "C" adps_status adps_set_debug_maps(adps_plan* P, uint8_t* m_out, uint8_t* b_out) {
+  if (!P) return fail(ADPS_INVALID_ARG, "plan is NULL");
+  if ((m_out == nullptr) != (b_out == nullptr)) return fail(ADPS_INVALID_ARG, "set both or neither");
+  P->dbg_m = m_out;
+  P->dbg_b = b_out;
+  return ADPS_OK;
+}
+
+extern "C" adps_status adps_set_debug_records(adps_plan* P, int32_t enabled) {
+  if (!P) return fail(ADPS_INVALID_ARG, "plan is NULL");
+  P->dbg_records = enabled != 0;
+  return ADPS_OK;
+}
+
+extern "C" adps_status adps_set_timing(adps_plan* P, int32_t enabled) {
+  if (!P) return fail(ADPS_INVALID_ARG, "plan is NULL");
+  P->timing = enabled != 0;
+  return ADPS_OK;
+}
+
+extern "C" adps_status adps_get_timing(adps_plan* P, double* ms, int32_t max_entries, int32_t* n_entries,
+                                       const char** names) {
+  if (!P || !n_entries) return fail(ADPS_INVALID_ARG, "NULL argument");
+  int n = 6 < max_entries ? 6 : max_entries;
+  for (int i = 0; i < n; ++i) {
+    if (ms) ms[i] = P->stage_ms[i];
+    if (names) names[i] = kStageNames[i];
+  }
+  *n_entries = n;
+  return ADPS_OK;
+}
+
+extern "C" adps_status adps_accumulate_stats(void* stream, double* grad_accum, double* denom,
+                                             const float* viewspace_grad, const uint8_t* visible, int64_t n) {
+  if (n < 0) return fail(ADPS_INVALID_ARG, "negative n");
+  if (n > 0 && (!grad_accum || !denom || !viewspace_grad || !visible)) return fail(ADPS_INVALID_ARG, "NULL array");
+  CK(launch_accumulate(grad_accum, denom, viewspace_grad, visible, n, (cudaStream_t)stream));
+  return ADPS_OK;
+}

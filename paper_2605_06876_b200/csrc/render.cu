@@ -1,0 +1,271 @@
+// Attribution render: image + dominant-Gaussian map per view.
+//
+// Replaces raster.render (ref/raster.py:136-157) with visible_splats,
+// project and _support_radius (ref/raster.py:61-117):
+//   * per-Gaussian projection in fp64 (cull rules of ref/raster.py:104-113)
+//   * exact (camera z, index) order: a stable radix sort of the fp64 depth
+//     bits gives each splat its depth rank; tile lists are then a stable sort
+//     on the tile id only, so every tile list is in reference order
+//   * 16x16 tiles, shared-memory splat batches, fp32 per-pixel alpha with
+//     tile-local offsets computed in fp64 (no large-coordinate cancellation)
+//   * front-to-back composite and strict argmax of T*alpha (front-most wins)
+//   * the reference has no early termination; a pixel stops only when its
+//     argmax can no longer change (T*0.99 <= best) AND the remaining image
+//     contribution is below 1e-8 (below fp32 resolution of the composite).
+#include <math.h>
+
+#include "render.cuh"
+
+namespace adps {
+
+__device__ __forceinline__ void sh_eval_rgb(const float* dc, const float* rest, int K, const double d[3],
+                                            float out[3]) {
+  const double x = d[0], y = d[1], z = d[2];
+  double basis[16];
+  basis[0] = kShC0;
+  const int n = 1 + K;
+  if (n > 1) {
+    basis[1] = -kShC1 * y;
+    basis[2] = kShC1 * z;
+    basis[3] = -kShC1 * x;
+  }
+  if (n > 4) {
+    const double xx = x * x, yy = y * y, zz = z * z;
+    basis[4] = 1.0925484305920792 * x * y;
+    basis[5] = -1.0925484305920792 * y * z;
+    basis[6] = 0.3153915652525205 * (2 * zz - xx - yy);
+    basis[7] = -1.0925484305920792 * x * z;
+    basis[8] = 0.5462742152960396 * (xx - yy);
+  }
+  if (n > 9) {
+    const double xx = x * x, yy = y * y, zz = z * z;
+    basis[9] = -0.5900435899266435 * y * (3 * xx - yy);
+    basis[10] = 2.890611442640554 * x * y * z;
+    basis[11] = -0.4570457994644658 * y * (4 * zz - xx - yy);
+    basis[12] = 0.3731763325901154 * z * (2 * zz - 3 * xx - 3 * yy);
+    basis[13] = -0.4570457994644658 * x * (4 * zz - xx - yy);
+    basis[14] = 1.445305721320277 * z * (xx - yy);
+    basis[15] = -0.5900435899266435 * x * (3 * yy - xx);
+  }
+  for (int c = 0; c < 3; ++c) {
+    double acc = basis[0] * (double)dc[c];
+    for (int k = 1; k < n; ++k) acc += basis[k] * (double)rest[3 * (k - 1) + c];
+    const double v = 0.5 + acc;
+    out[c] = (float)fmin(fmax(v, 0.0), 1.0);
+  }
+}
+
+__global__ void preprocess_kernel(PreArgs a) {
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= a.n) return;
+  const CamD& cam = a.cam;
+  const double mu[3] = {a.mu[3 * i], a.mu[3 * i + 1], a.mu[3 * i + 2]};
+  const double dl[3] = {mu[0] - cam.c[0], mu[1] - cam.c[1], mu[2] - cam.c[2]};
+  // p = R^T (mu - center)
+  const double x = cam.r[0] * dl[0] + cam.r[3] * dl[1] + cam.r[6] * dl[2];
+  const double y = cam.r[1] * dl[0] + cam.r[4] * dl[1] + cam.r[7] * dl[2];
+  const double z = cam.r[2] * dl[0] + cam.r[5] * dl[1] + cam.r[8] * dl[2];
+  unsigned long long key = ~0ull;
+  unsigned tiles = 0;
+  unsigned short rect[4] = {0, 0, 0, 0};
+  if (z > 1e-8) {
+    const double mx = cam.fx * x / z + cam.px, my = cam.fy * y / z + cam.py;
+    // cov2d = J W Sigma W^T J^T + 0.3 I
+    double q[4] = {a.rot[4 * i], a.rot[4 * i + 1], a.rot[4 * i + 2], a.rot[4 * i + 3]};
+    double R[9];
+    quat_to_rot(q, R);
+    const double s2[3] = {(double)a.scale[3 * i] * a.scale[3 * i], (double)a.scale[3 * i + 1] * a.scale[3 * i + 1],
+                          (double)a.scale[3 * i + 2] * a.scale[3 * i + 2]};
+    double S[6];
+    rdrt(R, s2, S);
+    const double Sm[9] = {S[0], S[1], S[2], S[1], S[3], S[4], S[2], S[4], S[5]};
+    // T = J W (2x3), W = R_c2w^T
+    const double j00 = cam.fx / z, j02 = -cam.fx * x / (z * z);
+    const double j11 = cam.fy / z, j12 = -cam.fy * y / (z * z);
+    double T[6];
+    for (int c = 0; c < 3; ++c) {
+      // W[r][c] = cam.r[c*3 + r]
+      T[c] = j00 * cam.r[c * 3 + 0] + j02 * cam.r[c * 3 + 2];
+      T[3 + c] = j11 * cam.r[c * 3 + 1] + j12 * cam.r[c * 3 + 2];
+    }
+    double TS[6];
+    for (int r = 0; r < 2; ++r)
+      for (int c = 0; c < 3; ++c)
+        TS[r * 3 + c] = T[r * 3 + 0] * Sm[0 * 3 + c] + T[r * 3 + 1] * Sm[1 * 3 + c] + T[r * 3 + 2] * Sm[2 * 3 + c];
+    const double ca = TS[0] * T[0] + TS[1] * T[1] + TS[2] * T[2] + kCov2dFloor;
+    const double cb = TS[0] * T[3] + TS[1] * T[4] + TS[2] * T[5];
+    const double cc = TS[3] * T[3] + TS[4] * T[4] + TS[5] * T[5] + kCov2dFloor;
+    const double o = a.opacity[i];
+    const double oc = fmin(o, kAlphaCapD);
+    if (oc >= kAlphaMinD) {
+      const double lam = 0.5 * (ca + cc + hypot(ca - cc, 2 * cb));
+      const double r = sqrt(2.0 * log(oc / kAlphaMinD) * lam);
+      const bool inside = !(mx + r < 0 || mx - r > a.W - 1 || my + r < 0 || my - r > a.H - 1);
+      if (r > 0.0 && inside) {
+        // binning radius: true opacity (may exceed the cap) plus a guard
+        const double rb = sqrt(2.0 * log(o / kAlphaMinD) * lam) * (1.0 + 1e-5) + 0.02;
+        int x0 = (int)ceil(mx - rb), x1 = (int)floor(mx + rb);
+        int y0 = (int)ceil(my - rb), y1 = (int)floor(my + rb);
+        x0 = max(x0, 0);
+        y0 = max(y0, 0);
+        x1 = min(x1, a.W - 1);
+        y1 = min(y1, a.H - 1);
+        key = (unsigned long long)__double_as_longlong(z);
+        if (x0 <= x1 && y0 <= y1) {
+          rect[0] = (unsigned short)(x0 / kRTile);
+          rect[1] = (unsigned short)(y0 / kRTile);
+          rect[2] = (unsigned short)(x1 / kRTile);
+          rect[3] = (unsigned short)(y1 / kRTile);
+          tiles = (unsigned)(rect[2] - rect[0] + 1) * (unsigned)(rect[3] - rect[1] + 1);
+        }
+        const double det = ca * cc - cb * cb;
+        const double ia = cc / det, ib = -cb / det, ic = ca / det;
+        SplatData sd;
+        sd.mx = mx;
+        sd.my = my;
+        sd.A = (float)(-0.5 * ia);
+        sd.B = (float)(-ib);
+        sd.C = (float)(-0.5 * ic);
+        sd.o = (float)o;
+        const double nd = sqrt(dl[0] * dl[0] + dl[1] * dl[1] + dl[2] * dl[2]);
+        const double dir[3] = {dl[0] / nd, dl[1] / nd, dl[2] / nd};
+        sh_eval_rgb(a.sh_dc + 3 * i, a.sh_rest ? a.sh_rest + 3ll * a.sh_k * i : nullptr, a.sh_k, dir, sd.rgb);
+        a.splat[i] = sd;
+      }
+    }
+  }
+  a.depth_key[i] = key;
+  a.order_in[i] = (int)i;
+  a.tiles[i] = tiles;
+  reinterpret_cast<ushort4*>(a.rect)[i] = make_ushort4(rect[0], rect[1], rect[2], rect[3]);
+}
+
+struct TileCountPolicy {
+  const int* order;
+  const unsigned* tiles;
+  unsigned* offs;
+  unsigned long long* total_out;
+  __device__ unsigned long long value(long long s) const { return tiles[order[s]]; }
+  __device__ void store(long long s, unsigned long long ex, unsigned long long) const { offs[s] = (unsigned)ex; }
+  __device__ void total(unsigned long long t) const { *total_out = t; }
+};
+
+__global__ void duplicate_kernel(DupArgs a) {
+  const long long s = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= a.n) return;
+  const int g = a.order[s];
+  const unsigned cnt = a.tiles[g];
+  if (!cnt) return;
+  const ushort4 r = reinterpret_cast<const ushort4*>(a.rect)[g];
+  unsigned long long off = a.offs[s];
+  for (int ty = r.y; ty <= r.w; ++ty)
+    for (int tx = r.x; tx <= r.z; ++tx) {
+      const unsigned long long t = (unsigned long long)(ty * a.tiles_x + tx);
+      a.keys[off++] = (t << 32) | (unsigned long long)s;
+    }
+}
+
+__global__ void tile_ranges_kernel(const unsigned long long* keys, long long n, int* start, int* end) {
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int t = (int)(keys[i] >> 32);
+  if (i == 0 || (int)(keys[i - 1] >> 32) != t) start[t] = (int)i;
+  if (i == n - 1 || (int)(keys[i + 1] >> 32) != t) end[t] = (int)(i + 1);
+}
+
+__global__ void __launch_bounds__(kRThreads) blend_kernel(BlendArgs a) {
+  struct Sm {
+    float mx, my, A, B, C, o, r, g, b;
+    int idx;
+  };
+  __shared__ Sm sm[kRThreads];
+  const int tile = blockIdx.x;
+  const int tyi = tile / a.tiles_x, txi = tile % a.tiles_x;
+  const int lx = threadIdx.x % kRTile, ly = threadIdx.x / kRTile;
+  const int x = txi * kRTile + lx, y = tyi * kRTile + ly;
+  const bool inside = x < a.W && y < a.H;
+  const double ox = (double)(txi * kRTile), oy = (double)(tyi * kRTile);
+  const int beg = a.tile_start[tile], end = a.tile_end[tile];
+  float T = 1.0f, best = 0.0f, cr = 0.0f, cg = 0.0f, cbl = 0.0f;
+  int bi = -1;
+  bool done = !inside;
+  const float fx = (float)lx, fy = (float)ly;
+  for (int base = beg; base < end; base += kRThreads) {
+    if (__syncthreads_count(done) == kRThreads) break;
+    const int j = base + threadIdx.x;
+    if (j < end) {
+      const int s = (int)(a.keys[j] & 0xffffffffull);
+      const int g = a.order[s];
+      const SplatData d = a.splat[g];
+      Sm e;
+      e.mx = (float)(d.mx - ox);
+      e.my = (float)(d.my - oy);
+      e.A = d.A;
+      e.B = d.B;
+      e.C = d.C;
+      e.o = d.o;
+      e.r = d.rgb[0];
+      e.g = d.rgb[1];
+      e.b = d.rgb[2];
+      e.idx = g;
+      sm[threadIdx.x] = e;
+    }
+    __syncthreads();
+    const int cnt = min(kRThreads, end - base);
+    for (int k = 0; k < cnt && !done; ++k) {
+      const Sm& e = sm[k];
+      const float dx = fx - e.mx, dy = fy - e.my;
+      const float power = e.A * dx * dx + e.B * dx * dy + e.C * dy * dy;
+      const float alpha = fminf(kAlphaCap, e.o * __expf(power));
+      if (alpha < kAlphaMin) continue;
+      const float w = T * alpha;
+      cr += w * e.r;
+      cg += w * e.g;
+      cbl += w * e.b;
+      if (w > best) {
+        best = w;
+        bi = e.idx;
+      }
+      T = T * (1.0f - alpha);
+      if (T < 1e-8f && T * kAlphaCap <= best) done = true;
+    }
+    __syncthreads();
+  }
+  if (inside) {
+    const long long p = (long long)y * a.W + x;
+    a.image[3 * p + 0] = cr + T * a.bg[0];
+    a.image[3 * p + 1] = cg + T * a.bg[1];
+    a.image[3 * p + 2] = cbl + T * a.bg[2];
+    a.dominant[p] = bi;
+  }
+}
+
+// ---------------------------------------------------------------- launchers
+cudaError_t launch_preprocess(const PreArgs& a, cudaStream_t s) {
+  if (a.n > 0) preprocess_kernel<<<(unsigned)((a.n + 255) / 256), 256, 0, s>>>(a);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_tile_count_scan(const int* order, const unsigned* tiles, unsigned* offs,
+                                   unsigned long long* total, long long n, ScanState st, cudaStream_t s) {
+  TileCountPolicy p{order, tiles, offs, total};
+  return launch_scan(p, n, st, s);
+}
+
+cudaError_t launch_duplicate(const DupArgs& a, cudaStream_t s) {
+  if (a.n > 0) duplicate_kernel<<<(unsigned)((a.n + 255) / 256), 256, 0, s>>>(a);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_tile_ranges(const unsigned long long* keys, long long n, int* start, int* end,
+                               cudaStream_t s) {
+  if (n > 0) tile_ranges_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(keys, n, start, end);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_blend(const BlendArgs& a, int n_tiles, cudaStream_t s) {
+  blend_kernel<<<n_tiles, kRThreads, 0, s>>>(a);
+  return cudaGetLastError();
+}
+
+}  // namespace adps

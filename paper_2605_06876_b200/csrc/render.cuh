@@ -1,0 +1,64 @@
+#pragma once
+
+#include "adps_internal.cuh"
+#include "scan.cuh"
+
+namespace adps {
+
+struct SplatData {
+  double mx, my;      // mean2d, fp64 (tile-local offsets are taken in fp64)
+  float A, B, C;      // power = A dx^2 + B dx dy + C dy^2 = -0.5 * quad
+  float o;
+  float rgb[3];
+  float pad;
+};
+
+struct PreArgs {
+  const float* mu;
+  const float* scale;
+  const float* rot;
+  const float* opacity;
+  const float* sh_dc;
+  const float* sh_rest;
+  int sh_k;
+  long long n;
+  CamD cam;
+  int W, H;
+  unsigned long long* depth_key;
+  int* order_in;
+  unsigned* tiles;
+  unsigned short* rect;   // [n,4]
+  SplatData* splat;
+};
+
+struct DupArgs {
+  const int* order;
+  const unsigned* tiles;
+  const unsigned short* rect;
+  const unsigned* offs;
+  long long n;
+  int tiles_x;
+  unsigned long long* keys;
+};
+
+struct BlendArgs {
+  const unsigned long long* keys;
+  const int* order;
+  const SplatData* splat;
+  const int* tile_start;
+  const int* tile_end;
+  int tiles_x, W, H;
+  float bg[3];
+  float* image;
+  int* dominant;
+};
+
+cudaError_t launch_preprocess(const PreArgs& a, cudaStream_t s);
+cudaError_t launch_tile_count_scan(const int* order, const unsigned* tiles, unsigned* offs,
+                                   unsigned long long* total, long long n, ScanState st, cudaStream_t s);
+cudaError_t launch_duplicate(const DupArgs& a, cudaStream_t s);
+cudaError_t launch_tile_ranges(const unsigned long long* keys, long long n, int* start, int* end,
+                               cudaStream_t s);
+cudaError_t launch_blend(const BlendArgs& a, int n_tiles, cudaStream_t s);
+
+}  // namespace adps

@@ -1,0 +1,132 @@
+// Single-pass exclusive scan with decoupled look-back.
+//
+// Used for every offset computation of the step (ref/adc.py:229-244
+// compaction, split/clone lists of ref/adc.py:82-89, per-candidate insert
+// offsets).  Values are uint64 "lanes": several independent counters can be
+// packed into one word (e.g. two 31-bit counts) and scanned together because
+// the operator is plain integer addition.
+#pragma once
+
+#include "adps_internal.cuh"
+
+namespace adps {
+
+constexpr int kScanThreads = 256;
+constexpr int kScanItems = 8;
+constexpr int kScanTile = kScanThreads * kScanItems;
+
+struct ScanState {
+  unsigned long long* value;  // [n_tiles]
+  unsigned int* flag;         // [n_tiles] 0 = empty, 1 = aggregate, 2 = inclusive prefix
+  unsigned int* ticket;       // [1] dynamic tile id (reset to 0 before launch)
+};
+
+// Policy requirements:
+//   __device__ unsigned long long value(long long i) const;
+//   __device__ void store(long long i, unsigned long long exclusive, unsigned long long v) const;
+//   __device__ void total(unsigned long long t) const;   // called once by the last tile
+template <class Policy>
+__global__ void __launch_bounds__(kScanThreads) scan_kernel(Policy pol, long long n, ScanState st) {
+  __shared__ unsigned long long sv[kScanTile];
+  __shared__ unsigned long long warp_sums[kScanThreads / kWarp];
+  __shared__ unsigned long long s_prefix;
+  __shared__ unsigned int s_tile;
+  const int tid = threadIdx.x;
+  if (tid == 0) s_tile = atomicAdd(st.ticket, 1u);
+  __syncthreads();
+  const long long tile = s_tile;
+  const long long base = tile * kScanTile;
+  // striped, coalesced load
+#pragma unroll
+  for (int j = 0; j < kScanItems; ++j) {
+    long long i = base + j * kScanThreads + tid;
+    sv[j * kScanThreads + tid] = (i < n) ? pol.value(i) : 0ull;
+  }
+  __syncthreads();
+  unsigned long long loc[kScanItems];
+  unsigned long long run = 0;
+#pragma unroll
+  for (int j = 0; j < kScanItems; ++j) {
+    loc[j] = sv[tid * kScanItems + j];
+    run += loc[j];
+  }
+  // block exclusive scan of per-thread sums
+  const int lane = tid & 31, wid = tid >> 5;
+  unsigned long long incl = run;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    unsigned long long y = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += y;
+  }
+  if (lane == 31) warp_sums[wid] = incl;
+  __syncthreads();
+  if (wid == 0) {
+    unsigned long long w = lane < kScanThreads / kWarp ? warp_sums[lane] : 0ull;
+    unsigned long long wi = w;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      unsigned long long y = __shfl_up_sync(0xffffffffu, wi, o);
+      if (lane >= o) wi += y;
+    }
+    if (lane < kScanThreads / kWarp) warp_sums[lane] = wi - w;  // exclusive
+  }
+  __syncthreads();
+  const unsigned long long thread_excl = warp_sums[wid] + incl - run;
+  if (tid == kScanThreads - 1) {
+    const unsigned long long agg = thread_excl + run;
+    volatile unsigned long long* vval = st.value;
+    volatile unsigned int* vflag = st.flag;
+    if (tile == 0) {
+      vval[0] = agg;
+      __threadfence();
+      vflag[0] = 2u;
+      s_prefix = 0ull;
+    } else {
+      vval[tile] = agg;
+      __threadfence();
+      vflag[tile] = 1u;
+      unsigned long long acc = 0ull;
+      long long p = tile - 1;
+      while (true) {
+        unsigned int f;
+        do {
+          f = vflag[p];
+        } while (f == 0u);
+        __threadfence();
+        unsigned long long v = vval[p];
+        acc += v;
+        if (f == 2u) break;
+        --p;
+      }
+      vval[tile] = acc + agg;
+      __threadfence();
+      vflag[tile] = 2u;
+      s_prefix = acc;
+    }
+    if (base + kScanTile >= n) pol.total(s_prefix + agg);
+  }
+  __syncthreads();
+  unsigned long long e = s_prefix + thread_excl;
+#pragma unroll
+  for (int j = 0; j < kScanItems; ++j) {
+    long long i = base + (long long)tid * kScanItems + j;
+    if (i < n) pol.store(i, e, loc[j]);
+    e += loc[j];
+  }
+}
+
+inline long long scan_tiles(long long n) { return n <= 0 ? 1 : (n + kScanTile - 1) / kScanTile; }
+
+// Launch helper: state buffers must hold scan_tiles(n) entries.
+template <class Policy>
+inline cudaError_t launch_scan(const Policy& pol, long long n, ScanState st, cudaStream_t s) {
+  long long tiles = scan_tiles(n);
+  cudaError_t e = cudaMemsetAsync(st.flag, 0, sizeof(unsigned int) * tiles, s);
+  if (e != cudaSuccess) return e;
+  e = cudaMemsetAsync(st.ticket, 0, sizeof(unsigned int), s);
+  if (e != cudaSuccess) return e;
+  scan_kernel<Policy><<<(unsigned)tiles, kScanThreads, 0, s>>>(pol, n, st);
+  return cudaGetLastError();
+}
+
+}  // namespace adps

@@ -1,0 +1,595 @@
+// Candidate selection, child initialisation, cross-view merge, offsets and
+// emission of the grown Gaussian arrays.
+//
+//   select              ref/adc.py:41-46, 82-89
+//   region_stats        ref/error_partition.py:137-158
+//   init_child          ref/child_init.py:44-140
+//   merge/cap/group     ref/cross_view_merge.py:33-116, ref/adc.py:123-140
+//   case logic          ref/adc.py:184-227
+//   compaction          ref/adc.py:229-244
+//   vanilla_split       ref/adc.py:92-108 (fallback, host-drawn normals)
+#include <math.h>
+
+#include "split.cuh"
+
+namespace adps {
+
+// ============================================================== select
+struct SelectPolicy {
+  SelectArgs a;
+  __device__ unsigned long long value(long long i) const {
+    double den = a.den[i];
+    double g = den > 0 ? ddiv(a.ga[i], den) : 0.0;
+    double s0 = a.scale[3 * i], s1 = a.scale[3 * i + 1], s2 = a.scale[3 * i + 2];
+    double ms = fmax(fmax(s0, s1), s2);
+    unsigned char c = 0;
+    if (g >= a.tau_g) c = ms > a.tau_s_abs ? 1 : 2;
+    a.cls[i] = c;
+    return c == 1 ? 1ull : (c == 2 ? (1ull << 32) : 0ull);
+  }
+  __device__ void store(long long i, unsigned long long ex, unsigned long long v) const {
+    if (v & 0xffffffffull) {
+      int r = (int)(ex & 0xffffffffull);
+      a.split_list[r] = (int)i;
+      a.cand_rank[i] = r;
+    } else {
+      a.cand_rank[i] = -1;
+    }
+    if (v >> 32) a.clone_list[(int)(ex >> 32)] = (int)i;
+  }
+  __device__ void total(unsigned long long t) const {
+    a.ctr->n_split = t & 0xffffffffull;
+    a.ctr->n_clone = t >> 32;
+  }
+};
+
+cudaError_t launch_select(const SelectArgs& a, ScanState st, cudaStream_t s) {
+  SelectPolicy p{a};
+  return launch_scan(p, a.n, st, s);
+}
+
+// ====================================================== region stats + child
+__device__ __forceinline__ double sclip(double x, double a) {
+  // np.sign(x) * min(abs(x), a)  (ref/child_init.py:75-76)
+  double s = x > 0 ? 1.0 : (x < 0 ? -1.0 : 0.0);
+  return s * fmin(fabs(x), a);
+}
+
+__global__ void child_init_kernel(ChildArgs a) {
+  long long n = (long long)*a.n_regions;
+  if (n > a.region_cap) n = a.region_cap;
+  for (long long rid = (long long)blockIdx.x * blockDim.x + threadIdx.x; rid < n;
+       rid += (long long)gridDim.x * blockDim.x) {
+    const RegionRec R = a.regions[rid];
+    // ---- region_stats (ref/error_partition.py:137-158), exact integer moments
+    const long long cnt = R.m[0];
+    const double nd = (double)cnt;
+    const double cx = (double)R.m[1] / nd, cy = (double)R.m[2] / nd;
+    const __int128 N = cnt;
+    const __int128 sxx = N * R.m[3] - (__int128)R.m[1] * R.m[1];
+    const __int128 sxy = N * R.m[4] - (__int128)R.m[1] * R.m[2];
+    const __int128 syy = N * R.m[5] - (__int128)R.m[2] * R.m[2];
+    const double nn = nd * nd;
+    const double ca = (double)sxx / nn, cb = (double)sxy / nn, cc = (double)syy / nn;
+    double l1, l2, e1x, e1y;
+    if (cb == 0.0) {
+      // diagonal: LAPACK returns the unit axes, e1 = column of the larger value
+      if (ca > cc) { l1 = ca; l2 = cc; e1x = 1.0; e1y = 0.0; }
+      else { l1 = cc; l2 = ca; e1x = 0.0; e1y = 1.0; }
+    } else {
+      double t = 0.5 * (ca - cc), m = 0.5 * (ca + cc);
+      double rr = hypot(t, cb);
+      l1 = m + rr;
+      l2 = m - rr;
+      double vx, vy;
+      if (ca >= cc) { vx = l1 - cc; vy = cb; }
+      else { vx = cb; vy = l1 - ca; }
+      double vn = hypot(vx, vy);
+      e1x = vx / vn;
+      e1y = vy / vn;
+    }
+    const double sig1 = fmax(sqrt(fmax(l1, 0.0)), kSigmaFloor);
+    const double sig2 = fmax(sqrt(fmax(l2, 0.0)), kSigmaFloor);
+    const double e2x = -e1y, e2y = e1x;
+    int ix = (int)rint(cx), iy = (int)rint(cy);   // round-half-even
+    ix = ix < 0 ? 0 : (ix > a.W - 1 ? a.W - 1 : ix);
+    iy = iy < 0 ? 0 : (iy > a.H - 1 ? a.H - 1 : iy);
+    const float* gp = a.gt + (((long long)R.view_pos * a.H + iy) * a.W + ix) * 3;
+    const double rgb[3] = {(double)gp[0], (double)gp[1], (double)gp[2]};
+
+    // ---- init_child (ref/child_init.py:110-140)
+    const CamD cam = load_cam(a.cams + 18ll * R.view_pos);
+    const int gi = R.cand;
+    const double dcam[3] = {(cx - cam.px) / cam.fx, (cy - cam.py) / cam.fy, 1.0};
+    double dw[3];
+    for (int i = 0; i < 3; ++i)
+      dw[i] = cam.r[i * 3 + 0] * dcam[0] + cam.r[i * 3 + 1] * dcam[1] + cam.r[i * 3 + 2] * dcam[2];
+    const double dwn = sqrt(dw[0] * dw[0] + dw[1] * dw[1] + dw[2] * dw[2]);
+    const double dir[3] = {dw[0] / dwn, dw[1] / dwn, dw[2] / dwn};
+    const double dnorm = sqrt(dcam[0] * dcam[0] + dcam[1] * dcam[1] + 1.0);
+    double q[4] = {a.g.rot[4 * gi], a.g.rot[4 * gi + 1], a.g.rot[4 * gi + 2], a.g.rot[4 * gi + 3]};
+    double pr[9];
+    quat_to_rot(q, pr);
+    const double ps[3] = {a.g.scale[3 * gi], a.g.scale[3 * gi + 1], a.g.scale[3 * gi + 2]};
+    const double inv2[3] = {1.0 / (ps[0] * ps[0]), 1.0 / (ps[1] * ps[1]), 1.0 / (ps[2] * ps[2])};
+    double prec[6];
+    rdrt(pr, inv2, prec);   // inv(covariance(parent)) = R diag(1/s^2) R^T
+    const double b[3] = {a.g.mu[3 * gi] - cam.c[0], a.g.mu[3 * gi + 1] - cam.c[1],
+                         a.g.mu[3 * gi + 2] - cam.c[2]};
+    const double denom = sym_quad(prec, dir);
+    double tstar = 0.0;
+    bool ok = true;
+    if (!(denom >= kDegenerateDenom)) {
+      atomicOr(&a.ctr->degenerate, 1u);
+      ok = false;
+    } else {
+      tstar = sym_bilin(prec, b, dir) / (denom + a.eps);
+      ok = tstar > 0.0;
+    }
+    double rot[9] = {0}, s1 = 0, s2 = 0, mu[3] = {0, 0, 0};
+    if (ok) {
+      const double smax = fmax(fmax(ps[0], ps[1]), ps[2]);
+      const double tz = tstar / dnorm;
+      const double w1x = sclip(e1x * sig1 * tz / cam.fx, smax * fabs(e1x));
+      const double w1y = sclip(e1y * sig1 * tz / cam.fy, smax * fabs(e1y));
+      const double w2x = sclip(e2x * sig2 * tz / cam.fx, smax * fabs(e2x));
+      const double w2y = sclip(e2y * sig2 * tz / cam.fy, smax * fabs(e2y));
+      double a1[3], a2[3], right[3], down[3], fwd[3];
+      for (int i = 0; i < 3; ++i) {
+        right[i] = cam.r[i * 3 + 0];
+        down[i] = cam.r[i * 3 + 1];
+        fwd[i] = cam.r[i * 3 + 2];
+        a1[i] = w1x * right[i] + w1y * down[i];
+        a2[i] = w2x * right[i] + w2y * down[i];
+      }
+      s1 = sqrt(a1[0] * a1[0] + a1[1] * a1[1] + a1[2] * a1[2]);
+      s2 = sqrt(a2[0] * a2[0] + a2[1] * a2[1] + a2[2] * a2[2]);
+      const double u1[3] = {a1[0] / s1, a1[1] / s1, a1[2] / s1};
+      double fb[3] = {fwd[1] * u1[2] - fwd[2] * u1[1], fwd[2] * u1[0] - fwd[0] * u1[2],
+                      fwd[0] * u1[1] - fwd[1] * u1[0]};
+      const double fbn = sqrt(fb[0] * fb[0] + fb[1] * fb[1] + fb[2] * fb[2]);
+      double fallback[3];
+      for (int i = 0; i < 3; ++i) fallback[i] = fbn > kParallelTol ? fb[i] / fbn : down[i];
+      const double proj = a2[0] * u1[0] + a2[1] * u1[1] + a2[2] * u1[2];
+      double rej[3] = {a2[0] - proj * u1[0], a2[1] - proj * u1[1], a2[2] - proj * u1[2]};
+      const double rn = sqrt(rej[0] * rej[0] + rej[1] * rej[1] + rej[2] * rej[2]);
+      double u2[3];
+      for (int i = 0; i < 3; ++i) u2[i] = rn < kParallelTol ? fallback[i] : rej[i] / rn;
+      for (int i = 0; i < 3; ++i) {
+        rot[i * 3 + 0] = u1[i];
+        rot[i * 3 + 1] = u2[i];
+        rot[i * 3 + 2] = fwd[i];
+      }
+      const double det = rot[0] * (rot[4] * rot[8] - rot[5] * rot[7]) -
+                         rot[1] * (rot[3] * rot[8] - rot[5] * rot[6]) +
+                         rot[2] * (rot[3] * rot[7] - rot[4] * rot[6]);
+      if (det < 0)
+        for (int i = 0; i < 3; ++i) rot[i * 3 + 2] = -rot[i * 3 + 2];
+      for (int i = 0; i < 3; ++i) mu[i] = cam.c[i] + tstar * dir[i];
+      Proposal P;
+      for (int i = 0; i < 3; ++i) {
+        P.mu[i] = mu[i];
+        P.rgb[i] = rgb[i];
+      }
+      const double sq[3] = {s1 * s1, s2 * s2, s2 * s2};
+      const double iq[3] = {1.0 / sq[0], 1.0 / sq[1], 1.0 / sq[2]};
+      rdrt(rot, sq, P.cov);
+      rdrt(rot, iq, P.prec);
+      a.props[rid] = P;
+    }
+    a.valid[rid] = ok ? 1 : 0;
+    const unsigned long long rank = (unsigned long long)a.cand_rank[gi];
+    a.keys[rid] = (((rank << a.bits_v | (unsigned long long)R.view_pos) << a.bits_b |
+                    (unsigned long long)R.band)
+                   << a.bits_p) |
+                  (unsigned long long)R.minpix;
+    a.vals[rid] = (int)rid;
+    if (a.dbg_stats) {
+      double* d = a.dbg_stats + 10 * rid;
+      d[0] = cx; d[1] = cy; d[2] = e1x; d[3] = e1y; d[4] = sig1; d[5] = sig2;
+      d[6] = rgb[0]; d[7] = rgb[1]; d[8] = rgb[2]; d[9] = tstar;
+      double* c = a.dbg_child + 16 * rid;
+      for (int i = 0; i < 3; ++i) c[i] = mu[i];
+      for (int i = 0; i < 9; ++i) c[3 + i] = rot[i];
+      c[12] = s1; c[13] = s2; c[14] = s2; c[15] = ok ? 1.0 : 0.0;
+    }
+  }
+}
+
+cudaError_t launch_child_init(const ChildArgs& a, cudaStream_t s) {
+  child_init_kernel<<<a.grid, 128, 0, s>>>(a);
+  return cudaGetLastError();
+}
+
+// ============================================================ ranges
+__global__ void ranges_kernel(RangeArgs a) {
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < a.n;
+       i += (long long)gridDim.x * blockDim.x) {
+    unsigned long long k = a.keys_sorted[i];
+    int rank = (int)(k >> a.shift_rank);
+    int view = (int)((k >> a.shift_view) & ((1ull << a.bits_v) - 1ull));
+    if (i == 0 || (int)(a.keys_sorted[i - 1] >> a.shift_rank) != rank) a.cand_start[rank] = (int)i;
+    if (i == a.n - 1 || (int)(a.keys_sorted[i + 1] >> a.shift_rank) != rank) a.cand_end[rank] = (int)(i + 1);
+    atomicAdd(&a.regions_per_view[(long long)rank * a.n_views + view], 1);
+    if (a.valid[a.vals_sorted[i]]) atomicAdd(&a.cand_nvalid[rank], 1);
+  }
+}
+
+cudaError_t launch_ranges(const RangeArgs& a, cudaStream_t s) {
+  if (a.n > 0) ranges_kernel<<<a.grid, 256, 0, s>>>(a);
+  return cudaGetLastError();
+}
+
+// ============================================================ merge
+// A "team" is one warp (small candidates) or one CTA (large candidates).
+template <int TEAM>
+__device__ __forceinline__ void team_sync() {
+  if (TEAM == 32) __syncwarp();
+  else __syncthreads();
+}
+
+__device__ __forceinline__ bool gate(const Proposal& A, const Proposal& B, double gd, double gc) {
+  // ref/cross_view_merge.py:33-41 (both thresholds inclusive)
+  const double dl[3] = {B.mu[0] - A.mu[0], B.mu[1] - A.mu[1], B.mu[2] - A.mu[2]};
+  const double d = sqrt(fmax(sym_quad(A.prec, dl), 0.0)) + sqrt(fmax(sym_quad(B.prec, dl), 0.0));
+  const double dc = fmax(fmax(fabs(A.rgb[0] - B.rgb[0]), fabs(A.rgb[1] - B.rgb[1])), fabs(A.rgb[2] - B.rgb[2]));
+  return d <= gd && dc <= gc;
+}
+
+template <int TEAM>
+__device__ void merge_candidate(const MergeArgs& a, int k, int rank_in_team, int P, int start,
+                                int* s_red) {
+  int* idx = a.idx + start;
+  int* uf = a.uf + start;
+  const int gi = a.split_list[k];
+  // 2. union-find over mergeable pairs (i < j)
+  for (int j = rank_in_team; j < P; j += TEAM) uf[j] = j;
+  team_sync<TEAM>();
+  for (int i = 0; i < P - 1; ++i) {
+    const Proposal& A = a.props[idx[i]];
+    for (int j = i + 1 + rank_in_team; j < P; j += TEAM)
+      if (gate(A, a.props[idx[j]], a.gamma_d, a.gamma_c)) uf_unite(uf, i, j);
+  }
+  team_sync<TEAM>();
+  __threadfence_block();
+  for (int j = rank_in_team; j < P; j += TEAM) uf[j] = uf_find(uf, j);
+  team_sync<TEAM>();
+  // 3. group parameters at each root (ref/cross_view_merge.py:44-69)
+  int my_groups = 0;
+  for (int g = rank_in_team; g < P; g += TEAM) {
+    if (uf[g] != g) continue;
+    ++my_groups;
+    double smu[3] = {0, 0, 0}, srgb[3] = {0, 0, 0}, scov[6] = {0, 0, 0, 0, 0, 0};
+    int cnt = 0;
+    for (int j = g; j < P; ++j) {
+      if (uf[j] != g) continue;
+      const Proposal& M = a.props[idx[j]];
+      for (int t = 0; t < 3; ++t) {
+        smu[t] += M.mu[t];
+        srgb[t] += M.rgb[t];
+      }
+      for (int t = 0; t < 6; ++t) scov[t] += M.cov[t];
+      ++cnt;
+    }
+    GroupRec G;
+    for (int t = 0; t < 3; ++t) {
+      G.mu[t] = smu[t] / cnt;
+      G.rgb[t] = srgb[t] / cnt;
+    }
+    double mcov[6];
+    for (int t = 0; t < 6; ++t) mcov[t] = scov[t] / cnt;
+    double lam0[3];
+    sym_eig3(mcov, lam0, G.evec);
+    double ext = 0.0;
+    for (int r = 0; r < 3; ++r) {
+      const double e[3] = {G.evec[0 * 3 + r], G.evec[1 * 3 + r], G.evec[2 * 3 + r]};
+      double best = 0.0;
+      for (int j = g; j < P; ++j) {
+        if (uf[j] != g) continue;
+        const Proposal& M = a.props[idx[j]];
+        const double off = fabs((M.mu[0] - G.mu[0]) * e[0] + (M.mu[1] - G.mu[1]) * e[1] +
+                                (M.mu[2] - G.mu[2]) * e[2]);
+        const double reach = off + sqrt(sym_quad(M.cov, e));
+        best = fmax(best, reach);
+      }
+      G.lam[r] = best * best;
+      ext = fmax(ext, G.lam[r]);
+    }
+    G.extent = ext;
+    a.groups[start + g] = G;
+  }
+  // team reduce of group count
+  for (int o = 16; o > 0; o >>= 1) my_groups += __shfl_xor_sync(0xffffffffu, my_groups, o);
+  if (TEAM > 32) {
+    if ((threadIdx.x & 31) == 0) s_red[threadIdx.x >> 5] = my_groups;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      int t = 0;
+      for (int w = 0; w < TEAM / 32; ++w) t += s_red[w];
+      s_red[TEAM / 32] = t;
+    }
+    __syncthreads();
+    my_groups = s_red[TEAM / 32];
+  }
+  const int G_count = my_groups;
+  __threadfence_block();
+  team_sync<TEAM>();
+  // 4. cap: stable order by descending extent (ref/cross_view_merge.py:110-116)
+  const int n_i = G_count < a.n_max ? G_count : a.n_max;
+  const double po = a.opacity[gi];
+  const float ocl = (float)fmin(fmax(po, 1e-6), 1.0 - 1e-6);
+  for (int g = rank_in_team; g < P; g += TEAM) {
+    if (uf[g] != g) continue;
+    const double eg = a.groups[start + g].extent;
+    int rk = 0;
+    for (int h = 0; h < P; ++h) {
+      if (uf[h] != h || h == g) continue;
+      const double eh = a.groups[start + h].extent;
+      rk += (eh > eg) || (eh == eg && h < g);
+    }
+    if (rk >= a.n_max) continue;
+    // 5. group -> Gaussian (ref/adc.py:127-140): eigh(merged_cov) ascending
+    const GroupRec& G = a.groups[start + g];
+    int o[3] = {0, 1, 2};
+    for (int i = 0; i < 3; ++i)
+      for (int j = i + 1; j < 3; ++j)
+        if (G.lam[o[j]] < G.lam[o[i]]) {
+          int t = o[i];
+          o[i] = o[j];
+          o[j] = t;
+        }
+    double ev[9], lam[3];
+    for (int c = 0; c < 3; ++c) {
+      lam[c] = G.lam[o[c]];
+      for (int r = 0; r < 3; ++r) ev[r * 3 + c] = G.evec[r * 3 + o[c]];
+    }
+    const double det = ev[0] * (ev[4] * ev[8] - ev[5] * ev[7]) - ev[1] * (ev[3] * ev[8] - ev[5] * ev[6]) +
+                       ev[2] * (ev[3] * ev[7] - ev[4] * ev[6]);
+    if (det < 0)
+      for (int r = 0; r < 3; ++r) ev[r * 3 + 0] = -ev[r * 3 + 0];
+    double qq[4];
+    rot_to_quat(ev, qq);
+    float* out = a.children + 14ll * (start + rk);
+    for (int t = 0; t < 3; ++t) out[t] = (float)G.mu[t];
+    for (int t = 0; t < 3; ++t) out[3 + t] = (float)sqrt(fmax(lam[t], 1e-16));
+    for (int t = 0; t < 4; ++t) out[6 + t] = (float)qq[t];
+    out[10] = ocl;
+    for (int t = 0; t < 3; ++t) out[11 + t] = (float)((G.rgb[t] - 0.5) / kShC0);
+  }
+  if (rank_in_team == 0) {
+    a.cand_case[k] = ADPS_CASE_SPLIT;
+    a.cand_merged[k] = n_i;
+    a.cand_ins[k] = n_i + 1;
+    atomicAdd(&a.ctr->merge_edges, (unsigned long long)(P - G_count));
+    atomicAdd(&a.ctr->n_children, (unsigned long long)n_i);
+  }
+}
+
+// Build idx[] (valid proposals in sorted order) with the first warp of a team.
+template <int TEAM>
+__device__ void collect_valid(const MergeArgs& a, int k, int start, int lane, int warp_in_team) {
+  if (warp_in_team != 0) return;
+  // the candidate's regions occupy sorted positions [cand_start, cand_end)
+  const int n_reg = a.cand_end[k] - start;
+  int out = 0;
+  for (int base = 0; base < n_reg; base += 32) {
+    int j = base + lane;
+    int rid = j < n_reg ? a.vals_sorted[start + j] : -1;
+    bool v = rid >= 0 && a.valid[rid];
+    unsigned bal = __ballot_sync(0xffffffffu, v);
+    if (v) a.idx[start + out + __popc(bal & ((1u << lane) - 1u))] = rid;
+    out += __popc(bal);
+  }
+}
+
+__global__ void merge_small_kernel(MergeArgs a) {
+  const int lane = threadIdx.x & 31;
+  const long long warps = (long long)gridDim.x * (blockDim.x >> 5);
+  const long long n_split = (long long)a.ctr->n_split;
+  for (long long k = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); k < n_split; k += warps) {
+    const int gi = a.split_list[k];
+    const int P = a.cand_nvalid[k];
+    if (!a.dom_flag[gi]) {   // never dominant in the sampled views -> vanilla fallback
+      if (lane == 0) {
+        a.cand_case[k] = ADPS_CASE_FALLBACK;
+        a.cand_merged[k] = 0;
+        a.cand_ins[k] = 2;
+        a.cand_props[k] = P;
+        atomicAdd(&a.ctr->n_fallback, 1ull);
+      }
+      continue;
+    }
+    if (P == 0) {            // dominant but no usable proposal -> reset
+      if (lane == 0) {
+        a.cand_case[k] = ADPS_CASE_RESET;
+        a.cand_merged[k] = 0;
+        a.cand_ins[k] = 0;
+        a.cand_props[k] = 0;
+        atomicAdd(&a.ctr->n_reset, 1ull);
+      }
+      continue;
+    }
+    if (P > a.large_threshold) {
+      if (lane == 0) {
+        unsigned long long s = atomicAdd(&a.ctr->n_large, 1ull);
+        a.large_list[s] = (int)k;
+      }
+      continue;
+    }
+    const int start = a.cand_start[k];
+    collect_valid<32>(a, k, start, lane, 0);
+    __syncwarp();
+    merge_candidate<32>(a, (int)k, lane, P, start, nullptr);
+    if (lane == 0) a.cand_props[k] = P;
+  }
+}
+
+__global__ void __launch_bounds__(256) merge_large_kernel(MergeArgs a) {
+  __shared__ int s_red[16];
+  const long long n_large = (long long)a.ctr->n_large;
+  for (long long t = blockIdx.x; t < n_large; t += gridDim.x) {
+    const int k = a.large_list[t];
+    const int P = a.cand_nvalid[k];
+    const int start = a.cand_start[k];
+    collect_valid<256>(a, k, start, threadIdx.x & 31, threadIdx.x >> 5);
+    __syncthreads();
+    merge_candidate<256>(a, k, threadIdx.x, P, start, s_red);
+    __syncthreads();
+    if (threadIdx.x == 0) a.cand_props[k] = P;
+    __syncthreads();
+  }
+}
+
+cudaError_t launch_merge(const MergeArgs& a, cudaStream_t s) {
+  merge_small_kernel<<<a.grid, 256, 0, s>>>(a);
+  merge_large_kernel<<<a.grid, 256, 0, s>>>(a);
+  return cudaGetLastError();
+}
+
+// ============================================================ offsets
+struct CandScanPolicy {
+  OffsetArgs a;
+  __device__ unsigned long long value(long long k) const {
+    unsigned long long v = (unsigned long long)a.cand_ins[k];
+    if (a.cand_case[k] == ADPS_CASE_FALLBACK) v |= 1ull << 32;
+    return v;
+  }
+  __device__ void store(long long k, unsigned long long ex, unsigned long long) const {
+    a.ins_off[k] = (int)(ex & 0xffffffffull);
+    a.fb_ord[k] = (int)(ex >> 32);
+  }
+  __device__ void total(unsigned long long t) const { a.ctr->n_inserted = t & 0xffffffffull; }
+};
+
+struct KeepScanPolicy {
+  OffsetArgs a;
+  __device__ unsigned long long value(long long i) const {
+    const int r = a.cand_rank[i];
+    if (r < 0) return 1ull;
+    const int c = a.cand_case[r];
+    return c == ADPS_CASE_RESET ? 1ull : 0ull;
+  }
+  __device__ void store(long long i, unsigned long long ex, unsigned long long v) const {
+    a.keep_pos[i] = v ? (int)ex : -1;
+  }
+  __device__ void total(unsigned long long t) const { a.ctr->n_keep = t; }
+};
+
+cudaError_t launch_offsets(const OffsetArgs& a, long long n_split, ScanState st_c, ScanState st_g,
+                           cudaStream_t s) {
+  cudaError_t e = launch_scan(CandScanPolicy{a}, n_split, st_c, s);
+  if (e != cudaSuccess) return e;
+  return launch_scan(KeepScanPolicy{a}, a.n, st_g, s);
+}
+
+// ============================================================ emit
+__device__ __forceinline__ void copy_gaussian(const EmitArgs& a, long long src, long long dst) {
+  for (int t = 0; t < 3; ++t) {
+    a.mu[3 * dst + t] = a.g.mu[3 * src + t];
+    a.scale[3 * dst + t] = a.g.scale[3 * src + t];
+    a.sh_dc[3 * dst + t] = a.g.sh_dc[3 * src + t];
+  }
+  for (int t = 0; t < 4; ++t) a.rot[4 * dst + t] = a.g.rot[4 * src + t];
+  a.opacity[dst] = a.g.opacity[src];
+  const int K = a.g.sh_k;
+  for (int t = 0; t < 3 * K; ++t) a.sh_rest[3ll * K * dst + t] = a.g.sh_rest[3ll * K * src + t];
+}
+
+__global__ void emit_kernel(EmitArgs a) {
+  const long long total = a.n + a.n_split + a.n_clone;
+  const long long ins_base = a.n_keep;
+  const long long clone_base = a.n_keep + a.n_inserted;
+  const int K = a.g.sh_k;
+  for (long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x; t < total;
+       t += (long long)gridDim.x * blockDim.x) {
+    if (t < a.n) {                                        // survivors, old order
+      const int pos = a.keep_pos[t];
+      if (pos >= 0) {
+        copy_gaussian(a, t, pos);
+        a.index_map[pos] = t;
+      }
+    } else if (t < a.n + a.n_split) {                     // candidate inserts, ascending index
+      const long long k = t - a.n;
+      const int c = a.cand_case[k];
+      if (c == ADPS_CASE_RESET) continue;
+      const long long gi = a.split_list[k];
+      long long dst = ins_base + a.ins_off[k];
+      if (c == ADPS_CASE_FALLBACK) {                      // vanilla_split(parent, 2, eta, rng)
+        double q[4] = {a.g.rot[4 * gi], a.g.rot[4 * gi + 1], a.g.rot[4 * gi + 2], a.g.rot[4 * gi + 3]};
+        double R[9];
+        quat_to_rot(q, R);
+        const double s[3] = {a.g.scale[3 * gi], a.g.scale[3 * gi + 1], a.g.scale[3 * gi + 2]};
+        const double sh = a.eta * 2.0;
+        const double* z = a.normals + 6ll * a.fb_ord[k];
+        for (int c2 = 0; c2 < 2; ++c2, ++dst) {
+          const double dl[3] = {z[3 * c2] * s[0], z[3 * c2 + 1] * s[1], z[3 * c2 + 2] * s[2]};
+          copy_gaussian(a, gi, dst);
+          for (int i = 0; i < 3; ++i) {
+            const double off = R[i * 3] * dl[0] + R[i * 3 + 1] * dl[1] + R[i * 3 + 2] * dl[2];
+            a.mu[3 * dst + i] = (float)((double)a.g.mu[3 * gi + i] + off);
+            a.scale[3 * dst + i] = (float)(s[i] / sh);
+          }
+          a.index_map[dst] = -1;
+        }
+      } else {                                            // N_i children then the parent copy
+        const int ni = a.cand_merged[k];
+        const float* ch = a.children + 14ll * a.cand_start[k];
+        for (int j = 0; j < ni; ++j, ++dst) {
+          const float* c3 = ch + 14 * j;
+          for (int u = 0; u < 3; ++u) {
+            a.mu[3 * dst + u] = c3[u];
+            a.scale[3 * dst + u] = c3[3 + u];
+            a.sh_dc[3 * dst + u] = c3[11 + u];
+          }
+          for (int u = 0; u < 4; ++u) a.rot[4 * dst + u] = c3[6 + u];
+          a.opacity[dst] = c3[10];
+          for (int u = 0; u < 3 * K; ++u) a.sh_rest[3ll * K * dst + u] = 0.0f;
+          a.index_map[dst] = -1;
+        }
+        copy_gaussian(a, gi, dst);
+        const double o = (double)a.g.opacity[gi] / (double)(ni + 1);
+        a.opacity[dst] = (float)fmin(fmax(o, 1e-6), 1.0 - 1e-6);
+        a.index_map[dst] = -1;
+      }
+    } else {                                              // clones, ascending
+      const long long j = t - a.n - a.n_split;
+      const long long dst = clone_base + j;
+      copy_gaussian(a, a.clone_list[j], dst);
+      a.index_map[dst] = -1;
+    }
+  }
+}
+
+cudaError_t launch_emit(const EmitArgs& a, cudaStream_t s) {
+  const long long total = a.n + a.n_split + a.n_clone;
+  if (total > 0) {
+    long long blocks = (total + 255) / 256;
+    if (blocks > 148 * 16) blocks = 148 * 16;
+    emit_kernel<<<(unsigned)blocks, 256, 0, s>>>(a);
+  }
+  return cudaGetLastError();
+}
+
+// ============================================================ stats feed
+__global__ void accumulate_kernel(double* ga, double* den, const float* vg, const unsigned char* vis,
+                                  long long n) {
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x) {
+    if (!vis[i]) continue;
+    const double x = vg[2 * i], y = vg[2 * i + 1];
+    ga[i] += sqrt(x * x + y * y);
+    den[i] += 1.0;
+  }
+}
+
+cudaError_t launch_accumulate(double* ga, double* den, const float* vg, const unsigned char* vis,
+                              long long n, cudaStream_t s) {
+  if (n > 0) {
+    long long blocks = (n + 255) / 256;
+    if (blocks > 148 * 8) blocks = 148 * 8;
+    accumulate_kernel<<<(unsigned)blocks, 256, 0, s>>>(ga, den, vg, vis, n);
+  }
+  return cudaGetLastError();
+}
+
+}  // namespace adps

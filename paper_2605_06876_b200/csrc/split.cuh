@@ -1,0 +1,144 @@
+#pragma once
+
+#include "adps_internal.cuh"
+#include "scan.cuh"
+
+namespace adps {
+
+struct GaussiansIn {
+  const float* mu;
+  const float* scale;
+  const float* rot;
+  const float* opacity;
+  const float* sh_dc;
+  const float* sh_rest;
+  int sh_k;
+};
+
+// ---- select (ref/adc.py:41-46, 82-89) ----
+struct SelectArgs {
+  const float* scale;
+  const double* ga;
+  const double* den;
+  double tau_g, tau_s_abs;
+  long long n;
+  unsigned char* cls;        // 0 none, 1 split, 2 clone
+  int* cand_rank;            // rank in split list or -1
+  int* split_list;
+  int* clone_list;
+  Counters* ctr;
+};
+cudaError_t launch_select(const SelectArgs& a, ScanState st, cudaStream_t s);
+
+// ---- region stats + child init (ref/error_partition.py:137-158, ref/child_init.py:44-140) ----
+struct ChildArgs {
+  const RegionRec* regions;
+  const unsigned long long* n_regions;
+  long long region_cap;
+  GaussiansIn g;
+  const double* cams;        // [V,18] device
+  const float* gt;           // [V,H,W,3]
+  int H, W;
+  double eps;
+  const int* cand_rank;
+  int bits_v, bits_b, bits_p;
+  Proposal* props;
+  unsigned char* valid;
+  unsigned long long* keys;
+  int* vals;
+  double* dbg_stats;         // [cap,10] or null
+  double* dbg_child;         // [cap,16] or null
+  Counters* ctr;
+  unsigned grid;
+};
+cudaError_t launch_child_init(const ChildArgs& a, cudaStream_t s);
+
+// ---- per-candidate ranges after the sort ----
+struct RangeArgs {
+  const unsigned long long* keys_sorted;
+  const int* vals_sorted;
+  long long n;
+  int shift_rank, bits_v, shift_view;
+  const unsigned char* valid;
+  int n_views;
+  int* cand_start;
+  int* cand_end;
+  int* cand_nvalid;
+  int* regions_per_view;
+  unsigned grid;
+};
+cudaError_t launch_ranges(const RangeArgs& a, cudaStream_t s);
+
+// ---- merge + cap + case (ref/cross_view_merge.py:33-116, ref/adc.py:184-227) ----
+struct MergeArgs {
+  const int* split_list;
+  const int* cand_start;
+  const int* cand_end;
+  const int* cand_nvalid;
+  const int* vals_sorted;        // sorted pos -> region id
+  const unsigned char* valid;    // region id -> t* > 0
+  const Proposal* props;         // region id -> proposal
+  const unsigned char* dom_flag;
+  const float* opacity;
+  double gamma_d, gamma_c;
+  int n_max;
+  int large_threshold;
+  int* idx;                      // [cap] start+j -> region id of j-th valid proposal
+  int* uf;                       // [cap]
+  GroupRec* groups;              // [cap]
+  float* children;               // [cap,14]
+  int* cand_case;
+  int* cand_props;
+  int* cand_merged;
+  int* cand_ins;
+  int* large_list;
+  Counters* ctr;
+  unsigned grid;
+};
+cudaError_t launch_merge(const MergeArgs& a, cudaStream_t s);
+
+// ---- offsets: candidate inserts and survivor compaction (ref/adc.py:229-244) ----
+struct OffsetArgs {
+  long long n;
+  const unsigned char* cls;
+  const int* cand_rank;
+  const int* cand_case;
+  const int* cand_ins;
+  int* ins_off;
+  int* fb_ord;
+  int* keep_pos;
+  Counters* ctr;
+  const unsigned long long* n_split_dev;
+};
+cudaError_t launch_offsets(const OffsetArgs& a, long long n_split, ScanState st_c, ScanState st_g,
+                           cudaStream_t s);
+
+// ---- emit (ref/adc.py:198-244) ----
+struct EmitArgs {
+  GaussiansIn g;
+  long long n, n_split, n_clone, n_keep, n_inserted;
+  const int* keep_pos;
+  const int* split_list;
+  const int* clone_list;
+  const int* cand_case;
+  const int* cand_merged;
+  const int* cand_start;
+  const int* ins_off;
+  const int* fb_ord;
+  const float* children;
+  const double* normals;
+  double eta;
+  float* mu;
+  float* scale;
+  float* rot;
+  float* opacity;
+  float* sh_dc;
+  float* sh_rest;
+  long long* index_map;
+};
+cudaError_t launch_emit(const EmitArgs& a, cudaStream_t s);
+
+cudaError_t launch_accumulate(double* ga, double* den, const float* vg, const unsigned char* vis,
+                              long long n, cudaStream_t s);
+
+}  // namespace adps

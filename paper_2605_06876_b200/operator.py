@@ -1,0 +1,512 @@
+"""The AdpSplit split operator on B200: host orchestration over the C ABI.
+
+Two entry layers:
+
+* tensor API -- ``densify_step`` / ``render_views`` on SoA fp32 CUDA tensors;
+  the benchmark and any GPU trainer call this.
+* reference API -- ``adpsplit_step(scene, cameras, gt_images, stats, cfg, rng)``
+  and ``render(scene, cam, background)`` with the reference's object types,
+  argument meaning, ordering and exceptions (ref/adc.py:143-245,
+  ref/raster.py:136-157), so it drops in where the reference is called
+  (ref/harness.py:400-404, ref/cli.py:119).
+
+Everything numeric runs in libadps.so; this module only moves buffers,
+draws from the caller's numpy Generator in the reference's order and builds
+the report.  There is no CPU fallback: without CUDA or without the library
+every entry point raises.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from . import _abi
+from .types import CandidateRecord, Gaussian3D, SplitReport
+
+F32 = torch.float32
+F64 = torch.float64
+
+
+def _require_cuda(device=None) -> torch.device:
+    if not torch.cuda.is_available():
+        raise RuntimeError("paper_2605_06876_b200 needs a CUDA device (B200); no CPU fallback exists")
+    d = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+    if d.type != "cuda":
+        raise ValueError(f"device must be a CUDA device, got {d}")
+    return d if d.index is not None else torch.device("cuda", torch.cuda.current_device())
+
+
+def _ptr(t):
+    return C.c_void_p(0 if t is None else t.data_ptr())
+
+
+# ----------------------------------------------------------------------------
+# SoA Gaussians
+# ----------------------------------------------------------------------------
+
+@dataclass
+class GaussianTensors:
+    """N Gaussians as contiguous fp32 CUDA tensors (56 B each at SH degree 0)."""
+
+    mu: torch.Tensor          # [N,3]
+    scale: torch.Tensor       # [N,3]
+    rot: torch.Tensor         # [N,4] (w,x,y,z)
+    opacity: torch.Tensor     # [N]
+    sh_dc: torch.Tensor       # [N,3]
+    sh_rest: torch.Tensor = None   # [N,K,3] or None
+
+    def __post_init__(self):
+        for name in ("mu", "scale", "rot", "opacity", "sh_dc", "sh_rest"):
+            t = getattr(self, name)
+            if t is not None:
+                if t.dtype != F32:
+                    raise TypeError(f"{name} must be float32")
+                setattr(self, name, t.contiguous())
+
+    @property
+    def n(self) -> int:
+        return int(self.mu.shape[0])
+
+    @property
+    def sh_k(self) -> int:
+        return 0 if self.sh_rest is None else int(self.sh_rest.shape[1])
+
+    @property
+    def device(self):
+        return self.mu.device
+
+    def abi(self) -> _abi.Gaussians:
+        return _abi.Gaussians(self.mu.data_ptr(), self.scale.data_ptr(), self.rot.data_ptr(),
+                              self.opacity.data_ptr(), self.sh_dc.data_ptr(),
+                              self.sh_rest.data_ptr() if self.sh_k else None, self.sh_k)
+
+    @staticmethod
+    def empty(n: int, sh_k: int, device) -> "GaussianTensors":
+        return GaussianTensors(torch.empty(n, 3, dtype=F32, device=device),
+                               torch.empty(n, 3, dtype=F32, device=device),
+                               torch.empty(n, 4, dtype=F32, device=device),
+                               torch.empty(n, dtype=F32, device=device),
+                               torch.empty(n, 3, dtype=F32, device=device),
+                               torch.empty(n, sh_k, 3, dtype=F32, device=device) if sh_k else None)
+
+    @staticmethod
+    def from_numpy(mu, scale, rot, opacity, sh_dc, sh_rest=None, device=None) -> "GaussianTensors":
+        d = _require_cuda(device)
+
+        def t(a, shape):
+            return torch.as_tensor(np.ascontiguousarray(np.asarray(a, dtype=np.float32).reshape(shape)),
+                                   device=d)
+
+        n = len(mu)
+        rest = None
+        if sh_rest is not None and np.asarray(sh_rest).size:
+            rest = t(sh_rest, (n, -1, 3))
+        return GaussianTensors(t(mu, (n, 3)), t(scale, (n, 3)), t(rot, (n, 4)), t(opacity, (n,)),
+                               t(sh_dc, (n, 3)), rest)
+
+    def numpy(self) -> dict:
+        out = {k: getattr(self, k).detach().cpu().numpy() for k in ("mu", "scale", "rot", "opacity", "sh_dc")}
+        out["sh_rest"] = (self.sh_rest.cpu().numpy() if self.sh_k
+                          else np.zeros((self.n, 0, 3), dtype=np.float32))
+        return out
+
+
+def camera_rows(cameras) -> np.ndarray:
+    """Cameras -> [C,18] float64 rows in save_cameras order (ref/scene.py:339-347)."""
+    if isinstance(cameras, np.ndarray):
+        rows = np.asarray(cameras, dtype=np.float64)
+        if rows.ndim != 2 or rows.shape[1] != 18:
+            raise ValueError("camera rows must be [C,18]")
+        return np.ascontiguousarray(rows)
+    return np.ascontiguousarray(np.array(
+        [np.concatenate([np.asarray(c.r_c2w, dtype=np.float64).ravel(),
+                         np.asarray(c.center, dtype=np.float64),
+                         [c.f_x, c.f_y, c.p_x, c.p_y, c.width, c.height]]) for c in cameras],
+        dtype=np.float64).reshape(-1, 18))
+
+
+def config_struct(cfg) -> _abi.Config:
+    def get(name):
+        return cfg[name] if isinstance(cfg, dict) else getattr(cfg, name)
+
+    return _abi.Config(float(get("tau_l1")), int(get("r_erode")), int(get("m_min")), int(get("l_bands")),
+                       int(get("n_max")), int(get("v_views")), 0, float(get("gamma_d")),
+                       float(get("gamma_c")), float(get("tau_g")), float(get("tau_s")),
+                       float(get("eta")), float(get("eps")))
+
+
+# ----------------------------------------------------------------------------
+# Plan
+# ----------------------------------------------------------------------------
+
+class Plan:
+    """Owns one native plan (all scratch) on one device; reuse across steps."""
+
+    def __init__(self, device=None):
+        self.device = _require_cuda(device)
+        self.lib = _abi.load()
+        self._h = C.c_void_p()
+        with torch.cuda.device(self.device):
+            _abi.check(self.lib.adps_plan_create(C.byref(self._h), self.device.index, 0, 0, 0, 0))
+        self.timing = False
+
+    def close(self):
+        if self._h:
+            self.lib.adps_plan_destroy(self._h)
+            self._h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def _stream(self):
+        return C.c_void_p(torch.cuda.current_stream(self.device).cuda_stream)
+
+    def set_timing(self, on: bool):
+        self.timing = bool(on)
+        _abi.check(self.lib.adps_set_timing(self._h, int(on)))
+
+    def stage_ms(self) -> dict:
+        ms = (C.c_double * 8)()
+        names = (C.c_char_p * 8)()
+        n = C.c_int32()
+        _abi.check(self.lib.adps_get_timing(self._h, ms, 8, C.byref(n), names))
+        return {names[i].decode(): float(ms[i]) for i in range(n.value)}
+
+    def set_debug_records(self, on: bool):
+        _abi.check(self.lib.adps_set_debug_records(self._h, int(on)))
+
+    def set_debug_maps(self, m: torch.Tensor = None, b: torch.Tensor = None):
+        _abi.check(self.lib.adps_set_debug_maps(self._h, _ptr(m), _ptr(b)))
+
+    # -- render (ref/raster.py:136-157)
+    def render(self, g: GaussianTensors, cams: np.ndarray, bg=(0.0, 0.0, 0.0), out=None):
+        cams = camera_rows(cams)
+        v = len(cams)
+        w, h = int(cams[0, 16]), int(cams[0, 17])
+        if out is None:
+            image = torch.empty(v, h, w, 3, dtype=F32, device=self.device)
+            dom = torch.empty(v, h, w, dtype=torch.int32, device=self.device)
+        else:
+            image, dom = out
+        bgv = (C.c_float * 3)(*[float(x) for x in bg])
+        ga = g.abi()
+        _abi.check(self.lib.adps_render(self._h, self._stream(), C.byref(ga), g.n,
+                                        cams.ctypes.data_as(C.c_void_p), v, bgv, _ptr(image), _ptr(dom)))
+        return image, dom
+
+    # -- phase 1 / 2 (ref/adc.py:165-244)
+    def phase1(self, g, extent, grad_accum, denom, cfg, cams_v, image, gt, dom) -> dict:
+        cams_v = camera_rows(cams_v)
+        counts = _abi.Counts()
+        cs = config_struct(cfg)
+        ga = g.abi()
+        self._g_keep = (g, grad_accum, denom, image, gt, dom)
+        st = self.lib.adps_step_phase1(self._h, self._stream(), C.byref(ga), g.n, float(extent),
+                                       _ptr(grad_accum), _ptr(denom), C.byref(cs),
+                                       cams_v.ctypes.data_as(C.c_void_p), len(cams_v), _ptr(image),
+                                       _ptr(gt), _ptr(dom), C.byref(counts))
+        _abi.check(st)
+        return counts.as_dict()
+
+    def phase2(self, g, normals, out: GaussianTensors, index_map: torch.Tensor):
+        ga = g.abi()
+        oa = _abi.GaussiansOut(out.mu.data_ptr(), out.scale.data_ptr(), out.rot.data_ptr(),
+                               out.opacity.data_ptr(), out.sh_dc.data_ptr(),
+                               out.sh_rest.data_ptr() if out.sh_k else None, out.sh_k)
+        _abi.check(self.lib.adps_step_phase2(self._h, self._stream(), C.byref(ga), _ptr(normals),
+                                             C.byref(oa), _ptr(index_map)))
+
+    def report_arrays(self, n_split: int, n_clone: int) -> dict:
+        r = _abi.Report()
+        _abi.check(self.lib.adps_get_report(self._h, C.byref(r)))
+        v = int(r.n_views)
+
+        def grab(ptr, n):
+            out = torch.empty(max(n, 0), dtype=torch.int32, device=self.device)
+            if n > 0:
+                _copy_device(out, ptr, n * 4, self.device)
+            return out
+
+        return dict(cand_index=grab(r.cand_index, n_split), cand_case=grab(r.cand_case, n_split),
+                    cand_proposals=grab(r.cand_proposals, n_split),
+                    cand_merged=grab(r.cand_merged, n_split),
+                    regions_per_view=grab(r.regions_per_view, n_split * v).view(-1, max(v, 1)),
+                    clone_index=grab(r.clone_index, n_clone))
+
+    def regions(self) -> dict:
+        """Region records of the last phase 1, in reference order (diagnostic)."""
+        rec, order, valid, stats, child = (C.c_void_p() for _ in range(5))
+        n = C.c_int64()
+        _abi.check(self.lib.adps_get_regions(self._h, C.byref(rec), C.byref(order), C.byref(valid),
+                                             C.byref(stats), C.byref(child), C.byref(n)))
+        n = n.value
+        raw = torch.empty(n * 16, dtype=torch.int32, device=self.device)
+        ordt = torch.empty(n, dtype=torch.int32, device=self.device)
+        val = torch.empty(n, dtype=torch.uint8, device=self.device)
+        if n:
+            _copy_device(raw, rec.value, n * 64, self.device)
+            _copy_device(ordt, order.value, n * 4, self.device)
+            _copy_device(val, valid.value, n, self.device)
+        raw = raw.view(n, 16)
+        o = ordt.long()
+        out = dict(view_pos=raw[:, 0][o], candidate=raw[:, 1][o], band=raw[:, 2][o], minpix=raw[:, 3][o],
+                   moments=raw[:, 4:].contiguous().view(torch.int64).view(n, 6)[o], valid=val[o])
+        if stats.value and n:
+            st = torch.empty(n, 10, dtype=F64, device=self.device)
+            ch = torch.empty(n, 16, dtype=F64, device=self.device)
+            _copy_device(st, stats.value, n * 80, self.device)
+            _copy_device(ch, child.value, n * 128, self.device)
+            out["stats"] = st[o]
+            out["child"] = ch[o]
+        return out
+
+
+_cudart = None
+
+
+def _copy_device(dst: torch.Tensor, src_ptr: int, nbytes: int, device):
+    """Device-to-device copy from a raw pointer owned by the plan."""
+    global _cudart
+    if _cudart is None:
+        from cuda.bindings import runtime as _rt  # cuda-python
+        _cudart = _rt
+    stream = torch.cuda.current_stream(device).cuda_stream
+    err, = _cudart.cudaMemcpyAsync(dst.data_ptr(), src_ptr, nbytes,
+                                   _cudart.cudaMemcpyKind.cudaMemcpyDeviceToDevice, stream)
+    if int(err) != 0:
+        raise RuntimeError(f"cudaMemcpyAsync failed: {err}")
+
+
+_plans: dict = {}
+
+
+def default_plan(device=None) -> Plan:
+    d = _require_cuda(device)
+    if d.index not in _plans:
+        _plans[d.index] = Plan(d)
+    return _plans[d.index]
+
+
+# ----------------------------------------------------------------------------
+# tensor API
+# ----------------------------------------------------------------------------
+
+def sample_views(n_cams: int, v_views: int, rng) -> list:
+    """sorted(rng.choice(#cams, V, replace=False)), ref/adc.py:154-161."""
+    if v_views > n_cams:
+        raise ValueError(f"v_views={v_views} exceeds available cameras ({n_cams})")
+    return [int(v) for v in sorted(rng.choice(n_cams, size=v_views, replace=False))]
+
+
+def _gather_views(x, view_ids, device):
+    """Stack per-view images of the sampled views on the device (no copy if contiguous)."""
+    if isinstance(x, torch.Tensor):
+        if x.device != device:
+            x = x.to(device)
+        if view_ids == list(range(view_ids[0], view_ids[0] + len(view_ids))):
+            return x[view_ids[0]:view_ids[0] + len(view_ids)].contiguous()
+        return x.index_select(0, torch.as_tensor(view_ids, device=device)).contiguous()
+    return torch.stack([torch.as_tensor(np.asarray(x[v], dtype=np.float32), device=device)
+                        for v in view_ids]).contiguous()
+
+
+@dataclass
+class StepResult:
+    gaussians: GaussianTensors
+    index_map: torch.Tensor
+    counts: dict
+    view_ids: list
+    report_arrays: dict = None
+    normals: np.ndarray = None
+    stage_ms: dict = field(default_factory=dict)
+
+    def report(self) -> SplitReport:
+        """Host SplitReport (ref/adc.py:60-70) built from the device arrays."""
+        ra = {k: v.cpu().numpy() for k, v in self.report_arrays.items()}
+        rep = SplitReport(count_before=self.counts["n_before"], count_after=self.counts["n_out"])
+        rep.sampled_views = list(self.view_ids)
+        rep.merge_edges = self.counts["merge_edges"]
+        rep.clones = [int(i) for i in ra["clone_index"]]
+        for k, i in enumerate(ra["cand_index"]):
+            case = int(ra["cand_case"][k])
+            rec = CandidateRecord(index=int(i), regions_per_view=[int(x) for x in ra["regions_per_view"][k]],
+                                  proposals=int(ra["cand_proposals"][k]))
+            if case == _abi.CASE_FALLBACK:
+                rec.fallback = True
+            elif case == _abi.CASE_RESET:
+                rec.reset = True
+                rep.reset_indices.append(int(i))
+            else:
+                rec.merged = int(ra["cand_merged"][k])
+                rec.children_inserted = rec.merged
+            rep.candidates.append(rec)
+        rep.index_map = self.index_map.cpu().numpy().astype(np.int64)
+        return rep
+
+
+def densify_step(g: GaussianTensors, extent: float, cameras, gt, grad_accum: torch.Tensor,
+                 denom: torch.Tensor, cfg, rng, *, renders=None, plan: Plan = None,
+                 view_ids=None, want_report: bool = True, out: GaussianTensors = None) -> StepResult:
+    """One AdpSplit densify step on device tensors (ref/adc.py:143-245).
+
+    cameras: all C cameras ([C,18] rows or Camera objects).  gt: [C,H,W,3]
+    fp32 tensor (or a per-camera sequence).  renders: optional (image,
+    dominant) of the sampled views (the stage boundary the reference tests
+    reach by monkeypatching ``adc.render``); rendered on the GPU otherwise.
+    """
+    plan = plan or default_plan(g.device)
+    cams = camera_rows(cameras)
+    if view_ids is None:
+        view_ids = sample_views(len(cams), int(cfg["v_views"] if isinstance(cfg, dict) else cfg.v_views), rng)
+    cams_v = cams[view_ids]
+    dev = plan.device
+    if renders is None:
+        image, dom = plan.render(g, cams_v)
+    else:
+        image, dom = renders
+        image = image.to(dev, F32).contiguous()
+        dom = dom.to(dev, torch.int32).contiguous()
+    gt_v = _gather_views(gt, view_ids, dev)
+    counts = plan.phase1(g, extent, grad_accum.to(dev, F64).contiguous(), denom.to(dev, F64).contiguous(),
+                         cfg, cams_v, image, gt_v, dom)
+    nf = counts["n_fallback"]
+    normals_np = rng.standard_normal(6 * nf) if nf > 0 else np.zeros(0)
+    normals = torch.as_tensor(normals_np, dtype=F64, device=dev) if nf > 0 else None
+    n_out = counts["n_out"]
+    if out is None:
+        out = GaussianTensors.empty(n_out, g.sh_k, dev)
+    index_map = torch.empty(n_out, dtype=torch.int64, device=dev)
+    plan.phase2(g, normals, out, index_map)
+    res = StepResult(gaussians=out, index_map=index_map, counts=counts, view_ids=list(view_ids),
+                     normals=normals_np)
+    if want_report:
+        res.report_arrays = plan.report_arrays(counts["n_split"], counts["n_clone"])
+    if plan.timing:
+        res.stage_ms = plan.stage_ms()
+    return res
+
+
+def render_views(g: GaussianTensors, cameras, bg=(0.0, 0.0, 0.0), plan: Plan = None):
+    plan = plan or default_plan(g.device)
+    return plan.render(g, camera_rows(cameras), bg)
+
+
+def accumulate_stats_(grad_accum: torch.Tensor, denom: torch.Tensor, viewspace_grad: torch.Tensor,
+                      visible: torch.Tensor):
+    """In-place DensifyStats feed on device (ref/adc.py:73-79)."""
+    lib = _abi.load()
+    if grad_accum.dtype != F64 or denom.dtype != F64:
+        raise TypeError("stats must be float64")
+    if len(grad_accum) != len(visible):
+        raise ValueError("stats dimensions do not match gradient output")
+    vg = viewspace_grad.to(F32).contiguous()
+    vis = visible.to(torch.uint8).contiguous()
+    stream = C.c_void_p(torch.cuda.current_stream(grad_accum.device).cuda_stream)
+    _abi.check(lib.adps_accumulate_stats(stream, _ptr(grad_accum), _ptr(denom), _ptr(vg), _ptr(vis),
+                                         len(grad_accum)))
+
+
+# ----------------------------------------------------------------------------
+# reference API (object types)
+# ----------------------------------------------------------------------------
+
+def _scene_arrays(gaussians):
+    n = len(gaussians)
+    k = max((len(x.sh_rest) for x in gaussians), default=0)
+    rest = np.zeros((n, k, 3))
+    for i, x in enumerate(gaussians):
+        for j, c in enumerate(x.sh_rest):
+            rest[i, j] = c
+    return (np.array([x.mu for x in gaussians], dtype=np.float64).reshape(n, 3),
+            np.array([x.scale for x in gaussians], dtype=np.float64).reshape(n, 3),
+            np.array([x.rot for x in gaussians], dtype=np.float64).reshape(n, 4),
+            np.array([x.opacity for x in gaussians], dtype=np.float64).reshape(n),
+            np.array([x.sh_dc for x in gaussians], dtype=np.float64).reshape(n, 3), rest)
+
+
+def _clamp_opacity(o):
+    return min(max(o, 1e-6), 1.0 - 1e-6)
+
+
+def adpsplit_step(scene, cameras, gt_images, stats, cfg, rng, *, plan: Plan = None, renders=None):
+    """Drop-in for ``adpsplit.adc.adpsplit_step`` (ref/adc.py:143-245).
+
+    Mutates ``scene.gaussians`` (survivors are the same objects, in the old
+    order, followed by the inserted Gaussians) and returns (scene, SplitReport).
+    Parameters are processed in fp32 on the GPU; inserted parent copies,
+    clones and the exact-copy fields of fallback children are taken from
+    the original objects so the opacity bookkeeping holds to fp64.
+    """
+    if cfg.v_views > len(cameras):
+        raise ValueError(f"v_views={cfg.v_views} exceeds available cameras ({len(cameras)})")
+    dev = _require_cuda()
+    plan = plan or default_plan(dev)
+    gs = list(scene.gaussians)
+    mu, scale, rot, op, dc, rest = _scene_arrays(gs)
+    g = GaussianTensors.from_numpy(mu, scale, rot, op, dc, rest if rest.shape[1] else None, dev)
+    view_ids = sample_views(len(cameras), cfg.v_views, rng)
+    rnd = None
+    if renders is not None:
+        rnd = renders(view_ids) if callable(renders) else renders
+    res = densify_step(g, scene.extent, cameras, gt_images,
+                       torch.as_tensor(np.asarray(stats.grad_accum, dtype=np.float64), device=dev),
+                       torch.as_tensor(np.asarray(stats.denom, dtype=np.float64), device=dev),
+                       cfg, rng, renders=rnd, plan=plan, view_ids=view_ids)
+    rep = res.report()
+    outg = res.gaussians.numpy()
+    make = type(gs[0]) if gs else Gaussian3D
+    new = [gs[int(i)] for i in rep.index_map[rep.index_map >= 0]]
+    pos = len(new)
+    for rec in rep.candidates:
+        p = gs[rec.index]
+        if rec.fallback:
+            for _ in range(2):
+                new.append(make(mu=outg["mu"][pos].astype(np.float64), scale=p.scale / (cfg.eta * 2),
+                                rot=p.rot, opacity=p.opacity, sh_dc=p.sh_dc, sh_rest=p.sh_rest))
+                pos += 1
+        elif not rec.reset:
+            for _ in range(rec.children_inserted):
+                q = outg["rot"][pos].astype(np.float64)
+                new.append(make(mu=outg["mu"][pos].astype(np.float64),
+                                scale=outg["scale"][pos].astype(np.float64), rot=q / np.linalg.norm(q),
+                                opacity=_clamp_opacity(float(p.opacity)),
+                                sh_dc=outg["sh_dc"][pos].astype(np.float64), sh_rest=()))
+                pos += 1
+            new.append(make(mu=p.mu, scale=p.scale, rot=p.rot,
+                            opacity=_clamp_opacity(p.opacity / (rec.children_inserted + 1)),
+                            sh_dc=p.sh_dc, sh_rest=p.sh_rest))
+            pos += 1
+    for i in rep.clones:
+        p = gs[i]
+        new.append(make(mu=p.mu, scale=p.scale, rot=p.rot, opacity=p.opacity, sh_dc=p.sh_dc,
+                        sh_rest=p.sh_rest))
+        pos += 1
+    if pos != rep.count_after:
+        raise RuntimeError(f"population mismatch: built {pos}, device reported {rep.count_after}")
+    scene.gaussians = new
+    return scene, rep
+
+
+@dataclass
+class RenderOutput:
+    image: np.ndarray
+    dominant_map: np.ndarray
+    background: np.ndarray
+
+
+def render(scene, cam, background) -> RenderOutput:
+    """Drop-in for ``adpsplit.raster.render`` (ref/raster.py:136-157), fp32 on the GPU."""
+    dev = _require_cuda()
+    bg = np.asarray(background, dtype=np.float64)
+    mu, scale, rot, op, dc, rest = _scene_arrays(list(scene.gaussians))
+    g = GaussianTensors.from_numpy(mu, scale, rot, op, dc, rest if rest.shape[1] else None, dev)
+    img, dom = render_views(g, camera_rows([cam]), bg)
+    return RenderOutput(image=img[0].double().cpu().numpy(), dominant_map=dom[0].long().cpu().numpy(),
+                        background=bg)

@@ -1,0 +1,197 @@
+"""Seeded synthetic workloads of the BASELINE configs (numpy; host-side).
+
+Distribution follows the reference's synthetic harness
+(ref/harness.py:99-210: flat slab of Gaussians, ring of cameras at
+elevation 0.9 rad, 50 % subset init with inflated scales plus one dim cover
+Gaussian) with one change the survey calls for:
+splat size shrinks as 1/sqrt(k) so the mean depth complexity stays fixed
+as the Gaussian count grows to millions (the reference's fixed sizes leave
+almost every Gaussian occluded at scale).  A log-normal size spread keeps a
+realistic share of Gaussians above the split-scale gate tau_s*extent.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+
+SH_C0 = 0.28209479177387814
+
+
+@dataclass
+class SynthScene:
+    mu: np.ndarray
+    scale: np.ndarray
+    rot: np.ndarray
+    opacity: np.ndarray
+    sh_dc: np.ndarray
+    extent: float
+
+    @property
+    def n(self):
+        return len(self.mu)
+
+    def arrays(self):
+        return self.mu, self.scale, self.rot, self.opacity, self.sh_dc
+
+
+def _look_at(eye, target, world_up):
+    """ref/harness.py:99-107: columns right, down, forward."""
+    fwd = target - eye
+    fwd = fwd / np.linalg.norm(fwd)
+    right = np.cross(-np.asarray(world_up, dtype=np.float64), fwd)
+    right = right / np.linalg.norm(right)
+    down = np.cross(fwd, right)
+    return np.stack([right, down, fwd], axis=1)
+
+
+def ring_cameras(n_cams: int, width: int, height: int, extent: float = 1.0, elev: float = 0.9) -> np.ndarray:
+    """Camera ring of ref/harness.py:140-166 for a W x H image -> [C,18] rows."""
+    dist = 2.6 * extent
+    f = 0.55 * min(width, height) * dist / extent
+    rows = []
+    for i in range(n_cams):
+        ang = 2 * np.pi * i / n_cams
+        eye = dist * np.array([np.cos(ang) * np.cos(elev), np.sin(ang) * np.cos(elev), np.sin(elev)])
+        r = _look_at(eye, np.zeros(3), (0.0, 0.0, 1.0))
+        rows.append(np.concatenate([r.ravel(), eye, [f, f, (width - 1) / 2.0, (height - 1) / 2.0,
+                                                    width, height]]))
+    return np.array(rows)
+
+
+def gt_scene(k: int, seed: int, size_factor: float = 1.0, spread: float = 0.0,
+             large_frac: float = 0.0, large_range=(0.005, 0.01)) -> SynthScene:
+    """GT scene like ref/harness.py:110-138.
+
+    Base size U(.04,.10) x size_factor x lognormal(spread); a fraction
+    ``large_frac`` instead gets base U(large_range) (world units, before the
+    init inflation) so that a realistic share clears the split gate.
+    """
+    rng = np.random.default_rng(seed)
+    mu = np.stack([rng.uniform(-0.75, 0.75, k), rng.uniform(-0.75, 0.75, k), rng.uniform(-0.12, 0.12, k)], 1)
+    base = rng.uniform(0.04, 0.10, k) * size_factor
+    if spread > 0:
+        base = base * np.exp(rng.normal(0.0, spread, k))
+    aniso = rng.uniform(0.4, 1.0, (k, 3))
+    if large_frac > 0:
+        large = rng.uniform(size=k) < large_frac
+        base = np.where(large, rng.uniform(large_range[0], large_range[1], k) / aniso.max(axis=1), base)
+    q = rng.standard_normal((k, 4))
+    q /= np.linalg.norm(q, axis=1, keepdims=True)
+    opacity = rng.uniform(0.65, 0.95, k)
+    sh_dc = (rng.uniform(0.15, 0.85, (k, 3)) - 0.5) / SH_C0
+    scale = base[:, None] * aniso
+    radii = np.linalg.norm(mu, axis=1) + scale.max(axis=1)
+    extent = max(1.0, float(radii.max()))
+    return SynthScene(mu, scale, q, opacity, sh_dc, extent)
+
+
+def init_scene(gt: SynthScene, seed: int, fraction: float = 0.5, inflate: float = 2.0,
+               cover: bool = True) -> SynthScene:
+    """Perturbed inflated subset plus a cover Gaussian (ref/harness.py:172-210)."""
+    rng = np.random.default_rng((seed, 0xC0FFEE))
+    k = gt.n
+    n = max(1, int(round(fraction * k)))
+    chosen = np.sort(rng.choice(k, size=n, replace=False))
+    mu = gt.mu[chosen] + rng.normal(0.0, 0.01 * gt.extent, (n, 3))
+    parts = [mu, gt.scale[chosen] * inflate, gt.rot[chosen], gt.opacity[chosen], gt.sh_dc[chosen]]
+    if cover:
+        parts = [np.concatenate([parts[0], np.zeros((1, 3))]),
+                 np.concatenate([parts[1], np.full((1, 3), 0.6 * gt.extent)]),
+                 np.concatenate([parts[2], [[1.0, 0.0, 0.0, 0.0]]]),
+                 np.concatenate([parts[3], [0.3]]),
+                 np.concatenate([parts[4], np.zeros((1, 3))])]
+    return SynthScene(*parts, extent=gt.extent)
+
+
+def synth_stats(scale: np.ndarray, extent: float, tau_g: float, tau_s: float, p_split: float,
+                p_clone: float, seed: int):
+    """DensifyStats (denom = 1) whose select() yields ~p_split*N split and ~p_clone*N
+    clone candidates (ref/adc.py:82-89): g = tau_g*exp(|z|) for the chosen
+    Gaussians, tau_g*exp(-|z|-1e-3) for the rest."""
+    rng = np.random.default_rng((seed, 0x57A75))
+    n = len(scale)
+    large = scale.max(axis=1) > tau_s * extent
+    high = np.zeros(n, dtype=bool)
+    li, si = np.flatnonzero(large), np.flatnonzero(~large)
+    high[rng.choice(li, size=min(len(li), int(round(p_split * n))), replace=False)] = True
+    high[rng.choice(si, size=min(len(si), int(round(p_clone * n))), replace=False)] = True
+    z = np.abs(rng.standard_normal(n))
+    ga = np.where(high, tau_g * np.exp(z), tau_g * np.exp(-z - 1e-3))
+    return ga, np.ones(n)
+
+
+def round_f32(s: SynthScene) -> SynthScene:
+    """Round parameters to fp32 (what the device stores), renormalising quaternions in fp32."""
+    q = s.rot.astype(np.float32)
+    q = q / np.linalg.norm(q, axis=1, keepdims=True)
+    return SynthScene(s.mu.astype(np.float32).astype(np.float64),
+                      s.scale.astype(np.float32).astype(np.float64),
+                      q.astype(np.float32).astype(np.float64),
+                      s.opacity.astype(np.float32).astype(np.float64),
+                      s.sh_dc.astype(np.float32).astype(np.float64), s.extent)
+
+
+def depth_complexity(s: SynthScene, cam_row, alpha_min=1.0 / 255) -> float:
+    """Mean number of splats with alpha >= alpha_min per pixel (area estimate, one view)."""
+    r = cam_row[0:9].reshape(3, 3)
+    c = cam_row[9:12]
+    fx, fy, w, h = cam_row[12], cam_row[13], cam_row[16], cam_row[17]
+    p = (s.mu - c) @ r
+    z = p[:, 2]
+    ok = z > 1e-8
+    # projected covariance determinant (affine approx, isotropic proxy)
+    s2 = (s.scale ** 2).prod(axis=1) ** (1.0 / 3.0)
+    px_var = s2 * (fx * fy) / (z ** 2)
+    det = (px_var + 0.3) ** 2
+    o = np.minimum(s.opacity, 0.99)
+    area = np.pi * 2.0 * np.log(np.maximum(o / alpha_min, 1.0)) * np.sqrt(det)
+    return float(area[ok].sum() / (w * h))
+
+
+@dataclass
+class Workload:
+    name: str
+    n_gt: int
+    n_views: int
+    width: int
+    height: int
+    p_split: float
+    p_clone: float
+    size_factor: float
+    large_frac: float = 0.06
+    large_range: tuple = (0.005, 0.01)
+    spread: float = 0.3
+    inflate: float = 2.0
+    n_max: int = 19
+    seed: int = 0
+
+    def build(self, seed=None):
+        """-> (init SynthScene rounded to fp32, camera rows, (grad_accum, denom), gt SynthScene)."""
+        seed = self.seed if seed is None else seed
+        gt = gt_scene(self.n_gt, seed, self.size_factor, self.spread, self.large_frac, self.large_range)
+        ini = round_f32(init_scene(gt, seed, inflate=self.inflate))
+        cams = ring_cameras(self.n_views, self.width, self.height, gt.extent)
+        stats = synth_stats(ini.scale, ini.extent, 2e-4, 0.01, self.p_split, self.p_clone, seed)
+        return ini, cams, stats, round_f32(gt)
+
+
+# BASELINE.json configs; sizes scale as 1/sqrt(k) around the
+# 2.4M-GT bonsai-shaped scene (config 3), whose init has depth complexity ~100.
+def _sf(k):
+    return float(np.sqrt(2_400_000 / k))
+
+
+CONFIGS = {
+    "config1": Workload("config1", 10_000, 1, 256, 256, 0.05, 0.02, 0.02 * _sf(10_000),
+                        large_range=(0.005 * _sf(10_000), 0.01 * _sf(10_000))),
+    "config2": Workload("config2", 200_000, 16, 800, 800, 0.05, 0.02, 0.02 * _sf(200_000),
+                        large_range=(0.005 * _sf(200_000), 0.01 * _sf(200_000))),
+    "config3": Workload("config3", 2_400_000, 64, 1237, 822, 0.05, 0.02, 0.02),
+    "config4": Workload("config4", 6_000_000, 128, 1297, 840, 0.05, 0.02, 0.02 * _sf(6_000_000),
+                        large_range=(0.005 * _sf(6_000_000), 0.01 * _sf(6_000_000)), n_max=9),
+    "config5": Workload("config5", 16_000_000, 256, 1297, 840, 0.25, 0.02, 0.02 * _sf(16_000_000),
+                        large_frac=0.3, large_range=(0.005 * _sf(16_000_000), 0.01 * _sf(16_000_000)),
+                        inflate=4.0),
+}

@@ -1,0 +1,199 @@
+"""Parity helpers: run the GPU operator and the CPU oracle on identical inputs
+and compare with the classes of SURVEY.md 8(c):
+
+* exact     -- per-candidate case, regions_per_view, proposals, N_i,
+               merge_edges, clones, reset list, sampled views, index_map;
+* near-threshold (reported, excluded) -- candidates whose merge gate is
+               within 1e-9 of gamma_d / 1e-12 of gamma_c, |t*| <= 1e-12|b|,
+               cap-order extent ties, degenerate merged eigenspaces, and (end
+               to end only) pixels whose normalised error is within EPS_E of
+               a threshold or whose dominance is a near-tie;
+* float tolerance -- mu, sh_dc, opacity rel <= 2e-6 (fp32 outputs), covariance
+               max-abs <= 1e-5 * max|Sigma|; quaternions are not compared.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+
+from oracle import adpsplit_oracle as O
+
+EPS_E = 2e-5          # end-to-end: |e - threshold| band for the fp32 render
+EPS_TIE = 1e-4        # end-to-end: relative best/runner-up T*alpha gap
+
+
+def f32(a):
+    return np.asarray(a, dtype=np.float32).astype(np.float64)
+
+
+def oracle_gaussians_f32(g: O.Gaussians) -> O.Gaussians:
+    """The fp32 values the device stores, upcast exactly."""
+    return O.Gaussians(f32(g.mu), f32(g.scale), f32(g.rot), f32(g.opacity), f32(g.sh_dc), f32(g.sh_rest))
+
+
+def to_tensors(g: O.Gaussians, device="cuda"):
+    from paper_2605_06876_b200.operator import GaussianTensors
+    return GaussianTensors.from_numpy(g.mu, g.scale, g.rot, g.opacity, g.sh_dc,
+                                      g.sh_rest if g.sh_rest.shape[1] else None, device)
+
+
+def covs(scale, rot):
+    out = np.empty((len(scale), 3, 3))
+    for i in range(len(scale)):
+        out[i] = O.covariance(rot[i], scale[i])
+    return out
+
+
+def flag_candidates(res: O.StepResult, g: O.Gaussians, cams, cfg) -> set:
+    """Near-threshold candidates of an oracle step (stage-isolated classes)."""
+    flagged = set()
+    gd, gc = O.cfg_get(cfg, "gamma_d"), O.cfg_get(cfg, "gamma_c")
+    eps = O.cfg_get(cfg, "eps")
+    for i, props in res.proposals.items():
+        for a in range(len(props)):
+            for b in range(a + 1, len(props)):
+                d, dc = O.gate_terms(props[a], props[b])
+                if abs(d - gd) <= 1e-9 * max(gd, 1.0) or abs(dc - gc) <= 1e-12:
+                    flagged.add(i)
+    for v, regs in res.regions.items():
+        for reg in regs:
+            i = reg.candidate
+            orig, d, _ = O.pixel_ray(cams[v], reg.centroid[0], reg.centroid[1])
+            b = g.mu[i] - orig
+            t = O.optimal_t(g.mu[i], O.covariance(g.rot[i], g.scale[i]), orig, d, eps)
+            if abs(t) <= 1e-12 * np.linalg.norm(b):
+                flagged.add(i)
+    for i, groups in res.all_groups.items():
+        ext = np.array([gr.extent for gr in groups])
+        for a in range(len(ext)):
+            for b in range(a + 1, len(ext)):
+                if abs(ext[a] - ext[b]) <= 1e-12 * max(abs(ext[a]), abs(ext[b])):
+                    flagged.add(i)
+        for gr in groups:
+            if len(gr.members) > 1:
+                mc = np.mean([res.proposals[i][m].cov() for m in gr.members], axis=0)
+                ev = np.linalg.eigvalsh(mc)
+                if np.min(np.diff(ev)) <= 1e-9 * max(abs(ev).max(), 1e-300):
+                    flagged.add(i)
+    return flagged
+
+
+def flag_end_to_end(res: O.StepResult, gpu_renders: dict, gts, cfg, weights: dict) -> set:
+    """Extra flags when the oracle rendered in fp64 and the GPU in fp32."""
+    flagged = set()
+    tau, L, r = O.cfg_get(cfg, "tau_l1"), int(O.cfg_get(cfg, "l_bands")), int(O.cfg_get(cfg, "r_erode"))
+    edges = [tau] + [tau + k * (1.0 - tau) / L for k in range(1, L)]
+    for v, (img_o, dom_o) in res.renders.items():
+        img_g, dom_g = gpu_renders[v]
+        best, second = weights[v]
+        e = O.error_map(img_o, gts[v])
+        near = np.zeros(e.shape, dtype=bool)
+        for t in edges:
+            near |= np.abs(e - t) <= EPS_E
+        tie = (best - second) <= EPS_TIE * np.maximum(best, 1e-30)
+        diff = dom_o != dom_g
+        bad = near | (tie & diff) | diff
+        if r > 1:   # a flipped pixel moves the eroded mask within the footprint
+            k = r
+            pad = np.pad(bad, k)
+            grown = np.zeros_like(bad)
+            for dy in range(-k, k + 1):
+                for dx in range(-k, k + 1):
+                    grown |= pad[k + dy:k + dy + bad.shape[0], k + dx:k + dx + bad.shape[1]]
+            bad = grown
+        for arr in (dom_o, dom_g):
+            flagged.update(int(x) for x in np.unique(arr[bad]) if x >= 0)
+    return flagged
+
+
+def unexplained_dominance(res: O.StepResult, gpu_renders: dict, weights: dict) -> int:
+    """Pixels whose dominant index differs without a near-tie (must be 0)."""
+    n = 0
+    for v, (_, dom_o) in res.renders.items():
+        _, dom_g = gpu_renders[v]
+        best, second = weights[v]
+        tie = (best - second) <= EPS_TIE * np.maximum(best, 1e-30)
+        n += int(((dom_o != dom_g) & ~tie).sum())
+    return n
+
+
+def compare_step(gres, ores: O.StepResult, flagged: set, g_in: O.Gaussians, strict_floats=True):
+    """Assert GPU StepResult == oracle StepResult outside the flagged candidates.
+
+    Returns a dict of statistics (mismatches, flagged, max errors)."""
+    rep = gres.report()
+    assert rep.sampled_views == ores.sampled_views
+    assert rep.clones == ores.clones
+    o_recs = {r.index: r for r in ores.candidates}
+    g_recs = {r.index: r for r in rep.candidates}
+    assert set(o_recs) == set(g_recs), "split sets differ"
+    mism = []
+    for i, ro in o_recs.items():
+        rg = g_recs[i]
+        same = (ro.fallback == rg.fallback and ro.reset == rg.reset and ro.proposals == rg.proposals
+                and ro.merged == rg.merged and ro.children_inserted == rg.children_inserted
+                and list(ro.regions_per_view) == list(rg.regions_per_view))
+        if not same:
+            mism.append(i)
+    unexplained = [i for i in mism if i not in flagged]
+    assert not unexplained, f"integer mismatch on non-flagged candidates {unexplained[:10]}: " + \
+        "; ".join(f"gpu={g_recs[i]} oracle={o_recs[i]}" for i in unexplained[:3])
+    stats = dict(mismatched=len(mism), flagged=len(flagged), candidates=len(o_recs))
+    if mism:
+        return stats     # layouts diverge after a flagged mismatch; integer parity shown above
+    assert rep.count_after == ores.count_after
+    assert rep.merge_edges == ores.merge_edges
+    assert rep.reset_indices == ores.reset_indices
+    np.testing.assert_array_equal(rep.index_map, ores.index_map)
+    out = gres.gaussians.numpy()
+    og = ores.gaussians
+    # which rows may differ (children of flagged candidates)
+    skip = np.zeros(ores.count_after, dtype=bool)
+    cur = int((ores.index_map >= 0).sum())
+    for rec in ores.candidates:
+        k = 2 if rec.fallback else (0 if rec.reset else rec.children_inserted + 1)
+        if rec.index in flagged:
+            skip[cur:cur + k] = True
+        cur += k
+    keep = ~skip
+    exact_rows = ores.index_map >= 0
+    for f in ("mu", "scale", "rot", "opacity", "sh_dc"):
+        np.testing.assert_array_equal(out[f][exact_rows], f32(getattr(og, f))[exact_rows], err_msg=f)
+    for f in ("mu", "sh_dc", "opacity"):
+        a, b = out[f][keep].astype(np.float64), getattr(og, f)[keep]
+        err = np.abs(a - b) / np.maximum(np.abs(b), 1e-3)
+        stats[f"max_rel_{f}"] = float(err.max()) if err.size else 0.0
+        if strict_floats:
+            assert stats[f"max_rel_{f}"] <= 2e-6, (f, stats[f"max_rel_{f}"])
+    cg = covs(out["scale"][keep].astype(np.float64), out["rot"][keep].astype(np.float64))
+    co = covs(og.scale[keep], og.rot[keep])
+    scale_ = np.abs(co).reshape(len(co), -1).max(axis=1) if len(co) else np.zeros(0)
+    cerr = np.abs(cg - co).reshape(len(co), -1).max(axis=1) / np.maximum(scale_, 1e-300) if len(co) else np.zeros(0)
+    stats["max_rel_cov"] = float(cerr.max()) if cerr.size else 0.0
+    if strict_floats:
+        assert stats["max_rel_cov"] <= 1e-5, stats["max_rel_cov"]
+    return stats
+
+
+def oracle_regions(res: O.StepResult, view_ids) -> np.ndarray:
+    """Oracle regions as rows (candidate, view_pos, band, minpix, n, Sx, Sy, Sxx, Sxy, Syy)
+    in reference order (candidate, view, band, first pixel)."""
+    rows = []
+    pos = {v: k for k, v in enumerate(view_ids)}
+    for v in view_ids:
+        for r in res.regions[v]:
+            x = r.pixels[:, 0].astype(np.int64)
+            y = r.pixels[:, 1].astype(np.int64)
+            rows.append([r.candidate, pos[v], r.band, r.minpix, len(x), x.sum(), y.sum(), (x * x).sum(),
+                         (x * y).sum(), (y * y).sum()])
+    rows = np.array(rows, dtype=np.int64).reshape(-1, 10)
+    order = np.lexsort((rows[:, 3], rows[:, 2], rows[:, 1], rows[:, 0]))
+    return rows[order]
+
+
+def gpu_regions(plan) -> np.ndarray:
+    r = plan.regions()
+    cols = [r["candidate"], r["view_pos"], r["band"], r["minpix"]]
+    rows = np.concatenate([np.stack([c.long().cpu().numpy() for c in cols], 1),
+                           r["moments"].cpu().numpy()], 1) if len(r["candidate"]) else np.zeros((0, 10), np.int64)
+    return rows.astype(np.int64)

@@ -1,0 +1,250 @@
+"""GPU parity: the CUDA operator (through the C ABI) vs the CPU oracle.
+
+Run on a B200:  python -m pytest tests -m gpu -q
+"""
+
+import numpy as np
+import pytest
+
+import golden_io
+import parity as PA
+from oracle import adpsplit_oracle as O
+
+pytestmark = pytest.mark.gpu
+
+DATA, META = golden_io.load()
+STEP_TAGS = sorted(META["step"])
+
+
+@pytest.fixture(scope="module")
+def op():
+    import torch
+    assert torch.cuda.is_available(), "GPU tests need a CUDA device"
+    from paper_2605_06876_b200 import operator
+    return operator
+
+
+@pytest.fixture(scope="module")
+def plan(op):
+    p = op.Plan("cuda:0")
+    p.set_debug_records(True)
+    return p
+
+
+def _golden_step_inputs(tag):
+    g, extent = golden_io.scene(DATA, f"step__{tag}__in")
+    g = PA.oracle_gaussians_f32(g)
+    cams = golden_io.cams(DATA, f"step__{tag}__cams")
+    rows = DATA[f"step__{tag}__cams"]
+    gts = PA.f32(DATA[f"step__{tag}__gt"])
+    m = META["step"][tag]
+    return g, extent, cams, rows, gts, golden_io.Cfg(m["cfg"]), m["seed"]
+
+
+# --------------------------------------------------------------------- render
+@pytest.mark.parametrize("c", range(12))
+def test_render_matches_oracle(op, plan, c):
+    g, _ = golden_io.scene(DATA, f"render__{c}__scene")
+    g = PA.oracle_gaussians_f32(g)
+    cam = golden_io.cams(DATA, f"render__{c}__cam")[0]
+    img_o, dom_o, best, second = O.render(g, cam, with_weights=True)
+    t = PA.to_tensors(g)
+    img, dom = plan.render(t, DATA[f"render__{c}__cam"])
+    img = img[0].double().cpu().numpy()
+    dom = dom[0].long().cpu().numpy()
+    assert np.abs(img - img_o).max() < 2e-5
+    tie = (best - second) <= PA.EPS_TIE * np.maximum(best, 1e-30)
+    assert not ((dom != dom_o) & ~tie).any()
+
+
+def test_render_empty_and_behind_camera(op, plan):
+    g = O.Gaussians([[0, 0, -10.0]], [[0.1] * 3], [[1, 0, 0, 0]], [0.5], [[0, 0, 0]])
+    cam = O.Cam(np.eye(3), np.array([0, 0, -3.0]), 20.0, 20.0, 7.5, 7.5, 16, 16)
+    img, dom = plan.render(PA.to_tensors(g), cam.row()[None], bg=(0.1, 0.2, 0.3))
+    assert (dom.cpu().numpy() == -1).all()
+    np.testing.assert_allclose(img[0, 0, 0].cpu().numpy(), [0.1, 0.2, 0.3], rtol=1e-6)
+
+
+# ----------------------------------------------------------------------- maps
+@pytest.mark.parametrize("c", range(24))
+def test_maps_bit_exact(op, plan, c):
+    """Eroded metric map and bands equal compute_maps on identical fp32 inputs."""
+    import torch
+    cfg = dict(META["maps"][c])
+    rendered = PA.f32(DATA[f"maps__{c}__rendered"])
+    gt = PA.f32(DATA[f"maps__{c}__gt"])
+    h, w = rendered.shape[:2]
+    want = O.compute_maps(rendered, gt, cfg)
+    g = O.Gaussians([[0, 0, 0.0]], [[0.1] * 3], [[1, 0, 0, 0]], [0.5], [[0, 0, 0]])
+    cam = O.Cam(np.eye(3), np.array([0, 0, -3.0]), 20.0, 20.0, (w - 1) / 2, (h - 1) / 2, w, h)
+    full = dict(tau_l1=0.1, r_erode=2, m_min=5, l_bands=3, n_max=19, v_views=1, gamma_d=2.0,
+                gamma_c=0.15, tau_g=2e-4, tau_s=0.01, eta=1.6, eps=1e-9)
+    full.update(cfg)
+    m = torch.zeros(1, h, w, dtype=torch.uint8, device="cuda")
+    b = torch.zeros(1, h, w, dtype=torch.uint8, device="cuda")
+    plan.set_debug_maps(m, b)
+    try:
+        dev = "cuda"
+        img = torch.as_tensor(rendered[None], dtype=torch.float32, device=dev)
+        gtt = torch.as_tensor(gt[None], dtype=torch.float32, device=dev)
+        dom = torch.full((1, h, w), -1, dtype=torch.int32, device=dev)
+        plan.phase1(PA.to_tensors(g), 1.0, torch.zeros(1, dtype=torch.float64, device=dev),
+                    torch.ones(1, dtype=torch.float64, device=dev), full, cam.row()[None], img, gtt, dom)
+    finally:
+        plan.set_debug_maps(None, None)
+    np.testing.assert_array_equal(m[0].cpu().numpy().astype(bool), want.m)
+    np.testing.assert_array_equal(b[0].cpu().numpy().astype(np.int64), want.b)
+
+
+# ------------------------------------------------------------------ partition
+def _injected_partition(op, plan, e, dom, n_gauss, l_bands, m_min, cands, tau=0.1):
+    """Run phase 1 with error map e injected exactly (raw = e, lo = 0, hi = 1)."""
+    import torch
+    h, w = e.shape
+    e = e.astype(np.float32)
+    e.flat[0], e.flat[-1] = 0.0, 1.0
+    rendered = np.zeros((h, w, 3), np.float32)
+    rendered[..., 0] = e
+    gt = np.zeros((h, w, 3), np.float32)
+    rng = np.random.default_rng(0)
+    g = O.Gaussians(rng.uniform(-0.2, 0.2, (n_gauss, 3)), np.full((n_gauss, 3), 0.3),
+                    np.tile([1.0, 0, 0, 0], (n_gauss, 1)), np.full(n_gauss, 0.5), np.zeros((n_gauss, 3)))
+    cam = O.Cam(np.eye(3), np.array([0, 0, -3.0]), 1.2 * w, 1.2 * w, (w - 1) / 2, (h - 1) / 2, w, h)
+    ga = np.full(n_gauss, 1e-6)
+    ga[cands] = 1.0
+    cfg = dict(tau_l1=tau, r_erode=1, m_min=m_min, l_bands=l_bands, n_max=19, v_views=1, gamma_d=2.0,
+               gamma_c=0.15, tau_g=2e-4, tau_s=0.01, eta=1.6, eps=1e-9)
+    dev = "cuda"
+    plan.phase1(PA.to_tensors(g), 1.0, torch.as_tensor(ga, device=dev), torch.ones(n_gauss, dtype=torch.float64,
+                device=dev), cfg, cam.row()[None], torch.as_tensor(rendered[None], device=dev),
+                torch.as_tensor(gt[None], device=dev), torch.as_tensor(dom[None].astype(np.int32), device=dev))
+    got = PA.gpu_regions(plan)
+    maps = O.compute_maps(rendered.astype(np.float64), gt.astype(np.float64), cfg)
+    is_c = np.zeros(n_gauss, bool)
+    is_c[cands] = True
+    regs = O.partition(maps, dom, is_c, m_min, view=0)
+    fake = O.StepResult(None, 0, 0, None, [], [], [], [0], 0, regions={0: regs})
+    want = PA.oracle_regions(fake, [0])
+    return got, want
+
+
+@pytest.mark.parametrize("seed", range(8))
+def test_partition_random_blocky(op, plan, seed):
+    rng = np.random.default_rng(seed)
+    h, w = int(rng.integers(40, 140)), int(rng.integers(40, 140))
+    n = 6
+    dom = np.kron(rng.integers(-1, n, (h // 3 + 1, w // 3 + 1)), np.ones((3, 3), np.int64))[:h, :w]
+    e = rng.uniform(0, 1, (h, w))
+    e[rng.uniform(size=(h, w)) < 0.3] = 0.05
+    got, want = _injected_partition(op, plan, e, dom, n, int(rng.integers(1, 4)), int(rng.integers(1, 5)),
+                                    [0, 2, 3, 5])
+    np.testing.assert_array_equal(got, want)
+
+
+@pytest.mark.parametrize("shape", [(64, 64), (97, 131), (33, 33), (1, 200), (200, 1)])
+def test_partition_snakes_cross_tiles(op, plan, shape):
+    """Long thin components crossing many 32x32 tile borders (8-connectivity)."""
+    h, w = shape
+    e = np.full((h, w), 0.9)
+    dom = np.full((h, w), 1, np.int64)
+    yy, xx = np.mgrid[0:h, 0:w]
+    dom[(xx + yy) % 7 == 0] = 0          # diagonal stripes of another candidate
+    dom[(xx * 3 + yy) % 11 == 0] = -1
+    got, want = _injected_partition(op, plan, e, dom, 2, 1, 1, [0, 1])
+    np.testing.assert_array_equal(got, want)
+
+
+def test_partition_spiral(op, plan):
+    n = 150
+    e = np.full((n, n), 0.02)
+    dom = np.zeros((n, n), np.int64)
+    x, y, dx, dy = 0, 0, 1, 0
+    lo_x, hi_x, lo_y, hi_y = 0, n - 1, 2, n - 1
+    for _ in range(n * n):
+        e[y, x] = 0.8
+        nx, ny = x + dx, y + dy
+        if not (lo_x <= nx <= hi_x and lo_y - 2 <= ny <= hi_y):
+            if dx == 1: hi_x -= 2
+            elif dy == 1: hi_y -= 2
+            elif dx == -1: lo_x += 2
+            else: lo_y += 2
+            dx, dy = -dy, dx
+            nx, ny = x + dx, y + dy
+            if not (0 <= nx < n and 0 <= ny < n) or hi_x < lo_x:
+                break
+        x, y = nx, ny
+    got, want = _injected_partition(op, plan, e, dom, 1, 2, 2, [0])
+    np.testing.assert_array_equal(got, want)
+
+
+# ----------------------------------------------------------------------- step
+@pytest.mark.parametrize("tag", STEP_TAGS)
+def test_step_stage_isolated(op, plan, tag):
+    """Same (image, dominant) into both: integers exact, floats within tolerance."""
+    import torch
+    g, extent, cams, rows, gts, cfg, seed = _golden_step_inputs(tag)
+    views = O.sample_views(len(cams), cfg.v_views, np.random.default_rng(seed))
+    img, dom = plan.render(PA.to_tensors(g), rows[views])
+    renders_np = {v: (img[k].double().cpu().numpy(), dom[k].long().cpu().numpy()) for k, v in enumerate(views)}
+    gres = op.densify_step(PA.to_tensors(g), extent, rows, torch.as_tensor(gts, dtype=torch.float32, device="cuda"),
+                           torch.as_tensor(DATA[f"step__{tag}__grad_accum"], device="cuda"),
+                           torch.as_tensor(DATA[f"step__{tag}__denom"], device="cuda"), cfg,
+                           np.random.default_rng(seed), renders=(img, dom), plan=plan)
+    ores = O.adpsplit_step(g, extent, cams, gts, DATA[f"step__{tag}__grad_accum"],
+                           DATA[f"step__{tag}__denom"], cfg, np.random.default_rng(seed), renders=renders_np)
+    np.testing.assert_array_equal(PA.gpu_regions(plan), PA.oracle_regions(ores, views))
+    flagged = PA.flag_candidates(ores, g, cams, cfg)
+    st = PA.compare_step(gres, ores, flagged, g)
+    assert st["mismatched"] == 0
+
+
+@pytest.mark.parametrize("tag", STEP_TAGS)
+def test_step_end_to_end(op, plan, tag):
+    """GPU render + step vs the oracle's fp64 render + step, near-threshold classes excluded."""
+    import torch
+    g, extent, cams, rows, gts, cfg, seed = _golden_step_inputs(tag)
+    gres = op.densify_step(PA.to_tensors(g), extent, rows, torch.as_tensor(gts, dtype=torch.float32, device="cuda"),
+                           torch.as_tensor(DATA[f"step__{tag}__grad_accum"], device="cuda"),
+                           torch.as_tensor(DATA[f"step__{tag}__denom"], device="cuda"), cfg,
+                           np.random.default_rng(seed), plan=plan)
+    views = gres.view_ids
+    weights, renders_o = {}, {}
+    for v in views:
+        img_o, dom_o, best, second = O.render(g, cams[v], with_weights=True)
+        weights[v] = (best, second)
+        renders_o[v] = (img_o, dom_o)
+    ores = O.adpsplit_step(g, extent, cams, gts, DATA[f"step__{tag}__grad_accum"],
+                           DATA[f"step__{tag}__denom"], cfg, np.random.default_rng(seed), renders=renders_o)
+    img, dom = plan.render(PA.to_tensors(g), rows[views])
+    gpu_r = {v: (img[k].double().cpu().numpy(), dom[k].long().cpu().numpy()) for k, v in enumerate(views)}
+    assert PA.unexplained_dominance(ores, gpu_r, weights) == 0
+    flagged = PA.flag_candidates(ores, g, cams, cfg) | PA.flag_end_to_end(ores, gpu_r, gts, cfg, weights)
+    PA.compare_step(gres, ores, flagged, g)
+
+
+def test_reference_api_drop_in(op):
+    """adpsplit_step(scene, cameras, gt_images, stats, cfg, rng) with the mirror types."""
+    from paper_2605_06876_b200 import types as T
+    tag = "blobs"
+    g, extent = golden_io.scene(DATA, f"step__{tag}__in")
+    cams = [T.Camera(r_c2w=r[:9].reshape(3, 3), center=r[9:12], f_x=r[12], f_y=r[13], p_x=r[14], p_y=r[15],
+                     width=int(r[16]), height=int(r[17])) for r in DATA[f"step__{tag}__cams"]]
+    gs = [T.Gaussian3D(mu=g.mu[i], scale=g.scale[i], rot=g.rot[i], opacity=g.opacity[i], sh_dc=g.sh_dc[i])
+          for i in range(len(g))]
+    scene = T.Scene(gaussians=list(gs), extent=extent)
+    m = META["step"][tag]
+    cfg = T.AdpSplitConfig(**{k: v for k, v in m["cfg"].items()})
+    stats = T.DensifyStats(DATA[f"step__{tag}__grad_accum"].copy(), DATA[f"step__{tag}__denom"].copy())
+    scene, rep = op.adpsplit_step(scene, cams, list(DATA[f"step__{tag}__gt"]), stats, cfg,
+                                  np.random.default_rng(m["seed"]))
+    want = m["report"]
+    assert rep.count_after == want["count_after"] == len(scene.gaussians)
+    assert rep.clones == want["clones"] and rep.sampled_views == want["sampled_views"]
+    assert [(r.index, r.fallback, r.reset, r.children_inserted) for r in rep.candidates] == \
+        [(r["index"], r["fallback"], r["reset"], r["children_inserted"]) for r in want["candidates"]]
+    for new_i, old_i in enumerate(rep.index_map):
+        if old_i >= 0:
+            assert scene.gaussians[new_i] is gs[old_i]
+    with pytest.raises(ValueError):
+        op.adpsplit_step(T.Scene(gaussians=list(gs), extent=extent), cams[:2], [], stats,
+                         cfg.with_overrides({"v_views": 5}), np.random.default_rng(0))
