@@ -192,6 +192,11 @@ ADPS_API adps_status adps_set_timing(adps_plan* plan, int32_t enabled);
 ADPS_API adps_status adps_get_timing(adps_plan* plan, double* ms, int32_t max_entries, int32_t* n_entries,
                             const char** names);
 
+/* Cumulative number of kernels this plan launched (own kernels) and of
+ * library sort calls (CUB radix sort) -- used by the benchmark's
+ * gpu_launches accounting. */
+ADPS_API adps_status adps_get_launch_count(adps_plan* plan, int64_t* kernels, int64_t* library_calls);
+
 /* DensifyStats feed (ref/adc.py:73-79): grad_accum[vis] += |vg|, denom[vis] += 1.
  * viewspace_grad [n,2] fp32, visible [n] uint8. */
 ADPS_API adps_status adps_accumulate_stats(void* stream, double* grad_accum, double* denom,

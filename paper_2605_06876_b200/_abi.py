@@ -57,7 +57,7 @@ EXPORTS = (
     "adps_abi_version", "adps_last_error", "adps_plan_create", "adps_plan_destroy", "adps_render",
     "adps_step_phase1", "adps_step_phase2", "adps_get_report", "adps_get_regions",
     "adps_set_debug_records", "adps_set_debug_maps", "adps_set_timing", "adps_get_timing",
-    "adps_accumulate_stats",
+    "adps_accumulate_stats", "adps_get_launch_count",
 )
 
 _lib = None
@@ -89,6 +89,7 @@ def load(path: str = LIB_PATH):
     lib.adps_get_timing.argtypes = [vp, C.POINTER(C.c_double), C.c_int32, C.POINTER(C.c_int32),
                                     C.POINTER(C.c_char_p)]
     lib.adps_accumulate_stats.argtypes = [vp, vp, vp, vp, vp, C.c_int64]
+    lib.adps_get_launch_count.argtypes = [vp, C.POINTER(C.c_int64), C.POINTER(C.c_int64)]
     for name in EXPORTS:
         fn = getattr(lib, name)
         if name not in ("adps_abi_version", "adps_last_error"):

@@ -421,13 +421,14 @@ __global__ void partial_emit_kernel(const PartialRec* __restrict__ partials, con
 // --------------------------------------------------------------- launchers
 size_t tile_smem_bytes() { return sizeof(TileSmem); }
 
-cudaError_t launch_attribution(const AttributionArgs& a, cudaStream_t s) {
+cudaError_t launch_attribution(const AttributionArgs& a, cudaStream_t s, MarkFn mark, void* ctx) {
   const long long hw = (long long)a.H * a.W;
   dim3 mg((unsigned)((hw + 256 * 8 - 1) / (256 * 8)), (unsigned)a.V);
   if (mg.x > 1024) mg.x = 1024;
   minmax_kernel<<<mg, 256, 0, s>>>(a.image, a.gt, hw, a.lohi);
   int nt = a.V * a.L;
   thresholds_kernel<<<(nt + 127) / 128, 128, 0, s>>>(a.lohi, a.V, a.L, a.tau, a.lo, a.thr);
+  if (mark) mark(ctx, "minmax", s, 2);
   TileParams P;
   P.image = a.image;
   P.gt = a.gt;
@@ -461,6 +462,7 @@ cudaError_t launch_attribution(const AttributionArgs& a, cudaStream_t s) {
   cudaError_t e = cudaFuncSetAttribute(tile_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   tile_kernel<<<(unsigned)nblocks, kTileThreads, smem, s>>>(P);
+  if (mark) mark(ctx, "tile_ccl", s, 1);
   BorderParams B;
   B.border = a.border;
   B.partials = a.partials;
@@ -473,6 +475,7 @@ cudaError_t launch_attribution(const AttributionArgs& a, cudaStream_t s) {
   resolve_kernel<<<a.grid_small, 256, 0, s>>>(a.partials, a.partial_parent, a.n_partials, a.partial_cap);
   partial_emit_kernel<<<a.grid_small, 256, 0, s>>>(a.partials, a.partial_parent, a.n_partials, a.partial_cap,
                                                     a.m_min, a.regions, a.n_regions, a.region_cap, a.overflow);
+  if (mark) mark(ctx, "border_merge", s, 3);
   return cudaGetLastError();
 }
 

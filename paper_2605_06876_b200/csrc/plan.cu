@@ -61,8 +61,7 @@ cudaError_t ensure(Buf& b, size_t bytes) {
   return cudaSuccess;
 }
 
-const char* kStageNames[] = {"select", "attribution", "child_init", "sort", "merge", "offsets", "emit"};
-constexpr int kStages = 7;
+constexpr int kMaxMarks = 32;
 
 }  // namespace
 
@@ -102,9 +101,31 @@ struct adps_plan {
   unsigned char* dbg_b = nullptr;
   bool dbg_records = false;
   bool timing = false;
-  cudaEvent_t ev[kStages + 1] = {};
-  double stage_ms[kStages] = {};
+  // timing marks: ev[0] is the start of a phase, ev[i] ends stage names[i]
+  cudaEvent_t ev[kMaxMarks] = {};
+  const char* names[kMaxMarks] = {};
+  int n_marks = 0;
+  // launch accounting (own kernels / library sort calls), cumulative
+  long long launches = 0;
+  long long lib_calls = 0;
 };
+
+static void mark(adps_plan* P, const char* name, cudaStream_t s, int kernels) {
+  P->launches += kernels;
+  if (!P->timing || P->n_marks >= kMaxMarks) return;
+  cudaEventRecord(P->ev[P->n_marks], s);
+  P->names[P->n_marks] = name;
+  ++P->n_marks;
+}
+
+static void mark_cb(void* ctx, const char* name, cudaStream_t s, int kernels) {
+  mark(reinterpret_cast<adps_plan*>(ctx), name, s, kernels);
+}
+
+static void mark_start(adps_plan* P, cudaStream_t s, bool reset) {
+  if (reset) P->n_marks = 0;
+  mark(P, "start", s, 0);
+}
 
 static adps_status scan_state(adps_plan* P, Buf& val, Buf& flag, Buf& ticket, long long n, ScanState* st) {
   long long tiles = scan_tiles(n);
@@ -139,7 +160,7 @@ extern "C" adps_status adps_plan_create(adps_plan** plan, int32_t device, int64_
     delete P;
     return fail(ADPS_OOM, "pinned allocation failed: %s", cudaGetErrorString(e));
   }
-  for (int i = 0; i <= kStages; ++i) cudaEventCreate(&P->ev[i]);
+  for (int i = 0; i < kMaxMarks; ++i) cudaEventCreate(&P->ev[i]);
   (void)max_n;
   (void)max_views;
   (void)height;
@@ -169,7 +190,7 @@ extern "C" adps_status adps_plan_destroy(adps_plan* P) {
   if (P->lohi_host) cudaFreeHost(P->lohi_host);
   if (P->cams_host) cudaFreeHost(P->cams_host);
   if (P->r_total_host) cudaFreeHost(P->r_total_host);
-  for (int i = 0; i <= kStages; ++i)
+  for (int i = 0; i < kMaxMarks; ++i)
     if (P->ev[i]) cudaEventDestroy(P->ev[i]);
   delete P;
   return ADPS_OK;
@@ -318,14 +339,13 @@ extern "C" adps_status adps_render(adps_plan* P, void* stream_v, const adps_gaus
     ba.image = image + (long long)v * hw * 3;
     ba.dominant = dominant + (long long)v * hw;
     CK(launch_blend(ba, n_tiles, s));
+    P->launches += n_dup > 0 ? 5 : 3;
+    P->lib_calls += n_dup > 0 ? 2 : 1;
   }
   return ADPS_OK;
 }
 
 // ------------------------------------------------------------------ phase 1
-static void rec(adps_plan* P, int i, cudaStream_t s) {
-  if (P->timing) cudaEventRecord(P->ev[i], s);
-}
 
 static adps_status run_attribution(adps_plan* P, cudaStream_t s, int V, int H, int W, const adps_config* cfg,
                                    int N, const float* image, const float* gt, const int32_t* dominant) {
@@ -369,7 +389,7 @@ static adps_status run_attribution(adps_plan* P, cudaStream_t s, int V, int H, i
   a.dbg_b = P->dbg_b;
   a.overflow = &ctr->overflow;
   a.grid_small = (unsigned)(P->sm_count * 4);
-  CK(launch_attribution(a, s));
+  CK(launch_attribution(a, s, mark_cb, P));
   return ADPS_OK;
 }
 
@@ -440,7 +460,7 @@ extern "C" adps_status adps_step_phase1(adps_plan* P, void* stream_v, const adps
   CK(cudaMemcpyAsync(P->cams.p, P->cams_host, sizeof(double) * 18 * V, cudaMemcpyHostToDevice, s));
   Counters* ctr = P->ctr.as<Counters>();
   CK(cudaMemsetAsync(ctr, 0, sizeof(Counters), s));
-  rec(P, 0, s);
+  mark_start(P, s, true);
 
   // ---- select (ref/adc.py:165)
   ScanState sst, sst2;
@@ -459,7 +479,7 @@ extern "C" adps_status adps_step_phase1(adps_plan* P, void* stream_v, const adps
   sa.clone_list = P->clone_list.as<int>();
   sa.ctr = ctr;
   CK(launch_select(sa, sst, s));
-  rec(P, 1, s);
+  mark(P, "select", s, 1);
 
   // ---- maps + partition + moments + ever-dominant (ref/adc.py:168-180)
   for (int attempt = 0;; ++attempt) {
@@ -484,7 +504,7 @@ extern "C" adps_status adps_step_phase1(adps_plan* P, void* stream_v, const adps
   const long long n_regions = (long long)P->ctr_host->n_regions;
   const long long n_split = (long long)P->ctr_host->n_split;
   const long long n_clone = (long long)P->ctr_host->n_clone;
-  rec(P, 2, s);
+  mark(P, "host_sync", s, 0);
 
   // ---- region stats + child init (ref/adc.py:172-176, 190-196)
   const long long rc = n_regions > 0 ? n_regions : 1;
@@ -532,7 +552,7 @@ extern "C" adps_status adps_step_phase1(adps_plan* P, void* stream_v, const adps
   long long cgrid = (n_regions + 127) / 128;
   ca.grid = (unsigned)(cgrid < 1 ? 1 : (cgrid > 65535 ? 65535 : cgrid));
   if (n_regions > 0) CK(launch_child_init(ca, s));
-  rec(P, 3, s);
+  mark(P, "child_init", s, n_regions > 0 ? 1 : 0);
 
   // ---- order (candidate, view, band, first pixel)  (ref/adc.py:190-195)
   if (n_regions > 0) {
@@ -578,7 +598,8 @@ extern "C" adps_status adps_step_phase1(adps_plan* P, void* stream_v, const adps
   long long rgrid = (n_regions + 255) / 256;
   ra.grid = (unsigned)(rgrid < 1 ? 1 : (rgrid > 65535 ? 65535 : rgrid));
   CK(launch_ranges(ra, s));
-  rec(P, 4, s);
+  mark(P, "sort_ranges", s, n_regions > 0 ? 1 : 0);
+  if (n_regions > 0) P->lib_calls += 1;
 
   // ---- per-candidate case, merge, cap (ref/adc.py:184-227)
   MergeArgs ma;
@@ -608,7 +629,7 @@ extern "C" adps_status adps_step_phase1(adps_plan* P, void* stream_v, const adps
   long long mgrid = (n_split + 7) / 8;
   ma.grid = (unsigned)(mgrid < 1 ? 1 : (mgrid > (long long)P->sm_count * 16 ? P->sm_count * 16 : mgrid));
   if (n_split > 0) CK(launch_merge(ma, s));
-  rec(P, 5, s);
+  mark(P, "merge_cap", s, n_split > 0 ? 2 : 0);
 
   // ---- offsets (ref/adc.py:229-244)
   st = scan_state(P, P->scan2_val, P->scan2_flag, P->scan2_ticket, sc, &sst2);
@@ -625,17 +646,10 @@ extern "C" adps_status adps_step_phase1(adps_plan* P, void* stream_v, const adps
   oa.ctr = ctr;
   oa.n_split_dev = &ctr->n_split;
   CK(launch_offsets(oa, n_split, sst2, sst, s));
-  rec(P, 6, s);
+  mark(P, "offsets", s, 2);
   CK(cudaMemcpyAsync(P->ctr_host, ctr, sizeof(Counters), cudaMemcpyDeviceToHost, s));
   CK(cudaStreamSynchronize(s));
   const Counters& C = *P->ctr_host;
-  if (P->timing) {
-    for (int i = 0; i < 6; ++i) {
-      float ms = 0;
-      cudaEventElapsedTime(&ms, P->ev[i], P->ev[i + 1]);
-      P->stage_ms[i] = ms;
-    }
-  }
   adps_counts& K = P->counts;
   K.n_before = n;
   K.n_split = n_split;
@@ -677,7 +691,7 @@ extern "C" adps_status adps_step_phase2(adps_plan* P, void* stream_v, const adps
   if (P->sh_k > 0 && !out->sh_rest) return fail(ADPS_INVALID_ARG, "out.sh_rest is NULL");
   CK(cudaSetDevice(P->device));
   cudaStream_t s = (cudaStream_t)stream_v;
-  if (P->timing) cudaEventRecord(P->ev[0], s);
+  mark_start(P, s, false);
   EmitArgs ea;
   ea.g = to_in(g);
   ea.n = P->n;
@@ -704,9 +718,7 @@ extern "C" adps_status adps_step_phase2(adps_plan* P, void* stream_v, const adps
   ea.sh_rest = out->sh_rest;
   ea.index_map = (long long*)index_map;
   CK(launch_emit(ea, s));
-  if (P->timing) {
-    cudaEventRecord(P->ev[1], s);
-  }
+  mark(P, "emit", s, (P->n + P->counts.n_split + P->counts.n_clone) > 0 ? 1 : 0);
   return ADPS_OK;
 }
 
@@ -761,12 +773,24 @@ extern "C" adps_status adps_set_timing(adps_plan* P, int32_t enabled) {
 extern "C" adps_status adps_get_timing(adps_plan* P, double* ms, int32_t max_entries, int32_t* n_entries,
                                        const char** names) {
   if (!P || !n_entries) return fail(ADPS_INVALID_ARG, "NULL argument");
-  int n = 6 < max_entries ? 6 : max_entries;
-  for (int i = 0; i < n; ++i) {
-    if (ms) ms[i] = P->stage_ms[i];
-    if (names) names[i] = kStageNames[i];
+  int n = 0;
+  if (P->n_marks > 0) CK(cudaEventSynchronize(P->ev[P->n_marks - 1]));
+  for (int i = 1; i < P->n_marks && n < max_entries; ++i) {
+    if (strcmp(P->names[i], "start") == 0) continue;
+    float t = 0.f;
+    CK(cudaEventElapsedTime(&t, P->ev[i - 1], P->ev[i]));
+    if (ms) ms[n] = t;
+    if (names) names[n] = P->names[i];
+    ++n;
   }
   *n_entries = n;
+  return ADPS_OK;
+}
+
+extern "C" adps_status adps_get_launch_count(adps_plan* P, int64_t* kernels, int64_t* library_calls) {
+  if (!P || !kernels || !library_calls) return fail(ADPS_INVALID_ARG, "NULL argument");
+  *kernels = P->launches;
+  *library_calls = P->lib_calls;
   return ADPS_OK;
 }
 

@@ -173,11 +173,22 @@ class Plan:
         _abi.check(self.lib.adps_set_timing(self._h, int(on)))
 
     def stage_ms(self) -> dict:
-        ms = (C.c_double * 8)()
-        names = (C.c_char_p * 8)()
+        """Per-stage device times (ms) of the last phase 1 + phase 2 (timing mode)."""
+        ms = (C.c_double * 32)()
+        names = (C.c_char_p * 32)()
         n = C.c_int32()
-        _abi.check(self.lib.adps_get_timing(self._h, ms, 8, C.byref(n), names))
-        return {names[i].decode(): float(ms[i]) for i in range(n.value)}
+        _abi.check(self.lib.adps_get_timing(self._h, ms, 32, C.byref(n), names))
+        out = {}
+        for i in range(n.value):
+            k = names[i].decode()
+            out[k] = out.get(k, 0.0) + float(ms[i])
+        return out
+
+    def launch_count(self):
+        """(own kernels, library sort calls) launched by this plan so far."""
+        k, lib = C.c_int64(), C.c_int64()
+        _abi.check(self.lib.adps_get_launch_count(self._h, C.byref(k), C.byref(lib)))
+        return int(k.value), int(lib.value)
 
     def set_debug_records(self, on: bool):
         _abi.check(self.lib.adps_set_debug_records(self._h, int(on)))
