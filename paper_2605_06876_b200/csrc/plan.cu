@@ -129,7 +129,7 @@ static void mark_start(adps_plan* P, cudaStream_t s, bool reset) {
 
 static adps_status scan_state(adps_plan* P, Buf& val, Buf& flag, Buf& ticket, long long n, ScanState* st) {
   long long tiles = scan_tiles(n);
-  CK(ensure(val, sizeof(unsigned long long) * tiles));
+  CK(ensure(val, 2 * sizeof(unsigned long long) * tiles));
   CK(ensure(flag, sizeof(unsigned int) * tiles));
   CK(ensure(ticket, sizeof(unsigned int)));
   st->value = val.as<unsigned long long>();

@@ -16,8 +16,8 @@ constexpr int kScanItems = 8;
 constexpr int kScanTile = kScanThreads * kScanItems;
 
 struct ScanState {
-  unsigned long long* value;  // [n_tiles]
-  unsigned int* flag;         // [n_tiles] 0 = empty, 1 = aggregate, 2 = inclusive prefix
+  unsigned long long* value;  // [2 * n_tiles]: aggregate at [2t], inclusive prefix at [2t+1]
+  unsigned int* flag;         // [n_tiles] 0 = empty, 1 = aggregate ready, 2 = inclusive ready
   unsigned int* ticket;       // [1] dynamic tile id (reset to 0 before launch)
 };
 
@@ -76,13 +76,15 @@ __global__ void __launch_bounds__(kScanThreads) scan_kernel(Policy pol, long lon
     const unsigned long long agg = thread_excl + run;
     volatile unsigned long long* vval = st.value;
     volatile unsigned int* vflag = st.flag;
+    // The aggregate and the inclusive prefix live in separate words: a reader
+    // that saw flag==1 must never pick up the later inclusive value.
     if (tile == 0) {
-      vval[0] = agg;
+      vval[1] = agg;
       __threadfence();
       vflag[0] = 2u;
       s_prefix = 0ull;
     } else {
-      vval[tile] = agg;
+      vval[2 * tile] = agg;
       __threadfence();
       vflag[tile] = 1u;
       unsigned long long acc = 0ull;
@@ -93,12 +95,14 @@ __global__ void __launch_bounds__(kScanThreads) scan_kernel(Policy pol, long lon
           f = vflag[p];
         } while (f == 0u);
         __threadfence();
-        unsigned long long v = vval[p];
-        acc += v;
-        if (f == 2u) break;
+        if (f == 2u) {
+          acc += vval[2 * p + 1];
+          break;
+        }
+        acc += vval[2 * p];
         --p;
       }
-      vval[tile] = acc + agg;
+      vval[2 * tile + 1] = acc + agg;
       __threadfence();
       vflag[tile] = 2u;
       s_prefix = acc;

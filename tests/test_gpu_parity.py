@@ -248,3 +248,78 @@ def test_reference_api_drop_in(op):
     with pytest.raises(ValueError):
         op.adpsplit_step(T.Scene(gaussians=list(gs), extent=extent), cams[:2], [], stats,
                          cfg.with_overrides({"v_views": 5}), np.random.default_rng(0))
+
+
+# ------------------------------------------------------------ larger sizes
+def test_select_and_scans_large(op, plan):
+    """Split/clone lists and offsets over millions of Gaussians (multi-tile scans)."""
+    import torch
+    n = 3_000_001
+    rng = np.random.default_rng(7)
+    scale = rng.uniform(0.001, 0.03, (n, 3)).astype(np.float32)
+    ga = rng.uniform(0, 4e-4, n)
+    den = np.where(rng.uniform(size=n) < 0.1, 0.0, rng.integers(1, 3, n).astype(np.float64))
+    g = O.Gaussians(rng.uniform(-1, 1, (n, 3)), scale, np.tile([1.0, 0, 0, 0], (n, 1)), np.full(n, 0.5),
+                    np.zeros((n, 3)))
+    w = h = 8
+    cam = O.Cam(np.eye(3), np.array([0, 0, -3.0]), 10.0, 10.0, 3.5, 3.5, w, h)
+    cfg = dict(tau_l1=0.1, r_erode=2, m_min=5, l_bands=3, n_max=19, v_views=1, gamma_d=2.0, gamma_c=0.15,
+               tau_g=2e-4, tau_s=0.01, eta=1.6, eps=1e-9)
+    dev = "cuda"
+    z = torch.zeros(1, h, w, 3, dtype=torch.float32, device=dev)
+    counts = plan.phase1(PA.to_tensors(g), 1.0, torch.as_tensor(ga, device=dev), torch.as_tensor(den, device=dev),
+                         cfg, cam.row()[None], z, z, torch.full((1, h, w), -1, dtype=torch.int32, device=dev))
+    split, clone = O.select(ga, den, scale.astype(np.float64), 2e-4, 0.01)
+    ra = plan.report_arrays(counts["n_split"], counts["n_clone"])
+    np.testing.assert_array_equal(ra["cand_index"].cpu().numpy(), split)
+    np.testing.assert_array_equal(ra["clone_index"].cpu().numpy(), clone)
+    assert (ra["cand_case"].cpu().numpy() == 1).all()      # nothing dominant -> all fallback
+    assert counts["n_keep"] == n - len(split)
+    assert counts["n_out"] == n - len(split) + 2 * len(split) + len(clone)
+
+
+def test_render_medium_vs_c_oracle(op, plan):
+    """20k Gaussians, non-multiple-of-16 image: GPU render vs the C restatement."""
+    from oracle import c_render
+    from paper_2605_06876_b200 import synth as S
+    wl = S.Workload("t", 40_000, 2, 210, 150, 0.05, 0.02, 0.02 * np.sqrt(2.4e6 / 4e4),
+                    large_range=(0.005 * np.sqrt(60), 0.01 * np.sqrt(60)))
+    ini, cams, _, _ = wl.build(seed=3)
+    g = O.Gaussians(ini.mu, ini.scale, ini.rot, ini.opacity, ini.sh_dc)
+    img, dom = plan.render(PA.to_tensors(g), cams)
+    for v in range(len(cams)):
+        io, do = c_render.render(g, cams[v])
+        ig = img[v].double().cpu().numpy()
+        dg = dom[v].long().cpu().numpy()
+        assert np.abs(ig - io).max() < 1e-4
+        assert (dg != do).mean() < 1e-3      # near-ties only (fp32 vs fp64 weights)
+
+
+@pytest.mark.parametrize("seed", [0, 1])
+def test_synthetic_step_stage_isolated(op, plan, seed):
+    """Paper-default cfg on a 8k-Gaussian synthetic scene, 3 of 5 views, 160x112 px."""
+    import torch
+    from paper_2605_06876_b200 import synth as S
+    sf = np.sqrt(2.4e6 / 16000)
+    wl = S.Workload("t", 16_000, 5, 160, 112, 0.2, 0.05, 0.02 * sf, large_range=(0.005 * sf, 0.01 * sf))
+    ini, cams, (ga, den), gts = wl.build(seed=seed)
+    g = O.Gaussians(ini.mu, ini.scale, ini.rot, ini.opacity, ini.sh_dc)
+    gt_g = O.Gaussians(gts.mu, gts.scale, gts.rot, gts.opacity, gts.sh_dc)
+    gt_img, _ = plan.render(PA.to_tensors(gt_g), cams)
+    cfg = golden_io.Cfg(dict(tau_l1=0.1, r_erode=2, m_min=5, l_bands=3, n_max=19, v_views=3, gamma_d=2.0,
+                             gamma_c=0.15, tau_g=2e-4, tau_s=0.01, eta=1.6, eps=1e-9))
+    views = O.sample_views(len(cams), 3, np.random.default_rng(seed))
+    img, dom = plan.render(PA.to_tensors(g), cams[views])
+    gres = op.densify_step(PA.to_tensors(g), ini.extent, cams, gt_img, torch.as_tensor(ga, device="cuda"),
+                           torch.as_tensor(den, device="cuda"), cfg, np.random.default_rng(seed),
+                           renders=(img, dom), plan=plan)
+    gts_np = {v: gt_img[v].double().cpu().numpy() for v in range(len(cams))}
+    renders_np = {v: (img[k].double().cpu().numpy(), dom[k].long().cpu().numpy()) for k, v in enumerate(views)}
+    cam_objs = [O.Cam.from_row(r) for r in cams]
+    ores = O.adpsplit_step(g, ini.extent, cam_objs, gts_np, ga, den, cfg, np.random.default_rng(seed),
+                           renders=renders_np)
+    np.testing.assert_array_equal(PA.gpu_regions(plan), PA.oracle_regions(ores, views))
+    flagged = PA.flag_candidates(ores, g, cam_objs, cfg)
+    st = PA.compare_step(gres, ores, flagged, g)
+    assert st["mismatched"] == 0
+    assert gres.counts["n_regions"] > 50 and gres.counts["n_children"] > 20
