@@ -302,6 +302,10 @@ def run_ours(args, wl):
         ms = float(t.item())
     counts = res.counts
     n_split = counts["n_split"]
+    pp = res.report_arrays["cand_proposals"].cpu().numpy()
+    props_stats = {"max": int(pp.max()) if len(pp) else 0, "p99": float(np.percentile(pp, 99)) if len(pp) else 0,
+                   "mean": float(pp.mean()) if len(pp) else 0, "over_96": int((pp > 96).sum()),
+                   "total": int(pp.sum())}
 
     # ---- per-stage breakdown with CUDA events on the launching stream
     plan.set_timing(True)
@@ -402,6 +406,7 @@ def run_ours(args, wl):
                        "note": "attribution render (compute-bound), not part of value"},
             "full_step": {"ms": full_ms, "parents_per_s": n_split / (full_ms * 1e-3)},
             "counts": counts,
+            "proposals_per_parent": props_stats,
             "e2e": e2e,
             "gpu_launches": int((k1 - k0) / args.steps),
             "library_sort_calls_per_step": (l1 - l0) / args.steps,

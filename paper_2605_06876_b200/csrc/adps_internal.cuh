@@ -88,6 +88,7 @@ struct Counters {
   unsigned long long n_inserted;
   unsigned long long n_keep;
   unsigned long long n_large;
+  unsigned long long n_seg;
   unsigned int degenerate;
   unsigned int overflow;   // bit0 regions, bit1 partials
 };

@@ -78,6 +78,8 @@ struct adps_plan {
   // tiles / fragments / regions
   Buf border, partials, partial_parent, regions, props, valid, keys, vals, keys_sorted, vals_sorted;
   Buf idx, uf, groups, children, dbg_stats, dbg_child;
+  Buf l_keys, l_vals, l_keys_sorted, l_vals_sorted, l_seg_begin, l_seg_end, l_seg_list, l_work_cnt, l_work_off,
+      l_n_groups, l_rank_of;
   Buf scan_val, scan_flag, scan_ticket, scan2_val, scan2_flag, scan2_ticket, cub_tmp;
   Buf ctr;
   Counters* ctr_host = nullptr;
@@ -108,6 +110,7 @@ struct adps_plan {
   // launch accounting (own kernels / library sort calls), cumulative
   long long launches = 0;
   long long lib_calls = 0;
+  int large_threshold = 96;
 };
 
 static void mark(adps_plan* P, const char* name, cudaStream_t s, int kernels) {
@@ -183,7 +186,8 @@ extern "C" adps_status adps_plan_destroy(adps_plan* P) {
                  &P->scan2_val, &P->scan2_flag, &P->scan2_ticket, &P->cub_tmp, &P->ctr, &P->r_key,
                  &P->r_key_sorted, &P->r_order_in, &P->r_order, &P->r_tiles, &P->r_rect, &P->r_splat,
                  &P->r_offs, &P->r_dup, &P->r_dup_sorted, &P->r_tstart, &P->r_tend, &P->r_total,
-                 &P->r_cams};
+                 &P->r_cams, &P->l_keys, &P->l_vals, &P->l_keys_sorted, &P->l_vals_sorted, &P->l_seg_begin,
+                 &P->l_seg_end, &P->l_seg_list, &P->l_work_cnt, &P->l_work_off, &P->l_n_groups, &P->l_rank_of};
   for (Buf* b : bufs)
     if (b->p) cudaFree(b->p);
   if (P->ctr_host) cudaFreeHost(P->ctr_host);
@@ -577,6 +581,17 @@ extern "C" adps_status adps_step_phase1(adps_plan* P, void* stream_v, const adps
   CK(ensure(P->ins_off, 4 * sc));
   CK(ensure(P->fb_ord, 4 * sc));
   CK(ensure(P->large_list, 4 * sc));
+  CK(ensure(P->l_work_cnt, 8 * sc));
+  CK(ensure(P->l_work_off, 8 * (sc + 1)));
+  CK(ensure(P->l_n_groups, 4 * sc));
+  CK(ensure(P->l_keys, 8 * rc));
+  CK(ensure(P->l_vals, 4 * rc));
+  CK(ensure(P->l_keys_sorted, 8 * rc));
+  CK(ensure(P->l_vals_sorted, 4 * rc));
+  CK(ensure(P->l_seg_begin, 4 * rc));
+  CK(ensure(P->l_seg_end, 4 * rc));
+  CK(ensure(P->l_seg_list, 8 * rc));
+  CK(ensure(P->l_rank_of, 4 * rc));
   CK(ensure(P->regions_per_view, 4 * sc * V));
   CK(cudaMemsetAsync(P->cand_start.p, 0, 4 * sc, s));
   CK(cudaMemsetAsync(P->cand_end.p, 0, 4 * sc, s));
@@ -615,7 +630,7 @@ extern "C" adps_status adps_step_phase1(adps_plan* P, void* stream_v, const adps
   ma.gamma_d = cfg->gamma_d;
   ma.gamma_c = cfg->gamma_c;
   ma.n_max = cfg->n_max;
-  ma.large_threshold = 96;
+  ma.large_threshold = P->large_threshold;
   ma.idx = P->idx.as<int>();
   ma.uf = P->uf.as<int>();
   ma.groups = P->groups.as<GroupRec>();
@@ -628,8 +643,40 @@ extern "C" adps_status adps_step_phase1(adps_plan* P, void* stream_v, const adps
   ma.ctr = ctr;
   long long mgrid = (n_split + 7) / 8;
   ma.grid = (unsigned)(mgrid < 1 ? 1 : (mgrid > (long long)P->sm_count * 16 ? P->sm_count * 16 : mgrid));
-  if (n_split > 0) CK(launch_merge(ma, s));
-  mark(P, "merge_cap", s, n_split > 0 ? 2 : 0);
+  if (n_split > 0) {
+    CK(launch_merge_small(ma, s));
+    mark(P, "merge_small", s, 1);
+    LargeArgs L;
+    L.keys = P->l_keys.as<unsigned long long>();
+    L.vals = P->l_vals.as<int>();
+    L.keys_sorted = P->l_keys_sorted.as<unsigned long long>();
+    L.vals_sorted = P->l_vals_sorted.as<int>();
+    L.seg_begin = P->l_seg_begin.as<int>();
+    L.seg_end = P->l_seg_end.as<int>();
+    L.seg_list = P->l_seg_list.as<long long>();
+    L.n_seg = &ctr->n_seg;
+    L.work_cnt = P->l_work_cnt.as<unsigned long long>();
+    L.work_off = P->l_work_off.as<unsigned long long>();
+    L.n_groups = P->l_n_groups.as<int>();
+    L.rank_of = P->l_rank_of.as<int>();
+    const unsigned lgrid = (unsigned)(P->sm_count * 8);
+    CK(cudaMemsetAsync(L.keys, 0xff, 8 * rc, s));
+    CK(launch_merge_large_gates(ma, L, lgrid, s));
+    mark(P, "merge_large_gates", s, 5);
+    if (n_regions > 0) {
+      const int lbits = 32 + ceil_log2((unsigned long long)(n_split + 1));
+      size_t tb = 0;
+      CK(cub::DeviceRadixSort::SortPairs(nullptr, tb, L.keys, L.keys_sorted, L.vals, L.vals_sorted,
+                                         (int)n_regions, 0, lbits, s));
+      CK(ensure(P->cub_tmp, tb));
+      tb = P->cub_tmp.bytes;
+      CK(cub::DeviceRadixSort::SortPairs(P->cub_tmp.p, tb, L.keys, L.keys_sorted, L.vals, L.vals_sorted,
+                                         (int)n_regions, 0, lbits, s));
+      P->lib_calls += 1;
+    }
+    CK(launch_merge_large_groups(ma, L, n_regions, lgrid, s));
+    mark(P, "merge_large_groups", s, n_regions > 0 ? 3 : 2);
+  }
 
   // ---- offsets (ref/adc.py:229-244)
   st = scan_state(P, P->scan2_val, P->scan2_flag, P->scan2_ticket, sc, &sst2);
@@ -785,6 +832,16 @@ extern "C" adps_status adps_get_timing(adps_plan* P, double* ms, int32_t max_ent
   }
   *n_entries = n;
   return ADPS_OK;
+}
+
+extern "C" adps_status adps_set_param(adps_plan* P, int32_t key, int64_t value) {
+  if (!P) return fail(ADPS_INVALID_ARG, "plan is NULL");
+  if (key == ADPS_PARAM_LARGE_THRESHOLD) {
+    if (value < 0 || value > 1000000) return fail(ADPS_INVALID_ARG, "large threshold out of range");
+    P->large_threshold = (int)value;
+    return ADPS_OK;
+  }
+  return fail(ADPS_INVALID_ARG, "unknown parameter %d", key);
 }
 
 extern "C" adps_status adps_get_launch_count(adps_plan* P, int64_t* kernels, int64_t* library_calls) {

@@ -95,7 +95,25 @@ struct MergeArgs {
   Counters* ctr;
   unsigned grid;
 };
-cudaError_t launch_merge(const MergeArgs& a, cudaStream_t s);
+// scratch of the large-candidate path (P > large_threshold)
+struct LargeArgs {
+  unsigned long long* keys;         // [n_regions] (large id << 32 | root), ~0 elsewhere
+  int* vals;                        // [n_regions] local proposal index j
+  unsigned long long* keys_sorted;  // [n_regions]
+  int* vals_sorted;                 // [n_regions]
+  int* seg_begin;                   // [n_regions] at start + root
+  int* seg_end;                     // [n_regions]
+  long long* seg_list;              // [n_regions]
+  unsigned long long* n_seg;        // [1]
+  unsigned long long* work_cnt;     // [n_split]
+  unsigned long long* work_off;     // [n_split + 1]
+  int* n_groups;                    // [n_split]
+  int* rank_of;                     // [n_regions] cap rank of a root or -1
+};
+cudaError_t launch_merge_small(const MergeArgs& a, cudaStream_t s);
+cudaError_t launch_merge_large_gates(const MergeArgs& a, const LargeArgs& L, unsigned grid, cudaStream_t s);
+cudaError_t launch_merge_large_groups(const MergeArgs& a, const LargeArgs& L, long long n_keys, unsigned grid,
+                                      cudaStream_t s);
 
 // ---- offsets: candidate inserts and survivor compaction (ref/adc.py:229-244) ----
 struct OffsetArgs {

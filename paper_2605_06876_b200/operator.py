@@ -190,6 +190,10 @@ class Plan:
         _abi.check(self.lib.adps_get_launch_count(self._h, C.byref(k), C.byref(lib)))
         return int(k.value), int(lib.value)
 
+    def set_large_threshold(self, p: int):
+        """Parents with more than p proposals take the grid-wide merge path (default 96)."""
+        _abi.check(self.lib.adps_set_param(self._h, _abi.PARAM_LARGE_THRESHOLD, int(p)))
+
     def set_debug_records(self, on: bool):
         _abi.check(self.lib.adps_set_debug_records(self._h, int(on)))
 

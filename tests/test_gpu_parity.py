@@ -323,3 +323,58 @@ def test_synthetic_step_stage_isolated(op, plan, seed):
     st = PA.compare_step(gres, ores, flagged, g)
     assert st["mismatched"] == 0
     assert gres.counts["n_regions"] > 50 and gres.counts["n_children"] > 20
+
+
+@pytest.mark.parametrize("tag", ["paper0", "paper2", "desk3", "blobs"])
+def test_large_merge_path_matches_warp_path(op, plan, tag):
+    """Routing every parent through the grid-wide pair-tile merge gives the oracle's result."""
+    import torch
+    g, extent, cams, rows, gts, cfg, seed = _golden_step_inputs(tag)
+    views = O.sample_views(len(cams), cfg.v_views, np.random.default_rng(seed))
+    img, dom = plan.render(PA.to_tensors(g), rows[views])
+    renders_np = {v: (img[k].double().cpu().numpy(), dom[k].long().cpu().numpy()) for k, v in enumerate(views)}
+    plan.set_large_threshold(0)
+    try:
+        gres = op.densify_step(PA.to_tensors(g), extent, rows, torch.as_tensor(gts, dtype=torch.float32,
+                               device="cuda"), torch.as_tensor(DATA[f"step__{tag}__grad_accum"], device="cuda"),
+                               torch.as_tensor(DATA[f"step__{tag}__denom"], device="cuda"), cfg,
+                               np.random.default_rng(seed), renders=(img, dom), plan=plan)
+    finally:
+        plan.set_large_threshold(96)
+    ores = O.adpsplit_step(g, extent, cams, gts, DATA[f"step__{tag}__grad_accum"],
+                           DATA[f"step__{tag}__denom"], cfg, np.random.default_rng(seed), renders=renders_np)
+    st = PA.compare_step(gres, ores, PA.flag_candidates(ores, g, cams, cfg), g)
+    assert st["mismatched"] == 0
+
+
+def test_large_merge_path_synthetic(op, plan):
+    """A parent with hundreds of proposals (multi-tile gate matrix) vs the oracle."""
+    import torch
+    from paper_2605_06876_b200 import synth as S
+    sf = np.sqrt(2.4e6 / 16000)
+    wl = S.Workload("t", 16_000, 6, 192, 128, 0.3, 0.05, 0.02 * sf, large_range=(0.005 * sf, 0.01 * sf))
+    ini, cams, (ga, den), gts = wl.build(seed=5)
+    ga[-1] = 1.0                      # the cover Gaussian: many regions in every view
+    g = O.Gaussians(ini.mu, ini.scale, ini.rot, ini.opacity, ini.sh_dc)
+    gt_g = O.Gaussians(gts.mu, gts.scale, gts.rot, gts.opacity, gts.sh_dc)
+    gt_img, _ = plan.render(PA.to_tensors(gt_g), cams)
+    cfg = golden_io.Cfg(dict(tau_l1=0.1, r_erode=1, m_min=2, l_bands=3, n_max=19, v_views=6, gamma_d=2.0,
+                             gamma_c=0.15, tau_g=2e-4, tau_s=0.01, eta=1.6, eps=1e-9))
+    views = list(range(6))
+    img, dom = plan.render(PA.to_tensors(g), cams)
+    plan.set_large_threshold(64)
+    try:
+        gres = op.densify_step(PA.to_tensors(g), ini.extent, cams, gt_img, torch.as_tensor(ga, device="cuda"),
+                               torch.as_tensor(den, device="cuda"), cfg, np.random.default_rng(1),
+                               renders=(img, dom), plan=plan)
+    finally:
+        plan.set_large_threshold(96)
+    props = gres.report_arrays["cand_proposals"].cpu().numpy()
+    assert props.max() > 200, props.max()
+    gts_np = {v: gt_img[v].double().cpu().numpy() for v in views}
+    renders_np = {v: (img[v].double().cpu().numpy(), dom[v].long().cpu().numpy()) for v in views}
+    cam_objs = [O.Cam.from_row(r) for r in cams]
+    ores = O.adpsplit_step(g, ini.extent, cam_objs, gts_np, ga, den, cfg, np.random.default_rng(1),
+                           renders=renders_np)
+    st = PA.compare_step(gres, ores, PA.flag_candidates(ores, g, cam_objs, cfg), g)
+    assert st["mismatched"] == 0
