@@ -86,7 +86,7 @@ struct adps_plan {
   unsigned long long* lohi_host = nullptr;
   double* cams_host = nullptr;
   int cams_host_cap = 0;
-  long long region_cap = 0, partial_cap = 0;
+  long long region_cap = 0, partial_cap = 0, region_hint = 0, partial_hint = 0;
   // render scratch
   Buf r_key, r_key_sorted, r_order_in, r_order, r_tiles, r_rect, r_splat, r_offs, r_dup, r_dup_sorted,
       r_tstart, r_tend, r_total, r_cams;
@@ -453,10 +453,15 @@ extern "C" adps_status adps_step_phase1(adps_plan* P, void* stream_v, const adps
   }
   const long long region_bound = total_px / (cfg->m_min > 1 ? cfg->m_min : 1) + 1;
   const long long partial_bound = n_tiles * (2 * kTileW + 2 * kTileH) + 1;
-  if (P->region_cap == 0) P->region_cap = region_bound < (1ll << 21) ? region_bound : (1ll << 21);
-  if (P->partial_cap == 0) P->partial_cap = partial_bound < (1ll << 21) ? partial_bound : (1ll << 21);
-  if (P->region_cap > region_bound) P->region_cap = region_bound;
-  if (P->partial_cap > partial_bound) P->partial_cap = partial_bound;
+  // per-call capacities: the largest seen so far (at least 2^21), never above the analytic bound
+  P->region_hint = P->region_cap > P->region_hint ? P->region_cap : P->region_hint;
+  P->partial_hint = P->partial_cap > P->partial_hint ? P->partial_cap : P->partial_hint;
+  {
+    long long r = P->region_hint > (1ll << 21) ? P->region_hint : (1ll << 21);
+    long long q = P->partial_hint > (1ll << 21) ? P->partial_hint : (1ll << 21);
+    P->region_cap = r < region_bound ? r : region_bound;
+    P->partial_cap = q < partial_bound ? q : partial_bound;
+  }
   CK(ensure(P->regions, sizeof(RegionRec) * P->region_cap));
   CK(ensure(P->partials, sizeof(PartialRec) * P->partial_cap));
   CK(ensure(P->partial_parent, sizeof(int) * P->partial_cap));
@@ -492,18 +497,19 @@ extern "C" adps_status adps_step_phase1(adps_plan* P, void* stream_v, const adps
     CK(cudaMemcpyAsync(P->ctr_host, ctr, sizeof(Counters), cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
     if (!P->ctr_host->overflow) break;
-    if (attempt > 0) return fail(ADPS_BAD_STATE, "region capacity overflow after regrow");
-    if (P->ctr_host->overflow & 1u) {
-      long long want = (long long)P->ctr_host->n_regions + (long long)P->ctr_host->n_partials + 1;
-      P->region_cap = want < region_bound ? want : region_bound;
-      CK(ensure(P->regions, sizeof(RegionRec) * P->region_cap));
+    if (attempt >= 2) return fail(ADPS_BAD_STATE, "region capacity overflow at the analytic bound");
+    // grow: first to what this run needed, then (if still short) to the analytic bounds
+    long long want_r = (long long)P->ctr_host->n_regions + (long long)P->ctr_host->n_partials + 1;
+    long long want_p = (long long)P->ctr_host->n_partials + 1;
+    if (attempt == 1) {
+      want_r = region_bound;
+      want_p = partial_bound;
     }
-    if (P->ctr_host->overflow & 2u) {
-      long long want = (long long)P->ctr_host->n_partials + 1;
-      P->partial_cap = want < partial_bound ? want : partial_bound;
-      CK(ensure(P->partials, sizeof(PartialRec) * P->partial_cap));
-      CK(ensure(P->partial_parent, sizeof(int) * P->partial_cap));
-    }
+    P->region_cap = want_r < region_bound ? (want_r > P->region_cap ? want_r : P->region_cap) : region_bound;
+    P->partial_cap = want_p < partial_bound ? (want_p > P->partial_cap ? want_p : P->partial_cap) : partial_bound;
+    CK(ensure(P->regions, sizeof(RegionRec) * P->region_cap));
+    CK(ensure(P->partials, sizeof(PartialRec) * P->partial_cap));
+    CK(ensure(P->partial_parent, sizeof(int) * P->partial_cap));
   }
   const long long n_regions = (long long)P->ctr_host->n_regions;
   const long long n_split = (long long)P->ctr_host->n_split;
