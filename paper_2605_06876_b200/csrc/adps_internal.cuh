@@ -88,7 +88,8 @@ struct Counters {
   unsigned long long n_inserted;
   unsigned long long n_keep;
   unsigned long long n_large;
-  unsigned long long n_seg;
+  unsigned long long n_small;
+  unsigned long long n_groups_all;
   unsigned int degenerate;
   unsigned int overflow;   // bit0 regions, bit1 partials
 };
@@ -250,11 +251,25 @@ __device__ __forceinline__ int uf_find(volatile int* p, int x) {
   return x;
 }
 
+// find with path halving: only non-root entries are rewritten, always to an
+// ancestor (a smaller index in the same tree), so concurrent atomicMin links
+// on roots are never lost (ECL-CC style benign races).
+__device__ __forceinline__ int uf_find_halve(volatile int* p, int x) {
+  while (true) {
+    const int y = p[x];
+    if (y == x) return x;
+    const int z = p[y];
+    if (z == y) return y;
+    p[x] = z;
+    x = z;
+  }
+}
+
 __device__ __forceinline__ void uf_unite(int* p, int a, int b) {
   volatile int* vp = p;
   while (true) {
-    a = uf_find(vp, a);
-    b = uf_find(vp, b);
+    a = uf_find_halve(vp, a);
+    b = uf_find_halve(vp, b);
     if (a == b) return;
     if (a > b) {
       int t = a;

@@ -184,7 +184,9 @@ __global__ void __launch_bounds__(kTileThreads) tile_kernel(TileParams P) {
     }
     __syncthreads();
   }
-  // 3. keys + ever-dominant flags
+  // 3. keys + ever-dominant flags; each warp owns whole 32-px rows (lane = x),
+  //    so horizontal runs of equal key are found with ballots and every pixel
+  //    starts labelled with its run's first pixel (short union-find paths).
   for (int p = tid; p < kTilePx; p += kTileThreads) {
     int tx = p % kTileW, ty = p / kTileW;
     int x = x0 + tx, y = y0 + ty;
@@ -209,31 +211,38 @@ __global__ void __launch_bounds__(kTileThreads) tile_kernel(TileParams P) {
         P.dbg_b[q] = S.band[p];
       }
     }
+    const int band = S.band[p];
+    const unsigned keyed_m = __ballot_sync(0xffffffffu, key >= 0);
+    const int lkey = __shfl_up_sync(0xffffffffu, key, 1);
+    const int lband = __shfl_up_sync(0xffffffffu, band, 1);
+    const unsigned cont_m = __ballot_sync(0xffffffffu, key >= 0 && tx > 0 && lkey == key && lband == band);
+    const unsigned starts = keyed_m & ~cont_m;
+    const int run0 = 31 - __clz(starts & (0xffffffffu >> (31 - tx)));
     S.d[p] = key;
-    S.label[p] = key >= 0 ? p : -1;
+    S.label[p] = key >= 0 ? ty * kTileW + run0 : -1;
     S.touch[p] = 0;
 #pragma unroll
     for (int k = 0; k < 6; ++k) S.mom[k][p] = 0;
   }
   __syncthreads();
-  // 4. unions with W, NW, N, NE neighbours of equal (candidate, band)
+  // 4. unions with the row above (NW, N, NE) of equal (candidate, band); W is the run
   for (int p = tid; p < kTilePx; p += kTileThreads) {
     int key = S.d[p];
-    if (key < 0) continue;
-    int tx = p % kTileW, ty = p / kTileW;
+    int ty = p / kTileW;
+    if (key < 0 || ty == 0) continue;
+    int tx = p % kTileW;
     unsigned char b = S.band[p];
-    const int nx[4] = {-1, -1, 0, 1}, ny[4] = {0, -1, -1, -1};
 #pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      int qx = tx + nx[k], qy = ty + ny[k];
-      if (qx < 0 || qx >= kTileW || qy < 0) continue;
-      int q = qy * kTileW + qx;
+    for (int dx = -1; dx <= 1; ++dx) {
+      int qx = tx + dx;
+      if (qx < 0 || qx >= kTileW) continue;
+      int q = p - kTileW + dx;
       if (S.d[q] == key && S.band[q] == b) uf_unite(S.label, p, q);
     }
   }
   __syncthreads();
   for (int p = tid; p < kTilePx; p += kTileThreads)
-    if (S.d[p] >= 0) S.label[p] = uf_find(S.label, p);
+    if (S.d[p] >= 0) S.label[p] = uf_find_halve(S.label, p);
   __syncthreads();
   // 5. warp-aggregated integer moments (tile-local coordinates, exact)
   const bool left_in = x0 > 0, top_in = y0 > 0;

@@ -1,0 +1,372 @@
+// Cross-view merge, cap and per-candidate case for all split candidates.
+//
+//   mergeable / merge_groups   ref/cross_view_merge.py:33-41, 72-107
+//   merge_params               ref/cross_view_merge.py:44-69
+//   cap_children + extent      ref/cross_view_merge.py:26-30, 110-116
+//   _group_to_gaussian         ref/adc.py:127-140
+//   case branch order          ref/adc.py:198-227
+//
+// Flat, skew-proof structure (one parent may own tens of thousands of
+// proposals, e.g. a background Gaussian):
+//   prepare   gather valid proposals in reference order (scan), case per parent
+//   gates     warp per parent for P <= small_max, 64x64 tiles over the whole
+//             GPU for larger parents; links by atomicMin union-find, so the
+//             components (roots = smallest index) do not depend on order
+//   groups    stable sort by root -> contiguous member lists in ascending
+//             index order; one warp per group reduces mean, eigenbasis, reach
+//   cap       stable sorts by (-extent) then parent -> rank within parent;
+//             the first n_max become children in cap order
+#include <math.h>
+
+#include "merge.cuh"
+
+namespace adps {
+
+__device__ __forceinline__ bool gate(const Proposal& A, const Proposal& B, double gd, double gc) {
+  // sqrt(d^T Sa^-1 d) + sqrt(d^T Sb^-1 d) <= gamma_d and max|drgb| <= gamma_c, inclusive
+  const double dl[3] = {B.mu[0] - A.mu[0], B.mu[1] - A.mu[1], B.mu[2] - A.mu[2]};
+  const double d = sqrt(fmax(sym_quad(A.prec, dl), 0.0)) + sqrt(fmax(sym_quad(B.prec, dl), 0.0));
+  const double dc = fmax(fmax(fabs(A.rgb[0] - B.rgb[0]), fabs(A.rgb[1] - B.rgb[1])), fabs(A.rgb[2] - B.rgb[2]));
+  return d <= gd && dc <= gc;
+}
+
+// group -> Gaussian: eigh(merged_cov) ascending, det fix on column 0,
+// scale = sqrt(max(lambda, 1e-16)), clamped parent opacity, rgb_to_dc.
+// out: 14 floats mu3 scale3 rot4 opacity sh_dc3.
+__device__ void write_child(const GroupRec& G, float ocl, float* out) {
+  int o[3] = {0, 1, 2};
+  for (int i = 0; i < 3; ++i)
+    for (int j = i + 1; j < 3; ++j)
+      if (G.lam[o[j]] < G.lam[o[i]]) {
+        int t = o[i];
+        o[i] = o[j];
+        o[j] = t;
+      }
+  double ev[9], lam[3];
+  for (int c = 0; c < 3; ++c) {
+    lam[c] = G.lam[o[c]];
+    for (int r = 0; r < 3; ++r) ev[r * 3 + c] = G.evec[r * 3 + o[c]];
+  }
+  const double det = ev[0] * (ev[4] * ev[8] - ev[5] * ev[7]) - ev[1] * (ev[3] * ev[8] - ev[5] * ev[6]) +
+                     ev[2] * (ev[3] * ev[7] - ev[4] * ev[6]);
+  if (det < 0)
+    for (int r = 0; r < 3; ++r) ev[r * 3 + 0] = -ev[r * 3 + 0];
+  double qq[4];
+  rot_to_quat(ev, qq);
+  for (int t = 0; t < 3; ++t) out[t] = (float)G.mu[t];
+  for (int t = 0; t < 3; ++t) out[3 + t] = (float)sqrt(fmax(lam[t], 1e-16));
+  for (int t = 0; t < 4; ++t) out[6 + t] = (float)qq[t];
+  out[10] = ocl;
+  for (int t = 0; t < 3; ++t) out[11 + t] = (float)((G.rgb[t] - 0.5) / kShC0);
+}
+
+// ------------------------------------------------------------------ prepare
+struct GatherPolicy {
+  MergeArgs a;
+  __device__ unsigned long long value(long long p) const { return a.valid[a.vals_sorted[p]] ? 1ull : 0ull; }
+  __device__ void store(long long p, unsigned long long ex, unsigned long long v) const {
+    const int rank = (int)(a.keys_sorted[p] >> a.shift_rank);
+    if (p == 0 || (int)(a.keys_sorted[p - 1] >> a.shift_rank) != rank) a.pstart[rank] = (int)ex;
+    if (v) {
+      a.props_s[ex] = a.props[a.vals_sorted[p]];
+      a.pcand[ex] = rank;
+      a.uf[ex] = (int)ex;
+    }
+  }
+  __device__ void total(unsigned long long t) const { a.ctr->n_proposals = t; }
+};
+
+__global__ void case_kernel(MergeArgs a) {
+  const long long n_split = (long long)a.ctr->n_split;
+  for (long long k = (long long)blockIdx.x * blockDim.x + threadIdx.x; k < n_split;
+       k += (long long)gridDim.x * blockDim.x) {
+    const int gi = a.split_list[k];
+    const int P = a.cand_nvalid[k];
+    a.cand_props[k] = P;
+    a.n_groups[k] = 0;
+    a.cand_merged[k] = 0;
+    if (!a.dom_flag[gi]) {            // never dominant in the sampled views: vanilla fallback
+      a.cand_case[k] = ADPS_CASE_FALLBACK;
+      a.cand_ins[k] = 2;
+      atomicAdd(&a.ctr->n_fallback, 1ull);
+    } else if (P == 0) {              // dominant, no usable proposal: keep + reset
+      a.cand_case[k] = ADPS_CASE_RESET;
+      a.cand_ins[k] = 0;
+      atomicAdd(&a.ctr->n_reset, 1ull);
+    } else {
+      a.cand_case[k] = ADPS_CASE_SPLIT;
+      if (P >= 2 && P <= a.small_max) {
+        a.small_list[atomicAdd(&a.ctr->n_small, 1ull)] = (int)k;
+      } else if (P > a.small_max) {
+        const unsigned long long l = atomicAdd(&a.ctr->n_large, 1ull);
+        a.large_list[l] = (int)k;
+        const long long T = (P + 63) / 64;
+        a.work_cnt[l] = (unsigned long long)(T * (T + 1) / 2);
+      }
+    }
+  }
+}
+
+cudaError_t launch_merge_prepare(const MergeArgs& a, long long n_split, ScanState st, cudaStream_t s) {
+  cudaError_t e = launch_scan(GatherPolicy{a}, a.n_regions, st, s);
+  if (e != cudaSuccess) return e;
+  long long b = (n_split + 255) / 256;
+  case_kernel<<<(unsigned)(b < 1 ? 1 : (b > 4096 ? 4096 : b)), 256, 0, s>>>(a);
+  return cudaGetLastError();
+}
+
+// -------------------------------------------------------------------- gates
+__global__ void small_pairs_kernel(MergeArgs a) {
+  const int lane = threadIdx.x & 31;
+  const long long warps = (long long)gridDim.x * (blockDim.x >> 5);
+  const long long n_small = (long long)a.ctr->n_small;
+  for (long long t = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); t < n_small; t += warps) {
+    const int k = a.small_list[t];
+    const int P = a.cand_nvalid[k];
+    const int ps = a.pstart[k];
+    const Proposal* pr = a.props_s + ps;
+    for (int i = 0; i < P - 1; ++i) {
+      const Proposal& A = pr[i];
+      for (int j = i + 1 + lane; j < P; j += 32)
+        if (gate(A, pr[j], a.gamma_d, a.gamma_c)) uf_unite(a.uf, ps + i, ps + j);
+    }
+  }
+}
+
+__global__ void __launch_bounds__(1024) offsets_1block_kernel(const unsigned long long* __restrict__ in,
+                                                              unsigned long long* __restrict__ out,
+                                                              const unsigned long long* __restrict__ n_dev) {
+  __shared__ unsigned long long warp_tot[32];
+  __shared__ unsigned long long carry;
+  const long long n = (long long)*n_dev;
+  if (threadIdx.x == 0) carry = 0;
+  __syncthreads();
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  for (long long base = 0; base < n; base += blockDim.x) {
+    const long long i = base + threadIdx.x;
+    const unsigned long long v = i < n ? in[i] : 0ull;
+    unsigned long long x = v;
+    for (int o = 1; o < 32; o <<= 1) {
+      unsigned long long y = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x += y;
+    }
+    if (lane == 31) warp_tot[wid] = x;
+    __syncthreads();
+    if (wid == 0) {
+      unsigned long long w = warp_tot[lane];
+      unsigned long long wi = w;
+      for (int o = 1; o < 32; o <<= 1) {
+        unsigned long long y = __shfl_up_sync(0xffffffffu, wi, o);
+        if (lane >= o) wi += y;
+      }
+      warp_tot[lane] = wi - w;
+    }
+    __syncthreads();
+    const unsigned long long excl = carry + warp_tot[wid] + x - v;
+    if (i < n) out[i] = excl;
+    __syncthreads();
+    if (threadIdx.x == blockDim.x - 1) carry = excl + v;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) out[n] = carry;
+}
+
+// 64x64 tiles of the upper-triangular gate matrix of every large parent,
+// spread over the whole grid (work item -> (parent, tile row, tile column)).
+__global__ void __launch_bounds__(256) pair_tiles_kernel(MergeArgs a) {
+  __shared__ Proposal si[64], sj[64];
+  const long long n_large = (long long)a.ctr->n_large;
+  const unsigned long long W = a.work_off[n_large];
+  for (unsigned long long w = blockIdx.x; w < W; w += gridDim.x) {
+    long long lo = 0, hi = n_large - 1;
+    while (lo < hi) {
+      const long long mid = (lo + hi + 1) / 2;
+      if (a.work_off[mid] <= w) lo = mid;
+      else hi = mid - 1;
+    }
+    const int k = a.large_list[lo];
+    const int P = a.cand_nvalid[k];
+    const int ps = a.pstart[k];
+    const long long T = (P + 63) / 64;
+    const long long q = (long long)(w - a.work_off[lo]);
+    long long bi = (long long)floor(((2.0 * T + 1.0) - sqrt((2.0 * T + 1.0) * (2.0 * T + 1.0) - 8.0 * q)) / 2.0);
+    if (bi < 0) bi = 0;
+    while (bi > 0 && bi * T - bi * (bi - 1) / 2 > q) --bi;
+    while ((bi + 1) * T - (bi + 1) * bi / 2 <= q) ++bi;
+    const long long bj = bi + (q - (bi * T - bi * (bi - 1) / 2));
+    const int i0 = (int)(bi * 64), j0 = (int)(bj * 64);
+    for (int t = threadIdx.x; t < 128; t += blockDim.x) {
+      const int loc = t & 63;
+      const int src = (t < 64 ? i0 : j0) + loc;
+      if (src < P) (t < 64 ? si : sj)[loc] = a.props_s[ps + src];
+    }
+    __syncthreads();
+    for (int t = threadIdx.x; t < 64 * 64; t += blockDim.x) {
+      const int ii = t >> 6, jj = t & 63;
+      const int i = i0 + ii, j = j0 + jj;
+      if (i < j && j < P && gate(si[ii], sj[jj], a.gamma_d, a.gamma_c)) uf_unite(a.uf, ps + i, ps + j);
+    }
+    __syncthreads();
+  }
+}
+
+cudaError_t launch_merge_gates(const MergeArgs& a, cudaStream_t s) {
+  small_pairs_kernel<<<a.grid, 256, 0, s>>>(a);
+  offsets_1block_kernel<<<1, 1024, 0, s>>>(a.work_cnt, a.work_off, &a.ctr->n_large);
+  pair_tiles_kernel<<<a.grid, 256, 0, s>>>(a);
+  return cudaGetLastError();
+}
+
+// ----------------------------------------------------------------- flatten
+__global__ void flatten_kernel(MergeArgs a, long long cap) {
+  const long long np = (long long)a.ctr->n_proposals;
+  for (long long q = (long long)blockIdx.x * blockDim.x + threadIdx.x; q < cap;
+       q += (long long)gridDim.x * blockDim.x) {
+    a.gkey[q] = q < np ? (unsigned)uf_find_halve(a.uf, (int)q) : 0xffffffffu;
+    a.gval[q] = (int)q;
+  }
+}
+
+cudaError_t launch_merge_flatten(const MergeArgs& a, long long cap, cudaStream_t s) {
+  long long b = (cap + 255) / 256;
+  flatten_kernel<<<(unsigned)(b < 1 ? 1 : (b > 65535 ? 65535 : b)), 256, 0, s>>>(a, cap);
+  return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------ groups
+struct GroupStartPolicy {
+  MergeArgs a;
+  __device__ unsigned long long value(long long s) const {
+    const unsigned k = a.gkey_sorted[s];
+    return (k != 0xffffffffu && (s == 0 || a.gkey_sorted[s - 1] != k)) ? 1ull : 0ull;
+  }
+  __device__ void store(long long s, unsigned long long ex, unsigned long long v) const {
+    if (v) a.grp_first[ex] = (int)s;
+  }
+  __device__ void total(unsigned long long t) const {
+    a.ctr->n_groups_all = t;
+    a.grp_first[t] = (int)a.ctr->n_proposals;
+  }
+};
+
+// one warp per group: member means, mean-covariance eigenbasis, reach
+__global__ void group_kernel(MergeArgs a, long long cap) {
+  const int lane = threadIdx.x & 31;
+  const long long warps = (long long)gridDim.x * (blockDim.x >> 5);
+  const long long G = (long long)a.ctr->n_groups_all;
+  for (long long g = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); g < cap; g += warps) {
+    if (g >= G) {
+      if (lane == 0) {
+        a.ext_key[g] = ~0ull;
+        a.ext_val[g] = (int)g;
+      }
+      continue;
+    }
+    const int b = a.grp_first[g], e = a.grp_first[g + 1];
+    const int cnt = e - b;
+    double acc[12] = {0};
+    for (int m = b + lane; m < e; m += 32) {
+      const Proposal& M = a.props_s[a.gval_sorted[m]];
+      for (int t = 0; t < 3; ++t) {
+        acc[t] += M.mu[t];
+        acc[3 + t] += M.rgb[t];
+      }
+      for (int t = 0; t < 6; ++t) acc[6 + t] += M.cov[t];
+    }
+    // butterfly: every lane ends with the identical (commutative) sums
+    for (int t = 0; t < 12; ++t)
+      for (int o = 16; o > 0; o >>= 1) acc[t] += __shfl_xor_sync(0xffffffffu, acc[t], o);
+    GroupRec R;
+    for (int t = 0; t < 3; ++t) {
+      R.mu[t] = acc[t] / cnt;
+      R.rgb[t] = acc[3 + t] / cnt;
+    }
+    double mcov[6];
+    for (int t = 0; t < 6; ++t) mcov[t] = acc[6 + t] / cnt;
+    double lam0[3];
+    sym_eig3(mcov, lam0, R.evec);
+    double ext = 0.0;
+    for (int r = 0; r < 3; ++r) {
+      const double ev[3] = {R.evec[r], R.evec[3 + r], R.evec[6 + r]};
+      double best = 0.0;
+      for (int m = b + lane; m < e; m += 32) {
+        const Proposal& M = a.props_s[a.gval_sorted[m]];
+        const double off = fabs((M.mu[0] - R.mu[0]) * ev[0] + (M.mu[1] - R.mu[1]) * ev[1] +
+                                (M.mu[2] - R.mu[2]) * ev[2]);
+        best = fmax(best, off + sqrt(sym_quad(M.cov, ev)));
+      }
+      for (int o = 16; o > 0; o >>= 1) best = fmax(best, __shfl_xor_sync(0xffffffffu, best, o));
+      R.lam[r] = best * best;
+      ext = fmax(ext, R.lam[r]);
+    }
+    R.extent = ext;
+    if (lane == 0) {
+      a.groups[g] = R;
+      a.ext_key[g] = ~(unsigned long long)__double_as_longlong(ext);   // descending extent
+      a.ext_val[g] = (int)g;
+      atomicAdd(&a.n_groups[a.pcand[a.gkey_sorted[b]]], 1);
+    }
+  }
+}
+
+cudaError_t launch_merge_groups(const MergeArgs& a, long long cap, ScanState st, cudaStream_t s) {
+  cudaError_t e = launch_scan(GroupStartPolicy{a}, cap, st, s);
+  if (e != cudaSuccess) return e;
+  group_kernel<<<a.grid, 256, 0, s>>>(a, cap);
+  return cudaGetLastError();
+}
+
+// --------------------------------------------------------------------- cap
+__global__ void cand_key_kernel(MergeArgs a, long long cap) {
+  const long long G = (long long)a.ctr->n_groups_all;
+  for (long long s = (long long)blockIdx.x * blockDim.x + threadIdx.x; s < cap;
+       s += (long long)gridDim.x * blockDim.x) {
+    const int gid = a.ext_val_sorted[s];
+    a.cand_val[s] = gid;
+    a.cand_key[s] = gid < G ? (unsigned)a.pcand[a.gkey_sorted[a.grp_first[gid]]] : 0xffffffffu;
+  }
+}
+
+// position s of the (parent, -extent, root)-ordered group list -> child rank s - first
+__global__ void cap_emit_kernel(MergeArgs a) {
+  const long long G = (long long)a.ctr->n_groups_all;
+  for (long long s = (long long)blockIdx.x * blockDim.x + threadIdx.x; s < G;
+       s += (long long)gridDim.x * blockDim.x) {
+    const unsigned k = a.cand_key_sorted[s];
+    // first position of this parent: groups of a parent are contiguous and
+    // number n_groups[k]; walk back at most n_max steps to find the rank
+    long long first = s;
+    int steps = 0;
+    while (first > 0 && a.cand_key_sorted[first - 1] == k && steps <= a.n_max) {
+      --first;
+      ++steps;
+    }
+    const long long rank = s - first;
+    if (rank >= a.n_max) continue;
+    const int gi = a.split_list[k];
+    const float ocl = (float)fmin(fmax((double)a.opacity[gi], 1e-6), 1.0 - 1e-6);
+    write_child(a.groups[a.cand_val_sorted[s]], ocl, a.children + 14ll * (a.pstart[k] + rank));
+    if (rank == 0) {
+      const int Gk = a.n_groups[k];
+      const int ni = Gk < a.n_max ? Gk : a.n_max;
+      a.cand_merged[k] = ni;
+      a.cand_ins[k] = ni + 1;
+      atomicAdd(&a.ctr->merge_edges, (unsigned long long)(a.cand_nvalid[k] - Gk));
+      atomicAdd(&a.ctr->n_children, (unsigned long long)ni);
+    }
+  }
+}
+
+cudaError_t launch_merge_cap(const MergeArgs& a, long long cap, cudaStream_t s) {
+  long long b = (cap + 255) / 256;
+  cand_key_kernel<<<(unsigned)(b < 1 ? 1 : (b > 65535 ? 65535 : b)), 256, 0, s>>>(a, cap);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_merge_emit(const MergeArgs& a, long long cap, cudaStream_t s) {
+  long long b = (cap + 255) / 256;
+  cap_emit_kernel<<<(unsigned)(b < 1 ? 1 : (b > 65535 ? 65535 : b)), 256, 0, s>>>(a);
+  return cudaGetLastError();
+}
+
+}  // namespace adps

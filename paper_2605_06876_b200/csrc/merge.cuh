@@ -1,0 +1,71 @@
+#pragma once
+
+#include "adps_internal.cuh"
+#include "scan.cuh"
+
+namespace adps {
+
+// Cross-view merge + cap over all split candidates at once
+// (ref/cross_view_merge.py:33-116, ref/adc.py:184-227).
+//
+// Proposal space: valid proposals (t* > 0) gathered in reference order
+// (candidate, view, band, first pixel); candidate k owns [pstart[k], +P_k).
+struct MergeArgs {
+  // inputs
+  const unsigned long long* keys_sorted;   // region sort keys
+  const int* vals_sorted;                  // sorted pos -> region id
+  long long n_regions;
+  int shift_rank;
+  const unsigned char* valid;              // region id -> t* > 0
+  const Proposal* props;                   // region id -> proposal
+  const int* split_list;
+  const int* cand_start;                   // first sorted region position of a candidate
+  const int* cand_nvalid;                  // P_k
+  const unsigned char* dom_flag;
+  const float* opacity;
+  double gamma_d, gamma_c;
+  int n_max;
+  int small_max;                           // P <= small_max: warp path for the gates
+  // proposal space
+  Proposal* props_s;                       // [cap]
+  int* pcand;                              // [cap] candidate rank
+  int* uf;                                 // [cap]
+  unsigned* gkey;                          // [cap] root (group key), padding UINT_MAX
+  int* gval;                               // [cap] proposal q
+  unsigned* gkey_sorted;
+  int* gval_sorted;
+  // groups
+  int* grp_first;                          // [cap] first sorted position of group g
+  GroupRec* groups;                        // [cap]
+  unsigned long long* ext_key;             // [cap] ~extent bits (descending), padding ~0
+  int* ext_val;                            // [cap] group id
+  unsigned long long* ext_key_sorted;
+  int* ext_val_sorted;
+  unsigned* cand_key;                      // [cap] candidate rank of group, padding UINT_MAX
+  int* cand_val;                           // [cap] group id (in extent order)
+  unsigned* cand_key_sorted;
+  int* cand_val_sorted;
+  // per candidate
+  int* pstart;                             // [n_split]
+  int* n_groups;                           // [n_split]
+  int* cand_case;
+  int* cand_props;
+  int* cand_merged;
+  int* cand_ins;
+  int* small_list;                         // [n_split]
+  int* large_list;                         // [n_split]
+  unsigned long long* work_cnt;            // [n_split]
+  unsigned long long* work_off;            // [n_split + 1]
+  float* children;                         // [cap,14]
+  Counters* ctr;
+  unsigned grid;
+};
+
+cudaError_t launch_merge_prepare(const MergeArgs& a, long long n_split, ScanState st, cudaStream_t s);
+cudaError_t launch_merge_gates(const MergeArgs& a, cudaStream_t s);
+cudaError_t launch_merge_flatten(const MergeArgs& a, long long cap, cudaStream_t s);
+cudaError_t launch_merge_groups(const MergeArgs& a, long long cap, ScanState st, cudaStream_t s);
+cudaError_t launch_merge_cap(const MergeArgs& a, long long cap, cudaStream_t s);
+cudaError_t launch_merge_emit(const MergeArgs& a, long long cap, cudaStream_t s);
+
+}  // namespace adps

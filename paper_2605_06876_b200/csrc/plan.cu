@@ -11,6 +11,7 @@
 
 #include "adps_internal.cuh"
 #include "attribution.cuh"
+#include "merge.cuh"
 #include "render.cuh"
 #include "split.cuh"
 
@@ -78,8 +79,10 @@ struct adps_plan {
   // tiles / fragments / regions
   Buf border, partials, partial_parent, regions, props, valid, keys, vals, keys_sorted, vals_sorted;
   Buf idx, uf, groups, children, dbg_stats, dbg_child;
-  Buf l_keys, l_vals, l_keys_sorted, l_vals_sorted, l_seg_begin, l_seg_end, l_seg_list, l_work_cnt, l_work_off,
-      l_n_groups, l_rank_of;
+  // merge / cap scratch (proposal space)
+  Buf small_list, pstart, n_groups, work_cnt, work_off, props_s, pcand, gkey, gval, gkey_sorted, gval_sorted,
+      grp_first, ext_key, ext_val, ext_key_sorted, ext_val_sorted, cand_key, cand_val, cand_key_sorted,
+      cand_val_sorted, scan3_val, scan3_flag, scan3_ticket;
   Buf scan_val, scan_flag, scan_ticket, scan2_val, scan2_flag, scan2_ticket, cub_tmp;
   Buf ctr;
   Counters* ctr_host = nullptr;
@@ -128,6 +131,21 @@ static void mark_cb(void* ctx, const char* name, cudaStream_t s, int kernels) {
 static void mark_start(adps_plan* P, cudaStream_t s, bool reset) {
   if (reset) P->n_marks = 0;
   mark(P, "start", s, 0);
+}
+
+// stable CUB radix sort of (key, value) pairs over [0, end_bit), temp storage owned by the plan
+template <class K, class V>
+static cudaError_t cub_sort_pairs(adps_plan* P, const K* kin, K* kout, const V* vin, V* vout, long long n,
+                                  int end_bit, cudaStream_t s) {
+  if (n <= 0) return cudaSuccess;
+  size_t tb = 0;
+  cudaError_t e = cub::DeviceRadixSort::SortPairs(nullptr, tb, kin, kout, vin, vout, (int)n, 0, end_bit, s);
+  if (e != cudaSuccess) return e;
+  e = ensure(P->cub_tmp, tb);
+  if (e != cudaSuccess) return e;
+  tb = P->cub_tmp.bytes;
+  P->lib_calls += 1;
+  return cub::DeviceRadixSort::SortPairs(P->cub_tmp.p, tb, kin, kout, vin, vout, (int)n, 0, end_bit, s);
 }
 
 static adps_status scan_state(adps_plan* P, Buf& val, Buf& flag, Buf& ticket, long long n, ScanState* st) {
@@ -186,8 +204,10 @@ extern "C" adps_status adps_plan_destroy(adps_plan* P) {
                  &P->scan2_val, &P->scan2_flag, &P->scan2_ticket, &P->cub_tmp, &P->ctr, &P->r_key,
                  &P->r_key_sorted, &P->r_order_in, &P->r_order, &P->r_tiles, &P->r_rect, &P->r_splat,
                  &P->r_offs, &P->r_dup, &P->r_dup_sorted, &P->r_tstart, &P->r_tend, &P->r_total,
-                 &P->r_cams, &P->l_keys, &P->l_vals, &P->l_keys_sorted, &P->l_vals_sorted, &P->l_seg_begin,
-                 &P->l_seg_end, &P->l_seg_list, &P->l_work_cnt, &P->l_work_off, &P->l_n_groups, &P->l_rank_of};
+                 &P->r_cams, &P->small_list, &P->pstart, &P->n_groups, &P->work_cnt, &P->work_off,
+                 &P->props_s, &P->pcand, &P->gkey, &P->gval, &P->gkey_sorted, &P->gval_sorted, &P->grp_first,
+                 &P->ext_key, &P->ext_val, &P->ext_key_sorted, &P->ext_val_sorted, &P->cand_key, &P->cand_val,
+                 &P->cand_key_sorted, &P->cand_val_sorted, &P->scan3_val, &P->scan3_flag, &P->scan3_ticket};
   for (Buf* b : bufs)
     if (b->p) cudaFree(b->p);
   if (P->ctr_host) cudaFreeHost(P->ctr_host);
@@ -587,17 +607,26 @@ extern "C" adps_status adps_step_phase1(adps_plan* P, void* stream_v, const adps
   CK(ensure(P->ins_off, 4 * sc));
   CK(ensure(P->fb_ord, 4 * sc));
   CK(ensure(P->large_list, 4 * sc));
-  CK(ensure(P->l_work_cnt, 8 * sc));
-  CK(ensure(P->l_work_off, 8 * (sc + 1)));
-  CK(ensure(P->l_n_groups, 4 * sc));
-  CK(ensure(P->l_keys, 8 * rc));
-  CK(ensure(P->l_vals, 4 * rc));
-  CK(ensure(P->l_keys_sorted, 8 * rc));
-  CK(ensure(P->l_vals_sorted, 4 * rc));
-  CK(ensure(P->l_seg_begin, 4 * rc));
-  CK(ensure(P->l_seg_end, 4 * rc));
-  CK(ensure(P->l_seg_list, 8 * rc));
-  CK(ensure(P->l_rank_of, 4 * rc));
+  CK(ensure(P->small_list, 4 * sc));
+  CK(ensure(P->pstart, 4 * sc));
+  CK(ensure(P->n_groups, 4 * sc));
+  CK(ensure(P->work_cnt, 8 * sc));
+  CK(ensure(P->work_off, 8 * (sc + 1)));
+  CK(ensure(P->props_s, sizeof(Proposal) * rc));
+  CK(ensure(P->pcand, 4 * rc));
+  CK(ensure(P->gkey, 4 * rc));
+  CK(ensure(P->gval, 4 * rc));
+  CK(ensure(P->gkey_sorted, 4 * rc));
+  CK(ensure(P->gval_sorted, 4 * rc));
+  CK(ensure(P->grp_first, 4 * (rc + 1)));
+  CK(ensure(P->ext_key, 8 * rc));
+  CK(ensure(P->ext_val, 4 * rc));
+  CK(ensure(P->ext_key_sorted, 8 * rc));
+  CK(ensure(P->ext_val_sorted, 4 * rc));
+  CK(ensure(P->cand_key, 4 * rc));
+  CK(ensure(P->cand_val, 4 * rc));
+  CK(ensure(P->cand_key_sorted, 4 * rc));
+  CK(ensure(P->cand_val_sorted, 4 * rc));
   CK(ensure(P->regions_per_view, 4 * sc * V));
   CK(cudaMemsetAsync(P->cand_start.p, 0, 4 * sc, s));
   CK(cudaMemsetAsync(P->cand_end.p, 0, 4 * sc, s));
@@ -624,64 +653,72 @@ extern "C" adps_status adps_step_phase1(adps_plan* P, void* stream_v, const adps
 
   // ---- per-candidate case, merge, cap (ref/adc.py:184-227)
   MergeArgs ma;
-  ma.split_list = P->split_list.as<int>();
-  ma.cand_start = P->cand_start.as<int>();
-  ma.cand_end = P->cand_end.as<int>();
-  ma.cand_nvalid = P->cand_nvalid.as<int>();
+  ma.keys_sorted = P->keys_sorted.as<unsigned long long>();
   ma.vals_sorted = P->vals_sorted.as<int>();
+  ma.n_regions = n_regions;
+  ma.shift_rank = bits_v + bits_b + bits_p;
   ma.valid = P->valid.as<unsigned char>();
   ma.props = P->props.as<Proposal>();
+  ma.split_list = P->split_list.as<int>();
+  ma.cand_start = P->cand_start.as<int>();
+  ma.cand_nvalid = P->cand_nvalid.as<int>();
   ma.dom_flag = P->dom_flag.as<unsigned char>();
   ma.opacity = g->opacity;
   ma.gamma_d = cfg->gamma_d;
   ma.gamma_c = cfg->gamma_c;
   ma.n_max = cfg->n_max;
-  ma.large_threshold = P->large_threshold;
-  ma.idx = P->idx.as<int>();
+  ma.small_max = P->large_threshold;
+  ma.props_s = P->props_s.as<Proposal>();
+  ma.pcand = P->pcand.as<int>();
   ma.uf = P->uf.as<int>();
+  ma.gkey = P->gkey.as<unsigned>();
+  ma.gval = P->gval.as<int>();
+  ma.gkey_sorted = P->gkey_sorted.as<unsigned>();
+  ma.gval_sorted = P->gval_sorted.as<int>();
+  ma.grp_first = P->grp_first.as<int>();
   ma.groups = P->groups.as<GroupRec>();
-  ma.children = P->children.as<float>();
+  ma.ext_key = P->ext_key.as<unsigned long long>();
+  ma.ext_val = P->ext_val.as<int>();
+  ma.ext_key_sorted = P->ext_key_sorted.as<unsigned long long>();
+  ma.ext_val_sorted = P->ext_val_sorted.as<int>();
+  ma.cand_key = P->cand_key.as<unsigned>();
+  ma.cand_val = P->cand_val.as<int>();
+  ma.cand_key_sorted = P->cand_key_sorted.as<unsigned>();
+  ma.cand_val_sorted = P->cand_val_sorted.as<int>();
+  ma.pstart = P->pstart.as<int>();
+  ma.n_groups = P->n_groups.as<int>();
   ma.cand_case = P->cand_case.as<int>();
   ma.cand_props = P->cand_props.as<int>();
   ma.cand_merged = P->cand_merged.as<int>();
   ma.cand_ins = P->cand_ins.as<int>();
+  ma.small_list = P->small_list.as<int>();
   ma.large_list = P->large_list.as<int>();
+  ma.work_cnt = P->work_cnt.as<unsigned long long>();
+  ma.work_off = P->work_off.as<unsigned long long>();
+  ma.children = P->children.as<float>();
   ma.ctr = ctr;
-  long long mgrid = (n_split + 7) / 8;
-  ma.grid = (unsigned)(mgrid < 1 ? 1 : (mgrid > (long long)P->sm_count * 16 ? P->sm_count * 16 : mgrid));
+  ma.grid = (unsigned)(P->sm_count * 8);
   if (n_split > 0) {
-    CK(launch_merge_small(ma, s));
-    mark(P, "merge_small", s, 1);
-    LargeArgs L;
-    L.keys = P->l_keys.as<unsigned long long>();
-    L.vals = P->l_vals.as<int>();
-    L.keys_sorted = P->l_keys_sorted.as<unsigned long long>();
-    L.vals_sorted = P->l_vals_sorted.as<int>();
-    L.seg_begin = P->l_seg_begin.as<int>();
-    L.seg_end = P->l_seg_end.as<int>();
-    L.seg_list = P->l_seg_list.as<long long>();
-    L.n_seg = &ctr->n_seg;
-    L.work_cnt = P->l_work_cnt.as<unsigned long long>();
-    L.work_off = P->l_work_off.as<unsigned long long>();
-    L.n_groups = P->l_n_groups.as<int>();
-    L.rank_of = P->l_rank_of.as<int>();
-    const unsigned lgrid = (unsigned)(P->sm_count * 8);
-    CK(cudaMemsetAsync(L.keys, 0xff, 8 * rc, s));
-    CK(launch_merge_large_gates(ma, L, lgrid, s));
-    mark(P, "merge_large_gates", s, 5);
+    ScanState sst3;
+    st = scan_state(P, P->scan3_val, P->scan3_flag, P->scan3_ticket, rc, &sst3);
+    if (st != ADPS_OK) return st;
+    CK(launch_merge_prepare(ma, n_split, sst3, s));
+    mark(P, "merge_prepare", s, 2);
+    CK(launch_merge_gates(ma, s));
+    mark(P, "merge_gates", s, 3);
     if (n_regions > 0) {
-      const int lbits = 32 + ceil_log2((unsigned long long)(n_split + 1));
-      size_t tb = 0;
-      CK(cub::DeviceRadixSort::SortPairs(nullptr, tb, L.keys, L.keys_sorted, L.vals, L.vals_sorted,
-                                         (int)n_regions, 0, lbits, s));
-      CK(ensure(P->cub_tmp, tb));
-      tb = P->cub_tmp.bytes;
-      CK(cub::DeviceRadixSort::SortPairs(P->cub_tmp.p, tb, L.keys, L.keys_sorted, L.vals, L.vals_sorted,
-                                         (int)n_regions, 0, lbits, s));
-      P->lib_calls += 1;
+      CK(launch_merge_flatten(ma, rc, s));
+      const int gbits = ceil_log2((unsigned long long)rc + 2);
+      CK(cub_sort_pairs(P, ma.gkey, ma.gkey_sorted, ma.gval, ma.gval_sorted, rc, gbits, s));
+      CK(launch_merge_groups(ma, rc, sst3, s));
+      mark(P, "merge_groups", s, 3);
+      CK(cub_sort_pairs(P, ma.ext_key, ma.ext_key_sorted, ma.ext_val, ma.ext_val_sorted, rc, 64, s));
+      CK(launch_merge_cap(ma, rc, s));
+      const int cbits = ceil_log2((unsigned long long)n_split + 2);
+      CK(cub_sort_pairs(P, ma.cand_key, ma.cand_key_sorted, ma.cand_val, ma.cand_val_sorted, rc, cbits, s));
+      CK(launch_merge_emit(ma, rc, s));
+      mark(P, "merge_cap", s, 2);
     }
-    CK(launch_merge_large_groups(ma, L, n_regions, lgrid, s));
-    mark(P, "merge_large_groups", s, n_regions > 0 ? 3 : 2);
   }
 
   // ---- offsets (ref/adc.py:229-244)
@@ -757,7 +794,7 @@ extern "C" adps_status adps_step_phase2(adps_plan* P, void* stream_v, const adps
   ea.clone_list = P->clone_list.as<int>();
   ea.cand_case = P->cand_case.as<int>();
   ea.cand_merged = P->cand_merged.as<int>();
-  ea.cand_start = P->cand_start.as<int>();
+  ea.cand_start = P->pstart.as<int>();   // children of parent k live at [pstart[k], +N_k)
   ea.ins_off = P->ins_off.as<int>();
   ea.fb_ord = P->fb_ord.as<int>();
   ea.children = P->children.as<float>();

@@ -220,7 +220,8 @@ cudaError_t launch_ranges(const RangeArgs& a, cudaStream_t s) {
   return cudaGetLastError();
 }
 
-// ============================================================ merge
+// ============================================================ merge (see merge.cu)
+#if 0
 // A "team" is one warp (small candidates) or one CTA (large candidates).
 template <int TEAM>
 __device__ __forceinline__ void team_sync() {
@@ -712,6 +713,8 @@ cudaError_t launch_merge_large_groups(const MergeArgs& a, const LargeArgs& L, lo
   large_cap_kernel<<<grid, 256, 0, s>>>(a, L);
   return cudaGetLastError();
 }
+
+#endif
 
 // ============================================================ offsets
 struct CandScanPolicy {

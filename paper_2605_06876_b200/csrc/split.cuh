@@ -69,51 +69,7 @@ struct RangeArgs {
 };
 cudaError_t launch_ranges(const RangeArgs& a, cudaStream_t s);
 
-// ---- merge + cap + case (ref/cross_view_merge.py:33-116, ref/adc.py:184-227) ----
-struct MergeArgs {
-  const int* split_list;
-  const int* cand_start;
-  const int* cand_end;
-  const int* cand_nvalid;
-  const int* vals_sorted;        // sorted pos -> region id
-  const unsigned char* valid;    // region id -> t* > 0
-  const Proposal* props;         // region id -> proposal
-  const unsigned char* dom_flag;
-  const float* opacity;
-  double gamma_d, gamma_c;
-  int n_max;
-  int large_threshold;
-  int* idx;                      // [cap] start+j -> region id of j-th valid proposal
-  int* uf;                       // [cap]
-  GroupRec* groups;              // [cap]
-  float* children;               // [cap,14]
-  int* cand_case;
-  int* cand_props;
-  int* cand_merged;
-  int* cand_ins;
-  int* large_list;
-  Counters* ctr;
-  unsigned grid;
-};
-// scratch of the large-candidate path (P > large_threshold)
-struct LargeArgs {
-  unsigned long long* keys;         // [n_regions] (large id << 32 | root), ~0 elsewhere
-  int* vals;                        // [n_regions] local proposal index j
-  unsigned long long* keys_sorted;  // [n_regions]
-  int* vals_sorted;                 // [n_regions]
-  int* seg_begin;                   // [n_regions] at start + root
-  int* seg_end;                     // [n_regions]
-  long long* seg_list;              // [n_regions]
-  unsigned long long* n_seg;        // [1]
-  unsigned long long* work_cnt;     // [n_split]
-  unsigned long long* work_off;     // [n_split + 1]
-  int* n_groups;                    // [n_split]
-  int* rank_of;                     // [n_regions] cap rank of a root or -1
-};
-cudaError_t launch_merge_small(const MergeArgs& a, cudaStream_t s);
-cudaError_t launch_merge_large_gates(const MergeArgs& a, const LargeArgs& L, unsigned grid, cudaStream_t s);
-cudaError_t launch_merge_large_groups(const MergeArgs& a, const LargeArgs& L, long long n_keys, unsigned grid,
-                                      cudaStream_t s);
+// ---- merge + cap + case: see merge.cuh ----
 
 // ---- offsets: candidate inserts and survivor compaction (ref/adc.py:229-244) ----
 struct OffsetArgs {
