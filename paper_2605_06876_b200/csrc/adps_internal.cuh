@@ -63,6 +63,15 @@ struct Proposal {
   double cov[6];    // xx xy xz yy yz zz
   double prec[6];
   double rgb[3];
+  double smax;      // max(s1, s2): sqrt of the largest covariance eigenvalue
+};
+
+// Bounding data of 64 spatially sorted proposals (exact gate pruning).
+struct TileBox {
+  double c[3];      // centre
+  double r;         // max |mu - c|
+  double smax;      // max proposal smax
+  double lo[3], hi[3];   // rgb box
 };
 
 // Merged group record (ref/cross_view_merge.py:17-30), stored at its root slot.

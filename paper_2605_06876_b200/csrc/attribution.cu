@@ -152,6 +152,28 @@ __global__ void __launch_bounds__(kTileThreads) tile_kernel(TileParams P) {
     S.n_part = 0;
     S.n_reg = 0;
   }
+  // 0. dominant map: candidate id per pixel, ever-dominant flags over ALL
+  //    pixels (ref/adc.py:177-180).  Tiles without any split-candidate pixel
+  //    cannot hold a region: they skip the image/gt reads entirely.
+  int n_cand = 0;
+  for (int p = tid; p < kTilePx; p += kTileThreads) {
+    const int x = x0 + p % kTileW, y = y0 + p / kTileW;
+    int c = -1;
+    if (x < W && y < H) {
+      const int dd = __ldg(dom + (long long)y * W + x);
+      if (dd >= 0 && dd < P.N && __ldg(P.cls + dd) == 1) {
+        if (P.dom_flag[dd] == 0) P.dom_flag[dd] = 1;   // idempotent, race-benign
+        c = dd;
+      }
+    }
+    S.d[p] = c;
+    n_cand += c >= 0;
+  }
+  if (__syncthreads_count(n_cand) == 0 && !P.dbg_m) {
+    int* border = P.border + (long long)blockIdx.x * kBorderSlots;
+    for (int s = tid; s < kBorderSlots; s += kTileThreads) border[s] = -1;
+    return;
+  }
   // 1. pre-erosion metric on the haloed tile, band on the tile itself
   for (int idx = tid; idx < ew * eh; idx += kTileThreads) {
     int ex = idx % ew, ey = idx / ew;
@@ -200,11 +222,7 @@ __global__ void __launch_bounds__(kTileThreads) tile_kernel(TileParams P) {
       } else {
         mer = S.mext[ty * ew + tx];
       }
-      int dd = __ldg(dom + (long long)y * W + x);
-      if (dd >= 0 && dd < P.N && __ldg(P.cls + dd) == 1) {
-        if (P.dom_flag[dd] == 0) P.dom_flag[dd] = 1;   // idempotent, race-benign
-        if (mer) key = dd;
-      }
+      if (mer) key = S.d[p];
       if (P.dbg_m) {
         long long q = (long long)v * hw + (long long)y * W + x;
         P.dbg_m[q] = mer;

@@ -85,6 +85,7 @@ __global__ void case_kernel(MergeArgs a) {
     a.cand_props[k] = P;
     a.n_groups[k] = 0;
     a.cand_merged[k] = 0;
+    a.large_of[k] = -1;
     if (!a.dom_flag[gi]) {            // never dominant in the sampled views: vanilla fallback
       a.cand_case[k] = ADPS_CASE_FALLBACK;
       a.cand_ins[k] = 2;
@@ -100,8 +101,11 @@ __global__ void case_kernel(MergeArgs a) {
       } else if (P > a.small_max) {
         const unsigned long long l = atomicAdd(&a.ctr->n_large, 1ull);
         a.large_list[l] = (int)k;
+        a.large_of[k] = (int)l;
         const long long T = (P + 63) / 64;
         a.work_cnt[l] = (unsigned long long)(T * (T + 1) / 2);
+        a.lp_cnt[l] = (unsigned long long)P;
+        a.tile_cnt[l] = (unsigned long long)T;
       }
     }
   }
@@ -171,48 +175,175 @@ __global__ void __launch_bounds__(1024) offsets_1block_kernel(const unsigned lon
   if (threadIdx.x == 0) out[n] = carry;
 }
 
+cudaError_t launch_merge_small_gates(const MergeArgs& a, cudaStream_t s) {
+  small_pairs_kernel<<<a.grid, 256, 0, s>>>(a);
+  offsets_1block_kernel<<<1, 1024, 0, s>>>(a.work_cnt, a.work_off, &a.ctr->n_large);
+  offsets_1block_kernel<<<1, 1024, 0, s>>>(a.lp_cnt, a.lp_off, &a.ctr->n_large);
+  offsets_1block_kernel<<<1, 1024, 0, s>>>(a.tile_cnt, a.tile_off, &a.ctr->n_large);
+  return cudaGetLastError();
+}
+
+// ---- exact spatial pruning for large parents --------------------------------
+// Proposals of each large parent are put in Morton order of their centres;
+// per 64-proposal tile a bounding sphere, the largest proposal sigma and the
+// rgb box bound every pair: sqrt(d' Sa^-1 d) >= |d| / smax_a, so a tile pair
+// whose minimum centre distance gives (dmin/sA + dmin/sB) > gamma_d, or whose
+// rgb boxes are more than gamma_c apart, contains no mergeable pair.
+__device__ __forceinline__ unsigned spread10(unsigned v) {
+  v &= 0x3ffu;
+  v = (v | (v << 16)) & 0x030000FFu;
+  v = (v | (v << 8)) & 0x0300F00Fu;
+  v = (v | (v << 4)) & 0x030C30C3u;
+  v = (v | (v << 2)) & 0x09249249u;
+  return v;
+}
+
+__global__ void morton_kernel(MergeArgs a, long long cap) {
+  const long long np = (long long)a.ctr->n_proposals;
+  const double inv = 1.0 / (4.0 * a.extent);
+  for (long long q = (long long)blockIdx.x * blockDim.x + threadIdx.x; q < cap;
+       q += (long long)gridDim.x * blockDim.x) {
+    unsigned long long key = ~0ull;
+    if (q < np) {
+      const int l = a.large_of[a.pcand[q]];
+      if (l >= 0) {
+        unsigned c[3];
+        for (int t = 0; t < 3; ++t) {
+          const double u = (a.props_s[q].mu[t] * inv + 0.5) * 1024.0;
+          c[t] = u <= 0.0 ? 0u : (u >= 1023.0 ? 1023u : (unsigned)u);
+        }
+        const unsigned m = spread10(c[0]) | (spread10(c[1]) << 1) | (spread10(c[2]) << 2);
+        key = ((unsigned long long)l << 32) | m;
+      }
+    }
+    a.mkey[q] = key;
+    a.mval[q] = (int)q;
+  }
+}
+
+cudaError_t launch_merge_morton(const MergeArgs& a, long long cap, cudaStream_t s) {
+  long long b = (cap + 255) / 256;
+  morton_kernel<<<(unsigned)(b < 1 ? 1 : (b > 65535 ? 65535 : b)), 256, 0, s>>>(a, cap);
+  return cudaGetLastError();
+}
+
+__device__ __forceinline__ long long find_owner(const unsigned long long* off, long long n, unsigned long long w) {
+  long long lo = 0, hi = n - 1;
+  while (lo < hi) {
+    const long long mid = (lo + hi + 1) / 2;
+    if (off[mid] <= w) lo = mid;
+    else hi = mid - 1;
+  }
+  return lo;
+}
+
+// one warp per 64-proposal tile of a large parent (Morton order)
+__global__ void box_kernel(MergeArgs a) {
+  const int lane = threadIdx.x & 31;
+  const long long warps = (long long)gridDim.x * (blockDim.x >> 5);
+  const long long n_large = (long long)a.ctr->n_large;
+  const unsigned long long n_tiles = n_large > 0 ? a.tile_off[n_large] : 0;
+  for (long long t = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); t < (long long)n_tiles;
+       t += warps) {
+    const long long l = find_owner(a.tile_off, n_large, (unsigned long long)t);
+    const long long tl = t - (long long)a.tile_off[l];
+    const long long b = (long long)a.lp_off[l] + tl * 64;
+    const long long e = min(b + 64, (long long)(a.lp_off[l] + a.lp_cnt[l]));
+    double s[3] = {0, 0, 0}, smax = 0.0, lo[3] = {1e300, 1e300, 1e300}, hi[3] = {-1e300, -1e300, -1e300};
+    for (long long m = b + lane; m < e; m += 32) {
+      const Proposal& M = a.props_s[a.mval_sorted[m]];
+      for (int c = 0; c < 3; ++c) {
+        s[c] += M.mu[c];
+        lo[c] = fmin(lo[c], M.rgb[c]);
+        hi[c] = fmax(hi[c], M.rgb[c]);
+      }
+      smax = fmax(smax, M.smax);
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+      for (int c = 0; c < 3; ++c) {
+        s[c] += __shfl_xor_sync(0xffffffffu, s[c], o);
+        lo[c] = fmin(lo[c], __shfl_xor_sync(0xffffffffu, lo[c], o));
+        hi[c] = fmax(hi[c], __shfl_xor_sync(0xffffffffu, hi[c], o));
+      }
+      smax = fmax(smax, __shfl_xor_sync(0xffffffffu, smax, o));
+    }
+    const double cnt = (double)(e - b);
+    const double cen[3] = {s[0] / cnt, s[1] / cnt, s[2] / cnt};
+    double r = 0.0;
+    for (long long m = b + lane; m < e; m += 32) {
+      const Proposal& M = a.props_s[a.mval_sorted[m]];
+      const double dx = M.mu[0] - cen[0], dy = M.mu[1] - cen[1], dz = M.mu[2] - cen[2];
+      r = fmax(r, sqrt(dx * dx + dy * dy + dz * dz));
+    }
+    for (int o = 16; o > 0; o >>= 1) r = fmax(r, __shfl_xor_sync(0xffffffffu, r, o));
+    if (lane == 0) {
+      TileBox B;
+      for (int c = 0; c < 3; ++c) {
+        B.c[c] = cen[c];
+        B.lo[c] = lo[c];
+        B.hi[c] = hi[c];
+      }
+      B.r = r * (1.0 + 1e-12) + 1e-300;   // rounding guard: the sphere really encloses
+      B.smax = smax;
+      a.boxes[t] = B;
+    }
+  }
+}
+
+__device__ __forceinline__ bool boxes_may_merge(const TileBox& A, const TileBox& B, double gd, double gc) {
+  for (int c = 0; c < 3; ++c)
+    if (B.lo[c] - A.hi[c] > gc || A.lo[c] - B.hi[c] > gc) return false;   // colour gate fails for all pairs
+  const double dx = A.c[0] - B.c[0], dy = A.c[1] - B.c[1], dz = A.c[2] - B.c[2];
+  const double dmin = sqrt(dx * dx + dy * dy + dz * dz) - A.r - B.r;
+  if (dmin <= 0.0) return true;
+  const double lb = dmin / A.smax + dmin / B.smax;
+  return !(lb > gd * (1.0 + 1e-9));
+}
+
 // 64x64 tiles of the upper-triangular gate matrix of every large parent,
 // spread over the whole grid (work item -> (parent, tile row, tile column)).
 __global__ void __launch_bounds__(256) pair_tiles_kernel(MergeArgs a) {
   __shared__ Proposal si[64], sj[64];
+  __shared__ int qi[64], qj[64];
   const long long n_large = (long long)a.ctr->n_large;
-  const unsigned long long W = a.work_off[n_large];
+  const unsigned long long W = n_large > 0 ? a.work_off[n_large] : 0;
   for (unsigned long long w = blockIdx.x; w < W; w += gridDim.x) {
-    long long lo = 0, hi = n_large - 1;
-    while (lo < hi) {
-      const long long mid = (lo + hi + 1) / 2;
-      if (a.work_off[mid] <= w) lo = mid;
-      else hi = mid - 1;
-    }
-    const int k = a.large_list[lo];
-    const int P = a.cand_nvalid[k];
-    const int ps = a.pstart[k];
+    const long long l = find_owner(a.work_off, n_large, w);
+    const long long P = (long long)a.lp_cnt[l];
     const long long T = (P + 63) / 64;
-    const long long q = (long long)(w - a.work_off[lo]);
+    const long long q = (long long)(w - a.work_off[l]);
     long long bi = (long long)floor(((2.0 * T + 1.0) - sqrt((2.0 * T + 1.0) * (2.0 * T + 1.0) - 8.0 * q)) / 2.0);
     if (bi < 0) bi = 0;
     while (bi > 0 && bi * T - bi * (bi - 1) / 2 > q) --bi;
     while ((bi + 1) * T - (bi + 1) * bi / 2 <= q) ++bi;
     const long long bj = bi + (q - (bi * T - bi * (bi - 1) / 2));
+    const long long tb = (long long)a.tile_off[l];
+    if (!boxes_may_merge(a.boxes[tb + bi], a.boxes[tb + bj], a.gamma_d, a.gamma_c)) continue;   // uniform
+    const long long base = (long long)a.lp_off[l];
     const int i0 = (int)(bi * 64), j0 = (int)(bj * 64);
     for (int t = threadIdx.x; t < 128; t += blockDim.x) {
       const int loc = t & 63;
-      const int src = (t < 64 ? i0 : j0) + loc;
-      if (src < P) (t < 64 ? si : sj)[loc] = a.props_s[ps + src];
+      const long long src = (t < 64 ? i0 : j0) + loc;
+      if (src < P) {
+        const int qq = a.mval_sorted[base + src];
+        (t < 64 ? qi : qj)[loc] = qq;
+        (t < 64 ? si : sj)[loc] = a.props_s[qq];
+      }
     }
     __syncthreads();
     for (int t = threadIdx.x; t < 64 * 64; t += blockDim.x) {
       const int ii = t >> 6, jj = t & 63;
-      const int i = i0 + ii, j = j0 + jj;
-      if (i < j && j < P && gate(si[ii], sj[jj], a.gamma_d, a.gamma_c)) uf_unite(a.uf, ps + i, ps + j);
+      const long long i = i0 + ii, j = j0 + jj;
+      // unordered pairs: within a diagonal tile take ii < jj once
+      if (j < P && i < P && (bi != bj || ii < jj) && gate(si[ii], sj[jj], a.gamma_d, a.gamma_c))
+        uf_unite(a.uf, qi[ii], qj[jj]);
     }
     __syncthreads();
   }
 }
 
-cudaError_t launch_merge_gates(const MergeArgs& a, cudaStream_t s) {
-  small_pairs_kernel<<<a.grid, 256, 0, s>>>(a);
-  offsets_1block_kernel<<<1, 1024, 0, s>>>(a.work_cnt, a.work_off, &a.ctr->n_large);
+cudaError_t launch_merge_tile_gates(const MergeArgs& a, cudaStream_t s) {
+  box_kernel<<<a.grid, 256, 0, s>>>(a);
   pair_tiles_kernel<<<a.grid, 256, 0, s>>>(a);
   return cudaGetLastError();
 }

@@ -54,15 +54,29 @@ struct MergeArgs {
   int* cand_ins;
   int* small_list;                         // [n_split]
   int* large_list;                         // [n_split]
-  unsigned long long* work_cnt;            // [n_split]
+  unsigned long long* work_cnt;            // [n_split]   tile pairs of large parent l
   unsigned long long* work_off;            // [n_split + 1]
+  // exact spatial pruning of large parents' gate matrices
+  double extent;
+  int* large_of;                           // [n_split] large id or -1
+  unsigned long long* lp_cnt;              // [n_split]   proposals of large parent l
+  unsigned long long* lp_off;              // [n_split + 1]
+  unsigned long long* tile_cnt;            // [n_split]   64-proposal tiles of large parent l
+  unsigned long long* tile_off;            // [n_split + 1]
+  unsigned long long* mkey;                // [cap] (l << 32) | morton(mu), ~0 elsewhere
+  int* mval;                               // [cap]
+  unsigned long long* mkey_sorted;
+  int* mval_sorted;                        // Morton order: [lp_off[l], +P_l) -> proposal q
+  TileBox* boxes;                          // [cap / 64 + n_split]
   float* children;                         // [cap,14]
   Counters* ctr;
   unsigned grid;
 };
 
 cudaError_t launch_merge_prepare(const MergeArgs& a, long long n_split, ScanState st, cudaStream_t s);
-cudaError_t launch_merge_gates(const MergeArgs& a, cudaStream_t s);
+cudaError_t launch_merge_small_gates(const MergeArgs& a, cudaStream_t s);
+cudaError_t launch_merge_morton(const MergeArgs& a, long long cap, cudaStream_t s);
+cudaError_t launch_merge_tile_gates(const MergeArgs& a, cudaStream_t s);
 cudaError_t launch_merge_flatten(const MergeArgs& a, long long cap, cudaStream_t s);
 cudaError_t launch_merge_groups(const MergeArgs& a, long long cap, ScanState st, cudaStream_t s);
 cudaError_t launch_merge_cap(const MergeArgs& a, long long cap, cudaStream_t s);

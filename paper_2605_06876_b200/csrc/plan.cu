@@ -82,7 +82,8 @@ struct adps_plan {
   // merge / cap scratch (proposal space)
   Buf small_list, pstart, n_groups, work_cnt, work_off, props_s, pcand, gkey, gval, gkey_sorted, gval_sorted,
       grp_first, ext_key, ext_val, ext_key_sorted, ext_val_sorted, cand_key, cand_val, cand_key_sorted,
-      cand_val_sorted, scan3_val, scan3_flag, scan3_ticket;
+      cand_val_sorted, scan3_val, scan3_flag, scan3_ticket, large_of, lp_cnt, lp_off, tile_cnt, tile_off, mkey,
+      mval, mkey_sorted, mval_sorted, boxes;
   Buf scan_val, scan_flag, scan_ticket, scan2_val, scan2_flag, scan2_ticket, cub_tmp;
   Buf ctr;
   Counters* ctr_host = nullptr;
@@ -207,7 +208,9 @@ extern "C" adps_status adps_plan_destroy(adps_plan* P) {
                  &P->r_cams, &P->small_list, &P->pstart, &P->n_groups, &P->work_cnt, &P->work_off,
                  &P->props_s, &P->pcand, &P->gkey, &P->gval, &P->gkey_sorted, &P->gval_sorted, &P->grp_first,
                  &P->ext_key, &P->ext_val, &P->ext_key_sorted, &P->ext_val_sorted, &P->cand_key, &P->cand_val,
-                 &P->cand_key_sorted, &P->cand_val_sorted, &P->scan3_val, &P->scan3_flag, &P->scan3_ticket};
+                 &P->cand_key_sorted, &P->cand_val_sorted, &P->scan3_val, &P->scan3_flag, &P->scan3_ticket,
+                 &P->large_of, &P->lp_cnt, &P->lp_off, &P->tile_cnt, &P->tile_off, &P->mkey, &P->mval,
+                 &P->mkey_sorted, &P->mval_sorted, &P->boxes};
   for (Buf* b : bufs)
     if (b->p) cudaFree(b->p);
   if (P->ctr_host) cudaFreeHost(P->ctr_host);
@@ -627,6 +630,16 @@ extern "C" adps_status adps_step_phase1(adps_plan* P, void* stream_v, const adps
   CK(ensure(P->cand_val, 4 * rc));
   CK(ensure(P->cand_key_sorted, 4 * rc));
   CK(ensure(P->cand_val_sorted, 4 * rc));
+  CK(ensure(P->large_of, 4 * sc));
+  CK(ensure(P->lp_cnt, 8 * sc));
+  CK(ensure(P->lp_off, 8 * (sc + 1)));
+  CK(ensure(P->tile_cnt, 8 * sc));
+  CK(ensure(P->tile_off, 8 * (sc + 1)));
+  CK(ensure(P->mkey, 8 * rc));
+  CK(ensure(P->mval, 4 * rc));
+  CK(ensure(P->mkey_sorted, 8 * rc));
+  CK(ensure(P->mval_sorted, 4 * rc));
+  CK(ensure(P->boxes, sizeof(TileBox) * (rc / 64 + sc + 1)));
   CK(ensure(P->regions_per_view, 4 * sc * V));
   CK(cudaMemsetAsync(P->cand_start.p, 0, 4 * sc, s));
   CK(cudaMemsetAsync(P->cand_end.p, 0, 4 * sc, s));
@@ -696,6 +709,17 @@ extern "C" adps_status adps_step_phase1(adps_plan* P, void* stream_v, const adps
   ma.work_cnt = P->work_cnt.as<unsigned long long>();
   ma.work_off = P->work_off.as<unsigned long long>();
   ma.children = P->children.as<float>();
+  ma.extent = extent;
+  ma.large_of = P->large_of.as<int>();
+  ma.lp_cnt = P->lp_cnt.as<unsigned long long>();
+  ma.lp_off = P->lp_off.as<unsigned long long>();
+  ma.tile_cnt = P->tile_cnt.as<unsigned long long>();
+  ma.tile_off = P->tile_off.as<unsigned long long>();
+  ma.mkey = P->mkey.as<unsigned long long>();
+  ma.mval = P->mval.as<int>();
+  ma.mkey_sorted = P->mkey_sorted.as<unsigned long long>();
+  ma.mval_sorted = P->mval_sorted.as<int>();
+  ma.boxes = P->boxes.as<TileBox>();
   ma.ctr = ctr;
   ma.grid = (unsigned)(P->sm_count * 8);
   if (n_split > 0) {
@@ -704,8 +728,15 @@ extern "C" adps_status adps_step_phase1(adps_plan* P, void* stream_v, const adps
     if (st != ADPS_OK) return st;
     CK(launch_merge_prepare(ma, n_split, sst3, s));
     mark(P, "merge_prepare", s, 2);
-    CK(launch_merge_gates(ma, s));
-    mark(P, "merge_gates", s, 3);
+    CK(launch_merge_small_gates(ma, s));
+    mark(P, "merge_small_gates", s, 4);
+    if (n_regions > 0) {
+      CK(launch_merge_morton(ma, rc, s));
+      const int mbits = 32 + ceil_log2((unsigned long long)n_split + 2);
+      CK(cub_sort_pairs(P, ma.mkey, ma.mkey_sorted, ma.mval, ma.mval_sorted, rc, mbits, s));
+      CK(launch_merge_tile_gates(ma, s));
+      mark(P, "merge_tile_gates", s, 3);
+    }
     if (n_regions > 0) {
       CK(launch_merge_flatten(ma, rc, s));
       const int gbits = ceil_log2((unsigned long long)rc + 2);
