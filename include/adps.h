@@ -194,7 +194,7 @@ ADPS_API adps_status adps_get_timing(adps_plan* plan, double* ms, int32_t max_en
 
 /* Tuning knobs (diagnostic/testing).  ADPS_PARAM_LARGE_THRESHOLD: parents
  * with more proposals than this use the grid-wide pair-tile merge path
- * (default 96; 0 routes every split parent through it). */
+ * (default 32; 0 routes every split parent through it). */
 #define ADPS_PARAM_LARGE_THRESHOLD 1
 ADPS_API adps_status adps_set_param(adps_plan* plan, int32_t key, int64_t value);
 

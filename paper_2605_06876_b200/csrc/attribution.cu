@@ -114,8 +114,8 @@ __global__ void thresholds_kernel(const unsigned long long* __restrict__ lohi, i
 
 // ----------------------------------------------------------------- tile pass
 struct TileSmem {
-  unsigned char mext[(kTileH + 2 * kMaxErodeHalo) * (kTileW + 2 * kMaxErodeHalo)];
-  unsigned char hor[(kTileH + 2 * kMaxErodeHalo) * kTileW];
+  unsigned long long mrow[kTileH + 2 * kMaxErodeHalo];   // pre-erosion m of haloed rows, bit = x - x0 + hl
+  unsigned erow[kTileH];                                  // eroded m of the tile rows, bit = x - x0
   unsigned char band[kTilePx];
   unsigned char touch[kTilePx];
   int d[kTilePx];
@@ -174,38 +174,59 @@ __global__ void __launch_bounds__(kTileThreads) tile_kernel(TileParams P) {
     for (int s = tid; s < kBorderSlots; s += kTileThreads) border[s] = -1;
     return;
   }
-  // 1. pre-erosion metric on the haloed tile, band on the tile itself
-  for (int idx = tid; idx < ew * eh; idx += kTileThreads) {
-    int ex = idx % ew, ey = idx / ew;
-    int x = x0 - hl + ex, y = y0 - hl + ey;
-    unsigned char m = 0;
-    int tx = ex - hl, ty = ey - hl;
-    bool in_tile = tx >= 0 && tx < kTileW && ty >= 0 && ty < kTileH;
+  // 1. pre-erosion metric as row bitmasks: tile rows by ballot (lane = x),
+  //    band on the tile itself; the (r-1)-pixel halo afterwards
+  const int lane = tid & 31, wid = tid >> 5;
+  for (int ty = wid; ty < kTileH; ty += kTileThreads / 32) {
+    const int x = x0 + lane, y = y0 + ty;
+    bool m = false;
     unsigned char b = 0;
-    if (x >= 0 && x < W && y >= 0 && y < H) {
-      long long p = (long long)y * W + x;
-      double xr = dsub(raw_l1(img, gtv, p), lo);
+    if (x < W && y < H) {
+      const double xr = dsub(raw_l1(img, gtv, (long long)y * W + x), lo);
       m = xr >= x_m;
-      if (in_tile) {
-        int bb = 0;
-        for (int k = 1; k < P.L; ++k) bb += xr >= thr[k];
-        b = (unsigned char)bb;
-      }
+      int bb = 0;
+      for (int k = 1; k < P.L; ++k) bb += xr >= thr[k];
+      b = (unsigned char)bb;
     }
-    S.mext[ey * ew + ex] = m;
-    if (in_tile) S.band[ty * kTileW + tx] = b;
+    S.band[ty * kTileW + lane] = b;
+    const unsigned bits = __ballot_sync(0xffffffffu, m);
+    if (lane == 0) S.mrow[ty + hl] = (unsigned long long)bits << hl;
+  }
+  if (r > 1) {
+    if (tid < hl + hh) S.mrow[tid < hl ? tid : kTileH + tid] = 0ull;   // halo rows start empty
+    __syncthreads();
+    const int n_halo = ew * eh - kTilePx;
+    for (int h = tid; h < n_halo; h += kTileThreads) {
+      int ex, ey;
+      const int top = hl * ew, bot = hh * ew;
+      if (h < top) { ey = h / ew; ex = h % ew; }
+      else if (h < top + bot) { ey = hl + kTileH + (h - top) / ew; ex = (h - top) % ew; }
+      else {
+        const int c = h - top - bot, side = hl + hh;
+        ey = hl + c / side;
+        const int k = c % side;
+        ex = k < hl ? k : kTileW + k;
+      }
+      const int x = x0 - hl + ex, y = y0 - hl + ey;
+      if (x >= 0 && x < W && y >= 0 && y < H &&
+          dsub(raw_l1(img, gtv, (long long)y * W + x), lo) >= x_m)
+        atomicOr(&S.mrow[ey], 1ull << ex);
+    }
   }
   __syncthreads();
-  // 2. r x r erosion (offsets -(r//2) .. r-r//2-1; outside the image = 0), separable
-  if (r > 1) {
-    for (int idx = tid; idx < eh * kTileW; idx += kTileThreads) {
-      int tx = idx % kTileW, ey = idx / kTileW;
-      unsigned char a = 1;
-      for (int dx = -hl; dx <= hh; ++dx) a &= S.mext[ey * ew + tx + hl + dx];
-      S.hor[ey * kTileW + tx] = a;
+  // 2. r x r erosion on the bitmasks (offsets -(r//2) .. r-r//2-1; outside = 0)
+  if (tid < kTileH) {
+    const int span = hl + hh;
+    unsigned long long acc = ~0ull;
+    for (int dy = 0; dy <= span; ++dy) {
+      const unsigned long long row = S.mrow[tid + dy];
+      unsigned long long h = row;
+      for (int dx = 1; dx <= span; ++dx) h &= row >> dx;
+      acc &= h;
     }
-    __syncthreads();
+    S.erow[tid] = (unsigned)acc;
   }
+  __syncthreads();
   // 3. keys + ever-dominant flags; each warp owns whole 32-px rows (lane = x),
   //    so horizontal runs of equal key are found with ballots and every pixel
   //    starts labelled with its run's first pixel (short union-find paths).
@@ -215,13 +236,7 @@ __global__ void __launch_bounds__(kTileThreads) tile_kernel(TileParams P) {
     int key = -1;
     unsigned char mer = 0;
     if (x < W && y < H) {
-      if (r > 1) {
-        unsigned char a = 1;
-        for (int dy = -hl; dy <= hh; ++dy) a &= S.hor[(ty + hl + dy) * kTileW + tx];
-        mer = a;
-      } else {
-        mer = S.mext[ty * ew + tx];
-      }
+      mer = (S.erow[ty] >> tx) & 1u;
       if (mer) key = S.d[p];
       if (P.dbg_m) {
         long long q = (long long)v * hw + (long long)y * W + x;

@@ -24,10 +24,16 @@ namespace adps {
 
 __device__ __forceinline__ bool gate(const Proposal& A, const Proposal& B, double gd, double gc) {
   // sqrt(d^T Sa^-1 d) + sqrt(d^T Sb^-1 d) <= gamma_d and max|drgb| <= gamma_c, inclusive
-  const double dl[3] = {B.mu[0] - A.mu[0], B.mu[1] - A.mu[1], B.mu[2] - A.mu[2]};
-  const double d = sqrt(fmax(sym_quad(A.prec, dl), 0.0)) + sqrt(fmax(sym_quad(B.prec, dl), 0.0));
   const double dc = fmax(fmax(fabs(A.rgb[0] - B.rgb[0]), fabs(A.rgb[1] - B.rgb[1])), fabs(A.rgb[2] - B.rgb[2]));
-  return d <= gd && dc <= gc;
+  if (!(dc <= gc)) return false;
+  const double dl[3] = {B.mu[0] - A.mu[0], B.mu[1] - A.mu[1], B.mu[2] - A.mu[2]};
+  // exact early reject: d >= |dl| (1/smax_a + 1/smax_b) (largest covariance eigenvalue
+  // is smax^2); a 1e-9 relative guard keeps it strictly conservative
+  const double n2 = dl[0] * dl[0] + dl[1] * dl[1] + dl[2] * dl[2];
+  const double w = 1.0 / A.smax + 1.0 / B.smax;
+  if (n2 * w * w > gd * gd * (1.0 + 1e-9)) return false;
+  const double d = sqrt(fmax(sym_quad(A.prec, dl), 0.0)) + sqrt(fmax(sym_quad(B.prec, dl), 0.0));
+  return d <= gd;
 }
 
 // group -> Gaussian: eigh(merged_cov) ascending, det fix on column 0,

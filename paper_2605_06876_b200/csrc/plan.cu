@@ -114,7 +114,7 @@ struct adps_plan {
   // launch accounting (own kernels / library sort calls), cumulative
   long long launches = 0;
   long long lib_calls = 0;
-  int large_threshold = 96;
+  int large_threshold = 32;
 };
 
 static void mark(adps_plan* P, const char* name, cudaStream_t s, int kernels) {
@@ -782,7 +782,7 @@ extern "C" adps_status adps_step_phase1(adps_plan* P, void* stream_v, const adps
   K.n_reset = (long long)C.n_reset;
   K.n_children = (long long)C.n_children;
   K.n_regions = n_regions;
-  K.n_proposals = 0;
+  K.n_proposals = (long long)C.n_proposals;
   K.merge_edges = (long long)C.merge_edges;
   K.n_partials = (long long)C.n_partials;
   K.degenerate_ray = C.degenerate ? 1 : 0;

@@ -191,7 +191,7 @@ class Plan:
         return int(k.value), int(lib.value)
 
     def set_large_threshold(self, p: int):
-        """Parents with more than p proposals take the grid-wide merge path (default 96)."""
+        """Parents with more than p proposals take the grid-wide merge path (default 32)."""
         _abi.check(self.lib.adps_set_param(self._h, _abi.PARAM_LARGE_THRESHOLD, int(p)))
 
     def set_debug_records(self, on: bool):

@@ -340,7 +340,7 @@ def test_large_merge_path_matches_warp_path(op, plan, tag):
                                torch.as_tensor(DATA[f"step__{tag}__denom"], device="cuda"), cfg,
                                np.random.default_rng(seed), renders=(img, dom), plan=plan)
     finally:
-        plan.set_large_threshold(96)
+        plan.set_large_threshold(32)
     ores = O.adpsplit_step(g, extent, cams, gts, DATA[f"step__{tag}__grad_accum"],
                            DATA[f"step__{tag}__denom"], cfg, np.random.default_rng(seed), renders=renders_np)
     st = PA.compare_step(gres, ores, PA.flag_candidates(ores, g, cams, cfg), g)
@@ -368,7 +368,7 @@ def test_large_merge_path_synthetic(op, plan):
                                torch.as_tensor(den, device="cuda"), cfg, np.random.default_rng(1),
                                renders=(img, dom), plan=plan)
     finally:
-        plan.set_large_threshold(96)
+        plan.set_large_threshold(32)
     props = gres.report_arrays["cand_proposals"].cpu().numpy()
     assert props.max() > 64 and (props > 16).sum() >= 3, (props.max(), (props > 16).sum())
     gts_np = {v: gt_img[v].double().cpu().numpy() for v in views}
