@@ -99,6 +99,7 @@ struct Counters {
   unsigned long long n_large;
   unsigned long long n_small;
   unsigned long long n_groups_all;
+  unsigned long long n_tile_pairs;
   unsigned int degenerate;
   unsigned int overflow;   // bit0 regions, bit1 partials
 };

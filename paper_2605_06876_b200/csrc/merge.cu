@@ -306,25 +306,57 @@ __device__ __forceinline__ bool boxes_may_merge(const TileBox& A, const TileBox&
   return !(lb > gd * (1.0 + 1e-9));
 }
 
-// 64x64 tiles of the upper-triangular gate matrix of every large parent,
-// spread over the whole grid (work item -> (parent, tile row, tile column)).
+// work item w -> (large parent l, tile row bi, tile column bj), row-major upper triangle
+__device__ __forceinline__ void decode_tile_pair(const MergeArgs& a, long long n_large, unsigned long long w,
+                                                 long long& l, long long& bi, long long& bj) {
+  l = find_owner(a.work_off, n_large, w);
+  const long long T = ((long long)a.lp_cnt[l] + 63) / 64;
+  const long long q = (long long)(w - a.work_off[l]);
+  bi = (long long)floor(((2.0 * T + 1.0) - sqrt((2.0 * T + 1.0) * (2.0 * T + 1.0) - 8.0 * q)) / 2.0);
+  if (bi < 0) bi = 0;
+  while (bi > 0 && bi * T - bi * (bi - 1) / 2 > q) --bi;
+  while ((bi + 1) * T - (bi + 1) * bi / 2 <= q) ++bi;
+  bj = bi + (q - (bi * T - bi * (bi - 1) / 2));
+}
+
+// one thread per (parent, tile row, tile column) of the upper-triangular
+// tile matrix: keep the pairs the bounding data cannot exclude
+__global__ void tile_pair_filter_kernel(MergeArgs a) {
+  const long long n_large = (long long)a.ctr->n_large;
+  const unsigned long long W = n_large > 0 ? a.work_off[n_large] : 0;
+  for (unsigned long long w = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; w < W;
+       w += (unsigned long long)gridDim.x * blockDim.x) {
+    long long l, bi, bj;
+    decode_tile_pair(a, n_large, w, l, bi, bj);
+    const long long tb = (long long)a.tile_off[l];
+    if (!boxes_may_merge(a.boxes[tb + bi], a.boxes[tb + bj], a.gamma_d, a.gamma_c)) continue;
+    const unsigned long long s = atomicAdd(&a.ctr->n_tile_pairs, 1ull);
+    if ((long long)s < a.tile_pairs_cap) a.tile_pairs[s] = make_int4((int)l, (int)bi, (int)bj, 0);
+    else atomicOr(&a.ctr->overflow, 4u);
+  }
+}
+
+// one block per surviving 64x64 tile pair of a large parent's gate matrix (or,
+// if the survivor list overflowed, every tile pair with the box test inline)
 __global__ void __launch_bounds__(256) pair_tiles_kernel(MergeArgs a) {
   __shared__ Proposal si[64], sj[64];
   __shared__ int qi[64], qj[64];
+  const bool overflow = (a.ctr->overflow & 4u) != 0;
   const long long n_large = (long long)a.ctr->n_large;
-  const unsigned long long W = n_large > 0 ? a.work_off[n_large] : 0;
+  const unsigned long long W = overflow ? (n_large > 0 ? a.work_off[n_large] : 0) : a.ctr->n_tile_pairs;
   for (unsigned long long w = blockIdx.x; w < W; w += gridDim.x) {
-    const long long l = find_owner(a.work_off, n_large, w);
+    long long l, bi, bj;
+    if (overflow) {
+      decode_tile_pair(a, n_large, w, l, bi, bj);
+      const long long tb = (long long)a.tile_off[l];
+      if (!boxes_may_merge(a.boxes[tb + bi], a.boxes[tb + bj], a.gamma_d, a.gamma_c)) continue;   // uniform
+    } else {
+      const int4 tp = a.tile_pairs[w];
+      l = tp.x;
+      bi = tp.y;
+      bj = tp.z;
+    }
     const long long P = (long long)a.lp_cnt[l];
-    const long long T = (P + 63) / 64;
-    const long long q = (long long)(w - a.work_off[l]);
-    long long bi = (long long)floor(((2.0 * T + 1.0) - sqrt((2.0 * T + 1.0) * (2.0 * T + 1.0) - 8.0 * q)) / 2.0);
-    if (bi < 0) bi = 0;
-    while (bi > 0 && bi * T - bi * (bi - 1) / 2 > q) --bi;
-    while ((bi + 1) * T - (bi + 1) * bi / 2 <= q) ++bi;
-    const long long bj = bi + (q - (bi * T - bi * (bi - 1) / 2));
-    const long long tb = (long long)a.tile_off[l];
-    if (!boxes_may_merge(a.boxes[tb + bi], a.boxes[tb + bj], a.gamma_d, a.gamma_c)) continue;   // uniform
     const long long base = (long long)a.lp_off[l];
     const int i0 = (int)(bi * 64), j0 = (int)(bj * 64);
     for (int t = threadIdx.x; t < 128; t += blockDim.x) {
@@ -350,6 +382,7 @@ __global__ void __launch_bounds__(256) pair_tiles_kernel(MergeArgs a) {
 
 cudaError_t launch_merge_tile_gates(const MergeArgs& a, cudaStream_t s) {
   box_kernel<<<a.grid, 256, 0, s>>>(a);
+  tile_pair_filter_kernel<<<a.grid, 256, 0, s>>>(a);
   pair_tiles_kernel<<<a.grid, 256, 0, s>>>(a);
   return cudaGetLastError();
 }

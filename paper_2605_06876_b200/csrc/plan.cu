@@ -83,7 +83,7 @@ struct adps_plan {
   Buf small_list, pstart, n_groups, work_cnt, work_off, props_s, pcand, gkey, gval, gkey_sorted, gval_sorted,
       grp_first, ext_key, ext_val, ext_key_sorted, ext_val_sorted, cand_key, cand_val, cand_key_sorted,
       cand_val_sorted, scan3_val, scan3_flag, scan3_ticket, large_of, lp_cnt, lp_off, tile_cnt, tile_off, mkey,
-      mval, mkey_sorted, mval_sorted, boxes;
+      mval, mkey_sorted, mval_sorted, boxes, tile_pairs;
   Buf scan_val, scan_flag, scan_ticket, scan2_val, scan2_flag, scan2_ticket, cub_tmp;
   Buf ctr;
   Counters* ctr_host = nullptr;
@@ -210,7 +210,7 @@ extern "C" adps_status adps_plan_destroy(adps_plan* P) {
                  &P->ext_key, &P->ext_val, &P->ext_key_sorted, &P->ext_val_sorted, &P->cand_key, &P->cand_val,
                  &P->cand_key_sorted, &P->cand_val_sorted, &P->scan3_val, &P->scan3_flag, &P->scan3_ticket,
                  &P->large_of, &P->lp_cnt, &P->lp_off, &P->tile_cnt, &P->tile_off, &P->mkey, &P->mval,
-                 &P->mkey_sorted, &P->mval_sorted, &P->boxes};
+                 &P->mkey_sorted, &P->mval_sorted, &P->boxes, &P->tile_pairs};
   for (Buf* b : bufs)
     if (b->p) cudaFree(b->p);
   if (P->ctr_host) cudaFreeHost(P->ctr_host);
@@ -640,6 +640,14 @@ extern "C" adps_status adps_step_phase1(adps_plan* P, void* stream_v, const adps
   CK(ensure(P->mkey_sorted, 8 * rc));
   CK(ensure(P->mval_sorted, 4 * rc));
   CK(ensure(P->boxes, sizeof(TileBox) * (rc / 64 + sc + 1)));
+  {
+    // surviving tile pairs: worst case every pair of (rc/64 + n_split) tiles; capped at
+    // 2^24 entries (overflow falls back to inline filtering inside pair_tiles_kernel)
+    const long long t = rc / 64 + sc + 1;
+    long long want = t * (t + 1) / 2;
+    if (want > (1ll << 24)) want = 1ll << 24;
+    CK(ensure(P->tile_pairs, sizeof(int4) * want));
+  }
   CK(ensure(P->regions_per_view, 4 * sc * V));
   CK(cudaMemsetAsync(P->cand_start.p, 0, 4 * sc, s));
   CK(cudaMemsetAsync(P->cand_end.p, 0, 4 * sc, s));
@@ -720,6 +728,8 @@ extern "C" adps_status adps_step_phase1(adps_plan* P, void* stream_v, const adps
   ma.mkey_sorted = P->mkey_sorted.as<unsigned long long>();
   ma.mval_sorted = P->mval_sorted.as<int>();
   ma.boxes = P->boxes.as<TileBox>();
+  ma.tile_pairs = P->tile_pairs.as<int4>();
+  ma.tile_pairs_cap = (long long)(P->tile_pairs.bytes / sizeof(int4));
   ma.ctr = ctr;
   ma.grid = (unsigned)(P->sm_count * 8);
   if (n_split > 0) {
