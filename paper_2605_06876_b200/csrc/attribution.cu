@@ -156,6 +156,7 @@ __global__ void __launch_bounds__(kTileThreads) tile_kernel(TileParams P) {
   //    pixels (ref/adc.py:177-180).  Tiles without any split-candidate pixel
   //    cannot hold a region: they skip the image/gt reads entirely.
   int n_cand = 0;
+#pragma unroll
   for (int p = tid; p < kTilePx; p += kTileThreads) {
     const int x = x0 + p % kTileW, y = y0 + p / kTileW;
     int c = -1;
@@ -177,6 +178,7 @@ __global__ void __launch_bounds__(kTileThreads) tile_kernel(TileParams P) {
   // 1. pre-erosion metric as row bitmasks: tile rows by ballot (lane = x),
   //    band on the tile itself; the (r-1)-pixel halo afterwards
   const int lane = tid & 31, wid = tid >> 5;
+#pragma unroll
   for (int ty = wid; ty < kTileH; ty += kTileThreads / 32) {
     const int x = x0 + lane, y = y0 + ty;
     bool m = false;
@@ -258,51 +260,60 @@ __global__ void __launch_bounds__(kTileThreads) tile_kernel(TileParams P) {
     for (int k = 0; k < 6; ++k) S.mom[k][p] = 0;
   }
   __syncthreads();
-  // 4. unions with the row above (NW, N, NE) of equal (candidate, band); W is the run
+  // 4. run-level unions with the row above: 8-connectivity with equal
+  //    (candidate, band) is "horizontal run" + one union per (run, run above)
+  //    adjacency -- N at the first overlapping pixel, NW at the run start, NE
+  //    at the run end.
   for (int p = tid; p < kTilePx; p += kTileThreads) {
-    int key = S.d[p];
-    int ty = p / kTileW;
+    const int key = S.d[p];
+    const int ty = p / kTileW, tx = p % kTileW;
     if (key < 0 || ty == 0) continue;
-    int tx = p % kTileW;
-    unsigned char b = S.band[p];
-#pragma unroll
-    for (int dx = -1; dx <= 1; ++dx) {
-      int qx = tx + dx;
-      if (qx < 0 || qx >= kTileW) continue;
-      int q = p - kTileW + dx;
-      if (S.d[q] == key && S.band[q] == b) uf_unite(S.label, p, q);
-    }
+    const unsigned char b = S.band[p];
+    const int q = p - kTileW;
+    const bool a0 = S.d[q] == key && S.band[q] == b;
+    const bool am = tx > 0 && S.d[q - 1] == key && S.band[q - 1] == b;
+    const bool ap = tx < kTileW - 1 && S.d[q + 1] == key && S.band[q + 1] == b;
+    const bool start = tx == 0 || !(S.d[p - 1] == key && S.band[p - 1] == b);
+    const bool end = tx == kTileW - 1 || !(S.d[p + 1] == key && S.band[p + 1] == b);
+    if (a0 && (start || !am)) uf_unite(S.label, p, q);
+    if (start && am && !a0) uf_unite(S.label, p, q - 1);
+    if (end && ap && !a0) uf_unite(S.label, p, q + 1);
   }
   __syncthreads();
-  for (int p = tid; p < kTilePx; p += kTileThreads)
-    if (S.d[p] >= 0) S.label[p] = uf_find_halve(S.label, p);
+  // compress run starts (every label points at a run start; roots are run starts)
+  for (int p = tid; p < kTilePx; p += kTileThreads) {
+    const int key = S.d[p];
+    if (key < 0) continue;
+    const int tx = p % kTileW;
+    const bool start = tx == 0 || !(S.d[p - 1] == key && S.band[p - 1] == S.band[p]);
+    if (start) S.label[p] = uf_find_halve(S.label, p);
+  }
   __syncthreads();
-  // 5. warp-aggregated integer moments (tile-local coordinates, exact)
+  // 5. integer moments per run in closed form (tile-local coordinates, exact),
+  //    one shared atomic per run and moment
   const bool left_in = x0 > 0, top_in = y0 > 0;
   const bool right_in = x0 + kTileW < W, bottom_in = y0 + kTileH < H;
   for (int p = tid; p < kTilePx; p += kTileThreads) {
-    bool keyed = S.d[p] >= 0;
-    unsigned act = __ballot_sync(0xffffffffu, keyed);
-    if (keyed) {
-      int root = S.label[p];
-      int tx = p % kTileW, ty = p / kTileW;
-      unsigned grp = __match_any_sync(act, root);
-      int v0 = __reduce_add_sync(grp, 1);
-      int v1 = __reduce_add_sync(grp, tx);
-      int v2 = __reduce_add_sync(grp, ty);
-      int v3 = __reduce_add_sync(grp, tx * tx);
-      int v4 = __reduce_add_sync(grp, tx * ty);
-      int v5 = __reduce_add_sync(grp, ty * ty);
-      if ((tid & 31) == __ffs(grp) - 1) {
-        atomicAdd(&S.mom[0][root], v0);
-        atomicAdd(&S.mom[1][root], v1);
-        atomicAdd(&S.mom[2][root], v2);
-        atomicAdd(&S.mom[3][root], v3);
-        atomicAdd(&S.mom[4][root], v4);
-        atomicAdd(&S.mom[5][root], v5);
-      }
-      bool edge = (tx == 0 && left_in) || (ty == 0 && top_in) || (tx == kTileW - 1 && right_in) ||
-                  (ty == kTileH - 1 && bottom_in);
+    const int key = S.d[p];
+    const int tx = p % kTileW, ty = p / kTileW;
+    const bool keyed = key >= 0;
+    const bool cont = keyed && tx < kTileW - 1 && S.d[p + 1] == key && S.band[p + 1] == S.band[p];
+    const unsigned ends = __ballot_sync(0xffffffffu, keyed && !cont);
+    const bool start = keyed && (tx == 0 || !(S.d[p - 1] == key && S.band[p - 1] == S.band[p]));
+    if (start) {
+      const int e = __ffs(ends & (0xffffffffu << tx)) - 1;
+      const int root = S.label[p];
+      const int n = e - tx + 1;
+      const int sx = (tx + e) * n / 2;
+      const int sxx = (e * (e + 1) * (2 * e + 1) - (tx - 1) * tx * (2 * tx - 1)) / 6;
+      atomicAdd(&S.mom[0][root], n);
+      atomicAdd(&S.mom[1][root], sx);
+      atomicAdd(&S.mom[2][root], ty * n);
+      atomicAdd(&S.mom[3][root], sxx);
+      atomicAdd(&S.mom[4][root], ty * sx);
+      atomicAdd(&S.mom[5][root], ty * ty * n);
+      const bool edge = (ty == 0 && top_in) || (ty == kTileH - 1 && bottom_in) || (tx == 0 && left_in) ||
+                        (e == kTileW - 1 && right_in);
       if (edge) S.touch[root] = 1;
     }
   }
@@ -375,7 +386,7 @@ __global__ void __launch_bounds__(kTileThreads) tile_kernel(TileParams P) {
     else { tx = kTileW - 1; ty = s - 2 * kTileW - kTileH; }
     int p = ty * kTileW + tx;
     int g = -1;
-    if (S.d[p] >= 0) g = S.slot[S.label[p]];
+    if (S.d[p] >= 0) g = S.slot[S.label[S.label[p]]];   // pixel -> run start -> root
     border[s] = g;
   }
 }
