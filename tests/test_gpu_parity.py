@@ -378,3 +378,48 @@ def test_large_merge_path_synthetic(op, plan):
                            renders=renders_np)
     st = PA.compare_step(gres, ores, PA.flag_candidates(ores, g, cam_objs, cfg), g)
     assert st["mismatched"] == 0
+
+
+def _step_digest(op, plan, res):
+    r = plan.regions()
+    out = res.gaussians.numpy()
+    d = {k: res.report_arrays[k].cpu().numpy() for k in res.report_arrays}
+    d.update({f"out_{k}": v for k, v in out.items()})
+    d["index_map"] = res.index_map.cpu().numpy()
+    order = np.lexsort((r["minpix"].cpu().numpy(), r["band"].cpu().numpy(), r["view_pos"].cpu().numpy(),
+                        r["candidate"].cpu().numpy()))
+    for k in ("candidate", "view_pos", "band", "minpix", "moments"):
+        d[f"reg_{k}"] = r[k].cpu().numpy()[order]
+    return d
+
+
+@pytest.mark.parametrize("cfg_name", ["config2"])
+def test_determinism_at_scale(op, cfg_name):
+    """Two runs of the same step are bitwise identical at BASELINE size."""
+    import torch
+    from paper_2605_06876_b200 import synth as S
+    from paper_2605_06876_b200.types import AdpSplitConfig
+    wl = S.CONFIGS[cfg_name]
+    ini, cams, (ga, den), gt = wl.build()
+    plan = op.Plan("cuda:0")
+    g = op.GaussianTensors.from_numpy(*ini.arrays(), device="cuda")
+    gt_img, _ = plan.render(op.GaussianTensors.from_numpy(*gt.arrays(), device="cuda"), cams)
+    img, dom = plan.render(g, cams)
+    cfg = AdpSplitConfig(v_views=len(cams), n_max=wl.n_max)
+    digests = []
+    for _ in range(3):
+        res = op.densify_step(g, ini.extent, cams, gt_img, torch.as_tensor(ga, device="cuda"),
+                              torch.as_tensor(den, device="cuda"), cfg, np.random.default_rng(0),
+                              renders=(img, dom), plan=plan, view_ids=list(range(len(cams))))
+        digests.append((res.counts, _step_digest(op, plan, res)))
+    for counts, dg in digests[1:]:
+        assert counts == digests[0][0]
+        for k in dg:
+            np.testing.assert_array_equal(dg[k], digests[0][1][k], err_msg=k)
+    # population accounting (SPEC.md:484) and index_map structure
+    c = digests[0][0]
+    rep = res.report()
+    assert c["n_out"] == c["n_keep"] + c["n_inserted"] + c["n_clone"]
+    kept = rep.index_map[rep.index_map >= 0]
+    assert (np.diff(kept) > 0).all() and len(kept) == c["n_keep"]
+    assert all(r.children_inserted <= wl.n_max for r in rep.candidates)
