@@ -286,7 +286,9 @@ __global__ void __launch_bounds__(kTileThreads) tile_kernel(TileParams P) {
     if (key < 0) continue;
     const int tx = p % kTileW;
     const bool start = tx == 0 || !(S.d[p - 1] == key && S.band[p - 1] == S.band[p]);
-    if (start) S.label[p] = uf_find_halve(S.label, p);
+    // read-only find: a halving find would rewrite labels of other run starts
+    // on its path and could overwrite their freshly stored roots
+    if (start) S.label[p] = uf_find(S.label, p);
   }
   __syncthreads();
   // 5. integer moments per run in closed form (tile-local coordinates, exact),

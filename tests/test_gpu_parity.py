@@ -382,14 +382,14 @@ def test_large_merge_path_synthetic(op, plan):
 
 def _step_digest(op, plan, res):
     r = plan.regions()
-    out = res.gaussians.numpy()
-    d = {k: res.report_arrays[k].cpu().numpy() for k in res.report_arrays}
-    d.update({f"out_{k}": v for k, v in out.items()})
-    d["index_map"] = res.index_map.cpu().numpy()
+    d = {}
     order = np.lexsort((r["minpix"].cpu().numpy(), r["band"].cpu().numpy(), r["view_pos"].cpu().numpy(),
                         r["candidate"].cpu().numpy()))
-    for k in ("candidate", "view_pos", "band", "minpix", "moments"):
+    for k in ("candidate", "view_pos", "band", "minpix", "moments", "valid"):
         d[f"reg_{k}"] = r[k].cpu().numpy()[order]
+    d.update({k: res.report_arrays[k].cpu().numpy() for k in res.report_arrays})
+    d.update({f"out_{k}": v for k, v in res.gaussians.numpy().items()})
+    d["index_map"] = res.index_map.cpu().numpy()
     return d
 
 
