@@ -178,16 +178,34 @@ __global__ void __launch_bounds__(kTileThreads) tile_kernel(TileParams P) {
   // 1. pre-erosion metric as row bitmasks: tile rows by ballot (lane = x),
   //    band on the tile itself; the (r-1)-pixel halo afterwards
   const int lane = tid & 31, wid = tid >> 5;
+  constexpr int kRowsPerWarp = kTileH / (kTileThreads / 32);
+  float fi[kRowsPerWarp][3], fg[kRowsPerWarp][3];
 #pragma unroll
-  for (int ty = wid; ty < kTileH; ty += kTileThreads / 32) {
+  for (int k = 0; k < kRowsPerWarp; ++k) {   // all loads of the warp's rows in flight at once
+    const int x = x0 + lane, y = y0 + wid + k * (kTileThreads / 32);
+    const bool inb = x < W && y < H;
+    const long long p = inb ? (long long)y * W + x : 0;
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      fi[k][c] = inb ? __ldg(img + 3 * p + c) : 0.0f;
+      fg[k][c] = inb ? __ldg(gtv + 3 * p + c) : 0.0f;
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < kRowsPerWarp; ++k) {
+    const int ty = wid + k * (kTileThreads / 32);
     const int x = x0 + lane, y = y0 + ty;
     bool m = false;
     unsigned char b = 0;
     if (x < W && y < H) {
-      const double xr = dsub(raw_l1(img, gtv, (long long)y * W + x), lo);
+      // np.abs(rendered - gt).sum(axis=-1) == (|d0| + |d1|) + |d2| in fp64, minus lo
+      const double raw = dadd(dadd(fabs(dsub((double)fi[k][0], (double)fg[k][0])),
+                                   fabs(dsub((double)fi[k][1], (double)fg[k][1]))),
+                              fabs(dsub((double)fi[k][2], (double)fg[k][2])));
+      const double xr = dsub(raw, lo);
       m = xr >= x_m;
       int bb = 0;
-      for (int k = 1; k < P.L; ++k) bb += xr >= thr[k];
+      for (int q = 1; q < P.L; ++q) bb += xr >= thr[q];
       b = (unsigned char)bb;
     }
     S.band[ty * kTileW + lane] = b;
@@ -255,9 +273,11 @@ __global__ void __launch_bounds__(kTileThreads) tile_kernel(TileParams P) {
     const int run0 = 31 - __clz(starts & (0xffffffffu >> (31 - tx)));
     S.d[p] = key;
     S.label[p] = key >= 0 ? ty * kTileW + run0 : -1;
-    S.touch[p] = 0;
+    if (key >= 0 && run0 == tx) {   // only run starts can become roots
+      S.touch[p] = 0;
 #pragma unroll
-    for (int k = 0; k < 6; ++k) S.mom[k][p] = 0;
+      for (int k = 0; k < 6; ++k) S.mom[k][p] = 0;
+    }
   }
   __syncthreads();
   // 4. run-level unions with the row above: 8-connectivity with equal

@@ -419,21 +419,70 @@ struct GroupStartPolicy {
   }
 };
 
-// one warp per group: member means, mean-covariance eigenbasis, reach
-__global__ void group_kernel(MergeArgs a, long long cap) {
-  const int lane = threadIdx.x & 31;
-  const long long warps = (long long)gridDim.x * (blockDim.x >> 5);
+constexpr int kSmallGroup = 8;
+
+// groups of up to kSmallGroup members: one thread per group, members summed in
+// ascending index order; also writes the sort padding beyond the group count
+__global__ void group_small_kernel(MergeArgs a, long long cap) {
   const long long G = (long long)a.ctr->n_groups_all;
-  for (long long g = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); g < cap; g += warps) {
+  for (long long g = (long long)blockIdx.x * blockDim.x + threadIdx.x; g < cap;
+       g += (long long)gridDim.x * blockDim.x) {
     if (g >= G) {
-      if (lane == 0) {
-        a.ext_key[g] = ~0ull;
-        a.ext_val[g] = (int)g;
-      }
+      a.ext_key[g] = ~0ull;
+      a.ext_val[g] = (int)g;
       continue;
     }
     const int b = a.grp_first[g], e = a.grp_first[g + 1];
     const int cnt = e - b;
+    if (cnt > kSmallGroup) continue;
+    double acc[12] = {0};
+    for (int m = b; m < e; ++m) {
+      const Proposal& M = a.props_s[a.gval_sorted[m]];
+      for (int t = 0; t < 3; ++t) {
+        acc[t] += M.mu[t];
+        acc[3 + t] += M.rgb[t];
+      }
+      for (int t = 0; t < 6; ++t) acc[6 + t] += M.cov[t];
+    }
+    GroupRec R;
+    for (int t = 0; t < 3; ++t) {
+      R.mu[t] = acc[t] / cnt;
+      R.rgb[t] = acc[3 + t] / cnt;
+    }
+    double mcov[6];
+    for (int t = 0; t < 6; ++t) mcov[t] = acc[6 + t] / cnt;
+    double lam0[3];
+    sym_eig3(mcov, lam0, R.evec);
+    double ext = 0.0;
+    for (int r = 0; r < 3; ++r) {
+      const double ev[3] = {R.evec[r], R.evec[3 + r], R.evec[6 + r]};
+      double best = 0.0;
+      for (int m = b; m < e; ++m) {
+        const Proposal& M = a.props_s[a.gval_sorted[m]];
+        const double off = fabs((M.mu[0] - R.mu[0]) * ev[0] + (M.mu[1] - R.mu[1]) * ev[1] +
+                                (M.mu[2] - R.mu[2]) * ev[2]);
+        best = fmax(best, off + sqrt(sym_quad(M.cov, ev)));
+      }
+      R.lam[r] = best * best;
+      ext = fmax(ext, R.lam[r]);
+    }
+    R.extent = ext;
+    a.groups[g] = R;
+    a.ext_key[g] = ~(unsigned long long)__double_as_longlong(ext);   // descending extent
+    a.ext_val[g] = (int)g;
+    atomicAdd(&a.n_groups[a.pcand[a.gkey_sorted[b]]], 1);
+  }
+}
+
+// larger groups: one warp per group, lane-strided sums + butterfly
+__global__ void group_kernel(MergeArgs a, long long cap) {
+  const int lane = threadIdx.x & 31;
+  const long long warps = (long long)gridDim.x * (blockDim.x >> 5);
+  const long long G = (long long)a.ctr->n_groups_all;
+  for (long long g = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); g < G; g += warps) {
+    const int b = a.grp_first[g], e = a.grp_first[g + 1];
+    const int cnt = e - b;
+    if (cnt <= kSmallGroup) continue;
     double acc[12] = {0};
     for (int m = b + lane; m < e; m += 32) {
       const Proposal& M = a.props_s[a.gval_sorted[m]];
@@ -482,6 +531,8 @@ __global__ void group_kernel(MergeArgs a, long long cap) {
 cudaError_t launch_merge_groups(const MergeArgs& a, long long cap, ScanState st, cudaStream_t s) {
   cudaError_t e = launch_scan(GroupStartPolicy{a}, cap, st, s);
   if (e != cudaSuccess) return e;
+  long long b = (cap + 127) / 128;
+  group_small_kernel<<<(unsigned)(b < 1 ? 1 : (b > 65535 ? 65535 : b)), 128, 0, s>>>(a, cap);
   group_kernel<<<a.grid, 256, 0, s>>>(a, cap);
   return cudaGetLastError();
 }

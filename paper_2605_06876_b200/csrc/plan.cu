@@ -752,7 +752,7 @@ extern "C" adps_status adps_step_phase1(adps_plan* P, void* stream_v, const adps
       const int gbits = ceil_log2((unsigned long long)rc + 2);
       CK(cub_sort_pairs(P, ma.gkey, ma.gkey_sorted, ma.gval, ma.gval_sorted, rc, gbits, s));
       CK(launch_merge_groups(ma, rc, sst3, s));
-      mark(P, "merge_groups", s, 3);
+      mark(P, "merge_groups", s, 4);
       CK(cub_sort_pairs(P, ma.ext_key, ma.ext_key_sorted, ma.ext_val, ma.ext_val_sorted, rc, 64, s));
       CK(launch_merge_cap(ma, rc, s));
       const int cbits = ceil_log2((unsigned long long)n_split + 2);
