@@ -152,44 +152,39 @@ __global__ void __launch_bounds__(kTileThreads) tile_kernel(TileParams P) {
     S.n_part = 0;
     S.n_reg = 0;
   }
-  // 0. dominant map: candidate id per pixel, ever-dominant flags over ALL
-  //    pixels (ref/adc.py:177-180).  Tiles without any split-candidate pixel
-  //    cannot hold a region: they skip the image/gt reads entirely.
-  int n_cand = 0;
-#pragma unroll
-  for (int p = tid; p < kTilePx; p += kTileThreads) {
-    const int x = x0 + p % kTileW, y = y0 + p / kTileW;
-    int c = -1;
-    if (x < W && y < H) {
-      const int dd = __ldg(dom + (long long)y * W + x);
-      if (dd >= 0 && dd < P.N && __ldg(P.cls + dd) == 1) {
-        if (P.dom_flag[dd] == 0) P.dom_flag[dd] = 1;   // idempotent, race-benign
-        c = dd;
-      }
-    }
-    S.d[p] = c;
-    n_cand += c >= 0;
-  }
-  if (__syncthreads_count(n_cand) == 0 && !P.dbg_m) {
-    int* border = P.border + (long long)blockIdx.x * kBorderSlots;
-    for (int s = tid; s < kBorderSlots; s += kTileThreads) border[s] = -1;
-    return;
-  }
-  // 1. pre-erosion metric as row bitmasks: tile rows by ballot (lane = x),
-  //    band on the tile itself; the (r-1)-pixel halo afterwards
+  // 0+1. each warp owns 4 tile rows (lane = x): dominant map, image and gt of
+  //    all its rows are loaded at once; candidate ids and ever-dominant flags
+  //    (over ALL pixels, ref/adc.py:177-180) once per run of equal dominant id;
+  //    pre-erosion metric as row bitmasks (ballot) and band per pixel.
   const int lane = tid & 31, wid = tid >> 5;
   constexpr int kRowsPerWarp = kTileH / (kTileThreads / 32);
   float fi[kRowsPerWarp][3], fg[kRowsPerWarp][3];
+  int dd[kRowsPerWarp];
 #pragma unroll
-  for (int k = 0; k < kRowsPerWarp; ++k) {   // all loads of the warp's rows in flight at once
+  for (int k = 0; k < kRowsPerWarp; ++k) {
     const int x = x0 + lane, y = y0 + wid + k * (kTileThreads / 32);
     const bool inb = x < W && y < H;
     const long long p = inb ? (long long)y * W + x : 0;
+    dd[k] = inb ? __ldg(dom + p) : -1;
 #pragma unroll
     for (int c = 0; c < 3; ++c) {
       fi[k][c] = inb ? __ldg(img + 3 * p + c) : 0.0f;
       fg[k][c] = inb ? __ldg(gtv + 3 * p + c) : 0.0f;
     }
+  }
+  int n_cand = 0;
+#pragma unroll
+  for (int k = 0; k < kRowsPerWarp; ++k) {
+    const int ty = wid + k * (kTileThreads / 32);
+    const int left = __shfl_up_sync(0xffffffffu, dd[k], 1);
+    const bool head = lane == 0 || left != dd[k];
+    bool isc = false;
+    if (head && dd[k] >= 0 && dd[k] < P.N) isc = __ldg(P.cls + dd[k]) == 1;
+    const unsigned heads = __ballot_sync(0xffffffffu, head);
+    isc = __shfl_sync(0xffffffffu, isc, 31 - __clz(heads & (0xffffffffu >> (31 - lane))));
+    if (isc && head && P.dom_flag[dd[k]] == 0) P.dom_flag[dd[k]] = 1;   // idempotent, race-benign
+    S.d[ty * kTileW + lane] = isc ? dd[k] : -1;
+    n_cand += isc;
   }
 #pragma unroll
   for (int k = 0; k < kRowsPerWarp; ++k) {
@@ -211,6 +206,12 @@ __global__ void __launch_bounds__(kTileThreads) tile_kernel(TileParams P) {
     S.band[ty * kTileW + lane] = b;
     const unsigned bits = __ballot_sync(0xffffffffu, m);
     if (lane == 0) S.mrow[ty + hl] = (unsigned long long)bits << hl;
+  }
+  // a tile without split-candidate pixels cannot hold a region
+  if (__syncthreads_count(n_cand) == 0 && !P.dbg_m) {
+    int* border = P.border + (long long)blockIdx.x * kBorderSlots;
+    for (int s = tid; s < kBorderSlots; s += kTileThreads) border[s] = -1;
+    return;
   }
   if (r > 1) {
     if (tid < hl + hh) S.mrow[tid < hl ? tid : kTileH + tid] = 0ull;   // halo rows start empty
@@ -235,16 +236,17 @@ __global__ void __launch_bounds__(kTileThreads) tile_kernel(TileParams P) {
   }
   __syncthreads();
   // 2. r x r erosion on the bitmasks (offsets -(r//2) .. r-r//2-1; outside = 0)
-  if (tid < kTileH) {
+  if (lane < kRowsPerWarp) {   // every warp erodes its own 4 rows
+    const int row0 = wid + lane * (kTileThreads / 32);
     const int span = hl + hh;
     unsigned long long acc = ~0ull;
     for (int dy = 0; dy <= span; ++dy) {
-      const unsigned long long row = S.mrow[tid + dy];
+      const unsigned long long row = S.mrow[row0 + dy];
       unsigned long long h = row;
       for (int dx = 1; dx <= span; ++dx) h &= row >> dx;
       acc &= h;
     }
-    S.erow[tid] = (unsigned)acc;
+    S.erow[row0] = (unsigned)acc;
   }
   __syncthreads();
   // 3. keys + ever-dominant flags; each warp owns whole 32-px rows (lane = x),
