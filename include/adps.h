@@ -159,6 +159,19 @@ ADPS_API adps_status adps_step_phase1(adps_plan* plan, void* stream, const adps_
                              const float* image, const float* gt, const int32_t* dominant,
                              adps_counts* counts);
 
+/* Split form of phase 1 for overlap: _begin runs select and the
+ * ever-dominant flags (ref/adc.py:165, 177-180), synchronises once and
+ * fills counts->n_split, n_clone and n_fallback, so the host can draw the
+ * 6*n_fallback normals from its Generator while _end runs the rest of
+ * phase 1 on the GPU.  Same arguments as adps_step_phase1, which is
+ * exactly _begin followed by _end. */
+ADPS_API adps_status adps_step_phase1_begin(adps_plan* plan, void* stream, const adps_gaussians* g, int64_t n,
+                             double extent, const double* grad_accum, const double* denom,
+                             const adps_config* cfg, const double* cams_host, int32_t n_views,
+                             const float* image, const float* gt, const int32_t* dominant,
+                             adps_counts* counts);
+ADPS_API adps_status adps_step_phase1_end(adps_plan* plan, void* stream, adps_counts* counts);
+
 /* Phase 2 (ref/adc.py:198-244): emit children, parent copies, fallback
  * children, clones and survivors into caller-allocated arrays of
  * counts.n_out rows plus index_map (old index or -1).

@@ -56,7 +56,7 @@ class Report(C.Structure):
 
 EXPORTS = (
     "adps_abi_version", "adps_last_error", "adps_plan_create", "adps_plan_destroy", "adps_render",
-    "adps_step_phase1", "adps_step_phase2", "adps_get_report", "adps_get_regions",
+    "adps_step_phase1", "adps_step_phase1_begin", "adps_step_phase1_end", "adps_step_phase2", "adps_get_report", "adps_get_regions",
     "adps_set_debug_records", "adps_set_debug_maps", "adps_set_timing", "adps_get_timing",
     "adps_accumulate_stats", "adps_get_launch_count", "adps_set_param",
 )
@@ -81,6 +81,8 @@ def load(path: str = LIB_PATH):
     lib.adps_render.argtypes = [vp, vp, C.POINTER(Gaussians), C.c_int64, vp, C.c_int32, vp, vp, vp]
     lib.adps_step_phase1.argtypes = [vp, vp, C.POINTER(Gaussians), C.c_int64, C.c_double, vp, vp,
                                      C.POINTER(Config), vp, C.c_int32, vp, vp, vp, C.POINTER(Counts)]
+    lib.adps_step_phase1_begin.argtypes = lib.adps_step_phase1.argtypes
+    lib.adps_step_phase1_end.argtypes = [vp, vp, C.POINTER(Counts)]
     lib.adps_step_phase2.argtypes = [vp, vp, C.POINTER(Gaussians), vp, C.POINTER(GaussiansOut), vp]
     lib.adps_get_report.argtypes = [vp, C.POINTER(Report)]
     lib.adps_get_regions.argtypes = [vp] + [C.POINTER(vp)] * 5 + [C.POINTER(C.c_int64)]

@@ -100,6 +100,7 @@ struct Counters {
   unsigned long long n_small;
   unsigned long long n_groups_all;
   unsigned long long n_tile_pairs;
+  unsigned long long n_fallback_pre;
   unsigned int degenerate;
   unsigned int overflow;   // bit0 regions, bit1 partials
 };

@@ -112,6 +112,42 @@ __global__ void thresholds_kernel(const unsigned long long* __restrict__ lohi, i
   thr[t] = min_true(d, k, tau, omt, (double)L);
 }
 
+// ---------------------------------------------------- ever-dominant (early)
+// ever_dominant[i] = any sampled pixel has D == i (ref/adc.py:177-180), for
+// split candidates; one check/store per run of equal ids along a warp's 32
+// consecutive pixels.  Runs first so the host learns the fallback count (and
+// can draw its normals) while the rest of phase 1 runs on the GPU.
+__global__ void dominance_kernel(const int* __restrict__ dom, long long n_px, const unsigned char* __restrict__ cls,
+                                 int N, unsigned char* __restrict__ dom_flag) {
+  const int lane = threadIdx.x & 31;
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long base = (long long)blockIdx.x * blockDim.x; base < n_px; base += stride) {
+    const long long p = base + threadIdx.x;
+    const int d = p < n_px ? __ldg(dom + p) : -1;
+    const int left = __shfl_up_sync(0xffffffffu, d, 1);
+    if ((lane == 0 || left != d) && d >= 0 && d < N && __ldg(cls + d) == 1 && dom_flag[d] == 0) dom_flag[d] = 1;
+  }
+}
+
+__global__ void fallback_count_kernel(const int* __restrict__ split_list, const unsigned char* __restrict__ dom_flag,
+                                      Counters* ctr) {
+  const long long n = (long long)ctr->n_split;
+  int c = 0;
+  for (long long k = (long long)blockIdx.x * blockDim.x + threadIdx.x; k < n; k += (long long)gridDim.x * blockDim.x)
+    c += dom_flag[split_list[k]] == 0;
+  for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+  if ((threadIdx.x & 31) == 0 && c) atomicAdd(&ctr->n_fallback_pre, (unsigned long long)c);
+}
+
+cudaError_t launch_dominance(const int* dom, long long n_px, const unsigned char* cls, int N, unsigned char* dom_flag,
+                             const int* split_list, Counters* ctr, int sm_count, cudaStream_t s) {
+  long long b = (n_px + 255) / 256;
+  const long long cap = (long long)sm_count * 16;
+  dominance_kernel<<<(unsigned)(b < 1 ? 1 : (b > cap ? cap : b)), 256, 0, s>>>(dom, n_px, cls, N, dom_flag);
+  fallback_count_kernel<<<sm_count * 2, 256, 0, s>>>(split_list, dom_flag, ctr);
+  return cudaGetLastError();
+}
+
 // ----------------------------------------------------------------- tile pass
 struct TileSmem {
   unsigned long long mrow[kTileH + 2 * kMaxErodeHalo];   // pre-erosion m of haloed rows, bit = x - x0 + hl
@@ -182,7 +218,6 @@ __global__ void __launch_bounds__(kTileThreads) tile_kernel(TileParams P) {
     if (head && dd[k] >= 0 && dd[k] < P.N) isc = __ldg(P.cls + dd[k]) == 1;
     const unsigned heads = __ballot_sync(0xffffffffu, head);
     isc = __shfl_sync(0xffffffffu, isc, 31 - __clz(heads & (0xffffffffu >> (31 - lane))));
-    if (isc && head && P.dom_flag[dd[k]] == 0) P.dom_flag[dd[k]] = 1;   // idempotent, race-benign
     S.d[ty * kTileW + lane] = isc ? dd[k] : -1;
     n_cand += isc;
   }

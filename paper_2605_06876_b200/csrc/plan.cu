@@ -115,6 +115,18 @@ struct adps_plan {
   long long launches = 0;
   long long lib_calls = 0;
   int large_threshold = 32;
+  // arguments saved by phase1_begin for phase1_end
+  bool have_begin = false;
+  struct {
+    adps_gaussians g;
+    long long n;
+    double extent;
+    adps_config cfg;
+    int V, H, W;
+    const float* image;
+    const float* gt;
+    const int32_t* dominant;
+  } cx{};
 };
 
 static void mark(adps_plan* P, const char* name, cudaStream_t s, int kernels) {
@@ -381,7 +393,6 @@ static adps_status run_attribution(adps_plan* P, cudaStream_t s, int V, int H, i
     P->lohi_host[2 * v + 1] = 0ull;                // +0.0
   }
   CK(cudaMemcpyAsync(P->lohi.p, P->lohi_host, sizeof(unsigned long long) * 2 * V, cudaMemcpyHostToDevice, s));
-  CK(cudaMemsetAsync(P->dom_flag.p, 0, (size_t)(N > 0 ? N : 1), s));
   Counters* ctr = P->ctr.as<Counters>();
   CK(cudaMemsetAsync(&ctr->n_regions, 0, sizeof(unsigned long long), s));
   CK(cudaMemsetAsync(&ctr->n_partials, 0, sizeof(unsigned long long), s));
@@ -425,8 +436,20 @@ extern "C" adps_status adps_step_phase1(adps_plan* P, void* stream_v, const adps
                                         const adps_config* cfg, const double* cams_host, int32_t n_views,
                                         const float* image, const float* gt, const int32_t* dominant,
                                         adps_counts* counts) {
+  adps_status st = adps_step_phase1_begin(P, stream_v, g, n, extent, grad_accum, denom, cfg, cams_host, n_views,
+                                          image, gt, dominant, counts);
+  if (st != ADPS_OK) return st;
+  return adps_step_phase1_end(P, stream_v, counts);
+}
+
+extern "C" adps_status adps_step_phase1_begin(adps_plan* P, void* stream_v, const adps_gaussians* g, int64_t n,
+                                              double extent, const double* grad_accum, const double* denom,
+                                              const adps_config* cfg, const double* cams_host, int32_t n_views,
+                                              const float* image, const float* gt, const int32_t* dominant,
+                                              adps_counts* counts) {
   if (!P) return fail(ADPS_INVALID_ARG, "plan is NULL");
   P->have_phase1 = false;
+  P->have_begin = false;
   adps_status st = check_gaussians(g, n);
   if (st != ADPS_OK) return st;
   if (!cfg || !counts) return fail(ADPS_INVALID_ARG, "cfg/counts is NULL");
@@ -495,7 +518,7 @@ extern "C" adps_status adps_step_phase1(adps_plan* P, void* stream_v, const adps
   mark_start(P, s, true);
 
   // ---- select (ref/adc.py:165)
-  ScanState sst, sst2;
+  ScanState sst;
   st = scan_state(P, P->scan_val, P->scan_flag, P->scan_ticket, nn, &sst);
   if (st != ADPS_OK) return st;
   SelectArgs sa;
@@ -513,7 +536,65 @@ extern "C" adps_status adps_step_phase1(adps_plan* P, void* stream_v, const adps
   CK(launch_select(sa, sst, s));
   mark(P, "select", s, 1);
 
-  // ---- maps + partition + moments + ever-dominant (ref/adc.py:168-180)
+  // ---- ever-dominant flags (ref/adc.py:177-180) and the fallback count, so
+  //      the host can draw the fallback normals while the rest runs
+  CK(cudaMemsetAsync(P->dom_flag.p, 0, (size_t)nn, s));
+  CK(launch_dominance(dominant, total_px, P->cls.as<unsigned char>(), N, P->dom_flag.as<unsigned char>(),
+                      P->split_list.as<int>(), ctr, P->sm_count, s));
+  mark(P, "dominance", s, 2);
+  CK(cudaMemcpyAsync(P->ctr_host, ctr, sizeof(Counters), cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  {
+    adps_counts K{};
+    K.n_before = n;
+    K.n_split = (long long)P->ctr_host->n_split;
+    K.n_clone = (long long)P->ctr_host->n_clone;
+    K.n_fallback = (long long)P->ctr_host->n_fallback_pre;
+    *counts = K;
+  }
+  P->cx.g = *g;
+  P->cx.n = n;
+  P->cx.extent = extent;
+  P->cx.cfg = *cfg;
+  P->cx.V = V;
+  P->cx.H = H;
+  P->cx.W = W;
+  P->cx.image = image;
+  P->cx.gt = gt;
+  P->cx.dominant = dominant;
+  P->have_begin = true;
+  return ADPS_OK;
+}
+
+extern "C" adps_status adps_step_phase1_end(adps_plan* P, void* stream_v, adps_counts* counts) {
+  if (!P || !counts) return fail(ADPS_INVALID_ARG, "NULL argument");
+  if (!P->have_begin) return fail(ADPS_BAD_STATE, "phase1_end without phase1_begin");
+  P->have_begin = false;
+  CK(cudaSetDevice(P->device));
+  cudaStream_t s = (cudaStream_t)stream_v;
+  adps_status st = ADPS_OK;
+  const adps_gaussians* g = &P->cx.g;
+  const long long n = P->cx.n;
+  const double extent = P->cx.extent;
+  const adps_config* cfg = &P->cx.cfg;
+  const int V = P->cx.V, H = P->cx.H, W = P->cx.W;
+  const float* image = P->cx.image;
+  const float* gt = P->cx.gt;
+  const int32_t* dominant = P->cx.dominant;
+  const long long hw = (long long)H * W;
+  const long long total_px = hw * V;
+  const int tiles_x = (W + kTileW - 1) / kTileW, tiles_y = (H + kTileH - 1) / kTileH;
+  const long long n_tiles = (long long)tiles_x * tiles_y * V;
+  const int N = (int)n;
+  const long long nn = n > 0 ? n : 1;
+  const long long region_bound = total_px / (cfg->m_min > 1 ? cfg->m_min : 1) + 1;
+  const long long partial_bound = n_tiles * (2 * kTileW + 2 * kTileH) + 1;
+  Counters* ctr = P->ctr.as<Counters>();
+  ScanState sst, sst2;
+  st = scan_state(P, P->scan_val, P->scan_flag, P->scan_ticket, nn, &sst);
+  if (st != ADPS_OK) return st;
+
+  // ---- maps + partition + moments (ref/adc.py:168-176)
   for (int attempt = 0;; ++attempt) {
     st = run_attribution(P, s, V, H, W, cfg, N, image, gt, dominant);
     if (st != ADPS_OK) return st;

@@ -19,6 +19,7 @@ every entry point raises.
 from __future__ import annotations
 
 import ctypes as C
+import threading
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -230,6 +231,25 @@ class Plan:
         _abi.check(st)
         return counts.as_dict()
 
+    def phase1_begin(self, g, extent, grad_accum, denom, cfg, cams_v, image, gt, dom) -> dict:
+        """select + ever-dominant flags; returns n_split/n_clone/n_fallback after one sync."""
+        cams_v = camera_rows(cams_v)
+        counts = _abi.Counts()
+        cs = config_struct(cfg)
+        ga = g.abi()
+        self._g_keep = (g, grad_accum, denom, image, gt, dom)
+        _abi.check(self.lib.adps_step_phase1_begin(self._h, self._stream(), C.byref(ga), g.n, float(extent),
+                                                   _ptr(grad_accum), _ptr(denom), C.byref(cs),
+                                                   cams_v.ctypes.data_as(C.c_void_p), len(cams_v), _ptr(image),
+                                                   _ptr(gt), _ptr(dom), C.byref(counts)))
+        return counts.as_dict()
+
+    def phase1_end(self) -> dict:
+        """The rest of phase 1 (maps ... offsets); releases the GIL while the GPU works."""
+        counts = _abi.Counts()
+        _abi.check(self.lib.adps_step_phase1_end(self._h, self._stream(), C.byref(counts)))
+        return counts.as_dict()
+
     def phase2(self, g, normals, out: GaussianTensors, index_map: torch.Tensor):
         ga = g.abi()
         oa = _abi.GaussiansOut(out.mu.data_ptr(), out.scale.data_ptr(), out.rot.data_ptr(),
@@ -389,11 +409,28 @@ def densify_step(g: GaussianTensors, extent: float, cameras, gt, grad_accum: tor
         image = image.to(dev, F32).contiguous()
         dom = dom.to(dev, torch.int32).contiguous()
     gt_v = _gather_views(gt, view_ids, dev)
-    counts = plan.phase1(g, extent, grad_accum.to(dev, F64).contiguous(), denom.to(dev, F64).contiguous(),
-                         cfg, cams_v, image, gt_v, dom)
+    counts = plan.phase1_begin(g, extent, grad_accum.to(dev, F64).contiguous(), denom.to(dev, F64).contiguous(),
+                               cfg, cams_v, image, gt_v, dom)
     nf = counts["n_fallback"]
-    normals_np = rng.standard_normal(6 * nf) if nf > 0 else np.zeros(0)
-    normals = torch.as_tensor(normals_np, dtype=F64, device=dev) if nf > 0 else None
+    # the caller's Generator draws 3 normals per fallback child in ascending
+    # parent order (ref/adc.py:97); the stream is chunk-invariant, so one call
+    # for 6F values is identical.  It runs on a host thread while the GPU
+    # finishes phase 1 (the C call releases the GIL).
+    drawn = {}
+
+    def _draw():
+        drawn["z"] = rng.standard_normal(6 * nf) if nf > 0 else np.zeros(0)
+
+    th = threading.Thread(target=_draw)
+    th.start()
+    try:
+        counts = plan.phase1_end()
+    finally:
+        th.join()
+    if counts["n_fallback"] != nf:
+        raise RuntimeError("fallback count changed between phase-1 halves")
+    normals_np = drawn["z"]
+    normals = torch.from_numpy(normals_np).to(dev) if nf > 0 else None
     n_out = counts["n_out"]
     if out is None:
         out = GaussianTensors.empty(n_out, g.sh_k, dev)
