@@ -63,14 +63,14 @@ struct Proposal {
   double cov[6];    // xx xy xz yy yz zz
   double prec[6];
   double rgb[3];
-  double smax;      // max(s1, s2): sqrt of the largest covariance eigenvalue
+  double inv_smax;  // 1 / max(s1, s2): 1/sqrt of the largest covariance eigenvalue
 };
 
 // Bounding data of 64 spatially sorted proposals (exact gate pruning).
 struct TileBox {
   double c[3];      // centre
   double r;         // max |mu - c|
-  double smax;      // max proposal smax
+  double inv_s;     // min proposal inv_smax
   double lo[3], hi[3];   // rgb box
 };
 

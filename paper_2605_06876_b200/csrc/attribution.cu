@@ -33,24 +33,38 @@ __device__ __forceinline__ double raw_l1(const float* __restrict__ img, const fl
   return dadd(dadd(a0, a1), a2);
 }
 
+// Per-view min/max of the raw L1 error and, in the same pass over the view,
+// the ever-dominant flags of split candidates (ref/adc.py:177-180): every
+// input byte of the view (image, gt, dominant map) is read exactly once.
 __global__ void minmax_kernel(const float* __restrict__ image, const float* __restrict__ gt,
-                              long long hw, unsigned long long* __restrict__ lohi) {
+                              const int* __restrict__ dominant, long long hw, unsigned long long* __restrict__ lohi,
+                              const unsigned char* __restrict__ cls, int N, unsigned char* __restrict__ dom_flag) {
   const int v = blockIdx.y;
   const float* img = image + (long long)v * hw * 3;
   const float* g = gt + (long long)v * hw * 3;
+  const int* dom = dominant + (long long)v * hw;
+  const int lane = threadIdx.x & 31;
   double lo = INFINITY, hi = 0.0;
-  for (long long p = (long long)blockIdx.x * blockDim.x + threadIdx.x; p < hw;
-       p += (long long)gridDim.x * blockDim.x) {
-    double r = raw_l1(img, g, p);
-    lo = fmin(lo, r);
-    hi = fmax(hi, r);
+  for (long long base = (long long)blockIdx.x * blockDim.x; base < hw; base += (long long)gridDim.x * blockDim.x) {
+    const long long p = base + threadIdx.x;
+    int d = -1;
+    if (p < hw) {
+      const double r = raw_l1(img, g, p);
+      lo = fmin(lo, r);
+      hi = fmax(hi, r);
+      d = __ldg(dom + p);
+    }
+    if (dom_flag) {
+      const int left = __shfl_up_sync(0xffffffffu, d, 1);
+      if ((lane == 0 || left != d) && d >= 0 && d < N && __ldg(cls + d) == 1 && dom_flag[d] == 0) dom_flag[d] = 1;
+    }
   }
   for (int o = 16; o > 0; o >>= 1) {
     lo = fmin(lo, __shfl_xor_sync(0xffffffffu, lo, o));
     hi = fmax(hi, __shfl_xor_sync(0xffffffffu, hi, o));
   }
   __shared__ double slo[32], shi[32];
-  int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int wid = threadIdx.x >> 5;
   if (lane == 0) {
     slo[wid] = lo;
     shi[wid] = hi;
@@ -117,18 +131,6 @@ __global__ void thresholds_kernel(const unsigned long long* __restrict__ lohi, i
 // split candidates; one check/store per run of equal ids along a warp's 32
 // consecutive pixels.  Runs first so the host learns the fallback count (and
 // can draw its normals) while the rest of phase 1 runs on the GPU.
-__global__ void dominance_kernel(const int* __restrict__ dom, long long n_px, const unsigned char* __restrict__ cls,
-                                 int N, unsigned char* __restrict__ dom_flag) {
-  const int lane = threadIdx.x & 31;
-  const long long stride = (long long)gridDim.x * blockDim.x;
-  for (long long base = (long long)blockIdx.x * blockDim.x; base < n_px; base += stride) {
-    const long long p = base + threadIdx.x;
-    const int d = p < n_px ? __ldg(dom + p) : -1;
-    const int left = __shfl_up_sync(0xffffffffu, d, 1);
-    if ((lane == 0 || left != d) && d >= 0 && d < N && __ldg(cls + d) == 1 && dom_flag[d] == 0) dom_flag[d] = 1;
-  }
-}
-
 __global__ void fallback_count_kernel(const int* __restrict__ split_list, const unsigned char* __restrict__ dom_flag,
                                       Counters* ctr) {
   const long long n = (long long)ctr->n_split;
@@ -137,15 +139,6 @@ __global__ void fallback_count_kernel(const int* __restrict__ split_list, const 
     c += dom_flag[split_list[k]] == 0;
   for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
   if ((threadIdx.x & 31) == 0 && c) atomicAdd(&ctr->n_fallback_pre, (unsigned long long)c);
-}
-
-cudaError_t launch_dominance(const int* dom, long long n_px, const unsigned char* cls, int N, unsigned char* dom_flag,
-                             const int* split_list, Counters* ctr, int sm_count, cudaStream_t s) {
-  long long b = (n_px + 255) / 256;
-  const long long cap = (long long)sm_count * 16;
-  dominance_kernel<<<(unsigned)(b < 1 ? 1 : (b > cap ? cap : b)), 256, 0, s>>>(dom, n_px, cls, N, dom_flag);
-  fallback_count_kernel<<<sm_count * 2, 256, 0, s>>>(split_list, dom_flag, ctr);
-  return cudaGetLastError();
 }
 
 // ----------------------------------------------------------------- tile pass
@@ -533,14 +526,19 @@ __global__ void partial_emit_kernel(const PartialRec* __restrict__ partials, con
 // --------------------------------------------------------------- launchers
 size_t tile_smem_bytes() { return sizeof(TileSmem); }
 
-cudaError_t launch_attribution(const AttributionArgs& a, cudaStream_t s, MarkFn mark, void* ctx) {
+cudaError_t launch_minmax(const AttributionArgs& a, const int* split_list, Counters* ctr, int sm_count,
+                          cudaStream_t s) {
   const long long hw = (long long)a.H * a.W;
   dim3 mg((unsigned)((hw + 256 * 8 - 1) / (256 * 8)), (unsigned)a.V);
   if (mg.x > 1024) mg.x = 1024;
-  minmax_kernel<<<mg, 256, 0, s>>>(a.image, a.gt, hw, a.lohi);
+  minmax_kernel<<<mg, 256, 0, s>>>(a.image, a.gt, a.dom, hw, a.lohi, a.cls, a.N, a.dom_flag);
   int nt = a.V * a.L;
   thresholds_kernel<<<(nt + 127) / 128, 128, 0, s>>>(a.lohi, a.V, a.L, a.tau, a.lo, a.thr);
-  if (mark) mark(ctx, "minmax", s, 2);
+  fallback_count_kernel<<<sm_count * 2, 256, 0, s>>>(split_list, a.dom_flag, ctr);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_attribution(const AttributionArgs& a, cudaStream_t s, MarkFn mark, void* ctx) {
   TileParams P;
   P.image = a.image;
   P.gt = a.gt;

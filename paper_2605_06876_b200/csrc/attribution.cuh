@@ -66,8 +66,9 @@ struct AttributionArgs {
 };
 
 size_t tile_smem_bytes();
-cudaError_t launch_dominance(const int* dom, long long n_px, const unsigned char* cls, int N, unsigned char* dom_flag,
-                             const int* split_list, Counters* ctr, int sm_count, cudaStream_t s);
+// minmax + ever-dominant flags + thresholds + fallback count (phase-1 begin)
+cudaError_t launch_minmax(const AttributionArgs& a, const int* split_list, Counters* ctr, int sm_count,
+                          cudaStream_t s);
 // Called after each group of launches: name, stream, number of kernels launched.
 typedef void (*MarkFn)(void* ctx, const char* name, cudaStream_t s, int kernels);
 cudaError_t launch_attribution(const AttributionArgs& a, cudaStream_t s, MarkFn mark, void* ctx);

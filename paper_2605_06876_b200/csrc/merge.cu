@@ -30,7 +30,7 @@ __device__ __forceinline__ bool gate(const Proposal& A, const Proposal& B, doubl
   // exact early reject: d >= |dl| (1/smax_a + 1/smax_b) (largest covariance eigenvalue
   // is smax^2); a 1e-9 relative guard keeps it strictly conservative
   const double n2 = dl[0] * dl[0] + dl[1] * dl[1] + dl[2] * dl[2];
-  const double w = 1.0 / A.smax + 1.0 / B.smax;
+  const double w = A.inv_smax + B.inv_smax;
   if (n2 * w * w > gd * gd * (1.0 + 1e-9)) return false;
   const double d = sqrt(fmax(sym_quad(A.prec, dl), 0.0)) + sqrt(fmax(sym_quad(B.prec, dl), 0.0));
   return d <= gd;
@@ -255,7 +255,7 @@ __global__ void box_kernel(MergeArgs a) {
     const long long tl = t - (long long)a.tile_off[l];
     const long long b = (long long)a.lp_off[l] + tl * 64;
     const long long e = min(b + 64, (long long)(a.lp_off[l] + a.lp_cnt[l]));
-    double s[3] = {0, 0, 0}, smax = 0.0, lo[3] = {1e300, 1e300, 1e300}, hi[3] = {-1e300, -1e300, -1e300};
+    double s[3] = {0, 0, 0}, inv_s = 1e300, lo[3] = {1e300, 1e300, 1e300}, hi[3] = {-1e300, -1e300, -1e300};
     for (long long m = b + lane; m < e; m += 32) {
       const Proposal& M = a.props_s[a.mval_sorted[m]];
       for (int c = 0; c < 3; ++c) {
@@ -263,7 +263,7 @@ __global__ void box_kernel(MergeArgs a) {
         lo[c] = fmin(lo[c], M.rgb[c]);
         hi[c] = fmax(hi[c], M.rgb[c]);
       }
-      smax = fmax(smax, M.smax);
+      inv_s = fmin(inv_s, M.inv_smax);
     }
     for (int o = 16; o > 0; o >>= 1) {
       for (int c = 0; c < 3; ++c) {
@@ -271,7 +271,7 @@ __global__ void box_kernel(MergeArgs a) {
         lo[c] = fmin(lo[c], __shfl_xor_sync(0xffffffffu, lo[c], o));
         hi[c] = fmax(hi[c], __shfl_xor_sync(0xffffffffu, hi[c], o));
       }
-      smax = fmax(smax, __shfl_xor_sync(0xffffffffu, smax, o));
+      inv_s = fmin(inv_s, __shfl_xor_sync(0xffffffffu, inv_s, o));
     }
     const double cnt = (double)(e - b);
     const double cen[3] = {s[0] / cnt, s[1] / cnt, s[2] / cnt};
@@ -290,7 +290,7 @@ __global__ void box_kernel(MergeArgs a) {
         B.hi[c] = hi[c];
       }
       B.r = r * (1.0 + 1e-12) + 1e-300;   // rounding guard: the sphere really encloses
-      B.smax = smax;
+      B.inv_s = inv_s;
       a.boxes[t] = B;
     }
   }
@@ -302,7 +302,7 @@ __device__ __forceinline__ bool boxes_may_merge(const TileBox& A, const TileBox&
   const double dx = A.c[0] - B.c[0], dy = A.c[1] - B.c[1], dz = A.c[2] - B.c[2];
   const double dmin = sqrt(dx * dx + dy * dy + dz * dz) - A.r - B.r;
   if (dmin <= 0.0) return true;
-  const double lb = dmin / A.smax + dmin / B.smax;
+  const double lb = dmin * (A.inv_s + B.inv_s);
   return !(lb > gd * (1.0 + 1e-9));
 }
 

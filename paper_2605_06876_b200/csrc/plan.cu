@@ -386,17 +386,9 @@ extern "C" adps_status adps_render(adps_plan* P, void* stream_v, const adps_gaus
 
 // ------------------------------------------------------------------ phase 1
 
-static adps_status run_attribution(adps_plan* P, cudaStream_t s, int V, int H, int W, const adps_config* cfg,
-                                   int N, const float* image, const float* gt, const int32_t* dominant) {
-  for (int v = 0; v < V; ++v) {
-    P->lohi_host[2 * v] = 0x7ff0000000000000ull;   // +inf
-    P->lohi_host[2 * v + 1] = 0ull;                // +0.0
-  }
-  CK(cudaMemcpyAsync(P->lohi.p, P->lohi_host, sizeof(unsigned long long) * 2 * V, cudaMemcpyHostToDevice, s));
+static AttributionArgs attr_args(adps_plan* P, int V, int H, int W, const adps_config* cfg, int N,
+                                 const float* image, const float* gt, const int32_t* dominant) {
   Counters* ctr = P->ctr.as<Counters>();
-  CK(cudaMemsetAsync(&ctr->n_regions, 0, sizeof(unsigned long long), s));
-  CK(cudaMemsetAsync(&ctr->n_partials, 0, sizeof(unsigned long long), s));
-  CK(cudaMemsetAsync(&ctr->overflow, 0, sizeof(unsigned int), s));
   AttributionArgs a;
   a.image = image;
   a.gt = gt;
@@ -427,6 +419,17 @@ static adps_status run_attribution(adps_plan* P, cudaStream_t s, int V, int H, i
   a.dbg_b = P->dbg_b;
   a.overflow = &ctr->overflow;
   a.grid_small = (unsigned)(P->sm_count * 4);
+  return a;
+}
+
+// tile CCL + border merge (after the per-view thresholds exist)
+static adps_status run_attribution(adps_plan* P, cudaStream_t s, int V, int H, int W, const adps_config* cfg,
+                                   int N, const float* image, const float* gt, const int32_t* dominant) {
+  Counters* ctr = P->ctr.as<Counters>();
+  CK(cudaMemsetAsync(&ctr->n_regions, 0, sizeof(unsigned long long), s));
+  CK(cudaMemsetAsync(&ctr->n_partials, 0, sizeof(unsigned long long), s));
+  CK(cudaMemsetAsync(&ctr->overflow, 0, sizeof(unsigned int), s));
+  const AttributionArgs a = attr_args(P, V, H, W, cfg, N, image, gt, dominant);
   CK(launch_attribution(a, s, mark_cb, P));
   return ADPS_OK;
 }
@@ -539,9 +542,16 @@ extern "C" adps_status adps_step_phase1_begin(adps_plan* P, void* stream_v, cons
   // ---- ever-dominant flags (ref/adc.py:177-180) and the fallback count, so
   //      the host can draw the fallback normals while the rest runs
   CK(cudaMemsetAsync(P->dom_flag.p, 0, (size_t)nn, s));
-  CK(launch_dominance(dominant, total_px, P->cls.as<unsigned char>(), N, P->dom_flag.as<unsigned char>(),
-                      P->split_list.as<int>(), ctr, P->sm_count, s));
-  mark(P, "dominance", s, 2);
+  for (int v = 0; v < V; ++v) {
+    P->lohi_host[2 * v] = 0x7ff0000000000000ull;   // +inf
+    P->lohi_host[2 * v + 1] = 0ull;                // +0.0
+  }
+  CK(cudaMemcpyAsync(P->lohi.p, P->lohi_host, sizeof(unsigned long long) * 2 * V, cudaMemcpyHostToDevice, s));
+  {
+    const AttributionArgs a = attr_args(P, V, H, W, cfg, N, image, gt, dominant);
+    CK(launch_minmax(a, P->split_list.as<int>(), ctr, P->sm_count, s));
+  }
+  mark(P, "minmax_dominance", s, 3);
   CK(cudaMemcpyAsync(P->ctr_host, ctr, sizeof(Counters), cudaMemcpyDeviceToHost, s));
   CK(cudaStreamSynchronize(s));
   {

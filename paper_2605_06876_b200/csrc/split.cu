@@ -175,7 +175,7 @@ __global__ void child_init_kernel(ChildArgs a) {
       const double iq[3] = {1.0 / sq[0], 1.0 / sq[1], 1.0 / sq[2]};
       rdrt(rot, sq, P.cov);
       rdrt(rot, iq, P.prec);
-      P.smax = fmax(s1, s2);
+      P.inv_smax = 1.0 / fmax(s1, s2);
       a.props[rid] = P;
     }
     a.valid[rid] = ok ? 1 : 0;
