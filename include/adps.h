@@ -207,9 +207,16 @@ ADPS_API adps_status adps_get_timing(adps_plan* plan, double* ms, int32_t max_en
 
 /* Tuning knobs (diagnostic/testing).  ADPS_PARAM_LARGE_THRESHOLD: parents
  * with more proposals than this use the grid-wide pair-tile merge path
- * (default 32; 0 routes every split parent through it). */
+ * (default 32; 0 routes every split parent through it).
+ * ADPS_PARAM_TILE_PATH: 0 (default) warp-per-tile CCL with the block CCL for
+ * the tiles it defers (> 256 runs) and for r_erode > 3 / debug maps; 1 the
+ * block CCL for every tile.  Both give identical results.
+ * ADPS_PARAM_DEFERRED_TILES (read-only): tiles the last phase 1 deferred. */
 #define ADPS_PARAM_LARGE_THRESHOLD 1
+#define ADPS_PARAM_TILE_PATH 2
+#define ADPS_PARAM_DEFERRED_TILES 3
 ADPS_API adps_status adps_set_param(adps_plan* plan, int32_t key, int64_t value);
+ADPS_API adps_status adps_get_param(adps_plan* plan, int32_t key, int64_t* value);
 
 /* Cumulative number of kernels this plan launched (own kernels) and of
  * library sort calls (CUB radix sort) -- used by the benchmark's

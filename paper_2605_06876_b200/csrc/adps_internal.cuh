@@ -101,6 +101,7 @@ struct Counters {
   unsigned long long n_groups_all;
   unsigned long long n_tile_pairs;
   unsigned long long n_fallback_pre;
+  unsigned long long n_deferred;   // tiles the warp CCL handed to the block CCL
   unsigned int degenerate;
   unsigned int overflow;   // bit0 regions, bit1 partials
 };

@@ -155,13 +155,14 @@ struct TileSmem {
   unsigned long long base_part, base_reg;
 };
 
-__global__ void __launch_bounds__(kTileThreads) tile_kernel(TileParams P) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  TileSmem& S = *reinterpret_cast<TileSmem*>(smem_raw);
+// Block-per-tile CCL (general r_erode, any number of runs, debug maps).  The
+// warp-per-tile kernel (tile_warp.cu) handles the common case and defers
+// the tiles it cannot (too many runs) to this one.
+__device__ void tile_block(const TileParams& P, TileSmem& S, const int tile) {
   const int tid = threadIdx.x;
   const int tiles_per_view = P.tiles_x * P.tiles_y;
-  const int v = blockIdx.x / tiles_per_view;
-  const int tile_in_view = blockIdx.x % tiles_per_view;
+  const int v = tile / tiles_per_view;
+  const int tile_in_view = tile % tiles_per_view;
   const int tyi = tile_in_view / P.tiles_x, txi = tile_in_view % P.tiles_x;
   const int x0 = txi * kTileW, y0 = tyi * kTileH;
   const int W = P.W, H = P.H;
@@ -237,7 +238,7 @@ __global__ void __launch_bounds__(kTileThreads) tile_kernel(TileParams P) {
   }
   // a tile without split-candidate pixels cannot hold a region
   if (__syncthreads_count(n_cand) == 0 && !P.dbg_m) {
-    int* border = P.border + (long long)blockIdx.x * kBorderSlots;
+    int* border = P.border + (long long)tile * kBorderSlots;
     for (int s = tid; s < kBorderSlots; s += kTileThreads) border[s] = -1;
     return;
   }
@@ -429,7 +430,7 @@ __global__ void __launch_bounds__(kTileThreads) tile_kernel(TileParams P) {
   }
   __syncthreads();
   // 7. border labels: top, bottom, left, right
-  int* border = P.border + (long long)blockIdx.x * kBorderSlots;
+  int* border = P.border + (long long)tile * kBorderSlots;
   for (int s = tid; s < kBorderSlots; s += kTileThreads) {
     int tx, ty;
     if (s < kTileW) { tx = s; ty = 0; }
@@ -440,6 +441,18 @@ __global__ void __launch_bounds__(kTileThreads) tile_kernel(TileParams P) {
     int g = -1;
     if (S.d[p] >= 0) g = S.slot[S.label[S.label[p]]];   // pixel -> run start -> root
     border[s] = g;
+  }
+}
+
+// all tiles (list == nullptr) or the tiles the warp kernel deferred
+__global__ void __launch_bounds__(kTileThreads) tile_kernel(TileParams P, const int* list,
+                                                            const unsigned long long* n_list) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  TileSmem& S = *reinterpret_cast<TileSmem*>(smem_raw);
+  const long long n = list ? (long long)*n_list : (long long)P.tiles_x * P.tiles_y * P.n_views;
+  for (long long t = blockIdx.x; t < n; t += gridDim.x) {
+    tile_block(P, S, list ? list[t] : (int)t);
+    __syncthreads();
   }
 }
 
@@ -567,12 +580,25 @@ cudaError_t launch_attribution(const AttributionArgs& a, cudaStream_t s, MarkFn 
   P.dbg_m = a.dbg_m;
   P.dbg_b = a.dbg_b;
   P.overflow = a.overflow;
+  P.n_views = a.V;
+  P.deferred = a.deferred;
+  P.n_deferred = a.n_deferred;
   const long long nblocks = (long long)P.tiles_x * P.tiles_y * a.V;
   size_t smem = sizeof(TileSmem);
   cudaError_t e = cudaFuncSetAttribute(tile_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  tile_kernel<<<(unsigned)nblocks, kTileThreads, smem, s>>>(P);
-  if (mark) mark(ctx, "tile_ccl", s, 1);
+  // the warp kernel covers r_erode <= 3 without debug maps; the block kernel
+  // takes everything else and the tiles the warp kernel defers
+  const bool warp_path = a.tile_path == 0 && !a.dbg_m && a.r_erode <= 3 && a.deferred && a.n_deferred;
+  if (warp_path) {
+    e = launch_tile_warp(P, nblocks, s);
+    if (e != cudaSuccess) return e;
+    tile_kernel<<<a.grid_small, kTileThreads, smem, s>>>(P, a.deferred, a.n_deferred);
+    if (mark) mark(ctx, "tile_ccl", s, 2);
+  } else {
+    tile_kernel<<<(unsigned)nblocks, kTileThreads, smem, s>>>(P, nullptr, nullptr);
+    if (mark) mark(ctx, "tile_ccl", s, 1);
+  }
   BorderParams B;
   B.border = a.border;
   B.partials = a.partials;

@@ -28,6 +28,9 @@ struct TileParams {
   unsigned char* dbg_m;
   unsigned char* dbg_b;
   unsigned int* overflow;
+  int n_views;
+  int* deferred;                     // tiles the warp kernel hands to the block kernel
+  unsigned long long* n_deferred;
 };
 
 struct BorderParams {
@@ -63,7 +66,14 @@ struct AttributionArgs {
   unsigned char* dbg_b;
   unsigned int* overflow;
   unsigned grid_small;
+  int* deferred;                     // [n_tiles]
+  unsigned long long* n_deferred;
+  int tile_path;                     // 0 auto (warp kernel + deferred), 1 block kernel only
 };
+
+// warp-per-tile scanline CCL (r_erode <= 3); defers tiles with > kWarpMaxRuns runs
+cudaError_t launch_tile_warp(const TileParams& P, long long n_tiles, cudaStream_t s);
+size_t tile_warp_smem_bytes();
 
 size_t tile_smem_bytes();
 // minmax + ever-dominant flags + thresholds + fallback count (phase-1 begin)

@@ -78,7 +78,7 @@ struct adps_plan {
   Buf lohi, lo, thr, cams;
   // tiles / fragments / regions
   Buf border, partials, partial_parent, regions, props, valid, keys, vals, keys_sorted, vals_sorted;
-  Buf idx, uf, groups, children, dbg_stats, dbg_child;
+  Buf idx, uf, groups, children, dbg_stats, dbg_child, deferred;
   // merge / cap scratch (proposal space)
   Buf small_list, pstart, n_groups, work_cnt, work_off, props_s, pcand, gkey, gval, gkey_sorted, gval_sorted,
       grp_first, ext_key, ext_val, ext_key_sorted, ext_val_sorted, cand_key, cand_val, cand_key_sorted,
@@ -115,6 +115,7 @@ struct adps_plan {
   long long launches = 0;
   long long lib_calls = 0;
   int large_threshold = 32;
+  int tile_path = 0;   // 0 warp CCL + deferred block CCL, 1 block CCL only
   // arguments saved by phase1_begin for phase1_end
   bool have_begin = false;
   struct {
@@ -419,6 +420,9 @@ static AttributionArgs attr_args(adps_plan* P, int V, int H, int W, const adps_c
   a.dbg_b = P->dbg_b;
   a.overflow = &ctr->overflow;
   a.grid_small = (unsigned)(P->sm_count * 4);
+  a.deferred = P->deferred.as<int>();
+  a.n_deferred = &ctr->n_deferred;
+  a.tile_path = P->tile_path;
   return a;
 }
 
@@ -429,6 +433,7 @@ static adps_status run_attribution(adps_plan* P, cudaStream_t s, int V, int H, i
   CK(cudaMemsetAsync(&ctr->n_regions, 0, sizeof(unsigned long long), s));
   CK(cudaMemsetAsync(&ctr->n_partials, 0, sizeof(unsigned long long), s));
   CK(cudaMemsetAsync(&ctr->overflow, 0, sizeof(unsigned int), s));
+  CK(cudaMemsetAsync(&ctr->n_deferred, 0, sizeof(unsigned long long), s));
   const AttributionArgs a = attr_args(P, V, H, W, cfg, N, image, gt, dominant);
   CK(launch_attribution(a, s, mark_cb, P));
   return ADPS_OK;
@@ -492,6 +497,7 @@ extern "C" adps_status adps_step_phase1_begin(adps_plan* P, void* stream_v, cons
   CK(ensure(P->thr, 8ll * V * cfg->l_bands));
   CK(ensure(P->cams, 8ll * 18 * V));
   CK(ensure(P->border, 4ll * n_tiles * kBorderSlots));
+  CK(ensure(P->deferred, 4ll * n_tiles));
   CK(ensure(P->ctr, sizeof(Counters)));
   if (P->cams_host_cap < V) {
     if (P->cams_host) cudaFreeHost(P->cams_host);
@@ -1016,7 +1022,22 @@ extern "C" adps_status adps_set_param(adps_plan* P, int32_t key, int64_t value) 
     P->large_threshold = (int)value;
     return ADPS_OK;
   }
+  if (key == ADPS_PARAM_TILE_PATH) {
+    if (value < 0 || value > 1) return fail(ADPS_INVALID_ARG, "tile path must be 0 (warp) or 1 (block)");
+    P->tile_path = (int)value;
+    return ADPS_OK;
+  }
   return fail(ADPS_INVALID_ARG, "unknown parameter %d", key);
+}
+
+extern "C" adps_status adps_get_param(adps_plan* P, int32_t key, int64_t* value) {
+  if (!P || !value) return fail(ADPS_INVALID_ARG, "NULL argument");
+  switch (key) {
+    case ADPS_PARAM_LARGE_THRESHOLD: *value = P->large_threshold; return ADPS_OK;
+    case ADPS_PARAM_TILE_PATH: *value = P->tile_path; return ADPS_OK;
+    case ADPS_PARAM_DEFERRED_TILES: *value = P->ctr_host ? (int64_t)P->ctr_host->n_deferred : 0; return ADPS_OK;
+    default: return fail(ADPS_INVALID_ARG, "unknown parameter %d", key);
+  }
 }
 
 extern "C" adps_status adps_get_launch_count(adps_plan* P, int64_t* kernels, int64_t* library_calls) {

@@ -195,6 +195,19 @@ class Plan:
         """Parents with more than p proposals take the grid-wide merge path (default 32)."""
         _abi.check(self.lib.adps_set_param(self._h, _abi.PARAM_LARGE_THRESHOLD, int(p)))
 
+    def set_tile_path(self, path: int):
+        """0: warp-per-tile CCL (+ block CCL for deferred tiles), 1: block CCL only."""
+        _abi.check(self.lib.adps_set_param(self._h, _abi.PARAM_TILE_PATH, int(path)))
+
+    def get_param(self, key: int) -> int:
+        v = C.c_int64()
+        _abi.check(self.lib.adps_get_param(self._h, int(key), C.byref(v)))
+        return int(v.value)
+
+    def deferred_tiles(self) -> int:
+        """Tiles the warp CCL of the last phase 1 handed to the block CCL."""
+        return self.get_param(_abi.PARAM_DEFERRED_TILES)
+
     def set_debug_records(self, on: bool):
         _abi.check(self.lib.adps_set_debug_records(self._h, int(on)))
 

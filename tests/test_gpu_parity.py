@@ -97,8 +97,11 @@ def test_maps_bit_exact(op, plan, c):
 
 
 # ------------------------------------------------------------------ partition
-def _injected_partition(op, plan, e, dom, n_gauss, l_bands, m_min, cands, tau=0.1):
-    """Run phase 1 with error map e injected exactly (raw = e, lo = 0, hi = 1)."""
+def _injected_partition(op, plan, e, dom, n_gauss, l_bands, m_min, cands, tau=0.1, r_erode=1, deferred=None):
+    """Run phase 1 with error map e injected exactly (raw = e, lo = 0, hi = 1).
+
+    Both CCL paths run (block kernel for every tile, then the warp kernel with
+    its deferred tiles) and must agree bit for bit; returns (warp path, oracle)."""
     import torch
     h, w = e.shape
     e = e.astype(np.float32)
@@ -112,13 +115,24 @@ def _injected_partition(op, plan, e, dom, n_gauss, l_bands, m_min, cands, tau=0.
     cam = O.Cam(np.eye(3), np.array([0, 0, -3.0]), 1.2 * w, 1.2 * w, (w - 1) / 2, (h - 1) / 2, w, h)
     ga = np.full(n_gauss, 1e-6)
     ga[cands] = 1.0
-    cfg = dict(tau_l1=tau, r_erode=1, m_min=m_min, l_bands=l_bands, n_max=19, v_views=1, gamma_d=2.0,
+    cfg = dict(tau_l1=tau, r_erode=r_erode, m_min=m_min, l_bands=l_bands, n_max=19, v_views=1, gamma_d=2.0,
                gamma_c=0.15, tau_g=2e-4, tau_s=0.01, eta=1.6, eps=1e-9)
     dev = "cuda"
-    plan.phase1(PA.to_tensors(g), 1.0, torch.as_tensor(ga, device=dev), torch.ones(n_gauss, dtype=torch.float64,
-                device=dev), cfg, cam.row()[None], torch.as_tensor(rendered[None], device=dev),
-                torch.as_tensor(gt[None], device=dev), torch.as_tensor(dom[None].astype(np.int32), device=dev))
-    got = PA.gpu_regions(plan)
+    got_by_path = []
+    for path in (1, 0):
+        plan.set_tile_path(path)
+        try:
+            plan.phase1(PA.to_tensors(g), 1.0, torch.as_tensor(ga, device=dev),
+                        torch.ones(n_gauss, dtype=torch.float64, device=dev), cfg, cam.row()[None],
+                        torch.as_tensor(rendered[None], device=dev), torch.as_tensor(gt[None], device=dev),
+                        torch.as_tensor(dom[None].astype(np.int32), device=dev))
+        finally:
+            plan.set_tile_path(0)
+        got_by_path.append(PA.gpu_regions(plan))
+        if path == 0 and deferred is not None:
+            assert (plan.deferred_tiles() > 0) == deferred, plan.deferred_tiles()
+    np.testing.assert_array_equal(got_by_path[1], got_by_path[0], err_msg="warp CCL != block CCL")
+    got = got_by_path[1]
     maps = O.compute_maps(rendered.astype(np.float64), gt.astype(np.float64), cfg)
     is_c = np.zeros(n_gauss, bool)
     is_c[cands] = True
@@ -151,6 +165,33 @@ def test_partition_snakes_cross_tiles(op, plan, shape):
     dom[(xx + yy) % 7 == 0] = 0          # diagonal stripes of another candidate
     dom[(xx * 3 + yy) % 11 == 0] = -1
     got, want = _injected_partition(op, plan, e, dom, 2, 1, 1, [0, 1])
+    np.testing.assert_array_equal(got, want)
+
+
+@pytest.mark.parametrize("r_erode", [1, 2, 3])
+@pytest.mark.parametrize("seed", range(4))
+def test_partition_erosion_both_paths(op, plan, seed, r_erode):
+    """Warp CCL (r <= 3: ring-buffer erosion with halo columns) vs block CCL vs oracle."""
+    rng = np.random.default_rng(100 + seed)
+    h, w = int(rng.integers(30, 170)), int(rng.integers(30, 170))
+    n = 5
+    dom = np.kron(rng.integers(-1, n, (h // 4 + 1, w // 4 + 1)), np.ones((4, 4), np.int64))[:h, :w]
+    e = np.kron(rng.uniform(0, 1, (h // 2 + 1, w // 2 + 1)), np.ones((2, 2)))[:h, :w]
+    e[rng.uniform(size=(h, w)) < 0.05] = 0.01
+    got, want = _injected_partition(op, plan, e, dom, n, int(rng.integers(1, 4)), int(rng.integers(1, 4)),
+                                    [0, 1, 3, 4], r_erode=r_erode)
+    np.testing.assert_array_equal(got, want)
+
+
+@pytest.mark.parametrize("shape", [(64, 64), (70, 45)])
+def test_partition_deferred_tiles(op, plan, shape):
+    """Tiles with more than 256 runs (alternating candidates) go to the block CCL."""
+    h, w = shape
+    yy, xx = np.mgrid[0:h, 0:w]
+    dom = ((xx + (yy // 2)) % 2).astype(np.int64)     # runs of length 1, diagonal links
+    dom[:, w // 2:] = 0                              # right half: one big component
+    e = np.full((h, w), 0.9)
+    got, want = _injected_partition(op, plan, e, dom, 2, 1, 1, [0, 1], deferred=True)
     np.testing.assert_array_equal(got, want)
 
 
@@ -407,11 +448,13 @@ def test_determinism_at_scale(op, cfg_name):
     img, dom = plan.render(g, cams)
     cfg = AdpSplitConfig(v_views=len(cams), n_max=wl.n_max)
     digests = []
-    for _ in range(3):
+    for path in (0, 0, 1):      # the last run takes the block CCL for every tile: same bits
+        plan.set_tile_path(path)
         res = op.densify_step(g, ini.extent, cams, gt_img, torch.as_tensor(ga, device="cuda"),
                               torch.as_tensor(den, device="cuda"), cfg, np.random.default_rng(0),
                               renders=(img, dom), plan=plan, view_ids=list(range(len(cams))))
         digests.append((res.counts, _step_digest(op, plan, res)))
+    plan.set_tile_path(0)
     for counts, dg in digests[1:]:
         assert counts == digests[0][0]
         for k in dg:
