@@ -215,6 +215,8 @@ ADPS_API adps_status adps_get_timing(adps_plan* plan, double* ms, int32_t max_en
 #define ADPS_PARAM_LARGE_THRESHOLD 1
 #define ADPS_PARAM_TILE_PATH 2
 #define ADPS_PARAM_DEFERRED_TILES 3
+#define ADPS_PARAM_NORMALS_CONSUMED 4   /* read-only, see adps_normals_pcg64 */
+#define ADPS_PARAM_NORMALS_STATUS 5     /* read-only, see adps_normals_pcg64 */
 ADPS_API adps_status adps_set_param(adps_plan* plan, int32_t key, int64_t value);
 ADPS_API adps_status adps_get_param(adps_plan* plan, int32_t key, int64_t* value);
 
@@ -222,6 +224,21 @@ ADPS_API adps_status adps_get_param(adps_plan* plan, int32_t key, int64_t* value
  * library sort calls (CUB radix sort) -- used by the benchmark's
  * gpu_launches accounting. */
 ADPS_API adps_status adps_get_launch_count(adps_plan* plan, int64_t* kernels, int64_t* library_calls);
+
+/* numpy.random.Generator(PCG64).standard_normal(n), bit-identical, on the
+ * device.  Replaces the host draw of the fallback children's normals
+ * (ref/adc.py:97 -> rng.normal(size=(k, 3)) per fallback parent, which is
+ * one contiguous slice of the Generator's normal stream).  state/inc: the
+ * bit generator's 128-bit state and increment as (low, high) 64-bit words
+ * (bit_generator.state["state"]).  Writes n doubles to `out` (device) on
+ * `stream`.  *consumed = 64-bit draws used (advance the host generator by
+ * it); *status = 0 exact, bit0 a wedge comparison within a few ulp of the
+ * host libm's exp (redraw on the host), bit1 internal window too short.
+ * With sync == 0 nothing is waited for: consumed/status are read with
+ * adps_get_param(ADPS_PARAM_NORMALS_*) after the plan's next phase-1 end
+ * (call it between adps_step_phase1_begin and adps_step_phase1_end). */
+ADPS_API adps_status adps_normals_pcg64(adps_plan* plan, void* stream, const uint64_t state[2], const uint64_t inc[2],
+                                        int64_t n, double* out, int32_t sync, int64_t* consumed, int32_t* status);
 
 /* DensifyStats feed (ref/adc.py:73-79): grad_accum[vis] += |vg|, denom[vis] += 1.
  * viewspace_grad [n,2] fp32, visible [n] uint8. */

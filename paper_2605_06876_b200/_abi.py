@@ -17,6 +17,7 @@ ADPS_OK, ADPS_INVALID_ARG, ADPS_V_TOO_LARGE, ADPS_DEGENERATE_RAY = 0, 1, 2, 3
 ADPS_CUDA_ERROR, ADPS_OOM, ADPS_BAD_STATE = 4, 5, 6
 CASE_SPLIT, CASE_FALLBACK, CASE_RESET = 0, 1, 2
 PARAM_LARGE_THRESHOLD, PARAM_TILE_PATH, PARAM_DEFERRED_TILES = 1, 2, 3
+PARAM_NORMALS_CONSUMED, PARAM_NORMALS_STATUS = 4, 5
 
 vp = C.c_void_p
 
@@ -58,7 +59,7 @@ EXPORTS = (
     "adps_abi_version", "adps_last_error", "adps_plan_create", "adps_plan_destroy", "adps_render",
     "adps_step_phase1", "adps_step_phase1_begin", "adps_step_phase1_end", "adps_step_phase2", "adps_get_report", "adps_get_regions",
     "adps_set_debug_records", "adps_set_debug_maps", "adps_set_timing", "adps_get_timing",
-    "adps_accumulate_stats", "adps_get_launch_count", "adps_set_param", "adps_get_param",
+    "adps_accumulate_stats", "adps_get_launch_count", "adps_set_param", "adps_get_param", "adps_normals_pcg64",
 )
 
 _lib = None
@@ -95,6 +96,8 @@ def load(path: str = LIB_PATH):
     lib.adps_get_launch_count.argtypes = [vp, C.POINTER(C.c_int64), C.POINTER(C.c_int64)]
     lib.adps_set_param.argtypes = [vp, C.c_int32, C.c_int64]
     lib.adps_get_param.argtypes = [vp, C.c_int32, C.POINTER(C.c_int64)]
+    lib.adps_normals_pcg64.argtypes = [vp, vp, C.POINTER(C.c_uint64), C.POINTER(C.c_uint64), C.c_int64, vp,
+                                       C.c_int32, C.POINTER(C.c_int64), C.POINTER(C.c_int32)]
     for name in EXPORTS:
         fn = getattr(lib, name)
         if name not in ("adps_abi_version", "adps_last_error"):

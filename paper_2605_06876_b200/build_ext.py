@@ -26,8 +26,8 @@ BUILD = os.path.join(ROOT, "build", "adps")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 COMMON = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-Xcompiler", "-fvisibility=hidden",
           "-I", os.path.join(ROOT, "include")]
-NO_FMA = {"attribution.cu", "split.cu", "merge.cu", "plan.cu"}
-SOURCES = ["attribution.cu", "tile_warp.cu", "split.cu", "merge.cu", "render.cu", "plan.cu"]
+NO_FMA = {"attribution.cu", "tile_warp.cu", "normals.cu", "split.cu", "merge.cu", "plan.cu"}
+SOURCES = ["attribution.cu", "tile_warp.cu", "normals.cu", "split.cu", "merge.cu", "render.cu", "plan.cu"]
 
 
 def nvcc() -> str:

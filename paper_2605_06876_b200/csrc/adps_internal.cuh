@@ -102,6 +102,8 @@ struct Counters {
   unsigned long long n_tile_pairs;
   unsigned long long n_fallback_pre;
   unsigned long long n_deferred;   // tiles the warp CCL handed to the block CCL
+  unsigned long long normals_consumed;   // 64-bit draws used by adps_normals_pcg64
+  unsigned int normals_status;           // bit0 near-tie (redraw on host), bit1 window short
   unsigned int degenerate;
   unsigned int overflow;   // bit0 regions, bit1 partials
 };

@@ -12,6 +12,7 @@
 #include "adps_internal.cuh"
 #include "attribution.cuh"
 #include "merge.cuh"
+#include "normals.cuh"
 #include "render.cuh"
 #include "split.cuh"
 
@@ -79,6 +80,8 @@ struct adps_plan {
   // tiles / fragments / regions
   Buf border, partials, partial_parent, regions, props, valid, keys, vals, keys_sorted, vals_sorted;
   Buf idx, uf, groups, children, dbg_stats, dbg_child, deferred;
+  // device normals (numpy PCG64 stream)
+  Buf nrm_val, nrm_len, nrm_acc, nrm_reach, nrm_rmax, nrm_walked, nrm_idx, nrm_tmp;
   // merge / cap scratch (proposal space)
   Buf small_list, pstart, n_groups, work_cnt, work_off, props_s, pcand, gkey, gval, gkey_sorted, gval_sorted,
       grp_first, ext_key, ext_val, ext_key_sorted, ext_val_sorted, cand_key, cand_val, cand_key_sorted,
@@ -223,7 +226,9 @@ extern "C" adps_status adps_plan_destroy(adps_plan* P) {
                  &P->ext_key, &P->ext_val, &P->ext_key_sorted, &P->ext_val_sorted, &P->cand_key, &P->cand_val,
                  &P->cand_key_sorted, &P->cand_val_sorted, &P->scan3_val, &P->scan3_flag, &P->scan3_ticket,
                  &P->large_of, &P->lp_cnt, &P->lp_off, &P->tile_cnt, &P->tile_off, &P->mkey, &P->mval,
-                 &P->mkey_sorted, &P->mval_sorted, &P->boxes, &P->tile_pairs};
+                 &P->mkey_sorted, &P->mval_sorted, &P->boxes, &P->tile_pairs, &P->deferred,
+                 &P->nrm_val, &P->nrm_len, &P->nrm_acc, &P->nrm_reach, &P->nrm_rmax, &P->nrm_walked,
+                 &P->nrm_idx, &P->nrm_tmp};
   for (Buf* b : bufs)
     if (b->p) cudaFree(b->p);
   if (P->ctr_host) cudaFreeHost(P->ctr_host);
@@ -1036,6 +1041,10 @@ extern "C" adps_status adps_get_param(adps_plan* P, int32_t key, int64_t* value)
     case ADPS_PARAM_LARGE_THRESHOLD: *value = P->large_threshold; return ADPS_OK;
     case ADPS_PARAM_TILE_PATH: *value = P->tile_path; return ADPS_OK;
     case ADPS_PARAM_DEFERRED_TILES: *value = P->ctr_host ? (int64_t)P->ctr_host->n_deferred : 0; return ADPS_OK;
+    case ADPS_PARAM_NORMALS_CONSUMED:
+      *value = P->ctr_host ? (int64_t)P->ctr_host->normals_consumed : 0;
+      return ADPS_OK;
+    case ADPS_PARAM_NORMALS_STATUS: *value = P->ctr_host ? (int64_t)P->ctr_host->normals_status : 0; return ADPS_OK;
     default: return fail(ADPS_INVALID_ARG, "unknown parameter %d", key);
   }
 }
@@ -1044,6 +1053,64 @@ extern "C" adps_status adps_get_launch_count(adps_plan* P, int64_t* kernels, int
   if (!P || !kernels || !library_calls) return fail(ADPS_INVALID_ARG, "NULL argument");
   *kernels = P->launches;
   *library_calls = P->lib_calls;
+  return ADPS_OK;
+}
+
+extern "C" adps_status adps_normals_pcg64(adps_plan* P, void* stream_v, const uint64_t state[2],
+                                          const uint64_t inc[2], int64_t n, double* out, int32_t sync,
+                                          int64_t* consumed, int32_t* status) {
+  if (!P || !state || !inc) return fail(ADPS_INVALID_ARG, "NULL argument");
+  if (n < 0) return fail(ADPS_INVALID_ARG, "negative n");
+  if (n > 0 && !out) return fail(ADPS_INVALID_ARG, "out is NULL");
+  if (n > (1ll << 30)) return fail(ADPS_INVALID_ARG, "n too large");
+  CK(cudaSetDevice(P->device));
+  cudaStream_t s = (cudaStream_t)stream_v;
+  CK(ensure(P->ctr, sizeof(Counters)));
+  if (!P->ctr_host) CK(cudaMallocHost(&P->ctr_host, sizeof(Counters)));
+  Counters* ctr = P->ctr.as<Counters>();
+  CK(cudaMemsetAsync(&ctr->normals_consumed, 0, sizeof(unsigned long long), s));
+  CK(cudaMemsetAsync(&ctr->normals_status, 0, sizeof(unsigned int), s));
+  if (n > 0) {
+    const long long w = normals_window(n);
+    CK(ensure(P->nrm_val, 8ll * w));
+    CK(ensure(P->nrm_len, w));
+    CK(ensure(P->nrm_acc, w));
+    CK(ensure(P->nrm_reach, 4ll * w));
+    CK(ensure(P->nrm_rmax, 4ll * w));
+    CK(ensure(P->nrm_walked, w));
+    CK(ensure(P->nrm_idx, 4ll * w));
+    const size_t tb = normals_temp_bytes(w);
+    CK(ensure(P->nrm_tmp, tb));
+    NormalsArgs a;
+    a.state_lo = state[0];
+    a.state_hi = state[1];
+    a.inc_lo = inc[0];
+    a.inc_hi = inc[1];
+    a.n = n;
+    a.window = w;
+    a.out = out;
+    a.val = P->nrm_val.as<double>();
+    a.len = P->nrm_len.as<unsigned char>();
+    a.acc = P->nrm_acc.as<unsigned char>();
+    a.reach = P->nrm_reach.as<int>();
+    a.reach_max = P->nrm_rmax.as<int>();
+    a.walked = P->nrm_walked.as<unsigned char>();
+    a.emit_idx = P->nrm_idx.as<int>();
+    a.consumed = &ctr->normals_consumed;
+    a.status = &ctr->normals_status;
+    CK(launch_normals(a, P->nrm_tmp.p, P->nrm_tmp.bytes, s));
+    P->launches += 5;
+    P->lib_calls += 2;
+  }
+  if (sync) {
+    CK(cudaMemcpyAsync(&P->ctr_host->normals_consumed, &ctr->normals_consumed, sizeof(unsigned long long),
+                       cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(&P->ctr_host->normals_status, &ctr->normals_status, sizeof(unsigned int),
+                       cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    if (consumed) *consumed = (int64_t)P->ctr_host->normals_consumed;
+    if (status) *status = (int32_t)P->ctr_host->normals_status;
+  }
   return ADPS_OK;
 }
 

@@ -208,6 +208,29 @@ class Plan:
         """Tiles the warp CCL of the last phase 1 handed to the block CCL."""
         return self.get_param(_abi.PARAM_DEFERRED_TILES)
 
+    def normals_pcg64(self, bitgen_state: dict, n: int, out: torch.Tensor = None, sync: bool = True):
+        """numpy Generator(PCG64).standard_normal(n) on the device, bit-identical.
+
+        bitgen_state: ``rng.bit_generator.state``.  Returns (out, consumed,
+        status) when sync, else (out, None, None) with consumed/status
+        readable via normals_result() after the next phase1_end."""
+        st = bitgen_state["state"]
+        m64 = (1 << 64) - 1
+        state = (C.c_uint64 * 2)(st["state"] & m64, st["state"] >> 64)
+        inc = (C.c_uint64 * 2)(st["inc"] & m64, st["inc"] >> 64)
+        if out is None:
+            out = torch.empty(max(n, 0), dtype=F64, device=self.device)
+        consumed, status = C.c_int64(), C.c_int32()
+        _abi.check(self.lib.adps_normals_pcg64(self._h, self._stream(), state, inc, int(n), _ptr(out) if n else None,
+                                               int(sync), C.byref(consumed), C.byref(status)))
+        if sync:
+            return out, int(consumed.value), int(status.value)
+        return out, None, None
+
+    def normals_result(self):
+        """(consumed, status) of the last normals_pcg64 after the plan synchronised."""
+        return self.get_param(_abi.PARAM_NORMALS_CONSUMED), self.get_param(_abi.PARAM_NORMALS_STATUS)
+
     def set_debug_records(self, on: bool):
         _abi.check(self.lib.adps_set_debug_records(self._h, int(on)))
 
@@ -372,7 +395,7 @@ class StepResult:
     counts: dict
     view_ids: list
     report_arrays: dict = None
-    normals: np.ndarray = None
+    normals: torch.Tensor = None   # the 6F fallback normals (device)
     stage_ms: dict = field(default_factory=dict)
 
     def report(self) -> SplitReport:
@@ -426,31 +449,45 @@ def densify_step(g: GaussianTensors, extent: float, cameras, gt, grad_accum: tor
                                cfg, cams_v, image, gt_v, dom)
     nf = counts["n_fallback"]
     # the caller's Generator draws 3 normals per fallback child in ascending
-    # parent order (ref/adc.py:97); the stream is chunk-invariant, so one call
-    # for 6F values is identical.  It runs on a host thread while the GPU
-    # finishes phase 1 (the C call releases the GIL).
+    # parent order (ref/adc.py:97); the stream is chunk-invariant, so the 6F
+    # values are one slice of rng.standard_normal.  A PCG64 Generator's slice
+    # is produced on the device, bit-identical, and the host Generator is
+    # advanced past it; any other bit generator is drawn on a host thread
+    # while the GPU finishes phase 1 (the C call releases the GIL).
+    normals = None
+    gpu_rng = nf > 0 and isinstance(rng.bit_generator, np.random.PCG64)
     drawn = {}
+    th = None
+    if gpu_rng:
+        normals, _, _ = plan.normals_pcg64(rng.bit_generator.state, 6 * nf, sync=False)
+    elif nf > 0:
+        def _draw():
+            drawn["z"] = rng.standard_normal(6 * nf)
 
-    def _draw():
-        drawn["z"] = rng.standard_normal(6 * nf) if nf > 0 else np.zeros(0)
-
-    th = threading.Thread(target=_draw)
-    th.start()
+        th = threading.Thread(target=_draw)
+        th.start()
     try:
         counts = plan.phase1_end()
     finally:
-        th.join()
+        if th is not None:
+            th.join()
     if counts["n_fallback"] != nf:
         raise RuntimeError("fallback count changed between phase-1 halves")
-    normals_np = drawn["z"]
-    normals = torch.from_numpy(normals_np).to(dev) if nf > 0 else None
+    if gpu_rng:
+        consumed, status = plan.normals_result()
+        if status == 0:
+            rng.bit_generator.advance(consumed)
+        else:   # a wedge test too close to call against the host libm: draw on the host
+            normals = torch.from_numpy(rng.standard_normal(6 * nf)).to(dev)
+    elif nf > 0:
+        normals = torch.from_numpy(drawn["z"]).to(dev)
     n_out = counts["n_out"]
     if out is None:
         out = GaussianTensors.empty(n_out, g.sh_k, dev)
     index_map = torch.empty(n_out, dtype=torch.int64, device=dev)
     plan.phase2(g, normals, out, index_map)
     res = StepResult(gaussians=out, index_map=index_map, counts=counts, view_ids=list(view_ids),
-                     normals=normals_np)
+                     normals=normals)
     if want_report:
         res.report_arrays = plan.report_arrays(counts["n_split"], counts["n_clone"])
     if plan.timing:
