@@ -11,7 +11,7 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libadps.so")
+LIB_PATH = os.environ.get("ADPS_LIB") or os.path.join(HERE, "libadps.so")   # ADPS_LIB: dev variants
 
 ADPS_OK, ADPS_INVALID_ARG, ADPS_V_TOO_LARGE, ADPS_DEGENERATE_RAY = 0, 1, 2, 3
 ADPS_CUDA_ERROR, ADPS_OOM, ADPS_BAD_STATE = 4, 5, 6

@@ -28,6 +28,18 @@ namespace adps {
 constexpr int kWarpMaxRuns = 256;
 constexpr int kWarpsPerBlock = 8;
 
+// rows reach the warp either by per-lane loads a row ahead (default) or staged
+// kRing rows ahead in shared memory by bulk async copies (kStaged)
+#ifndef ADPS_TW_STAGED
+#define ADPS_TW_STAGED 0
+#endif
+#ifndef ADPS_TW_FAST
+#define ADPS_TW_FAST 1
+#endif
+#ifndef ADPS_TW_MINBLOCKS
+#define ADPS_TW_MINBLOCKS 4
+#endif
+constexpr bool kStaged = ADPS_TW_STAGED != 0;
 constexpr int kRing = 4;            // rows in flight per warp (bulk async copies)
 constexpr int kRingF = 112;         // floats per staged image row: 32 px * 3 + 16 B alignment slack, x16 B
 constexpr int kRingD = 40;          // ints per staged dominant row: 32 + slack
@@ -48,7 +60,9 @@ struct WarpSmem {
   int uf[kWarpMaxRuns];
   unsigned run[kWarpMaxRuns];       // ty | s << 5 | e << 10 | band << 16
   union {
+#if ADPS_TW_STAGED
     RingSlot ring[kRing];
+#endif
     PostSmem post;
   } u;
   unsigned long long bar[kRing];    // one mbarrier per ring slot
@@ -122,6 +136,32 @@ __device__ __forceinline__ Cover cover(const void* p, unsigned bytes, const void
   return c;
 }
 
+// one image row of the tile (lane = x)
+struct RowIn {
+  float a[3], g[3];
+  int d;
+  bool inb;
+};
+
+template <int HL>
+__device__ __forceinline__ void load_row(RowIn& r, const TileConst& T, int ey, int lane) {
+  const int y = T.y0 - HL + ey;
+  const int x = T.x0 + lane;
+  r.inb = y >= 0 && y < T.H && x < T.W;
+  const long long p = r.inb ? (long long)y * T.W + x : 0;
+  const bool tile_row = ey >= HL && ey < HL + kTileH;
+#pragma unroll
+  for (int c = 0; c < 3; ++c) {
+    r.a[c] = r.inb ? __ldg(T.img + 3 * p + c) : 0.0f;
+    r.g[c] = r.inb ? __ldg(T.gtv + 3 * p + c) : 0.0f;
+  }
+  r.d = r.inb && tile_row ? __ldg(T.dom + p) : -1;
+}
+
+__device__ __forceinline__ int cand_of_px(const TileConst& T, const int d) {
+  return d >= 0 && d < T.N && __ldg(T.cls + d) == 1 ? d : -1;
+}
+
 // np.abs(rendered - gt).sum(axis=-1) == (|d0| + |d1|) + |d2| in fp64
 __device__ __forceinline__ double raw_l1_f(const float* a, const float* g) {
   const double a0 = fabs(dsub((double)a[0], (double)g[0]));
@@ -141,6 +181,7 @@ __device__ __forceinline__ bool metric_at(const TileConst& T, int x, int y) {
   return dsub(raw_l1_f(a, g), T.lo) >= T.x_m;
 }
 
+#if ADPS_TW_STAGED
 // lane 0: stage ext row ey (image, gt and -- for tile rows -- dominant ids)
 // into its ring slot with bulk async copies completing on the slot's mbarrier
 template <int HL>
@@ -174,6 +215,8 @@ __device__ __forceinline__ void issue_row(WarpSmem& S, const int ey, const TileC
   if (cg.ok) bulk_g2s(S.u.ring[slot].gt, cg.lo, cg.bytes, bar);
   if (cd.ok) bulk_g2s(S.u.ring[slot].dom, cd.lo, cd.bytes, bar);
 }
+
+#endif
 
 // one ext row: metric mask, then (once its erosion window is complete) the
 // runs of tile row ey - SPAN and their unions with the row above.
@@ -214,51 +257,59 @@ __device__ __forceinline__ bool scan_row(const float* a, const float* g, const b
     const int key = ((er >> lane) & 1u) ? cand : -1;
     // ---- runs of equal (candidate, band)
     const unsigned K = __ballot_sync(FULL, key >= 0);
-    const int lkey = __shfl_up_sync(FULL, key, 1);
-    const int lband = __shfl_up_sync(FULL, band, 1);
-    const unsigned C = __ballot_sync(FULL, key >= 0 && lane > 0 && lkey == key && lband == band);
-    const unsigned starts = K & ~C;
-    const unsigned ends = K & ~(C >> 1);
-    const int nr = __popc(starts);
-    if (st.n_runs + nr > kWarpMaxRuns) {
-      overflow = true;
-    } else {
-      const bool is_start = (starts >> lane) & 1u;
-      const bool is_end = (ends >> lane) & 1u;
-      const int rid_start = st.n_runs + __popc(starts & ((1u << lane) - 1u));
-      const int src = 31 - __clz(starts & (FULL >> (31 - lane)));
-      const int rid_b = __shfl_sync(FULL, rid_start, src & 31);
-      const int rid = key >= 0 ? rid_b : -1;
-      if (is_start) {
-        const int e = __ffs(ends & (FULL << lane)) - 1;
-        S.run[rid] = (unsigned)ty | ((unsigned)lane << 5) | ((unsigned)e << 10) | ((unsigned)band << 16);
-        S.uf[rid] = rid;
+#if ADPS_TW_FAST
+    if (K == 0) {   // no keyed pixel in this row: no runs, nothing to unite
+      st.prev_key = -1;
+      st.prev_rid = -1;
+    } else
+#endif
+    {
+      const int lkey = __shfl_up_sync(FULL, key, 1);
+      const int lband = __shfl_up_sync(FULL, band, 1);
+      const unsigned C = __ballot_sync(FULL, key >= 0 && lane > 0 && lkey == key && lband == band);
+      const unsigned starts = K & ~C;
+      const unsigned ends = K & ~(C >> 1);
+      const int nr = __popc(starts);
+      if (st.n_runs + nr > kWarpMaxRuns) {
+        overflow = true;
+      } else {
+        const bool is_start = (starts >> lane) & 1u;
+        const bool is_end = (ends >> lane) & 1u;
+        const int rid_start = st.n_runs + __popc(starts & ((1u << lane) - 1u));
+        const int src = 31 - __clz(starts & (FULL >> (31 - lane)));
+        const int rid_b = __shfl_sync(FULL, rid_start, src & 31);
+        const int rid = key >= 0 ? rid_b : -1;
+        if (is_start) {
+          const int e = __ffs(ends & (FULL << lane)) - 1;
+          S.run[rid] = (unsigned)ty | ((unsigned)lane << 5) | ((unsigned)e << 10) | ((unsigned)band << 16);
+          S.uf[rid] = rid;
+        }
+        __syncwarp();
+        // ---- one union per adjacency with the runs of the row above
+        const int pk_m = __shfl_up_sync(FULL, st.prev_key, 1), pb_m = __shfl_up_sync(FULL, st.prev_band, 1);
+        const int pr_m = __shfl_up_sync(FULL, st.prev_rid, 1);
+        const int pk_p = __shfl_down_sync(FULL, st.prev_key, 1), pb_p = __shfl_down_sync(FULL, st.prev_band, 1);
+        const int pr_p = __shfl_down_sync(FULL, st.prev_rid, 1);
+        if (key >= 0 && ty > 0) {
+          const bool a0 = st.prev_key == key && st.prev_band == band;
+          const bool am = lane > 0 && pk_m == key && pb_m == band;
+          const bool ap = lane < 31 && pk_p == key && pb_p == band;
+          if (a0 && (is_start || !am)) uf_unite(S.uf, rid, st.prev_rid);
+          if (is_start && am && !a0) uf_unite(S.uf, rid, pr_m);
+          if (is_end && ap && !a0) uf_unite(S.uf, rid, pr_p);
+        }
+        if (ty == 0) st.b_top = rid;
+        if (ty == kTileH - 1) st.b_bot = rid;
+        const int lc = __shfl_sync(FULL, rid, 0), rc = __shfl_sync(FULL, rid, 31);
+        if (lane == ty) {
+          st.b_left = lc;
+          st.b_right = rc;
+        }
+        st.prev_key = key;
+        st.prev_band = band;
+        st.prev_rid = rid;
+        st.n_runs += nr;
       }
-      __syncwarp();
-      // ---- one union per adjacency with the runs of the row above
-      const int pk_m = __shfl_up_sync(FULL, st.prev_key, 1), pb_m = __shfl_up_sync(FULL, st.prev_band, 1);
-      const int pr_m = __shfl_up_sync(FULL, st.prev_rid, 1);
-      const int pk_p = __shfl_down_sync(FULL, st.prev_key, 1), pb_p = __shfl_down_sync(FULL, st.prev_band, 1);
-      const int pr_p = __shfl_down_sync(FULL, st.prev_rid, 1);
-      if (key >= 0 && ty > 0) {
-        const bool a0 = st.prev_key == key && st.prev_band == band;
-        const bool am = lane > 0 && pk_m == key && pb_m == band;
-        const bool ap = lane < 31 && pk_p == key && pb_p == band;
-        if (a0 && (is_start || !am)) uf_unite(S.uf, rid, st.prev_rid);
-        if (is_start && am && !a0) uf_unite(S.uf, rid, pr_m);
-        if (is_end && ap && !a0) uf_unite(S.uf, rid, pr_p);
-      }
-      if (ty == 0) st.b_top = rid;
-      if (ty == kTileH - 1) st.b_bot = rid;
-      const int lc = __shfl_sync(FULL, rid, 0), rc = __shfl_sync(FULL, rid, 31);
-      if (lane == ty) {
-        st.b_left = lc;
-        st.b_right = rc;
-      }
-      st.prev_key = key;
-      st.prev_band = band;
-      st.prev_rid = rid;
-      st.n_runs += nr;
     }
   }
   st.m2 = st.m1;
@@ -325,68 +376,91 @@ __device__ __forceinline__ void tile_warp_body(const TileParams& P, WarpSmem& S,
   st.b_top = st.b_bot = st.b_left = st.b_right = -1;
   st.n_runs = 0;
   bool overflow = false;
-  // rows are staged kRing ahead by bulk async copies; the candidate test of
-  // row ey + 1 (a dependent load) is issued while row ey is scanned
-  if (lane == 0) {
-#pragma unroll
-    for (int k = 0; k < kRing; ++k) bar_init(&S.bar[k]);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    for (int r = 0; r < kRing && r < NR; ++r) issue_row<HL>(S, r, T, P, hw);
+  if constexpr (!kStaged) {
+    // rows are loaded one ahead into two alternating register buffers
+    RowIn A, B;
+    load_row<HL>(A, T, 0, lane);
+    for (int ey = 0; ey < NR; ey += 2) {
+      if (ey + 1 < NR) load_row<HL>(B, T, ey + 1, lane);
+      if (scan_row<R>(A.a, A.g, A.inb, cand_of_px(T, A.d), ey, st, S, T, lane)) {
+        overflow = true;
+        break;
+      }
+      if (ey + 1 < NR) {
+        if (ey + 2 < NR) load_row<HL>(A, T, ey + 2, lane);
+        if (scan_row<R>(B.a, B.g, B.inb, cand_of_px(T, B.d), ey + 1, st, S, T, lane)) {
+          overflow = true;
+          break;
+        }
+      }
+    }
   }
-  __syncwarp();
-  const bool col_in = x0 + lane < W;
-  auto dom_of = [&](const int r) -> int {   // dominant id of ext row r (staged and waited for)
-    const int slot = r % kRing;
-    const unsigned meta = S.meta[slot];
-    if (!(r >= HL && r < HL + kTileH) || !(meta & 8u) || !col_in) return -1;
-    if (meta & 4u) return S.u.ring[slot].dom[((meta >> 12) & 3u) + lane];
-    return __ldg(T.dom + (long long)(y0 - HL + r) * W + x0 + lane);
-  };
-  auto cand_of = [&](const int d) -> int {
-    return d >= 0 && d < T.N && __ldg(T.cls + d) == 1 ? d : -1;
-  };
-  bar_wait(&S.bar[0], 0);
-  int c_next = cand_of(dom_of(0));
-  int ey = 0;
-  for (; ey < NR; ++ey) {
-    const int slot = ey % kRing;
-    const unsigned meta = S.meta[slot];
-    const bool inb = (meta & 8u) && col_in;
-    float a[3], g[3];
-    if (inb) {
-      const long long p = (long long)(y0 - HL + ey) * W + x0 + lane;
-      if (meta & 1u) {
-        const float* r = S.u.ring[slot].img + ((meta >> 8) & 3u) + 3 * lane;
-        a[0] = r[0]; a[1] = r[1]; a[2] = r[2];
-      } else {
-        a[0] = __ldg(T.img + 3 * p); a[1] = __ldg(T.img + 3 * p + 1); a[2] = __ldg(T.img + 3 * p + 2);
-      }
-      if (meta & 2u) {
-        const float* r = S.u.ring[slot].gt + ((meta >> 10) & 3u) + 3 * lane;
-        g[0] = r[0]; g[1] = r[1]; g[2] = r[2];
-      } else {
-        g[0] = __ldg(T.gtv + 3 * p); g[1] = __ldg(T.gtv + 3 * p + 1); g[2] = __ldg(T.gtv + 3 * p + 2);
-      }
-    } else {
-      a[0] = a[1] = a[2] = g[0] = g[1] = g[2] = 0.0f;
-    }
-    const int c_now = c_next;
-    int d_next = -1;
-    if (ey + 1 < NR) {
-      bar_wait(&S.bar[(ey + 1) % kRing], ((ey + 1) / kRing) & 1);
-      d_next = dom_of(ey + 1);
-      c_next = cand_of(d_next);
-    }
-    if (scan_row<R>(a, g, inb, c_now, ey, st, S, T, lane)) {
-      overflow = true;
-      break;
+#if ADPS_TW_STAGED
+  else {
+    // rows are staged kRing ahead by bulk async copies; the candidate test of
+    // row ey + 1 (a dependent load) is issued while row ey is scanned
+    if (lane == 0) {
+  #pragma unroll
+      for (int k = 0; k < kRing; ++k) bar_init(&S.bar[k]);
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+      for (int r = 0; r < kRing && r < NR; ++r) issue_row<HL>(S, r, T, P, hw);
     }
     __syncwarp();
-    if (lane == 0 && ey + kRing < NR) issue_row<HL>(S, ey + kRing, T, P, hw);
+    const bool col_in = x0 + lane < W;
+    auto dom_of = [&](const int r) -> int {   // dominant id of ext row r (staged and waited for)
+      const int slot = r % kRing;
+      const unsigned meta = S.meta[slot];
+      if (!(r >= HL && r < HL + kTileH) || !(meta & 8u) || !col_in) return -1;
+      if (meta & 4u) return S.u.ring[slot].dom[((meta >> 12) & 3u) + lane];
+      return __ldg(T.dom + (long long)(y0 - HL + r) * W + x0 + lane);
+    };
+    auto cand_of = [&](const int d) -> int {
+      return d >= 0 && d < T.N && __ldg(T.cls + d) == 1 ? d : -1;
+    };
+    bar_wait(&S.bar[0], 0);
+    int c_next = cand_of(dom_of(0));
+    int ey = 0;
+    for (; ey < NR; ++ey) {
+      const int slot = ey % kRing;
+      const unsigned meta = S.meta[slot];
+      const bool inb = (meta & 8u) && col_in;
+      float a[3], g[3];
+      if (inb) {
+        const long long p = (long long)(y0 - HL + ey) * W + x0 + lane;
+        if (meta & 1u) {
+          const float* r = S.u.ring[slot].img + ((meta >> 8) & 3u) + 3 * lane;
+          a[0] = r[0]; a[1] = r[1]; a[2] = r[2];
+        } else {
+          a[0] = __ldg(T.img + 3 * p); a[1] = __ldg(T.img + 3 * p + 1); a[2] = __ldg(T.img + 3 * p + 2);
+        }
+        if (meta & 2u) {
+          const float* r = S.u.ring[slot].gt + ((meta >> 10) & 3u) + 3 * lane;
+          g[0] = r[0]; g[1] = r[1]; g[2] = r[2];
+        } else {
+          g[0] = __ldg(T.gtv + 3 * p); g[1] = __ldg(T.gtv + 3 * p + 1); g[2] = __ldg(T.gtv + 3 * p + 2);
+        }
+      } else {
+        a[0] = a[1] = a[2] = g[0] = g[1] = g[2] = 0.0f;
+      }
+      const int c_now = c_next;
+      int d_next = -1;
+      if (ey + 1 < NR) {
+        bar_wait(&S.bar[(ey + 1) % kRing], ((ey + 1) / kRing) & 1);
+        d_next = dom_of(ey + 1);
+        c_next = cand_of(d_next);
+      }
+      if (scan_row<R>(a, g, inb, c_now, ey, st, S, T, lane)) {
+        overflow = true;
+        break;
+      }
+      __syncwarp();
+      if (lane == 0 && ey + kRing < NR) issue_row<HL>(S, ey + kRing, T, P, hw);
+    }
+    if (overflow) {   // no bulk copy may still target this warp's ring when it leaves
+      for (int r = ey + 2; r < NR && r < ey + kRing; ++r) bar_wait(&S.bar[r % kRing], (r / kRing) & 1);
+    }
   }
-  if (overflow) {   // no bulk copy may still target this warp's ring when it leaves
-    for (int r = ey + 2; r < NR && r < ey + kRing; ++r) bar_wait(&S.bar[r % kRing], (r / kRing) & 1);
-  }
+#endif
   const int n_runs = st.n_runs;
   const int b_top = st.b_top, b_bot = st.b_bot, b_left = st.b_left, b_right = st.b_right;
   if (overflow) {
@@ -499,7 +573,7 @@ __device__ __forceinline__ void tile_warp_body(const TileParams& P, WarpSmem& S,
 }
 
 template <int R>
-__global__ void __launch_bounds__(kWarpsPerBlock * 32, 4) tile_warp_kernel(TileParams P, long long n_tiles) {
+__global__ void __launch_bounds__(kWarpsPerBlock * 32, ADPS_TW_MINBLOCKS) tile_warp_kernel(TileParams P, long long n_tiles) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   WarpSmem& S = reinterpret_cast<WarpSmem*>(smem_raw)[wid];
