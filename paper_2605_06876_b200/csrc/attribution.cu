@@ -38,13 +38,16 @@ __device__ __forceinline__ double raw_l1(const float* __restrict__ img, const fl
 // input byte of the view (image, gt, dominant map) is read exactly once.
 __global__ void minmax_kernel(const float* __restrict__ image, const float* __restrict__ gt,
                               const int* __restrict__ dominant, long long hw, unsigned long long* __restrict__ lohi,
-                              const unsigned char* __restrict__ cls, int N, unsigned char* __restrict__ dom_flag) {
+                              const unsigned char* __restrict__ cls, int N, unsigned char* __restrict__ dom_flag,
+                              unsigned* __restrict__ cand_bits) {
   const int v = blockIdx.y;
   const float* img = image + (long long)v * hw * 3;
   const float* g = gt + (long long)v * hw * 3;
   const int* dom = dominant + (long long)v * hw;
+  unsigned* bits = cand_bits + (long long)v * ((hw + 31) / 32);
   const int lane = threadIdx.x & 31;
   double lo = INFINITY, hi = 0.0;
+  // base is a multiple of 32, so a warp's pixels are one word of cand_bits
   for (long long base = (long long)blockIdx.x * blockDim.x; base < hw; base += (long long)gridDim.x * blockDim.x) {
     const long long p = base + threadIdx.x;
     int d = -1;
@@ -54,10 +57,19 @@ __global__ void minmax_kernel(const float* __restrict__ image, const float* __re
       hi = fmax(hi, r);
       d = __ldg(dom + p);
     }
-    if (dom_flag) {
-      const int left = __shfl_up_sync(0xffffffffu, d, 1);
-      if ((lane == 0 || left != d) && d >= 0 && d < N && __ldg(cls + d) == 1 && dom_flag[d] == 0) dom_flag[d] = 1;
+    // split-candidate test once per run of equal ids: ever-dominant flag and
+    // the per-pixel candidate bit the tile pass reads instead of cls[D]
+    const int left = __shfl_up_sync(0xffffffffu, d, 1);
+    const bool head = lane == 0 || left != d;
+    bool isc = false;
+    if (head && d >= 0 && d < N && __ldg(cls + d) == 1) {
+      isc = true;
+      if (dom_flag && dom_flag[d] == 0) dom_flag[d] = 1;
     }
+    const unsigned heads = __ballot_sync(0xffffffffu, head);
+    isc = __shfl_sync(0xffffffffu, isc, 31 - __clz(heads & (0xffffffffu >> (31 - lane))));
+    const unsigned word = __ballot_sync(0xffffffffu, isc);
+    if (lane == 0 && base + (threadIdx.x & ~31) < hw) bits[(base + threadIdx.x) >> 5] = word;
   }
   for (int o = 16; o > 0; o >>= 1) {
     lo = fmin(lo, __shfl_xor_sync(0xffffffffu, lo, o));
@@ -544,7 +556,7 @@ cudaError_t launch_minmax(const AttributionArgs& a, const int* split_list, Count
   const long long hw = (long long)a.H * a.W;
   dim3 mg((unsigned)((hw + 256 * 8 - 1) / (256 * 8)), (unsigned)a.V);
   if (mg.x > 1024) mg.x = 1024;
-  minmax_kernel<<<mg, 256, 0, s>>>(a.image, a.gt, a.dom, hw, a.lohi, a.cls, a.N, a.dom_flag);
+  minmax_kernel<<<mg, 256, 0, s>>>(a.image, a.gt, a.dom, hw, a.lohi, a.cls, a.N, a.dom_flag, a.cand_bits);
   int nt = a.V * a.L;
   thresholds_kernel<<<(nt + 127) / 128, 128, 0, s>>>(a.lohi, a.V, a.L, a.tau, a.lo, a.thr);
   fallback_count_kernel<<<sm_count * 2, 256, 0, s>>>(split_list, a.dom_flag, ctr);
@@ -581,6 +593,7 @@ cudaError_t launch_attribution(const AttributionArgs& a, cudaStream_t s, MarkFn 
   P.dbg_b = a.dbg_b;
   P.overflow = a.overflow;
   P.n_views = a.V;
+  P.cand_bits = a.cand_bits;
   P.deferred = a.deferred;
   P.n_deferred = a.n_deferred;
   const long long nblocks = (long long)P.tiles_x * P.tiles_y * a.V;

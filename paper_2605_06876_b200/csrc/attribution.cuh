@@ -31,6 +31,7 @@ struct TileParams {
   int n_views;
   int* deferred;                     // tiles the warp kernel hands to the block kernel
   unsigned long long* n_deferred;
+  const unsigned* cand_bits;         // [V][ceil(H*W/32)]: bit p = D[p] is a split candidate
 };
 
 struct BorderParams {
@@ -69,6 +70,7 @@ struct AttributionArgs {
   int* deferred;                     // [n_tiles]
   unsigned long long* n_deferred;
   int tile_path;                     // 0 auto (warp kernel + deferred), 1 block kernel only
+  unsigned* cand_bits;               // [V][ceil(H*W/32)], written by the minmax pass
 };
 
 // warp-per-tile scanline CCL (r_erode <= 3); defers tiles with > kWarpMaxRuns runs

@@ -79,7 +79,7 @@ struct adps_plan {
   Buf lohi, lo, thr, cams;
   // tiles / fragments / regions
   Buf border, partials, partial_parent, regions, props, valid, keys, vals, keys_sorted, vals_sorted;
-  Buf idx, uf, groups, children, dbg_stats, dbg_child, deferred;
+  Buf idx, uf, groups, children, dbg_stats, dbg_child, deferred, cand_bits;
   // device normals (numpy PCG64 stream)
   Buf nrm_val, nrm_len, nrm_acc, nrm_reach, nrm_rmax, nrm_walked, nrm_idx, nrm_tmp;
   // merge / cap scratch (proposal space)
@@ -226,7 +226,7 @@ extern "C" adps_status adps_plan_destroy(adps_plan* P) {
                  &P->ext_key, &P->ext_val, &P->ext_key_sorted, &P->ext_val_sorted, &P->cand_key, &P->cand_val,
                  &P->cand_key_sorted, &P->cand_val_sorted, &P->scan3_val, &P->scan3_flag, &P->scan3_ticket,
                  &P->large_of, &P->lp_cnt, &P->lp_off, &P->tile_cnt, &P->tile_off, &P->mkey, &P->mval,
-                 &P->mkey_sorted, &P->mval_sorted, &P->boxes, &P->tile_pairs, &P->deferred,
+                 &P->mkey_sorted, &P->mval_sorted, &P->boxes, &P->tile_pairs, &P->deferred, &P->cand_bits,
                  &P->nrm_val, &P->nrm_len, &P->nrm_acc, &P->nrm_reach, &P->nrm_rmax, &P->nrm_walked,
                  &P->nrm_idx, &P->nrm_tmp};
   for (Buf* b : bufs)
@@ -428,6 +428,7 @@ static AttributionArgs attr_args(adps_plan* P, int V, int H, int W, const adps_c
   a.deferred = P->deferred.as<int>();
   a.n_deferred = &ctr->n_deferred;
   a.tile_path = P->tile_path;
+  a.cand_bits = P->cand_bits.as<unsigned>();
   return a;
 }
 
@@ -503,6 +504,7 @@ extern "C" adps_status adps_step_phase1_begin(adps_plan* P, void* stream_v, cons
   CK(ensure(P->cams, 8ll * 18 * V));
   CK(ensure(P->border, 4ll * n_tiles * kBorderSlots));
   CK(ensure(P->deferred, 4ll * n_tiles));
+  CK(ensure(P->cand_bits, 4ll * V * ((hw + 31) / 32)));
   CK(ensure(P->ctr, sizeof(Counters)));
   if (P->cams_host_cap < V) {
     if (P->cams_host) cudaFreeHost(P->cams_host);

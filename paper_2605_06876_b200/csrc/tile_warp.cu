@@ -28,29 +28,14 @@ namespace adps {
 constexpr int kWarpMaxRuns = 256;
 constexpr int kWarpsPerBlock = 8;
 
-// rows reach the warp either by per-lane loads a row ahead (default) or staged
-// kRing rows ahead in shared memory by bulk async copies (kStaged)
-#ifndef ADPS_TW_STAGED
-#define ADPS_TW_STAGED 0
-#endif
 #ifndef ADPS_TW_FAST
 #define ADPS_TW_FAST 1
 #endif
 #ifndef ADPS_TW_MINBLOCKS
 #define ADPS_TW_MINBLOCKS 4
 #endif
-constexpr bool kStaged = ADPS_TW_STAGED != 0;
-constexpr int kRing = 4;            // rows in flight per warp (bulk async copies)
-constexpr int kRingF = 112;         // floats per staged image row: 32 px * 3 + 16 B alignment slack, x16 B
-constexpr int kRingD = 40;          // ints per staged dominant row: 32 + slack
 
-struct RingSlot {
-  float img[kRingF];
-  float gt[kRingF];
-  int dom[kRingD];
-};
-
-struct PostSmem {                   // used after the row scan; aliases the ring
+struct PostSmem {                   // used after the row scan
   int aux[kWarpMaxRuns];            // fragment id of a root, -1 otherwise
   int mom[32][6];
   unsigned char touch[32];
@@ -60,16 +45,9 @@ struct WarpSmem {
   int uf[kWarpMaxRuns];
   unsigned run[kWarpMaxRuns];       // ty | s << 5 | e << 10 | band << 16
   union {
-#if ADPS_TW_STAGED
-    RingSlot ring[kRing];
-#endif
     PostSmem post;
   } u;
-  unsigned long long bar[kRing];    // one mbarrier per ring slot
-  unsigned meta[kRing];             // per staged row: bit0/1/2 img/gt/dom staged, bit3 row inside
-                                    // the image, bits 8-9/10-11/12-13 element offset of x0
 };
-static_assert(sizeof(RingSlot) % 16 == 0 && sizeof(WarpSmem) % 16 == 0, "bulk copy alignment");
 
 size_t tile_warp_smem_bytes() { return sizeof(WarpSmem) * kWarpsPerBlock; }
 
@@ -86,80 +64,38 @@ struct TileConst {
   const float* img;
   const float* gtv;
   const int* dom;
-  const unsigned char* cls;
+  const unsigned* cbits;   // candidate bits of the view
   const double* thr;
   double lo, x_m, t1, t2, t3;
-  int x0, y0, W, H, L, N;
+  long long p0;            // pixel index of (x0 + lane, y0 - HL): ext row ey is p0 + ey * W
+  int W, L;
+  int ey_lo, ey_hi;        // ext rows inside the image
+  bool col_in;             // x0 + lane < W
   unsigned long long hl_mask, hr_mask;   // bit ey: metric bit of the left/right halo pixel of ext row ey
 };
-
-// ---------------------------------------------------------------- row ring
-__device__ __forceinline__ unsigned smem_u32(const void* p) {
-  return (unsigned)__cvta_generic_to_shared(p);
-}
-__device__ __forceinline__ void bar_init(unsigned long long* bar) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(bar)) : "memory");
-}
-__device__ __forceinline__ void bar_arrive_tx(unsigned long long* bar, unsigned bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
-               : "memory");
-}
-__device__ __forceinline__ void bar_wait(unsigned long long* bar, unsigned parity) {
-  asm volatile(
-      "{\n\t.reg .pred P;\n"
-      "WAIT_%=:\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 P, [%0], %1;\n\t"
-      "@!P bra WAIT_%=;\n}" ::"r"(smem_u32(bar)),
-      "r"(parity)
-      : "memory");
-}
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, unsigned long long* bar) {
-  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                   smem_u32(dst)),
-               "l"(src), "r"(bytes), "r"(smem_u32(bar))
-               : "memory");
-}
-
-// 16-byte aligned cover [lo, hi) of [p, p + bytes); usable when it stays inside [base, end)
-struct Cover {
-  const char* lo;
-  unsigned bytes;
-  bool ok;
-};
-__device__ __forceinline__ Cover cover(const void* p, unsigned bytes, const void* base, const void* end) {
-  const unsigned long long a = (unsigned long long)p;
-  const unsigned long long lo = a & ~15ull, hi = (a + bytes + 15) & ~15ull;
-  Cover c;
-  c.lo = (const char*)lo;
-  c.bytes = (unsigned)(hi - lo);
-  c.ok = lo >= (unsigned long long)base && hi <= (unsigned long long)end;
-  return c;
-}
 
 // one image row of the tile (lane = x)
 struct RowIn {
   float a[3], g[3];
-  int d;
+  int d;      // dominant id if it is a split candidate (tile rows), else -1
   bool inb;
 };
 
 template <int HL>
 __device__ __forceinline__ void load_row(RowIn& r, const TileConst& T, int ey, int lane) {
-  const int y = T.y0 - HL + ey;
-  const int x = T.x0 + lane;
-  r.inb = y >= 0 && y < T.H && x < T.W;
-  const long long p = r.inb ? (long long)y * T.W + x : 0;
+  r.inb = ey >= T.ey_lo && ey < T.ey_hi && T.col_in;
+  const long long p = T.p0 + (long long)ey * T.W;
   const bool tile_row = ey >= HL && ey < HL + kTileH;
 #pragma unroll
   for (int c = 0; c < 3; ++c) {
     r.a[c] = r.inb ? __ldg(T.img + 3 * p + c) : 0.0f;
     r.g[c] = r.inb ? __ldg(T.gtv + 3 * p + c) : 0.0f;
   }
-  r.d = r.inb && tile_row ? __ldg(T.dom + p) : -1;
-}
-
-__device__ __forceinline__ int cand_of_px(const TileConst& T, const int d) {
-  return d >= 0 && d < T.N && __ldg(T.cls + d) == 1 ? d : -1;
+  // candidate bit (written by the minmax pass) instead of a dependent cls[D] load
+  const bool need = r.inb && tile_row;
+  const int d = need ? __ldg(T.dom + p) : -1;
+  const unsigned cb = need ? __ldg(T.cbits + (p >> 5)) : 0u;
+  r.d = (cb >> (p & 31)) & 1u ? d : -1;
 }
 
 // np.abs(rendered - gt).sum(axis=-1) == (|d0| + |d1|) + |d2| in fp64
@@ -181,42 +117,6 @@ __device__ __forceinline__ bool metric_at(const TileConst& T, int x, int y) {
   return dsub(raw_l1_f(a, g), T.lo) >= T.x_m;
 }
 
-#if ADPS_TW_STAGED
-// lane 0: stage ext row ey (image, gt and -- for tile rows -- dominant ids)
-// into its ring slot with bulk async copies completing on the slot's mbarrier
-template <int HL>
-__device__ __forceinline__ void issue_row(WarpSmem& S, const int ey, const TileConst& T, const TileParams& P,
-                                          const long long hw) {
-  const int slot = ey % kRing;
-  unsigned long long* bar = &S.bar[slot];
-  const int y = T.y0 - HL + ey;
-  unsigned meta = 0, tx = 0;
-  Cover ci, cg, cd;
-  ci.ok = cg.ok = cd.ok = false;
-  if (y >= 0 && y < T.H) {
-    meta |= 8u;
-    const int n = min(kTileW, T.W - T.x0);
-    const long long p = (long long)y * T.W + T.x0;
-    const long long total = hw * P.n_views;
-    ci = cover(T.img + 3 * p, 12u * n, P.image, P.image + 3 * total);
-    cg = cover(T.gtv + 3 * p, 12u * n, P.gt, P.gt + 3 * total);
-    meta |= (ci.ok ? 1u : 0u) | (cg.ok ? 2u : 0u);
-    meta |= (unsigned)(((unsigned long long)(T.img + 3 * p) & 15) >> 2) << 8;
-    meta |= (unsigned)(((unsigned long long)(T.gtv + 3 * p) & 15) >> 2) << 10;
-    if (ey >= HL && ey < HL + kTileH) {
-      cd = cover(T.dom + p, 4u * n, P.dom, P.dom + total);
-      meta |= (cd.ok ? 4u : 0u) | ((unsigned)(((unsigned long long)(T.dom + p) & 15) >> 2) << 12);
-    }
-    tx = (ci.ok ? ci.bytes : 0u) + (cg.ok ? cg.bytes : 0u) + (cd.ok ? cd.bytes : 0u);
-  }
-  S.meta[slot] = meta;
-  bar_arrive_tx(bar, tx);   // released by the copies (or at once when nothing is staged)
-  if (ci.ok) bulk_g2s(S.u.ring[slot].img, ci.lo, ci.bytes, bar);
-  if (cg.ok) bulk_g2s(S.u.ring[slot].gt, cg.lo, cg.bytes, bar);
-  if (cd.ok) bulk_g2s(S.u.ring[slot].dom, cd.lo, cd.bytes, bar);
-}
-
-#endif
 
 // one ext row: metric mask, then (once its erosion window is complete) the
 // runs of tile row ey - SPAN and their unions with the row above.
@@ -331,16 +231,18 @@ __device__ __forceinline__ void tile_warp_body(const TileParams& P, WarpSmem& S,
   const int v = (int)(tile / tiles_per_view);
   const int tin = (int)(tile % tiles_per_view);
   TileConst T;
-  T.x0 = (tin % P.tiles_x) * kTileW;
-  T.y0 = (tin / P.tiles_x) * kTileH;
-  T.W = P.W;
-  T.H = P.H;
-  const long long hw = (long long)T.W * T.H;
+  const int x0 = (tin % P.tiles_x) * kTileW, y0 = (tin / P.tiles_x) * kTileH;
+  const int W = P.W, H = P.H;
+  T.W = W;
+  T.p0 = (long long)(y0 - HL) * W + x0 + lane;
+  T.ey_lo = HL - y0 > 0 ? HL - y0 : 0;
+  T.ey_hi = H - y0 + HL < NR ? H - y0 + HL : NR;
+  T.col_in = x0 + lane < W;
+  const long long hw = (long long)W * H;
   T.img = P.image + (long long)v * hw * 3;
   T.gtv = P.gt + (long long)v * hw * 3;
   T.dom = P.dom + (long long)v * hw;
-  T.cls = P.cls;
-  T.N = P.N;
+  T.cbits = P.cand_bits + (long long)v * ((hw + 31) / 32);
   T.L = P.L;
   T.lo = P.lo[v];
   T.thr = P.thr + (long long)v * P.L;
@@ -349,7 +251,6 @@ __device__ __forceinline__ void tile_warp_body(const TileParams& P, WarpSmem& S,
   T.t1 = T.L > 1 ? T.thr[1] : kInf;
   T.t2 = T.L > 2 ? T.thr[2] : kInf;
   T.t3 = T.L > 3 ? T.thr[3] : kInf;
-  const int x0 = T.x0, y0 = T.y0, W = T.W, H = T.H;
   // halo columns of all ext rows at once (lane = ext row, then ext rows 32..)
   T.hl_mask = 0;
   T.hr_mask = 0;
@@ -376,91 +277,25 @@ __device__ __forceinline__ void tile_warp_body(const TileParams& P, WarpSmem& S,
   st.b_top = st.b_bot = st.b_left = st.b_right = -1;
   st.n_runs = 0;
   bool overflow = false;
-  if constexpr (!kStaged) {
+  {
     // rows are loaded one ahead into two alternating register buffers
     RowIn A, B;
     load_row<HL>(A, T, 0, lane);
     for (int ey = 0; ey < NR; ey += 2) {
       if (ey + 1 < NR) load_row<HL>(B, T, ey + 1, lane);
-      if (scan_row<R>(A.a, A.g, A.inb, cand_of_px(T, A.d), ey, st, S, T, lane)) {
+      if (scan_row<R>(A.a, A.g, A.inb, A.d, ey, st, S, T, lane)) {
         overflow = true;
         break;
       }
       if (ey + 1 < NR) {
         if (ey + 2 < NR) load_row<HL>(A, T, ey + 2, lane);
-        if (scan_row<R>(B.a, B.g, B.inb, cand_of_px(T, B.d), ey + 1, st, S, T, lane)) {
+        if (scan_row<R>(B.a, B.g, B.inb, B.d, ey + 1, st, S, T, lane)) {
           overflow = true;
           break;
         }
       }
     }
   }
-#if ADPS_TW_STAGED
-  else {
-    // rows are staged kRing ahead by bulk async copies; the candidate test of
-    // row ey + 1 (a dependent load) is issued while row ey is scanned
-    if (lane == 0) {
-  #pragma unroll
-      for (int k = 0; k < kRing; ++k) bar_init(&S.bar[k]);
-      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-      for (int r = 0; r < kRing && r < NR; ++r) issue_row<HL>(S, r, T, P, hw);
-    }
-    __syncwarp();
-    const bool col_in = x0 + lane < W;
-    auto dom_of = [&](const int r) -> int {   // dominant id of ext row r (staged and waited for)
-      const int slot = r % kRing;
-      const unsigned meta = S.meta[slot];
-      if (!(r >= HL && r < HL + kTileH) || !(meta & 8u) || !col_in) return -1;
-      if (meta & 4u) return S.u.ring[slot].dom[((meta >> 12) & 3u) + lane];
-      return __ldg(T.dom + (long long)(y0 - HL + r) * W + x0 + lane);
-    };
-    auto cand_of = [&](const int d) -> int {
-      return d >= 0 && d < T.N && __ldg(T.cls + d) == 1 ? d : -1;
-    };
-    bar_wait(&S.bar[0], 0);
-    int c_next = cand_of(dom_of(0));
-    int ey = 0;
-    for (; ey < NR; ++ey) {
-      const int slot = ey % kRing;
-      const unsigned meta = S.meta[slot];
-      const bool inb = (meta & 8u) && col_in;
-      float a[3], g[3];
-      if (inb) {
-        const long long p = (long long)(y0 - HL + ey) * W + x0 + lane;
-        if (meta & 1u) {
-          const float* r = S.u.ring[slot].img + ((meta >> 8) & 3u) + 3 * lane;
-          a[0] = r[0]; a[1] = r[1]; a[2] = r[2];
-        } else {
-          a[0] = __ldg(T.img + 3 * p); a[1] = __ldg(T.img + 3 * p + 1); a[2] = __ldg(T.img + 3 * p + 2);
-        }
-        if (meta & 2u) {
-          const float* r = S.u.ring[slot].gt + ((meta >> 10) & 3u) + 3 * lane;
-          g[0] = r[0]; g[1] = r[1]; g[2] = r[2];
-        } else {
-          g[0] = __ldg(T.gtv + 3 * p); g[1] = __ldg(T.gtv + 3 * p + 1); g[2] = __ldg(T.gtv + 3 * p + 2);
-        }
-      } else {
-        a[0] = a[1] = a[2] = g[0] = g[1] = g[2] = 0.0f;
-      }
-      const int c_now = c_next;
-      int d_next = -1;
-      if (ey + 1 < NR) {
-        bar_wait(&S.bar[(ey + 1) % kRing], ((ey + 1) / kRing) & 1);
-        d_next = dom_of(ey + 1);
-        c_next = cand_of(d_next);
-      }
-      if (scan_row<R>(a, g, inb, c_now, ey, st, S, T, lane)) {
-        overflow = true;
-        break;
-      }
-      __syncwarp();
-      if (lane == 0 && ey + kRing < NR) issue_row<HL>(S, ey + kRing, T, P, hw);
-    }
-    if (overflow) {   // no bulk copy may still target this warp's ring when it leaves
-      for (int r = ey + 2; r < NR && r < ey + kRing; ++r) bar_wait(&S.bar[r % kRing], (r / kRing) & 1);
-    }
-  }
-#endif
   const int n_runs = st.n_runs;
   const int b_top = st.b_top, b_bot = st.b_bot, b_left = st.b_left, b_right = st.b_right;
   if (overflow) {

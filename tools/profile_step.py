@@ -1,0 +1,40 @@
+"""One densify step of a bench config bracketed by cudaProfilerStart/Stop (dev tool).
+
+ncu --profile-from-start off ... python tools/profile_step.py [config3]
+captures exactly the launches of one warm step (renders resident, as bench.py).
+"""
+import os
+import sys
+
+import numpy as np
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from paper_2605_06876_b200 import operator as op  # noqa: E402
+from paper_2605_06876_b200 import synth as S  # noqa: E402
+from paper_2605_06876_b200.types import AdpSplitConfig  # noqa: E402
+
+name = sys.argv[1] if len(sys.argv) > 1 else "config3"
+wl = S.CONFIGS[name]
+ini, cams, (ga, den), gt = wl.build()
+plan = op.Plan("cuda:0")
+g = op.GaussianTensors.from_numpy(*ini.arrays(), device="cuda")
+gt_img, _ = plan.render(op.GaussianTensors.from_numpy(*gt.arrays(), device="cuda"), cams)
+img, dom = plan.render(g, cams)
+cfg = AdpSplitConfig(v_views=len(cams), n_max=wl.n_max)
+ga_t, den_t = torch.as_tensor(ga, device="cuda"), torch.as_tensor(den, device="cuda")
+
+
+def step():
+    return op.densify_step(g, ini.extent, cams, gt_img, ga_t, den_t, cfg, np.random.default_rng(0),
+                           renders=(img, dom), plan=plan, view_ids=list(range(len(cams))))
+
+
+for _ in range(3):
+    step()
+torch.cuda.synchronize()
+torch.cuda.cudart().cudaProfilerStart()
+res = step()
+torch.cuda.synchronize()
+torch.cuda.cudart().cudaProfilerStop()
+print("deferred tiles", plan.deferred_tiles(), "counts", res.counts)
