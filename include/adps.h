@@ -217,6 +217,8 @@ ADPS_API adps_status adps_get_timing(adps_plan* plan, double* ms, int32_t max_en
 #define ADPS_PARAM_DEFERRED_TILES 3
 #define ADPS_PARAM_NORMALS_CONSUMED 4   /* read-only, see adps_normals_pcg64 */
 #define ADPS_PARAM_NORMALS_STATUS 5     /* read-only, see adps_normals_pcg64 */
+#define ADPS_PARAM_RAW_CACHE 6          /* 1 (default): the minmax pass caches the fp64 raw
+                                           L1 error (8 B/px) for the warp CCL; 0: recompute */
 ADPS_API adps_status adps_set_param(adps_plan* plan, int32_t key, int64_t value);
 ADPS_API adps_status adps_get_param(adps_plan* plan, int32_t key, int64_t* value);
 

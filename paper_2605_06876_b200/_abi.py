@@ -17,7 +17,7 @@ ADPS_OK, ADPS_INVALID_ARG, ADPS_V_TOO_LARGE, ADPS_DEGENERATE_RAY = 0, 1, 2, 3
 ADPS_CUDA_ERROR, ADPS_OOM, ADPS_BAD_STATE = 4, 5, 6
 CASE_SPLIT, CASE_FALLBACK, CASE_RESET = 0, 1, 2
 PARAM_LARGE_THRESHOLD, PARAM_TILE_PATH, PARAM_DEFERRED_TILES = 1, 2, 3
-PARAM_NORMALS_CONSUMED, PARAM_NORMALS_STATUS = 4, 5
+PARAM_NORMALS_CONSUMED, PARAM_NORMALS_STATUS, PARAM_RAW_CACHE = 4, 5, 6
 
 vp = C.c_void_p
 

@@ -39,7 +39,7 @@ __device__ __forceinline__ double raw_l1(const float* __restrict__ img, const fl
 __global__ void minmax_kernel(const float* __restrict__ image, const float* __restrict__ gt,
                               const int* __restrict__ dominant, long long hw, unsigned long long* __restrict__ lohi,
                               const unsigned char* __restrict__ cls, int N, unsigned char* __restrict__ dom_flag,
-                              unsigned* __restrict__ cand_bits) {
+                              unsigned* __restrict__ cand_bits, double* __restrict__ raw_out) {
   const int v = blockIdx.y;
   const float* img = image + (long long)v * hw * 3;
   const float* g = gt + (long long)v * hw * 3;
@@ -53,6 +53,7 @@ __global__ void minmax_kernel(const float* __restrict__ image, const float* __re
     int d = -1;
     if (p < hw) {
       const double r = raw_l1(img, g, p);
+      if (raw_out) raw_out[(long long)v * hw + p] = r;
       lo = fmin(lo, r);
       hi = fmax(hi, r);
       d = __ldg(dom + p);
@@ -556,7 +557,7 @@ cudaError_t launch_minmax(const AttributionArgs& a, const int* split_list, Count
   const long long hw = (long long)a.H * a.W;
   dim3 mg((unsigned)((hw + 256 * 8 - 1) / (256 * 8)), (unsigned)a.V);
   if (mg.x > 1024) mg.x = 1024;
-  minmax_kernel<<<mg, 256, 0, s>>>(a.image, a.gt, a.dom, hw, a.lohi, a.cls, a.N, a.dom_flag, a.cand_bits);
+  minmax_kernel<<<mg, 256, 0, s>>>(a.image, a.gt, a.dom, hw, a.lohi, a.cls, a.N, a.dom_flag, a.cand_bits, a.raw);
   int nt = a.V * a.L;
   thresholds_kernel<<<(nt + 127) / 128, 128, 0, s>>>(a.lohi, a.V, a.L, a.tau, a.lo, a.thr);
   fallback_count_kernel<<<sm_count * 2, 256, 0, s>>>(split_list, a.dom_flag, ctr);
@@ -594,6 +595,7 @@ cudaError_t launch_attribution(const AttributionArgs& a, cudaStream_t s, MarkFn 
   P.overflow = a.overflow;
   P.n_views = a.V;
   P.cand_bits = a.cand_bits;
+  P.raw = a.raw;
   P.deferred = a.deferred;
   P.n_deferred = a.n_deferred;
   const long long nblocks = (long long)P.tiles_x * P.tiles_y * a.V;

@@ -32,6 +32,7 @@ struct TileParams {
   int* deferred;                     // tiles the warp kernel hands to the block kernel
   unsigned long long* n_deferred;
   const unsigned* cand_bits;         // [V][ceil(H*W/32)]: bit p = D[p] is a split candidate
+  const double* raw;                 // [V][H*W] raw L1 error cached by the minmax pass, or null
 };
 
 struct BorderParams {
@@ -71,6 +72,7 @@ struct AttributionArgs {
   unsigned long long* n_deferred;
   int tile_path;                     // 0 auto (warp kernel + deferred), 1 block kernel only
   unsigned* cand_bits;               // [V][ceil(H*W/32)], written by the minmax pass
+  double* raw;                       // [V][H*W] raw L1 error written by the minmax pass, or null
 };
 
 // warp-per-tile scanline CCL (r_erode <= 3); defers tiles with > kWarpMaxRuns runs

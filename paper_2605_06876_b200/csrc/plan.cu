@@ -13,6 +13,10 @@
 #include "attribution.cuh"
 #include "merge.cuh"
 #include "normals.cuh"
+
+#ifndef ADPS_RAW_CACHE_DEFAULT
+#define ADPS_RAW_CACHE_DEFAULT 1
+#endif
 #include "render.cuh"
 #include "split.cuh"
 
@@ -79,7 +83,7 @@ struct adps_plan {
   Buf lohi, lo, thr, cams;
   // tiles / fragments / regions
   Buf border, partials, partial_parent, regions, props, valid, keys, vals, keys_sorted, vals_sorted;
-  Buf idx, uf, groups, children, dbg_stats, dbg_child, deferred, cand_bits;
+  Buf idx, uf, groups, children, dbg_stats, dbg_child, deferred, cand_bits, rawc;
   // device normals (numpy PCG64 stream)
   Buf nrm_val, nrm_len, nrm_acc, nrm_reach, nrm_rmax, nrm_walked, nrm_idx, nrm_tmp;
   // merge / cap scratch (proposal space)
@@ -119,6 +123,8 @@ struct adps_plan {
   long long lib_calls = 0;
   int large_threshold = 32;
   int tile_path = 0;   // 0 warp CCL + deferred block CCL, 1 block CCL only
+  int raw_cache = ADPS_RAW_CACHE_DEFAULT;   // minmax pass caches the raw L1 error for the warp CCL
+  bool use_raw = false;                     // decided per phase 1
   // arguments saved by phase1_begin for phase1_end
   bool have_begin = false;
   struct {
@@ -226,7 +232,7 @@ extern "C" adps_status adps_plan_destroy(adps_plan* P) {
                  &P->ext_key, &P->ext_val, &P->ext_key_sorted, &P->ext_val_sorted, &P->cand_key, &P->cand_val,
                  &P->cand_key_sorted, &P->cand_val_sorted, &P->scan3_val, &P->scan3_flag, &P->scan3_ticket,
                  &P->large_of, &P->lp_cnt, &P->lp_off, &P->tile_cnt, &P->tile_off, &P->mkey, &P->mval,
-                 &P->mkey_sorted, &P->mval_sorted, &P->boxes, &P->tile_pairs, &P->deferred, &P->cand_bits,
+                 &P->mkey_sorted, &P->mval_sorted, &P->boxes, &P->tile_pairs, &P->deferred, &P->cand_bits, &P->rawc,
                  &P->nrm_val, &P->nrm_len, &P->nrm_acc, &P->nrm_reach, &P->nrm_rmax, &P->nrm_walked,
                  &P->nrm_idx, &P->nrm_tmp};
   for (Buf* b : bufs)
@@ -429,6 +435,7 @@ static AttributionArgs attr_args(adps_plan* P, int V, int H, int W, const adps_c
   a.n_deferred = &ctr->n_deferred;
   a.tile_path = P->tile_path;
   a.cand_bits = P->cand_bits.as<unsigned>();
+  a.raw = P->use_raw ? P->rawc.as<double>() : nullptr;
   return a;
 }
 
@@ -505,6 +512,8 @@ extern "C" adps_status adps_step_phase1_begin(adps_plan* P, void* stream_v, cons
   CK(ensure(P->border, 4ll * n_tiles * kBorderSlots));
   CK(ensure(P->deferred, 4ll * n_tiles));
   CK(ensure(P->cand_bits, 4ll * V * ((hw + 31) / 32)));
+  P->use_raw = P->raw_cache && P->tile_path == 0 && !P->dbg_m && cfg->r_erode <= 3;
+  if (P->use_raw) CK(ensure(P->rawc, 8ll * total_px));
   CK(ensure(P->ctr, sizeof(Counters)));
   if (P->cams_host_cap < V) {
     if (P->cams_host) cudaFreeHost(P->cams_host);
@@ -1029,6 +1038,11 @@ extern "C" adps_status adps_set_param(adps_plan* P, int32_t key, int64_t value) 
     P->large_threshold = (int)value;
     return ADPS_OK;
   }
+  if (key == ADPS_PARAM_RAW_CACHE) {
+    if (value < 0 || value > 1) return fail(ADPS_INVALID_ARG, "raw cache must be 0 or 1");
+    P->raw_cache = (int)value;
+    return ADPS_OK;
+  }
   if (key == ADPS_PARAM_TILE_PATH) {
     if (value < 0 || value > 1) return fail(ADPS_INVALID_ARG, "tile path must be 0 (warp) or 1 (block)");
     P->tile_path = (int)value;
@@ -1042,6 +1056,7 @@ extern "C" adps_status adps_get_param(adps_plan* P, int32_t key, int64_t* value)
   switch (key) {
     case ADPS_PARAM_LARGE_THRESHOLD: *value = P->large_threshold; return ADPS_OK;
     case ADPS_PARAM_TILE_PATH: *value = P->tile_path; return ADPS_OK;
+    case ADPS_PARAM_RAW_CACHE: *value = P->raw_cache; return ADPS_OK;
     case ADPS_PARAM_DEFERRED_TILES: *value = P->ctr_host ? (int64_t)P->ctr_host->n_deferred : 0; return ADPS_OK;
     case ADPS_PARAM_NORMALS_CONSUMED:
       *value = P->ctr_host ? (int64_t)P->ctr_host->normals_consumed : 0;

@@ -65,6 +65,7 @@ struct TileConst {
   const float* gtv;
   const int* dom;
   const unsigned* cbits;   // candidate bits of the view
+  const double* raw;       // cached raw L1 error of the view (RAW path)
   const double* thr;
   double lo, x_m, t1, t2, t3;
   long long p0;            // pixel index of (x0 + lane, y0 - HL): ext row ey is p0 + ey * W
@@ -75,21 +76,34 @@ struct TileConst {
 };
 
 // one image row of the tile (lane = x)
+// RAW: the minmax pass cached the fp64 raw L1 error per pixel (8 B instead
+// of re-reading 24 B of image + gt and redoing the arithmetic)
+template <bool RAW>
 struct RowIn {
   float a[3], g[3];
   int d;      // dominant id if it is a split candidate (tile rows), else -1
   bool inb;
 };
+template <>
+struct RowIn<true> {
+  double raw;
+  int d;
+  bool inb;
+};
 
-template <int HL>
-__device__ __forceinline__ void load_row(RowIn& r, const TileConst& T, int ey, int lane) {
+template <int HL, bool RAW>
+__device__ __forceinline__ void load_row(RowIn<RAW>& r, const TileConst& T, int ey, int lane) {
   r.inb = ey >= T.ey_lo && ey < T.ey_hi && T.col_in;
   const long long p = T.p0 + (long long)ey * T.W;
   const bool tile_row = ey >= HL && ey < HL + kTileH;
+  if constexpr (RAW) {
+    r.raw = r.inb ? __ldg(T.raw + p) : 0.0;
+  } else {
 #pragma unroll
-  for (int c = 0; c < 3; ++c) {
-    r.a[c] = r.inb ? __ldg(T.img + 3 * p + c) : 0.0f;
-    r.g[c] = r.inb ? __ldg(T.gtv + 3 * p + c) : 0.0f;
+    for (int c = 0; c < 3; ++c) {
+      r.a[c] = r.inb ? __ldg(T.img + 3 * p + c) : 0.0f;
+      r.g[c] = r.inb ? __ldg(T.gtv + 3 * p + c) : 0.0f;
+    }
   }
   // candidate bit (written by the minmax pass) instead of a dependent cls[D] load
   const bool need = r.inb && tile_row;
@@ -106,24 +120,37 @@ __device__ __forceinline__ double raw_l1_f(const float* a, const float* g) {
   return dadd(dadd(a0, a1), a2);
 }
 
+template <bool RAW>
 __device__ __forceinline__ bool metric_at(const TileConst& T, int x, int y) {
   const long long p = (long long)y * T.W + x;
-  float a[3], g[3];
+  if constexpr (RAW) {
+    return dsub(__ldg(T.raw + p), T.lo) >= T.x_m;
+  } else {
+    float a[3], g[3];
 #pragma unroll
-  for (int c = 0; c < 3; ++c) {
-    a[c] = __ldg(T.img + 3 * p + c);
-    g[c] = __ldg(T.gtv + 3 * p + c);
+    for (int c = 0; c < 3; ++c) {
+      a[c] = __ldg(T.img + 3 * p + c);
+      g[c] = __ldg(T.gtv + 3 * p + c);
+    }
+    return dsub(raw_l1_f(a, g), T.lo) >= T.x_m;
   }
-  return dsub(raw_l1_f(a, g), T.lo) >= T.x_m;
 }
 
 
 // one ext row: metric mask, then (once its erosion window is complete) the
 // runs of tile row ey - SPAN and their unions with the row above.
 // Returns true when the tile has too many runs for the warp path.
-template <int R>
-__device__ __forceinline__ bool scan_row(const float* a, const float* g, const bool inb, const int c_now, const int ey,
-                                         ScanState& st, WarpSmem& S, const TileConst& T, const int lane) {
+template <bool RAW>
+__device__ __forceinline__ double row_raw(const RowIn<RAW>& r) {
+  if constexpr (RAW) return r.raw;
+  else return raw_l1_f(r.a, r.g);
+}
+
+template <int R, bool RAW>
+__device__ __forceinline__ bool scan_row(const RowIn<RAW>& row, const int ey, ScanState& st, WarpSmem& S,
+                                         const TileConst& T, const int lane) {
+  const bool inb = row.inb;
+  const int c_now = row.d;
   constexpr int HL = R > 1 ? R / 2 : 0;
   constexpr int HH = R > 1 ? R - R / 2 - 1 : 0;
   constexpr int SPAN = HL + HH;
@@ -131,7 +158,7 @@ __device__ __forceinline__ bool scan_row(const float* a, const float* g, const b
   bool m = false;
   int band_now = 0;
   if (inb) {
-    const double xr = dsub(raw_l1_f(a, g), T.lo);
+    const double xr = dsub(row_raw<RAW>(row), T.lo);
     m = xr >= T.x_m;
     if (T.L <= 4) {
       band_now = (xr >= T.t1) + (xr >= T.t2) + (xr >= T.t3);
@@ -219,7 +246,7 @@ __device__ __forceinline__ bool scan_row(const float* a, const float* g, const b
   return overflow;
 }
 
-template <int R>
+template <int R, bool RAW>
 __device__ __forceinline__ void tile_warp_body(const TileParams& P, WarpSmem& S, const long long tile,
                                                const int lane) {
   constexpr int HL = R > 1 ? R / 2 : 0;
@@ -243,6 +270,7 @@ __device__ __forceinline__ void tile_warp_body(const TileParams& P, WarpSmem& S,
   T.gtv = P.gt + (long long)v * hw * 3;
   T.dom = P.dom + (long long)v * hw;
   T.cbits = P.cand_bits + (long long)v * ((hw + 31) / 32);
+  T.raw = RAW ? P.raw + (long long)v * hw : nullptr;
   T.L = P.L;
   T.lo = P.lo[v];
   T.thr = P.thr + (long long)v * P.L;
@@ -260,8 +288,8 @@ __device__ __forceinline__ void tile_warp_body(const TileParams& P, WarpSmem& S,
       const int ey = lane + 32 * k;
       const int y = y0 - HL + ey;
       const bool row_ok = ey < NR && y >= 0 && y < H;
-      const bool ml = HL > 0 && row_ok && x0 - 1 >= 0 && metric_at(T, x0 - 1, y);
-      const bool mr = HH > 0 && row_ok && x0 + kTileW < W && metric_at(T, x0 + kTileW, y);
+      const bool ml = HL > 0 && row_ok && x0 - 1 >= 0 && metric_at<RAW>(T, x0 - 1, y);
+      const bool mr = HH > 0 && row_ok && x0 + kTileW < W && metric_at<RAW>(T, x0 + kTileW, y);
       T.hl_mask |= (unsigned long long)__ballot_sync(FULL, ml) << (32 * k);
       T.hr_mask |= (unsigned long long)__ballot_sync(FULL, mr) << (32 * k);
     }
@@ -279,17 +307,17 @@ __device__ __forceinline__ void tile_warp_body(const TileParams& P, WarpSmem& S,
   bool overflow = false;
   {
     // rows are loaded one ahead into two alternating register buffers
-    RowIn A, B;
-    load_row<HL>(A, T, 0, lane);
+    RowIn<RAW> A, B;
+    load_row<HL, RAW>(A, T, 0, lane);
     for (int ey = 0; ey < NR; ey += 2) {
-      if (ey + 1 < NR) load_row<HL>(B, T, ey + 1, lane);
-      if (scan_row<R>(A.a, A.g, A.inb, A.d, ey, st, S, T, lane)) {
+      if (ey + 1 < NR) load_row<HL, RAW>(B, T, ey + 1, lane);
+      if (scan_row<R, RAW>(A, ey, st, S, T, lane)) {
         overflow = true;
         break;
       }
       if (ey + 1 < NR) {
-        if (ey + 2 < NR) load_row<HL>(A, T, ey + 2, lane);
-        if (scan_row<R>(B.a, B.g, B.inb, B.d, ey + 1, st, S, T, lane)) {
+        if (ey + 2 < NR) load_row<HL, RAW>(A, T, ey + 2, lane);
+        if (scan_row<R, RAW>(B, ey + 1, st, S, T, lane)) {
           overflow = true;
           break;
         }
@@ -407,30 +435,36 @@ __device__ __forceinline__ void tile_warp_body(const TileParams& P, WarpSmem& S,
   border[2 * kTileW + kTileH + lane] = b_right >= 0 ? S.u.post.aux[S.uf[b_right]] : -1;
 }
 
-template <int R>
+template <int R, bool RAW>
 __global__ void __launch_bounds__(kWarpsPerBlock * 32, ADPS_TW_MINBLOCKS) tile_warp_kernel(TileParams P, long long n_tiles) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   WarpSmem& S = reinterpret_cast<WarpSmem*>(smem_raw)[wid];
   const long long tile = (long long)blockIdx.x * kWarpsPerBlock + wid;
   if (tile >= n_tiles) return;   // warp-uniform
-  tile_warp_body<R>(P, S, tile, lane);
+  tile_warp_body<R, RAW>(P, S, tile, lane);
 }
 
-template <int R>
+template <int R, bool RAW>
 static cudaError_t launch_r(const TileParams& P, long long n_tiles, cudaStream_t s) {
   const size_t smem = tile_warp_smem_bytes();
-  cudaError_t e = cudaFuncSetAttribute(tile_warp_kernel<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaError_t e = cudaFuncSetAttribute(tile_warp_kernel<R, RAW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   const long long blocks = (n_tiles + kWarpsPerBlock - 1) / kWarpsPerBlock;
-  tile_warp_kernel<R><<<(unsigned)blocks, kWarpsPerBlock * 32, smem, s>>>(P, n_tiles);
+  tile_warp_kernel<R, RAW><<<(unsigned)blocks, kWarpsPerBlock * 32, smem, s>>>(P, n_tiles);
   return cudaGetLastError();
 }
 
 cudaError_t launch_tile_warp(const TileParams& P, long long n_tiles, cudaStream_t s) {
-  if (P.r_erode <= 1) return launch_r<1>(P, n_tiles, s);
-  if (P.r_erode == 2) return launch_r<2>(P, n_tiles, s);
-  if (P.r_erode == 3) return launch_r<3>(P, n_tiles, s);
+  if (P.raw) {
+    if (P.r_erode <= 1) return launch_r<1, true>(P, n_tiles, s);
+    if (P.r_erode == 2) return launch_r<2, true>(P, n_tiles, s);
+    if (P.r_erode == 3) return launch_r<3, true>(P, n_tiles, s);
+  } else {
+    if (P.r_erode <= 1) return launch_r<1, false>(P, n_tiles, s);
+    if (P.r_erode == 2) return launch_r<2, false>(P, n_tiles, s);
+    if (P.r_erode == 3) return launch_r<3, false>(P, n_tiles, s);
+  }
   return cudaErrorInvalidValue;
 }
 

@@ -199,6 +199,10 @@ class Plan:
         """0: warp-per-tile CCL (+ block CCL for deferred tiles), 1: block CCL only."""
         _abi.check(self.lib.adps_set_param(self._h, _abi.PARAM_TILE_PATH, int(path)))
 
+    def set_raw_cache(self, on: bool):
+        """Minmax pass caches the fp64 raw L1 error for the warp CCL (default on)."""
+        _abi.check(self.lib.adps_set_param(self._h, _abi.PARAM_RAW_CACHE, int(bool(on))))
+
     def get_param(self, key: int) -> int:
         v = C.c_int64()
         _abi.check(self.lib.adps_get_param(self._h, int(key), C.byref(v)))

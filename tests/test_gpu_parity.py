@@ -119,8 +119,9 @@ def _injected_partition(op, plan, e, dom, n_gauss, l_bands, m_min, cands, tau=0.
                gamma_c=0.15, tau_g=2e-4, tau_s=0.01, eta=1.6, eps=1e-9)
     dev = "cuda"
     got_by_path = []
-    for path in (1, 0):
+    for path, raw in ((1, 1), (0, 0), (0, 1)):   # block CCL; warp CCL recomputing / caching raw error
         plan.set_tile_path(path)
+        plan.set_raw_cache(raw)
         try:
             plan.phase1(PA.to_tensors(g), 1.0, torch.as_tensor(ga, device=dev),
                         torch.ones(n_gauss, dtype=torch.float64, device=dev), cfg, cam.row()[None],
@@ -128,11 +129,13 @@ def _injected_partition(op, plan, e, dom, n_gauss, l_bands, m_min, cands, tau=0.
                         torch.as_tensor(dom[None].astype(np.int32), device=dev))
         finally:
             plan.set_tile_path(0)
+            plan.set_raw_cache(1)
         got_by_path.append(PA.gpu_regions(plan))
         if path == 0 and deferred is not None:
             assert (plan.deferred_tiles() > 0) == deferred, plan.deferred_tiles()
     np.testing.assert_array_equal(got_by_path[1], got_by_path[0], err_msg="warp CCL != block CCL")
-    got = got_by_path[1]
+    np.testing.assert_array_equal(got_by_path[2], got_by_path[0], err_msg="cached-raw warp CCL != block CCL")
+    got = got_by_path[2]
     maps = O.compute_maps(rendered.astype(np.float64), gt.astype(np.float64), cfg)
     is_c = np.zeros(n_gauss, bool)
     is_c[cands] = True
@@ -448,13 +451,15 @@ def test_determinism_at_scale(op, cfg_name):
     img, dom = plan.render(g, cams)
     cfg = AdpSplitConfig(v_views=len(cams), n_max=wl.n_max)
     digests = []
-    for path in (0, 0, 1):      # the last run takes the block CCL for every tile: same bits
+    for path, raw in ((0, 1), (0, 1), (1, 1), (0, 0)):   # block CCL / recomputed raw error: same bits
         plan.set_tile_path(path)
+        plan.set_raw_cache(raw)
         res = op.densify_step(g, ini.extent, cams, gt_img, torch.as_tensor(ga, device="cuda"),
                               torch.as_tensor(den, device="cuda"), cfg, np.random.default_rng(0),
                               renders=(img, dom), plan=plan, view_ids=list(range(len(cams))))
         digests.append((res.counts, _step_digest(op, plan, res)))
     plan.set_tile_path(0)
+    plan.set_raw_cache(1)
     for counts, dg in digests[1:]:
         assert counts == digests[0][0]
         for k in dg:
