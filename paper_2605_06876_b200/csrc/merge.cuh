@@ -68,6 +68,8 @@ struct MergeArgs {
   unsigned long long* mkey_sorted;
   int* mval_sorted;                        // Morton order: [lp_off[l], +P_l) -> proposal q
   TileBox* boxes;                          // [cap / 64 + n_split]
+  double* gsoa;                            // [13][soa_cap] gate operands in Morton order
+  long long soa_cap;
   int4* tile_pairs;                        // surviving (l, bi, bj) tile pairs
   long long tile_pairs_cap;
   float* children;                         // [cap,14]

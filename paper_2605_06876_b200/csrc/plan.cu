@@ -90,7 +90,7 @@ struct adps_plan {
   Buf small_list, pstart, n_groups, work_cnt, work_off, props_s, pcand, gkey, gval, gkey_sorted, gval_sorted,
       grp_first, ext_key, ext_val, ext_key_sorted, ext_val_sorted, cand_key, cand_val, cand_key_sorted,
       cand_val_sorted, scan3_val, scan3_flag, scan3_ticket, large_of, lp_cnt, lp_off, tile_cnt, tile_off, mkey,
-      mval, mkey_sorted, mval_sorted, boxes, tile_pairs;
+      mval, mkey_sorted, mval_sorted, boxes, tile_pairs, gsoa;
   Buf scan_val, scan_flag, scan_ticket, scan2_val, scan2_flag, scan2_ticket, cub_tmp;
   Buf ctr;
   Counters* ctr_host = nullptr;
@@ -232,7 +232,7 @@ extern "C" adps_status adps_plan_destroy(adps_plan* P) {
                  &P->ext_key, &P->ext_val, &P->ext_key_sorted, &P->ext_val_sorted, &P->cand_key, &P->cand_val,
                  &P->cand_key_sorted, &P->cand_val_sorted, &P->scan3_val, &P->scan3_flag, &P->scan3_ticket,
                  &P->large_of, &P->lp_cnt, &P->lp_off, &P->tile_cnt, &P->tile_off, &P->mkey, &P->mval,
-                 &P->mkey_sorted, &P->mval_sorted, &P->boxes, &P->tile_pairs, &P->deferred, &P->cand_bits, &P->rawc,
+                 &P->mkey_sorted, &P->mval_sorted, &P->boxes, &P->tile_pairs, &P->gsoa, &P->deferred, &P->cand_bits, &P->rawc,
                  &P->nrm_val, &P->nrm_len, &P->nrm_acc, &P->nrm_reach, &P->nrm_rmax, &P->nrm_walked,
                  &P->nrm_idx, &P->nrm_tmp};
   for (Buf* b : bufs)
@@ -753,6 +753,7 @@ extern "C" adps_status adps_step_phase1_end(adps_plan* P, void* stream_v, adps_c
   CK(ensure(P->mkey_sorted, 8 * rc));
   CK(ensure(P->mval_sorted, 4 * rc));
   CK(ensure(P->boxes, sizeof(TileBox) * (rc / 64 + sc + 1)));
+  CK(ensure(P->gsoa, 8ll * 13 * rc));
   {
     // surviving tile pairs: worst case every pair of (rc/64 + n_split) tiles; capped at
     // 2^24 entries (overflow falls back to inline filtering inside pair_tiles_kernel)
@@ -841,6 +842,8 @@ extern "C" adps_status adps_step_phase1_end(adps_plan* P, void* stream_v, adps_c
   ma.mkey_sorted = P->mkey_sorted.as<unsigned long long>();
   ma.mval_sorted = P->mval_sorted.as<int>();
   ma.boxes = P->boxes.as<TileBox>();
+  ma.gsoa = P->gsoa.as<double>();
+  ma.soa_cap = rc;
   ma.tile_pairs = P->tile_pairs.as<int4>();
   ma.tile_pairs_cap = (long long)(P->tile_pairs.bytes / sizeof(int4));
   ma.ctr = ctr;
