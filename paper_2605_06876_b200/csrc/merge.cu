@@ -108,7 +108,7 @@ __global__ void case_kernel(MergeArgs a) {
         const unsigned long long l = atomicAdd(&a.ctr->n_large, 1ull);
         a.large_list[l] = (int)k;
         a.large_of[k] = (int)l;
-        const long long T = (P + 63) / 64;
+        const long long T = (P + kMT - 1) / kMT;
         a.work_cnt[l] = (unsigned long long)(T * (T + 1) / 2);
         a.lp_cnt[l] = (unsigned long long)P;
         a.tile_cnt[l] = (unsigned long long)T;
@@ -245,7 +245,7 @@ __device__ __forceinline__ long long find_owner(const unsigned long long* off, l
   return lo;
 }
 
-// one warp per 64-proposal tile of a large parent (Morton order)
+// one warp per kMT-proposal tile of a large parent (Morton order)
 __global__ void box_kernel(MergeArgs a) {
   const int lane = threadIdx.x & 31;
   const long long warps = (long long)gridDim.x * (blockDim.x >> 5);
@@ -255,8 +255,8 @@ __global__ void box_kernel(MergeArgs a) {
        t += warps) {
     const long long l = find_owner(a.tile_off, n_large, (unsigned long long)t);
     const long long tl = t - (long long)a.tile_off[l];
-    const long long b = (long long)a.lp_off[l] + tl * 64;
-    const long long e = min(b + 64, (long long)(a.lp_off[l] + a.lp_cnt[l]));
+    const long long b = (long long)a.lp_off[l] + tl * kMT;
+    const long long e = min(b + kMT, (long long)(a.lp_off[l] + a.lp_cnt[l]));
     double s[3] = {0, 0, 0}, inv_s = 1e300, lo[3] = {1e300, 1e300, 1e300}, hi[3] = {-1e300, -1e300, -1e300};
     for (long long m = b + lane; m < e; m += 32) {
       const Proposal& M = a.props_s[a.mval_sorted[m]];
@@ -318,7 +318,7 @@ __device__ __forceinline__ bool boxes_may_merge(const TileBox& A, const TileBox&
 __device__ __forceinline__ void decode_tile_pair(const MergeArgs& a, long long n_large, unsigned long long w,
                                                  long long& l, long long& bi, long long& bj) {
   l = find_owner(a.work_off, n_large, w);
-  const long long T = ((long long)a.lp_cnt[l] + 63) / 64;
+  const long long T = ((long long)a.lp_cnt[l] + kMT - 1) / kMT;
   const long long q = (long long)(w - a.work_off[l]);
   bi = (long long)floor(((2.0 * T + 1.0) - sqrt((2.0 * T + 1.0) * (2.0 * T + 1.0) - 8.0 * q)) / 2.0);
   if (bi < 0) bi = 0;
@@ -348,7 +348,7 @@ __global__ void tile_pair_filter_kernel(MergeArgs a) {
 // of arrays (written by box_kernel): contiguous 64-proposal tiles load
 // coalesced, 13 doubles per proposal instead of a gathered 152-byte record.
 
-__device__ __forceinline__ bool gate_soa(const double* A, const double (*Bs)[64], int j, double gd, double gc) {
+__device__ __forceinline__ bool gate_soa(const double* A, const double (*Bs)[kMT], int j, double gd, double gc) {
   const double dc = fmax(fmax(fabs(A[kG_rgb + 0] - Bs[kG_rgb + 0][j]), fabs(A[kG_rgb + 1] - Bs[kG_rgb + 1][j])),
                          fabs(A[kG_rgb + 2] - Bs[kG_rgb + 2][j]));
   if (!(dc <= gc)) return false;
@@ -364,11 +364,11 @@ __device__ __forceinline__ bool gate_soa(const double* A, const double (*Bs)[64]
   return d <= gd;
 }
 
-// one block per surviving 64x64 tile pair of a large parent's gate matrix (or,
+// one block per surviving kMT x kMT tile pair of a large parent's gate matrix (or,
 // if the survivor list overflowed, every tile pair with the box test inline)
 __global__ void __launch_bounds__(256) pair_tiles_kernel(MergeArgs a) {
-  __shared__ double si[kG_fields][64], sj[kG_fields][64];
-  __shared__ int qi[64], qj[64];
+  __shared__ double si[kG_fields][kMT], sj[kG_fields][kMT];
+  __shared__ int qi[kMT], qj[kMT];
   const bool overflow = (a.ctr->overflow & 4u) != 0;
   const long long n_large = (long long)a.ctr->n_large;
   const unsigned long long W = overflow ? (n_large > 0 ? a.work_off[n_large] : 0) : a.ctr->n_tile_pairs;
@@ -386,23 +386,23 @@ __global__ void __launch_bounds__(256) pair_tiles_kernel(MergeArgs a) {
     }
     const long long P = (long long)a.lp_cnt[l];
     const long long base = (long long)a.lp_off[l];
-    const int i0 = (int)(bi * 64), j0 = (int)(bj * 64);
-    const int ni = (int)min(64ll, P - i0), nj = (int)min(64ll, P - j0);
-    for (int t = threadIdx.x; t < 2 * kG_fields * 64; t += blockDim.x) {
-      const int half = t / (kG_fields * 64), r = t % (kG_fields * 64);
-      const int f = r >> 6, loc = r & 63;
+    const int i0 = (int)(bi * kMT), j0 = (int)(bj * kMT);
+    const int ni = (int)min((long long)kMT, P - i0), nj = (int)min((long long)kMT, P - j0);
+    for (int t = threadIdx.x; t < 2 * kG_fields * kMT; t += blockDim.x) {
+      const int half = t / (kG_fields * kMT), r = t % (kG_fields * kMT);
+      const int f = r / kMT, loc = r % kMT;
       if (loc < (half ? nj : ni)) {
         const double x = a.gsoa[(long long)f * a.soa_cap + base + (half ? j0 : i0) + loc];
         (half ? sj : si)[f][loc] = x;
       }
     }
-    for (int t = threadIdx.x; t < 128; t += blockDim.x) {
-      const int loc = t & 63;
-      if (loc < (t < 64 ? ni : nj)) (t < 64 ? qi : qj)[loc] = a.mval_sorted[base + (t < 64 ? i0 : j0) + loc];
+    for (int t = threadIdx.x; t < 2 * kMT; t += blockDim.x) {
+      const int loc = t % kMT;
+      if (loc < (t < kMT ? ni : nj)) (t < kMT ? qi : qj)[loc] = a.mval_sorted[base + (t < kMT ? i0 : j0) + loc];
     }
     __syncthreads();
-    for (int t = threadIdx.x; t < 64 * 64; t += blockDim.x) {
-      const int ii = t >> 6, jj = t & 63;
+    for (int t = threadIdx.x; t < kMT * kMT; t += blockDim.x) {
+      const int ii = t / kMT, jj = t % kMT;
       // unordered pairs: within a diagonal tile take ii < jj once
       if (ii < ni && jj < nj && (bi != bj || ii < jj)) {
         double A[kG_fields];

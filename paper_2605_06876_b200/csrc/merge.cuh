@@ -5,6 +5,12 @@
 
 namespace adps {
 
+#ifndef ADPS_MERGE_TILE
+#define ADPS_MERGE_TILE 32
+#endif
+// proposals per Morton tile of a large parent's gate matrix (exact pruning unit)
+constexpr int kMT = ADPS_MERGE_TILE;
+
 // Cross-view merge + cap over all split candidates at once
 // (ref/cross_view_merge.py:33-116, ref/adc.py:184-227).
 //

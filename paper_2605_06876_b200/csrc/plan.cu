@@ -752,12 +752,12 @@ extern "C" adps_status adps_step_phase1_end(adps_plan* P, void* stream_v, adps_c
   CK(ensure(P->mval, 4 * rc));
   CK(ensure(P->mkey_sorted, 8 * rc));
   CK(ensure(P->mval_sorted, 4 * rc));
-  CK(ensure(P->boxes, sizeof(TileBox) * (rc / 64 + sc + 1)));
+  CK(ensure(P->boxes, sizeof(TileBox) * (rc / kMT + sc + 1)));
   CK(ensure(P->gsoa, 8ll * 13 * rc));
   {
-    // surviving tile pairs: worst case every pair of (rc/64 + n_split) tiles; capped at
+    // surviving tile pairs: worst case every pair of (rc/kMT + n_split) tiles; capped at
     // 2^24 entries (overflow falls back to inline filtering inside pair_tiles_kernel)
-    const long long t = rc / 64 + sc + 1;
+    const long long t = rc / kMT + sc + 1;
     long long want = t * (t + 1) / 2;
     if (want > (1ll << 24)) want = 1ll << 24;
     CK(ensure(P->tile_pairs, sizeof(int4) * want));
