@@ -205,6 +205,33 @@ ADPS_API adps_status adps_set_timing(adps_plan* plan, int32_t enabled);
 ADPS_API adps_status adps_get_timing(adps_plan* plan, double* ms, int32_t max_entries, int32_t* n_entries,
                             const char** names);
 
+/* ---- multi-GPU sharding (one plan per rank) ----
+ * Phase A is view-sharded: rank r passes its local views (every world-th
+ * sampled view starting at r) to adps_step_phase1_begin after
+ * adps_set_view_sharding(plan, r, world, V), so region records carry global
+ * view positions.  Between the calls the host reduces the ever-dominant flags
+ * (ADPS_BUF_DOM_FLAG, uint8 [n], MAX) over ranks and calls
+ * adps_step_phase1_refresh for the global fallback count; then
+ * adps_step_phase1_local builds this rank's region records and proposals
+ * (ADPS_BUF_REGIONS / _PROPOSALS / _VALID), the host all-gathers them and
+ * hands the concatenation back with adps_step_phase1_import, and
+ * adps_step_phase1_merge finishes phase 1 exactly as adps_step_phase1_end
+ * would have on one GPU (records are ordered by their sort key, so the
+ * concatenation order does not matter).  adps_step_phase1_end ==
+ * adps_step_phase1_local + adps_step_phase1_merge. */
+#define ADPS_BUF_DOM_FLAG 1
+#define ADPS_BUF_REGIONS 2
+#define ADPS_BUF_PROPOSALS 3
+#define ADPS_BUF_VALID 4
+ADPS_API adps_status adps_set_view_sharding(adps_plan* plan, int32_t view_offset, int32_t view_stride,
+                                            int32_t n_views_global);
+ADPS_API adps_status adps_get_buffer(adps_plan* plan, int32_t which, void** ptr, int64_t* count, int64_t* elem_bytes);
+ADPS_API adps_status adps_step_phase1_refresh(adps_plan* plan, void* stream, adps_counts* counts);
+ADPS_API adps_status adps_step_phase1_local(adps_plan* plan, void* stream, int64_t* n_regions);
+ADPS_API adps_status adps_step_phase1_import(adps_plan* plan, void* stream, const adps_region_record* regions,
+                                             const void* proposals, const uint8_t* valid, int64_t n);
+ADPS_API adps_status adps_step_phase1_merge(adps_plan* plan, void* stream, adps_counts* counts);
+
 /* Tuning knobs (diagnostic/testing).  ADPS_PARAM_LARGE_THRESHOLD: parents
  * with more proposals than this use the grid-wide pair-tile merge path
  * (default 32; 0 routes every split parent through it).

@@ -18,6 +18,7 @@ ADPS_CUDA_ERROR, ADPS_OOM, ADPS_BAD_STATE = 4, 5, 6
 CASE_SPLIT, CASE_FALLBACK, CASE_RESET = 0, 1, 2
 PARAM_LARGE_THRESHOLD, PARAM_TILE_PATH, PARAM_DEFERRED_TILES = 1, 2, 3
 PARAM_NORMALS_CONSUMED, PARAM_NORMALS_STATUS, PARAM_RAW_CACHE = 4, 5, 6
+BUF_DOM_FLAG, BUF_REGIONS, BUF_PROPOSALS, BUF_VALID = 1, 2, 3, 4
 
 vp = C.c_void_p
 
@@ -60,6 +61,8 @@ EXPORTS = (
     "adps_step_phase1", "adps_step_phase1_begin", "adps_step_phase1_end", "adps_step_phase2", "adps_get_report", "adps_get_regions",
     "adps_set_debug_records", "adps_set_debug_maps", "adps_set_timing", "adps_get_timing",
     "adps_accumulate_stats", "adps_get_launch_count", "adps_set_param", "adps_get_param", "adps_normals_pcg64",
+    "adps_set_view_sharding", "adps_get_buffer", "adps_step_phase1_refresh", "adps_step_phase1_local",
+    "adps_step_phase1_import", "adps_step_phase1_merge",
 )
 
 _lib = None
@@ -96,6 +99,12 @@ def load(path: str = LIB_PATH):
     lib.adps_get_launch_count.argtypes = [vp, C.POINTER(C.c_int64), C.POINTER(C.c_int64)]
     lib.adps_set_param.argtypes = [vp, C.c_int32, C.c_int64]
     lib.adps_get_param.argtypes = [vp, C.c_int32, C.POINTER(C.c_int64)]
+    lib.adps_set_view_sharding.argtypes = [vp, C.c_int32, C.c_int32, C.c_int32]
+    lib.adps_get_buffer.argtypes = [vp, C.c_int32, C.POINTER(vp), C.POINTER(C.c_int64), C.POINTER(C.c_int64)]
+    lib.adps_step_phase1_refresh.argtypes = [vp, vp, C.POINTER(Counts)]
+    lib.adps_step_phase1_local.argtypes = [vp, vp, C.POINTER(C.c_int64)]
+    lib.adps_step_phase1_import.argtypes = [vp, vp, vp, vp, vp, C.c_int64]
+    lib.adps_step_phase1_merge.argtypes = [vp, vp, C.POINTER(Counts)]
     lib.adps_normals_pcg64.argtypes = [vp, vp, C.POINTER(C.c_uint64), C.POINTER(C.c_uint64), C.c_int64, vp,
                                        C.c_int32, C.POINTER(C.c_int64), C.POINTER(C.c_int32)]
     for name in EXPORTS:

@@ -415,7 +415,7 @@ __device__ void tile_block(const TileParams& P, TileSmem& S, const int tile) {
       unsigned long long gid = S.base_part + s;
       if ((long long)gid < P.partial_cap) {
         PartialRec& R = P.partials[gid];
-        R.view_pos = P.view_offset + v;
+        R.view_pos = P.view_offset + v * P.view_stride;
         R.cand = S.d[p];
         R.band = S.band[p];
         R.minpix = minpix;
@@ -430,7 +430,7 @@ __device__ void tile_block(const TileParams& P, TileSmem& S, const int tile) {
       unsigned long long rid = S.base_reg + s;
       if ((long long)rid < P.region_cap) {
         RegionRec& R = P.regions[rid];
-        R.view_pos = P.view_offset + v;
+        R.view_pos = P.view_offset + v * P.view_stride;
         R.cand = S.d[p];
         R.band = S.band[p];
         R.minpix = minpix;
@@ -564,6 +564,12 @@ cudaError_t launch_minmax(const AttributionArgs& a, const int* split_list, Count
   return cudaGetLastError();
 }
 
+cudaError_t launch_fallback_count(const int* split_list, const unsigned char* dom_flag, Counters* ctr, int sm_count,
+                                  cudaStream_t s) {
+  fallback_count_kernel<<<sm_count * 2, 256, 0, s>>>(split_list, dom_flag, ctr);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_attribution(const AttributionArgs& a, cudaStream_t s, MarkFn mark, void* ctx) {
   TileParams P;
   P.image = a.image;
@@ -574,6 +580,7 @@ cudaError_t launch_attribution(const AttributionArgs& a, cudaStream_t s, MarkFn 
   P.tiles_x = (a.W + kTileW - 1) / kTileW;
   P.tiles_y = (a.H + kTileH - 1) / kTileH;
   P.view_offset = a.view_offset;
+  P.view_stride = a.view_stride;
   P.lo = a.lo;
   P.thr = a.thr;
   P.L = a.L;

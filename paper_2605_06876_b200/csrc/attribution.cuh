@@ -10,7 +10,7 @@ struct TileParams {
   const int* dom;
   int H, W;
   int tiles_x, tiles_y;
-  int view_offset;
+  int view_offset, view_stride;     // global view position = view_offset + v * view_stride
   const double* lo;
   const double* thr;
   int L, r_erode, m_min;
@@ -47,7 +47,7 @@ struct AttributionArgs {
   const float* image;
   const float* gt;
   const int* dom;
-  int V, H, W, view_offset;
+  int V, H, W, view_offset, view_stride;
   int L, r_erode, m_min;
   double tau;
   const unsigned char* cls;
@@ -83,6 +83,9 @@ size_t tile_smem_bytes();
 // minmax + ever-dominant flags + thresholds + fallback count (phase-1 begin)
 cudaError_t launch_minmax(const AttributionArgs& a, const int* split_list, Counters* ctr, int sm_count,
                           cudaStream_t s);
+// fallback count alone (after the dom_flag buffer was reduced across ranks)
+cudaError_t launch_fallback_count(const int* split_list, const unsigned char* dom_flag, Counters* ctr, int sm_count,
+                                  cudaStream_t s);
 // Called after each group of launches: name, stream, number of kernels launched.
 typedef void (*MarkFn)(void* ctx, const char* name, cudaStream_t s, int kernels);
 cudaError_t launch_attribution(const AttributionArgs& a, cudaStream_t s, MarkFn mark, void* ctx);

@@ -122,6 +122,11 @@ struct adps_plan {
   long long launches = 0;
   long long lib_calls = 0;
   int large_threshold = 32;
+  // view sharding: this plan's local view v is global view position view_offset + v * view_stride
+  // of v_global_cfg sampled views (0 = the local views are all of them)
+  int view_offset = 0, view_stride = 1, v_global_cfg = 0, v_glob = 0;
+  long long n_regions_cur = 0;   // region records the merge half consumes
+  bool have_local = false;
   int tile_path = 0;   // 0 warp CCL + deferred block CCL, 1 block CCL only
   int raw_cache = ADPS_RAW_CACHE_DEFAULT;   // minmax pass caches the raw L1 error for the warp CCL
   bool use_raw = false;                     // decided per phase 1
@@ -408,7 +413,8 @@ static AttributionArgs attr_args(adps_plan* P, int V, int H, int W, const adps_c
   a.V = V;
   a.H = H;
   a.W = W;
-  a.view_offset = 0;
+  a.view_offset = P->view_offset;
+  a.view_stride = P->view_stride;
   a.L = cfg->l_bands;
   a.r_erode = cfg->r_erode;
   a.m_min = cfg->m_min;
@@ -491,6 +497,12 @@ extern "C" adps_status adps_step_phase1_begin(adps_plan* P, void* stream_v, cons
     if (cv.w != W || cv.h != H) return fail(ADPS_INVALID_ARG, "all sampled views must share H x W");
   }
   if (W <= 0 || H <= 0) return fail(ADPS_INVALID_ARG, "empty image");
+  P->v_glob = P->v_global_cfg > 0 ? P->v_global_cfg : V;
+  if (P->view_offset + (long long)(V - 1) * P->view_stride >= P->v_glob)
+    return fail(ADPS_INVALID_ARG, "local views exceed the global view count of the sharding");
+  P->v_glob = P->v_global_cfg > 0 ? P->v_global_cfg : V;
+  if (P->view_offset + (long long)(V - 1) * P->view_stride >= P->v_glob)
+    return fail(ADPS_INVALID_ARG, "local views exceed the global view count of the sharding");
   const long long hw = (long long)H * W;
   const long long total_px = hw * V;
   const int tiles_x = (W + kTileW - 1) / kTileW, tiles_y = (H + kTileH - 1) / kTileH;
@@ -598,16 +610,12 @@ extern "C" adps_status adps_step_phase1_begin(adps_plan* P, void* stream_v, cons
   return ADPS_OK;
 }
 
-extern "C" adps_status adps_step_phase1_end(adps_plan* P, void* stream_v, adps_counts* counts) {
-  if (!P || !counts) return fail(ADPS_INVALID_ARG, "NULL argument");
-  if (!P->have_begin) return fail(ADPS_BAD_STATE, "phase1_end without phase1_begin");
-  P->have_begin = false;
+// attribution + region statistics + child init over this plan's (local) views
+static adps_status phase1_local(adps_plan* P, cudaStream_t s, long long* n_regions_out) {
   CK(cudaSetDevice(P->device));
-  cudaStream_t s = (cudaStream_t)stream_v;
   adps_status st = ADPS_OK;
   const adps_gaussians* g = &P->cx.g;
   const long long n = P->cx.n;
-  const double extent = P->cx.extent;
   const adps_config* cfg = &P->cx.cfg;
   const int V = P->cx.V, H = P->cx.H, W = P->cx.W;
   const float* image = P->cx.image;
@@ -618,13 +626,9 @@ extern "C" adps_status adps_step_phase1_end(adps_plan* P, void* stream_v, adps_c
   const int tiles_x = (W + kTileW - 1) / kTileW, tiles_y = (H + kTileH - 1) / kTileH;
   const long long n_tiles = (long long)tiles_x * tiles_y * V;
   const int N = (int)n;
-  const long long nn = n > 0 ? n : 1;
   const long long region_bound = total_px / (cfg->m_min > 1 ? cfg->m_min : 1) + 1;
   const long long partial_bound = n_tiles * (2 * kTileW + 2 * kTileH) + 1;
   Counters* ctr = P->ctr.as<Counters>();
-  ScanState sst, sst2;
-  st = scan_state(P, P->scan_val, P->scan_flag, P->scan_ticket, nn, &sst);
-  if (st != ADPS_OK) return st;
 
   // ---- maps + partition + moments (ref/adc.py:168-176)
   for (int attempt = 0;; ++attempt) {
@@ -649,7 +653,6 @@ extern "C" adps_status adps_step_phase1_end(adps_plan* P, void* stream_v, adps_c
   }
   const long long n_regions = (long long)P->ctr_host->n_regions;
   const long long n_split = (long long)P->ctr_host->n_split;
-  const long long n_clone = (long long)P->ctr_host->n_clone;
   mark(P, "host_sync", s, 0);
 
   // ---- region stats + child init (ref/adc.py:172-176, 190-196)
@@ -668,7 +671,7 @@ extern "C" adps_status adps_step_phase1_end(adps_plan* P, void* stream_v, adps_c
     CK(ensure(P->dbg_stats, sizeof(double) * 10 * rc));
     CK(ensure(P->dbg_child, sizeof(double) * 16 * rc));
   }
-  const int bits_v = ceil_log2((unsigned long long)V);
+  const int bits_v = ceil_log2((unsigned long long)P->v_glob);
   const int bits_b = ceil_log2((unsigned long long)cfg->l_bands);
   const int bits_p = ceil_log2((unsigned long long)hw);
   const int bits_c = ceil_log2((unsigned long long)(n_split > 0 ? n_split : 1));
@@ -683,6 +686,8 @@ extern "C" adps_status adps_step_phase1_end(adps_plan* P, void* stream_v, adps_c
   ca.gt = gt;
   ca.H = H;
   ca.W = W;
+  ca.view_offset = P->view_offset;
+  ca.view_stride = P->view_stride;
   ca.eps = cfg->eps;
   ca.cand_rank = P->cand_rank.as<int>();
   ca.bits_v = bits_v;
@@ -699,7 +704,37 @@ extern "C" adps_status adps_step_phase1_end(adps_plan* P, void* stream_v, adps_c
   ca.grid = (unsigned)(cgrid < 1 ? 1 : (cgrid > 65535 ? 65535 : cgrid));
   if (n_regions > 0) CK(launch_child_init(ca, s));
   mark(P, "child_init", s, n_regions > 0 ? 1 : 0);
+  P->n_regions_cur = n_regions;
+  *n_regions_out = n_regions;
+  return ADPS_OK;
+}
 
+// sort + ranges + merge + cap + case + offsets over the plan's region records
+// (local ones, or the gathered records of all ranks after adps_step_phase1_import)
+static adps_status phase1_merge(adps_plan* P, cudaStream_t s, adps_counts* counts) {
+  CK(cudaSetDevice(P->device));
+  adps_status st = ADPS_OK;
+  const adps_gaussians* g = &P->cx.g;
+  const long long n = P->cx.n;
+  const double extent = P->cx.extent;
+  const adps_config* cfg = &P->cx.cfg;
+  const int V = P->v_glob, H = P->cx.H, W = P->cx.W;
+  const long long hw = (long long)H * W;
+  const long long nn = n > 0 ? n : 1;
+  Counters* ctr = P->ctr.as<Counters>();
+  ScanState sst, sst2;
+  st = scan_state(P, P->scan_val, P->scan_flag, P->scan_ticket, nn, &sst);
+  if (st != ADPS_OK) return st;
+  const long long n_regions = P->n_regions_cur;
+  const long long n_split = (long long)P->ctr_host->n_split;
+  const long long n_clone = (long long)P->ctr_host->n_clone;
+  const long long rc = n_regions > 0 ? n_regions : 1;
+  const int bits_v = ceil_log2((unsigned long long)V);
+  const int bits_b = ceil_log2((unsigned long long)cfg->l_bands);
+  const int bits_p = ceil_log2((unsigned long long)hw);
+  const int bits_c = ceil_log2((unsigned long long)(n_split > 0 ? n_split : 1));
+  const int total_bits = bits_c + bits_v + bits_b + bits_p;
+  if (total_bits > 64) return fail(ADPS_INVALID_ARG, "region sort key needs %d bits (> 64)", total_bits);
   // ---- order (candidate, view, band, first pixel)  (ref/adc.py:190-195)
   if (n_regions > 0) {
     size_t tb = 0;
@@ -924,6 +959,77 @@ extern "C" adps_status adps_step_phase1_end(adps_plan* P, void* stream_v, adps_c
   return ADPS_OK;
 }
 
+extern "C" adps_status adps_step_phase1_end(adps_plan* P, void* stream_v, adps_counts* counts) {
+  if (!P || !counts) return fail(ADPS_INVALID_ARG, "NULL argument");
+  if (!P->have_begin) return fail(ADPS_BAD_STATE, "phase1_end without phase1_begin");
+  P->have_begin = false;
+  cudaStream_t s = (cudaStream_t)stream_v;
+  long long nr = 0;
+  adps_status st = phase1_local(P, s, &nr);
+  if (st != ADPS_OK) return st;
+  return phase1_merge(P, s, counts);
+}
+
+extern "C" adps_status adps_step_phase1_local(adps_plan* P, void* stream_v, int64_t* n_regions) {
+  if (!P || !n_regions) return fail(ADPS_INVALID_ARG, "NULL argument");
+  if (!P->have_begin) return fail(ADPS_BAD_STATE, "phase1_local without phase1_begin");
+  P->have_begin = false;
+  long long nr = 0;
+  adps_status st = phase1_local(P, (cudaStream_t)stream_v, &nr);
+  if (st != ADPS_OK) return st;
+  *n_regions = nr;
+  P->have_local = true;
+  return ADPS_OK;
+}
+
+extern "C" adps_status adps_step_phase1_import(adps_plan* P, void* stream_v, const adps_region_record* regions,
+                                               const void* proposals, const uint8_t* valid, int64_t n) {
+  if (!P) return fail(ADPS_INVALID_ARG, "plan is NULL");
+  if (!P->have_local) return fail(ADPS_BAD_STATE, "phase1_import without phase1_local");
+  if (n < 0 || (n > 0 && (!regions || !proposals || !valid))) return fail(ADPS_INVALID_ARG, "bad records");
+  CK(cudaSetDevice(P->device));
+  cudaStream_t s = (cudaStream_t)stream_v;
+  const long long rc = n > 0 ? n : 1;
+  if (P->region_cap < rc) {
+    P->region_cap = rc;
+    CK(ensure(P->regions, sizeof(RegionRec) * rc));
+  }
+  CK(ensure(P->props, sizeof(Proposal) * rc));
+  CK(ensure(P->valid, rc));
+  CK(ensure(P->keys, 8 * rc));
+  CK(ensure(P->vals, 4 * rc));
+  CK(ensure(P->keys_sorted, 8 * rc));
+  CK(ensure(P->vals_sorted, 4 * rc));
+  CK(ensure(P->idx, 4 * rc));
+  CK(ensure(P->uf, 4 * rc));
+  CK(ensure(P->groups, sizeof(GroupRec) * rc));
+  CK(ensure(P->children, sizeof(float) * 14 * rc));
+  if (n > 0) {
+    CK(cudaMemcpyAsync(P->regions.p, regions, sizeof(RegionRec) * n, cudaMemcpyDeviceToDevice, s));
+    CK(cudaMemcpyAsync(P->props.p, proposals, sizeof(Proposal) * n, cudaMemcpyDeviceToDevice, s));
+    CK(cudaMemcpyAsync(P->valid.p, valid, n, cudaMemcpyDeviceToDevice, s));
+    const adps_config* cfg = &P->cx.cfg;
+    const long long hw = (long long)P->cx.H * P->cx.W;
+    CK(launch_region_keys(P->regions.as<RegionRec>(), n, P->cand_rank.as<int>(),
+                          ceil_log2((unsigned long long)P->v_glob), ceil_log2((unsigned long long)cfg->l_bands),
+                          ceil_log2((unsigned long long)hw), P->keys.as<unsigned long long>(), P->vals.as<int>(), s));
+    P->launches += 1;
+  }
+  Counters* ctr = P->ctr.as<Counters>();
+  const unsigned long long nu = (unsigned long long)n;
+  CK(cudaMemcpyAsync(&ctr->n_regions, &nu, sizeof(nu), cudaMemcpyHostToDevice, s));
+  CK(cudaStreamSynchronize(s));
+  P->n_regions_cur = n;
+  return ADPS_OK;
+}
+
+extern "C" adps_status adps_step_phase1_merge(adps_plan* P, void* stream_v, adps_counts* counts) {
+  if (!P || !counts) return fail(ADPS_INVALID_ARG, "NULL argument");
+  if (!P->have_local) return fail(ADPS_BAD_STATE, "phase1_merge without phase1_local");
+  P->have_local = false;
+  return phase1_merge(P, (cudaStream_t)stream_v, counts);
+}
+
 extern "C" adps_status adps_step_phase2(adps_plan* P, void* stream_v, const adps_gaussians* g,
                                         const double* fallback_normals, adps_gaussians_out* out,
                                         int64_t* index_map) {
@@ -1031,6 +1137,59 @@ extern "C" adps_status adps_get_timing(adps_plan* P, double* ms, int32_t max_ent
     ++n;
   }
   *n_entries = n;
+  return ADPS_OK;
+}
+
+extern "C" adps_status adps_set_view_sharding(adps_plan* P, int32_t view_offset, int32_t view_stride,
+                                              int32_t n_views_global) {
+  if (!P) return fail(ADPS_INVALID_ARG, "plan is NULL");
+  if (view_offset < 0 || view_stride < 1 || n_views_global < 0) return fail(ADPS_INVALID_ARG, "bad view sharding");
+  P->view_offset = view_offset;
+  P->view_stride = view_stride;
+  P->v_global_cfg = n_views_global;
+  return ADPS_OK;
+}
+
+extern "C" adps_status adps_get_buffer(adps_plan* P, int32_t which, void** ptr, int64_t* count, int64_t* elem_bytes) {
+  if (!P || !ptr || !count || !elem_bytes) return fail(ADPS_INVALID_ARG, "NULL argument");
+  switch (which) {
+    case ADPS_BUF_DOM_FLAG:
+      *ptr = P->dom_flag.p;
+      *count = P->cx.n;
+      *elem_bytes = 1;
+      return ADPS_OK;
+    case ADPS_BUF_REGIONS:
+      *ptr = P->regions.p;
+      *count = P->n_regions_cur;
+      *elem_bytes = sizeof(RegionRec);
+      return ADPS_OK;
+    case ADPS_BUF_PROPOSALS:
+      *ptr = P->props.p;
+      *count = P->n_regions_cur;
+      *elem_bytes = sizeof(Proposal);
+      return ADPS_OK;
+    case ADPS_BUF_VALID:
+      *ptr = P->valid.p;
+      *count = P->n_regions_cur;
+      *elem_bytes = 1;
+      return ADPS_OK;
+    default:
+      return fail(ADPS_INVALID_ARG, "unknown buffer %d", which);
+  }
+}
+
+extern "C" adps_status adps_step_phase1_refresh(adps_plan* P, void* stream_v, adps_counts* counts) {
+  if (!P || !counts) return fail(ADPS_INVALID_ARG, "NULL argument");
+  if (!P->have_begin) return fail(ADPS_BAD_STATE, "phase1_refresh without phase1_begin");
+  CK(cudaSetDevice(P->device));
+  cudaStream_t s = (cudaStream_t)stream_v;
+  Counters* ctr = P->ctr.as<Counters>();
+  CK(cudaMemsetAsync(&ctr->n_fallback_pre, 0, sizeof(unsigned long long), s));
+  CK(launch_fallback_count(P->split_list.as<int>(), P->dom_flag.as<unsigned char>(), ctr, P->sm_count, s));
+  P->launches += 1;
+  CK(cudaMemcpyAsync(P->ctr_host, ctr, sizeof(Counters), cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  counts->n_fallback = (long long)P->ctr_host->n_fallback_pre;
   return ADPS_OK;
 }
 

@@ -94,11 +94,12 @@ __global__ void child_init_kernel(ChildArgs a) {
     int ix = (int)rint(cx), iy = (int)rint(cy);   // round-half-even
     ix = ix < 0 ? 0 : (ix > a.W - 1 ? a.W - 1 : ix);
     iy = iy < 0 ? 0 : (iy > a.H - 1 ? a.H - 1 : iy);
-    const float* gp = a.gt + (((long long)R.view_pos * a.H + iy) * a.W + ix) * 3;
+    const int lv = (R.view_pos - a.view_offset) / a.view_stride;   // local view of this region
+    const float* gp = a.gt + (((long long)lv * a.H + iy) * a.W + ix) * 3;
     const double rgb[3] = {(double)gp[0], (double)gp[1], (double)gp[2]};
 
     // ---- init_child (ref/child_init.py:110-140)
-    const CamD cam = load_cam(a.cams + 18ll * R.view_pos);
+    const CamD cam = load_cam(a.cams + 18ll * lv);
     const int gi = R.cand;
     const double dcam[3] = {(cx - cam.px) / cam.fx, (cy - cam.py) / cam.fy, 1.0};
     double dw[3];
@@ -195,6 +196,26 @@ __global__ void child_init_kernel(ChildArgs a) {
       c[12] = s1; c[13] = s2; c[14] = s2; c[15] = ok ? 1.0 : 0.0;
     }
   }
+}
+
+__global__ void region_keys_kernel(const RegionRec* __restrict__ regions, long long n, const int* __restrict__ cand_rank,
+                                   int bits_v, int bits_b, int bits_p, unsigned long long* __restrict__ keys,
+                                   int* __restrict__ vals) {
+  for (long long rid = (long long)blockIdx.x * blockDim.x + threadIdx.x; rid < n; rid += (long long)gridDim.x * blockDim.x) {
+    const RegionRec& R = regions[rid];
+    const unsigned long long rank = (unsigned long long)cand_rank[R.cand];
+    keys[rid] = (((rank << bits_v | (unsigned long long)R.view_pos) << bits_b | (unsigned long long)R.band) << bits_p) |
+                (unsigned long long)R.minpix;
+    vals[rid] = (int)rid;
+  }
+}
+
+cudaError_t launch_region_keys(const RegionRec* regions, long long n, const int* cand_rank, int bits_v, int bits_b,
+                               int bits_p, unsigned long long* keys, int* vals, cudaStream_t s) {
+  long long b = (n + 255) / 256;
+  region_keys_kernel<<<(unsigned)(b < 1 ? 1 : (b > 65535 ? 65535 : b)), 256, 0, s>>>(regions, n, cand_rank, bits_v,
+                                                                                     bits_b, bits_p, keys, vals);
+  return cudaGetLastError();
 }
 
 cudaError_t launch_child_init(const ChildArgs& a, cudaStream_t s) {

@@ -36,9 +36,10 @@ struct ChildArgs {
   const unsigned long long* n_regions;
   long long region_cap;
   GaussiansIn g;
-  const double* cams;        // [V,18] device
-  const float* gt;           // [V,H,W,3]
+  const double* cams;        // [V,18] device (local views)
+  const float* gt;           // [V,H,W,3] (local views)
   int H, W;
+  int view_offset, view_stride;   // region view_pos (global) -> local view (view_pos - offset) / stride
   double eps;
   const int* cand_rank;
   int bits_v, bits_b, bits_p;
@@ -52,6 +53,9 @@ struct ChildArgs {
   unsigned grid;
 };
 cudaError_t launch_child_init(const ChildArgs& a, cudaStream_t s);
+// sort keys (candidate rank, view, band, first pixel) of imported region records
+cudaError_t launch_region_keys(const RegionRec* regions, long long n, const int* cand_rank, int bits_v, int bits_b,
+                               int bits_p, unsigned long long* keys, int* vals, cudaStream_t s);
 
 // ---- per-candidate ranges after the sort ----
 struct RangeArgs {

@@ -399,7 +399,7 @@ __device__ __forceinline__ void tile_warp_body(const TileParams& P, WarpSmem& S,
         const unsigned long long gid = pbase + __popc(pm & ((1u << lane) - 1u));
         if ((long long)gid < P.partial_cap) {
           PartialRec& Rr = P.partials[gid];
-          Rr.view_pos = P.view_offset + v;
+          Rr.view_pos = P.view_offset + v * P.view_stride;
           Rr.cand = cand;
           Rr.band = bnd;
           Rr.minpix = minpix;
@@ -414,7 +414,7 @@ __device__ __forceinline__ void tile_warp_body(const TileParams& P, WarpSmem& S,
         const unsigned long long rid2 = rbase + __popc(rm & ((1u << lane) - 1u));
         if ((long long)rid2 < P.region_cap) {
           RegionRec& Rr = P.regions[rid2];
-          Rr.view_pos = P.view_offset + v;
+          Rr.view_pos = P.view_offset + v * P.view_stride;
           Rr.cand = cand;
           Rr.band = bnd;
           Rr.minpix = minpix;

@@ -290,6 +290,72 @@ class Plan:
         _abi.check(self.lib.adps_step_phase1_end(self._h, self._stream(), C.byref(counts)))
         return counts.as_dict()
 
+    # -- view-sharded phase 1 (multi-GPU; see sharded.py and include/adps.h)
+    def set_view_sharding(self, offset: int, stride: int, n_views_global: int):
+        _abi.check(self.lib.adps_set_view_sharding(self._h, int(offset), int(stride), int(n_views_global)))
+
+    def buffer(self, which: int):
+        """(device pointer, count, element bytes) of a plan-owned buffer."""
+        ptr, cnt, eb = C.c_void_p(), C.c_int64(), C.c_int64()
+        _abi.check(self.lib.adps_get_buffer(self._h, int(which), C.byref(ptr), C.byref(cnt), C.byref(eb)))
+        return ptr.value, int(cnt.value), int(eb.value)
+
+    def _buffer_copy(self, which: int) -> torch.Tensor:
+        ptr, cnt, eb = self.buffer(which)
+        out = torch.empty(cnt * eb, dtype=torch.uint8, device=self.device)
+        if cnt:
+            _copy_device(out, ptr, cnt * eb, self.device)
+        return out
+
+    def dom_flags(self) -> torch.Tensor:
+        """Copy of the ever-dominant flags of the last phase1_begin (uint8 [n])."""
+        return self._buffer_copy(_abi.BUF_DOM_FLAG)
+
+    def set_dom_flags(self, flags: torch.Tensor):
+        ptr, cnt, eb = self.buffer(_abi.BUF_DOM_FLAG)
+        if flags.numel() != cnt * eb or flags.dtype != torch.uint8:
+            raise ValueError("dom flags must be uint8 [n]")
+        if cnt:
+            global _cudart
+            if _cudart is None:
+                from cuda.bindings import runtime as _rt
+                _cudart = _rt
+            stream = torch.cuda.current_stream(self.device).cuda_stream
+            err, = _cudart.cudaMemcpyAsync(ptr, flags.contiguous().data_ptr(), cnt,
+                                           _cudart.cudaMemcpyKind.cudaMemcpyDeviceToDevice, stream)
+            if int(err) != 0:
+                raise RuntimeError(f"cudaMemcpyAsync failed: {err}")
+
+    def phase1_refresh(self) -> dict:
+        """Fallback count from the (externally reduced) ever-dominant flags."""
+        counts = _abi.Counts()
+        _abi.check(self.lib.adps_step_phase1_refresh(self._h, self._stream(), C.byref(counts)))
+        return counts.as_dict()
+
+    def phase1_local(self) -> int:
+        n = C.c_int64()
+        _abi.check(self.lib.adps_step_phase1_local(self._h, self._stream(), C.byref(n)))
+        return int(n.value)
+
+    def export_records(self) -> dict:
+        """This rank's region records, proposals and valid flags as uint8 tensors."""
+        return {"regions": self._buffer_copy(_abi.BUF_REGIONS), "proposals": self._buffer_copy(_abi.BUF_PROPOSALS),
+                "valid": self._buffer_copy(_abi.BUF_VALID)}
+
+    def record_sizes(self):
+        return self.buffer(_abi.BUF_REGIONS)[2], self.buffer(_abi.BUF_PROPOSALS)[2]
+
+    def phase1_import(self, regions: torch.Tensor, proposals: torch.Tensor, valid: torch.Tensor):
+        n = valid.numel()
+        self._import_keep = (regions, proposals, valid)
+        _abi.check(self.lib.adps_step_phase1_import(self._h, self._stream(), _ptr(regions) if n else None,
+                                                    _ptr(proposals) if n else None, _ptr(valid) if n else None, n))
+
+    def phase1_merge(self) -> dict:
+        counts = _abi.Counts()
+        _abi.check(self.lib.adps_step_phase1_merge(self._h, self._stream(), C.byref(counts)))
+        return counts.as_dict()
+
     def phase2(self, g, normals, out: GaussianTensors, index_map: torch.Tensor):
         ga = g.abi()
         oa = _abi.GaussiansOut(out.mu.data_ptr(), out.scale.data_ptr(), out.rot.data_ptr(),
@@ -426,6 +492,52 @@ class StepResult:
         return rep
 
 
+class FallbackNormals:
+    """The 6F normals of the fallback children (ref/adc.py:97).
+
+    The caller's Generator draws 3 normals per fallback child in ascending
+    parent order; the stream is chunk-invariant, so the 6F values are one
+    slice of rng.standard_normal.  A PCG64 Generator's slice is produced on
+    the device, bit-identical (adps_normals_pcg64), and the host Generator is
+    advanced past it once phase 1 has synchronised; any other bit generator is
+    drawn on a host thread while the GPU finishes phase 1 (the C calls
+    release the GIL).  Start it after phase1_begin, call join() after the
+    phase-1 end, then result().
+    """
+
+    def __init__(self, plan: Plan, rng, nf: int):
+        self.plan, self.rng, self.nf = plan, rng, int(nf)
+        self.gpu = self.nf > 0 and isinstance(rng.bit_generator, np.random.PCG64)
+        self.normals, self._drawn, self._th = None, {}, None
+        if self.gpu:
+            self.normals, _, _ = plan.normals_pcg64(rng.bit_generator.state, 6 * self.nf, sync=False)
+        elif self.nf > 0:
+            def _draw():
+                self._drawn["z"] = rng.standard_normal(6 * self.nf)
+
+            self._th = threading.Thread(target=_draw)
+            self._th.start()
+
+    def join(self):
+        if self._th is not None:
+            self._th.join()
+            self._th = None
+
+    def result(self):
+        """Device tensor of the normals (None when there are no fallbacks)."""
+        self.join()
+        if self.gpu:
+            consumed, status = self.plan.normals_result()
+            if status == 0:
+                self.rng.bit_generator.advance(consumed)
+            else:   # a wedge test too close to call against the host libm: draw on the host
+                self.normals = torch.from_numpy(self.rng.standard_normal(6 * self.nf)).to(self.plan.device)
+            self.gpu = False
+        elif self.nf > 0 and self.normals is None:
+            self.normals = torch.from_numpy(self._drawn["z"]).to(self.plan.device)
+        return self.normals
+
+
 def densify_step(g: GaussianTensors, extent: float, cameras, gt, grad_accum: torch.Tensor,
                  denom: torch.Tensor, cfg, rng, *, renders=None, plan: Plan = None,
                  view_ids=None, want_report: bool = True, out: GaussianTensors = None) -> StepResult:
@@ -452,39 +564,14 @@ def densify_step(g: GaussianTensors, extent: float, cameras, gt, grad_accum: tor
     counts = plan.phase1_begin(g, extent, grad_accum.to(dev, F64).contiguous(), denom.to(dev, F64).contiguous(),
                                cfg, cams_v, image, gt_v, dom)
     nf = counts["n_fallback"]
-    # the caller's Generator draws 3 normals per fallback child in ascending
-    # parent order (ref/adc.py:97); the stream is chunk-invariant, so the 6F
-    # values are one slice of rng.standard_normal.  A PCG64 Generator's slice
-    # is produced on the device, bit-identical, and the host Generator is
-    # advanced past it; any other bit generator is drawn on a host thread
-    # while the GPU finishes phase 1 (the C call releases the GIL).
-    normals = None
-    gpu_rng = nf > 0 and isinstance(rng.bit_generator, np.random.PCG64)
-    drawn = {}
-    th = None
-    if gpu_rng:
-        normals, _, _ = plan.normals_pcg64(rng.bit_generator.state, 6 * nf, sync=False)
-    elif nf > 0:
-        def _draw():
-            drawn["z"] = rng.standard_normal(6 * nf)
-
-        th = threading.Thread(target=_draw)
-        th.start()
+    draw = FallbackNormals(plan, rng, nf)
     try:
         counts = plan.phase1_end()
     finally:
-        if th is not None:
-            th.join()
+        draw.join()
     if counts["n_fallback"] != nf:
         raise RuntimeError("fallback count changed between phase-1 halves")
-    if gpu_rng:
-        consumed, status = plan.normals_result()
-        if status == 0:
-            rng.bit_generator.advance(consumed)
-        else:   # a wedge test too close to call against the host libm: draw on the host
-            normals = torch.from_numpy(rng.standard_normal(6 * nf)).to(dev)
-    elif nf > 0:
-        normals = torch.from_numpy(drawn["z"]).to(dev)
+    normals = draw.result()
     n_out = counts["n_out"]
     if out is None:
         out = GaussianTensors.empty(n_out, g.sh_k, dev)

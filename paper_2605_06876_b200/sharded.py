@@ -1,0 +1,212 @@
+"""Multi-GPU AdpSplit densify step: one process per GPU over torch.distributed.
+
+SURVEY.md 8(e), following the path's own data dependencies:
+
+  Phase A (view-sharded).  Rank r owns the sampled-view positions r, r+g,
+  r+2g, ... (g = world size).  It runs select, the per-view error maps,
+  partition, region statistics and child initialisation for its views only
+  (ref/adc.py:165-196) -- every per-view stage is independent across views.
+  The ever-dominant flags (ref/adc.py:177-180, an OR over all sampled views)
+  are combined with ONE all_reduce(MAX) of an N-byte vector, after which the
+  global fallback count is known and the fallback normals can be drawn.
+
+  Exchange.  Region records (64 B, global view positions) and their proposals
+  (152 B) are all-gathered; each rank hands the concatenation to its plan.
+  Records are merged in their (candidate, view, band, first pixel) key order,
+  which is the reference's order (ref/adc.py:190-195), so the concatenation
+  order is irrelevant and every rank sees identical inputs.
+
+  Phase B (replicated).  Merge, cap, per-candidate case, offsets and the
+  compaction run on every rank over identical inputs, so every rank ends with
+  the identical grown arrays (what the next data-parallel training step
+  needs) without a further collective.
+
+The orchestration is written against a small executor interface so that the
+same code drives the CUDA plan (GpuExecutor) and, in the CPU tests, a
+stand-in executor built on the oracle (tests/test_sharded.py, gloo, world 2).
+"""
+
+from __future__ import annotations
+
+import torch
+import torch.distributed as dist
+
+from . import operator as op
+
+
+def shard_views(n_views: int, world: int, rank: int) -> list:
+    """Positions (into the sorted sampled view ids) owned by `rank`: r, r+g, ..."""
+    if world < 1 or not 0 <= rank < world:
+        raise ValueError("bad world/rank")
+    return list(range(rank, n_views, world))
+
+
+def all_gather_bytes(t: torch.Tensor, group=None) -> list:
+    """all_gather of 1-D uint8 tensors of different lengths (padded to the max)."""
+    world = dist.get_world_size(group)
+    n = torch.tensor([t.numel()], dtype=torch.int64, device=t.device)
+    sizes = [torch.zeros_like(n) for _ in range(world)]
+    dist.all_gather(sizes, n, group=group)
+    sizes = [int(x.item()) for x in sizes]
+    m = max(sizes) if sizes else 0
+    if m == 0:
+        return [t.new_empty(0) for _ in range(world)]
+    pad = torch.zeros(m, dtype=torch.uint8, device=t.device)
+    pad[:t.numel()] = t
+    outs = [torch.empty(m, dtype=torch.uint8, device=t.device) for _ in range(world)]
+    dist.all_gather(outs, pad, group=group)
+    return [o[:k] for o, k in zip(outs, sizes)]
+
+
+def run_sharded(ex, n_views: int, group=None):
+    """The sharded step over an executor; returns the executor's emit() result.
+
+    Executor interface (all tensors on the collective backend's device):
+      begin(positions) -> counts       select + ever-dominant flags of the local views
+      dom_flags() / set_dom_flags(t)   uint8 [N]
+      refresh() -> n_fallback          fallback count from the reduced flags
+      start_normals(n_fallback)        start drawing the 6F fallback normals
+      local() -> {name: uint8 tensor}  local region records / proposals / valid flags
+      import_(dict of per-rank lists)  the gathered records
+      merge() -> counts                merge, cap, case, offsets over all records
+      emit() -> result                 the grown Gaussians (identical on every rank)
+    """
+    world = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    if world > n_views:
+        raise ValueError(f"{world} ranks but only {n_views} sampled views to shard")
+    ex.begin(shard_views(n_views, world, rank))
+    flags = ex.dom_flags()
+    dist.all_reduce(flags, op=dist.ReduceOp.MAX, group=group)
+    ex.set_dom_flags(flags)
+    ex.start_normals(ex.refresh())
+    recs = ex.local()
+    ex.import_({k: all_gather_bytes(v, group) for k, v in recs.items()})
+    ex.merge()
+    return ex.emit()
+
+
+def run_lockstep(executors: list, n_views: int):
+    """run_sharded for a list of executors (rank = list position) in ONE process,
+    with the two collectives done in place (OR of the flags, concatenation of
+    the records).  Same stage sequence as run_sharded; used to check the
+    sharded C-ABI flow on a single GPU."""
+    world = len(executors)
+    if world > n_views:
+        raise ValueError(f"{world} ranks but only {n_views} sampled views to shard")
+    for r, ex in enumerate(executors):
+        ex.begin(shard_views(n_views, world, r))
+    flags = [ex.dom_flags() for ex in executors]
+    red = flags[0].clone()
+    for f in flags[1:]:
+        red = torch.maximum(red, f.to(red.device))
+    for ex in executors:
+        ex.set_dom_flags(red.to(flags[0].device))
+        ex.start_normals(ex.refresh())
+    recs = [ex.local() for ex in executors]
+    gathered = {k: [r[k] for r in recs] for k in recs[0]}
+    for ex in executors:
+        ex.import_(gathered)
+    for ex in executors:
+        ex.merge()
+    return [ex.emit() for ex in executors]
+
+
+class GpuExecutor:
+    """The executor interface over one rank's CUDA plan."""
+
+    def __init__(self, g: op.GaussianTensors, extent: float, cameras, gt, grad_accum, denom, cfg, rng, *,
+                 renders=None, plan: op.Plan = None, view_ids=None, want_report: bool = True,
+                 world: int = 1, rank: int = 0):
+        self.plan = plan or op.default_plan(g.device)
+        self.g, self.extent, self.cfg, self.rng = g, extent, cfg, rng
+        self.cams = op.camera_rows(cameras)
+        v_views = int(cfg["v_views"] if isinstance(cfg, dict) else cfg.v_views)
+        self.view_ids = list(view_ids) if view_ids is not None else op.sample_views(len(self.cams), v_views, rng)
+        self.gt, self.renders = gt, renders
+        self.ga = grad_accum.to(self.plan.device, op.F64).contiguous()
+        self.den = denom.to(self.plan.device, op.F64).contiguous()
+        self.want_report, self.world, self.rank = want_report, world, rank
+        self.counts = None
+        self.normals = None
+
+    def begin(self, positions):
+        P, dev = self.plan, self.plan.device
+        self.positions = list(positions)
+        vids = [self.view_ids[p] for p in self.positions]
+        cams_v = self.cams[vids]
+        if self.renders is None:
+            image, dom = P.render(self.g, cams_v)
+        else:
+            idx = torch.as_tensor(self.positions, device=dev)
+            image = self.renders[0].to(dev, op.F32).index_select(0, idx).contiguous()
+            dom = self.renders[1].to(dev, torch.int32).index_select(0, idx).contiguous()
+        gt_v = op._gather_views(self.gt, vids, dev)
+        self._keep = (image, dom, gt_v)
+        P.set_view_sharding(self.rank, self.world, len(self.view_ids))
+        self.counts = P.phase1_begin(self.g, self.extent, self.ga, self.den, self.cfg, cams_v, image, gt_v, dom)
+        return self.counts
+
+    def dom_flags(self):
+        return self.plan.dom_flags()
+
+    def set_dom_flags(self, t):
+        self.plan.set_dom_flags(t)
+
+    def refresh(self):
+        self.counts["n_fallback"] = self.plan.phase1_refresh()["n_fallback"]
+        return self.counts["n_fallback"]
+
+    def start_normals(self, nf):
+        self._draw = op.FallbackNormals(self.plan, self.rng, nf)
+
+    def local(self):
+        self.plan.phase1_local()
+        return self.plan.export_records()
+
+    def import_(self, gathered):
+        cat = {k: torch.cat(v) if v else torch.empty(0, dtype=torch.uint8, device=self.plan.device)
+               for k, v in gathered.items()}
+        self.plan.phase1_import(cat["regions"], cat["proposals"], cat["valid"])
+
+    def merge(self):
+        try:
+            self.counts = self.plan.phase1_merge()
+        finally:
+            self._draw.join()
+            self.plan.set_view_sharding(0, 1, 0)
+        return self.counts
+
+    def emit(self):
+        normals = self._draw.result()
+        counts, dev = self.counts, self.plan.device
+        out = op.GaussianTensors.empty(counts["n_out"], self.g.sh_k, dev)
+        index_map = torch.empty(counts["n_out"], dtype=torch.int64, device=dev)
+        self.plan.phase2(self.g, normals, out, index_map)
+        res = op.StepResult(gaussians=out, index_map=index_map, counts=counts, view_ids=list(self.view_ids),
+                            normals=normals)
+        if self.want_report:
+            res.report_arrays = self.plan.report_arrays(counts["n_split"], counts["n_clone"])
+        return res
+
+
+def densify_step_sharded(g: op.GaussianTensors, extent: float, cameras, gt, grad_accum, denom, cfg, rng, *,
+                         renders=None, plan: op.Plan = None, view_ids=None, want_report: bool = True,
+                         group=None) -> op.StepResult:
+    """op.densify_step over all ranks of `group` (one GPU each); identical result on every rank.
+
+    Every rank passes the same arguments (same Generator state, same sampled
+    views; `renders`, if given, are the attribution of ALL sampled views, of
+    which each rank reads only its own).  With world size 1 this is
+    op.densify_step.
+    """
+    if not dist.is_initialized() or dist.get_world_size(group) == 1:
+        return op.densify_step(g, extent, cameras, gt, grad_accum, denom, cfg, rng, renders=renders, plan=plan,
+                               view_ids=view_ids, want_report=want_report)
+    ex = GpuExecutor(g, extent, cameras, gt, grad_accum, denom, cfg, rng, renders=renders, plan=plan,
+                     view_ids=view_ids, want_report=want_report, world=dist.get_world_size(group),
+                     rank=dist.get_rank(group))
+    return run_sharded(ex, len(ex.view_ids), group)
+
+
+__all__ = ["shard_views", "all_gather_bytes", "run_sharded", "run_lockstep", "GpuExecutor", "densify_step_sharded"]

@@ -471,3 +471,41 @@ def test_determinism_at_scale(op, cfg_name):
     kept = rep.index_map[rep.index_map >= 0]
     assert (np.diff(kept) > 0).all() and len(kept) == c["n_keep"]
     assert all(r.children_inserted <= wl.n_max for r in rep.candidates)
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_sharded_lockstep_matches_single_gpu(op, world):
+    """The view-sharded C-ABI flow (phase1_begin on each rank's views, flag
+    reduction, refresh, local records, import of the concatenation, merge)
+    gives the single-plan result bit for bit -- all ranks run in one process
+    (sharded.run_lockstep) since the test box has one GPU."""
+    import torch
+    from paper_2605_06876_b200 import sharded as SH
+    from paper_2605_06876_b200 import synth as S
+    from paper_2605_06876_b200.types import AdpSplitConfig
+    wl = S.CONFIGS["config2"]
+    ini, cams, (ga, den), gt = wl.build()
+    base = op.Plan("cuda:0")
+    g = op.GaussianTensors.from_numpy(*ini.arrays(), device="cuda")
+    gt_img, _ = base.render(op.GaussianTensors.from_numpy(*gt.arrays(), device="cuda"), cams)
+    img, dom = base.render(g, cams)
+    cfg = AdpSplitConfig(v_views=len(cams), n_max=wl.n_max)
+    vids = list(range(len(cams)))
+    ga_t, den_t = torch.as_tensor(ga, device="cuda"), torch.as_tensor(den, device="cuda")
+    rng1 = np.random.default_rng(5)
+    single = op.densify_step(g, ini.extent, cams, gt_img, ga_t, den_t, cfg, rng1, renders=(img, dom), plan=base,
+                             view_ids=vids)
+    want = _step_digest(op, base, single)
+    exs = [SH.GpuExecutor(g, ini.extent, cams, gt_img, ga_t, den_t, cfg, np.random.default_rng(5),
+                          renders=(img, dom), plan=op.Plan("cuda:0"), view_ids=vids, world=world, rank=r)
+           for r in range(world)]
+    results = SH.run_lockstep(exs, len(vids))
+    assert single.counts["n_fallback"] > 0
+    for r, (ex, res) in enumerate(zip(exs, results)):
+        drop = ("n_partials",)   # tile-border fragments: a per-rank diagnostic
+        assert {k: v for k, v in res.counts.items() if k not in drop} == \
+            {k: v for k, v in single.counts.items() if k not in drop}, r
+        got = _step_digest(op, ex.plan, res)
+        for k in want:
+            np.testing.assert_array_equal(got[k], want[k], err_msg=f"rank {r}: {k}")
+        assert ex.rng.bit_generator.state == rng1.bit_generator.state

@@ -1,0 +1,167 @@
+"""Sharded densify step (paper_2605_06876_b200/sharded.py) on CPU: gloo, world size 2 and 3.
+
+The orchestration -- view sharding, the all_reduce(MAX) of the ever-dominant
+flags, the variable-length all_gather of the region records -- runs for real
+over gloo with a stand-in executor built on the oracle's phases
+(O.view_regions / O.ever_dominant / O.step_finish), and every rank's result
+must equal the single-process oracle step bit for bit.  The CUDA executor
+drives the same run_sharded over the plan's C ABI (tests/test_gpu_parity.py
+checks that flow on one GPU with run_lockstep).
+"""
+import os
+import pickle
+import socket
+import sys
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+import golden_io  # noqa: E402
+import parity as PA  # noqa: E402
+from oracle import adpsplit_oracle as O  # noqa: E402
+from paper_2605_06876_b200 import sharded as SH  # noqa: E402
+
+TAGS = ["blobs", "desk0", "desk3", "paper1"]
+
+
+def _inputs(tag):
+    data, meta = golden_io.load()
+    g, extent = golden_io.scene(data, f"step__{tag}__in")
+    g = PA.oracle_gaussians_f32(g)
+    cams = golden_io.cams(data, f"step__{tag}__cams")
+    gts = PA.f32(data[f"step__{tag}__gt"])
+    m = meta["step"][tag]
+    return (g, extent, cams, gts, data[f"step__{tag}__grad_accum"], data[f"step__{tag}__denom"],
+            golden_io.Cfg(m["cfg"]), m["seed"])
+
+
+class OracleExecutor:
+    """run_sharded's executor interface over the oracle's per-phase functions."""
+
+    def __init__(self, g, extent, cams, gts, ga, den, cfg, rng, renders):
+        self.g, self.extent, self.cams, self.gts, self.cfg, self.rng = g, extent, cams, gts, cfg, rng
+        self.ga, self.den, self.renders = ga, den, renders
+        self.view_ids = O.sample_views(len(cams), int(O.cfg_get(cfg, "v_views")), rng)
+
+    def begin(self, positions):
+        n = len(self.g)
+        self.split, self.clone = O.select(self.ga, self.den, self.g.scale, O.cfg_get(self.cfg, "tau_g"),
+                                          O.cfg_get(self.cfg, "tau_s") * self.extent)
+        is_cand = np.zeros(n, dtype=bool)
+        is_cand[self.split] = True
+        local = [self.view_ids[p] for p in positions]
+        self.flags = O.ever_dominant([self.renders[v][1] for v in local], n).astype(np.uint8)
+        self.regions = {v: O.view_regions(self.renders[v], self.gts[v], is_cand, self.cfg, v) for v in local}
+
+    def dom_flags(self):
+        return torch.from_numpy(self.flags.copy())
+
+    def set_dom_flags(self, t):
+        self.dom_any = t.numpy().astype(bool)
+
+    def refresh(self):
+        return int((~self.dom_any[np.asarray(self.split, dtype=np.int64)]).sum())
+
+    def start_normals(self, nf):
+        self.nf = nf   # the oracle draws them inline, in ascending parent order
+
+    def local(self):
+        return {"regions": torch.frombuffer(bytearray(pickle.dumps(self.regions)), dtype=torch.uint8)}
+
+    def import_(self, gathered):
+        self.all_regions = {}
+        for t in gathered["regions"]:
+            self.all_regions.update(pickle.loads(t.numpy().tobytes()))
+
+    def merge(self):
+        assert sorted(self.all_regions) == self.view_ids
+
+    def emit(self):
+        return O.step_finish(self.g, self.cams, self.view_ids, self.all_regions, self.dom_any, self.split,
+                             self.clone, self.cfg, self.rng)
+
+
+def _digest(res):
+    gs = res.gaussians
+    return {"mu": gs.mu, "scale": gs.scale, "rot": gs.rot, "opacity": gs.opacity, "sh_dc": gs.sh_dc,
+            "index_map": res.index_map, "clones": np.array(res.clones), "reset": np.array(res.reset_indices),
+            "merge_edges": np.array([res.merge_edges]),
+            "cands": np.array([[c.index, c.proposals, c.merged, c.children_inserted, int(c.fallback), int(c.reset)]
+                               + list(c.regions_per_view) for c in res.candidates])}
+
+
+def _renders(g, cams):
+    return {v: O.render(g, cams[v]) for v in range(len(cams))}
+
+
+def _worker(rank, world, port, tag, out_dir):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        g, extent, cams, gts, ga, den, cfg, seed = _inputs(tag)
+        renders = _renders(g, cams)
+        ex = OracleExecutor(g, extent, cams, gts, ga, den, cfg, np.random.default_rng(seed), renders)
+        res = SH.run_sharded(ex, len(ex.view_ids))
+        with open(os.path.join(out_dir, f"r{rank}.pkl"), "wb") as f:
+            pickle.dump((_digest(res), ex.rng.bit_generator.state), f)
+    finally:
+        dist.destroy_process_group()
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def test_shard_views_partition():
+    for V in (1, 5, 64):
+        for world in range(1, min(V, 8) + 1):
+            parts = [SH.shard_views(V, world, r) for r in range(world)]
+            assert sorted(sum(parts, [])) == list(range(V))
+            assert max(map(len, parts)) - min(map(len, parts)) <= 1
+    with pytest.raises(ValueError):
+        SH.shard_views(4, 2, 2)
+
+
+@pytest.mark.parametrize("world", [2, 3])
+@pytest.mark.parametrize("tag", TAGS)
+def test_sharded_step_matches_single_process(tmp_path, tag, world):
+    g, extent, cams, gts, ga, den, cfg, seed = _inputs(tag)
+    if world > int(O.cfg_get(cfg, "v_views")):
+        pytest.skip("fewer sampled views than ranks")
+    mp.spawn(_worker, args=(world, _free_port(), tag, str(tmp_path)), nprocs=world, join=True)
+    rng = np.random.default_rng(seed)
+    want = _digest(O.adpsplit_step(g, extent, cams, gts, ga, den, cfg, rng, renders=_renders(g, cams)))
+    for r in range(world):
+        with open(tmp_path / f"r{r}.pkl", "rb") as f:
+            got, state = pickle.load(f)
+        for k in want:
+            np.testing.assert_array_equal(got[k], want[k], err_msg=f"rank {r}: {k}")
+        assert state == rng.bit_generator.state   # the Generator advanced exactly as one process would
+
+
+def test_all_gather_bytes_ragged(tmp_path):
+    mp.spawn(_gather_worker, args=(3, _free_port(), str(tmp_path)), nprocs=3, join=True)
+    for r in range(3):
+        with open(tmp_path / f"g{r}.pkl", "rb") as f:
+            got = pickle.load(f)
+        assert got == [list(range(k * 5)) for k in range(3)]
+
+
+def _gather_worker(rank, world, port, out_dir):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        t = torch.arange(rank * 5, dtype=torch.uint8)
+        parts = SH.all_gather_bytes(t)
+        with open(os.path.join(out_dir, f"g{rank}.pkl"), "wb") as f:
+            pickle.dump([p.tolist() for p in parts], f)
+    finally:
+        dist.destroy_process_group()
