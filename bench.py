@@ -277,10 +277,17 @@ def run_ours(args, wl):
     torch.cuda.synchronize()
     render_ms = ev0.elapsed_time(ev1)
 
+    sharded = world > 1 and not args.replicas
+    if sharded:
+        from paper_2605_06876_b200 import sharded as SH
+        step_fn = SH.densify_step_sharded   # views sharded over ranks, records gathered
+    else:
+        step_fn = op.densify_step
+
     def step():
         rng = np.random.default_rng((args.seed, 0))
-        return op.densify_step(g, ini.extent, cams, gt_img, ga, den, cfg, rng, renders=(img, dom),
-                               plan=plan, view_ids=view_ids, want_report=True)
+        return step_fn(g, ini.extent, cams, gt_img, ga, den, cfg, rng, renders=(img, dom),
+                       plan=plan, view_ids=view_ids, want_report=True)
 
     for _ in range(max(args.warmup, 1)):
         res = step()
@@ -351,9 +358,9 @@ def run_ours(args, wl):
         def e2e_step():
             d = {k_: t_.to(dev, non_blocking=True) for k_, t_ in host.items()}
             gg = op.GaussianTensors(d["mu"], d["scale"], d["rot"], d["opacity"], d["sh_dc"])
-            r = op.densify_step(gg, ini.extent, cams, d["gt"], d["ga"], d["den"], cfg,
-                                np.random.default_rng((args.seed, 0)), renders=(d["img"], d["dom"]), plan=plan,
-                                view_ids=view_ids, want_report=True)
+            r = step_fn(gg, ini.extent, cams, d["gt"], d["ga"], d["den"], cfg,
+                        np.random.default_rng((args.seed, 0)), renders=(d["img"], d["dom"]), plan=plan,
+                        view_ids=view_ids, want_report=True)
             for k_ in out_h:
                 out_h[k_].copy_(getattr(r.gaussians, k_), non_blocking=True)
             im_h.copy_(r.index_map, non_blocking=True)
@@ -447,15 +454,14 @@ def main():
     ap.add_argument("--cpu-cand-frac", type=float, default=0.25)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--replicas", action="store_true", help="N>1: independent replicas (weak scaling)")
+    ap.add_argument("--replicas", action="store_true",
+                    help="N>1: independent replicas (weak scaling) instead of the view-sharded step")
     args = ap.parse_args()
     from paper_2605_06876_b200.synth import CONFIGS
     wl = CONFIGS[args.config]
     if args.impl == "reference":
         run_reference(args, wl)
     else:
-        if int(os.environ.get("WORLD_SIZE", "1")) > 1:
-            args.replicas = True   # sharded step: see DESIGN.md (replicas until the sharded path lands)
         run_ours(args, wl)
 
 
