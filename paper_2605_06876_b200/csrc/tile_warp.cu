@@ -81,13 +81,17 @@ struct TileConst {
 template <bool RAW>
 struct RowIn {
   float a[3], g[3];
-  int d;      // dominant id if it is a split candidate (tile rows), else -1
+  int d;        // dominant id (tile rows), else -1
+  unsigned cb;  // candidate bits word holding this pixel (consumed in scan_row, so the
+  int sh;       // loads stay in flight while the previous row is scanned); bit index
   bool inb;
 };
 template <>
 struct RowIn<true> {
   double raw;
   int d;
+  unsigned cb;
+  int sh;
   bool inb;
 };
 
@@ -107,9 +111,9 @@ __device__ __forceinline__ void load_row(RowIn<RAW>& r, const TileConst& T, int 
   }
   // candidate bit (written by the minmax pass) instead of a dependent cls[D] load
   const bool need = r.inb && tile_row;
-  const int d = need ? __ldg(T.dom + p) : -1;
-  const unsigned cb = need ? __ldg(T.cbits + (p >> 5)) : 0u;
-  r.d = (cb >> (p & 31)) & 1u ? d : -1;
+  r.d = need ? __ldg(T.dom + p) : -1;
+  r.cb = need ? __ldg(T.cbits + (p >> 5)) : 0u;
+  r.sh = (int)(p & 31);
 }
 
 // np.abs(rendered - gt).sum(axis=-1) == (|d0| + |d1|) + |d2| in fp64
@@ -150,7 +154,7 @@ template <int R, bool RAW>
 __device__ __forceinline__ bool scan_row(const RowIn<RAW>& row, const int ey, ScanState& st, WarpSmem& S,
                                          const TileConst& T, const int lane) {
   const bool inb = row.inb;
-  const int c_now = row.d;
+  const int c_now = (row.cb >> row.sh) & 1u ? row.d : -1;
   constexpr int HL = R > 1 ? R / 2 : 0;
   constexpr int HH = R > 1 ? R - R / 2 - 1 : 0;
   constexpr int SPAN = HL + HH;
@@ -306,7 +310,8 @@ __device__ __forceinline__ void tile_warp_body(const TileParams& P, WarpSmem& S,
   st.n_runs = 0;
   bool overflow = false;
   {
-    // rows are loaded one ahead into two alternating register buffers
+    // rows are loaded one ahead into two alternating register buffers (deeper
+    // rings measured slower: register spills)
     RowIn<RAW> A, B;
     load_row<HL, RAW>(A, T, 0, lane);
     for (int ey = 0; ey < NR; ey += 2) {
