@@ -244,6 +244,9 @@ ADPS_API adps_status adps_step_phase1_merge(adps_plan* plan, void* stream, adps_
 #define ADPS_PARAM_DEFERRED_TILES 3
 #define ADPS_PARAM_NORMALS_CONSUMED 4   /* read-only, see adps_normals_pcg64 */
 #define ADPS_PARAM_NORMALS_STATUS 5     /* read-only, see adps_normals_pcg64 */
+#define ADPS_PARAM_STAT_TILE_PAIRS 7     /* read-only diagnostics of the last phase 1: surviving */
+#define ADPS_PARAM_STAT_GATES 8          /* large-parent tile pairs; gates evaluated and passed */
+#define ADPS_PARAM_STAT_GATES_PASSED 9   /* in them (the last two only in stats builds) */
 #define ADPS_PARAM_RAW_CACHE 6          /* 1 (default): the minmax pass caches the fp64 raw
                                            L1 error (8 B/px) for the warp CCL; 0: recompute */
 ADPS_API adps_status adps_set_param(adps_plan* plan, int32_t key, int64_t value);

@@ -103,6 +103,7 @@ struct Counters {
   unsigned long long n_fallback_pre;
   unsigned long long n_deferred;   // tiles the warp CCL handed to the block CCL
   unsigned long long normals_consumed;   // 64-bit draws used by adps_normals_pcg64
+  unsigned long long stat_gates, stat_pass;   // diagnostics (ADPS_MERGE_STATS builds)
   unsigned int normals_status;           // bit0 near-tie (redraw on host), bit1 window short
   unsigned int degenerate;
   unsigned int overflow;   // bit0 regions, bit1 partials

@@ -20,6 +20,10 @@
 
 #include "merge.cuh"
 
+#ifndef ADPS_MERGE_STATS
+#define ADPS_MERGE_STATS 0
+#endif
+
 namespace adps {
 
 __device__ __forceinline__ bool gate(const Proposal& A, const Proposal& B, double gd, double gc) {
@@ -364,54 +368,101 @@ __device__ __forceinline__ bool gate_soa(const double* A, const double (*Bs)[kMT
   return d <= gd;
 }
 
-// one block per surviving kMT x kMT tile pair of a large parent's gate matrix (or,
-// if the survivor list overflowed, every tile pair with the box test inline)
+struct PairBuf {
+  double s[2][kG_fields][kMT];   // [tile i / tile j][field][proposal]
+  int q[2][kMT];
+};
+
+__device__ __forceinline__ void cp_async(void* dst, const void* src, int bytes) {
+  const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+  if (bytes == 8) asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(d), "l"(src) : "memory");
+  else asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(d), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+// stage the gate operands of tile pair (l, bi, bj) into B (asynchronous copies)
+__device__ __forceinline__ void stage_pair(const MergeArgs& a, PairBuf& B, long long l, long long bi, long long bj) {
+  const long long P = (long long)a.lp_cnt[l];
+  const long long base = (long long)a.lp_off[l];
+  const int i0 = (int)(bi * kMT), j0 = (int)(bj * kMT);
+  const int ni = (int)min((long long)kMT, P - i0), nj = (int)min((long long)kMT, P - j0);
+  for (int t = threadIdx.x; t < 2 * kG_fields * kMT; t += blockDim.x) {
+    const int half = t / (kG_fields * kMT), r = t % (kG_fields * kMT);
+    const int f = r / kMT, loc = r % kMT;
+    if (loc < (half ? nj : ni))
+      cp_async(&B.s[half][f][loc], a.gsoa + (long long)f * a.soa_cap + base + (half ? j0 : i0) + loc, 8);
+  }
+  for (int t = threadIdx.x; t < 2 * kMT; t += blockDim.x) {
+    const int half = t / kMT, loc = t % kMT;
+    if (loc < (half ? nj : ni)) cp_async(&B.q[half][loc], a.mval_sorted + base + (half ? j0 : i0) + loc, 4);
+  }
+  cp_async_commit();
+}
+
+__device__ __forceinline__ void gates_pair(const MergeArgs& a, const PairBuf& B, long long l, long long bi,
+                                           long long bj) {
+  const long long P = (long long)a.lp_cnt[l];
+  const int ni = (int)min((long long)kMT, P - bi * kMT), nj = (int)min((long long)kMT, P - bj * kMT);
+  for (int t = threadIdx.x; t < kMT * kMT; t += blockDim.x) {
+    const int ii = t / kMT, jj = t % kMT;
+    // unordered pairs: within a diagonal tile take ii < jj once
+    if (ii < ni && jj < nj && (bi != bj || ii < jj)) {
+      double A[kG_fields];
+#pragma unroll
+      for (int f = 0; f < kG_fields; ++f) A[f] = B.s[0][f][ii];
+      const bool ok = gate_soa(A, B.s[1], jj, a.gamma_d, a.gamma_c);
+#if ADPS_MERGE_STATS
+      atomicAdd(&a.ctr->stat_gates, 1ull);
+      if (ok) atomicAdd(&a.ctr->stat_pass, 1ull);
+#endif
+      if (ok) uf_unite(a.uf, B.q[0][ii], B.q[1][jj]);
+    }
+  }
+}
+
+// one CTA per surviving kMT x kMT tile pair of a large parent's gate matrix,
+// the next pair's operands staged by cp.async while this pair is gated (or, if
+// the survivor list overflowed, every tile pair with the box test inline)
 __global__ void __launch_bounds__(256) pair_tiles_kernel(MergeArgs a) {
-  __shared__ double si[kG_fields][kMT], sj[kG_fields][kMT];
-  __shared__ int qi[kMT], qj[kMT];
+  __shared__ PairBuf buf[2];
   const bool overflow = (a.ctr->overflow & 4u) != 0;
   const long long n_large = (long long)a.ctr->n_large;
-  const unsigned long long W = overflow ? (n_large > 0 ? a.work_off[n_large] : 0) : a.ctr->n_tile_pairs;
-  for (unsigned long long w = blockIdx.x; w < W; w += gridDim.x) {
-    long long l, bi, bj;
-    if (overflow) {
+  if (overflow) {
+    const unsigned long long W = n_large > 0 ? a.work_off[n_large] : 0;
+    for (unsigned long long w = blockIdx.x; w < W; w += gridDim.x) {
+      long long l, bi, bj;
       decode_tile_pair(a, n_large, w, l, bi, bj);
       const long long tb = (long long)a.tile_off[l];
       if (!boxes_may_merge(a.boxes[tb + bi], a.boxes[tb + bj], a.gamma_d, a.gamma_c)) continue;   // uniform
+      stage_pair(a, buf[0], l, bi, bj);
+      cp_async_wait<0>();
+      __syncthreads();
+      gates_pair(a, buf[0], l, bi, bj);
+      __syncthreads();
+    }
+    return;
+  }
+  const unsigned long long W = a.ctr->n_tile_pairs;
+  unsigned long long w = blockIdx.x;
+  if (w >= W) return;
+  int4 cur = a.tile_pairs[w];
+  stage_pair(a, buf[0], cur.x, cur.y, cur.z);
+  for (int it = 0; w < W; ++it, w += gridDim.x) {
+    const unsigned long long nw = w + gridDim.x;
+    int4 nxt = cur;
+    if (nw < W) {
+      nxt = a.tile_pairs[nw];
+      stage_pair(a, buf[(it + 1) & 1], nxt.x, nxt.y, nxt.z);
+      cp_async_wait<1>();
     } else {
-      const int4 tp = a.tile_pairs[w];
-      l = tp.x;
-      bi = tp.y;
-      bj = tp.z;
-    }
-    const long long P = (long long)a.lp_cnt[l];
-    const long long base = (long long)a.lp_off[l];
-    const int i0 = (int)(bi * kMT), j0 = (int)(bj * kMT);
-    const int ni = (int)min((long long)kMT, P - i0), nj = (int)min((long long)kMT, P - j0);
-    for (int t = threadIdx.x; t < 2 * kG_fields * kMT; t += blockDim.x) {
-      const int half = t / (kG_fields * kMT), r = t % (kG_fields * kMT);
-      const int f = r / kMT, loc = r % kMT;
-      if (loc < (half ? nj : ni)) {
-        const double x = a.gsoa[(long long)f * a.soa_cap + base + (half ? j0 : i0) + loc];
-        (half ? sj : si)[f][loc] = x;
-      }
-    }
-    for (int t = threadIdx.x; t < 2 * kMT; t += blockDim.x) {
-      const int loc = t % kMT;
-      if (loc < (t < kMT ? ni : nj)) (t < kMT ? qi : qj)[loc] = a.mval_sorted[base + (t < kMT ? i0 : j0) + loc];
+      cp_async_wait<0>();
     }
     __syncthreads();
-    for (int t = threadIdx.x; t < kMT * kMT; t += blockDim.x) {
-      const int ii = t / kMT, jj = t % kMT;
-      // unordered pairs: within a diagonal tile take ii < jj once
-      if (ii < ni && jj < nj && (bi != bj || ii < jj)) {
-        double A[kG_fields];
-#pragma unroll
-        for (int f = 0; f < kG_fields; ++f) A[f] = si[f][ii];
-        if (gate_soa(A, sj, jj, a.gamma_d, a.gamma_c)) uf_unite(a.uf, qi[ii], qj[jj]);
-      }
-    }
-    __syncthreads();
+    gates_pair(a, buf[it & 1], cur.x, cur.y, cur.z);
+    __syncthreads();   // buf[it & 1] is restaged two iterations on
+    cur = nxt;
   }
 }
 

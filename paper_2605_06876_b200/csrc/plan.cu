@@ -1219,6 +1219,9 @@ extern "C" adps_status adps_get_param(adps_plan* P, int32_t key, int64_t* value)
     case ADPS_PARAM_LARGE_THRESHOLD: *value = P->large_threshold; return ADPS_OK;
     case ADPS_PARAM_TILE_PATH: *value = P->tile_path; return ADPS_OK;
     case ADPS_PARAM_RAW_CACHE: *value = P->raw_cache; return ADPS_OK;
+    case ADPS_PARAM_STAT_TILE_PAIRS: *value = P->ctr_host ? (int64_t)P->ctr_host->n_tile_pairs : 0; return ADPS_OK;
+    case ADPS_PARAM_STAT_GATES: *value = P->ctr_host ? (int64_t)P->ctr_host->stat_gates : 0; return ADPS_OK;
+    case ADPS_PARAM_STAT_GATES_PASSED: *value = P->ctr_host ? (int64_t)P->ctr_host->stat_pass : 0; return ADPS_OK;
     case ADPS_PARAM_DEFERRED_TILES: *value = P->ctr_host ? (int64_t)P->ctr_host->n_deferred : 0; return ADPS_OK;
     case ADPS_PARAM_NORMALS_CONSUMED:
       *value = P->ctr_host ? (int64_t)P->ctr_host->normals_consumed : 0;

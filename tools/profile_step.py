@@ -38,3 +38,5 @@ res = step()
 torch.cuda.synchronize()
 torch.cuda.cudart().cudaProfilerStop()
 print("deferred tiles", plan.deferred_tiles(), "counts", res.counts)
+for k, name in ((7, "tile_pairs"), (8, "gates"), (9, "gates_passed")):
+    print(name, plan.get_param(k))
