@@ -272,6 +272,26 @@ ADPS_API adps_status adps_get_launch_count(adps_plan* plan, int64_t* kernels, in
 ADPS_API adps_status adps_normals_pcg64(adps_plan* plan, void* stream, const uint64_t state[2], const uint64_t inc[2],
                                         int64_t n, double* out, int32_t sync, int64_t* consumed, int32_t* status);
 
+/* ---- the next rows of the path ----
+ * vanilla_densify (ref/adc.py:248-280): select, then every split candidate is
+ * replaced by n_children vanilla_split children (3 normals each from the
+ * caller's Generator, ascending parent order -> 3*n_children*n_split normals,
+ * e.g. adps_normals_pcg64), clones appended; adps_step_phase2 writes the
+ * grown arrays.  Same plan/report machinery as adpsplit. */
+ADPS_API adps_status adps_vanilla_phase1(adps_plan* plan, void* stream, const adps_gaussians* g, int64_t n,
+                                         double extent, const double* grad_accum, const double* denom,
+                                         const adps_config* cfg, int32_t n_children, adps_counts* counts);
+/* Post-step state remap.  adps_reset_flags: flags[old] = 1 for the last
+ * step's reset candidates (and, with include_clones, clone sources) -- the
+ * `reset` set of remap_stats (ref/adc.py:283-296, with clones) and of the
+ * trainer's optimizer-moment remap (ref/harness.py:285-295, without).
+ * adps_remap_rows: out[new] = in[index_map[new]] (rows of row_bytes, a
+ * multiple of 4) when index_map[new] >= 0 and not zero_old[index_map[new]]
+ * (zero_old may be NULL), else zeros. */
+ADPS_API adps_status adps_reset_flags(adps_plan* plan, void* stream, uint8_t* flags, int32_t include_clones);
+ADPS_API adps_status adps_remap_rows(void* stream, const int64_t* index_map, int64_t n_out, const uint8_t* zero_old,
+                                     const void* in, int64_t row_bytes, void* out);
+
 /* DensifyStats feed (ref/adc.py:73-79): grad_accum[vis] += |vg|, denom[vis] += 1.
  * viewspace_grad [n,2] fp32, visible [n] uint8. */
 ADPS_API adps_status adps_accumulate_stats(void* stream, double* grad_accum, double* denom,

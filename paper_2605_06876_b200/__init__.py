@@ -2,6 +2,7 @@
 reference package's ``adpsplit_step`` (ref/adc.py:143-245).
 
 Public API mirrors the reference (ref/__init__.py): ``adpsplit_step``,
+``vanilla_densify``, ``remap_stats_ref`` (ref ``remap_stats``),
 ``render``, ``DensifyStats``, ``SplitReport``, ``CandidateRecord``,
 ``AdpSplitConfig``, ``Gaussian3D``, ``Camera``, ``Scene`` plus the tensor
 API ``densify_step`` / ``render_views`` / ``GaussianTensors`` / ``Plan``.
@@ -13,7 +14,8 @@ from .types import (AdpSplitConfig, Camera, CandidateRecord, DegenerateRayError,
 __version__ = "0.1.0"
 
 _OPS = ("adpsplit_step", "render", "densify_step", "render_views", "GaussianTensors", "Plan",
-        "StepResult", "sample_views", "camera_rows", "accumulate_stats_", "default_plan")
+        "StepResult", "sample_views", "camera_rows", "accumulate_stats_", "default_plan",
+        "vanilla_densify", "vanilla_densify_step", "remap_stats", "remap_stats_ref", "remap_rows")
 
 
 def __getattr__(name):

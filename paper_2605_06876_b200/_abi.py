@@ -62,7 +62,8 @@ EXPORTS = (
     "adps_set_debug_records", "adps_set_debug_maps", "adps_set_timing", "adps_get_timing",
     "adps_accumulate_stats", "adps_get_launch_count", "adps_set_param", "adps_get_param", "adps_normals_pcg64",
     "adps_set_view_sharding", "adps_get_buffer", "adps_step_phase1_refresh", "adps_step_phase1_local",
-    "adps_step_phase1_import", "adps_step_phase1_merge",
+    "adps_step_phase1_import", "adps_step_phase1_merge", "adps_vanilla_phase1", "adps_reset_flags",
+    "adps_remap_rows",
 )
 
 _lib = None
@@ -105,6 +106,10 @@ def load(path: str = LIB_PATH):
     lib.adps_step_phase1_local.argtypes = [vp, vp, C.POINTER(C.c_int64)]
     lib.adps_step_phase1_import.argtypes = [vp, vp, vp, vp, vp, C.c_int64]
     lib.adps_step_phase1_merge.argtypes = [vp, vp, C.POINTER(Counts)]
+    lib.adps_vanilla_phase1.argtypes = [vp, vp, C.POINTER(Gaussians), C.c_int64, C.c_double, vp, vp,
+                                        C.POINTER(Config), C.c_int32, C.POINTER(Counts)]
+    lib.adps_reset_flags.argtypes = [vp, vp, vp, C.c_int32]
+    lib.adps_remap_rows.argtypes = [vp, vp, C.c_int64, vp, vp, C.c_int64, vp]
     lib.adps_normals_pcg64.argtypes = [vp, vp, C.POINTER(C.c_uint64), C.POINTER(C.c_uint64), C.c_int64, vp,
                                        C.c_int32, C.POINTER(C.c_int64), C.POINTER(C.c_int32)]
     for name in EXPORTS:

@@ -122,6 +122,7 @@ struct adps_plan {
   long long launches = 0;
   long long lib_calls = 0;
   int large_threshold = 32;
+  int fb_children = 2;   // children per fallback parent of the last phase 1
   // view sharding: this plan's local view v is global view position view_offset + v * view_stride
   // of v_global_cfg sampled views (0 = the local views are all of them)
   int view_offset = 0, view_stride = 1, v_global_cfg = 0, v_glob = 0;
@@ -954,6 +955,7 @@ static adps_status phase1_merge(adps_plan* P, cudaStream_t s, adps_counts* count
   P->W = W;
   P->eta = cfg->eta;
   P->sh_k = g->sh_rest_k;
+  P->fb_children = 2;
   P->have_phase1 = true;
   if (C.degenerate) return fail(ADPS_DEGENERATE_RAY, "quadratic coefficient underflows (DegenerateRayError)");
   return ADPS_OK;
@@ -1063,6 +1065,7 @@ extern "C" adps_status adps_step_phase2(adps_plan* P, void* stream_v, const adps
   ea.children = P->children.as<float>();
   ea.normals = fallback_normals;
   ea.eta = P->eta;
+  ea.fb_children = P->fb_children;
   ea.mu = out->mu;
   ea.scale = out->scale;
   ea.rot = out->rot;
@@ -1293,6 +1296,116 @@ extern "C" adps_status adps_normals_pcg64(adps_plan* P, void* stream_v, const ui
     if (consumed) *consumed = (int64_t)P->ctr_host->normals_consumed;
     if (status) *status = (int32_t)P->ctr_host->normals_status;
   }
+  return ADPS_OK;
+}
+
+extern "C" adps_status adps_vanilla_phase1(adps_plan* P, void* stream_v, const adps_gaussians* g, int64_t n,
+                                           double extent, const double* grad_accum, const double* denom,
+                                           const adps_config* cfg, int32_t n_children, adps_counts* counts) {
+  if (!P) return fail(ADPS_INVALID_ARG, "plan is NULL");
+  P->have_phase1 = false;
+  P->have_begin = false;
+  adps_status st = check_gaussians(g, n);
+  if (st != ADPS_OK) return st;
+  if (!cfg || !counts) return fail(ADPS_INVALID_ARG, "cfg/counts is NULL");
+  if (n > 0 && (!grad_accum || !denom)) return fail(ADPS_INVALID_ARG, "stats arrays are NULL");
+  if (n_children < 1) return fail(ADPS_INVALID_ARG, "n_children must be >= 1");
+  if (!(extent > 0)) return fail(ADPS_INVALID_ARG, "scene extent must be > 0");
+  CK(cudaSetDevice(P->device));
+  cudaStream_t s = (cudaStream_t)stream_v;
+  const long long nn = n > 0 ? n : 1;
+  CK(ensure(P->cls, nn));
+  CK(ensure(P->cand_rank, 4 * nn));
+  CK(ensure(P->split_list, 4 * nn));
+  CK(ensure(P->clone_list, 4 * nn));
+  CK(ensure(P->keep_pos, 4 * nn));
+  CK(ensure(P->ctr, sizeof(Counters)));
+  Counters* ctr = P->ctr.as<Counters>();
+  CK(cudaMemsetAsync(ctr, 0, sizeof(Counters), s));
+  mark_start(P, s, true);
+  ScanState sst, sst2;
+  st = scan_state(P, P->scan_val, P->scan_flag, P->scan_ticket, nn, &sst);
+  if (st != ADPS_OK) return st;
+  SelectArgs sa;
+  sa.scale = g->scale;
+  sa.ga = grad_accum;
+  sa.den = denom;
+  sa.tau_g = cfg->tau_g;
+  sa.tau_s_abs = cfg->tau_s * extent;
+  sa.n = n;
+  sa.cls = P->cls.as<unsigned char>();
+  sa.cand_rank = P->cand_rank.as<int>();
+  sa.split_list = P->split_list.as<int>();
+  sa.clone_list = P->clone_list.as<int>();
+  sa.ctr = ctr;
+  CK(launch_select(sa, sst, s));
+  mark(P, "select", s, 1);
+  CK(cudaMemcpyAsync(P->ctr_host, ctr, sizeof(Counters), cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  const long long n_split = (long long)P->ctr_host->n_split;
+  const long long n_clone = (long long)P->ctr_host->n_clone;
+  const long long sc = n_split > 0 ? n_split : 1;
+  CK(ensure(P->cand_case, 4 * sc));
+  CK(ensure(P->cand_ins, 4 * sc));
+  CK(ensure(P->cand_merged, 4 * sc));
+  CK(ensure(P->cand_props, 4 * sc));
+  CK(ensure(P->ins_off, 4 * sc));
+  CK(ensure(P->fb_ord, 4 * sc));
+  CK(ensure(P->pstart, 4 * sc));
+  CK(ensure(P->children, 16));
+  CK(cudaMemsetAsync(P->cand_props.p, 0, 4 * sc, s));
+  CK(launch_vanilla_cases(P->cand_case.as<int>(), P->cand_ins.as<int>(), P->cand_merged.as<int>(), &ctr->n_split,
+                          n_children, s));
+  st = scan_state(P, P->scan2_val, P->scan2_flag, P->scan2_ticket, sc, &sst2);
+  if (st != ADPS_OK) return st;
+  OffsetArgs oa;
+  oa.n = n;
+  oa.cls = P->cls.as<unsigned char>();
+  oa.cand_rank = P->cand_rank.as<int>();
+  oa.cand_case = P->cand_case.as<int>();
+  oa.cand_ins = P->cand_ins.as<int>();
+  oa.ins_off = P->ins_off.as<int>();
+  oa.fb_ord = P->fb_ord.as<int>();
+  oa.keep_pos = P->keep_pos.as<int>();
+  oa.ctr = ctr;
+  oa.n_split_dev = &ctr->n_split;
+  CK(launch_offsets(oa, n_split, sst2, sst, s));
+  mark(P, "offsets", s, 3);
+  CK(cudaMemcpyAsync(P->ctr_host, ctr, sizeof(Counters), cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  adps_counts& K = P->counts;
+  K = adps_counts{};
+  K.n_before = n;
+  K.n_split = n_split;
+  K.n_clone = n_clone;
+  K.n_keep = (long long)P->ctr_host->n_keep;
+  K.n_inserted = (long long)P->ctr_host->n_inserted;
+  K.n_out = K.n_keep + K.n_inserted + n_clone;
+  K.n_fallback = n_split;
+  *counts = K;
+  P->n = n;
+  P->V = 0;
+  P->eta = cfg->eta;
+  P->sh_k = g->sh_rest_k;
+  P->fb_children = n_children;
+  P->have_phase1 = true;
+  return ADPS_OK;
+}
+
+extern "C" adps_status adps_reset_flags(adps_plan* P, void* stream_v, uint8_t* flags, int32_t include_clones) {
+  if (!P || !flags) return fail(ADPS_INVALID_ARG, "NULL argument");
+  if (!P->have_phase1) return fail(ADPS_BAD_STATE, "no phase 1 result");
+  CK(cudaSetDevice(P->device));
+  CK(launch_reset_flags(flags, P->n, P->split_list.as<int>(), P->cand_case.as<int>(), P->counts.n_split,
+                        P->clone_list.as<int>(), P->counts.n_clone, include_clones != 0, (cudaStream_t)stream_v));
+  return ADPS_OK;
+}
+
+extern "C" adps_status adps_remap_rows(void* stream, const int64_t* index_map, int64_t n_out, const uint8_t* zero_old,
+                                       const void* in, int64_t row_bytes, void* out) {
+  if (n_out < 0 || row_bytes < 0 || row_bytes % 4) return fail(ADPS_INVALID_ARG, "row_bytes must be a multiple of 4");
+  if (n_out > 0 && row_bytes > 0 && (!index_map || !in || !out)) return fail(ADPS_INVALID_ARG, "NULL array");
+  CK(launch_remap_rows((const long long*)index_map, n_out, zero_old, in, row_bytes, out, (cudaStream_t)stream));
   return ADPS_OK;
 }
 

@@ -806,14 +806,15 @@ __global__ void emit_kernel(EmitArgs a) {
       if (c == ADPS_CASE_RESET) continue;
       const long long gi = a.split_list[k];
       long long dst = ins_base + a.ins_off[k];
-      if (c == ADPS_CASE_FALLBACK) {                      // vanilla_split(parent, 2, eta, rng)
+      if (c == ADPS_CASE_FALLBACK) {                      // vanilla_split(parent, n, eta, rng)
         double q[4] = {a.g.rot[4 * gi], a.g.rot[4 * gi + 1], a.g.rot[4 * gi + 2], a.g.rot[4 * gi + 3]};
         double R[9];
         quat_to_rot(q, R);
         const double s[3] = {a.g.scale[3 * gi], a.g.scale[3 * gi + 1], a.g.scale[3 * gi + 2]};
-        const double sh = a.eta * 2.0;
-        const double* z = a.normals + 6ll * a.fb_ord[k];
-        for (int c2 = 0; c2 < 2; ++c2, ++dst) {
+        const int nc = a.fb_children;
+        const double sh = a.eta * (double)nc;
+        const double* z = a.normals + 3ll * nc * a.fb_ord[k];
+        for (int c2 = 0; c2 < nc; ++c2, ++dst) {
           const double dl[3] = {z[3 * c2] * s[0], z[3 * c2 + 1] * s[1], z[3 * c2 + 2] * s[2]};
           copy_gaussian(a, gi, dst);
           for (int i = 0; i < 3; ++i) {
@@ -858,6 +859,73 @@ cudaError_t launch_emit(const EmitArgs& a, cudaStream_t s) {
     long long blocks = (total + 255) / 256;
     if (blocks > 148 * 16) blocks = 148 * 16;
     emit_kernel<<<(unsigned)blocks, 256, 0, s>>>(a);
+  }
+  return cudaGetLastError();
+}
+
+// ============================================================ vanilla_densify / remaps
+__global__ void vanilla_cases_kernel(int* cand_case, int* cand_ins, int* cand_merged,
+                                     const unsigned long long* n_split, int n_children) {
+  const long long n = (long long)*n_split;
+  for (long long k = (long long)blockIdx.x * blockDim.x + threadIdx.x; k < n; k += (long long)gridDim.x * blockDim.x) {
+    cand_case[k] = ADPS_CASE_FALLBACK;
+    cand_ins[k] = n_children;
+    cand_merged[k] = 0;
+  }
+}
+
+cudaError_t launch_vanilla_cases(int* cand_case, int* cand_ins, int* cand_merged, const unsigned long long* n_split,
+                                 int n_children, cudaStream_t s) {
+  vanilla_cases_kernel<<<148 * 4, 256, 0, s>>>(cand_case, cand_ins, cand_merged, n_split, n_children);
+  return cudaGetLastError();
+}
+
+__global__ void reset_flags_kernel(unsigned char* flags, long long n, const int* split_list, const int* cand_case,
+                                   long long n_split, const int* clone_list, long long n_clone, bool clones) {
+  const long long total = n_split + (clones ? n_clone : 0);
+  for (long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x; t < total;
+       t += (long long)gridDim.x * blockDim.x) {
+    if (t < n_split) {
+      if (cand_case[t] == ADPS_CASE_RESET) flags[split_list[t]] = 1;
+    } else {
+      flags[clone_list[t - n_split]] = 1;
+    }
+  }
+}
+
+cudaError_t launch_reset_flags(unsigned char* flags, long long n, const int* split_list, const int* cand_case,
+                               long long n_split, const int* clone_list, long long n_clone, bool clones,
+                               cudaStream_t s) {
+  cudaError_t e = cudaMemsetAsync(flags, 0, (size_t)(n > 0 ? n : 1), s);
+  if (e != cudaSuccess) return e;
+  if (n_split + n_clone > 0)
+    reset_flags_kernel<<<148 * 4, 256, 0, s>>>(flags, n, split_list, cand_case, n_split, clone_list, n_clone, clones);
+  return cudaGetLastError();
+}
+
+// out[new] = in[index_map[new]] for carried rows not flagged, zero otherwise; rows are
+// copied as 4-byte words (row_bytes % 4 == 0)
+__global__ void remap_rows_kernel(const long long* __restrict__ index_map, long long n_out,
+                                  const unsigned char* __restrict__ zero_old, const unsigned* __restrict__ in,
+                                  long long row_words, unsigned* __restrict__ out) {
+  const long long total = n_out * row_words;
+  for (long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x; t < total;
+       t += (long long)gridDim.x * blockDim.x) {
+    const long long r = t / row_words, w = t - r * row_words;
+    const long long old = index_map[r];
+    const bool carry = old >= 0 && !(zero_old && zero_old[old]);
+    out[t] = carry ? in[old * row_words + w] : 0u;
+  }
+}
+
+cudaError_t launch_remap_rows(const long long* index_map, long long n_out, const unsigned char* zero_old,
+                              const void* in, long long row_bytes, void* out, cudaStream_t s) {
+  const long long words = n_out * (row_bytes / 4);
+  if (words > 0) {
+    long long b = (words + 255) / 256;
+    if (b > 148 * 32) b = 148 * 32;
+    remap_rows_kernel<<<(unsigned)b, 256, 0, s>>>(index_map, n_out, zero_old, (const unsigned*)in, row_bytes / 4,
+                                                 (unsigned*)out);
   }
   return cudaGetLastError();
 }

@@ -106,6 +106,7 @@ struct EmitArgs {
   const float* children;
   const double* normals;
   double eta;
+  int fb_children;          // children per fallback parent: 2 (ref/adc.py:219), n (vanilla_densify)
   float* mu;
   float* scale;
   float* rot;
@@ -118,5 +119,15 @@ cudaError_t launch_emit(const EmitArgs& a, cudaStream_t s);
 
 cudaError_t launch_accumulate(double* ga, double* den, const float* vg, const unsigned char* vis,
                               long long n, cudaStream_t s);
+
+// vanilla_densify (ref/adc.py:248-280): every split candidate is split into n children
+cudaError_t launch_vanilla_cases(int* cand_case, int* cand_ins, int* cand_merged, const unsigned long long* n_split,
+                                 int n_children, cudaStream_t s);
+// post-step remaps (ref/adc.py:283-296, ref/harness.py:285-295)
+cudaError_t launch_reset_flags(unsigned char* flags, long long n, const int* split_list, const int* cand_case,
+                               long long n_split, const int* clone_list, long long n_clone, bool clones,
+                               cudaStream_t s);
+cudaError_t launch_remap_rows(const long long* index_map, long long n_out, const unsigned char* zero_old,
+                              const void* in, long long row_bytes, void* out, cudaStream_t s);
 
 }  // namespace adps

@@ -356,6 +356,24 @@ class Plan:
         _abi.check(self.lib.adps_step_phase1_merge(self._h, self._stream(), C.byref(counts)))
         return counts.as_dict()
 
+    def vanilla_phase1(self, g, extent, grad_accum, denom, cfg, n_children: int) -> dict:
+        """select + every split candidate -> n_children vanilla children (ref/adc.py:248-280)."""
+        counts = _abi.Counts()
+        cs = config_struct(cfg)
+        ga = g.abi()
+        self._g_keep = (g, grad_accum, denom)
+        _abi.check(self.lib.adps_vanilla_phase1(self._h, self._stream(), C.byref(ga), g.n, float(extent),
+                                                _ptr(grad_accum), _ptr(denom), C.byref(cs), int(n_children),
+                                                C.byref(counts)))
+        return counts.as_dict()
+
+    def reset_flags(self, include_clones: bool) -> torch.Tensor:
+        """uint8 [n_before]: the last step's reset candidates (and clone sources)."""
+        n = self._g_keep[0].n
+        flags = torch.empty(max(n, 1), dtype=torch.uint8, device=self.device)
+        _abi.check(self.lib.adps_reset_flags(self._h, self._stream(), _ptr(flags), int(bool(include_clones))))
+        return flags[:n]
+
     def phase2(self, g, normals, out: GaussianTensors, index_map: torch.Tensor):
         ga = g.abi()
         oa = _abi.GaussiansOut(out.mu.data_ptr(), out.scale.data_ptr(), out.rot.data_ptr(),
@@ -477,7 +495,9 @@ class StepResult:
         rep.clones = [int(i) for i in ra["clone_index"]]
         for k, i in enumerate(ra["cand_index"]):
             case = int(ra["cand_case"][k])
-            rec = CandidateRecord(index=int(i), regions_per_view=[int(x) for x in ra["regions_per_view"][k]],
+            rpv = ra["regions_per_view"]
+            rec = CandidateRecord(index=int(i),
+                                  regions_per_view=[int(x) for x in rpv[k]] if rpv.ndim == 2 and k < len(rpv) else [],
                                   proposals=int(ra["cand_proposals"][k]))
             if case == _abi.CASE_FALLBACK:
                 rec.fallback = True
@@ -505,15 +525,16 @@ class FallbackNormals:
     phase-1 end, then result().
     """
 
-    def __init__(self, plan: Plan, rng, nf: int):
+    def __init__(self, plan: Plan, rng, nf: int, children: int = 2):
         self.plan, self.rng, self.nf = plan, rng, int(nf)
+        self.count = 3 * int(children) * self.nf
         self.gpu = self.nf > 0 and isinstance(rng.bit_generator, np.random.PCG64)
         self.normals, self._drawn, self._th = None, {}, None
         if self.gpu:
-            self.normals, _, _ = plan.normals_pcg64(rng.bit_generator.state, 6 * self.nf, sync=False)
+            self.normals, _, _ = plan.normals_pcg64(rng.bit_generator.state, self.count, sync=False)
         elif self.nf > 0:
             def _draw():
-                self._drawn["z"] = rng.standard_normal(6 * self.nf)
+                self._drawn["z"] = rng.standard_normal(self.count)
 
             self._th = threading.Thread(target=_draw)
             self._th.start()
@@ -531,7 +552,7 @@ class FallbackNormals:
             if status == 0:
                 self.rng.bit_generator.advance(consumed)
             else:   # a wedge test too close to call against the host libm: draw on the host
-                self.normals = torch.from_numpy(self.rng.standard_normal(6 * self.nf)).to(self.plan.device)
+                self.normals = torch.from_numpy(self.rng.standard_normal(self.count)).to(self.plan.device)
             self.gpu = False
         elif self.nf > 0 and self.normals is None:
             self.normals = torch.from_numpy(self._drawn["z"]).to(self.plan.device)
@@ -584,6 +605,56 @@ def densify_step(g: GaussianTensors, extent: float, cameras, gt, grad_accum: tor
     if plan.timing:
         res.stage_ms = plan.stage_ms()
     return res
+
+
+def vanilla_densify_step(g: GaussianTensors, extent: float, grad_accum: torch.Tensor, denom: torch.Tensor, cfg,
+                         n_children: int, rng, *, plan: Plan = None, want_report: bool = True) -> StepResult:
+    """The binary ADC baseline on the device (ref/adc.py:248-280): every split
+    candidate becomes n_children vanilla_split children, clones appended."""
+    plan = plan or default_plan(g.device)
+    dev = plan.device
+    counts = plan.vanilla_phase1(g, extent, grad_accum.to(dev, F64).contiguous(), denom.to(dev, F64).contiguous(),
+                                 cfg, n_children)
+    nf, count = counts["n_split"], 3 * int(n_children) * counts["n_split"]
+    normals = None
+    if nf > 0 and isinstance(rng.bit_generator, np.random.PCG64):
+        normals, consumed, status = plan.normals_pcg64(rng.bit_generator.state, count, sync=True)
+        if status == 0:
+            rng.bit_generator.advance(consumed)
+        else:   # a wedge test too close to call against the host libm
+            normals = torch.from_numpy(rng.standard_normal(count)).to(dev)
+    elif nf > 0:
+        normals = torch.from_numpy(rng.standard_normal(count)).to(dev)
+    out = GaussianTensors.empty(counts["n_out"], g.sh_k, dev)
+    index_map = torch.empty(counts["n_out"], dtype=torch.int64, device=dev)
+    plan.phase2(g, normals, out, index_map)
+    res = StepResult(gaussians=out, index_map=index_map, counts=counts, view_ids=[], normals=normals)
+    if want_report:
+        res.report_arrays = plan.report_arrays(counts["n_split"], counts["n_clone"])
+    return res
+
+
+def remap_rows(index_map: torch.Tensor, values: torch.Tensor, zero_old: torch.Tensor = None) -> torch.Tensor:
+    """out[new] = values[index_map[new]] for carried rows not flagged in zero_old,
+    zeros for new rows (ref/adc.py:283-296, ref/harness.py:285-295), on the device."""
+    lib = _abi.load()
+    n_out = index_map.numel()
+    v = values.contiguous()
+    out = torch.empty((n_out,) + tuple(v.shape[1:]), dtype=v.dtype, device=v.device)
+    row_bytes = v.element_size() * (v[0].numel() if v.dim() > 1 and v.shape[0] else
+                                    int(np.prod(v.shape[1:], dtype=np.int64)))
+    stream = torch.cuda.current_stream(v.device).cuda_stream
+    _abi.check(lib.adps_remap_rows(C.c_void_p(stream), _ptr(index_map.contiguous()), n_out,
+                                   _ptr(zero_old) if zero_old is not None else None, _ptr(v), row_bytes,
+                                   _ptr(out)))
+    return out
+
+
+def remap_stats(plan: Plan, res: StepResult, grad_accum: torch.Tensor, denom: torch.Tensor):
+    """remap_stats (ref/adc.py:283-296) after densify_step / vanilla_densify_step:
+    carried Gaussians keep their accumulators unless reset or cloned; new ones start at 0."""
+    flags = plan.reset_flags(include_clones=True)
+    return (remap_rows(res.index_map, grad_accum.to(F64), flags), remap_rows(res.index_map, denom.to(F64), flags))
 
 
 def render_views(g: GaussianTensors, cameras, bg=(0.0, 0.0, 0.0), plan: Plan = None):
@@ -685,6 +756,56 @@ def adpsplit_step(scene, cameras, gt_images, stats, cfg, rng, *, plan: Plan = No
         raise RuntimeError(f"population mismatch: built {pos}, device reported {rep.count_after}")
     scene.gaussians = new
     return scene, rep
+
+
+def vanilla_densify(scene, stats, cfg, n_children: int, rng, *, plan: Plan = None):
+    """Drop-in for ``adpsplit.adc.vanilla_densify`` (ref/adc.py:248-280): the
+    binary ADC baseline, computed on the GPU; mutates ``scene.gaussians``
+    (survivors are the same objects) and returns (scene, SplitReport)."""
+    dev = _require_cuda()
+    plan = plan or default_plan(dev)
+    gs = list(scene.gaussians)
+    mu, scale, rot, op, dc, rest = _scene_arrays(gs)
+    g = GaussianTensors.from_numpy(mu, scale, rot, op, dc, rest if rest.shape[1] else None, dev)
+    res = vanilla_densify_step(g, scene.extent, torch.as_tensor(np.asarray(stats.grad_accum, dtype=np.float64),
+                                                                device=dev),
+                               torch.as_tensor(np.asarray(stats.denom, dtype=np.float64), device=dev), cfg,
+                               n_children, rng, plan=plan)
+    rep = res.report()
+    for rec in rep.candidates:
+        rec.children_inserted = int(n_children)
+    outg = res.gaussians.numpy()
+    make = type(gs[0]) if gs else Gaussian3D
+    new = [gs[int(i)] for i in rep.index_map[rep.index_map >= 0]]
+    pos = len(new)
+    for rec in rep.candidates:
+        p = gs[rec.index]
+        for _ in range(n_children):
+            new.append(make(mu=outg["mu"][pos].astype(np.float64), scale=p.scale / (cfg.eta * n_children),
+                            rot=p.rot, opacity=p.opacity, sh_dc=p.sh_dc, sh_rest=p.sh_rest))
+            pos += 1
+    for i in rep.clones:
+        p = gs[i]
+        new.append(make(mu=p.mu, scale=p.scale, rot=p.rot, opacity=p.opacity, sh_dc=p.sh_dc, sh_rest=p.sh_rest))
+        pos += 1
+    if pos != rep.count_after:
+        raise RuntimeError(f"population mismatch: built {pos}, device reported {rep.count_after}")
+    scene.gaussians = new
+    return scene, rep
+
+
+def remap_stats_ref(stats, report):
+    """Drop-in for ``adpsplit.adc.remap_stats`` (ref/adc.py:283-296) on the GPU:
+    carried Gaussians keep their accumulators unless reset or cloned."""
+    dev = _require_cuda()
+    n_old = len(np.asarray(stats.grad_accum))
+    flags = np.zeros(max(n_old, 1), np.uint8)
+    flags[[int(i) for i in report.reset_indices] + [int(i) for i in report.clones]] = 1
+    im = torch.as_tensor(np.asarray(report.index_map, dtype=np.int64), device=dev)
+    fl = torch.as_tensor(flags, device=dev)
+    ga = remap_rows(im, torch.as_tensor(np.asarray(stats.grad_accum, dtype=np.float64), device=dev), fl)
+    de = remap_rows(im, torch.as_tensor(np.asarray(stats.denom, dtype=np.float64), device=dev), fl)
+    return type(stats)(grad_accum=ga.cpu().numpy(), denom=de.cpu().numpy())
 
 
 @dataclass

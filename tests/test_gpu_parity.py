@@ -509,3 +509,87 @@ def test_sharded_lockstep_matches_single_gpu(op, world):
         for k in want:
             np.testing.assert_array_equal(got[k], want[k], err_msg=f"rank {r}: {k}")
         assert ex.rng.bit_generator.state == rng1.bit_generator.state
+
+
+# ------------------------------------------------- next rows: vanilla ADC, remaps
+@pytest.mark.parametrize("n_children", [2, 3])
+@pytest.mark.parametrize("tag", ["blobs", "desk0", "paper1"])
+def test_vanilla_densify_matches_oracle(op, tag, n_children):
+    """vanilla_densify (ref/adc.py:248-280) on the device vs the oracle: layout,
+    index_map and clones exact; children within float tolerance; the Generator
+    advanced exactly as numpy's."""
+    import torch
+    g, extent, cams, rows, gts, cfg, seed = _golden_step_inputs(tag)
+    ga, den = DATA[f"step__{tag}__grad_accum"], DATA[f"step__{tag}__denom"]
+    plan = op.Plan("cuda:0")
+    rng_g, rng_o = np.random.default_rng(seed), np.random.default_rng(seed)
+    res = op.vanilla_densify_step(PA.to_tensors(g), extent, torch.as_tensor(ga, device="cuda"),
+                                  torch.as_tensor(den, device="cuda"), cfg, n_children, rng_g, plan=plan)
+    want = O.vanilla_densify(g, extent, ga, den, cfg, n_children, rng_o)
+    assert res.counts["n_out"] == want.count_after
+    np.testing.assert_array_equal(res.index_map.cpu().numpy(), want.index_map)
+    got = res.gaussians.numpy()
+    w = PA.oracle_gaussians_f32(want.gaussians)
+    np.testing.assert_allclose(got["mu"], w.mu, rtol=2e-6, atol=1e-7)
+    np.testing.assert_allclose(got["scale"], w.scale, rtol=2e-6)
+    np.testing.assert_array_equal(got["opacity"], w.opacity.astype(np.float32))
+    rep = res.report()
+    assert [c.index for c in rep.candidates] == [c.index for c in want.candidates]
+    assert rep.clones == want.clones
+    assert rng_g.bit_generator.state == rng_o.bit_generator.state
+
+
+@pytest.mark.parametrize("tag", ["desk0", "paper1"])
+def test_remap_stats_matches_oracle(op, plan, tag):
+    """remap_stats (ref/adc.py:283-296) and the trainer's moment remap
+    (ref/harness.py:285-295) through the step's index_map, on the device."""
+    import torch
+    g, extent, cams, rows, gts, cfg, seed = _golden_step_inputs(tag)
+    ga, den = DATA[f"step__{tag}__grad_accum"], DATA[f"step__{tag}__denom"]
+    views = O.sample_views(len(cams), cfg.v_views, np.random.default_rng(seed))
+    img, dom = plan.render(PA.to_tensors(g), rows[views])
+    res = op.densify_step(PA.to_tensors(g), extent, rows, torch.as_tensor(gts, dtype=torch.float32, device="cuda"),
+                          torch.as_tensor(ga, device="cuda"), torch.as_tensor(den, device="cuda"), cfg,
+                          np.random.default_rng(seed), renders=(img, dom), plan=plan)
+    rep = res.report()
+    ga2, den2 = op.remap_stats(plan, res, torch.as_tensor(ga, device="cuda"), torch.as_tensor(den, device="cuda"))
+    want_g, want_d = O.remap_stats(ga, den, rep.index_map, rep.reset_indices, rep.clones)
+    np.testing.assert_array_equal(ga2.cpu().numpy(), want_g)
+    np.testing.assert_array_equal(den2.cpu().numpy(), want_d)
+    # optimizer moments: [n, 3] rows, reset candidates zeroed, clone sources carried
+    m = np.random.default_rng(1).normal(size=(len(ga), 3)).astype(np.float32)
+    got = op.remap_rows(res.index_map, torch.as_tensor(m, device="cuda"), plan.reset_flags(include_clones=False))
+    want = np.zeros((len(rep.index_map), 3), np.float32)
+    reset = set(rep.reset_indices)
+    for new_i, old_i in enumerate(rep.index_map):
+        if old_i >= 0 and old_i not in reset:
+            want[new_i] = m[old_i]
+    np.testing.assert_array_equal(got.cpu().numpy(), want)
+
+
+def test_reference_api_vanilla_and_remap(op):
+    """vanilla_densify(scene, stats, cfg, n, rng) and remap_stats(stats, report)
+    with the mirror types, against the oracle's restatements."""
+    from paper_2605_06876_b200 import types as T
+    tag = "desk3"
+    g, extent = golden_io.scene(DATA, f"step__{tag}__in")
+    gs = [T.Gaussian3D(mu=g.mu[i], scale=g.scale[i], rot=g.rot[i], opacity=g.opacity[i], sh_dc=g.sh_dc[i])
+          for i in range(len(g))]
+    scene = T.Scene(gaussians=list(gs), extent=extent)
+    m = META["step"][tag]
+    cfg = T.AdpSplitConfig(**{k: v for k, v in m["cfg"].items()})
+    ga, den = DATA[f"step__{tag}__grad_accum"].copy(), DATA[f"step__{tag}__denom"].copy()
+    stats = T.DensifyStats(ga, den)
+    rng = np.random.default_rng(7)
+    scene, rep = op.vanilla_densify(scene, stats, cfg, 3, rng)
+    want = O.vanilla_densify(g, extent, ga, den, golden_io.Cfg(m["cfg"]), 3, np.random.default_rng(7))
+    assert rep.count_after == want.count_after == len(scene.gaussians)
+    np.testing.assert_array_equal(rep.index_map, want.index_map)
+    assert rep.clones == want.clones
+    assert all(r.fallback and r.children_inserted == 3 for r in rep.candidates)
+    got = np.array([np.asarray(x.mu) for x in scene.gaussians])
+    np.testing.assert_allclose(got, want.gaussians.mu, rtol=1e-6, atol=1e-6)
+    st2 = op.remap_stats_ref(stats, rep)
+    wg, wd = O.remap_stats(ga, den, want.index_map, [], want.clones)
+    np.testing.assert_array_equal(st2.grad_accum, wg)
+    np.testing.assert_array_equal(st2.denom, wd)
