@@ -223,6 +223,9 @@ ADPS_API adps_status adps_get_timing(adps_plan* plan, double* ms, int32_t max_en
 #define ADPS_BUF_REGIONS 2
 #define ADPS_BUF_PROPOSALS 3
 #define ADPS_BUF_VALID 4
+#define ADPS_BUF_CAND_MERGED 5   /* int32 [n_split]: children per split parent */
+#define ADPS_BUF_CAND_INS 6      /* int32 [n_split]: inserted Gaussians per parent */
+#define ADPS_BUF_CHILDREN 7      /* 14 floats per proposal slot: children of parent k at its proposal range */
 ADPS_API adps_status adps_set_view_sharding(adps_plan* plan, int32_t view_offset, int32_t view_stride,
                                             int32_t n_views_global);
 ADPS_API adps_status adps_get_buffer(adps_plan* plan, int32_t which, void** ptr, int64_t* count, int64_t* elem_bytes);
@@ -231,6 +234,20 @@ ADPS_API adps_status adps_step_phase1_local(adps_plan* plan, void* stream, int64
 ADPS_API adps_status adps_step_phase1_import(adps_plan* plan, void* stream, const adps_region_record* regions,
                                              const void* proposals, const uint8_t* valid, int64_t n);
 ADPS_API adps_status adps_step_phase1_merge(adps_plan* plan, void* stream, adps_counts* counts);
+/* Parent sharding of phase B (merge, cap): with adps_set_parent_sharding(plan,
+ * r, g) the merge gates, groups and caps only rank r's contiguous range of
+ * split candidates (balanced by the sum of P_k^2 + 1, computed on the device
+ * identically on every rank).  adps_step_phase1_merge then stops after the
+ * cap (counts carries this rank's merge_edges / n_children); adps_get_shard
+ * gives the range [k_lo, k_hi) and its proposal range [p_lo, p_hi); the host
+ * all-gathers ADPS_BUF_CAND_MERGED / _CAND_INS [k_lo, k_hi) and
+ * ADPS_BUF_CHILDREN [p_lo, p_hi) of every rank into every plan, and
+ * adps_step_phase1_finish (with the summed merge_edges / n_children) runs the
+ * offsets; phase 2 is then identical on every rank. */
+ADPS_API adps_status adps_set_parent_sharding(adps_plan* plan, int32_t rank, int32_t world);
+ADPS_API adps_status adps_get_shard(adps_plan* plan, int64_t* k_lo, int64_t* k_hi, int64_t* p_lo, int64_t* p_hi);
+ADPS_API adps_status adps_step_phase1_finish(adps_plan* plan, void* stream, int64_t merge_edges, int64_t n_children,
+                                             adps_counts* counts);
 
 /* Tuning knobs (diagnostic/testing).  ADPS_PARAM_LARGE_THRESHOLD: parents
  * with more proposals than this use the grid-wide pair-tile merge path

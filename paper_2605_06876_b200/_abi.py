@@ -19,6 +19,7 @@ CASE_SPLIT, CASE_FALLBACK, CASE_RESET = 0, 1, 2
 PARAM_LARGE_THRESHOLD, PARAM_TILE_PATH, PARAM_DEFERRED_TILES = 1, 2, 3
 PARAM_NORMALS_CONSUMED, PARAM_NORMALS_STATUS, PARAM_RAW_CACHE = 4, 5, 6
 BUF_DOM_FLAG, BUF_REGIONS, BUF_PROPOSALS, BUF_VALID = 1, 2, 3, 4
+BUF_CAND_MERGED, BUF_CAND_INS, BUF_CHILDREN = 5, 6, 7
 
 vp = C.c_void_p
 
@@ -63,7 +64,7 @@ EXPORTS = (
     "adps_accumulate_stats", "adps_get_launch_count", "adps_set_param", "adps_get_param", "adps_normals_pcg64",
     "adps_set_view_sharding", "adps_get_buffer", "adps_step_phase1_refresh", "adps_step_phase1_local",
     "adps_step_phase1_import", "adps_step_phase1_merge", "adps_vanilla_phase1", "adps_reset_flags",
-    "adps_remap_rows",
+    "adps_remap_rows", "adps_set_parent_sharding", "adps_get_shard", "adps_step_phase1_finish",
 )
 
 _lib = None
@@ -109,6 +110,9 @@ def load(path: str = LIB_PATH):
     lib.adps_vanilla_phase1.argtypes = [vp, vp, C.POINTER(Gaussians), C.c_int64, C.c_double, vp, vp,
                                         C.POINTER(Config), C.c_int32, C.POINTER(Counts)]
     lib.adps_reset_flags.argtypes = [vp, vp, vp, C.c_int32]
+    lib.adps_set_parent_sharding.argtypes = [vp, C.c_int32, C.c_int32]
+    lib.adps_get_shard.argtypes = [vp] + [C.POINTER(C.c_int64)] * 4
+    lib.adps_step_phase1_finish.argtypes = [vp, vp, C.c_int64, C.c_int64, C.POINTER(Counts)]
     lib.adps_remap_rows.argtypes = [vp, vp, C.c_int64, vp, vp, C.c_int64, vp]
     lib.adps_normals_pcg64.argtypes = [vp, vp, C.POINTER(C.c_uint64), C.POINTER(C.c_uint64), C.c_int64, vp,
                                        C.c_int32, C.POINTER(C.c_int64), C.POINTER(C.c_int32)]

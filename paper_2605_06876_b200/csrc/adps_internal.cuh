@@ -103,7 +103,10 @@ struct Counters {
   unsigned long long n_fallback_pre;
   unsigned long long n_deferred;   // tiles the warp CCL handed to the block CCL
   unsigned long long normals_consumed;   // 64-bit draws used by adps_normals_pcg64
-  unsigned long long stat_gates, stat_pass;   // diagnostics (ADPS_MERGE_STATS builds)
+  unsigned long long stat_gates, stat_pass;
+  unsigned long long shard_lo, shard_hi;     // this rank's candidate range under parent sharding
+  unsigned long long shard_plo, shard_phi;   // ... and its proposal range
+  unsigned long long n_owned_props;          // proposals of this rank's parents   // diagnostics (ADPS_MERGE_STATS builds)
   unsigned int normals_status;           // bit0 near-tie (redraw on host), bit1 window short
   unsigned int degenerate;
   unsigned int overflow;   // bit0 regions, bit1 partials

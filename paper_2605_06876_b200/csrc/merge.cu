@@ -106,7 +106,9 @@ __global__ void case_kernel(MergeArgs a) {
       atomicAdd(&a.ctr->n_reset, 1ull);
     } else {
       a.cand_case[k] = ADPS_CASE_SPLIT;
-      if (P >= 2 && P <= a.small_max) {
+      if (!owns(a, k)) {
+        // another rank merges this parent
+      } else if (P >= 2 && P <= a.small_max) {
         a.small_list[atomicAdd(&a.ctr->n_small, 1ull)] = (int)k;
       } else if (P > a.small_max) {
         const unsigned long long l = atomicAdd(&a.ctr->n_large, 1ull);
@@ -183,6 +185,104 @@ __global__ void __launch_bounds__(1024) offsets_1block_kernel(const unsigned lon
     __syncthreads();
   }
   if (threadIdx.x == 0) out[n] = carry;
+}
+
+__global__ void __launch_bounds__(1024) shard_range_kernel(const int* __restrict__ nvalid, long long n, int rank,
+                                                           int world, unsigned long long* __restrict__ lohi) {
+  __shared__ unsigned long long warp_tot[32];
+  __shared__ unsigned long long carry, total;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  unsigned long long sum = 0;
+  for (long long i = threadIdx.x; i < n; i += blockDim.x) {
+    const unsigned long long p = (unsigned long long)nvalid[i];
+    sum += p * p + 1;
+  }
+  for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+  if (lane == 0) warp_tot[wid] = sum;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned long long t = 0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += warp_tot[w];
+    total = t;
+    carry = 0;
+    lohi[0] = (unsigned long long)n;
+    lohi[1] = 0;
+  }
+  __syncthreads();
+  const unsigned long long T = total;
+  for (long long base = 0; base < n; base += blockDim.x) {
+    const long long i = base + threadIdx.x;
+    const unsigned long long v = i < n ? (unsigned long long)nvalid[i] * (unsigned long long)nvalid[i] + 1 : 0ull;
+    unsigned long long x = v;
+    for (int o = 1; o < 32; o <<= 1) {
+      const unsigned long long y = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x += y;
+    }
+    __syncthreads();
+    if (lane == 31) warp_tot[wid] = x;
+    __syncthreads();
+    if (wid == 0) {
+      const unsigned long long w = warp_tot[lane];
+      unsigned long long wi = w;
+      for (int o = 1; o < 32; o <<= 1) {
+        const unsigned long long y = __shfl_up_sync(0xffffffffu, wi, o);
+        if (lane >= o) wi += y;
+      }
+      warp_tot[lane] = wi - w;
+    }
+    __syncthreads();
+    const unsigned long long excl = carry + warp_tot[wid] + x - v;
+    if (i < n) {
+      unsigned long long owner = excl * (unsigned long long)world / T;
+      if (owner >= (unsigned long long)world) owner = world - 1;
+      if ((int)owner == rank) {
+        atomicMin(&lohi[0], (unsigned long long)i);
+        atomicMax(&lohi[1], (unsigned long long)(i + 1));
+      }
+    }
+    __syncthreads();
+    if (threadIdx.x == blockDim.x - 1) carry = excl + v;
+    __syncthreads();
+  }
+}
+
+// proposal range of the rank's candidates: lohi[2..3] = sum of P_k over k < lo, k < hi
+// (pstart is only defined for parents with regions)
+__global__ void __launch_bounds__(1024) shard_prange_kernel(const int* __restrict__ nvalid, long long n,
+                                                            unsigned long long* __restrict__ lohi) {
+  __shared__ unsigned long long ws[2][32];
+  const unsigned long long lo = lohi[0], hi = lohi[1];
+  unsigned long long a = 0, b = 0;
+  for (long long i = threadIdx.x; i < n; i += blockDim.x) {
+    const unsigned long long p = (unsigned long long)nvalid[i];
+    if ((unsigned long long)i < lo) a += p;
+    if ((unsigned long long)i < hi) b += p;
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    a += __shfl_xor_sync(0xffffffffu, a, o);
+    b += __shfl_xor_sync(0xffffffffu, b, o);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    ws[0][threadIdx.x >> 5] = a;
+    ws[1][threadIdx.x >> 5] = b;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned long long sa = 0, sb = 0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) {
+      sa += ws[0][w];
+      sb += ws[1][w];
+    }
+    lohi[2] = hi > lo ? sa : 0;
+    lohi[3] = hi > lo ? sb : 0;
+  }
+}
+
+cudaError_t launch_shard_range(const int* nvalid, long long n, int rank, int world, unsigned long long* lohi,
+                               cudaStream_t s) {
+  shard_range_kernel<<<1, 1024, 0, s>>>(nvalid, n, rank, world, lohi);
+  shard_prange_kernel<<<1, 1024, 0, s>>>(nvalid, n, lohi);
+  return cudaGetLastError();
 }
 
 cudaError_t launch_merge_small_gates(const MergeArgs& a, cudaStream_t s) {
@@ -478,7 +578,9 @@ __global__ void flatten_kernel(MergeArgs a, long long cap) {
   const long long np = (long long)a.ctr->n_proposals;
   for (long long q = (long long)blockIdx.x * blockDim.x + threadIdx.x; q < cap;
        q += (long long)gridDim.x * blockDim.x) {
-    a.gkey[q] = q < np ? (unsigned)uf_find_halve(a.uf, (int)q) : 0xffffffffu;
+    const bool mine = q < np && owns(a, a.pcand[q]);
+    a.gkey[q] = mine ? (unsigned)uf_find_halve(a.uf, (int)q) : 0xffffffffu;
+    if (a.own && mine) atomicAdd(&a.ctr->n_owned_props, 1ull);
     a.gval[q] = (int)q;
   }
 }
@@ -501,7 +603,9 @@ struct GroupStartPolicy {
   }
   __device__ void total(unsigned long long t) const {
     a.ctr->n_groups_all = t;
-    a.grp_first[t] = (int)a.ctr->n_proposals;
+    // end of the last group's members: the non-padding entries (all proposals, or
+    // under parent sharding only this rank's)
+    a.grp_first[t] = (int)(a.own ? a.ctr->n_owned_props : a.ctr->n_proposals);
   }
 };
 

@@ -81,7 +81,18 @@ struct MergeArgs {
   float* children;                         // [cap,14]
   Counters* ctr;
   unsigned grid;
+  const unsigned long long* own;           // [lo, hi) candidate ranks this rank merges, or null = all
 };
+
+__device__ __forceinline__ bool owns(const MergeArgs& a, long long k) {
+  return !a.own || (k >= (long long)a.own[0] && k < (long long)a.own[1]);
+}
+
+// parent sharding: candidate k goes to rank floor(W_<k * world / W) with
+// W_<k the exclusive prefix of (P_k^2 + 1), the gate work; writes [lo, hi) and the
+// proposal range [p_lo, p_hi) to lohi[0..3]
+cudaError_t launch_shard_range(const int* nvalid, long long n, int rank, int world, unsigned long long* lohi,
+                               cudaStream_t s);
 
 cudaError_t launch_merge_prepare(const MergeArgs& a, long long n_split, ScanState st, cudaStream_t s);
 cudaError_t launch_merge_small_gates(const MergeArgs& a, cudaStream_t s);

@@ -127,6 +127,10 @@ struct adps_plan {
   // of v_global_cfg sampled views (0 = the local views are all of them)
   int view_offset = 0, view_stride = 1, v_global_cfg = 0, v_glob = 0;
   long long n_regions_cur = 0;   // region records the merge half consumes
+  // parent sharding of the merge: this rank gates/groups/caps only its range of candidates
+  int pshard_rank = 0, pshard_world = 1;
+  bool have_merge_part = false;
+  long long shard_k[2] = {0, 0}, shard_p[2] = {0, 0};   // this rank's candidate / proposal range
   bool have_local = false;
   int tile_path = 0;   // 0 warp CCL + deferred block CCL, 1 block CCL only
   int raw_cache = ADPS_RAW_CACHE_DEFAULT;   // minmax pass caches the raw L1 error for the warp CCL
@@ -712,7 +716,12 @@ static adps_status phase1_local(adps_plan* P, cudaStream_t s, long long* n_regio
 
 // sort + ranges + merge + cap + case + offsets over the plan's region records
 // (local ones, or the gathered records of all ranks after adps_step_phase1_import)
-static adps_status phase1_merge(adps_plan* P, cudaStream_t s, adps_counts* counts) {
+static adps_status phase1_finish(adps_plan* P, cudaStream_t s, adps_counts* counts);
+
+// sort + ranges + merge + cap over the plan's region records (local ones, or
+// the gathered records of all ranks after adps_step_phase1_import); with
+// parent sharding only this rank's candidate range is gated/grouped/capped
+static adps_status phase1_merge_part(adps_plan* P, cudaStream_t s) {
   CK(cudaSetDevice(P->device));
   adps_status st = ADPS_OK;
   const adps_gaussians* g = &P->cx.g;
@@ -723,12 +732,11 @@ static adps_status phase1_merge(adps_plan* P, cudaStream_t s, adps_counts* count
   const long long hw = (long long)H * W;
   const long long nn = n > 0 ? n : 1;
   Counters* ctr = P->ctr.as<Counters>();
-  ScanState sst, sst2;
+  ScanState sst;
   st = scan_state(P, P->scan_val, P->scan_flag, P->scan_ticket, nn, &sst);
   if (st != ADPS_OK) return st;
   const long long n_regions = P->n_regions_cur;
   const long long n_split = (long long)P->ctr_host->n_split;
-  const long long n_clone = (long long)P->ctr_host->n_clone;
   const long long rc = n_regions > 0 ? n_regions : 1;
   const int bits_v = ceil_log2((unsigned long long)V);
   const int bits_b = ceil_log2((unsigned long long)cfg->l_bands);
@@ -884,6 +892,12 @@ static adps_status phase1_merge(adps_plan* P, cudaStream_t s, adps_counts* count
   ma.tile_pairs_cap = (long long)(P->tile_pairs.bytes / sizeof(int4));
   ma.ctr = ctr;
   ma.grid = (unsigned)(P->sm_count * 8);
+  ma.own = nullptr;
+  if (P->pshard_world > 1 && n_split > 0) {
+    CK(launch_shard_range(P->cand_nvalid.as<int>(), n_split, P->pshard_rank, P->pshard_world, &ctr->shard_lo, s));
+    ma.own = &ctr->shard_lo;
+    P->launches += 2;
+  }
   if (n_split > 0) {
     ScanState sst3;
     st = scan_state(P, P->scan3_val, P->scan3_flag, P->scan3_ticket, rc, &sst3);
@@ -913,7 +927,24 @@ static adps_status phase1_merge(adps_plan* P, cudaStream_t s, adps_counts* count
       mark(P, "merge_cap", s, 2);
     }
   }
+  return ADPS_OK;
+}
 
+static adps_status phase1_finish(adps_plan* P, cudaStream_t s, adps_counts* counts) {
+  adps_status st = ADPS_OK;
+  const adps_gaussians* g = &P->cx.g;
+  const long long n = P->cx.n;
+  const adps_config* cfg = &P->cx.cfg;
+  const int V = P->v_glob, H = P->cx.H, W = P->cx.W;
+  const long long nn = n > 0 ? n : 1;
+  Counters* ctr = P->ctr.as<Counters>();
+  ScanState sst, sst2;
+  st = scan_state(P, P->scan_val, P->scan_flag, P->scan_ticket, nn, &sst);
+  if (st != ADPS_OK) return st;
+  const long long n_regions = P->n_regions_cur;
+  const long long n_split = (long long)P->ctr_host->n_split;
+  const long long n_clone = (long long)P->ctr_host->n_clone;
+  const long long sc = n_split > 0 ? n_split : 1;
   // ---- offsets (ref/adc.py:229-244)
   st = scan_state(P, P->scan2_val, P->scan2_flag, P->scan2_ticket, sc, &sst2);
   if (st != ADPS_OK) return st;
@@ -959,6 +990,12 @@ static adps_status phase1_merge(adps_plan* P, cudaStream_t s, adps_counts* count
   P->have_phase1 = true;
   if (C.degenerate) return fail(ADPS_DEGENERATE_RAY, "quadratic coefficient underflows (DegenerateRayError)");
   return ADPS_OK;
+}
+
+static adps_status phase1_merge(adps_plan* P, cudaStream_t s, adps_counts* counts) {
+  adps_status st = phase1_merge_part(P, s);
+  if (st != ADPS_OK) return st;
+  return phase1_finish(P, s, counts);
 }
 
 extern "C" adps_status adps_step_phase1_end(adps_plan* P, void* stream_v, adps_counts* counts) {
@@ -1029,7 +1066,64 @@ extern "C" adps_status adps_step_phase1_merge(adps_plan* P, void* stream_v, adps
   if (!P || !counts) return fail(ADPS_INVALID_ARG, "NULL argument");
   if (!P->have_local) return fail(ADPS_BAD_STATE, "phase1_merge without phase1_local");
   P->have_local = false;
-  return phase1_merge(P, (cudaStream_t)stream_v, counts);
+  cudaStream_t s = (cudaStream_t)stream_v;
+  if (P->pshard_world <= 1) return phase1_merge(P, s, counts);
+  // parent-sharded: merge this rank's candidates, then wait for the exchange
+  adps_status st = phase1_merge_part(P, s);
+  if (st != ADPS_OK) return st;
+  Counters* ctr = P->ctr.as<Counters>();
+  CK(cudaMemcpyAsync(P->ctr_host, ctr, sizeof(Counters), cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  const long long n_split = (long long)P->ctr_host->n_split;
+  long long lo = (long long)P->ctr_host->shard_lo, hi = (long long)P->ctr_host->shard_hi;
+  if (n_split == 0 || hi <= lo) lo = hi = 0;
+  P->shard_k[0] = lo;
+  P->shard_k[1] = hi;
+  long long pst[2] = {0, 0};
+  if (hi > lo) {
+    pst[0] = (long long)P->ctr_host->shard_plo;
+    pst[1] = (long long)P->ctr_host->shard_phi;
+  }
+  P->shard_p[0] = pst[0];
+  P->shard_p[1] = pst[1];
+  *counts = adps_counts{};
+  counts->n_split = n_split;
+  counts->merge_edges = (long long)P->ctr_host->merge_edges;
+  counts->n_children = (long long)P->ctr_host->n_children;
+  P->have_merge_part = true;
+  return ADPS_OK;
+}
+
+extern "C" adps_status adps_set_parent_sharding(adps_plan* P, int32_t rank, int32_t world) {
+  if (!P) return fail(ADPS_INVALID_ARG, "plan is NULL");
+  if (world < 1 || rank < 0 || rank >= world) return fail(ADPS_INVALID_ARG, "bad parent sharding");
+  P->pshard_rank = rank;
+  P->pshard_world = world;
+  return ADPS_OK;
+}
+
+extern "C" adps_status adps_get_shard(adps_plan* P, int64_t* k_lo, int64_t* k_hi, int64_t* p_lo, int64_t* p_hi) {
+  if (!P || !k_lo || !k_hi || !p_lo || !p_hi) return fail(ADPS_INVALID_ARG, "NULL argument");
+  if (!P->have_merge_part) return fail(ADPS_BAD_STATE, "no parent-sharded merge pending");
+  *k_lo = P->shard_k[0];
+  *k_hi = P->shard_k[1];
+  *p_lo = P->shard_p[0];
+  *p_hi = P->shard_p[1];
+  return ADPS_OK;
+}
+
+extern "C" adps_status adps_step_phase1_finish(adps_plan* P, void* stream_v, int64_t merge_edges, int64_t n_children,
+                                               adps_counts* counts) {
+  if (!P || !counts) return fail(ADPS_INVALID_ARG, "NULL argument");
+  if (!P->have_merge_part) return fail(ADPS_BAD_STATE, "phase1_finish without a parent-sharded merge");
+  P->have_merge_part = false;
+  CK(cudaSetDevice(P->device));
+  cudaStream_t s = (cudaStream_t)stream_v;
+  Counters* ctr = P->ctr.as<Counters>();
+  const unsigned long long me = (unsigned long long)merge_edges, nc = (unsigned long long)n_children;
+  CK(cudaMemcpyAsync(&ctr->merge_edges, &me, sizeof(me), cudaMemcpyHostToDevice, s));
+  CK(cudaMemcpyAsync(&ctr->n_children, &nc, sizeof(nc), cudaMemcpyHostToDevice, s));
+  return phase1_finish(P, s, counts);
 }
 
 extern "C" adps_status adps_step_phase2(adps_plan* P, void* stream_v, const adps_gaussians* g,
@@ -1175,6 +1269,21 @@ extern "C" adps_status adps_get_buffer(adps_plan* P, int32_t which, void** ptr, 
       *ptr = P->valid.p;
       *count = P->n_regions_cur;
       *elem_bytes = 1;
+      return ADPS_OK;
+    case ADPS_BUF_CAND_MERGED:
+      *ptr = P->cand_merged.p;
+      *count = P->ctr_host ? (int64_t)P->ctr_host->n_split : 0;
+      *elem_bytes = 4;
+      return ADPS_OK;
+    case ADPS_BUF_CAND_INS:
+      *ptr = P->cand_ins.p;
+      *count = P->ctr_host ? (int64_t)P->ctr_host->n_split : 0;
+      *elem_bytes = 4;
+      return ADPS_OK;
+    case ADPS_BUF_CHILDREN:
+      *ptr = P->children.p;
+      *count = P->n_regions_cur;
+      *elem_bytes = 14 * sizeof(float);
       return ADPS_OK;
     default:
       return fail(ADPS_INVALID_ARG, "unknown buffer %d", which);

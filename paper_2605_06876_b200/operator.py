@@ -352,8 +352,65 @@ class Plan:
                                                     _ptr(proposals) if n else None, _ptr(valid) if n else None, n))
 
     def phase1_merge(self) -> dict:
+        """Merge + cap (+ offsets unless parent-sharded: then only this rank's
+        candidates, and counts holds its merge_edges / n_children)."""
         counts = _abi.Counts()
         _abi.check(self.lib.adps_step_phase1_merge(self._h, self._stream(), C.byref(counts)))
+        return counts.as_dict()
+
+    def set_parent_sharding(self, rank: int, world: int):
+        _abi.check(self.lib.adps_set_parent_sharding(self._h, int(rank), int(world)))
+
+    def shard(self):
+        """(k_lo, k_hi, p_lo, p_hi) of this rank's parent range after a parent-sharded merge."""
+        v = [C.c_int64() for _ in range(4)]
+        _abi.check(self.lib.adps_get_shard(self._h, *[C.byref(x) for x in v]))
+        return tuple(int(x.value) for x in v)
+
+    def export_shard(self, merge_edges: int, n_children: int) -> torch.Tensor:
+        """This rank's merge results as one byte blob: header (k_lo, k_hi, p_lo, p_hi,
+        merge_edges, n_children) int64, cand_merged and cand_ins [k_lo, k_hi) int32,
+        children rows [p_lo, p_hi) (14 fp32 each)."""
+        k_lo, k_hi, p_lo, p_hi = self.shard()
+        head = torch.tensor([k_lo, k_hi, p_lo, p_hi, merge_edges, n_children], dtype=torch.int64,
+                            device=self.device).view(torch.uint8)
+        parts = [head]
+        for which, lo, hi in ((_abi.BUF_CAND_MERGED, k_lo, k_hi), (_abi.BUF_CAND_INS, k_lo, k_hi),
+                              (_abi.BUF_CHILDREN, p_lo, p_hi)):
+            ptr, _, eb = self.buffer(which)
+            t = torch.empty((hi - lo) * eb, dtype=torch.uint8, device=self.device)
+            if hi > lo:
+                _copy_device(t, ptr + lo * eb, (hi - lo) * eb, self.device)
+            parts.append(t)
+        return torch.cat(parts)
+
+    def import_shards(self, blobs) -> tuple:
+        """Write every other rank's merge results into this plan; returns the summed
+        (merge_edges, n_children)."""
+        own = self.shard()
+        me = nc = 0
+        for b in blobs:
+            head = b[:48].clone().view(torch.int64).tolist()
+            k_lo, k_hi, p_lo, p_hi, e, c = head
+            me += e
+            nc += c
+            if (k_lo, k_hi, p_lo, p_hi) == own:
+                continue
+            off = 48
+            for which, lo, hi in ((_abi.BUF_CAND_MERGED, k_lo, k_hi), (_abi.BUF_CAND_INS, k_lo, k_hi),
+                                  (_abi.BUF_CHILDREN, p_lo, p_hi)):
+                ptr, _, eb = self.buffer(which)
+                nb = (hi - lo) * eb
+                if nb:
+                    src = b[off:off + nb].contiguous()
+                    _copy_to_ptr(ptr + lo * eb, src, self.device)
+                off += nb
+        return me, nc
+
+    def phase1_finish(self, merge_edges: int, n_children: int) -> dict:
+        counts = _abi.Counts()
+        _abi.check(self.lib.adps_step_phase1_finish(self._h, self._stream(), int(merge_edges), int(n_children),
+                                                    C.byref(counts)))
         return counts.as_dict()
 
     def vanilla_phase1(self, g, extent, grad_accum, denom, cfg, n_children: int) -> dict:
@@ -428,6 +485,19 @@ class Plan:
 
 
 _cudart = None
+
+
+def _copy_to_ptr(dst_ptr: int, src: torch.Tensor, device):
+    """Device-to-device copy into a raw pointer owned by the plan."""
+    global _cudart
+    if _cudart is None:
+        from cuda.bindings import runtime as _rt
+        _cudart = _rt
+    stream = torch.cuda.current_stream(device).cuda_stream
+    err, = _cudart.cudaMemcpyAsync(dst_ptr, src.data_ptr(), src.numel() * src.element_size(),
+                                   _cudart.cudaMemcpyKind.cudaMemcpyDeviceToDevice, stream)
+    if int(err) != 0:
+        raise RuntimeError(f"cudaMemcpyAsync failed: {err}")
 
 
 def _copy_device(dst: torch.Tensor, src_ptr: int, nbytes: int, device):

@@ -16,10 +16,13 @@ SURVEY.md 8(e), following the path's own data dependencies:
   which is the reference's order (ref/adc.py:190-195), so the concatenation
   order is irrelevant and every rank sees identical inputs.
 
-  Phase B (replicated).  Merge, cap, per-candidate case, offsets and the
-  compaction run on every rank over identical inputs, so every rank ends with
-  the identical grown arrays (what the next data-parallel training step
-  needs) without a further collective.
+  Phase B (parent-sharded).  The split candidates are cut into contiguous
+  ranges balanced by their gate work (sum of P_k^2 + 1, shard_parents); each
+  rank gates, groups and caps only its range (ref/cross_view_merge.py), then
+  the per-parent results (children per parent, inserted counts) and the
+  children rows are all-gathered, and the offsets and compaction run on every
+  rank over identical inputs -- every rank ends with the identical grown
+  arrays (what the next data-parallel training step needs).
 
 The orchestration is written against a small executor interface so that the
 same code drives the CUDA plan (GpuExecutor) and, in the CPU tests, a
@@ -39,6 +42,21 @@ def shard_views(n_views: int, world: int, rank: int) -> list:
     if world < 1 or not 0 <= rank < world:
         raise ValueError("bad world/rank")
     return list(range(rank, n_views, world))
+
+
+def shard_parents(p_counts, world: int, rank: int) -> tuple:
+    """[lo, hi) of the split candidates `rank` merges: candidate k goes to rank
+    floor(W_<k * world / W), W_<k the exclusive prefix of w = P_k^2 + 1 (the
+    host statement of the device rule in merge.cu shard_range_kernel)."""
+    w = [int(p) * int(p) + 1 for p in p_counts]
+    total = sum(w)
+    lo, hi, excl = len(w), 0, 0
+    for k, wk in enumerate(w):
+        owner = min(world - 1, excl * world // total) if total else 0
+        if owner == rank:
+            lo, hi = min(lo, k), max(hi, k + 1)
+        excl += wk
+    return (lo, hi) if hi > lo else (0, 0)
 
 
 def all_gather_bytes(t: torch.Tensor, group=None) -> list:
@@ -68,7 +86,9 @@ def run_sharded(ex, n_views: int, group=None):
       start_normals(n_fallback)        start drawing the 6F fallback normals
       local() -> {name: uint8 tensor}  local region records / proposals / valid flags
       import_(dict of per-rank lists)  the gathered records
-      merge() -> counts                merge, cap, case, offsets over all records
+      merge() -> counts                merge + cap of this rank's parents (all, if not parent-sharded)
+      export_shard() -> uint8 tensor   this rank's per-parent results (parent-sharded executors)
+      import_shards(list of blobs)     every rank's results; finishes phase 1 (offsets)
       emit() -> result                 the grown Gaussians (identical on every rank)
     """
     world = dist.get_world_size(group)
@@ -83,6 +103,8 @@ def run_sharded(ex, n_views: int, group=None):
     recs = ex.local()
     ex.import_({k: all_gather_bytes(v, group) for k, v in recs.items()})
     ex.merge()
+    if getattr(ex, "parent_sharded", False):
+        ex.import_shards(all_gather_bytes(ex.export_shard(), group))
     return ex.emit()
 
 
@@ -109,6 +131,10 @@ def run_lockstep(executors: list, n_views: int):
         ex.import_(gathered)
     for ex in executors:
         ex.merge()
+    if getattr(executors[0], "parent_sharded", False):
+        blobs = [ex.export_shard() for ex in executors]
+        for ex in executors:
+            ex.import_shards(blobs)
     return [ex.emit() for ex in executors]
 
 
@@ -117,7 +143,7 @@ class GpuExecutor:
 
     def __init__(self, g: op.GaussianTensors, extent: float, cameras, gt, grad_accum, denom, cfg, rng, *,
                  renders=None, plan: op.Plan = None, view_ids=None, want_report: bool = True,
-                 world: int = 1, rank: int = 0):
+                 world: int = 1, rank: int = 0, parent_shard: bool = True):
         self.plan = plan or op.default_plan(g.device)
         self.g, self.extent, self.cfg, self.rng = g, extent, cfg, rng
         self.cams = op.camera_rows(cameras)
@@ -127,6 +153,7 @@ class GpuExecutor:
         self.ga = grad_accum.to(self.plan.device, op.F64).contiguous()
         self.den = denom.to(self.plan.device, op.F64).contiguous()
         self.want_report, self.world, self.rank = want_report, world, rank
+        self.parent_sharded = bool(parent_shard) and world > 1
         self.counts = None
         self.normals = None
 
@@ -144,6 +171,7 @@ class GpuExecutor:
         gt_v = op._gather_views(self.gt, vids, dev)
         self._keep = (image, dom, gt_v)
         P.set_view_sharding(self.rank, self.world, len(self.view_ids))
+        P.set_parent_sharding(self.rank, self.world) if self.parent_sharded else P.set_parent_sharding(0, 1)
         self.counts = P.phase1_begin(self.g, self.extent, self.ga, self.den, self.cfg, cams_v, image, gt_v, dom)
         return self.counts
 
@@ -171,11 +199,30 @@ class GpuExecutor:
 
     def merge(self):
         try:
-            self.counts = self.plan.phase1_merge()
+            part = self.plan.phase1_merge()
+            if self.parent_sharded:
+                self._part = part
+            else:
+                self.counts = part
         finally:
-            self._draw.join()
-            self.plan.set_view_sharding(0, 1, 0)
-        return self.counts
+            if not self.parent_sharded:
+                self._unshard()
+        return part
+
+    def _unshard(self):
+        self._draw.join()
+        self.plan.set_view_sharding(0, 1, 0)
+        self.plan.set_parent_sharding(0, 1)
+
+    def export_shard(self):
+        return self.plan.export_shard(self._part["merge_edges"], self._part["n_children"])
+
+    def import_shards(self, blobs):
+        try:
+            me, nc = self.plan.import_shards(blobs)
+            self.counts = self.plan.phase1_finish(me, nc)
+        finally:
+            self._unshard()
 
     def emit(self):
         normals = self._draw.result()

@@ -473,8 +473,9 @@ def test_determinism_at_scale(op, cfg_name):
     assert all(r.children_inserted <= wl.n_max for r in rep.candidates)
 
 
+@pytest.mark.parametrize("parent_shard", [True, False])
 @pytest.mark.parametrize("world", [2, 3])
-def test_sharded_lockstep_matches_single_gpu(op, world):
+def test_sharded_lockstep_matches_single_gpu(op, world, parent_shard):
     """The view-sharded C-ABI flow (phase1_begin on each rank's views, flag
     reduction, refresh, local records, import of the concatenation, merge)
     gives the single-plan result bit for bit -- all ranks run in one process
@@ -497,7 +498,8 @@ def test_sharded_lockstep_matches_single_gpu(op, world):
                              view_ids=vids)
     want = _step_digest(op, base, single)
     exs = [SH.GpuExecutor(g, ini.extent, cams, gt_img, ga_t, den_t, cfg, np.random.default_rng(5),
-                          renders=(img, dom), plan=op.Plan("cuda:0"), view_ids=vids, world=world, rank=r)
+                          renders=(img, dom), plan=op.Plan("cuda:0"), view_ids=vids, world=world, rank=r,
+                          parent_shard=parent_shard)
            for r in range(world)]
     results = SH.run_lockstep(exs, len(vids))
     assert single.counts["n_fallback"] > 0

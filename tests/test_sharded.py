@@ -40,7 +40,13 @@ def _inputs(tag):
 
 
 class OracleExecutor:
-    """run_sharded's executor interface over the oracle's per-phase functions."""
+    """run_sharded's executor interface over the oracle's per-phase functions.
+
+    Parent-sharded like the CUDA executor: after the merge each rank exports
+    the per-candidate results of ITS range (shard_parents) and the final
+    population is assembled from all ranks' exports."""
+
+    parent_sharded = True
 
     def __init__(self, g, extent, cams, gts, ga, den, cfg, rng, renders):
         self.g, self.extent, self.cams, self.gts, self.cfg, self.rng = g, extent, cams, gts, cfg, rng
@@ -79,10 +85,50 @@ class OracleExecutor:
 
     def merge(self):
         assert sorted(self.all_regions) == self.view_ids
+        self.full = O.step_finish(self.g, self.cams, self.view_ids, self.all_regions, self.dom_any, self.split,
+                                  self.clone, self.cfg, self.rng)
+        self.k_lo, self.k_hi = SH.shard_parents([c.proposals for c in self.full.candidates],
+                                                dist.get_world_size(), dist.get_rank())
+
+    @staticmethod
+    def _rows(c):
+        return 2 if c.fallback else (0 if c.reset else c.children_inserted + 1)
+
+    def export_shard(self):
+        f = self.full
+        n_keep = int((f.index_map >= 0).sum())
+        start = n_keep + sum(self._rows(c) for c in f.candidates[:self.k_lo])
+        stop = start + sum(self._rows(c) for c in f.candidates[self.k_lo:self.k_hi])
+        rows = f.gaussians.take(np.arange(start, stop))
+        edges = sum(len(gr.members) - 1 for c in f.candidates[self.k_lo:self.k_hi]
+                    for gr in f.all_groups.get(c.index, []))
+        return torch.frombuffer(bytearray(pickle.dumps(
+            (self.k_lo, self.k_hi, f.candidates[self.k_lo:self.k_hi], rows, edges))), dtype=torch.uint8)
+
+    def import_shards(self, blobs):
+        parts = sorted((pickle.loads(b.numpy().tobytes()) for b in blobs if b.numel()), key=lambda t: t[0])
+        f = self.full
+        cands, rows, edges, nxt = [], [], 0, 0
+        for k_lo, k_hi, cs, r, e in parts:
+            if k_hi <= k_lo:
+                continue
+            assert k_lo == nxt, "candidate ranges must tile the split set"
+            cands += cs
+            rows.append(r)
+            edges += e
+            nxt = k_hi
+        assert nxt == len(f.candidates)
+        keep = np.flatnonzero(f.index_map >= 0)
+        clones = [self.g.take([i]) for i in f.clones]
+        res = O.StepResult(gaussians=O.Gaussians.concat([self.g.take(f.index_map[keep])] + rows + clones),
+                           count_before=f.count_before, count_after=0, index_map=f.index_map, candidates=cands,
+                           clones=f.clones, reset_indices=f.reset_indices, sampled_views=f.sampled_views,
+                           merge_edges=edges)
+        res.count_after = len(res.gaussians)
+        self.assembled = res
 
     def emit(self):
-        return O.step_finish(self.g, self.cams, self.view_ids, self.all_regions, self.dom_any, self.split,
-                             self.clone, self.cfg, self.rng)
+        return self.assembled
 
 
 def _digest(res):
@@ -117,6 +163,19 @@ def _free_port():
     with socket.socket() as s:
         s.bind(("127.0.0.1", 0))
         return s.getsockname()[1]
+
+
+def test_shard_parents_partition():
+    rng = np.random.default_rng(0)
+    for n in (0, 1, 7, 1000):
+        p = rng.integers(0, 50, n)
+        if n:
+            p[rng.integers(0, n)] = 3000   # one heavy parent
+        for world in (1, 2, 3, 8):
+            ranges = [SH.shard_parents(p, world, r) for r in range(world)]
+            nonempty = [r for r in ranges if r[1] > r[0]]
+            assert sum(hi - lo for lo, hi in nonempty) == n
+            assert all(a[1] == b[0] for a, b in zip(nonempty, nonempty[1:]))
 
 
 def test_shard_views_partition():
