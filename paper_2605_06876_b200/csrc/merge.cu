@@ -431,20 +431,42 @@ __device__ __forceinline__ void decode_tile_pair(const MergeArgs& a, long long n
   bj = bi + (q - (bi * T - bi * (bi - 1) / 2));
 }
 
-// one thread per (parent, tile row, tile column) of the upper-triangular
-// tile matrix: keep the pairs the bounding data cannot exclude
+// one warp per (parent, tile row bi) of the upper-triangular tile matrix:
+// keep the pairs (bi, bj >= bi) the bounding data cannot exclude; a row's
+// survivors are stored contiguously in bj order (one reservation per row), so
+// the gate kernel can keep tile bi resident across them
 __global__ void tile_pair_filter_kernel(MergeArgs a) {
+  const int lane = threadIdx.x & 31;
+  const long long warps = (long long)gridDim.x * (blockDim.x >> 5);
   const long long n_large = (long long)a.ctr->n_large;
-  const unsigned long long W = n_large > 0 ? a.work_off[n_large] : 0;
-  for (unsigned long long w = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; w < W;
-       w += (unsigned long long)gridDim.x * blockDim.x) {
-    long long l, bi, bj;
-    decode_tile_pair(a, n_large, w, l, bi, bj);
+  const long long rows = n_large > 0 ? (long long)a.tile_off[n_large] : 0;
+  for (long long r = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); r < rows; r += warps) {
+    const long long l = find_owner(a.tile_off, n_large, (unsigned long long)r);
     const long long tb = (long long)a.tile_off[l];
-    if (!boxes_may_merge(a.boxes[tb + bi], a.boxes[tb + bj], a.gamma_d, a.gamma_c)) continue;
-    const unsigned long long s = atomicAdd(&a.ctr->n_tile_pairs, 1ull);
-    if ((long long)s < a.tile_pairs_cap) a.tile_pairs[s] = make_int4((int)l, (int)bi, (int)bj, 0);
-    else atomicOr(&a.ctr->overflow, 4u);
+    const long long bi = r - tb;
+    const long long T = (long long)a.tile_cnt[l];
+    const TileBox A = a.boxes[tb + bi];
+    int cnt = 0;
+    for (long long j0 = bi; j0 < T; j0 += 32) {
+      const long long bj = j0 + lane;
+      const bool keep = bj < T && boxes_may_merge(A, a.boxes[tb + bj], a.gamma_d, a.gamma_c);
+      cnt += __popc(__ballot_sync(0xffffffffu, keep));
+    }
+    if (cnt == 0) continue;
+    unsigned long long base = 0;
+    if (lane == 0) base = atomicAdd(&a.ctr->n_tile_pairs, (unsigned long long)cnt);
+    base = __shfl_sync(0xffffffffu, base, 0);
+    if ((long long)(base + cnt) > a.tile_pairs_cap) {
+      if (lane == 0) atomicOr(&a.ctr->overflow, 4u);
+      continue;
+    }
+    for (long long j0 = bi; j0 < T; j0 += 32) {
+      const long long bj = j0 + lane;
+      const bool keep = bj < T && boxes_may_merge(A, a.boxes[tb + bj], a.gamma_d, a.gamma_c);
+      const unsigned m = __ballot_sync(0xffffffffu, keep);
+      if (keep) a.tile_pairs[base + __popc(m & ((1u << lane) - 1u))] = make_int4((int)l, (int)bi, (int)bj, 0);
+      base += __popc(m);
+    }
   }
 }
 
@@ -468,9 +490,9 @@ __device__ __forceinline__ bool gate_soa(const double* A, const double (*Bs)[kMT
   return d <= gd;
 }
 
-struct PairBuf {
-  double s[2][kG_fields][kMT];   // [tile i / tile j][field][proposal]
-  int q[2][kMT];
+struct SideBuf {
+  double s[kG_fields][kMT];   // [field][proposal]
+  int q[kMT];
 };
 
 __device__ __forceinline__ void cp_async(void* dst, const void* src, int bytes) {
@@ -482,51 +504,49 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
-// stage the gate operands of tile pair (l, bi, bj) into B (asynchronous copies)
-__device__ __forceinline__ void stage_pair(const MergeArgs& a, PairBuf& B, long long l, long long bi, long long bj) {
+// stage the gate operands of tile bt of large parent l into B (asynchronous copies)
+__device__ __forceinline__ void stage_tile(const MergeArgs& a, SideBuf& B, long long l, long long bt) {
   const long long P = (long long)a.lp_cnt[l];
-  const long long base = (long long)a.lp_off[l];
-  const int i0 = (int)(bi * kMT), j0 = (int)(bj * kMT);
-  const int ni = (int)min((long long)kMT, P - i0), nj = (int)min((long long)kMT, P - j0);
-  for (int t = threadIdx.x; t < 2 * kG_fields * kMT; t += blockDim.x) {
-    const int half = t / (kG_fields * kMT), r = t % (kG_fields * kMT);
-    const int f = r / kMT, loc = r % kMT;
-    if (loc < (half ? nj : ni))
-      cp_async(&B.s[half][f][loc], a.gsoa + (long long)f * a.soa_cap + base + (half ? j0 : i0) + loc, 8);
+  const long long base = (long long)a.lp_off[l] + bt * kMT;
+  const int nt = (int)min((long long)kMT, P - bt * kMT);
+  for (int t = threadIdx.x; t < kG_fields * kMT; t += blockDim.x) {
+    const int f = t / kMT, loc = t % kMT;
+    if (loc < nt) cp_async(&B.s[f][loc], a.gsoa + (long long)f * a.soa_cap + base + loc, 8);
   }
-  for (int t = threadIdx.x; t < 2 * kMT; t += blockDim.x) {
-    const int half = t / kMT, loc = t % kMT;
-    if (loc < (half ? nj : ni)) cp_async(&B.q[half][loc], a.mval_sorted + base + (half ? j0 : i0) + loc, 4);
-  }
+  for (int t = threadIdx.x; t < kMT; t += blockDim.x)
+    if (t < nt) cp_async(&B.q[t], a.mval_sorted + base + t, 4);
   cp_async_commit();
 }
 
-__device__ __forceinline__ void gates_pair(const MergeArgs& a, const PairBuf& B, long long l, long long bi,
-                                           long long bj) {
+__device__ __forceinline__ void gates_pair(const MergeArgs& a, const SideBuf& I, const SideBuf& J, long long l,
+                                           long long bi, long long bj) {
   const long long P = (long long)a.lp_cnt[l];
   const int ni = (int)min((long long)kMT, P - bi * kMT), nj = (int)min((long long)kMT, P - bj * kMT);
+  // lanes take different columns jj of one row ii: the unions of a warp then hit
+  // different roots (lanes sharing a column would contend on one atomic)
   for (int t = threadIdx.x; t < kMT * kMT; t += blockDim.x) {
     const int ii = t / kMT, jj = t % kMT;
     // unordered pairs: within a diagonal tile take ii < jj once
     if (ii < ni && jj < nj && (bi != bj || ii < jj)) {
       double A[kG_fields];
 #pragma unroll
-      for (int f = 0; f < kG_fields; ++f) A[f] = B.s[0][f][ii];
-      const bool ok = gate_soa(A, B.s[1], jj, a.gamma_d, a.gamma_c);
+      for (int f = 0; f < kG_fields; ++f) A[f] = I.s[f][ii];
+      const bool ok = gate_soa(A, J.s, jj, a.gamma_d, a.gamma_c);
 #if ADPS_MERGE_STATS
       atomicAdd(&a.ctr->stat_gates, 1ull);
       if (ok) atomicAdd(&a.ctr->stat_pass, 1ull);
 #endif
-      if (ok) uf_unite(a.uf, B.q[0][ii], B.q[1][jj]);
+      if (ok) uf_unite(a.uf, I.q[ii], J.q[jj]);
     }
   }
 }
 
-// one CTA per surviving kMT x kMT tile pair of a large parent's gate matrix,
-// the next pair's operands staged by cp.async while this pair is gated (or, if
-// the survivor list overflowed, every tile pair with the box test inline)
+// the surviving kMT x kMT tile pairs of the large parents' gate matrices, in
+// contiguous chunks per CTA: pairs of one tile row are adjacent, so tile bi
+// stays resident and only tile bj is staged (cp.async, one pair ahead); if the
+// survivor list overflowed, every tile pair with the box test inline
 __global__ void __launch_bounds__(256) pair_tiles_kernel(MergeArgs a) {
-  __shared__ PairBuf buf[2];
+  __shared__ SideBuf bi_buf, bj_buf[2];
   const bool overflow = (a.ctr->overflow & 4u) != 0;
   const long long n_large = (long long)a.ctr->n_large;
   if (overflow) {
@@ -536,39 +556,47 @@ __global__ void __launch_bounds__(256) pair_tiles_kernel(MergeArgs a) {
       decode_tile_pair(a, n_large, w, l, bi, bj);
       const long long tb = (long long)a.tile_off[l];
       if (!boxes_may_merge(a.boxes[tb + bi], a.boxes[tb + bj], a.gamma_d, a.gamma_c)) continue;   // uniform
-      stage_pair(a, buf[0], l, bi, bj);
+      stage_tile(a, bi_buf, l, bi);
+      stage_tile(a, bj_buf[0], l, bj);
       cp_async_wait<0>();
       __syncthreads();
-      gates_pair(a, buf[0], l, bi, bj);
+      gates_pair(a, bi_buf, bj_buf[0], l, bi, bj);
       __syncthreads();
     }
     return;
   }
-  const unsigned long long W = a.ctr->n_tile_pairs;
-  unsigned long long w = blockIdx.x;
-  if (w >= W) return;
-  int4 cur = a.tile_pairs[w];
-  stage_pair(a, buf[0], cur.x, cur.y, cur.z);
-  for (int it = 0; w < W; ++it, w += gridDim.x) {
-    const unsigned long long nw = w + gridDim.x;
+  const long long W = (long long)a.ctr->n_tile_pairs;
+  const long long chunk = (W + gridDim.x - 1) / gridDim.x;
+  const long long w0 = (long long)blockIdx.x * chunk, w1 = min(W, w0 + chunk);
+  if (w0 >= w1) return;
+  long long cur_l = -1, cur_bi = -1;
+  int4 cur = a.tile_pairs[w0];
+  stage_tile(a, bj_buf[0], cur.x, cur.z);
+  for (long long w = w0; w < w1; ++w) {
+    const int it = (int)(w - w0);
+    if (cur.x != cur_l || cur.y != cur_bi) {   // new tile row: stage tile bi (rare)
+      stage_tile(a, bi_buf, cur.x, cur.y);
+      cur_l = cur.x;
+      cur_bi = cur.y;
+    }
     int4 nxt = cur;
-    if (nw < W) {
-      nxt = a.tile_pairs[nw];
-      stage_pair(a, buf[(it + 1) & 1], nxt.x, nxt.y, nxt.z);
+    if (w + 1 < w1) {
+      nxt = a.tile_pairs[w + 1];
+      stage_tile(a, bj_buf[(it + 1) & 1], nxt.x, nxt.z);
       cp_async_wait<1>();
     } else {
       cp_async_wait<0>();
     }
     __syncthreads();
-    gates_pair(a, buf[it & 1], cur.x, cur.y, cur.z);
-    __syncthreads();   // buf[it & 1] is restaged two iterations on
+    gates_pair(a, bi_buf, bj_buf[it & 1], cur.x, cur.y, cur.z);
+    __syncthreads();   // both buffers are restaged from the next iteration on
     cur = nxt;
   }
 }
 
 cudaError_t launch_merge_tile_gates(const MergeArgs& a, cudaStream_t s) {
   box_kernel<<<a.grid, 256, 0, s>>>(a);
-  tile_pair_filter_kernel<<<a.grid, 256, 0, s>>>(a);
+  tile_pair_filter_kernel<<<a.grid, 256, 0, s>>>(a);   // warp per tile row
   pair_tiles_kernel<<<a.grid, 256, 0, s>>>(a);
   return cudaGetLastError();
 }
