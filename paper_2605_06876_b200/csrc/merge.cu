@@ -285,6 +285,18 @@ cudaError_t launch_shard_range(const int* nvalid, long long n, int rank, int wor
   return cudaGetLastError();
 }
 
+cudaError_t launch_small_pairs(const MergeArgs& a, cudaStream_t s) {
+  small_pairs_kernel<<<a.grid, 256, 0, s>>>(a);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_large_offsets(const MergeArgs& a, cudaStream_t s) {
+  offsets_1block_kernel<<<1, 1024, 0, s>>>(a.work_cnt, a.work_off, &a.ctr->n_large);
+  offsets_1block_kernel<<<1, 1024, 0, s>>>(a.lp_cnt, a.lp_off, &a.ctr->n_large);
+  offsets_1block_kernel<<<1, 1024, 0, s>>>(a.tile_cnt, a.tile_off, &a.ctr->n_large);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_merge_small_gates(const MergeArgs& a, cudaStream_t s) {
   small_pairs_kernel<<<a.grid, 256, 0, s>>>(a);
   offsets_1block_kernel<<<1, 1024, 0, s>>>(a.work_cnt, a.work_off, &a.ctr->n_large);

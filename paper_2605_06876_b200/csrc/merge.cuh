@@ -96,6 +96,9 @@ cudaError_t launch_shard_range(const int* nvalid, long long n, int rank, int wor
 
 cudaError_t launch_merge_prepare(const MergeArgs& a, long long n_split, ScanState st, cudaStream_t s);
 cudaError_t launch_merge_small_gates(const MergeArgs& a, cudaStream_t s);
+// the same split in two: gates of the small parents / offsets of the large ones
+cudaError_t launch_small_pairs(const MergeArgs& a, cudaStream_t s);
+cudaError_t launch_large_offsets(const MergeArgs& a, cudaStream_t s);
 cudaError_t launch_merge_morton(const MergeArgs& a, long long cap, cudaStream_t s);
 cudaError_t launch_merge_tile_gates(const MergeArgs& a, cudaStream_t s);
 cudaError_t launch_merge_flatten(const MergeArgs& a, long long cap, cudaStream_t s);

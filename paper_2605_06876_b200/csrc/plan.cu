@@ -122,6 +122,10 @@ struct adps_plan {
   long long launches = 0;
   long long lib_calls = 0;
   int large_threshold = 32;
+  // second stream: small-parent gates and the survivor scan overlap the merge
+  cudaStream_t aux = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_small = nullptr, ev_keep = nullptr;
+  bool keep_pending = false;
   int fb_children = 2;   // children per fallback parent of the last phase 1
   // view sharding: this plan's local view v is global view position view_offset + v * view_stride
   // of v_global_cfg sampled views (0 = the local views are all of them)
@@ -215,6 +219,10 @@ extern "C" adps_status adps_plan_create(adps_plan** plan, int32_t device, int64_
     return fail(ADPS_OOM, "pinned allocation failed: %s", cudaGetErrorString(e));
   }
   for (int i = 0; i < kMaxMarks; ++i) cudaEventCreate(&P->ev[i]);
+  cudaStreamCreateWithFlags(&P->aux, cudaStreamNonBlocking);
+  cudaEventCreateWithFlags(&P->ev_fork, cudaEventDisableTiming);
+  cudaEventCreateWithFlags(&P->ev_small, cudaEventDisableTiming);
+  cudaEventCreateWithFlags(&P->ev_keep, cudaEventDisableTiming);
   (void)max_n;
   (void)max_views;
   (void)height;
@@ -253,6 +261,10 @@ extern "C" adps_status adps_plan_destroy(adps_plan* P) {
   if (P->r_total_host) cudaFreeHost(P->r_total_host);
   for (int i = 0; i < kMaxMarks; ++i)
     if (P->ev[i]) cudaEventDestroy(P->ev[i]);
+  if (P->ev_fork) cudaEventDestroy(P->ev_fork);
+  if (P->ev_small) cudaEventDestroy(P->ev_small);
+  if (P->ev_keep) cudaEventDestroy(P->ev_keep);
+  if (P->aux) cudaStreamDestroy(P->aux);
   delete P;
   return ADPS_OK;
 }
@@ -904,8 +916,30 @@ static adps_status phase1_merge_part(adps_plan* P, cudaStream_t s) {
     if (st != ADPS_OK) return st;
     CK(launch_merge_prepare(ma, n_split, sst3, s));
     mark(P, "merge_prepare", s, 2);
-    CK(launch_merge_small_gates(ma, s));
-    mark(P, "merge_small_gates", s, 4);
+    // fork: the small parents' gates and the survivor scan (it only needs the
+    // cases) run on the second stream while the large parents are gated
+    CK(cudaEventRecord(P->ev_fork, s));
+    CK(cudaStreamWaitEvent(P->aux, P->ev_fork, 0));
+    CK(launch_small_pairs(ma, P->aux));
+    CK(cudaEventRecord(P->ev_small, P->aux));
+    {
+      OffsetArgs ka;
+      ka.n = n;
+      ka.cls = P->cls.as<unsigned char>();
+      ka.cand_rank = P->cand_rank.as<int>();
+      ka.cand_case = P->cand_case.as<int>();
+      ka.cand_ins = P->cand_ins.as<int>();
+      ka.ins_off = P->ins_off.as<int>();
+      ka.fb_ord = P->fb_ord.as<int>();
+      ka.keep_pos = P->keep_pos.as<int>();
+      ka.ctr = ctr;
+      ka.n_split_dev = &ctr->n_split;
+      CK(launch_offsets_keep(ka, sst, P->aux));
+      CK(cudaEventRecord(P->ev_keep, P->aux));
+      P->keep_pending = true;
+    }
+    CK(launch_large_offsets(ma, s));
+    mark(P, "merge_small_gates", s, 5);
     if (n_regions > 0) {
       CK(launch_merge_morton(ma, rc, s));
       const int mbits = 32 + ceil_log2((unsigned long long)n_split + 2);
@@ -913,6 +947,7 @@ static adps_status phase1_merge_part(adps_plan* P, cudaStream_t s) {
       CK(launch_merge_tile_gates(ma, s));
       mark(P, "merge_tile_gates", s, 3);
     }
+    CK(cudaStreamWaitEvent(s, P->ev_small, 0));   // join: all unions are in before the groups
     if (n_regions > 0) {
       CK(launch_merge_flatten(ma, rc, s));
       const int gbits = ceil_log2((unsigned long long)rc + 2);
@@ -959,7 +994,13 @@ static adps_status phase1_finish(adps_plan* P, cudaStream_t s, adps_counts* coun
   oa.keep_pos = P->keep_pos.as<int>();
   oa.ctr = ctr;
   oa.n_split_dev = &ctr->n_split;
-  CK(launch_offsets(oa, n_split, sst2, sst, s));
+  CK(launch_offsets_cand(oa, n_split, sst2, s));
+  if (P->keep_pending) {   // join the survivor scan started with the merge
+    CK(cudaStreamWaitEvent(s, P->ev_keep, 0));
+    P->keep_pending = false;
+  } else {
+    CK(launch_offsets_keep(oa, sst, s));
+  }
   mark(P, "offsets", s, 2);
   CK(cudaMemcpyAsync(P->ctr_host, ctr, sizeof(Counters), cudaMemcpyDeviceToHost, s));
   CK(cudaStreamSynchronize(s));

@@ -242,501 +242,7 @@ cudaError_t launch_ranges(const RangeArgs& a, cudaStream_t s) {
   return cudaGetLastError();
 }
 
-// ============================================================ merge (see merge.cu)
-#if 0
-// A "team" is one warp (small candidates) or one CTA (large candidates).
-template <int TEAM>
-__device__ __forceinline__ void team_sync() {
-  if (TEAM == 32) __syncwarp();
-  else __syncthreads();
-}
-
-__device__ __forceinline__ bool gate(const Proposal& A, const Proposal& B, double gd, double gc) {
-  // ref/cross_view_merge.py:33-41 (both thresholds inclusive)
-  const double dl[3] = {B.mu[0] - A.mu[0], B.mu[1] - A.mu[1], B.mu[2] - A.mu[2]};
-  const double d = sqrt(fmax(sym_quad(A.prec, dl), 0.0)) + sqrt(fmax(sym_quad(B.prec, dl), 0.0));
-  const double dc = fmax(fmax(fabs(A.rgb[0] - B.rgb[0]), fabs(A.rgb[1] - B.rgb[1])), fabs(A.rgb[2] - B.rgb[2]));
-  return d <= gd && dc <= gc;
-}
-
-// group -> Gaussian (ref/adc.py:127-140): eigh(merged_cov) ascending, det fix on
-// column 0, scale = sqrt(max(lambda, 1e-16)), opacity = clamped parent opacity,
-// sh_dc = rgb_to_dc(merged_rgb).  out: 14 floats mu3 scale3 rot4 o sh_dc3.
-__device__ void write_child(const GroupRec& G, float ocl, float* out) {
-  int o[3] = {0, 1, 2};
-  for (int i = 0; i < 3; ++i)
-    for (int j = i + 1; j < 3; ++j)
-      if (G.lam[o[j]] < G.lam[o[i]]) {
-        int t = o[i];
-        o[i] = o[j];
-        o[j] = t;
-      }
-  double ev[9], lam[3];
-  for (int c = 0; c < 3; ++c) {
-    lam[c] = G.lam[o[c]];
-    for (int r = 0; r < 3; ++r) ev[r * 3 + c] = G.evec[r * 3 + o[c]];
-  }
-  const double det = ev[0] * (ev[4] * ev[8] - ev[5] * ev[7]) - ev[1] * (ev[3] * ev[8] - ev[5] * ev[6]) +
-                     ev[2] * (ev[3] * ev[7] - ev[4] * ev[6]);
-  if (det < 0)
-    for (int r = 0; r < 3; ++r) ev[r * 3 + 0] = -ev[r * 3 + 0];
-  double qq[4];
-  rot_to_quat(ev, qq);
-  for (int t = 0; t < 3; ++t) out[t] = (float)G.mu[t];
-  for (int t = 0; t < 3; ++t) out[3 + t] = (float)sqrt(fmax(lam[t], 1e-16));
-  for (int t = 0; t < 4; ++t) out[6 + t] = (float)qq[t];
-  out[10] = ocl;
-  for (int t = 0; t < 3; ++t) out[11 + t] = (float)((G.rgb[t] - 0.5) / kShC0);
-}
-
-template <int TEAM>
-__device__ void merge_candidate(const MergeArgs& a, int k, int rank_in_team, int P, int start,
-                                int* s_red) {
-  int* idx = a.idx + start;
-  int* uf = a.uf + start;
-  const int gi = a.split_list[k];
-  // 2. union-find over mergeable pairs (i < j)
-  for (int j = rank_in_team; j < P; j += TEAM) uf[j] = j;
-  team_sync<TEAM>();
-  for (int i = 0; i < P - 1; ++i) {
-    const Proposal& A = a.props[idx[i]];
-    for (int j = i + 1 + rank_in_team; j < P; j += TEAM)
-      if (gate(A, a.props[idx[j]], a.gamma_d, a.gamma_c)) uf_unite(uf, i, j);
-  }
-  team_sync<TEAM>();
-  __threadfence_block();
-  for (int j = rank_in_team; j < P; j += TEAM) uf[j] = uf_find(uf, j);
-  team_sync<TEAM>();
-  // 3. group parameters at each root (ref/cross_view_merge.py:44-69)
-  int my_groups = 0;
-  for (int g = rank_in_team; g < P; g += TEAM) {
-    if (uf[g] != g) continue;
-    ++my_groups;
-    double smu[3] = {0, 0, 0}, srgb[3] = {0, 0, 0}, scov[6] = {0, 0, 0, 0, 0, 0};
-    int cnt = 0;
-    for (int j = g; j < P; ++j) {
-      if (uf[j] != g) continue;
-      const Proposal& M = a.props[idx[j]];
-      for (int t = 0; t < 3; ++t) {
-        smu[t] += M.mu[t];
-        srgb[t] += M.rgb[t];
-      }
-      for (int t = 0; t < 6; ++t) scov[t] += M.cov[t];
-      ++cnt;
-    }
-    GroupRec G;
-    for (int t = 0; t < 3; ++t) {
-      G.mu[t] = smu[t] / cnt;
-      G.rgb[t] = srgb[t] / cnt;
-    }
-    double mcov[6];
-    for (int t = 0; t < 6; ++t) mcov[t] = scov[t] / cnt;
-    double lam0[3];
-    sym_eig3(mcov, lam0, G.evec);
-    double ext = 0.0;
-    for (int r = 0; r < 3; ++r) {
-      const double e[3] = {G.evec[0 * 3 + r], G.evec[1 * 3 + r], G.evec[2 * 3 + r]};
-      double best = 0.0;
-      for (int j = g; j < P; ++j) {
-        if (uf[j] != g) continue;
-        const Proposal& M = a.props[idx[j]];
-        const double off = fabs((M.mu[0] - G.mu[0]) * e[0] + (M.mu[1] - G.mu[1]) * e[1] +
-                                (M.mu[2] - G.mu[2]) * e[2]);
-        const double reach = off + sqrt(sym_quad(M.cov, e));
-        best = fmax(best, reach);
-      }
-      G.lam[r] = best * best;
-      ext = fmax(ext, G.lam[r]);
-    }
-    G.extent = ext;
-    a.groups[start + g] = G;
-  }
-  // team reduce of group count
-  for (int o = 16; o > 0; o >>= 1) my_groups += __shfl_xor_sync(0xffffffffu, my_groups, o);
-  if (TEAM > 32) {
-    if ((threadIdx.x & 31) == 0) s_red[threadIdx.x >> 5] = my_groups;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      int t = 0;
-      for (int w = 0; w < TEAM / 32; ++w) t += s_red[w];
-      s_red[TEAM / 32] = t;
-    }
-    __syncthreads();
-    my_groups = s_red[TEAM / 32];
-  }
-  const int G_count = my_groups;
-  __threadfence_block();
-  team_sync<TEAM>();
-  // 4. cap: stable order by descending extent (ref/cross_view_merge.py:110-116)
-  const int n_i = G_count < a.n_max ? G_count : a.n_max;
-  const double po = a.opacity[gi];
-  const float ocl = (float)fmin(fmax(po, 1e-6), 1.0 - 1e-6);
-  for (int g = rank_in_team; g < P; g += TEAM) {
-    if (uf[g] != g) continue;
-    const double eg = a.groups[start + g].extent;
-    int rk = 0;
-    for (int h = 0; h < P; ++h) {
-      if (uf[h] != h || h == g) continue;
-      const double eh = a.groups[start + h].extent;
-      rk += (eh > eg) || (eh == eg && h < g);
-    }
-    if (rk >= a.n_max) continue;
-    write_child(a.groups[start + g], ocl, a.children + 14ll * (start + rk));
-  }
-  if (rank_in_team == 0) {
-    a.cand_case[k] = ADPS_CASE_SPLIT;
-    a.cand_merged[k] = n_i;
-    a.cand_ins[k] = n_i + 1;
-    atomicAdd(&a.ctr->merge_edges, (unsigned long long)(P - G_count));
-    atomicAdd(&a.ctr->n_children, (unsigned long long)n_i);
-  }
-}
-
-// Build idx[] (valid proposals in sorted order) with the first warp of a team.
-template <int TEAM>
-__device__ void collect_valid(const MergeArgs& a, int k, int start, int lane, int warp_in_team) {
-  if (warp_in_team != 0) return;
-  // the candidate's regions occupy sorted positions [cand_start, cand_end)
-  const int n_reg = a.cand_end[k] - start;
-  int out = 0;
-  for (int base = 0; base < n_reg; base += 32) {
-    int j = base + lane;
-    int rid = j < n_reg ? a.vals_sorted[start + j] : -1;
-    bool v = rid >= 0 && a.valid[rid];
-    unsigned bal = __ballot_sync(0xffffffffu, v);
-    if (v) a.idx[start + out + __popc(bal & ((1u << lane) - 1u))] = rid;
-    out += __popc(bal);
-  }
-}
-
-__global__ void merge_small_kernel(MergeArgs a) {
-  const int lane = threadIdx.x & 31;
-  const long long warps = (long long)gridDim.x * (blockDim.x >> 5);
-  const long long n_split = (long long)a.ctr->n_split;
-  for (long long k = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); k < n_split; k += warps) {
-    const int gi = a.split_list[k];
-    const int P = a.cand_nvalid[k];
-    if (!a.dom_flag[gi]) {   // never dominant in the sampled views -> vanilla fallback
-      if (lane == 0) {
-        a.cand_case[k] = ADPS_CASE_FALLBACK;
-        a.cand_merged[k] = 0;
-        a.cand_ins[k] = 2;
-        a.cand_props[k] = P;
-        atomicAdd(&a.ctr->n_fallback, 1ull);
-      }
-      continue;
-    }
-    if (P == 0) {            // dominant but no usable proposal -> reset
-      if (lane == 0) {
-        a.cand_case[k] = ADPS_CASE_RESET;
-        a.cand_merged[k] = 0;
-        a.cand_ins[k] = 0;
-        a.cand_props[k] = 0;
-        atomicAdd(&a.ctr->n_reset, 1ull);
-      }
-      continue;
-    }
-    if (P > a.large_threshold) {
-      if (lane == 0) {
-        unsigned long long s = atomicAdd(&a.ctr->n_large, 1ull);
-        a.large_list[s] = (int)k;
-      }
-      continue;
-    }
-    const int start = a.cand_start[k];
-    collect_valid<32>(a, k, start, lane, 0);
-    __syncwarp();
-    merge_candidate<32>(a, (int)k, lane, P, start, nullptr);
-    if (lane == 0) a.cand_props[k] = P;
-  }
-}
-
-// ------------------------------------------------------------------------
-// Large candidates (P > large_threshold proposals): the O(P^2) gate matrix is
-// spread over the whole GPU in 64x64 tiles, groups are formed by a stable sort
-// on (candidate, root) and reduced one warp per group, and the cap is a
-// block-wide top-n_max selection.  Same results as the warp path.
-// ------------------------------------------------------------------------
-constexpr int kPairTile = 64;
-
-__global__ void __launch_bounds__(256) large_collect_kernel(MergeArgs a, LargeArgs L) {
-  const long long n_large = (long long)a.ctr->n_large;
-  for (long long l = blockIdx.x; l < n_large; l += gridDim.x) {
-    const int k = a.large_list[l];
-    const int P = a.cand_nvalid[k];
-    const int start = a.cand_start[k];
-    collect_valid<256>(a, k, start, threadIdx.x & 31, threadIdx.x >> 5);
-    for (int j = threadIdx.x; j < P; j += blockDim.x) {
-      a.uf[start + j] = j;
-      L.rank_of[start + j] = -1;
-    }
-    if (threadIdx.x == 0) {
-      const long long T = (P + kPairTile - 1) / kPairTile;
-      L.work_cnt[l] = (unsigned long long)(T * (T + 1) / 2);
-      L.n_groups[l] = 0;
-      a.cand_props[k] = P;
-    }
-  }
-}
-
-// exclusive scan of work_cnt[0..n) -> work_off[0..n], one block (n is small)
-__global__ void __launch_bounds__(1024) small_scan_kernel(const unsigned long long* __restrict__ in,
-                                                          unsigned long long* __restrict__ out,
-                                                          const unsigned long long* __restrict__ n_dev) {
-  __shared__ unsigned long long warp_tot[32];
-  __shared__ unsigned long long carry;
-  const long long n = (long long)*n_dev;
-  if (threadIdx.x == 0) carry = 0;
-  __syncthreads();
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  for (long long base = 0; base < n; base += blockDim.x) {
-    const long long i = base + threadIdx.x;
-    const unsigned long long v = i < n ? in[i] : 0ull;
-    unsigned long long x = v;
-    for (int o = 1; o < 32; o <<= 1) {
-      unsigned long long y = __shfl_up_sync(0xffffffffu, x, o);
-      if (lane >= o) x += y;
-    }
-    if (lane == 31) warp_tot[wid] = x;
-    __syncthreads();
-    if (wid == 0) {
-      unsigned long long w = warp_tot[lane];
-      unsigned long long wi = w;
-      for (int o = 1; o < 32; o <<= 1) {
-        unsigned long long y = __shfl_up_sync(0xffffffffu, wi, o);
-        if (lane >= o) wi += y;
-      }
-      warp_tot[lane] = wi - w;
-    }
-    __syncthreads();
-    const unsigned long long excl = carry + warp_tot[wid] + x - v;
-    if (i < n) out[i] = excl;
-    __syncthreads();
-    if (threadIdx.x == blockDim.x - 1) carry = excl + v;
-    __syncthreads();
-  }
-  if (threadIdx.x == 0) out[n] = carry;
-}
-
-__global__ void __launch_bounds__(256) pair_tile_kernel(MergeArgs a, LargeArgs L) {
-  __shared__ Proposal si[kPairTile], sj[kPairTile];
-  const long long n_large = (long long)a.ctr->n_large;
-  const unsigned long long W = L.work_off[n_large];
-  for (unsigned long long w = blockIdx.x; w < W; w += gridDim.x) {
-    // candidate owning work item w: last l with work_off[l] <= w
-    long long lo = 0, hi = n_large - 1;
-    while (lo < hi) {
-      long long mid = (lo + hi + 1) / 2;
-      if (L.work_off[mid] <= w) lo = mid;
-      else hi = mid - 1;
-    }
-    const int k = a.large_list[lo];
-    const int P = a.cand_nvalid[k];
-    const int start = a.cand_start[k];
-    const long long T = (P + kPairTile - 1) / kPairTile;
-    const long long q = (long long)(w - L.work_off[lo]);
-    // row-major upper triangle incl. diagonal: row bi holds T - bi tiles
-    long long bi = (long long)floor(((2.0 * T + 1.0) - sqrt((2.0 * T + 1.0) * (2.0 * T + 1.0) - 8.0 * q)) / 2.0);
-    if (bi < 0) bi = 0;
-    while (bi > 0 && bi * T - bi * (bi - 1) / 2 > q) --bi;
-    while ((bi + 1) * T - (bi + 1) * bi / 2 <= q) ++bi;
-    const long long bj = bi + (q - (bi * T - bi * (bi - 1) / 2));
-    const int i0 = (int)(bi * kPairTile), j0 = (int)(bj * kPairTile);
-    for (int t = threadIdx.x; t < 2 * kPairTile; t += blockDim.x) {
-      const int loc = t % kPairTile;
-      const int src = (t < kPairTile ? i0 : j0) + loc;
-      if (src < P) (t < kPairTile ? si : sj)[loc] = a.props[a.idx[start + src]];
-    }
-    __syncthreads();
-    for (int t = threadIdx.x; t < kPairTile * kPairTile; t += blockDim.x) {
-      const int ii = t / kPairTile, jj = t % kPairTile;
-      const int i = i0 + ii, j = j0 + jj;
-      if (i < j && j < P && gate(si[ii], sj[jj], a.gamma_d, a.gamma_c)) uf_unite(a.uf + start, i, j);
-    }
-    __syncthreads();
-  }
-}
-
-__global__ void large_flatten_kernel(MergeArgs a, LargeArgs L) {
-  const long long n_large = (long long)a.ctr->n_large;
-  for (long long l = blockIdx.x; l < n_large; l += gridDim.x) {
-    const int k = a.large_list[l];
-    const int P = a.cand_nvalid[k];
-    const int start = a.cand_start[k];
-    int* uf = a.uf + start;
-    int groups = 0;
-    for (int j = threadIdx.x; j < P; j += blockDim.x) {
-      const int r = uf_find(uf, j);
-      L.keys[start + j] = ((unsigned long long)l << 32) | (unsigned long long)r;
-      L.vals[start + j] = j;
-      groups += r == j;
-    }
-    for (int o = 16; o > 0; o >>= 1) groups += __shfl_xor_sync(0xffffffffu, groups, o);
-    if ((threadIdx.x & 31) == 0) atomicAdd(&L.n_groups[l], groups);
-  }
-}
-
-// compress after all finds completed (separate launch: no reader races a writer)
-__global__ void large_compress_kernel(MergeArgs a, LargeArgs L) {
-  const long long n_large = (long long)a.ctr->n_large;
-  for (long long l = blockIdx.x; l < n_large; l += gridDim.x) {
-    const int k = a.large_list[l];
-    const int P = a.cand_nvalid[k];
-    const int start = a.cand_start[k];
-    for (int j = threadIdx.x; j < P; j += blockDim.x) a.uf[start + j] = (int)(L.keys[start + j] & 0xffffffffull);
-  }
-}
-
-// segment begin/end per (candidate, root) in the sorted key array
-__global__ void large_segments_kernel(MergeArgs a, LargeArgs L, long long n) {
-  for (long long p = (long long)blockIdx.x * blockDim.x + threadIdx.x; p < n;
-       p += (long long)gridDim.x * blockDim.x) {
-    const unsigned long long key = L.keys_sorted[p];
-    if (key == ~0ull) continue;
-    const int l = (int)(key >> 32), r = (int)(key & 0xffffffffull);
-    const int start = a.cand_start[a.large_list[l]];
-    if (p == 0 || L.keys_sorted[p - 1] != key) {
-      L.seg_begin[start + r] = (int)p;
-      const unsigned long long s = atomicAdd(L.n_seg, 1ull);
-      L.seg_list[s] = (long long)p;
-    }
-    if (p == n - 1 || L.keys_sorted[p + 1] != key) L.seg_end[start + r] = (int)(p + 1);
-  }
-}
-
-// one warp per merged group: mean, mean-covariance eigenbasis, reach (ref/cross_view_merge.py:44-69)
-__global__ void large_group_kernel(MergeArgs a, LargeArgs L) {
-  const int lane = threadIdx.x & 31;
-  const long long warps = (long long)gridDim.x * (blockDim.x >> 5);
-  const long long n_seg = (long long)*L.n_seg;
-  for (long long s = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); s < n_seg; s += warps) {
-    const long long p0 = L.seg_list[s];
-    const unsigned long long key = L.keys_sorted[p0];
-    const int l = (int)(key >> 32), r = (int)(key & 0xffffffffull);
-    const int start = a.cand_start[a.large_list[l]];
-    const int b = L.seg_begin[start + r], e = L.seg_end[start + r];
-    const int cnt = e - b;
-    double acc[12] = {0};
-    for (int m = b + lane; m < e; m += 32) {
-      const Proposal& M = a.props[a.idx[start + L.vals_sorted[m]]];
-      for (int t = 0; t < 3; ++t) {
-        acc[t] += M.mu[t];
-        acc[3 + t] += M.rgb[t];
-      }
-      for (int t = 0; t < 6; ++t) acc[6 + t] += M.cov[t];
-    }
-    for (int t = 0; t < 12; ++t)
-      for (int o = 16; o > 0; o >>= 1) acc[t] += __shfl_xor_sync(0xffffffffu, acc[t], o);
-    GroupRec G;
-    for (int t = 0; t < 3; ++t) {
-      G.mu[t] = acc[t] / cnt;
-      G.rgb[t] = acc[3 + t] / cnt;
-    }
-    double mcov[6];
-    for (int t = 0; t < 6; ++t) mcov[t] = acc[6 + t] / cnt;
-    double lam0[3];
-    sym_eig3(mcov, lam0, G.evec);   // identical inputs on every lane -> identical basis
-    double ext = 0.0;
-    for (int rr = 0; rr < 3; ++rr) {
-      const double ev[3] = {G.evec[rr], G.evec[3 + rr], G.evec[6 + rr]};
-      double best = 0.0;
-      for (int m = b + lane; m < e; m += 32) {
-        const Proposal& M = a.props[a.idx[start + L.vals_sorted[m]]];
-        const double off = fabs((M.mu[0] - G.mu[0]) * ev[0] + (M.mu[1] - G.mu[1]) * ev[1] +
-                                (M.mu[2] - G.mu[2]) * ev[2]);
-        best = fmax(best, off + sqrt(sym_quad(M.cov, ev)));
-      }
-      for (int o = 16; o > 0; o >>= 1) best = fmax(best, __shfl_xor_sync(0xffffffffu, best, o));
-      G.lam[rr] = best * best;
-      ext = fmax(ext, G.lam[rr]);
-    }
-    G.extent = ext;
-    if (lane == 0) a.groups[start + r] = G;
-  }
-}
-
-// block per large candidate: top-n_max groups by (extent desc, root asc), children, case
-__global__ void __launch_bounds__(256) large_cap_kernel(MergeArgs a, LargeArgs L) {
-  __shared__ double s_ext[256];
-  __shared__ int s_root[256];
-  const long long n_large = (long long)a.ctr->n_large;
-  for (long long l = blockIdx.x; l < n_large; l += gridDim.x) {
-    const int k = a.large_list[l];
-    const int P = a.cand_nvalid[k];
-    const int start = a.cand_start[k];
-    const int G = L.n_groups[l];
-    const int n_i = G < a.n_max ? G : a.n_max;
-    const int gi = a.split_list[k];
-    const float ocl = (float)fmin(fmax((double)a.opacity[gi], 1e-6), 1.0 - 1e-6);
-    for (int rk = 0; rk < n_i; ++rk) {
-      double be = -1.0;
-      int br = 0x7fffffff;
-      for (int j = threadIdx.x; j < P; j += blockDim.x) {
-        if (a.uf[start + j] != j || L.rank_of[start + j] >= 0) continue;
-        const double ej = a.groups[start + j].extent;
-        if (ej > be || (ej == be && j < br)) {
-          be = ej;
-          br = j;
-        }
-      }
-      s_ext[threadIdx.x] = be;
-      s_root[threadIdx.x] = br;
-      __syncthreads();
-      for (int st = blockDim.x / 2; st > 0; st >>= 1) {
-        if (threadIdx.x < st) {
-          const double e2 = s_ext[threadIdx.x + st];
-          const int r2 = s_root[threadIdx.x + st];
-          if (e2 > s_ext[threadIdx.x] || (e2 == s_ext[threadIdx.x] && r2 < s_root[threadIdx.x])) {
-            s_ext[threadIdx.x] = e2;
-            s_root[threadIdx.x] = r2;
-          }
-        }
-        __syncthreads();
-      }
-      if (threadIdx.x == 0) {
-        const int w = s_root[0];
-        L.rank_of[start + w] = rk;
-        write_child(a.groups[start + w], ocl, a.children + 14ll * (start + rk));
-      }
-      __syncthreads();
-    }
-    if (threadIdx.x == 0) {
-      a.cand_case[k] = ADPS_CASE_SPLIT;
-      a.cand_merged[k] = n_i;
-      a.cand_ins[k] = n_i + 1;
-      atomicAdd(&a.ctr->merge_edges, (unsigned long long)(P - G));
-      atomicAdd(&a.ctr->n_children, (unsigned long long)n_i);
-    }
-    __syncthreads();
-  }
-}
-
-cudaError_t launch_merge_small(const MergeArgs& a, cudaStream_t s) {
-  merge_small_kernel<<<a.grid, 256, 0, s>>>(a);
-  return cudaGetLastError();
-}
-
-cudaError_t launch_merge_large_gates(const MergeArgs& a, const LargeArgs& L, unsigned grid, cudaStream_t s) {
-  large_collect_kernel<<<grid, 256, 0, s>>>(a, L);
-  small_scan_kernel<<<1, 1024, 0, s>>>(L.work_cnt, L.work_off, &a.ctr->n_large);
-  pair_tile_kernel<<<grid, 256, 0, s>>>(a, L);
-  large_flatten_kernel<<<grid, 256, 0, s>>>(a, L);
-  large_compress_kernel<<<grid, 256, 0, s>>>(a, L);
-  return cudaGetLastError();
-}
-
-cudaError_t launch_merge_large_groups(const MergeArgs& a, const LargeArgs& L, long long n_keys, unsigned grid,
-                                      cudaStream_t s) {
-  if (n_keys > 0) {
-    long long b = (n_keys + 255) / 256;
-    large_segments_kernel<<<(unsigned)(b > 65535 ? 65535 : b), 256, 0, s>>>(a, L, n_keys);
-  }
-  large_group_kernel<<<grid, 256, 0, s>>>(a, L);
-  large_cap_kernel<<<grid, 256, 0, s>>>(a, L);
-  return cudaGetLastError();
-}
-
-#endif
+// ============================================================ merge: merge.cu
 
 // ============================================================ offsets
 struct CandScanPolicy {
@@ -766,6 +272,14 @@ struct KeepScanPolicy {
   }
   __device__ void total(unsigned long long t) const { a.ctr->n_keep = t; }
 };
+
+cudaError_t launch_offsets_cand(const OffsetArgs& a, long long n_split, ScanState st_c, cudaStream_t s) {
+  return launch_scan(CandScanPolicy{a}, n_split, st_c, s);
+}
+
+cudaError_t launch_offsets_keep(const OffsetArgs& a, ScanState st_g, cudaStream_t s) {
+  return launch_scan(KeepScanPolicy{a}, a.n, st_g, s);
+}
 
 cudaError_t launch_offsets(const OffsetArgs& a, long long n_split, ScanState st_c, ScanState st_g,
                            cudaStream_t s) {

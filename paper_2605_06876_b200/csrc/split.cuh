@@ -88,6 +88,10 @@ struct OffsetArgs {
   Counters* ctr;
   const unsigned long long* n_split_dev;
 };
+// the two offset scans separately (the survivor scan only needs the cases, so
+// it can overlap the merge on a second stream)
+cudaError_t launch_offsets_cand(const OffsetArgs& a, long long n_split, ScanState st_c, cudaStream_t s);
+cudaError_t launch_offsets_keep(const OffsetArgs& a, ScanState st_g, cudaStream_t s);
 cudaError_t launch_offsets(const OffsetArgs& a, long long n_split, ScanState st_c, ScanState st_g,
                            cudaStream_t s);
 
