@@ -124,8 +124,9 @@ struct adps_plan {
   int large_threshold = 32;
   // second stream: small-parent gates and the survivor scan overlap the merge
   cudaStream_t aux = nullptr;
-  cudaEvent_t ev_fork = nullptr, ev_small = nullptr, ev_keep = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_small = nullptr, ev_keep = nullptr, ev_nfork = nullptr, ev_norm = nullptr;
   bool keep_pending = false;
+  bool norm_pending = false;   // fallback normals running on the second stream
   int fb_children = 2;   // children per fallback parent of the last phase 1
   // view sharding: this plan's local view v is global view position view_offset + v * view_stride
   // of v_global_cfg sampled views (0 = the local views are all of them)
@@ -223,6 +224,8 @@ extern "C" adps_status adps_plan_create(adps_plan** plan, int32_t device, int64_
   cudaEventCreateWithFlags(&P->ev_fork, cudaEventDisableTiming);
   cudaEventCreateWithFlags(&P->ev_small, cudaEventDisableTiming);
   cudaEventCreateWithFlags(&P->ev_keep, cudaEventDisableTiming);
+  cudaEventCreateWithFlags(&P->ev_nfork, cudaEventDisableTiming);
+  cudaEventCreateWithFlags(&P->ev_norm, cudaEventDisableTiming);
   (void)max_n;
   (void)max_views;
   (void)height;
@@ -264,6 +267,8 @@ extern "C" adps_status adps_plan_destroy(adps_plan* P) {
   if (P->ev_fork) cudaEventDestroy(P->ev_fork);
   if (P->ev_small) cudaEventDestroy(P->ev_small);
   if (P->ev_keep) cudaEventDestroy(P->ev_keep);
+  if (P->ev_nfork) cudaEventDestroy(P->ev_nfork);
+  if (P->ev_norm) cudaEventDestroy(P->ev_norm);
   if (P->aux) cudaStreamDestroy(P->aux);
   delete P;
   return ADPS_OK;
@@ -995,6 +1000,10 @@ static adps_status phase1_finish(adps_plan* P, cudaStream_t s, adps_counts* coun
   oa.ctr = ctr;
   oa.n_split_dev = &ctr->n_split;
   CK(launch_offsets_cand(oa, n_split, sst2, s));
+  if (P->norm_pending) {   // join the fallback normals (read by phase 2; consumed count below)
+    CK(cudaStreamWaitEvent(s, P->ev_norm, 0));
+    P->norm_pending = false;
+  }
   if (P->keep_pending) {   // join the survivor scan started with the merge
     CK(cudaStreamWaitEvent(s, P->ev_keep, 0));
     P->keep_pending = false;
@@ -1433,9 +1442,19 @@ extern "C" adps_status adps_normals_pcg64(adps_plan* P, void* stream_v, const ui
     a.emit_idx = P->nrm_idx.as<int>();
     a.consumed = &ctr->normals_consumed;
     a.status = &ctr->normals_status;
-    CK(launch_normals(a, P->nrm_tmp.p, P->nrm_tmp.bytes, s));
+    // on the second stream: phase 1 continues on `stream` meanwhile; joined
+    // before phase 1's final counts (or right here when sync)
+    CK(cudaEventRecord(P->ev_nfork, s));
+    CK(cudaStreamWaitEvent(P->aux, P->ev_nfork, 0));
+    CK(launch_normals(a, P->nrm_tmp.p, P->nrm_tmp.bytes, P->aux));
+    CK(cudaEventRecord(P->ev_norm, P->aux));
+    P->norm_pending = true;
     P->launches += 5;
     P->lib_calls += 2;
+  }
+  if (sync && P->norm_pending) {
+    CK(cudaStreamWaitEvent(s, P->ev_norm, 0));
+    P->norm_pending = false;
   }
   if (sync) {
     CK(cudaMemcpyAsync(&P->ctr_host->normals_consumed, &ctr->normals_consumed, sizeof(unsigned long long),
