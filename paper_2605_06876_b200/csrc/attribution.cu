@@ -39,8 +39,8 @@ __device__ __forceinline__ double raw_l1(const float* __restrict__ img, const fl
 __global__ void minmax_kernel(const float* __restrict__ image, const float* __restrict__ gt,
                               const int* __restrict__ dominant, long long hw, unsigned long long* __restrict__ lohi,
                               const unsigned char* __restrict__ cls, int N, unsigned char* __restrict__ dom_flag,
-                              unsigned* __restrict__ cand_bits, double* __restrict__ raw_out) {
-  const int v = blockIdx.y;
+                              unsigned* __restrict__ cand_bits, double* __restrict__ raw_out, int v0) {
+  const int v = v0 + blockIdx.y;
   const float* img = image + (long long)v * hw * 3;
   const float* g = gt + (long long)v * hw * 3;
   const int* dom = dominant + (long long)v * hw;
@@ -122,10 +122,10 @@ __device__ double min_true(double d, int k, double tau, double omt, double nb) {
 }
 
 // thr[v*L + 0] = x threshold of m; thr[v*L + k] = x threshold of band >= k.
-__global__ void thresholds_kernel(const unsigned long long* __restrict__ lohi, int n_views, int L,
+__global__ void thresholds_kernel(const unsigned long long* __restrict__ lohi, int v0, int n_views, int L,
                                   double tau, double* __restrict__ lo_out, double* __restrict__ thr) {
-  int t = blockIdx.x * blockDim.x + threadIdx.x;
-  if (t >= n_views * L) return;
+  int t = v0 * L + blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= (v0 + n_views) * L) return;
   int v = t / L, k = t % L;
   double lo = __longlong_as_double((long long)lohi[2 * v]);
   double hi = __longlong_as_double((long long)lohi[2 * v + 1]);
@@ -552,14 +552,21 @@ __global__ void partial_emit_kernel(const PartialRec* __restrict__ partials, con
 // --------------------------------------------------------------- launchers
 size_t tile_smem_bytes() { return sizeof(TileSmem); }
 
+cudaError_t launch_minmax_views(const AttributionArgs& a, int v0, int v1, cudaStream_t s) {
+  if (v1 <= v0) return cudaSuccess;
+  const long long hw = (long long)a.H * a.W;
+  dim3 mg((unsigned)((hw + 256 * 8 - 1) / (256 * 8)), (unsigned)(v1 - v0));
+  if (mg.x > 1024) mg.x = 1024;
+  minmax_kernel<<<mg, 256, 0, s>>>(a.image, a.gt, a.dom, hw, a.lohi, a.cls, a.N, a.dom_flag, a.cand_bits, a.raw, v0);
+  const int nt = (v1 - v0) * a.L;
+  thresholds_kernel<<<(nt + 127) / 128, 128, 0, s>>>(a.lohi, v0, v1 - v0, a.L, a.tau, a.lo, a.thr);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_minmax(const AttributionArgs& a, const int* split_list, Counters* ctr, int sm_count,
                           cudaStream_t s) {
-  const long long hw = (long long)a.H * a.W;
-  dim3 mg((unsigned)((hw + 256 * 8 - 1) / (256 * 8)), (unsigned)a.V);
-  if (mg.x > 1024) mg.x = 1024;
-  minmax_kernel<<<mg, 256, 0, s>>>(a.image, a.gt, a.dom, hw, a.lohi, a.cls, a.N, a.dom_flag, a.cand_bits, a.raw);
-  int nt = a.V * a.L;
-  thresholds_kernel<<<(nt + 127) / 128, 128, 0, s>>>(a.lohi, a.V, a.L, a.tau, a.lo, a.thr);
+  cudaError_t e = launch_minmax_views(a, 0, a.V, s);
+  if (e != cudaSuccess) return e;
   fallback_count_kernel<<<sm_count * 2, 256, 0, s>>>(split_list, a.dom_flag, ctr);
   return cudaGetLastError();
 }
@@ -570,7 +577,7 @@ cudaError_t launch_fallback_count(const int* split_list, const unsigned char* do
   return cudaGetLastError();
 }
 
-cudaError_t launch_attribution(const AttributionArgs& a, cudaStream_t s, MarkFn mark, void* ctx) {
+static TileParams tile_params(const AttributionArgs& a) {
   TileParams P;
   P.image = a.image;
   P.gt = a.gt;
@@ -605,16 +612,29 @@ cudaError_t launch_attribution(const AttributionArgs& a, cudaStream_t s, MarkFn 
   P.raw = a.raw;
   P.deferred = a.deferred;
   P.n_deferred = a.n_deferred;
+  return P;
+}
+
+bool attribution_warp_path(const AttributionArgs& a) {
+  // the warp kernel covers r_erode <= 3 without debug maps; the block kernel
+  // takes everything else and the tiles the warp kernel defers
+  return a.tile_path == 0 && !a.dbg_m && a.r_erode <= 3 && a.deferred && a.n_deferred;
+}
+
+cudaError_t launch_tiles_views(const AttributionArgs& a, int v0, int v1, cudaStream_t s) {
+  if (!attribution_warp_path(a) || v1 <= v0) return cudaSuccess;
+  const TileParams P = tile_params(a);
+  const long long tpv = (long long)P.tiles_x * P.tiles_y;
+  return launch_tile_warp(P, tpv * v0, tpv * v1, s);
+}
+
+cudaError_t launch_attribution_tail(const AttributionArgs& a, cudaStream_t s, MarkFn mark, void* ctx) {
+  const TileParams P = tile_params(a);
   const long long nblocks = (long long)P.tiles_x * P.tiles_y * a.V;
   size_t smem = sizeof(TileSmem);
   cudaError_t e = cudaFuncSetAttribute(tile_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  // the warp kernel covers r_erode <= 3 without debug maps; the block kernel
-  // takes everything else and the tiles the warp kernel defers
-  const bool warp_path = a.tile_path == 0 && !a.dbg_m && a.r_erode <= 3 && a.deferred && a.n_deferred;
-  if (warp_path) {
-    e = launch_tile_warp(P, nblocks, s);
-    if (e != cudaSuccess) return e;
+  if (attribution_warp_path(a)) {
     tile_kernel<<<a.grid_small, kTileThreads, smem, s>>>(P, a.deferred, a.n_deferred);
     if (mark) mark(ctx, "tile_ccl", s, 2);
   } else {
@@ -635,6 +655,12 @@ cudaError_t launch_attribution(const AttributionArgs& a, cudaStream_t s, MarkFn 
                                                     a.m_min, a.regions, a.n_regions, a.region_cap, a.overflow);
   if (mark) mark(ctx, "border_merge", s, 3);
   return cudaGetLastError();
+}
+
+cudaError_t launch_attribution(const AttributionArgs& a, cudaStream_t s, MarkFn mark, void* ctx) {
+  cudaError_t e = launch_tiles_views(a, 0, a.V, s);
+  if (e != cudaSuccess) return e;
+  return launch_attribution_tail(a, s, mark, ctx);
 }
 
 }  // namespace adps

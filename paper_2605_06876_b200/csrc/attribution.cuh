@@ -75,8 +75,8 @@ struct AttributionArgs {
   double* raw;                       // [V][H*W] raw L1 error written by the minmax pass, or null
 };
 
-// warp-per-tile scanline CCL (r_erode <= 3); defers tiles with > kWarpMaxRuns runs
-cudaError_t launch_tile_warp(const TileParams& P, long long n_tiles, cudaStream_t s);
+// warp-per-tile scanline CCL (r_erode <= 3) over tiles [t0, t1); defers tiles with > kWarpMaxRuns runs
+cudaError_t launch_tile_warp(const TileParams& P, long long t0, long long t1, cudaStream_t s);
 size_t tile_warp_smem_bytes();
 
 size_t tile_smem_bytes();
@@ -89,5 +89,11 @@ cudaError_t launch_fallback_count(const int* split_list, const unsigned char* do
 // Called after each group of launches: name, stream, number of kernels launched.
 typedef void (*MarkFn)(void* ctx, const char* name, cudaStream_t s, int kernels);
 cudaError_t launch_attribution(const AttributionArgs& a, cudaStream_t s, MarkFn mark, void* ctx);
+// the same in pieces, so views can be pipelined: minmax + thresholds of views
+// [v0, v1); warp CCL of their tiles; then the deferred tiles + border merge
+cudaError_t launch_minmax_views(const AttributionArgs& a, int v0, int v1, cudaStream_t s);
+cudaError_t launch_tiles_views(const AttributionArgs& a, int v0, int v1, cudaStream_t s);
+cudaError_t launch_attribution_tail(const AttributionArgs& a, cudaStream_t s, MarkFn mark, void* ctx);
+bool attribution_warp_path(const AttributionArgs& a);
 
 }  // namespace adps

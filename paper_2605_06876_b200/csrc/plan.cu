@@ -14,6 +14,12 @@
 #include "merge.cuh"
 #include "normals.cuh"
 
+#ifndef ADPS_PIPELINE_DEFAULT
+#define ADPS_PIPELINE_DEFAULT 1
+#endif
+#ifndef ADPS_PIPELINE_CHUNKS
+#define ADPS_PIPELINE_CHUNKS 2
+#endif
 #ifndef ADPS_RAW_CACHE_DEFAULT
 #define ADPS_RAW_CACHE_DEFAULT 1
 #endif
@@ -127,6 +133,13 @@ struct adps_plan {
   cudaEvent_t ev_fork = nullptr, ev_small = nullptr, ev_keep = nullptr, ev_nfork = nullptr, ev_norm = nullptr;
   bool keep_pending = false;
   bool norm_pending = false;   // fallback normals running on the second stream
+  // attribution pipelined with the input pass: the warp CCL of view chunk c runs
+  // on the second stream while the minmax pass reads chunk c+1
+  static constexpr int kMaxChunks = 16;
+  cudaEvent_t ev_chunk[kMaxChunks] = {};
+  cudaEvent_t ev_attr = nullptr;
+  bool attr_pending = false;
+  int pipeline = ADPS_PIPELINE_DEFAULT;
   int fb_children = 2;   // children per fallback parent of the last phase 1
   // view sharding: this plan's local view v is global view position view_offset + v * view_stride
   // of v_global_cfg sampled views (0 = the local views are all of them)
@@ -226,6 +239,8 @@ extern "C" adps_status adps_plan_create(adps_plan** plan, int32_t device, int64_
   cudaEventCreateWithFlags(&P->ev_keep, cudaEventDisableTiming);
   cudaEventCreateWithFlags(&P->ev_nfork, cudaEventDisableTiming);
   cudaEventCreateWithFlags(&P->ev_norm, cudaEventDisableTiming);
+  cudaEventCreateWithFlags(&P->ev_attr, cudaEventDisableTiming);
+  for (int i = 0; i < adps_plan::kMaxChunks; ++i) cudaEventCreateWithFlags(&P->ev_chunk[i], cudaEventDisableTiming);
   (void)max_n;
   (void)max_views;
   (void)height;
@@ -269,6 +284,9 @@ extern "C" adps_status adps_plan_destroy(adps_plan* P) {
   if (P->ev_keep) cudaEventDestroy(P->ev_keep);
   if (P->ev_nfork) cudaEventDestroy(P->ev_nfork);
   if (P->ev_norm) cudaEventDestroy(P->ev_norm);
+  if (P->ev_attr) cudaEventDestroy(P->ev_attr);
+  for (int i = 0; i < adps_plan::kMaxChunks; ++i)
+    if (P->ev_chunk[i]) cudaEventDestroy(P->ev_chunk[i]);
   if (P->aux) cudaStreamDestroy(P->aux);
   delete P;
   return ADPS_OK;
@@ -605,9 +623,31 @@ extern "C" adps_status adps_step_phase1_begin(adps_plan* P, void* stream_v, cons
   CK(cudaMemcpyAsync(P->lohi.p, P->lohi_host, sizeof(unsigned long long) * 2 * V, cudaMemcpyHostToDevice, s));
   {
     const AttributionArgs a = attr_args(P, V, H, W, cfg, N, image, gt, dominant);
-    CK(launch_minmax(a, P->split_list.as<int>(), ctr, P->sm_count, s));
+    P->attr_pending = false;
+    if (P->pipeline && !P->timing && V >= 2 && attribution_warp_path(a)) {
+      // views in chunks: minmax of chunk c on `stream`, the warp CCL of chunk c
+      // on the second stream as soon as its thresholds exist; the tail (deferred
+      // tiles, border merge) after the last chunk; phase1_end joins it
+      const int maxc = ADPS_PIPELINE_CHUNKS < adps_plan::kMaxChunks ? ADPS_PIPELINE_CHUNKS : adps_plan::kMaxChunks;
+      const int chunks = V < maxc ? V : maxc;
+      for (int c = 0; c < chunks; ++c) {
+        const int v0 = (int)((long long)V * c / chunks), v1 = (int)((long long)V * (c + 1) / chunks);
+        CK(launch_minmax_views(a, v0, v1, s));
+        CK(cudaEventRecord(P->ev_chunk[c], s));
+        CK(cudaStreamWaitEvent(P->aux, P->ev_chunk[c], 0));
+        CK(launch_tiles_views(a, v0, v1, P->aux));
+      }
+      CK(launch_fallback_count(P->split_list.as<int>(), P->dom_flag.as<unsigned char>(), ctr, P->sm_count, s));
+      CK(launch_attribution_tail(a, P->aux, nullptr, nullptr));
+      CK(cudaEventRecord(P->ev_attr, P->aux));
+      P->attr_pending = true;
+      P->launches += 3 * chunks + 1 + 4;
+    } else {
+      CK(launch_minmax(a, P->split_list.as<int>(), ctr, P->sm_count, s));
+      P->launches += 3;
+    }
   }
-  mark(P, "minmax_dominance", s, 3);
+  mark(P, "minmax_dominance", s, 0);
   CK(cudaMemcpyAsync(P->ctr_host, ctr, sizeof(Counters), cudaMemcpyDeviceToHost, s));
   CK(cudaStreamSynchronize(s));
   {
@@ -654,8 +694,13 @@ static adps_status phase1_local(adps_plan* P, cudaStream_t s, long long* n_regio
 
   // ---- maps + partition + moments (ref/adc.py:168-176)
   for (int attempt = 0;; ++attempt) {
-    st = run_attribution(P, s, V, H, W, cfg, N, image, gt, dominant);
-    if (st != ADPS_OK) return st;
+    if (attempt == 0 && P->attr_pending) {   // launched by phase1_begin, pipelined with the input pass
+      CK(cudaStreamWaitEvent(s, P->ev_attr, 0));
+      P->attr_pending = false;
+    } else {
+      st = run_attribution(P, s, V, H, W, cfg, N, image, gt, dominant);
+      if (st != ADPS_OK) return st;
+    }
     CK(cudaMemcpyAsync(P->ctr_host, ctr, sizeof(Counters), cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
     if (!P->ctr_host->overflow) break;

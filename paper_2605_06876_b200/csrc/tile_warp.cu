@@ -441,34 +441,35 @@ __device__ __forceinline__ void tile_warp_body(const TileParams& P, WarpSmem& S,
 }
 
 template <int R, bool RAW>
-__global__ void __launch_bounds__(kWarpsPerBlock * 32, ADPS_TW_MINBLOCKS) tile_warp_kernel(TileParams P, long long n_tiles) {
+__global__ void __launch_bounds__(kWarpsPerBlock * 32, ADPS_TW_MINBLOCKS) tile_warp_kernel(TileParams P, long long t0, long long t1) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   WarpSmem& S = reinterpret_cast<WarpSmem*>(smem_raw)[wid];
-  const long long tile = (long long)blockIdx.x * kWarpsPerBlock + wid;
-  if (tile >= n_tiles) return;   // warp-uniform
+  const long long tile = t0 + (long long)blockIdx.x * kWarpsPerBlock + wid;
+  if (tile >= t1) return;   // warp-uniform
   tile_warp_body<R, RAW>(P, S, tile, lane);
 }
 
 template <int R, bool RAW>
-static cudaError_t launch_r(const TileParams& P, long long n_tiles, cudaStream_t s) {
+static cudaError_t launch_r(const TileParams& P, long long t0, long long t1, cudaStream_t s) {
   const size_t smem = tile_warp_smem_bytes();
   cudaError_t e = cudaFuncSetAttribute(tile_warp_kernel<R, RAW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  const long long blocks = (n_tiles + kWarpsPerBlock - 1) / kWarpsPerBlock;
-  tile_warp_kernel<R, RAW><<<(unsigned)blocks, kWarpsPerBlock * 32, smem, s>>>(P, n_tiles);
+  const long long blocks = (t1 - t0 + kWarpsPerBlock - 1) / kWarpsPerBlock;
+  if (blocks <= 0) return cudaSuccess;
+  tile_warp_kernel<R, RAW><<<(unsigned)blocks, kWarpsPerBlock * 32, smem, s>>>(P, t0, t1);
   return cudaGetLastError();
 }
 
-cudaError_t launch_tile_warp(const TileParams& P, long long n_tiles, cudaStream_t s) {
+cudaError_t launch_tile_warp(const TileParams& P, long long t0, long long t1, cudaStream_t s) {
   if (P.raw) {
-    if (P.r_erode <= 1) return launch_r<1, true>(P, n_tiles, s);
-    if (P.r_erode == 2) return launch_r<2, true>(P, n_tiles, s);
-    if (P.r_erode == 3) return launch_r<3, true>(P, n_tiles, s);
+    if (P.r_erode <= 1) return launch_r<1, true>(P, t0, t1, s);
+    if (P.r_erode == 2) return launch_r<2, true>(P, t0, t1, s);
+    if (P.r_erode == 3) return launch_r<3, true>(P, t0, t1, s);
   } else {
-    if (P.r_erode <= 1) return launch_r<1, false>(P, n_tiles, s);
-    if (P.r_erode == 2) return launch_r<2, false>(P, n_tiles, s);
-    if (P.r_erode == 3) return launch_r<3, false>(P, n_tiles, s);
+    if (P.r_erode <= 1) return launch_r<1, false>(P, t0, t1, s);
+    if (P.r_erode == 2) return launch_r<2, false>(P, t0, t1, s);
+    if (P.r_erode == 3) return launch_r<3, false>(P, t0, t1, s);
   }
   return cudaErrorInvalidValue;
 }
