@@ -1,6 +1,6 @@
 """One densify step of a bench config bracketed by cudaProfilerStart/Stop (dev tool).
 
-ncu --profile-from-start off ... python tools/profile_step.py [config3]
+ncu --profile-from-start off ... python tools/profile_step.py [config3] [--timing]
 captures exactly the launches of one warm step (renders resident, as bench.py).
 """
 import os
@@ -14,7 +14,8 @@ from paper_2605_06876_b200 import operator as op  # noqa: E402
 from paper_2605_06876_b200 import synth as S  # noqa: E402
 from paper_2605_06876_b200.types import AdpSplitConfig  # noqa: E402
 
-name = sys.argv[1] if len(sys.argv) > 1 else "config3"
+args = [a for a in sys.argv[1:] if not a.startswith("--")]
+name = args[0] if args else "config3"
 wl = S.CONFIGS[name]
 ini, cams, (ga, den), gt = wl.build()
 plan = op.Plan("cuda:0")
@@ -23,6 +24,8 @@ gt_img, _ = plan.render(op.GaussianTensors.from_numpy(*gt.arrays(), device="cuda
 img, dom = plan.render(g, cams)
 cfg = AdpSplitConfig(v_views=len(cams), n_max=wl.n_max)
 ga_t, den_t = torch.as_tensor(ga, device="cuda"), torch.as_tensor(den, device="cuda")
+if "--timing" in sys.argv:   # stage-timing mode: one tile launch over all views (no pipelining), as bench's breakdown
+    plan.set_timing(True)
 
 
 def step():
