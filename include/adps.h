@@ -226,6 +226,8 @@ ADPS_API adps_status adps_get_timing(adps_plan* plan, double* ms, int32_t max_en
 #define ADPS_BUF_CAND_MERGED 5   /* int32 [n_split]: children per split parent */
 #define ADPS_BUF_CAND_INS 6      /* int32 [n_split]: inserted Gaussians per parent */
 #define ADPS_BUF_CHILDREN 7      /* 14 floats per proposal slot: children of parent k at its proposal range */
+#define ADPS_BUF_LO 8            /* double [V]: per-view min raw L1 error (diagnostic) */
+#define ADPS_BUF_THRESHOLDS 9    /* double [V][L]: x thresholds of m and of each band (diagnostic) */
 ADPS_API adps_status adps_set_view_sharding(adps_plan* plan, int32_t view_offset, int32_t view_stride,
                                             int32_t n_views_global);
 ADPS_API adps_status adps_get_buffer(adps_plan* plan, int32_t which, void** ptr, int64_t* count, int64_t* elem_bytes);

@@ -1228,7 +1228,9 @@ extern "C" adps_status adps_step_phase2(adps_plan* P, void* stream_v, const adps
   if (!P->have_phase1) return fail(ADPS_BAD_STATE, "phase 2 without a successful phase 1");
   adps_status st = check_gaussians(g, P->n);
   if (st != ADPS_OK) return st;
-  if (!out || !index_map) return fail(ADPS_INVALID_ARG, "outputs are NULL");
+  if (P->counts.n_out == 0) return ADPS_OK;   // nothing to write (e.g. an empty scene)
+  if (!out || !index_map || !out->mu || !out->scale || !out->rot || !out->opacity || !out->sh_dc)
+    return fail(ADPS_INVALID_ARG, "outputs are NULL");
   if (P->counts.n_fallback > 0 && !fallback_normals) return fail(ADPS_INVALID_ARG, "fallback normals are NULL");
   if (g->sh_rest_k != P->sh_k || out->sh_rest_k != P->sh_k)
     return fail(ADPS_INVALID_ARG, "sh_rest_k differs between phases/outputs");
@@ -1364,6 +1366,16 @@ extern "C" adps_status adps_get_buffer(adps_plan* P, int32_t which, void** ptr, 
       *ptr = P->valid.p;
       *count = P->n_regions_cur;
       *elem_bytes = 1;
+      return ADPS_OK;
+    case ADPS_BUF_LO:
+      *ptr = P->lo.p;
+      *count = P->cx.V;
+      *elem_bytes = 8;
+      return ADPS_OK;
+    case ADPS_BUF_THRESHOLDS:
+      *ptr = P->thr.p;
+      *count = (int64_t)P->cx.V * P->cx.cfg.l_bands;
+      *elem_bytes = 8;
       return ADPS_OK;
     case ADPS_BUF_CAND_MERGED:
       *ptr = P->cand_merged.p;

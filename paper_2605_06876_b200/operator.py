@@ -258,8 +258,19 @@ class Plan:
         return image, dom
 
     # -- phase 1 / 2 (ref/adc.py:165-244)
+    @staticmethod
+    def _check_inputs(grad_accum, denom, image, gt, dom):
+        """The C ABI takes raw pointers: reject tensors of the wrong type/layout loudly."""
+        for name, t, dt in (("grad_accum", grad_accum, F64), ("denom", denom, F64), ("image", image, F32),
+                            ("gt", gt, F32), ("dominant", dom, torch.int32)):
+            if t.dtype != dt:
+                raise ValueError(f"{name} must be {dt}, got {t.dtype}")
+            if not t.is_cuda or not t.is_contiguous():
+                raise ValueError(f"{name} must be a contiguous CUDA tensor")
+
     def phase1(self, g, extent, grad_accum, denom, cfg, cams_v, image, gt, dom) -> dict:
         cams_v = camera_rows(cams_v)
+        self._check_inputs(grad_accum, denom, image, gt, dom)
         counts = _abi.Counts()
         cs = config_struct(cfg)
         ga = g.abi()
@@ -274,6 +285,7 @@ class Plan:
     def phase1_begin(self, g, extent, grad_accum, denom, cfg, cams_v, image, gt, dom) -> dict:
         """select + ever-dominant flags; returns n_split/n_clone/n_fallback after one sync."""
         cams_v = camera_rows(cams_v)
+        self._check_inputs(grad_accum, denom, image, gt, dom)
         counts = _abi.Counts()
         cs = config_struct(cfg)
         ga = g.abi()
@@ -540,8 +552,8 @@ def _gather_views(x, view_ids, device):
         if x.device != device:
             x = x.to(device)
         if view_ids == list(range(view_ids[0], view_ids[0] + len(view_ids))):
-            return x[view_ids[0]:view_ids[0] + len(view_ids)].contiguous()
-        return x.index_select(0, torch.as_tensor(view_ids, device=device)).contiguous()
+            return x[view_ids[0]:view_ids[0] + len(view_ids)].to(F32).contiguous()
+        return x.index_select(0, torch.as_tensor(view_ids, device=device)).to(F32).contiguous()
     return torch.stack([torch.as_tensor(np.asarray(x[v], dtype=np.float32), device=device)
                         for v in view_ids]).contiguous()
 

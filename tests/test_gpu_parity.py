@@ -171,17 +171,19 @@ def test_partition_snakes_cross_tiles(op, plan, shape):
     np.testing.assert_array_equal(got, want)
 
 
-@pytest.mark.parametrize("r_erode", [1, 2, 3])
-@pytest.mark.parametrize("seed", range(4))
-def test_partition_erosion_both_paths(op, plan, seed, r_erode):
-    """Warp CCL (r <= 3: ring-buffer erosion with halo columns) vs block CCL vs oracle."""
+@pytest.mark.parametrize("l_bands", [1, 3, 6])
+@pytest.mark.parametrize("r_erode", [1, 2, 3, 4])
+@pytest.mark.parametrize("seed", range(3))
+def test_partition_erosion_both_paths(op, plan, seed, r_erode, l_bands):
+    """Warp CCL (r <= 3: erosion masks with halo columns; L <= 4 and the general
+    band loop) vs block CCL (r = 4) vs oracle."""
     rng = np.random.default_rng(100 + seed)
     h, w = int(rng.integers(30, 170)), int(rng.integers(30, 170))
     n = 5
     dom = np.kron(rng.integers(-1, n, (h // 4 + 1, w // 4 + 1)), np.ones((4, 4), np.int64))[:h, :w]
     e = np.kron(rng.uniform(0, 1, (h // 2 + 1, w // 2 + 1)), np.ones((2, 2)))[:h, :w]
     e[rng.uniform(size=(h, w)) < 0.05] = 0.01
-    got, want = _injected_partition(op, plan, e, dom, n, int(rng.integers(1, 4)), int(rng.integers(1, 4)),
+    got, want = _injected_partition(op, plan, e, dom, n, l_bands, int(rng.integers(1, 4)),
                                     [0, 1, 3, 4], r_erode=r_erode)
     np.testing.assert_array_equal(got, want)
 
@@ -595,3 +597,66 @@ def test_reference_api_vanilla_and_remap(op):
     wg, wd = O.remap_stats(ga, den, want.index_map, [], want.clones)
     np.testing.assert_array_equal(st2.grad_accum, wg)
     np.testing.assert_array_equal(st2.denom, wd)
+
+
+
+# ------------------------------------------------------------- degenerate steps
+def _tiny_step_inputs(n, seed=0, w=9, h=7, views=2):
+    rng = np.random.default_rng(seed)
+    g = O.Gaussians(rng.uniform(-0.3, 0.3, (n, 3)), rng.uniform(0.05, 0.2, (n, 3)),
+                    np.tile([1.0, 0, 0, 0], (n, 1)), rng.uniform(0.5, 0.9, n), rng.uniform(-1, 1, (n, 3)))
+    g = PA.oracle_gaussians_f32(g)
+    cams = [O.Cam(np.eye(3), np.array([0.1 * v, 0, -2.0]), 1.0 * w, 1.0 * w, (w - 1) / 2, (h - 1) / 2, w, h)
+            for v in range(views)]
+    gts = PA.f32(rng.uniform(0, 1, (views, h, w, 3)))
+    return g, cams, gts
+
+
+@pytest.mark.parametrize("case", ["empty", "no_candidates", "tiny_image", "all_split"])
+def test_degenerate_steps_match_oracle(op, plan, case):
+    """N = 0, no split/clone candidate, a 9x7 image, every Gaussian a candidate."""
+    import torch
+    n = 0 if case == "empty" else 12
+    g, cams, gts = _tiny_step_inputs(n)
+    rows = np.stack([c.row() for c in cams])
+    ga = np.full(n, 1.0) if case == "all_split" else (np.zeros(n) if case == "no_candidates" else
+                                                     np.random.default_rng(3).uniform(0, 1e-3, n))
+    den = np.ones(n)
+    cfg = golden_io.Cfg(dict(tau_l1=0.1, r_erode=2, m_min=1, l_bands=3, n_max=4, v_views=2, gamma_d=2.0,
+                             gamma_c=0.15, tau_g=2e-4, tau_s=0.01 if case != "all_split" else 1e-9, eta=1.6,
+                             eps=1e-9))
+    views = O.sample_views(len(cams), cfg.v_views, np.random.default_rng(1))
+    if n:
+        img, dom = plan.render(PA.to_tensors(g), rows[views])
+    else:
+        img = torch.zeros((len(views), 7, 9, 3), device="cuda")
+        dom = torch.full((len(views), 7, 9), -1, dtype=torch.int32, device="cuda")
+    res = op.densify_step(PA.to_tensors(g), 1.0, rows, torch.as_tensor(gts, device="cuda"),
+                          torch.as_tensor(ga, device="cuda"), torch.as_tensor(den, device="cuda"), cfg,
+                          np.random.default_rng(1), renders=(img, dom), plan=plan)
+    renders = {v: (img[k].double().cpu().numpy(), dom[k].long().cpu().numpy()) for k, v in enumerate(views)}
+    want = O.adpsplit_step(g, 1.0, cams, gts, ga, den, cfg, np.random.default_rng(1), renders=renders)
+    assert res.counts["n_out"] == want.count_after
+    np.testing.assert_array_equal(res.index_map.cpu().numpy(), want.index_map)
+    rep = res.report()
+    assert [(c.index, c.fallback, c.reset, c.children_inserted) for c in rep.candidates] == \
+        [(c.index, c.fallback, c.reset, c.children_inserted) for c in want.candidates]
+    if case == "no_candidates":
+        assert res.counts["n_out"] == n and res.counts["n_split"] == 0
+
+
+def test_wrong_dtypes_are_rejected(op, plan):
+    """Raw pointers cross the C ABI: a float64 image or int64 dominant map must raise, not be misread."""
+    import torch
+    g, cams, gts = _tiny_step_inputs(4)
+    rows = np.stack([c.row() for c in cams])
+    img = torch.zeros((1, 7, 9, 3), dtype=torch.float64, device="cuda")
+    dom = torch.full((1, 7, 9), -1, dtype=torch.int32, device="cuda")
+    gt = torch.zeros((1, 7, 9, 3), dtype=torch.float32, device="cuda")
+    ga, den = torch.zeros(4, dtype=torch.float64, device="cuda"), torch.ones(4, dtype=torch.float64, device="cuda")
+    cfg = dict(tau_l1=0.1, r_erode=2, m_min=1, l_bands=3, n_max=4, v_views=1, gamma_d=2.0, gamma_c=0.15,
+               tau_g=2e-4, tau_s=0.01, eta=1.6, eps=1e-9)
+    with pytest.raises(ValueError):
+        plan.phase1(PA.to_tensors(g), 1.0, ga, den, cfg, rows[:1], img, gt, dom)
+    with pytest.raises(ValueError):
+        plan.phase1(PA.to_tensors(g), 1.0, ga, den, cfg, rows[:1], img.float(), gt, dom.long())
