@@ -122,8 +122,25 @@ __device__ double min_true(double d, int k, double tau, double omt, double nb) {
 }
 
 // thr[v*L + 0] = x threshold of m; thr[v*L + k] = x threshold of band >= k.
+// the same threshold in the raw domain: the smallest raw in [lo, hi] with
+// fl(raw - lo) >= t (the subtraction is monotone, and every raw of the view lies
+// in [lo, hi]), so the warp CCL compares raw directly
+__device__ double raw_threshold(double lo, double hi, double t) {
+  if (t == INFINITY) return INFINITY;
+  if (!(dsub(hi, lo) >= t)) return INFINITY;
+  if (dsub(lo, lo) >= t) return lo;
+  long long a = __double_as_longlong(lo), b = __double_as_longlong(hi);   // pred(a) false, pred(b) true
+  while (b - a > 1) {
+    const long long mid = a + (b - a) / 2;
+    if (dsub(__longlong_as_double(mid), lo) >= t) b = mid;
+    else a = mid;
+  }
+  return __longlong_as_double(b);
+}
+
 __global__ void thresholds_kernel(const unsigned long long* __restrict__ lohi, int v0, int n_views, int L,
-                                  double tau, double* __restrict__ lo_out, double* __restrict__ thr) {
+                                  double tau, double* __restrict__ lo_out, double* __restrict__ thr,
+                                  double* __restrict__ thr_raw) {
   int t = v0 * L + blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= (v0 + n_views) * L) return;
   int v = t / L, k = t % L;
@@ -132,11 +149,13 @@ __global__ void thresholds_kernel(const unsigned long long* __restrict__ lohi, i
   if (k == 0) lo_out[v] = lo;
   if (hi == lo) {  // error_map returns zeros: m false, band 0 (ref/error_partition.py:52-53)
     thr[t] = INFINITY;
+    if (thr_raw) thr_raw[t] = INFINITY;
     return;
   }
   double d = dsub(hi, lo);
   double omt = dsub(1.0, tau);
   thr[t] = min_true(d, k, tau, omt, (double)L);
+  if (thr_raw) thr_raw[t] = raw_threshold(lo, hi, thr[t]);
 }
 
 // ---------------------------------------------------- ever-dominant (early)
@@ -559,7 +578,7 @@ cudaError_t launch_minmax_views(const AttributionArgs& a, int v0, int v1, cudaSt
   if (mg.x > 1024) mg.x = 1024;
   minmax_kernel<<<mg, 256, 0, s>>>(a.image, a.gt, a.dom, hw, a.lohi, a.cls, a.N, a.dom_flag, a.cand_bits, a.raw, v0);
   const int nt = (v1 - v0) * a.L;
-  thresholds_kernel<<<(nt + 127) / 128, 128, 0, s>>>(a.lohi, v0, v1 - v0, a.L, a.tau, a.lo, a.thr);
+  thresholds_kernel<<<(nt + 127) / 128, 128, 0, s>>>(a.lohi, v0, v1 - v0, a.L, a.tau, a.lo, a.thr, a.thr_raw);
   return cudaGetLastError();
 }
 
@@ -590,6 +609,7 @@ static TileParams tile_params(const AttributionArgs& a) {
   P.view_stride = a.view_stride;
   P.lo = a.lo;
   P.thr = a.thr;
+  P.thr_raw = a.thr_raw;
   P.L = a.L;
   P.r_erode = a.r_erode;
   P.m_min = a.m_min;

@@ -13,6 +13,7 @@ struct TileParams {
   int view_offset, view_stride;     // global view position = view_offset + v * view_stride
   const double* lo;
   const double* thr;
+  const double* thr_raw;             // the thresholds in the raw domain (warp CCL)
   int L, r_erode, m_min;
   const unsigned char* cls;
   int N;
@@ -56,6 +57,7 @@ struct AttributionArgs {
   unsigned long long* lohi;   // [2V], preset to (+inf bits, 0)
   double* lo;                 // [V]
   double* thr;                // [V*L]
+  double* thr_raw;            // [V*L] the same as raw L1 thresholds
   RegionRec* regions;
   unsigned long long* n_regions;
   long long region_cap;

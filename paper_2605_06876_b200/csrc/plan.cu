@@ -86,7 +86,7 @@ struct adps_plan {
   Buf cand_start, cand_end, cand_nvalid, cand_case, cand_props, cand_merged, cand_ins, ins_off, fb_ord,
       large_list, regions_per_view;
   // per-view
-  Buf lohi, lo, thr, cams;
+  Buf lohi, lo, thr, thr_raw, cams;
   // tiles / fragments / regions
   Buf border, partials, partial_parent, regions, props, valid, keys, vals, keys_sorted, vals_sorted;
   Buf idx, uf, groups, children, dbg_stats, dbg_child, deferred, cand_bits, rawc;
@@ -256,7 +256,7 @@ extern "C" adps_status adps_plan_destroy(adps_plan* P) {
   Buf* bufs[] = {&P->cls, &P->cand_rank, &P->split_list, &P->clone_list, &P->dom_flag, &P->keep_pos,
                  &P->cand_start, &P->cand_end, &P->cand_nvalid, &P->cand_case, &P->cand_props,
                  &P->cand_merged, &P->cand_ins, &P->ins_off, &P->fb_ord, &P->large_list,
-                 &P->regions_per_view, &P->lohi, &P->lo, &P->thr, &P->cams, &P->border, &P->partials,
+                 &P->regions_per_view, &P->lohi, &P->lo, &P->thr, &P->thr_raw, &P->cams, &P->border, &P->partials,
                  &P->partial_parent, &P->regions, &P->props, &P->valid, &P->keys, &P->vals,
                  &P->keys_sorted, &P->vals_sorted, &P->idx, &P->uf, &P->groups, &P->children,
                  &P->dbg_stats, &P->dbg_child, &P->scan_val, &P->scan_flag, &P->scan_ticket,
@@ -465,6 +465,7 @@ static AttributionArgs attr_args(adps_plan* P, int V, int H, int W, const adps_c
   a.lohi = P->lohi.as<unsigned long long>();
   a.lo = P->lo.as<double>();
   a.thr = P->thr.as<double>();
+  a.thr_raw = P->thr_raw.as<double>();
   a.regions = P->regions.as<RegionRec>();
   a.n_regions = &ctr->n_regions;
   a.region_cap = P->region_cap;
@@ -560,6 +561,7 @@ extern "C" adps_status adps_step_phase1_begin(adps_plan* P, void* stream_v, cons
   CK(ensure(P->lohi, 16ll * V));
   CK(ensure(P->lo, 8ll * V));
   CK(ensure(P->thr, 8ll * V * cfg->l_bands));
+  CK(ensure(P->thr_raw, 8ll * V * cfg->l_bands));
   CK(ensure(P->cams, 8ll * 18 * V));
   CK(ensure(P->border, 4ll * n_tiles * kBorderSlots));
   CK(ensure(P->deferred, 4ll * n_tiles));

@@ -67,7 +67,7 @@ struct TileConst {
   const unsigned* cbits;   // candidate bits of the view
   const double* raw;       // cached raw L1 error of the view (RAW path)
   const double* thr;
-  double lo, x_m, t1, t2, t3;
+  double x_m, t1, t2, t3;   // raw-domain thresholds of m and of bands 1..3
   long long p0;            // pixel index of (x0 + lane, y0 - HL): ext row ey is p0 + ey * W
   int W, L;
   int ey_lo, ey_hi;        // ext rows inside the image
@@ -128,7 +128,7 @@ template <bool RAW>
 __device__ __forceinline__ bool metric_at(const TileConst& T, int x, int y) {
   const long long p = (long long)y * T.W + x;
   if constexpr (RAW) {
-    return dsub(__ldg(T.raw + p), T.lo) >= T.x_m;
+    return __ldg(T.raw + p) >= T.x_m;
   } else {
     float a[3], g[3];
 #pragma unroll
@@ -136,7 +136,7 @@ __device__ __forceinline__ bool metric_at(const TileConst& T, int x, int y) {
       a[c] = __ldg(T.img + 3 * p + c);
       g[c] = __ldg(T.gtv + 3 * p + c);
     }
-    return dsub(raw_l1_f(a, g), T.lo) >= T.x_m;
+    return raw_l1_f(a, g) >= T.x_m;
   }
 }
 
@@ -162,7 +162,7 @@ __device__ __forceinline__ bool scan_row(const RowIn<RAW>& row, const int ey, Sc
   bool m = false;
   int band_now = 0;
   if (inb) {
-    const double xr = dsub(row_raw<RAW>(row), T.lo);
+    const double xr = row_raw<RAW>(row);   // thresholds are in the raw domain
     m = xr >= T.x_m;
     if (T.L <= 4) {
       band_now = (xr >= T.t1) + (xr >= T.t2) + (xr >= T.t3);
@@ -276,8 +276,7 @@ __device__ __forceinline__ void tile_warp_body(const TileParams& P, WarpSmem& S,
   T.cbits = P.cand_bits + (long long)v * ((hw + 31) / 32);
   T.raw = RAW ? P.raw + (long long)v * hw : nullptr;
   T.L = P.L;
-  T.lo = P.lo[v];
-  T.thr = P.thr + (long long)v * P.L;
+  T.thr = P.thr_raw + (long long)v * P.L;   // raw-domain thresholds (thresholds_kernel)
   T.x_m = T.thr[0];
   const double kInf = __longlong_as_double(0x7ff0000000000000ll);
   T.t1 = T.L > 1 ? T.thr[1] : kInf;
