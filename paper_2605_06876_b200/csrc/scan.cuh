@@ -72,42 +72,62 @@ __global__ void __launch_bounds__(kScanThreads) scan_kernel(Policy pol, long lon
   }
   __syncthreads();
   const unsigned long long thread_excl = warp_sums[wid] + incl - run;
-  if (tid == kScanThreads - 1) {
-    const unsigned long long agg = thread_excl + run;
+  __shared__ unsigned long long s_agg;
+  if (tid == kScanThreads - 1) s_agg = thread_excl + run;
+  __syncthreads();
+  // decoupled look-back by the last warp, 32 predecessors per round: each lane
+  // reads one predecessor's flag; the nearest inclusive prefix ends the walk,
+  // aggregates before it are summed with a warp reduction
+  if (wid == kScanThreads / kWarp - 1) {
+    const unsigned long long agg = s_agg;
     volatile unsigned long long* vval = st.value;
     volatile unsigned int* vflag = st.flag;
     // The aggregate and the inclusive prefix live in separate words: a reader
     // that saw flag==1 must never pick up the later inclusive value.
     if (tile == 0) {
-      vval[1] = agg;
-      __threadfence();
-      vflag[0] = 2u;
-      s_prefix = 0ull;
+      if (lane == 0) {
+        vval[1] = agg;
+        __threadfence();
+        vflag[0] = 2u;
+        s_prefix = 0ull;
+      }
     } else {
-      vval[2 * tile] = agg;
-      __threadfence();
-      vflag[tile] = 1u;
+      if (lane == 0) {
+        vval[2 * tile] = agg;
+        __threadfence();
+        vflag[tile] = 1u;
+      }
       unsigned long long acc = 0ull;
       long long p = tile - 1;
       while (true) {
+        const long long q = p - lane;
         unsigned int f;
         do {
-          f = vflag[p];
-        } while (f == 0u);
+          f = q >= 0 ? vflag[q] : 2u;
+        } while (__any_sync(0xffffffffu, f == 0u));
         __threadfence();
-        if (f == 2u) {
-          acc += vval[2 * p + 1];
-          break;
+        const unsigned incl_mask = __ballot_sync(0xffffffffu, f == 2u);
+        unsigned long long v = 0ull;
+        if (incl_mask) {
+          const int first = __ffs(incl_mask) - 1;   // nearest predecessor with an inclusive prefix
+          if (lane < first) v = vval[2 * q];
+          else if (lane == first && q >= 0) v = vval[2 * q + 1];
+        } else {
+          v = vval[2 * q];
         }
-        acc += vval[2 * p];
-        --p;
+        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        acc += v;
+        if (incl_mask) break;
+        p -= 32;
       }
-      vval[2 * tile + 1] = acc + agg;
-      __threadfence();
-      vflag[tile] = 2u;
-      s_prefix = acc;
+      if (lane == 0) {
+        vval[2 * tile + 1] = acc + agg;
+        __threadfence();
+        vflag[tile] = 2u;
+        s_prefix = acc;
+      }
     }
-    if (base + kScanTile >= n) pol.total(s_prefix + agg);
+    if (lane == 0 && base + kScanTile >= n) pol.total(s_prefix + agg);
   }
   __syncthreads();
   unsigned long long e = s_prefix + thread_excl;
