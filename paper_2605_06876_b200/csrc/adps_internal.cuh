@@ -107,6 +107,9 @@ struct Counters {
   unsigned long long shard_lo, shard_hi;     // this rank's candidate range under parent sharding
   unsigned long long shard_plo, shard_phi;   // ... and its proposal range
   unsigned long long n_owned_props;          // proposals of this rank's parents   // diagnostics (ADPS_MERGE_STATS builds)
+  unsigned long long n_mid_groups, n_huge_groups;   // work lists of the group reduction
+  unsigned long long n_cap_large;                   // groups of parents with many groups
+  unsigned long long n_cap_huge;                    // parents whose groups are selected in shared memory
   unsigned int normals_status;           // bit0 near-tie (redraw on host), bit1 window short
   unsigned int degenerate;
   unsigned int overflow;   // bit0 regions, bit1 partials

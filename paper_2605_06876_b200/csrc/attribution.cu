@@ -630,6 +630,7 @@ static TileParams tile_params(const AttributionArgs& a) {
   P.n_views = a.V;
   P.cand_bits = a.cand_bits;
   P.raw = a.raw;
+  P.words = a.words;
   P.deferred = a.deferred;
   P.n_deferred = a.n_deferred;
   return P;
@@ -638,12 +639,13 @@ static TileParams tile_params(const AttributionArgs& a) {
 bool attribution_warp_path(const AttributionArgs& a) {
   // the warp kernel covers r_erode <= 3 without debug maps; the block kernel
   // takes everything else and the tiles the warp kernel defers
-  return a.tile_path == 0 && !a.dbg_m && a.r_erode <= 3 && a.deferred && a.n_deferred;
+  return a.tile_path != 1 && !a.dbg_m && a.r_erode <= 3 && a.deferred && a.n_deferred;
 }
 
 cudaError_t launch_tiles_views(const AttributionArgs& a, int v0, int v1, cudaStream_t s) {
   if (!attribution_warp_path(a) || v1 <= v0) return cudaSuccess;
   const TileParams P = tile_params(a);
+  if (P.words && P.raw) return launch_tile_bits(P, v0, v1, s);
   const long long tpv = (long long)P.tiles_x * P.tiles_y;
   return launch_tile_warp(P, tpv * v0, tpv * v1, s);
 }
@@ -656,7 +658,7 @@ cudaError_t launch_attribution_tail(const AttributionArgs& a, cudaStream_t s, Ma
   if (e != cudaSuccess) return e;
   if (attribution_warp_path(a)) {
     tile_kernel<<<a.grid_small, kTileThreads, smem, s>>>(P, a.deferred, a.n_deferred);
-    if (mark) mark(ctx, "tile_ccl", s, 2);
+    if (mark) mark(ctx, "tile_ccl", s, a.words && a.raw ? 3 : 2);
   } else {
     tile_kernel<<<(unsigned)nblocks, kTileThreads, smem, s>>>(P, nullptr, nullptr);
     if (mark) mark(ctx, "tile_ccl", s, 1);

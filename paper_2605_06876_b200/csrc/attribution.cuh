@@ -34,6 +34,7 @@ struct TileParams {
   unsigned long long* n_deferred;
   const unsigned* cand_bits;         // [V][ceil(H*W/32)]: bit p = D[p] is a split candidate
   const double* raw;                 // [V][H*W] raw L1 error cached by the minmax pass, or null
+  uint4* words;                      // [V][H][ceil(W/32)] bit planes (m, cand, band0, band1), or null
 };
 
 struct BorderParams {
@@ -72,14 +73,19 @@ struct AttributionArgs {
   unsigned grid_small;
   int* deferred;                     // [n_tiles]
   unsigned long long* n_deferred;
-  int tile_path;                     // 0 auto (warp kernel + deferred), 1 block kernel only
+  int tile_path;                     // 0 auto (warp kernel + deferred), 1 block kernel only,
+                                     // 2 warp kernel on the raw cache without bit planes
   unsigned* cand_bits;               // [V][ceil(H*W/32)], written by the minmax pass
   double* raw;                       // [V][H*W] raw L1 error written by the minmax pass, or null
+  uint4* words;                      // [V][H][ceil(W/32)] bit planes for tile_bits_kernel, or null
 };
 
 // warp-per-tile scanline CCL (r_erode <= 3) over tiles [t0, t1); defers tiles with > kWarpMaxRuns runs
 cudaError_t launch_tile_warp(const TileParams& P, long long t0, long long t1, cudaStream_t s);
 size_t tile_warp_smem_bytes();
+// bit-plane path (raw cache, l_bands <= 4, r_erode <= 3): words pass + tile_bits_kernel over views [v0, v1)
+cudaError_t launch_tile_bits(const TileParams& P, int v0, int v1, cudaStream_t s);
+size_t tile_words_bytes(int V, int H, int W);
 
 size_t tile_smem_bytes();
 // minmax + ever-dominant flags + thresholds + fallback count (phase-1 begin)

@@ -650,6 +650,7 @@ struct GroupStartPolicy {
 };
 
 constexpr int kSmallGroup = 8;
+constexpr int kBlockGroup = 512;   // larger groups: a block per group
 
 // groups of up to kSmallGroup members: one thread per group, members summed in
 // ascending index order; also writes the sort padding beyond the group count
@@ -657,14 +658,18 @@ __global__ void group_small_kernel(MergeArgs a, long long cap) {
   const long long G = (long long)a.ctr->n_groups_all;
   for (long long g = (long long)blockIdx.x * blockDim.x + threadIdx.x; g < cap;
        g += (long long)gridDim.x * blockDim.x) {
-    if (g >= G) {
-      a.ext_key[g] = ~0ull;
-      a.ext_val[g] = (int)g;
-      continue;
-    }
+    if (g >= G) continue;
     const int b = a.grp_first[g], e = a.grp_first[g + 1];
     const int cnt = e - b;
-    if (cnt > kSmallGroup) continue;
+    {   // groups of a candidate are contiguous: mark the first one
+      const int k = a.pcand[a.gkey_sorted[b]];
+      if (g == 0 || a.pcand[a.gkey_sorted[a.grp_first[g - 1]]] != k) a.gfirst_of[k] = (int)g;
+    }
+    if (cnt > kSmallGroup) {   // work lists for the warp / block reductions
+      if (cnt > kBlockGroup) a.glist[cap + atomicAdd(&a.ctr->n_huge_groups, 1ull)] = (int)g;
+      else a.glist[atomicAdd(&a.ctr->n_mid_groups, 1ull)] = (int)g;
+      continue;
+    }
     double acc[12] = {0};
     for (int m = b; m < e; ++m) {
       const Proposal& M = a.props_s[a.gval_sorted[m]];
@@ -698,9 +703,10 @@ __global__ void group_small_kernel(MergeArgs a, long long cap) {
     }
     R.extent = ext;
     a.groups[g] = R;
-    a.ext_key[g] = ~(unsigned long long)__double_as_longlong(ext);   // descending extent
-    a.ext_val[g] = (int)g;
-    atomicAdd(&a.n_groups[a.pcand[a.gkey_sorted[b]]], 1);
+    const int k = a.pcand[a.gkey_sorted[b]];
+    a.gpar[g] = k;
+    a.gext[g] = ext;
+    atomicAdd(&a.n_groups[k], 1);
   }
 }
 
@@ -708,11 +714,11 @@ __global__ void group_small_kernel(MergeArgs a, long long cap) {
 __global__ void group_kernel(MergeArgs a, long long cap) {
   const int lane = threadIdx.x & 31;
   const long long warps = (long long)gridDim.x * (blockDim.x >> 5);
-  const long long G = (long long)a.ctr->n_groups_all;
-  for (long long g = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); g < G; g += warps) {
+  const long long nl = (long long)a.ctr->n_mid_groups;
+  for (long long i = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); i < nl; i += warps) {
+    const long long g = a.glist[i];
     const int b = a.grp_first[g], e = a.grp_first[g + 1];
     const int cnt = e - b;
-    if (cnt <= kSmallGroup) continue;
     double acc[12] = {0};
     for (int m = b + lane; m < e; m += 32) {
       const Proposal& M = a.props_s[a.gval_sorted[m]];
@@ -751,10 +757,83 @@ __global__ void group_kernel(MergeArgs a, long long cap) {
     R.extent = ext;
     if (lane == 0) {
       a.groups[g] = R;
-      a.ext_key[g] = ~(unsigned long long)__double_as_longlong(ext);   // descending extent
-      a.ext_val[g] = (int)g;
-      atomicAdd(&a.n_groups[a.pcand[a.gkey_sorted[b]]], 1);
+      const int k = a.pcand[a.gkey_sorted[b]];
+      a.gpar[g] = k;
+      a.gext[g] = ext;
+      atomicAdd(&a.n_groups[k], 1);
     }
+  }
+}
+
+
+// the largest groups (a background Gaussian's proposals): a block per group,
+// thread-strided sums, fixed-order warp + block trees (deterministic)
+__global__ void __launch_bounds__(256) group_block_kernel(MergeArgs a, long long cap) {
+  __shared__ double red[8][12];
+  __shared__ double bc[12];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const long long nl = (long long)a.ctr->n_huge_groups;
+  for (long long i = blockIdx.x; i < nl; i += gridDim.x) {
+    const long long g = a.glist[cap + i];
+    const int b = a.grp_first[g], e = a.grp_first[g + 1];
+    const int cnt = e - b;
+    double acc[12] = {0};
+    for (int m = b + threadIdx.x; m < e; m += 256) {
+      const Proposal& M = a.props_s[a.gval_sorted[m]];
+      for (int t = 0; t < 3; ++t) {
+        acc[t] += M.mu[t];
+        acc[3 + t] += M.rgb[t];
+      }
+      for (int t = 0; t < 6; ++t) acc[6 + t] += M.cov[t];
+    }
+    for (int t = 0; t < 12; ++t)
+      for (int o = 16; o > 0; o >>= 1) acc[t] += __shfl_xor_sync(0xffffffffu, acc[t], o);
+    if (lane == 0)
+      for (int t = 0; t < 12; ++t) red[wid][t] = acc[t];
+    __syncthreads();
+    if (threadIdx.x < 12) {
+      double v = 0.0;
+      for (int w = 0; w < 8; ++w) v += red[w][threadIdx.x];
+      bc[threadIdx.x] = v;
+    }
+    __syncthreads();
+    GroupRec R;
+    for (int t = 0; t < 3; ++t) {
+      R.mu[t] = bc[t] / cnt;
+      R.rgb[t] = bc[3 + t] / cnt;
+    }
+    double mcov[6];
+    for (int t = 0; t < 6; ++t) mcov[t] = bc[6 + t] / cnt;
+    double lam0[3];
+    sym_eig3(mcov, lam0, R.evec);
+    double ext = 0.0;
+    for (int r = 0; r < 3; ++r) {
+      const double ev[3] = {R.evec[r], R.evec[3 + r], R.evec[6 + r]};
+      double best = 0.0;
+      for (int m = b + threadIdx.x; m < e; m += 256) {
+        const Proposal& M = a.props_s[a.gval_sorted[m]];
+        const double off = fabs((M.mu[0] - R.mu[0]) * ev[0] + (M.mu[1] - R.mu[1]) * ev[1] +
+                                (M.mu[2] - R.mu[2]) * ev[2]);
+        best = fmax(best, off + sqrt(sym_quad(M.cov, ev)));
+      }
+      for (int o = 16; o > 0; o >>= 1) best = fmax(best, __shfl_xor_sync(0xffffffffu, best, o));
+      __syncthreads();
+      if (lane == 0) red[wid][0] = best;
+      __syncthreads();
+      best = 0.0;
+      for (int w = 0; w < 8; ++w) best = fmax(best, red[w][0]);
+      R.lam[r] = best * best;
+      ext = fmax(ext, R.lam[r]);
+    }
+    if (threadIdx.x == 0) {
+      R.extent = ext;
+      a.groups[g] = R;
+      const int k = a.pcand[a.gkey_sorted[b]];
+      a.gpar[g] = k;
+      a.gext[g] = ext;
+      atomicAdd(&a.n_groups[k], 1);
+    }
+    __syncthreads();
   }
 }
 
@@ -764,59 +843,267 @@ cudaError_t launch_merge_groups(const MergeArgs& a, long long cap, ScanState st,
   long long b = (cap + 127) / 128;
   group_small_kernel<<<(unsigned)(b < 1 ? 1 : (b > 65535 ? 65535 : b)), 128, 0, s>>>(a, cap);
   group_kernel<<<a.grid, 256, 0, s>>>(a, cap);
+  group_block_kernel<<<a.grid, 256, 0, s>>>(a, cap);
   return cudaGetLastError();
 }
 
 // --------------------------------------------------------------------- cap
-__global__ void cand_key_kernel(MergeArgs a, long long cap) {
-  const long long G = (long long)a.ctr->n_groups_all;
-  for (long long s = (long long)blockIdx.x * blockDim.x + threadIdx.x; s < cap;
-       s += (long long)gridDim.x * blockDim.x) {
-    const int gid = a.ext_val_sorted[s];
-    a.cand_val[s] = gid;
-    a.cand_key[s] = gid < G ? (unsigned)a.pcand[a.gkey_sorted[a.grp_first[gid]]] : 0xffffffffu;
+// cap_children (ref/cross_view_merge.py:110-116): a stable sort of a parent's
+// groups by -extent keeps the first min(n_max, #groups).  The groups of a
+// parent are contiguous in g (roots ascend with the proposal index, which is
+// in parent order) and in the reference's group order, so a group's rank is
+// the number of its parent's groups with a larger extent, or an equal extent
+// and a smaller g -- no sort needed.  Parents with few groups: a thread per
+// group; many groups: a warp per group counting 32 at a time (early exit at
+// n_max).
+
+constexpr int kCapThreadMax = 64;
+constexpr int kSelMax = 1024;   // n_max up to this: block top-n_max selection per parent
+constexpr int kSelHuge = 4096;  // parents with more groups: extents staged in shared memory
+constexpr int kSelSmemKeys = 49152;   // high 32 bits of the extent bits, 4 B each
+
+__device__ __forceinline__ void cap_write(const MergeArgs& a, long long g, int k, int Gk, int rank) {
+  const int gi = a.split_list[k];
+  const float ocl = (float)fmin(fmax((double)a.opacity[gi], 1e-6), 1.0 - 1e-6);
+  write_child(a.groups[g], ocl, a.children + 14ll * (a.pstart[k] + rank));
+  if (rank == 0) {
+    const int ni = Gk < a.n_max ? Gk : a.n_max;
+    a.cand_merged[k] = ni;
+    a.cand_ins[k] = ni + 1;
+    atomicAdd(&a.ctr->merge_edges, (unsigned long long)(a.cand_nvalid[k] - Gk));
+    atomicAdd(&a.ctr->n_children, (unsigned long long)ni);
   }
 }
 
-// position s of the (parent, -extent, root)-ordered group list -> child rank s - first
-__global__ void cap_emit_kernel(MergeArgs a) {
+__global__ void cap_small_kernel(MergeArgs a, long long cap) {
   const long long G = (long long)a.ctr->n_groups_all;
-  for (long long s = (long long)blockIdx.x * blockDim.x + threadIdx.x; s < G;
-       s += (long long)gridDim.x * blockDim.x) {
-    const unsigned k = a.cand_key_sorted[s];
-    // first position of this parent: groups of a parent are contiguous and
-    // number n_groups[k]; walk back at most n_max steps to find the rank
-    long long first = s;
-    int steps = 0;
-    while (first > 0 && a.cand_key_sorted[first - 1] == k && steps <= a.n_max) {
-      --first;
-      ++steps;
+  for (long long g = (long long)blockIdx.x * blockDim.x + threadIdx.x; g < G;
+       g += (long long)gridDim.x * blockDim.x) {
+    const int k = a.gpar[g];
+    const int Gk = a.n_groups[k];
+    if (Gk > kCapThreadMax) {
+      if (a.n_max <= kSelMax) {   // one entry per parent for the block selection
+        if (g == a.gfirst_of[k]) {
+          if (Gk > kSelHuge) a.glist[2 * cap - 1 - (long long)atomicAdd(&a.ctr->n_cap_huge, 1ull)] = k;
+          else a.glist[2 * cap + atomicAdd(&a.ctr->n_cap_large, 1ull)] = k;
+        }
+      } else {                    // one entry per group for the block-per-group ranks
+        a.glist[2 * cap + atomicAdd(&a.ctr->n_cap_large, 1ull)] = (int)g;
+      }
+      continue;
     }
-    const long long rank = s - first;
-    if (rank >= a.n_max) continue;
-    const int gi = a.split_list[k];
-    const float ocl = (float)fmin(fmax((double)a.opacity[gi], 1e-6), 1.0 - 1e-6);
-    write_child(a.groups[a.cand_val_sorted[s]], ocl, a.children + 14ll * (a.pstart[k] + rank));
-    if (rank == 0) {
-      const int Gk = a.n_groups[k];
-      const int ni = Gk < a.n_max ? Gk : a.n_max;
-      a.cand_merged[k] = ni;
-      a.cand_ins[k] = ni + 1;
-      atomicAdd(&a.ctr->merge_edges, (unsigned long long)(a.cand_nvalid[k] - Gk));
-      atomicAdd(&a.ctr->n_children, (unsigned long long)ni);
+    const long long f = a.gfirst_of[k];
+    const double e = a.gext[g];
+    int rank = 0;
+    for (long long h = f; h < f + Gk && rank < a.n_max; ++h) {
+      const double eh = a.gext[h];
+      rank += (eh > e) || (eh == e && h < g);
     }
+    if (rank < a.n_max) cap_write(a, g, k, Gk, rank);
+  }
+}
+
+__global__ void __launch_bounds__(256) cap_large_kernel(MergeArgs a, long long cap) {
+  // a block per group of a parent with many groups: 1024 extents per round
+  __shared__ int part[8];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const long long nl = (long long)a.ctr->n_cap_large;
+  for (long long i = blockIdx.x; i < nl; i += gridDim.x) {
+    const long long g = a.glist[2 * cap + i];
+    const int k = a.gpar[g];
+    const int Gk = a.n_groups[k];
+    const long long f = a.gfirst_of[k];
+    const double e = a.gext[g];
+    int rank = 0;
+    constexpr int U = 4;
+    for (long long h0 = f; h0 < f + Gk && rank < a.n_max; h0 += 256 * U) {
+      double eh[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const long long h = h0 + 256 * u + threadIdx.x;
+        eh[u] = h < f + Gk ? __ldg(a.gext + h) : -1.0;
+      }
+      int c = 0;
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const long long h = h0 + 256 * u + threadIdx.x;
+        c += (eh[u] > e) || (eh[u] == e && h < g);
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+      if (lane == 0) part[wid] = c;
+      __syncthreads();
+      int t = 0;
+#pragma unroll
+      for (int w = 0; w < 8; ++w) t += part[w];
+      rank += t;
+      __syncthreads();
+    }
+    if (threadIdx.x == 0 && rank < a.n_max) cap_write(a, g, k, Gk, rank);
+  }
+}
+
+
+// a block per parent with many groups (n_max <= kSelMax): radix-select the
+// n_max-th largest extent over the parent's groups (8-bit digits of the
+// extent's bit pattern, which orders non-negative doubles; stops as soon as
+// the selected digit bin holds exactly the groups still needed), collect the
+// kept groups (ties at the threshold in group order), rank them among
+// themselves by (-extent, group order) and write their children.
+template <bool HUGE>
+__global__ void __launch_bounds__(HUGE ? 1024 : 256) cap_select_kernel(MergeArgs a, long long cap) {
+  constexpr int NT = HUGE ? 1024 : 256;   // threads
+  constexpr int NW = NT / 32;
+  constexpr int J = 8;            // consecutive groups per thread per round
+  extern __shared__ __align__(16) unsigned skeys_hi[];
+  constexpr int RND = NT * J;    // groups per round
+  __shared__ unsigned hist[256];
+  __shared__ unsigned long long s_prefix, s_mask;
+  __shared__ int s_need, s_done, s_nkeep, s_tie_base;
+  __shared__ int keep_g[kSelMax];
+  __shared__ int wtot[NW];
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const long long nl = HUGE ? (long long)a.ctr->n_cap_huge : (long long)a.ctr->n_cap_large;
+  for (long long i = blockIdx.x; i < nl; i += gridDim.x) {
+    const int k = HUGE ? a.glist[2 * cap - 1 - i] : a.glist[2 * cap + i];
+    const int Gk = a.n_groups[k];
+    const long long f0 = a.gfirst_of[k];
+    // the keys: global (index f0 + h); for a huge parent the high 32 bits are
+    // staged in shared memory and the low bits read only when the high bits
+    // tie with the selected prefix
+    const unsigned long long* key = reinterpret_cast<const unsigned long long*>(a.gext) + f0;
+    const bool staged = HUGE && Gk <= kSelSmemKeys;
+    if (staged) {
+      for (int h = tid; h < Gk; h += NT) skeys_hi[h] = (unsigned)(__ldg(key + h) >> 32);
+      __syncthreads();
+    }
+    const long long f = 0, fe = Gk;
+    // key of group h as far as the mask `m` (selected digits) can see it
+    auto key_at = [&](long long h, unsigned long long m, unsigned long long p) -> unsigned long long {
+      if (!staged) return __ldg(key + h);
+      const unsigned hi = skeys_hi[h];
+      unsigned long long kv = (unsigned long long)hi << 32;
+      if ((m & 0xffffffffull) && (hi & (unsigned)(m >> 32)) == (unsigned)(p >> 32)) kv = __ldg(key + h);
+      return kv;
+    };
+    if (tid == 0) {
+      s_prefix = 0ull;
+      s_mask = 0ull;
+      s_need = a.n_max < Gk ? a.n_max : Gk;
+      s_done = Gk <= a.n_max;   // every group is kept
+      s_nkeep = 0;
+      s_tie_base = 0;
+    }
+    __syncthreads();
+    for (int shift = 56; shift >= 0 && !s_done; shift -= 8) {
+      if (tid < 256) hist[tid] = 0u;
+      __syncthreads();
+      const unsigned long long pre = s_prefix, msk = s_mask;
+      for (long long h0 = f; h0 < fe; h0 += RND) {   // block-uniform trip count
+        unsigned long long kv[J];
+#pragma unroll
+        for (int j = 0; j < J; ++j) {
+          const long long h = h0 + (long long)j * NT + tid;
+          kv[j] = h < fe ? key_at(h, msk | (255ull << shift), pre) : 0ull;
+        }
+#pragma unroll
+        for (int j = 0; j < J; ++j) {
+          const long long h = h0 + (long long)j * NT + tid;
+          const bool hit = h < fe && (kv[j] & msk) == pre;
+          // extents cluster in few bins: one shared atomic per distinct bin per warp
+          const unsigned bin = hit ? (unsigned)((kv[j] >> shift) & 255u) : 256u;
+          const unsigned peers = __match_any_sync(0xffffffffu, bin);
+          if (hit && lane == __ffs(peers) - 1) atomicAdd(&hist[bin], (unsigned)__popc(peers));
+        }
+      }
+      __syncthreads();
+      if (tid == 0) {
+        int need = s_need;
+        int b = 255;
+        for (; b > 0; --b) {
+          if ((int)hist[b] >= need) break;
+          need -= (int)hist[b];
+        }
+        s_need = need;   // still needed from bin b
+        s_prefix = pre | ((unsigned long long)b << shift);
+        s_mask = msk | (255ull << shift);
+        if ((int)hist[b] == need || shift == 0) s_done = 1;
+      }
+      __syncthreads();
+    }
+    // kept: keys above the selected prefix range, and from inside it the first
+    // s_need in group order (all of it when the bin held exactly s_need)
+    const bool all = Gk <= a.n_max;
+    const unsigned long long pre = s_prefix, msk = s_mask;
+    const int need = s_need;
+    for (long long h0 = f; h0 < fe; h0 += RND) {
+      // thread tid owns groups [h0 + tid*J, +J): group order = (tid, j)
+      const long long hb = h0 + (long long)tid * J;
+      unsigned long long kv[J];
+#pragma unroll
+      for (int j = 0; j < J; ++j) kv[j] = hb + j < fe ? key_at(hb + j, msk, pre) : 0ull;
+      unsigned above = 0u, in = 0u;
+#pragma unroll
+      for (int j = 0; j < J; ++j) {
+        if (hb + j < fe) {
+          if (all || (kv[j] & msk) > pre) above |= 1u << j;
+          else if ((kv[j] & msk) == pre) in |= 1u << j;
+        }
+      }
+      // exclusive prefix of the in-range counts over threads (group order)
+      const int cnt = __popc(in);
+      int x = cnt;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int t = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += t;
+      }
+      if (lane == 31) wtot[wid] = x;
+      __syncthreads();
+      int before = x - cnt, tot = 0;
+      for (int w = 0; w < NW; ++w) {
+        if (w < wid) before += wtot[w];
+        tot += wtot[w];
+      }
+      int tr = s_tie_base + before;
+      for (int j = 0; j < J; ++j) {
+        const bool is_in = (in >> j) & 1u;
+        if (((above >> j) & 1u) || (is_in && tr < need)) keep_g[atomicAdd(&s_nkeep, 1)] = (int)(f0 + hb + j);
+        tr += is_in;
+      }
+      __syncthreads();
+      if (tid == 0) s_tie_base += tot;
+      __syncthreads();
+    }
+    // rank among the kept by (-extent, group order) and write
+    const int nk = s_nkeep;
+    for (int q = tid; q < nk; q += NT) {
+      const long long g = keep_g[q];
+      const double e = a.gext[g];
+      int rank = 0;
+      for (int j = 0; j < nk; ++j) {
+        const long long h = keep_g[j];
+        const double eh = a.gext[h];
+        rank += (eh > e) || (eh == e && h < g);
+      }
+      cap_write(a, g, k, Gk, rank);
+    }
+    __syncthreads();
   }
 }
 
 cudaError_t launch_merge_cap(const MergeArgs& a, long long cap, cudaStream_t s) {
   long long b = (cap + 255) / 256;
-  cand_key_kernel<<<(unsigned)(b < 1 ? 1 : (b > 65535 ? 65535 : b)), 256, 0, s>>>(a, cap);
-  return cudaGetLastError();
-}
-
-cudaError_t launch_merge_emit(const MergeArgs& a, long long cap, cudaStream_t s) {
-  long long b = (cap + 255) / 256;
-  cap_emit_kernel<<<(unsigned)(b < 1 ? 1 : (b > 65535 ? 65535 : b)), 256, 0, s>>>(a);
+  cap_small_kernel<<<(unsigned)(b < 1 ? 1 : (b > 65535 ? 65535 : b)), 256, 0, s>>>(a, cap);
+  if (a.n_max <= kSelMax) {
+    cap_select_kernel<false><<<a.grid, 256, 0, s>>>(a, cap);
+    const int smem = kSelSmemKeys * 4;
+    cudaError_t e = cudaFuncSetAttribute(cap_select_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return e;
+    cap_select_kernel<true><<<16, 1024, smem, s>>>(a, cap);
+  } else {
+    cap_large_kernel<<<a.grid * 4, 256, 0, s>>>(a, cap);
+  }
   return cudaGetLastError();
 }
 

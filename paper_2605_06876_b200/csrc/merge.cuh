@@ -43,14 +43,11 @@ struct MergeArgs {
   // groups
   int* grp_first;                          // [cap] first sorted position of group g
   GroupRec* groups;                        // [cap]
-  unsigned long long* ext_key;             // [cap] ~extent bits (descending), padding ~0
-  int* ext_val;                            // [cap] group id
-  unsigned long long* ext_key_sorted;
-  int* ext_val_sorted;
-  unsigned* cand_key;                      // [cap] candidate rank of group, padding UINT_MAX
-  int* cand_val;                           // [cap] group id (in extent order)
-  unsigned* cand_key_sorted;
-  int* cand_val_sorted;
+  int* gpar;                               // [cap] candidate rank of group g (groups of a
+                                           // candidate are contiguous, in root order)
+  double* gext;                            // [cap] extent of group g (compact, for the cap)
+  int* gfirst_of;                          // [n_split] first group of candidate k
+  int* glist;                              // [3 cap] groups with > 8 / > 512 members; cap list
   // per candidate
   int* pstart;                             // [n_split]
   int* n_groups;                           // [n_split]
@@ -103,7 +100,8 @@ cudaError_t launch_merge_morton(const MergeArgs& a, long long cap, cudaStream_t 
 cudaError_t launch_merge_tile_gates(const MergeArgs& a, cudaStream_t s);
 cudaError_t launch_merge_flatten(const MergeArgs& a, long long cap, cudaStream_t s);
 cudaError_t launch_merge_groups(const MergeArgs& a, long long cap, ScanState st, cudaStream_t s);
+// cap (ref/cross_view_merge.py:110-116): rank of each group among its parent's
+// groups by (-extent, group order); ranks < n_max become children in rank order
 cudaError_t launch_merge_cap(const MergeArgs& a, long long cap, cudaStream_t s);
-cudaError_t launch_merge_emit(const MergeArgs& a, long long cap, cudaStream_t s);
 
 }  // namespace adps

@@ -89,13 +89,12 @@ struct adps_plan {
   Buf lohi, lo, thr, thr_raw, cams;
   // tiles / fragments / regions
   Buf border, partials, partial_parent, regions, props, valid, keys, vals, keys_sorted, vals_sorted;
-  Buf idx, uf, groups, children, dbg_stats, dbg_child, deferred, cand_bits, rawc;
+  Buf idx, uf, groups, children, dbg_stats, dbg_child, deferred, cand_bits, rawc, twords;
   // device normals (numpy PCG64 stream)
   Buf nrm_val, nrm_len, nrm_acc, nrm_reach, nrm_rmax, nrm_walked, nrm_idx, nrm_tmp;
   // merge / cap scratch (proposal space)
   Buf small_list, pstart, n_groups, work_cnt, work_off, props_s, pcand, gkey, gval, gkey_sorted, gval_sorted,
-      grp_first, ext_key, ext_val, ext_key_sorted, ext_val_sorted, cand_key, cand_val, cand_key_sorted,
-      cand_val_sorted, scan3_val, scan3_flag, scan3_ticket, large_of, lp_cnt, lp_off, tile_cnt, tile_off, mkey,
+      grp_first, gpar, gext, gfirst_of, glist, scan3_val, scan3_flag, scan3_ticket, large_of, lp_cnt, lp_off, tile_cnt, tile_off, mkey,
       mval, mkey_sorted, mval_sorted, boxes, tile_pairs, gsoa;
   Buf scan_val, scan_flag, scan_ticket, scan2_val, scan2_flag, scan2_ticket, cub_tmp;
   Buf ctr;
@@ -150,7 +149,9 @@ struct adps_plan {
   bool have_merge_part = false;
   long long shard_k[2] = {0, 0}, shard_p[2] = {0, 0};   // this rank's candidate / proposal range
   bool have_local = false;
-  int tile_path = 0;   // 0 warp CCL + deferred block CCL, 1 block CCL only
+  int tile_path = 0;   // 0 warp CCL (bit planes when l_bands <= 4) + deferred block CCL, 1 block CCL only,
+                       // 2 warp CCL on the raw cache without bit planes
+  bool use_words = false;
   int raw_cache = ADPS_RAW_CACHE_DEFAULT;   // minmax pass caches the raw L1 error for the warp CCL
   bool use_raw = false;                     // decided per phase 1
   // arguments saved by phase1_begin for phase1_end
@@ -265,10 +266,9 @@ extern "C" adps_status adps_plan_destroy(adps_plan* P) {
                  &P->r_offs, &P->r_dup, &P->r_dup_sorted, &P->r_tstart, &P->r_tend, &P->r_total,
                  &P->r_cams, &P->small_list, &P->pstart, &P->n_groups, &P->work_cnt, &P->work_off,
                  &P->props_s, &P->pcand, &P->gkey, &P->gval, &P->gkey_sorted, &P->gval_sorted, &P->grp_first,
-                 &P->ext_key, &P->ext_val, &P->ext_key_sorted, &P->ext_val_sorted, &P->cand_key, &P->cand_val,
-                 &P->cand_key_sorted, &P->cand_val_sorted, &P->scan3_val, &P->scan3_flag, &P->scan3_ticket,
+                 &P->gpar, &P->gext, &P->gfirst_of, &P->glist, &P->scan3_val, &P->scan3_flag, &P->scan3_ticket,
                  &P->large_of, &P->lp_cnt, &P->lp_off, &P->tile_cnt, &P->tile_off, &P->mkey, &P->mval,
-                 &P->mkey_sorted, &P->mval_sorted, &P->boxes, &P->tile_pairs, &P->gsoa, &P->deferred, &P->cand_bits, &P->rawc,
+                 &P->mkey_sorted, &P->mval_sorted, &P->boxes, &P->tile_pairs, &P->gsoa, &P->deferred, &P->cand_bits, &P->rawc, &P->twords,
                  &P->nrm_val, &P->nrm_len, &P->nrm_acc, &P->nrm_reach, &P->nrm_rmax, &P->nrm_walked,
                  &P->nrm_idx, &P->nrm_tmp};
   for (Buf* b : bufs)
@@ -483,6 +483,7 @@ static AttributionArgs attr_args(adps_plan* P, int V, int H, int W, const adps_c
   a.tile_path = P->tile_path;
   a.cand_bits = P->cand_bits.as<unsigned>();
   a.raw = P->use_raw ? P->rawc.as<double>() : nullptr;
+  a.words = P->use_words ? P->twords.as<uint4>() : nullptr;
   return a;
 }
 
@@ -566,8 +567,10 @@ extern "C" adps_status adps_step_phase1_begin(adps_plan* P, void* stream_v, cons
   CK(ensure(P->border, 4ll * n_tiles * kBorderSlots));
   CK(ensure(P->deferred, 4ll * n_tiles));
   CK(ensure(P->cand_bits, 4ll * V * ((hw + 31) / 32)));
-  P->use_raw = P->raw_cache && P->tile_path == 0 && !P->dbg_m && cfg->r_erode <= 3;
+  P->use_raw = P->raw_cache && P->tile_path != 1 && !P->dbg_m && cfg->r_erode <= 3;
   if (P->use_raw) CK(ensure(P->rawc, 8ll * total_px));
+  P->use_words = P->use_raw && P->tile_path == 0 && cfg->l_bands <= 4;
+  if (P->use_words) CK(ensure(P->twords, (long long)tile_words_bytes(V, H, W)));
   CK(ensure(P->ctr, sizeof(Counters)));
   if (P->cams_host_cap < V) {
     if (P->cams_host) cudaFreeHost(P->cams_host);
@@ -643,7 +646,7 @@ extern "C" adps_status adps_step_phase1_begin(adps_plan* P, void* stream_v, cons
       CK(launch_attribution_tail(a, P->aux, nullptr, nullptr));
       CK(cudaEventRecord(P->ev_attr, P->aux));
       P->attr_pending = true;
-      P->launches += 3 * chunks + 1 + 4;
+      P->launches += (P->use_words ? 4 : 3) * chunks + 1 + 4;
     } else {
       CK(launch_minmax(a, P->split_list.as<int>(), ctr, P->sm_count, s));
       P->launches += 3;
@@ -834,6 +837,7 @@ static adps_status phase1_merge_part(adps_plan* P, cudaStream_t s) {
   CK(ensure(P->small_list, 4 * sc));
   CK(ensure(P->pstart, 4 * sc));
   CK(ensure(P->n_groups, 4 * sc));
+  CK(ensure(P->gfirst_of, 4 * sc));
   CK(ensure(P->work_cnt, 8 * sc));
   CK(ensure(P->work_off, 8 * (sc + 1)));
   CK(ensure(P->props_s, sizeof(Proposal) * rc));
@@ -843,14 +847,9 @@ static adps_status phase1_merge_part(adps_plan* P, cudaStream_t s) {
   CK(ensure(P->gkey_sorted, 4 * rc));
   CK(ensure(P->gval_sorted, 4 * rc));
   CK(ensure(P->grp_first, 4 * (rc + 1)));
-  CK(ensure(P->ext_key, 8 * rc));
-  CK(ensure(P->ext_val, 4 * rc));
-  CK(ensure(P->ext_key_sorted, 8 * rc));
-  CK(ensure(P->ext_val_sorted, 4 * rc));
-  CK(ensure(P->cand_key, 4 * rc));
-  CK(ensure(P->cand_val, 4 * rc));
-  CK(ensure(P->cand_key_sorted, 4 * rc));
-  CK(ensure(P->cand_val_sorted, 4 * rc));
+  CK(ensure(P->gpar, 4 * rc));
+  CK(ensure(P->gext, 8 * rc));
+  CK(ensure(P->glist, 12 * rc));
   CK(ensure(P->large_of, 4 * sc));
   CK(ensure(P->lp_cnt, 8 * sc));
   CK(ensure(P->lp_off, 8 * (sc + 1)));
@@ -920,14 +919,10 @@ static adps_status phase1_merge_part(adps_plan* P, cudaStream_t s) {
   ma.gval_sorted = P->gval_sorted.as<int>();
   ma.grp_first = P->grp_first.as<int>();
   ma.groups = P->groups.as<GroupRec>();
-  ma.ext_key = P->ext_key.as<unsigned long long>();
-  ma.ext_val = P->ext_val.as<int>();
-  ma.ext_key_sorted = P->ext_key_sorted.as<unsigned long long>();
-  ma.ext_val_sorted = P->ext_val_sorted.as<int>();
-  ma.cand_key = P->cand_key.as<unsigned>();
-  ma.cand_val = P->cand_val.as<int>();
-  ma.cand_key_sorted = P->cand_key_sorted.as<unsigned>();
-  ma.cand_val_sorted = P->cand_val_sorted.as<int>();
+  ma.gpar = P->gpar.as<int>();
+  ma.gext = P->gext.as<double>();
+  ma.gfirst_of = P->gfirst_of.as<int>();
+  ma.glist = P->glist.as<int>();
   ma.pstart = P->pstart.as<int>();
   ma.n_groups = P->n_groups.as<int>();
   ma.cand_case = P->cand_case.as<int>();
@@ -1005,13 +1000,9 @@ static adps_status phase1_merge_part(adps_plan* P, cudaStream_t s) {
       const int gbits = ceil_log2((unsigned long long)rc + 2);
       CK(cub_sort_pairs(P, ma.gkey, ma.gkey_sorted, ma.gval, ma.gval_sorted, rc, gbits, s));
       CK(launch_merge_groups(ma, rc, sst3, s));
-      mark(P, "merge_groups", s, 4);
-      CK(cub_sort_pairs(P, ma.ext_key, ma.ext_key_sorted, ma.ext_val, ma.ext_val_sorted, rc, 64, s));
+      mark(P, "merge_groups", s, 5);
       CK(launch_merge_cap(ma, rc, s));
-      const int cbits = ceil_log2((unsigned long long)n_split + 2);
-      CK(cub_sort_pairs(P, ma.cand_key, ma.cand_key_sorted, ma.cand_val, ma.cand_val_sorted, rc, cbits, s));
-      CK(launch_merge_emit(ma, rc, s));
-      mark(P, "merge_cap", s, 2);
+      mark(P, "merge_cap", s, 3);
     }
   }
   return ADPS_OK;
@@ -1427,7 +1418,7 @@ extern "C" adps_status adps_set_param(adps_plan* P, int32_t key, int64_t value) 
     return ADPS_OK;
   }
   if (key == ADPS_PARAM_TILE_PATH) {
-    if (value < 0 || value > 1) return fail(ADPS_INVALID_ARG, "tile path must be 0 (warp) or 1 (block)");
+    if (value < 0 || value > 2) return fail(ADPS_INVALID_ARG, "tile path must be 0 (warp), 1 (block) or 2 (warp, no bit planes)");
     P->tile_path = (int)value;
     return ADPS_OK;
   }

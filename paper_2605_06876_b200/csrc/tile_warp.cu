@@ -46,6 +46,7 @@ struct WarpSmem {
   unsigned run[kWarpMaxRuns];       // ty | s << 5 | e << 10 | band << 16
   union {
     PostSmem post;
+    int d[kTileH][kTileW];          // bit-plane path: dominant ids of keyed pixels
   } u;
 };
 
@@ -150,6 +151,66 @@ __device__ __forceinline__ double row_raw(const RowIn<RAW>& r) {
   else return raw_l1_f(r.a, r.g);
 }
 
+
+// the runs of one tile row (lane = x; key = candidate id or -1, band) and their
+// unions with the runs of the row above (held in st.prev_*); K = keyed lanes.
+// Returns true when the tile has too many runs for the warp path.
+__device__ __forceinline__ bool runs_row(const int key, const int band, const unsigned K, const int ty,
+                                         ScanState& st, WarpSmem& S, const int lane) {
+  constexpr unsigned FULL = 0xffffffffu;
+#if ADPS_TW_FAST
+  if (K == 0) {   // no keyed pixel in this row: no runs, nothing to unite
+    st.prev_key = -1;
+    st.prev_rid = -1;
+    return false;
+  }
+#endif
+  const int lkey = __shfl_up_sync(FULL, key, 1);
+  const int lband = __shfl_up_sync(FULL, band, 1);
+  const unsigned C = __ballot_sync(FULL, key >= 0 && lane > 0 && lkey == key && lband == band);
+  const unsigned starts = K & ~C;
+  const unsigned ends = K & ~(C >> 1);
+  const int nr = __popc(starts);
+  if (st.n_runs + nr > kWarpMaxRuns) return true;
+  const bool is_start = (starts >> lane) & 1u;
+  const bool is_end = (ends >> lane) & 1u;
+  const int rid_start = st.n_runs + __popc(starts & ((1u << lane) - 1u));
+  const int src = 31 - __clz(starts & (FULL >> (31 - lane)));
+  const int rid_b = __shfl_sync(FULL, rid_start, src & 31);
+  const int rid = key >= 0 ? rid_b : -1;
+  if (is_start) {
+    const int e = __ffs(ends & (FULL << lane)) - 1;
+    S.run[rid] = (unsigned)ty | ((unsigned)lane << 5) | ((unsigned)e << 10) | ((unsigned)band << 16);
+    S.uf[rid] = rid;
+  }
+  __syncwarp();
+  // ---- one union per adjacency with the runs of the row above
+  const int pk_m = __shfl_up_sync(FULL, st.prev_key, 1), pb_m = __shfl_up_sync(FULL, st.prev_band, 1);
+  const int pr_m = __shfl_up_sync(FULL, st.prev_rid, 1);
+  const int pk_p = __shfl_down_sync(FULL, st.prev_key, 1), pb_p = __shfl_down_sync(FULL, st.prev_band, 1);
+  const int pr_p = __shfl_down_sync(FULL, st.prev_rid, 1);
+  if (key >= 0 && ty > 0) {
+    const bool a0 = st.prev_key == key && st.prev_band == band;
+    const bool am = lane > 0 && pk_m == key && pb_m == band;
+    const bool ap = lane < 31 && pk_p == key && pb_p == band;
+    if (a0 && (is_start || !am)) uf_unite(S.uf, rid, st.prev_rid);
+    if (is_start && am && !a0) uf_unite(S.uf, rid, pr_m);
+    if (is_end && ap && !a0) uf_unite(S.uf, rid, pr_p);
+  }
+  if (ty == 0) st.b_top = rid;
+  if (ty == kTileH - 1) st.b_bot = rid;
+  const int lc = __shfl_sync(FULL, rid, 0), rc = __shfl_sync(FULL, rid, 31);
+  if (lane == ty) {
+    st.b_left = lc;
+    st.b_right = rc;
+  }
+  st.prev_key = key;
+  st.prev_band = band;
+  st.prev_rid = rid;
+  st.n_runs += nr;
+  return false;
+}
+
 template <int R, bool RAW>
 __device__ __forceinline__ bool scan_row(const RowIn<RAW>& row, const int ey, ScanState& st, WarpSmem& S,
                                          const TileConst& T, const int lane) {
@@ -188,60 +249,7 @@ __device__ __forceinline__ bool scan_row(const RowIn<RAW>& row, const int ey, Sc
     const int key = ((er >> lane) & 1u) ? cand : -1;
     // ---- runs of equal (candidate, band)
     const unsigned K = __ballot_sync(FULL, key >= 0);
-#if ADPS_TW_FAST
-    if (K == 0) {   // no keyed pixel in this row: no runs, nothing to unite
-      st.prev_key = -1;
-      st.prev_rid = -1;
-    } else
-#endif
-    {
-      const int lkey = __shfl_up_sync(FULL, key, 1);
-      const int lband = __shfl_up_sync(FULL, band, 1);
-      const unsigned C = __ballot_sync(FULL, key >= 0 && lane > 0 && lkey == key && lband == band);
-      const unsigned starts = K & ~C;
-      const unsigned ends = K & ~(C >> 1);
-      const int nr = __popc(starts);
-      if (st.n_runs + nr > kWarpMaxRuns) {
-        overflow = true;
-      } else {
-        const bool is_start = (starts >> lane) & 1u;
-        const bool is_end = (ends >> lane) & 1u;
-        const int rid_start = st.n_runs + __popc(starts & ((1u << lane) - 1u));
-        const int src = 31 - __clz(starts & (FULL >> (31 - lane)));
-        const int rid_b = __shfl_sync(FULL, rid_start, src & 31);
-        const int rid = key >= 0 ? rid_b : -1;
-        if (is_start) {
-          const int e = __ffs(ends & (FULL << lane)) - 1;
-          S.run[rid] = (unsigned)ty | ((unsigned)lane << 5) | ((unsigned)e << 10) | ((unsigned)band << 16);
-          S.uf[rid] = rid;
-        }
-        __syncwarp();
-        // ---- one union per adjacency with the runs of the row above
-        const int pk_m = __shfl_up_sync(FULL, st.prev_key, 1), pb_m = __shfl_up_sync(FULL, st.prev_band, 1);
-        const int pr_m = __shfl_up_sync(FULL, st.prev_rid, 1);
-        const int pk_p = __shfl_down_sync(FULL, st.prev_key, 1), pb_p = __shfl_down_sync(FULL, st.prev_band, 1);
-        const int pr_p = __shfl_down_sync(FULL, st.prev_rid, 1);
-        if (key >= 0 && ty > 0) {
-          const bool a0 = st.prev_key == key && st.prev_band == band;
-          const bool am = lane > 0 && pk_m == key && pb_m == band;
-          const bool ap = lane < 31 && pk_p == key && pb_p == band;
-          if (a0 && (is_start || !am)) uf_unite(S.uf, rid, st.prev_rid);
-          if (is_start && am && !a0) uf_unite(S.uf, rid, pr_m);
-          if (is_end && ap && !a0) uf_unite(S.uf, rid, pr_p);
-        }
-        if (ty == 0) st.b_top = rid;
-        if (ty == kTileH - 1) st.b_bot = rid;
-        const int lc = __shfl_sync(FULL, rid, 0), rc = __shfl_sync(FULL, rid, 31);
-        if (lane == ty) {
-          st.b_left = lc;
-          st.b_right = rc;
-        }
-        st.prev_key = key;
-        st.prev_band = band;
-        st.prev_rid = rid;
-        st.n_runs += nr;
-      }
-    }
+    overflow = runs_row(key, band, K, ty, st, S, lane);
   }
   st.m2 = st.m1;
   st.m1 = m0;
@@ -249,6 +257,122 @@ __device__ __forceinline__ bool scan_row(const RowIn<RAW>& row, const int ey, Sc
   st.band_del = band_now;
   return overflow;
 }
+
+// components of a scanned tile (runs in S, border run ids in st): roots by a
+// read-only find, integer moments per root in closed form per run; interior
+// components >= m_min become regions, edge components fragments + border labels
+__device__ __forceinline__ void finish_tile(const TileParams& P, WarpSmem& S, const int* __restrict__ dom_v,
+                                            const long long tile, const int v, const int x0, const int y0,
+                                            const ScanState& st, const int lane) {
+  constexpr unsigned FULL = 0xffffffffu;
+  const int W = P.W, H = P.H;
+  const int n_runs = st.n_runs;
+  const int b_top = st.b_top, b_bot = st.b_bot, b_left = st.b_left, b_right = st.b_right;
+  __syncwarp();
+  // ---- roots (read-only finds: stored roots are never overwritten)
+  for (int q = lane; q < n_runs; q += 32) {
+    S.uf[q] = uf_find(S.uf, q);
+    S.u.post.aux[q] = -1;
+  }
+  __syncwarp();
+  const bool left_in = x0 > 0, top_in = y0 > 0;
+  const bool right_in = x0 + kTileW < W, bottom_in = y0 + kTileH < H;
+  for (int base = 0; base < n_runs; base += 32) {
+    const int q = base + lane;
+    const bool is_root = q < n_runs && S.uf[q] == q;
+    const unsigned roots = __ballot_sync(FULL, is_root);
+    if (!roots) continue;
+    // integer moments of this batch's roots, one closed form per run
+#pragma unroll
+    for (int k = 0; k < 6; ++k) S.u.post.mom[lane][k] = 0;
+    S.u.post.touch[lane] = 0;
+    __syncwarp();
+    for (int q2 = lane; q2 < n_runs; q2 += 32) {
+      const int root = S.uf[q2];
+      if (root < base || root >= base + 32) continue;
+      const int sl = __popc(roots & ((1u << (root - base)) - 1u));
+      const unsigned info = S.run[q2];
+      const int ty = info & 31, s = (info >> 5) & 31, e = (info >> 10) & 31;
+      const int n = e - s + 1;
+      const int sx = (s + e) * n / 2;
+      const int sxx = (e * (e + 1) * (2 * e + 1) - (s - 1) * s * (2 * s - 1)) / 6;
+      atomicAdd(&S.u.post.mom[sl][0], n);
+      atomicAdd(&S.u.post.mom[sl][1], sx);
+      atomicAdd(&S.u.post.mom[sl][2], ty * n);
+      atomicAdd(&S.u.post.mom[sl][3], sxx);
+      atomicAdd(&S.u.post.mom[sl][4], ty * sx);
+      atomicAdd(&S.u.post.mom[sl][5], ty * ty * n);
+      if ((ty == 0 && top_in) || (ty == kTileH - 1 && bottom_in) || (s == 0 && left_in) ||
+          (e == kTileW - 1 && right_in))
+        S.u.post.touch[sl] = 1;
+    }
+    __syncwarp();
+    // records: fragments for edge components, regions for interior ones >= m_min
+    const int sl = __popc(roots & ((1u << lane) - 1u));
+    const bool is_part = is_root && S.u.post.touch[sl];
+    const bool is_reg = is_root && !S.u.post.touch[sl] && S.u.post.mom[sl][0] >= P.m_min;
+    const unsigned pm = __ballot_sync(FULL, is_part), rm = __ballot_sync(FULL, is_reg);
+    unsigned long long pbase = 0, rbase = 0;
+    if (lane == 0) {
+      if (pm) pbase = atomicAdd(P.n_partials, (unsigned long long)__popc(pm));
+      if (rm) rbase = atomicAdd(P.n_regions, (unsigned long long)__popc(rm));
+    }
+    pbase = __shfl_sync(FULL, pbase, 0);
+    rbase = __shfl_sync(FULL, rbase, 0);
+    if (is_part || is_reg) {
+      const unsigned info = S.run[q];
+      const int ty = info & 31, s = (info >> 5) & 31, bnd = (info >> 16) & 0xff;
+      const long long n = S.u.post.mom[sl][0], mx = S.u.post.mom[sl][1], my = S.u.post.mom[sl][2];
+      const long long X = x0, Y = y0;
+      long long gm[6];
+      gm[0] = n;
+      gm[1] = mx + n * X;
+      gm[2] = my + n * Y;
+      gm[3] = (long long)S.u.post.mom[sl][3] + 2 * X * mx + n * X * X;
+      gm[4] = (long long)S.u.post.mom[sl][4] + X * my + Y * mx + n * X * Y;
+      gm[5] = (long long)S.u.post.mom[sl][5] + 2 * Y * my + n * Y * Y;
+      const int minpix = (y0 + ty) * W + (x0 + s);
+      const int cand = __ldg(dom_v + minpix);
+      if (is_part) {
+        const unsigned long long gid = pbase + __popc(pm & ((1u << lane) - 1u));
+        if ((long long)gid < P.partial_cap) {
+          PartialRec& Rr = P.partials[gid];
+          Rr.view_pos = P.view_offset + v * P.view_stride;
+          Rr.cand = cand;
+          Rr.band = bnd;
+          Rr.minpix = minpix;
+#pragma unroll
+          for (int k = 0; k < 6; ++k) Rr.m[k] = gm[k];
+          P.partial_parent[gid] = (int)gid;
+          S.u.post.aux[q] = (int)gid;
+        } else {
+          atomicOr(P.overflow, 2u);
+        }
+      } else {
+        const unsigned long long rid2 = rbase + __popc(rm & ((1u << lane) - 1u));
+        if ((long long)rid2 < P.region_cap) {
+          RegionRec& Rr = P.regions[rid2];
+          Rr.view_pos = P.view_offset + v * P.view_stride;
+          Rr.cand = cand;
+          Rr.band = bnd;
+          Rr.minpix = minpix;
+#pragma unroll
+          for (int k = 0; k < 6; ++k) Rr.m[k] = gm[k];
+        } else {
+          atomicOr(P.overflow, 1u);
+        }
+      }
+    }
+    __syncwarp();
+  }
+  // ---- border labels: top, bottom, left, right (slot = side * 32 + lane)
+  int* border = P.border + tile * kBorderSlots;
+  border[lane] = b_top >= 0 ? S.u.post.aux[S.uf[b_top]] : -1;
+  border[kTileW + lane] = b_bot >= 0 ? S.u.post.aux[S.uf[b_bot]] : -1;
+  border[2 * kTileW + lane] = b_left >= 0 ? S.u.post.aux[S.uf[b_left]] : -1;
+  border[2 * kTileW + kTileH + lane] = b_right >= 0 ? S.u.post.aux[S.uf[b_right]] : -1;
+}
+
 
 template <int R, bool RAW>
 __device__ __forceinline__ void tile_warp_body(const TileParams& P, WarpSmem& S, const long long tile,
@@ -328,115 +452,11 @@ __device__ __forceinline__ void tile_warp_body(const TileParams& P, WarpSmem& S,
       }
     }
   }
-  const int n_runs = st.n_runs;
-  const int b_top = st.b_top, b_bot = st.b_bot, b_left = st.b_left, b_right = st.b_right;
   if (overflow) {
     if (lane == 0) P.deferred[atomicAdd(P.n_deferred, 1ull)] = (int)tile;
     return;
   }
-  __syncwarp();
-  // ---- roots (read-only finds: stored roots are never overwritten)
-  for (int q = lane; q < n_runs; q += 32) {
-    S.uf[q] = uf_find(S.uf, q);
-    S.u.post.aux[q] = -1;
-  }
-  __syncwarp();
-  const bool left_in = x0 > 0, top_in = y0 > 0;
-  const bool right_in = x0 + kTileW < W, bottom_in = y0 + kTileH < H;
-  for (int base = 0; base < n_runs; base += 32) {
-    const int q = base + lane;
-    const bool is_root = q < n_runs && S.uf[q] == q;
-    const unsigned roots = __ballot_sync(FULL, is_root);
-    if (!roots) continue;
-    // integer moments of this batch's roots, one closed form per run
-#pragma unroll
-    for (int k = 0; k < 6; ++k) S.u.post.mom[lane][k] = 0;
-    S.u.post.touch[lane] = 0;
-    __syncwarp();
-    for (int q2 = lane; q2 < n_runs; q2 += 32) {
-      const int root = S.uf[q2];
-      if (root < base || root >= base + 32) continue;
-      const int sl = __popc(roots & ((1u << (root - base)) - 1u));
-      const unsigned info = S.run[q2];
-      const int ty = info & 31, s = (info >> 5) & 31, e = (info >> 10) & 31;
-      const int n = e - s + 1;
-      const int sx = (s + e) * n / 2;
-      const int sxx = (e * (e + 1) * (2 * e + 1) - (s - 1) * s * (2 * s - 1)) / 6;
-      atomicAdd(&S.u.post.mom[sl][0], n);
-      atomicAdd(&S.u.post.mom[sl][1], sx);
-      atomicAdd(&S.u.post.mom[sl][2], ty * n);
-      atomicAdd(&S.u.post.mom[sl][3], sxx);
-      atomicAdd(&S.u.post.mom[sl][4], ty * sx);
-      atomicAdd(&S.u.post.mom[sl][5], ty * ty * n);
-      if ((ty == 0 && top_in) || (ty == kTileH - 1 && bottom_in) || (s == 0 && left_in) ||
-          (e == kTileW - 1 && right_in))
-        S.u.post.touch[sl] = 1;
-    }
-    __syncwarp();
-    // records: fragments for edge components, regions for interior ones >= m_min
-    const int sl = __popc(roots & ((1u << lane) - 1u));
-    const bool is_part = is_root && S.u.post.touch[sl];
-    const bool is_reg = is_root && !S.u.post.touch[sl] && S.u.post.mom[sl][0] >= P.m_min;
-    const unsigned pm = __ballot_sync(FULL, is_part), rm = __ballot_sync(FULL, is_reg);
-    unsigned long long pbase = 0, rbase = 0;
-    if (lane == 0) {
-      if (pm) pbase = atomicAdd(P.n_partials, (unsigned long long)__popc(pm));
-      if (rm) rbase = atomicAdd(P.n_regions, (unsigned long long)__popc(rm));
-    }
-    pbase = __shfl_sync(FULL, pbase, 0);
-    rbase = __shfl_sync(FULL, rbase, 0);
-    if (is_part || is_reg) {
-      const unsigned info = S.run[q];
-      const int ty = info & 31, s = (info >> 5) & 31, bnd = (info >> 16) & 0xff;
-      const long long n = S.u.post.mom[sl][0], mx = S.u.post.mom[sl][1], my = S.u.post.mom[sl][2];
-      const long long X = x0, Y = y0;
-      long long gm[6];
-      gm[0] = n;
-      gm[1] = mx + n * X;
-      gm[2] = my + n * Y;
-      gm[3] = (long long)S.u.post.mom[sl][3] + 2 * X * mx + n * X * X;
-      gm[4] = (long long)S.u.post.mom[sl][4] + X * my + Y * mx + n * X * Y;
-      gm[5] = (long long)S.u.post.mom[sl][5] + 2 * Y * my + n * Y * Y;
-      const int minpix = (y0 + ty) * W + (x0 + s);
-      const int cand = __ldg(T.dom + minpix);
-      if (is_part) {
-        const unsigned long long gid = pbase + __popc(pm & ((1u << lane) - 1u));
-        if ((long long)gid < P.partial_cap) {
-          PartialRec& Rr = P.partials[gid];
-          Rr.view_pos = P.view_offset + v * P.view_stride;
-          Rr.cand = cand;
-          Rr.band = bnd;
-          Rr.minpix = minpix;
-#pragma unroll
-          for (int k = 0; k < 6; ++k) Rr.m[k] = gm[k];
-          P.partial_parent[gid] = (int)gid;
-          S.u.post.aux[q] = (int)gid;
-        } else {
-          atomicOr(P.overflow, 2u);
-        }
-      } else {
-        const unsigned long long rid2 = rbase + __popc(rm & ((1u << lane) - 1u));
-        if ((long long)rid2 < P.region_cap) {
-          RegionRec& Rr = P.regions[rid2];
-          Rr.view_pos = P.view_offset + v * P.view_stride;
-          Rr.cand = cand;
-          Rr.band = bnd;
-          Rr.minpix = minpix;
-#pragma unroll
-          for (int k = 0; k < 6; ++k) Rr.m[k] = gm[k];
-        } else {
-          atomicOr(P.overflow, 1u);
-        }
-      }
-    }
-    __syncwarp();
-  }
-  // ---- border labels: top, bottom, left, right (slot = side * 32 + lane)
-  int* border = P.border + tile * kBorderSlots;
-  border[lane] = b_top >= 0 ? S.u.post.aux[S.uf[b_top]] : -1;
-  border[kTileW + lane] = b_bot >= 0 ? S.u.post.aux[S.uf[b_bot]] : -1;
-  border[2 * kTileW + lane] = b_left >= 0 ? S.u.post.aux[S.uf[b_left]] : -1;
-  border[2 * kTileW + kTileH + lane] = b_right >= 0 ? S.u.post.aux[S.uf[b_right]] : -1;
+  finish_tile(P, S, T.dom, tile, v, x0, y0, st, lane);
 }
 
 template <int R, bool RAW>
@@ -447,6 +467,291 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, ADPS_TW_MINBLOCKS) tile_w
   const long long tile = t0 + (long long)blockIdx.x * kWarpsPerBlock + wid;
   if (tile >= t1) return;   // warp-uniform
   tile_warp_body<R, RAW>(P, S, tile, lane);
+}
+
+
+// ===================================================================== bit planes
+// The common configuration (raw cache on, l_bands <= 4) splits the tile pass:
+//   tile_words_kernel  streams the cached raw error once (coalesced, several
+//                      32-pixel words in flight per warp) and writes, per image
+//                      row and 32-column word, four bit planes: metric bit,
+//                      candidate bit, band bit 0, band bit 1 (16 B per 32 px);
+//   tile_bits_kernel   the warp-per-tile scanline CCL on those words: the whole
+//                      tile's masks arrive in one 16-byte load per lane (lane =
+//                      ext row), erosion and keying are word operations, tiles
+//                      without a keyed pixel exit at once, and only keyed rows
+//                      are scanned; the dominant ids of keyed pixels are staged in
+//                      shared memory with cp.async (one wait per tile).
+// Same run numbering, unions and records as tile_warp_kernel, so the results
+// are identical bit for bit (tests compare all CCL paths).
+
+__global__ void __launch_bounds__(256) tile_words_kernel(const double* __restrict__ raw,
+                                                         const unsigned* __restrict__ cand_bits,
+                                                         const double* __restrict__ thr_raw, int L, int H, int W,
+                                                         int WW, int v0, uint4* __restrict__ words) {
+  // one warp per image row, lane = x within a 32-column word, U words in flight
+  const int v = v0 + blockIdx.y;
+  const int y = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (y >= H) return;   // warp-uniform
+  const int lane = threadIdx.x & 31;
+  const long long hw = (long long)H * W;
+  const long long nwords = (hw + 31) / 32;
+  const double* rrow = raw + (long long)v * hw + (long long)y * W;
+  const unsigned* cv = cand_bits + (long long)v * nwords;
+  uint4* wrow = words + ((long long)v * H + y) * WW;
+  // raw >= +0.0 and the thresholds are >= +0.0 or +inf, so IEEE order is the
+  // signed order of the bit patterns: integer compares, no fp64 pipe
+  const long long kInf = 0x7ff0000000000000ll;
+  const double* tv = thr_raw + (long long)v * L;
+  const long long xm = __double_as_longlong(__ldg(tv));
+  const long long t1 = L > 1 ? __double_as_longlong(__ldg(tv + 1)) : kInf;
+  const long long t2 = L > 2 ? __double_as_longlong(__ldg(tv + 2)) : kInf;
+  const long long t3 = L > 3 ? __double_as_longlong(__ldg(tv + 3)) : kInf;
+  const long long* rrow_i = reinterpret_cast<const long long*>(rrow);
+  const long long p_row = (long long)y * W;
+  constexpr int U = 8;
+  for (int wx0 = 0; wx0 < WW; wx0 += U) {
+    long long r[U];
+    unsigned lo[U], hi[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int x = (wx0 + u) * 32 + lane;
+      r[u] = x < W ? __ldg(rrow_i + x) : -1ll;   // below every threshold
+      // the candidate bits of this word: a funnel shift of two linear words
+      const long long p0 = p_row + (wx0 + u) * 32;
+      const long long i0 = p0 >> 5;
+      lo[u] = wx0 + u < WW ? __ldg(cv + i0) : 0u;
+      hi[u] = (wx0 + u < WW && (p0 & 31) && i0 + 1 < nwords) ? __ldg(cv + i0 + 1) : 0u;
+    }
+    const int sh = (int)(p_row & 31);
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int wx = wx0 + u;
+      const int band = (r[u] >= t1) + (r[u] >= t2) + (r[u] >= t3);
+      const unsigned M = __ballot_sync(0xffffffffu, r[u] >= xm);
+      const unsigned B0 = __ballot_sync(0xffffffffu, band & 1);
+      const unsigned B1 = __ballot_sync(0xffffffffu, band & 2);
+      const int valid = W - wx * 32;   // columns of this word inside the row
+      unsigned C = __funnelshift_r(lo[u], hi[u], sh);
+      if (valid < 32) C &= (1u << (valid > 0 ? valid : 0)) - 1u;
+      if (lane == u && wx < WW) wrow[wx] = make_uint4(M, C, B0, B1);
+    }
+  }
+}
+
+// the word of ext row ey (image row y0 - HL + ey) of tile column tx, and its
+// 64-bit metric mask with the left/right halo bits (bit HL = column x0)
+template <int HL, int HH>
+__device__ __forceinline__ void load_ext_words(const uint4* __restrict__ wv, int WW, int H, int tx, int y0, int ey,
+                                               int NR, uint4& q, unsigned long long& m64) {
+  const int y = y0 - HL + ey;
+  q = make_uint4(0u, 0u, 0u, 0u);
+  m64 = 0ull;
+  if (ey < NR && y >= 0 && y < H) {
+    const uint4* row = wv + (long long)y * WW;
+    q = __ldg(row + tx);
+    m64 = (unsigned long long)q.x << HL;
+    if (HL > 0 && tx > 0) m64 |= (unsigned long long)(__ldg(reinterpret_cast<const unsigned*>(row + tx - 1)) >> 31);
+    if (HH > 0 && tx + 1 < WW)
+      m64 |= (unsigned long long)(__ldg(reinterpret_cast<const unsigned*>(row + tx + 1)) & 1u) << (kTileW + HL);
+  }
+}
+
+// value of ext row ey held by lane ey (set a) or lane ey - 32 (set b)
+template <typename Tv>
+__device__ __forceinline__ Tv ext_get(Tv a, Tv b, int ey) {
+  const Tv va = __shfl_sync(0xffffffffu, a, ey & 31);
+  const Tv vb = __shfl_sync(0xffffffffu, b, ey & 31);
+  return ey < 32 ? va : vb;
+}
+
+__device__ __forceinline__ void cp_async4(void* smem, const void* gmem) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(sa), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
+
+template <int R>
+__global__ void __launch_bounds__(kWarpsPerBlock * 32, ADPS_TW_MINBLOCKS)
+    tile_bits_kernel(TileParams P, const uint4* __restrict__ words, int WW, long long t0, long long t1) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  constexpr int HL = R > 1 ? R / 2 : 0;
+  constexpr int HH = R > 1 ? R - R / 2 - 1 : 0;
+  constexpr int SPAN = HL + HH;
+  constexpr int NR = kTileH + SPAN;
+  constexpr unsigned FULL = 0xffffffffu;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  WarpSmem& S = reinterpret_cast<WarpSmem*>(smem_raw)[wid];
+  const long long tile = t0 + (long long)blockIdx.x * kWarpsPerBlock + wid;
+  if (tile >= t1) return;   // warp-uniform
+  const int tpv = P.tiles_x * P.tiles_y;
+  const int v = (int)(tile / tpv);
+  const int tin = (int)(tile - (long long)v * tpv);
+  const int tx = tin % P.tiles_x;
+  const int x0 = tx * kTileW, y0 = (tin / P.tiles_x) * kTileH;
+  const int W = P.W, H = P.H;
+  const uint4* wv = words + (long long)v * H * WW;
+  // ---- all ext rows of the tile: lane ey (and 32 + lane for the last SPAN rows)
+  uint4 qa, qb = make_uint4(0u, 0u, 0u, 0u);
+  unsigned long long ma, mb = 0ull;
+  load_ext_words<HL, HH>(wv, WW, H, tx, y0, lane, NR, qa, ma);
+  if (NR > 32) load_ext_words<HL, HH>(wv, WW, H, tx, y0, 32 + lane, NR, qb, mb);
+  // ---- lane ty: eroded metric word of tile row ty, its candidate and band words
+  unsigned long long acc = ma;
+  if (SPAN >= 1) acc &= ext_get(ma, mb, lane + 1);
+  if (SPAN >= 2) acc &= ext_get(ma, mb, lane + 2);
+  unsigned long long h = acc;
+  if (SPAN >= 1) h &= acc >> 1;
+  if (SPAN >= 2) h &= acc >> 2;
+  const unsigned cw = HL > 0 ? ext_get(qa.y, qb.y, lane + HL) : qa.y;
+  const unsigned bw0 = HL > 0 ? ext_get(qa.z, qb.z, lane + HL) : qa.z;
+  const unsigned bw1 = HL > 0 ? ext_get(qa.w, qb.w, lane + HL) : qa.w;
+  const unsigned K = (unsigned)h & cw;
+  const unsigned keyed = __ballot_sync(FULL, K != 0u);
+  int* border = P.border + tile * kBorderSlots;
+  if (keyed == 0u) {   // no keyed pixel: no runs, no records, empty border labels
+#pragma unroll
+    for (int k = 0; k < 4; ++k) border[32 * k + lane] = -1;
+    return;
+  }
+  // ---- stage the dominant ids of keyed pixels (one wait for the whole tile)
+  const int* dom_v = P.dom + (long long)v * H * W;
+  for (unsigned rows = keyed; rows; rows &= rows - 1u) {
+    const int ty = __ffs(rows) - 1;
+    const unsigned kw = __shfl_sync(FULL, K, ty);
+    if ((kw >> lane) & 1u) cp_async4(&S.u.d[ty][lane], dom_v + (long long)(y0 + ty) * W + x0 + lane);
+  }
+  cp_async_wait_all();
+  // ---- (a) lane = column, per keyed row: the run-continuation mask (same
+  //      key|band as the left neighbour) and the three vertical same-key masks
+  //      against the row above (N, NW, NE); lane ty keeps row ty's masks.
+  unsigned my_cc = 0u, my_v0 = 0u, my_vm = 0u, my_vp = 0u;
+  {
+    int kb_prev = -1;   // key|band of the row above (-1 when it is not keyed)
+    int last = -2;
+    for (unsigned rows = keyed; rows; rows &= rows - 1u) {
+      const int ty = __ffs(rows) - 1;
+      if (ty != last + 1) kb_prev = -1;
+      last = ty;
+      const unsigned kw = __shfl_sync(FULL, K, ty);
+      const unsigned b0 = __shfl_sync(FULL, bw0, ty), b1 = __shfl_sync(FULL, bw1, ty);
+      const int band = (int)((b0 >> lane) & 1u) | (int)(((b1 >> lane) & 1u) << 1);
+      const bool kl = (kw >> lane) & 1u;
+      const int kb = kl ? (S.u.d[ty][lane] << 2) | band : -1;   // ids < 2^29
+      const int lkb = __shfl_up_sync(FULL, kb, 1);
+      const int pm = __shfl_up_sync(FULL, kb_prev, 1), pp = __shfl_down_sync(FULL, kb_prev, 1);
+      const unsigned cc = __ballot_sync(FULL, kl && lane > 0 && lkb == kb);
+      const unsigned v0 = __ballot_sync(FULL, kl && kb_prev == kb);
+      const unsigned vm = __ballot_sync(FULL, kl && lane > 0 && pm == kb);
+      const unsigned vp = __ballot_sync(FULL, kl && lane < 31 && pp == kb);
+      if (lane == ty) {
+        my_cc = cc;
+        my_v0 = v0;
+        my_vm = vm;
+        my_vp = vp;
+      }
+      kb_prev = kb;
+    }
+  }
+  // ---- (b) lane = row from here on.  Runs: starts/ends of this row; run ids
+  //      are row-major, so a row's base is the exclusive prefix of run counts
+  const unsigned my_starts = K & ~my_cc;
+  const unsigned my_ends = K & ~(my_cc >> 1);
+  const int my_nr = __popc(my_starts);
+  int base = my_nr;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int t = __shfl_up_sync(FULL, base, o);
+    if (lane >= o) base += t;
+  }
+  const int n_runs = __shfl_sync(FULL, base, 31);
+  base -= my_nr;
+  if (n_runs > kWarpMaxRuns) {
+    if (lane == 0) P.deferred[atomicAdd(P.n_deferred, 1ull)] = (int)tile;
+    return;
+  }
+  // ---- (c) run records of this row
+  {
+    int rid = base;
+    for (unsigned st_bits = my_starts; st_bits; st_bits &= st_bits - 1u, ++rid) {
+      const int x = __ffs(st_bits) - 1;
+      const int e = __ffs(my_ends & (FULL << x)) - 1;
+      const int band = (int)((bw0 >> x) & 1u) | (int)(((bw1 >> x) & 1u) << 1);
+      S.run[rid] = (unsigned)lane | ((unsigned)x << 5) | ((unsigned)e << 10) | ((unsigned)band << 16);
+      S.uf[rid] = rid;
+    }
+  }
+  __syncwarp();
+  // ---- (d) one union per adjacency with the runs of the row above (the rule
+  //      of runs_row): N at the first overlapping pixel, NW at a run start,
+  //      NE at a run end; run ids of both rows from popcounts of the starts
+  {
+    const unsigned sa = __shfl_up_sync(FULL, my_starts, 1);
+    const int ba = __shfl_up_sync(FULL, base, 1);
+    unsigned ev = (my_v0 & (my_starts | ~my_vm)) | (my_starts & my_vm & ~my_v0) | (my_ends & my_vp & ~my_v0);
+    if (lane == 0) ev = 0u;
+    for (; ev; ev &= ev - 1u) {
+      const int x = __ffs(ev) - 1;
+      const unsigned bit = 1u << x, le = bit | (bit - 1u);
+      const int rid = base + __popc(my_starts & le) - 1;
+      const bool a0 = my_v0 & bit, am = my_vm & bit, is_start = my_starts & bit;
+      if (a0 && (is_start || !am)) uf_unite(S.uf, rid, ba + __popc(sa & le) - 1);
+      if (is_start && am && !a0) uf_unite(S.uf, rid, ba + __popc(sa & (bit - 1u)) - 1);
+      if ((my_ends & bit) && (my_vp & bit) && !a0) uf_unite(S.uf, rid, ba + __popc(sa & ((le << 1) | 1u)) - 1);
+    }
+  }
+  // ---- (e) border run ids: rows 0 / 31 at column `lane`, columns 0 / 31 of row `lane`
+  ScanState st;
+  st.n_runs = n_runs;
+  {
+    __syncwarp();
+    const unsigned lt = (1u << lane) - 1u;
+    const unsigned k0w = __shfl_sync(FULL, K, 0), s0 = __shfl_sync(FULL, my_starts, 0);
+    const unsigned k31 = __shfl_sync(FULL, K, kTileH - 1), s31 = __shfl_sync(FULL, my_starts, kTileH - 1);
+    const int b0r = __shfl_sync(FULL, base, 0), b31r = __shfl_sync(FULL, base, kTileH - 1);
+    const unsigned le = lt | (1u << lane);
+    st.b_top = ((k0w >> lane) & 1u) ? b0r + __popc(s0 & le) - 1 : -1;
+    st.b_bot = ((k31 >> lane) & 1u) ? b31r + __popc(s31 & le) - 1 : -1;
+    st.b_left = (K & 1u) ? base : -1;
+    st.b_right = (K >> 31) ? base + my_nr - 1 : -1;
+  }
+  __syncwarp();   // the key|band words share the union with the post-scan scratch
+  finish_tile(P, S, dom_v, tile, v, x0, y0, st, lane);
+}
+
+size_t tile_words_bytes(int V, int H, int W) { return (size_t)V * H * ((W + 31) / 32) * sizeof(uint4); }
+
+cudaError_t launch_tile_bits(const TileParams& P, int v0, int v1, cudaStream_t s) {
+  if (v1 <= v0) return cudaSuccess;
+  const int WW = (P.W + 31) / 32;
+  const int per_view = P.H * WW;
+  (void)per_view;
+  const unsigned gx = (unsigned)((P.H + 7) / 8);   // warp per image row, 8 rows per block
+  tile_words_kernel<<<dim3(gx, (unsigned)(v1 - v0)), 256, 0, s>>>(P.raw, P.cand_bits, P.thr_raw, P.L, P.H, P.W, WW,
+                                                                   v0, P.words);
+  const long long tpv = (long long)P.tiles_x * P.tiles_y;
+  const long long t0 = tpv * v0, t1 = tpv * v1;
+  const size_t smem = tile_warp_smem_bytes();
+  const long long blocks = (t1 - t0 + kWarpsPerBlock - 1) / kWarpsPerBlock;
+  cudaError_t e = cudaSuccess;
+  switch (P.r_erode <= 1 ? 1 : P.r_erode) {
+    case 1:
+      e = cudaFuncSetAttribute(tile_bits_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      if (e == cudaSuccess) tile_bits_kernel<1><<<(unsigned)blocks, kWarpsPerBlock * 32, smem, s>>>(P, P.words, WW, t0, t1);
+      break;
+    case 2:
+      e = cudaFuncSetAttribute(tile_bits_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      if (e == cudaSuccess) tile_bits_kernel<2><<<(unsigned)blocks, kWarpsPerBlock * 32, smem, s>>>(P, P.words, WW, t0, t1);
+      break;
+    case 3:
+      e = cudaFuncSetAttribute(tile_bits_kernel<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      if (e == cudaSuccess) tile_bits_kernel<3><<<(unsigned)blocks, kWarpsPerBlock * 32, smem, s>>>(P, P.words, WW, t0, t1);
+      break;
+    default:
+      return cudaErrorInvalidValue;
+  }
+  if (e != cudaSuccess) return e;
+  return cudaGetLastError();
 }
 
 template <int R, bool RAW>
