@@ -39,7 +39,8 @@ __device__ __forceinline__ double raw_l1(const float* __restrict__ img, const fl
 __global__ void minmax_kernel(const float* __restrict__ image, const float* __restrict__ gt,
                               const int* __restrict__ dominant, long long hw, unsigned long long* __restrict__ lohi,
                               const unsigned char* __restrict__ cls, int N, unsigned char* __restrict__ dom_flag,
-                              unsigned* __restrict__ cand_bits, double* __restrict__ raw_out, int v0) {
+                              unsigned* __restrict__ cand_bits, double* __restrict__ raw_out,
+                              float* __restrict__ rawf_out, int v0) {
   const int v = v0 + blockIdx.y;
   const float* img = image + (long long)v * hw * 3;
   const float* g = gt + (long long)v * hw * 3;
@@ -54,6 +55,9 @@ __global__ void minmax_kernel(const float* __restrict__ image, const float* __re
     if (p < hw) {
       const double r = raw_l1(img, g, p);
       if (raw_out) raw_out[(long long)v * hw + p] = r;
+      // the bit-plane path keeps raw rounded toward zero (4 B/px); compares that
+      // the rounding cannot decide are redone exactly (tile_words_kernel)
+      if (rawf_out) rawf_out[(long long)v * hw + p] = __double2float_rz(r);
       lo = fmin(lo, r);
       hi = fmax(hi, r);
       d = __ldg(dom + p);
@@ -108,17 +112,38 @@ __device__ __forceinline__ double band_raw(double x, double d, double tau, doubl
   return floor(dmul(ddiv(dsub(ddiv(x, d), tau), omt), nb));
 }
 
+// Warp-parallel search over the bit patterns of non-negative doubles (their
+// integer order is their IEEE order): the smallest x in (lo, hi] with pred(x),
+// given pred monotone, pred(lo) false and pred(hi) true.  Each round the 32
+// lanes test 32 evenly spaced points, so the interval shrinks 33-fold.
+template <class Pred>
+__device__ long long warp_bits_search(long long lo, long long hi, Pred pred) {
+  const int lane = threadIdx.x & 31;
+  while (hi - lo > 1) {
+    const long long span = hi - lo;
+    const long long step = span / 33 > 0 ? span / 33 : 1;
+    const long long p = lo + (long long)(lane + 1) * step;
+    const bool ok = p < hi && pred(__longlong_as_double(p));
+    const unsigned b = __ballot_sync(0xffffffffu, ok);
+    const unsigned tested = __ballot_sync(0xffffffffu, p < hi);
+    if (b == 0u) {
+      const int last = 31 - __clz(tested);   // every tested point is false
+      lo = lo + (long long)(last + 1) * step;
+    } else {
+      const int first = __ffs(b) - 1;
+      const long long pf = lo + (long long)(first + 1) * step;
+      lo = first > 0 ? lo + (long long)first * step : lo;
+      hi = pf;
+    }
+  }
+  return hi;
+}
+
 __device__ double min_true(double d, int k, double tau, double omt, double nb) {
   auto pred = [&](double x) -> bool { return k == 0 ? m_pred(x, d, tau) : band_raw(x, d, tau, omt, nb) >= (double)k; };
   if (!pred(d)) return INFINITY;
-  long long lo = 0, hi = __double_as_longlong(d);   // pred(hi) true
   if (pred(0.0)) return 0.0;
-  while (hi - lo > 1) {
-    long long mid = lo + (hi - lo) / 2;
-    if (pred(__longlong_as_double(mid))) hi = mid;
-    else lo = mid;
-  }
-  return __longlong_as_double(hi);
+  return __longlong_as_double(warp_bits_search(0ll, __double_as_longlong(d), pred));
 }
 
 // thr[v*L + 0] = x threshold of m; thr[v*L + k] = x threshold of band >= k.
@@ -129,33 +154,36 @@ __device__ double raw_threshold(double lo, double hi, double t) {
   if (t == INFINITY) return INFINITY;
   if (!(dsub(hi, lo) >= t)) return INFINITY;
   if (dsub(lo, lo) >= t) return lo;
-  long long a = __double_as_longlong(lo), b = __double_as_longlong(hi);   // pred(a) false, pred(b) true
-  while (b - a > 1) {
-    const long long mid = a + (b - a) / 2;
-    if (dsub(__longlong_as_double(mid), lo) >= t) b = mid;
-    else a = mid;
-  }
-  return __longlong_as_double(b);
+  auto pred = [&](double r) -> bool { return dsub(r, lo) >= t; };
+  return __longlong_as_double(warp_bits_search(__double_as_longlong(lo), __double_as_longlong(hi), pred));
 }
 
+// a warp per (view, threshold)
 __global__ void thresholds_kernel(const unsigned long long* __restrict__ lohi, int v0, int n_views, int L,
                                   double tau, double* __restrict__ lo_out, double* __restrict__ thr,
                                   double* __restrict__ thr_raw) {
-  int t = v0 * L + blockIdx.x * blockDim.x + threadIdx.x;
-  if (t >= (v0 + n_views) * L) return;
+  const int t = v0 * L + (int)((blockIdx.x * blockDim.x + threadIdx.x) >> 5);
+  if (t >= (v0 + n_views) * L) return;   // warp-uniform
+  const bool lead = (threadIdx.x & 31) == 0;
   int v = t / L, k = t % L;
   double lo = __longlong_as_double((long long)lohi[2 * v]);
   double hi = __longlong_as_double((long long)lohi[2 * v + 1]);
-  if (k == 0) lo_out[v] = lo;
+  if (k == 0 && lead) lo_out[v] = lo;
   if (hi == lo) {  // error_map returns zeros: m false, band 0 (ref/error_partition.py:52-53)
-    thr[t] = INFINITY;
-    if (thr_raw) thr_raw[t] = INFINITY;
+    if (lead) {
+      thr[t] = INFINITY;
+      if (thr_raw) thr_raw[t] = INFINITY;
+    }
     return;
   }
   double d = dsub(hi, lo);
   double omt = dsub(1.0, tau);
-  thr[t] = min_true(d, k, tau, omt, (double)L);
-  if (thr_raw) thr_raw[t] = raw_threshold(lo, hi, thr[t]);
+  const double x = min_true(d, k, tau, omt, (double)L);
+  const double r = thr_raw ? raw_threshold(lo, hi, x) : 0.0;
+  if (lead) {
+    thr[t] = x;
+    if (thr_raw) thr_raw[t] = r;
+  }
 }
 
 // ---------------------------------------------------- ever-dominant (early)
@@ -576,9 +604,10 @@ cudaError_t launch_minmax_views(const AttributionArgs& a, int v0, int v1, cudaSt
   const long long hw = (long long)a.H * a.W;
   dim3 mg((unsigned)((hw + 256 * 8 - 1) / (256 * 8)), (unsigned)(v1 - v0));
   if (mg.x > 1024) mg.x = 1024;
-  minmax_kernel<<<mg, 256, 0, s>>>(a.image, a.gt, a.dom, hw, a.lohi, a.cls, a.N, a.dom_flag, a.cand_bits, a.raw, v0);
+  minmax_kernel<<<mg, 256, 0, s>>>(a.image, a.gt, a.dom, hw, a.lohi, a.cls, a.N, a.dom_flag, a.cand_bits, a.raw,
+                                   a.rawf, v0);
   const int nt = (v1 - v0) * a.L;
-  thresholds_kernel<<<(nt + 127) / 128, 128, 0, s>>>(a.lohi, v0, v1 - v0, a.L, a.tau, a.lo, a.thr, a.thr_raw);
+  thresholds_kernel<<<(nt + 3) / 4, 128, 0, s>>>(a.lohi, v0, v1 - v0, a.L, a.tau, a.lo, a.thr, a.thr_raw);
   return cudaGetLastError();
 }
 
@@ -631,6 +660,7 @@ static TileParams tile_params(const AttributionArgs& a) {
   P.cand_bits = a.cand_bits;
   P.raw = a.raw;
   P.words = a.words;
+  P.rawf = a.rawf;
   P.deferred = a.deferred;
   P.n_deferred = a.n_deferred;
   return P;
@@ -645,7 +675,7 @@ bool attribution_warp_path(const AttributionArgs& a) {
 cudaError_t launch_tiles_views(const AttributionArgs& a, int v0, int v1, cudaStream_t s) {
   if (!attribution_warp_path(a) || v1 <= v0) return cudaSuccess;
   const TileParams P = tile_params(a);
-  if (P.words && P.raw) return launch_tile_bits(P, v0, v1, s);
+  if (P.words && P.rawf) return launch_tile_bits(P, v0, v1, s);
   const long long tpv = (long long)P.tiles_x * P.tiles_y;
   return launch_tile_warp(P, tpv * v0, tpv * v1, s);
 }
@@ -658,7 +688,7 @@ cudaError_t launch_attribution_tail(const AttributionArgs& a, cudaStream_t s, Ma
   if (e != cudaSuccess) return e;
   if (attribution_warp_path(a)) {
     tile_kernel<<<a.grid_small, kTileThreads, smem, s>>>(P, a.deferred, a.n_deferred);
-    if (mark) mark(ctx, "tile_ccl", s, a.words && a.raw ? 3 : 2);
+    if (mark) mark(ctx, "tile_ccl", s, a.words && a.rawf ? 3 : 2);
   } else {
     tile_kernel<<<(unsigned)nblocks, kTileThreads, smem, s>>>(P, nullptr, nullptr);
     if (mark) mark(ctx, "tile_ccl", s, 1);

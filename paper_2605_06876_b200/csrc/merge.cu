@@ -77,8 +77,8 @@ struct GatherPolicy {
   __device__ void store(long long p, unsigned long long ex, unsigned long long v) const {
     const int rank = (int)(a.keys_sorted[p] >> a.shift_rank);
     if (p == 0 || (int)(a.keys_sorted[p - 1] >> a.shift_rank) != rank) a.pstart[rank] = (int)ex;
-    if (v) {
-      a.props_s[ex] = a.props[a.vals_sorted[p]];
+    if (v) {   // the 152-byte records are copied by gather_props_kernel (coalesced)
+      a.psrc[ex] = a.vals_sorted[p];
       a.pcand[ex] = rank;
       a.uf[ex] = (int)ex;
     }
@@ -123,9 +123,24 @@ __global__ void case_kernel(MergeArgs a) {
   }
 }
 
+// props_s[q] = props[psrc[q]]: thread per 8-byte word, so both the gathered
+// source records and the packed destination are read/written coalesced
+__global__ void gather_props_kernel(MergeArgs a) {
+  constexpr int WPR = (int)(sizeof(Proposal) / 8);
+  const long long nw = (long long)a.ctr->n_proposals * WPR;
+  const double* src = reinterpret_cast<const double*>(a.props);
+  double* dst = reinterpret_cast<double*>(a.props_s);
+  for (long long w = (long long)blockIdx.x * blockDim.x + threadIdx.x; w < nw; w += (long long)gridDim.x * blockDim.x) {
+    const long long q = w / WPR;
+    const int c = (int)(w - q * WPR);
+    dst[w] = __ldg(src + (long long)__ldg(a.psrc + q) * WPR + c);
+  }
+}
+
 cudaError_t launch_merge_prepare(const MergeArgs& a, long long n_split, ScanState st, cudaStream_t s) {
   cudaError_t e = launch_scan(GatherPolicy{a}, a.n_regions, st, s);
   if (e != cudaSuccess) return e;
+  gather_props_kernel<<<a.grid, 256, 0, s>>>(a);
   long long b = (n_split + 255) / 256;
   case_kernel<<<(unsigned)(b < 1 ? 1 : (b > 4096 ? 4096 : b)), 256, 0, s>>>(a);
   return cudaGetLastError();

@@ -34,6 +34,7 @@ struct MergeArgs {
   int small_max;                           // P <= small_max: warp path for the gates
   // proposal space
   Proposal* props_s;                       // [cap]
+  int* psrc;                               // [cap] proposal q -> region id (gather source)
   int* pcand;                              // [cap] candidate rank
   int* uf;                                 // [cap]
   unsigned* gkey;                          // [cap] root (group key), padding UINT_MAX

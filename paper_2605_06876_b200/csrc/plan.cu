@@ -93,7 +93,7 @@ struct adps_plan {
   // device normals (numpy PCG64 stream)
   Buf nrm_val, nrm_len, nrm_acc, nrm_reach, nrm_rmax, nrm_walked, nrm_idx, nrm_tmp;
   // merge / cap scratch (proposal space)
-  Buf small_list, pstart, n_groups, work_cnt, work_off, props_s, pcand, gkey, gval, gkey_sorted, gval_sorted,
+  Buf small_list, pstart, n_groups, work_cnt, work_off, props_s, psrc, pcand, gkey, gval, gkey_sorted, gval_sorted,
       grp_first, gpar, gext, gfirst_of, glist, scan3_val, scan3_flag, scan3_ticket, large_of, lp_cnt, lp_off, tile_cnt, tile_off, mkey,
       mval, mkey_sorted, mval_sorted, boxes, tile_pairs, gsoa;
   Buf scan_val, scan_flag, scan_ticket, scan2_val, scan2_flag, scan2_ticket, cub_tmp;
@@ -265,7 +265,7 @@ extern "C" adps_status adps_plan_destroy(adps_plan* P) {
                  &P->r_key_sorted, &P->r_order_in, &P->r_order, &P->r_tiles, &P->r_rect, &P->r_splat,
                  &P->r_offs, &P->r_dup, &P->r_dup_sorted, &P->r_tstart, &P->r_tend, &P->r_total,
                  &P->r_cams, &P->small_list, &P->pstart, &P->n_groups, &P->work_cnt, &P->work_off,
-                 &P->props_s, &P->pcand, &P->gkey, &P->gval, &P->gkey_sorted, &P->gval_sorted, &P->grp_first,
+                 &P->props_s, &P->psrc, &P->pcand, &P->gkey, &P->gval, &P->gkey_sorted, &P->gval_sorted, &P->grp_first,
                  &P->gpar, &P->gext, &P->gfirst_of, &P->glist, &P->scan3_val, &P->scan3_flag, &P->scan3_ticket,
                  &P->large_of, &P->lp_cnt, &P->lp_off, &P->tile_cnt, &P->tile_off, &P->mkey, &P->mval,
                  &P->mkey_sorted, &P->mval_sorted, &P->boxes, &P->tile_pairs, &P->gsoa, &P->deferred, &P->cand_bits, &P->rawc, &P->twords,
@@ -482,7 +482,9 @@ static AttributionArgs attr_args(adps_plan* P, int V, int H, int W, const adps_c
   a.n_deferred = &ctr->n_deferred;
   a.tile_path = P->tile_path;
   a.cand_bits = P->cand_bits.as<unsigned>();
-  a.raw = P->use_raw ? P->rawc.as<double>() : nullptr;
+  // the bit-plane path caches raw as fp32 (round toward zero), the others as fp64
+  a.raw = P->use_raw && !P->use_words ? P->rawc.as<double>() : nullptr;
+  a.rawf = P->use_words ? P->rawc.as<float>() : nullptr;
   a.words = P->use_words ? P->twords.as<uint4>() : nullptr;
   return a;
 }
@@ -566,10 +568,10 @@ extern "C" adps_status adps_step_phase1_begin(adps_plan* P, void* stream_v, cons
   CK(ensure(P->cams, 8ll * 18 * V));
   CK(ensure(P->border, 4ll * n_tiles * kBorderSlots));
   CK(ensure(P->deferred, 4ll * n_tiles));
-  CK(ensure(P->cand_bits, 4ll * V * ((hw + 31) / 32)));
+  CK(ensure(P->cand_bits, 4ll * V * ((hw + 31) / 32) + 4));   // + 1 word: tile_words_kernel reads one past a row
   P->use_raw = P->raw_cache && P->tile_path != 1 && !P->dbg_m && cfg->r_erode <= 3;
-  if (P->use_raw) CK(ensure(P->rawc, 8ll * total_px));
   P->use_words = P->use_raw && P->tile_path == 0 && cfg->l_bands <= 4;
+  if (P->use_raw) CK(ensure(P->rawc, (P->use_words ? 4ll : 8ll) * total_px));
   if (P->use_words) CK(ensure(P->twords, (long long)tile_words_bytes(V, H, W)));
   CK(ensure(P->ctr, sizeof(Counters)));
   if (P->cams_host_cap < V) {
@@ -841,6 +843,7 @@ static adps_status phase1_merge_part(adps_plan* P, cudaStream_t s) {
   CK(ensure(P->work_cnt, 8 * sc));
   CK(ensure(P->work_off, 8 * (sc + 1)));
   CK(ensure(P->props_s, sizeof(Proposal) * rc));
+  CK(ensure(P->psrc, 4 * rc));
   CK(ensure(P->pcand, 4 * rc));
   CK(ensure(P->gkey, 4 * rc));
   CK(ensure(P->gval, 4 * rc));
@@ -911,6 +914,7 @@ static adps_status phase1_merge_part(adps_plan* P, cudaStream_t s) {
   ma.n_max = cfg->n_max;
   ma.small_max = P->large_threshold;
   ma.props_s = P->props_s.as<Proposal>();
+  ma.psrc = P->psrc.as<int>();
   ma.pcand = P->pcand.as<int>();
   ma.uf = P->uf.as<int>();
   ma.gkey = P->gkey.as<unsigned>();
@@ -962,7 +966,7 @@ static adps_status phase1_merge_part(adps_plan* P, cudaStream_t s) {
     st = scan_state(P, P->scan3_val, P->scan3_flag, P->scan3_ticket, rc, &sst3);
     if (st != ADPS_OK) return st;
     CK(launch_merge_prepare(ma, n_split, sst3, s));
-    mark(P, "merge_prepare", s, 2);
+    mark(P, "merge_prepare", s, 3);
     // fork: the small parents' gates and the survivor scan (it only needs the
     // cases) run on the second stream while the large parents are gated
     CK(cudaEventRecord(P->ev_fork, s));

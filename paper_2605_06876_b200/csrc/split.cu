@@ -290,77 +290,99 @@ cudaError_t launch_offsets(const OffsetArgs& a, long long n_split, ScanState st_
 
 // ============================================================ emit
 __device__ __forceinline__ void copy_gaussian(const EmitArgs& a, long long src, long long dst) {
+  // all loads first: the output arrays may alias nothing, but the compiler
+  // cannot know, and interleaved load/store pairs would serialise on latency
+  float m[3], sc[3], dc[3], q[4];
   for (int t = 0; t < 3; ++t) {
-    a.mu[3 * dst + t] = a.g.mu[3 * src + t];
-    a.scale[3 * dst + t] = a.g.scale[3 * src + t];
-    a.sh_dc[3 * dst + t] = a.g.sh_dc[3 * src + t];
+    m[t] = __ldg(a.g.mu + 3 * src + t);
+    sc[t] = __ldg(a.g.scale + 3 * src + t);
+    dc[t] = __ldg(a.g.sh_dc + 3 * src + t);
   }
-  for (int t = 0; t < 4; ++t) a.rot[4 * dst + t] = a.g.rot[4 * src + t];
-  a.opacity[dst] = a.g.opacity[src];
+  for (int t = 0; t < 4; ++t) q[t] = __ldg(a.g.rot + 4 * src + t);
+  const float o = __ldg(a.g.opacity + src);
+  for (int t = 0; t < 3; ++t) {
+    a.mu[3 * dst + t] = m[t];
+    a.scale[3 * dst + t] = sc[t];
+    a.sh_dc[3 * dst + t] = dc[t];
+  }
+  for (int t = 0; t < 4; ++t) a.rot[4 * dst + t] = q[t];
+  a.opacity[dst] = o;
   const int K = a.g.sh_k;
   for (int t = 0; t < 3 * K; ++t) a.sh_rest[3ll * K * dst + t] = a.g.sh_rest[3ll * K * src + t];
 }
 
-__global__ void emit_kernel(EmitArgs a) {
-  const long long total = a.n + a.n_split + a.n_clone;
-  const long long ins_base = a.n_keep;
-  const long long clone_base = a.n_keep + a.n_inserted;
+// One launch, three block ranges: survivors (thread per old Gaussian, old
+// order), candidate inserts (a warp per candidate, lane = output row: N_i
+// children then the parent copy, or the fallback children), clones (thread
+// per clone).  Rows are written where the offsets put them.
+constexpr int kEmitThreads = 256;
+
+__device__ __forceinline__ void emit_insert_row(const EmitArgs& a, long long k, int j) {
+  const int c = a.cand_case[k];
+  const long long gi = a.split_list[k];
+  const long long dst = a.n_keep + a.ins_off[k] + j;
   const int K = a.g.sh_k;
-  for (long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x; t < total;
-       t += (long long)gridDim.x * blockDim.x) {
-    if (t < a.n) {                                        // survivors, old order
+  if (c == ADPS_CASE_FALLBACK) {                        // vanilla_split(parent, n, eta, rng)
+    double q[4] = {a.g.rot[4 * gi], a.g.rot[4 * gi + 1], a.g.rot[4 * gi + 2], a.g.rot[4 * gi + 3]};
+    double R[9];
+    quat_to_rot(q, R);
+    const double s[3] = {a.g.scale[3 * gi], a.g.scale[3 * gi + 1], a.g.scale[3 * gi + 2]};
+    const int nc = a.fb_children;
+    const double sh = a.eta * (double)nc;
+    const double* z = a.normals + 3ll * nc * a.fb_ord[k] + 3 * j;
+    const double dl[3] = {z[0] * s[0], z[1] * s[1], z[2] * s[2]};
+    copy_gaussian(a, gi, dst);
+    for (int i = 0; i < 3; ++i) {
+      const double off = R[i * 3] * dl[0] + R[i * 3 + 1] * dl[1] + R[i * 3 + 2] * dl[2];
+      a.mu[3 * dst + i] = (float)((double)a.g.mu[3 * gi + i] + off);
+      a.scale[3 * dst + i] = (float)(s[i] / sh);
+    }
+  } else {                                              // N_i children then the parent copy
+    const int ni = a.cand_merged[k];
+    if (j < ni) {
+      const float* c3 = a.children + 14ll * (a.cand_start[k] + j);
+      float c[14];
+      for (int u = 0; u < 14; ++u) c[u] = __ldg(c3 + u);
+      for (int u = 0; u < 3; ++u) {
+        a.mu[3 * dst + u] = c[u];
+        a.scale[3 * dst + u] = c[3 + u];
+        a.sh_dc[3 * dst + u] = c[11 + u];
+      }
+      for (int u = 0; u < 4; ++u) a.rot[4 * dst + u] = c[6 + u];
+      a.opacity[dst] = c[10];
+      for (int u = 0; u < 3 * K; ++u) a.sh_rest[3ll * K * dst + u] = 0.0f;
+    } else {
+      copy_gaussian(a, gi, dst);
+      const double o = (double)a.g.opacity[gi] / (double)(ni + 1);
+      a.opacity[dst] = (float)fmin(fmax(o, 1e-6), 1.0 - 1e-6);
+    }
+  }
+  a.index_map[dst] = -1;
+}
+
+__global__ void __launch_bounds__(kEmitThreads) emit_kernel(EmitArgs a, long long b_surv, long long b_ins) {
+  const long long blk = blockIdx.x;
+  if (blk < b_surv) {                                   // survivors, old order
+    const long long t = blk * kEmitThreads + threadIdx.x;
+    if (t < a.n) {
       const int pos = a.keep_pos[t];
       if (pos >= 0) {
         copy_gaussian(a, t, pos);
         a.index_map[pos] = t;
       }
-    } else if (t < a.n + a.n_split) {                     // candidate inserts, ascending index
-      const long long k = t - a.n;
-      const int c = a.cand_case[k];
-      if (c == ADPS_CASE_RESET) continue;
-      const long long gi = a.split_list[k];
-      long long dst = ins_base + a.ins_off[k];
-      if (c == ADPS_CASE_FALLBACK) {                      // vanilla_split(parent, n, eta, rng)
-        double q[4] = {a.g.rot[4 * gi], a.g.rot[4 * gi + 1], a.g.rot[4 * gi + 2], a.g.rot[4 * gi + 3]};
-        double R[9];
-        quat_to_rot(q, R);
-        const double s[3] = {a.g.scale[3 * gi], a.g.scale[3 * gi + 1], a.g.scale[3 * gi + 2]};
-        const int nc = a.fb_children;
-        const double sh = a.eta * (double)nc;
-        const double* z = a.normals + 3ll * nc * a.fb_ord[k];
-        for (int c2 = 0; c2 < nc; ++c2, ++dst) {
-          const double dl[3] = {z[3 * c2] * s[0], z[3 * c2 + 1] * s[1], z[3 * c2 + 2] * s[2]};
-          copy_gaussian(a, gi, dst);
-          for (int i = 0; i < 3; ++i) {
-            const double off = R[i * 3] * dl[0] + R[i * 3 + 1] * dl[1] + R[i * 3 + 2] * dl[2];
-            a.mu[3 * dst + i] = (float)((double)a.g.mu[3 * gi + i] + off);
-            a.scale[3 * dst + i] = (float)(s[i] / sh);
-          }
-          a.index_map[dst] = -1;
-        }
-      } else {                                            // N_i children then the parent copy
-        const int ni = a.cand_merged[k];
-        const float* ch = a.children + 14ll * a.cand_start[k];
-        for (int j = 0; j < ni; ++j, ++dst) {
-          const float* c3 = ch + 14 * j;
-          for (int u = 0; u < 3; ++u) {
-            a.mu[3 * dst + u] = c3[u];
-            a.scale[3 * dst + u] = c3[3 + u];
-            a.sh_dc[3 * dst + u] = c3[11 + u];
-          }
-          for (int u = 0; u < 4; ++u) a.rot[4 * dst + u] = c3[6 + u];
-          a.opacity[dst] = c3[10];
-          for (int u = 0; u < 3 * K; ++u) a.sh_rest[3ll * K * dst + u] = 0.0f;
-          a.index_map[dst] = -1;
-        }
-        copy_gaussian(a, gi, dst);
-        const double o = (double)a.g.opacity[gi] / (double)(ni + 1);
-        a.opacity[dst] = (float)fmin(fmax(o, 1e-6), 1.0 - 1e-6);
-        a.index_map[dst] = -1;
-      }
-    } else {                                              // clones, ascending
-      const long long j = t - a.n - a.n_split;
-      const long long dst = clone_base + j;
+    }
+  } else if (blk < b_surv + b_ins) {                    // candidate inserts, ascending index
+    const long long k = (blk - b_surv) * (kEmitThreads / 32) + (threadIdx.x >> 5);
+    const int lane = threadIdx.x & 31;
+    if (k >= a.n_split) return;
+    const int c = a.cand_case[k];
+    if (c == ADPS_CASE_RESET) return;
+    const int rows = c == ADPS_CASE_FALLBACK ? a.fb_children : a.cand_merged[k] + 1;
+    for (int j = lane; j < rows; j += 32) emit_insert_row(a, k, j);
+  } else {                                              // clones, ascending
+    const long long j = (blk - b_surv - b_ins) * kEmitThreads + threadIdx.x;
+    if (j < a.n_clone) {
+      const long long dst = a.n_keep + a.n_inserted + j;
       copy_gaussian(a, a.clone_list[j], dst);
       a.index_map[dst] = -1;
     }
@@ -368,12 +390,11 @@ __global__ void emit_kernel(EmitArgs a) {
 }
 
 cudaError_t launch_emit(const EmitArgs& a, cudaStream_t s) {
-  const long long total = a.n + a.n_split + a.n_clone;
-  if (total > 0) {
-    long long blocks = (total + 255) / 256;
-    if (blocks > 148 * 16) blocks = 148 * 16;
-    emit_kernel<<<(unsigned)blocks, 256, 0, s>>>(a);
-  }
+  const long long b_surv = (a.n + kEmitThreads - 1) / kEmitThreads;
+  const long long b_ins = (a.n_split + kEmitThreads / 32 - 1) / (kEmitThreads / 32);
+  const long long b_clone = (a.n_clone + kEmitThreads - 1) / kEmitThreads;
+  const long long blocks = b_surv + b_ins + b_clone;
+  if (blocks > 0) emit_kernel<<<(unsigned)blocks, kEmitThreads, 0, s>>>(a, b_surv, b_ins);
   return cudaGetLastError();
 }
 

@@ -25,14 +25,17 @@
 
 namespace adps {
 
-constexpr int kWarpMaxRuns = 256;
+#ifndef ADPS_TW_MAXRUNS
+#define ADPS_TW_MAXRUNS 192
+#endif
+constexpr int kWarpMaxRuns = ADPS_TW_MAXRUNS;
 constexpr int kWarpsPerBlock = 8;
 
 #ifndef ADPS_TW_FAST
 #define ADPS_TW_FAST 1
 #endif
 #ifndef ADPS_TW_MINBLOCKS
-#define ADPS_TW_MINBLOCKS 4
+#define ADPS_TW_MINBLOCKS 5
 #endif
 
 struct PostSmem {                   // used after the row scan
@@ -485,7 +488,25 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, ADPS_TW_MINBLOCKS) tile_w
 // Same run numbering, unions and records as tile_warp_kernel, so the results
 // are identical bit for bit (tests compare all CCL paths).
 
-__global__ void __launch_bounds__(256) tile_words_kernel(const double* __restrict__ raw,
+// raw >= X with raw known as f = RZ_fp32(raw) (bit pattern fi; non-negative
+// floats order as their bit patterns, the -1.0f sentinel is negative): with
+// Xf = RZ_fp32(X), raw >= X  <=>  fi > bits(Xf), or fi == bits(Xf) and X == Xf;
+// when fi == bits(Xf) and X is not a float the compare is ambiguous.  So
+// m = fi >= T with T = bits(Xf) + (X != Xf), ambiguous when fi == A with
+// A = bits(Xf) if X != Xf, else a value no pixel has.
+struct RzThreshold {
+  int T, A;
+};
+__device__ __forceinline__ RzThreshold rz_threshold(double X) {
+  const float xf = __double2float_rz(X);   // +inf stays +inf
+  const int k = __float_as_int(xf);
+  const bool exact = (double)xf == X;
+  return {exact ? k : k + 1, exact ? (int)0x80000000 : k};
+}
+
+__global__ void __launch_bounds__(256) tile_words_kernel(const float* __restrict__ rawf,
+                                                         const float* __restrict__ image,
+                                                         const float* __restrict__ gt,
                                                          const unsigned* __restrict__ cand_bits,
                                                          const double* __restrict__ thr_raw, int L, int H, int W,
                                                          int WW, int v0, uint4* __restrict__ words) {
@@ -496,45 +517,72 @@ __global__ void __launch_bounds__(256) tile_words_kernel(const double* __restric
   const int lane = threadIdx.x & 31;
   const long long hw = (long long)H * W;
   const long long nwords = (hw + 31) / 32;
-  const double* rrow = raw + (long long)v * hw + (long long)y * W;
+  const long long p_row = (long long)y * W;
+  const int* rrow = reinterpret_cast<const int*>(rawf + (long long)v * hw + p_row);
   const unsigned* cv = cand_bits + (long long)v * nwords;
   uint4* wrow = words + ((long long)v * H + y) * WW;
-  // raw >= +0.0 and the thresholds are >= +0.0 or +inf, so IEEE order is the
-  // signed order of the bit patterns: integer compares, no fp64 pipe
-  const long long kInf = 0x7ff0000000000000ll;
   const double* tv = thr_raw + (long long)v * L;
-  const long long xm = __double_as_longlong(__ldg(tv));
-  const long long t1 = L > 1 ? __double_as_longlong(__ldg(tv + 1)) : kInf;
-  const long long t2 = L > 2 ? __double_as_longlong(__ldg(tv + 2)) : kInf;
-  const long long t3 = L > 3 ? __double_as_longlong(__ldg(tv + 3)) : kInf;
-  const long long* rrow_i = reinterpret_cast<const long long*>(rrow);
-  const long long p_row = (long long)y * W;
+  const double kInf = __longlong_as_double(0x7ff0000000000000ll);
+  const double X0 = __ldg(tv), X1 = L > 1 ? __ldg(tv + 1) : kInf, X2 = L > 2 ? __ldg(tv + 2) : kInf,
+               X3 = L > 3 ? __ldg(tv + 3) : kInf;
+  const RzThreshold R0 = rz_threshold(X0), R1 = rz_threshold(X1), R2 = rz_threshold(X2), R3 = rz_threshold(X3);
+  const int sh = (int)(p_row & 31);
+  const unsigned* crow = cv + (p_row >> 5);   // linear candidate words of this row (+1 padding word)
+  auto emit_word = [&](int wx, int fi, unsigned lo, unsigned hi) {
+    bool m = fi >= R0.T;
+    int band = (fi >= R1.T) + (fi >= R2.T) + (fi >= R3.T);
+    const bool amb = (fi == R0.A) | (fi == R1.A) | (fi == R2.A) | (fi == R3.A);
+    if (__any_sync(0xffffffffu, amb) && amb) {   // rare: the exact fp64 raw error, numpy order
+      const long long p = (long long)v * hw + p_row + wx * 32 + lane;
+      const float* a3 = image + 3 * p;
+      const float* g3 = gt + 3 * p;
+      const double d0 = fabs(dsub((double)a3[0], (double)g3[0]));
+      const double d1 = fabs(dsub((double)a3[1], (double)g3[1]));
+      const double d2 = fabs(dsub((double)a3[2], (double)g3[2]));
+      const double xr = dadd(dadd(d0, d1), d2);
+      m = xr >= X0;
+      band = (xr >= X1) + (xr >= X2) + (xr >= X3);
+    }
+    const unsigned M = __ballot_sync(0xffffffffu, m);
+    const unsigned B0 = __ballot_sync(0xffffffffu, band & 1);
+    const unsigned B1 = __ballot_sync(0xffffffffu, band & 2);
+    unsigned C = __funnelshift_r(lo, hi, sh);
+    const int valid = W - wx * 32;   // columns of this word inside the row
+    if (valid < 32) C &= (1u << valid) - 1u;
+    return make_uint4(M, C, B0, B1);
+  };
   constexpr int U = 8;
-  for (int wx0 = 0; wx0 < WW; wx0 += U) {
-    long long r[U];
-    unsigned lo[U], hi[U];
+  const int WWf = W >> 5;   // full words
+  int wx0 = 0;
+  for (; wx0 + U <= WWf; wx0 += U) {   // full words: no bounds checks
+    int r[U];
+    unsigned cw[U + 1];
+#pragma unroll
+    for (int u = 0; u < U; ++u) r[u] = __ldg(rrow + (wx0 + u) * 32 + lane);
+#pragma unroll
+    for (int u = 0; u <= U; ++u) cw[u] = __ldg(crow + wx0 + u);
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const uint4 q = emit_word(wx0 + u, r[u], cw[u], cw[u + 1]);
+      if (lane == u) wrow[wx0 + u] = q;
+    }
+  }
+  if (wx0 < WW) {   // the rest (< U words), loads issued together
+    int r[U];
+    unsigned cw[U + 1];
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       const int x = (wx0 + u) * 32 + lane;
-      r[u] = x < W ? __ldg(rrow_i + x) : -1ll;   // below every threshold
-      // the candidate bits of this word: a funnel shift of two linear words
-      const long long p0 = p_row + (wx0 + u) * 32;
-      const long long i0 = p0 >> 5;
-      lo[u] = wx0 + u < WW ? __ldg(cv + i0) : 0u;
-      hi[u] = (wx0 + u < WW && (p0 & 31) && i0 + 1 < nwords) ? __ldg(cv + i0 + 1) : 0u;
+      r[u] = x < W ? __ldg(rrow + x) : (int)0xbf800000;   // -1.0f: below every threshold
     }
-    const int sh = (int)(p_row & 31);
+#pragma unroll
+    for (int u = 0; u <= U; ++u) cw[u] = wx0 + u <= WW ? __ldg(crow + wx0 + u) : 0u;
 #pragma unroll
     for (int u = 0; u < U; ++u) {
-      const int wx = wx0 + u;
-      const int band = (r[u] >= t1) + (r[u] >= t2) + (r[u] >= t3);
-      const unsigned M = __ballot_sync(0xffffffffu, r[u] >= xm);
-      const unsigned B0 = __ballot_sync(0xffffffffu, band & 1);
-      const unsigned B1 = __ballot_sync(0xffffffffu, band & 2);
-      const int valid = W - wx * 32;   // columns of this word inside the row
-      unsigned C = __funnelshift_r(lo[u], hi[u], sh);
-      if (valid < 32) C &= (1u << (valid > 0 ? valid : 0)) - 1u;
-      if (lane == u && wx < WW) wrow[wx] = make_uint4(M, C, B0, B1);
+      if (wx0 + u < WW) {   // warp-uniform
+        const uint4 q = emit_word(wx0 + u, r[u], cw[u], cw[u + 1]);
+        if (lane == u) wrow[wx0 + u] = q;
+      }
     }
   }
 }
@@ -727,8 +775,8 @@ cudaError_t launch_tile_bits(const TileParams& P, int v0, int v1, cudaStream_t s
   const int per_view = P.H * WW;
   (void)per_view;
   const unsigned gx = (unsigned)((P.H + 7) / 8);   // warp per image row, 8 rows per block
-  tile_words_kernel<<<dim3(gx, (unsigned)(v1 - v0)), 256, 0, s>>>(P.raw, P.cand_bits, P.thr_raw, P.L, P.H, P.W, WW,
-                                                                   v0, P.words);
+  tile_words_kernel<<<dim3(gx, (unsigned)(v1 - v0)), 256, 0, s>>>(P.rawf, P.image, P.gt, P.cand_bits, P.thr_raw,
+                                                                   P.L, P.H, P.W, WW, v0, P.words);
   const long long tpv = (long long)P.tiles_x * P.tiles_y;
   const long long t0 = tpv * v0, t1 = tpv * v1;
   const size_t smem = tile_warp_smem_bytes();

@@ -97,8 +97,10 @@ def test_maps_bit_exact(op, plan, c):
 
 
 # ------------------------------------------------------------------ partition
-def _injected_partition(op, plan, e, dom, n_gauss, l_bands, m_min, cands, tau=0.1, r_erode=1, deferred=None):
-    """Run phase 1 with error map e injected exactly (raw = e, lo = 0, hi = 1).
+def _injected_partition(op, plan, e, dom, n_gauss, l_bands, m_min, cands, tau=0.1, r_erode=1, deferred=None,
+                        e2=None):
+    """Run phase 1 with error map e injected exactly (raw = e, lo = 0, hi = 1;
+    raw = e + e2 in fp64 when a second channel e2 is given).
 
     Both CCL paths run (block kernel for every tile, then the warp kernel with
     its deferred tiles) and must agree bit for bit; returns (warp path, oracle)."""
@@ -108,6 +110,10 @@ def _injected_partition(op, plan, e, dom, n_gauss, l_bands, m_min, cands, tau=0.
     e.flat[0], e.flat[-1] = 0.0, 1.0
     rendered = np.zeros((h, w, 3), np.float32)
     rendered[..., 0] = e
+    if e2 is not None:
+        e2 = e2.astype(np.float32)
+        e2.flat[0], e2.flat[-1] = 0.0, 0.0
+        rendered[..., 1] = e2
     gt = np.zeros((h, w, 3), np.float32)
     rng = np.random.default_rng(0)
     g = O.Gaussians(rng.uniform(-0.2, 0.2, (n_gauss, 3)), np.full((n_gauss, 3), 0.3),
@@ -188,6 +194,22 @@ def test_partition_erosion_both_paths(op, plan, seed, r_erode, l_bands):
     got, want = _injected_partition(op, plan, e, dom, n, l_bands, int(rng.integers(1, 4)),
                                     [0, 1, 3, 4], r_erode=r_erode)
     np.testing.assert_array_equal(got, want)
+
+
+@pytest.mark.parametrize("seed", range(3))
+def test_partition_fp32_cache_near_thresholds(op, plan, seed):
+    """Raw errors within one fp32 ulp of the metric threshold and a band edge:
+    the bit-plane path's fp32 (round-toward-zero) raw cache cannot decide those
+    compares and must redo them exactly in fp64 (same bits as the block CCL)."""
+    rng = np.random.default_rng(300 + seed)
+    h, w = 70, 90
+    dom = np.kron(rng.integers(-1, 4, (h // 2 + 1, w // 2 + 1)), np.ones((2, 2), np.int64))[:h, :w]
+    base = np.where(rng.uniform(size=(h, w)) < 0.5, np.float32(0.099999994), np.float32(0.39999998))
+    e = base.astype(np.float32)
+    e2 = rng.uniform(0.0, 4e-8, (h, w)).astype(np.float32)   # raw = e + e2 straddles the thresholds
+    got, want = _injected_partition(op, plan, e, dom, 4, 3, 1, [0, 1, 2], e2=e2)
+    np.testing.assert_array_equal(got, want)
+    assert len(want) > 0
 
 
 @pytest.mark.parametrize("shape", [(64, 64), (70, 45)])
