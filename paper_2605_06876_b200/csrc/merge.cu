@@ -327,6 +327,7 @@ cudaError_t launch_merge_small_gates(const MergeArgs& a, cudaStream_t s) {
 // whose minimum centre distance gives (dmin/sA + dmin/sB) > gamma_d, or whose
 // rgb boxes are more than gamma_c apart, contains no mergeable pair.
 enum { kG_mu = 0, kG_rgb = 3, kG_inv = 6, kG_prec = 7, kG_fields = 13 };   // gsoa fields
+enum { kF_mu = 0, kF_rgb = 3, kF_inv = 6, kF_fields = 7 };                  // fsoa fields
 
 __device__ __forceinline__ unsigned spread10(unsigned v) {
   v &= 0x3ffu;
@@ -397,6 +398,11 @@ __global__ void box_kernel(MergeArgs a) {
       }
       a.gsoa[(long long)kG_inv * a.soa_cap + m] = M.inv_smax;
       for (int k = 0; k < 6; ++k) a.gsoa[(long long)(kG_prec + k) * a.soa_cap + m] = M.prec[k];
+      for (int c = 0; c < 3; ++c) {   // fp32 (round to nearest) copies for the conservative prefilter
+        a.fsoa[(long long)(kF_mu + c) * a.soa_cap + m] = (float)M.mu[c];
+        a.fsoa[(long long)(kF_rgb + c) * a.soa_cap + m] = (float)M.rgb[c];
+      }
+      a.fsoa[(long long)kF_inv * a.soa_cap + m] = (float)M.inv_smax;
       for (int c = 0; c < 3; ++c) {
         s[c] += M.mu[c];
         lo[c] = fmin(lo[c], M.rgb[c]);
@@ -501,27 +507,6 @@ __global__ void tile_pair_filter_kernel(MergeArgs a) {
 // of arrays (written by box_kernel): contiguous 64-proposal tiles load
 // coalesced, 13 doubles per proposal instead of a gathered 152-byte record.
 
-__device__ __forceinline__ bool gate_soa(const double* A, const double (*Bs)[kMT], int j, double gd, double gc) {
-  const double dc = fmax(fmax(fabs(A[kG_rgb + 0] - Bs[kG_rgb + 0][j]), fabs(A[kG_rgb + 1] - Bs[kG_rgb + 1][j])),
-                         fabs(A[kG_rgb + 2] - Bs[kG_rgb + 2][j]));
-  if (!(dc <= gc)) return false;
-  const double dl[3] = {Bs[kG_mu + 0][j] - A[kG_mu + 0], Bs[kG_mu + 1][j] - A[kG_mu + 1],
-                        Bs[kG_mu + 2][j] - A[kG_mu + 2]};
-  const double n2 = dl[0] * dl[0] + dl[1] * dl[1] + dl[2] * dl[2];
-  const double w = A[kG_inv] + Bs[kG_inv][j];
-  if (n2 * w * w > gd * gd * (1.0 + 1e-9)) return false;
-  double pb[6];
-#pragma unroll
-  for (int k = 0; k < 6; ++k) pb[k] = Bs[kG_prec + k][j];
-  const double d = sqrt(fmax(sym_quad(A + kG_prec, dl), 0.0)) + sqrt(fmax(sym_quad(pb, dl), 0.0));
-  return d <= gd;
-}
-
-struct SideBuf {
-  double s[kG_fields][kMT];   // [field][proposal]
-  int q[kMT];
-};
-
 __device__ __forceinline__ void cp_async(void* dst, const void* src, int bytes) {
   const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
   if (bytes == 8) asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(d), "l"(src) : "memory");
@@ -531,92 +516,155 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
-// stage the gate operands of tile bt of large parent l into B (asynchronous copies)
-__device__ __forceinline__ void stage_tile(const MergeArgs& a, SideBuf& B, long long l, long long bt) {
+// the exact gate of row operand A (registers) against column jj of a staged tile
+__device__ __forceinline__ bool gate_col(const double* A, const double (*Js)[kMT], int jj, double gd, double gd2,
+                                         double gc) {
+  const double dc = fmax(fmax(fabs(A[kG_rgb + 0] - Js[kG_rgb + 0][jj]), fabs(A[kG_rgb + 1] - Js[kG_rgb + 1][jj])),
+                         fabs(A[kG_rgb + 2] - Js[kG_rgb + 2][jj]));
+  if (!(dc <= gc)) return false;
+  const double dl[3] = {Js[kG_mu + 0][jj] - A[kG_mu + 0], Js[kG_mu + 1][jj] - A[kG_mu + 1],
+                        Js[kG_mu + 2][jj] - A[kG_mu + 2]};
+  const double n2 = dl[0] * dl[0] + dl[1] * dl[1] + dl[2] * dl[2];
+  const double w = A[kG_inv] + Js[kG_inv][jj];
+  if (n2 * w * w > gd2) return false;   // exact early reject (|d|/s_max bounds each term)
+  double pb[6];
+#pragma unroll
+  for (int k = 0; k < 6; ++k) pb[k] = Js[kG_prec + k][jj];
+  const double d = sqrt(fmax(sym_quad(A + kG_prec, dl), 0.0)) + sqrt(fmax(sym_quad(pb, dl), 0.0));
+  return d <= gd;
+}
+
+struct ColTile {
+  double s[kG_fields][kMT];   // [field][proposal]
+  float f[kF_fields][kMT];
+  int q[kMT];
+};
+
+// Conservative fp32 reject, exact in effect: true only when the fp64 gate
+// certainly fails.  Operands are the fp64 values rounded to nearest fp32
+// (relative error <= 2^-24 each); every bound below carries slack for that
+// and for the fp32 arithmetic:
+//   colour: |fb - fa| >= |b - a| - 3*2^-24*(|a| + |b|), so a computed
+//           difference above gc + 4e-7 * (|fa| + |fb| + 1) means > gc;
+//   distance: |d_c| >= |fb_c - fa_c| - 4e-7 * (|fa_c| + |fb_c|) per
+//           component, w >= (fa_inv + fb_inv)(1 - 1e-6), and the fp64
+//           early reject |d|^2 w^2 > gd^2 (1 + 1e-9) implies the gate fails.
+__device__ __forceinline__ bool reject32(const float* Af, const float (*Jf)[kMT], int jj, float gc, float gd2_hi) {
+  float dcx = 0.0f;
+#pragma unroll
+  for (int c = 0; c < 3; ++c) {
+    const float a = Af[kF_rgb + c], b = Jf[kF_rgb + c][jj];
+    const float d = fabsf(b - a) - 4e-7f * (fabsf(a) + fabsf(b) + 1.0f);
+    dcx = fmaxf(dcx, d);
+  }
+  if (dcx > gc) return true;
+  float n2 = 0.0f;
+#pragma unroll
+  for (int c = 0; c < 3; ++c) {
+    const float a = Af[kF_mu + c], b = Jf[kF_mu + c][jj];
+    const float d = fmaxf(fabsf(b - a) - 4e-7f * (fabsf(a) + fabsf(b)), 0.0f);
+    n2 += d * d;
+  }
+  const float w = (Af[kF_inv] + Jf[kF_inv][jj]) * (1.0f - 1e-6f);
+  return n2 * (1.0f - 1e-5f) * w * w > gd2_hi;
+}
+constexpr int kPairWarps = 4;
+
+// stage tile bt of large parent l into a warp's buffer (lane = proposal)
+__device__ __forceinline__ void stage_col(const MergeArgs& a, ColTile& B, long long l, long long bt, int lane) {
   const long long P = (long long)a.lp_cnt[l];
   const long long base = (long long)a.lp_off[l] + bt * kMT;
-  const int nt = (int)min((long long)kMT, P - bt * kMT);
-  for (int t = threadIdx.x; t < kG_fields * kMT; t += blockDim.x) {
-    const int f = t / kMT, loc = t % kMT;
-    if (loc < nt) cp_async(&B.s[f][loc], a.gsoa + (long long)f * a.soa_cap + base + loc, 8);
+  if (bt * kMT + lane < P) {
+#pragma unroll
+    for (int f = 0; f < kG_fields; ++f) cp_async(&B.s[f][lane], a.gsoa + (long long)f * a.soa_cap + base + lane, 8);
+#pragma unroll
+    for (int f = 0; f < kF_fields; ++f) cp_async(&B.f[f][lane], a.fsoa + (long long)f * a.soa_cap + base + lane, 4);
+    cp_async(&B.q[lane], a.mval_sorted + base + lane, 4);
   }
-  for (int t = threadIdx.x; t < kMT; t += blockDim.x)
-    if (t < nt) cp_async(&B.q[t], a.mval_sorted + base + t, 4);
   cp_async_commit();
 }
 
-__device__ __forceinline__ void gates_pair(const MergeArgs& a, const SideBuf& I, const SideBuf& J, long long l,
-                                           long long bi, long long bj) {
-  const long long P = (long long)a.lp_cnt[l];
-  const int ni = (int)min((long long)kMT, P - bi * kMT), nj = (int)min((long long)kMT, P - bj * kMT);
-  // lanes take different columns jj of one row ii: the unions of a warp then hit
-  // different roots (lanes sharing a column would contend on one atomic)
-  for (int t = threadIdx.x; t < kMT * kMT; t += blockDim.x) {
-    const int ii = t / kMT, jj = t % kMT;
-    // unordered pairs: within a diagonal tile take ii < jj once
-    if (ii < ni && jj < nj && (bi != bj || ii < jj)) {
-      double A[kG_fields];
-#pragma unroll
-      for (int f = 0; f < kG_fields; ++f) A[f] = I.s[f][ii];
-      const bool ok = gate_soa(A, J.s, jj, a.gamma_d, a.gamma_c);
-#if ADPS_MERGE_STATS
-      atomicAdd(&a.ctr->stat_gates, 1ull);
-      if (ok) atomicAdd(&a.ctr->stat_pass, 1ull);
-#endif
-      if (ok) uf_unite(a.uf, I.q[ii], J.q[jj]);
-    }
-  }
-}
-
-// the surviving kMT x kMT tile pairs of the large parents' gate matrices, in
-// contiguous chunks per CTA: pairs of one tile row are adjacent, so tile bi
-// stays resident and only tile bj is staged (cp.async, one pair ahead); if the
-// survivor list overflowed, every tile pair with the box test inline
-__global__ void __launch_bounds__(256) pair_tiles_kernel(MergeArgs a) {
-  __shared__ SideBuf bi_buf, bj_buf[2];
+// The surviving kMT x kMT tile pairs of the large parents' gate matrices, a
+// warp per pair and contiguous chunks of pairs per warp (pairs of one tile
+// row are adjacent): lane = row proposal with its gate operands in registers
+// while the row lasts, the column tile staged in shared memory one pair ahead
+// (cp.async), no block barriers.  If the survivor list overflowed, every tile
+// pair is taken with the box test inline.
+__global__ void __launch_bounds__(kPairWarps * 32) pair_tiles_kernel(MergeArgs a) {
+  extern __shared__ __align__(16) unsigned char pt_smem[];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  ColTile* buf = reinterpret_cast<ColTile*>(pt_smem) + 2 * wid;
   const bool overflow = (a.ctr->overflow & 4u) != 0;
   const long long n_large = (long long)a.ctr->n_large;
-  if (overflow) {
-    const unsigned long long W = n_large > 0 ? a.work_off[n_large] : 0;
-    for (unsigned long long w = blockIdx.x; w < W; w += gridDim.x) {
-      long long l, bi, bj;
-      decode_tile_pair(a, n_large, w, l, bi, bj);
-      const long long tb = (long long)a.tile_off[l];
-      if (!boxes_may_merge(a.boxes[tb + bi], a.boxes[tb + bj], a.gamma_d, a.gamma_c)) continue;   // uniform
-      stage_tile(a, bi_buf, l, bi);
-      stage_tile(a, bj_buf[0], l, bj);
-      cp_async_wait<0>();
-      __syncthreads();
-      gates_pair(a, bi_buf, bj_buf[0], l, bi, bj);
-      __syncthreads();
-    }
-    return;
-  }
-  const long long W = (long long)a.ctr->n_tile_pairs;
-  const long long chunk = (W + gridDim.x - 1) / gridDim.x;
-  const long long w0 = (long long)blockIdx.x * chunk, w1 = min(W, w0 + chunk);
+  const long long nwarps = (long long)gridDim.x * kPairWarps;
+  const long long gw = (long long)blockIdx.x * kPairWarps + wid;
+  const double gd = a.gamma_d, gc = a.gamma_c, gd2 = gd * gd * (1.0 + 1e-9);
+  const long long W = overflow ? (long long)(n_large > 0 ? a.work_off[n_large] : 0) : (long long)a.ctr->n_tile_pairs;
+  const long long chunk = (W + nwarps - 1) / nwarps;
+  const long long w0 = gw * chunk, w1 = min(W, w0 + chunk);
+  auto pair_at = [&](long long w) -> int4 {
+    if (!overflow) return a.tile_pairs[w];
+    long long l, bi, bj;
+    decode_tile_pair(a, n_large, (unsigned long long)w, l, bi, bj);
+    const long long tb = (long long)a.tile_off[l];
+    const bool live = boxes_may_merge(a.boxes[tb + bi], a.boxes[tb + bj], a.gamma_d, a.gamma_c);
+    return make_int4((int)l, (int)bi, (int)bj, live ? 1 : 0);
+  };
   if (w0 >= w1) return;
   long long cur_l = -1, cur_bi = -1;
-  int4 cur = a.tile_pairs[w0];
-  stage_tile(a, bj_buf[0], cur.x, cur.z);
+  double A[kG_fields];
+  float Af[kF_fields];
+  int qa = -1, ni = 0;
+  const float gc32 = (float)gc, gd2_hi = (float)(gd * gd) * (1.0f + 1e-5f);
+  int4 cur = pair_at(w0);
+  stage_col(a, buf[0], cur.x, cur.z, lane);
   for (long long w = w0; w < w1; ++w) {
     const int it = (int)(w - w0);
-    if (cur.x != cur_l || cur.y != cur_bi) {   // new tile row: stage tile bi (rare)
-      stage_tile(a, bi_buf, cur.x, cur.y);
+    if (cur.x != cur_l || cur.y != cur_bi) {   // new tile row: its operands into registers
       cur_l = cur.x;
       cur_bi = cur.y;
+      const long long P = (long long)a.lp_cnt[cur_l];
+      ni = (int)min((long long)kMT, P - cur_bi * kMT);
+      const long long m = (long long)a.lp_off[cur_l] + cur_bi * kMT + lane;
+      if (lane < ni) {
+#pragma unroll
+        for (int f = 0; f < kG_fields; ++f) A[f] = __ldg(a.gsoa + (long long)f * a.soa_cap + m);
+#pragma unroll
+        for (int f = 0; f < kF_fields; ++f) Af[f] = __ldg(a.fsoa + (long long)f * a.soa_cap + m);
+        qa = __ldg(a.mval_sorted + m);
+      }
     }
     int4 nxt = cur;
     if (w + 1 < w1) {
-      nxt = a.tile_pairs[w + 1];
-      stage_tile(a, bj_buf[(it + 1) & 1], nxt.x, nxt.z);
+      nxt = pair_at(w + 1);
+      stage_col(a, buf[(it + 1) & 1], nxt.x, nxt.z, lane);
       cp_async_wait<1>();
     } else {
       cp_async_wait<0>();
     }
-    __syncthreads();
-    gates_pair(a, bi_buf, bj_buf[it & 1], cur.x, cur.y, cur.z);
-    __syncthreads();   // both buffers are restaged from the next iteration on
+    __syncwarp();
+    if (!overflow || cur.w) {
+      const ColTile& J = buf[it & 1];
+      const long long P = (long long)a.lp_cnt[cur.x];
+      const int nj = (int)min((long long)kMT, P - (long long)cur.z * kMT);
+      const bool diag = cur.y == cur.z;
+      if (lane < ni) {
+        // gates first, unions after: a union inside the column loop would stall
+        // the whole warp on one lane's union-find latency whenever any lane passes
+        unsigned pass = 0u;
+        for (int jj = diag ? lane + 1 : 0; jj < nj; ++jj) {   // unordered pairs: ii < jj on the diagonal
+          if (reject32(Af, J.f, jj, gc32, gd2_hi)) continue;
+          const bool ok = gate_col(A, J.s, jj, gd, gd2, gc);
+#if ADPS_MERGE_STATS
+          atomicAdd(&a.ctr->stat_gates, 1ull);
+          if (ok) atomicAdd(&a.ctr->stat_pass, 1ull);
+#endif
+          if (ok) pass |= 1u << jj;
+        }
+        for (; pass; pass &= pass - 1u) uf_unite(a.uf, qa, J.q[__ffs(pass) - 1]);
+      }
+    }
+    __syncwarp();   // this buffer is restaged two pairs on
     cur = nxt;
   }
 }
@@ -624,7 +672,10 @@ __global__ void __launch_bounds__(256) pair_tiles_kernel(MergeArgs a) {
 cudaError_t launch_merge_tile_gates(const MergeArgs& a, cudaStream_t s) {
   box_kernel<<<a.grid, 256, 0, s>>>(a);
   tile_pair_filter_kernel<<<a.grid, 256, 0, s>>>(a);   // warp per tile row
-  pair_tiles_kernel<<<a.grid, 256, 0, s>>>(a);
+  const int smem = (int)(sizeof(ColTile) * 2 * kPairWarps);
+  cudaError_t e = cudaFuncSetAttribute(pair_tiles_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  if (e != cudaSuccess) return e;
+  pair_tiles_kernel<<<a.grid * 2, kPairWarps * 32, smem, s>>>(a);
   return cudaGetLastError();
 }
 
