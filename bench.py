@@ -13,11 +13,13 @@ including it under "full_step".
   e2e       the same step through the public API from pinned HOST buffers
             (image, gt, dominant, params, stats copied in; grown params and
             index_map copied out) inside the timed region
-  roofline  the dominant kernel (tile_warp_kernel: maps + erosion + CCL +
-            moments); algorithmic bytes 12.125 B/px (cached fp64 raw error 8 B,
-            dominant id 4 B, candidate bit) / its CUDA-event time, vs
-            MEASURED_PEAKS.  "minmax" reports the pass that reads the 28 B/px
-            inputs once (and writes the 8.125 B/px cache) the same way.
+  roofline  the dominant kernel, minmax_kernel: the one pass over the step's
+            attribution inputs (28 B/px = image fp32x3 + gt
+            fp32x3 + dominant int32) / its CUDA-event time, vs MEASURED_PEAKS;
+            traffic = its ncu dram bytes (it also writes the 4.125 B/px
+            fp32 raw-error cache and candidate bits).  "tile_pass" reports the
+            bit-plane pass (tile_words_kernel, HBM: 4.125 B/px read) and the
+            warp CCL (tile_bits_kernel, latency-bound) that follow.
   cpu_baseline  the oracle port on a bounded view sample (rank 0, N=1)
 
 Usage: python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
@@ -42,8 +44,8 @@ sys.path.insert(0, ROOT)
 METRIC = "AdpSplit densify-step ms & parents/s at 1M Gaussians; stat-accum GB/s vs HBM"
 UNIT = "parents/s"
 BYTES_PER_PX = 28      # image fp32x3 + gt fp32x3 + dominant int32 (the step's attribution inputs)
-TILE_BYTES_PER_PX = 8 + 4 + 0.125      # tile pass: cached raw L1 error f64 + dominant int32 + candidate bit
-MINMAX_BYTES_PER_PX = 28 + 8 + 0.125   # minmax pass: inputs read once, raw cache + candidate bits written
+WORDS_BYTES_PER_PX = 4 + 0.125 + 0.5   # bit-plane pass: fp32 raw cache + candidate bits read, 4 bit planes written
+MINMAX_TRAFFIC_PER_PX = 28 + 4 + 0.125   # minmax pass: inputs read once, fp32 raw cache + candidate bits written
 BYTES_PER_G_IN = 72    # params 56 B + grad_accum/denom 2 x f64
 BYTES_PER_G_OUT = 64   # params 56 B + index_map int64
 
@@ -58,13 +60,13 @@ def load_peaks():
 
 
 def load_traffic(config):
-    """dram bytes per tile_kernel launch from the committed ncu summary, if any."""
+    """dram bytes (read + write) of one minmax_kernel launch from the committed ncu summary, if any."""
     p = os.path.join(ROOT, "profiles", "traffic.json")
     if not os.path.exists(p):
         return None
     with open(p) as f:
         d = json.load(f)
-    return d.get(config, {}).get("tile_kernel_dram_bytes")
+    return d.get(config, {}).get("minmax_kernel_dram_bytes")
 
 
 class ClockSampler:
@@ -334,11 +336,10 @@ def run_ours(args, wl):
     px = V * H * W
     peak, peak_kind = load_peaks()
     tile_ms = stages.get("tile_ccl", float("nan"))
+    mm_ms = stages.get("minmax", float("nan"))
     # stat-accum: 28 B/px over the attribution stages (maps, partition, stats)
-    attr_ms = stages.get("minmax_dominance", 0) + stages.get("tile_ccl", 0) + stages.get("border_merge", 0)
-    achieved = TILE_BYTES_PER_PX * px / (tile_ms * 1e-3) / 1e9
-    mm_ms = stages.get("minmax_dominance", float("nan"))
-    mm_gbs = MINMAX_BYTES_PER_PX * px / (mm_ms * 1e-3) / 1e9
+    attr_ms = sum(stages.get(k_, 0) for k_ in ("minmax", "thresholds", "tile_ccl", "border_merge"))
+    achieved = BYTES_PER_PX * px / (mm_ms * 1e-3) / 1e9
     traffic = load_traffic(wl.name)
     b_step = BYTES_PER_PX * px + BYTES_PER_G_IN * g.n + BYTES_PER_G_OUT * counts["n_out"]
 
@@ -412,14 +413,15 @@ def run_ours(args, wl):
             "stat_accum": {"GB/s": BYTES_PER_PX * px / (attr_ms * 1e-3) / 1e9, "frac": None, "ms": attr_ms},
             "step_roofline": {"bytes": int(b_step), "GB/s": b_step / (ms * 1e-3) / 1e9,
                               "frac": b_step / (ms * 1e-3) / 1e9 / peak},
-            "roofline": {"bound": "hbm", "kernel": "tile_warp_kernel (maps+erosion+CCL+moments)",
+            "roofline": {"bound": "hbm", "kernel": "minmax_kernel (input pass: raw L1 error, per-view min/max, "
+                                                    "ever-dominant flags, candidate bits, fp32 raw cache)",
                          "achieved": achieved, "peak": peak, "peak_kind": peak_kind, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,
-                         "algorithmic_bytes_per_launch": TILE_BYTES_PER_PX * px, "ms_per_launch": tile_ms,
-                         "note": "issue/latency-bound (profiles/r01_ncu_top3.txt); traffic = ncu dram bytes"},
-            "minmax": {"bound": "hbm", "kernel": "minmax_kernel (per-view min/max, dominance flags, caches)",
-                       "achieved": mm_gbs, "frac": mm_gbs / peak, "ms_per_launch": mm_ms,
-                       "algorithmic_bytes_per_launch": MINMAX_BYTES_PER_PX * px},
+                         "algorithmic_bytes_per_launch": BYTES_PER_PX * px, "ms_per_launch": mm_ms,
+                         "note": "achieved counts the 28 B/px inputs only; traffic = ncu dram read+write of one "
+                                 "launch (incl. the 4.125 B/px cache it writes), profiles/"},
+            "tile_pass": {"ms": tile_ms, "kernels": "tile_words_kernel (HBM) + tile_bits_kernel (latency-bound CCL)",
+                          "words_bytes_per_launch": WORDS_BYTES_PER_PX * px},
             "stages_ms": stages,
             "render": {"ms_per_view": render_ms / V, "ms_total": render_ms, "views": V,
                        "note": "attribution render (compute-bound), not part of value"},

@@ -524,33 +524,46 @@ __device__ __forceinline__ int border_slot(int lx, int ly) {
 }
 
 __global__ void border_kernel(BorderParams P) {
+  // 128 threads = the tile's border slots; warp w = side w (top, bottom, left,
+  // right).  Runs along an edge ask for the same union many times: lanes
+  // holding the same (fragment, neighbour fragment) pair unite once (match_any)
   const int tiles_per_view = P.tiles_x * P.tiles_y;
   const int v = blockIdx.x / tiles_per_view;
   const int t = blockIdx.x % tiles_per_view;
   const int tyi = t / P.tiles_x, txi = t % P.tiles_x;
   const int s = threadIdx.x;
-  if (s >= kBorderSlots) return;
-  const int gp = P.border[(long long)blockIdx.x * kBorderSlots + s];
-  if (gp < 0) return;
+  const int gp = s < kBorderSlots ? P.border[(long long)blockIdx.x * kBorderSlots + s] : -1;
+  if (__all_sync(0xffffffffu, gp < 0)) return;   // warp-uniform
   int lx, ly;
   if (s < kTileW) { lx = s; ly = 0; }
   else if (s < 2 * kTileW) { lx = s - kTileW; ly = kTileH - 1; }
   else if (s < 2 * kTileW + kTileH) { lx = 0; ly = s - 2 * kTileW; }
   else { lx = kTileW - 1; ly = s - 2 * kTileW - kTileH; }
   const int x = txi * kTileW + lx, y = tyi * kTileH + ly;
-  const PartialRec& A = P.partials[gp];
   const int dxs[4] = {1, -1, 0, 1}, dys[4] = {0, 1, 1, 1};   // E, SW, S, SE
+  int gqs[4];
 #pragma unroll
   for (int k = 0; k < 4; ++k) {
-    int qx = x + dxs[k], qy = y + dys[k];
+    gqs[k] = -1;
+    if (gp < 0) continue;
+    const int qx = x + dxs[k], qy = y + dys[k];
     if (qx < 0 || qx >= P.W || qy >= P.H) continue;
-    int qtx = qx / kTileW, qty = qy / kTileH;
+    const int qtx = qx / kTileW, qty = qy / kTileH;
     if (qtx == txi && qty == tyi) continue;
-    long long qt = ((long long)v * P.tiles_y + qty) * P.tiles_x + qtx;
-    int gq = P.border[qt * kBorderSlots + border_slot(qx - qtx * kTileW, qy - qty * kTileH)];
-    if (gq < 0) continue;
+    const long long qt = ((long long)v * P.tiles_y + qty) * P.tiles_x + qtx;
+    gqs[k] = P.border[qt * kBorderSlots + border_slot(qx - qtx * kTileW, qy - qty * kTileH)];
+  }
+  const PartialRec* A = gp >= 0 ? &P.partials[gp] : nullptr;
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    int gq = gqs[k];
+    for (int k2 = 0; k2 < k; ++k2)
+      if (gqs[k2] == gq) gq = -1;   // the same pair through another direction
+    const unsigned long long key = gq >= 0 ? ((unsigned long long)(unsigned)gp << 32) | (unsigned)gq : ~0ull;
+    const unsigned peers = __match_any_sync(0xffffffffu, key);
+    if (gq < 0 || (int)(threadIdx.x & 31) != __ffs(peers) - 1) continue;
     const PartialRec& B = P.partials[gq];
-    if (A.cand == B.cand && A.band == B.band) uf_unite(P.parent, gp, gq);
+    if (A->cand == B.cand && A->band == B.band) uf_unite(P.parent, gp, gq);
   }
 }
 
@@ -598,6 +611,23 @@ __global__ void partial_emit_kernel(const PartialRec* __restrict__ partials, con
 
 // --------------------------------------------------------------- launchers
 size_t tile_smem_bytes() { return sizeof(TileSmem); }
+
+cudaError_t launch_minmax_kernel(const AttributionArgs& a, int v0, int v1, cudaStream_t s) {
+  if (v1 <= v0) return cudaSuccess;
+  const long long hw = (long long)a.H * a.W;
+  dim3 mg((unsigned)((hw + 256 * 8 - 1) / (256 * 8)), (unsigned)(v1 - v0));
+  if (mg.x > 1024) mg.x = 1024;
+  minmax_kernel<<<mg, 256, 0, s>>>(a.image, a.gt, a.dom, hw, a.lohi, a.cls, a.N, a.dom_flag, a.cand_bits, a.raw,
+                                   a.rawf, v0);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_thresholds(const AttributionArgs& a, int v0, int v1, cudaStream_t s) {
+  if (v1 <= v0) return cudaSuccess;
+  const int nt = (v1 - v0) * a.L;
+  thresholds_kernel<<<(nt + 3) / 4, 128, 0, s>>>(a.lohi, v0, v1 - v0, a.L, a.tau, a.lo, a.thr, a.thr_raw);
+  return cudaGetLastError();
+}
 
 cudaError_t launch_minmax_views(const AttributionArgs& a, int v0, int v1, cudaStream_t s) {
   if (v1 <= v0) return cudaSuccess;

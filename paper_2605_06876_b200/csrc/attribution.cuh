@@ -102,6 +102,9 @@ cudaError_t launch_attribution(const AttributionArgs& a, cudaStream_t s, MarkFn 
 // the same in pieces, so views can be pipelined: minmax + thresholds of views
 // [v0, v1); warp CCL of their tiles; then the deferred tiles + border merge
 cudaError_t launch_minmax_views(const AttributionArgs& a, int v0, int v1, cudaStream_t s);
+// the same in its two launches (stage timing): the input pass, then the thresholds
+cudaError_t launch_minmax_kernel(const AttributionArgs& a, int v0, int v1, cudaStream_t s);
+cudaError_t launch_thresholds(const AttributionArgs& a, int v0, int v1, cudaStream_t s);
 cudaError_t launch_tiles_views(const AttributionArgs& a, int v0, int v1, cudaStream_t s);
 cudaError_t launch_attribution_tail(const AttributionArgs& a, cudaStream_t s, MarkFn mark, void* ctx);
 bool attribution_warp_path(const AttributionArgs& a);

@@ -353,7 +353,7 @@ __global__ void morton_kernel(MergeArgs a, long long cap) {
           c[t] = u <= 0.0 ? 0u : (u >= 1023.0 ? 1023u : (unsigned)u);
         }
         const unsigned m = spread10(c[0]) | (spread10(c[1]) << 1) | (spread10(c[2]) << 2);
-        key = ((unsigned long long)l << 32) | m;
+        key = ((unsigned long long)l << 30) | m;   // 30-bit Morton code
       }
     }
     a.mkey[q] = key;

@@ -650,11 +650,14 @@ extern "C" adps_status adps_step_phase1_begin(adps_plan* P, void* stream_v, cons
       P->attr_pending = true;
       P->launches += (P->use_words ? 4 : 3) * chunks + 1 + 4;
     } else {
-      CK(launch_minmax(a, P->split_list.as<int>(), ctr, P->sm_count, s));
-      P->launches += 3;
+      // one launch over all views: the input pass, then thresholds + fallback count
+      CK(launch_minmax_kernel(a, 0, V, s));
+      mark(P, "minmax", s, 1);
+      CK(launch_thresholds(a, 0, V, s));
+      CK(launch_fallback_count(P->split_list.as<int>(), P->dom_flag.as<unsigned char>(), ctr, P->sm_count, s));
+      mark(P, "thresholds", s, 2);
     }
   }
-  mark(P, "minmax_dominance", s, 0);
   CK(cudaMemcpyAsync(P->ctr_host, ctr, sizeof(Counters), cudaMemcpyDeviceToHost, s));
   CK(cudaStreamSynchronize(s));
   {
@@ -995,7 +998,7 @@ static adps_status phase1_merge_part(adps_plan* P, cudaStream_t s) {
     mark(P, "merge_small_gates", s, 5);
     if (n_regions > 0) {
       CK(launch_merge_morton(ma, rc, s));
-      const int mbits = 32 + ceil_log2((unsigned long long)n_split + 2);
+      const int mbits = 30 + ceil_log2((unsigned long long)n_split + 2);
       CK(cub_sort_pairs(P, ma.mkey, ma.mkey_sorted, ma.mval, ma.mval_sorted, rc, mbits, s));
       CK(launch_merge_tile_gates(ma, s));
       mark(P, "merge_tile_gates", s, 3);
@@ -1264,7 +1267,7 @@ extern "C" adps_status adps_step_phase2(adps_plan* P, void* stream_v, const adps
   ea.sh_rest = out->sh_rest;
   ea.index_map = (long long*)index_map;
   CK(launch_emit(ea, s));
-  mark(P, "emit", s, (P->n + P->counts.n_split + P->counts.n_clone) > 0 ? 1 : 0);
+  mark(P, "emit", s, (P->n > 0 ? 1 : 0) + ((P->counts.n_split + P->counts.n_clone) > 0 ? 1 : 0));
   return ADPS_OK;
 }
 

@@ -360,27 +360,69 @@ __device__ __forceinline__ void emit_insert_row(const EmitArgs& a, long long k, 
   a.index_map[dst] = -1;
 }
 
-__global__ void __launch_bounds__(kEmitThreads) emit_kernel(EmitArgs a, long long b_surv, long long b_ins) {
-  const long long blk = blockIdx.x;
-  if (blk < b_surv) {                                   // survivors, old order
-    const long long t = blk * kEmitThreads + threadIdx.x;
-    if (t < a.n) {
-      const int pos = a.keep_pos[t];
-      if (pos >= 0) {
-        copy_gaussian(a, t, pos);
-        a.index_map[pos] = t;
+// survivors: one parameter array per blockIdx.y, thread per component, so
+// loads and stores are coalesced whatever the array's width (C: components
+// per Gaussian, a compile-time constant so the index split is a multiply)
+template <int C>
+__device__ __forceinline__ void copy_survivor_components(const EmitArgs& a, const float* __restrict__ in,
+                                                         float* __restrict__ out, bool index) {
+  // a warp takes 256 consecutive components, lane-strided (element base + 32 i
+  // + lane): every load and store instruction covers 128 contiguous bytes
+  // (survivor positions are contiguous between removed Gaussians), and a
+  // thread's 8 loads are in flight together
+  const unsigned ne = (unsigned)a.n * C;
+  const unsigned base = ((blockIdx.x * kEmitThreads + threadIdx.x) >> 5) * 256u + (threadIdx.x & 31);
+  float v[8];
+  int pos[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const unsigned e = base + 32u * i;
+    v[i] = e < ne ? __ldg(in + e) : 0.0f;
+    pos[i] = e < ne ? __ldg(a.keep_pos + e / C) : -1;
+  }
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const unsigned e = base + 32u * i;
+    if (pos[i] < 0) continue;
+    const unsigned t = e / C;
+    out[(unsigned)pos[i] * C + (e - t * C)] = v[i];
+    if (index) a.index_map[pos[i]] = t;
+  }
+}
+
+__global__ void __launch_bounds__(kEmitThreads) emit_survivors_kernel(EmitArgs a) {
+  switch (blockIdx.y) {
+    case 0: copy_survivor_components<3>(a, a.g.mu, a.mu, false); break;
+    case 1: copy_survivor_components<3>(a, a.g.scale, a.scale, false); break;
+    case 2: copy_survivor_components<4>(a, a.g.rot, a.rot, false); break;
+    case 3: copy_survivor_components<1>(a, a.g.opacity, a.opacity, true); break;
+    case 4: copy_survivor_components<3>(a, a.g.sh_dc, a.sh_dc, false); break;
+    default: {   // sh_rest: 3K components
+      const long long c = 3ll * a.g.sh_k;
+      const long long ne = a.n * c;
+      for (long long e = (long long)blockIdx.x * kEmitThreads + threadIdx.x; e < ne;
+           e += (long long)gridDim.x * kEmitThreads) {
+        const long long t = e / c;
+        const int pos = __ldg(a.keep_pos + t);
+        if (pos >= 0) a.sh_rest[pos * c + (e - t * c)] = __ldg(a.g.sh_rest + e);
       }
     }
-  } else if (blk < b_surv + b_ins) {                    // candidate inserts, ascending index
-    const long long k = (blk - b_surv) * (kEmitThreads / 32) + (threadIdx.x >> 5);
-    const int lane = threadIdx.x & 31;
+  }
+}
+
+__global__ void __launch_bounds__(kEmitThreads) emit_kernel(EmitArgs a, long long b_ins) {
+  const long long blk = blockIdx.x;
+  if (blk < b_ins) {                                    // candidate inserts, ascending index
+    // a thread per candidate (most insert 2 rows; a warp per candidate left
+    // 30 of 32 lanes idle), rows in order
+    const long long k = blk * kEmitThreads + threadIdx.x;
     if (k >= a.n_split) return;
     const int c = a.cand_case[k];
     if (c == ADPS_CASE_RESET) return;
     const int rows = c == ADPS_CASE_FALLBACK ? a.fb_children : a.cand_merged[k] + 1;
-    for (int j = lane; j < rows; j += 32) emit_insert_row(a, k, j);
+    for (int j = 0; j < rows; ++j) emit_insert_row(a, k, j);
   } else {                                              // clones, ascending
-    const long long j = (blk - b_surv - b_ins) * kEmitThreads + threadIdx.x;
+    const long long j = (blk - b_ins) * kEmitThreads + threadIdx.x;
     if (j < a.n_clone) {
       const long long dst = a.n_keep + a.n_inserted + j;
       copy_gaussian(a, a.clone_list[j], dst);
@@ -390,11 +432,14 @@ __global__ void __launch_bounds__(kEmitThreads) emit_kernel(EmitArgs a, long lon
 }
 
 cudaError_t launch_emit(const EmitArgs& a, cudaStream_t s) {
-  const long long b_surv = (a.n + kEmitThreads - 1) / kEmitThreads;
-  const long long b_ins = (a.n_split + kEmitThreads / 32 - 1) / (kEmitThreads / 32);
+  if (a.n > 0) {
+    // 8 components per thread (rot's 4 per Gaussian the widest; narrower arrays exit early)
+    long long b = (a.n * 4 + 8ll * kEmitThreads - 1) / (8ll * kEmitThreads);
+    emit_survivors_kernel<<<dim3((unsigned)b, a.g.sh_k > 0 ? 6u : 5u), kEmitThreads, 0, s>>>(a);
+  }
+  const long long b_ins = (a.n_split + kEmitThreads - 1) / kEmitThreads;
   const long long b_clone = (a.n_clone + kEmitThreads - 1) / kEmitThreads;
-  const long long blocks = b_surv + b_ins + b_clone;
-  if (blocks > 0) emit_kernel<<<(unsigned)blocks, kEmitThreads, 0, s>>>(a, b_surv, b_ins);
+  if (b_ins + b_clone > 0) emit_kernel<<<(unsigned)(b_ins + b_clone), kEmitThreads, 0, s>>>(a, b_ins);
   return cudaGetLastError();
 }
 
