@@ -949,10 +949,8 @@ __global__ void cap_small_kernel(MergeArgs a, long long cap) {
     const int Gk = a.n_groups[k];
     if (Gk > kCapThreadMax) {
       if (a.n_max <= kSelMax) {   // one entry per parent for the block selection
-        if (g == a.gfirst_of[k]) {
-          if (Gk > kSelHuge) a.glist[2 * cap - 1 - (long long)atomicAdd(&a.ctr->n_cap_huge, 1ull)] = k;
-          else a.glist[2 * cap + atomicAdd(&a.ctr->n_cap_large, 1ull)] = k;
-        }
+        // (parents with > kSelHuge groups are found by cap_select_kernel<true> itself)
+        if (g == a.gfirst_of[k] && Gk <= kSelHuge) a.glist[2 * cap + atomicAdd(&a.ctr->n_cap_large, 1ull)] = k;
       } else {                    // one entry per group for the block-per-group ranks
         a.glist[2 * cap + atomicAdd(&a.ctr->n_cap_large, 1ull)] = (int)g;
       }
@@ -1029,9 +1027,25 @@ __global__ void __launch_bounds__(HUGE ? 1024 : 256) cap_select_kernel(MergeArgs
   __shared__ int keep_g[kSelMax];
   __shared__ int wtot[NW];
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-  const long long nl = HUGE ? (long long)a.ctr->n_cap_huge : (long long)a.ctr->n_cap_large;
+  // the parents: from cap_small_kernel's list, or (HUGE, on the second stream,
+  // independent of cap_small_kernel) every candidate with > kSelHuge groups
+  __shared__ int huge_k[NT];
+  __shared__ int n_huge;
+  const long long n_split = (long long)a.ctr->n_split;
+  const long long nl = HUGE ? (n_split + NT - 1) / NT : (long long)a.ctr->n_cap_large;
   for (long long i = blockIdx.x; i < nl; i += gridDim.x) {
-    const int k = HUGE ? a.glist[2 * cap - 1 - i] : a.glist[2 * cap + i];
+    int n_here = 1;
+    if (HUGE) {
+      __syncthreads();   // every thread has read the previous n_huge
+      if (tid == 0) n_huge = 0;
+      __syncthreads();
+      const long long kk = i * NT + tid;
+      if (kk < n_split && a.n_groups[kk] > kSelHuge) huge_k[atomicAdd(&n_huge, 1)] = (int)kk;
+      __syncthreads();
+      n_here = n_huge;
+    }
+    for (int hi_ = 0; hi_ < n_here; ++hi_) {
+    const int k = HUGE ? huge_k[hi_] : a.glist[2 * cap + i];
     const int Gk = a.n_groups[k];
     const long long f0 = a.gfirst_of[k];
     // the keys: global (index f0 + h); for a huge parent the high 32 bits are
@@ -1155,19 +1169,28 @@ __global__ void __launch_bounds__(HUGE ? 1024 : 256) cap_select_kernel(MergeArgs
       cap_write(a, g, k, Gk, rank);
     }
     __syncthreads();
+    }
   }
 }
 
-cudaError_t launch_merge_cap(const MergeArgs& a, long long cap, cudaStream_t s) {
+cudaError_t launch_merge_cap(const MergeArgs& a, long long cap, cudaStream_t s, cudaStream_t aux,
+                             cudaEvent_t fork, cudaEvent_t join) {
   long long b = (cap + 255) / 256;
-  cap_small_kernel<<<(unsigned)(b < 1 ? 1 : (b > 65535 ? 65535 : b)), 256, 0, s>>>(a, cap);
   if (a.n_max <= kSelMax) {
-    cap_select_kernel<false><<<a.grid, 256, 0, s>>>(a, cap);
+    // the parents with the most groups (shared-memory selection) on the second
+    // stream, concurrently with the thread-per-group ranks and the block selection
     const int smem = kSelSmemKeys * 4;
     cudaError_t e = cudaFuncSetAttribute(cap_select_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;
-    cap_select_kernel<true><<<16, 1024, smem, s>>>(a, cap);
+    if ((e = cudaEventRecord(fork, s)) != cudaSuccess) return e;
+    if ((e = cudaStreamWaitEvent(aux, fork, 0)) != cudaSuccess) return e;
+    cap_select_kernel<true><<<16, 1024, smem, aux>>>(a, cap);
+    if ((e = cudaEventRecord(join, aux)) != cudaSuccess) return e;
+    cap_small_kernel<<<(unsigned)(b < 1 ? 1 : (b > 65535 ? 65535 : b)), 256, 0, s>>>(a, cap);
+    cap_select_kernel<false><<<a.grid, 256, 0, s>>>(a, cap);
+    if ((e = cudaStreamWaitEvent(s, join, 0)) != cudaSuccess) return e;
   } else {
+    cap_small_kernel<<<(unsigned)(b < 1 ? 1 : (b > 65535 ? 65535 : b)), 256, 0, s>>>(a, cap);
     cap_large_kernel<<<a.grid * 4, 256, 0, s>>>(a, cap);
   }
   return cudaGetLastError();

@@ -104,6 +104,7 @@ cudaError_t launch_merge_flatten(const MergeArgs& a, long long cap, cudaStream_t
 cudaError_t launch_merge_groups(const MergeArgs& a, long long cap, ScanState st, cudaStream_t s);
 // cap (ref/cross_view_merge.py:110-116): rank of each group among its parent's
 // groups by (-extent, group order); ranks < n_max become children in rank order
-cudaError_t launch_merge_cap(const MergeArgs& a, long long cap, cudaStream_t s);
+cudaError_t launch_merge_cap(const MergeArgs& a, long long cap, cudaStream_t s, cudaStream_t aux,
+                             cudaEvent_t fork, cudaEvent_t join);
 
 }  // namespace adps

@@ -1010,7 +1010,7 @@ static adps_status phase1_merge_part(adps_plan* P, cudaStream_t s) {
       CK(cub_sort_pairs(P, ma.gkey, ma.gkey_sorted, ma.gval, ma.gval_sorted, rc, gbits, s));
       CK(launch_merge_groups(ma, rc, sst3, s));
       mark(P, "merge_groups", s, 5);
-      CK(launch_merge_cap(ma, rc, s));
+      CK(launch_merge_cap(ma, rc, s, P->aux, P->ev_fork, P->ev_small));
       mark(P, "merge_cap", s, 3);
     }
   }
