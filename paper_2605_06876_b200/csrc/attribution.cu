@@ -103,6 +103,104 @@ __global__ void minmax_kernel(const float* __restrict__ image, const float* __re
   }
 }
 
+// bits 0..15 of x spread to the even bit positions
+__device__ __forceinline__ unsigned spread16(unsigned x) {
+  x &= 0xffffu;
+  x = (x | (x << 8)) & 0x00ff00ffu;
+  x = (x | (x << 4)) & 0x0f0f0f0fu;
+  x = (x | (x << 2)) & 0x33333333u;
+  x = (x | (x << 1)) & 0x55555555u;
+  return x;
+}
+
+__device__ __forceinline__ double raw_l1_3(float a0, float a1, float a2, float g0, float g1, float g2) {
+  // np.abs(rendered - gt).sum(axis=-1) == (|d0| + |d1|) + |d2| in fp64
+  return dadd(dadd(fabs(dsub((double)a0, (double)g0)), fabs(dsub((double)a1, (double)g1))),
+              fabs(dsub((double)a2, (double)g2)));
+}
+
+// The same pass, two pixels per thread (even hw: every view starts 8-byte
+// aligned, so the pixel pairs load as float2/int2 and 32-bit offsets suffice).
+// A warp covers 64 pixels = two candidate-bit words; the candidate test is
+// looked up for a thread's first pixel and for its second when the id changes.
+__global__ void __launch_bounds__(256) minmax2_kernel(const float* __restrict__ image, const float* __restrict__ gt,
+                                                      const int* __restrict__ dominant, int hw,
+                                                      unsigned long long* __restrict__ lohi,
+                                                      const unsigned char* __restrict__ cls, int N,
+                                                      unsigned char* __restrict__ dom_flag,
+                                                      unsigned* __restrict__ cand_bits, double* __restrict__ raw_out,
+                                                      float* __restrict__ rawf_out, int v0) {
+  const int v = v0 + blockIdx.y;
+  const long long vb = (long long)v * hw;
+  const float2* img2 = reinterpret_cast<const float2*>(image + vb * 3);
+  const float2* gt2 = reinterpret_cast<const float2*>(gt + vb * 3);
+  const int2* dom2 = reinterpret_cast<const int2*>(dominant + vb);
+  float2* rawf2 = rawf_out ? reinterpret_cast<float2*>(rawf_out + vb) : nullptr;
+  double* rawd = raw_out ? raw_out + vb : nullptr;
+  unsigned* bits = cand_bits + (long long)v * ((hw + 31) / 32);
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  double lo = INFINITY, hi = 0.0;
+  for (int base = blockIdx.x * 512; base < hw; base += gridDim.x * 512) {
+    const int p = base + 2 * threadIdx.x;   // even; p + 1 < hw whenever p < hw
+    int d0 = -1, d1 = -1;
+    if (p < hw) {
+      const int q = (3 * p) >> 1;
+      const float2 a0 = __ldg(img2 + q), a1 = __ldg(img2 + q + 1), a2 = __ldg(img2 + q + 2);
+      const float2 g0 = __ldg(gt2 + q), g1 = __ldg(gt2 + q + 1), g2 = __ldg(gt2 + q + 2);
+      const int2 dd = __ldg(dom2 + (p >> 1));
+      d0 = dd.x;
+      d1 = dd.y;
+      const double r0 = raw_l1_3(a0.x, a0.y, a1.x, g0.x, g0.y, g1.x);
+      const double r1 = raw_l1_3(a1.y, a2.x, a2.y, g1.y, g2.x, g2.y);
+      if (rawf2) rawf2[p >> 1] = make_float2(__double2float_rz(r0), __double2float_rz(r1));
+      if (rawd) {
+        rawd[p] = r0;
+        rawd[p + 1] = r1;
+      }
+      lo = fmin(lo, fmin(r0, r1));
+      hi = fmax(hi, fmax(r0, r1));
+    }
+    bool c0 = false, c1 = false;
+    if (d0 >= 0 && d0 < N && __ldg(cls + d0) == 1) {
+      c0 = true;
+      if (dom_flag && dom_flag[d0] == 0) dom_flag[d0] = 1;
+    }
+    if (d1 == d0) {
+      c1 = c0;
+    } else if (d1 >= 0 && d1 < N && __ldg(cls + d1) == 1) {
+      c1 = true;
+      if (dom_flag && dom_flag[d1] == 0) dom_flag[d1] = 1;
+    }
+    const unsigned b0 = __ballot_sync(0xffffffffu, c0), b1 = __ballot_sync(0xffffffffu, c1);
+    const int wp = base + 64 * wid;   // first pixel of this warp: a multiple of 64
+    if (lane == 0 && wp < hw) bits[wp >> 5] = spread16(b0) | (spread16(b1) << 1);
+    if (lane == 1 && wp + 32 < hw) bits[(wp >> 5) + 1] = spread16(b0 >> 16) | (spread16(b1 >> 16) << 1);
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    lo = fmin(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+    hi = fmax(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+  }
+  __shared__ double slo[32], shi[32];
+  if (lane == 0) {
+    slo[wid] = lo;
+    shi[wid] = hi;
+  }
+  __syncthreads();
+  if (wid == 0) {
+    const int nw = blockDim.x >> 5;
+    lo = lane < nw ? slo[lane] : INFINITY;
+    hi = lane < nw ? shi[lane] : 0.0;
+    for (int o = 16; o > 0; o >>= 1) {
+      lo = fmin(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+      hi = fmax(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+    }
+    if (lane == 0) {   // raw >= +0.0, so IEEE order == unsigned order of the bit patterns
+      atomicMin(&lohi[2 * v + 0], (unsigned long long)__double_as_longlong(lo));
+      atomicMax(&lohi[2 * v + 1], (unsigned long long)__double_as_longlong(hi));
+    }
+  }
+}
+
 // e(x) = x / d with x = fl(raw - lo) and d = fl(hi - lo); both predicates below
 // are monotone in x, so each is a single threshold on x.
 __device__ __forceinline__ bool m_pred(double x, double d, double tau) { return ddiv(x, d) > tau; }
@@ -615,6 +713,13 @@ size_t tile_smem_bytes() { return sizeof(TileSmem); }
 cudaError_t launch_minmax_kernel(const AttributionArgs& a, int v0, int v1, cudaStream_t s) {
   if (v1 <= v0) return cudaSuccess;
   const long long hw = (long long)a.H * a.W;
+  if (hw % 2 == 0 && hw < (1ll << 30)) {   // pixel pairs (float2 / int2 loads)
+    dim3 mg2((unsigned)((hw + 511) / 512), (unsigned)(v1 - v0));
+    if (mg2.x > 1024) mg2.x = 1024;
+    minmax2_kernel<<<mg2, 256, 0, s>>>(a.image, a.gt, a.dom, (int)hw, a.lohi, a.cls, a.N, a.dom_flag, a.cand_bits,
+                                       a.raw, a.rawf, v0);
+    return cudaGetLastError();
+  }
   dim3 mg((unsigned)((hw + 256 * 8 - 1) / (256 * 8)), (unsigned)(v1 - v0));
   if (mg.x > 1024) mg.x = 1024;
   minmax_kernel<<<mg, 256, 0, s>>>(a.image, a.gt, a.dom, hw, a.lohi, a.cls, a.N, a.dom_flag, a.cand_bits, a.raw,
@@ -630,15 +735,9 @@ cudaError_t launch_thresholds(const AttributionArgs& a, int v0, int v1, cudaStre
 }
 
 cudaError_t launch_minmax_views(const AttributionArgs& a, int v0, int v1, cudaStream_t s) {
-  if (v1 <= v0) return cudaSuccess;
-  const long long hw = (long long)a.H * a.W;
-  dim3 mg((unsigned)((hw + 256 * 8 - 1) / (256 * 8)), (unsigned)(v1 - v0));
-  if (mg.x > 1024) mg.x = 1024;
-  minmax_kernel<<<mg, 256, 0, s>>>(a.image, a.gt, a.dom, hw, a.lohi, a.cls, a.N, a.dom_flag, a.cand_bits, a.raw,
-                                   a.rawf, v0);
-  const int nt = (v1 - v0) * a.L;
-  thresholds_kernel<<<(nt + 3) / 4, 128, 0, s>>>(a.lohi, v0, v1 - v0, a.L, a.tau, a.lo, a.thr, a.thr_raw);
-  return cudaGetLastError();
+  cudaError_t e = launch_minmax_kernel(a, v0, v1, s);
+  if (e != cudaSuccess) return e;
+  return launch_thresholds(a, v0, v1, s);
 }
 
 cudaError_t launch_minmax(const AttributionArgs& a, const int* split_list, Counters* ctr, int sm_count,
