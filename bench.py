@@ -450,10 +450,10 @@ def main():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--config", default="config3")
     ap.add_argument("--seed", type=int, default=0)
-    ap.add_argument("--cpu-views", type=int, default=1)
+    ap.add_argument("--cpu-views", type=int, default=2)
     ap.add_argument("--ref-views", type=int, default=8)
     ap.add_argument("--ref-cand-frac", type=float, default=0.125)
-    ap.add_argument("--cpu-cand-frac", type=float, default=0.25)
+    ap.add_argument("--cpu-cand-frac", type=float, default=0.5)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--replicas", action="store_true",
