@@ -327,7 +327,6 @@ cudaError_t launch_merge_small_gates(const MergeArgs& a, cudaStream_t s) {
 // whose minimum centre distance gives (dmin/sA + dmin/sB) > gamma_d, or whose
 // rgb boxes are more than gamma_c apart, contains no mergeable pair.
 enum { kG_mu = 0, kG_rgb = 3, kG_inv = 6, kG_prec = 7, kG_fields = 13 };   // gsoa fields
-enum { kF_mu = 0, kF_rgb = 3, kF_inv = 6, kF_fields = 7 };                  // fsoa fields
 
 __device__ __forceinline__ unsigned spread10(unsigned v) {
   v &= 0x3ffu;
@@ -398,11 +397,10 @@ __global__ void box_kernel(MergeArgs a) {
       }
       a.gsoa[(long long)kG_inv * a.soa_cap + m] = M.inv_smax;
       for (int k = 0; k < 6; ++k) a.gsoa[(long long)(kG_prec + k) * a.soa_cap + m] = M.prec[k];
-      for (int c = 0; c < 3; ++c) {   // fp32 (round to nearest) copies for the conservative prefilter
-        a.fsoa[(long long)(kF_mu + c) * a.soa_cap + m] = (float)M.mu[c];
-        a.fsoa[(long long)(kF_rgb + c) * a.soa_cap + m] = (float)M.rgb[c];
-      }
-      a.fsoa[(long long)kF_inv * a.soa_cap + m] = (float)M.inv_smax;
+      // fp32 (round to nearest) copies for the conservative prefilter, two float4 per proposal
+      reinterpret_cast<float4*>(a.fsoa)[2 * m] =
+          make_float4((float)M.mu[0], (float)M.mu[1], (float)M.mu[2], (float)M.inv_smax);
+      reinterpret_cast<float4*>(a.fsoa)[2 * m + 1] = make_float4((float)M.rgb[0], (float)M.rgb[1], (float)M.rgb[2], 0.0f);
       for (int c = 0; c < 3; ++c) {
         s[c] += M.mu[c];
         lo[c] = fmin(lo[c], M.rgb[c]);
@@ -509,7 +507,8 @@ __global__ void tile_pair_filter_kernel(MergeArgs a) {
 
 __device__ __forceinline__ void cp_async(void* dst, const void* src, int bytes) {
   const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
-  if (bytes == 8) asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(d), "l"(src) : "memory");
+  if (bytes == 16) asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d), "l"(src) : "memory");
+  else if (bytes == 8) asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(d), "l"(src) : "memory");
   else asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(d), "l"(src) : "memory");
 }
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
@@ -536,37 +535,30 @@ __device__ __forceinline__ bool gate_col(const double* A, const double (*Js)[kMT
 
 struct ColTile {
   double s[kG_fields][kMT];   // [field][proposal]
-  float f[kF_fields][kMT];
+  float4 f[kMT][2];           // fp32 (mu, inv_smax), (rgb, 0)
   int q[kMT];
 };
 
 // Conservative fp32 reject, exact in effect: true only when the fp64 gate
 // certainly fails.  Operands are the fp64 values rounded to nearest fp32
-// (relative error <= 2^-24 each); every bound below carries slack for that
-// and for the fp32 arithmetic:
-//   colour: |fb - fa| >= |b - a| - 3*2^-24*(|a| + |b|), so a computed
-//           difference above gc + 4e-7 * (|fa| + |fb| + 1) means > gc;
-//   distance: |d_c| >= |fb_c - fa_c| - 4e-7 * (|fa_c| + |fb_c|) per
-//           component, w >= (fa_inv + fb_inv)(1 - 1e-6), and the fp64
-//           early reject |d|^2 w^2 > gd^2 (1 + 1e-9) implies the gate fails.
-__device__ __forceinline__ bool reject32(const float* Af, const float (*Jf)[kMT], int jj, float gc, float gd2_hi) {
-  float dcx = 0.0f;
-#pragma unroll
-  for (int c = 0; c < 3; ++c) {
-    const float a = Af[kF_rgb + c], b = Jf[kF_rgb + c][jj];
-    const float d = fabsf(b - a) - 4e-7f * (fabsf(a) + fabsf(b) + 1.0f);
-    dcx = fmaxf(dcx, d);
-  }
-  if (dcx > gc) return true;
-  float n2 = 0.0f;
-#pragma unroll
-  for (int c = 0; c < 3; ++c) {
-    const float a = Af[kF_mu + c], b = Jf[kF_mu + c][jj];
-    const float d = fmaxf(fabsf(b - a) - 4e-7f * (fabsf(a) + fabsf(b)), 0.0f);
-    n2 += d * d;
-  }
-  const float w = (Af[kF_inv] + Jf[kF_inv][jj]) * (1.0f - 1e-6f);
-  return n2 * (1.0f - 1e-5f) * w * w > gd2_hi;
+// (relative error <= 2^-24 each); the slacks cover that and the fp32
+// arithmetic, taken once per tile pair from the largest magnitudes of the
+// two tiles (Ma, Mb) instead of per pair:
+//   colour:   |fb - fa| > gc + 4e-7 (Ma_rgb + Mb_rgb + 1) implies |b - a| > gc;
+//   distance: |d_c| >= |fb_c - fa_c| - 4e-7 (Ma_mu + Mb_mu) per component,
+//             w >= (fa_inv + fb_inv)(1 - 1e-6), and |d|^2 w^2 > gd^2 (1 + 1e-9)
+//             (the fp64 early reject) implies the gate fails; the fp32
+//             rounding of n2 w^2 is inside the 2e-5 margin of gd2s.
+// Branch-free, so the warp stays converged over the column loop.
+__device__ __forceinline__ bool reject32(const float4 am, const float4 ac, const float4 bm, const float4 bc,
+                                         float gcs, float smu, float gd2s) {
+  const float dc = fmaxf(fmaxf(fabsf(bc.x - ac.x), fabsf(bc.y - ac.y)), fabsf(bc.z - ac.z));
+  const float dx = fmaxf(fabsf(bm.x - am.x) - smu, 0.0f);
+  const float dy = fmaxf(fabsf(bm.y - am.y) - smu, 0.0f);
+  const float dz = fmaxf(fabsf(bm.z - am.z) - smu, 0.0f);
+  const float w = am.w + bm.w;
+  const float n2 = dx * dx + dy * dy + dz * dz;
+  return (dc > gcs) | (n2 * (w * w) > gd2s);
 }
 constexpr int kPairWarps = 4;
 
@@ -577,8 +569,8 @@ __device__ __forceinline__ void stage_col(const MergeArgs& a, ColTile& B, long l
   if (bt * kMT + lane < P) {
 #pragma unroll
     for (int f = 0; f < kG_fields; ++f) cp_async(&B.s[f][lane], a.gsoa + (long long)f * a.soa_cap + base + lane, 8);
-#pragma unroll
-    for (int f = 0; f < kF_fields; ++f) cp_async(&B.f[f][lane], a.fsoa + (long long)f * a.soa_cap + base + lane, 4);
+    cp_async(&B.f[lane][0], a.fsoa + 8 * (base + lane), 16);
+    cp_async(&B.f[lane][1], a.fsoa + 8 * (base + lane) + 4, 16);
     cp_async(&B.q[lane], a.mval_sorted + base + lane, 4);
   }
   cp_async_commit();
@@ -613,9 +605,10 @@ __global__ void __launch_bounds__(kPairWarps * 32) pair_tiles_kernel(MergeArgs a
   if (w0 >= w1) return;
   long long cur_l = -1, cur_bi = -1;
   double A[kG_fields];
-  float Af[kF_fields];
+  float4 am = make_float4(0.f, 0.f, 0.f, 0.f), ac = am;
+  float ma_mu = 0.f, ma_rgb = 0.f;   // the row tile's largest |mu_c|, |rgb_c| (fp32 copies)
   int qa = -1, ni = 0;
-  const float gc32 = (float)gc, gd2_hi = (float)(gd * gd) * (1.0f + 1e-5f);
+  const float gc32 = (float)gc, gd2s = (float)(gd * gd) * (1.0f + 1e-5f) * (1.0f + 2e-5f);
   int4 cur = pair_at(w0);
   stage_col(a, buf[0], cur.x, cur.z, lane);
   for (long long w = w0; w < w1; ++w) {
@@ -626,12 +619,20 @@ __global__ void __launch_bounds__(kPairWarps * 32) pair_tiles_kernel(MergeArgs a
       const long long P = (long long)a.lp_cnt[cur_l];
       ni = (int)min((long long)kMT, P - cur_bi * kMT);
       const long long m = (long long)a.lp_off[cur_l] + cur_bi * kMT + lane;
+      am = ac = make_float4(0.f, 0.f, 0.f, 0.f);
       if (lane < ni) {
 #pragma unroll
         for (int f = 0; f < kG_fields; ++f) A[f] = __ldg(a.gsoa + (long long)f * a.soa_cap + m);
-#pragma unroll
-        for (int f = 0; f < kF_fields; ++f) Af[f] = __ldg(a.fsoa + (long long)f * a.soa_cap + m);
+        am = __ldg(reinterpret_cast<const float4*>(a.fsoa) + 2 * m);
+        ac = __ldg(reinterpret_cast<const float4*>(a.fsoa) + 2 * m + 1);
         qa = __ldg(a.mval_sorted + m);
+      }
+      ma_mu = fmaxf(fmaxf(fabsf(am.x), fabsf(am.y)), fabsf(am.z));
+      ma_rgb = fmaxf(fmaxf(fabsf(ac.x), fabsf(ac.y)), fabsf(ac.z));
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        ma_mu = fmaxf(ma_mu, __shfl_xor_sync(0xffffffffu, ma_mu, o));
+        ma_rgb = fmaxf(ma_rgb, __shfl_xor_sync(0xffffffffu, ma_rgb, o));
       }
     }
     int4 nxt = cur;
@@ -648,21 +649,43 @@ __global__ void __launch_bounds__(kPairWarps * 32) pair_tiles_kernel(MergeArgs a
       const long long P = (long long)a.lp_cnt[cur.x];
       const int nj = (int)min((long long)kMT, P - (long long)cur.z * kMT);
       const bool diag = cur.y == cur.z;
-      if (lane < ni) {
-        // gates first, unions after: a union inside the column loop would stall
-        // the whole warp on one lane's union-find latency whenever any lane passes
-        unsigned pass = 0u;
-        for (int jj = diag ? lane + 1 : 0; jj < nj; ++jj) {   // unordered pairs: ii < jj on the diagonal
-          if (reject32(Af, J.f, jj, gc32, gd2_hi)) continue;
-          const bool ok = gate_col(A, J.s, jj, gd, gd2, gc);
-#if ADPS_MERGE_STATS
-          atomicAdd(&a.ctr->stat_gates, 1ull);
-          if (ok) atomicAdd(&a.ctr->stat_pass, 1ull);
-#endif
-          if (ok) pass |= 1u << jj;
-        }
-        for (; pass; pass &= pass - 1u) uf_unite(a.uf, qa, J.q[__ffs(pass) - 1]);
+      // the column tile's largest magnitudes -> this tile pair's slacks
+      float mb_mu = 0.f, mb_rgb = 0.f;
+      if (lane < nj) {
+        const float4 bm = J.f[lane][0], bc = J.f[lane][1];
+        mb_mu = fmaxf(fmaxf(fabsf(bm.x), fabsf(bm.y)), fabsf(bm.z));
+        mb_rgb = fmaxf(fmaxf(fabsf(bc.x), fabsf(bc.y)), fabsf(bc.z));
       }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        mb_mu = fmaxf(mb_mu, __shfl_xor_sync(0xffffffffu, mb_mu, o));
+        mb_rgb = fmaxf(mb_rgb, __shfl_xor_sync(0xffffffffu, mb_rgb, o));
+      }
+      const float smu = 4e-7f * (ma_mu + mb_mu);
+      const float gcs = gc32 * (1.0f + 1e-6f) + 4e-7f * (ma_rgb + mb_rgb + 1.0f);
+      // fp32 prefilter over all columns, warp-converged: bit jj = "the fp64 gate may pass"
+      unsigned maybe = 0u;
+#pragma unroll 4
+      for (int jj = 0; jj < nj; ++jj) {
+        const float4 bm = J.f[jj][0], bc = J.f[jj][1];
+        maybe |= (reject32(am, ac, bm, bc, gcs, smu, gd2s) ? 0u : 1u) << jj;
+      }
+      // unordered pairs: ii < jj on the diagonal; rows past the tile's end have no pairs
+      if (diag) maybe &= lane >= 31 ? 0u : (0xffffffffu << (lane + 1));
+      if (lane >= ni) maybe = 0u;
+      // gates first, unions after: a union inside the column loop would stall
+      // the whole warp on one lane's union-find latency whenever any lane passes
+      unsigned pass = 0u;
+      for (; maybe; maybe &= maybe - 1u) {
+        const int jj = __ffs(maybe) - 1;
+        const bool ok = gate_col(A, J.s, jj, gd, gd2, gc);
+#if ADPS_MERGE_STATS
+        atomicAdd(&a.ctr->stat_gates, 1ull);
+        if (ok) atomicAdd(&a.ctr->stat_pass, 1ull);
+#endif
+        if (ok) pass |= 1u << jj;
+      }
+      for (; pass; pass &= pass - 1u) uf_unite(a.uf, qa, J.q[__ffs(pass) - 1]);
     }
     __syncwarp();   // this buffer is restaged two pairs on
     cur = nxt;

@@ -73,7 +73,7 @@ struct MergeArgs {
   int* mval_sorted;                        // Morton order: [lp_off[l], +P_l) -> proposal q
   TileBox* boxes;                          // [cap / 64 + n_split]
   double* gsoa;                            // [13][soa_cap] gate operands in Morton order
-  float* fsoa;                             // [7][soa_cap] fp32 copies of mu, rgb, inv_smax (prefilter)
+  float* fsoa;                             // [soa_cap][2] float4: fp32 (mu, inv_smax), (rgb, 0) (prefilter)
   long long soa_cap;
   int4* tile_pairs;                        // surviving (l, bi, bj) tile pairs
   long long tile_pairs_cap;

@@ -20,6 +20,9 @@
 #ifndef ADPS_PIPELINE_CHUNKS
 #define ADPS_PIPELINE_CHUNKS 2
 #endif
+#ifndef ADPS_AUX_PRIORITY
+#define ADPS_AUX_PRIORITY 0
+#endif
 #ifndef ADPS_RAW_CACHE_DEFAULT
 #define ADPS_RAW_CACHE_DEFAULT 1
 #endif
@@ -234,7 +237,13 @@ extern "C" adps_status adps_plan_create(adps_plan** plan, int32_t device, int64_
     return fail(ADPS_OOM, "pinned allocation failed: %s", cudaGetErrorString(e));
   }
   for (int i = 0; i < kMaxMarks; ++i) cudaEventCreate(&P->ev[i]);
-  cudaStreamCreateWithFlags(&P->aux, cudaStreamNonBlocking);
+  {
+    // ADPS_AUX_PRIORITY: the second stream's blocks (CCL of finished chunks, small
+    // gates) are dispatched ahead of the HBM-bound input pass's queued blocks
+    int lo = 0, hi = 0;
+    cudaDeviceGetStreamPriorityRange(&lo, &hi);
+    cudaStreamCreateWithPriority(&P->aux, cudaStreamNonBlocking, ADPS_AUX_PRIORITY ? hi : 0);
+  }
   cudaEventCreateWithFlags(&P->ev_fork, cudaEventDisableTiming);
   cudaEventCreateWithFlags(&P->ev_small, cudaEventDisableTiming);
   cudaEventCreateWithFlags(&P->ev_keep, cudaEventDisableTiming);
@@ -867,7 +876,7 @@ static adps_status phase1_merge_part(adps_plan* P, cudaStream_t s) {
   CK(ensure(P->mval_sorted, 4 * rc));
   CK(ensure(P->boxes, sizeof(TileBox) * (rc / kMT + sc + 1)));
   CK(ensure(P->gsoa, 8ll * 13 * rc));
-  CK(ensure(P->fsoa, 4ll * 7 * rc));
+  CK(ensure(P->fsoa, 4ll * 8 * rc));
   {
     // surviving tile pairs: worst case every pair of (rc/kMT + n_split) tiles; capped at
     // 2^24 entries (overflow falls back to inline filtering inside pair_tiles_kernel)

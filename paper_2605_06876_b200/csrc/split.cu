@@ -225,15 +225,31 @@ cudaError_t launch_child_init(const ChildArgs& a, cudaStream_t s) {
 
 // ============================================================ ranges
 __global__ void ranges_kernel(RangeArgs a) {
-  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < a.n;
-       i += (long long)gridDim.x * blockDim.x) {
-    unsigned long long k = a.keys_sorted[i];
-    int rank = (int)(k >> a.shift_rank);
-    int view = (int)((k >> a.shift_view) & ((1ull << a.bits_v) - 1ull));
-    if (i == 0 || (int)(a.keys_sorted[i - 1] >> a.shift_rank) != rank) a.cand_start[rank] = (int)i;
-    if (i == a.n - 1 || (int)(a.keys_sorted[i + 1] >> a.shift_rank) != rank) a.cand_end[rank] = (int)(i + 1);
-    atomicAdd(&a.regions_per_view[(long long)rank * a.n_views + view], 1);
-    if (a.valid[a.vals_sorted[i]]) atomicAdd(&a.cand_nvalid[rank], 1);
+  // keys are sorted, so one candidate's (and one (candidate, view)'s) regions are
+  // adjacent: counts are aggregated per warp (match_any) before the atomics, which
+  // keeps a parent with tens of thousands of regions from serialising on one word
+  const int lane = threadIdx.x & 31;
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long i0 = (long long)blockIdx.x * blockDim.x; i0 < a.n; i0 += stride) {
+    const long long i = i0 + threadIdx.x;
+    const bool in = i < a.n;
+    unsigned long long k = in ? a.keys_sorted[i] : ~0ull;
+    const int rank = (int)(k >> a.shift_rank);
+    const bool val = in && a.valid[a.vals_sorted[i]];
+    if (in) {
+      if (i == 0 || (int)(a.keys_sorted[i - 1] >> a.shift_rank) != rank) a.cand_start[rank] = (int)i;
+      if (i == a.n - 1 || (int)(a.keys_sorted[i + 1] >> a.shift_rank) != rank) a.cand_end[rank] = (int)(i + 1);
+    }
+    const unsigned live = __ballot_sync(0xffffffffu, in);
+    const unsigned long long rv = k >> a.shift_view;   // (rank, view)
+    const unsigned g_rv = __match_any_sync(0xffffffffu, rv) & live;
+    const unsigned g_r = __match_any_sync(0xffffffffu, (unsigned long long)rank) & live;
+    if (in && lane == __ffs(g_rv) - 1) {
+      const int view = (int)(rv & ((1ull << a.bits_v) - 1ull));
+      atomicAdd(&a.regions_per_view[(long long)rank * a.n_views + view], __popc(g_rv));
+    }
+    const int nv = __popc(__ballot_sync(0xffffffffu, val) & g_r);
+    if (in && lane == __ffs(g_r) - 1 && nv) atomicAdd(&a.cand_nvalid[rank], nv);
   }
 }
 
