@@ -100,6 +100,7 @@ struct Counters {
   unsigned long long n_small;
   unsigned long long n_groups_all;
   unsigned long long n_tile_pairs;
+  unsigned long long pair_next;            // pair_tiles_kernel work counter
   unsigned long long n_fallback_pre;
   unsigned long long n_deferred;   // tiles the warp CCL handed to the block CCL
   unsigned long long normals_consumed;   // 64-bit draws used by adps_normals_pcg64

@@ -462,6 +462,15 @@ __device__ __forceinline__ void decode_tile_pair(const MergeArgs& a, long long n
   bj = bi + (q - (bi * T - bi * (bi - 1) / 2));
 }
 
+// a surviving tile pair as the gate kernel consumes it, with no dependent
+// lookups left: x = first proposal of the row tile, y = first proposal of the
+// column tile (Morton-ordered operand index), z = ni | nj << 8, w = live
+__device__ __forceinline__ int4 pair_entry(const MergeArgs& a, long long l, long long bi, long long bj, bool live) {
+  const long long P = (long long)a.lp_cnt[l], o = (long long)a.lp_off[l];
+  const int ni = (int)min((long long)kMT, P - bi * kMT), nj = (int)min((long long)kMT, P - bj * kMT);
+  return make_int4((int)(o + bi * kMT), (int)(o + bj * kMT), ni | (nj << 8), live ? 1 : 0);
+}
+
 // one warp per (parent, tile row bi) of the upper-triangular tile matrix:
 // keep the pairs (bi, bj >= bi) the bounding data cannot exclude; a row's
 // survivors are stored contiguously in bj order (one reservation per row), so
@@ -495,7 +504,7 @@ __global__ void tile_pair_filter_kernel(MergeArgs a) {
       const long long bj = j0 + lane;
       const bool keep = bj < T && boxes_may_merge(A, a.boxes[tb + bj], a.gamma_d, a.gamma_c);
       const unsigned m = __ballot_sync(0xffffffffu, keep);
-      if (keep) a.tile_pairs[base + __popc(m & ((1u << lane) - 1u))] = make_int4((int)l, (int)bi, (int)bj, 0);
+      if (keep) a.tile_pairs[base + __popc(m & ((1u << lane) - 1u))] = pair_entry(a, l, bi, bj, true);
       base += __popc(m);
     }
   }
@@ -561,12 +570,14 @@ __device__ __forceinline__ bool reject32(const float4 am, const float4 ac, const
   return (dc > gcs) | (n2 * (w * w) > gd2s);
 }
 constexpr int kPairWarps = 4;
+#ifndef ADPS_PAIR_CHUNK
+#define ADPS_PAIR_CHUNK 1
+#endif
+constexpr int kPairChunk = ADPS_PAIR_CHUNK;
 
-// stage tile bt of large parent l into a warp's buffer (lane = proposal)
-__device__ __forceinline__ void stage_col(const MergeArgs& a, ColTile& B, long long l, long long bt, int lane) {
-  const long long P = (long long)a.lp_cnt[l];
-  const long long base = (long long)a.lp_off[l] + bt * kMT;
-  if (bt * kMT + lane < P) {
+// stage the nj-proposal column tile starting at operand index base (lane = proposal)
+__device__ __forceinline__ void stage_col(const MergeArgs& a, ColTile& B, long long base, int nj, int lane) {
+  if (lane < nj) {
 #pragma unroll
     for (int f = 0; f < kG_fields; ++f) cp_async(&B.s[f][lane], a.gsoa + (long long)f * a.soa_cap + base + lane, 8);
     cp_async(&B.f[lane][0], a.fsoa + 8 * (base + lane), 16);
@@ -592,33 +603,58 @@ __global__ void __launch_bounds__(kPairWarps * 32) pair_tiles_kernel(MergeArgs a
   const long long gw = (long long)blockIdx.x * kPairWarps + wid;
   const double gd = a.gamma_d, gc = a.gamma_c, gd2 = gd * gd * (1.0 + 1e-9);
   const long long W = overflow ? (long long)(n_large > 0 ? a.work_off[n_large] : 0) : (long long)a.ctr->n_tile_pairs;
-  const long long chunk = (W + nwarps - 1) / nwarps;
-  const long long w0 = gw * chunk, w1 = min(W, w0 + chunk);
+  // dynamic work: chunks of kPairChunk consecutive pairs (usually one tile row)
+  // from a global counter, the next chunk reserved while the current one runs
+  // (gate and union work is uneven across pairs: static ranges left long tails)
+  (void)nwarps;
+  (void)gw;
+  unsigned long long* const counter = &a.ctr->pair_next;
+  auto grab = [&]() -> unsigned long long {
+    unsigned long long v = 0;
+    if (lane == 0) v = atomicAdd(counter, (unsigned long long)kPairChunk);
+    return v;   // lane 0 only; broadcast when it is consumed
+  };
+  long long c_end = 0, pos = 0;
+  unsigned long long c_next = grab();
+  auto next_index = [&]() -> long long {   // -1 when exhausted
+    if (pos >= c_end) {
+      const long long c = (long long)__shfl_sync(0xffffffffu, c_next, 0);
+      if (c >= W) return -1;
+      pos = c;
+      c_end = min(W, c + kPairChunk);
+      c_next = grab();
+    }
+    return pos++;
+  };
   auto pair_at = [&](long long w) -> int4 {
+    if (w < 0) return make_int4(-1, -1, 0, 0);
     if (!overflow) return a.tile_pairs[w];
     long long l, bi, bj;
     decode_tile_pair(a, n_large, (unsigned long long)w, l, bi, bj);
     const long long tb = (long long)a.tile_off[l];
     const bool live = boxes_may_merge(a.boxes[tb + bi], a.boxes[tb + bj], a.gamma_d, a.gamma_c);
-    return make_int4((int)l, (int)bi, (int)bj, live ? 1 : 0);
+    return pair_entry(a, l, bi, bj, live);
   };
-  if (w0 >= w1) return;
-  long long cur_l = -1, cur_bi = -1;
+  long long i_cur = next_index();
+  if (i_cur < 0) return;
+  long long i_nxt = next_index();
+  int cur_row = -1;
   double A[kG_fields];
   float4 am = make_float4(0.f, 0.f, 0.f, 0.f), ac = am;
   float ma_mu = 0.f, ma_rgb = 0.f;   // the row tile's largest |mu_c|, |rgb_c| (fp32 copies)
   int qa = -1, ni = 0;
   const float gc32 = (float)gc, gd2s = (float)(gd * gd) * (1.0f + 1e-5f) * (1.0f + 2e-5f);
-  int4 cur = pair_at(w0);
-  stage_col(a, buf[0], cur.x, cur.z, lane);
-  for (long long w = w0; w < w1; ++w) {
-    const int it = (int)(w - w0);
-    if (cur.x != cur_l || cur.y != cur_bi) {   // new tile row: its operands into registers
-      cur_l = cur.x;
-      cur_bi = cur.y;
-      const long long P = (long long)a.lp_cnt[cur_l];
-      ni = (int)min((long long)kMT, P - cur_bi * kMT);
-      const long long m = (long long)a.lp_off[cur_l] + cur_bi * kMT + lane;
+  // entries are prefetched two ahead (registers), column tiles one ahead (cp.async)
+  int4 cur = pair_at(i_cur);
+  int4 nxt = pair_at(i_nxt);
+  stage_col(a, buf[0], cur.y, (cur.z >> 8) & 0xff, lane);
+  for (int it = 0; i_cur >= 0; ++it) {
+    const long long i_nn = i_nxt >= 0 ? next_index() : -1;
+    const int4 nn = pair_at(i_nn);
+    if (cur.x != cur_row) {   // new tile row: its operands into registers
+      cur_row = cur.x;
+      ni = cur.z & 0xff;
+      const long long m = (long long)cur.x + lane;
       am = ac = make_float4(0.f, 0.f, 0.f, 0.f);
       if (lane < ni) {
 #pragma unroll
@@ -635,10 +671,8 @@ __global__ void __launch_bounds__(kPairWarps * 32) pair_tiles_kernel(MergeArgs a
         ma_rgb = fmaxf(ma_rgb, __shfl_xor_sync(0xffffffffu, ma_rgb, o));
       }
     }
-    int4 nxt = cur;
-    if (w + 1 < w1) {
-      nxt = pair_at(w + 1);
-      stage_col(a, buf[(it + 1) & 1], nxt.x, nxt.z, lane);
+    if (i_nxt >= 0) {
+      stage_col(a, buf[(it + 1) & 1], nxt.y, (nxt.z >> 8) & 0xff, lane);
       cp_async_wait<1>();
     } else {
       cp_async_wait<0>();
@@ -646,9 +680,8 @@ __global__ void __launch_bounds__(kPairWarps * 32) pair_tiles_kernel(MergeArgs a
     __syncwarp();
     if (!overflow || cur.w) {
       const ColTile& J = buf[it & 1];
-      const long long P = (long long)a.lp_cnt[cur.x];
-      const int nj = (int)min((long long)kMT, P - (long long)cur.z * kMT);
-      const bool diag = cur.y == cur.z;
+      const int nj = (cur.z >> 8) & 0xff;
+      const bool diag = cur.x == cur.y;
       // the column tile's largest magnitudes -> this tile pair's slacks
       float mb_mu = 0.f, mb_rgb = 0.f;
       if (lane < nj) {
@@ -689,6 +722,9 @@ __global__ void __launch_bounds__(kPairWarps * 32) pair_tiles_kernel(MergeArgs a
     }
     __syncwarp();   // this buffer is restaged two pairs on
     cur = nxt;
+    nxt = nn;
+    i_cur = i_nxt;
+    i_nxt = i_nn;
   }
 }
 
@@ -698,7 +734,17 @@ cudaError_t launch_merge_tile_gates(const MergeArgs& a, cudaStream_t s) {
   const int smem = (int)(sizeof(ColTile) * 2 * kPairWarps);
   cudaError_t e = cudaFuncSetAttribute(pair_tiles_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return e;
-  pair_tiles_kernel<<<a.grid * 2, kPairWarps * 32, smem, s>>>(a);
+  // one wave of resident blocks: each warp takes one contiguous chunk of pairs
+  static int resident = 0;
+  if (resident == 0) {
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&resident, pair_tiles_kernel, kPairWarps * 32, smem);
+    if (e != cudaSuccess || resident < 1) resident = 4;
+  }
+#ifdef ADPS_PAIR_BLOCKS_PER_SM
+  resident = ADPS_PAIR_BLOCKS_PER_SM;
+#endif
+  const unsigned blocks = (unsigned)(a.grid / 8) * (unsigned)resident;   // a.grid = 8 x SM count
+  pair_tiles_kernel<<<blocks, kPairWarps * 32, smem, s>>>(a);
   return cudaGetLastError();
 }
 
