@@ -376,7 +376,10 @@ __device__ __forceinline__ long long find_owner(const unsigned long long* off, l
   return lo;
 }
 
-// one warp per kMT-proposal tile of a large parent (Morton order)
+// one warp per kMT-proposal tile of a large parent (Morton order), lane = proposal:
+// the gate operands into the structure of arrays, the tile's bounding data,
+// and the tile's owner (read by the filter instead of a search)
+static_assert(kMT == 32, "box_kernel: one proposal per lane");
 __global__ void box_kernel(MergeArgs a) {
   const int lane = threadIdx.x & 31;
   const long long warps = (long long)gridDim.x * (blockDim.x >> 5);
@@ -388,25 +391,38 @@ __global__ void box_kernel(MergeArgs a) {
     const long long tl = t - (long long)a.tile_off[l];
     const long long b = (long long)a.lp_off[l] + tl * kMT;
     const long long e = min(b + kMT, (long long)(a.lp_off[l] + a.lp_cnt[l]));
-    double s[3] = {0, 0, 0}, inv_s = 1e300, lo[3] = {1e300, 1e300, 1e300}, hi[3] = {-1e300, -1e300, -1e300};
-    for (long long m = b + lane; m < e; m += 32) {
+    const long long m = b + lane;
+    const bool in = m < e;
+    double mu[3] = {0, 0, 0}, rgb[3] = {0, 0, 0}, inv = 1e300;
+    if (in) {
       const Proposal& M = a.props_s[a.mval_sorted[m]];
+#pragma unroll
       for (int c = 0; c < 3; ++c) {
-        a.gsoa[(long long)(kG_mu + c) * a.soa_cap + m] = M.mu[c];
-        a.gsoa[(long long)(kG_rgb + c) * a.soa_cap + m] = M.rgb[c];
+        mu[c] = M.mu[c];
+        rgb[c] = M.rgb[c];
       }
-      a.gsoa[(long long)kG_inv * a.soa_cap + m] = M.inv_smax;
-      for (int k = 0; k < 6; ++k) a.gsoa[(long long)(kG_prec + k) * a.soa_cap + m] = M.prec[k];
+      inv = M.inv_smax;
+      double prec[6];
+#pragma unroll
+      for (int k = 0; k < 6; ++k) prec[k] = M.prec[k];
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        a.gsoa[(long long)(kG_mu + c) * a.soa_cap + m] = mu[c];
+        a.gsoa[(long long)(kG_rgb + c) * a.soa_cap + m] = rgb[c];
+      }
+      a.gsoa[(long long)kG_inv * a.soa_cap + m] = inv;
+#pragma unroll
+      for (int k = 0; k < 6; ++k) a.gsoa[(long long)(kG_prec + k) * a.soa_cap + m] = prec[k];
       // fp32 (round to nearest) copies for the conservative prefilter, two float4 per proposal
-      reinterpret_cast<float4*>(a.fsoa)[2 * m] =
-          make_float4((float)M.mu[0], (float)M.mu[1], (float)M.mu[2], (float)M.inv_smax);
-      reinterpret_cast<float4*>(a.fsoa)[2 * m + 1] = make_float4((float)M.rgb[0], (float)M.rgb[1], (float)M.rgb[2], 0.0f);
-      for (int c = 0; c < 3; ++c) {
-        s[c] += M.mu[c];
-        lo[c] = fmin(lo[c], M.rgb[c]);
-        hi[c] = fmax(hi[c], M.rgb[c]);
-      }
-      inv_s = fmin(inv_s, M.inv_smax);
+      reinterpret_cast<float4*>(a.fsoa)[2 * m] = make_float4((float)mu[0], (float)mu[1], (float)mu[2], (float)inv);
+      reinterpret_cast<float4*>(a.fsoa)[2 * m + 1] = make_float4((float)rgb[0], (float)rgb[1], (float)rgb[2], 0.0f);
+    }
+    double s[3] = {mu[0], mu[1], mu[2]}, inv_s = inv;
+    double lo[3], hi[3];
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      lo[c] = in ? rgb[c] : 1e300;
+      hi[c] = in ? rgb[c] : -1e300;
     }
     for (int o = 16; o > 0; o >>= 1) {
       for (int c = 0; c < 3; ++c) {
@@ -419,10 +435,9 @@ __global__ void box_kernel(MergeArgs a) {
     const double cnt = (double)(e - b);
     const double cen[3] = {s[0] / cnt, s[1] / cnt, s[2] / cnt};
     double r = 0.0;
-    for (long long m = b + lane; m < e; m += 32) {
-      const Proposal& M = a.props_s[a.mval_sorted[m]];
-      const double dx = M.mu[0] - cen[0], dy = M.mu[1] - cen[1], dz = M.mu[2] - cen[2];
-      r = fmax(r, sqrt(dx * dx + dy * dy + dz * dz));
+    if (in) {
+      const double dx = mu[0] - cen[0], dy = mu[1] - cen[1], dz = mu[2] - cen[2];
+      r = sqrt(dx * dx + dy * dy + dz * dz);
     }
     for (int o = 16; o > 0; o >>= 1) r = fmax(r, __shfl_xor_sync(0xffffffffu, r, o));
     if (lane == 0) {
@@ -435,6 +450,7 @@ __global__ void box_kernel(MergeArgs a) {
       B.r = r * (1.0 + 1e-12) + 1e-300;   // rounding guard: the sphere really encloses
       B.inv_s = inv_s;
       a.boxes[t] = B;
+      a.tile_owner[t] = (int)l;
     }
   }
 }
@@ -471,41 +487,34 @@ __device__ __forceinline__ int4 pair_entry(const MergeArgs& a, long long l, long
   return make_int4((int)(o + bi * kMT), (int)(o + bj * kMT), ni | (nj << 8), live ? 1 : 0);
 }
 
-// one warp per (parent, tile row bi) of the upper-triangular tile matrix:
-// keep the pairs (bi, bj >= bi) the bounding data cannot exclude; a row's
-// survivors are stored contiguously in bj order (one reservation per row), so
-// the gate kernel can keep tile bi resident across them
+// a block per (parent, tile row bi) of the upper-triangular tile matrix, a
+// warp per 32 columns: keep the pairs (bi, bj >= bi) the bounding data cannot
+// exclude (one reservation per warp chunk; the gate kernel takes pairs in any
+// order).  Blocks, not warps, per row: the longest rows (a parent with
+// thousands of proposals) no longer serialise on one warp.
 __global__ void tile_pair_filter_kernel(MergeArgs a) {
-  const int lane = threadIdx.x & 31;
-  const long long warps = (long long)gridDim.x * (blockDim.x >> 5);
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
   const long long n_large = (long long)a.ctr->n_large;
   const long long rows = n_large > 0 ? (long long)a.tile_off[n_large] : 0;
-  for (long long r = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); r < rows; r += warps) {
-    const long long l = find_owner(a.tile_off, n_large, (unsigned long long)r);
+  for (long long r = blockIdx.x; r < rows; r += gridDim.x) {
+    const long long l = a.tile_owner[r];
     const long long tb = (long long)a.tile_off[l];
     const long long bi = r - tb;
     const long long T = (long long)a.tile_cnt[l];
-    const TileBox A = a.boxes[tb + bi];
-    int cnt = 0;
-    for (long long j0 = bi; j0 < T; j0 += 32) {
-      const long long bj = j0 + lane;
-      const bool keep = bj < T && boxes_may_merge(A, a.boxes[tb + bj], a.gamma_d, a.gamma_c);
-      cnt += __popc(__ballot_sync(0xffffffffu, keep));
-    }
-    if (cnt == 0) continue;
-    unsigned long long base = 0;
-    if (lane == 0) base = atomicAdd(&a.ctr->n_tile_pairs, (unsigned long long)cnt);
-    base = __shfl_sync(0xffffffffu, base, 0);
-    if ((long long)(base + cnt) > a.tile_pairs_cap) {
-      if (lane == 0) atomicOr(&a.ctr->overflow, 4u);
-      continue;
-    }
-    for (long long j0 = bi; j0 < T; j0 += 32) {
+    const TileBox A = a.boxes[r];
+    for (long long j0 = bi + 32 * wid; j0 < T; j0 += 32 * nw) {   // warp-uniform
       const long long bj = j0 + lane;
       const bool keep = bj < T && boxes_may_merge(A, a.boxes[tb + bj], a.gamma_d, a.gamma_c);
       const unsigned m = __ballot_sync(0xffffffffu, keep);
+      if (!m) continue;
+      unsigned long long base = 0;
+      if (lane == 0) base = atomicAdd(&a.ctr->n_tile_pairs, (unsigned long long)__popc(m));
+      base = __shfl_sync(0xffffffffu, base, 0);
+      if ((long long)(base + __popc(m)) > a.tile_pairs_cap) {
+        if (lane == 0) atomicOr(&a.ctr->overflow, 4u);
+        continue;
+      }
       if (keep) a.tile_pairs[base + __popc(m & ((1u << lane) - 1u))] = pair_entry(a, l, bi, bj, true);
-      base += __popc(m);
     }
   }
 }
@@ -730,7 +739,7 @@ __global__ void __launch_bounds__(kPairWarps * 32) pair_tiles_kernel(MergeArgs a
 
 cudaError_t launch_merge_tile_gates(const MergeArgs& a, cudaStream_t s) {
   box_kernel<<<a.grid, 256, 0, s>>>(a);
-  tile_pair_filter_kernel<<<a.grid, 256, 0, s>>>(a);   // warp per tile row
+  tile_pair_filter_kernel<<<a.grid, 128, 0, s>>>(a);   // block per tile row
   const int smem = (int)(sizeof(ColTile) * 2 * kPairWarps);
   cudaError_t e = cudaFuncSetAttribute(pair_tiles_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return e;

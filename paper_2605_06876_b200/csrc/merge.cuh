@@ -71,7 +71,8 @@ struct MergeArgs {
   int* mval;                               // [cap]
   unsigned long long* mkey_sorted;
   int* mval_sorted;                        // Morton order: [lp_off[l], +P_l) -> proposal q
-  TileBox* boxes;                          // [cap / 64 + n_split]
+  TileBox* boxes;                          // [cap / kMT + n_split]
+  int* tile_owner;                         // [cap / kMT + n_split] large parent of each tile
   double* gsoa;                            // [13][soa_cap] gate operands in Morton order
   float* fsoa;                             // [soa_cap][2] float4: fp32 (mu, inv_smax), (rgb, 0) (prefilter)
   long long soa_cap;

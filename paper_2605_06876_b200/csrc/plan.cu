@@ -98,7 +98,7 @@ struct adps_plan {
   // merge / cap scratch (proposal space)
   Buf small_list, pstart, n_groups, work_cnt, work_off, props_s, psrc, pcand, gkey, gval, gkey_sorted, gval_sorted,
       grp_first, gpar, gext, gfirst_of, glist, scan3_val, scan3_flag, scan3_ticket, large_of, lp_cnt, lp_off, tile_cnt, tile_off, mkey,
-      mval, mkey_sorted, mval_sorted, boxes, tile_pairs, gsoa, fsoa;
+      mval, mkey_sorted, mval_sorted, boxes, tile_owner, tile_pairs, gsoa, fsoa;
   Buf scan_val, scan_flag, scan_ticket, scan2_val, scan2_flag, scan2_ticket, cub_tmp;
   Buf ctr;
   Counters* ctr_host = nullptr;
@@ -277,7 +277,7 @@ extern "C" adps_status adps_plan_destroy(adps_plan* P) {
                  &P->props_s, &P->psrc, &P->pcand, &P->gkey, &P->gval, &P->gkey_sorted, &P->gval_sorted, &P->grp_first,
                  &P->gpar, &P->gext, &P->gfirst_of, &P->glist, &P->scan3_val, &P->scan3_flag, &P->scan3_ticket,
                  &P->large_of, &P->lp_cnt, &P->lp_off, &P->tile_cnt, &P->tile_off, &P->mkey, &P->mval,
-                 &P->mkey_sorted, &P->mval_sorted, &P->boxes, &P->tile_pairs, &P->gsoa, &P->fsoa, &P->deferred, &P->cand_bits, &P->rawc, &P->twords,
+                 &P->mkey_sorted, &P->mval_sorted, &P->boxes, &P->tile_owner, &P->tile_pairs, &P->gsoa, &P->fsoa, &P->deferred, &P->cand_bits, &P->rawc, &P->twords,
                  &P->nrm_val, &P->nrm_len, &P->nrm_acc, &P->nrm_reach, &P->nrm_rmax, &P->nrm_walked,
                  &P->nrm_idx, &P->nrm_tmp};
   for (Buf* b : bufs)
@@ -875,6 +875,7 @@ static adps_status phase1_merge_part(adps_plan* P, cudaStream_t s) {
   CK(ensure(P->mkey_sorted, 8 * rc));
   CK(ensure(P->mval_sorted, 4 * rc));
   CK(ensure(P->boxes, sizeof(TileBox) * (rc / kMT + sc + 1)));
+  CK(ensure(P->tile_owner, sizeof(int) * (rc / kMT + sc + 1)));
   CK(ensure(P->gsoa, 8ll * 13 * rc));
   CK(ensure(P->fsoa, 4ll * 8 * rc));
   {
@@ -962,6 +963,7 @@ static adps_status phase1_merge_part(adps_plan* P, cudaStream_t s) {
   ma.mkey_sorted = P->mkey_sorted.as<unsigned long long>();
   ma.mval_sorted = P->mval_sorted.as<int>();
   ma.boxes = P->boxes.as<TileBox>();
+  ma.tile_owner = P->tile_owner.as<int>();
   ma.gsoa = P->gsoa.as<double>();
   ma.fsoa = P->fsoa.as<float>();
   ma.soa_cap = rc;

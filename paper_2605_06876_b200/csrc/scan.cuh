@@ -12,7 +12,10 @@
 namespace adps {
 
 constexpr int kScanThreads = 256;
-constexpr int kScanItems = 8;
+#ifndef ADPS_SCAN_ITEMS
+#define ADPS_SCAN_ITEMS 8
+#endif
+constexpr int kScanItems = ADPS_SCAN_ITEMS;
 constexpr int kScanTile = kScanThreads * kScanItems;
 
 struct ScanState {
@@ -130,12 +133,24 @@ __global__ void __launch_bounds__(kScanThreads) scan_kernel(Policy pol, long lon
     if (lane == 0 && base + kScanTile >= n) pol.total(s_prefix + agg);
   }
   __syncthreads();
+  // exclusive prefixes back through shared memory, so the stores are striped
+  // (coalesced) like the loads; an item's value is the next prefix minus its own
   unsigned long long e = s_prefix + thread_excl;
 #pragma unroll
   for (int j = 0; j < kScanItems; ++j) {
-    long long i = base + (long long)tid * kScanItems + j;
-    if (i < n) pol.store(i, e, loc[j]);
+    sv[tid * kScanItems + j] = e;
     e += loc[j];
+  }
+  __syncthreads();
+  const unsigned long long end = s_prefix + s_agg;
+#pragma unroll
+  for (int j = 0; j < kScanItems; ++j) {
+    const int k = j * kScanThreads + tid;
+    const long long i = base + k;
+    if (i < n) {
+      const unsigned long long ex = sv[k];
+      pol.store(i, ex, (k + 1 < kScanTile ? sv[k + 1] : end) - ex);
+    }
   }
 }
 
