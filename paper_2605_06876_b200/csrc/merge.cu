@@ -798,7 +798,10 @@ constexpr int kBlockGroup = 512;   // larger groups: a block per group
 
 // groups of up to kSmallGroup members: one thread per group, members summed in
 // ascending index order; also writes the sort padding beyond the group count
-__global__ void group_small_kernel(MergeArgs a, long long cap) {
+#ifndef ADPS_GROUP_MINB
+#define ADPS_GROUP_MINB 6
+#endif
+__global__ void __launch_bounds__(128, ADPS_GROUP_MINB) group_small_kernel(MergeArgs a, long long cap) {
   const long long G = (long long)a.ctr->n_groups_all;
   for (long long g = (long long)blockIdx.x * blockDim.x + threadIdx.x; g < cap;
        g += (long long)gridDim.x * blockDim.x) {
@@ -855,7 +858,7 @@ __global__ void group_small_kernel(MergeArgs a, long long cap) {
 }
 
 // larger groups: one warp per group, lane-strided sums + butterfly
-__global__ void group_kernel(MergeArgs a, long long cap) {
+__global__ void __launch_bounds__(256, (ADPS_GROUP_MINB + 1) / 2) group_kernel(MergeArgs a, long long cap) {
   const int lane = threadIdx.x & 31;
   const long long warps = (long long)gridDim.x * (blockDim.x >> 5);
   const long long nl = (long long)a.ctr->n_mid_groups;

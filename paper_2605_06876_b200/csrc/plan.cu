@@ -1012,7 +1012,7 @@ static adps_status phase1_merge_part(adps_plan* P, cudaStream_t s) {
       const int mbits = 30 + ceil_log2((unsigned long long)n_split + 2);
       CK(cub_sort_pairs(P, ma.mkey, ma.mkey_sorted, ma.mval, ma.mval_sorted, rc, mbits, s));
       CK(launch_merge_tile_gates(ma, s));
-      mark(P, "merge_tile_gates", s, 3);
+      mark(P, "merge_tile_gates", s, 4);   // morton, box, filter, pair tiles
     }
     CK(cudaStreamWaitEvent(s, P->ev_small, 0));   // join: all unions are in before the groups
     if (n_regions > 0) {

@@ -55,7 +55,10 @@ __device__ __forceinline__ double sclip(double x, double a) {
   return s * fmin(fabs(x), a);
 }
 
-__global__ void child_init_kernel(ChildArgs a) {
+#ifndef ADPS_CHILD_MINB
+#define ADPS_CHILD_MINB 6
+#endif
+__global__ void __launch_bounds__(128, ADPS_CHILD_MINB) child_init_kernel(ChildArgs a) {
   long long n = (long long)*a.n_regions;
   if (n > a.region_cap) n = a.region_cap;
   for (long long rid = (long long)blockIdx.x * blockDim.x + threadIdx.x; rid < n;
