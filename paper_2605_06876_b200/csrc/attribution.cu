@@ -621,16 +621,20 @@ __device__ __forceinline__ int border_slot(int lx, int ly) {
   return 2 * kTileW + kTileH + ly;   // lx == kTileW - 1
 }
 
-__global__ void border_kernel(BorderParams P) {
+constexpr int kBorderTilesPerBlock = 1;
+__global__ void __launch_bounds__(kBorderSlots * kBorderTilesPerBlock) border_kernel(BorderParams P) {
   // 128 threads = the tile's border slots; warp w = side w (top, bottom, left,
   // right).  Runs along an edge ask for the same union many times: lanes
   // holding the same (fragment, neighbour fragment) pair unite once (match_any)
+  // kBorderTilesPerBlock tiles per block (short blocks: fewer of them to schedule)
   const int tiles_per_view = P.tiles_x * P.tiles_y;
-  const int v = blockIdx.x / tiles_per_view;
-  const int t = blockIdx.x % tiles_per_view;
+  const long long tile = (long long)blockIdx.x * kBorderTilesPerBlock + threadIdx.x / kBorderSlots;
+  if (tile >= P.n_tiles) return;   // warp-uniform
+  const int v = (int)(tile / tiles_per_view);
+  const int t = (int)(tile % tiles_per_view);
   const int tyi = t / P.tiles_x, txi = t % P.tiles_x;
-  const int s = threadIdx.x;
-  const int gp = s < kBorderSlots ? P.border[(long long)blockIdx.x * kBorderSlots + s] : -1;
+  const int s = threadIdx.x % kBorderSlots;
+  const int gp = P.border[tile * kBorderSlots + s];
   if (__all_sync(0xffffffffu, gp < 0)) return;   // warp-uniform
   int lx, ly;
   if (s < kTileW) { lx = s; ly = 0; }
@@ -830,7 +834,9 @@ cudaError_t launch_attribution_tail(const AttributionArgs& a, cudaStream_t s, Ma
   B.tiles_y = P.tiles_y;
   B.W = a.W;
   B.H = a.H;
-  border_kernel<<<(unsigned)nblocks, 128, 0, s>>>(B);
+  B.n_tiles = nblocks;
+  border_kernel<<<(unsigned)((nblocks + kBorderTilesPerBlock - 1) / kBorderTilesPerBlock),
+                  kBorderSlots * kBorderTilesPerBlock, 0, s>>>(B);
   resolve_kernel<<<a.grid_small, 256, 0, s>>>(a.partials, a.partial_parent, a.n_partials, a.partial_cap);
   partial_emit_kernel<<<a.grid_small, 256, 0, s>>>(a.partials, a.partial_parent, a.n_partials, a.partial_cap,
                                                     a.m_min, a.regions, a.n_regions, a.region_cap, a.overflow);

@@ -44,6 +44,7 @@ struct BorderParams {
   int* parent;
   int tiles_x, tiles_y;
   int W, H;
+  long long n_tiles;
 };
 
 struct AttributionArgs {

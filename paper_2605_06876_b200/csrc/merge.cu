@@ -164,9 +164,14 @@ __global__ void small_pairs_kernel(MergeArgs a) {
   }
 }
 
-__global__ void __launch_bounds__(1024) offsets_1block_kernel(const unsigned long long* __restrict__ in,
-                                                              unsigned long long* __restrict__ out,
-                                                              const unsigned long long* __restrict__ n_dev) {
+// exclusive scans of up to three count arrays (+ total at [n]), a block each
+struct Offsets3 {
+  const unsigned long long* in[3];
+  unsigned long long* out[3];
+};
+__global__ void __launch_bounds__(1024) offsets_1block_kernel(Offsets3 io, const unsigned long long* __restrict__ n_dev) {
+  const unsigned long long* __restrict__ in = io.in[blockIdx.x];
+  unsigned long long* __restrict__ out = io.out[blockIdx.x];
   __shared__ unsigned long long warp_tot[32];
   __shared__ unsigned long long carry;
   const long long n = (long long)*n_dev;
@@ -306,18 +311,20 @@ cudaError_t launch_small_pairs(const MergeArgs& a, cudaStream_t s) {
 }
 
 cudaError_t launch_large_offsets(const MergeArgs& a, cudaStream_t s) {
-  offsets_1block_kernel<<<1, 1024, 0, s>>>(a.work_cnt, a.work_off, &a.ctr->n_large);
-  offsets_1block_kernel<<<1, 1024, 0, s>>>(a.lp_cnt, a.lp_off, &a.ctr->n_large);
-  offsets_1block_kernel<<<1, 1024, 0, s>>>(a.tile_cnt, a.tile_off, &a.ctr->n_large);
+  Offsets3 io;
+  io.in[0] = a.work_cnt;
+  io.out[0] = a.work_off;
+  io.in[1] = a.lp_cnt;
+  io.out[1] = a.lp_off;
+  io.in[2] = a.tile_cnt;
+  io.out[2] = a.tile_off;
+  offsets_1block_kernel<<<3, 1024, 0, s>>>(io, &a.ctr->n_large);
   return cudaGetLastError();
 }
 
 cudaError_t launch_merge_small_gates(const MergeArgs& a, cudaStream_t s) {
   small_pairs_kernel<<<a.grid, 256, 0, s>>>(a);
-  offsets_1block_kernel<<<1, 1024, 0, s>>>(a.work_cnt, a.work_off, &a.ctr->n_large);
-  offsets_1block_kernel<<<1, 1024, 0, s>>>(a.lp_cnt, a.lp_off, &a.ctr->n_large);
-  offsets_1block_kernel<<<1, 1024, 0, s>>>(a.tile_cnt, a.tile_off, &a.ctr->n_large);
-  return cudaGetLastError();
+  return launch_large_offsets(a, s);
 }
 
 // ---- exact spatial pruning for large parents --------------------------------

@@ -1006,7 +1006,7 @@ static adps_status phase1_merge_part(adps_plan* P, cudaStream_t s) {
       P->keep_pending = true;
     }
     CK(launch_large_offsets(ma, s));
-    mark(P, "merge_small_gates", s, 5);
+    mark(P, "merge_small_gates", s, 3);   // small gates + survivor scan (second stream), large offsets
     if (n_regions > 0) {
       CK(launch_merge_morton(ma, rc, s));
       const int mbits = 30 + ceil_log2((unsigned long long)n_split + 2);
