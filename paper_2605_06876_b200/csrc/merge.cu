@@ -630,15 +630,19 @@ __global__ void __launch_bounds__(kPairWarps * 32) pair_tiles_kernel(MergeArgs a
     if (lane == 0) v = atomicAdd(counter, (unsigned long long)kPairChunk);
     return v;   // lane 0 only; broadcast when it is consumed
   };
+  // two reservations in flight: a contended counter's reply takes longer than
+  // one pair's work
   long long c_end = 0, pos = 0;
-  unsigned long long c_next = grab();
+  unsigned long long c_next1 = grab();
+  unsigned long long c_next2 = grab();
   auto next_index = [&]() -> long long {   // -1 when exhausted
     if (pos >= c_end) {
-      const long long c = (long long)__shfl_sync(0xffffffffu, c_next, 0);
+      const long long c = (long long)__shfl_sync(0xffffffffu, c_next1, 0);
       if (c >= W) return -1;
       pos = c;
       c_end = min(W, c + kPairChunk);
-      c_next = grab();
+      c_next1 = c_next2;
+      c_next2 = grab();
     }
     return pos++;
   };

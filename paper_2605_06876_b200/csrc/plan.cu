@@ -140,6 +140,8 @@ struct adps_plan {
   static constexpr int kMaxChunks = 16;
   cudaEvent_t ev_chunk[kMaxChunks] = {};
   cudaEvent_t ev_attr = nullptr;
+  cudaEvent_t ev_cfork = nullptr, ev_child = nullptr;   // child init on the second stream
+  bool child_pending = false;
   bool attr_pending = false;
   int pipeline = ADPS_PIPELINE_DEFAULT;
   int fb_children = 2;   // children per fallback parent of the last phase 1
@@ -247,6 +249,8 @@ extern "C" adps_status adps_plan_create(adps_plan** plan, int32_t device, int64_
   cudaEventCreateWithFlags(&P->ev_fork, cudaEventDisableTiming);
   cudaEventCreateWithFlags(&P->ev_small, cudaEventDisableTiming);
   cudaEventCreateWithFlags(&P->ev_keep, cudaEventDisableTiming);
+  cudaEventCreateWithFlags(&P->ev_cfork, cudaEventDisableTiming);
+  cudaEventCreateWithFlags(&P->ev_child, cudaEventDisableTiming);
   cudaEventCreateWithFlags(&P->ev_nfork, cudaEventDisableTiming);
   cudaEventCreateWithFlags(&P->ev_norm, cudaEventDisableTiming);
   cudaEventCreateWithFlags(&P->ev_attr, cudaEventDisableTiming);
@@ -291,6 +295,8 @@ extern "C" adps_status adps_plan_destroy(adps_plan* P) {
   if (P->ev_fork) cudaEventDestroy(P->ev_fork);
   if (P->ev_small) cudaEventDestroy(P->ev_small);
   if (P->ev_keep) cudaEventDestroy(P->ev_keep);
+  if (P->ev_cfork) cudaEventDestroy(P->ev_cfork);
+  if (P->ev_child) cudaEventDestroy(P->ev_child);
   if (P->ev_nfork) cudaEventDestroy(P->ev_nfork);
   if (P->ev_norm) cudaEventDestroy(P->ev_norm);
   if (P->ev_attr) cudaEventDestroy(P->ev_attr);
@@ -692,7 +698,7 @@ extern "C" adps_status adps_step_phase1_begin(adps_plan* P, void* stream_v, cons
 }
 
 // attribution + region statistics + child init over this plan's (local) views
-static adps_status phase1_local(adps_plan* P, cudaStream_t s, long long* n_regions_out) {
+static adps_status phase1_local(adps_plan* P, cudaStream_t s, long long* n_regions_out, bool defer_child = false) {
   CK(cudaSetDevice(P->device));
   adps_status st = ADPS_OK;
   const adps_gaussians* g = &P->cx.g;
@@ -788,8 +794,22 @@ static adps_status phase1_local(adps_plan* P, cudaStream_t s, long long* n_regio
   ca.ctr = ctr;
   long long cgrid = (n_regions + 127) / 128;
   ca.grid = (unsigned)(cgrid < 1 ? 1 : (cgrid > 65535 ? 65535 : cgrid));
-  if (n_regions > 0) CK(launch_child_init(ca, s));
-  mark(P, "child_init", s, n_regions > 0 ? 1 : 0);
+  ca.write_keys = true;
+  if (n_regions > 0 && defer_child && !P->timing) {
+    // the sort keys on this stream (the region sort starts at once); child init
+    // on the second stream, concurrently with the sort; joined before the ranges
+    ca.write_keys = false;
+    CK(launch_region_keys(ca.regions, n_regions, ca.cand_rank, bits_v, bits_b, bits_p, ca.keys, ca.vals, s));
+    CK(cudaEventRecord(P->ev_cfork, s));
+    CK(cudaStreamWaitEvent(P->aux, P->ev_cfork, 0));
+    CK(launch_child_init(ca, P->aux));
+    CK(cudaEventRecord(P->ev_child, P->aux));
+    P->child_pending = true;
+    mark(P, "child_init", s, 2);
+  } else {
+    if (n_regions > 0) CK(launch_child_init(ca, s));
+    mark(P, "child_init", s, n_regions > 0 ? 1 : 0);
+  }
   P->n_regions_cur = n_regions;
   *n_regions_out = n_regions;
   return ADPS_OK;
@@ -906,6 +926,10 @@ static adps_status phase1_merge_part(adps_plan* P, cudaStream_t s) {
   ra.regions_per_view = P->regions_per_view.as<int>();
   long long rgrid = (n_regions + 255) / 256;
   ra.grid = (unsigned)(rgrid < 1 ? 1 : (rgrid > 65535 ? 65535 : rgrid));
+  if (P->child_pending) {   // valid flags (read by the ranges) and proposals
+    CK(cudaStreamWaitEvent(s, P->ev_child, 0));
+    P->child_pending = false;
+  }
   CK(launch_ranges(ra, s));
   mark(P, "sort_ranges", s, n_regions > 0 ? 1 : 0);
   if (n_regions > 0) P->lib_calls += 1;
@@ -1112,7 +1136,7 @@ extern "C" adps_status adps_step_phase1_end(adps_plan* P, void* stream_v, adps_c
   P->have_begin = false;
   cudaStream_t s = (cudaStream_t)stream_v;
   long long nr = 0;
-  adps_status st = phase1_local(P, s, &nr);
+  adps_status st = phase1_local(P, s, &nr, /*defer_child=*/true);
   if (st != ADPS_OK) return st;
   return phase1_merge(P, s, counts);
 }

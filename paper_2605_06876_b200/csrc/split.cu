@@ -183,12 +183,14 @@ __global__ void __launch_bounds__(128, ADPS_CHILD_MINB) child_init_kernel(ChildA
       a.props[rid] = P;
     }
     a.valid[rid] = ok ? 1 : 0;
-    const unsigned long long rank = (unsigned long long)a.cand_rank[gi];
-    a.keys[rid] = (((rank << a.bits_v | (unsigned long long)R.view_pos) << a.bits_b |
-                    (unsigned long long)R.band)
-                   << a.bits_p) |
-                  (unsigned long long)R.minpix;
-    a.vals[rid] = (int)rid;
+    if (a.write_keys) {
+      const unsigned long long rank = (unsigned long long)a.cand_rank[gi];
+      a.keys[rid] = (((rank << a.bits_v | (unsigned long long)R.view_pos) << a.bits_b |
+                      (unsigned long long)R.band)
+                     << a.bits_p) |
+                    (unsigned long long)R.minpix;
+      a.vals[rid] = (int)rid;
+    }
     if (a.dbg_stats) {
       double* d = a.dbg_stats + 10 * rid;
       d[0] = cx; d[1] = cy; d[2] = e1x; d[3] = e1y; d[4] = sig1; d[5] = sig2;

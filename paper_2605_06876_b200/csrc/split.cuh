@@ -45,8 +45,9 @@ struct ChildArgs {
   int bits_v, bits_b, bits_p;
   Proposal* props;
   unsigned char* valid;
-  unsigned long long* keys;
+  unsigned long long* keys;   // written when write_keys (else by launch_region_keys)
   int* vals;
+  bool write_keys;
   double* dbg_stats;         // [cap,10] or null
   double* dbg_child;         // [cap,16] or null
   Counters* ctr;
