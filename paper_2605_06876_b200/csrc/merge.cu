@@ -586,6 +586,9 @@ __device__ __forceinline__ bool reject32(const float4 am, const float4 ac, const
   return (dc > gcs) | (n2 * (w * w) > gd2s);
 }
 constexpr int kPairWarps = 4;
+#ifndef ADPS_PAIR_LOCAL_UF
+#define ADPS_PAIR_LOCAL_UF 0
+#endif
 #ifndef ADPS_PAIR_CHUNK
 #define ADPS_PAIR_CHUNK 1
 #endif
@@ -611,6 +614,10 @@ __device__ __forceinline__ void stage_col(const MergeArgs& a, ColTile& B, long l
 // pair is taken with the box test inline.
 __global__ void __launch_bounds__(kPairWarps * 32) pair_tiles_kernel(MergeArgs a) {
   extern __shared__ __align__(16) unsigned char pt_smem[];
+#if ADPS_PAIR_LOCAL_UF
+  __shared__ int luf[kPairWarps][64];   // warp-local union-find of a tile pair
+  __shared__ int lq[kPairWarps][32];    // its row proposals
+#endif
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   ColTile* buf = reinterpret_cast<ColTile*>(pt_smem) + 2 * wid;
   const bool overflow = (a.ctr->overflow & 4u) != 0;
@@ -738,7 +745,30 @@ __global__ void __launch_bounds__(kPairWarps * 32) pair_tiles_kernel(MergeArgs a
 #endif
         if (ok) pass |= 1u << jj;
       }
+#if ADPS_PAIR_LOCAL_UF
+      // the tile pair's links first in a warp-local union-find over its 64
+      // nodes (rows 0..31, columns 32..63) in shared memory, then one global
+      // union per node whose local root differs: a dense tile pair costs at
+      // most 63 global unions instead of one per passing pair
+      if (__any_sync(0xffffffffu, pass != 0u)) {
+        int* L = luf[wid];
+        L[lane] = lane;
+        L[32 + lane] = 32 + lane;
+        lq[wid][lane] = qa;
+        __syncwarp();
+        for (unsigned p = pass; p; p &= p - 1u) uf_unite(L, lane, 32 + __ffs(p) - 1);
+        __syncwarp();
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int nd = lane + 32 * h;
+          const int r = uf_find(L, nd);
+          if (r != nd) uf_unite(a.uf, h ? J.q[lane] : qa, r < 32 ? lq[wid][r] : J.q[r - 32]);
+        }
+        __syncwarp();
+      }
+#else
       for (; pass; pass &= pass - 1u) uf_unite(a.uf, qa, J.q[__ffs(pass) - 1]);
+#endif
     }
     __syncwarp();   // this buffer is restaged two pairs on
     cur = nxt;
