@@ -103,16 +103,6 @@ __global__ void minmax_kernel(const float* __restrict__ image, const float* __re
   }
 }
 
-// bits 0..15 of x spread to the even bit positions
-__device__ __forceinline__ unsigned spread16(unsigned x) {
-  x &= 0xffffu;
-  x = (x | (x << 8)) & 0x00ff00ffu;
-  x = (x | (x << 4)) & 0x0f0f0f0fu;
-  x = (x | (x << 2)) & 0x33333333u;
-  x = (x | (x << 1)) & 0x55555555u;
-  return x;
-}
-
 __device__ __forceinline__ double raw_l1_3(float a0, float a1, float a2, float g0, float g1, float g2) {
   // np.abs(rendered - gt).sum(axis=-1) == (|d0| + |d1|) + |d2| in fp64
   return dadd(dadd(fabs(dsub((double)a0, (double)g0)), fabs(dsub((double)a1, (double)g1))),
@@ -171,10 +161,14 @@ __global__ void __launch_bounds__(256) minmax2_kernel(const float* __restrict__ 
       c1 = true;
       if (dom_flag && dom_flag[d1] == 0) dom_flag[d1] = 1;
     }
-    const unsigned b0 = __ballot_sync(0xffffffffu, c0), b1 = __ballot_sync(0xffffffffu, c1);
+    // lane t holds pixels 2t, 2t+1 of the warp's 64: its two bits go to positions
+    // 2(t & 15), 2(t & 15) + 1 of word t / 16 (one REDUX per word)
+    const unsigned cb = ((c0 ? 1u : 0u) | (c1 ? 2u : 0u)) << (2 * (lane & 15));
+    const unsigned w0 = __reduce_or_sync(0xffffffffu, lane < 16 ? cb : 0u);
+    const unsigned w1 = __reduce_or_sync(0xffffffffu, lane < 16 ? 0u : cb);
     const int wp = base + 64 * wid;   // first pixel of this warp: a multiple of 64
-    if (lane == 0 && wp < hw) bits[wp >> 5] = spread16(b0) | (spread16(b1) << 1);
-    if (lane == 1 && wp + 32 < hw) bits[(wp >> 5) + 1] = spread16(b0 >> 16) | (spread16(b1 >> 16) << 1);
+    if (lane == 0 && wp < hw) bits[wp >> 5] = w0;
+    if (lane == 1 && wp + 32 < hw) bits[(wp >> 5) + 1] = w1;
   }
   for (int o = 16; o > 0; o >>= 1) {
     lo = fmin(lo, __shfl_xor_sync(0xffffffffu, lo, o));
