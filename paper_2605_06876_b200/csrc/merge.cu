@@ -355,11 +355,12 @@ __global__ void morton_kernel(MergeArgs a, long long cap) {
       if (l >= 0) {
         unsigned c[3];
         for (int t = 0; t < 3; ++t) {
-          const double u = (a.props_s[q].mu[t] * inv + 0.5) * 1024.0;
-          c[t] = u <= 0.0 ? 0u : (u >= 1023.0 ? 1023u : (unsigned)u);
+          constexpr double kCells = (double)(1 << kMortonBits);
+          const double u = (a.props_s[q].mu[t] * inv + 0.5) * kCells;
+          c[t] = u <= 0.0 ? 0u : (u >= kCells - 1.0 ? (1u << kMortonBits) - 1u : (unsigned)u);
         }
         const unsigned m = spread10(c[0]) | (spread10(c[1]) << 1) | (spread10(c[2]) << 2);
-        key = ((unsigned long long)l << 30) | m;   // 30-bit Morton code
+        key = ((unsigned long long)l << (3 * kMortonBits)) | m;   // 3 x kMortonBits-bit Morton code
       }
     }
     a.mkey[q] = key;

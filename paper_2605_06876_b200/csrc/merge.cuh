@@ -10,6 +10,10 @@ namespace adps {
 #endif
 // proposals per Morton tile of a large parent's gate matrix (exact pruning unit)
 constexpr int kMT = ADPS_MERGE_TILE;
+#ifndef ADPS_MORTON_BITS
+#define ADPS_MORTON_BITS 9
+#endif
+constexpr int kMortonBits = ADPS_MORTON_BITS;   // per axis (<= 10)
 
 // Cross-view merge + cap over all split candidates at once
 // (ref/cross_view_merge.py:33-116, ref/adc.py:184-227).

@@ -1,3 +1,4 @@
+#include <algorithm>
 // C-ABI implementation: the plan (owner of all scratch) and the phase
 // orchestration of adpsplit_step (ref/adc.py:143-245) on one stream.
 #include <cub/cub.cuh>
@@ -1033,7 +1034,10 @@ static adps_status phase1_merge_part(adps_plan* P, cudaStream_t s) {
     mark(P, "merge_small_gates", s, 3);   // small gates + survivor scan (second stream), large offsets
     if (n_regions > 0) {
       CK(launch_merge_morton(ma, rc, s));
-      const int mbits = 30 + ceil_log2((unsigned long long)n_split + 2);
+      // large parents have > small_max proposals each, so their index l is below
+      // n_regions / (small_max + 1): fewer key bits, fewer radix passes
+      const long long l_bound = std::min<long long>(n_split, n_regions / (P->large_threshold + 1));
+      const int mbits = 3 * kMortonBits + ceil_log2((unsigned long long)l_bound + 2);
       CK(cub_sort_pairs(P, ma.mkey, ma.mkey_sorted, ma.mval, ma.mval_sorted, rc, mbits, s));
       CK(launch_merge_tile_gates(ma, s));
       mark(P, "merge_tile_gates", s, 4);   // morton, box, filter, pair tiles
@@ -1301,7 +1305,7 @@ extern "C" adps_status adps_step_phase2(adps_plan* P, void* stream_v, const adps
   ea.sh_dc = out->sh_dc;
   ea.sh_rest = out->sh_rest;
   ea.index_map = (long long*)index_map;
-  CK(launch_emit(ea, s));
+  CK(launch_emit(ea, s, P->timing ? nullptr : P->aux, P->ev_fork, P->ev_small));
   mark(P, "emit", s, (P->n > 0 ? 1 : 0) + ((P->counts.n_split + P->counts.n_clone) > 0 ? 1 : 0));
   return ADPS_OK;
 }

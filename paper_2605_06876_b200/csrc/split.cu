@@ -452,16 +452,30 @@ __global__ void __launch_bounds__(kEmitThreads) emit_kernel(EmitArgs a, long lon
   }
 }
 
-cudaError_t launch_emit(const EmitArgs& a, cudaStream_t s) {
+cudaError_t launch_emit(const EmitArgs& a, cudaStream_t s, cudaStream_t aux, cudaEvent_t fork, cudaEvent_t join) {
+  // the survivor copy (HBM-bound) on the second stream, concurrently with the
+  // latency-bound inserts and clones; `s` waits for it before returning
+  const bool two = aux && a.n > 0;
+  if (two) {
+    cudaError_t e = cudaEventRecord(fork, s);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(aux, fork, 0);
+    if (e != cudaSuccess) return e;
+  }
   if (a.n > 0) {
+    const cudaStream_t ss = two ? aux : s;
     // 8 components per thread (rot's 4 per Gaussian the widest; narrower arrays exit early)
     long long b = (a.n * 4 + 8ll * kEmitThreads - 1) / (8ll * kEmitThreads);
-    emit_survivors_kernel<<<dim3((unsigned)b, a.g.sh_k > 0 ? 6u : 5u), kEmitThreads, 0, s>>>(a);
+    emit_survivors_kernel<<<dim3((unsigned)b, a.g.sh_k > 0 ? 6u : 5u), kEmitThreads, 0, ss>>>(a);
   }
   const long long b_ins = (a.n_split + kEmitThreads - 1) / kEmitThreads;
   const long long b_clone = (a.n_clone + kEmitThreads - 1) / kEmitThreads;
   if (b_ins + b_clone > 0) emit_kernel<<<(unsigned)(b_ins + b_clone), kEmitThreads, 0, s>>>(a, b_ins);
-  return cudaGetLastError();
+  cudaError_t e = cudaGetLastError();
+  if (e == cudaSuccess && two) {
+    e = cudaEventRecord(join, aux);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(s, join, 0);
+  }
+  return e;
 }
 
 // ============================================================ vanilla_densify / remaps

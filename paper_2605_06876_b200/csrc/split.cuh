@@ -120,7 +120,8 @@ struct EmitArgs {
   float* sh_rest;
   long long* index_map;
 };
-cudaError_t launch_emit(const EmitArgs& a, cudaStream_t s);
+cudaError_t launch_emit(const EmitArgs& a, cudaStream_t s, cudaStream_t aux = nullptr, cudaEvent_t fork = nullptr,
+                        cudaEvent_t join = nullptr);
 
 cudaError_t launch_accumulate(double* ga, double* den, const float* vg, const unsigned char* vis,
                               long long n, cudaStream_t s);
