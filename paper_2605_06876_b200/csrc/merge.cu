@@ -818,6 +818,9 @@ cudaError_t launch_merge_flatten(const MergeArgs& a, long long cap, cudaStream_t
 }
 
 // ------------------------------------------------------------------ groups
+constexpr int kSmallGroup = 8;
+constexpr int kBlockGroup = 512;   // larger groups: a block per group
+
 struct GroupStartPolicy {
   MergeArgs a;
   __device__ unsigned long long value(long long s) const {
@@ -825,7 +828,18 @@ struct GroupStartPolicy {
     return (k != 0xffffffffu && (s == 0 || a.gkey_sorted[s - 1] != k)) ? 1ull : 0ull;
   }
   __device__ void store(long long s, unsigned long long ex, unsigned long long v) const {
-    if (v) a.grp_first[ex] = (int)s;
+    if (!v) return;
+    a.grp_first[ex] = (int)s;
+    // work lists of the warp / block reductions: members are sorted by root, so
+    // a group has more than m members iff entry s + m still carries its root
+    const unsigned k = a.gkey_sorted[s];
+    const long long n = a.own ? (long long)a.ctr->n_owned_props : (long long)a.ctr->n_proposals;
+    if (s + kSmallGroup < n && a.gkey_sorted[s + kSmallGroup] == k) {
+      if (s + kBlockGroup < n && a.gkey_sorted[s + kBlockGroup] == k)
+        a.glist[a.glist_cap + atomicAdd(&a.ctr->n_huge_groups, 1ull)] = (int)ex;
+      else
+        a.glist[atomicAdd(&a.ctr->n_mid_groups, 1ull)] = (int)ex;
+    }
   }
   __device__ void total(unsigned long long t) const {
     a.ctr->n_groups_all = t;
@@ -835,8 +849,6 @@ struct GroupStartPolicy {
   }
 };
 
-constexpr int kSmallGroup = 8;
-constexpr int kBlockGroup = 512;   // larger groups: a block per group
 
 // groups of up to kSmallGroup members: one thread per group, members summed in
 // ascending index order; also writes the sort padding beyond the group count
@@ -854,11 +866,7 @@ __global__ void __launch_bounds__(128, ADPS_GROUP_MINB) group_small_kernel(Merge
       const int k = a.pcand[a.gkey_sorted[b]];
       if (g == 0 || a.pcand[a.gkey_sorted[a.grp_first[g - 1]]] != k) a.gfirst_of[k] = (int)g;
     }
-    if (cnt > kSmallGroup) {   // work lists for the warp / block reductions
-      if (cnt > kBlockGroup) a.glist[cap + atomicAdd(&a.ctr->n_huge_groups, 1ull)] = (int)g;
-      else a.glist[atomicAdd(&a.ctr->n_mid_groups, 1ull)] = (int)g;
-      continue;
-    }
+    if (cnt > kSmallGroup) continue;   // the warp / block reductions (lists built by the scan)
     double acc[12] = {0};
     for (int m = b; m < e; ++m) {
       const Proposal& M = a.props_s[a.gval_sorted[m]];
@@ -1026,14 +1034,29 @@ __global__ void __launch_bounds__(256) group_block_kernel(MergeArgs a, long long
   }
 }
 
-cudaError_t launch_merge_groups(const MergeArgs& a, long long cap, ScanState st, cudaStream_t s) {
-  cudaError_t e = launch_scan(GroupStartPolicy{a}, cap, st, s);
+cudaError_t launch_merge_groups(const MergeArgs& a, long long cap, ScanState st, cudaStream_t s, cudaStream_t aux,
+                                cudaEvent_t fork, cudaEvent_t join) {
+  MergeArgs b_ = a;
+  b_.glist_cap = cap;
+  cudaError_t e = launch_scan(GroupStartPolicy{b_}, cap, st, s);
   if (e != cudaSuccess) return e;
+  // the warp / block reductions (lists from the scan) on the second stream,
+  // concurrently with the thread-per-group pass; joined before returning
+  const cudaStream_t s2 = aux ? aux : s;
+  if (aux) {
+    if ((e = cudaEventRecord(fork, s)) != cudaSuccess) return e;
+    if ((e = cudaStreamWaitEvent(aux, fork, 0)) != cudaSuccess) return e;
+  }
+  group_kernel<<<a.grid, 256, 0, s2>>>(a, cap);
+  group_block_kernel<<<a.grid, 256, 0, s2>>>(a, cap);
   long long b = (cap + 127) / 128;
   group_small_kernel<<<(unsigned)(b < 1 ? 1 : (b > 65535 ? 65535 : b)), 128, 0, s>>>(a, cap);
-  group_kernel<<<a.grid, 256, 0, s>>>(a, cap);
-  group_block_kernel<<<a.grid, 256, 0, s>>>(a, cap);
-  return cudaGetLastError();
+  if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  if (aux) {
+    if ((e = cudaEventRecord(join, aux)) != cudaSuccess) return e;
+    if ((e = cudaStreamWaitEvent(s, join, 0)) != cudaSuccess) return e;
+  }
+  return cudaSuccess;
 }
 
 // --------------------------------------------------------------------- cap

@@ -53,6 +53,7 @@ struct MergeArgs {
   double* gext;                            // [cap] extent of group g (compact, for the cap)
   int* gfirst_of;                          // [n_split] first group of candidate k
   int* glist;                              // [3 cap] groups with > 8 / > 512 members; cap list
+  long long glist_cap;                     // = cap (set by launch_merge_groups)
   // per candidate
   int* pstart;                             // [n_split]
   int* n_groups;                           // [n_split]
@@ -106,7 +107,8 @@ cudaError_t launch_large_offsets(const MergeArgs& a, cudaStream_t s);
 cudaError_t launch_merge_morton(const MergeArgs& a, long long cap, cudaStream_t s);
 cudaError_t launch_merge_tile_gates(const MergeArgs& a, cudaStream_t s);
 cudaError_t launch_merge_flatten(const MergeArgs& a, long long cap, cudaStream_t s);
-cudaError_t launch_merge_groups(const MergeArgs& a, long long cap, ScanState st, cudaStream_t s);
+cudaError_t launch_merge_groups(const MergeArgs& a, long long cap, ScanState st, cudaStream_t s,
+                                cudaStream_t aux = nullptr, cudaEvent_t fork = nullptr, cudaEvent_t join = nullptr);
 // cap (ref/cross_view_merge.py:110-116): rank of each group among its parent's
 // groups by (-extent, group order); ranks < n_max become children in rank order
 cudaError_t launch_merge_cap(const MergeArgs& a, long long cap, cudaStream_t s, cudaStream_t aux,

@@ -1047,7 +1047,7 @@ static adps_status phase1_merge_part(adps_plan* P, cudaStream_t s) {
       CK(launch_merge_flatten(ma, rc, s));
       const int gbits = ceil_log2((unsigned long long)rc + 2);
       CK(cub_sort_pairs(P, ma.gkey, ma.gkey_sorted, ma.gval, ma.gval_sorted, rc, gbits, s));
-      CK(launch_merge_groups(ma, rc, sst3, s));
+      CK(launch_merge_groups(ma, rc, sst3, s, P->timing ? nullptr : P->aux, P->ev_cfork, P->ev_child));
       mark(P, "merge_groups", s, 5);
       CK(launch_merge_cap(ma, rc, s, P->aux, P->ev_fork, P->ev_small));
       mark(P, "merge_cap", s, 3);
