@@ -183,6 +183,12 @@ ADPS_API adps_status adps_step_phase2(adps_plan* plan, void* stream, const adps_
 
 ADPS_API adps_status adps_get_report(adps_plan* plan, adps_report* report);
 
+/* The report arrays of adps_get_report copied on `stream` into one device
+ * int32 buffer `dst`, back to back: cand_index, cand_case, cand_proposals,
+ * cand_merged [n_split each], regions_per_view [n_split * n_views],
+ * clone_index [n_clone] (one call instead of six copies from the host). */
+ADPS_API adps_status adps_copy_report(adps_plan* plan, void* stream, int32_t* dst, int64_t n_split, int64_t n_clone);
+
 /* Stage-level parity access to the last phase 1 (device pointers):
  * records[n] in production order, order[n] = record index in
  * (candidate, view, band, first pixel) order (ref/adc.py:190-195),
@@ -287,7 +293,10 @@ ADPS_API adps_status adps_get_launch_count(adps_plan* plan, int64_t* kernels, in
  * host libm's exp (redraw on the host), bit1 internal window too short.
  * With sync == 0 nothing is waited for: consumed/status are read with
  * adps_get_param(ADPS_PARAM_NORMALS_*) after the plan's next phase-1 end
- * (call it between adps_step_phase1_begin and adps_step_phase1_end). */
+ * (call it between adps_step_phase1_begin and adps_step_phase1_end).
+ * sync == 2: as 0, but the kernels are only launched by the next
+ * adps_step_phase1_end at its first host wait, so their host-side launch
+ * cost overlaps GPU work instead of leaving the GPU idle. */
 ADPS_API adps_status adps_normals_pcg64(adps_plan* plan, void* stream, const uint64_t state[2], const uint64_t inc[2],
                                         int64_t n, double* out, int32_t sync, int64_t* consumed, int32_t* status);
 

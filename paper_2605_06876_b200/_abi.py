@@ -65,6 +65,7 @@ EXPORTS = (
     "adps_set_view_sharding", "adps_get_buffer", "adps_step_phase1_refresh", "adps_step_phase1_local",
     "adps_step_phase1_import", "adps_step_phase1_merge", "adps_vanilla_phase1", "adps_reset_flags",
     "adps_remap_rows", "adps_set_parent_sharding", "adps_get_shard", "adps_step_phase1_finish",
+    "adps_copy_report",
 )
 
 _lib = None
@@ -91,6 +92,7 @@ def load(path: str = LIB_PATH):
     lib.adps_step_phase1_end.argtypes = [vp, vp, C.POINTER(Counts)]
     lib.adps_step_phase2.argtypes = [vp, vp, C.POINTER(Gaussians), vp, C.POINTER(GaussiansOut), vp]
     lib.adps_get_report.argtypes = [vp, C.POINTER(Report)]
+    lib.adps_copy_report.argtypes = [vp, vp, vp, C.c_int64, C.c_int64]
     lib.adps_get_regions.argtypes = [vp] + [C.POINTER(vp)] * 5 + [C.POINTER(C.c_int64)]
     lib.adps_set_debug_records.argtypes = [vp, C.c_int32]
     lib.adps_set_debug_maps.argtypes = [vp, vp, vp]

@@ -135,7 +135,10 @@ struct adps_plan {
   cudaStream_t aux = nullptr;
   cudaEvent_t ev_fork = nullptr, ev_small = nullptr, ev_keep = nullptr, ev_nfork = nullptr, ev_norm = nullptr;
   bool keep_pending = false;
-  bool norm_pending = false;   // fallback normals running on the second stream
+  bool norm_pending = false;   // fallback normals running on their own stream
+  bool norm_deferred = false;  // requested (sync == 2), launched at phase 1's first host wait
+  NormalsArgs nrm_args{};
+  cudaStream_t nstream = nullptr;   // the fallback normals' stream
   // attribution pipelined with the input pass: the warp CCL of view chunk c runs
   // on the second stream while the minmax pass reads chunk c+1
   static constexpr int kMaxChunks = 16;
@@ -246,6 +249,7 @@ extern "C" adps_status adps_plan_create(adps_plan** plan, int32_t device, int64_
     int lo = 0, hi = 0;
     cudaDeviceGetStreamPriorityRange(&lo, &hi);
     cudaStreamCreateWithPriority(&P->aux, cudaStreamNonBlocking, ADPS_AUX_PRIORITY ? hi : 0);
+    cudaStreamCreateWithFlags(&P->nstream, cudaStreamNonBlocking);
   }
   cudaEventCreateWithFlags(&P->ev_fork, cudaEventDisableTiming);
   cudaEventCreateWithFlags(&P->ev_small, cudaEventDisableTiming);
@@ -304,6 +308,7 @@ extern "C" adps_status adps_plan_destroy(adps_plan* P) {
   for (int i = 0; i < adps_plan::kMaxChunks; ++i)
     if (P->ev_chunk[i]) cudaEventDestroy(P->ev_chunk[i]);
   if (P->aux) cudaStreamDestroy(P->aux);
+  if (P->nstream) cudaStreamDestroy(P->nstream);
   delete P;
   return ADPS_OK;
 }
@@ -698,6 +703,21 @@ extern "C" adps_status adps_step_phase1_begin(adps_plan* P, void* stream_v, cons
   return ADPS_OK;
 }
 
+// launch fallback normals requested with sync == 2 (waits on the event
+// recorded at the request, not on the work queued since)
+static cudaError_t launch_deferred_normals(adps_plan* P) {
+  if (!P->norm_deferred) return cudaSuccess;
+  P->norm_deferred = false;
+  cudaError_t e = cudaStreamWaitEvent(P->nstream, P->ev_nfork, 0);
+  if (e == cudaSuccess) e = launch_normals(P->nrm_args, P->nrm_tmp.p, P->nrm_tmp.bytes, P->nstream);
+  if (e == cudaSuccess) e = cudaEventRecord(P->ev_norm, P->nstream);
+  if (e != cudaSuccess) return e;
+  P->norm_pending = true;
+  P->launches += 5;
+  P->lib_calls += 2;
+  return cudaSuccess;
+}
+
 // attribution + region statistics + child init over this plan's (local) views
 static adps_status phase1_local(adps_plan* P, cudaStream_t s, long long* n_regions_out, bool defer_child = false) {
   CK(cudaSetDevice(P->device));
@@ -728,6 +748,7 @@ static adps_status phase1_local(adps_plan* P, cudaStream_t s, long long* n_regio
       if (st != ADPS_OK) return st;
     }
     CK(cudaMemcpyAsync(P->ctr_host, ctr, sizeof(Counters), cudaMemcpyDeviceToHost, s));
+    CK(launch_deferred_normals(P));   // host time while the GPU runs the attribution
     CK(cudaStreamSynchronize(s));
     if (!P->ctr_host->overflow) break;
     if (attempt >= 2) return fail(ADPS_BAD_STATE, "region capacity overflow at the analytic bound");
@@ -1086,6 +1107,7 @@ static adps_status phase1_finish(adps_plan* P, cudaStream_t s, adps_counts* coun
   oa.ctr = ctr;
   oa.n_split_dev = &ctr->n_split;
   CK(launch_offsets_cand(oa, n_split, sst2, s));
+  CK(launch_deferred_normals(P));
   if (P->norm_pending) {   // join the fallback normals (read by phase 2; consumed count below)
     CK(cudaStreamWaitEvent(s, P->ev_norm, 0));
     P->norm_pending = false;
@@ -1323,6 +1345,26 @@ extern "C" adps_status adps_get_report(adps_plan* P, adps_report* r) {
   return ADPS_OK;
 }
 
+extern "C" adps_status adps_copy_report(adps_plan* P, void* stream_v, int32_t* dst, int64_t n_split, int64_t n_clone) {
+  if (!P || (!dst && n_split + n_clone > 0)) return fail(ADPS_INVALID_ARG, "NULL argument");
+  if (!P->have_phase1) return fail(ADPS_BAD_STATE, "no phase 1 result");
+  if (n_split < 0 || n_clone < 0) return fail(ADPS_INVALID_ARG, "negative count");
+  if (n_split > (long long)P->counts.n_split || n_clone > (long long)P->counts.n_clone)
+    return fail(ADPS_INVALID_ARG, "counts exceed the last phase 1 (%lld split, %lld clone)",
+                (long long)P->counts.n_split, (long long)P->counts.n_clone);
+  CK(cudaSetDevice(P->device));
+  cudaStream_t s = (cudaStream_t)stream_v;
+  const void* src[6] = {P->split_list.p, P->cand_case.p, P->cand_props.p, P->cand_merged.p, P->regions_per_view.p,
+                        P->clone_list.p};
+  const long long len[6] = {n_split, n_split, n_split, n_split, n_split * P->V, n_clone};
+  long long off = 0;
+  for (int i = 0; i < 6; ++i) {
+    if (len[i] > 0) CK(cudaMemcpyAsync(dst + off, src[i], 4 * len[i], cudaMemcpyDeviceToDevice, s));
+    off += len[i];
+  }
+  return ADPS_OK;
+}
+
 extern "C" adps_status adps_get_regions(adps_plan* P, const adps_region_record** records,
                                         const int32_t** order, const uint8_t** valid, const double** stats,
                                         const double** child, int64_t* n) {
@@ -1540,16 +1582,16 @@ extern "C" adps_status adps_normals_pcg64(adps_plan* P, void* stream_v, const ui
     a.emit_idx = P->nrm_idx.as<int>();
     a.consumed = &ctr->normals_consumed;
     a.status = &ctr->normals_status;
-    // on the second stream: phase 1 continues on `stream` meanwhile; joined
-    // before phase 1's final counts (or right here when sync)
+    // on their own stream: phase 1 continues on `stream` meanwhile; joined
+    // before phase 1's final counts (or right here when sync).  sync == 2:
+    // only recorded here and launched at phase 1's first host wait, while the
+    // GPU is busy (the launches cost ~80 us of host time)
     CK(cudaEventRecord(P->ev_nfork, s));
-    CK(cudaStreamWaitEvent(P->aux, P->ev_nfork, 0));
-    CK(launch_normals(a, P->nrm_tmp.p, P->nrm_tmp.bytes, P->aux));
-    CK(cudaEventRecord(P->ev_norm, P->aux));
-    P->norm_pending = true;
-    P->launches += 5;
-    P->lib_calls += 2;
+    P->nrm_args = a;
+    P->norm_deferred = true;
+    if (sync != 2) CK(launch_deferred_normals(P));
   }
+  if (sync == 2) return ADPS_OK;
   if (sync && P->norm_pending) {
     CK(cudaStreamWaitEvent(s, P->ev_norm, 0));
     P->norm_pending = false;

@@ -212,12 +212,13 @@ class Plan:
         """Tiles the warp CCL of the last phase 1 handed to the block CCL."""
         return self.get_param(_abi.PARAM_DEFERRED_TILES)
 
-    def normals_pcg64(self, bitgen_state: dict, n: int, out: torch.Tensor = None, sync: bool = True):
+    def normals_pcg64(self, bitgen_state: dict, n: int, out: torch.Tensor = None, sync=True):
         """numpy Generator(PCG64).standard_normal(n) on the device, bit-identical.
 
         bitgen_state: ``rng.bit_generator.state``.  Returns (out, consumed,
         status) when sync, else (out, None, None) with consumed/status
-        readable via normals_result() after the next phase1_end."""
+        readable via normals_result() after the next phase1_end; sync=2
+        leaves the launch to that phase1_end (adps.h)."""
         st = bitgen_state["state"]
         m64 = (1 << 64) - 1
         state = (C.c_uint64 * 2)(st["state"] & m64, st["state"] >> 64)
@@ -227,7 +228,7 @@ class Plan:
         consumed, status = C.c_int64(), C.c_int32()
         _abi.check(self.lib.adps_normals_pcg64(self._h, self._stream(), state, inc, int(n), _ptr(out) if n else None,
                                                int(sync), C.byref(consumed), C.byref(status)))
-        if sync:
+        if sync is True or sync == 1:
             return out, int(consumed.value), int(status.value)
         return out, None, None
 
@@ -455,18 +456,12 @@ class Plan:
         r = _abi.Report()
         _abi.check(self.lib.adps_get_report(self._h, C.byref(r)))
         v = int(r.n_views)
-
-        def grab(ptr, n):
-            out = torch.empty(max(n, 0), dtype=torch.int32, device=self.device)
-            if n > 0:
-                _copy_device(out, ptr, n * 4, self.device)
-            return out
-
-        return dict(cand_index=grab(r.cand_index, n_split), cand_case=grab(r.cand_case, n_split),
-                    cand_proposals=grab(r.cand_proposals, n_split),
-                    cand_merged=grab(r.cand_merged, n_split),
-                    regions_per_view=grab(r.regions_per_view, n_split * v).view(-1, max(v, 1)),
-                    clone_index=grab(r.clone_index, n_clone))
+        # one buffer, one native call for the six copies
+        buf = torch.empty(4 * n_split + n_split * v + n_clone, dtype=torch.int32, device=self.device)
+        _abi.check(self.lib.adps_copy_report(self._h, self._stream(), _ptr(buf), int(n_split), int(n_clone)))
+        parts = torch.split(buf, [n_split] * 4 + [n_split * v, n_clone])
+        return dict(cand_index=parts[0], cand_case=parts[1], cand_proposals=parts[2], cand_merged=parts[3],
+                    regions_per_view=parts[4].view(-1, max(v, 1)), clone_index=parts[5])
 
     def regions(self) -> dict:
         """Region records of the last phase 1, in reference order (diagnostic)."""
@@ -613,7 +608,9 @@ class FallbackNormals:
         self.gpu = self.nf > 0 and isinstance(rng.bit_generator, np.random.PCG64)
         self.normals, self._drawn, self._th = None, {}, None
         if self.gpu:
-            self.normals, _, _ = plan.normals_pcg64(rng.bit_generator.state, self.count, sync=False)
+            # launched by phase1_end at its first host wait (sync=2): the ~80 us
+            # of launch calls then overlap the attribution instead of idling the GPU
+            self.normals, _, _ = plan.normals_pcg64(rng.bit_generator.state, self.count, sync=2)
         elif self.nf > 0:
             def _draw():
                 self._drawn["z"] = rng.standard_normal(self.count)
