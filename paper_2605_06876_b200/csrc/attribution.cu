@@ -616,6 +616,9 @@ __device__ __forceinline__ int border_slot(int lx, int ly) {
 }
 
 constexpr int kBorderTilesPerBlock = 1;
+#ifndef ADPS_BORDER_MATCH
+#define ADPS_BORDER_MATCH 1
+#endif
 __global__ void __launch_bounds__(kBorderSlots * kBorderTilesPerBlock) border_kernel(BorderParams P) {
   // 128 threads = the tile's border slots; warp w = side w (top, bottom, left,
   // right).  Runs along an edge ask for the same union many times: lanes
@@ -655,9 +658,16 @@ __global__ void __launch_bounds__(kBorderSlots * kBorderTilesPerBlock) border_ke
     int gq = gqs[k];
     for (int k2 = 0; k2 < k; ++k2)
       if (gqs[k2] == gq) gq = -1;   // the same pair through another direction
+#if ADPS_BORDER_MATCH
     const unsigned long long key = gq >= 0 ? ((unsigned long long)(unsigned)gp << 32) | (unsigned)gq : ~0ull;
     const unsigned peers = __match_any_sync(0xffffffffu, key);
     if (gq < 0 || (int)(threadIdx.x & 31) != __ffs(peers) - 1) continue;
+#else
+    // along an edge equal pairs come in runs: skip a lane whose left neighbour
+    // holds the same pair (unions are idempotent, so leftover duplicates only cost time)
+    const int lgp = __shfl_up_sync(0xffffffffu, gp, 1), lgq = __shfl_up_sync(0xffffffffu, gq, 1);
+    if (gq < 0 || ((threadIdx.x & 31) > 0 && lgp == gp && lgq == gq)) continue;
+#endif
     const PartialRec& B = P.partials[gq];
     if (A->cand == B.cand && A->band == B.band) uf_unite(P.parent, gp, gq);
   }
