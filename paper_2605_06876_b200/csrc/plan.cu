@@ -638,8 +638,17 @@ extern "C" adps_status adps_step_phase1_begin(adps_plan* P, void* stream_v, cons
   sa.split_list = P->split_list.as<int>();
   sa.clone_list = P->clone_list.as<int>();
   sa.ctr = ctr;
-  CK(launch_select(sa, sst, s));
-  mark(P, "select", s, 1);
+  // pipelined: the classes on `stream` (all the input pass needs), the list
+  // scan on the second stream alongside the input pass, joined before the
+  // fallback count
+  const bool split_select = P->pipeline && !P->timing;
+  if (split_select) {
+    CK(launch_select_split(sa, sst, s, P->aux, P->ev_cfork, P->ev_child));
+    mark(P, "select", s, 2);
+  } else {
+    CK(launch_select(sa, sst, s));
+    mark(P, "select", s, 1);
+  }
 
   // ---- ever-dominant flags (ref/adc.py:177-180) and the fallback count, so
   //      the host can draw the fallback normals while the rest runs
@@ -665,6 +674,7 @@ extern "C" adps_status adps_step_phase1_begin(adps_plan* P, void* stream_v, cons
         CK(cudaStreamWaitEvent(P->aux, P->ev_chunk[c], 0));
         CK(launch_tiles_views(a, v0, v1, P->aux));
       }
+      if (split_select) CK(cudaStreamWaitEvent(s, P->ev_child, 0));   // split list + n_split
       CK(launch_fallback_count(P->split_list.as<int>(), P->dom_flag.as<unsigned char>(), ctr, P->sm_count, s));
       CK(launch_attribution_tail(a, P->aux, nullptr, nullptr));
       CK(cudaEventRecord(P->ev_attr, P->aux));
@@ -675,6 +685,7 @@ extern "C" adps_status adps_step_phase1_begin(adps_plan* P, void* stream_v, cons
       CK(launch_minmax_kernel(a, 0, V, s));
       mark(P, "minmax", s, 1);
       CK(launch_thresholds(a, 0, V, s));
+      if (split_select) CK(cudaStreamWaitEvent(s, P->ev_child, 0));   // split list + n_split
       CK(launch_fallback_count(P->split_list.as<int>(), P->dom_flag.as<unsigned char>(), ctr, P->sm_count, s));
       mark(P, "thresholds", s, 2);
     }

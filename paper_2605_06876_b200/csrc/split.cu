@@ -15,16 +15,27 @@
 namespace adps {
 
 // ============================================================== select
+__device__ __forceinline__ unsigned char select_class(const SelectArgs& a, long long i) {
+  const double den = a.den[i];
+  const double g = den > 0 ? ddiv(a.ga[i], den) : 0.0;
+  const double s0 = a.scale[3 * i], s1 = a.scale[3 * i + 1], s2 = a.scale[3 * i + 2];
+  const double ms = fmax(fmax(s0, s1), s2);
+  unsigned char c = 0;
+  if (g >= a.tau_g) c = ms > a.tau_s_abs ? 1 : 2;
+  return c;
+}
+
+template <bool CLASSIFY>
 struct SelectPolicy {
   SelectArgs a;
   __device__ unsigned long long value(long long i) const {
-    double den = a.den[i];
-    double g = den > 0 ? ddiv(a.ga[i], den) : 0.0;
-    double s0 = a.scale[3 * i], s1 = a.scale[3 * i + 1], s2 = a.scale[3 * i + 2];
-    double ms = fmax(fmax(s0, s1), s2);
-    unsigned char c = 0;
-    if (g >= a.tau_g) c = ms > a.tau_s_abs ? 1 : 2;
-    a.cls[i] = c;
+    unsigned char c;
+    if (CLASSIFY) {
+      c = select_class(a, i);
+      a.cls[i] = c;
+    } else {
+      c = a.cls[i];   // written by classify_select_kernel
+    }
     return c == 1 ? 1ull : (c == 2 ? (1ull << 32) : 0ull);
   }
   __device__ void store(long long i, unsigned long long ex, unsigned long long v) const {
@@ -44,8 +55,25 @@ struct SelectPolicy {
 };
 
 cudaError_t launch_select(const SelectArgs& a, ScanState st, cudaStream_t s) {
-  SelectPolicy p{a};
-  return launch_scan(p, a.n, st, s);
+  return launch_scan(SelectPolicy<true>{a}, a.n, st, s);
+}
+
+// the classes alone (elementwise, HBM-bound): the input pass needs only them
+__global__ void classify_select_kernel(SelectArgs a) {
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < a.n; i += (long long)gridDim.x * blockDim.x)
+    a.cls[i] = select_class(a, i);
+}
+
+cudaError_t launch_select_split(const SelectArgs& a, ScanState st, cudaStream_t s, cudaStream_t aux, cudaEvent_t fork,
+                                cudaEvent_t join) {
+  long long b = (a.n + 255) / 256;
+  classify_select_kernel<<<(unsigned)(b < 1 ? 1 : (b > 65535 ? 65535 : b)), 256, 0, s>>>(a);
+  cudaError_t e = cudaGetLastError();
+  if (e == cudaSuccess) e = cudaEventRecord(fork, s);
+  if (e == cudaSuccess) e = cudaStreamWaitEvent(aux, fork, 0);
+  if (e == cudaSuccess) e = launch_scan(SelectPolicy<false>{a}, a.n, st, aux);
+  if (e == cudaSuccess) e = cudaEventRecord(join, aux);
+  return e;
 }
 
 // ====================================================== region stats + child

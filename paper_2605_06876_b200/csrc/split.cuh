@@ -29,6 +29,10 @@ struct SelectArgs {
   Counters* ctr;
 };
 cudaError_t launch_select(const SelectArgs& a, ScanState st, cudaStream_t s);
+// classes on `s`, then the split/clone list scan on `aux` (recorded into `join`):
+// the input pass on `s` needs only the classes
+cudaError_t launch_select_split(const SelectArgs& a, ScanState st, cudaStream_t s, cudaStream_t aux, cudaEvent_t fork,
+                                cudaEvent_t join);
 
 // ---- region stats + child init (ref/error_partition.py:137-158, ref/child_init.py:44-140) ----
 struct ChildArgs {
