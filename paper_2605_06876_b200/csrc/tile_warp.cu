@@ -675,23 +675,26 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, ADPS_TW_MINBLOCKS)
   //      against the row above (N, NW, NE); lane ty keeps row ty's masks.
   unsigned my_cc = 0u, my_v0 = 0u, my_vm = 0u, my_vp = 0u;
   {
-    int kb_prev = -1;   // key|band of the row above (-1 when it is not keyed)
+    // key|band of the row above and of its left / right neighbours (-1 when
+    // that row is not keyed): the neighbours are this row's shuffles carried
+    // over, so a row costs two shuffles of kb instead of three
+    int kb_prev = -1, lkb_prev = -1, rkb_prev = -1;
     int last = -2;
     for (unsigned rows = keyed; rows; rows &= rows - 1u) {
       const int ty = __ffs(rows) - 1;
-      if (ty != last + 1) kb_prev = -1;
+      if (ty != last + 1) kb_prev = lkb_prev = rkb_prev = -1;
       last = ty;
       const unsigned kw = __shfl_sync(FULL, K, ty);
       const unsigned b0 = __shfl_sync(FULL, bw0, ty), b1 = __shfl_sync(FULL, bw1, ty);
       const int band = (int)((b0 >> lane) & 1u) | (int)(((b1 >> lane) & 1u) << 1);
       const bool kl = (kw >> lane) & 1u;
       const int kb = kl ? (S.u.d[ty][lane] << 2) | band : -1;   // ids < 2^29
-      const int lkb = __shfl_up_sync(FULL, kb, 1);
-      const int pm = __shfl_up_sync(FULL, kb_prev, 1), pp = __shfl_down_sync(FULL, kb_prev, 1);
-      const unsigned cc = __ballot_sync(FULL, kl && lane > 0 && lkb == kb);
+      const int lkb = __shfl_up_sync(FULL, kb, 1), rkb = __shfl_down_sync(FULL, kb, 1);
+      // lane 0's shfl_up / lane 31's shfl_down return their own value: masked below
+      const unsigned cc = __ballot_sync(FULL, kl && lkb == kb) & ~1u;
       const unsigned v0 = __ballot_sync(FULL, kl && kb_prev == kb);
-      const unsigned vm = __ballot_sync(FULL, kl && lane > 0 && pm == kb);
-      const unsigned vp = __ballot_sync(FULL, kl && lane < 31 && pp == kb);
+      const unsigned vm = __ballot_sync(FULL, kl && lkb_prev == kb) & ~1u;
+      const unsigned vp = __ballot_sync(FULL, kl && rkb_prev == kb) & 0x7fffffffu;
       if (lane == ty) {
         my_cc = cc;
         my_v0 = v0;
@@ -699,6 +702,8 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, ADPS_TW_MINBLOCKS)
         my_vp = vp;
       }
       kb_prev = kb;
+      lkb_prev = lkb;
+      rkb_prev = rkb;
     }
   }
   // ---- (b) lane = row from here on.  Runs: starts/ends of this row; run ids
