@@ -26,7 +26,7 @@
 extern "C" {
 #endif
 
-#define ADPS_ABI_VERSION 1
+#define ADPS_ABI_VERSION 2
 
 #if defined(__GNUC__)
 #define ADPS_API __attribute__((visibility("default")))
@@ -147,6 +147,17 @@ ADPS_API adps_status adps_render(adps_plan* plan, void* stream, const adps_gauss
                         const double* cams_host, int32_t n_views, const float* bg,
                         float* image, int32_t* dominant);
 
+/* adps_render plus workload statistics (the benchmark's synthetic
+ * DensifyStats and measured depth complexity, not part of the step):
+ * weight [n] fp32 (device, accumulated into -- zero it first) += the sum of
+ * the blending weights T*alpha of each Gaussian over all rendered pixels, and
+ * *contributions (host) = the number of (pixel, splat) pairs with
+ * alpha >= 1/255 over the views (mean depth complexity = contributions /
+ * (n_views*H*W)).  Runs without the early termination. */
+ADPS_API adps_status adps_render_stats(adps_plan* plan, void* stream, const adps_gaussians* g, int64_t n,
+                              const double* cams_host, int32_t n_views, const float* bg,
+                              float* image, int32_t* dominant, float* weight, uint64_t* contributions);
+
 /* Phase 1 of adpsplit_step (ref/adc.py:165-227): select, error maps,
  * partition, region statistics, ever-dominant, child initialisation,
  * cross-view merge and cap, per-candidate case, offsets.  Consumes the
@@ -174,12 +185,22 @@ ADPS_API adps_status adps_step_phase1_end(adps_plan* plan, void* stream, adps_co
 
 /* Phase 2 (ref/adc.py:198-244): emit children, parent copies, fallback
  * children, clones and survivors into caller-allocated arrays of
- * counts.n_out rows plus index_map (old index or -1).
+ * counts.n_out rows plus index_map (old index or -1, ref/adc.py:233-244).
  * fallback_normals: device, 6*n_fallback doubles drawn by the host from the
- * caller's numpy Generator in ascending fallback order (ref/adc.py:97). */
+ * caller's numpy Generator in ascending fallback order (ref/adc.py:97).
+ * Optional integer outputs (NULL to skip):
+ *   child_parent  [n_out - n_keep] int32: for every appended row (candidate
+ *                 inserts in ascending candidate order, then clones) the old
+ *                 index of the Gaussian it came from -- the candidate for its
+ *                 children, parent copy and fallback children, the source for
+ *                 a clone (the `inserted` list of ref/adc.py:184-231);
+ *   insert_offset [n_split] int64: output row of candidate k's first inserted
+ *                 Gaussian (= the criterion-6 cursor of
+ *                 ref tests/test_acceptance.py:238-256; a reset candidate's
+ *                 empty range starts there too). */
 ADPS_API adps_status adps_step_phase2(adps_plan* plan, void* stream, const adps_gaussians* g,
                              const double* fallback_normals, adps_gaussians_out* out,
-                             int64_t* index_map);
+                             int64_t* index_map, int32_t* child_parent, int64_t* insert_offset);
 
 ADPS_API adps_status adps_get_report(adps_plan* plan, adps_report* report);
 
@@ -324,6 +345,24 @@ ADPS_API adps_status adps_remap_rows(void* stream, const int64_t* index_map, int
  * viewspace_grad [n,2] fp32, visible [n] uint8. */
 ADPS_API adps_status adps_accumulate_stats(void* stream, double* grad_accum, double* denom,
                                   const float* viewspace_grad, const uint8_t* visible, int64_t n);
+/* Same with the reference's fp64 gradients (GradOutput.viewspace_grad is
+ * float64, ref/raster.py:49-58): bit-identical to numpy's norm + add. */
+ADPS_API adps_status adps_accumulate_stats_f64(void* stream, double* grad_accum, double* denom,
+                                      const double* viewspace_grad, const uint8_t* visible, int64_t n);
+
+/* Opacity prune (ref/harness.py:320-340, _prune): keep = opacity >= threshold,
+ * evaluated on the fp32 opacity (exact compare) or, when opacity is NULL, on
+ * the fp64 logit as 1/(1+exp(-x)) (ref/harness.py:217-218).  Writes
+ * index_map[new] = old for the n_keep survivors in old order (device, n
+ * entries reserved) and synchronises once for *n_keep (host).  *n_near
+ * (host, may be NULL) counts logits whose sigmoid lies within 4 ulp of the
+ * threshold, where the device exp and the host libm may decide differently.
+ * The reference keeps everything when n_keep is 0 or n (the caller checks);
+ * the survivors' rows (parameters, optimizer moments, DensifyStats) are then
+ * gathered with adps_remap_rows. */
+ADPS_API adps_status adps_prune_index(adps_plan* plan, void* stream, const float* opacity, const double* logit_op,
+                                      int64_t n, double threshold, int64_t* index_map, int64_t* n_keep,
+                                      int64_t* n_near);
 
 #ifdef __cplusplus
 }

@@ -57,6 +57,8 @@ class Report(C.Structure):
                 ("regions_per_view", vp), ("clone_index", vp), ("n_views", C.c_int32)]
 
 
+ABI_VERSION = 2
+
 EXPORTS = (
     "adps_abi_version", "adps_last_error", "adps_plan_create", "adps_plan_destroy", "adps_render",
     "adps_step_phase1", "adps_step_phase1_begin", "adps_step_phase1_end", "adps_step_phase2", "adps_get_report", "adps_get_regions",
@@ -65,7 +67,7 @@ EXPORTS = (
     "adps_set_view_sharding", "adps_get_buffer", "adps_step_phase1_refresh", "adps_step_phase1_local",
     "adps_step_phase1_import", "adps_step_phase1_merge", "adps_vanilla_phase1", "adps_reset_flags",
     "adps_remap_rows", "adps_set_parent_sharding", "adps_get_shard", "adps_step_phase1_finish",
-    "adps_copy_report",
+    "adps_copy_report", "adps_accumulate_stats_f64", "adps_prune_index", "adps_render_stats",
 )
 
 _lib = None
@@ -86,11 +88,13 @@ def load(path: str = LIB_PATH):
     lib.adps_plan_create.argtypes = [C.POINTER(vp), C.c_int32, C.c_int64, C.c_int32, C.c_int32, C.c_int32]
     lib.adps_plan_destroy.argtypes = [vp]
     lib.adps_render.argtypes = [vp, vp, C.POINTER(Gaussians), C.c_int64, vp, C.c_int32, vp, vp, vp]
+    lib.adps_render_stats.argtypes = [vp, vp, C.POINTER(Gaussians), C.c_int64, vp, C.c_int32, vp, vp, vp, vp,
+                                      C.POINTER(C.c_uint64)]
     lib.adps_step_phase1.argtypes = [vp, vp, C.POINTER(Gaussians), C.c_int64, C.c_double, vp, vp,
                                      C.POINTER(Config), vp, C.c_int32, vp, vp, vp, C.POINTER(Counts)]
     lib.adps_step_phase1_begin.argtypes = lib.adps_step_phase1.argtypes
     lib.adps_step_phase1_end.argtypes = [vp, vp, C.POINTER(Counts)]
-    lib.adps_step_phase2.argtypes = [vp, vp, C.POINTER(Gaussians), vp, C.POINTER(GaussiansOut), vp]
+    lib.adps_step_phase2.argtypes = [vp, vp, C.POINTER(Gaussians), vp, C.POINTER(GaussiansOut), vp, vp, vp]
     lib.adps_get_report.argtypes = [vp, C.POINTER(Report)]
     lib.adps_copy_report.argtypes = [vp, vp, vp, C.c_int64, C.c_int64]
     lib.adps_get_regions.argtypes = [vp] + [C.POINTER(vp)] * 5 + [C.POINTER(C.c_int64)]
@@ -100,6 +104,9 @@ def load(path: str = LIB_PATH):
     lib.adps_get_timing.argtypes = [vp, C.POINTER(C.c_double), C.c_int32, C.POINTER(C.c_int32),
                                     C.POINTER(C.c_char_p)]
     lib.adps_accumulate_stats.argtypes = [vp, vp, vp, vp, vp, C.c_int64]
+    lib.adps_accumulate_stats_f64.argtypes = [vp, vp, vp, vp, vp, C.c_int64]
+    lib.adps_prune_index.argtypes = [vp, vp, vp, vp, C.c_int64, C.c_double, vp, C.POINTER(C.c_int64),
+                                     C.POINTER(C.c_int64)]
     lib.adps_get_launch_count.argtypes = [vp, C.POINTER(C.c_int64), C.POINTER(C.c_int64)]
     lib.adps_set_param.argtypes = [vp, C.c_int32, C.c_int64]
     lib.adps_get_param.argtypes = [vp, C.c_int32, C.POINTER(C.c_int64)]
@@ -122,7 +129,7 @@ def load(path: str = LIB_PATH):
         fn = getattr(lib, name)
         if name not in ("adps_abi_version", "adps_last_error"):
             fn.restype = st
-    if lib.adps_abi_version() != 1:
+    if lib.adps_abi_version() != ABI_VERSION:
         raise ImportError("libadps.so ABI version mismatch")
     _lib = lib
     return lib

@@ -313,13 +313,28 @@ extern "C" adps_status adps_plan_destroy(adps_plan* P) {
   return ADPS_OK;
 }
 
+constexpr long long kMaxGaussians = 1ll << 29;
+
+// forget a deferred normals request (and join a running one) that no phase 1
+// will consume: a stale request would later write through a dangling pointer
+static void drop_pending_normals(adps_plan* P) {
+  P->norm_deferred = false;
+  if (P->norm_pending) {
+    cudaEventSynchronize(P->ev_norm);
+    P->norm_pending = false;
+  }
+}
+
+
 static adps_status check_gaussians(const adps_gaussians* g, int64_t n) {
   if (!g) return fail(ADPS_INVALID_ARG, "gaussians is NULL");
   if (n > 0 && (!g->mu || !g->scale || !g->rot || !g->opacity || !g->sh_dc))
     return fail(ADPS_INVALID_ARG, "gaussian arrays must be non-NULL");
   if (g->sh_rest_k < 0 || g->sh_rest_k > 15) return fail(ADPS_INVALID_ARG, "sh_rest_k must be in [0,15]");
   if (g->sh_rest_k > 0 && !g->sh_rest) return fail(ADPS_INVALID_ARG, "sh_rest is NULL with sh_rest_k > 0");
-  if (n > 0x7ffffff0LL) return fail(ADPS_INVALID_ARG, "n=%lld exceeds int32 indexing", (long long)n);
+  // the tile CCL keys pixels by (candidate << 2 | band) in 32 bits and the survivor copy
+  // indexes components in 32 bits: both hold for n < 2^29
+  if (n >= kMaxGaussians) return fail(ADPS_INVALID_ARG, "n=%lld exceeds the supported 2^29 Gaussians", (long long)n);
   return ADPS_OK;
 }
 
@@ -336,9 +351,37 @@ static GaussiansIn to_in(const adps_gaussians* g) {
 }
 
 // ------------------------------------------------------------------ render
+static adps_status render_impl(adps_plan* P, void* stream_v, const adps_gaussians* g, int64_t n,
+                               const double* cams_host, int32_t n_views, const float* bg, float* image,
+                               int32_t* dominant, float* weight, unsigned long long* contrib_dev);
+
 extern "C" adps_status adps_render(adps_plan* P, void* stream_v, const adps_gaussians* g, int64_t n,
                                    const double* cams_host, int32_t n_views, const float* bg, float* image,
                                    int32_t* dominant) {
+  return render_impl(P, stream_v, g, n, cams_host, n_views, bg, image, dominant, nullptr, nullptr);
+}
+
+extern "C" adps_status adps_render_stats(adps_plan* P, void* stream_v, const adps_gaussians* g, int64_t n,
+                                         const double* cams_host, int32_t n_views, const float* bg, float* image,
+                                         int32_t* dominant, float* weight, uint64_t* contributions) {
+  if (!P) return fail(ADPS_INVALID_ARG, "plan is NULL");
+  if (n > 0 && !weight) return fail(ADPS_INVALID_ARG, "weight is NULL");
+  CK(cudaSetDevice(P->device));
+  cudaStream_t s = (cudaStream_t)stream_v;
+  CK(ensure(P->r_total, 2 * sizeof(unsigned long long)));
+  unsigned long long* cdev = P->r_total.as<unsigned long long>() + 1;
+  CK(cudaMemsetAsync(cdev, 0, sizeof(unsigned long long), s));
+  adps_status st = render_impl(P, stream_v, g, n, cams_host, n_views, bg, image, dominant, weight, cdev);
+  if (st != ADPS_OK) return st;
+  CK(cudaMemcpyAsync(P->r_total_host, cdev, sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  if (contributions) *contributions = (uint64_t)*P->r_total_host;
+  return ADPS_OK;
+}
+
+static adps_status render_impl(adps_plan* P, void* stream_v, const adps_gaussians* g, int64_t n,
+                               const double* cams_host, int32_t n_views, const float* bg, float* image,
+                               int32_t* dominant, float* weight, unsigned long long* contrib_dev) {
   if (!P) return fail(ADPS_INVALID_ARG, "plan is NULL");
   adps_status st = check_gaussians(g, n);
   if (st != ADPS_OK) return st;
@@ -380,7 +423,7 @@ extern "C" adps_status adps_render(adps_plan* P, void* stream_v, const adps_gaus
   CK(ensure(P->r_offs, sizeof(unsigned) * n));
   CK(ensure(P->r_tstart, sizeof(int) * n_tiles));
   CK(ensure(P->r_tend, sizeof(int) * n_tiles));
-  CK(ensure(P->r_total, sizeof(unsigned long long)));
+  CK(ensure(P->r_total, 2 * sizeof(unsigned long long)));
   ScanState sst;
   st = scan_state(P, P->scan_val, P->scan_flag, P->scan_ticket, n, &sst);
   if (st != ADPS_OK) return st;
@@ -455,6 +498,8 @@ extern "C" adps_status adps_render(adps_plan* P, void* stream_v, const adps_gaus
     for (int c = 0; c < 3; ++c) ba.bg[c] = bgv[c];
     ba.image = image + (long long)v * hw * 3;
     ba.dominant = dominant + (long long)v * hw;
+    ba.weight = weight;
+    ba.contrib = contrib_dev;
     CK(launch_blend(ba, n_tiles, s));
     P->launches += n_dup > 0 ? 5 : 3;
     P->lib_calls += n_dup > 0 ? 2 : 1;
@@ -542,6 +587,7 @@ extern "C" adps_status adps_step_phase1_begin(adps_plan* P, void* stream_v, cons
   if (!P) return fail(ADPS_INVALID_ARG, "plan is NULL");
   P->have_phase1 = false;
   P->have_begin = false;
+  drop_pending_normals(P);
   adps_status st = check_gaussians(g, n);
   if (st != ADPS_OK) return st;
   if (!cfg || !counts) return fail(ADPS_INVALID_ARG, "cfg/counts is NULL");
@@ -1174,8 +1220,9 @@ extern "C" adps_status adps_step_phase1_end(adps_plan* P, void* stream_v, adps_c
   cudaStream_t s = (cudaStream_t)stream_v;
   long long nr = 0;
   adps_status st = phase1_local(P, s, &nr, /*defer_child=*/true);
-  if (st != ADPS_OK) return st;
-  return phase1_merge(P, s, counts);
+  if (st == ADPS_OK) st = phase1_merge(P, s, counts);
+  if (st != ADPS_OK) drop_pending_normals(P);
+  return st;
 }
 
 extern "C" adps_status adps_step_phase1_local(adps_plan* P, void* stream_v, int64_t* n_regions) {
@@ -1184,7 +1231,10 @@ extern "C" adps_status adps_step_phase1_local(adps_plan* P, void* stream_v, int6
   P->have_begin = false;
   long long nr = 0;
   adps_status st = phase1_local(P, (cudaStream_t)stream_v, &nr);
-  if (st != ADPS_OK) return st;
+  if (st != ADPS_OK) {
+    drop_pending_normals(P);
+    return st;
+  }
   *n_regions = nr;
   P->have_local = true;
   return ADPS_OK;
@@ -1297,7 +1347,7 @@ extern "C" adps_status adps_step_phase1_finish(adps_plan* P, void* stream_v, int
 
 extern "C" adps_status adps_step_phase2(adps_plan* P, void* stream_v, const adps_gaussians* g,
                                         const double* fallback_normals, adps_gaussians_out* out,
-                                        int64_t* index_map) {
+                                        int64_t* index_map, int32_t* child_parent, int64_t* insert_offset) {
   if (!P) return fail(ADPS_INVALID_ARG, "plan is NULL");
   if (!P->have_phase1) return fail(ADPS_BAD_STATE, "phase 2 without a successful phase 1");
   adps_status st = check_gaussians(g, P->n);
@@ -1338,6 +1388,8 @@ extern "C" adps_status adps_step_phase2(adps_plan* P, void* stream_v, const adps
   ea.sh_dc = out->sh_dc;
   ea.sh_rest = out->sh_rest;
   ea.index_map = (long long*)index_map;
+  ea.child_parent = child_parent;
+  ea.insert_offset = (long long*)insert_offset;
   CK(launch_emit(ea, s, P->timing ? nullptr : P->aux, P->ev_fork, P->ev_small));
   mark(P, "emit", s, (P->n > 0 ? 1 : 0) + ((P->counts.n_split + P->counts.n_clone) > 0 ? 1 : 0));
   return ADPS_OK;
@@ -1558,6 +1610,8 @@ extern "C" adps_status adps_normals_pcg64(adps_plan* P, void* stream_v, const ui
   if (n < 0) return fail(ADPS_INVALID_ARG, "negative n");
   if (n > 0 && !out) return fail(ADPS_INVALID_ARG, "out is NULL");
   if (n > (1ll << 30)) return fail(ADPS_INVALID_ARG, "n too large");
+  // sync == 2 is consumed by the pending phase 1 (between _begin and _end/_local)
+  if (sync == 2 && !P->have_begin) return fail(ADPS_BAD_STATE, "deferred normals (sync=2) need a pending phase1_begin");
   CK(cudaSetDevice(P->device));
   cudaStream_t s = (cudaStream_t)stream_v;
   CK(ensure(P->ctr, sizeof(Counters)));
@@ -1625,6 +1679,7 @@ extern "C" adps_status adps_vanilla_phase1(adps_plan* P, void* stream_v, const a
   if (!P) return fail(ADPS_INVALID_ARG, "plan is NULL");
   P->have_phase1 = false;
   P->have_begin = false;
+  drop_pending_normals(P);
   adps_status st = check_gaussians(g, n);
   if (st != ADPS_OK) return st;
   if (!cfg || !counts) return fail(ADPS_INVALID_ARG, "cfg/counts is NULL");
@@ -1734,5 +1789,49 @@ extern "C" adps_status adps_accumulate_stats(void* stream, double* grad_accum, d
   if (n < 0) return fail(ADPS_INVALID_ARG, "negative n");
   if (n > 0 && (!grad_accum || !denom || !viewspace_grad || !visible)) return fail(ADPS_INVALID_ARG, "NULL array");
   CK(launch_accumulate(grad_accum, denom, viewspace_grad, visible, n, (cudaStream_t)stream));
+  return ADPS_OK;
+}
+
+extern "C" adps_status adps_accumulate_stats_f64(void* stream, double* grad_accum, double* denom,
+                                                 const double* viewspace_grad, const uint8_t* visible, int64_t n) {
+  if (n < 0) return fail(ADPS_INVALID_ARG, "negative n");
+  if (n > 0 && (!grad_accum || !denom || !viewspace_grad || !visible)) return fail(ADPS_INVALID_ARG, "NULL array");
+  CK(launch_accumulate_f64(grad_accum, denom, viewspace_grad, visible, n, (cudaStream_t)stream));
+  return ADPS_OK;
+}
+
+extern "C" adps_status adps_prune_index(adps_plan* P, void* stream_v, const float* opacity, const double* logit_op,
+                                        int64_t n, double threshold, int64_t* index_map, int64_t* n_keep,
+                                        int64_t* n_near) {
+  if (!P || !n_keep) return fail(ADPS_INVALID_ARG, "NULL argument");
+  if (n < 0) return fail(ADPS_INVALID_ARG, "negative n");
+  if (n >= kMaxGaussians) return fail(ADPS_INVALID_ARG, "n=%lld exceeds the supported 2^29 Gaussians", (long long)n);
+  if (n > 0 && ((!opacity && !logit_op) || !index_map)) return fail(ADPS_INVALID_ARG, "NULL array");
+  if (!(threshold == threshold)) return fail(ADPS_INVALID_ARG, "threshold is NaN");
+  CK(cudaSetDevice(P->device));
+  cudaStream_t s = (cudaStream_t)stream_v;
+  CK(ensure(P->ctr, sizeof(Counters)));
+  Counters* ctr = P->ctr.as<Counters>();
+  CK(cudaMemsetAsync(&ctr->prune_keep, 0, 2 * sizeof(unsigned long long), s));
+  if (n > 0) {
+    ScanState sst;
+    adps_status st = scan_state(P, P->scan2_val, P->scan2_flag, P->scan2_ticket, n, &sst);
+    if (st != ADPS_OK) return st;
+    PruneArgs pa;
+    pa.opacity = opacity;
+    pa.logit = opacity ? nullptr : logit_op;
+    pa.n = n;
+    pa.threshold = threshold;
+    pa.index_map = (long long*)index_map;
+    pa.n_keep = &ctr->prune_keep;
+    pa.n_near = &ctr->prune_near;
+    CK(launch_prune(pa, sst, s));
+    P->launches += 1;
+  }
+  CK(cudaMemcpyAsync(&P->ctr_host->prune_keep, &ctr->prune_keep, 2 * sizeof(unsigned long long),
+                     cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  *n_keep = (int64_t)P->ctr_host->prune_keep;
+  if (n_near) *n_near = (int64_t)P->ctr_host->prune_near;
   return ADPS_OK;
 }

@@ -173,12 +173,15 @@ __global__ void tile_ranges_kernel(const unsigned long long* keys, long long n, 
   if (i == n - 1 || (int)(keys[i + 1] >> 32) != t) end[t] = (int)(i + 1);
 }
 
+template <bool STATS>
 __global__ void __launch_bounds__(kRThreads) blend_kernel(BlendArgs a) {
   struct Sm {
     float mx, my, A, B, C, o, r, g, b;
     int idx;
   };
   __shared__ Sm sm[kRThreads];
+  __shared__ float wacc[STATS ? kRThreads : 1];
+  unsigned long long n_contrib = 0;
   const int tile = blockIdx.x;
   const int tyi = tile / a.tiles_x, txi = tile % a.tiles_x;
   const int lx = threadIdx.x % kRTile, ly = threadIdx.x / kRTile;
@@ -193,6 +196,7 @@ __global__ void __launch_bounds__(kRThreads) blend_kernel(BlendArgs a) {
   for (int base = beg; base < end; base += kRThreads) {
     if (__syncthreads_count(done) == kRThreads) break;
     const int j = base + threadIdx.x;
+    if (STATS) wacc[threadIdx.x] = 0.0f;
     if (j < end) {
       const int s = (int)(a.keys[j] & 0xffffffffull);
       const int g = a.order[s];
@@ -219,6 +223,10 @@ __global__ void __launch_bounds__(kRThreads) blend_kernel(BlendArgs a) {
       const float alpha = fminf(kAlphaCap, e.o * __expf(power));
       if (alpha < kAlphaMin) continue;
       const float w = T * alpha;
+      if (STATS) {
+        if (a.weight) atomicAdd(&wacc[k], w);
+        ++n_contrib;
+      }
       cr += w * e.r;
       cg += w * e.g;
       cbl += w * e.b;
@@ -227,9 +235,15 @@ __global__ void __launch_bounds__(kRThreads) blend_kernel(BlendArgs a) {
         bi = e.idx;
       }
       T = T * (1.0f - alpha);
-      if (T < 1e-8f && T * kAlphaCap <= best) done = true;
+      if (!STATS && T < 1e-8f && T * kAlphaCap <= best) done = true;
     }
     __syncthreads();
+    if (STATS && a.weight && threadIdx.x < cnt && wacc[threadIdx.x] > 0.0f)
+      atomicAdd(a.weight + sm[threadIdx.x].idx, wacc[threadIdx.x]);
+  }
+  if (STATS && a.contrib) {
+    for (int o = 16; o > 0; o >>= 1) n_contrib += __shfl_xor_sync(0xffffffffu, n_contrib, o);
+    if ((threadIdx.x & 31) == 0 && n_contrib) atomicAdd(a.contrib, n_contrib);
   }
   if (inside) {
     const long long p = (long long)y * a.W + x;
@@ -264,7 +278,10 @@ cudaError_t launch_tile_ranges(const unsigned long long* keys, long long n, int*
 }
 
 cudaError_t launch_blend(const BlendArgs& a, int n_tiles, cudaStream_t s) {
-  blend_kernel<<<n_tiles, kRThreads, 0, s>>>(a);
+  if (a.weight || a.contrib)
+    blend_kernel<true><<<n_tiles, kRThreads, 0, s>>>(a);
+  else
+    blend_kernel<false><<<n_tiles, kRThreads, 0, s>>>(a);
   return cudaGetLastError();
 }
 

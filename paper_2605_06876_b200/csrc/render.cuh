@@ -51,6 +51,12 @@ struct BlendArgs {
   float bg[3];
   float* image;
   int* dominant;
+  // workload statistics (optional; the benchmark's synthetic DensifyStats and
+  // its measured depth complexity): per-Gaussian sum of the blending weights
+  // T*alpha over the rendered pixels, and the number of (pixel, splat) pairs
+  // with alpha >= 1/255.  Either set disables the early termination.
+  float* weight;
+  unsigned long long* contrib;
 };
 
 cudaError_t launch_preprocess(const PreArgs& a, cudaStream_t s);

@@ -407,6 +407,7 @@ __device__ __forceinline__ void emit_insert_row(const EmitArgs& a, long long k, 
     }
   }
   a.index_map[dst] = -1;
+  if (a.child_parent) a.child_parent[a.ins_off[k] + j] = (int)gi;
 }
 
 // survivors: one parameter array per blockIdx.y, thread per component, so
@@ -467,6 +468,7 @@ __global__ void __launch_bounds__(kEmitThreads) emit_kernel(EmitArgs a, long lon
     const long long k = blk * kEmitThreads + threadIdx.x;
     if (k >= a.n_split) return;
     const int c = a.cand_case[k];
+    if (a.insert_offset) a.insert_offset[k] = a.n_keep + a.ins_off[k];
     if (c == ADPS_CASE_RESET) return;
     const int rows = c == ADPS_CASE_FALLBACK ? a.fb_children : a.cand_merged[k] + 1;
     for (int j = 0; j < rows; ++j) emit_insert_row(a, k, j);
@@ -474,8 +476,10 @@ __global__ void __launch_bounds__(kEmitThreads) emit_kernel(EmitArgs a, long lon
     const long long j = (blk - b_ins) * kEmitThreads + threadIdx.x;
     if (j < a.n_clone) {
       const long long dst = a.n_keep + a.n_inserted + j;
-      copy_gaussian(a, a.clone_list[j], dst);
+      const int src = a.clone_list[j];
+      copy_gaussian(a, src, dst);
       a.index_map[dst] = -1;
+      if (a.child_parent) a.child_parent[a.n_inserted + j] = src;
     }
   }
 }
@@ -574,25 +578,76 @@ cudaError_t launch_remap_rows(const long long* index_map, long long n_out, const
 }
 
 // ============================================================ stats feed
-__global__ void accumulate_kernel(double* ga, double* den, const float* vg, const unsigned char* vis,
-                                  long long n) {
+// ref/adc.py:73-79: norms = np.linalg.norm(vg, axis=1) = sqrt(x*x + y*y) in the
+// gradient's precision (this file is compiled with -fmad=false, so the sum of
+// squares rounds exactly as numpy's does); grad_accum[vis] += norm, denom[vis] += 1.
+// HBM-bound: 41 B per Gaussian and view (vg 2 x fp64 or 8 B fp32, vis 1 B,
+// grad_accum/denom read + written 32 B).  Grid-stride, two Gaussians per thread
+// per iteration through 16-byte vector loads of the gradient pairs.
+template <class T>
+__global__ void __launch_bounds__(256) accumulate_kernel(double* __restrict__ ga, double* __restrict__ den,
+                                                         const T* __restrict__ vg,
+                                                         const unsigned char* __restrict__ vis, long long n) {
   for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
        i += (long long)gridDim.x * blockDim.x) {
-    if (!vis[i]) continue;
-    const double x = vg[2 * i], y = vg[2 * i + 1];
-    ga[i] += sqrt(x * x + y * y);
+    if (!__ldg(vis + i)) continue;
+    const T x = __ldg(vg + 2 * i), y = __ldg(vg + 2 * i + 1);
+    const T nrm = sqrt(x * x + y * y);
+    ga[i] += (double)nrm;
     den[i] += 1.0;
   }
 }
 
-cudaError_t launch_accumulate(double* ga, double* den, const float* vg, const unsigned char* vis,
-                              long long n, cudaStream_t s) {
+template <class T>
+static cudaError_t launch_accumulate_t(double* ga, double* den, const T* vg, const unsigned char* vis, long long n,
+                                       cudaStream_t s) {
   if (n > 0) {
     long long blocks = (n + 255) / 256;
-    if (blocks > 148 * 8) blocks = 148 * 8;
-    accumulate_kernel<<<(unsigned)blocks, 256, 0, s>>>(ga, den, vg, vis, n);
+    if (blocks > 148 * 16) blocks = 148 * 16;
+    accumulate_kernel<T><<<(unsigned)blocks, 256, 0, s>>>(ga, den, vg, vis, n);
   }
   return cudaGetLastError();
+}
+
+cudaError_t launch_accumulate(double* ga, double* den, const float* vg, const unsigned char* vis,
+                              long long n, cudaStream_t s) {
+  return launch_accumulate_t<float>(ga, den, vg, vis, n, s);
+}
+
+cudaError_t launch_accumulate_f64(double* ga, double* den, const double* vg, const unsigned char* vis,
+                                  long long n, cudaStream_t s) {
+  return launch_accumulate_t<double>(ga, den, vg, vis, n, s);
+}
+
+// ============================================================ opacity prune
+// ref/harness.py:320-340 (_prune): keep = sigmoid(logit_op) >= threshold, the
+// survivors compacted in old order.  The keep test runs on the trainer's
+// representation: the stored opacity (fp32, compared exactly in fp64), or the
+// fp64 logit through 1/(1+exp(-x)) (ref/harness.py:217-218) -- CUDA's exp and
+// the host libm's may differ by an ulp, so logits whose sigmoid lies within
+// 4 ulp of the threshold are counted as near-threshold (reported separately).
+struct PruneScanPolicy {
+  PruneArgs a;
+  __device__ bool keep(long long i) const {
+    if (a.opacity) return (double)__ldg(a.opacity + i) >= a.threshold;
+    const double x = __ldg(a.logit + i);
+    const double sg = 1.0 / (1.0 + exp(-x));
+    if (fabs(sg - a.threshold) <= 4.0 * ulp_of(a.threshold)) atomicAdd(a.n_near, 1ull);
+    return sg >= a.threshold;
+  }
+  __device__ static double ulp_of(double v) {
+    const double av = fabs(v);
+    return __longlong_as_double(__double_as_longlong(av) + 1) - av;
+  }
+  __device__ unsigned long long value(long long i) const { return keep(i) ? 1ull : 0ull; }
+  __device__ void store(long long i, unsigned long long ex, unsigned long long v) const {
+    if (v) a.index_map[ex] = i;
+  }
+  __device__ void total(unsigned long long t) const { *a.n_keep = t; }
+};
+
+cudaError_t launch_prune(const PruneArgs& a, ScanState st, cudaStream_t s) {
+  return launch_scan(PruneScanPolicy{a}, a.n, st, s);
 }
 
 }  // namespace adps

@@ -123,12 +123,28 @@ struct EmitArgs {
   float* sh_dc;
   float* sh_rest;
   long long* index_map;
+  int* child_parent;        // [n_out - n_keep] old index each appended row came from, or null
+  long long* insert_offset; // [n_split] output row of candidate k's first insert, or null
 };
 cudaError_t launch_emit(const EmitArgs& a, cudaStream_t s, cudaStream_t aux = nullptr, cudaEvent_t fork = nullptr,
                         cudaEvent_t join = nullptr);
 
 cudaError_t launch_accumulate(double* ga, double* den, const float* vg, const unsigned char* vis,
                               long long n, cudaStream_t s);
+cudaError_t launch_accumulate_f64(double* ga, double* den, const double* vg, const unsigned char* vis,
+                                  long long n, cudaStream_t s);
+
+// opacity prune (ref/harness.py:320-340): index_map[new] = old for the kept Gaussians
+struct PruneArgs {
+  const float* opacity;      // [n] fp32 opacity, or null (then logit is used)
+  const double* logit;       // [n] fp64 logit_op
+  long long n;
+  double threshold;
+  long long* index_map;      // [n] (first n_keep entries written)
+  unsigned long long* n_keep;
+  unsigned long long* n_near;
+};
+cudaError_t launch_prune(const PruneArgs& a, ScanState st, cudaStream_t s);
 
 // vanilla_densify (ref/adc.py:248-280): every split candidate is split into n children
 cudaError_t launch_vanilla_cases(int* cand_case, int* cand_ins, int* cand_merged, const unsigned long long* n_split,

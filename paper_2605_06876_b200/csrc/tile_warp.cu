@@ -56,7 +56,7 @@ struct WarpSmem {
 size_t tile_warp_smem_bytes() { return sizeof(WarpSmem) * kWarpsPerBlock; }
 
 // per-tile scan state carried from row to row (registers)
-struct ScanState {
+struct TileRowState {
   unsigned long long m1, m2;   // metric masks of ext rows ey-1, ey-2
   int c_del, band_del;         // candidate/band of the tile row awaiting its erosion window
   int prev_key, prev_band, prev_rid;
@@ -159,7 +159,7 @@ __device__ __forceinline__ double row_raw(const RowIn<RAW>& r) {
 // unions with the runs of the row above (held in st.prev_*); K = keyed lanes.
 // Returns true when the tile has too many runs for the warp path.
 __device__ __forceinline__ bool runs_row(const int key, const int band, const unsigned K, const int ty,
-                                         ScanState& st, WarpSmem& S, const int lane) {
+                                         TileRowState& st, WarpSmem& S, const int lane) {
   constexpr unsigned FULL = 0xffffffffu;
 #if ADPS_TW_FAST
   if (K == 0) {   // no keyed pixel in this row: no runs, nothing to unite
@@ -215,7 +215,7 @@ __device__ __forceinline__ bool runs_row(const int key, const int band, const un
 }
 
 template <int R, bool RAW>
-__device__ __forceinline__ bool scan_row(const RowIn<RAW>& row, const int ey, ScanState& st, WarpSmem& S,
+__device__ __forceinline__ bool scan_row(const RowIn<RAW>& row, const int ey, TileRowState& st, WarpSmem& S,
                                          const TileConst& T, const int lane) {
   const bool inb = row.inb;
   const int c_now = (row.cb >> row.sh) & 1u ? row.d : -1;
@@ -266,7 +266,7 @@ __device__ __forceinline__ bool scan_row(const RowIn<RAW>& row, const int ey, Sc
 // components >= m_min become regions, edge components fragments + border labels
 __device__ __forceinline__ void finish_tile(const TileParams& P, WarpSmem& S, const int* __restrict__ dom_v,
                                             const long long tile, const int v, const int x0, const int y0,
-                                            const ScanState& st, const int lane) {
+                                            const TileRowState& st, const int lane) {
   constexpr unsigned FULL = 0xffffffffu;
   const int W = P.W, H = P.H;
   const int n_runs = st.n_runs;
@@ -425,7 +425,7 @@ __device__ __forceinline__ void tile_warp_body(const TileParams& P, WarpSmem& S,
     }
   }
 
-  ScanState st;
+  TileRowState st;
   st.m1 = st.m2 = 0;
   st.c_del = -1;
   st.band_del = 0;
@@ -754,7 +754,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, ADPS_TW_MINBLOCKS)
     }
   }
   // ---- (e) border run ids: rows 0 / 31 at column `lane`, columns 0 / 31 of row `lane`
-  ScanState st;
+  TileRowState st;
   st.n_runs = n_runs;
   {
     __syncwarp();

@@ -258,6 +258,24 @@ class Plan:
                                         cams.ctypes.data_as(C.c_void_p), v, bgv, _ptr(image), _ptr(dom)))
         return image, dom
 
+    def render_stats(self, g: GaussianTensors, cams: np.ndarray, bg=(0.0, 0.0, 0.0)):
+        """(image, dominant, weight [n] fp32, depth complexity): the render plus each
+        Gaussian's summed blending weight T*alpha and the mean number of splats with
+        alpha >= 1/255 per pixel (workload statistics for the benchmark)."""
+        cams = camera_rows(cams)
+        v = len(cams)
+        w, h = int(cams[0, 16]), int(cams[0, 17])
+        image = torch.empty(v, h, w, 3, dtype=F32, device=self.device)
+        dom = torch.empty(v, h, w, dtype=torch.int32, device=self.device)
+        weight = torch.zeros(max(g.n, 1), dtype=F32, device=self.device)
+        bgv = (C.c_float * 3)(*[float(x) for x in bg])
+        ga = g.abi()
+        contrib = C.c_uint64()
+        _abi.check(self.lib.adps_render_stats(self._h, self._stream(), C.byref(ga), g.n,
+                                              cams.ctypes.data_as(C.c_void_p), v, bgv, _ptr(image), _ptr(dom),
+                                              _ptr(weight), C.byref(contrib)))
+        return image, dom, weight[:g.n], contrib.value / float(v * h * w)
+
     # -- phase 1 / 2 (ref/adc.py:165-244)
     @staticmethod
     def _check_inputs(grad_accum, denom, image, gt, dom):
@@ -444,13 +462,35 @@ class Plan:
         _abi.check(self.lib.adps_reset_flags(self._h, self._stream(), _ptr(flags), int(bool(include_clones))))
         return flags[:n]
 
-    def phase2(self, g, normals, out: GaussianTensors, index_map: torch.Tensor):
+    def phase2(self, g, normals, out: GaussianTensors, index_map: torch.Tensor, child_parent: torch.Tensor = None,
+               insert_offset: torch.Tensor = None):
         ga = g.abi()
         oa = _abi.GaussiansOut(out.mu.data_ptr(), out.scale.data_ptr(), out.rot.data_ptr(),
                                out.opacity.data_ptr(), out.sh_dc.data_ptr(),
                                out.sh_rest.data_ptr() if out.sh_k else None, out.sh_k)
         _abi.check(self.lib.adps_step_phase2(self._h, self._stream(), C.byref(ga), _ptr(normals),
-                                             C.byref(oa), _ptr(index_map)))
+                                             C.byref(oa), _ptr(index_map),
+                                             _ptr(child_parent) if child_parent is not None and child_parent.numel()
+                                             else None,
+                                             _ptr(insert_offset) if insert_offset is not None and insert_offset.numel()
+                                             else None))
+
+    def prune_index(self, threshold: float, opacity: torch.Tensor = None, logit_op: torch.Tensor = None):
+        """(index_map [n_keep] int64, n_keep, n_near) of ref/harness.py:320-340's keep test."""
+        src = opacity if opacity is not None else logit_op
+        if src is None:
+            raise ValueError("need opacity (fp32) or logit_op (fp64)")
+        want = F32 if opacity is not None else F64
+        if src.dtype != want or not src.is_cuda or src.dim() != 1:
+            raise ValueError(f"{'opacity' if opacity is not None else 'logit_op'} must be a 1-D {want} CUDA tensor")
+        src = src.contiguous()
+        n = src.numel()
+        im = torch.empty(max(n, 1), dtype=torch.int64, device=self.device)
+        nk, nn = C.c_int64(), C.c_int64()
+        _abi.check(self.lib.adps_prune_index(self._h, self._stream(), _ptr(src) if opacity is not None else None,
+                                             _ptr(src) if opacity is None else None, n, float(threshold),
+                                             _ptr(im), C.byref(nk), C.byref(nn)))
+        return im[:nk.value], int(nk.value), int(nn.value)
 
     def report_arrays(self, n_split: int, n_clone: int) -> dict:
         r = _abi.Report()
@@ -561,6 +601,8 @@ class StepResult:
     view_ids: list
     report_arrays: dict = None
     normals: torch.Tensor = None   # the 6F fallback normals (device)
+    child_parent: torch.Tensor = None    # int32 [n_out - n_keep]: old index of every appended row
+    insert_offset: torch.Tensor = None   # int64 [n_split]: output row of candidate k's first insert
     stage_ms: dict = field(default_factory=dict)
 
     def report(self) -> SplitReport:
@@ -676,9 +718,11 @@ def densify_step(g: GaussianTensors, extent: float, cameras, gt, grad_accum: tor
     if out is None:
         out = GaussianTensors.empty(n_out, g.sh_k, dev)
     index_map = torch.empty(n_out, dtype=torch.int64, device=dev)
-    plan.phase2(g, normals, out, index_map)
+    child_parent = torch.empty(n_out - counts["n_keep"], dtype=torch.int32, device=dev)
+    insert_offset = torch.empty(counts["n_split"], dtype=torch.int64, device=dev)
+    plan.phase2(g, normals, out, index_map, child_parent, insert_offset)
     res = StepResult(gaussians=out, index_map=index_map, counts=counts, view_ids=list(view_ids),
-                     normals=normals)
+                     normals=normals, child_parent=child_parent, insert_offset=insert_offset)
     if want_report:
         res.report_arrays = plan.report_arrays(counts["n_split"], counts["n_clone"])
     if plan.timing:
@@ -706,8 +750,11 @@ def vanilla_densify_step(g: GaussianTensors, extent: float, grad_accum: torch.Te
         normals = torch.from_numpy(rng.standard_normal(count)).to(dev)
     out = GaussianTensors.empty(counts["n_out"], g.sh_k, dev)
     index_map = torch.empty(counts["n_out"], dtype=torch.int64, device=dev)
-    plan.phase2(g, normals, out, index_map)
-    res = StepResult(gaussians=out, index_map=index_map, counts=counts, view_ids=[], normals=normals)
+    child_parent = torch.empty(counts["n_out"] - counts["n_keep"], dtype=torch.int32, device=dev)
+    insert_offset = torch.empty(counts["n_split"], dtype=torch.int64, device=dev)
+    plan.phase2(g, normals, out, index_map, child_parent, insert_offset)
+    res = StepResult(gaussians=out, index_map=index_map, counts=counts, view_ids=[], normals=normals,
+                     child_parent=child_parent, insert_offset=insert_offset)
     if want_report:
         res.report_arrays = plan.report_arrays(counts["n_split"], counts["n_clone"])
     return res
@@ -743,17 +790,55 @@ def render_views(g: GaussianTensors, cameras, bg=(0.0, 0.0, 0.0), plan: Plan = N
 
 def accumulate_stats_(grad_accum: torch.Tensor, denom: torch.Tensor, viewspace_grad: torch.Tensor,
                       visible: torch.Tensor):
-    """In-place DensifyStats feed on device (ref/adc.py:73-79)."""
+    """In-place DensifyStats feed on device (ref/adc.py:73-79):
+    grad_accum[visible] += |viewspace_grad|_2, denom[visible] += 1.
+
+    viewspace_grad is the [N,2] d loss / d projected mean (GradOutput,
+    ref/raster.py:49-58) in fp64 (the reference's precision, bit-identical
+    norms) or fp32 (a GPU rasterizer's); visible is a [N] bool/uint8 mask.
+    grad_accum/denom are updated in place and must be contiguous fp64 CUDA
+    tensors on the gradient's device."""
     lib = _abi.load()
     if grad_accum.dtype != F64 or denom.dtype != F64:
         raise TypeError("stats must be float64")
-    if len(grad_accum) != len(visible):
+    n = len(grad_accum)
+    if len(denom) != n or len(visible) != n or len(viewspace_grad) != n:
         raise ValueError("stats dimensions do not match gradient output")
-    vg = viewspace_grad.to(F32).contiguous()
+    if viewspace_grad.dim() != 2 or viewspace_grad.shape[1] != 2:
+        raise ValueError(f"viewspace_grad must be [N,2], got {tuple(viewspace_grad.shape)}")
+    if viewspace_grad.dtype not in (F32, F64):
+        raise TypeError("viewspace_grad must be float32 or float64")
+    for name, t in (("grad_accum", grad_accum), ("denom", denom), ("viewspace_grad", viewspace_grad),
+                    ("visible", visible)):
+        if not t.is_cuda or t.device != grad_accum.device:
+            raise ValueError(f"{name} must be on {grad_accum.device}")
+    for name, t in (("grad_accum", grad_accum), ("denom", denom)):
+        if t.dim() != 1 or not t.is_contiguous():
+            raise ValueError(f"{name} must be a contiguous 1-D tensor (updated in place)")
+    vg = viewspace_grad.contiguous()
     vis = visible.to(torch.uint8).contiguous()
     stream = C.c_void_p(torch.cuda.current_stream(grad_accum.device).cuda_stream)
-    _abi.check(lib.adps_accumulate_stats(stream, _ptr(grad_accum), _ptr(denom), _ptr(vg), _ptr(vis),
-                                         len(grad_accum)))
+    fn = lib.adps_accumulate_stats_f64 if vg.dtype == F64 else lib.adps_accumulate_stats
+    _abi.check(fn(stream, _ptr(grad_accum), _ptr(denom), _ptr(vg), _ptr(vis), n))
+
+
+def prune(g: GaussianTensors, threshold: float, *, rows=(), logit_op: torch.Tensor = None, plan: Plan = None):
+    """Opacity prune on the device (ref/harness.py:320-340, ``_prune``).
+
+    keep = opacity >= threshold (the fp32 opacity, or sigmoid(logit_op) when
+    the trainer keeps fp64 logits, ref/harness.py:217-218); like the
+    reference, nothing is pruned when every or no Gaussian survives.  ``rows``
+    are per-Gaussian tensors carried over for the survivors (optimizer
+    moments, DensifyStats, logits), gathered by adps_remap_rows.
+    Returns (GaussianTensors, [rows...], index_map [n_keep] int64 or None, n_near)."""
+    plan = plan or default_plan(g.device)
+    im, nk, near = plan.prune_index(threshold, opacity=None if logit_op is not None else g.opacity,
+                                    logit_op=logit_op)
+    if nk == 0 or nk == g.n:
+        return g, list(rows), None, near
+    gather = [remap_rows(im, getattr(g, f)) for f in ("mu", "scale", "rot", "opacity", "sh_dc")]
+    rest = remap_rows(im, g.sh_rest) if g.sh_k else None
+    return GaussianTensors(*gather, rest), [remap_rows(im, r) for r in rows], im, near
 
 
 # ----------------------------------------------------------------------------

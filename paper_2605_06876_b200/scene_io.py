@@ -1,18 +1,12 @@
-"""Scene and camera files: the reference's v1 text format plus a binary v1
-format for large fixtures.
+"""Binary scene and camera files for large fixtures.
 
-Text (byte-compatible with the reference):
-  ``save_scene`` / ``load_scene``       ref/scene.py:283-337
-  ``save_cameras`` / ``load_cameras``   ref/scene.py:340-381
-  same headers, ``repr`` float formatting, record layout
-  ``mu scale rot opacity sh_dc sh_rest...`` and the same exceptions
-  (``SceneFormatError`` for malformed files, ``InvariantError`` with the line
-  number for records that violate a domain invariant).
-
-Binary (this repo's addition): the text format parses 1-8M Gaussians at a few
-MB/s; the binary files hold the same float64 values as little-endian
-structure-of-arrays blocks, so a load is one read per field and a scene goes
-to the device as ``GaussianTensors`` without a per-Gaussian Python object.
+The reference stores scenes and cameras as ``repr`` text (ref/scene.py:279-381),
+which parses 1-8M Gaussians at a few MB/s.  The binary v1 files hold the same
+float64 values as little-endian structure-of-arrays blocks, so a load is one
+read per field and a scene goes to the device as ``GaussianTensors`` without a
+per-Gaussian Python object.  The text format itself is not re-implemented here
+(SURVEY.md §2 marks it out of scope); tests/golden/make_io_golden.py converts
+files written and parsed by the reference into these binary fixtures.
 
   scene:   b"ADPSSCN1" | u64 N | u32 K | u32 0 | f64 extent |
            f64 mu[N,3] | scale[N,3] | rot[N,4] | opacity[N] | sh_dc[N,3] | sh_rest[N,K,3]
@@ -33,8 +27,6 @@ import numpy as np
 
 from .types import Camera, Gaussian3D, InvariantError, Scene
 
-SCENE_HEADER = "adpsplit-scene v1"      # ref/scene.py:35
-CAMERA_HEADER = "adpsplit-cameras v1"   # ref/scene.py:36
 SCENE_MAGIC = b"ADPSSCN1"
 CAMERA_MAGIC = b"ADPSCAM1"
 
@@ -62,7 +54,7 @@ class SceneArrays:
         return (self.mu, self.scale, self.rot, self.opacity, self.sh_dc, self.sh_rest)
 
 
-def check_invariants(a: SceneArrays, where: str = "", first_line: int | None = None) -> None:
+def check_invariants(a: SceneArrays, where: str = "") -> None:
     """The reference's per-Gaussian invariants (ref/scene.py:54-81, 131-144), vectorised;
     the first offending Gaussian is reported as the reference reports it."""
     if not a.extent > 0:
@@ -82,7 +74,7 @@ def check_invariants(a: SceneArrays, where: str = "", first_line: int | None = N
         msg = f"scale components must be > 0: {a.scale[i]}"
     else:
         msg = f"opacity must lie in (0,1): {a.opacity[i]}"
-    loc = f"{where}:{first_line + i}: " if first_line is not None else (f"{where}: " if where else "")
+    loc = f"{where}: " if where else ""
     raise InvariantError(f"{loc}Gaussian {i}: {msg}")
 
 
@@ -121,116 +113,9 @@ def scene_tensors(a: SceneArrays, device="cuda"):
                                       a.sh_rest if a.sh_rest.shape[1] else None, device=device), a.extent
 
 
-# ---------------------------------------------------------------- text v1
-def _fmt(values) -> str:
-    return " ".join(repr(float(v)) for v in values)
-
-
-def save_scene(scene, path) -> None:
-    """Write the v1 text format (ref/scene.py:283-289); accepts a Scene or SceneArrays."""
-    if isinstance(scene, SceneArrays):
-        a = scene
-        lines = [SCENE_HEADER, f"extent {float(a.extent)!r}"]
-        rec = np.concatenate([a.mu, a.scale, a.rot, a.opacity[:, None], a.sh_dc,
-                              a.sh_rest.reshape(len(a), -1)], axis=1)
-        lines += [_fmt(r) for r in rec]
-    else:
-        lines = [SCENE_HEADER, f"extent {scene.extent!r}"]
-        for g in scene.gaussians:
-            rest = [c for coeff in g.sh_rest for c in coeff]
-            lines.append(_fmt([*g.mu, *g.scale, *g.rot, g.opacity, *g.sh_dc, *rest]))
-    Path(path).write_text("\n".join(lines) + "\n")
-
-
-def _scene_records(path):
-    lines = Path(path).read_text().splitlines()
-    if not lines or lines[0].strip() != SCENE_HEADER:
-        raise SceneFormatError(f"{path}: missing '{SCENE_HEADER}' header")
-    if len(lines) < 2 or not lines[1].startswith("extent "):
-        raise SceneFormatError(f"{path}: line 2 must declare the scene extent")
-    try:
-        extent = float(lines[1].split()[1])
-    except (IndexError, ValueError) as exc:
-        raise SceneFormatError(f"{path}: bad extent line: {lines[1]!r}") from exc
-    recs, linenos = [], []
-    for lineno, line in enumerate(lines[2:], start=3):
-        if not line.strip():
-            continue
-        try:
-            vals = [float(t) for t in line.split()]
-        except ValueError as exc:
-            raise SceneFormatError(f"{path}:{lineno}: non-numeric token") from exc
-        if len(vals) < 14 or (len(vals) - 14) % 3 != 0:
-            raise SceneFormatError(f"{path}:{lineno}: record has {len(vals)} values, "
-                                   "expected 14 + 3k (truncated record?)")
-        recs.append(vals)
-        linenos.append(lineno)
-    if not recs:
-        raise SceneFormatError(f"{path}: scene contains no Gaussians")
-    return extent, recs, linenos
-
-
-def load_scene(path) -> Scene:
-    """Read a v1 text scene (ref/scene.py:292-337) into a reference-style Scene."""
-    extent, recs, linenos = _scene_records(path)
-    gaussians = []
-    for vals, lineno in zip(recs, linenos):
-        rest = tuple(np.array(vals[14 + 3 * i:17 + 3 * i]) for i in range((len(vals) - 14) // 3))
-        try:
-            gaussians.append(Gaussian3D(mu=vals[0:3], scale=vals[3:6], rot=vals[6:10], opacity=vals[10],
-                                        sh_dc=vals[11:14], sh_rest=rest))
-        except InvariantError as exc:
-            raise InvariantError(f"{path}:{lineno}: Gaussian {len(gaussians)}: {exc}") from exc
-    return Scene(gaussians=gaussians, extent=extent)
-
-
-def load_scene_arrays(path) -> SceneArrays:
-    """Read a v1 text scene straight into SoA arrays (uniform K), same checks."""
-    extent, recs, linenos = _scene_records(path)
-    widths = {len(r) for r in recs}
-    if len(widths) > 1:
-        raise SceneFormatError(f"{path}: ragged records {sorted(widths)}: the SoA layout needs one K")
-    m = np.asarray(recs, dtype=np.float64)
-    n, k = m.shape[0], (m.shape[1] - 14) // 3
-    a = SceneArrays(m[:, 0:3].copy(), m[:, 3:6].copy(), m[:, 6:10].copy(), m[:, 10].copy(),
-                    m[:, 11:14].copy(), m[:, 14:].reshape(n, k, 3).copy(), extent)
-    check_invariants(a, str(path), linenos[0])
-    return a
-
-
-def save_cameras(cameras, path) -> None:
-    """Write the v1 camera text format (ref/scene.py:340-349)."""
-    lines = [CAMERA_HEADER]
-    for c in cameras:
-        lines.append(_fmt([*c.r_c2w.ravel(), *c.center, c.f_x, c.f_y, c.p_x, c.p_y]) + f" {c.width} {c.height}")
-    Path(path).write_text("\n".join(lines) + "\n")
-
-
 def _camera(vals):
     return Camera(r_c2w=np.array(vals[0:9]).reshape(3, 3), center=vals[9:12], f_x=vals[12], f_y=vals[13],
                   p_x=vals[14], p_y=vals[15], width=int(vals[16]), height=int(vals[17]))
-
-
-def load_cameras(path) -> list:
-    """Read a v1 camera text file (ref/scene.py:352-381)."""
-    lines = Path(path).read_text().splitlines()
-    if not lines or lines[0].strip() != CAMERA_HEADER:
-        raise SceneFormatError(f"{path}: missing '{CAMERA_HEADER}' header")
-    cameras = []
-    for lineno, line in enumerate(lines[1:], start=2):
-        if not line.strip():
-            continue
-        try:
-            vals = [float(t) for t in line.split()]
-        except ValueError as exc:
-            raise SceneFormatError(f"{path}:{lineno}: non-numeric token") from exc
-        if len(vals) != 18:
-            raise SceneFormatError(f"{path}:{lineno}: camera record has {len(vals)} values, expected 18")
-        try:
-            cameras.append(_camera(vals))
-        except InvariantError as exc:
-            raise InvariantError(f"{path}:{lineno}: camera {len(cameras)}: {exc}") from exc
-    return cameras
 
 
 # ---------------------------------------------------------------- binary v1

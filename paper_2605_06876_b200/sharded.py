@@ -2,16 +2,19 @@
 
 SURVEY.md 8(e), following the path's own data dependencies:
 
-  Phase A (view-sharded).  Rank r owns the sampled-view positions r, r+g,
-  r+2g, ... (g = world size).  It runs select, the per-view error maps,
+  Phase A (view-sharded).  Rank r owns a contiguous block of the sampled-view
+  positions, [r*V/g, (r+1)*V/g) (g = world size), so its attribution inputs
+  (image, dominant, gt) are zero-copy slices of the [V,H,W,...] arrays.  It runs select, the per-view error maps,
   partition, region statistics and child initialisation for its views only
   (ref/adc.py:165-196) -- every per-view stage is independent across views.
   The ever-dominant flags (ref/adc.py:177-180, an OR over all sampled views)
   are combined with ONE all_reduce(MAX) of an N-byte vector, after which the
   global fallback count is known and the fallback normals can be drawn.
 
-  Exchange.  Region records (64 B, global view positions) and their proposals
-  (152 B) are all-gathered; each rank hands the concatenation to its plan.
+  Exchange.  Region records (64 B, global view positions), their proposals
+  (152 B) and valid flags are packed into one byte blob per rank and
+  all-gathered (one size all_gather + one padded data all_gather, one host
+  read of the sizes); each rank hands the concatenation to its plan.
   Records are merged in their (candidate, view, band, first pixel) key order,
   which is the reference's order (ref/adc.py:190-195), so the concatenation
   order is irrelevant and every rank sees identical inputs.
@@ -37,11 +40,17 @@ import torch.distributed as dist
 from . import operator as op
 
 
-def shard_views(n_views: int, world: int, rank: int) -> list:
-    """Positions (into the sorted sampled view ids) owned by `rank`: r, r+g, ..."""
+def view_block(n_views: int, world: int, rank: int) -> tuple:
+    """[lo, hi) of the sampled-view positions owned by `rank` (contiguous blocks)."""
     if world < 1 or not 0 <= rank < world:
         raise ValueError("bad world/rank")
-    return list(range(rank, n_views, world))
+    return rank * n_views // world, (rank + 1) * n_views // world
+
+
+def shard_views(n_views: int, world: int, rank: int) -> list:
+    """Positions (into the sorted sampled view ids) owned by `rank`: one contiguous block."""
+    lo, hi = view_block(n_views, world, rank)
+    return list(range(lo, hi))
 
 
 def shard_parents(p_counts, world: int, rank: int) -> tuple:
@@ -59,21 +68,60 @@ def shard_parents(p_counts, world: int, rank: int) -> tuple:
     return (lo, hi) if hi > lo else (0, 0)
 
 
+def _comm_device(t: torch.Tensor, group=None) -> torch.device:
+    """Where a collective on `t` runs: gloo takes host tensors, NCCL device tensors."""
+    return torch.device("cpu") if dist.get_backend(group) == "gloo" else t.device
+
+
+def all_reduce_max_(t: torch.Tensor, group=None) -> torch.Tensor:
+    cd = _comm_device(t, group)
+    if cd == t.device:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX, group=group)
+        return t
+    h = t.to(cd)
+    dist.all_reduce(h, op=dist.ReduceOp.MAX, group=group)
+    t.copy_(h)
+    return t
+
+
 def all_gather_bytes(t: torch.Tensor, group=None) -> list:
-    """all_gather of 1-D uint8 tensors of different lengths (padded to the max)."""
+    """all_gather of 1-D uint8 tensors of different lengths: one all_gather of the
+    sizes (one host read), one all_gather_into_tensor of the blobs padded to the
+    largest.  Returns the per-rank blobs on t's device."""
     world = dist.get_world_size(group)
-    n = torch.tensor([t.numel()], dtype=torch.int64, device=t.device)
-    sizes = [torch.zeros_like(n) for _ in range(world)]
-    dist.all_gather(sizes, n, group=group)
-    sizes = [int(x.item()) for x in sizes]
+    cd = _comm_device(t, group)
+    n = torch.tensor([t.numel()], dtype=torch.int64, device=cd)
+    sizes_t = torch.empty(world, dtype=torch.int64, device=cd)
+    dist.all_gather_into_tensor(sizes_t, n, group=group)
+    sizes = sizes_t.tolist()
     m = max(sizes) if sizes else 0
     if m == 0:
         return [t.new_empty(0) for _ in range(world)]
-    pad = torch.zeros(m, dtype=torch.uint8, device=t.device)
-    pad[:t.numel()] = t
-    outs = [torch.empty(m, dtype=torch.uint8, device=t.device) for _ in range(world)]
-    dist.all_gather(outs, pad, group=group)
-    return [o[:k] for o, k in zip(outs, sizes)]
+    pad = torch.zeros(m, dtype=torch.uint8, device=cd)
+    pad[:t.numel()] = t.to(cd)
+    out = torch.empty(world * m, dtype=torch.uint8, device=cd)
+    dist.all_gather_into_tensor(out, pad, group=group)
+    out = out.to(t.device)
+    return [out[r * m:r * m + k] for r, k in enumerate(sizes)]
+
+
+def _pack(parts: dict) -> torch.Tensor:
+    """{name: uint8 tensor} -> one blob: int64 lengths header, then the parts in key order."""
+    keys = sorted(parts)
+    dev = parts[keys[0]].device
+    head = torch.tensor([parts[k].numel() for k in keys], dtype=torch.int64).view(torch.uint8).to(dev)
+    return torch.cat([head] + [parts[k].reshape(-1) for k in keys])
+
+
+def _unpack(blob: torch.Tensor, keys) -> dict:
+    keys = sorted(keys)
+    h = 8 * len(keys)
+    lens = blob[:h].cpu().clone().view(torch.int64).tolist() if blob.numel() else [0] * len(keys)
+    out, off = {}, h
+    for k, ln in zip(keys, lens):
+        out[k] = blob[off:off + ln]
+        off += ln
+    return out
 
 
 def run_sharded(ex, n_views: int, group=None):
@@ -97,11 +145,13 @@ def run_sharded(ex, n_views: int, group=None):
         raise ValueError(f"{world} ranks but only {n_views} sampled views to shard")
     ex.begin(shard_views(n_views, world, rank))
     flags = ex.dom_flags()
-    dist.all_reduce(flags, op=dist.ReduceOp.MAX, group=group)
+    all_reduce_max_(flags, group)
     ex.set_dom_flags(flags)
     ex.start_normals(ex.refresh())
     recs = ex.local()
-    ex.import_({k: all_gather_bytes(v, group) for k, v in recs.items()})
+    blobs = all_gather_bytes(_pack(recs), group)
+    per_rank = [_unpack(b, recs.keys()) for b in blobs]
+    ex.import_({k: [p[k] for p in per_rank] for k in recs})
     ex.merge()
     if getattr(ex, "parent_sharded", False):
         ex.import_shards(all_gather_bytes(ex.export_shard(), group))
@@ -162,15 +212,17 @@ class GpuExecutor:
         self.positions = list(positions)
         vids = [self.view_ids[p] for p in self.positions]
         cams_v = self.cams[vids]
+        lo, hi = self.positions[0], self.positions[-1] + 1
+        if self.positions != list(range(lo, hi)):
+            raise ValueError("view shards must be contiguous blocks of sampled-view positions")
         if self.renders is None:
             image, dom = P.render(self.g, cams_v)
-        else:
-            idx = torch.as_tensor(self.positions, device=dev)
-            image = self.renders[0].to(dev, op.F32).index_select(0, idx).contiguous()
-            dom = self.renders[1].to(dev, torch.int32).index_select(0, idx).contiguous()
+        else:   # zero-copy slices of the [V,...] attribution of all sampled views
+            image = self.renders[0].to(dev, op.F32)[lo:hi].contiguous()
+            dom = self.renders[1].to(dev, torch.int32)[lo:hi].contiguous()
         gt_v = op._gather_views(self.gt, vids, dev)
         self._keep = (image, dom, gt_v)
-        P.set_view_sharding(self.rank, self.world, len(self.view_ids))
+        P.set_view_sharding(lo, 1, len(self.view_ids))
         P.set_parent_sharding(self.rank, self.world) if self.parent_sharded else P.set_parent_sharding(0, 1)
         self.counts = P.phase1_begin(self.g, self.extent, self.ga, self.den, self.cfg, cams_v, image, gt_v, dom)
         return self.counts
@@ -229,9 +281,11 @@ class GpuExecutor:
         counts, dev = self.counts, self.plan.device
         out = op.GaussianTensors.empty(counts["n_out"], self.g.sh_k, dev)
         index_map = torch.empty(counts["n_out"], dtype=torch.int64, device=dev)
-        self.plan.phase2(self.g, normals, out, index_map)
+        child_parent = torch.empty(counts["n_out"] - counts["n_keep"], dtype=torch.int32, device=dev)
+        insert_offset = torch.empty(counts["n_split"], dtype=torch.int64, device=dev)
+        self.plan.phase2(self.g, normals, out, index_map, child_parent, insert_offset)
         res = op.StepResult(gaussians=out, index_map=index_map, counts=counts, view_ids=list(self.view_ids),
-                            normals=normals)
+                            normals=normals, child_parent=child_parent, insert_offset=insert_offset)
         if self.want_report:
             res.report_arrays = self.plan.report_arrays(counts["n_split"], counts["n_clone"])
         return res
@@ -256,4 +310,4 @@ def densify_step_sharded(g: op.GaussianTensors, extent: float, cameras, gt, grad
     return run_sharded(ex, len(ex.view_ids), group)
 
 
-__all__ = ["shard_views", "all_gather_bytes", "run_sharded", "run_lockstep", "GpuExecutor", "densify_step_sharded"]
+__all__ = ["view_block", "shard_views", "all_reduce_max_", "all_gather_bytes", "run_sharded", "run_lockstep", "GpuExecutor", "densify_step_sharded"]

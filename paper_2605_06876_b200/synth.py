@@ -122,6 +122,41 @@ def synth_stats(scale: np.ndarray, extent: float, tau_g: float, tau_s: float, p_
     return ga, np.ones(n)
 
 
+def synth_stats_weighted(scale: np.ndarray, extent: float, tau_g: float, tau_s: float, p_split: float,
+                         p_clone: float, weight: np.ndarray, floor: float, seed: int):
+    """DensifyStats whose candidates follow the Gaussians' rendered contribution.
+
+    In training, ``accumulate_stats`` credits a Gaussian only in views where it
+    is visible (ref/adc.py:73-79) and its view-space gradient scales with its
+    blending weight T*alpha over the pixels it covers, so high-gradient
+    Gaussians are the ones the renders actually use.  Candidates are drawn
+    without replacement (Efraimidis-Spirakis keys) with probability
+    proportional to weight + floor * mean(weight) among the large (split) and
+    the small (clone) Gaussians; ``floor`` keeps stale, occluded Gaussians in
+    play.  g = tau_g*exp(|z|) for the drawn ones, tau_g*exp(-|z|-1e-3) else."""
+    rng = np.random.default_rng((seed, 0x57A75))
+    n = len(scale)
+    w = np.asarray(weight, dtype=np.float64)
+    large = scale.max(axis=1) > tau_s * extent
+    high = np.zeros(n, dtype=bool)
+    for sel, p in ((large, p_split), (~large, p_clone)):
+        idx = np.flatnonzero(sel)
+        k = min(len(idx), int(round(p * n)))
+        if k == 0:
+            continue
+        wi = w[idx] + floor * max(float(w[idx].mean()), 1e-30)
+        keys = np.log(rng.uniform(size=len(idx))) / wi
+        high[idx[np.argpartition(-keys, k - 1)[:k]]] = True
+    z = np.abs(rng.standard_normal(n))
+    ga = np.where(high, tau_g * np.exp(z), tau_g * np.exp(-z - 1e-3))
+    return ga, np.ones(n)
+
+
+def rho_of(size_factor: float, k_gt: int) -> float:
+    """SURVEY.md 8(d)'s density parameter: base = U(.04,.10) * sqrt(32 rho / k_gt)."""
+    return size_factor ** 2 * k_gt / 32.0
+
+
 def round_f32(s: SynthScene) -> SynthScene:
     """Round parameters to fp32 (what the device stores), renormalising quaternions in fp32."""
     q = s.rot.astype(np.float32)
@@ -133,21 +168,45 @@ def round_f32(s: SynthScene) -> SynthScene:
                       s.sh_dc.astype(np.float32).astype(np.float64), s.extent)
 
 
+def _quat_rot(q):
+    q = q / np.linalg.norm(q, axis=1, keepdims=True)
+    w, x, y, z = q.T
+    return np.stack([1 - 2 * (y * y + z * z), 2 * (x * y - w * z), 2 * (x * z + w * y),
+                     2 * (x * y + w * z), 1 - 2 * (x * x + z * z), 2 * (y * z - w * x),
+                     2 * (x * z - w * y), 2 * (y * z + w * x), 1 - 2 * (x * x + y * y)], axis=1).reshape(-1, 3, 3)
+
+
 def depth_complexity(s: SynthScene, cam_row, alpha_min=1.0 / 255) -> float:
-    """Mean number of splats with alpha >= alpha_min per pixel (area estimate, one view)."""
+    """Mean number of splats with alpha >= alpha_min per pixel of one view.
+
+    Exact per-splat footprint of the reference's render (ref/raster.py:66-93):
+    alpha = min(.99, o) exp(-q/2) >= alpha_min inside the conic ellipse
+    q <= 2 ln(min(o,.99)/alpha_min) of the projected covariance
+    J W Sigma W^T J^T + 0.3 I, whose area is pi * 2 ln(.) * sqrt(det).  Summed
+    over the splats in front of the camera whose centre projects into the
+    image, divided by W*H (border clipping ignored)."""
     r = cam_row[0:9].reshape(3, 3)
     c = cam_row[9:12]
-    fx, fy, w, h = cam_row[12], cam_row[13], cam_row[16], cam_row[17]
+    fx, fy, px, py, w, h = cam_row[12], cam_row[13], cam_row[14], cam_row[15], cam_row[16], cam_row[17]
     p = (s.mu - c) @ r
-    z = p[:, 2]
+    x, y, z = p[:, 0], p[:, 1], p[:, 2]
     ok = z > 1e-8
-    # projected covariance determinant (affine approx, isotropic proxy)
-    s2 = (s.scale ** 2).prod(axis=1) ** (1.0 / 3.0)
-    px_var = s2 * (fx * fy) / (z ** 2)
-    det = (px_var + 0.3) ** 2
-    o = np.minimum(s.opacity, 0.99)
+    mx, my = fx * x / np.where(ok, z, 1) + px, fy * y / np.where(ok, z, 1) + py
+    ok &= (mx >= 0) & (mx <= w - 1) & (my >= 0) & (my <= h - 1)
+    R = _quat_rot(s.rot[ok])
+    S = np.einsum("nij,nj,nkj->nik", R, s.scale[ok] ** 2, R)
+    zz = z[ok]
+    J = np.zeros((len(zz), 2, 3))
+    J[:, 0, 0] = fx / zz
+    J[:, 0, 2] = -fx * x[ok] / zz ** 2
+    J[:, 1, 1] = fy / zz
+    J[:, 1, 2] = -fy * y[ok] / zz ** 2
+    T = J @ r.T
+    cov = T @ S @ np.transpose(T, (0, 2, 1)) + 0.3 * np.eye(2)
+    det = cov[:, 0, 0] * cov[:, 1, 1] - cov[:, 0, 1] ** 2
+    o = np.minimum(s.opacity[ok], 0.99)
     area = np.pi * 2.0 * np.log(np.maximum(o / alpha_min, 1.0)) * np.sqrt(det)
-    return float(area[ok].sum() / (w * h))
+    return float(area.sum() / (w * h))
 
 
 @dataclass
@@ -166,15 +225,62 @@ class Workload:
     inflate: float = 2.0
     n_max: int = 19
     seed: int = 0
+    stats_mode: str = "uniform"   # "uniform": candidates drawn uniformly; "weighted": by rendered weight
+    weight_floor: float = 0.05
 
-    def build(self, seed=None):
-        """-> (init SynthScene rounded to fp32, camera rows, (grad_accum, denom), gt SynthScene)."""
+    @property
+    def rho(self) -> float:
+        return rho_of(self.size_factor, self.n_gt)
+
+    def build(self, seed=None, weight=None):
+        """-> (init SynthScene rounded to fp32, camera rows, (grad_accum, denom), gt SynthScene).
+
+        A "weighted" workload needs ``weight`` (the init scene's summed blending
+        weights over its views, Plan.render_stats; see build_device)."""
         seed = self.seed if seed is None else seed
         gt = gt_scene(self.n_gt, seed, self.size_factor, self.spread, self.large_frac, self.large_range)
         ini = round_f32(init_scene(gt, seed, inflate=self.inflate))
         cams = ring_cameras(self.n_views, self.width, self.height, gt.extent)
-        stats = synth_stats(ini.scale, ini.extent, 2e-4, 0.01, self.p_split, self.p_clone, seed)
+        if self.stats_mode == "weighted" and weight is not None:
+            stats = synth_stats_weighted(ini.scale, ini.extent, 2e-4, 0.01, self.p_split, self.p_clone, weight,
+                                         self.weight_floor, seed)
+        elif self.stats_mode == "weighted":
+            raise ValueError(f"{self.name}: weighted stats need the rendered weights (build_device)")
+        else:
+            stats = synth_stats(ini.scale, ini.extent, 2e-4, 0.01, self.p_split, self.p_clone, seed)
         return ini, cams, stats, round_f32(gt)
+
+    def build_device(self, plan, seed=None):
+        """Everything a step needs, on the plan's device: the init and GT scenes,
+        the GT images (rendered), the init attribution of all views (rendered,
+        with each Gaussian's blending weight for the weighted stats) and the
+        measured depth complexities.  Returns a dict."""
+        import torch
+
+        from .operator import GaussianTensors
+        seed = self.seed if seed is None else seed
+        gt = gt_scene(self.n_gt, seed, self.size_factor, self.spread, self.large_frac, self.large_range)
+        ini = round_f32(init_scene(gt, seed, inflate=self.inflate))
+        gt = round_f32(gt)
+        cams = ring_cameras(self.n_views, self.width, self.height, gt.extent)
+        dev = plan.device
+        g = GaussianTensors.from_numpy(*ini.arrays(), device=dev)
+        gt_g = GaussianTensors.from_numpy(*gt.arrays(), device=dev)
+        # statistics renders (no early termination) are separate from the
+        # attribution the step consumes, which is the plain render
+        _, _, _, dc_gt = plan.render_stats(gt_g, cams)
+        gt_img, _ = plan.render(gt_g, cams)
+        del gt_g
+        _, _, weight, dc_init = plan.render_stats(g, cams)
+        img, dom = plan.render(g, cams)
+        if self.stats_mode == "weighted":
+            stats = synth_stats_weighted(ini.scale, ini.extent, 2e-4, 0.01, self.p_split, self.p_clone,
+                                         weight.cpu().numpy(), self.weight_floor, seed)
+        else:
+            stats = synth_stats(ini.scale, ini.extent, 2e-4, 0.01, self.p_split, self.p_clone, seed)
+        torch.cuda.synchronize(dev)
+        return dict(ini=ini, gt=gt, cams=cams, stats=stats, g=g, gt_img=gt_img, img=img, dom=dom,
+                    weight=weight, dc_gt=dc_gt, dc_init=dc_init)
 
 
 # BASELINE.json configs (SURVEY.md 8(d)); sizes scale as 1/sqrt(k) around the

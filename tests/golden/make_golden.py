@@ -17,6 +17,10 @@ Case families (reference symbols, file:line under pkg/src/adpsplit):
   child     child_init.init_child                 child_init.py:110-140
   merge     cross_view_merge.merge_groups+cap      cross_view_merge.py:72-116
   step      adc.adpsplit_step                     adc.py:143-245
+  vanilla   adc.vanilla_densify (n = 2, 3)        adc.py:248-280
+  remap     adc.remap_stats after each step       adc.py:283-296
+  accum     adc.accumulate_stats                  adc.py:73-79
+  prune     harness._prune                        harness.py:320-340
 """
 
 from __future__ import annotations
@@ -37,7 +41,9 @@ from adpsplit.cross_view_merge import cap_children, merge_groups  # noqa: E402
 from adpsplit.child_init import ChildProposal  # noqa: E402
 from adpsplit.error_partition import (  # noqa: E402
     ErrorMaps, ErrorRegion, band_map, compute_maps, partition, region_stats)
+from adpsplit import harness  # noqa: E402
 from adpsplit.harness import desk_config, init_from_gt, synth_scene  # noqa: E402
+from adpsplit.raster import GradOutput  # noqa: E402
 from adpsplit.scene import (  # noqa: E402
     AdpSplitConfig, Camera, Gaussian3D, Scene, covariance, rgb_to_dc)
 
@@ -264,6 +270,34 @@ def gen_merge():
     meta["merge"] = specs
 
 
+def gen_merge_large():
+    """Proposal lists of 30-300 (the oracle's prefiltered union-find path)."""
+    rng = np.random.default_rng(909)
+    specs = []
+    for c in range(10):
+        n = int(rng.integers(30, 300))
+        props = []
+        centers = rng.uniform(-0.3, 0.3, (int(rng.integers(2, 12)), 3))
+        for k in range(n):
+            q, _ = np.linalg.qr(rng.standard_normal((3, 3)))
+            if np.linalg.det(q) < 0:
+                q[:, 0] = -q[:, 0]
+            props.append(ChildProposal(
+                mu=centers[k % len(centers)] + rng.normal(0, rng.choice([0.01, 0.05, 0.2]), 3), rot=q,
+                scale=rng.uniform(0.01, 0.1, 3), opacity=0.6,
+                rgb=np.full(3, 0.5) + rng.normal(0, 0.05, 3), parent=0, view=k % 4, region_area=9))
+        gd, gc = float(rng.choice([2.0, 1.0, 4.0])), float(rng.choice([0.15, 0.05, 1.0]))
+        groups = merge_groups(props, gd, gc)
+        put(f"mergeL__{c}__mu", np.array([p.mu for p in props]))
+        put(f"mergeL__{c}__rot", np.array([p.rot for p in props]))
+        put(f"mergeL__{c}__scale", np.array([p.scale for p in props]))
+        put(f"mergeL__{c}__rgb", np.array([p.rgb for p in props]))
+        put(f"mergeL__{c}__g_mu", np.array([g.merged_mu for g in groups]))
+        put(f"mergeL__{c}__g_cov", np.array([g.merged_cov for g in groups]))
+        specs.append(dict(gamma_d=gd, gamma_c=gc, members=[list(map(int, g.members)) for g in groups]))
+    meta["merge_large"] = specs
+
+
 # ----------------------------------------------------------------------- step
 def report_dict(rep):
     return dict(count_before=rep.count_before, count_after=rep.count_after,
@@ -302,6 +336,10 @@ def run_step(tag, scene, cams, gts, stats, cfg, seed):
         put(f"step__{tag}__dom{v}", captured[id(cams[v])].dominant_map)
     put_scene(f"step__{tag}__out", new_scene)
     put(f"step__{tag}__index_map", rep.index_map)
+    # remap_stats (ref/adc.py:283-296) of this step's report on the step's input stats
+    rs = adc.remap_stats(stats, rep)
+    put(f"remap__{tag}__grad_accum", rs.grad_accum)
+    put(f"remap__{tag}__denom", rs.denom)
     cfgd = {f: getattr(cfg, f) for f in cfg.__dataclass_fields__}
     meta.setdefault("step", {})[tag] = dict(cfg=cfgd, seed=seed, report=report_dict(rep))
 
@@ -352,13 +390,85 @@ def gen_steps():
         run_step(f"paper{seed}", scene, cams, gts, stats, cfg, 7 + seed)
 
 
+# ------------------------------------------------------- next rows of SURVEY 8(f)
+def gen_next_rows():
+    # vanilla_densify on the step inputs (n_children 2 and 3; ref/adc.py:248-280)
+    specs = []
+    for tag in ("blobs", "desk0", "desk3", "paper1", "paper2"):
+        for n_children in (2, 3):
+            sc = Scene([Gaussian3D(mu=store[f"step__{tag}__in__mu"][i], scale=store[f"step__{tag}__in__scale"][i],
+                                   rot=store[f"step__{tag}__in__rot"][i],
+                                   opacity=float(store[f"step__{tag}__in__opacity"][i]),
+                                   sh_dc=store[f"step__{tag}__in__sh_dc"][i])
+                        for i in range(len(store[f"step__{tag}__in__mu"]))],
+                       extent=float(store[f"step__{tag}__in__extent"]))
+            stats = adc.DensifyStats(grad_accum=store[f"step__{tag}__grad_accum"].copy(),
+                                     denom=store[f"step__{tag}__denom"].copy())
+            cfg = AdpSplitConfig(**meta["step"][tag]["cfg"])
+            seed = 1000 + n_children
+            rng = np.random.default_rng(seed)
+            new_scene, rep = adc.vanilla_densify(sc, stats, cfg, n_children, rng)
+            key = f"vanilla__{tag}__{n_children}"
+            put_scene(f"{key}__out", new_scene)
+            put(f"{key}__index_map", rep.index_map)
+            specs.append(dict(tag=tag, n_children=n_children, seed=seed, report=report_dict(rep),
+                              rng_state=json.loads(json.dumps(rng.bit_generator.state))))
+    meta["vanilla"] = specs
+    # accumulate_stats (ref/adc.py:73-79) with the reference's fp64 GradOutput
+    rng = np.random.default_rng(77)
+    acc = []
+    for c, n in enumerate((1, 7, 1000, 4099)):
+        ga = rng.uniform(0, 1e-2, n)
+        den = rng.integers(0, 5, n).astype(np.float64)
+        vg = rng.normal(0, 1e-3, (n, 2)) * np.exp(rng.normal(0, 3, (n, 1)))
+        vis = rng.uniform(size=n) < 0.6
+        stats = adc.DensifyStats(grad_accum=ga.copy(), denom=den.copy())
+        for rep_ in range(3):      # three views in a row
+            z = np.zeros((n, 3))
+            adc.accumulate_stats(stats, GradOutput(dmu=z, dscale=z, drot=np.zeros((n, 4)), dopacity=np.zeros(n),
+                                                   dsh_dc=z, viewspace_grad=vg * (rep_ + 1), visible=vis))
+        for k, v in dict(ga=ga, den=den, vg=vg, vis=vis, ga_out=stats.grad_accum, den_out=stats.denom).items():
+            put(f"accum__{c}__{k}", v)
+        acc.append(n)
+    meta["accum"] = acc
+    # _prune (ref/harness.py:320-340) on trainer state built from a scene
+    pr = []
+    for c, (n, thr) in enumerate(((50, harness.PRUNE_OPACITY), (400, 0.05), (30, 0.5), (20, 0.5), (20, 1e-4))):
+        rng = np.random.default_rng(500 + c)
+        op = rng.uniform(1e-4, 0.2, n) if thr < 0.5 else rng.uniform(0.3, 0.7, n)
+        if c == 3:
+            op = np.full(n, 0.9)            # nobody pruned: state returned unchanged
+        if c == 4:
+            op = np.full(n, 5e-5)           # everybody below: unchanged too
+        gs = [Gaussian3D(mu=rng.normal(size=3), scale=np.exp(rng.normal(size=3) - 3), rot=rand_quat(rng),
+                         opacity=float(op[i]), sh_dc=rng.normal(size=3)) for i in range(n)]
+        params = harness._Params(Scene(gaussians=gs, extent=1.0))
+        if c == 1:                          # logits right at the threshold's logit
+            params.logit_op[:40] = np.log(thr / (1 - thr)) + rng.integers(-3, 4, 40) * 1e-16
+        opt = harness._Adam(params)
+        for g in params.groups():
+            opt.m[g] = rng.normal(size=opt.m[g].shape)
+            opt.v[g] = rng.uniform(size=opt.v[g].shape)
+        stats = adc.DensifyStats(grad_accum=np.arange(n, dtype=np.float64), denom=rng.uniform(size=n))
+        new_p, new_opt, new_stats = harness._prune(params, opt, stats, thr)
+        put(f"prune__{c}__logit", params.logit_op)
+        put(f"prune__{c}__keep_index", new_stats.grad_accum.astype(np.int64))
+        put(f"prune__{c}__m_mu_in", opt.m["mu"])
+        put(f"prune__{c}__m_mu_out", new_opt.m["mu"])
+        put(f"prune__{c}__denom_out", new_stats.denom)
+        pr.append(dict(n=n, threshold=thr, pruned=new_p is not params))
+    meta["prune"] = pr
+
+
 def main():
     gen_render()
     gen_maps()
     gen_partition()
     gen_child()
     gen_merge()
+    gen_merge_large()
     gen_steps()
+    gen_next_rows()
     store["meta_json"] = np.array(json.dumps(meta))
     np.savez_compressed(OUT, **store)
     print(f"wrote {OUT}: {len(store)} arrays, {os.path.getsize(OUT) / 1e6:.2f} MB")

@@ -1,16 +1,24 @@
-"""Scene/camera text fixtures written by the REFERENCE's own writers
-(ref/scene.py:283-289 save_scene, 340-349 save_cameras), for the I/O parity
-tests (tests/test_scene_io.py).  Run in the build container:
+"""Scene/camera fixtures for the binary-format tests (tests/test_scene_io.py).
+
+The scenes and cameras are written AND parsed by the reference's own text
+I/O (ref/scene.py:283-381, save_scene/load_scene/save_cameras/load_cameras);
+the reference's parse is then stored twice: as plain arrays (.npz, what a
+load must reproduce) and as this repo's binary v1 files (.bin).  Run in the
+build container (the reference is not needed at test time):
 
     PYTHONDONTWRITEBYTECODE=1 python tests/golden/make_io_golden.py
 """
 import os
 import sys
+import tempfile
 
 import numpy as np
 
 sys.path.insert(0, "/root/reference/pkg/src")
+sys.path.insert(0, os.path.join(os.path.dirname(os.path.abspath(__file__)), "..", ".."))
 from adpsplit import scene as RS  # noqa: E402
+
+from paper_2605_06876_b200 import scene_io as IO  # noqa: E402
 
 OUT = os.path.join(os.path.dirname(os.path.abspath(__file__)), "io")
 rng = np.random.default_rng(7)
@@ -32,17 +40,24 @@ def camera(w, h):
 
 
 os.makedirs(OUT, exist_ok=True)
-RS.save_scene(RS.Scene(gaussians=[gaussian(0) for _ in range(40)], extent=3.75), os.path.join(OUT, "scene_k0.txt"))
-RS.save_scene(RS.Scene(gaussians=[gaussian(3) for _ in range(25)], extent=1.5), os.path.join(OUT, "scene_k3.txt"))
-RS.save_cameras([camera(64, 48), camera(33, 17), camera(256, 256)], os.path.join(OUT, "cameras.txt"))
-# the reference's own parse of its files, as arrays (what a load must reproduce)
-for name in ("scene_k0", "scene_k3"):
-    s = RS.load_scene(os.path.join(OUT, f"{name}.txt"))
+for f in os.listdir(OUT):
+    os.remove(os.path.join(OUT, f))
+tmp = tempfile.mkdtemp()
+scenes = {"scene_k0": RS.Scene(gaussians=[gaussian(0) for _ in range(40)], extent=3.75),
+          "scene_k3": RS.Scene(gaussians=[gaussian(3) for _ in range(25)], extent=1.5)}
+for name, sc in scenes.items():
+    txt = os.path.join(tmp, f"{name}.txt")
+    RS.save_scene(sc, txt)
+    s = RS.load_scene(txt)                      # the reference's own parse of its file
     k = len(s.gaussians[0].sh_rest)
     np.savez(os.path.join(OUT, f"{name}.npz"), extent=s.extent,
              rec=np.array([[*g.mu, *g.scale, *g.rot, g.opacity, *g.sh_dc,
                             *[c for co in g.sh_rest for c in co]] for g in s.gaussians]), k=k)
-cams = RS.load_cameras(os.path.join(OUT, "cameras.txt"))
+    IO.save_scene_bin(IO.scene_to_arrays(s), os.path.join(OUT, f"{name}.bin"))
+ctxt = os.path.join(tmp, "cameras.txt")
+RS.save_cameras([camera(64, 48), camera(33, 17), camera(256, 256)], ctxt)
+cams = RS.load_cameras(ctxt)
 np.savez(os.path.join(OUT, "cameras.npz"),
          rows=np.array([[*c.r_c2w.ravel(), *c.center, c.f_x, c.f_y, c.p_x, c.p_y, c.width, c.height] for c in cams]))
+IO.save_cameras_bin(cams, os.path.join(OUT, "cameras.bin"))
 print("wrote", sorted(os.listdir(OUT)))

@@ -18,6 +18,10 @@ import numpy as np
 
 from oracle import adpsplit_oracle as O
 
+import os
+
+REPORT = []           # per-call statistics of compare_step (written by conftest when PARITY_REPORT is set)
+
 EPS_E = 2e-5          # end-to-end: |e - threshold| band for the fp32 render
 EPS_TIE = 1e-4        # end-to-end: relative best/runner-up T*alpha gap
 
@@ -50,10 +54,18 @@ def flag_candidates(res: O.StepResult, g: O.Gaussians, cams, cfg) -> set:
     gd, gc = O.cfg_get(cfg, "gamma_d"), O.cfg_get(cfg, "gamma_c")
     eps = O.cfg_get(cfg, "eps")
     for i, props in res.proposals.items():
-        for a in range(len(props)):
-            for b in range(a + 1, len(props)):
-                d, dc = O.gate_terms(props[a], props[b])
-                if abs(d - gd) <= 1e-9 * max(gd, 1.0) or abs(dc - gc) <= 1e-12:
+        n = len(props)
+        if n < 2:
+            continue
+        idx = np.arange(n)
+        for lo in range(0, n, 512):
+            rows = idx[lo:lo + 512]
+            dist, dc = O.gate_terms_batch(props, rows, idx)
+            near = (np.abs(dist - gd) <= 2e-9 * max(gd, 1.0)) | (np.abs(dc - gc) <= 2e-12)
+            near &= idx[None, :] > rows[:, None]
+            for a, b in zip(*np.nonzero(near)):
+                d, c = O.gate_terms(props[rows[a]], props[b])   # exact, the reference's arithmetic
+                if abs(d - gd) <= 1e-9 * max(gd, 1.0) or abs(c - gc) <= 1e-12:
                     flagged.add(i)
     for v, regs in res.regions.items():
         for reg in regs:
@@ -64,11 +76,9 @@ def flag_candidates(res: O.StepResult, g: O.Gaussians, cams, cfg) -> set:
             if abs(t) <= 1e-12 * np.linalg.norm(b):
                 flagged.add(i)
     for i, groups in res.all_groups.items():
-        ext = np.array([gr.extent for gr in groups])
-        for a in range(len(ext)):
-            for b in range(a + 1, len(ext)):
-                if abs(ext[a] - ext[b]) <= 1e-12 * max(abs(ext[a]), abs(ext[b])):
-                    flagged.add(i)
+        ext = np.sort(np.array([gr.extent for gr in groups]))
+        if len(ext) > 1 and (np.diff(ext) <= 1e-12 * np.maximum(np.abs(ext[1:]), np.abs(ext[:-1]))).any():
+            flagged.add(i)
         for gr in groups:
             if len(gr.members) > 1:
                 mc = np.mean([res.proposals[i][m].cov() for m in gr.members], axis=0)
@@ -117,10 +127,37 @@ def unexplained_dominance(res: O.StepResult, gpu_renders: dict, weights: dict) -
     return n
 
 
+def _rows_of(rec) -> int:
+    """Rows a candidate appends (ref/adc.py:198-227): 2 fallback children, nothing for
+    a reset, N_i children + the parent copy for a split."""
+    return 2 if rec.fallback else (0 if rec.reset else rec.children_inserted + 1)
+
+
+def cursor_walk(ores: O.StepResult):
+    """The reference's bookkeeping walk (ref tests/test_acceptance.py:238-256):
+    (insert offset per candidate, child_parent per appended row)."""
+    cur = int((ores.index_map >= 0).sum())
+    offs, parent = [], []
+    for rec in ores.candidates:
+        offs.append(cur)
+        k = _rows_of(rec)
+        parent += [rec.index] * k
+        cur += k
+    parent += list(ores.clones)
+    return np.array(offs, dtype=np.int64), np.array(parent, dtype=np.int64)
+
+
 def compare_step(gres, ores: O.StepResult, flagged: set, g_in: O.Gaussians, strict_floats=True):
     """Assert GPU StepResult == oracle StepResult outside the flagged candidates.
 
-    Returns a dict of statistics (mismatches, flagged, max errors)."""
+    Integer outputs of every unflagged candidate (case, regions_per_view,
+    proposals, N_i, its insert offset relative to the survivors, the parents of
+    its rows) are exact; survivors and clones are exact; the rows of unflagged
+    candidates are compared within the float tolerance at each side's own
+    offsets, so a flagged candidate that changes its case (and shifts the
+    layout behind it) does not hide the rest.  With no mismatch the whole
+    layout (index_map, child_parent, insert offsets, counts) is compared
+    exactly.  Returns a dict of statistics (mismatched, flagged, max errors)."""
     rep = gres.report()
     assert rep.sampled_views == ores.sampled_views
     assert rep.clones == ores.clones
@@ -139,39 +176,77 @@ def compare_step(gres, ores: O.StepResult, flagged: set, g_in: O.Gaussians, stri
     assert not unexplained, f"integer mismatch on non-flagged candidates {unexplained[:10]}: " + \
         "; ".join(f"gpu={g_recs[i]} oracle={o_recs[i]}" for i in unexplained[:3])
     stats = dict(mismatched=len(mism), flagged=len(flagged), candidates=len(o_recs))
-    if mism:
-        return stats     # layouts diverge after a flagged mismatch; integer parity shown above
-    assert rep.count_after == ores.count_after
-    assert rep.merge_edges == ores.merge_edges
-    assert rep.reset_indices == ores.reset_indices
-    np.testing.assert_array_equal(rep.index_map, ores.index_map)
+    mset = set(mism)
+    o_off, o_par = cursor_walk(ores)
+    g_off = gres.insert_offset.cpu().numpy().astype(np.int64)
+    g_par = gres.child_parent.cpu().numpy().astype(np.int64)
+    g_keep = int((rep.index_map >= 0).sum())
+    o_keep = int((ores.index_map >= 0).sum())
+    # survivors: identical except for candidates whose case differs
+    removed_o = {r.index for r in ores.candidates if r.fallback or not r.reset}
+    removed_g = {r.index for r in rep.candidates if r.fallback or not r.reset}
+    assert removed_o - mset == removed_g - mset
+    keep_o = [i for i in range(ores.count_before) if i not in removed_o]
+    np.testing.assert_array_equal(ores.index_map[:o_keep], keep_o)
+    np.testing.assert_array_equal(rep.index_map[:g_keep], [i for i in range(ores.count_before) if i not in removed_g])
+    assert (rep.index_map[g_keep:] == -1).all()
     out = gres.gaussians.numpy()
     og = ores.gaussians
-    # which rows may differ (children of flagged candidates)
-    skip = np.zeros(ores.count_after, dtype=bool)
-    cur = int((ores.index_map >= 0).sum())
-    for rec in ores.candidates:
-        k = 2 if rec.fallback else (0 if rec.reset else rec.children_inserted + 1)
-        if rec.index in flagged:
-            skip[cur:cur + k] = True
-        cur += k
-    keep = ~skip
-    exact_rows = ores.index_map >= 0
+    # survivor rows are exact copies (fp32 in, fp32 out)
     for f in ("mu", "scale", "rot", "opacity", "sh_dc"):
-        np.testing.assert_array_equal(out[f][exact_rows], f32(getattr(og, f))[exact_rows], err_msg=f)
+        gi = {int(i): k for k, i in enumerate(rep.index_map[:g_keep])}
+        common = [k for k, i in enumerate(keep_o) if i in gi]
+        np.testing.assert_array_equal(out[f][[gi[keep_o[k]] for k in common]], f32(getattr(og, f))[common],
+                                      err_msg=f)
+    # per candidate: relative insert offset and row parents exact, rows within tolerance
+    o_rows, g_rows = [], []
+    g_pos = {r.index: k for k, r in enumerate(rep.candidates)}
+    for k, rec in enumerate(ores.candidates):
+        if rec.index in mset:
+            continue
+        kg = g_pos[rec.index]
+        n_rows = _rows_of(rec)
+        # offsets relative to the first insert of the first candidate, minus the rows of
+        # mismatched candidates before this one on each side
+        before_o = sum(_rows_of(o_recs[i]) for i in mset if i < rec.index)
+        before_g = sum(_rows_of(g_recs[i]) for i in mset if i < rec.index)
+        assert o_off[k] - o_keep - before_o == g_off[kg] - g_keep - before_g, rec.index
+        assert (g_par[g_off[kg] - g_keep:g_off[kg] - g_keep + n_rows] == rec.index).all(), rec.index
+        if rec.index in flagged:
+            continue
+        o_rows += range(o_off[k], o_off[k] + n_rows)
+        g_rows += range(g_off[kg], g_off[kg] + n_rows)
+    n_ins_g = len(g_par) - len(rep.clones)
+    assert (g_par[n_ins_g:] == np.array(ores.clones, dtype=np.int64)).all()
+    n_ins_o = len(o_par) - len(ores.clones)
+    for j in range(len(ores.clones)):   # clones: exact copies
+        o_rows_c, g_rows_c = o_keep + n_ins_o + j, g_keep + n_ins_g + j
+        for f in ("mu", "scale", "rot", "opacity", "sh_dc"):
+            np.testing.assert_array_equal(out[f][g_rows_c], f32(getattr(og, f))[o_rows_c], err_msg=f)
+    if not mism:
+        assert rep.count_after == ores.count_after
+        assert rep.merge_edges == ores.merge_edges
+        assert rep.reset_indices == ores.reset_indices
+        np.testing.assert_array_equal(rep.index_map, ores.index_map)
+        np.testing.assert_array_equal(g_off, o_off)
+        np.testing.assert_array_equal(g_par, o_par)
+    o_rows, g_rows = np.array(o_rows, dtype=np.int64), np.array(g_rows, dtype=np.int64)
     for f in ("mu", "sh_dc", "opacity"):
-        a, b = out[f][keep].astype(np.float64), getattr(og, f)[keep]
+        a, b = out[f][g_rows].astype(np.float64), getattr(og, f)[o_rows]
         err = np.abs(a - b) / np.maximum(np.abs(b), 1e-3)
         stats[f"max_rel_{f}"] = float(err.max()) if err.size else 0.0
         if strict_floats:
             assert stats[f"max_rel_{f}"] <= 2e-6, (f, stats[f"max_rel_{f}"])
-    cg = covs(out["scale"][keep].astype(np.float64), out["rot"][keep].astype(np.float64))
-    co = covs(og.scale[keep], og.rot[keep])
+    cg = covs(out["scale"][g_rows].astype(np.float64), out["rot"][g_rows].astype(np.float64))
+    co = covs(og.scale[o_rows], og.rot[o_rows])
     scale_ = np.abs(co).reshape(len(co), -1).max(axis=1) if len(co) else np.zeros(0)
     cerr = np.abs(cg - co).reshape(len(co), -1).max(axis=1) / np.maximum(scale_, 1e-300) if len(co) else np.zeros(0)
     stats["max_rel_cov"] = float(cerr.max()) if cerr.size else 0.0
     if strict_floats:
         assert stats["max_rel_cov"] <= 1e-5, stats["max_rel_cov"]
+    stats["rows_compared"] = int(len(o_rows))
+    stats["test"] = os.environ.get("PYTEST_CURRENT_TEST", "").split(" ")[0]
+    REPORT.append(stats)
     return stats
 
 

@@ -1,0 +1,230 @@
+"""GPU parity for the rows around the step:
+accumulate_stats, opacity prune, vanilla_densify against reference goldens,
+the new phase-2 integer outputs, and argument validation at the boundary.
+
+Run on a B200:  python -m pytest tests -m gpu -q
+"""
+
+import ctypes as C
+
+import numpy as np
+import pytest
+
+import golden_io
+import parity as PA
+from oracle import adpsplit_oracle as O
+
+pytestmark = pytest.mark.gpu
+
+DATA, META = golden_io.load()
+
+
+@pytest.fixture(scope="module")
+def op():
+    import torch
+    assert torch.cuda.is_available(), "GPU tests need a CUDA device"
+    from paper_2605_06876_b200 import operator
+    return operator
+
+
+@pytest.fixture(scope="module")
+def plan(op):
+    return op.Plan("cuda:0")
+
+
+# ------------------------------------------------------------ accumulate_stats
+@pytest.mark.parametrize("c", range(4))
+def test_accumulate_stats_f64_bit_exact_vs_reference(op, c):
+    """ref/adc.py:73-79 with the reference's fp64 GradOutput: bit-identical."""
+    import torch
+    ga = torch.as_tensor(DATA[f"accum__{c}__ga"].copy(), device="cuda")
+    den = torch.as_tensor(DATA[f"accum__{c}__den"].copy(), device="cuda")
+    vg = torch.as_tensor(DATA[f"accum__{c}__vg"], device="cuda")
+    vis = torch.as_tensor(DATA[f"accum__{c}__vis"], device="cuda")
+    for k in range(3):
+        op.accumulate_stats_(ga, den, vg * (k + 1), vis)
+    np.testing.assert_array_equal(ga.cpu().numpy(), DATA[f"accum__{c}__ga_out"])
+    np.testing.assert_array_equal(den.cpu().numpy(), DATA[f"accum__{c}__den_out"])
+
+
+def test_accumulate_stats_f32_and_masked_rows(op):
+    """fp32 gradients (a GPU rasterizer's): the norm is computed in fp32 as numpy
+    does for a float32 array; invisible rows are untouched."""
+    import torch
+    rng = np.random.default_rng(3)
+    n = 1_000_003
+    ga0 = rng.uniform(0, 1e-2, n)
+    den0 = rng.integers(0, 9, n).astype(np.float64)
+    vg = (rng.normal(0, 1e-3, (n, 2)) * np.exp(rng.normal(0, 2, (n, 1)))).astype(np.float32)
+    vis = rng.uniform(size=n) < 0.3
+    ga, den = ga0.copy(), den0.copy()
+    O.accumulate_stats(ga, den, vg, vis)
+    tg, td = torch.as_tensor(ga0, device="cuda"), torch.as_tensor(den0, device="cuda")
+    op.accumulate_stats_(tg, td, torch.as_tensor(vg, device="cuda"), torch.as_tensor(vis, device="cuda"))
+    np.testing.assert_array_equal(tg.cpu().numpy(), ga)
+    np.testing.assert_array_equal(td.cpu().numpy(), den)
+    assert (tg.cpu().numpy()[~vis] == ga0[~vis]).all()
+
+
+def test_accumulate_stats_rejects_bad_inputs(op):
+    import torch
+    ga = torch.zeros(10, dtype=torch.float64, device="cuda")
+    den = torch.zeros(10, dtype=torch.float64, device="cuda")
+    vis = torch.ones(10, dtype=torch.bool, device="cuda")
+    with pytest.raises(ValueError, match=r"\[N,2\]"):
+        op.accumulate_stats_(ga, den, torch.zeros(10, 3, device="cuda"), vis)
+    with pytest.raises(ValueError, match="dimensions"):
+        op.accumulate_stats_(ga, den, torch.zeros(9, 2, device="cuda"), vis)
+    with pytest.raises(ValueError, match="contiguous"):
+        op.accumulate_stats_(torch.zeros(20, dtype=torch.float64, device="cuda")[::2], den,
+                             torch.zeros(10, 2, device="cuda"), vis)
+    with pytest.raises(TypeError):
+        op.accumulate_stats_(ga.float(), den, torch.zeros(10, 2, device="cuda"), vis)
+
+
+# ---------------------------------------------------------------- opacity prune
+@pytest.mark.parametrize("c", range(5))
+def test_prune_keep_vs_reference(op, plan, c):
+    """ref/harness.py:320-340 on the reference's fp64 logits: the kept set (or
+    'unchanged') equals the reference's, outside near-threshold logits."""
+    import torch
+    spec = META["prune"][c]
+    logit = torch.as_tensor(DATA[f"prune__{c}__logit"], device="cuda")
+    im, nk, near = plan.prune_index(spec["threshold"], logit_op=logit)
+    want = O.prune_keep(DATA[f"prune__{c}__logit"], spec["threshold"])
+    if want is None:
+        assert nk in (0, len(logit)) and not spec["pruned"]
+        return
+    got = im.cpu().numpy()
+    sig = O.sigmoid(DATA[f"prune__{c}__logit"])
+    ulp = np.spacing(spec["threshold"])
+    near_set = set(np.flatnonzero(np.abs(sig - spec["threshold"]) <= 4 * ulp))
+    assert near == len(near_set)
+    assert set(got) - near_set == set(want) - near_set
+    if not near_set:
+        np.testing.assert_array_equal(got, DATA[f"prune__{c}__keep_index"])
+
+
+def test_prune_tensors_carry_rows(op, plan):
+    """prune() on fp32 opacities: survivors' parameters, moments and stats gathered
+    in old order (ref/harness.py:320-340), nothing pruned when all/none survive."""
+    import torch
+    rng = np.random.default_rng(9)
+    n = 200_001
+    g = O.Gaussians(rng.normal(size=(n, 3)), rng.uniform(0.01, 0.1, (n, 3)), np.tile([1.0, 0, 0, 0], (n, 1)),
+                    rng.uniform(1e-4, 0.05, n), rng.normal(size=(n, 3)))
+    g = PA.oracle_gaussians_f32(g)
+    t = PA.to_tensors(g)
+    m = torch.as_tensor(rng.normal(size=(n, 3)).astype(np.float32), device="cuda")
+    ga = torch.as_tensor(rng.uniform(size=n), device="cuda")
+    thr = 0.005
+    g2, (m2, ga2), im, near = op.prune(t, thr, rows=(m, ga), plan=plan)
+    keep = np.flatnonzero(g.opacity >= thr)
+    assert 0 < len(keep) < n and near == 0
+    np.testing.assert_array_equal(im.cpu().numpy(), keep)
+    np.testing.assert_array_equal(g2.mu.cpu().numpy(), g.mu[keep].astype(np.float32))
+    np.testing.assert_array_equal(g2.opacity.cpu().numpy(), g.opacity[keep].astype(np.float32))
+    np.testing.assert_array_equal(m2.cpu().numpy(), m.cpu().numpy()[keep])
+    np.testing.assert_array_equal(ga2.cpu().numpy(), ga.cpu().numpy()[keep])
+    g3, rows3, im3, _ = op.prune(t, 0.0, rows=(m,), plan=plan)    # all survive: unchanged
+    assert g3 is t and im3 is None and rows3[0] is m
+
+
+# ----------------------------------------------------- vanilla_densify goldens
+@pytest.mark.parametrize("c", range(10))
+def test_vanilla_densify_vs_reference_golden(op, plan, c):
+    """ref/adc.py:248-280 on the device: layout and index_map exact, children within
+    the float tolerance of the reference's own output, Generator state exact."""
+    import torch
+    spec = META["vanilla"][c]
+    tag, nc = spec["tag"], spec["n_children"]
+    g, extent = golden_io.scene(DATA, f"step__{tag}__in")
+    g32 = PA.oracle_gaussians_f32(g)
+    cfg = golden_io.Cfg(META["step"][tag]["cfg"])
+    rng = np.random.default_rng(spec["seed"])
+    res = op.vanilla_densify_step(PA.to_tensors(g32), extent,
+                                  torch.as_tensor(DATA[f"step__{tag}__grad_accum"], device="cuda"),
+                                  torch.as_tensor(DATA[f"step__{tag}__denom"], device="cuda"), cfg, nc, rng,
+                                  plan=plan)
+    key = f"vanilla__{tag}__{nc}"
+    np.testing.assert_array_equal(res.index_map.cpu().numpy(), DATA[f"{key}__index_map"])
+    out = res.gaussians.numpy()
+    np.testing.assert_allclose(out["mu"], DATA[f"{key}__out__mu"], rtol=2e-6, atol=2e-7)
+    np.testing.assert_allclose(out["scale"], DATA[f"{key}__out__scale"], rtol=2e-6)
+    np.testing.assert_array_equal(out["opacity"], DATA[f"{key}__out__opacity"].astype(np.float32))
+    assert rng.bit_generator.state["state"]["state"] == spec["rng_state"]["state"]["state"]
+    # child_parent / insert offsets: nc rows per candidate in ascending order, then clones
+    rep = spec["report"]
+    n_keep = int((DATA[f"{key}__index_map"] >= 0).sum())
+    want_par = [c_["index"] for c_ in rep["candidates"] for _ in range(nc)] + rep["clones"]
+    np.testing.assert_array_equal(res.child_parent.cpu().numpy(), want_par)
+    np.testing.assert_array_equal(res.insert_offset.cpu().numpy(),
+                                  n_keep + nc * np.arange(len(rep["candidates"])))
+
+
+# ------------------------------------------- phase-2 integer outputs vs criterion 6
+@pytest.mark.parametrize("tag", sorted(META["step"]))
+def test_child_parent_and_offsets_vs_reference_report(op, plan, tag):
+    """child_parent and per-candidate insert offsets reproduce the reference's own
+    bookkeeping walk (ref tests/test_acceptance.py:238-256) over its golden report."""
+    import torch
+    g, extent = golden_io.scene(DATA, f"step__{tag}__in")
+    g = PA.oracle_gaussians_f32(g)
+    cams = DATA[f"step__{tag}__cams"]
+    m = META["step"][tag]
+    cfg = golden_io.Cfg(m["cfg"])
+    views = m["report"]["sampled_views"]
+    img = torch.as_tensor(np.stack([DATA[f"step__{tag}__img{v}"] for v in views]), dtype=torch.float32,
+                          device="cuda")
+    dom = torch.as_tensor(np.stack([DATA[f"step__{tag}__dom{v}"] for v in views]), dtype=torch.int32,
+                          device="cuda")
+    res = op.densify_step(PA.to_tensors(g), extent, cams,
+                          torch.as_tensor(PA.f32(DATA[f"step__{tag}__gt"]), dtype=torch.float32, device="cuda"),
+                          torch.as_tensor(DATA[f"step__{tag}__grad_accum"], device="cuda"),
+                          torch.as_tensor(DATA[f"step__{tag}__denom"], device="cuda"), cfg,
+                          np.random.default_rng(m["seed"]), renders=(img, dom), plan=plan)
+    rep = m["report"]
+    im = DATA[f"step__{tag}__index_map"]
+    cur = int((im >= 0).sum())
+    offs, par = [], []
+    for c in rep["candidates"]:
+        offs.append(cur)
+        k = 2 if c["fallback"] else (0 if c["reset"] else c["children_inserted"] + 1)
+        par += [c["index"]] * k
+        cur += k
+    par += rep["clones"]
+    got = res.report()
+    if [(c.index, c.fallback, c.reset, c.children_inserted) for c in got.candidates] != \
+            [(c["index"], c["fallback"], c["reset"], c["children_inserted"]) for c in rep["candidates"]]:
+        pytest.skip("fp32 inputs moved a near-threshold decision; covered by test_step_stage_isolated")
+    np.testing.assert_array_equal(res.insert_offset.cpu().numpy(), offs)
+    np.testing.assert_array_equal(res.child_parent.cpu().numpy(), par)
+    np.testing.assert_array_equal(res.index_map.cpu().numpy(), im)
+
+
+# ------------------------------------------------------------- boundary checks
+def test_gaussian_count_bound_rejected(op, plan):
+    """n >= 2^29 is rejected before any device access (the tile CCL's 32-bit
+    (candidate << 2 | band) key and the survivor copy's 32-bit indices)."""
+    from paper_2605_06876_b200 import _abi
+    lib = _abi.load()
+    fake = 0x1000
+    ga = _abi.Gaussians(fake, fake, fake, fake, fake, None, 0)
+    cs = op.config_struct(golden_io.Cfg(META["step"]["blobs"]["cfg"]))
+    cams = np.ascontiguousarray(DATA["step__blobs__cams"][:1])
+    counts = _abi.Counts()
+    st = lib.adps_step_phase1_begin(plan._h, plan._stream(), C.byref(ga), 1 << 29, 1.0, C.c_void_p(fake),
+                                    C.c_void_p(fake), C.byref(cs), cams.ctypes.data_as(C.c_void_p), 1,
+                                    C.c_void_p(fake), C.c_void_p(fake), C.c_void_p(fake), C.byref(counts))
+    assert st == _abi.ADPS_INVALID_ARG
+    assert b"2^29" in lib.adps_last_error()
+    st = lib.adps_vanilla_phase1(plan._h, plan._stream(), C.byref(ga), (1 << 29) - 1 + 1, 1.0, C.c_void_p(fake),
+                                 C.c_void_p(fake), C.byref(cs), 2, C.byref(counts))
+    assert st == _abi.ADPS_INVALID_ARG
+
+
+def test_deferred_normals_need_pending_phase1(op, plan):
+    """A sync=2 normals request outside a phase 1 is refused (no stale launch)."""
+    rng = np.random.default_rng(0)
+    with pytest.raises(Exception, match="phase1_begin"):
+        plan.normals_pcg64(rng.bit_generator.state, 12, sync=2)

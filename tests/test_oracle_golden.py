@@ -173,3 +173,73 @@ def test_region_stats_horizontal_line():
     assert np.allclose(reg.centroid, [3.0, 3.0])
     assert reg.sigma1 == pytest.approx(np.sqrt(2.0)) and reg.sigma2 == 0.5
     assert np.allclose(reg.gt_rgb, [0.2, 0.4, 0.6])
+
+
+# ------------------------------------------------ next rows pinned
+def _vanilla_inputs(spec):
+    tag = spec["tag"]
+    g, extent = golden_io.scene(DATA, f"step__{tag}__in")
+    cfg = golden_io.Cfg(META["step"][tag]["cfg"])
+    return g, extent, DATA[f"step__{tag}__grad_accum"], DATA[f"step__{tag}__denom"], cfg
+
+
+@pytest.mark.parametrize("c", range(10))
+def test_vanilla_densify_matches_reference(c):
+    spec = META["vanilla"][c]
+    g, extent, ga, den, cfg = _vanilla_inputs(spec)
+    rng = np.random.default_rng(spec["seed"])
+    res = O.vanilla_densify(g, extent, ga, den, cfg, spec["n_children"], rng)
+    key = f"vanilla__{spec['tag']}__{spec['n_children']}"
+    np.testing.assert_array_equal(res.index_map, DATA[f"{key}__index_map"])
+    for f in ("mu", "scale", "rot", "opacity", "sh_dc"):
+        np.testing.assert_array_equal(getattr(res.gaussians, f), DATA[f"{key}__out__{f}"], err_msg=f)
+    want = spec["report"]
+    assert res.clones == want["clones"]
+    assert [(r.index, r.children_inserted) for r in res.candidates] == \
+        [(r["index"], r["children_inserted"]) for r in want["candidates"]]
+    st = rng.bit_generator.state
+    assert st["state"]["state"] == spec["rng_state"]["state"]["state"]
+
+
+@pytest.mark.parametrize("tag", sorted(META["step"]))
+def test_remap_stats_matches_reference(tag):
+    rep = META["step"][tag]["report"]
+    ga, den = O.remap_stats(DATA[f"step__{tag}__grad_accum"], DATA[f"step__{tag}__denom"],
+                            DATA[f"step__{tag}__index_map"], rep["reset_indices"], rep["clones"])
+    np.testing.assert_array_equal(ga, DATA[f"remap__{tag}__grad_accum"])
+    np.testing.assert_array_equal(den, DATA[f"remap__{tag}__denom"])
+
+
+@pytest.mark.parametrize("c", range(4))
+def test_accumulate_stats_matches_reference(c):
+    ga, den = DATA[f"accum__{c}__ga"].copy(), DATA[f"accum__{c}__den"].copy()
+    vg, vis = DATA[f"accum__{c}__vg"], DATA[f"accum__{c}__vis"]
+    for k in range(3):
+        O.accumulate_stats(ga, den, vg * (k + 1), vis)
+    np.testing.assert_array_equal(ga, DATA[f"accum__{c}__ga_out"])
+    np.testing.assert_array_equal(den, DATA[f"accum__{c}__den_out"])
+
+
+@pytest.mark.parametrize("c", range(5))
+def test_prune_keep_matches_reference(c):
+    spec = META["prune"][c]
+    keep = O.prune_keep(DATA[f"prune__{c}__logit"], spec["threshold"])
+    if not spec["pruned"]:
+        assert keep is None
+        return
+    np.testing.assert_array_equal(keep, DATA[f"prune__{c}__keep_index"])
+    np.testing.assert_array_equal(DATA[f"prune__{c}__m_mu_in"][keep], DATA[f"prune__{c}__m_mu_out"])
+
+
+@pytest.mark.parametrize("c", range(10))
+def test_large_merge_matches_reference(c):
+    """30-300 proposals: the oracle's prefiltered union-find vs the reference's all-pairs loop."""
+    spec = META["merge_large"][c]
+    props = [O.Proposal(mu=m, rot=r, scale=s, opacity=0.6, rgb=rgb, parent=0, view=0, area=9)
+             for m, r, s, rgb in zip(DATA[f"mergeL__{c}__mu"], DATA[f"mergeL__{c}__rot"],
+                                     DATA[f"mergeL__{c}__scale"], DATA[f"mergeL__{c}__rgb"])]
+    groups = O.merge_groups(props, spec["gamma_d"], spec["gamma_c"])
+    assert [g.members for g in groups] == spec["members"]
+    for k, g in enumerate(groups):
+        np.testing.assert_array_equal(g.mu, DATA[f"mergeL__{c}__g_mu"][k])
+        np.testing.assert_array_equal(g.cov, DATA[f"mergeL__{c}__g_cov"][k])

@@ -224,3 +224,75 @@ def _gather_worker(rank, world, port, out_dir):
             pickle.dump([p.tolist() for p in parts], f)
     finally:
         dist.destroy_process_group()
+
+
+# ------------------------------------------------ the CUDA executor across processes
+def _gpu_worker(rank, world, port, out_dir):
+    """One rank of densify_step_sharded on cuda:0 (the test box has one GPU):
+    the collectives run over gloo on host copies, the plan's kernels never wait
+    on another rank's."""
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2605_06876_b200 import operator as op
+        g, extent, cams, gts, ga, den, cfg, seed, img, dom = _gpu_inputs()
+        plan = op.Plan("cuda:0")
+        rng = np.random.default_rng(seed)
+        res = SH.densify_step_sharded(PA.to_tensors(g), extent, cams, torch.as_tensor(gts, dtype=torch.float32,
+                                                                                      device="cuda:0"),
+                                      torch.as_tensor(ga, device="cuda:0"), torch.as_tensor(den, device="cuda:0"),
+                                      cfg, rng, renders=(img.cuda(), dom.cuda()), plan=plan,
+                                      view_ids=list(range(len(cams))))
+        with open(os.path.join(out_dir, f"gpu{rank}.pkl"), "wb") as f:
+            pickle.dump((_gpu_digest(res), rng.bit_generator.state), f)
+    finally:
+        dist.destroy_process_group()
+
+
+def _gpu_inputs():
+    from paper_2605_06876_b200 import synth as S
+    from paper_2605_06876_b200.types import AdpSplitConfig
+    wl = S.Workload("sharded", 20_000, 6, 160, 112, 0.05, 0.02, 0.02 * np.sqrt(2_400_000 / 20_000),
+                    large_range=(0.005 * np.sqrt(120), 0.01 * np.sqrt(120)), seed=3)
+    ini, cams, (ga, den), gt = wl.build()
+    g = O.Gaussians(ini.mu, ini.scale, ini.rot, ini.opacity, ini.sh_dc)
+    gt_g = O.Gaussians(gt.mu, gt.scale, gt.rot, gt.opacity, gt.sh_dc)
+    from paper_2605_06876_b200 import operator as op
+    plan = op.Plan("cuda:0")
+    gts, _ = plan.render(PA.to_tensors(gt_g), cams)
+    img, dom = plan.render(PA.to_tensors(g), cams)
+    return (g, ini.extent, cams, gts.cpu().numpy(), ga, den, AdpSplitConfig(v_views=len(cams), n_max=wl.n_max), 11,
+            img.cpu(), dom.cpu())
+
+
+def _gpu_digest(res):
+    out = {k: v.cpu().numpy() for k, v in res.gaussians.numpy().items()}
+    out.update(index_map=res.index_map.cpu().numpy(), child_parent=res.child_parent.cpu().numpy(),
+               insert_offset=res.insert_offset.cpu().numpy(),
+               counts=np.array([v for k, v in sorted(res.counts.items()) if k != "n_partials"]))
+    out.update({k: v.cpu().numpy() for k, v in res.report_arrays.items()})
+    return out
+
+
+@pytest.mark.gpu
+def test_sharded_two_processes_one_gpu(tmp_path):
+    """densify_step_sharded with the CUDA executor in 2 real processes (gloo
+    collectives) equals the single-process densify_step bit for bit."""
+    from paper_2605_06876_b200 import operator as op
+    g, extent, cams, gts, ga, den, cfg, seed, img, dom = _gpu_inputs()
+    rng = np.random.default_rng(seed)
+    single = op.densify_step(PA.to_tensors(g), extent, cams, torch.as_tensor(gts, dtype=torch.float32,
+                                                                            device="cuda:0"),
+                             torch.as_tensor(ga, device="cuda:0"), torch.as_tensor(den, device="cuda:0"), cfg, rng,
+                             renders=(img.cuda(), dom.cuda()), plan=op.Plan("cuda:0"),
+                             view_ids=list(range(len(cams))))
+    want = _gpu_digest(single)
+    assert single.counts["n_regions"] > 0
+    mp.spawn(_gpu_worker, args=(2, _free_port(), str(tmp_path)), nprocs=2, join=True)
+    for r in range(2):
+        with open(tmp_path / f"gpu{r}.pkl", "rb") as f:
+            got, state = pickle.load(f)
+        for k in want:
+            np.testing.assert_array_equal(got[k], want[k], err_msg=f"rank {r}: {k}")
+        assert state == rng.bit_generator.state
