@@ -22,8 +22,10 @@ including it under "full_step".
             warp CCL (tile_bits_kernel, latency-bound) that follow.
   cpu_baseline  the oracle port on a bounded view sample (rank 0, N=1)
 
-Usage: python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-Multi-GPU: launched by torchrun, one rank per GPU.
+Usage: python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config configN]
+Multi-GPU: one rank per GPU; launched by torchrun, or bench.py re-executes
+itself under torch.distributed.run when --gpus N > 1 and WORLD_SIZE is unset
+(it exits with an error line when fewer than N GPUs are visible).
 """
 
 from __future__ import annotations
@@ -142,6 +144,13 @@ def dist_env():
     return world, rank, local
 
 
+def host_cores():
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:
+        return os.cpu_count() or 1
+
+
 def make_cfg(wl, v_views):
     from paper_2605_06876_b200.types import AdpSplitConfig
     return AdpSplitConfig(v_views=v_views, n_max=wl.n_max)
@@ -151,67 +160,94 @@ def make_cfg(wl, v_views):
 # CPU side (oracle port): cpu_baseline leg and --impl reference arm
 # ---------------------------------------------------------------------------
 
-def cpu_sample(wl, ini, cams, stats, gt_scene, view_ids, workers, renders=None, gts=None, cand_frac=1.0):
+def cpu_sample(wl, ini, cams, stats, view_ids, workers, renders, gts, cand_frac=1.0):
     from oracle import adpsplit_oracle as O
-    from oracle import c_render
     from oracle.cpu_baseline import time_sample
 
     g = O.Gaussians(ini.mu, ini.scale, ini.rot, ini.opacity, ini.sh_dc)
     cam_objs = [O.Cam.from_row(r) for r in cams]
-    if renders is None:
-        gt_g = O.Gaussians(gt_scene.mu, gt_scene.scale, gt_scene.rot, gt_scene.opacity, gt_scene.sh_dc)
-        renders, gts = {}, {}
-        for v in view_ids:
-            renders[v] = c_render.render(g, cams[v])
-            gts[v] = c_render.render(gt_g, cams[v])[0]
     cfg = make_cfg(wl, len(cams))
     return time_sample(g, ini.extent, cam_objs, view_ids, renders, gts, stats[0], stats[1], cfg,
                        n_views_total=len(cams), workers=workers, cand_frac=cand_frac)
 
 
+def _workload_stats(wl, seed):
+    """Candidates of a weighted workload need the rendered weights: on the box's GPU
+    when there is one (the same numbers as the GPU arm), else the uniform draw."""
+    if wl.stats_mode == "uniform":
+        return wl.build(seed=seed), None
+    import torch
+    if not torch.cuda.is_available():
+        raise RuntimeError(f"{wl.name}: the weighted workload needs a GPU to render its statistics")
+    from paper_2605_06876_b200 import operator as op
+    plan = op.Plan("cuda:0")
+    d = wl.build_device(plan, seed=seed)
+    out = (d["ini"], d["cams"], d["stats"], d["gt"])
+    renders = {v: (d["img"][v].double().cpu().numpy(), d["dom"][v].long().cpu().numpy())
+               for v in range(min(len(d["cams"]), 64))}
+    gts = {v: d["gt_img"][v].double().cpu().numpy() for v in renders}
+    del d, plan
+    torch.cuda.empty_cache()
+    return out, (renders, gts)
+
+
 def run_reference(args, wl):
-    """--impl reference: the oracle port on the box's host cores (rank 0 only)."""
+    """--impl reference: the oracle port on the box's host cores (rank 0 only).
+
+    Each step is a bounded sample of the config's step: all per-view stages on
+    k of the V sampled views (fanned out over worker processes), the merges of
+    the sampled parents, select and compaction; its measured wall time is
+    ms_per_step, and value = |split set| / (the sample extrapolated linearly in
+    V to the full step), a lower bound on the CPU time since the merge grows
+    faster than linearly in V."""
     world, rank, _ = dist_env()
     if world > 1 and rank != 0:
         return
-    import multiprocessing as mp
-
-    from oracle import c_render
-    from oracle import adpsplit_oracle as O
-
-    c_render.build()
-    ini, cams, stats, gt_scene = wl.build()
-    cores = os.cpu_count() or 1
-    k = max(1, min(cores, args.ref_views))
-    # inputs for all k views (untimed preparation), rendered by the C oracle in parallel
-    g = O.Gaussians(ini.mu, ini.scale, ini.rot, ini.opacity, ini.sh_dc)
-    gt_g = O.Gaussians(gt_scene.mu, gt_scene.scale, gt_scene.rot, gt_scene.opacity, gt_scene.sh_dc)
-    _PREP.update(g=g, gt=gt_g, cams=cams)
+    (ini, cams, stats, gt_scene), attr = _workload_stats(wl, args.seed)
+    cores = host_cores()
+    k = max(1, min(cores, args.ref_views, len(cams)))
     views = list(range(k))
-    with mp.get_context("fork").Pool(min(k, cores)) as pool:
-        outs = pool.map(_prep_view, views)
-    renders = {v: (img, dom) for v, img, dom, _ in outs}
-    gts = {v: gt for v, _, _, gt in outs}
-    times = []
+    if attr is not None:
+        renders = {v: attr[0][v] for v in views}
+        gts = {v: attr[1][v] for v in views}
+    else:
+        import multiprocessing as mp
+
+        from oracle import adpsplit_oracle as O
+        from oracle import c_render
+        c_render.build()
+        g = O.Gaussians(ini.mu, ini.scale, ini.rot, ini.opacity, ini.sh_dc)
+        gt_g = O.Gaussians(gt_scene.mu, gt_scene.scale, gt_scene.rot, gt_scene.opacity, gt_scene.sh_dc)
+        _PREP.update(g=g, gt=gt_g, cams=cams)
+        with mp.get_context("fork").Pool(min(k, cores)) as pool:
+            outs = pool.map(_prep_view, views)
+        renders = {v: (img, dom) for v, img, dom, _ in outs}
+        gts = {v: gt for v, _, _, gt in outs}
+    walls, ests = [], []
     info = None
     for it in range(args.warmup + args.steps):
-        info = cpu_sample(wl, ini, cams, stats, gt_scene, views, workers=min(k, cores), renders=renders, gts=gts,
+        t0 = time.perf_counter()
+        info = cpu_sample(wl, ini, cams, stats, views, workers=min(k, cores), renders=renders, gts=gts,
                           cand_frac=args.ref_cand_frac)
         if it >= args.warmup:
-            times.append(info["extrapolated_step_s"])
-    t = float(np.mean(times))
-    value = info["n_split"] / t
-    sample = (f"oracle port: {k} of {len(cams)} views per step ({min(k, cores)} worker processes), "
-              f"per-view stages timed on all parents, merge/cap/emit on every "
-              f"{int(round(1 / args.ref_cand_frac))}th parent with proposals "
-              f"({info['parents_merged']} of {info['parents_with_proposals']}), extrapolated linearly "
-              f"to all parents and to V={len(cams)}; {info['n_regions']} regions, "
+            walls.append(time.perf_counter() - t0)
+            ests.append(info["extrapolated_step_s"])
+    t_full = float(np.mean(ests))
+    value = info["n_split"] / t_full
+    workers = min(k, cores)
+    sample = (f"oracle port (numpy): {k} of {len(cams)} views per step on {workers} worker processes "
+              f"({workers} of {cores} host cores), merge/cap/emit on {info['parents_merged']} of "
+              f"{info['parents_with_proposals']} parents with proposals; measured sample wall "
+              f"{np.mean(walls):.2f} s/step (= ms_per_step), extrapolated linearly to all parents and "
+              f"V={len(cams)}: {t_full:.2f} s per full step (value = |S| / that; a lower bound on CPU time, "
+              f"merges grow faster than linearly in V); {info['n_regions']} regions, "
               f"{info['n_proposals']} proposals in the sample")
     line = {"metric": METRIC, "value": value, "unit": UNIT, "impl": "reference", "n_gpus": world,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": float(np.mean(walls)) * 1e3,
+            "extrapolated_ms_per_full_step": t_full * 1e3, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": config_dict(wl, args),
-            "cpu_baseline": {"value": value, "unit": UNIT, "cores": min(k, cores), "kind": "port",
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": workers, "host_cores": cores, "kind": "port",
                              "sample": sample, "stages_s": info["stages_s"]},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
@@ -227,17 +263,85 @@ def _prep_view(v):
     return v, img, dom, gt
 
 
-def config_dict(wl, args):
-    return {"workload": f"{wl.name}: bonsai-shaped synthetic {wl.n_gt // 2:,}-Gaussian init "
-                        f"({wl.n_gt:,}-Gaussian GT), {wl.n_views} views {wl.width}x{wl.height}, full densify step",
-            "n_gaussians": wl.n_gt // 2 + 1, "views": wl.n_views, "width": wl.width, "height": wl.height,
-            "v_views": wl.n_views, "n_max": wl.n_max, "cfg": "paper defaults (ref/scene.py:151-163)",
-            "l2": "inputs larger than L2 (image+gt+dominant = 28 B/px x V x H x W)"}
+def config_dict(wl, args, extra=None):
+    d = {"workload": f"{wl.name}: slab-shaped synthetic {wl.n_gt // 2:,}-Gaussian init "
+                     f"({wl.n_gt:,}-Gaussian GT), {wl.n_views} views {wl.width}x{wl.height}, full densify step",
+         "n_gaussians": wl.n_gt // 2 + 1, "views": wl.n_views, "width": wl.width, "height": wl.height,
+         "v_views": wl.n_views, "n_max": wl.n_max, "cfg": "paper defaults (ref/scene.py:151-163)",
+         "rho": wl.rho, "stats": wl.stats_mode, "p_split": wl.p_split, "p_clone": wl.p_clone,
+         "l2": "inputs larger than L2 (image+gt+dominant = 28 B/px x V x H x W)"}
+    if extra:
+        d.update(extra)
+    return d
 
 
 # ---------------------------------------------------------------------------
 # GPU arm
 # ---------------------------------------------------------------------------
+
+def time_accumulate(dev, n, peak, launches=10):
+    """accumulate_stats (ref/adc.py:73-79) on n Gaussians, one launch per view with
+    fp32 viewspace gradients (a GPU rasterizer's): 41 B per Gaussian per view
+    (vg 8 + visible 1 + grad_accum/denom read+write 32).  L2 is flushed before
+    every launch; each launch is timed with events on the launching stream."""
+    import torch
+
+    from paper_2605_06876_b200 import operator as op
+    gen = torch.Generator(device=dev).manual_seed(0)
+    ga = torch.zeros(n, dtype=torch.float64, device=dev)
+    den = torch.zeros(n, dtype=torch.float64, device=dev)
+    vg = torch.randn(n, 2, device=dev, generator=gen)
+    vis = torch.rand(n, device=dev, generator=gen) < 0.7
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(launches)]
+    op.accumulate_stats_(ga, den, vg, vis)
+    for e0, e1 in evs:
+        flush.zero_()
+        e0.record()
+        op.accumulate_stats_(ga, den, vg, vis)
+        e1.record()
+    torch.cuda.synchronize(dev)
+    ms = float(np.mean([e0.elapsed_time(e1) for e0, e1 in evs]))
+    gbs = 41.0 * n / (ms * 1e-3) / 1e9
+    return {"GB/s": gbs, "frac": gbs / peak, "ms_per_launch": ms, "n": n, "bytes_per_gaussian": 41,
+            "note": "one launch per view, fp32 viewspace grads, L2 flushed before each launch"}
+
+
+def parity_on_sample(op, plan, wl, d, vs, cfg_k):
+    """The GPU step and the oracle step on the same k sampled views (stage-isolated:
+    the same GPU attribution into both); every integer output compared, near-
+    threshold candidates reported (tests/parity.py)."""
+    import torch
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    import parity as PA
+    from oracle import adpsplit_oracle as O
+    ini, cams = d["ini"], d["cams"]
+    ga, den = d["stats"]
+    cams_k = cams[vs]
+    rng_seed = 0
+    # the k cameras are the step's camera list and v_views = k: both sides sample all
+    # of them with the same Generator call (ref/adc.py:161), then draw the same normals
+    gres = op.densify_step(d["g"], ini.extent, cams_k, d["gt_img"][vs[0]:vs[-1] + 1],
+                           torch.as_tensor(ga, device=plan.device), torch.as_tensor(den, device=plan.device), cfg_k,
+                           np.random.default_rng(rng_seed),
+                           renders=(d["img"][vs[0]:vs[-1] + 1], d["dom"][vs[0]:vs[-1] + 1]), plan=plan)
+    g = O.Gaussians(ini.mu, ini.scale, ini.rot, ini.opacity, ini.sh_dc)
+    cam_objs = [O.Cam.from_row(r) for r in cams_k]
+    renders = {k: (d["img"][v].double().cpu().numpy(), d["dom"][v].long().cpu().numpy()) for k, v in enumerate(vs)}
+    gts = {k: d["gt_img"][v].double().cpu().numpy() for k, v in enumerate(vs)}
+    t0 = time.perf_counter()
+    ores = O.adpsplit_step(g, ini.extent, cam_objs, gts, ga, den, cfg_k, np.random.default_rng(rng_seed),
+                           renders=renders)
+    np.testing.assert_array_equal(PA.gpu_regions(plan), PA.oracle_regions(ores, list(range(len(vs)))))
+    flagged = PA.flag_candidates(ores, g, cam_objs, cfg_k)
+    st = PA.compare_step(gres, ores, flagged, g)
+    return {"views": [int(v) for v in vs], "candidates": st["candidates"], "mismatched": st["mismatched"],
+            "flagged": st["flagged"], "regions": int(gres.counts["n_regions"]),
+            "rows_compared": st["rows_compared"], "max_rel_cov": st["max_rel_cov"],
+            "max_rel_mu": st["max_rel_mu"], "oracle_s": time.perf_counter() - t0,
+            "checked": "regions, cases, regions_per_view, proposals, N_i, merge_edges, clones, resets, "
+                       "index_map, child_parent, insert offsets exact; child params within tolerance"}
+
 
 def run_ours(args, wl):
     import torch
@@ -246,6 +350,8 @@ def run_ours(args, wl):
     from paper_2605_06876_b200 import operator as op
 
     world, rank, local = dist_env()
+    if world != args.gpus:
+        raise SystemExit(f"bench.py --gpus {args.gpus} but WORLD_SIZE={world}")
     if world > 1:
         torch.cuda.set_device(local)
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
@@ -255,13 +361,11 @@ def run_ours(args, wl):
     clocks.start()
     plan = op.Plan(dev)
 
-    # ---- workload (seeded numpy), GT images rendered by the operator's own render
+    # ---- workload (seeded numpy scenes; GT images, attribution and statistics rendered on the device)
     t0 = time.time()
-    ini, cams, stats, gt_scene = wl.build(seed=args.seed + (rank if args.replicas else 0))
-    g = op.GaussianTensors.from_numpy(*ini.arrays(), device=dev)
-    gt_g = op.GaussianTensors.from_numpy(*gt_scene.arrays(), device=dev)
-    gt_img, _ = plan.render(gt_g, cams)
-    del gt_g
+    d = wl.build_device(plan, seed=args.seed + (rank if args.replicas else 0))
+    ini, cams, stats = d["ini"], d["cams"], d["stats"]
+    g, gt_img = d["g"], d["gt_img"]
     ga = torch.as_tensor(stats[0], device=dev)
     den = torch.as_tensor(stats[1], device=dev)
     cfg = make_cfg(wl, len(cams))
@@ -271,7 +375,7 @@ def run_ours(args, wl):
 
     # ---- attribution render of the sampled views (reported separately)
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    img, dom = plan.render(g, cams[view_ids])
+    img, dom = d["img"], d["dom"]
     torch.cuda.synchronize()
     ev0.record()
     img, dom = plan.render(g, cams[view_ids], out=(img, dom))
@@ -282,14 +386,21 @@ def run_ours(args, wl):
     sharded = world > 1 and not args.replicas
     if sharded:
         from paper_2605_06876_b200 import sharded as SH
-        step_fn = SH.densify_step_sharded   # views sharded over ranks, records gathered
+        lo, hi = SH.view_block(len(view_ids), world, rank)
+
+        def step_fn(gg, gt_, ga_, den_, rng, renders):
+            return SH.densify_step_sharded(gg, ini.extent, cams, gt_, ga_, den_, cfg, rng, renders=renders,
+                                           plan=plan, view_ids=view_ids, want_report=True, local_views=True)
+        # each rank holds (and, e2e, copies in) only its own block of views
+        img_l, dom_l, gt_l = img[lo:hi], dom[lo:hi], gt_img[lo:hi]
     else:
-        step_fn = op.densify_step
+        def step_fn(gg, gt_, ga_, den_, rng, renders):
+            return op.densify_step(gg, ini.extent, cams, gt_, ga_, den_, cfg, rng, renders=renders, plan=plan,
+                                   view_ids=view_ids, want_report=True)
+        img_l, dom_l, gt_l = img, dom, gt_img
 
     def step():
-        rng = np.random.default_rng((args.seed, 0))
-        return step_fn(g, ini.extent, cams, gt_img, ga, den, cfg, rng, renders=(img, dom),
-                       plan=plan, view_ids=view_ids, want_report=True)
+        return step_fn(g, gt_l, ga, den, np.random.default_rng((args.seed, 0)), (img_l, dom_l))
 
     for _ in range(max(args.warmup, 1)):
         res = step()
@@ -320,17 +431,23 @@ def run_ours(args, wl):
     props_stats = {"max": int(pp.max()) if len(pp) else 0, "p99": float(np.percentile(pp, 99)) if len(pp) else 0,
                    "mean": float(pp.mean()) if len(pp) else 0, "over_96": int((pp > 96).sum()),
                    "total": int(pp.sum())}
+    ns = max(n_split, 1)
+    shares = {"split_candidates": n_split, "clone_candidates": counts["n_clone"],
+              "adaptive": (n_split - counts["n_fallback"] - counts["n_reset"]) / ns,
+              "fallback": counts["n_fallback"] / ns, "reset": counts["n_reset"] / ns}
 
-    # ---- per-stage breakdown with CUDA events on the launching stream
-    plan.set_timing(True)
-    stage_acc = {}
-    n_t = max(3, min(args.steps, 10))
-    for _ in range(n_t):
-        step()
-        for k_, v_ in plan.stage_ms().items():
-            stage_acc[k_] = stage_acc.get(k_, 0.0) + v_
-    plan.set_timing(False)
-    stages = {k_: v_ / n_t for k_, v_ in stage_acc.items()}
+    # ---- per-stage breakdown with CUDA events on the launching stream (1 GPU)
+    stages = {}
+    if world == 1:
+        plan.set_timing(True)
+        stage_acc = {}
+        n_t = max(3, min(args.steps, 10))
+        for _ in range(n_t):
+            step()
+            for k_, v_ in plan.stage_ms().items():
+                stage_acc[k_] = stage_acc.get(k_, 0.0) + v_
+        plan.set_timing(False)
+        stages = {k_: v_ / n_t for k_, v_ in stage_acc.items()}
 
     V, H, W = len(view_ids), wl.height, wl.width
     px = V * H * W
@@ -339,29 +456,29 @@ def run_ours(args, wl):
     mm_ms = stages.get("minmax", float("nan"))
     # stat-accum: 28 B/px over the attribution stages (maps, partition, stats)
     attr_ms = sum(stages.get(k_, 0) for k_ in ("minmax", "thresholds", "tile_ccl", "border_merge"))
-    achieved = BYTES_PER_PX * px / (mm_ms * 1e-3) / 1e9
+    achieved = BYTES_PER_PX * px / (mm_ms * 1e-3) / 1e9 if stages else None
     traffic = load_traffic(wl.name)
     b_step = BYTES_PER_PX * px + BYTES_PER_G_IN * g.n + BYTES_PER_G_OUT * counts["n_out"]
+    acc = time_accumulate(dev, g.n, peak) if rank == 0 else None
 
     # ---- e2e: same step through the API from pinned host buffers
     e2e = None
     if not args.no_e2e:
         host = {k_: t_.cpu().pin_memory() for k_, t_ in
                 dict(mu=g.mu, scale=g.scale, rot=g.rot, opacity=g.opacity, sh_dc=g.sh_dc, ga=ga, den=den,
-                     img=img, gt=gt_img, dom=dom).items()}
+                     img=img_l, gt=gt_l, dom=dom_l).items()}
         h2d = sum(t_.numel() * t_.element_size() for t_ in host.values())
         n_out = counts["n_out"]
-        out_h = {k_: torch.empty((n_out,) + tuple(s), dtype=torch.float32).pin_memory()
-                 for k_, s in dict(mu=(3,), scale=(3,), rot=(4,), opacity=(), sh_dc=(3,)).items()}
+        out_h = {k_: torch.empty((n_out,) + tuple(s_), dtype=torch.float32).pin_memory()
+                 for k_, s_ in dict(mu=(3,), scale=(3,), rot=(4,), opacity=(), sh_dc=(3,)).items()}
         im_h = torch.empty(n_out, dtype=torch.int64).pin_memory()
         d2h = sum(t_.numel() * t_.element_size() for t_ in out_h.values()) + im_h.numel() * 8
 
         def e2e_step():
-            d = {k_: t_.to(dev, non_blocking=True) for k_, t_ in host.items()}
-            gg = op.GaussianTensors(d["mu"], d["scale"], d["rot"], d["opacity"], d["sh_dc"])
-            r = step_fn(gg, ini.extent, cams, d["gt"], d["ga"], d["den"], cfg,
-                        np.random.default_rng((args.seed, 0)), renders=(d["img"], d["dom"]), plan=plan,
-                        view_ids=view_ids, want_report=True)
+            dd = {k_: t_.to(dev, non_blocking=True) for k_, t_ in host.items()}
+            gg = op.GaussianTensors(dd["mu"], dd["scale"], dd["rot"], dd["opacity"], dd["sh_dc"])
+            r = step_fn(gg, dd["gt"], dd["ga"], dd["den"], np.random.default_rng((args.seed, 0)),
+                        (dd["img"], dd["dom"]))
             for k_ in out_h:
                 out_h[k_].copy_(getattr(r.gaussians, k_), non_blocking=True)
             im_h.copy_(r.index_map, non_blocking=True)
@@ -370,6 +487,8 @@ def run_ours(args, wl):
         for _ in range(2):
             e2e_step()
         torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
         n_e = max(2, min(args.steps, 5))
         ev0.record()
         for _ in range(n_e):
@@ -377,8 +496,14 @@ def run_ours(args, wl):
         ev1.record()
         torch.cuda.synchronize()
         e2e_ms = ev0.elapsed_time(ev1) / n_e
+        if world > 1:
+            t = torch.tensor([e2e_ms], device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            e2e_ms = float(t.item())
         e2e = {"value": n_split / (e2e_ms * 1e-3), "unit": UNIT, "ms_per_step": e2e_ms,
-               "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h)}
+               "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+               "note": "per rank: params + stats + its own block of views in, grown params + index_map out"
+                       if world > 1 else "params + stats + all views in, grown params + index_map out"}
         del host
 
     # ---- full step incl. the attribution render
@@ -386,37 +511,44 @@ def run_ours(args, wl):
     clocks.stop()
     clk = clocks.summary()
 
-    # ---- CPU baseline (rank 0, N = 1): oracle port on GPU-produced inputs of k views
-    cpu = None
+    # ---- CPU baseline + parity on the same sample (rank 0, N = 1)
+    cpu, parity = None, None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         k = max(1, args.cpu_views)
         vs = view_ids[:k]
         renders = {v: (img[v].double().cpu().numpy(), dom[v].long().cpu().numpy()) for v in vs}
         gts = {v: gt_img[v].double().cpu().numpy() for v in vs}
-        info = cpu_sample(wl, ini, cams, stats, gt_scene, vs, workers=1, renders=renders, gts=gts,
+        info = cpu_sample(wl, ini, cams, stats, vs, workers=1, renders=renders, gts=gts,
                           cand_frac=args.cpu_cand_frac)
-        cpu = {"value": info["n_split"] / info["extrapolated_step_s"], "unit": UNIT, "cores": 1, "kind": "port",
-               "sample": (f"oracle port (numpy, 1 thread) on {k} of {V} views of the same step inputs, "
-                          f"merge/cap/emit on {info['parents_merged']} of {info['parents_with_proposals']} "
-                          f"parents with proposals; per-view + per-parent stages timed and extrapolated "
-                          f"linearly to all parents and V={V} "
-                          f"(sample wall {info['sample_wall_s']:.1f} s; host has {os.cpu_count()} cores)"),
+        cpu = {"value": info["n_split"] / info["extrapolated_step_s"], "unit": UNIT, "cores": 1,
+               "host_cores": host_cores(), "kind": "port",
+               "sample": (f"oracle port (numpy, 1 of {host_cores()} host cores) on {k} of {V} views of the "
+                          f"same step inputs, merge/cap/emit on {info['parents_merged']} of "
+                          f"{info['parents_with_proposals']} parents with proposals; per-view + per-parent "
+                          f"stages timed and extrapolated linearly to all parents and V={V} "
+                          f"(sample wall {info['sample_wall_s']:.1f} s)"),
                "step_s_extrapolated": info["extrapolated_step_s"], "stages_s": info["stages_s"]}
+        if not args.no_parity:
+            parity = parity_on_sample(op, plan, wl, d, vs, make_cfg(wl, k))
 
     if rank == 0:
+        extra = {"dc_gt": d["dc_gt"], "dc_init": d["dc_init"], "shares": shares}
         line = {
             "metric": METRIC, "value": n_split * world / (ms * 1e-3) if args.replicas else n_split / (ms * 1e-3),
             "unit": UNIT, "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
             "higher_is_better": True, "scaling": "weak" if args.replicas else "strong", "vs_baseline": None,
-            "dtype": "f64+i64 (decisions), fp32 (params)", "data": "synthetic", "config": config_dict(wl, args),
+            "dtype": "f64+i64 (decisions), fp32 (params)", "data": "synthetic",
+            "config": config_dict(wl, args, extra),
             "densify_step_ms": ms,
-            "stat_accum": {"GB/s": BYTES_PER_PX * px / (attr_ms * 1e-3) / 1e9, "frac": None, "ms": attr_ms},
+            "stat_accum": {"GB/s": BYTES_PER_PX * px / (attr_ms * 1e-3) / 1e9 if attr_ms else None,
+                           "frac": None, "ms": attr_ms},
+            "accumulate_stats": acc,
             "step_roofline": {"bytes": int(b_step), "GB/s": b_step / (ms * 1e-3) / 1e9,
                               "frac": b_step / (ms * 1e-3) / 1e9 / peak},
-            "roofline": {"bound": "hbm", "kernel": "minmax_kernel (input pass: raw L1 error, per-view min/max, "
+            "roofline": {"bound": "hbm", "kernel": "minmax2_kernel (input pass: raw L1 error, per-view min/max, "
                                                     "ever-dominant flags, candidate bits, fp32 raw cache)",
                          "achieved": achieved, "peak": peak, "peak_kind": peak_kind, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": traffic,
+                         "frac": achieved / peak if achieved else None, "traffic": traffic,
                          "algorithmic_bytes_per_launch": BYTES_PER_PX * px, "ms_per_launch": mm_ms,
                          "note": "achieved counts the 28 B/px inputs only; traffic = ncu dram read+write of one "
                                  "launch (incl. the 4.125 B/px cache it writes), profiles/"},
@@ -424,7 +556,9 @@ def run_ours(args, wl):
                           "words_bytes_per_launch": WORDS_BYTES_PER_PX * px},
             "stages_ms": stages,
             "render": {"ms_per_view": render_ms / V, "ms_total": render_ms, "views": V,
-                       "note": "attribution render (compute-bound), not part of value"},
+                       "splat_px_per_s": d["dc_init"] * px / (render_ms * 1e-3),
+                       "note": "attribution render (compute-bound), not part of value; splat-px = (pixel, splat) "
+                               "pairs with alpha >= 1/255 (measured depth complexity x pixels)"},
             "full_step": {"ms": full_ms, "parents_per_s": n_split / (full_ms * 1e-3)},
             "counts": counts,
             "proposals_per_parent": props_stats,
@@ -433,13 +567,35 @@ def run_ours(args, wl):
             "library_sort_calls_per_step": (l1 - l0) / args.steps,
             "clocks": clk,
             "cpu_baseline": cpu,
+            "parity": parity,
             "setup_s": setup_s,
         }
-        line["stat_accum"]["frac"] = line["stat_accum"]["GB/s"] / peak
+        if line["stat_accum"]["GB/s"]:
+            line["stat_accum"]["frac"] = line["stat_accum"]["GB/s"] / peak
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
+
+
+def _free_port():
+    import socket
+    with socket.socket() as s_:
+        s_.bind(("127.0.0.1", 0))
+        return s_.getsockname()[1]
+
+
+def _spawn_ranks(args):
+    """--gpus N without torchrun: re-exec under torch.distributed.run, one rank per GPU."""
+    import torch
+    have = torch.cuda.device_count()
+    if have < args.gpus:
+        print(json.dumps({"metric": METRIC, "error": f"--gpus {args.gpus} but only {have} GPU(s) visible"}),
+              flush=True)
+        raise SystemExit(2)
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={_free_port()}", os.path.abspath(__file__)] + sys.argv[1:]
+    os.execv(sys.executable, cmd)
 
 
 def main():
@@ -452,10 +608,11 @@ def main():
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--cpu-views", type=int, default=2)
     ap.add_argument("--ref-views", type=int, default=8)
-    ap.add_argument("--ref-cand-frac", type=float, default=0.125)
-    ap.add_argument("--cpu-cand-frac", type=float, default=0.5)
+    ap.add_argument("--ref-cand-frac", type=float, default=1.0)
+    ap.add_argument("--cpu-cand-frac", type=float, default=1.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-parity", action="store_true", help="skip the oracle parity check on the cpu sample")
     ap.add_argument("--replicas", action="store_true",
                     help="N>1: independent replicas (weak scaling) instead of the view-sharded step")
     args = ap.parse_args()
@@ -463,8 +620,10 @@ def main():
     wl = CONFIGS[args.config]
     if args.impl == "reference":
         run_reference(args, wl)
-    else:
-        run_ours(args, wl)
+        return
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        _spawn_ranks(args)
+    run_ours(args, wl)
 
 
 if __name__ == "__main__":

@@ -193,7 +193,7 @@ class GpuExecutor:
 
     def __init__(self, g: op.GaussianTensors, extent: float, cameras, gt, grad_accum, denom, cfg, rng, *,
                  renders=None, plan: op.Plan = None, view_ids=None, want_report: bool = True,
-                 world: int = 1, rank: int = 0, parent_shard: bool = True):
+                 world: int = 1, rank: int = 0, parent_shard: bool = True, local_views: bool = False):
         self.plan = plan or op.default_plan(g.device)
         self.g, self.extent, self.cfg, self.rng = g, extent, cfg, rng
         self.cams = op.camera_rows(cameras)
@@ -204,6 +204,7 @@ class GpuExecutor:
         self.den = denom.to(self.plan.device, op.F64).contiguous()
         self.want_report, self.world, self.rank = want_report, world, rank
         self.parent_sharded = bool(parent_shard) and world > 1
+        self.local_views = bool(local_views)   # renders / gt hold only this rank's view block
         self.counts = None
         self.normals = None
 
@@ -217,10 +218,18 @@ class GpuExecutor:
             raise ValueError("view shards must be contiguous blocks of sampled-view positions")
         if self.renders is None:
             image, dom = P.render(self.g, cams_v)
+        elif self.local_views:
+            image = self.renders[0].to(dev, op.F32).contiguous()
+            dom = self.renders[1].to(dev, torch.int32).contiguous()
         else:   # zero-copy slices of the [V,...] attribution of all sampled views
             image = self.renders[0].to(dev, op.F32)[lo:hi].contiguous()
             dom = self.renders[1].to(dev, torch.int32)[lo:hi].contiguous()
-        gt_v = op._gather_views(self.gt, vids, dev)
+        if self.local_views:
+            gt_v = self.gt.to(dev, op.F32).contiguous()
+            if image.shape[0] != hi - lo or gt_v.shape[0] != hi - lo:
+                raise ValueError(f"local_views: expected the {hi - lo} views of this rank's block")
+        else:
+            gt_v = op._gather_views(self.gt, vids, dev)
         self._keep = (image, dom, gt_v)
         P.set_view_sharding(lo, 1, len(self.view_ids))
         P.set_parent_sharding(self.rank, self.world) if self.parent_sharded else P.set_parent_sharding(0, 1)
@@ -293,20 +302,22 @@ class GpuExecutor:
 
 def densify_step_sharded(g: op.GaussianTensors, extent: float, cameras, gt, grad_accum, denom, cfg, rng, *,
                          renders=None, plan: op.Plan = None, view_ids=None, want_report: bool = True,
-                         group=None) -> op.StepResult:
+                         group=None, local_views: bool = False) -> op.StepResult:
     """op.densify_step over all ranks of `group` (one GPU each); identical result on every rank.
 
     Every rank passes the same arguments (same Generator state, same sampled
     views; `renders`, if given, are the attribution of ALL sampled views, of
-    which each rank reads only its own).  With world size 1 this is
-    op.densify_step.
+    which each rank reads only its own block).  With ``local_views`` the
+    renders and gt hold only this rank's block of sampled views
+    (view_block(V, world, rank)), so a rank never stages the others' pixels.
+    With world size 1 this is op.densify_step.
     """
     if not dist.is_initialized() or dist.get_world_size(group) == 1:
         return op.densify_step(g, extent, cameras, gt, grad_accum, denom, cfg, rng, renders=renders, plan=plan,
                                view_ids=view_ids, want_report=want_report)
     ex = GpuExecutor(g, extent, cameras, gt, grad_accum, denom, cfg, rng, renders=renders, plan=plan,
                      view_ids=view_ids, want_report=want_report, world=dist.get_world_size(group),
-                     rank=dist.get_rank(group))
+                     rank=dist.get_rank(group), local_views=local_views)
     return run_sharded(ex, len(ex.view_ids), group)
 
 

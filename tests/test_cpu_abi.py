@@ -83,7 +83,8 @@ def test_fallback_normals_are_chunk_invariant():
 
 def test_synthetic_workload_counts():
     from paper_2605_06876_b200 import synth as S
-    ini, cams, (ga, den), gt = S.CONFIGS["config2"].build()
+    import dataclasses
+    ini, cams, (ga, den), gt = dataclasses.replace(S.CONFIGS["config2"], stats_mode="uniform").build()
     assert ini.n == S.CONFIGS["config2"].n_gt // 2 + 1 and cams.shape == (16, 18)
     split = (ga / den >= 2e-4) & (ini.scale.max(1) > 0.01 * ini.extent)
     assert abs(split.sum() - 0.05 * ini.n) < 2

@@ -470,11 +470,10 @@ def test_determinism_at_scale(op, cfg_name):
     from paper_2605_06876_b200 import synth as S
     from paper_2605_06876_b200.types import AdpSplitConfig
     wl = S.CONFIGS[cfg_name]
-    ini, cams, (ga, den), gt = wl.build()
     plan = op.Plan("cuda:0")
-    g = op.GaussianTensors.from_numpy(*ini.arrays(), device="cuda")
-    gt_img, _ = plan.render(op.GaussianTensors.from_numpy(*gt.arrays(), device="cuda"), cams)
-    img, dom = plan.render(g, cams)
+    d = wl.build_device(plan)
+    ini, cams, (ga, den) = d["ini"], d["cams"], d["stats"]
+    g, gt_img, img, dom = d["g"], d["gt_img"], d["img"], d["dom"]
     cfg = AdpSplitConfig(v_views=len(cams), n_max=wl.n_max)
     digests = []
     for path, raw in ((0, 1), (0, 1), (1, 1), (0, 0), (2, 1)):   # block CCL / recomputed raw / no bit planes: same bits
@@ -511,11 +510,10 @@ def test_sharded_lockstep_matches_single_gpu(op, world, parent_shard):
     from paper_2605_06876_b200 import synth as S
     from paper_2605_06876_b200.types import AdpSplitConfig
     wl = S.CONFIGS["config2"]
-    ini, cams, (ga, den), gt = wl.build()
     base = op.Plan("cuda:0")
-    g = op.GaussianTensors.from_numpy(*ini.arrays(), device="cuda")
-    gt_img, _ = base.render(op.GaussianTensors.from_numpy(*gt.arrays(), device="cuda"), cams)
-    img, dom = base.render(g, cams)
+    d = wl.build_device(base)
+    ini, cams, (ga, den) = d["ini"], d["cams"], d["stats"]
+    g, gt_img, img, dom = d["g"], d["gt_img"], d["img"], d["dom"]
     cfg = AdpSplitConfig(v_views=len(cams), n_max=wl.n_max)
     vids = list(range(len(cams)))
     ga_t, den_t = torch.as_tensor(ga, device="cuda"), torch.as_tensor(den, device="cuda")

@@ -267,7 +267,7 @@ def _gpu_inputs():
 
 
 def _gpu_digest(res):
-    out = {k: v.cpu().numpy() for k, v in res.gaussians.numpy().items()}
+    out = dict(res.gaussians.numpy())
     out.update(index_map=res.index_map.cpu().numpy(), child_parent=res.child_parent.cpu().numpy(),
                insert_offset=res.insert_offset.cpu().numpy(),
                counts=np.array([v for k, v in sorted(res.counts.items()) if k != "n_partials"]))

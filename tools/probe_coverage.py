@@ -4,10 +4,10 @@ sys.path.insert(0, os.getcwd())
 from paper_2605_06876_b200 import operator as op, synth as S
 from paper_2605_06876_b200.types import AdpSplitConfig
 wl = S.CONFIGS["config3"]
-ini, cams, (ga, den), gt = wl.build()
 plan = op.Plan("cuda:0")
-g = op.GaussianTensors.from_numpy(*ini.arrays(), device="cuda")
-img, dom = plan.render(g, cams)
+_d = wl.build_device(plan)
+ini, cams, (ga, den) = _d["ini"], _d["cams"], _d["stats"]
+g, img, dom = _d["g"], _d["img"], _d["dom"]
 cfg = AdpSplitConfig(v_views=len(cams), n_max=wl.n_max)
 arr = ini.arrays()
 scale = np.asarray(arr[1]).reshape(-1, 3)

@@ -17,11 +17,10 @@ from paper_2605_06876_b200.types import AdpSplitConfig  # noqa: E402
 args = [a for a in sys.argv[1:] if not a.startswith("--")]
 name = args[0] if args else "config3"
 wl = S.CONFIGS[name]
-ini, cams, (ga, den), gt = wl.build()
 plan = op.Plan("cuda:0")
-g = op.GaussianTensors.from_numpy(*ini.arrays(), device="cuda")
-gt_img, _ = plan.render(op.GaussianTensors.from_numpy(*gt.arrays(), device="cuda"), cams)
-img, dom = plan.render(g, cams)
+_d = wl.build_device(plan)
+ini, cams, (ga, den) = _d["ini"], _d["cams"], _d["stats"]
+g, gt_img, img, dom = _d["g"], _d["gt_img"], _d["img"], _d["dom"]
 cfg = AdpSplitConfig(v_views=len(cams), n_max=wl.n_max)
 ga_t, den_t = torch.as_tensor(ga, device="cuda"), torch.as_tensor(den, device="cuda")
 if "--timing" in sys.argv:   # stage-timing mode: one tile launch over all views (no pipelining), as bench's breakdown

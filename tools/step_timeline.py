@@ -18,11 +18,10 @@ from paper_2605_06876_b200 import synth as S  # noqa: E402
 from paper_2605_06876_b200.types import AdpSplitConfig  # noqa: E402
 
 wl = S.CONFIGS[sys.argv[1] if len(sys.argv) > 1 else "config3"]
-ini, cams, (ga, den), gt = wl.build()
 plan = op.Plan("cuda:0")
-g = op.GaussianTensors.from_numpy(*ini.arrays(), device="cuda")
-gt_img, _ = plan.render(op.GaussianTensors.from_numpy(*gt.arrays(), device="cuda"), cams)
-img, dom = plan.render(g, cams)
+_d = wl.build_device(plan)
+ini, cams, (ga, den) = _d["ini"], _d["cams"], _d["stats"]
+g, gt_img, img, dom = _d["g"], _d["gt_img"], _d["img"], _d["dom"]
 ga_t, den_t = torch.as_tensor(ga, device="cuda"), torch.as_tensor(den, device="cuda")
 cfg = AdpSplitConfig(v_views=len(cams), n_max=wl.n_max)
 marks = []
