@@ -87,7 +87,15 @@ def test_synthetic_workload_counts():
     ini, cams, (ga, den), gt = dataclasses.replace(S.CONFIGS["config2"], stats_mode="uniform").build()
     assert ini.n == S.CONFIGS["config2"].n_gt // 2 + 1 and cams.shape == (16, 18)
     split = (ga / den >= 2e-4) & (ini.scale.max(1) > 0.01 * ini.extent)
-    assert abs(split.sum() - 0.05 * ini.n) < 2
+    assert abs(split.sum() - S.CONFIGS["config2"].p_split * ini.n) < 2
+    # the dominance-weighted draw: p_S * N candidates, the heavy ones first
+    w = np.zeros(ini.n)
+    large = np.flatnonzero(ini.scale.max(1) > 0.01 * ini.extent)
+    w[large[: len(large) // 10]] = 1000.0
+    ga2, den2 = S.synth_stats_weighted(ini.scale, ini.extent, 2e-4, 0.01, 0.01, 0.02, w, 0.0, 0)
+    split2 = np.flatnonzero((ga2 / den2 >= 2e-4) & (ini.scale.max(1) > 0.01 * ini.extent))
+    assert abs(len(split2) - 0.01 * ini.n) < 2
+    assert set(split2) <= set(large[: len(large) // 10]) or len(split2) > len(large) // 10
     # fp32-representable parameters
     assert np.array_equal(ini.mu, ini.mu.astype(np.float32).astype(np.float64))
 
