@@ -186,18 +186,22 @@ def compare_step(gres, ores: O.StepResult, flagged: set, g_in: O.Gaussians, stri
     removed_o = {r.index for r in ores.candidates if r.fallback or not r.reset}
     removed_g = {r.index for r in rep.candidates if r.fallback or not r.reset}
     assert removed_o - mset == removed_g - mset
-    keep_o = [i for i in range(ores.count_before) if i not in removed_o]
+
+    def _kept(removed):
+        mask = np.ones(ores.count_before, dtype=bool)
+        mask[np.fromiter(removed, dtype=np.int64, count=len(removed))] = False
+        return np.flatnonzero(mask)
+
+    keep_o, keep_g = _kept(removed_o), _kept(removed_g)
     np.testing.assert_array_equal(ores.index_map[:o_keep], keep_o)
-    np.testing.assert_array_equal(rep.index_map[:g_keep], [i for i in range(ores.count_before) if i not in removed_g])
+    np.testing.assert_array_equal(rep.index_map[:g_keep], keep_g)
     assert (rep.index_map[g_keep:] == -1).all()
     out = gres.gaussians.numpy()
     og = ores.gaussians
-    # survivor rows are exact copies (fp32 in, fp32 out)
+    # survivor rows are exact copies (fp32 in, fp32 out), matched by old index
+    common, io, ig = np.intersect1d(keep_o, keep_g, assume_unique=True, return_indices=True)
     for f in ("mu", "scale", "rot", "opacity", "sh_dc"):
-        gi = {int(i): k for k, i in enumerate(rep.index_map[:g_keep])}
-        common = [k for k, i in enumerate(keep_o) if i in gi]
-        np.testing.assert_array_equal(out[f][[gi[keep_o[k]] for k in common]], f32(getattr(og, f))[common],
-                                      err_msg=f)
+        np.testing.assert_array_equal(out[f][ig], f32(getattr(og, f))[io], err_msg=f)
     # per candidate: relative insert offset and row parents exact, rows within tolerance
     o_rows, g_rows = [], []
     g_pos = {r.index: k for k, r in enumerate(rep.candidates)}
