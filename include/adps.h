@@ -281,9 +281,12 @@ ADPS_API adps_status adps_step_phase1_finish(adps_plan* plan, void* stream, int6
 /* Tuning knobs (diagnostic/testing).  ADPS_PARAM_LARGE_THRESHOLD: parents
  * with more proposals than this use the grid-wide pair-tile merge path
  * (default 32; 0 routes every split parent through it).
- * ADPS_PARAM_TILE_PATH: 0 (default) warp-per-tile CCL with the block CCL for
- * the tiles it defers (> 192 runs) and for r_erode > 3 / debug maps; 1 the
- * block CCL for every tile.  Both give identical results.
+ * ADPS_PARAM_TILE_PATH: 0 (default) warp-per-tile CCL on bit planes written by
+ * a words pass over the fp32 raw cache, with the block CCL for the tiles it
+ * defers (> 192 runs) and for r_erode > 3 / debug maps; 1 the block CCL for
+ * every tile; 2 the warp CCL thresholding the fp64 raw cache row by row; 3 as
+ * 0 with the bit planes computed per tile inside the CCL kernel (no words
+ * pass; slower at config 3).  All give identical results.
  * ADPS_PARAM_DEFERRED_TILES (read-only): tiles the last phase 1 deferred. */
 #define ADPS_PARAM_LARGE_THRESHOLD 1
 #define ADPS_PARAM_TILE_PATH 2

@@ -722,8 +722,23 @@ cudaError_t launch_minmax_kernel(const AttributionArgs& a, int v0, int v1, cudaS
   if (v1 <= v0) return cudaSuccess;
   const long long hw = (long long)a.H * a.W;
   if (hw % 2 == 0 && hw < (1ll << 30)) {   // pixel pairs (float2 / int2 loads)
-    dim3 mg2((unsigned)((hw + 511) / 512), (unsigned)(v1 - v0));
-    if (mg2.x > 1024) mg2.x = 1024;
+    // one wave of resident blocks over the whole launch, each looping over many
+    // 512-pixel chunks of its view: the per-block min/max reduction and its
+    // barrier are paid once per ~50 chunks instead of every other chunk
+    static int resident = 0;
+    if (resident == 0) {
+      int dev = 0, sms = 148;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+      int per_sm = 0;
+      if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, minmax2_kernel, 256, 0) != cudaSuccess || per_sm < 1)
+        per_sm = 8;
+      resident = per_sm * sms;
+    }
+    const long long per_view = (hw + 511) / 512;
+    // floor: at most one wave (a second, short wave would run whole view slices on a few SMs)
+    const long long want = (long long)resident / (v1 - v0);
+    dim3 mg2((unsigned)(want < 1 ? 1 : (want > per_view ? per_view : want)), (unsigned)(v1 - v0));
     minmax2_kernel<<<mg2, 256, 0, s>>>(a.image, a.gt, a.dom, (int)hw, a.lohi, a.cls, a.N, a.dom_flag, a.cand_bits,
                                        a.raw, a.rawf, v0);
     return cudaGetLastError();
@@ -812,7 +827,7 @@ bool attribution_warp_path(const AttributionArgs& a) {
 cudaError_t launch_tiles_views(const AttributionArgs& a, int v0, int v1, cudaStream_t s) {
   if (!attribution_warp_path(a) || v1 <= v0) return cudaSuccess;
   const TileParams P = tile_params(a);
-  if (P.words && P.rawf) return launch_tile_bits(P, v0, v1, s);
+  if (P.rawf) return launch_tile_bits(P, v0, v1, s);   // bit planes (after the words pass, or fused)
   const long long tpv = (long long)P.tiles_x * P.tiles_y;
   return launch_tile_warp(P, tpv * v0, tpv * v1, s);
 }
@@ -825,7 +840,7 @@ cudaError_t launch_attribution_tail(const AttributionArgs& a, cudaStream_t s, Ma
   if (e != cudaSuccess) return e;
   if (attribution_warp_path(a)) {
     tile_kernel<<<a.grid_small, kTileThreads, smem, s>>>(P, a.deferred, a.n_deferred);
-    if (mark) mark(ctx, "tile_ccl", s, a.words && a.rawf ? 3 : 2);
+    if (mark) mark(ctx, "tile_ccl", s, a.words ? 3 : 2);
   } else {
     tile_kernel<<<(unsigned)nblocks, kTileThreads, smem, s>>>(P, nullptr, nullptr);
     if (mark) mark(ctx, "tile_ccl", s, 1);

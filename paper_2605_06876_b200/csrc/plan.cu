@@ -160,7 +160,8 @@ struct adps_plan {
   bool have_local = false;
   int tile_path = 0;   // 0 warp CCL (bit planes when l_bands <= 4) + deferred block CCL, 1 block CCL only,
                        // 2 warp CCL on the raw cache without bit planes
-  bool use_words = false;
+  bool use_bits = false;    // bit-plane warp CCL from the fp32 raw cache (tile paths 0 and 3)
+  bool use_words = false;   // ... with the separate words pass (tile path 3)
   int raw_cache = ADPS_RAW_CACHE_DEFAULT;   // minmax pass caches the raw L1 error for the warp CCL
   bool use_raw = false;                     // decided per phase 1
   // arguments saved by phase1_begin for phase1_end
@@ -549,8 +550,8 @@ static AttributionArgs attr_args(adps_plan* P, int V, int H, int W, const adps_c
   a.tile_path = P->tile_path;
   a.cand_bits = P->cand_bits.as<unsigned>();
   // the bit-plane path caches raw as fp32 (round toward zero), the others as fp64
-  a.raw = P->use_raw && !P->use_words ? P->rawc.as<double>() : nullptr;
-  a.rawf = P->use_words ? P->rawc.as<float>() : nullptr;
+  a.raw = P->use_raw && !P->use_bits ? P->rawc.as<double>() : nullptr;
+  a.rawf = P->use_bits ? P->rawc.as<float>() : nullptr;
   a.words = P->use_words ? P->twords.as<uint4>() : nullptr;
   return a;
 }
@@ -637,8 +638,9 @@ extern "C" adps_status adps_step_phase1_begin(adps_plan* P, void* stream_v, cons
   CK(ensure(P->deferred, 4ll * n_tiles));
   CK(ensure(P->cand_bits, 4ll * V * ((hw + 31) / 32) + 4));   // + 1 word: tile_words_kernel reads one past a row
   P->use_raw = P->raw_cache && P->tile_path != 1 && !P->dbg_m && cfg->r_erode <= 3;
-  P->use_words = P->use_raw && P->tile_path == 0 && cfg->l_bands <= 4;
-  if (P->use_raw) CK(ensure(P->rawc, (P->use_words ? 4ll : 8ll) * total_px));
+  P->use_bits = P->use_raw && (P->tile_path == 0 || P->tile_path == 3) && cfg->l_bands <= 4;
+  P->use_words = P->use_bits && P->tile_path == 0;   // path 3: planes computed per tile (fused)
+  if (P->use_raw) CK(ensure(P->rawc, (P->use_bits ? 4ll : 8ll) * total_px));
   if (P->use_words) CK(ensure(P->twords, (long long)tile_words_bytes(V, H, W)));
   CK(ensure(P->ctr, sizeof(Counters)));
   if (P->cams_host_cap < V) {
@@ -725,7 +727,7 @@ extern "C" adps_status adps_step_phase1_begin(adps_plan* P, void* stream_v, cons
       CK(launch_attribution_tail(a, P->aux, nullptr, nullptr));
       CK(cudaEventRecord(P->ev_attr, P->aux));
       P->attr_pending = true;
-      P->launches += (P->use_words ? 4 : 3) * chunks + 1 + 4;
+      P->launches += (P->use_words ? 4 : 3) * chunks + 1 + 4;   // minmax, thresholds, [words,] bits per chunk
     } else {
       // one launch over all views: the input pass, then thresholds + fallback count
       CK(launch_minmax_kernel(a, 0, V, s));
@@ -1571,7 +1573,9 @@ extern "C" adps_status adps_set_param(adps_plan* P, int32_t key, int64_t value) 
     return ADPS_OK;
   }
   if (key == ADPS_PARAM_TILE_PATH) {
-    if (value < 0 || value > 2) return fail(ADPS_INVALID_ARG, "tile path must be 0 (warp), 1 (block) or 2 (warp, no bit planes)");
+    if (value < 0 || value > 3)
+      return fail(ADPS_INVALID_ARG, "tile path must be 0 (bit planes, words pass), 1 (block), 2 (warp, fp64 raw) "
+                                    "or 3 (bit planes computed per tile)");
     P->tile_path = (int)value;
     return ADPS_OK;
   }

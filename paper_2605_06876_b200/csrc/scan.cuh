@@ -100,28 +100,44 @@ __global__ void __launch_bounds__(kScanThreads) scan_kernel(Policy pol, long lon
         __threadfence();
         vflag[tile] = 1u;
       }
+      // 128 predecessors per round (4 per lane, nearest first: q = p - lane - 32 j):
+      // inclusive prefixes propagate 128 tiles per round instead of 32
       unsigned long long acc = 0ull;
       long long p = tile - 1;
       while (true) {
-        const long long q = p - lane;
-        unsigned int f;
+        unsigned int f[4];
+        bool busy;
         do {
-          f = q >= 0 ? vflag[q] : 2u;
-        } while (__any_sync(0xffffffffu, f == 0u));
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            const long long q = p - lane - 32 * j;
+            f[j] = q >= 0 ? vflag[q] : 2u;
+          }
+          busy = f[0] == 0u || f[1] == 0u || f[2] == 0u || f[3] == 0u;
+        } while (__any_sync(0xffffffffu, busy));
         __threadfence();
-        const unsigned incl_mask = __ballot_sync(0xffffffffu, f == 2u);
+        unsigned incl[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) incl[j] = __ballot_sync(0xffffffffu, f[j] == 2u);
+        // the nearest predecessor with an inclusive prefix: slot (jf, first)
+        int jf = 4, first = 32;
+#pragma unroll
+        for (int j = 3; j >= 0; --j)
+          if (incl[j]) {
+            jf = j;
+            first = __ffs(incl[j]) - 1;
+          }
         unsigned long long v = 0ull;
-        if (incl_mask) {
-          const int first = __ffs(incl_mask) - 1;   // nearest predecessor with an inclusive prefix
-          if (lane < first) v = vval[2 * q];
-          else if (lane == first && q >= 0) v = vval[2 * q + 1];
-        } else {
-          v = vval[2 * q];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const long long q = p - lane - 32 * j;
+          if (j < jf || (j == jf && lane < first)) v += vval[2 * q];
+          else if (j == jf && lane == first && q >= 0) v += vval[2 * q + 1];
         }
         for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
         acc += v;
-        if (incl_mask) break;
-        p -= 32;
+        if (jf < 4) break;
+        p -= 128;
       }
       if (lane == 0) {
         vval[2 * tile + 1] = acc + agg;

@@ -49,7 +49,8 @@ struct WarpSmem {
   unsigned run[kWarpMaxRuns];       // ty | s << 5 | e << 10 | band << 16
   union {
     PostSmem post;
-    int d[kTileH][kTileW];          // bit-plane path: dominant ids of keyed pixels
+    int d[kTileH][kTileW];          // bit-plane path: fp32 raw cache of the tile rows (bit patterns),
+                                    // then the dominant ids of keyed pixels
   } u;
 };
 
@@ -619,7 +620,134 @@ __device__ __forceinline__ void cp_async4(void* smem, const void* gmem) {
 }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
 
-template <int R>
+// The bit planes of one tile computed in place from the fp32 raw cache (no
+// words pass): lane = column, one coalesced row load per needed ext row, the
+// same exact compares as tile_words_kernel (ambiguous pixels redo the fp64 raw
+// error from image and gt), ballots to words.  The candidate words come first:
+// a tile without a candidate pixel exits before touching the raw cache, and
+// only ext rows inside the erosion window of a candidate row are thresholded.
+// Out: ma / mb = 64-bit metric masks (halo bits included) of ext rows lane and
+// 32 + lane, cw / bw0 / bw1 = candidate and band words of tile row lane.
+template <int HL, int HH>
+__device__ __forceinline__ bool fused_tile_rows(const TileParams& P, WarpSmem& S, int v, int x0, int y0, int lane,
+                                                unsigned long long& ma, unsigned long long& mb, unsigned& cw,
+                                                unsigned& bw0, unsigned& bw1) {
+  constexpr int SPAN = HL + HH;
+  constexpr int NR = kTileH + SPAN;
+  static_assert(HL <= 1 && HH <= 1, "fused bit planes: erosion halo of one pixel");
+  constexpr unsigned FULL = 0xffffffffu;
+  const int W = P.W, H = P.H;
+  const long long hw = (long long)H * W;
+  ma = mb = 0ull;
+  cw = bw0 = bw1 = 0u;
+  {   // candidate word of tile row `lane`
+    const int y = y0 + lane;
+    if (y < H) {
+      const unsigned* cv = P.cand_bits + (long long)v * ((hw + 31) / 32);
+      const long long p = (long long)y * W + x0;
+      const unsigned lo = __ldg(cv + (p >> 5)), hi = __ldg(cv + (p >> 5) + 1);
+      cw = __funnelshift_r(lo, hi, (int)(p & 31));
+      const int valid = W - x0;
+      if (valid < 32) cw &= (1u << valid) - 1u;
+    }
+  }
+  const unsigned cmask = __ballot_sync(FULL, cw != 0u);
+  if (cmask == 0u) return false;
+  // ext rows to threshold: those inside the erosion window of a candidate row
+  // (tile rows ty in [ey - SPAN, ey] use ext row ey)
+  unsigned long long need = (unsigned long long)cmask;
+  if (SPAN >= 1) need |= (unsigned long long)cmask << 1;
+  if (SPAN >= 2) need |= (unsigned long long)cmask << 2;
+  {
+    const int y_lo = y0 - HL, y_hi = H - 1 - (y0 - HL);   // ext row ey is inside the image iff 0 <= y_lo + ey < H
+    if (y_lo < 0) need &= ~((1ull << (-y_lo)) - 1ull);
+    if (y_hi < NR - 1) need &= (2ull << y_hi) - 1ull;
+  }
+  const int* rv = reinterpret_cast<const int*>(P.rawf + (long long)v * hw);
+  const bool inb = x0 + lane < W;
+  // ---- stage the needed rows' raw bit patterns (cp.async, all in flight):
+  //      tile rows into S.u.d, the halo pixels of every ext row into S.halo
+  for (unsigned long long r = need; r; r &= r - 1ull) {
+    const int ey = __ffsll((long long)r) - 1;
+    const long long prow = (long long)(y0 - HL + ey) * W;
+    const int ty = ey - HL;
+    if (ty >= 0 && ty < kTileH && inb) cp_async4(&S.u.d[ty][lane], rv + prow + x0 + lane);
+  }
+  // lane ey (and 32 + lane): the halo pixels x0 - 1 (if HL) and x0 + 32 (if HH) of
+  // ext row ey, in registers (loads in flight with the copies)
+  int hl_a = (int)0xbf800000, hr_a = (int)0xbf800000, hl_b = (int)0xbf800000, hr_b = (int)0xbf800000;
+#pragma unroll
+  for (int h = 0; h < (NR > 32 ? 2 : 1); ++h) {
+    const int ey = lane + 32 * h;
+    if (ey < NR && ((need >> ey) & 1ull)) {
+      const long long prow = (long long)(y0 - HL + ey) * W;
+      if (HL > 0 && x0 > 0) (h ? hl_b : hl_a) = __ldg(rv + prow + x0 - 1);
+      if (HH > 0 && x0 + kTileW < W) (h ? hr_b : hr_a) = __ldg(rv + prow + x0 + kTileW);
+    }
+  }
+  // halo rows (outside the tile rows) straight into registers
+  int f_top = (int)0xbf800000, f_bot = (int)0xbf800000;   // -1.0f: below every threshold
+  if (HL > 0 && (need & 1ull) && inb) f_top = __ldg(rv + (long long)(y0 - 1) * W + x0 + lane);
+  if (HH > 0 && ((need >> (NR - 1)) & 1ull) && inb) f_bot = __ldg(rv + (long long)(y0 + kTileH) * W + x0 + lane);
+  const double* tv = P.thr_raw + (long long)v * P.L;
+  const double kInf = __longlong_as_double(0x7ff0000000000000ll);
+  const double X0 = __ldg(tv), X1 = P.L > 1 ? __ldg(tv + 1) : kInf, X2 = P.L > 2 ? __ldg(tv + 2) : kInf,
+               X3 = P.L > 3 ? __ldg(tv + 3) : kInf;
+  const RzThreshold R0 = rz_threshold(X0), R1 = rz_threshold(X1), R2 = rz_threshold(X2), R3 = rz_threshold(X3);
+  auto classify = [&](int fi, long long p, bool& m, int& band) {
+    m = fi >= R0.T;
+    band = (fi >= R1.T) + (fi >= R2.T) + (fi >= R3.T);
+    const bool amb = (fi == R0.A) | (fi == R1.A) | (fi == R2.A) | (fi == R3.A);
+    if (amb) {   // rare: the exact fp64 raw error, numpy order
+      const float* a3 = P.image + 3 * p;
+      const float* g3 = P.gt + 3 * p;
+      const double xr = dadd(dadd(fabs(dsub((double)a3[0], (double)g3[0])), fabs(dsub((double)a3[1], (double)g3[1]))),
+                             fabs(dsub((double)a3[2], (double)g3[2])));
+      m = xr >= X0;
+      band = (xr >= X1) + (xr >= X2) + (xr >= X3);
+    }
+  };
+  cp_async_wait_all();
+  __syncwarp();
+  const int hx = lane == 0 ? x0 - 1 : x0 + kTileW;
+  const bool h_on = (lane == 0 && HL > 0 && x0 > 0) || (lane == 1 && HH > 0 && x0 + kTileW < W);
+  for (unsigned long long r = need; r; r &= r - 1ull) {   // warp-uniform
+    const int ey = __ffsll((long long)r) - 1;
+    const int ty = ey - HL;
+    const long long prow = (long long)(y0 - HL + ey) * W;
+    const int fi = !inb ? (int)0xbf800000 : (ty < 0 ? f_top : (ty >= kTileH ? f_bot : S.u.d[ty][lane]));
+    int fh = (int)0xbf800000;
+    if (HL > 0 || HH > 0) {   // lane 0: left halo of ext row ey, lane 1: right halo
+      const int l = __shfl_sync(FULL, ey < 32 ? hl_a : hl_b, ey & 31);
+      const int r = __shfl_sync(FULL, ey < 32 ? hr_a : hr_b, ey & 31);
+      fh = !h_on ? (int)0xbf800000 : (lane == 0 ? l : r);
+    }
+    bool m, mh;
+    int band, bh;
+    classify(fi, (long long)v * hw + prow + x0 + lane, m, band);
+    classify(fh, (long long)v * hw + prow + hx, mh, bh);
+    const unsigned M = __ballot_sync(FULL, m);
+    const unsigned hb = __ballot_sync(FULL, mh && h_on);
+    unsigned long long m64 = (unsigned long long)M << HL;
+    if (HL > 0) m64 |= (unsigned long long)(hb & 1u);
+    if (HH > 0) m64 |= (unsigned long long)((hb >> 1) & 1u) << (kTileW + HL);
+    if (lane == (ey & 31)) {
+      if (ey < 32) ma = m64;
+      else mb = m64;
+    }
+    if (ty >= 0 && ty < kTileH && ((cmask >> ty) & 1u)) {   // warp-uniform: band words of a candidate row
+      const unsigned B0 = __ballot_sync(FULL, band & 1), B1 = __ballot_sync(FULL, band & 2);
+      if (lane == ty) {
+        bw0 = B0;
+        bw1 = B1;
+      }
+    }
+  }
+  __syncwarp();   // S.u.d is restaged with the dominant ids next
+  return true;
+}
+
+template <int R, bool FUSED>
 __global__ void __launch_bounds__(kWarpsPerBlock * 32, ADPS_TW_MINBLOCKS)
     tile_bits_kernel(TileParams P, const uint4* __restrict__ words, int WW, long long t0, long long t1) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -638,12 +766,21 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, ADPS_TW_MINBLOCKS)
   const int tx = tin % P.tiles_x;
   const int x0 = tx * kTileW, y0 = (tin / P.tiles_x) * kTileH;
   const int W = P.W, H = P.H;
-  const uint4* wv = words + (long long)v * H * WW;
-  // ---- all ext rows of the tile: lane ey (and 32 + lane for the last SPAN rows)
-  uint4 qa, qb = make_uint4(0u, 0u, 0u, 0u);
   unsigned long long ma, mb = 0ull;
-  load_ext_words<HL, HH>(wv, WW, H, tx, y0, lane, NR, qa, ma);
-  if (NR > 32) load_ext_words<HL, HH>(wv, WW, H, tx, y0, 32 + lane, NR, qb, mb);
+  unsigned cw, bw0, bw1;
+  bool any_cand = true;
+  if (FUSED) {
+    any_cand = fused_tile_rows<HL, HH>(P, S, v, x0, y0, lane, ma, mb, cw, bw0, bw1);
+  } else {
+    const uint4* wv = words + (long long)v * H * WW;
+    // ---- all ext rows of the tile: lane ey (and 32 + lane for the last SPAN rows)
+    uint4 qa, qb = make_uint4(0u, 0u, 0u, 0u);
+    load_ext_words<HL, HH>(wv, WW, H, tx, y0, lane, NR, qa, ma);
+    if (NR > 32) load_ext_words<HL, HH>(wv, WW, H, tx, y0, 32 + lane, NR, qb, mb);
+    cw = HL > 0 ? ext_get(qa.y, qb.y, lane + HL) : qa.y;
+    bw0 = HL > 0 ? ext_get(qa.z, qb.z, lane + HL) : qa.z;
+    bw1 = HL > 0 ? ext_get(qa.w, qb.w, lane + HL) : qa.w;
+  }
   // ---- lane ty: eroded metric word of tile row ty, its candidate and band words
   unsigned long long acc = ma;
   if (SPAN >= 1) acc &= ext_get(ma, mb, lane + 1);
@@ -651,10 +788,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, ADPS_TW_MINBLOCKS)
   unsigned long long h = acc;
   if (SPAN >= 1) h &= acc >> 1;
   if (SPAN >= 2) h &= acc >> 2;
-  const unsigned cw = HL > 0 ? ext_get(qa.y, qb.y, lane + HL) : qa.y;
-  const unsigned bw0 = HL > 0 ? ext_get(qa.z, qb.z, lane + HL) : qa.z;
-  const unsigned bw1 = HL > 0 ? ext_get(qa.w, qb.w, lane + HL) : qa.w;
-  const unsigned K = (unsigned)h & cw;
+  const unsigned K = any_cand ? (unsigned)h & cw : 0u;
   const unsigned keyed = __ballot_sync(FULL, K != 0u);
   int* border = P.border + tile * kBorderSlots;
   if (keyed == 0u) {   // no keyed pixel: no runs, no records, empty border labels
@@ -774,37 +908,35 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, ADPS_TW_MINBLOCKS)
 
 size_t tile_words_bytes(int V, int H, int W) { return (size_t)V * H * ((W + 31) / 32) * sizeof(uint4); }
 
+template <int R, bool FUSED>
+static cudaError_t launch_bits_r(const TileParams& P, int WW, long long t0, long long t1, cudaStream_t s) {
+  const size_t smem = tile_warp_smem_bytes();
+  cudaError_t e = cudaFuncSetAttribute(tile_bits_kernel<R, FUSED>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  const long long blocks = (t1 - t0 + kWarpsPerBlock - 1) / kWarpsPerBlock;
+  if (blocks > 0) tile_bits_kernel<R, FUSED><<<(unsigned)blocks, kWarpsPerBlock * 32, smem, s>>>(P, P.words, WW, t0, t1);
+  return cudaGetLastError();
+}
+
+// fused: the bit planes per tile straight from the raw cache (default); else the
+// separate words pass (tile_words_kernel) first -- both give identical bits
 cudaError_t launch_tile_bits(const TileParams& P, int v0, int v1, cudaStream_t s) {
   if (v1 <= v0) return cudaSuccess;
   const int WW = (P.W + 31) / 32;
-  const int per_view = P.H * WW;
-  (void)per_view;
-  const unsigned gx = (unsigned)((P.H + 7) / 8);   // warp per image row, 8 rows per block
-  tile_words_kernel<<<dim3(gx, (unsigned)(v1 - v0)), 256, 0, s>>>(P.rawf, P.image, P.gt, P.cand_bits, P.thr_raw,
-                                                                   P.L, P.H, P.W, WW, v0, P.words);
+  const bool fused = P.words == nullptr;
+  if (!fused) {
+    const unsigned gx = (unsigned)((P.H + 7) / 8);   // warp per image row, 8 rows per block
+    tile_words_kernel<<<dim3(gx, (unsigned)(v1 - v0)), 256, 0, s>>>(P.rawf, P.image, P.gt, P.cand_bits, P.thr_raw,
+                                                                     P.L, P.H, P.W, WW, v0, P.words);
+  }
   const long long tpv = (long long)P.tiles_x * P.tiles_y;
   const long long t0 = tpv * v0, t1 = tpv * v1;
-  const size_t smem = tile_warp_smem_bytes();
-  const long long blocks = (t1 - t0 + kWarpsPerBlock - 1) / kWarpsPerBlock;
-  cudaError_t e = cudaSuccess;
   switch (P.r_erode <= 1 ? 1 : P.r_erode) {
-    case 1:
-      e = cudaFuncSetAttribute(tile_bits_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      if (e == cudaSuccess) tile_bits_kernel<1><<<(unsigned)blocks, kWarpsPerBlock * 32, smem, s>>>(P, P.words, WW, t0, t1);
-      break;
-    case 2:
-      e = cudaFuncSetAttribute(tile_bits_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      if (e == cudaSuccess) tile_bits_kernel<2><<<(unsigned)blocks, kWarpsPerBlock * 32, smem, s>>>(P, P.words, WW, t0, t1);
-      break;
-    case 3:
-      e = cudaFuncSetAttribute(tile_bits_kernel<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      if (e == cudaSuccess) tile_bits_kernel<3><<<(unsigned)blocks, kWarpsPerBlock * 32, smem, s>>>(P, P.words, WW, t0, t1);
-      break;
-    default:
-      return cudaErrorInvalidValue;
+    case 1: return fused ? launch_bits_r<1, true>(P, WW, t0, t1, s) : launch_bits_r<1, false>(P, WW, t0, t1, s);
+    case 2: return fused ? launch_bits_r<2, true>(P, WW, t0, t1, s) : launch_bits_r<2, false>(P, WW, t0, t1, s);
+    case 3: return fused ? launch_bits_r<3, true>(P, WW, t0, t1, s) : launch_bits_r<3, false>(P, WW, t0, t1, s);
+    default: return cudaErrorInvalidValue;
   }
-  if (e != cudaSuccess) return e;
-  return cudaGetLastError();
 }
 
 template <int R, bool RAW>

@@ -125,8 +125,9 @@ def _injected_partition(op, plan, e, dom, n_gauss, l_bands, m_min, cands, tau=0.
                gamma_c=0.15, tau_g=2e-4, tau_s=0.01, eta=1.6, eps=1e-9)
     dev = "cuda"
     got_by_path = []
-    # block CCL; warp CCL recomputing / caching the raw error; bit-plane warp CCL (l_bands <= 4)
-    for path, raw in ((1, 1), (0, 0), (2, 1), (0, 1)):
+    # block CCL; warp CCL recomputing / caching the raw error; bit-plane warp CCL (l_bands <= 4),
+    # fused and with the separate words pass
+    for path, raw in ((1, 1), (0, 0), (2, 1), (0, 1), (3, 1)):
         plan.set_tile_path(path)
         plan.set_raw_cache(raw)
         try:
@@ -143,6 +144,7 @@ def _injected_partition(op, plan, e, dom, n_gauss, l_bands, m_min, cands, tau=0.
     np.testing.assert_array_equal(got_by_path[1], got_by_path[0], err_msg="warp CCL != block CCL")
     np.testing.assert_array_equal(got_by_path[2], got_by_path[0], err_msg="cached-raw warp CCL != block CCL")
     np.testing.assert_array_equal(got_by_path[3], got_by_path[0], err_msg="bit-plane warp CCL != block CCL")
+    np.testing.assert_array_equal(got_by_path[4], got_by_path[0], err_msg="words-pass warp CCL != block CCL")
     got = got_by_path[3]
     maps = O.compute_maps(rendered.astype(np.float64), gt.astype(np.float64), cfg)
     is_c = np.zeros(n_gauss, bool)
@@ -476,7 +478,8 @@ def test_determinism_at_scale(op, cfg_name):
     g, gt_img, img, dom = d["g"], d["gt_img"], d["img"], d["dom"]
     cfg = AdpSplitConfig(v_views=len(cams), n_max=wl.n_max)
     digests = []
-    for path, raw in ((0, 1), (0, 1), (1, 1), (0, 0), (2, 1)):   # block CCL / recomputed raw / no bit planes: same bits
+    # block CCL / recomputed raw / no bit planes / words pass: same bits
+    for path, raw in ((0, 1), (0, 1), (1, 1), (0, 0), (2, 1), (3, 1)):
         plan.set_tile_path(path)
         plan.set_raw_cache(raw)
         res = op.densify_step(g, ini.extent, cams, gt_img, torch.as_tensor(ga, device="cuda"),
