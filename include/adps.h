@@ -298,6 +298,9 @@ ADPS_API adps_status adps_step_phase1_finish(adps_plan* plan, void* stream, int6
 #define ADPS_PARAM_STAT_GATES_PASSED 9   /* in them (the last two only in stats builds) */
 #define ADPS_PARAM_RAW_CACHE 6          /* 1 (default): the minmax pass caches the fp64 raw
                                            L1 error (8 B/px) for the warp CCL; 0: recompute */
+#define ADPS_PARAM_PIPELINE_CHUNKS 10      /* view chunks of the attribution pipeline (input pass of chunk
+                                              c+1 beside the CCL of chunk c; default 1) */
+#define ADPS_PARAM_INPUT_BLOCKS_PER_SM 11  /* resident blocks per SM of the input pass (0 = all that fit) */
 ADPS_API adps_status adps_set_param(adps_plan* plan, int32_t key, int64_t value);
 ADPS_API adps_status adps_get_param(adps_plan* plan, int32_t key, int64_t* value);
 

@@ -725,16 +725,20 @@ cudaError_t launch_minmax_kernel(const AttributionArgs& a, int v0, int v1, cudaS
     // one wave of resident blocks over the whole launch, each looping over many
     // 512-pixel chunks of its view: the per-block min/max reduction and its
     // barrier are paid once per ~50 chunks instead of every other chunk
-    static int resident = 0;
-    if (resident == 0) {
-      int dev = 0, sms = 148;
+    static int per_sm_max = 0, sms = 148;
+    if (per_sm_max == 0) {
+      int dev = 0;
       cudaGetDevice(&dev);
       cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-      int per_sm = 0;
-      if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, minmax2_kernel, 256, 0) != cudaSuccess || per_sm < 1)
-        per_sm = 8;
-      resident = per_sm * sms;
+      if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_max, minmax2_kernel, 256, 0) != cudaSuccess ||
+          per_sm_max < 1)
+        per_sm_max = 8;
     }
+    // fewer than all resident blocks leaves SM room for the CCL of the previous
+    // view chunk running concurrently on the second stream
+    const int per_sm = a.input_blocks_per_sm > 0 && a.input_blocks_per_sm < per_sm_max ? a.input_blocks_per_sm
+                                                                                          : per_sm_max;
+    const int resident = per_sm * sms;
     const long long per_view = (hw + 511) / 512;
     // floor: at most one wave (a second, short wave would run whole view slices on a few SMs)
     const long long want = (long long)resident / (v1 - v0);

@@ -73,6 +73,7 @@ struct AttributionArgs {
   unsigned char* dbg_b;
   unsigned int* overflow;
   unsigned grid_small;
+  int input_blocks_per_sm;   // resident blocks per SM of the input pass (0: all that fit)
   int* deferred;                     // [n_tiles]
   unsigned long long* n_deferred;
   int tile_path;                     // 0 auto (warp kernel + deferred), 1 block kernel only,

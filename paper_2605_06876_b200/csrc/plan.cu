@@ -19,7 +19,7 @@
 #define ADPS_PIPELINE_DEFAULT 1
 #endif
 #ifndef ADPS_PIPELINE_CHUNKS
-#define ADPS_PIPELINE_CHUNKS 2
+#define ADPS_PIPELINE_CHUNKS 1
 #endif
 #ifndef ADPS_AUX_PRIORITY
 #define ADPS_AUX_PRIORITY 0
@@ -148,6 +148,8 @@ struct adps_plan {
   bool child_pending = false;
   bool attr_pending = false;
   int pipeline = ADPS_PIPELINE_DEFAULT;
+  int pipeline_chunks = ADPS_PIPELINE_CHUNKS;   // view chunks of the attribution pipeline
+  int input_blocks_per_sm = 0;                  // input pass residency (0: all that fit)
   int fb_children = 2;   // children per fallback parent of the last phase 1
   // view sharding: this plan's local view v is global view position view_offset + v * view_stride
   // of v_global_cfg sampled views (0 = the local views are all of them)
@@ -545,6 +547,7 @@ static AttributionArgs attr_args(adps_plan* P, int V, int H, int W, const adps_c
   a.dbg_b = P->dbg_b;
   a.overflow = &ctr->overflow;
   a.grid_small = (unsigned)(P->sm_count * 4);
+  a.input_blocks_per_sm = P->input_blocks_per_sm;
   a.deferred = P->deferred.as<int>();
   a.n_deferred = &ctr->n_deferred;
   a.tile_path = P->tile_path;
@@ -713,7 +716,7 @@ extern "C" adps_status adps_step_phase1_begin(adps_plan* P, void* stream_v, cons
       // views in chunks: minmax of chunk c on `stream`, the warp CCL of chunk c
       // on the second stream as soon as its thresholds exist; the tail (deferred
       // tiles, border merge) after the last chunk; phase1_end joins it
-      const int maxc = ADPS_PIPELINE_CHUNKS < adps_plan::kMaxChunks ? ADPS_PIPELINE_CHUNKS : adps_plan::kMaxChunks;
+      const int maxc = P->pipeline_chunks < adps_plan::kMaxChunks ? P->pipeline_chunks : adps_plan::kMaxChunks;
       const int chunks = V < maxc ? V : maxc;
       for (int c = 0; c < chunks; ++c) {
         const int v0 = (int)((long long)V * c / chunks), v1 = (int)((long long)V * (c + 1) / chunks);
@@ -1567,6 +1570,16 @@ extern "C" adps_status adps_set_param(adps_plan* P, int32_t key, int64_t value) 
     P->large_threshold = (int)value;
     return ADPS_OK;
   }
+  if (key == ADPS_PARAM_PIPELINE_CHUNKS) {
+    if (value < 1 || value > adps_plan::kMaxChunks) return fail(ADPS_INVALID_ARG, "pipeline chunks must be in [1,16]");
+    P->pipeline_chunks = (int)value;
+    return ADPS_OK;
+  }
+  if (key == ADPS_PARAM_INPUT_BLOCKS_PER_SM) {
+    if (value < 0 || value > 64) return fail(ADPS_INVALID_ARG, "input blocks per SM must be in [0,64]");
+    P->input_blocks_per_sm = (int)value;
+    return ADPS_OK;
+  }
   if (key == ADPS_PARAM_RAW_CACHE) {
     if (value < 0 || value > 1) return fail(ADPS_INVALID_ARG, "raw cache must be 0 or 1");
     P->raw_cache = (int)value;
@@ -1588,6 +1601,8 @@ extern "C" adps_status adps_get_param(adps_plan* P, int32_t key, int64_t* value)
     case ADPS_PARAM_LARGE_THRESHOLD: *value = P->large_threshold; return ADPS_OK;
     case ADPS_PARAM_TILE_PATH: *value = P->tile_path; return ADPS_OK;
     case ADPS_PARAM_RAW_CACHE: *value = P->raw_cache; return ADPS_OK;
+    case ADPS_PARAM_PIPELINE_CHUNKS: *value = P->pipeline_chunks; return ADPS_OK;
+    case ADPS_PARAM_INPUT_BLOCKS_PER_SM: *value = P->input_blocks_per_sm; return ADPS_OK;
     case ADPS_PARAM_STAT_TILE_PAIRS: *value = P->ctr_host ? (int64_t)P->ctr_host->n_tile_pairs : 0; return ADPS_OK;
     case ADPS_PARAM_STAT_GATES: *value = P->ctr_host ? (int64_t)P->ctr_host->stat_gates : 0; return ADPS_OK;
     case ADPS_PARAM_STAT_GATES_PASSED: *value = P->ctr_host ? (int64_t)P->ctr_host->stat_pass : 0; return ADPS_OK;

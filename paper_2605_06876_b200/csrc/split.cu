@@ -463,17 +463,30 @@ __global__ void __launch_bounds__(kEmitThreads) emit_survivors_kernel(EmitArgs a
 __global__ void __launch_bounds__(kEmitThreads) emit_kernel(EmitArgs a, long long b_ins) {
   const long long blk = blockIdx.x;
   if (blk < b_ins) {                                    // candidate inserts, ascending index
-    // a thread per candidate (most insert 2 rows; a warp per candidate left
-    // 30 of 32 lanes idle), rows in order
-    const long long k = blk * kEmitThreads + threadIdx.x;
-    if (k >= a.n_split) return;
-    const int c = a.cand_case[k];
-    if (a.insert_offset) a.insert_offset[k] = a.n_keep + a.ins_off[k];
-    if (c == ADPS_CASE_RESET) return;
-    const int rows = c == ADPS_CASE_FALLBACK ? a.fb_children : a.cand_merged[k] + 1;
-    for (int j = 0; j < rows; ++j) emit_insert_row(a, k, j);
+    // a thread per inserted row: its candidate is the last k with ins_off[k] <= r
+    // (ins_off is the exclusive prefix of the rows per candidate), found by a
+    // binary search; rows of one candidate are adjacent, so neighbouring threads
+    // mostly search the same path (cached)
+    const long long r = blk * kEmitThreads + threadIdx.x;
+    if (r >= a.n_inserted) return;
+    long long lo = 0, hi = a.n_split - 1;
+    while (lo < hi) {
+      const long long mid = (lo + hi + 1) >> 1;
+      if ((long long)__ldg(a.ins_off + mid) <= r) lo = mid;
+      else hi = mid - 1;
+    }
+    // (a reset candidate inserts nothing, so its offset equals the next
+    // candidate's: the last k with ins_off[k] <= r always has rows)
+    const long long k = lo;
+    const int j = (int)(r - __ldg(a.ins_off + k));
+    emit_insert_row(a, k, j);
+    if (a.insert_offset && j == 0) a.insert_offset[k] = a.n_keep + a.ins_off[k];
+  } else if (blk < b_ins + a.b_off) {                   // insert offsets of the reset candidates
+    const long long k = (blk - b_ins) * kEmitThreads + threadIdx.x;
+    if (k < a.n_split && a.insert_offset && a.cand_case[k] == ADPS_CASE_RESET)
+      a.insert_offset[k] = a.n_keep + a.ins_off[k];
   } else {                                              // clones, ascending
-    const long long j = (blk - b_ins) * kEmitThreads + threadIdx.x;
+    const long long j = (blk - b_ins - a.b_off) * kEmitThreads + threadIdx.x;
     if (j < a.n_clone) {
       const long long dst = a.n_keep + a.n_inserted + j;
       const int src = a.clone_list[j];
@@ -499,9 +512,12 @@ cudaError_t launch_emit(const EmitArgs& a, cudaStream_t s, cudaStream_t aux, cud
     long long b = (a.n * 4 + 8ll * kEmitThreads - 1) / (8ll * kEmitThreads);
     emit_survivors_kernel<<<dim3((unsigned)b, a.g.sh_k > 0 ? 6u : 5u), kEmitThreads, 0, ss>>>(a);
   }
-  const long long b_ins = (a.n_split + kEmitThreads - 1) / kEmitThreads;
+  const long long b_ins = (a.n_inserted + kEmitThreads - 1) / kEmitThreads;
   const long long b_clone = (a.n_clone + kEmitThreads - 1) / kEmitThreads;
-  if (b_ins + b_clone > 0) emit_kernel<<<(unsigned)(b_ins + b_clone), kEmitThreads, 0, s>>>(a, b_ins);
+  EmitArgs a2 = a;
+  a2.b_off = a.insert_offset ? (a.n_split + kEmitThreads - 1) / kEmitThreads : 0;
+  if (b_ins + a2.b_off + b_clone > 0)
+    emit_kernel<<<(unsigned)(b_ins + a2.b_off + b_clone), kEmitThreads, 0, s>>>(a2, b_ins);
   cudaError_t e = cudaGetLastError();
   if (e == cudaSuccess && two) {
     e = cudaEventRecord(join, aux);

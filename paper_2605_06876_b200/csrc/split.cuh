@@ -125,6 +125,7 @@ struct EmitArgs {
   long long* index_map;
   int* child_parent;        // [n_out - n_keep] old index each appended row came from, or null
   long long* insert_offset; // [n_split] output row of candidate k's first insert, or null
+  long long b_off;          // (launch internal) blocks writing the reset candidates' insert offsets
 };
 cudaError_t launch_emit(const EmitArgs& a, cudaStream_t s, cudaStream_t aux = nullptr, cudaEvent_t fork = nullptr,
                         cudaEvent_t join = nullptr);
