@@ -461,6 +461,48 @@ def run_ours(args, wl):
     b_step = BYTES_PER_PX * px + BYTES_PER_G_IN * g.n + BYTES_PER_G_OUT * counts["n_out"]
     acc = time_accumulate(dev, g.n, peak) if rank == 0 else None
 
+    # ---- K1-epilogue variant (reported separately): the render's
+    #      epilogue runs select and the input pass, the step starts from the
+    #      8 B/px boundary (fp32 raw cache + dominant map); 1 GPU
+    fused = None
+    if world == 1 and not args.no_fused:
+        gt_v = gt_img   # all views sampled (contiguous): the step's own gt tensor
+        img_f = torch.empty_like(img)
+        dom_f = torch.empty_like(dom)
+
+        def fused_render():
+            return plan.render_fused(g, ini.extent, ga, den, cfg, cams[view_ids], gt_v, out=(img_f, dom_f))
+
+        def fused_step():
+            return op.densify_step(g, ini.extent, cams, gt_l, ga, den, cfg, np.random.default_rng((args.seed, 0)),
+                                   renders=(img_f, dom_f), plan=plan, view_ids=view_ids, want_report=True)
+
+        for _ in range(2):
+            fused_render()
+            rf = fused_step()
+        assert rf.counts["n_out"] == counts["n_out"] and rf.counts["n_regions"] == counts["n_regions"]
+        n_f = max(3, min(args.steps, 10))
+        r_ms, s_ms = [], []
+        for _ in range(n_f):
+            e_a, e_b, e_c = (torch.cuda.Event(enable_timing=True) for _ in range(3))
+            e_a.record()
+            fused_render()
+            e_b.record()
+            fused_step()
+            e_c.record()
+            torch.cuda.synchronize()
+            r_ms.append(e_a.elapsed_time(e_b))
+            s_ms.append(e_b.elapsed_time(e_c))
+        fr, fs = float(np.mean(r_ms)), float(np.mean(s_ms))
+        b8 = 8 * px + BYTES_PER_G_IN * g.n + BYTES_PER_G_OUT * counts["n_out"]
+        fused = {"render_ms": fr, "render_ms_plain": render_ms, "step_ms": fs,
+                 "parents_per_s": n_split / (fs * 1e-3), "full_step_ms": fr + fs,
+                 "full_step_parents_per_s": n_split / ((fr + fs) * 1e-3),
+                 "step_bytes": int(b8), "step_roofline_frac": b8 / (fs * 1e-3) / 1e9 / peak,
+                 "note": "render epilogue = select + input pass (raw L1 fp64, per-view min/max, candidate bits, "
+                         "ever-dominant flags); step from the 8 B/px boundary (raw cache + dominant map); "
+                         "identical results (tests/test_gpu_rows.py)"}
+
     # ---- e2e: same step through the API from pinned host buffers
     e2e = None
     if not args.no_e2e:
@@ -560,6 +602,7 @@ def run_ours(args, wl):
                        "note": "attribution render (compute-bound), not part of value; splat-px = (pixel, splat) "
                                "pairs with alpha >= 1/255 (measured depth complexity x pixels)"},
             "full_step": {"ms": full_ms, "parents_per_s": n_split / (full_ms * 1e-3)},
+            "fused_epilogue": fused,
             "counts": counts,
             "proposals_per_parent": props_stats,
             "e2e": e2e,
@@ -613,6 +656,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-parity", action="store_true", help="skip the oracle parity check on the cpu sample")
+    ap.add_argument("--no-fused", action="store_true", help="skip the K1-epilogue (fused render) variant")
     ap.add_argument("--replicas", action="store_true",
                     help="N>1: independent replicas (weak scaling) instead of the view-sharded step")
     args = ap.parse_args()

@@ -158,6 +158,21 @@ ADPS_API adps_status adps_render_stats(adps_plan* plan, void* stream, const adps
                               const double* cams_host, int32_t n_views, const float* bg,
                               float* image, int32_t* dominant, float* weight, uint64_t* contributions);
 
+/* Fused attribution ("K1 epilogue"): select (ref/adc.py:165)
+ * and the attribution render of the sampled views (as adps_render) whose
+ * epilogue also computes, from each pixel's stored image value and gt, what
+ * the step's input pass would: the raw L1 error (numpy's fp64 order) into the
+ * plan's fp32 raw cache, the per-view min/max, the candidate bits and the
+ * ever-dominant flags (ref/adc.py:168-180).  The next
+ * adps_step_phase1_begin with the same arguments (same g, stats, cfg, cameras,
+ * image, gt and dominant pointers) then skips select and the input pass and
+ * starts from that 8 B/px boundary; any other call uses the full path.
+ * gt: [V,H,W,3] fp32 of the same views. */
+ADPS_API adps_status adps_render_fused(adps_plan* plan, void* stream, const adps_gaussians* g, int64_t n,
+                              double extent, const double* grad_accum, const double* denom,
+                              const adps_config* cfg, const double* cams_host, int32_t n_views,
+                              const float* bg, const float* gt, float* image, int32_t* dominant);
+
 /* Phase 1 of adpsplit_step (ref/adc.py:165-227): select, error maps,
  * partition, region statistics, ever-dominant, child initialisation,
  * cross-view merge and cap, per-candidate case, offsets.  Consumes the

@@ -11,11 +11,11 @@ API ``densify_step`` / ``render_views`` / ``GaussianTensors`` / ``Plan``.
 from .types import (AdpSplitConfig, Camera, CandidateRecord, DegenerateRayError, DensifyStats,
                     Gaussian3D, InvariantError, Scene, SplitReport)
 
-__version__ = "0.1.0"
+__version__ = "0.2.0"
 
 _OPS = ("adpsplit_step", "render", "densify_step", "render_views", "GaussianTensors", "Plan",
         "StepResult", "sample_views", "camera_rows", "accumulate_stats_", "default_plan",
-        "vanilla_densify", "vanilla_densify_step", "remap_stats", "remap_stats_ref", "remap_rows")
+        "vanilla_densify", "vanilla_densify_step", "remap_stats", "remap_stats_ref", "remap_rows", "prune")
 
 
 def __getattr__(name):

@@ -22,6 +22,10 @@
 #include "adps_internal.cuh"
 #include "attribution.cuh"
 
+#ifndef ADPS_DEFERRED_BLOCK
+#define ADPS_DEFERRED_BLOCK 0   // 1: deferred tiles by the block CCL (tile_kernel) instead of the big warp kernel
+#endif
+
 namespace adps {
 
 __device__ __forceinline__ double raw_l1(const float* __restrict__ img, const float* __restrict__ gt,
@@ -842,7 +846,12 @@ cudaError_t launch_attribution_tail(const AttributionArgs& a, cudaStream_t s, Ma
   size_t smem = sizeof(TileSmem);
   cudaError_t e = cudaFuncSetAttribute(tile_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  if (attribution_warp_path(a)) {
+  if (attribution_warp_path(a) && P.rawf && !ADPS_DEFERRED_BLOCK) {
+    // bit-plane path: the deferred tiles by the big-capacity warp kernel
+    e = launch_tile_bits_deferred(P, a.grid_small / 2, s);
+    if (e != cudaSuccess) return e;
+    if (mark) mark(ctx, "tile_ccl", s, a.words ? 3 : 2);
+  } else if (attribution_warp_path(a)) {
     tile_kernel<<<a.grid_small, kTileThreads, smem, s>>>(P, a.deferred, a.n_deferred);
     if (mark) mark(ctx, "tile_ccl", s, a.words ? 3 : 2);
   } else {

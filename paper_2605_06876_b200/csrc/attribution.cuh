@@ -89,6 +89,8 @@ cudaError_t launch_tile_warp(const TileParams& P, long long t0, long long t1, cu
 size_t tile_warp_smem_bytes();
 // bit-plane path (raw cache, l_bands <= 4, r_erode <= 3): words pass + tile_bits_kernel over views [v0, v1)
 cudaError_t launch_tile_bits(const TileParams& P, int v0, int v1, cudaStream_t s);
+// the tiles launch_tile_bits deferred (P.deferred / P.n_deferred), a warp each
+cudaError_t launch_tile_bits_deferred(const TileParams& P, unsigned blocks, cudaStream_t s);
 size_t tile_words_bytes(int V, int H, int W);
 
 size_t tile_smem_bytes();

@@ -613,7 +613,10 @@ __device__ __forceinline__ void stage_col(const MergeArgs& a, ColTile& B, long l
 // while the row lasts, the column tile staged in shared memory one pair ahead
 // (cp.async), no block barriers.  If the survivor list overflowed, every tile
 // pair is taken with the box test inline.
-__global__ void __launch_bounds__(kPairWarps * 32) pair_tiles_kernel(MergeArgs a) {
+#ifndef ADPS_PAIR_MINB
+#define ADPS_PAIR_MINB 1
+#endif
+__global__ void __launch_bounds__(kPairWarps * 32, ADPS_PAIR_MINB) pair_tiles_kernel(MergeArgs a) {
   extern __shared__ __align__(16) unsigned char pt_smem[];
 #if ADPS_PAIR_LOCAL_UF
   __shared__ int luf[kPairWarps][64];   // warp-local union-find of a tile pair

@@ -166,6 +166,21 @@ struct adps_plan {
   bool use_words = false;   // ... with the separate words pass (tile path 3)
   int raw_cache = ADPS_RAW_CACHE_DEFAULT;   // minmax pass caches the raw L1 error for the warp CCL
   bool use_raw = false;                     // decided per phase 1
+  // the attribution a fused render (adps_render_fused) left for the next
+  // phase1_begin on the same inputs: select classes/lists, raw cache, per-view
+  // min/max, candidate bits, ever-dominant flags
+  struct {
+    bool valid = false;
+    adps_gaussians g;
+    long long n;
+    double extent;
+    const double *ga, *den;
+    adps_config cfg;
+    int V, H, W;
+    const float *image, *gt;
+    const int32_t* dom;
+    std::vector<double> cams;
+  } fused;
   // arguments saved by phase1_begin for phase1_end
   bool have_begin = false;
   struct {
@@ -356,7 +371,8 @@ static GaussiansIn to_in(const adps_gaussians* g) {
 // ------------------------------------------------------------------ render
 static adps_status render_impl(adps_plan* P, void* stream_v, const adps_gaussians* g, int64_t n,
                                const double* cams_host, int32_t n_views, const float* bg, float* image,
-                               int32_t* dominant, float* weight, unsigned long long* contrib_dev);
+                               int32_t* dominant, float* weight, unsigned long long* contrib_dev,
+                               const float* epi_gt = nullptr);
 
 extern "C" adps_status adps_render(adps_plan* P, void* stream_v, const adps_gaussians* g, int64_t n,
                                    const double* cams_host, int32_t n_views, const float* bg, float* image,
@@ -384,7 +400,8 @@ extern "C" adps_status adps_render_stats(adps_plan* P, void* stream_v, const adp
 
 static adps_status render_impl(adps_plan* P, void* stream_v, const adps_gaussians* g, int64_t n,
                                const double* cams_host, int32_t n_views, const float* bg, float* image,
-                               int32_t* dominant, float* weight, unsigned long long* contrib_dev) {
+                               int32_t* dominant, float* weight, unsigned long long* contrib_dev,
+                               const float* epi_gt) {
   if (!P) return fail(ADPS_INVALID_ARG, "plan is NULL");
   adps_status st = check_gaussians(g, n);
   if (st != ADPS_OK) return st;
@@ -503,6 +520,16 @@ static adps_status render_impl(adps_plan* P, void* stream_v, const adps_gaussian
     ba.dominant = dominant + (long long)v * hw;
     ba.weight = weight;
     ba.contrib = contrib_dev;
+    ba.gt = nullptr;
+    if (epi_gt) {   // fused attribution epilogue into the plan's step buffers
+      ba.gt = epi_gt + (long long)v * hw * 3;
+      ba.rawf = P->rawc.as<float>() + (long long)v * hw;
+      ba.lohi = P->lohi.as<unsigned long long>() + 2ll * v;
+      ba.cls = P->cls.as<unsigned char>();
+      ba.N = (int)n;
+      ba.dom_flag = P->dom_flag.as<unsigned char>();
+      ba.cand_bits = P->cand_bits.as<unsigned>() + (long long)v * ((hw + 31) / 32);
+    }
     CK(launch_blend(ba, n_tiles, s));
     P->launches += n_dup > 0 ? 5 : 3;
     P->lib_calls += n_dup > 0 ? 2 : 1;
@@ -570,6 +597,101 @@ static adps_status run_attribution(adps_plan* P, cudaStream_t s, int V, int H, i
   const AttributionArgs a = attr_args(P, V, H, W, cfg, N, image, gt, dominant);
   CK(launch_attribution(a, s, mark_cb, P));
   return ADPS_OK;
+}
+
+// Fused attribution (SURVEY.md 8(d) "K1 epilogue"): select, then the
+// attribution render of the sampled views whose epilogue also writes what the
+// step's input pass would (raw cache, per-view min/max, candidate bits,
+// ever-dominant flags).  The next adps_step_phase1_begin with the same inputs
+// skips select and the input pass and starts from that 8 B/px boundary.
+extern "C" adps_status adps_render_fused(adps_plan* P, void* stream_v, const adps_gaussians* g, int64_t n,
+                                         double extent, const double* grad_accum, const double* denom,
+                                         const adps_config* cfg, const double* cams_host, int32_t n_views,
+                                         const float* bg, const float* gt, float* image, int32_t* dominant) {
+  if (!P) return fail(ADPS_INVALID_ARG, "plan is NULL");
+  P->fused.valid = false;
+  adps_status st = check_gaussians(g, n);
+  if (st != ADPS_OK) return st;
+  if (!cfg) return fail(ADPS_INVALID_ARG, "cfg is NULL");
+  if (n > 0 && (!grad_accum || !denom)) return fail(ADPS_INVALID_ARG, "stats arrays are NULL");
+  if (n_views < 1 || !cams_host || !gt || !image || !dominant) return fail(ADPS_INVALID_ARG, "view arrays are NULL");
+  if (!(extent > 0)) return fail(ADPS_INVALID_ARG, "scene extent must be > 0");
+  CK(cudaSetDevice(P->device));
+  cudaStream_t s = (cudaStream_t)stream_v;
+  const CamD c0 = load_cam(cams_host);
+  const int W = c0.w, H = c0.h, V = n_views;
+  if (W <= 0 || H <= 0) return fail(ADPS_INVALID_ARG, "empty image");
+  for (int v = 1; v < V; ++v) {
+    const CamD cv = load_cam(cams_host + 18ll * v);
+    if (cv.w != W || cv.h != H) return fail(ADPS_INVALID_ARG, "all sampled views must share H x W");
+  }
+  if (n == 0) return render_impl(P, stream_v, g, n, cams_host, n_views, bg, image, dominant, nullptr, nullptr);
+  const long long hw = (long long)H * W;
+  const long long nn = n;
+  CK(ensure(P->cls, nn));
+  CK(ensure(P->cand_rank, 4 * nn));
+  CK(ensure(P->split_list, 4 * nn));
+  CK(ensure(P->clone_list, 4 * nn));
+  CK(ensure(P->dom_flag, nn));
+  CK(ensure(P->lohi, 16ll * V));
+  CK(ensure(P->rawc, 4ll * hw * V));
+  CK(ensure(P->cand_bits, 4ll * V * ((hw + 31) / 32) + 4));
+  CK(ensure(P->ctr, sizeof(Counters)));
+  if (P->cams_host_cap < V) {
+    if (P->cams_host) cudaFreeHost(P->cams_host);
+    if (P->lohi_host) cudaFreeHost(P->lohi_host);
+    CK(cudaMallocHost(&P->cams_host, sizeof(double) * 18 * V));
+    CK(cudaMallocHost(&P->lohi_host, sizeof(unsigned long long) * 2 * V));
+    P->cams_host_cap = V;
+  }
+  Counters* ctr = P->ctr.as<Counters>();
+  CK(cudaMemsetAsync(ctr, 0, sizeof(Counters), s));
+  CK(cudaMemsetAsync(P->dom_flag.p, 0, (size_t)nn, s));
+  CK(cudaMemsetAsync(P->cand_bits.p, 0, 4ll * V * ((hw + 31) / 32) + 4, s));
+  for (int v = 0; v < V; ++v) {
+    P->lohi_host[2 * v] = 0x7ff0000000000000ull;   // +inf
+    P->lohi_host[2 * v + 1] = 0ull;                // +0.0
+  }
+  CK(cudaMemcpyAsync(P->lohi.p, P->lohi_host, sizeof(unsigned long long) * 2 * V, cudaMemcpyHostToDevice, s));
+  ScanState sst;
+  st = scan_state(P, P->scan_val, P->scan_flag, P->scan_ticket, nn, &sst);
+  if (st != ADPS_OK) return st;
+  SelectArgs sa;
+  sa.scale = g->scale;
+  sa.ga = grad_accum;
+  sa.den = denom;
+  sa.tau_g = cfg->tau_g;
+  sa.tau_s_abs = cfg->tau_s * extent;
+  sa.n = n;
+  sa.cls = P->cls.as<unsigned char>();
+  sa.cand_rank = P->cand_rank.as<int>();
+  sa.split_list = P->split_list.as<int>();
+  sa.clone_list = P->clone_list.as<int>();
+  sa.ctr = ctr;
+  CK(launch_select(sa, sst, s));
+  P->launches += 1;
+  st = render_impl(P, stream_v, g, n, cams_host, n_views, bg, image, dominant, nullptr, nullptr, gt);
+  if (st != ADPS_OK) return st;
+  P->fused.valid = true;
+  P->fused.g = *g;
+  P->fused.n = n;
+  P->fused.extent = extent;
+  P->fused.ga = grad_accum;
+  P->fused.den = denom;
+  P->fused.cfg = *cfg;
+  P->fused.V = V;
+  P->fused.H = H;
+  P->fused.W = W;
+  P->fused.image = image;
+  P->fused.gt = gt;
+  P->fused.dom = dominant;
+  P->fused.cams.assign(cams_host, cams_host + 18ll * V);
+  return ADPS_OK;
+}
+
+static bool same_gaussians(const adps_gaussians& a, const adps_gaussians& b) {
+  return a.mu == b.mu && a.scale == b.scale && a.rot == b.rot && a.opacity == b.opacity && a.sh_dc == b.sh_dc &&
+         a.sh_rest == b.sh_rest && a.sh_rest_k == b.sh_rest_k;
 }
 
 extern "C" adps_status adps_step_phase1(adps_plan* P, void* stream_v, const adps_gaussians* g, int64_t n,
@@ -670,8 +792,32 @@ extern "C" adps_status adps_step_phase1_begin(adps_plan* P, void* stream_v, cons
   memcpy(P->cams_host, cams_host, sizeof(double) * 18 * V);
   CK(cudaMemcpyAsync(P->cams.p, P->cams_host, sizeof(double) * 18 * V, cudaMemcpyHostToDevice, s));
   Counters* ctr = P->ctr.as<Counters>();
-  CK(cudaMemsetAsync(ctr, 0, sizeof(Counters), s));
+  // the attribution of a fused render on exactly these inputs (one use)
+  const bool fused = P->fused.valid && P->use_bits && same_gaussians(P->fused.g, *g) && P->fused.n == n &&
+                     P->fused.extent == extent && P->fused.ga == grad_accum && P->fused.den == denom &&
+                     memcmp(&P->fused.cfg, cfg, sizeof(adps_config)) == 0 && P->fused.V == V && P->fused.H == H &&
+                     P->fused.W == W && P->fused.image == image && P->fused.gt == gt && P->fused.dom == dominant &&
+                     P->view_offset == 0 && P->view_stride == 1 && P->v_glob == V &&
+                     memcmp(P->fused.cams.data(), cams_host, sizeof(double) * 18 * V) == 0;
+  P->fused.valid = false;
+  if (!fused) CK(cudaMemsetAsync(ctr, 0, sizeof(Counters), s));
   mark_start(P, s, true);
+  if (fused) {   // select and the input pass ran in the render's epilogue
+    const AttributionArgs a = attr_args(P, V, H, W, cfg, N, image, gt, dominant);
+    P->attr_pending = false;
+    CK(launch_thresholds(a, 0, V, s));
+    CK(launch_fallback_count(P->split_list.as<int>(), P->dom_flag.as<unsigned char>(), ctr, P->sm_count, s));
+    mark(P, "thresholds", s, 2);
+    if (P->pipeline && !P->timing && attribution_warp_path(a)) {   // the CCL on the second stream
+      CK(cudaEventRecord(P->ev_chunk[0], s));
+      CK(cudaStreamWaitEvent(P->aux, P->ev_chunk[0], 0));
+      CK(launch_tiles_views(a, 0, V, P->aux));
+      CK(launch_attribution_tail(a, P->aux, nullptr, nullptr));
+      CK(cudaEventRecord(P->ev_attr, P->aux));
+      P->attr_pending = true;
+      P->launches += (P->use_words ? 2 : 1) + 4;
+    }
+  } else {
 
   // ---- select (ref/adc.py:165)
   ScanState sst;
@@ -741,6 +887,7 @@ extern "C" adps_status adps_step_phase1_begin(adps_plan* P, void* stream_v, cons
       mark(P, "thresholds", s, 2);
     }
   }
+  }   // not fused
   CK(cudaMemcpyAsync(P->ctr_host, ctr, sizeof(Counters), cudaMemcpyDeviceToHost, s));
   CK(cudaStreamSynchronize(s));
   {

@@ -173,7 +173,67 @@ __global__ void tile_ranges_kernel(const unsigned long long* keys, long long n, 
   if (i == n - 1 || (int)(keys[i + 1] >> 32) != t) end[t] = (int)(i + 1);
 }
 
-template <bool STATS>
+// The fused attribution epilogue (BlendArgs::gt set): the stored fp32 image
+// value i and gt give the raw L1 error exactly as the step's input pass
+// computes it (fp64, numpy order: (|d0| + |d1|) + |d2|, no contraction);
+// per-view min/max by a block reduction and two atomics, the candidate bit
+// by one atomicOr per (warp, word), the ever-dominant flag per candidate.
+__device__ __forceinline__ void render_epilogue(const BlendArgs& a, bool inside, int y, int x, float i0, float i1,
+                                                float i2, int bi) {
+  __shared__ double s_lo[kRThreads / 32], s_hi[kRThreads / 32];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  double lo = INFINITY, hi = 0.0;
+  bool cand = false;
+  long long p = 0;
+  if (inside) {
+    p = (long long)y * a.W + x;
+    const float* g3 = a.gt + 3 * p;
+    const double r = __dadd_rn(__dadd_rn(fabs(__dsub_rn((double)i0, (double)g3[0])),
+                                         fabs(__dsub_rn((double)i1, (double)g3[1]))),
+                               fabs(__dsub_rn((double)i2, (double)g3[2])));
+    a.rawf[p] = __double2float_rz(r);
+    lo = r;
+    hi = r;
+    if (bi >= 0 && bi < a.N && __ldg(a.cls + bi) == 1) {
+      cand = true;
+      if (a.dom_flag[bi] == 0) a.dom_flag[bi] = 1;
+    }
+  }
+  // candidate bits: a warp holds two 16-pixel row segments of the tile (lanes
+  // 0-15 and 16-31); each segment's 16 bits land in one or two 32-bit words
+  static_assert(kRTile == 16 && kRThreads == 256, "epilogue: a warp = two 16-pixel tile rows");
+  const unsigned b = __ballot_sync(0xffffffffu, cand);
+  if ((lane & 15) == 0 && y < a.H) {   // lanes 0 and 16: the first pixel of their segment (x may be >= W)
+    const long long p0 = (long long)y * a.W + x;
+    const unsigned seg = (b >> (lane & 16)) & 0xffffu;
+    if (seg) {
+      const unsigned long long w = (unsigned long long)seg << (p0 & 31);
+      if ((unsigned)w) atomicOr(a.cand_bits + (p0 >> 5), (unsigned)w);
+      if ((unsigned)(w >> 32)) atomicOr(a.cand_bits + (p0 >> 5) + 1, (unsigned)(w >> 32));
+    }
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    lo = fmin(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+    hi = fmax(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+  }
+  if (lane == 0) {
+    s_lo[wid] = lo;
+    s_hi[wid] = hi;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w = 1; w < kRThreads / 32; ++w) {
+      lo = fmin(lo, s_lo[w]);
+      hi = fmax(hi, s_hi[w]);
+    }
+    if (lo <= hi) {   // raw >= +0.0: IEEE order == unsigned order of the bit patterns
+      atomicMin(a.lohi + 0, (unsigned long long)__double_as_longlong(lo));
+      atomicMax(a.lohi + 1, (unsigned long long)__double_as_longlong(hi));
+    }
+  }
+}
+
+template <bool STATS, bool EPI>
 __global__ void __launch_bounds__(kRThreads) blend_kernel(BlendArgs a) {
   struct Sm {
     float mx, my, A, B, C, o, r, g, b;
@@ -245,13 +305,16 @@ __global__ void __launch_bounds__(kRThreads) blend_kernel(BlendArgs a) {
     for (int o = 16; o > 0; o >>= 1) n_contrib += __shfl_xor_sync(0xffffffffu, n_contrib, o);
     if ((threadIdx.x & 31) == 0 && n_contrib) atomicAdd(a.contrib, n_contrib);
   }
+  // the composite once: the epilogue must see exactly the stored values
+  const float i0 = cr + T * a.bg[0], i1 = cg + T * a.bg[1], i2 = cbl + T * a.bg[2];
   if (inside) {
     const long long p = (long long)y * a.W + x;
-    a.image[3 * p + 0] = cr + T * a.bg[0];
-    a.image[3 * p + 1] = cg + T * a.bg[1];
-    a.image[3 * p + 2] = cbl + T * a.bg[2];
+    a.image[3 * p + 0] = i0;
+    a.image[3 * p + 1] = i1;
+    a.image[3 * p + 2] = i2;
     a.dominant[p] = bi;
   }
+  if (EPI) render_epilogue(a, inside, y, x, i0, i1, i2, bi);
 }
 
 // ---------------------------------------------------------------- launchers
@@ -279,9 +342,11 @@ cudaError_t launch_tile_ranges(const unsigned long long* keys, long long n, int*
 
 cudaError_t launch_blend(const BlendArgs& a, int n_tiles, cudaStream_t s) {
   if (a.weight || a.contrib)
-    blend_kernel<true><<<n_tiles, kRThreads, 0, s>>>(a);
+    blend_kernel<true, false><<<n_tiles, kRThreads, 0, s>>>(a);
+  else if (a.gt)
+    blend_kernel<false, true><<<n_tiles, kRThreads, 0, s>>>(a);
   else
-    blend_kernel<false><<<n_tiles, kRThreads, 0, s>>>(a);
+    blend_kernel<false, false><<<n_tiles, kRThreads, 0, s>>>(a);
   return cudaGetLastError();
 }
 

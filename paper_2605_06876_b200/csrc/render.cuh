@@ -57,6 +57,19 @@ struct BlendArgs {
   // with alpha >= 1/255.  Either set disables the early termination.
   float* weight;
   unsigned long long* contrib;
+  // fused attribution epilogue (optional; SURVEY.md 8(d) "K1 epilogue"): from
+  // the pixel's stored image value and gt, the raw L1 error in numpy's fp64
+  // order -> its fp32 round-toward-zero cache, the view's min/max, the
+  // candidate bit of the dominant id and its ever-dominant flag -- everything
+  // the densify step's input pass would compute, so the step starts from the
+  // 8 B/px boundary (raw cache + dominant map).  All pointers are the view's.
+  const float* gt;                // [H,W,3] or null (no epilogue)
+  float* rawf;                    // [H*W]
+  unsigned long long* lohi;       // [2]: min / max raw of the view (bit patterns)
+  const unsigned char* cls;       // [N] select classes (1 = split candidate)
+  int N;
+  unsigned char* dom_flag;        // [N]
+  unsigned* cand_bits;            // the view's candidate-bit words (zeroed before)
 };
 
 cudaError_t launch_preprocess(const PreArgs& a, cudaStream_t s);

@@ -34,25 +34,35 @@ constexpr int kWarpsPerBlock = 8;
 #ifndef ADPS_TW_FAST
 #define ADPS_TW_FAST 1
 #endif
+#ifndef ADPS_TW_ROWWISE
+#define ADPS_TW_ROWWISE 0   // 1: the row-wise words pass (ballots) instead of the transposed one
+#endif
 #ifndef ADPS_TW_MINBLOCKS
 #define ADPS_TW_MINBLOCKS 5
 #endif
 
-struct PostSmem {                   // used after the row scan
-  int aux[kWarpMaxRuns];            // fragment id of a root, -1 otherwise
+template <int MR>
+struct PostSmemT {                  // used after the row scan
+  int aux[MR];                      // fragment id of a root, -1 otherwise
   int mom[32][6];
   unsigned char touch[32];
 };
 
-struct WarpSmem {
-  int uf[kWarpMaxRuns];
-  unsigned run[kWarpMaxRuns];       // ty | s << 5 | e << 10 | band << 16
+template <int MR>                   // MR: run capacity of the tile
+struct WarpSmemT {
+  int uf[MR];
+  unsigned run[MR];                 // ty | s << 5 | e << 10 | band << 16
   union {
-    PostSmem post;
+    PostSmemT<MR> post;
     int d[kTileH][kTileW];          // bit-plane path: fp32 raw cache of the tile rows (bit patterns),
                                     // then the dominant ids of keyed pixels
   } u;
 };
+using WarpSmem = WarpSmemT<kWarpMaxRuns>;
+// the deferred tiles (more than kWarpMaxRuns runs) are redone by the same warp
+// kernel with room for every possible run of a 32 x 32 tile
+constexpr int kTileMaxRuns = kTileH * kTileW;
+constexpr int kBigWarpsPerBlock = 4;
 
 size_t tile_warp_smem_bytes() { return sizeof(WarpSmem) * kWarpsPerBlock; }
 
@@ -265,7 +275,8 @@ __device__ __forceinline__ bool scan_row(const RowIn<RAW>& row, const int ey, Ti
 // components of a scanned tile (runs in S, border run ids in st): roots by a
 // read-only find, integer moments per root in closed form per run; interior
 // components >= m_min become regions, edge components fragments + border labels
-__device__ __forceinline__ void finish_tile(const TileParams& P, WarpSmem& S, const int* __restrict__ dom_v,
+template <class WS>
+__device__ __forceinline__ void finish_tile(const TileParams& P, WS& S, const int* __restrict__ dom_v,
                                             const long long tile, const int v, const int x0, const int y0,
                                             const TileRowState& st, const int lane) {
   constexpr unsigned FULL = 0xffffffffu;
@@ -588,6 +599,86 @@ __global__ void __launch_bounds__(256) tile_words_kernel(const float* __restrict
   }
 }
 
+// The same bit planes, transposed: a warp per 32 x 32 pixel block (rows y0..+31
+// of word column tx).  The block's raw cache is staged in shared memory with
+// coalesced cp.async rows, then lane = row builds its row's four words with
+// shifts from 32 conflict-free shared loads (row stride 33 words) -- about 12
+// instructions per pixel-lane instead of a ballot round per word and plane.
+// Ambiguous pixels redo the exact fp64 raw error, exactly as tile_words_kernel.
+__device__ __forceinline__ void cp_async4(void* smem, const void* gmem) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(sa), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
+
+constexpr int kTwWarps = 8;
+__global__ void __launch_bounds__(kTwWarps * 32) tile_words_t_kernel(const float* __restrict__ rawf,
+                                                                    const float* __restrict__ image,
+                                                                    const float* __restrict__ gt,
+                                                                    const unsigned* __restrict__ cand_bits,
+                                                                    const double* __restrict__ thr_raw, int L, int H,
+                                                                    int W, int WW, int v0, uint4* __restrict__ words) {
+  __shared__ int tile[kTwWarps][32][33];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int v = v0 + blockIdx.z;
+  const int tx = blockIdx.x * kTwWarps + wid;
+  if (tx >= WW) return;   // warp-uniform
+  const int y0 = blockIdx.y * 32;
+  const int x0 = tx * 32;
+  const long long hw = (long long)H * W;
+  const int* rv = reinterpret_cast<const int*>(rawf + (long long)v * hw);
+  int (*S)[33] = tile[wid];
+  const bool col_in = x0 + lane < W;
+  const int nrows = H - y0 < 32 ? H - y0 : 32;
+  for (int r = 0; r < nrows; ++r) {
+    if (col_in) cp_async4(&S[r][lane], rv + (long long)(y0 + r) * W + x0 + lane);
+    else S[r][lane] = (int)0xbf800000;   // -1.0f: below every threshold
+  }
+  // thresholds of the view (warp-uniform) while the copies fly
+  const double* tv = thr_raw + (long long)v * L;
+  const double kInf = __longlong_as_double(0x7ff0000000000000ll);
+  const double X0 = __ldg(tv), X1 = L > 1 ? __ldg(tv + 1) : kInf, X2 = L > 2 ? __ldg(tv + 2) : kInf,
+               X3 = L > 3 ? __ldg(tv + 3) : kInf;
+  const RzThreshold R0 = rz_threshold(X0), R1 = rz_threshold(X1), R2 = rz_threshold(X2), R3 = rz_threshold(X3);
+  // candidate word of row y0 + lane
+  const int y = y0 + lane;
+  unsigned C = 0u;
+  if (lane < nrows) {
+    const unsigned* cv = cand_bits + (long long)v * ((hw + 31) / 32);
+    const long long p = (long long)y * W + x0;
+    C = __funnelshift_r(__ldg(cv + (p >> 5)), __ldg(cv + (p >> 5) + 1), (int)(p & 31));
+    const int valid = W - x0;
+    if (valid < 32) C &= (1u << valid) - 1u;
+  }
+  cp_async_wait_all();
+  __syncwarp();
+  if (lane >= nrows) return;
+  unsigned M = 0u, B0 = 0u, B1 = 0u, amb = 0u;
+#pragma unroll
+  for (int x = 0; x < 32; ++x) {
+    const int fi = S[lane][x];
+    const bool t1 = fi >= R1.T, t2 = fi >= R2.T, t3 = fi >= R3.T;
+    M |= (unsigned)(fi >= R0.T) << x;
+    B0 |= (unsigned)(t1 ^ t2 ^ t3) << x;   // band = t1 + t2 + t3 (monotone thresholds): bit 0
+    B1 |= (unsigned)t2 << x;               // bit 1: band >= 2
+    amb |= (unsigned)((fi == R0.A) | (fi == R1.A) | (fi == R2.A) | (fi == R3.A)) << x;
+  }
+  for (; amb; amb &= amb - 1u) {   // rare: the exact fp64 raw error, numpy order
+    const int x = __ffs(amb) - 1;
+    const long long p = (long long)v * hw + (long long)y * W + x0 + x;
+    const float* a3 = image + 3 * p;
+    const float* g3 = gt + 3 * p;
+    const double xr = dadd(dadd(fabs(dsub((double)a3[0], (double)g3[0])), fabs(dsub((double)a3[1], (double)g3[1]))),
+                           fabs(dsub((double)a3[2], (double)g3[2])));
+    const unsigned bit = 1u << x;
+    const int band = (xr >= X1) + (xr >= X2) + (xr >= X3);
+    M = (M & ~bit) | (xr >= X0 ? bit : 0u);
+    B0 = (B0 & ~bit) | ((band & 1) ? bit : 0u);
+    B1 = (B1 & ~bit) | ((band & 2) ? bit : 0u);
+  }
+  words[((long long)v * H + y) * WW + tx] = make_uint4(M, C, B0, B1);
+}
+
 // the word of ext row ey (image row y0 - HL + ey) of tile column tx, and its
 // 64-bit metric mask with the left/right halo bits (bit HL = column x0)
 template <int HL, int HH>
@@ -614,11 +705,6 @@ __device__ __forceinline__ Tv ext_get(Tv a, Tv b, int ey) {
   return ey < 32 ? va : vb;
 }
 
-__device__ __forceinline__ void cp_async4(void* smem, const void* gmem) {
-  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(sa), "l"(gmem) : "memory");
-}
-__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
 
 // The bit planes of one tile computed in place from the fp32 raw cache (no
 // words pass): lane = column, one coalesced row load per needed ext row, the
@@ -628,8 +714,8 @@ __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wai
 // only ext rows inside the erosion window of a candidate row are thresholded.
 // Out: ma / mb = 64-bit metric masks (halo bits included) of ext rows lane and
 // 32 + lane, cw / bw0 / bw1 = candidate and band words of tile row lane.
-template <int HL, int HH>
-__device__ __forceinline__ bool fused_tile_rows(const TileParams& P, WarpSmem& S, int v, int x0, int y0, int lane,
+template <int HL, int HH, class WS>
+__device__ __forceinline__ bool fused_tile_rows(const TileParams& P, WS& S, int v, int x0, int y0, int lane,
                                                 unsigned long long& ma, unsigned long long& mb, unsigned& cw,
                                                 unsigned& bw0, unsigned& bw1) {
   constexpr int SPAN = HL + HH;
@@ -747,19 +833,14 @@ __device__ __forceinline__ bool fused_tile_rows(const TileParams& P, WarpSmem& S
   return true;
 }
 
-template <int R, bool FUSED>
-__global__ void __launch_bounds__(kWarpsPerBlock * 32, ADPS_TW_MINBLOCKS)
-    tile_bits_kernel(TileParams P, const uint4* __restrict__ words, int WW, long long t0, long long t1) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
+template <int R, bool FUSED, int MR>
+__device__ __forceinline__ void tile_bits_body(const TileParams& P, const uint4* __restrict__ words, int WW,
+                                               WarpSmemT<MR>& S, const long long tile, const int lane) {
   constexpr int HL = R > 1 ? R / 2 : 0;
   constexpr int HH = R > 1 ? R - R / 2 - 1 : 0;
   constexpr int SPAN = HL + HH;
   constexpr int NR = kTileH + SPAN;
   constexpr unsigned FULL = 0xffffffffu;
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  WarpSmem& S = reinterpret_cast<WarpSmem*>(smem_raw)[wid];
-  const long long tile = t0 + (long long)blockIdx.x * kWarpsPerBlock + wid;
-  if (tile >= t1) return;   // warp-uniform
   const int tpv = P.tiles_x * P.tiles_y;
   const int v = (int)(tile / tpv);
   const int tin = (int)(tile - (long long)v * tpv);
@@ -853,7 +934,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, ADPS_TW_MINBLOCKS)
   }
   const int n_runs = __shfl_sync(FULL, base, 31);
   base -= my_nr;
-  if (n_runs > kWarpMaxRuns) {
+  if (n_runs > MR) {   // (never for MR = kTileMaxRuns)
     if (lane == 0) P.deferred[atomicAdd(P.n_deferred, 1ull)] = (int)tile;
     return;
   }
@@ -906,6 +987,33 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, ADPS_TW_MINBLOCKS)
   finish_tile(P, S, dom_v, tile, v, x0, y0, st, lane);
 }
 
+template <int R, bool FUSED>
+__global__ void __launch_bounds__(kWarpsPerBlock * 32, ADPS_TW_MINBLOCKS)
+    tile_bits_kernel(TileParams P, const uint4* __restrict__ words, int WW, long long t0, long long t1) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  WarpSmem& S = reinterpret_cast<WarpSmem*>(smem_raw)[wid];
+  const long long tile = t0 + (long long)blockIdx.x * kWarpsPerBlock + wid;
+  if (tile >= t1) return;   // warp-uniform
+  tile_bits_body<R, FUSED, kWarpMaxRuns>(P, words, WW, S, tile, lane);
+}
+
+// the tiles the first pass deferred (more than kWarpMaxRuns runs), a warp each
+// with room for every run a tile can have (so none is deferred again)
+template <int R, bool FUSED>
+__global__ void __launch_bounds__(kBigWarpsPerBlock * 32)
+    tile_bits_deferred_kernel(TileParams P, const uint4* __restrict__ words, int WW) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  WarpSmemT<kTileMaxRuns>& S = reinterpret_cast<WarpSmemT<kTileMaxRuns>*>(smem_raw)[wid];
+  const long long n = (long long)*P.n_deferred;
+  for (long long i = (long long)blockIdx.x * kBigWarpsPerBlock + wid; i < n;
+       i += (long long)gridDim.x * kBigWarpsPerBlock) {
+    tile_bits_body<R, FUSED, kTileMaxRuns>(P, words, WW, S, (long long)P.deferred[i], lane);
+    __syncwarp();
+  }
+}
+
 size_t tile_words_bytes(int V, int H, int W) { return (size_t)V * H * ((W + 31) / 32) * sizeof(uint4); }
 
 template <int R, bool FUSED>
@@ -925,9 +1033,15 @@ cudaError_t launch_tile_bits(const TileParams& P, int v0, int v1, cudaStream_t s
   const int WW = (P.W + 31) / 32;
   const bool fused = P.words == nullptr;
   if (!fused) {
+#if ADPS_TW_ROWWISE
     const unsigned gx = (unsigned)((P.H + 7) / 8);   // warp per image row, 8 rows per block
     tile_words_kernel<<<dim3(gx, (unsigned)(v1 - v0)), 256, 0, s>>>(P.rawf, P.image, P.gt, P.cand_bits, P.thr_raw,
                                                                      P.L, P.H, P.W, WW, v0, P.words);
+#else
+    const dim3 g((unsigned)((WW + kTwWarps - 1) / kTwWarps), (unsigned)((P.H + 31) / 32), (unsigned)(v1 - v0));
+    tile_words_t_kernel<<<g, kTwWarps * 32, 0, s>>>(P.rawf, P.image, P.gt, P.cand_bits, P.thr_raw, P.L, P.H, P.W, WW,
+                                                    v0, P.words);
+#endif
   }
   const long long tpv = (long long)P.tiles_x * P.tiles_y;
   const long long t0 = tpv * v0, t1 = tpv * v1;
@@ -935,6 +1049,27 @@ cudaError_t launch_tile_bits(const TileParams& P, int v0, int v1, cudaStream_t s
     case 1: return fused ? launch_bits_r<1, true>(P, WW, t0, t1, s) : launch_bits_r<1, false>(P, WW, t0, t1, s);
     case 2: return fused ? launch_bits_r<2, true>(P, WW, t0, t1, s) : launch_bits_r<2, false>(P, WW, t0, t1, s);
     case 3: return fused ? launch_bits_r<3, true>(P, WW, t0, t1, s) : launch_bits_r<3, false>(P, WW, t0, t1, s);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+template <int R, bool FUSED>
+static cudaError_t launch_deferred_r(const TileParams& P, int WW, unsigned blocks, cudaStream_t s) {
+  const size_t smem = sizeof(WarpSmemT<kTileMaxRuns>) * kBigWarpsPerBlock;
+  cudaError_t e = cudaFuncSetAttribute(tile_bits_deferred_kernel<R, FUSED>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)smem);
+  if (e != cudaSuccess) return e;
+  tile_bits_deferred_kernel<R, FUSED><<<blocks, kBigWarpsPerBlock * 32, smem, s>>>(P, P.words, WW);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_tile_bits_deferred(const TileParams& P, unsigned blocks, cudaStream_t s) {
+  const int WW = (P.W + 31) / 32;
+  const bool fused = P.words == nullptr;
+  switch (P.r_erode <= 1 ? 1 : P.r_erode) {
+    case 1: return fused ? launch_deferred_r<1, true>(P, WW, blocks, s) : launch_deferred_r<1, false>(P, WW, blocks, s);
+    case 2: return fused ? launch_deferred_r<2, true>(P, WW, blocks, s) : launch_deferred_r<2, false>(P, WW, blocks, s);
+    case 3: return fused ? launch_deferred_r<3, true>(P, WW, blocks, s) : launch_deferred_r<3, false>(P, WW, blocks, s);
     default: return cudaErrorInvalidValue;
   }
 }

@@ -258,6 +258,29 @@ class Plan:
                                         cams.ctypes.data_as(C.c_void_p), v, bgv, _ptr(image), _ptr(dom)))
         return image, dom
 
+    def render_fused(self, g: GaussianTensors, extent, grad_accum, denom, cfg, cams_v, gt_v, bg=(0.0, 0.0, 0.0),
+                     out=None):
+        """Attribution render of the sampled views with the step's input pass
+        fused into its epilogue (adps_render_fused): returns (image, dominant);
+        the next phase1_begin on the same tensors starts from the raw cache."""
+        cams_v = camera_rows(cams_v)
+        v = len(cams_v)
+        w, h = int(cams_v[0, 16]), int(cams_v[0, 17])
+        if out is None:
+            image = torch.empty(v, h, w, 3, dtype=F32, device=self.device)
+            dom = torch.empty(v, h, w, dtype=torch.int32, device=self.device)
+        else:
+            image, dom = out
+        self._check_inputs(grad_accum, denom, image, gt_v, dom)
+        bgv = (C.c_float * 3)(*[float(x) for x in bg])
+        ga = g.abi()
+        cs = config_struct(cfg)
+        _abi.check(self.lib.adps_render_fused(self._h, self._stream(), C.byref(ga), g.n, float(extent),
+                                              _ptr(grad_accum), _ptr(denom), C.byref(cs),
+                                              cams_v.ctypes.data_as(C.c_void_p), v, bgv, _ptr(gt_v), _ptr(image),
+                                              _ptr(dom)))
+        return image, dom
+
     def render_stats(self, g: GaussianTensors, cams: np.ndarray, bg=(0.0, 0.0, 0.0)):
         """(image, dominant, weight [n] fp32, depth complexity): the render plus each
         Gaussian's summed blending weight T*alpha and the mean number of splats with
@@ -682,13 +705,16 @@ class FallbackNormals:
 
 def densify_step(g: GaussianTensors, extent: float, cameras, gt, grad_accum: torch.Tensor,
                  denom: torch.Tensor, cfg, rng, *, renders=None, plan: Plan = None,
-                 view_ids=None, want_report: bool = True, out: GaussianTensors = None) -> StepResult:
+                 view_ids=None, want_report: bool = True, out: GaussianTensors = None,
+                 fused: bool = False) -> StepResult:
     """One AdpSplit densify step on device tensors (ref/adc.py:143-245).
 
     cameras: all C cameras ([C,18] rows or Camera objects).  gt: [C,H,W,3]
     fp32 tensor (or a per-camera sequence).  renders: optional (image,
     dominant) of the sampled views (the stage boundary the reference tests
-    reach by monkeypatching ``adc.render``); rendered on the GPU otherwise.
+    reach by monkeypatching ``adc.render``); rendered on the GPU otherwise --
+    with ``fused`` by the render whose epilogue also runs the step's input
+    pass (adps_render_fused; same results).
     """
     plan = plan or default_plan(g.device)
     cams = camera_rows(cameras)
@@ -696,15 +722,18 @@ def densify_step(g: GaussianTensors, extent: float, cameras, gt, grad_accum: tor
         view_ids = sample_views(len(cams), int(cfg["v_views"] if isinstance(cfg, dict) else cfg.v_views), rng)
     cams_v = cams[view_ids]
     dev = plan.device
-    if renders is None:
+    gt_v = _gather_views(gt, view_ids, dev)
+    grad_accum = grad_accum.to(dev, F64).contiguous()
+    denom = denom.to(dev, F64).contiguous()
+    if renders is None and fused:
+        image, dom = plan.render_fused(g, extent, grad_accum, denom, cfg, cams_v, gt_v)
+    elif renders is None:
         image, dom = plan.render(g, cams_v)
     else:
         image, dom = renders
         image = image.to(dev, F32).contiguous()
         dom = dom.to(dev, torch.int32).contiguous()
-    gt_v = _gather_views(gt, view_ids, dev)
-    counts = plan.phase1_begin(g, extent, grad_accum.to(dev, F64).contiguous(), denom.to(dev, F64).contiguous(),
-                               cfg, cams_v, image, gt_v, dom)
+    counts = plan.phase1_begin(g, extent, grad_accum, denom, cfg, cams_v, image, gt_v, dom)
     nf = counts["n_fallback"]
     draw = FallbackNormals(plan, rng, nf)
     try:

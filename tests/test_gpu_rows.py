@@ -228,3 +228,45 @@ def test_deferred_normals_need_pending_phase1(op, plan):
     rng = np.random.default_rng(0)
     with pytest.raises(Exception, match="phase1_begin"):
         plan.normals_pcg64(rng.bit_generator.state, 12, sync=2)
+
+
+# ---------------------------------------------- fused attribution (render epilogue)
+@pytest.mark.parametrize("which", ["config2", "paper1", "desk3"])
+def test_fused_render_epilogue_matches_two_pass(op, which):
+    """adps_render_fused + the step from the 8 B/px boundary gives exactly the
+    two-pass result (plain render, then the step's own input pass)."""
+    import torch
+    from paper_2605_06876_b200.types import AdpSplitConfig
+    plan = op.Plan("cuda:0")
+    if which.startswith("config"):
+        from paper_2605_06876_b200 import synth as S
+        wl = S.CONFIGS[which]
+        d = wl.build_device(plan)
+        g, extent, cams, gt = d["g"], d["ini"].extent, d["cams"], d["gt_img"]
+        ga, den = (torch.as_tensor(x, device="cuda") for x in d["stats"])
+        cfg = AdpSplitConfig(v_views=len(cams) // 2, n_max=wl.n_max)
+    else:
+        gg, extent = golden_io.scene(DATA, f"step__{which}__in")
+        g = PA.to_tensors(PA.oracle_gaussians_f32(gg))
+        cams = DATA[f"step__{which}__cams"]
+        gt = torch.as_tensor(PA.f32(DATA[f"step__{which}__gt"]), dtype=torch.float32, device="cuda")
+        ga = torch.as_tensor(DATA[f"step__{which}__grad_accum"], device="cuda")
+        den = torch.as_tensor(DATA[f"step__{which}__denom"], device="cuda")
+        cfg = golden_io.Cfg(META["step"][which]["cfg"])
+
+    def digest(res):
+        out = dict(res.gaussians.numpy())
+        out.update({k: v.cpu().numpy() for k, v in res.report_arrays.items()})
+        out.update(index_map=res.index_map.cpu().numpy(), child_parent=res.child_parent.cpu().numpy(),
+                   insert_offset=res.insert_offset.cpu().numpy())
+        return res.counts, out
+
+    for rep in range(2):   # the fused state is one-shot: a second fused step renders again
+        c1, d1 = digest(op.densify_step(g, extent, cams, gt, ga, den, cfg, np.random.default_rng(3), plan=plan,
+                                        fused=True))
+        c2, d2 = digest(op.densify_step(g, extent, cams, gt, ga, den, cfg, np.random.default_rng(3), plan=plan))
+        assert {k: v for k, v in c1.items() if k != "n_partials"} == \
+            {k: v for k, v in c2.items() if k != "n_partials"}
+        for k in d2:
+            np.testing.assert_array_equal(d1[k], d2[k], err_msg=k)
+    assert c1["n_split"] > 0

@@ -3,7 +3,7 @@
 # usage: tools/ab_bench.sh variant1 variant2 ...
 for v in default "$@"; do
   if [ "$v" = default ]; then unset ADPS_LIB; else export ADPS_LIB=$PWD/paper_2605_06876_b200/_variants/libadps_$v.so; fi
-  timeout 300 python bench.py --steps 10 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/ab_$v.log 2>&1
+  timeout 300 python bench.py --steps 10 --warmup 3 --no-cpu-baseline --no-e2e --no-fused > gpurun_out/ab_$v.log 2>&1
   python - "$v" <<'PY'
 import json, sys
 l = [x for x in open(f"gpurun_out/ab_{sys.argv[1]}.log") if x.startswith("{")]
