@@ -601,15 +601,61 @@ cudaError_t launch_remap_rows(const long long* index_map, long long n_out, const
 // grad_accum/denom read + written 32 B).  Grid-stride, two Gaussians per thread
 // per iteration through 16-byte vector loads of the gradient pairs.
 template <class T>
+__device__ __forceinline__ double vg_norm(T x, T y) {
+  const T nrm = sqrt(x * x + y * y);
+  return (double)nrm;
+}
+
+// two Gaussians per thread: grad_accum / denom as double2, the gradient pairs as
+// one 16-byte (fp32) or two 16-byte (fp64) loads, the visibility as a uchar2
+template <class T>
 __global__ void __launch_bounds__(256) accumulate_kernel(double* __restrict__ ga, double* __restrict__ den,
                                                          const T* __restrict__ vg,
                                                          const unsigned char* __restrict__ vis, long long n) {
+  const long long n2 = n >> 1;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n2;
+       i += (long long)gridDim.x * blockDim.x) {
+    const uchar2 v = __ldg(reinterpret_cast<const uchar2*>(vis) + i);
+    if (!(v.x | v.y)) continue;
+    T g[4];
+    if (sizeof(T) == 4) {
+      const float4 q = __ldg(reinterpret_cast<const float4*>(vg) + i);
+      g[0] = q.x; g[1] = q.y; g[2] = q.z; g[3] = q.w;
+    } else {
+      const double2 a = __ldg(reinterpret_cast<const double2*>(vg) + 2 * i);
+      const double2 b = __ldg(reinterpret_cast<const double2*>(vg) + 2 * i + 1);
+      g[0] = a.x; g[1] = a.y; g[2] = b.x; g[3] = b.y;
+    }
+    double2 A = reinterpret_cast<double2*>(ga)[i], D = reinterpret_cast<double2*>(den)[i];
+    if (v.x) {
+      A.x += vg_norm(g[0], g[1]);
+      D.x += 1.0;
+    }
+    if (v.y) {
+      A.y += vg_norm(g[2], g[3]);
+      D.y += 1.0;
+    }
+    reinterpret_cast<double2*>(ga)[i] = A;
+    reinterpret_cast<double2*>(den)[i] = D;
+  }
+  if ((n & 1) && blockIdx.x == 0 && threadIdx.x == 0) {   // the odd last Gaussian
+    const long long i = n - 1;
+    if (vis[i]) {
+      ga[i] += vg_norm(vg[2 * i], vg[2 * i + 1]);
+      den[i] += 1.0;
+    }
+  }
+}
+
+// any alignment: one Gaussian per thread
+template <class T>
+__global__ void __launch_bounds__(256) accumulate1_kernel(double* __restrict__ ga, double* __restrict__ den,
+                                                          const T* __restrict__ vg,
+                                                          const unsigned char* __restrict__ vis, long long n) {
   for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
        i += (long long)gridDim.x * blockDim.x) {
     if (!__ldg(vis + i)) continue;
-    const T x = __ldg(vg + 2 * i), y = __ldg(vg + 2 * i + 1);
-    const T nrm = sqrt(x * x + y * y);
-    ga[i] += (double)nrm;
+    ga[i] += vg_norm(__ldg(vg + 2 * i), __ldg(vg + 2 * i + 1));
     den[i] += 1.0;
   }
 }
@@ -617,9 +663,16 @@ __global__ void __launch_bounds__(256) accumulate_kernel(double* __restrict__ ga
 template <class T>
 static cudaError_t launch_accumulate_t(double* ga, double* den, const T* vg, const unsigned char* vis, long long n,
                                        cudaStream_t s) {
-  if (n > 0) {
+  const bool aligned = ((uintptr_t)ga % 16 == 0) && ((uintptr_t)den % 16 == 0) && ((uintptr_t)vg % 16 == 0) &&
+                       ((uintptr_t)vis % 2 == 0);
+  if (n > 0 && !aligned) {
     long long blocks = (n + 255) / 256;
     if (blocks > 148 * 16) blocks = 148 * 16;
+    accumulate1_kernel<T><<<(unsigned)blocks, 256, 0, s>>>(ga, den, vg, vis, n);
+  } else if (n > 0) {
+    long long blocks = (n / 2 + 255) / 256;
+    if (blocks > 148 * 16) blocks = 148 * 16;
+    if (blocks < 1) blocks = 1;
     accumulate_kernel<T><<<(unsigned)blocks, 256, 0, s>>>(ga, den, vg, vis, n);
   }
   return cudaGetLastError();
