@@ -11,7 +11,7 @@ namespace adps {
 // proposals per Morton tile of a large parent's gate matrix (exact pruning unit)
 constexpr int kMT = ADPS_MERGE_TILE;
 #ifndef ADPS_MORTON_BITS
-#define ADPS_MORTON_BITS 9
+#define ADPS_MORTON_BITS 6
 #endif
 constexpr int kMortonBits = ADPS_MORTON_BITS;   // per axis (<= 10)
 

@@ -223,10 +223,10 @@ def compare_step(gres, ores: O.StepResult, flagged: set, g_in: O.Gaussians, stri
     n_ins_g = len(g_par) - len(rep.clones)
     assert (g_par[n_ins_g:] == np.array(ores.clones, dtype=np.int64)).all()
     n_ins_o = len(o_par) - len(ores.clones)
-    for j in range(len(ores.clones)):   # clones: exact copies
-        o_rows_c, g_rows_c = o_keep + n_ins_o + j, g_keep + n_ins_g + j
-        for f in ("mu", "scale", "rot", "opacity", "sh_dc"):
-            np.testing.assert_array_equal(out[f][g_rows_c], f32(getattr(og, f))[o_rows_c], err_msg=f)
+    nc = len(ores.clones)   # clones: exact copies
+    for f in ("mu", "scale", "rot", "opacity", "sh_dc"):
+        np.testing.assert_array_equal(out[f][g_keep + n_ins_g:g_keep + n_ins_g + nc],
+                                      f32(getattr(og, f)[o_keep + n_ins_o:o_keep + n_ins_o + nc]), err_msg=f)
     if not mism:
         assert rep.count_after == ores.count_after
         assert rep.merge_edges == ores.merge_edges
