@@ -23,7 +23,7 @@
 #include "attribution.cuh"
 
 #ifndef ADPS_DEFERRED_BLOCK
-#define ADPS_DEFERRED_BLOCK 0   // 1: deferred tiles by the block CCL (tile_kernel) instead of the big warp kernel
+#define ADPS_DEFERRED_BLOCK 1   // 0: deferred tiles by the full-capacity warp kernel instead of the block CCL
 #endif
 
 namespace adps {
