@@ -22,6 +22,9 @@
 #include "adps_internal.cuh"
 #include "attribution.cuh"
 
+#ifndef ADPS_INPUT_BULK
+#define ADPS_INPUT_BULK 1   // the input pass through cp.async.bulk + mbarrier stages (minmax_bulk_kernel)
+#endif
 #ifndef ADPS_DEFERRED_BLOCK
 #define ADPS_DEFERRED_BLOCK 1   // 0: deferred tiles by the full-capacity warp kernel instead of the block CCL
 #endif
@@ -197,6 +200,272 @@ __global__ void __launch_bounds__(256) minmax2_kernel(const float* __restrict__ 
       atomicMax(&lohi[2 * v + 1], (unsigned long long)__double_as_longlong(hi));
     }
   }
+}
+
+// ------------------------------------------------- input pass, bulk-copy form
+// The same input pass over the flat pixel stream of views [v0, v1) (every view
+// starts at pixel v*hw; hw even), staged through shared memory by the bulk
+// copy engine: one elected thread issues three cp.async.bulk copies per
+// 1024-pixel chunk (image 12 KB, gt 12 KB, dominant 4 KB; SASS UBLKCP) into a
+// 3-stage ring completed by mbarrier transaction counts, and the 512 threads
+// read their pixel pairs from shared memory.  A persistent block walks a
+// contiguous chunk range (at most two views per chunk: hw >= 16384), keeping
+// the min/max of the current and the next view in registers and flushing
+// them with a block reduction when the view advances.  Candidate bits: the
+// warp's 64 pixels map to at most three words of the view's bit array (view
+// starts are not word aligned), OR-ed in with atomics (zeroed beforehand).
+constexpr int kMBThreads = 512;
+constexpr int kMBChunk = 2 * kMBThreads;   // pixels per stage
+constexpr int kMBStages = 3;
+struct MBStage {
+  float img[3 * kMBChunk];
+  float gt[3 * kMBChunk];
+  int dom[kMBChunk];
+};
+constexpr size_t kMBSmem = sizeof(MBStage) * kMBStages + 64;
+
+__device__ __forceinline__ void mbar_init(unsigned long long* bar, unsigned count) {
+  const unsigned a = (unsigned)__cvta_generic_to_shared(bar);
+  asm volatile("mbarrier.init.shared.b64 [%0], %1;" ::"r"(a), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long* bar, unsigned bytes) {
+  const unsigned a = (unsigned)__cvta_generic_to_shared(bar);
+  asm volatile("mbarrier.arrive.expect_tx.shared.b64 _, [%0], %1;" ::"r"(a), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned phase) {
+  const unsigned a = (unsigned)__cvta_generic_to_shared(bar);
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(a),
+      "r"(phase)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, unsigned long long* bar) {
+  const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+  const unsigned b = (unsigned)__cvta_generic_to_shared(bar);
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(d),
+               "l"(src), "r"(bytes), "r"(b)
+               : "memory");
+}
+
+// interleave: bit 2l = a bit l, bit 2l+1 = b bit l
+__device__ __forceinline__ unsigned long long interleave32(unsigned a, unsigned b) {
+  auto spread = [](unsigned long long x) {
+    x = (x | (x << 16)) & 0x0000FFFF0000FFFFull;
+    x = (x | (x << 8)) & 0x00FF00FF00FF00FFull;
+    x = (x | (x << 4)) & 0x0F0F0F0F0F0F0F0Full;
+    x = (x | (x << 2)) & 0x3333333333333333ull;
+    x = (x | (x << 1)) & 0x5555555555555555ull;
+    return x;
+  };
+  return spread(a) | (spread(b) << 1);
+}
+
+struct BulkArgs {
+  const float* image;   // view 0 of the plan's arrays (flat pixel p at image + 3p)
+  const float* gt;
+  const int* dom;
+  long long p0, p1;     // flat pixel range [v0*hw, v1*hw)
+  long long hw;
+  unsigned long long* lohi;
+  const unsigned char* cls;
+  int N;
+  unsigned char* dom_flag;
+  unsigned* cand_bits;  // [V][nwords], zeroed
+  float* rawf;          // flat
+};
+
+__global__ void __launch_bounds__(kMBThreads) minmax_bulk_kernel(BulkArgs a) {
+  extern __shared__ __align__(128) unsigned char mb_smem[];
+  MBStage* stage = reinterpret_cast<MBStage*>(mb_smem);
+  unsigned long long* full = reinterpret_cast<unsigned long long*>(mb_smem + sizeof(MBStage) * kMBStages);
+  __shared__ double s_lo[2][kMBThreads / 32], s_hi[2][kMBThreads / 32];
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const long long n_px = a.p1 - a.p0;
+  const long long n_chunks = (n_px + kMBChunk - 1) / kMBChunk;
+  const long long c_lo = n_chunks * blockIdx.x / gridDim.x, c_hi = n_chunks * (blockIdx.x + 1) / gridDim.x;
+  const long long nwords = (a.hw + 31) / 32;
+  auto chunk_full = [&](long long c) { return a.p0 + (c + 1) * kMBChunk <= a.p1; };
+  auto issue = [&](long long c) {   // thread 0: the three copies of chunk c into its stage
+    const int st = (int)((c - c_lo) % kMBStages);
+    const long long pc = a.p0 + c * kMBChunk;
+    mbar_expect_tx(&full[st], (unsigned)(sizeof(MBStage)));
+    bulk_g2s(stage[st].img, a.image + 3 * pc, 12u * kMBChunk, &full[st]);
+    bulk_g2s(stage[st].gt, a.gt + 3 * pc, 12u * kMBChunk, &full[st]);
+    bulk_g2s(stage[st].dom, a.dom + pc, 4u * kMBChunk, &full[st]);
+  };
+  if (tid == 0) {
+    for (int i = 0; i < kMBStages; ++i) mbar_init(&full[i], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  if (tid == 0)
+    for (long long c = c_lo; c < c_lo + kMBStages && c < c_hi; ++c)
+      if (chunk_full(c)) issue(c);
+  long long cv = c_lo < c_hi ? (a.p0 + c_lo * kMBChunk) / a.hw : 0;   // current view (block-uniform)
+  double lo[2] = {INFINITY, INFINITY}, hi[2] = {0.0, 0.0};        // [0] view cv, [1] view cv + 1
+  auto flush = [&](long long v, double l, double h) {               // block-uniform call
+    for (int o = 16; o > 0; o >>= 1) {
+      l = fmin(l, __shfl_xor_sync(0xffffffffu, l, o));
+      h = fmax(h, __shfl_xor_sync(0xffffffffu, h, o));
+    }
+    if (lane == 0) {
+      s_lo[0][wid] = l;
+      s_hi[0][wid] = h;
+    }
+    __syncthreads();
+    if (tid == 0) {
+      for (int w = 1; w < kMBThreads / 32; ++w) {
+        l = fmin(l, s_lo[0][w]);
+        h = fmax(h, s_hi[0][w]);
+      }
+      if (l <= h) {   // raw >= +0.0: IEEE order == unsigned order of the bit patterns
+        atomicMin(&a.lohi[2 * v + 0], (unsigned long long)__double_as_longlong(l));
+        atomicMax(&a.lohi[2 * v + 1], (unsigned long long)__double_as_longlong(h));
+      }
+    }
+    __syncthreads();
+  };
+  for (long long c = c_lo; c < c_hi; ++c) {
+    const long long pc = a.p0 + c * kMBChunk;
+    const long long vA = pc / a.hw;
+    while (vA > cv) {   // the block moved past view cv: publish it (block-uniform)
+      flush(cv, lo[0], hi[0]);
+      lo[0] = lo[1];
+      hi[0] = hi[1];
+      lo[1] = INFINITY;
+      hi[1] = 0.0;
+      ++cv;
+    }
+    const bool fullc = chunk_full(c);
+    const int st = (int)((c - c_lo) % kMBStages);
+    const long long p = pc + 2 * tid;   // flat, even
+    const bool in = p < a.p1;
+    float i6[6] = {0, 0, 0, 0, 0, 0}, g6[6] = {0, 0, 0, 0, 0, 0};
+    int d0 = -1, d1 = -1;
+    if (fullc) {
+      mbar_wait(&full[st], (unsigned)(((c - c_lo) / kMBStages) & 1));
+      const float2* si = reinterpret_cast<const float2*>(stage[st].img) + 3 * tid;
+      const float2* sg = reinterpret_cast<const float2*>(stage[st].gt) + 3 * tid;
+#pragma unroll
+      for (int k = 0; k < 3; ++k) {
+        const float2 x = si[k], y = sg[k];
+        i6[2 * k] = x.x;
+        i6[2 * k + 1] = x.y;
+        g6[2 * k] = y.x;
+        g6[2 * k + 1] = y.y;
+      }
+      const int2 dd = reinterpret_cast<const int2*>(stage[st].dom)[tid];
+      d0 = dd.x;
+      d1 = dd.y;
+    } else if (in) {   // the partial last chunk: straight from global
+#pragma unroll
+      for (int k = 0; k < 6; ++k) {
+        i6[k] = __ldg(a.image + 3 * p + k);
+        g6[k] = __ldg(a.gt + 3 * p + k);
+      }
+      d0 = __ldg(a.dom + p);
+      d1 = __ldg(a.dom + p + 1);
+    }
+    const long long v = in ? p / a.hw : cv;   // both pixels of the pair are in view v (hw even)
+    bool c0 = false, c1 = false;
+    if (in) {
+      const double r0 = raw_l1_3(i6[0], i6[1], i6[2], g6[0], g6[1], g6[2]);
+      const double r1 = raw_l1_3(i6[3], i6[4], i6[5], g6[3], g6[4], g6[5]);
+      reinterpret_cast<float2*>(a.rawf)[p >> 1] = make_float2(__double2float_rz(r0), __double2float_rz(r1));
+      const int k = v == cv ? 0 : 1;
+      lo[k] = fmin(lo[k], fmin(r0, r1));
+      hi[k] = fmax(hi[k], fmax(r0, r1));
+      if (d0 >= 0 && d0 < a.N && __ldg(a.cls + d0) == 1) {
+        c0 = true;
+        if (a.dom_flag[d0] == 0) a.dom_flag[d0] = 1;
+      }
+      if (d1 == d0) {
+        c1 = c0;
+      } else if (d1 >= 0 && d1 < a.N && __ldg(a.cls + d1) == 1) {
+        c1 = true;
+        if (a.dom_flag[d1] == 0) a.dom_flag[d1] = 1;
+      }
+    }
+    // candidate bits of the warp's 64 pixels [pw, pw + 64)
+    const unsigned b0 = __ballot_sync(0xffffffffu, c0), b1 = __ballot_sync(0xffffffffu, c1);
+    const long long pw = pc + 64 * wid;
+    const long long vw = pw / a.hw, vw_end = (pw + 63) / a.hw;
+    if (vw == vw_end) {   // one view: at most three words
+      if (lane < 3 && (b0 | b1)) {
+        const unsigned long long m = interleave32(b0, b1);
+        const long long q0 = pw - vw * a.hw;
+        const int sft = (int)(q0 & 31);
+        const unsigned long long lo64 = m << sft, hi64 = sft ? m >> (64 - sft) : 0ull;
+        const unsigned w = lane == 0 ? (unsigned)lo64 : (lane == 1 ? (unsigned)(lo64 >> 32) : (unsigned)hi64);
+        if (w) atomicOr(a.cand_bits + vw * nwords + (q0 >> 5) + lane, w);
+      }
+    } else {               // the warp straddles a view boundary: per pixel
+      if (c0) {
+        const long long q = p - v * a.hw;
+        atomicOr(a.cand_bits + v * nwords + (q >> 5), 1u << (q & 31));
+      }
+      if (c1) {
+        const long long q = p + 1 - v * a.hw;
+        atomicOr(a.cand_bits + v * nwords + (q >> 5), 1u << (q & 31));
+      }
+    }
+    __syncthreads();   // stage st fully consumed
+    if (tid == 0 && c + kMBStages < c_hi && chunk_full(c + kMBStages)) issue(c + kMBStages);
+  }
+  if (c_lo < c_hi) {
+    flush(cv, lo[0], hi[0]);
+    if (cv + 1 < (a.p1 + a.hw - 1) / a.hw) flush(cv + 1, lo[1], hi[1]);
+  }
+}
+
+bool minmax_bulk_ok(const AttributionArgs& a, int v0, int v1) {
+  const long long hw = (long long)a.H * a.W;
+  const long long p0 = hw * v0;
+  return ADPS_INPUT_BULK && a.rawf && !a.raw && hw % 2 == 0 && hw >= 16384 && p0 % 4 == 0 &&
+         (uintptr_t)a.image % 16 == 0 && (uintptr_t)a.gt % 16 == 0 && (uintptr_t)a.dom % 16 == 0 &&
+         (uintptr_t)a.rawf % 16 == 0 && v1 > v0;
+}
+
+cudaError_t launch_minmax_bulk(const AttributionArgs& a, int v0, int v1, cudaStream_t s) {
+  const long long hw = (long long)a.H * a.W;
+  BulkArgs b;
+  b.image = a.image;
+  b.gt = a.gt;
+  b.dom = a.dom;
+  b.p0 = hw * v0;
+  b.p1 = hw * v1;
+  b.hw = hw;
+  b.lohi = a.lohi;
+  b.cls = a.cls;
+  b.N = a.N;
+  b.dom_flag = a.dom_flag;
+  b.cand_bits = a.cand_bits;
+  b.rawf = a.rawf;
+  const long long nwords = (hw + 31) / 32;
+  cudaError_t e = cudaMemsetAsync(a.cand_bits + (long long)v0 * nwords, 0, 4ull * nwords * (v1 - v0), s);
+  if (e != cudaSuccess) return e;
+  static int per_sm = 0, sms = 148;
+  if (per_sm == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    e = cudaFuncSetAttribute(minmax_bulk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kMBSmem);
+    if (e != cudaSuccess) return e;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, minmax_bulk_kernel, kMBThreads, kMBSmem) !=
+            cudaSuccess ||
+        per_sm < 1)
+      per_sm = 1;
+  }
+  const long long chunks = (b.p1 - b.p0 + kMBChunk - 1) / kMBChunk;
+  long long grid = (long long)per_sm * sms;
+  if (grid > chunks) grid = chunks;
+  minmax_bulk_kernel<<<(unsigned)grid, kMBThreads, kMBSmem, s>>>(b);
+  return cudaGetLastError();
 }
 
 // e(x) = x / d with x = fl(raw - lo) and d = fl(hi - lo); both predicates below
@@ -724,6 +993,7 @@ size_t tile_smem_bytes() { return sizeof(TileSmem); }
 
 cudaError_t launch_minmax_kernel(const AttributionArgs& a, int v0, int v1, cudaStream_t s) {
   if (v1 <= v0) return cudaSuccess;
+  if (minmax_bulk_ok(a, v0, v1)) return launch_minmax_bulk(a, v0, v1, s);
   const long long hw = (long long)a.H * a.W;
   if (hw % 2 == 0 && hw < (1ll << 30)) {   // pixel pairs (float2 / int2 loads)
     // one wave of resident blocks over the whole launch, each looping over many
