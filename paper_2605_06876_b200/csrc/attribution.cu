@@ -23,7 +23,7 @@
 #include "attribution.cuh"
 
 #ifndef ADPS_INPUT_BULK
-#define ADPS_INPUT_BULK 1   // the input pass through cp.async.bulk + mbarrier stages (minmax_bulk_kernel)
+#define ADPS_INPUT_BULK 0   // 1: the input pass through cp.async.bulk + mbarrier stages (minmax_bulk_kernel; slower)
 #endif
 #ifndef ADPS_DEFERRED_BLOCK
 #define ADPS_DEFERRED_BLOCK 1   // 0: deferred tiles by the full-capacity warp kernel instead of the block CCL
@@ -330,6 +330,50 @@ __global__ void __launch_bounds__(kMBThreads) minmax_bulk_kernel(BulkArgs a) {
     }
     __syncthreads();
   };
+  // candidate bits + ever-dominant flags of a chunk, one iteration late: the
+  // class gathers of chunk c are issued with its loads and consumed after the
+  // next chunk's wait, so their latency hides behind it
+  auto finish_cand = [&](long long pc, int d0, int d1, unsigned char k0, unsigned char k1) {   // block-uniform
+    const long long p = pc + 2 * tid;
+    const bool in = p < a.p1;
+    const bool c0 = in && k0 == 1, c1 = in && k1 == 1;
+    // ever-dominant flags: one store per distinct candidate id of the warp (no read)
+    {
+      const int key0 = c0 ? d0 : -1;
+      const unsigned peers0 = __match_any_sync(0xffffffffu, key0);
+      if (c0 && lane == __ffs(peers0) - 1) a.dom_flag[d0] = 1;
+      const int key1 = c1 && d1 != d0 ? d1 : -1;
+      const unsigned peers1 = __match_any_sync(0xffffffffu, key1);
+      if (key1 >= 0 && lane == __ffs(peers1) - 1) a.dom_flag[d1] = 1;
+    }
+    const unsigned b0 = __ballot_sync(0xffffffffu, c0), b1 = __ballot_sync(0xffffffffu, c1);
+    if (!(b0 | b1)) return;
+    const long long pw = pc + 64 * wid;
+    const long long vw = pw / a.hw, vw_end = (pw + 63) / a.hw;
+    if (vw == vw_end) {   // one view: at most three words
+      if (lane < 3) {
+        const unsigned long long m = interleave32(b0, b1);
+        const long long q0 = pw - vw * a.hw;
+        const int sft = (int)(q0 & 31);
+        const unsigned long long lo64 = m << sft, hi64 = sft ? m >> (64 - sft) : 0ull;
+        const unsigned w = lane == 0 ? (unsigned)lo64 : (lane == 1 ? (unsigned)(lo64 >> 32) : (unsigned)hi64);
+        if (w) atomicOr(a.cand_bits + vw * nwords + (q0 >> 5) + lane, w);
+      }
+    } else {              // the warp straddles a view boundary: per pixel
+      const long long v = p / a.hw;
+      if (c0) {
+        const long long q = p - v * a.hw;
+        atomicOr(a.cand_bits + v * nwords + (q >> 5), 1u << (q & 31));
+      }
+      if (c1) {
+        const long long q = p + 1 - v * a.hw;
+        atomicOr(a.cand_bits + v * nwords + (q >> 5), 1u << (q & 31));
+      }
+    }
+  };
+  long long prev_pc = -1;
+  int pd0 = -1, pd1 = -1;
+  unsigned char pk0 = 0, pk1 = 0;
   for (long long c = c_lo; c < c_hi; ++c) {
     const long long pc = a.p0 + c * kMBChunk;
     const long long vA = pc / a.hw;
@@ -349,6 +393,17 @@ __global__ void __launch_bounds__(kMBThreads) minmax_bulk_kernel(BulkArgs a) {
     int d0 = -1, d1 = -1;
     if (fullc) {
       mbar_wait(&full[st], (unsigned)(((c - c_lo) / kMBStages) & 1));
+      const int2 dd = reinterpret_cast<const int2*>(stage[st].dom)[tid];
+      d0 = dd.x;
+      d1 = dd.y;
+    } else if (in) {   // the partial last chunk: straight from global
+      d0 = __ldg(a.dom + p);
+      d1 = __ldg(a.dom + p + 1);
+    }
+    // class gathers of this chunk (consumed next iteration)
+    const unsigned char k0 = d0 >= 0 && d0 < a.N ? __ldg(a.cls + d0) : 0;
+    const unsigned char k1 = d1 == d0 ? k0 : (d1 >= 0 && d1 < a.N ? __ldg(a.cls + d1) : 0);
+    if (fullc) {
       const float2* si = reinterpret_cast<const float2*>(stage[st].img) + 3 * tid;
       const float2* sg = reinterpret_cast<const float2*>(stage[st].gt) + 3 * tid;
 #pragma unroll
@@ -359,64 +414,32 @@ __global__ void __launch_bounds__(kMBThreads) minmax_bulk_kernel(BulkArgs a) {
         g6[2 * k] = y.x;
         g6[2 * k + 1] = y.y;
       }
-      const int2 dd = reinterpret_cast<const int2*>(stage[st].dom)[tid];
-      d0 = dd.x;
-      d1 = dd.y;
-    } else if (in) {   // the partial last chunk: straight from global
+    } else if (in) {
 #pragma unroll
       for (int k = 0; k < 6; ++k) {
         i6[k] = __ldg(a.image + 3 * p + k);
         g6[k] = __ldg(a.gt + 3 * p + k);
       }
-      d0 = __ldg(a.dom + p);
-      d1 = __ldg(a.dom + p + 1);
     }
-    const long long v = in ? p / a.hw : cv;   // both pixels of the pair are in view v (hw even)
-    bool c0 = false, c1 = false;
     if (in) {
+      const long long v = p / a.hw;   // both pixels of the pair are in view v (hw even)
       const double r0 = raw_l1_3(i6[0], i6[1], i6[2], g6[0], g6[1], g6[2]);
       const double r1 = raw_l1_3(i6[3], i6[4], i6[5], g6[3], g6[4], g6[5]);
       reinterpret_cast<float2*>(a.rawf)[p >> 1] = make_float2(__double2float_rz(r0), __double2float_rz(r1));
       const int k = v == cv ? 0 : 1;
       lo[k] = fmin(lo[k], fmin(r0, r1));
       hi[k] = fmax(hi[k], fmax(r0, r1));
-      if (d0 >= 0 && d0 < a.N && __ldg(a.cls + d0) == 1) {
-        c0 = true;
-        if (a.dom_flag[d0] == 0) a.dom_flag[d0] = 1;
-      }
-      if (d1 == d0) {
-        c1 = c0;
-      } else if (d1 >= 0 && d1 < a.N && __ldg(a.cls + d1) == 1) {
-        c1 = true;
-        if (a.dom_flag[d1] == 0) a.dom_flag[d1] = 1;
-      }
     }
-    // candidate bits of the warp's 64 pixels [pw, pw + 64)
-    const unsigned b0 = __ballot_sync(0xffffffffu, c0), b1 = __ballot_sync(0xffffffffu, c1);
-    const long long pw = pc + 64 * wid;
-    const long long vw = pw / a.hw, vw_end = (pw + 63) / a.hw;
-    if (vw == vw_end) {   // one view: at most three words
-      if (lane < 3 && (b0 | b1)) {
-        const unsigned long long m = interleave32(b0, b1);
-        const long long q0 = pw - vw * a.hw;
-        const int sft = (int)(q0 & 31);
-        const unsigned long long lo64 = m << sft, hi64 = sft ? m >> (64 - sft) : 0ull;
-        const unsigned w = lane == 0 ? (unsigned)lo64 : (lane == 1 ? (unsigned)(lo64 >> 32) : (unsigned)hi64);
-        if (w) atomicOr(a.cand_bits + vw * nwords + (q0 >> 5) + lane, w);
-      }
-    } else {               // the warp straddles a view boundary: per pixel
-      if (c0) {
-        const long long q = p - v * a.hw;
-        atomicOr(a.cand_bits + v * nwords + (q >> 5), 1u << (q & 31));
-      }
-      if (c1) {
-        const long long q = p + 1 - v * a.hw;
-        atomicOr(a.cand_bits + v * nwords + (q >> 5), 1u << (q & 31));
-      }
-    }
+    if (prev_pc >= 0) finish_cand(prev_pc, pd0, pd1, pk0, pk1);
+    prev_pc = pc;
+    pd0 = d0;
+    pd1 = d1;
+    pk0 = k0;
+    pk1 = k1;
     __syncthreads();   // stage st fully consumed
     if (tid == 0 && c + kMBStages < c_hi && chunk_full(c + kMBStages)) issue(c + kMBStages);
   }
+  if (prev_pc >= 0) finish_cand(prev_pc, pd0, pd1, pk0, pk1);
   if (c_lo < c_hi) {
     flush(cv, lo[0], hi[0]);
     if (cv + 1 < (a.p1 + a.hw - 1) / a.hw) flush(cv + 1, lo[1], hi[1]);
