@@ -137,6 +137,11 @@ ADPS_API const char* adps_last_error(void);
 ADPS_API adps_status adps_plan_create(adps_plan** plan, int32_t device, int64_t max_n,
                              int32_t max_views, int32_t height, int32_t width);
 ADPS_API adps_status adps_plan_destroy(adps_plan* plan);
+/* Debug: every plan buffer has a guard zone past its usable size, filled at
+ * allocation; after a device sync, *bad_bytes = guard bytes some kernel
+ * overwrote (0 = no out-of-bounds write past any plan buffer), *bad_buffers =
+ * buffers affected (may be NULL). */
+ADPS_API adps_status adps_check_guards(adps_plan* plan, int64_t* bad_bytes, int32_t* bad_buffers);
 
 /* Attribution render of n_views cameras: image [V,H,W,3] fp32 and dominant
  * map [V,H,W] int32 (-1 where nothing contributes).

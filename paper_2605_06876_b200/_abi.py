@@ -68,7 +68,7 @@ EXPORTS = (
     "adps_step_phase1_import", "adps_step_phase1_merge", "adps_vanilla_phase1", "adps_reset_flags",
     "adps_remap_rows", "adps_set_parent_sharding", "adps_get_shard", "adps_step_phase1_finish",
     "adps_copy_report", "adps_accumulate_stats_f64", "adps_prune_index", "adps_render_stats",
-    "adps_render_fused",
+    "adps_render_fused", "adps_check_guards",
 )
 
 _lib = None
@@ -89,6 +89,7 @@ def load(path: str = LIB_PATH):
     lib.adps_plan_create.argtypes = [C.POINTER(vp), C.c_int32, C.c_int64, C.c_int32, C.c_int32, C.c_int32]
     lib.adps_plan_destroy.argtypes = [vp]
     lib.adps_render.argtypes = [vp, vp, C.POINTER(Gaussians), C.c_int64, vp, C.c_int32, vp, vp, vp]
+    lib.adps_check_guards.argtypes = [vp, C.POINTER(C.c_int64), C.POINTER(C.c_int32)]
     lib.adps_render_fused.argtypes = [vp, vp, C.POINTER(Gaussians), C.c_int64, C.c_double, vp, vp,
                                       C.POINTER(Config), vp, C.c_int32, vp, vp, vp, vp]
     lib.adps_render_stats.argtypes = [vp, vp, C.POINTER(Gaussians), C.c_int64, vp, C.c_int32, vp, vp, vp, vp,

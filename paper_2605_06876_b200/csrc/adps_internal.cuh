@@ -305,4 +305,24 @@ __device__ __forceinline__ void uf_unite(int* p, int a, int b) {
   }
 }
 
+// uf_unite that returns the root the two trees now share (the smaller of the
+// two roots found; later links elsewhere may hang it below an even smaller
+// one, but a and b stay in the same tree under it)
+__device__ __forceinline__ int uf_unite_root(int* p, int a, int b) {
+  volatile int* vp = p;
+  while (true) {
+    a = uf_find_halve(vp, a);
+    b = uf_find_halve(vp, b);
+    if (a == b) return a;
+    if (a > b) {
+      int t = a;
+      a = b;
+      b = t;
+    }
+    int old = atomicMin(&p[b], a);
+    if (old == b) return a;
+    b = old;
+  }
+}
+
 }  // namespace adps

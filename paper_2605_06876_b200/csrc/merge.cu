@@ -613,6 +613,9 @@ __device__ __forceinline__ void stage_col(const MergeArgs& a, ColTile& B, long l
 // while the row lasts, the column tile staged in shared memory one pair ahead
 // (cp.async), no block barriers.  If the survivor list overflowed, every tile
 // pair is taken with the box test inline.
+#ifndef ADPS_PAIR_ROOT_CACHE
+#define ADPS_PAIR_ROOT_CACHE 1   // skip unions of columns already hanging below the row's cached root
+#endif
 #ifndef ADPS_PAIR_MINB
 #define ADPS_PAIR_MINB 1
 #endif
@@ -674,6 +677,7 @@ __global__ void __launch_bounds__(kPairWarps * 32, ADPS_PAIR_MINB) pair_tiles_ke
   float4 am = make_float4(0.f, 0.f, 0.f, 0.f), ac = am;
   float ma_mu = 0.f, ma_rgb = 0.f;   // the row tile's largest |mu_c|, |rgb_c| (fp32 copies)
   int qa = -1, ni = 0;
+  int ra = -1;   // a root qa was last united under (this row tile)
   const float gc32 = (float)gc, gd2s = (float)(gd * gd) * (1.0f + 1e-5f) * (1.0f + 2e-5f);
   // entries are prefetched two ahead (registers), column tiles one ahead (cp.async)
   int4 cur = pair_at(i_cur);
@@ -684,6 +688,7 @@ __global__ void __launch_bounds__(kPairWarps * 32, ADPS_PAIR_MINB) pair_tiles_ke
     const int4 nn = pair_at(i_nn);
     if (cur.x != cur_row) {   // new tile row: its operands into registers
       cur_row = cur.x;
+      ra = -1;
       ni = cur.z & 0xff;
       const long long m = (long long)cur.x + lane;
       am = ac = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -771,7 +776,13 @@ __global__ void __launch_bounds__(kPairWarps * 32, ADPS_PAIR_MINB) pair_tiles_ke
         __syncwarp();
       }
 #else
-      for (; pass; pass &= pass - 1u) uf_unite(a.uf, qa, J.q[__ffs(pass) - 1]);
+      // a column already hanging directly below the root this row proposal was
+      // last united under is in its tree: one load instead of two finds
+      for (; pass; pass &= pass - 1u) {
+        const int qb = J.q[__ffs(pass) - 1];
+        if (ADPS_PAIR_ROOT_CACHE && ra >= 0 && reinterpret_cast<volatile int*>(a.uf)[qb] == ra) continue;
+        ra = uf_unite_root(a.uf, qa, qb);
+      }
 #endif
     }
     __syncwarp();   // this buffer is restaged two pairs on

@@ -64,14 +64,23 @@ struct Buf {
   }
 };
 
+// Every plan buffer carries a guard zone of kGuard bytes past its usable size,
+// filled with kGuardByte at allocation: adps_check_guards reports any byte a
+// kernel wrote past the end of a buffer (a bounds check of our own; the pool's
+// compute-sanitizer is unavailable).
+constexpr size_t kGuard = 256;
+constexpr unsigned char kGuardByte = 0xA5;
+
 cudaError_t ensure(Buf& b, size_t bytes) {
   if (bytes == 0) bytes = 16;
   if (b.bytes >= bytes) return cudaSuccess;
   if (b.p) cudaFree(b.p);
   b.p = nullptr;
   b.bytes = 0;
-  size_t want = bytes + bytes / 8;   // headroom against small growth
-  cudaError_t e = cudaMalloc(&b.p, want);
+  size_t want = (bytes + bytes / 8 + 255) & ~(size_t)255;   // headroom against small growth
+  cudaError_t e = cudaMalloc(&b.p, want + kGuard);
+  if (e != cudaSuccess) return e;
+  e = cudaMemset((char*)b.p + want, kGuardByte, kGuard);
   if (e != cudaSuccess) return e;
   b.bytes = want;
   return cudaSuccess;
@@ -286,10 +295,8 @@ extern "C" adps_status adps_plan_create(adps_plan** plan, int32_t device, int64_
   return ADPS_OK;
 }
 
-extern "C" adps_status adps_plan_destroy(adps_plan* P) {
-  if (!P) return ADPS_OK;
-  cudaSetDevice(P->device);
-  cudaDeviceSynchronize();
+constexpr int kMaxBufs = 160;
+static int plan_buffers(adps_plan* P, Buf** out) {
   Buf* bufs[] = {&P->cls, &P->cand_rank, &P->split_list, &P->clone_list, &P->dom_flag, &P->keep_pos,
                  &P->cand_start, &P->cand_end, &P->cand_nvalid, &P->cand_case, &P->cand_props,
                  &P->cand_merged, &P->cand_ins, &P->ins_off, &P->fb_ord, &P->large_list,
@@ -307,8 +314,41 @@ extern "C" adps_status adps_plan_destroy(adps_plan* P) {
                  &P->mkey_sorted, &P->mval_sorted, &P->boxes, &P->tile_owner, &P->tile_pairs, &P->gsoa, &P->fsoa, &P->deferred, &P->cand_bits, &P->rawc, &P->twords,
                  &P->nrm_val, &P->nrm_len, &P->nrm_acc, &P->nrm_reach, &P->nrm_rmax, &P->nrm_walked,
                  &P->nrm_idx, &P->nrm_tmp};
-  for (Buf* b : bufs)
-    if (b->p) cudaFree(b->p);
+  int n = 0;
+  for (Buf* b : bufs) out[n++] = b;
+  return n;
+}
+
+extern "C" adps_status adps_check_guards(adps_plan* P, int64_t* bad_bytes, int32_t* bad_buffers) {
+  if (!P || !bad_bytes) return fail(ADPS_INVALID_ARG, "NULL argument");
+  CK(cudaSetDevice(P->device));
+  CK(cudaDeviceSynchronize());
+  Buf* bufs[kMaxBufs];
+  const int nb = plan_buffers(P, bufs);
+  long long bad = 0;
+  int nbad = 0;
+  unsigned char h[kGuard];
+  for (int i = 0; i < nb; ++i) {
+    if (!bufs[i]->p) continue;
+    CK(cudaMemcpy(h, (char*)bufs[i]->p + bufs[i]->bytes, kGuard, cudaMemcpyDeviceToHost));
+    int here = 0;
+    for (size_t k = 0; k < kGuard; ++k) here += h[k] != kGuardByte;
+    bad += here;
+    nbad += here > 0;
+  }
+  *bad_bytes = bad;
+  if (bad_buffers) *bad_buffers = nbad;
+  return ADPS_OK;
+}
+
+extern "C" adps_status adps_plan_destroy(adps_plan* P) {
+  if (!P) return ADPS_OK;
+  cudaSetDevice(P->device);
+  cudaDeviceSynchronize();
+  Buf* bufs[kMaxBufs];
+  const int nb = plan_buffers(P, bufs);
+  for (int i = 0; i < nb; ++i)
+    if (bufs[i]->p) cudaFree(bufs[i]->p);
   if (P->ctr_host) cudaFreeHost(P->ctr_host);
   if (P->lohi_host) cudaFreeHost(P->lohi_host);
   if (P->cams_host) cudaFreeHost(P->cams_host);

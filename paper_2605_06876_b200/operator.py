@@ -169,6 +169,12 @@ class Plan:
     def _stream(self):
         return C.c_void_p(torch.cuda.current_stream(self.device).cuda_stream)
 
+    def check_guards(self):
+        """(bytes, buffers) written past the end of a plan buffer since allocation (debug; syncs)."""
+        nb, nbuf = C.c_int64(), C.c_int32()
+        _abi.check(self.lib.adps_check_guards(self._h, C.byref(nb), C.byref(nbuf)))
+        return int(nb.value), int(nbuf.value)
+
     def set_timing(self, on: bool):
         self.timing = bool(on)
         _abi.check(self.lib.adps_set_timing(self._h, int(on)))

@@ -286,3 +286,39 @@ def test_accumulate_stats_unaligned_views(op):
     op.accumulate_stats_(tg[1:], td[1:], torch.as_tensor(vg, device="cuda")[1:], torch.as_tensor(vis, device="cuda")[1:])
     np.testing.assert_array_equal(tg[1:].cpu().numpy(), ga)
     np.testing.assert_array_equal(td[1:].cpu().numpy(), den)
+
+
+# --------------------------------------------------------- bounds checks of our own
+def test_no_write_past_any_plan_buffer(op):
+    """Every plan buffer has a guard zone past its usable size (adps_check_guards):
+    after steps on every golden scene (fused and two-pass), a BASELINE-size step,
+    vanilla_densify, the prune index and the device normals, no kernel has
+    written past the end of any buffer.  (compute-sanitizer is closed on this
+    GPU pool; this is the bounds check that stands in for memcheck.)"""
+    import torch
+    from paper_2605_06876_b200 import synth as S
+    from paper_2605_06876_b200.types import AdpSplitConfig
+    plan = op.Plan("cuda:0")
+    for tag in sorted(META["step"]):
+        gg, extent = golden_io.scene(DATA, f"step__{tag}__in")
+        g = PA.to_tensors(PA.oracle_gaussians_f32(gg))
+        cams = DATA[f"step__{tag}__cams"]
+        gt = torch.as_tensor(PA.f32(DATA[f"step__{tag}__gt"]), dtype=torch.float32, device="cuda")
+        ga = torch.as_tensor(DATA[f"step__{tag}__grad_accum"], device="cuda")
+        den = torch.as_tensor(DATA[f"step__{tag}__denom"], device="cuda")
+        cfg = golden_io.Cfg(META["step"][tag]["cfg"])
+        for fused in (False, True):
+            op.densify_step(g, extent, cams, gt, ga, den, cfg, np.random.default_rng(1), plan=plan, fused=fused)
+        op.vanilla_densify_step(g, extent, ga, den, cfg, 3, np.random.default_rng(2), plan=plan)
+        plan.prune_index(0.5, opacity=g.opacity)
+    wl = S.CONFIGS["config2"]
+    d = wl.build_device(plan)
+    ga, den = (torch.as_tensor(x, device="cuda") for x in d["stats"])
+    cfg = AdpSplitConfig(v_views=len(d["cams"]), n_max=wl.n_max)
+    for fused in (False, True):
+        op.densify_step(d["g"], d["ini"].extent, d["cams"], d["gt_img"], ga, den, cfg, np.random.default_rng(0),
+                        plan=plan, view_ids=list(range(len(d["cams"]))), fused=fused,
+                        renders=None if fused else (d["img"], d["dom"]))
+    plan.normals_pcg64(np.random.default_rng(9).bit_generator.state, 100_000)
+    bad_bytes, bad_buffers = plan.check_guards()
+    assert (bad_bytes, bad_buffers) == (0, 0)

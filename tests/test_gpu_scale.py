@@ -61,6 +61,7 @@ def _stage_isolated(op, name, views):
     flagged = PA.flag_candidates(ores, g, cam_objs, cfg)
     st = PA.compare_step(gres, ores, flagged, g)
     c = gres.counts
+    assert plan.check_guards() == (0, 0)   # no write past any plan buffer
     assert c["n_regions"] == sum(len(r) for r in ores.regions.values())
     assert c["n_fallback"] == sum(r.fallback for r in ores.candidates)
     assert c["n_reset"] == len(ores.reset_indices)
