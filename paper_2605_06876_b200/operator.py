@@ -709,6 +709,35 @@ class FallbackNormals:
         return self.normals
 
 
+def _step_outputs(n_out: int, sh_k: int, n_app: int, n_split: int, dev, out: GaussianTensors = None):
+    """The step's outputs carved out of ONE device allocation (the host time
+    between phase 1's last sync and phase 2's launch is GPU idle time):
+    (GaussianTensors, index_map int64, child_parent int32, insert_offset int64)."""
+    f32_cols = 0 if out is not None else 3 + 3 + 4 + 1 + 3 + 3 * sh_k
+    sizes = [8 * n_out, 8 * n_split, 4 * f32_cols * n_out, 4 * n_app]   # int64 first: 8-byte aligned
+    offs, tot = [], 0
+    for b in sizes:
+        offs.append(tot)
+        tot += (b + 255) // 256 * 256
+    buf = torch.empty(max(tot, 256), dtype=torch.uint8, device=dev)
+
+    def part(i, dtype, n):
+        return buf[offs[i]:offs[i] + sizes[i]].view(dtype)[:n]
+
+    index_map = part(0, torch.int64, n_out)
+    insert_offset = part(1, torch.int64, n_split)
+    child_parent = part(3, torch.int32, n_app)
+    if out is None:
+        cols = part(2, F32, f32_cols * n_out)
+        o, views = 0, []
+        for c in (3, 3, 4, 1, 3):
+            views.append(cols[o * n_out:(o + c) * n_out].view(n_out, c) if c > 1 else cols[o * n_out:(o + 1) * n_out])
+            o += c
+        rest = cols[o * n_out:].view(n_out, sh_k, 3) if sh_k else None
+        out = GaussianTensors(*views, rest)
+    return out, index_map, child_parent, insert_offset
+
+
 def densify_step(g: GaussianTensors, extent: float, cameras, gt, grad_accum: torch.Tensor,
                  denom: torch.Tensor, cfg, rng, *, renders=None, plan: Plan = None,
                  view_ids=None, want_report: bool = True, out: GaussianTensors = None,
@@ -750,11 +779,8 @@ def densify_step(g: GaussianTensors, extent: float, cameras, gt, grad_accum: tor
         raise RuntimeError("fallback count changed between phase-1 halves")
     normals = draw.result()
     n_out = counts["n_out"]
-    if out is None:
-        out = GaussianTensors.empty(n_out, g.sh_k, dev)
-    index_map = torch.empty(n_out, dtype=torch.int64, device=dev)
-    child_parent = torch.empty(n_out - counts["n_keep"], dtype=torch.int32, device=dev)
-    insert_offset = torch.empty(counts["n_split"], dtype=torch.int64, device=dev)
+    out, index_map, child_parent, insert_offset = _step_outputs(n_out, g.sh_k, n_out - counts["n_keep"],
+                                                                counts["n_split"], dev, out)
     plan.phase2(g, normals, out, index_map, child_parent, insert_offset)
     res = StepResult(gaussians=out, index_map=index_map, counts=counts, view_ids=list(view_ids),
                      normals=normals, child_parent=child_parent, insert_offset=insert_offset)
