@@ -118,7 +118,7 @@ struct adps_plan {
   long long region_cap = 0, partial_cap = 0, region_hint = 0, partial_hint = 0;
   // render scratch
   Buf r_key, r_key_sorted, r_order_in, r_order, r_tiles, r_rect, r_splat, r_offs, r_dup, r_dup_sorted,
-      r_tstart, r_tend, r_total, r_cams;
+      r_tstart, r_tend, r_total, r_cams, r_tile_lohi;
   unsigned long long* r_total_host = nullptr;
   // last phase-1 state
   bool have_phase1 = false;
@@ -306,7 +306,7 @@ static int plan_buffers(adps_plan* P, Buf** out) {
                  &P->dbg_stats, &P->dbg_child, &P->scan_val, &P->scan_flag, &P->scan_ticket,
                  &P->scan2_val, &P->scan2_flag, &P->scan2_ticket, &P->cub_tmp, &P->ctr, &P->r_key,
                  &P->r_key_sorted, &P->r_order_in, &P->r_order, &P->r_tiles, &P->r_rect, &P->r_splat,
-                 &P->r_offs, &P->r_dup, &P->r_dup_sorted, &P->r_tstart, &P->r_tend, &P->r_total,
+                 &P->r_offs, &P->r_dup, &P->r_dup_sorted, &P->r_tstart, &P->r_tend, &P->r_total, &P->r_tile_lohi,
                  &P->r_cams, &P->small_list, &P->pstart, &P->n_groups, &P->work_cnt, &P->work_off,
                  &P->props_s, &P->psrc, &P->pcand, &P->gkey, &P->gval, &P->gkey_sorted, &P->gval_sorted, &P->grp_first,
                  &P->gpar, &P->gext, &P->gfirst_of, &P->glist, &P->scan3_val, &P->scan3_flag, &P->scan3_ticket,
@@ -564,7 +564,7 @@ static adps_status render_impl(adps_plan* P, void* stream_v, const adps_gaussian
     if (epi_gt) {   // fused attribution epilogue into the plan's step buffers
       ba.gt = epi_gt + (long long)v * hw * 3;
       ba.rawf = P->rawc.as<float>() + (long long)v * hw;
-      ba.lohi = P->lohi.as<unsigned long long>() + 2ll * v;
+      ba.lohi = P->r_tile_lohi.as<unsigned long long>() + 2ll * n_tiles * v;
       ba.cls = P->cls.as<unsigned char>();
       ba.N = (int)n;
       ba.dom_flag = P->dom_flag.as<unsigned char>();
@@ -710,8 +710,18 @@ extern "C" adps_status adps_render_fused(adps_plan* P, void* stream_v, const adp
   sa.ctr = ctr;
   CK(launch_select(sa, sst, s));
   P->launches += 1;
+  {
+    const int tiles_x = (W + kRTile - 1) / kRTile, tiles_y = (H + kRTile - 1) / kRTile;
+    CK(ensure(P->r_tile_lohi, 16ll * tiles_x * tiles_y * V));
+  }
   st = render_impl(P, stream_v, g, n, cams_host, n_views, bg, image, dominant, nullptr, nullptr, gt);
   if (st != ADPS_OK) return st;
+  {
+    const int n_tiles = ((W + kRTile - 1) / kRTile) * ((H + kRTile - 1) / kRTile);
+    CK(launch_reduce_tile_minmax(P->r_tile_lohi.as<unsigned long long>(), n_tiles, V,
+                                 P->lohi.as<unsigned long long>(), s));
+    P->launches += 1;
+  }
   P->fused.valid = true;
   P->fused.g = *g;
   P->fused.n = n;

@@ -226,10 +226,10 @@ __device__ __forceinline__ void render_epilogue(const BlendArgs& a, bool inside,
       lo = fmin(lo, s_lo[w]);
       hi = fmax(hi, s_hi[w]);
     }
-    if (lo <= hi) {   // raw >= +0.0: IEEE order == unsigned order of the bit patterns
-      atomicMin(a.lohi + 0, (unsigned long long)__double_as_longlong(lo));
-      atomicMax(a.lohi + 1, (unsigned long long)__double_as_longlong(hi));
-    }
+    // this tile's min/max into its own slot (no same-address atomics: 4k tiles
+    // per view); reduce_tile_minmax folds them per view before the thresholds
+    a.lohi[2 * blockIdx.x + 0] = (unsigned long long)__double_as_longlong(lo);
+    a.lohi[2 * blockIdx.x + 1] = (unsigned long long)__double_as_longlong(hi);
   }
 }
 
@@ -337,6 +337,43 @@ cudaError_t launch_duplicate(const DupArgs& a, cudaStream_t s) {
 cudaError_t launch_tile_ranges(const unsigned long long* keys, long long n, int* start, int* end,
                                cudaStream_t s) {
   if (n > 0) tile_ranges_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(keys, n, start, end);
+  return cudaGetLastError();
+}
+
+// per view: the min/max over its tiles' slots (bit patterns of non-negative
+// doubles order as unsigned integers; an empty tile holds +inf / 0)
+__global__ void __launch_bounds__(256) reduce_tile_minmax_kernel(const unsigned long long* __restrict__ tiles,
+                                                                 int n_tiles, unsigned long long* __restrict__ lohi) {
+  const int v = blockIdx.x;
+  const unsigned long long* t = tiles + 2ll * n_tiles * v;
+  unsigned long long lo = ~0ull, hi = 0ull;
+  for (int i = threadIdx.x; i < n_tiles; i += blockDim.x) {
+    lo = min(lo, t[2 * i]);
+    hi = max(hi, t[2 * i + 1]);
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    lo = min(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+    hi = max(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+  }
+  __shared__ unsigned long long slo[8], shi[8];
+  if ((threadIdx.x & 31) == 0) {
+    slo[threadIdx.x >> 5] = lo;
+    shi[threadIdx.x >> 5] = hi;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w = 1; w < 8; ++w) {
+      lo = min(lo, slo[w]);
+      hi = max(hi, shi[w]);
+    }
+    lohi[2 * v] = min(lo, 0x7ff0000000000000ull);   // +inf when the view is empty
+    lohi[2 * v + 1] = hi;
+  }
+}
+
+cudaError_t launch_reduce_tile_minmax(const unsigned long long* tiles, int n_tiles, int n_views,
+                                      unsigned long long* lohi, cudaStream_t s) {
+  reduce_tile_minmax_kernel<<<n_views, 256, 0, s>>>(tiles, n_tiles, lohi);
   return cudaGetLastError();
 }
 

@@ -65,7 +65,7 @@ struct BlendArgs {
   // 8 B/px boundary (raw cache + dominant map).  All pointers are the view's.
   const float* gt;                // [H,W,3] or null (no epilogue)
   float* rawf;                    // [H*W]
-  unsigned long long* lohi;       // [2]: min / max raw of the view (bit patterns)
+  unsigned long long* lohi;       // [2 * n_tiles]: min / max raw per tile of the view (bit patterns)
   const unsigned char* cls;       // [N] select classes (1 = split candidate)
   int N;
   unsigned char* dom_flag;        // [N]
@@ -79,5 +79,8 @@ cudaError_t launch_duplicate(const DupArgs& a, cudaStream_t s);
 cudaError_t launch_tile_ranges(const unsigned long long* keys, long long n, int* start, int* end,
                                cudaStream_t s);
 cudaError_t launch_blend(const BlendArgs& a, int n_tiles, cudaStream_t s);
+// fused epilogue: per-view min/max from the per-tile slots
+cudaError_t launch_reduce_tile_minmax(const unsigned long long* tiles, int n_tiles, int n_views,
+                                      unsigned long long* lohi, cudaStream_t s);
 
 }  // namespace adps
