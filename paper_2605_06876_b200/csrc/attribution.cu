@@ -921,15 +921,14 @@ __global__ void __launch_bounds__(kBorderSlots * kBorderTilesPerBlock) border_ke
   // holding the same (fragment, neighbour fragment) pair unite once (match_any)
   // kBorderTilesPerBlock tiles per block (short blocks: fewer of them to schedule)
   const int tiles_per_view = P.tiles_x * P.tiles_y;
-  // persistent blocks over the tiles (most tiles have no fragment and exit at once)
-  for (long long tile = (long long)blockIdx.x * kBorderTilesPerBlock + threadIdx.x / kBorderSlots; tile < P.n_tiles;
-       tile += (long long)gridDim.x * kBorderTilesPerBlock) {
+  const long long tile = (long long)blockIdx.x * kBorderTilesPerBlock + threadIdx.x / kBorderSlots;
+  if (tile >= P.n_tiles) return;   // warp-uniform
   const int v = (int)(tile / tiles_per_view);
   const int t = (int)(tile % tiles_per_view);
   const int tyi = t / P.tiles_x, txi = t % P.tiles_x;
   const int s = threadIdx.x % kBorderSlots;
   const int gp = P.border[tile * kBorderSlots + s];
-  if (__all_sync(0xffffffffu, gp < 0)) continue;   // warp-uniform
+  if (__all_sync(0xffffffffu, gp < 0)) return;   // warp-uniform
   int lx, ly;
   if (s < kTileW) { lx = s; ly = 0; }
   else if (s < 2 * kTileW) { lx = s - kTileW; ly = kTileH - 1; }
@@ -967,7 +966,6 @@ __global__ void __launch_bounds__(kBorderSlots * kBorderTilesPerBlock) border_ke
 #endif
     const PartialRec& B = P.partials[gq];
     if (A->cand == B.cand && A->band == B.band) uf_unite(P.parent, gp, gq);
-  }
   }
 }
 
@@ -1162,9 +1160,7 @@ cudaError_t launch_attribution_tail(const AttributionArgs& a, cudaStream_t s, Ma
   B.W = a.W;
   B.H = a.H;
   B.n_tiles = nblocks;
-  long long bblocks = (nblocks + kBorderTilesPerBlock - 1) / kBorderTilesPerBlock;
-  if (bblocks > (long long)a.grid_small * 4) bblocks = (long long)a.grid_small * 4;   // 16 resident blocks per SM
-  border_kernel<<<(unsigned)bblocks,
+  border_kernel<<<(unsigned)((nblocks + kBorderTilesPerBlock - 1) / kBorderTilesPerBlock),
                   kBorderSlots * kBorderTilesPerBlock, 0, s>>>(B);
   resolve_kernel<<<a.grid_small, 256, 0, s>>>(a.partials, a.partial_parent, a.n_partials, a.partial_cap);
   partial_emit_kernel<<<a.grid_small, 256, 0, s>>>(a.partials, a.partial_parent, a.n_partials, a.partial_cap,

@@ -34,9 +34,6 @@ constexpr int kWarpsPerBlock = 8;
 #ifndef ADPS_TW_FAST
 #define ADPS_TW_FAST 1
 #endif
-#ifndef ADPS_TW_PERSISTENT
-#define ADPS_TW_PERSISTENT 1   // the bit-plane CCL as one wave of persistent warps
-#endif
 #ifndef ADPS_TW_ROWWISE
 #define ADPS_TW_ROWWISE 0   // 1: the row-wise words pass (ballots) instead of the transposed one
 #endif
@@ -996,14 +993,9 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, ADPS_TW_MINBLOCKS)
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   WarpSmem& S = reinterpret_cast<WarpSmem*>(smem_raw)[wid];
-  // persistent warps, tiles interleaved over them: tile costs vary from a few
-  // instructions (no keyed pixel) to thousands, and a block whose warps drew
-  // cheap tiles would otherwise idle its slots until its slowest warp ends
-  for (long long tile = t0 + (long long)blockIdx.x * kWarpsPerBlock + wid; tile < t1;
-       tile += (long long)gridDim.x * kWarpsPerBlock) {
-    tile_bits_body<R, FUSED, kWarpMaxRuns>(P, words, WW, S, tile, lane);
-    __syncwarp();
-  }
+  const long long tile = t0 + (long long)blockIdx.x * kWarpsPerBlock + wid;
+  if (tile >= t1) return;   // warp-uniform
+  tile_bits_body<R, FUSED, kWarpMaxRuns>(P, words, WW, S, tile, lane);
 }
 
 // the tiles the first pass deferred (more than kWarpMaxRuns runs), a warp each
@@ -1029,21 +1021,7 @@ static cudaError_t launch_bits_r(const TileParams& P, int WW, long long t0, long
   const size_t smem = tile_warp_smem_bytes();
   cudaError_t e = cudaFuncSetAttribute(tile_bits_kernel<R, FUSED>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  long long blocks = (t1 - t0 + kWarpsPerBlock - 1) / kWarpsPerBlock;
-#if ADPS_TW_PERSISTENT
-  static int resident = 0;   // per instantiation: one wave of resident blocks
-  if (resident == 0) {
-    int dev = 0, sms = 148, per_sm = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, tile_bits_kernel<R, FUSED>, kWarpsPerBlock * 32,
-                                                      smem) != cudaSuccess ||
-        per_sm < 1)
-      per_sm = 4;
-    resident = per_sm * sms;
-  }
-  if (blocks > resident) blocks = resident;
-#endif
+  const long long blocks = (t1 - t0 + kWarpsPerBlock - 1) / kWarpsPerBlock;
   if (blocks > 0) tile_bits_kernel<R, FUSED><<<(unsigned)blocks, kWarpsPerBlock * 32, smem, s>>>(P, P.words, WW, t0, t1);
   return cudaGetLastError();
 }
