@@ -653,16 +653,23 @@ __global__ void __launch_bounds__(kTwWarps * 32) tile_words_t_kernel(const float
   cp_async_wait_all();
   __syncwarp();
   if (lane >= nrows) return;
-  unsigned M = 0u, B0 = 0u, B1 = 0u, amb = 0u;
+  // one compare and one predicated OR per plane and pixel (the bit is an
+  // immediate after unrolling); band = t1 + t2 + t3 with monotone thresholds,
+  // so its bit 0 is t1 ^ t2 ^ t3 and its bit 1 is t2 (word operations after)
+  unsigned M = 0u, P1 = 0u, P2 = 0u, P3 = 0u, amb = 0u;
+  const int T0 = R0.T, T1 = R1.T, T2 = R2.T, T3 = R3.T;
+  const int A0 = R0.A, A1 = R1.A, A2 = R2.A, A3 = R3.A;
 #pragma unroll
   for (int x = 0; x < 32; ++x) {
     const int fi = S[lane][x];
-    const bool t1 = fi >= R1.T, t2 = fi >= R2.T, t3 = fi >= R3.T;
-    M |= (unsigned)(fi >= R0.T) << x;
-    B0 |= (unsigned)(t1 ^ t2 ^ t3) << x;   // band = t1 + t2 + t3 (monotone thresholds): bit 0
-    B1 |= (unsigned)t2 << x;               // bit 1: band >= 2
-    amb |= (unsigned)((fi == R0.A) | (fi == R1.A) | (fi == R2.A) | (fi == R3.A)) << x;
+    const unsigned bit = 1u << x;
+    if (fi >= T0) M |= bit;
+    if (fi >= T1) P1 |= bit;
+    if (fi >= T2) P2 |= bit;
+    if (fi >= T3) P3 |= bit;
+    if (fi == A0 || fi == A1 || fi == A2 || fi == A3) amb |= bit;
   }
+  unsigned B0 = P1 ^ P2 ^ P3, B1 = P2;
   for (; amb; amb &= amb - 1u) {   // rare: the exact fp64 raw error, numpy order
     const int x = __ffs(amb) - 1;
     const long long p = (long long)v * hw + (long long)y * W + x0 + x;
