@@ -352,10 +352,22 @@ def run_ours(args, wl):
     world, rank, local = dist_env()
     if world != args.gpus:
         raise SystemExit(f"bench.py --gpus {args.gpus} but WORLD_SIZE={world}")
+    # ADPS_BENCH_BACKEND=gloo: a functional check of the multi-rank path with host
+    # collectives (e.g. ranks sharing one GPU); numbers come from NCCL, one GPU per rank
+    backend = os.environ.get("ADPS_BENCH_BACKEND", "nccl")
+    local = local % max(torch.cuda.device_count(), 1)
     if world > 1:
         torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
     dev = torch.device("cuda", local if world > 1 else 0)
+
+    def max_over_ranks(x):
+        t = torch.tensor([x], dtype=torch.float64, device=dev if backend == "nccl" else "cpu")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
     torch.cuda.set_device(dev)
     clocks = ClockSampler(index=dev.index)
     clocks.start()
@@ -422,9 +434,7 @@ def run_ours(args, wl):
     k1, l1 = plan.launch_count()
     ms = ev0.elapsed_time(ev1) / args.steps
     if world > 1:
-        t = torch.tensor([ms], device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
+        ms = max_over_ranks(ms)
     counts = res.counts
     n_split = counts["n_split"]
     pp = res.report_arrays["cand_proposals"].cpu().numpy()
@@ -436,27 +446,27 @@ def run_ours(args, wl):
               "adaptive": (n_split - counts["n_fallback"] - counts["n_reset"]) / ns,
               "fallback": counts["n_fallback"] / ns, "reset": counts["n_reset"] / ns}
 
-    # ---- per-stage breakdown with CUDA events on the launching stream (1 GPU)
+    # ---- per-stage breakdown with CUDA events on the launching stream (each rank: its own views)
     stages = {}
-    if world == 1:
-        plan.set_timing(True)
-        stage_acc = {}
-        n_t = max(3, min(args.steps, 10))
-        for _ in range(n_t):
-            step()
-            for k_, v_ in plan.stage_ms().items():
-                stage_acc[k_] = stage_acc.get(k_, 0.0) + v_
-        plan.set_timing(False)
-        stages = {k_: v_ / n_t for k_, v_ in stage_acc.items()}
+    plan.set_timing(True)
+    stage_acc = {}
+    n_t = max(3, min(args.steps, 10))
+    for _ in range(n_t):
+        step()
+        for k_, v_ in plan.stage_ms().items():
+            stage_acc[k_] = stage_acc.get(k_, 0.0) + v_
+    plan.set_timing(False)
+    stages = {k_: v_ / n_t for k_, v_ in stage_acc.items()}
 
     V, H, W = len(view_ids), wl.height, wl.width
     px = V * H * W
+    px_local = (hi - lo) * H * W if sharded else px   # the input pass of this rank
     peak, peak_kind = load_peaks()
     tile_ms = stages.get("tile_ccl", float("nan"))
     mm_ms = stages.get("minmax", float("nan"))
     # stat-accum: 28 B/px over the attribution stages (maps, partition, stats)
     attr_ms = sum(stages.get(k_, 0) for k_ in ("minmax", "thresholds", "tile_ccl", "border_merge"))
-    achieved = BYTES_PER_PX * px / (mm_ms * 1e-3) / 1e9 if stages else None
+    achieved = BYTES_PER_PX * px_local / (mm_ms * 1e-3) / 1e9 if stages.get("minmax") else None
     traffic = load_traffic(wl.name)
     b_step = BYTES_PER_PX * px + BYTES_PER_G_IN * g.n + BYTES_PER_G_OUT * counts["n_out"]
     acc = time_accumulate(dev, g.n, peak) if rank == 0 else None
@@ -539,9 +549,7 @@ def run_ours(args, wl):
         torch.cuda.synchronize()
         e2e_ms = ev0.elapsed_time(ev1) / n_e
         if world > 1:
-            t = torch.tensor([e2e_ms], device=dev)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            e2e_ms = float(t.item())
+            e2e_ms = max_over_ranks(e2e_ms)
         e2e = {"value": n_split / (e2e_ms * 1e-3), "unit": UNIT, "ms_per_step": e2e_ms,
                "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
                "note": "per rank: params + stats + its own block of views in, grown params + index_map out"
@@ -582,7 +590,7 @@ def run_ours(args, wl):
             "dtype": "f64+i64 (decisions), fp32 (params)", "data": "synthetic",
             "config": config_dict(wl, args, extra),
             "densify_step_ms": ms,
-            "stat_accum": {"GB/s": BYTES_PER_PX * px / (attr_ms * 1e-3) / 1e9 if attr_ms else None,
+            "stat_accum": {"GB/s": BYTES_PER_PX * px_local / (attr_ms * 1e-3) / 1e9 if attr_ms else None,
                            "frac": None, "ms": attr_ms},
             "accumulate_stats": acc,
             "step_roofline": {"bytes": int(b_step), "GB/s": b_step / (ms * 1e-3) / 1e9,
@@ -591,7 +599,7 @@ def run_ours(args, wl):
                                                     "ever-dominant flags, candidate bits, fp32 raw cache)",
                          "achieved": achieved, "peak": peak, "peak_kind": peak_kind, "unit": "GB/s",
                          "frac": achieved / peak if achieved else None, "traffic": traffic,
-                         "algorithmic_bytes_per_launch": BYTES_PER_PX * px, "ms_per_launch": mm_ms,
+                         "algorithmic_bytes_per_launch": BYTES_PER_PX * px_local, "ms_per_launch": mm_ms,
                          "note": "achieved counts the 28 B/px inputs only; traffic = ncu dram read+write of one "
                                  "launch (incl. the 4.125 B/px cache it writes), profiles/"},
             "tile_pass": {"ms": tile_ms, "kernels": "tile_words_kernel (HBM) + tile_bits_kernel (latency-bound CCL)",
