@@ -46,8 +46,8 @@ sys.path.insert(0, ROOT)
 METRIC = "AdpSplit densify-step ms & parents/s at 1M Gaussians; stat-accum GB/s vs HBM"
 UNIT = "parents/s"
 BYTES_PER_PX = 28      # image fp32x3 + gt fp32x3 + dominant int32 (the step's attribution inputs)
-WORDS_BYTES_PER_PX = 4 + 0.125 + 0.5   # bit-plane pass: fp32 raw cache + candidate bits read, 4 bit planes written
-MINMAX_TRAFFIC_PER_PX = 28 + 4 + 0.125   # minmax pass: inputs read once, fp32 raw cache + candidate bits written
+WORDS_BYTES_PER_PX = 2 + 0.125 + 0.5   # bit-plane pass: 16-bit raw cache + candidate bits read, 4 bit planes written
+MINMAX_TRAFFIC_PER_PX = 28 + 2 + 0.125   # minmax pass: inputs read once, 16-bit raw cache + candidate bits written
 BYTES_PER_G_IN = 72    # params 56 B + grad_accum/denom 2 x f64
 BYTES_PER_G_OUT = 64   # params 56 B + index_map int64
 
@@ -596,12 +596,12 @@ def run_ours(args, wl):
             "step_roofline": {"bytes": int(b_step), "GB/s": b_step / (ms * 1e-3) / 1e9,
                               "frac": b_step / (ms * 1e-3) / 1e9 / peak},
             "roofline": {"bound": "hbm", "kernel": "minmax2_kernel (input pass: raw L1 error, per-view min/max, "
-                                                    "ever-dominant flags, candidate bits, fp32 raw cache)",
+                                                    "ever-dominant flags, candidate bits, 16-bit raw cache)",
                          "achieved": achieved, "peak": peak, "peak_kind": peak_kind, "unit": "GB/s",
                          "frac": achieved / peak if achieved else None, "traffic": traffic,
                          "algorithmic_bytes_per_launch": BYTES_PER_PX * px_local, "ms_per_launch": mm_ms,
                          "note": "achieved counts the 28 B/px inputs only; traffic = ncu dram read+write of one "
-                                 "launch (incl. the 4.125 B/px cache it writes), profiles/"},
+                                 "launch (incl. the 2.125 B/px caches it writes), profiles/"},
             "tile_pass": {"ms": tile_ms, "kernels": "tile_words_kernel (HBM) + tile_bits_kernel (latency-bound CCL)",
                           "words_bytes_per_launch": WORDS_BYTES_PER_PX * px},
             "stages_ms": stages,

@@ -263,6 +263,19 @@ __host__ __device__ inline int ceil_log2(unsigned long long x) {
   return b;
 }
 
+// ------------------------------------------------------------ raw-error cache
+// The input pass caches each pixel's raw L1 error in 16 bits: the top half of
+// the bit pattern of RZ_fp32(raw) (sign 0, 8-bit exponent, 7-bit mantissa), i.e.
+// raw rounded toward zero to that format.  Non-negative values order as their
+// bit patterns, so a threshold compare raw >= X is an integer compare against
+// T = top16(RZ_fp32(X)) + (X not representable), except when the pixel's code
+// equals top16(RZ_fp32(X)) for a non-representable X: those pixels (~0.2 % at
+// config 3) recompute the exact fp64 raw error from image and gt.
+typedef unsigned short raw16_t;
+__device__ __forceinline__ raw16_t raw16(double r) {
+  return (raw16_t)(__float_as_uint(__double2float_rz(r)) >> 16);
+}
+
 // ---------------------------------------------------------- union-find (min)
 // Roots are minimum indices; links only ever decrease (atomicMin).
 __device__ __forceinline__ int uf_find(volatile int* p, int x) {

@@ -47,7 +47,7 @@ __global__ void minmax_kernel(const float* __restrict__ image, const float* __re
                               const int* __restrict__ dominant, long long hw, unsigned long long* __restrict__ lohi,
                               const unsigned char* __restrict__ cls, int N, unsigned char* __restrict__ dom_flag,
                               unsigned* __restrict__ cand_bits, double* __restrict__ raw_out,
-                              float* __restrict__ rawf_out, int v0) {
+                              raw16_t* __restrict__ rawf_out, int v0) {
   const int v = v0 + blockIdx.y;
   const float* img = image + (long long)v * hw * 3;
   const float* g = gt + (long long)v * hw * 3;
@@ -64,7 +64,7 @@ __global__ void minmax_kernel(const float* __restrict__ image, const float* __re
       if (raw_out) raw_out[(long long)v * hw + p] = r;
       // the bit-plane path keeps raw rounded toward zero (4 B/px); compares that
       // the rounding cannot decide are redone exactly (tile_words_kernel)
-      if (rawf_out) rawf_out[(long long)v * hw + p] = __double2float_rz(r);
+      if (rawf_out) rawf_out[(long long)v * hw + p] = raw16(r);
       lo = fmin(lo, r);
       hi = fmax(hi, r);
       d = __ldg(dom + p);
@@ -126,13 +126,13 @@ __global__ void __launch_bounds__(256) minmax2_kernel(const float* __restrict__ 
                                                       const unsigned char* __restrict__ cls, int N,
                                                       unsigned char* __restrict__ dom_flag,
                                                       unsigned* __restrict__ cand_bits, double* __restrict__ raw_out,
-                                                      float* __restrict__ rawf_out, int v0) {
+                                                      raw16_t* __restrict__ rawf_out, int v0) {
   const int v = v0 + blockIdx.y;
   const long long vb = (long long)v * hw;
   const float2* img2 = reinterpret_cast<const float2*>(image + vb * 3);
   const float2* gt2 = reinterpret_cast<const float2*>(gt + vb * 3);
   const int2* dom2 = reinterpret_cast<const int2*>(dominant + vb);
-  float2* rawf2 = rawf_out ? reinterpret_cast<float2*>(rawf_out + vb) : nullptr;
+  unsigned* rawf2 = rawf_out ? reinterpret_cast<unsigned*>(rawf_out + vb) : nullptr;   // two codes per word
   double* rawd = raw_out ? raw_out + vb : nullptr;
   unsigned* bits = cand_bits + (long long)v * ((hw + 31) / 32);
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -149,7 +149,7 @@ __global__ void __launch_bounds__(256) minmax2_kernel(const float* __restrict__ 
       d1 = dd.y;
       const double r0 = raw_l1_3(a0.x, a0.y, a1.x, g0.x, g0.y, g1.x);
       const double r1 = raw_l1_3(a1.y, a2.x, a2.y, g1.y, g2.x, g2.y);
-      if (rawf2) rawf2[p >> 1] = make_float2(__double2float_rz(r0), __double2float_rz(r1));
+      if (rawf2) rawf2[p >> 1] = (unsigned)raw16(r0) | ((unsigned)raw16(r1) << 16);
       if (rawd) {
         rawd[p] = r0;
         rawd[p + 1] = r1;
@@ -276,7 +276,7 @@ struct BulkArgs {
   int N;
   unsigned char* dom_flag;
   unsigned* cand_bits;  // [V][nwords], zeroed
-  float* rawf;          // flat
+  raw16_t* rawf;        // flat
 };
 
 __global__ void __launch_bounds__(kMBThreads) minmax_bulk_kernel(BulkArgs a) {
@@ -425,7 +425,7 @@ __global__ void __launch_bounds__(kMBThreads) minmax_bulk_kernel(BulkArgs a) {
       const long long v = p / a.hw;   // both pixels of the pair are in view v (hw even)
       const double r0 = raw_l1_3(i6[0], i6[1], i6[2], g6[0], g6[1], g6[2]);
       const double r1 = raw_l1_3(i6[3], i6[4], i6[5], g6[3], g6[4], g6[5]);
-      reinterpret_cast<float2*>(a.rawf)[p >> 1] = make_float2(__double2float_rz(r0), __double2float_rz(r1));
+      reinterpret_cast<unsigned*>(a.rawf)[p >> 1] = (unsigned)raw16(r0) | ((unsigned)raw16(r1) << 16);
       const int k = v == cv ? 0 : 1;
       lo[k] = fmin(lo[k], fmin(r0, r1));
       hi[k] = fmax(hi[k], fmax(r0, r1));

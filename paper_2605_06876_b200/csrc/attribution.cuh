@@ -35,7 +35,7 @@ struct TileParams {
   const unsigned* cand_bits;         // [V][ceil(H*W/32)]: bit p = D[p] is a split candidate
   const double* raw;                 // [V][H*W] raw L1 error cached by the minmax pass, or null
   uint4* words;                      // [V][H][ceil(W/32)] bit planes (m, cand, band0, band1), or null
-  const float* rawf;                 // [V][H*W] raw L1 error rounded toward zero (bit-plane path), or null
+  const raw16_t* rawf;               // [V][H*W] 16-bit raw-error cache (bit-plane path), or null
 };
 
 struct BorderParams {
@@ -81,7 +81,7 @@ struct AttributionArgs {
   unsigned* cand_bits;               // [V][ceil(H*W/32)], written by the minmax pass
   double* raw;                       // [V][H*W] raw L1 error written by the minmax pass, or null
   uint4* words;                      // [V][H][ceil(W/32)] bit planes for tile_bits_kernel, or null
-  float* rawf;                       // [V][H*W] raw L1 error rounded toward zero (bit-plane path), or null
+  raw16_t* rawf;                     // [V][H*W] 16-bit raw-error cache (bit-plane path), or null
 };
 
 // warp-per-tile scanline CCL (r_erode <= 3) over tiles [t0, t1); defers tiles with > kWarpMaxRuns runs

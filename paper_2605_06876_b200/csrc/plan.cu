@@ -563,7 +563,7 @@ static adps_status render_impl(adps_plan* P, void* stream_v, const adps_gaussian
     ba.gt = nullptr;
     if (epi_gt) {   // fused attribution epilogue into the plan's step buffers
       ba.gt = epi_gt + (long long)v * hw * 3;
-      ba.rawf = P->rawc.as<float>() + (long long)v * hw;
+      ba.rawf = P->rawc.as<raw16_t>() + (long long)v * hw;
       ba.lohi = P->r_tile_lohi.as<unsigned long long>() + 2ll * n_tiles * v;
       ba.cls = P->cls.as<unsigned char>();
       ba.N = (int)n;
@@ -621,7 +621,7 @@ static AttributionArgs attr_args(adps_plan* P, int V, int H, int W, const adps_c
   a.cand_bits = P->cand_bits.as<unsigned>();
   // the bit-plane path caches raw as fp32 (round toward zero), the others as fp64
   a.raw = P->use_raw && !P->use_bits ? P->rawc.as<double>() : nullptr;
-  a.rawf = P->use_bits ? P->rawc.as<float>() : nullptr;
+  a.rawf = P->use_bits ? P->rawc.as<raw16_t>() : nullptr;
   a.words = P->use_words ? P->twords.as<uint4>() : nullptr;
   return a;
 }
@@ -674,7 +674,7 @@ extern "C" adps_status adps_render_fused(adps_plan* P, void* stream_v, const adp
   CK(ensure(P->clone_list, 4 * nn));
   CK(ensure(P->dom_flag, nn));
   CK(ensure(P->lohi, 16ll * V));
-  CK(ensure(P->rawc, 4ll * hw * V));
+  CK(ensure(P->rawc, 2ll * hw * V));
   CK(ensure(P->cand_bits, 4ll * V * ((hw + 31) / 32) + 4));
   CK(ensure(P->ctr, sizeof(Counters)));
   if (P->cams_host_cap < V) {
@@ -815,7 +815,7 @@ extern "C" adps_status adps_step_phase1_begin(adps_plan* P, void* stream_v, cons
   P->use_raw = P->raw_cache && P->tile_path != 1 && !P->dbg_m && cfg->r_erode <= 3;
   P->use_bits = P->use_raw && (P->tile_path == 0 || P->tile_path == 3) && cfg->l_bands <= 4;
   P->use_words = P->use_bits && P->tile_path == 0;   // path 3: planes computed per tile (fused)
-  if (P->use_raw) CK(ensure(P->rawc, (P->use_bits ? 4ll : 8ll) * total_px));
+  if (P->use_raw) CK(ensure(P->rawc, (P->use_bits ? 2ll : 8ll) * total_px));
   if (P->use_words) CK(ensure(P->twords, (long long)tile_words_bytes(V, H, W)));
   CK(ensure(P->ctr, sizeof(Counters)));
   if (P->cams_host_cap < V) {

@@ -191,7 +191,7 @@ __device__ __forceinline__ void render_epilogue(const BlendArgs& a, bool inside,
     const double r = __dadd_rn(__dadd_rn(fabs(__dsub_rn((double)i0, (double)g3[0])),
                                          fabs(__dsub_rn((double)i1, (double)g3[1]))),
                                fabs(__dsub_rn((double)i2, (double)g3[2])));
-    a.rawf[p] = __double2float_rz(r);
+    a.rawf[p] = raw16(r);
     lo = r;
     hi = r;
     if (bi >= 0 && bi < a.N && __ldg(a.cls + bi) == 1) {

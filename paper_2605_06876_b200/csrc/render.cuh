@@ -64,7 +64,7 @@ struct BlendArgs {
   // the densify step's input pass would compute, so the step starts from the
   // 8 B/px boundary (raw cache + dominant map).  All pointers are the view's.
   const float* gt;                // [H,W,3] or null (no epilogue)
-  float* rawf;                    // [H*W]
+  raw16_t* rawf;                  // [H*W] 16-bit raw-error cache
   unsigned long long* lohi;       // [2 * n_tiles]: min / max raw per tile of the view (bit patterns)
   const unsigned char* cls;       // [N] select classes (1 = split candidate)
   int N;

@@ -510,13 +510,17 @@ struct RzThreshold {
   int T, A;
 };
 __device__ __forceinline__ RzThreshold rz_threshold(double X) {
-  const float xf = __double2float_rz(X);   // +inf stays +inf
-  const int k = __float_as_int(xf);
-  const bool exact = (double)xf == X;
+  // against the 16-bit cache codes (raw16): the code of X is the top half of
+  // RZ_fp32(X); X is representable iff it equals that fp32 value and the low
+  // half is zero (+inf stays +inf: code 0x7f80, above every finite raw)
+  const float xf = __double2float_rz(X);
+  const unsigned b = __float_as_uint(xf);
+  const int k = (int)(b >> 16);
+  const bool exact = (double)xf == X && (b & 0xffffu) == 0u;
   return {exact ? k : k + 1, exact ? (int)0x80000000 : k};
 }
 
-__global__ void __launch_bounds__(256) tile_words_kernel(const float* __restrict__ rawf,
+__global__ void __launch_bounds__(256) tile_words_kernel(const raw16_t* __restrict__ rawf,
                                                          const float* __restrict__ image,
                                                          const float* __restrict__ gt,
                                                          const unsigned* __restrict__ cand_bits,
@@ -530,7 +534,7 @@ __global__ void __launch_bounds__(256) tile_words_kernel(const float* __restrict
   const long long hw = (long long)H * W;
   const long long nwords = (hw + 31) / 32;
   const long long p_row = (long long)y * W;
-  const int* rrow = reinterpret_cast<const int*>(rawf + (long long)v * hw + p_row);
+  const raw16_t* rrow = rawf + (long long)v * hw + p_row;
   const unsigned* cv = cand_bits + (long long)v * nwords;
   uint4* wrow = words + ((long long)v * H + y) * WW;
   const double* tv = thr_raw + (long long)v * L;
@@ -585,7 +589,7 @@ __global__ void __launch_bounds__(256) tile_words_kernel(const float* __restrict
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       const int x = (wx0 + u) * 32 + lane;
-      r[u] = x < W ? __ldg(rrow + x) : (int)0xbf800000;   // -1.0f: below every threshold
+      r[u] = x < W ? (int)__ldg(rrow + x) : -1;   // below every threshold
     }
 #pragma unroll
     for (int u = 0; u <= U; ++u) cw[u] = wx0 + u <= WW ? __ldg(crow + wx0 + u) : 0u;
@@ -612,7 +616,7 @@ __device__ __forceinline__ void cp_async4(void* smem, const void* gmem) {
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
 
 constexpr int kTwWarps = 8;
-__global__ void __launch_bounds__(kTwWarps * 32) tile_words_t_kernel(const float* __restrict__ rawf,
+__global__ void __launch_bounds__(kTwWarps * 32) tile_words_t_kernel(const raw16_t* __restrict__ rawf,
                                                                     const float* __restrict__ image,
                                                                     const float* __restrict__ gt,
                                                                     const unsigned* __restrict__ cand_bits,
@@ -626,13 +630,19 @@ __global__ void __launch_bounds__(kTwWarps * 32) tile_words_t_kernel(const float
   const int y0 = blockIdx.y * 32;
   const int x0 = tx * 32;
   const long long hw = (long long)H * W;
-  const int* rv = reinterpret_cast<const int*>(rawf + (long long)v * hw);
+  const raw16_t* rv = rawf + (long long)v * hw;
   int (*S)[33] = tile[wid];
   const bool col_in = x0 + lane < W;
   const int nrows = H - y0 < 32 ? H - y0 : 32;
-  for (int r = 0; r < nrows; ++r) {
-    if (col_in) cp_async4(&S[r][lane], rv + (long long)(y0 + r) * W + x0 + lane);
-    else S[r][lane] = (int)0xbf800000;   // -1.0f: below every threshold
+  // coalesced 64-byte row loads, 8 rows in flight, into shared memory
+  for (int r0 = 0; r0 < nrows; r0 += 8) {
+    int t[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k)
+      t[k] = r0 + k < nrows && col_in ? (int)__ldg(rv + (long long)(y0 + r0 + k) * W + x0 + lane) : -1;
+#pragma unroll
+    for (int k = 0; k < 8; ++k)
+      if (r0 + k < nrows) S[r0 + k][lane] = t[k];   // -1: below every threshold
   }
   // thresholds of the view (warp-uniform) while the copies fly
   const double* tv = thr_raw + (long long)v * L;
@@ -650,7 +660,6 @@ __global__ void __launch_bounds__(kTwWarps * 32) tile_words_t_kernel(const float
     const int valid = W - x0;
     if (valid < 32) C &= (1u << valid) - 1u;
   }
-  cp_async_wait_all();
   __syncwarp();
   if (lane >= nrows) return;
   // one compare and one predicated OR per plane and pixel (the bit is an
@@ -756,7 +765,7 @@ __device__ __forceinline__ bool fused_tile_rows(const TileParams& P, WS& S, int 
     if (y_lo < 0) need &= ~((1ull << (-y_lo)) - 1ull);
     if (y_hi < NR - 1) need &= (2ull << y_hi) - 1ull;
   }
-  const int* rv = reinterpret_cast<const int*>(P.rawf + (long long)v * hw);
+  const raw16_t* rv = P.rawf + (long long)v * hw;
   const bool inb = x0 + lane < W;
   // ---- stage the needed rows' raw bit patterns (cp.async, all in flight):
   //      tile rows into S.u.d, the halo pixels of every ext row into S.halo
@@ -764,24 +773,24 @@ __device__ __forceinline__ bool fused_tile_rows(const TileParams& P, WS& S, int 
     const int ey = __ffsll((long long)r) - 1;
     const long long prow = (long long)(y0 - HL + ey) * W;
     const int ty = ey - HL;
-    if (ty >= 0 && ty < kTileH && inb) cp_async4(&S.u.d[ty][lane], rv + prow + x0 + lane);
+    if (ty >= 0 && ty < kTileH && inb) S.u.d[ty][lane] = (int)__ldg(rv + prow + x0 + lane);
   }
   // lane ey (and 32 + lane): the halo pixels x0 - 1 (if HL) and x0 + 32 (if HH) of
   // ext row ey, in registers (loads in flight with the copies)
-  int hl_a = (int)0xbf800000, hr_a = (int)0xbf800000, hl_b = (int)0xbf800000, hr_b = (int)0xbf800000;
+  int hl_a = -1, hr_a = -1, hl_b = -1, hr_b = -1;   // -1: below every threshold
 #pragma unroll
   for (int h = 0; h < (NR > 32 ? 2 : 1); ++h) {
     const int ey = lane + 32 * h;
     if (ey < NR && ((need >> ey) & 1ull)) {
       const long long prow = (long long)(y0 - HL + ey) * W;
-      if (HL > 0 && x0 > 0) (h ? hl_b : hl_a) = __ldg(rv + prow + x0 - 1);
-      if (HH > 0 && x0 + kTileW < W) (h ? hr_b : hr_a) = __ldg(rv + prow + x0 + kTileW);
+      if (HL > 0 && x0 > 0) (h ? hl_b : hl_a) = (int)__ldg(rv + prow + x0 - 1);
+      if (HH > 0 && x0 + kTileW < W) (h ? hr_b : hr_a) = (int)__ldg(rv + prow + x0 + kTileW);
     }
   }
   // halo rows (outside the tile rows) straight into registers
-  int f_top = (int)0xbf800000, f_bot = (int)0xbf800000;   // -1.0f: below every threshold
-  if (HL > 0 && (need & 1ull) && inb) f_top = __ldg(rv + (long long)(y0 - 1) * W + x0 + lane);
-  if (HH > 0 && ((need >> (NR - 1)) & 1ull) && inb) f_bot = __ldg(rv + (long long)(y0 + kTileH) * W + x0 + lane);
+  int f_top = -1, f_bot = -1;   // below every threshold
+  if (HL > 0 && (need & 1ull) && inb) f_top = (int)__ldg(rv + (long long)(y0 - 1) * W + x0 + lane);
+  if (HH > 0 && ((need >> (NR - 1)) & 1ull) && inb) f_bot = (int)__ldg(rv + (long long)(y0 + kTileH) * W + x0 + lane);
   const double* tv = P.thr_raw + (long long)v * P.L;
   const double kInf = __longlong_as_double(0x7ff0000000000000ll);
   const double X0 = __ldg(tv), X1 = P.L > 1 ? __ldg(tv + 1) : kInf, X2 = P.L > 2 ? __ldg(tv + 2) : kInf,
@@ -800,7 +809,6 @@ __device__ __forceinline__ bool fused_tile_rows(const TileParams& P, WS& S, int 
       band = (xr >= X1) + (xr >= X2) + (xr >= X3);
     }
   };
-  cp_async_wait_all();
   __syncwarp();
   const int hx = lane == 0 ? x0 - 1 : x0 + kTileW;
   const bool h_on = (lane == 0 && HL > 0 && x0 > 0) || (lane == 1 && HH > 0 && x0 + kTileW < W);
@@ -808,12 +816,12 @@ __device__ __forceinline__ bool fused_tile_rows(const TileParams& P, WS& S, int 
     const int ey = __ffsll((long long)r) - 1;
     const int ty = ey - HL;
     const long long prow = (long long)(y0 - HL + ey) * W;
-    const int fi = !inb ? (int)0xbf800000 : (ty < 0 ? f_top : (ty >= kTileH ? f_bot : S.u.d[ty][lane]));
-    int fh = (int)0xbf800000;
+    const int fi = !inb ? -1 : (ty < 0 ? f_top : (ty >= kTileH ? f_bot : S.u.d[ty][lane]));
+    int fh = -1;
     if (HL > 0 || HH > 0) {   // lane 0: left halo of ext row ey, lane 1: right halo
       const int l = __shfl_sync(FULL, ey < 32 ? hl_a : hl_b, ey & 31);
       const int r = __shfl_sync(FULL, ey < 32 ? hr_a : hr_b, ey & 31);
-      fh = !h_on ? (int)0xbf800000 : (lane == 0 ? l : r);
+      fh = !h_on ? -1 : (lane == 0 ? l : r);
     }
     bool m, mh;
     int band, bh;
