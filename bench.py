@@ -16,9 +16,9 @@ including it under "full_step".
   roofline  the dominant kernel, minmax_kernel: the one pass over the step's
             attribution inputs (28 B/px = image fp32x3 + gt
             fp32x3 + dominant int32) / its CUDA-event time, vs MEASURED_PEAKS;
-            traffic = its ncu dram bytes (it also writes the 4.125 B/px
-            fp32 raw-error cache and candidate bits).  "tile_pass" reports the
-            bit-plane pass (tile_words_kernel, HBM: 4.125 B/px read) and the
+            traffic = its ncu dram bytes (it also writes the 2.125 B/px
+            16-bit raw-error cache and candidate bits).  "tile_pass" reports the
+            bit-plane pass (tile_words_kernel, HBM: 2.125 B/px read) and the
             warp CCL (tile_bits_kernel, latency-bound) that follow.
   cpu_baseline  the oracle port on a bounded view sample (rank 0, N=1)
 
@@ -473,7 +473,7 @@ def run_ours(args, wl):
 
     # ---- K1-epilogue variant (reported separately): the render's
     #      epilogue runs select and the input pass, the step starts from the
-    #      8 B/px boundary (fp32 raw cache + dominant map); 1 GPU
+    #      6 B/px boundary (16-bit raw cache + dominant map); 1 GPU
     fused = None
     if world == 1 and not args.no_fused:
         gt_v = gt_img   # all views sampled (contiguous): the step's own gt tensor
@@ -504,13 +504,13 @@ def run_ours(args, wl):
             r_ms.append(e_a.elapsed_time(e_b))
             s_ms.append(e_b.elapsed_time(e_c))
         fr, fs = float(np.mean(r_ms)), float(np.mean(s_ms))
-        b8 = 8 * px + BYTES_PER_G_IN * g.n + BYTES_PER_G_OUT * counts["n_out"]
+        b8 = 6 * px + BYTES_PER_G_IN * g.n + BYTES_PER_G_OUT * counts["n_out"]
         fused = {"render_ms": fr, "render_ms_plain": render_ms, "step_ms": fs,
                  "parents_per_s": n_split / (fs * 1e-3), "full_step_ms": fr + fs,
                  "full_step_parents_per_s": n_split / ((fr + fs) * 1e-3),
                  "step_bytes": int(b8), "step_roofline_frac": b8 / (fs * 1e-3) / 1e9 / peak,
                  "note": "render epilogue = select + input pass (raw L1 fp64, per-view min/max, candidate bits, "
-                         "ever-dominant flags); step from the 8 B/px boundary (raw cache + dominant map); "
+                         "ever-dominant flags); step from the 6 B/px boundary (16-bit raw cache + dominant map); "
                          "identical results (tests/test_gpu_rows.py)"}
 
     # ---- e2e: same step through the API from pinned host buffers
