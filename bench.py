@@ -408,7 +408,7 @@ def run_ours(args, wl):
     else:
         def step_fn(gg, gt_, ga_, den_, rng, renders):
             return op.densify_step(gg, ini.extent, cams, gt_, ga_, den_, cfg, rng, renders=renders, plan=plan,
-                                   view_ids=view_ids, want_report=True)
+                                   view_ids=view_ids, want_report=True, one_sync=not args.two_call)
         img_l, dom_l, gt_l = img, dom, gt_img
 
     def step():
@@ -485,7 +485,8 @@ def run_ours(args, wl):
 
         def fused_step():
             return op.densify_step(g, ini.extent, cams, gt_l, ga, den, cfg, np.random.default_rng((args.seed, 0)),
-                                   renders=(img_f, dom_f), plan=plan, view_ids=view_ids, want_report=True)
+                                   renders=(img_f, dom_f), plan=plan, view_ids=view_ids, want_report=True,
+                                   one_sync=not args.two_call)
 
         for _ in range(2):
             fused_render()
@@ -665,6 +666,8 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-parity", action="store_true", help="skip the oracle parity check on the cpu sample")
     ap.add_argument("--no-fused", action="store_true", help="skip the K1-epilogue (fused render) variant")
+    ap.add_argument("--two-call", action="store_true",
+                    help="phase 1 end and phase 2 as two calls (the emit after the host read the counts)")
     ap.add_argument("--replicas", action="store_true",
                     help="N>1: independent replicas (weak scaling) instead of the view-sharded step")
     args = ap.parse_args()

@@ -26,7 +26,7 @@
 extern "C" {
 #endif
 
-#define ADPS_ABI_VERSION 2
+#define ADPS_ABI_VERSION 3
 
 #if defined(__GNUC__)
 #define ADPS_API __attribute__((visibility("default")))
@@ -41,7 +41,8 @@ typedef enum {
   ADPS_DEGENERATE_RAY = 3,
   ADPS_CUDA_ERROR = 4,
   ADPS_OOM = 5,
-  ADPS_BAD_STATE = 6
+  ADPS_BAD_STATE = 6,
+  ADPS_INTERNAL = 7   /* a bound the implementation relies on was violated */
 } adps_status;
 
 /* Per-candidate outcome (ref/adc.py:198-226 branch order). */
@@ -221,6 +222,22 @@ ADPS_API adps_status adps_step_phase1_end(adps_plan* plan, void* stream, adps_co
 ADPS_API adps_status adps_step_phase2(adps_plan* plan, void* stream, const adps_gaussians* g,
                              const double* fallback_normals, adps_gaussians_out* out,
                              int64_t* index_map, int32_t* child_parent, int64_t* insert_offset);
+
+/* Sync-free end of the step: phase 1 end and phase 2 in one call, with the
+ * emit launched before the host reads any count (the counts arrive with the
+ * call's single synchronisation).  Arguments as adps_step_phase2, into
+ * arrays of out_cap rows (mu ... index_map) and app_cap rows (child_parent),
+ * which must reach adps_step_capacity's bounds (available after
+ * adps_step_phase1_begin); counts->n_out rows are written.  The fallback
+ * normals must be on the device when the stream reaches the emit: drawn by
+ * adps_normals_pcg64 (any sync mode) or uploaded before the call.
+ * report (optional, NULL to skip): int32 [4*n_split + n_split*V + n_clone]
+ * (the counts of phase1_begin), filled as adps_copy_report fills it. */
+ADPS_API adps_status adps_step_capacity(adps_plan* plan, int64_t* out_cap, int64_t* app_cap);
+ADPS_API adps_status adps_step_phase1_end_emit(adps_plan* plan, void* stream, const adps_gaussians* g,
+                             const double* fallback_normals, adps_gaussians_out* out,
+                             int64_t* index_map, int32_t* child_parent, int64_t* insert_offset,
+                             int64_t out_cap, int64_t app_cap, int32_t* report, adps_counts* counts);
 
 ADPS_API adps_status adps_get_report(adps_plan* plan, adps_report* report);
 

@@ -14,7 +14,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("ADPS_LIB") or os.path.join(HERE, "libadps.so")   # ADPS_LIB: dev variants
 
 ADPS_OK, ADPS_INVALID_ARG, ADPS_V_TOO_LARGE, ADPS_DEGENERATE_RAY = 0, 1, 2, 3
-ADPS_CUDA_ERROR, ADPS_OOM, ADPS_BAD_STATE = 4, 5, 6
+ADPS_CUDA_ERROR, ADPS_OOM, ADPS_BAD_STATE, ADPS_INTERNAL = 4, 5, 6, 7
 CASE_SPLIT, CASE_FALLBACK, CASE_RESET = 0, 1, 2
 PARAM_LARGE_THRESHOLD, PARAM_TILE_PATH, PARAM_DEFERRED_TILES = 1, 2, 3
 PARAM_NORMALS_CONSUMED, PARAM_NORMALS_STATUS, PARAM_RAW_CACHE = 4, 5, 6
@@ -57,7 +57,7 @@ class Report(C.Structure):
                 ("regions_per_view", vp), ("clone_index", vp), ("n_views", C.c_int32)]
 
 
-ABI_VERSION = 2
+ABI_VERSION = 3
 
 EXPORTS = (
     "adps_abi_version", "adps_last_error", "adps_plan_create", "adps_plan_destroy", "adps_render",
@@ -68,7 +68,7 @@ EXPORTS = (
     "adps_step_phase1_import", "adps_step_phase1_merge", "adps_vanilla_phase1", "adps_reset_flags",
     "adps_remap_rows", "adps_set_parent_sharding", "adps_get_shard", "adps_step_phase1_finish",
     "adps_copy_report", "adps_accumulate_stats_f64", "adps_prune_index", "adps_render_stats",
-    "adps_render_fused", "adps_check_guards",
+    "adps_render_fused", "adps_check_guards", "adps_step_capacity", "adps_step_phase1_end_emit",
 )
 
 _lib = None
@@ -99,6 +99,9 @@ def load(path: str = LIB_PATH):
     lib.adps_step_phase1_begin.argtypes = lib.adps_step_phase1.argtypes
     lib.adps_step_phase1_end.argtypes = [vp, vp, C.POINTER(Counts)]
     lib.adps_step_phase2.argtypes = [vp, vp, C.POINTER(Gaussians), vp, C.POINTER(GaussiansOut), vp, vp, vp]
+    lib.adps_step_capacity.argtypes = [vp, C.POINTER(C.c_int64), C.POINTER(C.c_int64)]
+    lib.adps_step_phase1_end_emit.argtypes = [vp, vp, C.POINTER(Gaussians), vp, C.POINTER(GaussiansOut), vp, vp, vp,
+                                              C.c_int64, C.c_int64, vp, C.POINTER(Counts)]
     lib.adps_get_report.argtypes = [vp, C.POINTER(Report)]
     lib.adps_copy_report.argtypes = [vp, vp, vp, C.c_int64, C.c_int64]
     lib.adps_get_regions.argtypes = [vp] + [C.POINTER(vp)] * 5 + [C.POINTER(C.c_int64)]

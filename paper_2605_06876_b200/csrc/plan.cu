@@ -1336,20 +1336,17 @@ static adps_status phase1_merge_part(adps_plan* P, cudaStream_t s) {
   return ADPS_OK;
 }
 
-static adps_status phase1_finish(adps_plan* P, cudaStream_t s, adps_counts* counts) {
+// the offsets (ref/adc.py:229-244) on the device: everything phase 2 needs,
+// with the counts still on the device (phase1_finish_collect reads them)
+static adps_status phase1_finish_launch(adps_plan* P, cudaStream_t s) {
   adps_status st = ADPS_OK;
-  const adps_gaussians* g = &P->cx.g;
   const long long n = P->cx.n;
-  const adps_config* cfg = &P->cx.cfg;
-  const int V = P->v_glob, H = P->cx.H, W = P->cx.W;
   const long long nn = n > 0 ? n : 1;
   Counters* ctr = P->ctr.as<Counters>();
   ScanState sst, sst2;
   st = scan_state(P, P->scan_val, P->scan_flag, P->scan_ticket, nn, &sst);
   if (st != ADPS_OK) return st;
-  const long long n_regions = P->n_regions_cur;
   const long long n_split = (long long)P->ctr_host->n_split;
-  const long long n_clone = (long long)P->ctr_host->n_clone;
   const long long sc = n_split > 0 ? n_split : 1;
   // ---- offsets (ref/adc.py:229-244)
   st = scan_state(P, P->scan2_val, P->scan2_flag, P->scan2_ticket, sc, &sst2);
@@ -1378,6 +1375,20 @@ static adps_status phase1_finish(adps_plan* P, cudaStream_t s, adps_counts* coun
     CK(launch_offsets_keep(oa, sst, s));
   }
   mark(P, "offsets", s, 2);
+  return ADPS_OK;
+}
+
+// the host side of the finish: one copy of the counters, one synchronisation
+static adps_status phase1_finish_collect(adps_plan* P, cudaStream_t s, adps_counts* counts) {
+  const adps_gaussians* g = &P->cx.g;
+  const long long n = P->cx.n;
+  const adps_config* cfg = &P->cx.cfg;
+  const int V = P->v_glob, H = P->cx.H, W = P->cx.W;
+  Counters* ctr = P->ctr.as<Counters>();
+  (void)g;
+  const long long n_regions = P->n_regions_cur;
+  const long long n_split = (long long)P->ctr_host->n_split;
+  const long long n_clone = (long long)P->ctr_host->n_clone;
   CK(cudaMemcpyAsync(P->ctr_host, ctr, sizeof(Counters), cudaMemcpyDeviceToHost, s));
   CK(cudaStreamSynchronize(s));
   const Counters& C = *P->ctr_host;
@@ -1407,6 +1418,12 @@ static adps_status phase1_finish(adps_plan* P, cudaStream_t s, adps_counts* coun
   P->have_phase1 = true;
   if (C.degenerate) return fail(ADPS_DEGENERATE_RAY, "quadratic coefficient underflows (DegenerateRayError)");
   return ADPS_OK;
+}
+
+static adps_status phase1_finish(adps_plan* P, cudaStream_t s, adps_counts* counts) {
+  adps_status st = phase1_finish_launch(P, s);
+  if (st != ADPS_OK) return st;
+  return phase1_finish_collect(P, s, counts);
 }
 
 static adps_status phase1_merge(adps_plan* P, cudaStream_t s, adps_counts* counts) {
@@ -1547,30 +1564,16 @@ extern "C" adps_status adps_step_phase1_finish(adps_plan* P, void* stream_v, int
   return phase1_finish(P, s, counts);
 }
 
-extern "C" adps_status adps_step_phase2(adps_plan* P, void* stream_v, const adps_gaussians* g,
-                                        const double* fallback_normals, adps_gaussians_out* out,
-                                        int64_t* index_map, int32_t* child_parent, int64_t* insert_offset) {
-  if (!P) return fail(ADPS_INVALID_ARG, "plan is NULL");
-  if (!P->have_phase1) return fail(ADPS_BAD_STATE, "phase 2 without a successful phase 1");
-  adps_status st = check_gaussians(g, P->n);
-  if (st != ADPS_OK) return st;
-  if (P->counts.n_out == 0) return ADPS_OK;   // nothing to write (e.g. an empty scene)
-  if (!out || !index_map || !out->mu || !out->scale || !out->rot || !out->opacity || !out->sh_dc)
-    return fail(ADPS_INVALID_ARG, "outputs are NULL");
-  if (P->counts.n_fallback > 0 && !fallback_normals) return fail(ADPS_INVALID_ARG, "fallback normals are NULL");
-  if (g->sh_rest_k != P->sh_k || out->sh_rest_k != P->sh_k)
-    return fail(ADPS_INVALID_ARG, "sh_rest_k differs between phases/outputs");
-  if (P->sh_k > 0 && !out->sh_rest) return fail(ADPS_INVALID_ARG, "out.sh_rest is NULL");
-  CK(cudaSetDevice(P->device));
-  cudaStream_t s = (cudaStream_t)stream_v;
-  mark_start(P, s, false);
+static adps_status copy_report_impl(adps_plan* P, cudaStream_t s, int32_t* dst, long long n_split, long long n_clone,
+                                    long long V);
+
+// EmitArgs of phase 2 from the plan's phase-1 state (counts filled by the caller)
+static EmitArgs emit_args(adps_plan* P, const adps_gaussians* g, const double* fallback_normals,
+                          const adps_gaussians_out* out, int64_t* index_map, int32_t* child_parent,
+                          int64_t* insert_offset) {
   EmitArgs ea;
   ea.g = to_in(g);
   ea.n = P->n;
-  ea.n_split = P->counts.n_split;
-  ea.n_clone = P->counts.n_clone;
-  ea.n_keep = P->counts.n_keep;
-  ea.n_inserted = P->counts.n_inserted;
   ea.keep_pos = P->keep_pos.as<int>();
   ea.split_list = P->split_list.as<int>();
   ea.clone_list = P->clone_list.as<int>();
@@ -1592,8 +1595,119 @@ extern "C" adps_status adps_step_phase2(adps_plan* P, void* stream_v, const adps
   ea.index_map = (long long*)index_map;
   ea.child_parent = child_parent;
   ea.insert_offset = (long long*)insert_offset;
+  return ea;
+}
+
+static adps_status check_outputs(adps_plan* P, const adps_gaussians* g, const adps_gaussians_out* out,
+                                 const int64_t* index_map) {
+  if (!out || !index_map || !out->mu || !out->scale || !out->rot || !out->opacity || !out->sh_dc)
+    return fail(ADPS_INVALID_ARG, "outputs are NULL");
+  if (g->sh_rest_k != P->sh_k || out->sh_rest_k != P->sh_k)
+    return fail(ADPS_INVALID_ARG, "sh_rest_k differs between phases/outputs");
+  if (P->sh_k > 0 && !out->sh_rest) return fail(ADPS_INVALID_ARG, "out.sh_rest is NULL");
+  return ADPS_OK;
+}
+
+extern "C" adps_status adps_step_phase2(adps_plan* P, void* stream_v, const adps_gaussians* g,
+                                        const double* fallback_normals, adps_gaussians_out* out,
+                                        int64_t* index_map, int32_t* child_parent, int64_t* insert_offset) {
+  if (!P) return fail(ADPS_INVALID_ARG, "plan is NULL");
+  if (!P->have_phase1) return fail(ADPS_BAD_STATE, "phase 2 without a successful phase 1");
+  adps_status st = check_gaussians(g, P->n);
+  if (st != ADPS_OK) return st;
+  if (P->counts.n_out == 0) return ADPS_OK;   // nothing to write (e.g. an empty scene)
+  st = check_outputs(P, g, out, index_map);
+  if (st != ADPS_OK) return st;
+  if (P->counts.n_fallback > 0 && !fallback_normals) return fail(ADPS_INVALID_ARG, "fallback normals are NULL");
+  CK(cudaSetDevice(P->device));
+  cudaStream_t s = (cudaStream_t)stream_v;
+  mark_start(P, s, false);
+  EmitArgs ea = emit_args(P, g, fallback_normals, out, index_map, child_parent, insert_offset);
+  ea.n_split = P->counts.n_split;
+  ea.n_clone = P->counts.n_clone;
+  ea.n_keep = P->counts.n_keep;
+  ea.n_inserted = P->counts.n_inserted;
   CK(launch_emit(ea, s, P->timing ? nullptr : P->aux, P->ev_fork, P->ev_small));
   mark(P, "emit", s, (P->n > 0 ? 1 : 0) + ((P->counts.n_split + P->counts.n_clone) > 0 ? 1 : 0));
+  return ADPS_OK;
+}
+
+extern "C" adps_status adps_step_capacity(adps_plan* P, int64_t* out_cap, int64_t* app_cap) {
+  if (!P || !out_cap || !app_cap) return fail(ADPS_INVALID_ARG, "NULL argument");
+  if (!P->have_begin) return fail(ADPS_BAD_STATE, "capacity without phase1_begin");
+  // a split parent leaves the survivors unless reset and inserts at most
+  // max(n_max + 1, 2) rows (N_i <= n_max children + the parent copy, or the 2
+  // fallback children); clones append one row each (ref/adc.py:198-244)
+  const long long n = P->cx.n;
+  const long long n_split = (long long)P->ctr_host->n_split;
+  const long long n_clone = (long long)P->ctr_host->n_clone;
+  const long long per = std::max<long long>((long long)P->cx.cfg.n_max + 1, 2);
+  *app_cap = n_split * per + n_clone;
+  *out_cap = n - n_split + *app_cap;   // (a reset parent stays a survivor: its 1 row <= per)
+  return ADPS_OK;
+}
+
+extern "C" adps_status adps_step_phase1_end_emit(adps_plan* P, void* stream_v, const adps_gaussians* g,
+                                                 const double* fallback_normals, adps_gaussians_out* out,
+                                                 int64_t* index_map, int32_t* child_parent, int64_t* insert_offset,
+                                                 int64_t out_cap, int64_t app_cap, int32_t* report,
+                                                 adps_counts* counts) {
+  if (!P || !counts) return fail(ADPS_INVALID_ARG, "NULL argument");
+  if (!P->have_begin) return fail(ADPS_BAD_STATE, "phase1_end_emit without phase1_begin");
+  adps_status st = check_gaussians(g, P->cx.n);
+  if (st != ADPS_OK) return st;
+  if (g->mu != P->cx.g.mu || g->opacity != P->cx.g.opacity)
+    return fail(ADPS_INVALID_ARG, "Gaussians differ from phase1_begin's");
+  int64_t need_out = 0, need_app = 0;
+  st = adps_step_capacity(P, &need_out, &need_app);
+  if (st != ADPS_OK) return st;
+  if (out_cap < need_out || app_cap < need_app)
+    return fail(ADPS_INVALID_ARG, "output capacity %lld/%lld below the step bound %lld/%lld", (long long)out_cap,
+                (long long)app_cap, (long long)need_out, (long long)need_app);
+  const bool any_out = need_out > 0;
+  P->sh_k = g->sh_rest_k;
+  if (any_out) {
+    st = check_outputs(P, g, out, index_map);
+    if (st != ADPS_OK) return st;
+  }
+  if (P->ctr_host->n_fallback_pre > 0 && !fallback_normals)
+    return fail(ADPS_INVALID_ARG, "fallback normals are NULL");
+  P->have_begin = false;
+  cudaStream_t s = (cudaStream_t)stream_v;
+  long long nr = 0;
+  st = phase1_local(P, s, &nr, /*defer_child=*/true);
+  if (st == ADPS_OK) st = phase1_merge_part(P, s);
+  if (st == ADPS_OK) st = phase1_finish_launch(P, s);
+  if (st != ADPS_OK) {
+    drop_pending_normals(P);
+    return st;
+  }
+  // phase 2 on the same stream, before the host reads a single count
+  P->n = P->cx.n;
+  P->eta = P->cx.cfg.eta;
+  P->fb_children = 2;
+  if (any_out) {
+    Counters* ctr = P->ctr.as<Counters>();
+    mark_start(P, s, false);
+    EmitArgs ea = emit_args(P, g, fallback_normals, out, index_map, child_parent, insert_offset);
+    ea.n_split = (long long)P->ctr_host->n_split;
+    ea.n_clone = (long long)P->ctr_host->n_clone;
+    ea.dev_keep = &ctr->n_keep;
+    ea.dev_inserted = &ctr->n_inserted;
+    ea.n_ins_max = need_app - ea.n_clone;
+    ea.out_cap = out_cap;
+    ea.app_cap = app_cap;
+    CK(launch_emit(ea, s, P->timing ? nullptr : P->aux, P->ev_fork, P->ev_small));
+    mark(P, "emit", s, (P->n > 0 ? 1 : 0) + ((ea.n_split + ea.n_clone) > 0 ? 1 : 0));
+  }
+  if (report) {   // the SplitReport arrays (adps_copy_report's layout), before the sync too
+    st = copy_report_impl(P, s, report, (long long)P->ctr_host->n_split, (long long)P->ctr_host->n_clone, P->v_glob);
+    if (st != ADPS_OK) return st;
+  }
+  st = phase1_finish_collect(P, s, counts);
+  if (st != ADPS_OK) return st;
+  if (counts->n_out > out_cap || counts->n_out - counts->n_keep > app_cap)
+    return fail(ADPS_INTERNAL, "step outgrew its capacity bound (%lld rows)", (long long)counts->n_out);
   return ADPS_OK;
 }
 
@@ -1610,6 +1724,19 @@ extern "C" adps_status adps_get_report(adps_plan* P, adps_report* r) {
   return ADPS_OK;
 }
 
+static adps_status copy_report_impl(adps_plan* P, cudaStream_t s, int32_t* dst, long long n_split, long long n_clone,
+                                    long long V) {
+  const void* src[6] = {P->split_list.p, P->cand_case.p, P->cand_props.p, P->cand_merged.p, P->regions_per_view.p,
+                        P->clone_list.p};
+  const long long len[6] = {n_split, n_split, n_split, n_split, n_split * V, n_clone};
+  long long off = 0;
+  for (int i = 0; i < 6; ++i) {
+    if (len[i] > 0) CK(cudaMemcpyAsync(dst + off, src[i], 4 * len[i], cudaMemcpyDeviceToDevice, s));
+    off += len[i];
+  }
+  return ADPS_OK;
+}
+
 extern "C" adps_status adps_copy_report(adps_plan* P, void* stream_v, int32_t* dst, int64_t n_split, int64_t n_clone) {
   if (!P || (!dst && n_split + n_clone > 0)) return fail(ADPS_INVALID_ARG, "NULL argument");
   if (!P->have_phase1) return fail(ADPS_BAD_STATE, "no phase 1 result");
@@ -1618,16 +1745,7 @@ extern "C" adps_status adps_copy_report(adps_plan* P, void* stream_v, int32_t* d
     return fail(ADPS_INVALID_ARG, "counts exceed the last phase 1 (%lld split, %lld clone)",
                 (long long)P->counts.n_split, (long long)P->counts.n_clone);
   CK(cudaSetDevice(P->device));
-  cudaStream_t s = (cudaStream_t)stream_v;
-  const void* src[6] = {P->split_list.p, P->cand_case.p, P->cand_props.p, P->cand_merged.p, P->regions_per_view.p,
-                        P->clone_list.p};
-  const long long len[6] = {n_split, n_split, n_split, n_split, n_split * P->V, n_clone};
-  long long off = 0;
-  for (int i = 0; i < 6; ++i) {
-    if (len[i] > 0) CK(cudaMemcpyAsync(dst + off, src[i], 4 * len[i], cudaMemcpyDeviceToDevice, s));
-    off += len[i];
-  }
-  return ADPS_OK;
+  return copy_report_impl(P, (cudaStream_t)stream_v, dst, n_split, n_clone, P->V);
 }
 
 extern "C" adps_status adps_get_regions(adps_plan* P, const adps_region_record** records,

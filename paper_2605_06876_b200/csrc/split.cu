@@ -366,10 +366,10 @@ __device__ __forceinline__ void copy_gaussian(const EmitArgs& a, long long src, 
 // per clone).  Rows are written where the offsets put them.
 constexpr int kEmitThreads = 256;
 
-__device__ __forceinline__ void emit_insert_row(const EmitArgs& a, long long k, int j) {
+__device__ __forceinline__ void emit_insert_row(const EmitArgs& a, long long n_keep, long long k, int j) {
   const int c = a.cand_case[k];
   const long long gi = a.split_list[k];
-  const long long dst = a.n_keep + a.ins_off[k] + j;
+  const long long dst = n_keep + a.ins_off[k] + j;
   const int K = a.g.sh_k;
   if (c == ADPS_CASE_FALLBACK) {                        // vanilla_split(parent, n, eta, rng)
     double q[4] = {a.g.rot[4 * gi], a.g.rot[4 * gi + 1], a.g.rot[4 * gi + 2], a.g.rot[4 * gi + 3]};
@@ -462,13 +462,21 @@ __global__ void __launch_bounds__(kEmitThreads) emit_survivors_kernel(EmitArgs a
 
 __global__ void __launch_bounds__(kEmitThreads) emit_kernel(EmitArgs a, long long b_ins) {
   const long long blk = blockIdx.x;
+  long long n_keep = a.n_keep, n_inserted = a.n_inserted;
+  bool capped = false;
+  if (a.dev_keep) {   // counts still on the device (sync-free form)
+    n_keep = (long long)*a.dev_keep;
+    n_inserted = (long long)*a.dev_inserted;
+    capped = true;
+  }
   if (blk < b_ins) {                                    // candidate inserts, ascending index
     // a thread per inserted row: its candidate is the last k with ins_off[k] <= r
     // (ins_off is the exclusive prefix of the rows per candidate), found by a
     // binary search; rows of one candidate are adjacent, so neighbouring threads
     // mostly search the same path (cached)
     const long long r = blk * kEmitThreads + threadIdx.x;
-    if (r >= a.n_inserted) return;
+    if (r >= n_inserted) return;
+    if (capped && (n_keep + r >= a.out_cap || r >= a.app_cap)) return;
     long long lo = 0, hi = a.n_split - 1;
     while (lo < hi) {
       const long long mid = (lo + hi + 1) >> 1;
@@ -479,20 +487,21 @@ __global__ void __launch_bounds__(kEmitThreads) emit_kernel(EmitArgs a, long lon
     // candidate's: the last k with ins_off[k] <= r always has rows)
     const long long k = lo;
     const int j = (int)(r - __ldg(a.ins_off + k));
-    emit_insert_row(a, k, j);
-    if (a.insert_offset && j == 0) a.insert_offset[k] = a.n_keep + a.ins_off[k];
+    emit_insert_row(a, n_keep, k, j);
+    if (a.insert_offset && j == 0) a.insert_offset[k] = n_keep + a.ins_off[k];
   } else if (blk < b_ins + a.b_off) {                   // insert offsets of the reset candidates
     const long long k = (blk - b_ins) * kEmitThreads + threadIdx.x;
     if (k < a.n_split && a.insert_offset && a.cand_case[k] == ADPS_CASE_RESET)
-      a.insert_offset[k] = a.n_keep + a.ins_off[k];
+      a.insert_offset[k] = n_keep + a.ins_off[k];
   } else {                                              // clones, ascending
     const long long j = (blk - b_ins - a.b_off) * kEmitThreads + threadIdx.x;
     if (j < a.n_clone) {
-      const long long dst = a.n_keep + a.n_inserted + j;
+      const long long dst = n_keep + n_inserted + j;
+      if (capped && (dst >= a.out_cap || n_inserted + j >= a.app_cap)) return;
       const int src = a.clone_list[j];
       copy_gaussian(a, src, dst);
       a.index_map[dst] = -1;
-      if (a.child_parent) a.child_parent[a.n_inserted + j] = src;
+      if (a.child_parent) a.child_parent[n_inserted + j] = src;
     }
   }
 }
@@ -512,7 +521,7 @@ cudaError_t launch_emit(const EmitArgs& a, cudaStream_t s, cudaStream_t aux, cud
     long long b = (a.n * 4 + 8ll * kEmitThreads - 1) / (8ll * kEmitThreads);
     emit_survivors_kernel<<<dim3((unsigned)b, a.g.sh_k > 0 ? 6u : 5u), kEmitThreads, 0, ss>>>(a);
   }
-  const long long b_ins = (a.n_inserted + kEmitThreads - 1) / kEmitThreads;
+  const long long b_ins = ((a.dev_keep ? a.n_ins_max : a.n_inserted) + kEmitThreads - 1) / kEmitThreads;
   const long long b_clone = (a.n_clone + kEmitThreads - 1) / kEmitThreads;
   EmitArgs a2 = a;
   a2.b_off = a.insert_offset ? (a.n_split + kEmitThreads - 1) / kEmitThreads : 0;

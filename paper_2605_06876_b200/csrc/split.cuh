@@ -126,6 +126,13 @@ struct EmitArgs {
   int* child_parent;        // [n_out - n_keep] old index each appended row came from, or null
   long long* insert_offset; // [n_split] output row of candidate k's first insert, or null
   long long b_off;          // (launch internal) blocks writing the reset candidates' insert offsets
+  // sync-free form (adps_step_phase1_end_emit): n_keep / n_inserted read on the
+  // device, the grid sized from n_inserted <= n_ins_max, rows past the caller's
+  // capacities dropped (never reached when the bounds hold)
+  const unsigned long long* dev_keep = nullptr;
+  const unsigned long long* dev_inserted = nullptr;
+  long long n_ins_max = 0;
+  long long out_cap = 0, app_cap = 0;
 };
 cudaError_t launch_emit(const EmitArgs& a, cudaStream_t s, cudaStream_t aux = nullptr, cudaEvent_t fork = nullptr,
                         cudaEvent_t join = nullptr);

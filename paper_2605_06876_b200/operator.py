@@ -94,6 +94,11 @@ class GaussianTensors:
                                torch.empty(n, 3, dtype=F32, device=device),
                                torch.empty(n, sh_k, 3, dtype=F32, device=device) if sh_k else None)
 
+    def head(self, n: int) -> "GaussianTensors":
+        """The first n rows (views of the same storage)."""
+        return GaussianTensors(self.mu[:n], self.scale[:n], self.rot[:n], self.opacity[:n], self.sh_dc[:n],
+                               self.sh_rest[:n] if self.sh_k else None)
+
     @staticmethod
     def from_numpy(mu, scale, rot, opacity, sh_dc, sh_rest=None, device=None) -> "GaussianTensors":
         d = _require_cuda(device)
@@ -350,6 +355,30 @@ class Plan:
         _abi.check(self.lib.adps_step_phase1_end(self._h, self._stream(), C.byref(counts)))
         return counts.as_dict()
 
+    def capacity(self) -> tuple:
+        """(out_cap, app_cap): row bounds of the step begun by phase1_begin."""
+        oc, ac = C.c_int64(), C.c_int64()
+        _abi.check(self.lib.adps_step_capacity(self._h, C.byref(oc), C.byref(ac)))
+        return int(oc.value), int(ac.value)
+
+    def phase1_end_emit(self, g, normals, out: GaussianTensors, index_map: torch.Tensor,
+                        child_parent: torch.Tensor, insert_offset: torch.Tensor, report: torch.Tensor = None) -> dict:
+        """phase1_end + phase2 with one synchronisation (adps_step_phase1_end_emit):
+        out/index_map hold capacity()[0] rows, child_parent capacity()[1]; report
+        (optional) int32 [4 n_split + n_split V + n_clone] gets the report arrays."""
+        counts = _abi.Counts()
+        ga = g.abi()
+        oa = _abi.GaussiansOut(out.mu.data_ptr(), out.scale.data_ptr(), out.rot.data_ptr(),
+                               out.opacity.data_ptr(), out.sh_dc.data_ptr(),
+                               out.sh_rest.data_ptr() if out.sh_k else None, out.sh_k)
+        _abi.check(self.lib.adps_step_phase1_end_emit(
+            self._h, self._stream(), C.byref(ga), _ptr(normals), C.byref(oa), _ptr(index_map),
+            _ptr(child_parent) if child_parent.numel() else None,
+            _ptr(insert_offset) if insert_offset.numel() else None,
+            out.n, child_parent.numel(), _ptr(report) if report is not None and report.numel() else None,
+            C.byref(counts)))
+        return counts.as_dict()
+
     # -- view-sharded phase 1 (multi-GPU; see sharded.py and include/adps.h)
     def set_view_sharding(self, offset: int, stride: int, n_views_global: int):
         _abi.check(self.lib.adps_set_view_sharding(self._h, int(offset), int(stride), int(n_views_global)))
@@ -528,9 +557,7 @@ class Plan:
         # one buffer, one native call for the six copies
         buf = torch.empty(4 * n_split + n_split * v + n_clone, dtype=torch.int32, device=self.device)
         _abi.check(self.lib.adps_copy_report(self._h, self._stream(), _ptr(buf), int(n_split), int(n_clone)))
-        parts = torch.split(buf, [n_split] * 4 + [n_split * v, n_clone])
-        return dict(cand_index=parts[0], cand_case=parts[1], cand_proposals=parts[2], cand_merged=parts[3],
-                    regions_per_view=parts[4].view(-1, max(v, 1)), clone_index=parts[5])
+        return _report_views(buf, n_split, n_clone, v)
 
     def regions(self) -> dict:
         """Region records of the last phase 1, in reference order (diagnostic)."""
@@ -709,6 +736,13 @@ class FallbackNormals:
         return self.normals
 
 
+def _report_views(buf: torch.Tensor, n_split: int, n_clone: int, v: int) -> dict:
+    """The SplitReport arrays as views of adps_copy_report's buffer."""
+    parts = torch.split(buf, [n_split] * 4 + [n_split * v, n_clone])
+    return dict(cand_index=parts[0], cand_case=parts[1], cand_proposals=parts[2], cand_merged=parts[3],
+                regions_per_view=parts[4].view(-1, max(v, 1)), clone_index=parts[5])
+
+
 def _step_outputs(n_out: int, sh_k: int, n_app: int, n_split: int, dev, out: GaussianTensors = None):
     """(GaussianTensors, index_map int64, child_parent int32, insert_offset int64) for phase 2.
     (Separate allocations: the caching allocator serves these sizes from its
@@ -722,7 +756,7 @@ def _step_outputs(n_out: int, sh_k: int, n_app: int, n_split: int, dev, out: Gau
 def densify_step(g: GaussianTensors, extent: float, cameras, gt, grad_accum: torch.Tensor,
                  denom: torch.Tensor, cfg, rng, *, renders=None, plan: Plan = None,
                  view_ids=None, want_report: bool = True, out: GaussianTensors = None,
-                 fused: bool = False) -> StepResult:
+                 fused: bool = False, one_sync: bool = True) -> StepResult:
     """One AdpSplit densify step on device tensors (ref/adc.py:143-245).
 
     cameras: all C cameras ([C,18] rows or Camera objects).  gt: [C,H,W,3]
@@ -730,7 +764,11 @@ def densify_step(g: GaussianTensors, extent: float, cameras, gt, grad_accum: tor
     dominant) of the sampled views (the stage boundary the reference tests
     reach by monkeypatching ``adc.render``); rendered on the GPU otherwise --
     with ``fused`` by the render whose epilogue also runs the step's input
-    pass (adps_render_fused; same results).
+    pass (adps_render_fused; same results).  one_sync: when the fallback
+    normals are drawn on the device (PCG64) and no ``out`` is given, phase 1's
+    end and the emit are one call with one synchronisation
+    (adps_step_phase1_end_emit); the outputs are then row-prefix views of
+    arrays sized by the step's bounds.  Same results either way.
     """
     plan = plan or default_plan(g.device)
     cams = camera_rows(cameras)
@@ -752,21 +790,42 @@ def densify_step(g: GaussianTensors, extent: float, cameras, gt, grad_accum: tor
     counts = plan.phase1_begin(g, extent, grad_accum, denom, cfg, cams_v, image, gt_v, dom)
     nf = counts["n_fallback"]
     draw = FallbackNormals(plan, rng, nf)
-    try:
-        counts = plan.phase1_end()
-    finally:
-        draw.join()
-    if counts["n_fallback"] != nf:
-        raise RuntimeError("fallback count changed between phase-1 halves")
-    normals = draw.result()
-    n_out = counts["n_out"]
-    out, index_map, child_parent, insert_offset = _step_outputs(n_out, g.sh_k, n_out - counts["n_keep"],
-                                                                counts["n_split"], dev, out)
-    plan.phase2(g, normals, out, index_map, child_parent, insert_offset)
+    if one_sync and out is None and (nf == 0 or draw.gpu):
+        # normals on the device: the emit goes out with phase 1's end, into
+        # arrays sized by the step's row bounds, before the host reads a count
+        out_cap, app_cap = plan.capacity()
+        out_full, im_full, cp_full, insert_offset = _step_outputs(out_cap, g.sh_k, app_cap, counts["n_split"], dev)
+        ns, ncl, nv = counts["n_split"], counts["n_clone"], len(view_ids)
+        rep_buf = torch.empty(4 * ns + ns * nv + ncl, dtype=torch.int32, device=dev) if want_report else None
+        dev_normals = draw.normals
+        counts = plan.phase1_end_emit(g, dev_normals, out_full, im_full, cp_full, insert_offset, rep_buf)
+        if counts["n_fallback"] != nf:
+            raise RuntimeError("fallback count changed between phase-1 halves")
+        normals = draw.result()
+        n_out = counts["n_out"]
+        out, index_map = out_full.head(n_out), im_full[:n_out]
+        child_parent = cp_full[:n_out - counts["n_keep"]]
+        if normals is not dev_normals:
+            # the device normals failed their wedge test: emit again with the host's
+            plan.phase2(g, normals, out, index_map, child_parent, insert_offset)
+    else:
+        rep_buf = None
+        try:
+            counts = plan.phase1_end()
+        finally:
+            draw.join()
+        if counts["n_fallback"] != nf:
+            raise RuntimeError("fallback count changed between phase-1 halves")
+        normals = draw.result()
+        n_out = counts["n_out"]
+        out, index_map, child_parent, insert_offset = _step_outputs(n_out, g.sh_k, n_out - counts["n_keep"],
+                                                                    counts["n_split"], dev, out)
+        plan.phase2(g, normals, out, index_map, child_parent, insert_offset)
     res = StepResult(gaussians=out, index_map=index_map, counts=counts, view_ids=list(view_ids),
                      normals=normals, child_parent=child_parent, insert_offset=insert_offset)
     if want_report:
-        res.report_arrays = plan.report_arrays(counts["n_split"], counts["n_clone"])
+        res.report_arrays = (_report_views(rep_buf, ns, ncl, nv) if rep_buf is not None
+                             else plan.report_arrays(counts["n_split"], counts["n_clone"]))
     if plan.timing:
         res.stage_ms = plan.stage_ms()
     return res

@@ -26,7 +26,7 @@ def test_library_exports_every_declared_symbol():
     for s in syms:
         assert hasattr(lib, s), s
     assert set(syms) == set(_abi.EXPORTS)
-    assert lib.adps_abi_version() == _abi.ABI_VERSION == 2
+    assert lib.adps_abi_version() == _abi.ABI_VERSION == 3
 
 
 def test_struct_layouts():

@@ -478,13 +478,14 @@ def test_determinism_at_scale(op, cfg_name):
     g, gt_img, img, dom = d["g"], d["gt_img"], d["img"], d["dom"]
     cfg = AdpSplitConfig(v_views=len(cams), n_max=wl.n_max)
     digests = []
-    # block CCL / recomputed raw / no bit planes / words pass: same bits
-    for path, raw in ((0, 1), (0, 1), (1, 1), (0, 0), (2, 1), (3, 1)):
+    # block CCL / recomputed raw / no bit planes / words pass / phase 2 as its own call: same bits
+    for path, raw, one_sync in ((0, 1, True), (0, 1, True), (1, 1, True), (0, 0, True), (2, 1, True),
+                                (3, 1, True), (0, 1, False)):
         plan.set_tile_path(path)
         plan.set_raw_cache(raw)
         res = op.densify_step(g, ini.extent, cams, gt_img, torch.as_tensor(ga, device="cuda"),
                               torch.as_tensor(den, device="cuda"), cfg, np.random.default_rng(0),
-                              renders=(img, dom), plan=plan, view_ids=list(range(len(cams))))
+                              renders=(img, dom), plan=plan, view_ids=list(range(len(cams))), one_sync=one_sync)
         digests.append((res.counts, _step_digest(op, plan, res)))
     plan.set_tile_path(0)
     plan.set_raw_cache(1)

@@ -322,3 +322,79 @@ def test_no_write_past_any_plan_buffer(op):
     plan.normals_pcg64(np.random.default_rng(9).bit_generator.state, 100_000)
     bad_bytes, bad_buffers = plan.check_guards()
     assert (bad_bytes, bad_buffers) == (0, 0)
+
+
+# ------------------------------------------- one-sync end of step (phase 1 end + emit)
+@pytest.mark.parametrize("which", ["config2", "paper1", "desk3", "blobs"])
+def test_one_sync_emit_matches_two_calls(op, which):
+    """adps_step_phase1_end_emit (emit launched before the host reads a count,
+    into arrays of adps_step_capacity rows) writes exactly the rows, index_map,
+    child_parent, insert offsets and report of phase1_end + phase2, advances the
+    Generator identically, and never writes past the first n_out rows."""
+    import torch
+    from paper_2605_06876_b200.types import AdpSplitConfig
+    plan = op.Plan("cuda:0")
+    if which.startswith("config"):
+        from paper_2605_06876_b200 import synth as S
+        wl = S.CONFIGS[which]
+        d = wl.build_device(plan)
+        g, extent, cams, gt = d["g"], d["ini"].extent, d["cams"], d["gt_img"]
+        ga, den = (torch.as_tensor(x, device="cuda") for x in d["stats"])
+        cfg = AdpSplitConfig(v_views=len(cams) // 2, n_max=wl.n_max)
+    else:
+        gg, extent = golden_io.scene(DATA, f"step__{which}__in")
+        g = PA.to_tensors(PA.oracle_gaussians_f32(gg))
+        cams = DATA[f"step__{which}__cams"]
+        gt = torch.as_tensor(PA.f32(DATA[f"step__{which}__gt"]), dtype=torch.float32, device="cuda")
+        ga = torch.as_tensor(DATA[f"step__{which}__grad_accum"], device="cuda")
+        den = torch.as_tensor(DATA[f"step__{which}__denom"], device="cuda")
+        cfg = golden_io.Cfg(META["step"][which]["cfg"])
+
+    def run(one_sync, bitgen=np.random.PCG64):
+        rng = np.random.Generator(bitgen(11))
+        res = op.densify_step(g, extent, cams, gt, ga, den, cfg, rng, plan=plan, one_sync=one_sync)
+        out = dict(res.gaussians.numpy())
+        out.update({k: v.cpu().numpy() for k, v in res.report_arrays.items()})
+        out.update(index_map=res.index_map.cpu().numpy(), child_parent=res.child_parent.cpu().numpy(),
+                   insert_offset=res.insert_offset.cpu().numpy(), rng_after=rng.standard_normal(4))
+        return res, out
+
+    r2, d2 = run(False)
+    r1, d1 = run(True)
+    assert r1.counts == r2.counts
+    for k in d2:
+        np.testing.assert_array_equal(d1[k], d2[k], err_msg=k)
+    # the one-sync outputs are prefixes of bound-sized arrays; rows past n_out untouched by design
+    n_out = r1.counts["n_out"]
+    assert r1.gaussians.n == n_out and r1.gaussians.mu.untyped_storage().nbytes() >= 12 * n_out
+    # a bit generator the device cannot reproduce takes the two-call path, same rows
+    if r2.counts["n_fallback"]:
+        r3, d3 = run(True, np.random.MT19937)
+        r4, d4 = run(False, np.random.MT19937)
+        for k in d4:
+            np.testing.assert_array_equal(d3[k], d4[k], err_msg=k)
+
+
+def test_one_sync_capacity_too_small_rejected(op, plan):
+    """Arrays below adps_step_capacity's bounds are refused before any launch."""
+    import torch
+    tag = "blobs"
+    gg, extent = golden_io.scene(DATA, f"step__{tag}__in")
+    g = PA.to_tensors(PA.oracle_gaussians_f32(gg))
+    cams = DATA[f"step__{tag}__cams"]
+    m = META["step"][tag]
+    cfg = golden_io.Cfg(m["cfg"])
+    views = list(range(min(int(cfg.v_views), len(cams))))
+    img, dom = plan.render(g, cams[views])
+    gt = torch.as_tensor(PA.f32(DATA[f"step__{tag}__gt"]), dtype=torch.float32, device="cuda")[views].contiguous()
+    c = plan.phase1_begin(g, extent, torch.as_tensor(DATA[f"step__{tag}__grad_accum"], device="cuda"),
+                          torch.as_tensor(DATA[f"step__{tag}__denom"], device="cuda"), cfg, cams[views], img, gt, dom)
+    oc, ac = plan.capacity()
+    assert oc >= g.n - c["n_split"] and ac >= c["n_clone"]
+    out = op.GaussianTensors.empty(max(oc - 1, 1), g.sh_k, "cuda")
+    im = torch.empty(max(oc - 1, 1), dtype=torch.int64, device="cuda")
+    cp = torch.empty(ac, dtype=torch.int32, device="cuda")
+    io = torch.empty(c["n_split"], dtype=torch.int64, device="cuda")
+    normals = torch.zeros(max(6 * c["n_fallback"], 1), dtype=torch.float64, device="cuda")
+    with pytest.raises(ValueError, match="capacity"):
+        plan.phase1_end_emit(g, normals, out, im, cp, io)

@@ -44,14 +44,15 @@ def wrap(obj, name):
     setattr(obj, name, w)
 
 
-for n in ("phase1_begin", "phase1_end", "phase2", "report_arrays", "normals_pcg64"):
+for n in ("phase1_begin", "phase1_end", "phase2", "report_arrays", "normals_pcg64", "capacity", "phase1_end_emit"):
     if hasattr(plan, n):
         wrap(plan, n)
 
 
 def step():
     return op.densify_step(g, ini.extent, cams, gt_img, ga_t, den_t, cfg, np.random.default_rng(0),
-                           renders=(img, dom), plan=plan, view_ids=list(range(len(cams))))
+                           renders=(img, dom), plan=plan, view_ids=list(range(len(cams))),
+                           one_sync=os.environ.get("ADPS_TWO_CALL", "0") != "1")
 
 
 for _ in range(3):
