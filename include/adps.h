@@ -338,6 +338,11 @@ ADPS_API adps_status adps_step_phase1_finish(adps_plan* plan, void* stream, int6
 #define ADPS_PARAM_PIPELINE_CHUNKS 10      /* view chunks of the attribution pipeline (input pass of chunk
                                               c+1 beside the CCL of chunk c; default 1) */
 #define ADPS_PARAM_INPUT_BLOCKS_PER_SM 11  /* resident blocks per SM of the input pass (0 = all that fit) */
+#define ADPS_PARAM_RENDER_BINNING 12       /* adps_render's depth order: 1 (default) a 32-bit key sort plus a
+                                              fix-up of equal keys, no host sync between views; 0 the 64-bit
+                                              sort of the fp64 depths, a sync per view (same images) */
+#define ADPS_PARAM_RENDER_PAIR_CAP 13      /* (tile, splat) pairs the fast path's tile sort covers (learned
+                                              at the plan's first render; grown when a view exceeds it) */
 ADPS_API adps_status adps_set_param(adps_plan* plan, int32_t key, int64_t value);
 ADPS_API adps_status adps_get_param(adps_plan* plan, int32_t key, int64_t* value);
 

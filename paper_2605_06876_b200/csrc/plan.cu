@@ -118,7 +118,11 @@ struct adps_plan {
   long long region_cap = 0, partial_cap = 0, region_hint = 0, partial_hint = 0;
   // render scratch
   Buf r_key, r_key_sorted, r_order_in, r_order, r_tiles, r_rect, r_splat, r_offs, r_dup, r_dup_sorted,
-      r_tstart, r_tend, r_total, r_cams, r_tile_lohi;
+      r_tstart, r_tend, r_total, r_cams, r_tile_lohi, r_k32, r_k32_sorted, r_vflag, r_vtotal;
+  int render_fast = 1;               // ADPS_PARAM_RENDER_BINNING: 1 = 32-bit depth keys, no per-view sync
+  long long dup_cap = 0;             // (tile, splat) pairs the tile sort covers (0: learn at the next render)
+  std::vector<int> vflag_host;
+  std::vector<unsigned long long> vtotal_host;
   unsigned long long* r_total_host = nullptr;
   // last phase-1 state
   bool have_phase1 = false;
@@ -307,6 +311,7 @@ static int plan_buffers(adps_plan* P, Buf** out) {
                  &P->scan2_val, &P->scan2_flag, &P->scan2_ticket, &P->cub_tmp, &P->ctr, &P->r_key,
                  &P->r_key_sorted, &P->r_order_in, &P->r_order, &P->r_tiles, &P->r_rect, &P->r_splat,
                  &P->r_offs, &P->r_dup, &P->r_dup_sorted, &P->r_tstart, &P->r_tend, &P->r_total, &P->r_tile_lohi,
+                 &P->r_k32, &P->r_k32_sorted, &P->r_vflag, &P->r_vtotal,
                  &P->r_cams, &P->small_list, &P->pstart, &P->n_groups, &P->work_cnt, &P->work_off,
                  &P->props_s, &P->psrc, &P->pcand, &P->gkey, &P->gval, &P->gkey_sorted, &P->gval_sorted, &P->grp_first,
                  &P->gpar, &P->gext, &P->gfirst_of, &P->glist, &P->scan3_val, &P->scan3_flag, &P->scan3_ticket,
@@ -473,8 +478,8 @@ static adps_status render_impl(adps_plan* P, void* stream_v, const adps_gaussian
     CK(cudaStreamSynchronize(s));
     return ADPS_OK;
   }
+  if (W > 32767 || H > 32767) return fail(ADPS_INVALID_ARG, "image side above 32767");
   CK(ensure(P->r_key, sizeof(unsigned long long) * n));
-  CK(ensure(P->r_key_sorted, sizeof(unsigned long long) * n));
   CK(ensure(P->r_order_in, sizeof(int) * n));
   CK(ensure(P->r_order, sizeof(int) * n));
   CK(ensure(P->r_tiles, sizeof(unsigned) * n));
@@ -484,16 +489,14 @@ static adps_status render_impl(adps_plan* P, void* stream_v, const adps_gaussian
   CK(ensure(P->r_tstart, sizeof(int) * n_tiles));
   CK(ensure(P->r_tend, sizeof(int) * n_tiles));
   CK(ensure(P->r_total, 2 * sizeof(unsigned long long)));
+  CK(ensure(P->r_vflag, sizeof(int) * (n_views + 1)));
+  CK(ensure(P->r_vtotal, sizeof(unsigned long long) * (n_views + 1)));
+  // tile ids below 2^tile_bits - 1: the padding keys (all ones) sort after every real key
+  const int tile_bits = ceil_log2((unsigned long long)n_tiles + 1);
   ScanState sst;
   st = scan_state(P, P->scan_val, P->scan_flag, P->scan_ticket, n, &sst);
   if (st != ADPS_OK) return st;
-  size_t tmp1 = 0;
-  CK(cub::DeviceRadixSort::SortPairs(nullptr, tmp1, P->r_key.as<unsigned long long>(),
-                                     P->r_key_sorted.as<unsigned long long>(), P->r_order_in.as<int>(),
-                                     P->r_order.as<int>(), (int)n, 0, 64, s));
-  CK(ensure(P->cub_tmp, tmp1));
-  const int tile_bits = ceil_log2((unsigned long long)n_tiles) > 0 ? ceil_log2((unsigned long long)n_tiles) : 1;
-  for (int v = 0; v < n_views; ++v) {
+  auto preprocess = [&](int v, bool k32) -> adps_status {
     PreArgs pa;
     pa.mu = g->mu;
     pa.scale = g->scale;
@@ -511,44 +514,16 @@ static adps_status render_impl(adps_plan* P, void* stream_v, const adps_gaussian
     pa.tiles = P->r_tiles.as<unsigned>();
     pa.rect = P->r_rect.as<unsigned short>();
     pa.splat = P->r_splat.as<SplatData>();
+    pa.depth32 = k32 ? P->r_k32.as<unsigned>() : nullptr;
+    pa.tiles_x = tiles_x;
     CK(launch_preprocess(pa, s));
-    size_t tb = P->cub_tmp.bytes;
-    CK(cub::DeviceRadixSort::SortPairs(P->cub_tmp.p, tb, P->r_key.as<unsigned long long>(),
-                                       P->r_key_sorted.as<unsigned long long>(), P->r_order_in.as<int>(),
-                                       P->r_order.as<int>(), (int)n, 0, 64, s));
-    CK(launch_tile_count_scan(P->r_order.as<int>(), P->r_tiles.as<unsigned>(), P->r_offs.as<unsigned>(),
-                              P->r_total.as<unsigned long long>(), n, sst, s));
-    CK(cudaMemcpyAsync(P->r_total_host, P->r_total.p, sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
-    CK(cudaStreamSynchronize(s));
-    const long long n_dup = (long long)*P->r_total_host;
-    if (n_dup > 0x7fffffffLL) return fail(ADPS_INVALID_ARG, "tile list too long (%lld)", n_dup);
-    CK(ensure(P->r_dup, sizeof(unsigned long long) * (n_dup > 0 ? n_dup : 1)));
-    CK(ensure(P->r_dup_sorted, sizeof(unsigned long long) * (n_dup > 0 ? n_dup : 1)));
-    CK(cudaMemsetAsync(P->r_tstart.p, 0, sizeof(int) * n_tiles, s));
-    CK(cudaMemsetAsync(P->r_tend.p, 0, sizeof(int) * n_tiles, s));
-    if (n_dup > 0) {
-      DupArgs da;
-      da.order = P->r_order.as<int>();
-      da.tiles = P->r_tiles.as<unsigned>();
-      da.rect = P->r_rect.as<unsigned short>();
-      da.offs = P->r_offs.as<unsigned>();
-      da.n = n;
-      da.tiles_x = tiles_x;
-      da.keys = P->r_dup.as<unsigned long long>();
-      CK(launch_duplicate(da, s));
-      size_t tmp2 = 0;
-      CK(cub::DeviceRadixSort::SortKeys(nullptr, tmp2, P->r_dup.as<unsigned long long>(),
-                                        P->r_dup_sorted.as<unsigned long long>(), (int)n_dup, 32, 32 + tile_bits, s));
-      CK(ensure(P->cub_tmp, tmp2 > tmp1 ? tmp2 : tmp1));
-      tb = P->cub_tmp.bytes;
-      CK(cub::DeviceRadixSort::SortKeys(P->cub_tmp.p, tb, P->r_dup.as<unsigned long long>(),
-                                        P->r_dup_sorted.as<unsigned long long>(), (int)n_dup, 32, 32 + tile_bits, s));
-      CK(launch_tile_ranges(P->r_dup_sorted.as<unsigned long long>(), n_dup, P->r_tstart.as<int>(),
-                            P->r_tend.as<int>(), s));
-    }
+    return ADPS_OK;
+  };
+  auto blend = [&](int v, const int* vflag) -> adps_status {
     BlendArgs ba;
     ba.keys = P->r_dup_sorted.as<unsigned long long>();
     ba.order = P->r_order.as<int>();
+    ba.vflag = vflag;
     ba.splat = P->r_splat.as<SplatData>();
     ba.tile_start = P->r_tstart.as<int>();
     ba.tile_end = P->r_tend.as<int>();
@@ -571,9 +546,159 @@ static adps_status render_impl(adps_plan* P, void* stream_v, const adps_gaussian
       ba.cand_bits = P->cand_bits.as<unsigned>() + (long long)v * ((hw + 31) / 32);
     }
     CK(launch_blend(ba, n_tiles, s));
-    P->launches += n_dup > 0 ? 5 : 3;
-    P->lib_calls += n_dup > 0 ? 2 : 1;
+    return ADPS_OK;
+  };
+  auto sort_temp = [&](long long dup_items) -> adps_status {
+    size_t t1 = 0, t2 = 0, t3 = 0;
+    CK(cub::DeviceRadixSort::SortPairs(nullptr, t1, P->r_key.as<unsigned long long>(),
+                                       P->r_key_sorted.as<unsigned long long>(), P->r_order_in.as<int>(),
+                                       P->r_order.as<int>(), (int)n, 0, 64, s));
+    CK(cub::DeviceRadixSort::SortPairs(nullptr, t2, P->r_k32.as<unsigned>(), P->r_k32_sorted.as<unsigned>(),
+                                       P->r_order_in.as<int>(), P->r_order.as<int>(), (int)n, 0, 32, s));
+    if (dup_items > 0)
+      CK(cub::DeviceRadixSort::SortKeys(nullptr, t3, P->r_dup.as<unsigned long long>(),
+                                        P->r_dup_sorted.as<unsigned long long>(), (int)dup_items, 32,
+                                        32 + tile_bits, s));
+    CK(ensure(P->cub_tmp, std::max(t1, std::max(t2, t3))));
+    return ADPS_OK;
+  };
+  auto tile_sort = [&](long long items) -> adps_status {
+    size_t tb = P->cub_tmp.bytes;
+    CK(cub::DeviceRadixSort::SortKeys(P->cub_tmp.p, tb, P->r_dup.as<unsigned long long>(),
+                                      P->r_dup_sorted.as<unsigned long long>(), (int)items, 32, 32 + tile_bits, s));
+    return ADPS_OK;
+  };
+  // one view through the 64-bit depth sort, with a host synchronisation for
+  // the pair count (ADPS_PARAM_RENDER_BINNING 0, and the views the fast path
+  // hands back: a depth run too long for its fix-up)
+  auto render_sorted64 = [&](int v) -> adps_status {
+    CK(ensure(P->r_key_sorted, sizeof(unsigned long long) * n));
+    adps_status e = preprocess(v, false);
+    if (e != ADPS_OK) return e;
+    e = sort_temp(0);
+    if (e != ADPS_OK) return e;
+    size_t tb = P->cub_tmp.bytes;
+    CK(cub::DeviceRadixSort::SortPairs(P->cub_tmp.p, tb, P->r_key.as<unsigned long long>(),
+                                       P->r_key_sorted.as<unsigned long long>(), P->r_order_in.as<int>(),
+                                       P->r_order.as<int>(), (int)n, 0, 64, s));
+    unsigned long long* tot = P->r_vtotal.as<unsigned long long>() + n_views;   // scratch slot
+    int* flag = P->r_vflag.as<int>() + n_views;
+    CK(launch_tile_count_scan(P->r_order.as<int>(), P->r_tiles.as<unsigned>(), P->r_offs.as<unsigned>(), tot, n,
+                              sst, s));
+    CK(cudaMemsetAsync(flag, 0, sizeof(int), s));
+    CK(cudaMemcpyAsync(P->r_total_host, tot, sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    const long long n_dup = (long long)*P->r_total_host;
+    if (n_dup > 0x7fffffffLL) return fail(ADPS_INVALID_ARG, "tile list too long (%lld)", n_dup);
+    const long long items = n_dup > 0 ? n_dup : 1;
+    CK(ensure(P->r_dup, sizeof(unsigned long long) * items));
+    CK(ensure(P->r_dup_sorted, sizeof(unsigned long long) * items));
+    e = sort_temp(items);
+    if (e != ADPS_OK) return e;
+    CK(cudaMemsetAsync(P->r_tstart.p, 0, sizeof(int) * n_tiles, s));
+    CK(cudaMemsetAsync(P->r_tend.p, 0, sizeof(int) * n_tiles, s));
+    DupArgs da{P->r_order.as<int>(), P->r_tiles.as<unsigned>(), P->r_rect.as<unsigned short>(),
+               P->r_offs.as<unsigned>(), n, tiles_x, P->r_dup.as<unsigned long long>(), items, tot, flag};
+    CK(launch_duplicate(da, s));
+    e = tile_sort(items);
+    if (e != ADPS_OK) return e;
+    CK(launch_tile_ranges(P->r_dup_sorted.as<unsigned long long>(), items, tot, flag, P->r_tstart.as<int>(),
+                          P->r_tend.as<int>(), s));
+    e = blend(v, nullptr);
+    if (e != ADPS_OK) return e;
+    P->launches += 5;
+    P->lib_calls += 2;
+    return ADPS_OK;
+  };
+  if (!P->render_fast) {
+    for (int v = 0; v < n_views; ++v) {
+      st = render_sorted64(v);
+      if (st != ADPS_OK) return st;
+    }
+    return ADPS_OK;
   }
+  // ---- fast path: no host synchronisation between views.  The tile sort
+  //      covers dup_cap pairs (padding keys past the view's own); a view with
+  //      more pairs, or a depth run too long for the fix-up, is flagged,
+  //      skipped, and rendered again after the call's one synchronisation.
+  CK(ensure(P->r_k32, sizeof(unsigned) * n));
+  CK(ensure(P->r_k32_sorted, sizeof(unsigned) * n));
+  CK(cudaMemsetAsync(P->r_vflag.p, 0, sizeof(int) * (n_views + 1), s));
+  auto render_fast = [&](int v, bool learn) -> adps_status {
+    int* flag = P->r_vflag.as<int>() + v;
+    unsigned long long* tot = P->r_vtotal.as<unsigned long long>() + v;
+    adps_status e = preprocess(v, true);
+    if (e != ADPS_OK) return e;
+    e = sort_temp(P->dup_cap);
+    if (e != ADPS_OK) return e;
+    size_t tb = P->cub_tmp.bytes;
+    CK(cub::DeviceRadixSort::SortPairs(P->cub_tmp.p, tb, P->r_k32.as<unsigned>(), P->r_k32_sorted.as<unsigned>(),
+                                       P->r_order_in.as<int>(), P->r_order.as<int>(), (int)n, 0, 32, s));
+    CK(launch_depth_fixup(P->r_k32_sorted.as<unsigned>(), P->r_order.as<int>(), P->r_key.as<unsigned long long>(),
+                          n, flag, s));
+    CK(launch_tile_count_scan(P->r_order.as<int>(), P->r_tiles.as<unsigned>(), P->r_offs.as<unsigned>(), tot, n,
+                              sst, s));
+    if (learn) {   // the first view of a plan: learn the pair count once
+      CK(cudaMemcpyAsync(P->r_total_host, tot, sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
+      CK(cudaStreamSynchronize(s));
+      const long long want = (long long)*P->r_total_host;
+      P->dup_cap = std::min(want + want / 8 + 1024, 0x7fffffffLL);
+      e = sort_temp(P->dup_cap);
+      if (e != ADPS_OK) return e;
+    }
+    CK(ensure(P->r_dup, sizeof(unsigned long long) * P->dup_cap));
+    CK(ensure(P->r_dup_sorted, sizeof(unsigned long long) * P->dup_cap));
+    CK(cudaMemsetAsync(P->r_tstart.p, 0, sizeof(int) * n_tiles, s));
+    CK(cudaMemsetAsync(P->r_tend.p, 0, sizeof(int) * n_tiles, s));
+    DupArgs da{P->r_order.as<int>(), P->r_tiles.as<unsigned>(), P->r_rect.as<unsigned short>(),
+               P->r_offs.as<unsigned>(), n, tiles_x, P->r_dup.as<unsigned long long>(), P->dup_cap, tot, flag};
+    CK(launch_duplicate(da, s));
+    e = tile_sort(P->dup_cap);
+    if (e != ADPS_OK) return e;
+    CK(launch_tile_ranges(P->r_dup_sorted.as<unsigned long long>(), P->dup_cap, tot, flag, P->r_tstart.as<int>(),
+                          P->r_tend.as<int>(), s));
+    e = blend(v, flag);
+    if (e != ADPS_OK) return e;
+    P->launches += 6;
+    P->lib_calls += 2;
+    return ADPS_OK;
+  };
+  for (int v = 0; v < n_views; ++v) {
+    st = render_fast(v, v == 0 && P->dup_cap <= 0);
+    if (st != ADPS_OK) return st;
+  }
+  P->vflag_host.resize(n_views);
+  P->vtotal_host.resize(n_views);
+  CK(cudaMemcpyAsync(P->vflag_host.data(), P->r_vflag.p, sizeof(int) * n_views, cudaMemcpyDeviceToHost, s));
+  CK(cudaMemcpyAsync(P->vtotal_host.data(), P->r_vtotal.p, sizeof(unsigned long long) * n_views,
+                     cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  long long need = 0, most = 0;
+  for (int v = 0; v < n_views; ++v) {
+    most = std::max(most, (long long)P->vtotal_host[v]);
+    if (P->vflag_host[v] == 1) need = std::max(need, (long long)P->vtotal_host[v]);
+  }
+  if (need > 0x7fffffffLL) return fail(ADPS_INVALID_ARG, "tile lists too long (%lld pairs)", need);
+  if (need > 0) {   // more pairs than the sort covered: redo those views with room for them
+    P->dup_cap = std::min(need + need / 8 + 1024, 0x7fffffffLL);
+    for (int v = 0; v < n_views; ++v)
+      if (P->vflag_host[v] == 1) {
+        CK(cudaMemsetAsync(P->r_vflag.as<int>() + v, 0, sizeof(int), s));
+        st = render_fast(v, false);
+        if (st != ADPS_OK) return st;
+      }
+    CK(cudaMemcpyAsync(P->vflag_host.data(), P->r_vflag.p, sizeof(int) * n_views, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    for (int v = 0; v < n_views; ++v)
+      if (P->vflag_host[v] == 1) return fail(ADPS_BAD_STATE, "tile pairs still exceed the grown capacity");
+  } else if (most > 0 && P->dup_cap > 2 * most + 4096) {
+    P->dup_cap = most + most / 8 + 1024;   // shrink a stale capacity (the padding is sorted too)
+  }
+  for (int v = 0; v < n_views; ++v)
+    if (P->vflag_host[v] == 2) {   // a run of equal 32-bit depth keys too long for the fix-up
+      st = render_sorted64(v);
+      if (st != ADPS_OK) return st;
+    }
   return ADPS_OK;
 }
 
@@ -1895,6 +2020,17 @@ extern "C" adps_status adps_set_param(adps_plan* P, int32_t key, int64_t value) 
     P->input_blocks_per_sm = (int)value;
     return ADPS_OK;
   }
+  if (key == ADPS_PARAM_RENDER_PAIR_CAP) {
+    if (value < 1 || value > 0x7fffffffLL) return fail(ADPS_INVALID_ARG, "pair capacity must be in [1, 2^31)");
+    P->dup_cap = value;   // (grown again by the first render that overflows it)
+    return ADPS_OK;
+  }
+  if (key == ADPS_PARAM_RENDER_BINNING) {
+    if (value < 0 || value > 1)
+      return fail(ADPS_INVALID_ARG, "render binning must be 0 (64-bit depth sort) or 1 (32-bit keys + fix-up)");
+    P->render_fast = (int)value;
+    return ADPS_OK;
+  }
   if (key == ADPS_PARAM_RAW_CACHE) {
     if (value < 0 || value > 1) return fail(ADPS_INVALID_ARG, "raw cache must be 0 or 1");
     P->raw_cache = (int)value;
@@ -1916,6 +2052,8 @@ extern "C" adps_status adps_get_param(adps_plan* P, int32_t key, int64_t* value)
     case ADPS_PARAM_LARGE_THRESHOLD: *value = P->large_threshold; return ADPS_OK;
     case ADPS_PARAM_TILE_PATH: *value = P->tile_path; return ADPS_OK;
     case ADPS_PARAM_RAW_CACHE: *value = P->raw_cache; return ADPS_OK;
+    case ADPS_PARAM_RENDER_BINNING: *value = P->render_fast; return ADPS_OK;
+    case ADPS_PARAM_RENDER_PAIR_CAP: *value = P->dup_cap; return ADPS_OK;
     case ADPS_PARAM_PIPELINE_CHUNKS: *value = P->pipeline_chunks; return ADPS_OK;
     case ADPS_PARAM_INPUT_BLOCKS_PER_SM: *value = P->input_blocks_per_sm; return ADPS_OK;
     case ADPS_PARAM_STAT_TILE_PAIRS: *value = P->ctr_host ? (int64_t)P->ctr_host->n_tile_pairs : 0; return ADPS_OK;

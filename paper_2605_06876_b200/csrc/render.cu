@@ -3,9 +3,11 @@
 // Replaces raster.render (ref/raster.py:136-157) with visible_splats,
 // project and _support_radius (ref/raster.py:61-117):
 //   * per-Gaussian projection in fp64 (cull rules of ref/raster.py:104-113)
-//   * exact (camera z, index) order: a stable radix sort of the fp64 depth
-//     bits gives each splat its depth rank; tile lists are then a stable sort
-//     on the tile id only, so every tile list is in reference order
+//   * exact (camera z, index) order: a stable radix sort of monotone 32-bit
+//     depth keys (the float below z), then runs of equal keys put in (z, index)
+//     order, gives each splat its depth rank; tile lists are then a stable sort
+//     on the tile id only, so every tile list is in reference order (the
+//     64-bit sort of the fp64 depth bits remains as ADPS_PARAM_RENDER_BINNING 0)
 //   * 16x16 tiles, shared-memory splat batches, fp32 per-pixel alpha with
 //     tile-local offsets computed in fp64 (no large-coordinate cancellation)
 //   * front-to-back composite and strict argmax of T*alpha (front-most wins)
@@ -13,6 +15,7 @@
 //     argmax can no longer change (T*0.99 <= best) AND the remaining image
 //     contribution is below 1e-8 (below fp32 resolution of the composite).
 #include <math.h>
+
 
 #include "render.cuh"
 
@@ -56,8 +59,9 @@ __device__ __forceinline__ void sh_eval_rgb(const float* dc, const float* rest, 
 }
 
 __global__ void preprocess_kernel(PreArgs a) {
-  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= a.n) return;
+  const long long i0 = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const bool in_range = i0 < a.n;
+  const long long i = in_range ? i0 : a.n - 1;   // out-of-range lanes recompute the last one, write nothing
   const CamD& cam = a.cam;
   const double mu[3] = {a.mu[3 * i], a.mu[3 * i + 1], a.mu[3 * i + 2]};
   const double dl[3] = {mu[0] - cam.c[0], mu[1] - cam.c[1], mu[2] - cam.c[2]};
@@ -68,6 +72,7 @@ __global__ void preprocess_kernel(PreArgs a) {
   unsigned long long key = ~0ull;
   unsigned tiles = 0;
   unsigned short rect[4] = {0, 0, 0, 0};
+  short bx0 = 0, bx1 = -1, by0 = 0, by1 = -1;
   if (z > 1e-8) {
     const double mx = cam.fx * x / z + cam.px, my = cam.fy * y / z + cam.py;
     // cov2d = J W Sigma W^T J^T + 0.3 I
@@ -102,14 +107,21 @@ __global__ void preprocess_kernel(PreArgs a) {
       const double r = sqrt(2.0 * log(oc / kAlphaMinD) * lam);
       const bool inside = !(mx + r < 0 || mx - r > a.W - 1 || my + r < 0 || my - r > a.H - 1);
       if (r > 0.0 && inside) {
-        // binning radius: true opacity (may exceed the cap) plus a guard
-        const double rb = sqrt(2.0 * log(o / kAlphaMinD) * lam) * (1.0 + 1e-5) + 0.02;
-        int x0 = (int)ceil(mx - rb), x1 = (int)floor(mx + rb);
-        int y0 = (int)ceil(my - rb), y1 = (int)floor(my + rb);
+        // binning box: the alpha >= 1/255 ellipse at the true opacity (which may
+        // exceed the cap) reaches |dx| <= sqrt(k cov_xx), |dy| <= sqrt(k cov_yy),
+        // k = 2 ln(o / alpha_min); plus a guard for the fp32 evaluation
+        const double kq = 2.0 * log(o / kAlphaMinD);
+        const double hx = sqrt(kq * ca) * (1.0 + 1e-5) + 0.02, hy = sqrt(kq * cc) * (1.0 + 1e-5) + 0.02;
+        int x0 = (int)ceil(mx - hx), x1 = (int)floor(mx + hx);
+        int y0 = (int)ceil(my - hy), y1 = (int)floor(my + hy);
         x0 = max(x0, 0);
         y0 = max(y0, 0);
         x1 = min(x1, a.W - 1);
         y1 = min(y1, a.H - 1);
+        bx0 = (short)x0;
+        bx1 = (short)x1;
+        by0 = (short)y0;
+        by1 = (short)y1;
         key = (unsigned long long)__double_as_longlong(z);
         if (x0 <= x1 && y0 <= y1) {
           rect[0] = (unsigned short)(x0 / kRTile);
@@ -130,14 +142,23 @@ __global__ void preprocess_kernel(PreArgs a) {
         const double nd = sqrt(dl[0] * dl[0] + dl[1] * dl[1] + dl[2] * dl[2]);
         const double dir[3] = {dl[0] / nd, dl[1] / nd, dl[2] / nd};
         sh_eval_rgb(a.sh_dc + 3 * i, a.sh_rest ? a.sh_rest + 3ll * a.sh_k * i : nullptr, a.sh_k, dir, sd.rgb);
-        a.splat[i] = sd;
+        sd.bx0 = bx0;
+        sd.bx1 = bx1;
+        sd.by0 = by0;
+        sd.by1 = by1;
+        if (in_range) a.splat[i] = sd;
       }
     }
   }
-  a.depth_key[i] = key;
-  a.order_in[i] = (int)i;
-  a.tiles[i] = tiles;
-  reinterpret_cast<ushort4*>(a.rect)[i] = make_ushort4(rect[0], rect[1], rect[2], rect[3]);
+  const ushort4 r4 = make_ushort4(rect[0], rect[1], rect[2], rect[3]);
+  if (in_range) {
+    a.depth_key[i] = key;
+    a.order_in[i] = (int)i;
+    a.tiles[i] = tiles;
+    reinterpret_cast<ushort4*>(a.rect)[i] = r4;
+  }
+  if (in_range && a.depth32)   // a monotone 32-bit depth key: the float below z (culled: last)
+    a.depth32[i] = key == ~0ull ? 0xffffffffu : __float_as_uint(__double2float_rd(z));
 }
 
 struct TileCountPolicy {
@@ -149,29 +170,6 @@ struct TileCountPolicy {
   __device__ void store(long long s, unsigned long long ex, unsigned long long) const { offs[s] = (unsigned)ex; }
   __device__ void total(unsigned long long t) const { *total_out = t; }
 };
-
-__global__ void duplicate_kernel(DupArgs a) {
-  const long long s = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (s >= a.n) return;
-  const int g = a.order[s];
-  const unsigned cnt = a.tiles[g];
-  if (!cnt) return;
-  const ushort4 r = reinterpret_cast<const ushort4*>(a.rect)[g];
-  unsigned long long off = a.offs[s];
-  for (int ty = r.y; ty <= r.w; ++ty)
-    for (int tx = r.x; tx <= r.z; ++tx) {
-      const unsigned long long t = (unsigned long long)(ty * a.tiles_x + tx);
-      a.keys[off++] = (t << 32) | (unsigned long long)s;
-    }
-}
-
-__global__ void tile_ranges_kernel(const unsigned long long* keys, long long n, int* start, int* end) {
-  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n) return;
-  const int t = (int)(keys[i] >> 32);
-  if (i == 0 || (int)(keys[i - 1] >> 32) != t) start[t] = (int)i;
-  if (i == n - 1 || (int)(keys[i + 1] >> 32) != t) end[t] = (int)(i + 1);
-}
 
 // The fused attribution epilogue (BlendArgs::gt set): the stored fp32 image
 // value i and gt give the raw L1 error exactly as the step's input pass
@@ -199,13 +197,14 @@ __device__ __forceinline__ void render_epilogue(const BlendArgs& a, bool inside,
       if (a.dom_flag[bi] == 0) a.dom_flag[bi] = 1;
     }
   }
-  // candidate bits: a warp holds two 16-pixel row segments of the tile (lanes
-  // 0-15 and 16-31); each segment's 16 bits land in one or two 32-bit words
-  static_assert(kRTile == 16 && kRThreads == 256, "epilogue: a warp = two 16-pixel tile rows");
+  // candidate bits: a warp holds four 8-pixel row segments of the tile (lanes
+  // 8r .. 8r + 7 = row r of its 8 x 4 block); each segment's 8 bits land in one
+  // or two 32-bit words
+  static_assert(kRTile == 16 && kRThreads == 256, "epilogue: a warp = an 8 x 4 pixel block");
   const unsigned b = __ballot_sync(0xffffffffu, cand);
-  if ((lane & 15) == 0 && y < a.H) {   // lanes 0 and 16: the first pixel of their segment (x may be >= W)
+  if ((lane & 7) == 0 && y < a.H) {   // the first pixel of its segment (x may be >= W)
     const long long p0 = (long long)y * a.W + x;
-    const unsigned seg = (b >> (lane & 16)) & 0xffffu;
+    const unsigned seg = (b >> (lane & 24)) & 0xffu;
     if (seg) {
       const unsigned long long w = (unsigned long long)seg << (p0 & 31);
       if ((unsigned)w) atomicOr(a.cand_bits + (p0 >> 5), (unsigned)w);
@@ -233,18 +232,33 @@ __device__ __forceinline__ void render_epilogue(const BlendArgs& a, bool inside,
   }
 }
 
+__device__ __forceinline__ float ex2_ftz(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
+// A block per 16 x 16 tile, a warp per 8 x 4 pixel block of it.  Splats come in
+// batches of 256 (shared memory); each carries the mask of the 8 pixel blocks
+// its alpha >= 1/255 box touches, so a warp walks only its own splats (ballot
+// over the masks, then the set bits) -- the box is exact up to a guard, so a
+// skipped (pixel, splat) pair has alpha below 1/255 and would be skipped anyway.
 template <bool STATS, bool EPI>
 __global__ void __launch_bounds__(kRThreads) blend_kernel(BlendArgs a) {
   struct Sm {
     float mx, my, A, B, C, o, r, g, b;
     int idx;
   };
+  constexpr unsigned FULL = 0xffffffffu;
   __shared__ Sm sm[kRThreads];
+  __shared__ unsigned char smask[kRThreads];
   __shared__ float wacc[STATS ? kRThreads : 1];
   unsigned long long n_contrib = 0;
   const int tile = blockIdx.x;
+  if (a.vflag && *a.vflag) return;   // the view's binning overflowed: the host renders it again
   const int tyi = tile / a.tiles_x, txi = tile % a.tiles_x;
-  const int lx = threadIdx.x % kRTile, ly = threadIdx.x / kRTile;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int lx = 8 * (wid & 1) + (lane & 7), ly = 4 * (wid >> 1) + (lane >> 3);
   const int x = txi * kRTile + lx, y = tyi * kRTile + ly;
   const bool inside = x < a.W && y < a.H;
   const double ox = (double)(txi * kRTile), oy = (double)(tyi * kRTile);
@@ -257,9 +271,9 @@ __global__ void __launch_bounds__(kRThreads) blend_kernel(BlendArgs a) {
     if (__syncthreads_count(done) == kRThreads) break;
     const int j = base + threadIdx.x;
     if (STATS) wacc[threadIdx.x] = 0.0f;
+    unsigned m = 0u;
     if (j < end) {
-      const int s = (int)(a.keys[j] & 0xffffffffull);
-      const int g = a.order[s];
+      const int g = a.order[(int)(a.keys[j] & 0xffffffffull)];
       const SplatData d = a.splat[g];
       Sm e;
       e.mx = (float)(d.mx - ox);
@@ -273,29 +287,48 @@ __global__ void __launch_bounds__(kRThreads) blend_kernel(BlendArgs a) {
       e.b = d.rgb[2];
       e.idx = g;
       sm[threadIdx.x] = e;
+      // pixel blocks of the support box: column halves x 4 row quarters
+      const int xl = (int)d.bx0 - txi * kRTile, xh = (int)d.bx1 - txi * kRTile;
+      const int yl = (int)d.by0 - tyi * kRTile, yh = (int)d.by1 - tyi * kRTile;
+      if (xh >= 0 && xl < kRTile && yh >= 0 && yl < kRTile) {
+        const unsigned cm = (xl < 8 ? 1u : 0u) | (xh >= 8 ? 2u : 0u);
+        const int r0 = max(yl, 0) >> 2, r1 = min(yh, kRTile - 1) >> 2;
+        for (int r = r0; r <= r1; ++r) m |= cm << (2 * r);
+      }
     }
+    smask[threadIdx.x] = (unsigned char)m;
     __syncthreads();
     const int cnt = min(kRThreads, end - base);
-    for (int k = 0; k < cnt && !done; ++k) {
-      const Sm& e = sm[k];
-      const float dx = fx - e.mx, dy = fy - e.my;
-      const float power = e.A * dx * dx + e.B * dx * dy + e.C * dy * dy;
-      const float alpha = fminf(kAlphaCap, e.o * __expf(power));
-      if (alpha < kAlphaMin) continue;
-      const float w = T * alpha;
-      if (STATS) {
-        if (a.weight) atomicAdd(&wacc[k], w);
-        ++n_contrib;
+    if (!__all_sync(FULL, done)) {
+      for (int c = 0; c < cnt; c += 32) {
+        unsigned bits = __ballot_sync(FULL, c + lane < cnt && ((smask[c + lane] >> wid) & 1u));
+        while (bits) {   // warp-uniform
+          const int k = c + __ffs(bits) - 1;
+          bits &= bits - 1u;
+          if (done) continue;
+          const Sm& e = sm[k];
+          const float dx = fx - e.mx, dy = fy - e.my;
+          const float power = e.A * dx * dx + e.B * dx * dy + e.C * dy * dy;
+          // __expf without its denormal path: results below 2^-126 give alpha < 1/255 either way
+          const float alpha = fminf(kAlphaCap, e.o * ex2_ftz(power * 1.4426950408889634f));
+          if (alpha < kAlphaMin) continue;
+          const float w = T * alpha;
+          if (STATS) {
+            if (a.weight) atomicAdd(&wacc[k], w);
+            ++n_contrib;
+          }
+          cr += w * e.r;
+          cg += w * e.g;
+          cbl += w * e.b;
+          if (w > best) {
+            best = w;
+            bi = e.idx;
+          }
+          T = T * (1.0f - alpha);
+          if (!STATS && T < 1e-8f && T * kAlphaCap <= best) done = true;
+        }
+        if (__all_sync(FULL, done)) break;
       }
-      cr += w * e.r;
-      cg += w * e.g;
-      cbl += w * e.b;
-      if (w > best) {
-        best = w;
-        bi = e.idx;
-      }
-      T = T * (1.0f - alpha);
-      if (!STATS && T < 1e-8f && T * kAlphaCap <= best) done = true;
     }
     __syncthreads();
     if (STATS && a.weight && threadIdx.x < cnt && wacc[threadIdx.x] > 0.0f)
@@ -317,6 +350,76 @@ __global__ void __launch_bounds__(kRThreads) blend_kernel(BlendArgs a) {
   if (EPI) render_epilogue(a, inside, y, x, i0, i1, i2, bi);
 }
 
+// ---------------------------------------------------------------- depth order
+// After the stable sort on the 32-bit keys, runs of equal keys (distinct
+// doubles inside one float, or equal depths) are in index order; each run
+// goes to (z, index) order here, the reference's order (ref/raster.py:118).
+// A run longer than kFixupMax flags the view (the 64-bit sort redoes it).
+constexpr int kFixupMax = 256;
+__global__ void depth_fixup_kernel(const unsigned* __restrict__ k32, int* __restrict__ order,
+                                   const unsigned long long* __restrict__ z64, long long n, int* flag) {
+  const long long s = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= n) return;
+  const unsigned k = k32[s];
+  if (k == 0xffffffffu) return;                  // culled: sorted last, never drawn
+  if (s > 0 && k32[s - 1] == k) return;           // not the head of its run
+  if (s + 1 >= n || k32[s + 1] != k) return;      // a run of one
+  long long e = s + 1;
+  while (e < n && k32[e] == k && e - s < kFixupMax) ++e;
+  if (e < n && k32[e] == k) {
+    atomicExch(flag, 2);
+    return;
+  }
+  for (long long i = s + 1; i < e; ++i) {         // insertion sort by (z bits, index)
+    const int gi = order[i];
+    const unsigned long long zi = z64[gi];
+    long long j = i - 1;
+    while (j >= s) {
+      const int gj = order[j];
+      const unsigned long long zj = z64[gj];
+      if (zj < zi || (zj == zi && gj < gi)) break;
+      order[j + 1] = gj;
+      --j;
+    }
+    order[j + 1] = gi;
+  }
+}
+
+// the (tile << 32 | depth rank) keys of every (tile, splat) pair, and padding
+// keys (sorted last) up to the capacity the host sorts; a view whose pairs
+// exceed the capacity is flagged and skipped (rendered again by the host)
+__global__ void duplicate_kernel(DupArgs a) {
+  const long long s = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const unsigned long long total = *a.total;
+  if (*a.flag) return;
+  if (total > (unsigned long long)a.cap) {
+    if (s == 0) *a.flag = 1;
+    return;
+  }
+  if (s >= (long long)total && s < a.cap) a.keys[s] = ~0ull;
+  if (s >= a.n) return;
+  const int g = a.order[s];
+  const unsigned cnt = a.tiles[g];
+  if (!cnt) return;
+  const ushort4 r = reinterpret_cast<const ushort4*>(a.rect)[g];
+  unsigned long long off = a.offs[s];
+  for (int ty = r.y; ty <= r.w; ++ty)
+    for (int tx = r.x; tx <= r.z; ++tx) {
+      const unsigned long long t = (unsigned long long)(ty * a.tiles_x + tx);
+      a.keys[off++] = (t << 32) | (unsigned long long)s;
+    }
+}
+
+__global__ void tile_ranges_kernel(const unsigned long long* keys, const unsigned long long* total, const int* flag,
+                                   int* start, int* end) {
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const long long n = (long long)*total;
+  if (i >= n || *flag) return;
+  const int t = (int)(keys[i] >> 32);
+  if (i == 0 || (int)(keys[i - 1] >> 32) != t) start[t] = (int)i;
+  if (i == n - 1 || (int)(keys[i + 1] >> 32) != t) end[t] = (int)(i + 1);
+}
+
 // ---------------------------------------------------------------- launchers
 cudaError_t launch_preprocess(const PreArgs& a, cudaStream_t s) {
   if (a.n > 0) preprocess_kernel<<<(unsigned)((a.n + 255) / 256), 256, 0, s>>>(a);
@@ -330,13 +433,20 @@ cudaError_t launch_tile_count_scan(const int* order, const unsigned* tiles, unsi
 }
 
 cudaError_t launch_duplicate(const DupArgs& a, cudaStream_t s) {
-  if (a.n > 0) duplicate_kernel<<<(unsigned)((a.n + 255) / 256), 256, 0, s>>>(a);
+  const long long m = a.n > a.cap ? a.n : a.cap;
+  if (m > 0) duplicate_kernel<<<(unsigned)((m + 255) / 256), 256, 0, s>>>(a);
   return cudaGetLastError();
 }
 
-cudaError_t launch_tile_ranges(const unsigned long long* keys, long long n, int* start, int* end,
+cudaError_t launch_tile_ranges(const unsigned long long* keys, long long cap, const unsigned long long* total,
+                               const int* flag, int* start, int* end, cudaStream_t s) {
+  if (cap > 0) tile_ranges_kernel<<<(unsigned)((cap + 255) / 256), 256, 0, s>>>(keys, total, flag, start, end);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_depth_fixup(const unsigned* k32, int* order, const unsigned long long* z64, long long n, int* flag,
                                cudaStream_t s) {
-  if (n > 0) tile_ranges_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(keys, n, start, end);
+  if (n > 0) depth_fixup_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(k32, order, z64, n, flag);
   return cudaGetLastError();
 }
 

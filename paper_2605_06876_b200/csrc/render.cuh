@@ -10,7 +10,7 @@ struct SplatData {
   float A, B, C;      // power = A dx^2 + B dx dy + C dy^2 = -0.5 * quad
   float o;
   float rgb[3];
-  float pad;
+  short bx0, bx1, by0, by1;   // pixel box of the alpha >= 1/255 support (clipped to the image)
 };
 
 struct PreArgs {
@@ -29,6 +29,8 @@ struct PreArgs {
   unsigned* tiles;
   unsigned short* rect;   // [n,4]
   SplatData* splat;
+  unsigned* depth32;      // [n] monotone 32-bit depth keys, or null
+  int tiles_x;
 };
 
 struct DupArgs {
@@ -38,12 +40,16 @@ struct DupArgs {
   const unsigned* offs;
   long long n;
   int tiles_x;
-  unsigned long long* keys;
+  unsigned long long* keys;               // [cap]
+  long long cap;
+  const unsigned long long* total;        // device: pairs of the view
+  int* flag;                              // device: the view's flag (1: over capacity, 2: depth run too long)
 };
 
 struct BlendArgs {
-  const unsigned long long* keys;
+  const unsigned long long* keys;   // sorted-key binning: keys -> order
   const int* order;
+  const int* vflag;                 // skip the view when its flag is set (the host renders it again)
   const SplatData* splat;
   const int* tile_start;
   const int* tile_end;
@@ -76,9 +82,12 @@ cudaError_t launch_preprocess(const PreArgs& a, cudaStream_t s);
 cudaError_t launch_tile_count_scan(const int* order, const unsigned* tiles, unsigned* offs,
                                    unsigned long long* total, long long n, ScanState st, cudaStream_t s);
 cudaError_t launch_duplicate(const DupArgs& a, cudaStream_t s);
-cudaError_t launch_tile_ranges(const unsigned long long* keys, long long n, int* start, int* end,
+cudaError_t launch_tile_ranges(const unsigned long long* keys, long long cap, const unsigned long long* total,
+                               const int* flag, int* start, int* end, cudaStream_t s);
+cudaError_t launch_depth_fixup(const unsigned* k32, int* order, const unsigned long long* z64, long long n, int* flag,
                                cudaStream_t s);
 cudaError_t launch_blend(const BlendArgs& a, int n_tiles, cudaStream_t s);
+
 // fused epilogue: per-view min/max from the per-tile slots
 cudaError_t launch_reduce_tile_minmax(const unsigned long long* tiles, int n_tiles, int n_views,
                                       unsigned long long* lohi, cudaStream_t s);

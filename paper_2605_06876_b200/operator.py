@@ -214,6 +214,13 @@ class Plan:
         """Minmax pass caches the fp64 raw L1 error for the warp CCL (default on)."""
         _abi.check(self.lib.adps_set_param(self._h, _abi.PARAM_RAW_CACHE, int(bool(on))))
 
+    def set_render_binning(self, fast: bool):
+        """Render depth order: 32-bit keys + fix-up, no per-view sync (default), or the 64-bit sort."""
+        _abi.check(self.lib.adps_set_param(self._h, _abi.PARAM_RENDER_BINNING, int(bool(fast))))
+
+    def set_param(self, key: int, value: int):
+        _abi.check(self.lib.adps_set_param(self._h, int(key), int(value)))
+
     def get_param(self, key: int) -> int:
         v = C.c_int64()
         _abi.check(self.lib.adps_get_param(self._h, int(key), C.byref(v)))
