@@ -118,7 +118,7 @@ struct adps_plan {
   long long region_cap = 0, partial_cap = 0, region_hint = 0, partial_hint = 0;
   // render scratch
   Buf r_key, r_key_sorted, r_order_in, r_order, r_tiles, r_rect, r_splat, r_offs, r_dup, r_dup_sorted,
-      r_tstart, r_tend, r_total, r_cams, r_tile_lohi, r_k32, r_k32_sorted, r_vflag, r_vtotal;
+      r_tstart, r_tend, r_total, r_cams, r_tile_lohi, r_k32, r_k32_sorted, r_vflag, r_vtotal, r_cov3, r_rgb0;
   int render_fast = 1;               // ADPS_PARAM_RENDER_BINNING: 1 = 32-bit depth keys, no per-view sync
   long long dup_cap = 0;             // (tile, splat) pairs the tile sort covers (0: learn at the next render)
   std::vector<int> vflag_host;
@@ -311,7 +311,7 @@ static int plan_buffers(adps_plan* P, Buf** out) {
                  &P->scan2_val, &P->scan2_flag, &P->scan2_ticket, &P->cub_tmp, &P->ctr, &P->r_key,
                  &P->r_key_sorted, &P->r_order_in, &P->r_order, &P->r_tiles, &P->r_rect, &P->r_splat,
                  &P->r_offs, &P->r_dup, &P->r_dup_sorted, &P->r_tstart, &P->r_tend, &P->r_total, &P->r_tile_lohi,
-                 &P->r_k32, &P->r_k32_sorted, &P->r_vflag, &P->r_vtotal,
+                 &P->r_k32, &P->r_k32_sorted, &P->r_vflag, &P->r_vtotal, &P->r_cov3, &P->r_rgb0,
                  &P->r_cams, &P->small_list, &P->pstart, &P->n_groups, &P->work_cnt, &P->work_off,
                  &P->props_s, &P->psrc, &P->pcand, &P->gkey, &P->gval, &P->gkey_sorted, &P->gval_sorted, &P->grp_first,
                  &P->gpar, &P->gext, &P->gfirst_of, &P->glist, &P->scan3_val, &P->scan3_flag, &P->scan3_ticket,
@@ -496,6 +496,18 @@ static adps_status render_impl(adps_plan* P, void* stream_v, const adps_gaussian
   ScanState sst;
   st = scan_state(P, P->scan_val, P->scan_flag, P->scan_ticket, n, &sst);
   if (st != ADPS_OK) return st;
+  // the view-independent covariances (and degree-0 colours), once per call
+  CK(ensure(P->r_cov3, sizeof(double) * 6 * n));
+  if (g->sh_rest_k == 0) CK(ensure(P->r_rgb0, sizeof(float) * 3 * n));
+  {
+    PreArgs pa{};
+    pa.rot = g->rot;
+    pa.scale = g->scale;
+    pa.sh_dc = g->sh_dc;
+    pa.n = n;
+    CK(launch_splat3d(pa, P->r_cov3.as<double>(), g->sh_rest_k == 0 ? P->r_rgb0.as<float>() : nullptr, s));
+    P->launches += 1;
+  }
   auto preprocess = [&](int v, bool k32) -> adps_status {
     PreArgs pa;
     pa.mu = g->mu;
@@ -516,6 +528,8 @@ static adps_status render_impl(adps_plan* P, void* stream_v, const adps_gaussian
     pa.splat = P->r_splat.as<SplatData>();
     pa.depth32 = k32 ? P->r_k32.as<unsigned>() : nullptr;
     pa.tiles_x = tiles_x;
+    pa.cov3 = P->r_cov3.as<double>();
+    pa.rgb0 = g->sh_rest_k == 0 ? P->r_rgb0.as<float>() : nullptr;
     CK(launch_preprocess(pa, s));
     return ADPS_OK;
   };
@@ -659,7 +673,7 @@ static adps_status render_impl(adps_plan* P, void* stream_v, const adps_gaussian
                           P->r_tend.as<int>(), s));
     e = blend(v, flag);
     if (e != ADPS_OK) return e;
-    P->launches += 6;
+    P->launches += 6;   // preprocess, fix-up, scan, duplication, ranges, blend
     P->lib_calls += 2;
     return ADPS_OK;
   };

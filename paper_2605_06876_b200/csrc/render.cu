@@ -58,6 +58,33 @@ __device__ __forceinline__ void sh_eval_rgb(const float* dc, const float* rest, 
   }
 }
 
+// the view-independent part of the projection, once per render call: the 3D
+// covariance R diag(s^2) R^T (fp64) and, at SH degree 0, the colour
+__global__ void splat3d_kernel(PreArgs a, double* __restrict__ cov3, float* __restrict__ rgb0) {
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= a.n) return;
+  double q[4] = {a.rot[4 * i], a.rot[4 * i + 1], a.rot[4 * i + 2], a.rot[4 * i + 3]};
+  double R[9];
+  quat_to_rot(q, R);
+  const double s2[3] = {(double)a.scale[3 * i] * a.scale[3 * i], (double)a.scale[3 * i + 1] * a.scale[3 * i + 1],
+                        (double)a.scale[3 * i + 2] * a.scale[3 * i + 2]};
+  double S[6];
+  rdrt(R, s2, S);
+#pragma unroll
+  for (int k = 0; k < 6; ++k) cov3[6 * i + k] = S[k];
+  if (rgb0) {
+    const double dir[3] = {0.0, 0.0, 1.0};   // unused at degree 0
+    float c[3];
+    sh_eval_rgb(a.sh_dc + 3 * i, nullptr, 0, dir, c);
+    for (int k = 0; k < 3; ++k) rgb0[3 * i + k] = c[k];
+  }
+}
+
+cudaError_t launch_splat3d(const PreArgs& a, double* cov3, float* rgb0, cudaStream_t s) {
+  if (a.n > 0) splat3d_kernel<<<(unsigned)((a.n + 255) / 256), 256, 0, s>>>(a, cov3, rgb0);
+  return cudaGetLastError();
+}
+
 __global__ void preprocess_kernel(PreArgs a) {
   const long long i0 = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   const bool in_range = i0 < a.n;
@@ -76,13 +103,18 @@ __global__ void preprocess_kernel(PreArgs a) {
   if (z > 1e-8) {
     const double mx = cam.fx * x / z + cam.px, my = cam.fy * y / z + cam.py;
     // cov2d = J W Sigma W^T J^T + 0.3 I
-    double q[4] = {a.rot[4 * i], a.rot[4 * i + 1], a.rot[4 * i + 2], a.rot[4 * i + 3]};
-    double R[9];
-    quat_to_rot(q, R);
-    const double s2[3] = {(double)a.scale[3 * i] * a.scale[3 * i], (double)a.scale[3 * i + 1] * a.scale[3 * i + 1],
-                          (double)a.scale[3 * i + 2] * a.scale[3 * i + 2]};
     double S[6];
-    rdrt(R, s2, S);
+    if (a.cov3) {   // view-independent, once per render call (splat3d_kernel)
+#pragma unroll
+      for (int k = 0; k < 6; ++k) S[k] = __ldg(a.cov3 + 6 * i + k);
+    } else {
+      double q[4] = {a.rot[4 * i], a.rot[4 * i + 1], a.rot[4 * i + 2], a.rot[4 * i + 3]};
+      double R[9];
+      quat_to_rot(q, R);
+      const double s2[3] = {(double)a.scale[3 * i] * a.scale[3 * i], (double)a.scale[3 * i + 1] * a.scale[3 * i + 1],
+                            (double)a.scale[3 * i + 2] * a.scale[3 * i + 2]};
+      rdrt(R, s2, S);
+    }
     const double Sm[9] = {S[0], S[1], S[2], S[1], S[3], S[4], S[2], S[4], S[5]};
     // T = J W (2x3), W = R_c2w^T
     const double j00 = cam.fx / z, j02 = -cam.fx * x / (z * z);
@@ -139,9 +171,13 @@ __global__ void preprocess_kernel(PreArgs a) {
         sd.B = (float)(-ib);
         sd.C = (float)(-0.5 * ic);
         sd.o = (float)o;
-        const double nd = sqrt(dl[0] * dl[0] + dl[1] * dl[1] + dl[2] * dl[2]);
-        const double dir[3] = {dl[0] / nd, dl[1] / nd, dl[2] / nd};
-        sh_eval_rgb(a.sh_dc + 3 * i, a.sh_rest ? a.sh_rest + 3ll * a.sh_k * i : nullptr, a.sh_k, dir, sd.rgb);
+        if (a.rgb0) {   // degree-0 colour: view-independent (splat3d_kernel)
+          for (int c = 0; c < 3; ++c) sd.rgb[c] = __ldg(a.rgb0 + 3 * i + c);
+        } else {
+          const double nd = sqrt(dl[0] * dl[0] + dl[1] * dl[1] + dl[2] * dl[2]);
+          const double dir[3] = {dl[0] / nd, dl[1] / nd, dl[2] / nd};
+          sh_eval_rgb(a.sh_dc + 3 * i, a.sh_rest ? a.sh_rest + 3ll * a.sh_k * i : nullptr, a.sh_k, dir, sd.rgb);
+        }
         sd.bx0 = bx0;
         sd.bx1 = bx1;
         sd.by0 = by0;
@@ -250,9 +286,11 @@ __global__ void __launch_bounds__(kRThreads) blend_kernel(BlendArgs a) {
     int idx;
   };
   constexpr unsigned FULL = 0xffffffffu;
-  __shared__ Sm sm[kRThreads];
-  __shared__ unsigned char smask[kRThreads];
-  __shared__ float wacc[STATS ? kRThreads : 1];
+  // two batch buffers: batch i + 1 is staged while batch i is walked, one
+  // barrier per batch
+  __shared__ Sm sm[2][kRThreads];
+  __shared__ unsigned char smask[2][kRThreads];
+  __shared__ float wacc[STATS ? 2 : 1][STATS ? kRThreads : 1];
   unsigned long long n_contrib = 0;
   const int tile = blockIdx.x;
   if (a.vflag && *a.vflag) return;   // the view's binning overflowed: the host renders it again
@@ -267,10 +305,9 @@ __global__ void __launch_bounds__(kRThreads) blend_kernel(BlendArgs a) {
   int bi = -1;
   bool done = !inside;
   const float fx = (float)lx, fy = (float)ly;
-  for (int base = beg; base < end; base += kRThreads) {
-    if (__syncthreads_count(done) == kRThreads) break;
+  auto stage = [&](int base, int buf) {   // this thread's splat of the batch at `base`
     const int j = base + threadIdx.x;
-    if (STATS) wacc[threadIdx.x] = 0.0f;
+    if (STATS) wacc[buf][threadIdx.x] = 0.0f;
     unsigned m = 0u;
     if (j < end) {
       const int g = a.order[(int)(a.keys[j] & 0xffffffffull)];
@@ -286,7 +323,7 @@ __global__ void __launch_bounds__(kRThreads) blend_kernel(BlendArgs a) {
       e.g = d.rgb[1];
       e.b = d.rgb[2];
       e.idx = g;
-      sm[threadIdx.x] = e;
+      sm[buf][threadIdx.x] = e;
       // pixel blocks of the support box: column halves x 4 row quarters
       const int xl = (int)d.bx0 - txi * kRTile, xh = (int)d.bx1 - txi * kRTile;
       const int yl = (int)d.by0 - tyi * kRTile, yh = (int)d.by1 - tyi * kRTile;
@@ -296,17 +333,28 @@ __global__ void __launch_bounds__(kRThreads) blend_kernel(BlendArgs a) {
         for (int r = r0; r <= r1; ++r) m |= cm << (2 * r);
       }
     }
-    smask[threadIdx.x] = (unsigned char)m;
-    __syncthreads();
+    smask[buf][threadIdx.x] = (unsigned char)m;
+  };
+  auto flush = [&](int base, int buf) {   // the batch's summed weights (statistics mode)
+    if (STATS && a.weight && base + (int)threadIdx.x < end && wacc[buf][threadIdx.x] > 0.0f)
+      atomicAdd(a.weight + sm[buf][threadIdx.x].idx, wacc[buf][threadIdx.x]);
+  };
+  if (beg < end) stage(beg, 0);
+  int buf = 0;
+  for (int base = beg; base < end; base += kRThreads, buf ^= 1) {
+    // the barrier publishes batch `base` and retires the walk of the one before
+    if (__syncthreads_count(done) == kRThreads) break;
+    if (STATS && base > beg) flush(base - kRThreads, buf ^ 1);
+    if (base + kRThreads < end) stage(base + kRThreads, buf ^ 1);
     const int cnt = min(kRThreads, end - base);
     if (!__all_sync(FULL, done)) {
       for (int c = 0; c < cnt; c += 32) {
-        unsigned bits = __ballot_sync(FULL, c + lane < cnt && ((smask[c + lane] >> wid) & 1u));
+        unsigned bits = __ballot_sync(FULL, c + lane < cnt && ((smask[buf][c + lane] >> wid) & 1u));
         while (bits) {   // warp-uniform
           const int k = c + __ffs(bits) - 1;
           bits &= bits - 1u;
           if (done) continue;
-          const Sm& e = sm[k];
+          const Sm& e = sm[buf][k];
           const float dx = fx - e.mx, dy = fy - e.my;
           const float power = e.A * dx * dx + e.B * dx * dy + e.C * dy * dy;
           // __expf without its denormal path: results below 2^-126 give alpha < 1/255 either way
@@ -314,7 +362,7 @@ __global__ void __launch_bounds__(kRThreads) blend_kernel(BlendArgs a) {
           if (alpha < kAlphaMin) continue;
           const float w = T * alpha;
           if (STATS) {
-            if (a.weight) atomicAdd(&wacc[k], w);
+            if (a.weight) atomicAdd(&wacc[buf][k], w);
             ++n_contrib;
           }
           cr += w * e.r;
@@ -330,9 +378,11 @@ __global__ void __launch_bounds__(kRThreads) blend_kernel(BlendArgs a) {
         if (__all_sync(FULL, done)) break;
       }
     }
+  }
+  if (STATS && beg < end) {   // the last walked batch (statistics mode never stops early)
     __syncthreads();
-    if (STATS && a.weight && threadIdx.x < cnt && wacc[threadIdx.x] > 0.0f)
-      atomicAdd(a.weight + sm[threadIdx.x].idx, wacc[threadIdx.x]);
+    const int last = beg + ((end - beg - 1) / kRThreads) * kRThreads;
+    flush(last, ((end - beg - 1) / kRThreads) & 1);
   }
   if (STATS && a.contrib) {
     for (int o = 16; o > 0; o >>= 1) n_contrib += __shfl_xor_sync(0xffffffffu, n_contrib, o);
@@ -388,26 +438,44 @@ __global__ void depth_fixup_kernel(const unsigned* __restrict__ k32, int* __rest
 // the (tile << 32 | depth rank) keys of every (tile, splat) pair, and padding
 // keys (sorted last) up to the capacity the host sorts; a view whose pairs
 // exceed the capacity is flagged and skipped (rendered again by the host)
-__global__ void duplicate_kernel(DupArgs a) {
+__global__ void __launch_bounds__(256) duplicate_kernel(DupArgs a) {
+  constexpr unsigned FULL = 0xffffffffu;
   const long long s = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   const unsigned long long total = *a.total;
-  if (*a.flag) return;
+  if (*a.flag) return;   // grid-uniform
   if (total > (unsigned long long)a.cap) {
     if (s == 0) *a.flag = 1;
     return;
   }
   if (s >= (long long)total && s < a.cap) a.keys[s] = ~0ull;
-  if (s >= a.n) return;
-  const int g = a.order[s];
-  const unsigned cnt = a.tiles[g];
-  if (!cnt) return;
-  const ushort4 r = reinterpret_cast<const ushort4*>(a.rect)[g];
-  unsigned long long off = a.offs[s];
-  for (int ty = r.y; ty <= r.w; ++ty)
-    for (int tx = r.x; tx <= r.z; ++tx) {
-      const unsigned long long t = (unsigned long long)(ty * a.tiles_x + tx);
-      a.keys[off++] = (t << 32) | (unsigned long long)s;
-    }
+  if (((long long)blockIdx.x * blockDim.x) >= a.n) return;   // block-uniform: no splats in this block
+  const bool in = s < a.n;
+  const int g = in ? a.order[s] : 0;
+  const unsigned cnt = in ? a.tiles[g] : 0u;
+  const ushort4 r = cnt ? reinterpret_cast<const ushort4*>(a.rect)[g] : make_ushort4(0, 0, 0, 0);
+  const unsigned long long off = cnt ? a.offs[s] : 0ull;
+  // small rects by their own thread; large ones (a background splat over the
+  // whole image) by the whole warp
+  const bool big = cnt > 16u;
+  if (cnt && !big) {
+    unsigned long long o = off;
+    for (int ty = r.y; ty <= r.w; ++ty)
+      for (int tx = r.x; tx <= r.z; ++tx) a.keys[o++] = ((unsigned long long)(ty * a.tiles_x + tx) << 32) | (unsigned long long)s;
+  }
+  unsigned bm = __ballot_sync(FULL, big);
+  const int lane = threadIdx.x & 31;
+  const unsigned r01 = (unsigned)r.x | ((unsigned)r.y << 16), r23 = (unsigned)r.z | ((unsigned)r.w << 16);
+  while (bm) {
+    const int src = __ffs(bm) - 1;
+    bm &= bm - 1u;
+    const unsigned p = __shfl_sync(FULL, r01, src), q = __shfl_sync(FULL, r23, src);
+    const unsigned long long o0 = __shfl_sync(FULL, off, src);
+    const long long ss = __shfl_sync(FULL, s, src);
+    const int x0 = (int)(p & 0xffffu), y0 = (int)(p >> 16), x1 = (int)(q & 0xffffu), y1 = (int)(q >> 16);
+    const int w = x1 - x0 + 1, tot = w * (y1 - y0 + 1);
+    for (int k = lane; k < tot; k += 32)
+      a.keys[o0 + k] = ((unsigned long long)((y0 + k / w) * a.tiles_x + x0 + k % w) << 32) | (unsigned long long)ss;
+  }
 }
 
 __global__ void tile_ranges_kernel(const unsigned long long* keys, const unsigned long long* total, const int* flag,

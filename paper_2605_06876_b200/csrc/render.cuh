@@ -31,6 +31,8 @@ struct PreArgs {
   SplatData* splat;
   unsigned* depth32;      // [n] monotone 32-bit depth keys, or null
   int tiles_x;
+  const double* cov3 = nullptr;   // [n,6] 3D covariances (splat3d_kernel), or null: computed per view
+  const float* rgb0 = nullptr;    // [n,3] degree-0 colours, or null
 };
 
 struct DupArgs {
@@ -79,6 +81,7 @@ struct BlendArgs {
 };
 
 cudaError_t launch_preprocess(const PreArgs& a, cudaStream_t s);
+cudaError_t launch_splat3d(const PreArgs& a, double* cov3, float* rgb0, cudaStream_t s);
 cudaError_t launch_tile_count_scan(const int* order, const unsigned* tiles, unsigned* offs,
                                    unsigned long long* total, long long n, ScanState st, cudaStream_t s);
 cudaError_t launch_duplicate(const DupArgs& a, cudaStream_t s);
