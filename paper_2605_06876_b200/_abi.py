@@ -50,7 +50,14 @@ class Counts(C.Structure):
         [("degenerate_ray", C.c_int32), ("reserved1", C.c_int32)]
 
     def as_dict(self):
-        return {f: int(getattr(self, f)) for f, _ in self._fields_ if not f.startswith("reserved")}
+        d = dict(zip(_COUNTS_NAMES, _COUNTS_FMT.unpack(bytes(self))))   # one copy, not a getattr per field
+        del d["reserved1"]
+        return d
+
+
+_COUNTS_FMT = __import__("struct").Struct("=13q2i")
+_COUNTS_NAMES = tuple(f for f, _ in Counts._fields_)
+assert _COUNTS_FMT.size == C.sizeof(Counts)
 
 
 class Report(C.Structure):

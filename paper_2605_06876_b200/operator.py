@@ -95,9 +95,12 @@ class GaussianTensors:
                                torch.empty(n, sh_k, 3, dtype=F32, device=device) if sh_k else None)
 
     def head(self, n: int) -> "GaussianTensors":
-        """The first n rows (views of the same storage)."""
-        return GaussianTensors(self.mu[:n], self.scale[:n], self.rot[:n], self.opacity[:n], self.sh_dc[:n],
-                               self.sh_rest[:n] if self.sh_k else None)
+        """The first n rows (views of the same storage; contiguous, fp32 by construction)."""
+        t = object.__new__(GaussianTensors)
+        t.mu, t.scale, t.rot, t.opacity, t.sh_dc = self.mu[:n], self.scale[:n], self.rot[:n], self.opacity[:n], \
+            self.sh_dc[:n]
+        t.sh_rest = self.sh_rest[:n] if self.sh_rest is not None else None
+        return t
 
     @staticmethod
     def from_numpy(mu, scale, rot, opacity, sh_dc, sh_rest=None, device=None) -> "GaussianTensors":
@@ -154,6 +157,7 @@ class Plan:
 
     def __init__(self, device=None):
         self.device = _require_cuda(device)
+        self._dev_index = self.device.index if self.device.index is not None else torch.cuda.current_device()
         self.lib = _abi.load()
         self._h = C.c_void_p()
         with torch.cuda.device(self.device):
@@ -172,7 +176,9 @@ class Plan:
             pass
 
     def _stream(self):
-        return C.c_void_p(torch.cuda.current_stream(self.device).cuda_stream)
+        # the raw cudaStream_t of torch's current stream on this device (what
+        # torch.cuda.current_stream(dev).cuda_stream returns, without the wrapper)
+        return C.c_void_p(torch._C._cuda_getCurrentRawStream(self._dev_index))
 
     def check_guards(self):
         """(bytes, buffers) written past the end of a plan buffer since allocation (debug; syncs)."""

@@ -1,5 +1,5 @@
 """cProfile of the host side of densify_step at a bench config (dev tool): where the
-Python/ctypes time goes between and around the kernels."""
+Python/ctypes time goes between and around the kernels (us per step, by own time)."""
 import cProfile
 import os
 import pstats
@@ -30,11 +30,14 @@ def step():
 for _ in range(3):
     step()
 torch.cuda.synchronize()
+K = 200
 pr = cProfile.Profile()
 pr.enable()
-for _ in range(20):
+for _ in range(K):
     step()
 torch.cuda.synchronize()
 pr.disable()
 st = pstats.Stats(pr)
-st.sort_stats("tottime").print_stats(30)
+rows = sorted(st.stats.items(), key=lambda kv: -kv[1][2])
+for (fn, line, name), (cc, nc, tt, ct, callers) in rows[:45]:
+    print(f"{tt / K * 1e6:9.1f} us/step own  {ct / K * 1e6:9.1f} cum  calls/step {nc / K:5.1f}  {os.path.basename(fn)}:{line}({name})")
