@@ -291,14 +291,21 @@ __device__ __forceinline__ int uf_find(volatile int* p, int x) {
 // ancestor (a smaller index in the same tree), so concurrent atomicMin links
 // on roots are never lost (ECL-CC style benign races).
 __device__ __forceinline__ int uf_find_halve(volatile int* p, int x) {
-  while (true) {
-    const int y = p[x];
-    if (y == x) return x;
+  // (single-exit loops throughout: early returns from inside inlined loops
+  // leave ptxas without a reconvergence point, and the warp's next shuffles
+  // and votes then run as divergent "collective" sequences)
+  int y = p[x];
+  while (y != x) {
     const int z = p[y];
-    if (z == y) return y;
+    if (z == y) {
+      x = y;
+      break;
+    }
     p[x] = z;
     x = z;
+    y = p[x];
   }
+  return x;
 }
 
 __device__ __forceinline__ void uf_unite(int* p, int a, int b) {
@@ -306,14 +313,14 @@ __device__ __forceinline__ void uf_unite(int* p, int a, int b) {
   while (true) {
     a = uf_find_halve(vp, a);
     b = uf_find_halve(vp, b);
-    if (a == b) return;
+    if (a == b) break;
     if (a > b) {
       int t = a;
       a = b;
       b = t;
     }
-    int old = atomicMin(&p[b], a);
-    if (old == b) return;
+    const int old = atomicMin(&p[b], a);
+    if (old == b) break;
     b = old;
   }
 }
@@ -326,16 +333,17 @@ __device__ __forceinline__ int uf_unite_root(int* p, int a, int b) {
   while (true) {
     a = uf_find_halve(vp, a);
     b = uf_find_halve(vp, b);
-    if (a == b) return a;
+    if (a == b) break;
     if (a > b) {
       int t = a;
       a = b;
       b = t;
     }
-    int old = atomicMin(&p[b], a);
-    if (old == b) return a;
+    const int old = atomicMin(&p[b], a);
+    if (old == b) break;
     b = old;
   }
+  return a;
 }
 
 }  // namespace adps

@@ -285,9 +285,12 @@ __device__ __forceinline__ void finish_tile(const TileParams& P, WS& S, const in
   const int b_top = st.b_top, b_bot = st.b_bot, b_left = st.b_left, b_right = st.b_right;
   __syncwarp();
   // ---- roots (read-only finds: stored roots are never overwritten)
-  for (int q = lane; q < n_runs; q += 32) {
-    S.uf[q] = uf_find(S.uf, q);
-    S.u.post.aux[q] = -1;
+  for (int b = 0; b < n_runs; b += 32) {   // warp-uniform trip count
+    const int q = b + lane;
+    if (q < n_runs) {
+      S.uf[q] = uf_find(S.uf, q);
+      S.u.post.aux[q] = -1;
+    }
   }
   __syncwarp();
   const bool left_in = x0 > 0, top_in = y0 > 0;
@@ -302,7 +305,9 @@ __device__ __forceinline__ void finish_tile(const TileParams& P, WS& S, const in
     for (int k = 0; k < 6; ++k) S.u.post.mom[lane][k] = 0;
     S.u.post.touch[lane] = 0;
     __syncwarp();
-    for (int q2 = lane; q2 < n_runs; q2 += 32) {
+    for (int b2 = 0; b2 < n_runs; b2 += 32) {   // warp-uniform trip count
+      const int q2 = b2 + lane;
+      if (q2 >= n_runs) continue;
       const int root = S.uf[q2];
       if (root < base || root >= base + 32) continue;
       const int sl = __popc(roots & ((1u << (root - base)) - 1u));
@@ -954,14 +959,23 @@ __device__ __forceinline__ void tile_bits_body(const TileParams& P, const uint4*
     return;
   }
   // ---- (c) run records of this row
+  // (warp-uniform trip counts with predicated bodies in (c), (d) and the
+  // finish: per-lane loops left the warp split in two halves for the rest of
+  // the tile -- ptxas placed no reconvergence point -- so every later
+  // instruction issued twice)
   {
     int rid = base;
-    for (unsigned st_bits = my_starts; st_bits; st_bits &= st_bits - 1u, ++rid) {
-      const int x = __ffs(st_bits) - 1;
-      const int e = __ffs(my_ends & (FULL << x)) - 1;
-      const int band = (int)((bw0 >> x) & 1u) | (int)(((bw1 >> x) & 1u) << 1);
-      S.run[rid] = (unsigned)lane | ((unsigned)x << 5) | ((unsigned)e << 10) | ((unsigned)band << 16);
-      S.uf[rid] = rid;
+    unsigned st_bits = my_starts;
+    while (__any_sync(FULL, st_bits != 0u)) {
+      if (st_bits) {
+        const int x = __ffs(st_bits) - 1;
+        const int e = __ffs(my_ends & (FULL << x)) - 1;
+        const int band = (int)((bw0 >> x) & 1u) | (int)(((bw1 >> x) & 1u) << 1);
+        S.run[rid] = (unsigned)lane | ((unsigned)x << 5) | ((unsigned)e << 10) | ((unsigned)band << 16);
+        S.uf[rid] = rid;
+        st_bits &= st_bits - 1u;
+        ++rid;
+      }
     }
   }
   __syncwarp();
@@ -973,14 +987,17 @@ __device__ __forceinline__ void tile_bits_body(const TileParams& P, const uint4*
     const int ba = __shfl_up_sync(FULL, base, 1);
     unsigned ev = (my_v0 & (my_starts | ~my_vm)) | (my_starts & my_vm & ~my_v0) | (my_ends & my_vp & ~my_v0);
     if (lane == 0) ev = 0u;
-    for (; ev; ev &= ev - 1u) {
-      const int x = __ffs(ev) - 1;
-      const unsigned bit = 1u << x, le = bit | (bit - 1u);
-      const int rid = base + __popc(my_starts & le) - 1;
-      const bool a0 = my_v0 & bit, am = my_vm & bit, is_start = my_starts & bit;
-      if (a0 && (is_start || !am)) uf_unite(S.uf, rid, ba + __popc(sa & le) - 1);
-      if (is_start && am && !a0) uf_unite(S.uf, rid, ba + __popc(sa & (bit - 1u)) - 1);
-      if ((my_ends & bit) && (my_vp & bit) && !a0) uf_unite(S.uf, rid, ba + __popc(sa & ((le << 1) | 1u)) - 1);
+    while (__any_sync(FULL, ev != 0u)) {
+      if (ev) {
+        const int x = __ffs(ev) - 1;
+        const unsigned bit = 1u << x, le = bit | (bit - 1u);
+        const int rid = base + __popc(my_starts & le) - 1;
+        const bool a0 = my_v0 & bit, am = my_vm & bit, is_start = my_starts & bit;
+        if (a0 && (is_start || !am)) uf_unite(S.uf, rid, ba + __popc(sa & le) - 1);
+        if (is_start && am && !a0) uf_unite(S.uf, rid, ba + __popc(sa & (bit - 1u)) - 1);
+        if ((my_ends & bit) && (my_vp & bit) && !a0) uf_unite(S.uf, rid, ba + __popc(sa & ((le << 1) | 1u)) - 1);
+        ev &= ev - 1u;
+      }
     }
   }
   // ---- (e) border run ids: rows 0 / 31 at column `lane`, columns 0 / 31 of row `lane`
