@@ -949,23 +949,35 @@ __global__ void __launch_bounds__(kBorderSlots * kBorderTilesPerBlock) border_ke
     gqs[k] = P.border[qt * kBorderSlots + border_slot(qx - qtx * kTileW, qy - qty * kTileH)];
   }
   const PartialRec* A = gp >= 0 ? &P.partials[gp] : nullptr;
+  // every warp-wide exchange first, then the unions: a shuffle after a lane's
+  // divergent union-find would run as a split-warp (collective) sequence
+  bool go[4];
+#if !ADPS_BORDER_MATCH
+  const int lgp = __shfl_up_sync(0xffffffffu, gp, 1);
+#endif
 #pragma unroll
   for (int k = 0; k < 4; ++k) {
     int gq = gqs[k];
     for (int k2 = 0; k2 < k; ++k2)
       if (gqs[k2] == gq) gq = -1;   // the same pair through another direction
+    gqs[k] = gq;
 #if ADPS_BORDER_MATCH
+    // lanes holding the same (fragment, neighbour fragment) pair unite once
     const unsigned long long key = gq >= 0 ? ((unsigned long long)(unsigned)gp << 32) | (unsigned)gq : ~0ull;
     const unsigned peers = __match_any_sync(0xffffffffu, key);
-    if (gq < 0 || (int)(threadIdx.x & 31) != __ffs(peers) - 1) continue;
+    go[k] = gq >= 0 && (int)(threadIdx.x & 31) == __ffs(peers) - 1;
 #else
     // along an edge equal pairs come in runs: skip a lane whose left neighbour
     // holds the same pair (unions are idempotent, so leftover duplicates only cost time)
-    const int lgp = __shfl_up_sync(0xffffffffu, gp, 1), lgq = __shfl_up_sync(0xffffffffu, gq, 1);
-    if (gq < 0 || ((threadIdx.x & 31) > 0 && lgp == gp && lgq == gq)) continue;
+    const int lgq = __shfl_up_sync(0xffffffffu, gq, 1);
+    go[k] = gq >= 0 && !((threadIdx.x & 31) > 0 && lgp == gp && lgq == gq);
 #endif
-    const PartialRec& B = P.partials[gq];
-    if (A->cand == B.cand && A->band == B.band) uf_unite(P.parent, gp, gq);
+  }
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    if (!go[k]) continue;
+    const PartialRec& B = P.partials[gqs[k]];
+    if (A->cand == B.cand && A->band == B.band) uf_unite(P.parent, gp, gqs[k]);
   }
 }
 

@@ -158,8 +158,10 @@ __global__ void small_pairs_kernel(MergeArgs a) {
     const Proposal* pr = a.props_s + ps;
     for (int i = 0; i < P - 1; ++i) {
       const Proposal& A = pr[i];
-      for (int j = i + 1 + lane; j < P; j += 32)
-        if (gate(A, pr[j], a.gamma_d, a.gamma_c)) uf_unite(a.uf, ps + i, ps + j);
+      for (int j0 = i + 1; j0 < P; j0 += 32) {   // warp-uniform trip count, predicated body
+        const int j = j0 + lane;
+        if (j < P && gate(A, pr[j], a.gamma_d, a.gamma_c)) uf_unite(a.uf, ps + i, ps + j);
+      }
     }
   }
 }
@@ -744,15 +746,20 @@ __global__ void __launch_bounds__(kPairWarps * 32, ADPS_PAIR_MINB) pair_tiles_ke
       if (lane >= ni) maybe = 0u;
       // gates first, unions after: a union inside the column loop would stall
       // the whole warp on one lane's union-find latency whenever any lane passes
+      // (warp-uniform trip counts, predicated bodies: per-lane loops left the
+      // warp split for the rest of the pair, every later instruction issued twice)
       unsigned pass = 0u;
-      for (; maybe; maybe &= maybe - 1u) {
-        const int jj = __ffs(maybe) - 1;
-        const bool ok = gate_col(A, J.s, jj, gd, gd2, gc);
+      while (__any_sync(0xffffffffu, maybe != 0u)) {
+        if (maybe) {
+          const int jj = __ffs(maybe) - 1;
+          const bool ok = gate_col(A, J.s, jj, gd, gd2, gc);
 #if ADPS_MERGE_STATS
-        atomicAdd(&a.ctr->stat_gates, 1ull);
-        if (ok) atomicAdd(&a.ctr->stat_pass, 1ull);
+          atomicAdd(&a.ctr->stat_gates, 1ull);
+          if (ok) atomicAdd(&a.ctr->stat_pass, 1ull);
 #endif
-        if (ok) pass |= 1u << jj;
+          if (ok) pass |= 1u << jj;
+          maybe &= maybe - 1u;
+        }
       }
 #if ADPS_PAIR_LOCAL_UF
       // the tile pair's links first in a warp-local union-find over its 64
@@ -778,10 +785,13 @@ __global__ void __launch_bounds__(kPairWarps * 32, ADPS_PAIR_MINB) pair_tiles_ke
 #else
       // a column already hanging directly below the root this row proposal was
       // last united under is in its tree: one load instead of two finds
-      for (; pass; pass &= pass - 1u) {
-        const int qb = J.q[__ffs(pass) - 1];
-        if (ADPS_PAIR_ROOT_CACHE && ra >= 0 && reinterpret_cast<volatile int*>(a.uf)[qb] == ra) continue;
-        ra = uf_unite_root(a.uf, qa, qb);
+      while (__any_sync(0xffffffffu, pass != 0u)) {
+        if (pass) {
+          const int qb = J.q[__ffs(pass) - 1];
+          if (!(ADPS_PAIR_ROOT_CACHE && ra >= 0 && reinterpret_cast<volatile int*>(a.uf)[qb] == ra))
+            ra = uf_unite_root(a.uf, qa, qb);
+          pass &= pass - 1u;
+        }
       }
 #endif
     }
@@ -931,7 +941,9 @@ __global__ void __launch_bounds__(256, (ADPS_GROUP_MINB + 1) / 2) group_kernel(M
     const int b = a.grp_first[g], e = a.grp_first[g + 1];
     const int cnt = e - b;
     double acc[12] = {0};
-    for (int m = b + lane; m < e; m += 32) {
+    for (int m0 = b; m0 < e; m0 += 32) {   // warp-uniform trip count, predicated body
+      const int m = m0 + lane;
+      if (m >= e) continue;
       const Proposal& M = a.props_s[a.gval_sorted[m]];
       for (int t = 0; t < 3; ++t) {
         acc[t] += M.mu[t];
@@ -955,7 +967,9 @@ __global__ void __launch_bounds__(256, (ADPS_GROUP_MINB + 1) / 2) group_kernel(M
     for (int r = 0; r < 3; ++r) {
       const double ev[3] = {R.evec[r], R.evec[3 + r], R.evec[6 + r]};
       double best = 0.0;
-      for (int m = b + lane; m < e; m += 32) {
+      for (int m0 = b; m0 < e; m0 += 32) {
+        const int m = m0 + lane;
+        if (m >= e) continue;
         const Proposal& M = a.props_s[a.gval_sorted[m]];
         const double off = fabs((M.mu[0] - R.mu[0]) * ev[0] + (M.mu[1] - R.mu[1]) * ev[1] +
                                 (M.mu[2] - R.mu[2]) * ev[2]);
