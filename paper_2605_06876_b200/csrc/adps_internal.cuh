@@ -110,6 +110,7 @@ struct Counters {
   unsigned long long n_owned_props;          // proposals of this rank's parents   // diagnostics (ADPS_MERGE_STATS builds)
   unsigned long long n_mid_groups, n_huge_groups;   // work lists of the group reduction
   unsigned long long n_cap_large;                   // groups of parents with many groups
+  unsigned long long tile_records;   // tile CCLs: partials << 32 | regions (one atomic per batch; unpacked after)
   unsigned long long n_cap_huge;                    // parents whose groups are selected in shared memory
   unsigned long long prune_keep, prune_near;        // adps_prune_index
   unsigned int normals_status;           // bit0 near-tie (redraw on host), bit1 window short

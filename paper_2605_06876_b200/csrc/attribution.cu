@@ -828,8 +828,11 @@ __device__ void tile_block(const TileParams& P, TileSmem& S, const int tile) {
   }
   __syncthreads();
   if (tid == 0) {
-    S.base_part = S.n_part ? atomicAdd(P.n_partials, (unsigned long long)S.n_part) : 0ull;
-    S.base_reg = S.n_reg ? atomicAdd(P.n_regions, (unsigned long long)S.n_reg) : 0ull;
+    // one atomic for both record kinds (partials << 32 | regions)
+    const unsigned long long old =
+        (S.n_part | S.n_reg) ? atomicAdd(P.tile_records, ((unsigned long long)S.n_part << 32) | (unsigned)S.n_reg) : 0ull;
+    S.base_part = old >> 32;
+    S.base_reg = old & 0xffffffffull;
   }
   __syncthreads();
   for (int p = tid; p < kTilePx; p += kTileThreads) {
@@ -981,6 +984,14 @@ __global__ void __launch_bounds__(kBorderSlots * kBorderTilesPerBlock) border_ke
   }
 }
 
+__global__ void unpack_records_kernel(const unsigned long long* __restrict__ packed,
+                                      unsigned long long* __restrict__ n_partials,
+                                      unsigned long long* __restrict__ n_regions) {
+  const unsigned long long v = *packed;
+  *n_partials = v >> 32;
+  *n_regions = v & 0xffffffffull;
+}
+
 __global__ void resolve_kernel(PartialRec* __restrict__ partials, int* __restrict__ parent,
                                const unsigned long long* __restrict__ n_partials, long long cap) {
   long long n = (long long)*n_partials;
@@ -1117,6 +1128,7 @@ static TileParams tile_params(const AttributionArgs& a) {
   P.n_partials = a.n_partials;
   P.partial_cap = a.partial_cap;
   P.partial_parent = a.partial_parent;
+  P.tile_records = a.tile_records;
   P.border = a.border;
   P.dbg_m = a.dbg_m;
   P.dbg_b = a.dbg_b;
@@ -1163,6 +1175,8 @@ cudaError_t launch_attribution_tail(const AttributionArgs& a, cudaStream_t s, Ma
     tile_kernel<<<(unsigned)nblocks, kTileThreads, smem, s>>>(P, nullptr, nullptr);
     if (mark) mark(ctx, "tile_ccl", s, 1);
   }
+  // the tile CCLs' packed record counts into n_partials / n_regions (zero before)
+  unpack_records_kernel<<<1, 1, 0, s>>>(a.tile_records, a.n_partials, a.n_regions);
   BorderParams B;
   B.border = a.border;
   B.partials = a.partials;

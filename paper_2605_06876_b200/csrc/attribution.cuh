@@ -25,6 +25,7 @@ struct TileParams {
   unsigned long long* n_partials;
   long long partial_cap;
   int* partial_parent;
+  unsigned long long* tile_records;   // packed partials << 32 | regions of the tile CCLs
   int* border;
   unsigned char* dbg_m;
   unsigned char* dbg_b;
@@ -68,6 +69,7 @@ struct AttributionArgs {
   unsigned long long* n_partials;
   long long partial_cap;
   int* partial_parent;
+  unsigned long long* tile_records;   // packed partials << 32 | regions of the tile CCLs
   int* border;                // [V * tiles * kBorderSlots]
   unsigned char* dbg_m;
   unsigned char* dbg_b;

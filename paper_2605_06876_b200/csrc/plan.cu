@@ -746,6 +746,7 @@ static AttributionArgs attr_args(adps_plan* P, int V, int H, int W, const adps_c
   a.region_cap = P->region_cap;
   a.partials = P->partials.as<PartialRec>();
   a.n_partials = &ctr->n_partials;
+  a.tile_records = &ctr->tile_records;
   a.partial_cap = P->partial_cap;
   a.partial_parent = P->partial_parent.as<int>();
   a.border = P->border.as<int>();
@@ -771,6 +772,7 @@ static adps_status run_attribution(adps_plan* P, cudaStream_t s, int V, int H, i
   Counters* ctr = P->ctr.as<Counters>();
   CK(cudaMemsetAsync(&ctr->n_regions, 0, sizeof(unsigned long long), s));
   CK(cudaMemsetAsync(&ctr->n_partials, 0, sizeof(unsigned long long), s));
+  CK(cudaMemsetAsync(&ctr->tile_records, 0, sizeof(unsigned long long), s));
   CK(cudaMemsetAsync(&ctr->overflow, 0, sizeof(unsigned int), s));
   CK(cudaMemsetAsync(&ctr->n_deferred, 0, sizeof(unsigned long long), s));
   const AttributionArgs a = attr_args(P, V, H, W, cfg, N, image, gt, dominant);
@@ -966,6 +968,9 @@ extern "C" adps_status adps_step_phase1_begin(adps_plan* P, void* stream_v, cons
   }
   const long long region_bound = total_px / (cfg->m_min > 1 ? cfg->m_min : 1) + 1;
   const long long partial_bound = n_tiles * (2 * kTileW + 2 * kTileH) + 1;
+  // the tile CCLs count both record kinds in the halves of one 64-bit word
+  if (region_bound >= (1ll << 32) || partial_bound >= (1ll << 32))
+    return fail(ADPS_INVALID_ARG, "%lld pixels: the region count may exceed 2^32", total_px);
   // per-call capacities: the largest seen so far (at least 2^21), never above the analytic bound
   P->region_hint = P->region_cap > P->region_hint ? P->region_cap : P->region_hint;
   P->partial_hint = P->partial_cap > P->partial_hint ? P->partial_cap : P->partial_hint;

@@ -333,9 +333,11 @@ __device__ __forceinline__ void finish_tile(const TileParams& P, WS& S, const in
     const bool is_reg = is_root && !S.u.post.touch[sl] && S.u.post.mom[sl][0] >= P.m_min;
     const unsigned pm = __ballot_sync(FULL, is_part), rm = __ballot_sync(FULL, is_reg);
     unsigned long long pbase = 0, rbase = 0;
-    if (lane == 0) {
-      if (pm) pbase = atomicAdd(P.n_partials, (unsigned long long)__popc(pm));
-      if (rm) rbase = atomicAdd(P.n_regions, (unsigned long long)__popc(rm));
+    if (lane == 0 && (pm | rm)) {   // one atomic for both record kinds (partials << 32 | regions)
+      const unsigned long long old =
+          atomicAdd(P.tile_records, ((unsigned long long)__popc(pm) << 32) | (unsigned long long)__popc(rm));
+      pbase = old >> 32;
+      rbase = old & 0xffffffffull;
     }
     pbase = __shfl_sync(FULL, pbase, 0);
     rbase = __shfl_sync(FULL, rbase, 0);
