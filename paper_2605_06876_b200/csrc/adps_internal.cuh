@@ -1,6 +1,9 @@
 // Internal definitions shared by the AdpSplit B200 kernels.
 #pragma once
 
+#include <cstdlib>
+#include <utility>
+
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -9,6 +12,40 @@
 namespace adps {
 
 constexpr int kWarp = 32;
+
+// ---------------------------------------------------- programmatic dependent launch
+// Every kernel of the library starts with pdl_wait() (griddepcontrol.wait:
+// returns once the previous kernel in the stream has completed and its writes
+// are visible; a no-op without a programmatic dependency) and is launched by
+// launch_k with programmatic stream serialization, so the next kernel's grid
+// is set up and its blocks become resident while the previous one drains
+// (1.3-3 us per kernel boundary on B200, tools/pdl_probe).  ADPS_PDL=0
+// launches plainly.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
+inline bool pdl_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("ADPS_PDL");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_k(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                            Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
+}
 
 // ---------------------------------------------------------------- constants
 // ref/raster.py:20-24

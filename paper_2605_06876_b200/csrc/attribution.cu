@@ -48,6 +48,7 @@ __global__ void minmax_kernel(const float* __restrict__ image, const float* __re
                               const unsigned char* __restrict__ cls, int N, unsigned char* __restrict__ dom_flag,
                               unsigned* __restrict__ cand_bits, double* __restrict__ raw_out,
                               raw16_t* __restrict__ rawf_out, int v0) {
+  pdl_wait();   // programmatic dependent launch: the previous kernel's results are visible
   const int v = v0 + blockIdx.y;
   const float* img = image + (long long)v * hw * 3;
   const float* g = gt + (long long)v * hw * 3;
@@ -127,6 +128,7 @@ __global__ void __launch_bounds__(256) minmax2_kernel(const float* __restrict__ 
                                                       unsigned char* __restrict__ dom_flag,
                                                       unsigned* __restrict__ cand_bits, double* __restrict__ raw_out,
                                                       raw16_t* __restrict__ rawf_out, int v0) {
+  pdl_wait();   // programmatic dependent launch: the previous kernel's results are visible
   const int v = v0 + blockIdx.y;
   const long long vb = (long long)v * hw;
   const float2* img2 = reinterpret_cast<const float2*>(image + vb * 3);
@@ -280,6 +282,7 @@ struct BulkArgs {
 };
 
 __global__ void __launch_bounds__(kMBThreads) minmax_bulk_kernel(BulkArgs a) {
+  pdl_wait();   // programmatic dependent launch: the previous kernel's results are visible
   extern __shared__ __align__(128) unsigned char mb_smem[];
   MBStage* stage = reinterpret_cast<MBStage*>(mb_smem);
   unsigned long long* full = reinterpret_cast<unsigned long long*>(mb_smem + sizeof(MBStage) * kMBStages);
@@ -487,7 +490,7 @@ cudaError_t launch_minmax_bulk(const AttributionArgs& a, int v0, int v1, cudaStr
   const long long chunks = (b.p1 - b.p0 + kMBChunk - 1) / kMBChunk;
   long long grid = (long long)per_sm * sms;
   if (grid > chunks) grid = chunks;
-  minmax_bulk_kernel<<<(unsigned)grid, kMBThreads, kMBSmem, s>>>(b);
+  launch_k(minmax_bulk_kernel, (unsigned)grid, kMBThreads, kMBSmem, s, b);
   return cudaGetLastError();
 }
 
@@ -550,6 +553,7 @@ __device__ double raw_threshold(double lo, double hi, double t) {
 __global__ void thresholds_kernel(const unsigned long long* __restrict__ lohi, int v0, int n_views, int L,
                                   double tau, double* __restrict__ lo_out, double* __restrict__ thr,
                                   double* __restrict__ thr_raw) {
+  pdl_wait();   // programmatic dependent launch: the previous kernel's results are visible
   const int t = v0 * L + (int)((blockIdx.x * blockDim.x + threadIdx.x) >> 5);
   if (t >= (v0 + n_views) * L) return;   // warp-uniform
   const bool lead = (threadIdx.x & 31) == 0;
@@ -581,6 +585,7 @@ __global__ void thresholds_kernel(const unsigned long long* __restrict__ lohi, i
 // can draw its normals) while the rest of phase 1 runs on the GPU.
 __global__ void fallback_count_kernel(const int* __restrict__ split_list, const unsigned char* __restrict__ dom_flag,
                                       Counters* ctr) {
+  pdl_wait();   // programmatic dependent launch: the previous kernel's results are visible
   const long long n = (long long)ctr->n_split;
   int c = 0;
   for (long long k = (long long)blockIdx.x * blockDim.x + threadIdx.x; k < n; k += (long long)gridDim.x * blockDim.x)
@@ -898,6 +903,7 @@ __device__ void tile_block(const TileParams& P, TileSmem& S, const int tile) {
 // all tiles (list == nullptr) or the tiles the warp kernel deferred
 __global__ void __launch_bounds__(kTileThreads) tile_kernel(TileParams P, const int* list,
                                                             const unsigned long long* n_list) {
+  pdl_wait();   // programmatic dependent launch: the previous kernel's results are visible
   extern __shared__ __align__(16) unsigned char smem_raw[];
   TileSmem& S = *reinterpret_cast<TileSmem*>(smem_raw);
   const long long n = list ? (long long)*n_list : (long long)P.tiles_x * P.tiles_y * P.n_views;
@@ -919,6 +925,7 @@ constexpr int kBorderTilesPerBlock = 1;
 #define ADPS_BORDER_MATCH 1
 #endif
 __global__ void __launch_bounds__(kBorderSlots * kBorderTilesPerBlock) border_kernel(BorderParams P) {
+  pdl_wait();   // programmatic dependent launch: the previous kernel's results are visible
   // 128 threads = the tile's border slots; warp w = side w (top, bottom, left,
   // right).  Runs along an edge ask for the same union many times: lanes
   // holding the same (fragment, neighbour fragment) pair unite once (match_any)
@@ -987,6 +994,7 @@ __global__ void __launch_bounds__(kBorderSlots * kBorderTilesPerBlock) border_ke
 __global__ void unpack_records_kernel(const unsigned long long* __restrict__ packed,
                                       unsigned long long* __restrict__ n_partials,
                                       unsigned long long* __restrict__ n_regions) {
+  pdl_wait();   // programmatic dependent launch: the previous kernel's results are visible
   const unsigned long long v = *packed;
   *n_partials = v >> 32;
   *n_regions = v & 0xffffffffull;
@@ -994,6 +1002,7 @@ __global__ void unpack_records_kernel(const unsigned long long* __restrict__ pac
 
 __global__ void resolve_kernel(PartialRec* __restrict__ partials, int* __restrict__ parent,
                                const unsigned long long* __restrict__ n_partials, long long cap) {
+  pdl_wait();   // programmatic dependent launch: the previous kernel's results are visible
   long long n = (long long)*n_partials;
   if (n > cap) n = cap;
   for (long long g = (long long)blockIdx.x * blockDim.x + threadIdx.x; g < n;
@@ -1013,6 +1022,7 @@ __global__ void partial_emit_kernel(const PartialRec* __restrict__ partials, con
                                     int m_min, RegionRec* __restrict__ regions,
                                     unsigned long long* __restrict__ n_regions, long long rcap,
                                     unsigned int* __restrict__ overflow) {
+  pdl_wait();   // programmatic dependent launch: the previous kernel's results are visible
   long long n = (long long)*n_partials;
   if (n > pcap) n = pcap;
   for (long long g = (long long)blockIdx.x * blockDim.x + threadIdx.x; g < n;
@@ -1063,13 +1073,13 @@ cudaError_t launch_minmax_kernel(const AttributionArgs& a, int v0, int v1, cudaS
     // floor: at most one wave (a second, short wave would run whole view slices on a few SMs)
     const long long want = (long long)resident / (v1 - v0);
     dim3 mg2((unsigned)(want < 1 ? 1 : (want > per_view ? per_view : want)), (unsigned)(v1 - v0));
-    minmax2_kernel<<<mg2, 256, 0, s>>>(a.image, a.gt, a.dom, (int)hw, a.lohi, a.cls, a.N, a.dom_flag, a.cand_bits,
+    launch_k(minmax2_kernel, mg2, 256, 0, s, a.image, a.gt, a.dom, (int)hw, a.lohi, a.cls, a.N, a.dom_flag, a.cand_bits,
                                        a.raw, a.rawf, v0);
     return cudaGetLastError();
   }
   dim3 mg((unsigned)((hw + 256 * 8 - 1) / (256 * 8)), (unsigned)(v1 - v0));
   if (mg.x > 1024) mg.x = 1024;
-  minmax_kernel<<<mg, 256, 0, s>>>(a.image, a.gt, a.dom, hw, a.lohi, a.cls, a.N, a.dom_flag, a.cand_bits, a.raw,
+  launch_k(minmax_kernel, mg, 256, 0, s, a.image, a.gt, a.dom, hw, a.lohi, a.cls, a.N, a.dom_flag, a.cand_bits, a.raw,
                                    a.rawf, v0);
   return cudaGetLastError();
 }
@@ -1077,7 +1087,7 @@ cudaError_t launch_minmax_kernel(const AttributionArgs& a, int v0, int v1, cudaS
 cudaError_t launch_thresholds(const AttributionArgs& a, int v0, int v1, cudaStream_t s) {
   if (v1 <= v0) return cudaSuccess;
   const int nt = (v1 - v0) * a.L;
-  thresholds_kernel<<<(nt + 3) / 4, 128, 0, s>>>(a.lohi, v0, v1 - v0, a.L, a.tau, a.lo, a.thr, a.thr_raw);
+  launch_k(thresholds_kernel, (nt + 3) / 4, 128, 0, s, a.lohi, v0, v1 - v0, a.L, a.tau, a.lo, a.thr, a.thr_raw);
   return cudaGetLastError();
 }
 
@@ -1091,13 +1101,13 @@ cudaError_t launch_minmax(const AttributionArgs& a, const int* split_list, Count
                           cudaStream_t s) {
   cudaError_t e = launch_minmax_views(a, 0, a.V, s);
   if (e != cudaSuccess) return e;
-  fallback_count_kernel<<<sm_count * 2, 256, 0, s>>>(split_list, a.dom_flag, ctr);
+  launch_k(fallback_count_kernel, sm_count * 2, 256, 0, s, split_list, a.dom_flag, ctr);
   return cudaGetLastError();
 }
 
 cudaError_t launch_fallback_count(const int* split_list, const unsigned char* dom_flag, Counters* ctr, int sm_count,
                                   cudaStream_t s) {
-  fallback_count_kernel<<<sm_count * 2, 256, 0, s>>>(split_list, dom_flag, ctr);
+  launch_k(fallback_count_kernel, sm_count * 2, 256, 0, s, split_list, dom_flag, ctr);
   return cudaGetLastError();
 }
 
@@ -1169,14 +1179,14 @@ cudaError_t launch_attribution_tail(const AttributionArgs& a, cudaStream_t s, Ma
     if (e != cudaSuccess) return e;
     if (mark) mark(ctx, "tile_ccl", s, a.words ? 3 : 2);
   } else if (attribution_warp_path(a)) {
-    tile_kernel<<<a.grid_small, kTileThreads, smem, s>>>(P, a.deferred, a.n_deferred);
+    launch_k(tile_kernel, a.grid_small, kTileThreads, smem, s, P, a.deferred, a.n_deferred);
     if (mark) mark(ctx, "tile_ccl", s, a.words ? 3 : 2);
   } else {
-    tile_kernel<<<(unsigned)nblocks, kTileThreads, smem, s>>>(P, nullptr, nullptr);
+    launch_k(tile_kernel, (unsigned)nblocks, kTileThreads, smem, s, P, nullptr, nullptr);
     if (mark) mark(ctx, "tile_ccl", s, 1);
   }
   // the tile CCLs' packed record counts into n_partials / n_regions (zero before)
-  unpack_records_kernel<<<1, 1, 0, s>>>(a.tile_records, a.n_partials, a.n_regions);
+  launch_k(unpack_records_kernel, 1, 1, 0, s, a.tile_records, a.n_partials, a.n_regions);
   BorderParams B;
   B.border = a.border;
   B.partials = a.partials;
@@ -1186,10 +1196,9 @@ cudaError_t launch_attribution_tail(const AttributionArgs& a, cudaStream_t s, Ma
   B.W = a.W;
   B.H = a.H;
   B.n_tiles = nblocks;
-  border_kernel<<<(unsigned)((nblocks + kBorderTilesPerBlock - 1) / kBorderTilesPerBlock),
-                  kBorderSlots * kBorderTilesPerBlock, 0, s>>>(B);
-  resolve_kernel<<<a.grid_small, 256, 0, s>>>(a.partials, a.partial_parent, a.n_partials, a.partial_cap);
-  partial_emit_kernel<<<a.grid_small, 256, 0, s>>>(a.partials, a.partial_parent, a.n_partials, a.partial_cap,
+  launch_k(border_kernel, (unsigned)((nblocks + kBorderTilesPerBlock - 1) / kBorderTilesPerBlock), kBorderSlots * kBorderTilesPerBlock, 0, s, B);
+  launch_k(resolve_kernel, a.grid_small, 256, 0, s, a.partials, a.partial_parent, a.n_partials, a.partial_cap);
+  launch_k(partial_emit_kernel, a.grid_small, 256, 0, s, a.partials, a.partial_parent, a.n_partials, a.partial_cap,
                                                     a.m_min, a.regions, a.n_regions, a.region_cap, a.overflow);
   if (mark) mark(ctx, "border_merge", s, 3);
   return cudaGetLastError();

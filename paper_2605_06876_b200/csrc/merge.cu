@@ -87,6 +87,7 @@ struct GatherPolicy {
 };
 
 __global__ void case_kernel(MergeArgs a) {
+  pdl_wait();   // programmatic dependent launch: the previous kernel's results are visible
   const long long n_split = (long long)a.ctr->n_split;
   for (long long k = (long long)blockIdx.x * blockDim.x + threadIdx.x; k < n_split;
        k += (long long)gridDim.x * blockDim.x) {
@@ -126,6 +127,7 @@ __global__ void case_kernel(MergeArgs a) {
 // props_s[q] = props[psrc[q]]: thread per 8-byte word, so both the gathered
 // source records and the packed destination are read/written coalesced
 __global__ void gather_props_kernel(MergeArgs a) {
+  pdl_wait();   // programmatic dependent launch: the previous kernel's results are visible
   constexpr int WPR = (int)(sizeof(Proposal) / 8);
   const long long nw = (long long)a.ctr->n_proposals * WPR;
   const double* src = reinterpret_cast<const double*>(a.props);
@@ -140,14 +142,15 @@ __global__ void gather_props_kernel(MergeArgs a) {
 cudaError_t launch_merge_prepare(const MergeArgs& a, long long n_split, ScanState st, cudaStream_t s) {
   cudaError_t e = launch_scan(GatherPolicy{a}, a.n_regions, st, s);
   if (e != cudaSuccess) return e;
-  gather_props_kernel<<<a.grid, 256, 0, s>>>(a);
+  launch_k(gather_props_kernel, a.grid, 256, 0, s, a);
   long long b = (n_split + 255) / 256;
-  case_kernel<<<(unsigned)(b < 1 ? 1 : (b > 4096 ? 4096 : b)), 256, 0, s>>>(a);
+  launch_k(case_kernel, (unsigned)(b < 1 ? 1 : (b > 4096 ? 4096 : b)), 256, 0, s, a);
   return cudaGetLastError();
 }
 
 // -------------------------------------------------------------------- gates
 __global__ void small_pairs_kernel(MergeArgs a) {
+  pdl_wait();   // programmatic dependent launch: the previous kernel's results are visible
   const int lane = threadIdx.x & 31;
   const long long warps = (long long)gridDim.x * (blockDim.x >> 5);
   const long long n_small = (long long)a.ctr->n_small;
@@ -172,6 +175,7 @@ struct Offsets3 {
   unsigned long long* out[3];
 };
 __global__ void __launch_bounds__(1024) offsets_1block_kernel(Offsets3 io, const unsigned long long* __restrict__ n_dev) {
+  pdl_wait();   // programmatic dependent launch: the previous kernel's results are visible
   const unsigned long long* __restrict__ in = io.in[blockIdx.x];
   unsigned long long* __restrict__ out = io.out[blockIdx.x];
   __shared__ unsigned long long warp_tot[32];
@@ -211,6 +215,7 @@ __global__ void __launch_bounds__(1024) offsets_1block_kernel(Offsets3 io, const
 
 __global__ void __launch_bounds__(1024) shard_range_kernel(const int* __restrict__ nvalid, long long n, int rank,
                                                            int world, unsigned long long* __restrict__ lohi) {
+  pdl_wait();   // programmatic dependent launch: the previous kernel's results are visible
   __shared__ unsigned long long warp_tot[32];
   __shared__ unsigned long long carry, total;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -272,6 +277,7 @@ __global__ void __launch_bounds__(1024) shard_range_kernel(const int* __restrict
 // (pstart is only defined for parents with regions)
 __global__ void __launch_bounds__(1024) shard_prange_kernel(const int* __restrict__ nvalid, long long n,
                                                             unsigned long long* __restrict__ lohi) {
+  pdl_wait();   // programmatic dependent launch: the previous kernel's results are visible
   __shared__ unsigned long long ws[2][32];
   const unsigned long long lo = lohi[0], hi = lohi[1];
   unsigned long long a = 0, b = 0;
@@ -302,13 +308,13 @@ __global__ void __launch_bounds__(1024) shard_prange_kernel(const int* __restric
 
 cudaError_t launch_shard_range(const int* nvalid, long long n, int rank, int world, unsigned long long* lohi,
                                cudaStream_t s) {
-  shard_range_kernel<<<1, 1024, 0, s>>>(nvalid, n, rank, world, lohi);
-  shard_prange_kernel<<<1, 1024, 0, s>>>(nvalid, n, lohi);
+  launch_k(shard_range_kernel, 1, 1024, 0, s, nvalid, n, rank, world, lohi);
+  launch_k(shard_prange_kernel, 1, 1024, 0, s, nvalid, n, lohi);
   return cudaGetLastError();
 }
 
 cudaError_t launch_small_pairs(const MergeArgs& a, cudaStream_t s) {
-  small_pairs_kernel<<<a.grid, 256, 0, s>>>(a);
+  launch_k(small_pairs_kernel, a.grid, 256, 0, s, a);
   return cudaGetLastError();
 }
 
@@ -320,12 +326,12 @@ cudaError_t launch_large_offsets(const MergeArgs& a, cudaStream_t s) {
   io.out[1] = a.lp_off;
   io.in[2] = a.tile_cnt;
   io.out[2] = a.tile_off;
-  offsets_1block_kernel<<<3, 1024, 0, s>>>(io, &a.ctr->n_large);
+  launch_k(offsets_1block_kernel, 3, 1024, 0, s, io, &a.ctr->n_large);
   return cudaGetLastError();
 }
 
 cudaError_t launch_merge_small_gates(const MergeArgs& a, cudaStream_t s) {
-  small_pairs_kernel<<<a.grid, 256, 0, s>>>(a);
+  launch_k(small_pairs_kernel, a.grid, 256, 0, s, a);
   return launch_large_offsets(a, s);
 }
 
@@ -347,6 +353,7 @@ __device__ __forceinline__ unsigned spread10(unsigned v) {
 }
 
 __global__ void morton_kernel(MergeArgs a, long long cap) {
+  pdl_wait();   // programmatic dependent launch: the previous kernel's results are visible
   const long long np = (long long)a.ctr->n_proposals;
   const double inv = 1.0 / (4.0 * a.extent);
   for (long long q = (long long)blockIdx.x * blockDim.x + threadIdx.x; q < cap;
@@ -372,7 +379,7 @@ __global__ void morton_kernel(MergeArgs a, long long cap) {
 
 cudaError_t launch_merge_morton(const MergeArgs& a, long long cap, cudaStream_t s) {
   long long b = (cap + 255) / 256;
-  morton_kernel<<<(unsigned)(b < 1 ? 1 : (b > 65535 ? 65535 : b)), 256, 0, s>>>(a, cap);
+  launch_k(morton_kernel, (unsigned)(b < 1 ? 1 : (b > 65535 ? 65535 : b)), 256, 0, s, a, cap);
   return cudaGetLastError();
 }
 
@@ -391,6 +398,7 @@ __device__ __forceinline__ long long find_owner(const unsigned long long* off, l
 // and the tile's owner (read by the filter instead of a search)
 static_assert(kMT == 32, "box_kernel: one proposal per lane");
 __global__ void box_kernel(MergeArgs a) {
+  pdl_wait();   // programmatic dependent launch: the previous kernel's results are visible
   const int lane = threadIdx.x & 31;
   const long long warps = (long long)gridDim.x * (blockDim.x >> 5);
   const long long n_large = (long long)a.ctr->n_large;
@@ -503,6 +511,7 @@ __device__ __forceinline__ int4 pair_entry(const MergeArgs& a, long long l, long
 // order).  Blocks, not warps, per row: the longest rows (a parent with
 // thousands of proposals) no longer serialise on one warp.
 __global__ void tile_pair_filter_kernel(MergeArgs a) {
+  pdl_wait();   // programmatic dependent launch: the previous kernel's results are visible
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
   const long long n_large = (long long)a.ctr->n_large;
   const long long rows = n_large > 0 ? (long long)a.tile_off[n_large] : 0;
@@ -622,6 +631,7 @@ __device__ __forceinline__ void stage_col(const MergeArgs& a, ColTile& B, long l
 #define ADPS_PAIR_MINB 1
 #endif
 __global__ void __launch_bounds__(kPairWarps * 32, ADPS_PAIR_MINB) pair_tiles_kernel(MergeArgs a) {
+  pdl_wait();   // programmatic dependent launch: the previous kernel's results are visible
   extern __shared__ __align__(16) unsigned char pt_smem[];
 #if ADPS_PAIR_LOCAL_UF
   __shared__ int luf[kPairWarps][64];   // warp-local union-find of a tile pair
@@ -804,8 +814,8 @@ __global__ void __launch_bounds__(kPairWarps * 32, ADPS_PAIR_MINB) pair_tiles_ke
 }
 
 cudaError_t launch_merge_tile_gates(const MergeArgs& a, cudaStream_t s) {
-  box_kernel<<<a.grid, 256, 0, s>>>(a);
-  tile_pair_filter_kernel<<<a.grid, 128, 0, s>>>(a);   // block per tile row
+  launch_k(box_kernel, a.grid, 256, 0, s, a);
+  launch_k(tile_pair_filter_kernel, a.grid, 128, 0, s, a);   // block per tile row
   const int smem = (int)(sizeof(ColTile) * 2 * kPairWarps);
   cudaError_t e = cudaFuncSetAttribute(pair_tiles_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return e;
@@ -819,12 +829,13 @@ cudaError_t launch_merge_tile_gates(const MergeArgs& a, cudaStream_t s) {
   resident = ADPS_PAIR_BLOCKS_PER_SM;
 #endif
   const unsigned blocks = (unsigned)(a.grid / 8) * (unsigned)resident;   // a.grid = 8 x SM count
-  pair_tiles_kernel<<<blocks, kPairWarps * 32, smem, s>>>(a);
+  launch_k(pair_tiles_kernel, blocks, kPairWarps * 32, smem, s, a);
   return cudaGetLastError();
 }
 
 // ----------------------------------------------------------------- flatten
 __global__ void flatten_kernel(MergeArgs a, long long cap) {
+  pdl_wait();   // programmatic dependent launch: the previous kernel's results are visible
   const long long np = (long long)a.ctr->n_proposals;
   for (long long q = (long long)blockIdx.x * blockDim.x + threadIdx.x; q < cap;
        q += (long long)gridDim.x * blockDim.x) {
@@ -837,7 +848,7 @@ __global__ void flatten_kernel(MergeArgs a, long long cap) {
 
 cudaError_t launch_merge_flatten(const MergeArgs& a, long long cap, cudaStream_t s) {
   long long b = (cap + 255) / 256;
-  flatten_kernel<<<(unsigned)(b < 1 ? 1 : (b > 65535 ? 65535 : b)), 256, 0, s>>>(a, cap);
+  launch_k(flatten_kernel, (unsigned)(b < 1 ? 1 : (b > 65535 ? 65535 : b)), 256, 0, s, a, cap);
   return cudaGetLastError();
 }
 
@@ -880,6 +891,7 @@ struct GroupStartPolicy {
 #define ADPS_GROUP_MINB 6
 #endif
 __global__ void __launch_bounds__(128, ADPS_GROUP_MINB) group_small_kernel(MergeArgs a, long long cap) {
+  pdl_wait();   // programmatic dependent launch: the previous kernel's results are visible
   const long long G = (long long)a.ctr->n_groups_all;
   for (long long g = (long long)blockIdx.x * blockDim.x + threadIdx.x; g < cap;
        g += (long long)gridDim.x * blockDim.x) {
@@ -933,6 +945,7 @@ __global__ void __launch_bounds__(128, ADPS_GROUP_MINB) group_small_kernel(Merge
 
 // larger groups: one warp per group, lane-strided sums + butterfly
 __global__ void __launch_bounds__(256, (ADPS_GROUP_MINB + 1) / 2) group_kernel(MergeArgs a, long long cap) {
+  pdl_wait();   // programmatic dependent launch: the previous kernel's results are visible
   const int lane = threadIdx.x & 31;
   const long long warps = (long long)gridDim.x * (blockDim.x >> 5);
   const long long nl = (long long)a.ctr->n_mid_groups;
@@ -994,6 +1007,7 @@ __global__ void __launch_bounds__(256, (ADPS_GROUP_MINB + 1) / 2) group_kernel(M
 // the largest groups (a background Gaussian's proposals): a block per group,
 // thread-strided sums, fixed-order warp + block trees (deterministic)
 __global__ void __launch_bounds__(256) group_block_kernel(MergeArgs a, long long cap) {
+  pdl_wait();   // programmatic dependent launch: the previous kernel's results are visible
   __shared__ double red[8][12];
   __shared__ double bc[12];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -1075,10 +1089,10 @@ cudaError_t launch_merge_groups(const MergeArgs& a, long long cap, ScanState st,
     if ((e = cudaEventRecord(fork, s)) != cudaSuccess) return e;
     if ((e = cudaStreamWaitEvent(aux, fork, 0)) != cudaSuccess) return e;
   }
-  group_kernel<<<a.grid, 256, 0, s2>>>(a, cap);
-  group_block_kernel<<<a.grid, 256, 0, s2>>>(a, cap);
+  launch_k(group_kernel, a.grid, 256, 0, s2, a, cap);
+  launch_k(group_block_kernel, a.grid, 256, 0, s2, a, cap);
   long long b = (cap + 127) / 128;
-  group_small_kernel<<<(unsigned)(b < 1 ? 1 : (b > 65535 ? 65535 : b)), 128, 0, s>>>(a, cap);
+  launch_k(group_small_kernel, (unsigned)(b < 1 ? 1 : (b > 65535 ? 65535 : b)), 128, 0, s, a, cap);
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
   if (aux) {
     if ((e = cudaEventRecord(join, aux)) != cudaSuccess) return e;
@@ -1116,6 +1130,7 @@ __device__ __forceinline__ void cap_write(const MergeArgs& a, long long g, int k
 }
 
 __global__ void cap_small_kernel(MergeArgs a, long long cap) {
+  pdl_wait();   // programmatic dependent launch: the previous kernel's results are visible
   const long long G = (long long)a.ctr->n_groups_all;
   for (long long g = (long long)blockIdx.x * blockDim.x + threadIdx.x; g < G;
        g += (long long)gridDim.x * blockDim.x) {
@@ -1142,6 +1157,7 @@ __global__ void cap_small_kernel(MergeArgs a, long long cap) {
 }
 
 __global__ void __launch_bounds__(256) cap_large_kernel(MergeArgs a, long long cap) {
+  pdl_wait();   // programmatic dependent launch: the previous kernel's results are visible
   // a block per group of a parent with many groups: 1024 extents per round
   __shared__ int part[8];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -1190,6 +1206,7 @@ __global__ void __launch_bounds__(256) cap_large_kernel(MergeArgs a, long long c
 // themselves by (-extent, group order) and write their children.
 template <bool HUGE>
 __global__ void __launch_bounds__(HUGE ? 1024 : 256) cap_select_kernel(MergeArgs a, long long cap) {
+  pdl_wait();   // programmatic dependent launch: the previous kernel's results are visible
   constexpr int NT = HUGE ? 1024 : 256;   // threads
   constexpr int NW = NT / 32;
   constexpr int J = 8;            // consecutive groups per thread per round
@@ -1358,14 +1375,14 @@ cudaError_t launch_merge_cap(const MergeArgs& a, long long cap, cudaStream_t s, 
     if (e != cudaSuccess) return e;
     if ((e = cudaEventRecord(fork, s)) != cudaSuccess) return e;
     if ((e = cudaStreamWaitEvent(aux, fork, 0)) != cudaSuccess) return e;
-    cap_select_kernel<true><<<16, 1024, smem, aux>>>(a, cap);
+    launch_k(cap_select_kernel<true>, 16, 1024, smem, aux, a, cap);
     if ((e = cudaEventRecord(join, aux)) != cudaSuccess) return e;
-    cap_small_kernel<<<(unsigned)(b < 1 ? 1 : (b > 65535 ? 65535 : b)), 256, 0, s>>>(a, cap);
-    cap_select_kernel<false><<<a.grid, 256, 0, s>>>(a, cap);
+    launch_k(cap_small_kernel, (unsigned)(b < 1 ? 1 : (b > 65535 ? 65535 : b)), 256, 0, s, a, cap);
+    launch_k(cap_select_kernel<false>, a.grid, 256, 0, s, a, cap);
     if ((e = cudaStreamWaitEvent(s, join, 0)) != cudaSuccess) return e;
   } else {
-    cap_small_kernel<<<(unsigned)(b < 1 ? 1 : (b > 65535 ? 65535 : b)), 256, 0, s>>>(a, cap);
-    cap_large_kernel<<<a.grid * 4, 256, 0, s>>>(a, cap);
+    launch_k(cap_small_kernel, (unsigned)(b < 1 ? 1 : (b > 65535 ? 65535 : b)), 256, 0, s, a, cap);
+    launch_k(cap_large_kernel, a.grid * 4, 256, 0, s, a, cap);
   }
   return cudaGetLastError();
 }

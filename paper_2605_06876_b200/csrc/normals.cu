@@ -158,6 +158,7 @@ constexpr int kChunk = 32;   // stream positions per thread
 
 // 1. every position p = 1..window as an attempt start
 __global__ void classify_kernel(NormalsArgs a) {
+  pdl_wait();   // programmatic dependent launch: the previous kernel's results are visible
   const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   const long long start = 1 + t * kChunk;
   if (start > a.window) return;
@@ -217,6 +218,7 @@ __device__ __forceinline__ bool is_start(const NormalsArgs& a, long long p) {
 
 // 2. positions inside a multi-draw attempt: follow the chain from the starts
 __global__ void walk_kernel(NormalsArgs a) {
+  pdl_wait();   // programmatic dependent launch: the previous kernel's results are visible
   for (long long k = (long long)blockIdx.x * blockDim.x + threadIdx.x; k < a.window;
        k += (long long)gridDim.x * blockDim.x) {
     if (a.len[k] == 1) continue;
@@ -231,6 +233,7 @@ __global__ void walk_kernel(NormalsArgs a) {
 }
 
 __global__ void emit_flag_kernel(NormalsArgs a) {
+  pdl_wait();   // programmatic dependent launch: the previous kernel's results are visible
   for (long long k = (long long)blockIdx.x * blockDim.x + threadIdx.x; k < a.window;
        k += (long long)gridDim.x * blockDim.x)
     a.emit_idx[k] = ((is_start(a, k + 1) || a.walked[k]) && a.acc[k]) ? 1 : 0;
@@ -238,6 +241,7 @@ __global__ void emit_flag_kernel(NormalsArgs a) {
 
 // 3. the first n accepted attempts in stream order
 __global__ void write_kernel(NormalsArgs a) {
+  pdl_wait();   // programmatic dependent launch: the previous kernel's results are visible
   for (long long k = (long long)blockIdx.x * blockDim.x + threadIdx.x; k < a.window;
        k += (long long)gridDim.x * blockDim.x) {
     const bool emit = (is_start(a, k + 1) || a.walked[k]) && a.acc[k];
@@ -268,19 +272,19 @@ size_t normals_temp_bytes(long long window) {
 cudaError_t launch_normals(const NormalsArgs& a, void* temp, size_t temp_bytes, cudaStream_t s) {
   if (a.n <= 0) return cudaSuccess;
   const long long threads = (a.window + kChunk - 1) / kChunk;
-  classify_kernel<<<(unsigned)((threads + 127) / 128), 128, 0, s>>>(a);
+  launch_k(classify_kernel, (unsigned)((threads + 127) / 128), 128, 0, s, a);
   size_t tb = temp_bytes;
   cudaError_t e = cub::DeviceScan::InclusiveScan(temp, tb, a.reach, a.reach_max, MaxOp(), (int)a.window, s);
   if (e != cudaSuccess) return e;
   e = cudaMemsetAsync(a.walked, 0, (size_t)a.window, s);
   if (e != cudaSuccess) return e;
   const unsigned grid = (unsigned)((a.window + 255) / 256);
-  walk_kernel<<<grid, 256, 0, s>>>(a);
-  emit_flag_kernel<<<grid, 256, 0, s>>>(a);
+  launch_k(walk_kernel, grid, 256, 0, s, a);
+  launch_k(emit_flag_kernel, grid, 256, 0, s, a);
   tb = temp_bytes;
   e = cub::DeviceScan::ExclusiveSum(temp, tb, a.emit_idx, a.emit_idx, (int)a.window, s);
   if (e != cudaSuccess) return e;
-  write_kernel<<<grid, 256, 0, s>>>(a);
+  launch_k(write_kernel, grid, 256, 0, s, a);
   return cudaGetLastError();
 }
 

@@ -61,6 +61,7 @@ __device__ __forceinline__ void sh_eval_rgb(const float* dc, const float* rest, 
 // the view-independent part of the projection, once per render call: the 3D
 // covariance R diag(s^2) R^T (fp64) and, at SH degree 0, the colour
 __global__ void splat3d_kernel(PreArgs a, double* __restrict__ cov3, float* __restrict__ rgb0) {
+  pdl_wait();   // programmatic dependent launch: the previous kernel's results are visible
   const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= a.n) return;
   double q[4] = {a.rot[4 * i], a.rot[4 * i + 1], a.rot[4 * i + 2], a.rot[4 * i + 3]};
@@ -81,11 +82,12 @@ __global__ void splat3d_kernel(PreArgs a, double* __restrict__ cov3, float* __re
 }
 
 cudaError_t launch_splat3d(const PreArgs& a, double* cov3, float* rgb0, cudaStream_t s) {
-  if (a.n > 0) splat3d_kernel<<<(unsigned)((a.n + 255) / 256), 256, 0, s>>>(a, cov3, rgb0);
+  if (a.n > 0) launch_k(splat3d_kernel, (unsigned)((a.n + 255) / 256), 256, 0, s, a, cov3, rgb0);
   return cudaGetLastError();
 }
 
 __global__ void preprocess_kernel(PreArgs a) {
+  pdl_wait();   // programmatic dependent launch: the previous kernel's results are visible
   const long long i0 = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   const bool in_range = i0 < a.n;
   const long long i = in_range ? i0 : a.n - 1;   // out-of-range lanes recompute the last one, write nothing
@@ -281,6 +283,7 @@ __device__ __forceinline__ float ex2_ftz(float x) {
 // skipped (pixel, splat) pair has alpha below 1/255 and would be skipped anyway.
 template <bool STATS, bool EPI>
 __global__ void __launch_bounds__(kRThreads) blend_kernel(BlendArgs a) {
+  pdl_wait();   // programmatic dependent launch: the previous kernel's results are visible
   struct Sm {
     float mx, my, A, B, C, o, r, g, b;
     int idx;
@@ -408,6 +411,7 @@ __global__ void __launch_bounds__(kRThreads) blend_kernel(BlendArgs a) {
 constexpr int kFixupMax = 256;
 __global__ void depth_fixup_kernel(const unsigned* __restrict__ k32, int* __restrict__ order,
                                    const unsigned long long* __restrict__ z64, long long n, int* flag) {
+  pdl_wait();   // programmatic dependent launch: the previous kernel's results are visible
   const long long s = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (s >= n) return;
   const unsigned k = k32[s];
@@ -439,6 +443,7 @@ __global__ void depth_fixup_kernel(const unsigned* __restrict__ k32, int* __rest
 // keys (sorted last) up to the capacity the host sorts; a view whose pairs
 // exceed the capacity is flagged and skipped (rendered again by the host)
 __global__ void __launch_bounds__(256) duplicate_kernel(DupArgs a) {
+  pdl_wait();   // programmatic dependent launch: the previous kernel's results are visible
   constexpr unsigned FULL = 0xffffffffu;
   const long long s = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   const unsigned long long total = *a.total;
@@ -480,6 +485,7 @@ __global__ void __launch_bounds__(256) duplicate_kernel(DupArgs a) {
 
 __global__ void tile_ranges_kernel(const unsigned long long* keys, const unsigned long long* total, const int* flag,
                                    int* start, int* end) {
+  pdl_wait();   // programmatic dependent launch: the previous kernel's results are visible
   const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   const long long n = (long long)*total;
   if (i >= n || *flag) return;
@@ -490,7 +496,7 @@ __global__ void tile_ranges_kernel(const unsigned long long* keys, const unsigne
 
 // ---------------------------------------------------------------- launchers
 cudaError_t launch_preprocess(const PreArgs& a, cudaStream_t s) {
-  if (a.n > 0) preprocess_kernel<<<(unsigned)((a.n + 255) / 256), 256, 0, s>>>(a);
+  if (a.n > 0) launch_k(preprocess_kernel, (unsigned)((a.n + 255) / 256), 256, 0, s, a);
   return cudaGetLastError();
 }
 
@@ -502,19 +508,19 @@ cudaError_t launch_tile_count_scan(const int* order, const unsigned* tiles, unsi
 
 cudaError_t launch_duplicate(const DupArgs& a, cudaStream_t s) {
   const long long m = a.n > a.cap ? a.n : a.cap;
-  if (m > 0) duplicate_kernel<<<(unsigned)((m + 255) / 256), 256, 0, s>>>(a);
+  if (m > 0) launch_k(duplicate_kernel, (unsigned)((m + 255) / 256), 256, 0, s, a);
   return cudaGetLastError();
 }
 
 cudaError_t launch_tile_ranges(const unsigned long long* keys, long long cap, const unsigned long long* total,
                                const int* flag, int* start, int* end, cudaStream_t s) {
-  if (cap > 0) tile_ranges_kernel<<<(unsigned)((cap + 255) / 256), 256, 0, s>>>(keys, total, flag, start, end);
+  if (cap > 0) launch_k(tile_ranges_kernel, (unsigned)((cap + 255) / 256), 256, 0, s, keys, total, flag, start, end);
   return cudaGetLastError();
 }
 
 cudaError_t launch_depth_fixup(const unsigned* k32, int* order, const unsigned long long* z64, long long n, int* flag,
                                cudaStream_t s) {
-  if (n > 0) depth_fixup_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(k32, order, z64, n, flag);
+  if (n > 0) launch_k(depth_fixup_kernel, (unsigned)((n + 255) / 256), 256, 0, s, k32, order, z64, n, flag);
   return cudaGetLastError();
 }
 
@@ -522,6 +528,7 @@ cudaError_t launch_depth_fixup(const unsigned* k32, int* order, const unsigned l
 // doubles order as unsigned integers; an empty tile holds +inf / 0)
 __global__ void __launch_bounds__(256) reduce_tile_minmax_kernel(const unsigned long long* __restrict__ tiles,
                                                                  int n_tiles, unsigned long long* __restrict__ lohi) {
+  pdl_wait();   // programmatic dependent launch: the previous kernel's results are visible
   const int v = blockIdx.x;
   const unsigned long long* t = tiles + 2ll * n_tiles * v;
   unsigned long long lo = ~0ull, hi = 0ull;
@@ -551,17 +558,17 @@ __global__ void __launch_bounds__(256) reduce_tile_minmax_kernel(const unsigned 
 
 cudaError_t launch_reduce_tile_minmax(const unsigned long long* tiles, int n_tiles, int n_views,
                                       unsigned long long* lohi, cudaStream_t s) {
-  reduce_tile_minmax_kernel<<<n_views, 256, 0, s>>>(tiles, n_tiles, lohi);
+  launch_k(reduce_tile_minmax_kernel, n_views, 256, 0, s, tiles, n_tiles, lohi);
   return cudaGetLastError();
 }
 
 cudaError_t launch_blend(const BlendArgs& a, int n_tiles, cudaStream_t s) {
   if (a.weight || a.contrib)
-    blend_kernel<true, false><<<n_tiles, kRThreads, 0, s>>>(a);
+    launch_k(blend_kernel<true, false>, n_tiles, kRThreads, 0, s, a);
   else if (a.gt)
-    blend_kernel<false, true><<<n_tiles, kRThreads, 0, s>>>(a);
+    launch_k(blend_kernel<false, true>, n_tiles, kRThreads, 0, s, a);
   else
-    blend_kernel<false, false><<<n_tiles, kRThreads, 0, s>>>(a);
+    launch_k(blend_kernel<false, false>, n_tiles, kRThreads, 0, s, a);
   return cudaGetLastError();
 }
 

@@ -30,6 +30,7 @@ struct ScanState {
 //   __device__ void total(unsigned long long t) const;   // called once by the last tile
 template <class Policy>
 __global__ void __launch_bounds__(kScanThreads) scan_kernel(Policy pol, long long n, ScanState st) {
+  pdl_wait();   // programmatic dependent launch: the previous kernel's results are visible
   __shared__ unsigned long long sv[kScanTile];
   __shared__ unsigned long long warp_sums[kScanThreads / kWarp];
   __shared__ unsigned long long s_prefix;
@@ -180,7 +181,7 @@ inline cudaError_t launch_scan(const Policy& pol, long long n, ScanState st, cud
   if (e != cudaSuccess) return e;
   e = cudaMemsetAsync(st.ticket, 0, sizeof(unsigned int), s);
   if (e != cudaSuccess) return e;
-  scan_kernel<Policy><<<(unsigned)tiles, kScanThreads, 0, s>>>(pol, n, st);
+  launch_k(scan_kernel<Policy>, (unsigned)tiles, kScanThreads, 0, s, pol, n, st);
   return cudaGetLastError();
 }
 

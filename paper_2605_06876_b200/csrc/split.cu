@@ -60,6 +60,7 @@ cudaError_t launch_select(const SelectArgs& a, ScanState st, cudaStream_t s) {
 
 // the classes alone (elementwise, HBM-bound): the input pass needs only them
 __global__ void classify_select_kernel(SelectArgs a) {
+  pdl_wait();   // programmatic dependent launch: the previous kernel's results are visible
   for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < a.n; i += (long long)gridDim.x * blockDim.x)
     a.cls[i] = select_class(a, i);
 }
@@ -67,7 +68,7 @@ __global__ void classify_select_kernel(SelectArgs a) {
 cudaError_t launch_select_split(const SelectArgs& a, ScanState st, cudaStream_t s, cudaStream_t aux, cudaEvent_t fork,
                                 cudaEvent_t join) {
   long long b = (a.n + 255) / 256;
-  classify_select_kernel<<<(unsigned)(b < 1 ? 1 : (b > 65535 ? 65535 : b)), 256, 0, s>>>(a);
+  launch_k(classify_select_kernel, (unsigned)(b < 1 ? 1 : (b > 65535 ? 65535 : b)), 256, 0, s, a);
   cudaError_t e = cudaGetLastError();
   if (e == cudaSuccess) e = cudaEventRecord(fork, s);
   if (e == cudaSuccess) e = cudaStreamWaitEvent(aux, fork, 0);
@@ -87,6 +88,7 @@ __device__ __forceinline__ double sclip(double x, double a) {
 #define ADPS_CHILD_MINB 6
 #endif
 __global__ void __launch_bounds__(128, ADPS_CHILD_MINB) child_init_kernel(ChildArgs a) {
+  pdl_wait();   // programmatic dependent launch: the previous kernel's results are visible
   long long n = (long long)*a.n_regions;
   if (n > a.region_cap) n = a.region_cap;
   for (long long rid = (long long)blockIdx.x * blockDim.x + threadIdx.x; rid < n;
@@ -234,6 +236,7 @@ __global__ void __launch_bounds__(128, ADPS_CHILD_MINB) child_init_kernel(ChildA
 __global__ void region_keys_kernel(const RegionRec* __restrict__ regions, long long n, const int* __restrict__ cand_rank,
                                    int bits_v, int bits_b, int bits_p, unsigned long long* __restrict__ keys,
                                    int* __restrict__ vals) {
+  pdl_wait();   // programmatic dependent launch: the previous kernel's results are visible
   for (long long rid = (long long)blockIdx.x * blockDim.x + threadIdx.x; rid < n; rid += (long long)gridDim.x * blockDim.x) {
     const RegionRec& R = regions[rid];
     const unsigned long long rank = (unsigned long long)cand_rank[R.cand];
@@ -246,18 +249,19 @@ __global__ void region_keys_kernel(const RegionRec* __restrict__ regions, long l
 cudaError_t launch_region_keys(const RegionRec* regions, long long n, const int* cand_rank, int bits_v, int bits_b,
                                int bits_p, unsigned long long* keys, int* vals, cudaStream_t s) {
   long long b = (n + 255) / 256;
-  region_keys_kernel<<<(unsigned)(b < 1 ? 1 : (b > 65535 ? 65535 : b)), 256, 0, s>>>(regions, n, cand_rank, bits_v,
+  launch_k(region_keys_kernel, (unsigned)(b < 1 ? 1 : (b > 65535 ? 65535 : b)), 256, 0, s, regions, n, cand_rank, bits_v,
                                                                                      bits_b, bits_p, keys, vals);
   return cudaGetLastError();
 }
 
 cudaError_t launch_child_init(const ChildArgs& a, cudaStream_t s) {
-  child_init_kernel<<<a.grid, 128, 0, s>>>(a);
+  launch_k(child_init_kernel, a.grid, 128, 0, s, a);
   return cudaGetLastError();
 }
 
 // ============================================================ ranges
 __global__ void ranges_kernel(RangeArgs a) {
+  pdl_wait();   // programmatic dependent launch: the previous kernel's results are visible
   // keys are sorted, so one candidate's (and one (candidate, view)'s) regions are
   // adjacent: counts are aggregated per warp (match_any) before the atomics, which
   // keeps a parent with tens of thousands of regions from serialising on one word
@@ -287,7 +291,7 @@ __global__ void ranges_kernel(RangeArgs a) {
 }
 
 cudaError_t launch_ranges(const RangeArgs& a, cudaStream_t s) {
-  if (a.n > 0) ranges_kernel<<<a.grid, 256, 0, s>>>(a);
+  if (a.n > 0) launch_k(ranges_kernel, a.grid, 256, 0, s, a);
   return cudaGetLastError();
 }
 
@@ -441,6 +445,7 @@ __device__ __forceinline__ void copy_survivor_components(const EmitArgs& a, cons
 }
 
 __global__ void __launch_bounds__(kEmitThreads) emit_survivors_kernel(EmitArgs a) {
+  pdl_wait();   // programmatic dependent launch: the previous kernel's results are visible
   switch (blockIdx.y) {
     case 0: copy_survivor_components<3>(a, a.g.mu, a.mu, false); break;
     case 1: copy_survivor_components<3>(a, a.g.scale, a.scale, false); break;
@@ -461,6 +466,7 @@ __global__ void __launch_bounds__(kEmitThreads) emit_survivors_kernel(EmitArgs a
 }
 
 __global__ void __launch_bounds__(kEmitThreads) emit_kernel(EmitArgs a, long long b_ins) {
+  pdl_wait();   // programmatic dependent launch: the previous kernel's results are visible
   const long long blk = blockIdx.x;
   long long n_keep = a.n_keep, n_inserted = a.n_inserted;
   bool capped = false;
@@ -519,14 +525,14 @@ cudaError_t launch_emit(const EmitArgs& a, cudaStream_t s, cudaStream_t aux, cud
     const cudaStream_t ss = two ? aux : s;
     // 8 components per thread (rot's 4 per Gaussian the widest; narrower arrays exit early)
     long long b = (a.n * 4 + 8ll * kEmitThreads - 1) / (8ll * kEmitThreads);
-    emit_survivors_kernel<<<dim3((unsigned)b, a.g.sh_k > 0 ? 6u : 5u), kEmitThreads, 0, ss>>>(a);
+    launch_k(emit_survivors_kernel, dim3((unsigned)b, a.g.sh_k > 0 ? 6u : 5u), kEmitThreads, 0, ss, a);
   }
   const long long b_ins = ((a.dev_keep ? a.n_ins_max : a.n_inserted) + kEmitThreads - 1) / kEmitThreads;
   const long long b_clone = (a.n_clone + kEmitThreads - 1) / kEmitThreads;
   EmitArgs a2 = a;
   a2.b_off = a.insert_offset ? (a.n_split + kEmitThreads - 1) / kEmitThreads : 0;
   if (b_ins + a2.b_off + b_clone > 0)
-    emit_kernel<<<(unsigned)(b_ins + a2.b_off + b_clone), kEmitThreads, 0, s>>>(a2, b_ins);
+    launch_k(emit_kernel, (unsigned)(b_ins + a2.b_off + b_clone), kEmitThreads, 0, s, a2, b_ins);
   cudaError_t e = cudaGetLastError();
   if (e == cudaSuccess && two) {
     e = cudaEventRecord(join, aux);
@@ -538,6 +544,7 @@ cudaError_t launch_emit(const EmitArgs& a, cudaStream_t s, cudaStream_t aux, cud
 // ============================================================ vanilla_densify / remaps
 __global__ void vanilla_cases_kernel(int* cand_case, int* cand_ins, int* cand_merged,
                                      const unsigned long long* n_split, int n_children) {
+  pdl_wait();   // programmatic dependent launch: the previous kernel's results are visible
   const long long n = (long long)*n_split;
   for (long long k = (long long)blockIdx.x * blockDim.x + threadIdx.x; k < n; k += (long long)gridDim.x * blockDim.x) {
     cand_case[k] = ADPS_CASE_FALLBACK;
@@ -548,12 +555,13 @@ __global__ void vanilla_cases_kernel(int* cand_case, int* cand_ins, int* cand_me
 
 cudaError_t launch_vanilla_cases(int* cand_case, int* cand_ins, int* cand_merged, const unsigned long long* n_split,
                                  int n_children, cudaStream_t s) {
-  vanilla_cases_kernel<<<148 * 4, 256, 0, s>>>(cand_case, cand_ins, cand_merged, n_split, n_children);
+  launch_k(vanilla_cases_kernel, 148 * 4, 256, 0, s, cand_case, cand_ins, cand_merged, n_split, n_children);
   return cudaGetLastError();
 }
 
 __global__ void reset_flags_kernel(unsigned char* flags, long long n, const int* split_list, const int* cand_case,
                                    long long n_split, const int* clone_list, long long n_clone, bool clones) {
+  pdl_wait();   // programmatic dependent launch: the previous kernel's results are visible
   const long long total = n_split + (clones ? n_clone : 0);
   for (long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x; t < total;
        t += (long long)gridDim.x * blockDim.x) {
@@ -571,7 +579,7 @@ cudaError_t launch_reset_flags(unsigned char* flags, long long n, const int* spl
   cudaError_t e = cudaMemsetAsync(flags, 0, (size_t)(n > 0 ? n : 1), s);
   if (e != cudaSuccess) return e;
   if (n_split + n_clone > 0)
-    reset_flags_kernel<<<148 * 4, 256, 0, s>>>(flags, n, split_list, cand_case, n_split, clone_list, n_clone, clones);
+    launch_k(reset_flags_kernel, 148 * 4, 256, 0, s, flags, n, split_list, cand_case, n_split, clone_list, n_clone, clones);
   return cudaGetLastError();
 }
 
@@ -580,6 +588,7 @@ cudaError_t launch_reset_flags(unsigned char* flags, long long n, const int* spl
 __global__ void remap_rows_kernel(const long long* __restrict__ index_map, long long n_out,
                                   const unsigned char* __restrict__ zero_old, const unsigned* __restrict__ in,
                                   long long row_words, unsigned* __restrict__ out) {
+  pdl_wait();   // programmatic dependent launch: the previous kernel's results are visible
   const long long total = n_out * row_words;
   for (long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x; t < total;
        t += (long long)gridDim.x * blockDim.x) {
@@ -596,7 +605,7 @@ cudaError_t launch_remap_rows(const long long* index_map, long long n_out, const
   if (words > 0) {
     long long b = (words + 255) / 256;
     if (b > 148 * 32) b = 148 * 32;
-    remap_rows_kernel<<<(unsigned)b, 256, 0, s>>>(index_map, n_out, zero_old, (const unsigned*)in, row_bytes / 4,
+    launch_k(remap_rows_kernel, (unsigned)b, 256, 0, s, index_map, n_out, zero_old, (const unsigned*)in, row_bytes / 4,
                                                  (unsigned*)out);
   }
   return cudaGetLastError();
@@ -621,6 +630,7 @@ template <class T>
 __global__ void __launch_bounds__(256) accumulate_kernel(double* __restrict__ ga, double* __restrict__ den,
                                                          const T* __restrict__ vg,
                                                          const unsigned char* __restrict__ vis, long long n) {
+  pdl_wait();   // programmatic dependent launch: the previous kernel's results are visible
   const long long n2 = n >> 1;
   for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n2;
        i += (long long)gridDim.x * blockDim.x) {
@@ -661,6 +671,7 @@ template <class T>
 __global__ void __launch_bounds__(256) accumulate1_kernel(double* __restrict__ ga, double* __restrict__ den,
                                                           const T* __restrict__ vg,
                                                           const unsigned char* __restrict__ vis, long long n) {
+  pdl_wait();   // programmatic dependent launch: the previous kernel's results are visible
   for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
        i += (long long)gridDim.x * blockDim.x) {
     if (!__ldg(vis + i)) continue;
@@ -677,12 +688,12 @@ static cudaError_t launch_accumulate_t(double* ga, double* den, const T* vg, con
   if (n > 0 && !aligned) {
     long long blocks = (n + 255) / 256;
     if (blocks > 148 * 16) blocks = 148 * 16;
-    accumulate1_kernel<T><<<(unsigned)blocks, 256, 0, s>>>(ga, den, vg, vis, n);
+    launch_k(accumulate1_kernel<T>, (unsigned)blocks, 256, 0, s, ga, den, vg, vis, n);
   } else if (n > 0) {
     long long blocks = (n / 2 + 255) / 256;
     if (blocks > 148 * 16) blocks = 148 * 16;
     if (blocks < 1) blocks = 1;
-    accumulate_kernel<T><<<(unsigned)blocks, 256, 0, s>>>(ga, den, vg, vis, n);
+    launch_k(accumulate_kernel<T>, (unsigned)blocks, 256, 0, s, ga, den, vg, vis, n);
   }
   return cudaGetLastError();
 }

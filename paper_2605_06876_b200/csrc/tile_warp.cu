@@ -483,6 +483,7 @@ __device__ __forceinline__ void tile_warp_body(const TileParams& P, WarpSmem& S,
 
 template <int R, bool RAW>
 __global__ void __launch_bounds__(kWarpsPerBlock * 32, ADPS_TW_MINBLOCKS) tile_warp_kernel(TileParams P, long long t0, long long t1) {
+  pdl_wait();   // programmatic dependent launch: the previous kernel's results are visible
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   WarpSmem& S = reinterpret_cast<WarpSmem*>(smem_raw)[wid];
@@ -533,6 +534,7 @@ __global__ void __launch_bounds__(256) tile_words_kernel(const raw16_t* __restri
                                                          const unsigned* __restrict__ cand_bits,
                                                          const double* __restrict__ thr_raw, int L, int H, int W,
                                                          int WW, int v0, uint4* __restrict__ words) {
+  pdl_wait();   // programmatic dependent launch: the previous kernel's results are visible
   // one warp per image row, lane = x within a 32-column word, U words in flight
   const int v = v0 + blockIdx.y;
   const int y = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
@@ -629,6 +631,7 @@ __global__ void __launch_bounds__(kTwWarps * 32) tile_words_t_kernel(const raw16
                                                                     const unsigned* __restrict__ cand_bits,
                                                                     const double* __restrict__ thr_raw, int L, int H,
                                                                     int W, int WW, int v0, uint4* __restrict__ words) {
+  pdl_wait();   // programmatic dependent launch: the previous kernel's results are visible
   __shared__ int tile[kTwWarps][32][33];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const int v = v0 + blockIdx.z;
@@ -1024,6 +1027,7 @@ __device__ __forceinline__ void tile_bits_body(const TileParams& P, const uint4*
 template <int R, bool FUSED>
 __global__ void __launch_bounds__(kWarpsPerBlock * 32, ADPS_TW_MINBLOCKS)
     tile_bits_kernel(TileParams P, const uint4* __restrict__ words, int WW, long long t0, long long t1) {
+  pdl_wait();   // programmatic dependent launch: the previous kernel's results are visible
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   WarpSmem& S = reinterpret_cast<WarpSmem*>(smem_raw)[wid];
@@ -1037,6 +1041,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, ADPS_TW_MINBLOCKS)
 template <int R, bool FUSED>
 __global__ void __launch_bounds__(kBigWarpsPerBlock * 32)
     tile_bits_deferred_kernel(TileParams P, const uint4* __restrict__ words, int WW) {
+  pdl_wait();   // programmatic dependent launch: the previous kernel's results are visible
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   WarpSmemT<kTileMaxRuns>& S = reinterpret_cast<WarpSmemT<kTileMaxRuns>*>(smem_raw)[wid];
@@ -1056,7 +1061,7 @@ static cudaError_t launch_bits_r(const TileParams& P, int WW, long long t0, long
   cudaError_t e = cudaFuncSetAttribute(tile_bits_kernel<R, FUSED>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   const long long blocks = (t1 - t0 + kWarpsPerBlock - 1) / kWarpsPerBlock;
-  if (blocks > 0) tile_bits_kernel<R, FUSED><<<(unsigned)blocks, kWarpsPerBlock * 32, smem, s>>>(P, P.words, WW, t0, t1);
+  if (blocks > 0) launch_k(tile_bits_kernel<R, FUSED>, (unsigned)blocks, kWarpsPerBlock * 32, smem, s, P, P.words, WW, t0, t1);
   return cudaGetLastError();
 }
 
@@ -1069,11 +1074,11 @@ cudaError_t launch_tile_bits(const TileParams& P, int v0, int v1, cudaStream_t s
   if (!fused) {
 #if ADPS_TW_ROWWISE
     const unsigned gx = (unsigned)((P.H + 7) / 8);   // warp per image row, 8 rows per block
-    tile_words_kernel<<<dim3(gx, (unsigned)(v1 - v0)), 256, 0, s>>>(P.rawf, P.image, P.gt, P.cand_bits, P.thr_raw,
+    launch_k(tile_words_kernel, dim3(gx, (unsigned)(v1 - v0)), 256, 0, s, P.rawf, P.image, P.gt, P.cand_bits, P.thr_raw,
                                                                      P.L, P.H, P.W, WW, v0, P.words);
 #else
     const dim3 g((unsigned)((WW + kTwWarps - 1) / kTwWarps), (unsigned)((P.H + 31) / 32), (unsigned)(v1 - v0));
-    tile_words_t_kernel<<<g, kTwWarps * 32, 0, s>>>(P.rawf, P.image, P.gt, P.cand_bits, P.thr_raw, P.L, P.H, P.W, WW,
+    launch_k(tile_words_t_kernel, g, kTwWarps * 32, 0, s, P.rawf, P.image, P.gt, P.cand_bits, P.thr_raw, P.L, P.H, P.W, WW,
                                                     v0, P.words);
 #endif
   }
@@ -1093,7 +1098,7 @@ static cudaError_t launch_deferred_r(const TileParams& P, int WW, unsigned block
   cudaError_t e = cudaFuncSetAttribute(tile_bits_deferred_kernel<R, FUSED>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)smem);
   if (e != cudaSuccess) return e;
-  tile_bits_deferred_kernel<R, FUSED><<<blocks, kBigWarpsPerBlock * 32, smem, s>>>(P, P.words, WW);
+  launch_k(tile_bits_deferred_kernel<R, FUSED>, blocks, kBigWarpsPerBlock * 32, smem, s, P, P.words, WW);
   return cudaGetLastError();
 }
 
@@ -1115,7 +1120,7 @@ static cudaError_t launch_r(const TileParams& P, long long t0, long long t1, cud
   if (e != cudaSuccess) return e;
   const long long blocks = (t1 - t0 + kWarpsPerBlock - 1) / kWarpsPerBlock;
   if (blocks <= 0) return cudaSuccess;
-  tile_warp_kernel<R, RAW><<<(unsigned)blocks, kWarpsPerBlock * 32, smem, s>>>(P, t0, t1);
+  launch_k(tile_warp_kernel<R, RAW>, (unsigned)blocks, kWarpsPerBlock * 32, smem, s, P, t0, t1);
   return cudaGetLastError();
 }
 
