@@ -214,31 +214,28 @@ struct TileCountPolicy {
 // computes it (fp64, numpy order: (|d0| + |d1|) + |d2|, no contraction);
 // per-view min/max by a block reduction and two atomics, the candidate bit
 // by one atomicOr per (warp, word), the ever-dominant flag per candidate.
-__device__ __forceinline__ void render_epilogue(const BlendArgs& a, bool inside, int y, int x, float i0, float i1,
-                                                float i2, int bi) {
-  __shared__ double s_lo[kRThreads / 32], s_hi[kRThreads / 32];
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  double lo = INFINITY, hi = 0.0;
+// the per-pixel part: raw error -> 16-bit cache, ever-dominant flag, the
+// candidate bits of the warp's four 8-pixel row segments (lanes 8r .. 8r + 7
+// = one row: the layout of both blend kernels), the running min/max
+__device__ __forceinline__ void epi_pixel(const BlendArgs& a, bool inside, int y, int x, float i0, float i1,
+                                          float i2, int bi, double& lo, double& hi) {
+  const int lane = threadIdx.x & 31;
   bool cand = false;
-  long long p = 0;
   if (inside) {
-    p = (long long)y * a.W + x;
+    const long long p = (long long)y * a.W + x;
     const float* g3 = a.gt + 3 * p;
     const double r = __dadd_rn(__dadd_rn(fabs(__dsub_rn((double)i0, (double)g3[0])),
                                          fabs(__dsub_rn((double)i1, (double)g3[1]))),
                                fabs(__dsub_rn((double)i2, (double)g3[2])));
     a.rawf[p] = raw16(r);
-    lo = r;
-    hi = r;
+    lo = fmin(lo, r);
+    hi = fmax(hi, r);
     if (bi >= 0 && bi < a.N && __ldg(a.cls + bi) == 1) {
       cand = true;
       if (a.dom_flag[bi] == 0) a.dom_flag[bi] = 1;
     }
   }
-  // candidate bits: a warp holds four 8-pixel row segments of the tile (lanes
-  // 8r .. 8r + 7 = row r of its 8 x 4 block); each segment's 8 bits land in one
-  // or two 32-bit words
-  static_assert(kRTile == 16 && kRThreads == 256, "epilogue: a warp = an 8 x 4 pixel block");
+  static_assert(kRTile == 16, "epilogue: 8-pixel row segments");
   const unsigned b = __ballot_sync(0xffffffffu, cand);
   if ((lane & 7) == 0 && y < a.H) {   // the first pixel of its segment (x may be >= W)
     const long long p0 = (long long)y * a.W + x;
@@ -249,6 +246,14 @@ __device__ __forceinline__ void render_epilogue(const BlendArgs& a, bool inside,
       if ((unsigned)(w >> 32)) atomicOr(a.cand_bits + (p0 >> 5) + 1, (unsigned)(w >> 32));
     }
   }
+}
+
+// the tile's min/max into its own slot (no same-address atomics: 4k tiles per
+// view); reduce_tile_minmax folds them per view before the thresholds
+template <int NW>
+__device__ __forceinline__ void epi_reduce(const BlendArgs& a, double lo, double hi) {
+  __shared__ double s_lo[NW], s_hi[NW];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   for (int o = 16; o > 0; o >>= 1) {
     lo = fmin(lo, __shfl_xor_sync(0xffffffffu, lo, o));
     hi = fmax(hi, __shfl_xor_sync(0xffffffffu, hi, o));
@@ -259,15 +264,20 @@ __device__ __forceinline__ void render_epilogue(const BlendArgs& a, bool inside,
   }
   __syncthreads();
   if (threadIdx.x == 0) {
-    for (int w = 1; w < kRThreads / 32; ++w) {
+    for (int w = 1; w < NW; ++w) {
       lo = fmin(lo, s_lo[w]);
       hi = fmax(hi, s_hi[w]);
     }
-    // this tile's min/max into its own slot (no same-address atomics: 4k tiles
-    // per view); reduce_tile_minmax folds them per view before the thresholds
     a.lohi[2 * blockIdx.x + 0] = (unsigned long long)__double_as_longlong(lo);
     a.lohi[2 * blockIdx.x + 1] = (unsigned long long)__double_as_longlong(hi);
   }
+}
+
+__device__ __forceinline__ void render_epilogue(const BlendArgs& a, bool inside, int y, int x, float i0, float i1,
+                                                float i2, int bi) {
+  double lo = INFINITY, hi = 0.0;
+  epi_pixel(a, inside, y, x, i0, i1, i2, bi, lo, hi);
+  epi_reduce<kRThreads / 32>(a, lo, hi);
 }
 
 __device__ __forceinline__ float ex2_ftz(float x) {

@@ -34,4 +34,6 @@ for fast in (False, True, False, True):
         ref = (img.clone(), dom.clone())
     else:
         same = bool(torch.equal(img, ref[0]) and torch.equal(dom, ref[1]))
-    print(f"fast={fast} ms/view={min(ts):.4f} (runs {', '.join(f'{t:.4f}' for t in ts)}) identical={same}")
+    import hashlib
+    h = hashlib.md5(img.cpu().numpy().tobytes() + dom.cpu().numpy().tobytes()).hexdigest()[:12]
+    print(f"fast={fast} ms/view={min(ts):.4f} (runs {', '.join(f'{t:.4f}' for t in ts)}) identical={same} md5={h}")
