@@ -307,6 +307,39 @@ def time_accumulate(dev, n, peak, launches=10):
             "note": "one launch per view, fp32 viewspace grads, L2 flushed before each launch"}
 
 
+def time_accumulate_sharded(dev, n, n_views, world, rank, peak, max_over_ranks):
+    """The sharded stat feed (sharded.accumulate_stats_sharded_): each rank
+    accumulates its block of the n_views training views (fp32 viewspace
+    gradients, one kernel per view) and one all_reduce(SUM) of the [2,n] fp64
+    partials combines them.  Timed with events, max over ranks."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2605_06876_b200 import sharded as SH
+    gen = torch.Generator(device=dev).manual_seed(rank)
+    ga = torch.zeros(n, dtype=torch.float64, device=dev)
+    den = torch.zeros(n, dtype=torch.float64, device=dev)
+    vg = torch.randn(n, 2, device=dev, generator=gen)
+    vis = torch.rand(n, device=dev, generator=gen) < 0.7
+    lo, hi = SH.view_block(n_views, world, rank)
+    views = [(vg, vis)] * (hi - lo)
+    SH.accumulate_stats_sharded_(ga, den, views)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    reps = 5
+    torch.cuda.synchronize(dev)
+    dist.barrier()
+    e0.record()
+    for _ in range(reps):
+        SH.accumulate_stats_sharded_(ga, den, views)
+    e1.record()
+    torch.cuda.synchronize(dev)
+    ms = max_over_ranks(e0.elapsed_time(e1) / reps)
+    gbs = 41.0 * n * n_views / (ms * 1e-3) / 1e9
+    return {"ms_per_feed": ms, "views": n_views, "n": n, "GB/s": gbs, "frac_of_world_peak": gbs / (peak * world),
+            "allreduce_bytes": 16 * n,
+            "note": "per rank its block of views, one kernel per view, one all_reduce(SUM) of the [2,n] fp64 partials"}
+
+
 def parity_on_sample(op, plan, wl, d, vs, cfg_k):
     """The GPU step and the oracle step on the same k sampled views (stage-isolated:
     the same GPU attribution into both); every integer output compared, near-
@@ -470,6 +503,12 @@ def run_ours(args, wl):
     traffic = load_traffic(wl.name)
     b_step = BYTES_PER_PX * px + BYTES_PER_G_IN * g.n + BYTES_PER_G_OUT * counts["n_out"]
     acc = time_accumulate(dev, g.n, peak) if rank == 0 else None
+    acc_sh = None
+    if world > 1:   # the sharded stat feed: views over ranks, one all_reduce
+        try:
+            acc_sh = time_accumulate_sharded(dev, g.n, len(view_ids), world, rank, peak, max_over_ranks)
+        except Exception as exc:   # reported, never fatal for the bench line
+            acc_sh = {"error": repr(exc)[:200]}
 
     # ---- K1-epilogue variant (reported separately): the render's
     #      epilogue runs select and the input pass, the step starts from the
@@ -594,6 +633,7 @@ def run_ours(args, wl):
             "stat_accum": {"GB/s": BYTES_PER_PX * px_local / (attr_ms * 1e-3) / 1e9 if attr_ms else None,
                            "frac": None, "ms": attr_ms},
             "accumulate_stats": acc,
+            "accumulate_stats_sharded": acc_sh,
             "step_roofline": {"bytes": int(b_step), "GB/s": b_step / (ms * 1e-3) / 1e9,
                               "frac": b_step / (ms * 1e-3) / 1e9 / peak},
             "roofline": {"bound": "hbm", "kernel": "minmax2_kernel (input pass: raw L1 error, per-view min/max, "

@@ -27,6 +27,10 @@ SURVEY.md 8(e), following the path's own data dependencies:
   rank over identical inputs -- every rank ends with the identical grown
   arrays (what the next data-parallel training step needs).
 
+  Stat feed.  accumulate_stats_sharded_ shards the per-view accumulation of
+  the training's DensifyStats (ref/adc.py:73-79) over views and sums the
+  per-rank partials with one all_reduce(SUM) of a [2,N] fp64 buffer.
+
 The orchestration is written against a small executor interface so that the
 same code drives the CUDA plan (GpuExecutor) and, in the CPU tests, a
 stand-in executor built on the oracle (tests/test_sharded.py, gloo, world 2).
@@ -82,6 +86,39 @@ def all_reduce_max_(t: torch.Tensor, group=None) -> torch.Tensor:
     dist.all_reduce(h, op=dist.ReduceOp.MAX, group=group)
     t.copy_(h)
     return t
+
+
+def all_reduce_sum_(t: torch.Tensor, group=None) -> torch.Tensor:
+    cd = _comm_device(t, group)
+    if cd == t.device:
+        dist.all_reduce(t, op=dist.ReduceOp.SUM, group=group)
+        return t
+    h = t.to(cd)
+    dist.all_reduce(h, op=dist.ReduceOp.SUM, group=group)
+    t.copy_(h)
+    return t
+
+
+def accumulate_stats_sharded_(grad_accum: torch.Tensor, denom: torch.Tensor, views, group=None,
+                              accumulate=None) -> None:
+    """The stat feed of data-parallel training (ref/adc.py:73-79 per view),
+    sharded over training views: each rank accumulates the gradient outputs of
+    ITS views -- ``views`` is a sequence of (viewspace_grad [N,2], visible [N])
+    -- into zeroed per-Gaussian partial sums with the CUDA kernel
+    (``operator.accumulate_stats_``), the partials of all ranks are summed
+    with ONE all_reduce(SUM) of a packed [2,N] fp64 buffer (NCCL over NVLink
+    on a GPU box), and every rank adds the identical totals to its
+    grad_accum / denom.  The counts in ``denom`` are exact; ``grad_accum``
+    differs from one process's view-by-view sum only in the fp64 rounding of
+    the summation order (the reference has no multi-process form)."""
+    n = grad_accum.numel()
+    part = torch.zeros(2, n, dtype=torch.float64, device=grad_accum.device)
+    acc = accumulate or op.accumulate_stats_
+    for vg, vis in views:
+        acc(part[0], part[1], vg, vis)
+    all_reduce_sum_(part.view(-1), group)
+    grad_accum.add_(part[0])
+    denom.add_(part[1])
 
 
 def all_gather_bytes(t: torch.Tensor, group=None) -> list:
@@ -321,4 +358,5 @@ def densify_step_sharded(g: op.GaussianTensors, extent: float, cameras, gt, grad
     return run_sharded(ex, len(ex.view_ids), group)
 
 
-__all__ = ["view_block", "shard_views", "all_reduce_max_", "all_gather_bytes", "run_sharded", "run_lockstep", "GpuExecutor", "densify_step_sharded"]
+__all__ = ["view_block", "shard_views", "all_reduce_max_", "all_reduce_sum_", "accumulate_stats_sharded_",
+           "all_gather_bytes", "run_sharded", "run_lockstep", "GpuExecutor", "densify_step_sharded"]

@@ -296,3 +296,94 @@ def test_sharded_two_processes_one_gpu(tmp_path):
         for k in want:
             np.testing.assert_array_equal(got[k], want[k], err_msg=f"rank {r}: {k}")
         assert state == rng.bit_generator.state
+
+
+# ------------------------------------------------ sharded stat feed (ref/adc.py:73-79)
+def _acc_views(n, n_views, seed):
+    rng = np.random.default_rng(seed)
+    return [(rng.normal(size=(n, 2)), rng.uniform(size=n) < 0.6) for _ in range(n_views)]
+
+
+def _torch_acc(ga, den, vg, vis):
+    """The oracle's accumulate_stats on torch CPU tensors (stand-in for the kernel)."""
+    g = ga.numpy()
+    d = den.numpy()
+    O.accumulate_stats(g, d, np.asarray(vg), np.asarray(vis))
+
+
+def _stats_worker(rank, world, port, out_dir, n, n_views):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        views = _acc_views(n, n_views, 5)
+        lo, hi = SH.view_block(n_views, world, rank)
+        ga = torch.full((n,), 0.25, dtype=torch.float64)
+        den = torch.full((n,), 2.0, dtype=torch.float64)
+        SH.accumulate_stats_sharded_(ga, den, views[lo:hi], accumulate=_torch_acc)
+        with open(os.path.join(out_dir, f"s{rank}.pkl"), "wb") as f:
+            pickle.dump((ga.numpy(), den.numpy()), f)
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_accumulate_stats_sharded_over_views(tmp_path, world):
+    """Each rank accumulates its block of views, one all_reduce(SUM) combines
+    them: every rank holds the same stats, denom exact, grad_accum equal to
+    the one-process view-by-view oracle within fp64 summation-order rounding."""
+    n, n_views = 2000, 7
+    views = _acc_views(n, n_views, 5)
+    ga = np.full(n, 0.25)
+    den = np.full(n, 2.0)
+    for vg, vis in views:
+        O.accumulate_stats(ga, den, vg, vis)
+    mp.spawn(_stats_worker, args=(world, _free_port(), str(tmp_path), n, n_views), nprocs=world, join=True)
+    got = []
+    for r in range(world):
+        with open(tmp_path / f"s{r}.pkl", "rb") as f:
+            got.append(pickle.load(f))
+    for g_, d_ in got:
+        np.testing.assert_array_equal(g_, got[0][0])
+        np.testing.assert_array_equal(d_, got[0][1])
+        np.testing.assert_array_equal(d_, den)
+        np.testing.assert_allclose(g_, ga, rtol=1e-13, atol=0)
+
+
+def _stats_gpu_worker(rank, world, port, out_dir, n, n_views):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        views = [(torch.as_tensor(vg, device="cuda:0"), torch.as_tensor(vis, device="cuda:0"))
+                 for vg, vis in _acc_views(n, n_views, 9)]
+        lo, hi = SH.view_block(n_views, world, rank)
+        ga = torch.full((n,), 0.25, dtype=torch.float64, device="cuda:0")
+        den = torch.full((n,), 2.0, dtype=torch.float64, device="cuda:0")
+        SH.accumulate_stats_sharded_(ga, den, views[lo:hi])   # the CUDA kernel per view
+        with open(os.path.join(out_dir, f"sg{rank}.pkl"), "wb") as f:
+            pickle.dump((ga.cpu().numpy(), den.cpu().numpy()), f)
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+def test_accumulate_stats_sharded_two_processes_one_gpu(tmp_path):
+    """The sharded stat feed with the CUDA kernel in 2 real processes: ranks
+    identical, denom exact, grad_accum within summation-order rounding of the
+    one-process kernel sum (itself bit-exact to the reference per view)."""
+    from paper_2605_06876_b200 import operator as op
+    n, n_views = 50_001, 6
+    ga = torch.full((n,), 0.25, dtype=torch.float64, device="cuda:0")
+    den = torch.full((n,), 2.0, dtype=torch.float64, device="cuda:0")
+    for vg, vis in _acc_views(n, n_views, 9):
+        op.accumulate_stats_(ga, den, torch.as_tensor(vg, device="cuda:0"), torch.as_tensor(vis, device="cuda:0"))
+    mp.spawn(_stats_gpu_worker, args=(2, _free_port(), str(tmp_path), n, n_views), nprocs=2, join=True)
+    got = []
+    for r in range(2):
+        with open(tmp_path / f"sg{r}.pkl", "rb") as f:
+            got.append(pickle.load(f))
+    for g_, d_ in got:
+        np.testing.assert_array_equal(g_, got[0][0])
+        np.testing.assert_array_equal(d_, den.cpu().numpy())
+        np.testing.assert_allclose(g_, ga.cpu().numpy(), rtol=1e-13, atol=0)
