@@ -13,6 +13,8 @@ counted and reported (PARITY_REPORT), their rows excluded from the float check.
   config2: 100k Gaussians, all 16 views of 800x800
   config3: 1.2M Gaussians, 4 of the 64 views of 1237x822 (views 0, 16, 32, 48),
            every parent merged
+  config4: 3M Gaussians, 2 of the 128 views of 1297x840 (views 0, 64)
+  config5: 8M Gaussians, 2 of its 256 views (views 0, 128)
 
 Run on a B200:  PARITY_REPORT=gpurun_out/parity.json python -m pytest tests -m gpu -q
 """
@@ -76,5 +78,17 @@ def test_config2_all_views_stage_isolated(op):
 
 def test_config3_view_subset_stage_isolated(op):
     st, c = _stage_isolated(op, "config3", [0, 16, 32, 48])
+    assert st["mismatched"] == 0, st
+    assert c["n_regions"] > 1000 and c["n_children"] > 100, c
+
+
+def test_config4_view_subset_stage_isolated(op):
+    st, c = _stage_isolated(op, "config4", [0, 64])
+    assert st["mismatched"] == 0, st
+    assert c["n_regions"] > 1000 and c["n_children"] > 100, c
+
+
+def test_config5_view_subset_stage_isolated(op):
+    st, c = _stage_isolated(op, "config5", [0, 128])
     assert st["mismatched"] == 0, st
     assert c["n_regions"] > 1000 and c["n_children"] > 100, c
