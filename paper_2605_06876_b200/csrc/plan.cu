@@ -705,8 +705,10 @@ static adps_status render_impl(adps_plan* P, void* stream_v, const adps_gaussian
     CK(cudaStreamSynchronize(s));
     for (int v = 0; v < n_views; ++v)
       if (P->vflag_host[v] == 1) return fail(ADPS_BAD_STATE, "tile pairs still exceed the grown capacity");
-  } else if (most > 0 && P->dup_cap > 2 * most + 4096) {
-    P->dup_cap = most + most / 8 + 1024;   // shrink a stale capacity (the padding is sorted too)
+  } else if (most > 0 && n_views >= 4) {
+    // follow the largest view of this call with a 3 % margin: the padding is
+    // sorted too (a view of the next call that exceeds it is redone)
+    P->dup_cap = std::min(most + most / 32 + 1024, 0x7fffffffLL);
   }
   for (int v = 0; v < n_views; ++v)
     if (P->vflag_host[v] == 2) {   // a run of equal 32-bit depth keys too long for the fix-up
