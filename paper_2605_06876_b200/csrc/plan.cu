@@ -158,6 +158,8 @@ struct adps_plan {
   cudaEvent_t ev_chunk[kMaxChunks] = {};
   cudaEvent_t ev_attr = nullptr;
   cudaEvent_t ev_cfork = nullptr, ev_child = nullptr;   // child init on the second stream
+  cudaEvent_t ev_cams = nullptr;                          // the cameras' host copy (second stream)
+  bool cams_pending = false;
   bool child_pending = false;
   bool attr_pending = false;
   int pipeline = ADPS_PIPELINE_DEFAULT;
@@ -225,6 +227,10 @@ static void mark_start(adps_plan* P, cudaStream_t s, bool reset) {
   mark(P, "start", s, 0);
 }
 
+#ifndef ADPS_SELECT_FOLD
+#define ADPS_SELECT_FOLD 1   // the classify pass zeroes the flags and seeds the min/max slots
+#endif
+
 // stable CUB radix sort of (key, value) pairs over [0, end_bit), temp storage owned by the plan
 template <class K, class V>
 static cudaError_t cub_sort_pairs(adps_plan* P, const K* kin, K* kout, const V* vin, V* vout, long long n,
@@ -286,6 +292,7 @@ extern "C" adps_status adps_plan_create(adps_plan** plan, int32_t device, int64_
   cudaEventCreateWithFlags(&P->ev_small, cudaEventDisableTiming);
   cudaEventCreateWithFlags(&P->ev_keep, cudaEventDisableTiming);
   cudaEventCreateWithFlags(&P->ev_cfork, cudaEventDisableTiming);
+  cudaEventCreateWithFlags(&P->ev_cams, cudaEventDisableTiming);
   cudaEventCreateWithFlags(&P->ev_child, cudaEventDisableTiming);
   cudaEventCreateWithFlags(&P->ev_nfork, cudaEventDisableTiming);
   cudaEventCreateWithFlags(&P->ev_norm, cudaEventDisableTiming);
@@ -364,6 +371,7 @@ extern "C" adps_status adps_plan_destroy(adps_plan* P) {
   if (P->ev_small) cudaEventDestroy(P->ev_small);
   if (P->ev_keep) cudaEventDestroy(P->ev_keep);
   if (P->ev_cfork) cudaEventDestroy(P->ev_cfork);
+  if (P->ev_cams) cudaEventDestroy(P->ev_cams);
   if (P->ev_child) cudaEventDestroy(P->ev_child);
   if (P->ev_nfork) cudaEventDestroy(P->ev_nfork);
   if (P->ev_norm) cudaEventDestroy(P->ev_norm);
@@ -986,7 +994,7 @@ extern "C" adps_status adps_step_phase1_begin(adps_plan* P, void* stream_v, cons
   CK(ensure(P->partials, sizeof(PartialRec) * P->partial_cap));
   CK(ensure(P->partial_parent, sizeof(int) * P->partial_cap));
   memcpy(P->cams_host, cams_host, sizeof(double) * 18 * V);
-  CK(cudaMemcpyAsync(P->cams.p, P->cams_host, sizeof(double) * 18 * V, cudaMemcpyHostToDevice, s));
+  P->cams_pending = true;   // copied at the end of the begin (below)
   Counters* ctr = P->ctr.as<Counters>();
   // the attribution of a fused render on exactly these inputs (one use)
   const bool fused = P->fused.valid && P->use_bits && same_gaussians(P->fused.g, *g) && P->fused.n == n &&
@@ -1035,7 +1043,13 @@ extern "C" adps_status adps_step_phase1_begin(adps_plan* P, void* stream_v, cons
   // scan on the second stream alongside the input pass, joined before the
   // fallback count
   const bool split_select = P->pipeline && !P->timing;
+  const bool fold_init = split_select && ADPS_SELECT_FOLD;
   if (split_select) {
+    if (fold_init) {
+      sa.dom_zero = P->dom_flag.as<unsigned char>();
+      sa.lohi_init = P->lohi.as<unsigned long long>();
+      sa.lohi_views = V;
+    }
     CK(launch_select_split(sa, sst, s, P->aux, P->ev_cfork, P->ev_child));
     mark(P, "select", s, 2);
   } else {
@@ -1045,12 +1059,14 @@ extern "C" adps_status adps_step_phase1_begin(adps_plan* P, void* stream_v, cons
 
   // ---- ever-dominant flags (ref/adc.py:177-180) and the fallback count, so
   //      the host can draw the fallback normals while the rest runs
-  CK(cudaMemsetAsync(P->dom_flag.p, 0, (size_t)nn, s));
-  for (int v = 0; v < V; ++v) {
-    P->lohi_host[2 * v] = 0x7ff0000000000000ull;   // +inf
-    P->lohi_host[2 * v + 1] = 0ull;                // +0.0
+  if (!fold_init) {   // (the split select's classify pass zeroed and seeded them)
+    CK(cudaMemsetAsync(P->dom_flag.p, 0, (size_t)nn, s));
+    for (int v = 0; v < V; ++v) {
+      P->lohi_host[2 * v] = 0x7ff0000000000000ull;   // +inf
+      P->lohi_host[2 * v + 1] = 0ull;                // +0.0
+    }
+    CK(cudaMemcpyAsync(P->lohi.p, P->lohi_host, sizeof(unsigned long long) * 2 * V, cudaMemcpyHostToDevice, s));
   }
-  CK(cudaMemcpyAsync(P->lohi.p, P->lohi_host, sizeof(unsigned long long) * 2 * V, cudaMemcpyHostToDevice, s));
   {
     const AttributionArgs a = attr_args(P, V, H, W, cfg, N, image, gt, dominant);
     P->attr_pending = false;
@@ -1084,6 +1100,11 @@ extern "C" adps_status adps_step_phase1_begin(adps_plan* P, void* stream_v, cons
     }
   }
   }   // not fused
+  // the cameras are read first by child init (after phase 1's first sync):
+  // copied on the second stream behind the work already queued there, off
+  // this stream's kernel chain
+  CK(cudaMemcpyAsync(P->cams.p, P->cams_host, sizeof(double) * 18 * V, cudaMemcpyHostToDevice, P->aux));
+  CK(cudaEventRecord(P->ev_cams, P->aux));
   CK(cudaMemcpyAsync(P->ctr_host, ctr, sizeof(Counters), cudaMemcpyDeviceToHost, s));
   CK(cudaStreamSynchronize(s));
   {
@@ -1196,6 +1217,10 @@ static adps_status phase1_local(adps_plan* P, cudaStream_t s, long long* n_regio
   const int bits_c = ceil_log2((unsigned long long)(n_split > 0 ? n_split : 1));
   const int total_bits = bits_c + bits_v + bits_b + bits_p;
   if (total_bits > 64) return fail(ADPS_INVALID_ARG, "region sort key needs %d bits (> 64)", total_bits);
+  if (P->cams_pending) {   // the cameras' copy on the second stream
+    CK(cudaStreamWaitEvent(s, P->ev_cams, 0));
+    P->cams_pending = false;
+  }
   ChildArgs ca;
   ca.regions = P->regions.as<RegionRec>();
   ca.n_regions = &ctr->n_regions;

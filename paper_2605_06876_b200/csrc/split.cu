@@ -61,8 +61,14 @@ cudaError_t launch_select(const SelectArgs& a, ScanState st, cudaStream_t s) {
 // the classes alone (elementwise, HBM-bound): the input pass needs only them
 __global__ void classify_select_kernel(SelectArgs a) {
   pdl_wait();   // programmatic dependent launch: the previous kernel's results are visible
-  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < a.n; i += (long long)gridDim.x * blockDim.x)
+  const long long t0 = (long long)blockIdx.x * blockDim.x + threadIdx.x, stride = (long long)gridDim.x * blockDim.x;
+  if (a.lohi_init)
+    for (long long t = t0; t < 2ll * a.lohi_views; t += stride)
+      a.lohi_init[t] = (t & 1) ? 0ull : 0x7ff0000000000000ull;   // lo = +inf, hi = +0.0
+  for (long long i = t0; i < a.n; i += stride) {
     a.cls[i] = select_class(a, i);
+    if (a.dom_zero) a.dom_zero[i] = 0;
+  }
 }
 
 cudaError_t launch_select_split(const SelectArgs& a, ScanState st, cudaStream_t s, cudaStream_t aux, cudaEvent_t fork,

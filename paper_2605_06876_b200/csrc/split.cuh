@@ -27,6 +27,11 @@ struct SelectArgs {
   int* split_list;
   int* clone_list;
   Counters* ctr;
+  // (classify kernel only) zero the ever-dominant flags and seed the per-view
+  // min/max slots (+inf, +0) in the same pass: no memset / host copy between kernels
+  unsigned char* dom_zero = nullptr;
+  unsigned long long* lohi_init = nullptr;
+  int lohi_views = 0;
 };
 cudaError_t launch_select(const SelectArgs& a, ScanState st, cudaStream_t s);
 // classes on `s`, then the split/clone list scan on `aux` (recorded into `join`):
