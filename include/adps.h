@@ -168,11 +168,12 @@ ADPS_API adps_status adps_render_stats(adps_plan* plan, void* stream, const adps
  * and the attribution render of the sampled views (as adps_render) whose
  * epilogue also computes, from each pixel's stored image value and gt, what
  * the step's input pass would: the raw L1 error (numpy's fp64 order) into the
- * plan's fp32 raw cache, the per-view min/max, the candidate bits and the
+ * plan's 16-bit raw cache, the per-view min/max, the candidate bits and the
  * ever-dominant flags (ref/adc.py:168-180).  The next
  * adps_step_phase1_begin with the same arguments (same g, stats, cfg, cameras,
  * image, gt and dominant pointers) then skips select and the input pass and
- * starts from that 8 B/px boundary; any other call uses the full path.
+ * starts from that 6 B/px boundary (cache + dominant map); any other call
+ * uses the full path.
  * gt: [V,H,W,3] fp32 of the same views. */
 ADPS_API adps_status adps_render_fused(adps_plan* plan, void* stream, const adps_gaussians* g, int64_t n,
                               double extent, const double* grad_accum, const double* denom,
@@ -319,7 +320,7 @@ ADPS_API adps_status adps_step_phase1_finish(adps_plan* plan, void* stream, int6
  * with more proposals than this use the grid-wide pair-tile merge path
  * (default 32; 0 routes every split parent through it).
  * ADPS_PARAM_TILE_PATH: 0 (default) warp-per-tile CCL on bit planes written by
- * a words pass over the fp32 raw cache, with the block CCL for the tiles it
+ * a words pass over the 16-bit raw cache, with the block CCL for the tiles it
  * defers (> 192 runs) and for r_erode > 3 / debug maps; 1 the block CCL for
  * every tile; 2 the warp CCL thresholding the fp64 raw cache row by row; 3 as
  * 0 with the bit planes computed per tile inside the CCL kernel (no words
@@ -333,8 +334,9 @@ ADPS_API adps_status adps_step_phase1_finish(adps_plan* plan, void* stream, int6
 #define ADPS_PARAM_STAT_TILE_PAIRS 7     /* read-only diagnostics of the last phase 1: surviving */
 #define ADPS_PARAM_STAT_GATES 8          /* large-parent tile pairs; gates evaluated and passed */
 #define ADPS_PARAM_STAT_GATES_PASSED 9   /* in them (the last two only in stats builds) */
-#define ADPS_PARAM_RAW_CACHE 6          /* 1 (default): the minmax pass caches the fp64 raw
-                                           L1 error (8 B/px) for the warp CCL; 0: recompute */
+#define ADPS_PARAM_RAW_CACHE 6          /* 1 (default): the input pass caches the raw L1 error
+                                           (16 bits/px, exact compares, ambiguous pixels redone
+                                           in fp64) for the CCL; 0: recompute */
 #define ADPS_PARAM_PIPELINE_CHUNKS 10      /* view chunks of the attribution pipeline (input pass of chunk
                                               c+1 beside the CCL of chunk c; default 1) */
 #define ADPS_PARAM_INPUT_BLOCKS_PER_SM 11  /* resident blocks per SM of the input pass (0 = all that fit) */
