@@ -1066,6 +1066,7 @@ extern "C" adps_status adps_step_phase1_begin(adps_plan* P, void* stream_v, cons
       P->lohi_host[2 * v + 1] = 0ull;                // +0.0
     }
     CK(cudaMemcpyAsync(P->lohi.p, P->lohi_host, sizeof(unsigned long long) * 2 * V, cudaMemcpyHostToDevice, s));
+    mark(P, "input_init", s, 0);   // (timing mode: the input pass's own stage starts here)
   }
   {
     const AttributionArgs a = attr_args(P, V, H, W, cfg, N, image, gt, dominant);
