@@ -668,11 +668,22 @@ class StepResult:
     index_map: torch.Tensor
     counts: dict
     view_ids: list
-    report_arrays: dict = None
+    _report: object = None         # the report arrays, or (buffer, n_split, n_clone, V) split on first use
     normals: torch.Tensor = None   # the 6F fallback normals (device)
     child_parent: torch.Tensor = None    # int32 [n_out - n_keep]: old index of every appended row
     insert_offset: torch.Tensor = None   # int64 [n_split]: output row of candidate k's first insert
     stage_ms: dict = field(default_factory=dict)
+
+    @property
+    def report_arrays(self) -> dict:
+        """The SplitReport arrays on the device (views of one buffer)."""
+        if isinstance(self._report, tuple):
+            self._report = _report_views(*self._report)
+        return self._report
+
+    @report_arrays.setter
+    def report_arrays(self, value):
+        self._report = value
 
     def report(self) -> SplitReport:
         """Host SplitReport (ref/adc.py:60-70) built from the device arrays."""
@@ -837,7 +848,7 @@ def densify_step(g: GaussianTensors, extent: float, cameras, gt, grad_accum: tor
     res = StepResult(gaussians=out, index_map=index_map, counts=counts, view_ids=list(view_ids),
                      normals=normals, child_parent=child_parent, insert_offset=insert_offset)
     if want_report:
-        res.report_arrays = (_report_views(rep_buf, ns, ncl, nv) if rep_buf is not None
+        res.report_arrays = ((rep_buf, ns, ncl, nv) if rep_buf is not None
                              else plan.report_arrays(counts["n_split"], counts["n_clone"]))
     if plan.timing:
         res.stage_ms = plan.stage_ms()
