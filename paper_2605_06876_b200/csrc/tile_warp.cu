@@ -37,6 +37,9 @@ constexpr int kWarpsPerBlock = 8;
 #ifndef ADPS_TW_ROWWISE
 #define ADPS_TW_ROWWISE 0   // 1: the row-wise words pass (ballots) instead of the transposed one
 #endif
+#ifndef ADPS_TW_DOMROWS
+#define ADPS_TW_DOMROWS 1   // stage the dominant ids of whole keyed rows
+#endif
 #ifndef ADPS_TW_MINBLOCKS
 #define ADPS_TW_MINBLOCKS 5
 #endif
@@ -904,11 +907,22 @@ __device__ __forceinline__ void tile_bits_body(const TileParams& P, const uint4*
   }
   // ---- stage the dominant ids of keyed pixels (one wait for the whole tile)
   const int* dom_v = P.dom + (long long)v * H * W;
+#if ADPS_TW_DOMROWS
+  {   // whole keyed rows (in-image columns): no per-pixel key test or shuffle
+    const int* drow = dom_v + (long long)y0 * W + x0 + lane;
+    if (x0 + lane < W)
+      for (unsigned rows = keyed; rows; rows &= rows - 1u) {
+        const int ty = __ffs(rows) - 1;
+        cp_async4(&S.u.d[ty][lane], drow + (long long)ty * W);
+      }
+  }
+#else
   for (unsigned rows = keyed; rows; rows &= rows - 1u) {
     const int ty = __ffs(rows) - 1;
     const unsigned kw = __shfl_sync(FULL, K, ty);
     if ((kw >> lane) & 1u) cp_async4(&S.u.d[ty][lane], dom_v + (long long)(y0 + ty) * W + x0 + lane);
   }
+#endif
   cp_async_wait_all();
   // ---- (a) lane = column, per keyed row: the run-continuation mask (same
   //      key|band as the left neighbour) and the three vertical same-key masks
