@@ -627,7 +627,9 @@ def run_ours(args, wl):
             parity = parity_on_sample(op, plan, wl, d, vs, make_cfg(wl, k))
 
     if rank == 0:
-        extra = {"dc_gt": d["dc_gt"], "dc_init": d["dc_init"], "shares": shares}
+        extra = {"dc_gt": d["dc_gt"], "dc_init": d["dc_init"], "shares": shares,
+                 "parallelism": (f"replicas x{world}" if args.replicas else
+                                 f"views and parents sharded over {world} ranks") if world > 1 else "single GPU"}
         line = {
             "metric": METRIC, "value": n_split * world / (ms * 1e-3) if args.replicas else n_split / (ms * 1e-3),
             "unit": UNIT, "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
