@@ -1288,17 +1288,35 @@ __global__ void __launch_bounds__(HUGE ? 1024 : 256) cap_select_kernel(MergeArgs
         }
       }
       __syncthreads();
-      if (tid == 0) {
-        int need = s_need;
-        int b = 255;
-        for (; b > 0; --b) {
-          if ((int)hist[b] >= need) break;
-          need -= (int)hist[b];
+      if (wid == 0) {
+        // the bin holding the need-th largest key, scanning from bin 255 down
+        // (bin 0 takes whatever is left): lane L holds bins 255 - 8L - j,
+        // a warp prefix over the lanes, then the owning lane walks its 8 bins
+        int hv[8], c = 0;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) c += (hv[j] = (int)hist[255 - 8 * lane - j]);
+        int x = c;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const int t = __shfl_up_sync(0xffffffffu, x, o);
+          if (lane >= o) x += t;
         }
-        s_need = need;   // still needed from bin b
-        s_prefix = pre | ((unsigned long long)b << shift);
-        s_mask = msk | (255ull << shift);
-        if ((int)hist[b] == need || shift == 0) s_done = 1;
+        const int need0 = s_need, before = x - c;
+        const unsigned own = __ballot_sync(0xffffffffu, before < need0 && need0 <= x);
+        if (lane == (own ? __ffs(own) - 1 : 31)) {
+          int need = need0 - before, b = 255 - 8 * lane, hb = hv[0];
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            b = 255 - 8 * lane - j;
+            hb = hv[j];
+            if (b == 0 || hb >= need) break;
+            need -= hb;
+          }
+          s_need = need;   // still needed from bin b
+          s_prefix = pre | ((unsigned long long)b << shift);
+          s_mask = msk | (255ull << shift);
+          if (hb == need || shift == 0) s_done = 1;
+        }
       }
       __syncthreads();
     }

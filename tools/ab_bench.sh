@@ -10,6 +10,6 @@ l = [x for x in open(f"gpurun_out/ab_{sys.argv[1]}.log") if x.startswith("{")]
 if not l:
     print(sys.argv[1], "FAILED"); sys.exit()
 d = json.loads(l[-1]); s = d["stages_ms"]
-print(f"{sys.argv[1]:10s} step={d['ms_per_step']:.3f}ms minmax={s['minmax']:.3f} tile_ccl={s['tile_ccl']:.3f} tile_gates={s['merge_tile_gates']:.3f} roof={d['roofline']['frac']:.3f} border={s['border_merge']:.3f}")
+print(f"{sys.argv[1]:10s} step={d['ms_per_step']:.3f}ms minmax={s['minmax']:.3f} tile_ccl={s['tile_ccl']:.3f} tile_gates={s['merge_tile_gates']:.3f} roof={d['roofline']['frac']:.3f} border={s["border_merge"]:.3f} cap={s["merge_cap"]:.3f} groups={s["merge_groups"]:.3f}")
 PY
 done
