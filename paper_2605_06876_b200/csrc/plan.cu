@@ -107,9 +107,10 @@ struct adps_plan {
   Buf nrm_val, nrm_len, nrm_acc, nrm_reach, nrm_rmax, nrm_walked, nrm_idx, nrm_tmp;
   // merge / cap scratch (proposal space)
   Buf small_list, pstart, n_groups, work_cnt, work_off, props_s, psrc, pcand, gkey, gval, gkey_sorted, gval_sorted,
-      grp_first, gpar, gext, gfirst_of, glist, scan3_val, scan3_flag, scan3_ticket, large_of, lp_cnt, lp_off, tile_cnt, tile_off, mkey,
+      grp_first, gpar, gext, gfirst_of, glist, scan3_val, scan3_flag, large_of, lp_cnt, lp_off, tile_cnt, tile_off, mkey,
       mval, mkey_sorted, mval_sorted, boxes, tile_owner, tile_pairs, gsoa, fsoa;
-  Buf scan_val, scan_flag, scan_ticket, scan2_val, scan2_flag, scan2_ticket, cub_tmp;
+  Buf scan_val, scan_flag, scan2_val, scan2_flag, cub_tmp;
+  unsigned scan_epoch = 0;   // scan launches so far (tile-flag epochs, scan.cuh)
   Buf ctr;
   Counters* ctr_host = nullptr;
   unsigned long long* lohi_host = nullptr;
@@ -246,15 +247,19 @@ static cudaError_t cub_sort_pairs(adps_plan* P, const K* kin, K* kout, const V* 
   return cub::DeviceRadixSort::SortPairs(P->cub_tmp.p, tb, kin, kout, vin, vout, (int)n, 0, end_bit, s);
 }
 
-static adps_status scan_state(adps_plan* P, Buf& val, Buf& flag, Buf& ticket, long long n, ScanState* st) {
+static adps_status scan_state(adps_plan* P, Buf& val, Buf& flag, long long n, ScanState* st) {
   long long tiles = scan_tiles(n);
   CK(ensure(val, 2 * sizeof(unsigned long long) * tiles));
+  const void* old = flag.p;
   CK(ensure(flag, sizeof(unsigned int) * tiles));
-  CK(ensure(ticket, sizeof(unsigned int)));
+  if (flag.p != old) {   // epoch 0 = empty; once per allocation, finished before any stream uses it
+    CK(cudaMemset(flag.p, 0, flag.bytes));
+    CK(cudaDeviceSynchronize());
+  }
   st->value = val.as<unsigned long long>();
   st->flag = flag.as<unsigned int>();
-  st->ticket = ticket.as<unsigned int>();
-  (void)P;
+  st->epoch_host = &P->scan_epoch;
+  st->epoch = 0;
   return ADPS_OK;
 }
 
@@ -314,14 +319,14 @@ static int plan_buffers(adps_plan* P, Buf** out) {
                  &P->regions_per_view, &P->lohi, &P->lo, &P->thr, &P->thr_raw, &P->cams, &P->border, &P->partials,
                  &P->partial_parent, &P->regions, &P->props, &P->valid, &P->keys, &P->vals,
                  &P->keys_sorted, &P->vals_sorted, &P->idx, &P->uf, &P->groups, &P->children,
-                 &P->dbg_stats, &P->dbg_child, &P->scan_val, &P->scan_flag, &P->scan_ticket,
-                 &P->scan2_val, &P->scan2_flag, &P->scan2_ticket, &P->cub_tmp, &P->ctr, &P->r_key,
+                 &P->dbg_stats, &P->dbg_child, &P->scan_val, &P->scan_flag,
+                 &P->scan2_val, &P->scan2_flag, &P->cub_tmp, &P->ctr, &P->r_key,
                  &P->r_key_sorted, &P->r_order_in, &P->r_order, &P->r_tiles, &P->r_rect, &P->r_splat,
                  &P->r_offs, &P->r_dup, &P->r_dup_sorted, &P->r_tstart, &P->r_tend, &P->r_total, &P->r_tile_lohi,
                  &P->r_k32, &P->r_k32_sorted, &P->r_vflag, &P->r_vtotal, &P->r_cov3, &P->r_rgb0,
                  &P->r_cams, &P->small_list, &P->pstart, &P->n_groups, &P->work_cnt, &P->work_off,
                  &P->props_s, &P->psrc, &P->pcand, &P->gkey, &P->gval, &P->gkey_sorted, &P->gval_sorted, &P->grp_first,
-                 &P->gpar, &P->gext, &P->gfirst_of, &P->glist, &P->scan3_val, &P->scan3_flag, &P->scan3_ticket,
+                 &P->gpar, &P->gext, &P->gfirst_of, &P->glist, &P->scan3_val, &P->scan3_flag,
                  &P->large_of, &P->lp_cnt, &P->lp_off, &P->tile_cnt, &P->tile_off, &P->mkey, &P->mval,
                  &P->mkey_sorted, &P->mval_sorted, &P->boxes, &P->tile_owner, &P->tile_pairs, &P->gsoa, &P->fsoa, &P->deferred, &P->cand_bits, &P->rawc, &P->twords,
                  &P->nrm_val, &P->nrm_len, &P->nrm_acc, &P->nrm_reach, &P->nrm_rmax, &P->nrm_walked,
@@ -502,7 +507,7 @@ static adps_status render_impl(adps_plan* P, void* stream_v, const adps_gaussian
   // tile ids below 2^tile_bits - 1: the padding keys (all ones) sort after every real key
   const int tile_bits = ceil_log2((unsigned long long)n_tiles + 1);
   ScanState sst;
-  st = scan_state(P, P->scan_val, P->scan_flag, P->scan_ticket, n, &sst);
+  st = scan_state(P, P->scan_val, P->scan_flag, n, &sst);
   if (st != ADPS_OK) return st;
   // the view-independent covariances (and degree-0 colours), once per call
   CK(ensure(P->r_cov3, sizeof(double) * 6 * n));
@@ -845,7 +850,7 @@ extern "C" adps_status adps_render_fused(adps_plan* P, void* stream_v, const adp
   }
   CK(cudaMemcpyAsync(P->lohi.p, P->lohi_host, sizeof(unsigned long long) * 2 * V, cudaMemcpyHostToDevice, s));
   ScanState sst;
-  st = scan_state(P, P->scan_val, P->scan_flag, P->scan_ticket, nn, &sst);
+  st = scan_state(P, P->scan_val, P->scan_flag, nn, &sst);
   if (st != ADPS_OK) return st;
   SelectArgs sa;
   sa.scale = g->scale;
@@ -1025,7 +1030,7 @@ extern "C" adps_status adps_step_phase1_begin(adps_plan* P, void* stream_v, cons
 
   // ---- select (ref/adc.py:165)
   ScanState sst;
-  st = scan_state(P, P->scan_val, P->scan_flag, P->scan_ticket, nn, &sst);
+  st = scan_state(P, P->scan_val, P->scan_flag, nn, &sst);
   if (st != ADPS_OK) return st;
   SelectArgs sa;
   sa.scale = g->scale;
@@ -1287,7 +1292,7 @@ static adps_status phase1_merge_part(adps_plan* P, cudaStream_t s) {
   const long long nn = n > 0 ? n : 1;
   Counters* ctr = P->ctr.as<Counters>();
   ScanState sst;
-  st = scan_state(P, P->scan_val, P->scan_flag, P->scan_ticket, nn, &sst);
+  st = scan_state(P, P->scan_val, P->scan_flag, nn, &sst);
   if (st != ADPS_OK) return st;
   const long long n_regions = P->n_regions_cur;
   const long long n_split = (long long)P->ctr_host->n_split;
@@ -1360,10 +1365,17 @@ static adps_status phase1_merge_part(adps_plan* P, cudaStream_t s) {
     CK(ensure(P->tile_pairs, sizeof(int4) * want));
   }
   CK(ensure(P->regions_per_view, 4 * sc * V));
-  CK(cudaMemsetAsync(P->cand_start.p, 0, 4 * sc, s));
-  CK(cudaMemsetAsync(P->cand_end.p, 0, 4 * sc, s));
-  CK(cudaMemsetAsync(P->cand_nvalid.p, 0, 4 * sc, s));
-  CK(cudaMemsetAsync(P->regions_per_view.p, 0, 4 * sc * V, s));
+  {
+    ZeroList z{};
+    z.p[0] = P->cand_start.as<int>();
+    z.p[1] = P->cand_end.as<int>();
+    z.p[2] = P->cand_nvalid.as<int>();
+    z.p[3] = P->regions_per_view.as<int>();
+    z.n[0] = z.n[1] = z.n[2] = sc;
+    z.n[3] = sc * V;
+    z.count = 4;
+    CK(launch_zero(z, s));
+  }
   RangeArgs ra;
   ra.keys_sorted = P->keys_sorted.as<unsigned long long>();
   ra.vals_sorted = P->vals_sorted.as<int>();
@@ -1456,7 +1468,7 @@ static adps_status phase1_merge_part(adps_plan* P, cudaStream_t s) {
   }
   if (n_split > 0) {
     ScanState sst3;
-    st = scan_state(P, P->scan3_val, P->scan3_flag, P->scan3_ticket, rc, &sst3);
+    st = scan_state(P, P->scan3_val, P->scan3_flag, rc, &sst3);
     if (st != ADPS_OK) return st;
     CK(launch_merge_prepare(ma, n_split, sst3, s));
     mark(P, "merge_prepare", s, 3);
@@ -1516,12 +1528,12 @@ static adps_status phase1_finish_launch(adps_plan* P, cudaStream_t s) {
   const long long nn = n > 0 ? n : 1;
   Counters* ctr = P->ctr.as<Counters>();
   ScanState sst, sst2;
-  st = scan_state(P, P->scan_val, P->scan_flag, P->scan_ticket, nn, &sst);
+  st = scan_state(P, P->scan_val, P->scan_flag, nn, &sst);
   if (st != ADPS_OK) return st;
   const long long n_split = (long long)P->ctr_host->n_split;
   const long long sc = n_split > 0 ? n_split : 1;
   // ---- offsets (ref/adc.py:229-244)
-  st = scan_state(P, P->scan2_val, P->scan2_flag, P->scan2_ticket, sc, &sst2);
+  st = scan_state(P, P->scan2_val, P->scan2_flag, sc, &sst2);
   if (st != ADPS_OK) return st;
   OffsetArgs oa;
   oa.n = n;
@@ -2218,7 +2230,7 @@ extern "C" adps_status adps_vanilla_phase1(adps_plan* P, void* stream_v, const a
   CK(cudaMemsetAsync(ctr, 0, sizeof(Counters), s));
   mark_start(P, s, true);
   ScanState sst, sst2;
-  st = scan_state(P, P->scan_val, P->scan_flag, P->scan_ticket, nn, &sst);
+  st = scan_state(P, P->scan_val, P->scan_flag, nn, &sst);
   if (st != ADPS_OK) return st;
   SelectArgs sa;
   sa.scale = g->scale;
@@ -2250,7 +2262,7 @@ extern "C" adps_status adps_vanilla_phase1(adps_plan* P, void* stream_v, const a
   CK(cudaMemsetAsync(P->cand_props.p, 0, 4 * sc, s));
   CK(launch_vanilla_cases(P->cand_case.as<int>(), P->cand_ins.as<int>(), P->cand_merged.as<int>(), &ctr->n_split,
                           n_children, s));
-  st = scan_state(P, P->scan2_val, P->scan2_flag, P->scan2_ticket, sc, &sst2);
+  st = scan_state(P, P->scan2_val, P->scan2_flag, sc, &sst2);
   if (st != ADPS_OK) return st;
   OffsetArgs oa;
   oa.n = n;
@@ -2334,7 +2346,7 @@ extern "C" adps_status adps_prune_index(adps_plan* P, void* stream_v, const floa
   CK(cudaMemsetAsync(&ctr->prune_keep, 0, 2 * sizeof(unsigned long long), s));
   if (n > 0) {
     ScanState sst;
-    adps_status st = scan_state(P, P->scan2_val, P->scan2_flag, P->scan2_ticket, n, &sst);
+    adps_status st = scan_state(P, P->scan2_val, P->scan2_flag, n, &sst);
     if (st != ADPS_OK) return st;
     PruneArgs pa;
     pa.opacity = opacity;

@@ -17,12 +17,23 @@ constexpr int kScanThreads = 256;
 #endif
 constexpr int kScanItems = ADPS_SCAN_ITEMS;
 constexpr int kScanTile = kScanThreads * kScanItems;
+#ifndef ADPS_SCAN_LB
+#define ADPS_SCAN_LB 4   // predecessors per lane per look-back round
+#endif
 
+// Tile flags carry the launch's epoch (flag = epoch << 2 | state), so a flag
+// left by an earlier scan over the same buffers reads as empty: no reset
+// between scans (the memsets were two extra stream operations per scan, and
+// they break the programmatic-launch chain).  Tile id = blockIdx.x: blocks
+// are dispatched in index order, so every predecessor a tile waits on has
+// been scheduled.
 struct ScanState {
   unsigned long long* value;  // [2 * n_tiles]: aggregate at [2t], inclusive prefix at [2t+1]
-  unsigned int* flag;         // [n_tiles] 0 = empty, 1 = aggregate ready, 2 = inclusive ready
-  unsigned int* ticket;       // [1] dynamic tile id (reset to 0 before launch)
+  unsigned int* flag;         // [n_tiles] epoch << 2 | 0 empty, 1 aggregate ready, 2 inclusive ready
+  unsigned int* epoch_host;   // host counter: each launch takes the next epoch
+  unsigned int epoch;         // this launch's epoch (set by launch_scan)
 };
+constexpr unsigned kScanEpochMask = 0x3fffffffu;
 
 // Policy requirements:
 //   __device__ unsigned long long value(long long i) const;
@@ -34,11 +45,9 @@ __global__ void __launch_bounds__(kScanThreads) scan_kernel(Policy pol, long lon
   __shared__ unsigned long long sv[kScanTile];
   __shared__ unsigned long long warp_sums[kScanThreads / kWarp];
   __shared__ unsigned long long s_prefix;
-  __shared__ unsigned int s_tile;
   const int tid = threadIdx.x;
-  if (tid == 0) s_tile = atomicAdd(st.ticket, 1u);
-  __syncthreads();
-  const long long tile = s_tile;
+  const long long tile = blockIdx.x;
+  const unsigned ep = st.epoch << 2;
   const long long base = tile * kScanTile;
   // striped, coalesced load
 #pragma unroll
@@ -92,58 +101,61 @@ __global__ void __launch_bounds__(kScanThreads) scan_kernel(Policy pol, long lon
       if (lane == 0) {
         vval[1] = agg;
         __threadfence();
-        vflag[0] = 2u;
+        vflag[0] = ep | 2u;
         s_prefix = 0ull;
       }
     } else {
       if (lane == 0) {
         vval[2 * tile] = agg;
         __threadfence();
-        vflag[tile] = 1u;
+        vflag[tile] = ep | 1u;
       }
       // 128 predecessors per round (4 per lane, nearest first: q = p - lane - 32 j):
       // inclusive prefixes propagate 128 tiles per round instead of 32
       unsigned long long acc = 0ull;
       long long p = tile - 1;
       while (true) {
-        unsigned int f[4];
+        constexpr int LB = ADPS_SCAN_LB;
+        unsigned int f[LB];
         bool busy;
         do {
+          busy = false;
 #pragma unroll
-          for (int j = 0; j < 4; ++j) {
+          for (int j = 0; j < LB; ++j) {
             const long long q = p - lane - 32 * j;
-            f[j] = q >= 0 ? vflag[q] : 2u;
+            const unsigned fv = q >= 0 ? vflag[q] : (ep | 2u);
+            f[j] = (fv & ~3u) == ep ? (fv & 3u) : 0u;   // another launch's flag: empty
+            busy |= f[j] == 0u;
           }
-          busy = f[0] == 0u || f[1] == 0u || f[2] == 0u || f[3] == 0u;
         } while (__any_sync(0xffffffffu, busy));
         __threadfence();
-        unsigned incl[4];
+        unsigned incl[LB];
 #pragma unroll
-        for (int j = 0; j < 4; ++j) incl[j] = __ballot_sync(0xffffffffu, f[j] == 2u);
+        for (int j = 0; j < LB; ++j) incl[j] = __ballot_sync(0xffffffffu, f[j] == 2u);
         // the nearest predecessor with an inclusive prefix: slot (jf, first)
-        int jf = 4, first = 32;
+        int jf = LB, first = 32;
 #pragma unroll
-        for (int j = 3; j >= 0; --j)
+        for (int j = LB - 1; j >= 0; --j)
           if (incl[j]) {
             jf = j;
             first = __ffs(incl[j]) - 1;
           }
         unsigned long long v = 0ull;
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
+        for (int j = 0; j < LB; ++j) {
           const long long q = p - lane - 32 * j;
           if (j < jf || (j == jf && lane < first)) v += vval[2 * q];
           else if (j == jf && lane == first && q >= 0) v += vval[2 * q + 1];
         }
         for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
         acc += v;
-        if (jf < 4) break;
-        p -= 128;
+        if (jf < LB) break;
+        p -= 32 * LB;
       }
       if (lane == 0) {
         vval[2 * tile + 1] = acc + agg;
         __threadfence();
-        vflag[tile] = 2u;
+        vflag[tile] = ep | 2u;
         s_prefix = acc;
       }
     }
@@ -177,10 +189,8 @@ inline long long scan_tiles(long long n) { return n <= 0 ? 1 : (n + kScanTile - 
 template <class Policy>
 inline cudaError_t launch_scan(const Policy& pol, long long n, ScanState st, cudaStream_t s) {
   long long tiles = scan_tiles(n);
-  cudaError_t e = cudaMemsetAsync(st.flag, 0, sizeof(unsigned int) * tiles, s);
-  if (e != cudaSuccess) return e;
-  e = cudaMemsetAsync(st.ticket, 0, sizeof(unsigned int), s);
-  if (e != cudaSuccess) return e;
+  do st.epoch = ++*st.epoch_host & kScanEpochMask;
+  while (st.epoch == 0);   // epoch 0 is the zeroed buffer's
   launch_k(scan_kernel<Policy>, (unsigned)tiles, kScanThreads, 0, s, pol, n, st);
   return cudaGetLastError();
 }

@@ -252,6 +252,21 @@ __global__ void region_keys_kernel(const RegionRec* __restrict__ regions, long l
   }
 }
 
+__global__ void zero_kernel(ZeroList z) {
+  pdl_wait();   // programmatic dependent launch: the previous kernel's results are visible
+  const long long t0 = (long long)blockIdx.x * blockDim.x + threadIdx.x, stride = (long long)gridDim.x * blockDim.x;
+  for (int e = 0; e < z.count; ++e)
+    for (long long i = t0; i < z.n[e]; i += stride) z.p[e][i] = 0;
+}
+
+cudaError_t launch_zero(const ZeroList& z, cudaStream_t s) {
+  long long m = 1;
+  for (int e = 0; e < z.count; ++e) m = z.n[e] > m ? z.n[e] : m;
+  const long long b = (m + 255) / 256;
+  launch_k(zero_kernel, (unsigned)(b > 1184 ? 1184 : b), 256, 0, s, z);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_region_keys(const RegionRec* regions, long long n, const int* cand_rank, int bits_v, int bits_b,
                                int bits_p, unsigned long long* keys, int* vals, cudaStream_t s) {
   long long b = (n + 255) / 256;

@@ -64,6 +64,14 @@ struct ChildArgs {
 };
 cudaError_t launch_child_init(const ChildArgs& a, cudaStream_t s);
 // sort keys (candidate rank, view, band, first pixel) of imported region records
+// zero up to 8 int32 arrays in one launch (instead of one memset node each)
+struct ZeroList {
+  int* p[8];
+  long long n[8];   // elements
+  int count;
+};
+cudaError_t launch_zero(const ZeroList& z, cudaStream_t s);
+
 cudaError_t launch_region_keys(const RegionRec* regions, long long n, const int* cand_rank, int bits_v, int bits_b,
                                int bits_p, unsigned long long* keys, int* vals, cudaStream_t s);
 
