@@ -924,18 +924,28 @@ constexpr int kBorderTilesPerBlock = 1;
 #ifndef ADPS_BORDER_MATCH
 #define ADPS_BORDER_MATCH 1
 #endif
+#ifndef ADPS_BORDER_GRID3
+#define ADPS_BORDER_GRID3 1
+#endif
+static_assert(!ADPS_BORDER_GRID3 || kBorderTilesPerBlock == 1, "the 3-D border grid is a block per tile");
 __global__ void __launch_bounds__(kBorderSlots * kBorderTilesPerBlock) border_kernel(BorderParams P) {
   pdl_wait();   // programmatic dependent launch: the previous kernel's results are visible
   // 128 threads = the tile's border slots; warp w = side w (top, bottom, left,
   // right).  Runs along an edge ask for the same union many times: lanes
   // holding the same (fragment, neighbour fragment) pair unite once (match_any)
   // kBorderTilesPerBlock tiles per block (short blocks: fewer of them to schedule)
+#if ADPS_BORDER_GRID3
+  // grid (tiles_x, tiles_y, views): the tile coordinates without integer divisions
+  const int txi = blockIdx.x, tyi = blockIdx.y, v = blockIdx.z;
+  const long long tile = ((long long)v * P.tiles_y + tyi) * P.tiles_x + txi;
+#else
   const int tiles_per_view = P.tiles_x * P.tiles_y;
   const long long tile = (long long)blockIdx.x * kBorderTilesPerBlock + threadIdx.x / kBorderSlots;
   if (tile >= P.n_tiles) return;   // warp-uniform
   const int v = (int)(tile / tiles_per_view);
   const int t = (int)(tile % tiles_per_view);
   const int tyi = t / P.tiles_x, txi = t % P.tiles_x;
+#endif
   const int s = threadIdx.x % kBorderSlots;
   const int gp = P.border[tile * kBorderSlots + s];
   if (__all_sync(0xffffffffu, gp < 0)) return;   // warp-uniform
@@ -1196,7 +1206,11 @@ cudaError_t launch_attribution_tail(const AttributionArgs& a, cudaStream_t s, Ma
   B.W = a.W;
   B.H = a.H;
   B.n_tiles = nblocks;
+#if ADPS_BORDER_GRID3
+  if (nblocks > 0) launch_k(border_kernel, dim3(P.tiles_x, P.tiles_y, a.V), kBorderSlots, 0, s, B);
+#else
   launch_k(border_kernel, (unsigned)((nblocks + kBorderTilesPerBlock - 1) / kBorderTilesPerBlock), kBorderSlots * kBorderTilesPerBlock, 0, s, B);
+#endif
   launch_k(resolve_kernel, a.grid_small, 256, 0, s, a.partials, a.partial_parent, a.n_partials, a.partial_cap);
   launch_k(partial_emit_kernel, a.grid_small, 256, 0, s, a.partials, a.partial_parent, a.n_partials, a.partial_cap,
                                                     a.m_min, a.regions, a.n_regions, a.region_cap, a.overflow);

@@ -630,9 +630,6 @@ __device__ __forceinline__ void stage_col(const MergeArgs& a, ColTile& B, long l
 #ifndef ADPS_PAIR_MINB
 #define ADPS_PAIR_MINB 1
 #endif
-#ifndef ADPS_PAIR_STATIC
-#define ADPS_PAIR_STATIC 0
-#endif
 __global__ void __launch_bounds__(kPairWarps * 32, ADPS_PAIR_MINB) pair_tiles_kernel(MergeArgs a) {
   pdl_wait();   // programmatic dependent launch: the previous kernel's results are visible
   extern __shared__ __align__(16) unsigned char pt_smem[];
@@ -662,16 +659,9 @@ __global__ void __launch_bounds__(kPairWarps * 32, ADPS_PAIR_MINB) pair_tiles_ke
   // two reservations in flight: a contended counter's reply takes longer than
   // one pair's work
   long long c_end = 0, pos = 0;
-  unsigned long long c_next1 = ADPS_PAIR_STATIC ? 0ull : grab();
-  unsigned long long c_next2 = ADPS_PAIR_STATIC ? 0ull : grab();
+  unsigned long long c_next1 = grab();
+  unsigned long long c_next2 = grab();
   auto next_index = [&]() -> long long {   // -1 when exhausted
-#if ADPS_PAIR_STATIC
-    // static round-robin (no counter): warp gw takes pairs gw, gw + nwarps, ...
-    const long long w_ = gw + pos * nwarps;
-    ++pos;
-    (void)c_end;
-    return w_ < W ? w_ : -1;
-#endif
     if (pos >= c_end) {
       const long long c = (long long)__shfl_sync(0xffffffffu, c_next1, 0);
       if (c >= W) return -1;

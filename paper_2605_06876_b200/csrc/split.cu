@@ -90,15 +90,21 @@ __device__ __forceinline__ double sclip(double x, double a) {
   return s * fmin(fabs(x), a);
 }
 
+#ifndef ADPS_CHILD_STAGE
+#define ADPS_CHILD_STAGE 1
+#endif
+constexpr int kChildThreads = 128;
+constexpr int kPropWords = (int)(sizeof(Proposal) / 8);
+static_assert(sizeof(Proposal) == 8 * kPropWords && (kPropWords & 1), "Proposal: whole doubles, odd count");
 #ifndef ADPS_CHILD_MINB
 #define ADPS_CHILD_MINB 6
 #endif
-__global__ void __launch_bounds__(128, ADPS_CHILD_MINB) child_init_kernel(ChildArgs a) {
+__global__ void __launch_bounds__(kChildThreads, ADPS_CHILD_MINB) child_init_kernel(ChildArgs a) {
   pdl_wait();   // programmatic dependent launch: the previous kernel's results are visible
   long long n = (long long)*a.n_regions;
   if (n > a.region_cap) n = a.region_cap;
-  for (long long rid = (long long)blockIdx.x * blockDim.x + threadIdx.x; rid < n;
-       rid += (long long)gridDim.x * blockDim.x) {
+  // a region's proposal record, into `prow` (a shared-memory row) or straight to global
+  auto body = [&](long long rid, double* prow) {
     const RegionRec R = a.regions[rid];
     // ---- region_stats (ref/error_partition.py:137-158), exact integer moments
     const long long cnt = R.m[0];
@@ -206,17 +212,18 @@ __global__ void __launch_bounds__(128, ADPS_CHILD_MINB) child_init_kernel(ChildA
       if (det < 0)
         for (int i = 0; i < 3; ++i) rot[i * 3 + 2] = -rot[i * 3 + 2];
       for (int i = 0; i < 3; ++i) mu[i] = cam.c[i] + tstar * dir[i];
-      Proposal P;
+      Proposal* const P = prow ? reinterpret_cast<Proposal*>(prow) : a.props + rid;
       for (int i = 0; i < 3; ++i) {
-        P.mu[i] = mu[i];
-        P.rgb[i] = rgb[i];
+        P->mu[i] = mu[i];
+        P->rgb[i] = rgb[i];
       }
       const double sq[3] = {s1 * s1, s2 * s2, s2 * s2};
       const double iq[3] = {1.0 / sq[0], 1.0 / sq[1], 1.0 / sq[2]};
-      rdrt(rot, sq, P.cov);
-      rdrt(rot, iq, P.prec);
-      P.inv_smax = 1.0 / fmax(s1, s2);
-      a.props[rid] = P;
+      rdrt(rot, sq, P->cov);
+      rdrt(rot, iq, P->prec);
+      P->inv_smax = 1.0 / fmax(s1, s2);
+    } else if (prow) {
+      for (int i = 0; i < kPropWords; ++i) prow[i] = 0.0;   // (an invalid region's record is never read)
     }
     a.valid[rid] = ok ? 1 : 0;
     if (a.write_keys) {
@@ -236,7 +243,24 @@ __global__ void __launch_bounds__(128, ADPS_CHILD_MINB) child_init_kernel(ChildA
       for (int i = 0; i < 9; ++i) c[3 + i] = rot[i];
       c[12] = s1; c[13] = s2; c[14] = s2; c[15] = ok ? 1.0 : 0.0;
     }
+  };
+#if ADPS_CHILD_STAGE
+  // records staged in shared memory, then stored as one contiguous run per
+  // block (a thread's 152-byte record stored directly is 19 strided stores)
+  __shared__ double sp[kChildThreads * kPropWords];   // odd row stride: no bank conflicts
+  for (long long base = (long long)blockIdx.x * kChildThreads; base < n; base += (long long)gridDim.x * kChildThreads) {
+    const long long rid = base + threadIdx.x;
+    if (rid < n) body(rid, sp + threadIdx.x * kPropWords);
+    __syncthreads();
+    const long long rows = n - base < kChildThreads ? n - base : kChildThreads;
+    double* dst = reinterpret_cast<double*>(a.props + base);
+    for (int w = threadIdx.x; w < rows * kPropWords; w += kChildThreads) dst[w] = sp[w];
+    __syncthreads();
   }
+#else
+  for (long long rid = (long long)blockIdx.x * blockDim.x + threadIdx.x; rid < n; rid += (long long)gridDim.x * blockDim.x)
+    body(rid, nullptr);
+#endif
 }
 
 __global__ void region_keys_kernel(const RegionRec* __restrict__ regions, long long n, const int* __restrict__ cand_rank,
@@ -276,7 +300,7 @@ cudaError_t launch_region_keys(const RegionRec* regions, long long n, const int*
 }
 
 cudaError_t launch_child_init(const ChildArgs& a, cudaStream_t s) {
-  launch_k(child_init_kernel, a.grid, 128, 0, s, a);
+  launch_k(child_init_kernel, a.grid, kChildThreads, 0, s, a);
   return cudaGetLastError();
 }
 
