@@ -886,23 +886,26 @@ struct GroupStartPolicy {
 
 
 // groups of up to kSmallGroup members: one thread per group, members summed in
-// ascending index order; also writes the sort padding beyond the group count
+// ascending index order; every group's first-of-candidate mark
 #ifndef ADPS_GROUP_MINB
 #define ADPS_GROUP_MINB 6
 #endif
-__global__ void __launch_bounds__(128, ADPS_GROUP_MINB) group_small_kernel(MergeArgs a, long long cap) {
+constexpr int kGroupThreads = 128;
+constexpr int kGroupWords = (int)(sizeof(GroupRec) / 8);
+static_assert(sizeof(GroupRec) == 8 * kGroupWords && (kGroupWords & 1), "GroupRec: whole doubles, odd count");
+__global__ void __launch_bounds__(kGroupThreads, ADPS_GROUP_MINB) group_small_kernel(MergeArgs a, long long cap) {
   pdl_wait();   // programmatic dependent launch: the previous kernel's results are visible
   const long long G = (long long)a.ctr->n_groups_all;
-  for (long long g = (long long)blockIdx.x * blockDim.x + threadIdx.x; g < cap;
-       g += (long long)gridDim.x * blockDim.x) {
-    if (g >= G) continue;
+  // the group's record into R (a shared-memory row, stored by the block after);
+  // false for the groups the warp / block reductions own
+  auto body = [&](long long g, GroupRec& R) -> bool {
     const int b = a.grp_first[g], e = a.grp_first[g + 1];
     const int cnt = e - b;
     {   // groups of a candidate are contiguous: mark the first one
       const int k = a.pcand[a.gkey_sorted[b]];
       if (g == 0 || a.pcand[a.gkey_sorted[a.grp_first[g - 1]]] != k) a.gfirst_of[k] = (int)g;
     }
-    if (cnt > kSmallGroup) continue;   // the warp / block reductions (lists built by the scan)
+    if (cnt > kSmallGroup) return false;   // the warp / block reductions (lists built by the scan)
     double acc[12] = {0};
     for (int m = b; m < e; ++m) {
       const Proposal& M = a.props_s[a.gval_sorted[m]];
@@ -912,7 +915,6 @@ __global__ void __launch_bounds__(128, ADPS_GROUP_MINB) group_small_kernel(Merge
       }
       for (int t = 0; t < 6; ++t) acc[6 + t] += M.cov[t];
     }
-    GroupRec R;
     for (int t = 0; t < 3; ++t) {
       R.mu[t] = acc[t] / cnt;
       R.rgb[t] = acc[3 + t] / cnt;
@@ -935,11 +937,29 @@ __global__ void __launch_bounds__(128, ADPS_GROUP_MINB) group_small_kernel(Merge
       ext = fmax(ext, R.lam[r]);
     }
     R.extent = ext;
-    a.groups[g] = R;
     const int k = a.pcand[a.gkey_sorted[b]];
     a.gpar[g] = k;
     a.gext[g] = ext;
     atomicAdd(&a.n_groups[k], 1);
+    return true;
+  };
+  // records staged in shared memory and stored per block (a thread's 152-byte
+  // record stored directly is 19 strided stores); only this kernel's rows
+  __shared__ double sr[kGroupThreads * kGroupWords];   // odd row stride: no bank conflicts
+  __shared__ unsigned mine[kGroupThreads / 32];
+  for (long long base = (long long)blockIdx.x * kGroupThreads; base < cap; base += (long long)gridDim.x * kGroupThreads) {
+    const long long g = base + threadIdx.x;
+    const bool w = g < G && body(g, *reinterpret_cast<GroupRec*>(sr + threadIdx.x * kGroupWords));
+    const unsigned m = __ballot_sync(0xffffffffu, w);
+    if ((threadIdx.x & 31) == 0) mine[threadIdx.x >> 5] = m;
+    __syncthreads();
+    const long long rows = G - base < kGroupThreads ? G - base : kGroupThreads;
+    double* dst = reinterpret_cast<double*>(a.groups + base);
+    for (int i = threadIdx.x; i < rows * kGroupWords; i += kGroupThreads) {
+      const int r = i / kGroupWords;
+      if ((mine[r >> 5] >> (r & 31)) & 1u) dst[i] = sr[i];
+    }
+    __syncthreads();
   }
 }
 
