@@ -345,6 +345,9 @@ ADPS_API adps_status adps_step_phase1_finish(adps_plan* plan, void* stream, int6
                                               sort of the fp64 depths, a sync per view (same images) */
 #define ADPS_PARAM_RENDER_PAIR_CAP 13      /* (tile, splat) pairs the fast path's tile sort covers (learned
                                               at the plan's first render; grown when a view exceeds it) */
+#define ADPS_PARAM_CAP_HUGE 14             /* parents with more merged groups than this (default 4096, at
+                                              least 64) take the cap's selection by a thread-block cluster
+                                              (distributed shared memory); same results */
 ADPS_API adps_status adps_set_param(adps_plan* plan, int32_t key, int64_t value);
 ADPS_API adps_status adps_get_param(adps_plan* plan, int32_t key, int64_t* value);
 

@@ -18,7 +18,7 @@ ADPS_CUDA_ERROR, ADPS_OOM, ADPS_BAD_STATE, ADPS_INTERNAL = 4, 5, 6, 7
 CASE_SPLIT, CASE_FALLBACK, CASE_RESET = 0, 1, 2
 PARAM_LARGE_THRESHOLD, PARAM_TILE_PATH, PARAM_DEFERRED_TILES = 1, 2, 3
 PARAM_NORMALS_CONSUMED, PARAM_NORMALS_STATUS, PARAM_RAW_CACHE = 4, 5, 6
-PARAM_RENDER_BINNING, PARAM_RENDER_PAIR_CAP = 12, 13
+PARAM_RENDER_BINNING, PARAM_RENDER_PAIR_CAP, PARAM_CAP_HUGE = 12, 13, 14
 BUF_DOM_FLAG, BUF_REGIONS, BUF_PROPOSALS, BUF_VALID = 1, 2, 3, 4
 BUF_CAND_MERGED, BUF_CAND_INS, BUF_CHILDREN, BUF_LO, BUF_THRESHOLDS = 5, 6, 7, 8, 9
 

@@ -20,6 +20,8 @@
 
 #include "merge.cuh"
 
+#include <cooperative_groups.h>
+
 #ifndef ADPS_MERGE_STATS
 #define ADPS_MERGE_STATS 0
 #endif
@@ -1133,7 +1135,6 @@ cudaError_t launch_merge_groups(const MergeArgs& a, long long cap, ScanState st,
 
 constexpr int kCapThreadMax = 64;
 constexpr int kSelMax = 1024;   // n_max up to this: block top-n_max selection per parent
-constexpr int kSelHuge = 4096;  // parents with more groups: extents staged in shared memory
 constexpr int kSelSmemKeys = 49152;   // high 32 bits of the extent bits, 4 B each
 
 __device__ __forceinline__ void cap_write(const MergeArgs& a, long long g, int k, int Gk, int rank) {
@@ -1158,8 +1159,8 @@ __global__ void cap_small_kernel(MergeArgs a, long long cap) {
     const int Gk = a.n_groups[k];
     if (Gk > kCapThreadMax) {
       if (a.n_max <= kSelMax) {   // one entry per parent for the block selection
-        // (parents with > kSelHuge groups are found by cap_select_kernel<true> itself)
-        if (g == a.gfirst_of[k] && Gk <= kSelHuge) a.glist[2 * cap + atomicAdd(&a.ctr->n_cap_large, 1ull)] = k;
+        // (parents with > sel_huge groups are found by the huge-parent kernel itself)
+        if (g == a.gfirst_of[k] && Gk <= a.sel_huge) a.glist[2 * cap + atomicAdd(&a.ctr->n_cap_large, 1ull)] = k;
       } else {                    // one entry per group for the block-per-group ranks
         a.glist[2 * cap + atomicAdd(&a.ctr->n_cap_large, 1ull)] = (int)g;
       }
@@ -1239,7 +1240,7 @@ __global__ void __launch_bounds__(HUGE ? 1024 : 256) cap_select_kernel(MergeArgs
   __shared__ int wtot[NW];
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   // the parents: from cap_small_kernel's list, or (HUGE, on the second stream,
-  // independent of cap_small_kernel) every candidate with > kSelHuge groups
+  // independent of cap_small_kernel) every candidate with > sel_huge groups
   __shared__ int huge_k[NT];
   __shared__ int n_huge;
   const long long n_split = (long long)a.ctr->n_split;
@@ -1251,7 +1252,7 @@ __global__ void __launch_bounds__(HUGE ? 1024 : 256) cap_select_kernel(MergeArgs
       if (tid == 0) n_huge = 0;
       __syncthreads();
       const long long kk = i * NT + tid;
-      if (kk < n_split && a.n_groups[kk] > kSelHuge) huge_k[atomicAdd(&n_huge, 1)] = (int)kk;
+      if (kk < n_split && a.n_groups[kk] > a.sel_huge) huge_k[atomicAdd(&n_huge, 1)] = (int)kk;
       __syncthreads();
       n_here = n_huge;
     }
@@ -1402,18 +1403,251 @@ __global__ void __launch_bounds__(HUGE ? 1024 : 256) cap_select_kernel(MergeArgs
   }
 }
 
+// The parents with > sel_huge groups (a background Gaussian's thousands of
+// groups): the same radix selection as cap_select_kernel<true>, by a cluster
+// of kCapCS blocks.  Each block holds a contiguous 1/kCapCS of the parent's
+// groups (their extents' high words staged in its shared memory) and counts
+// its digit histogram; the counts are added into the leading block's
+// histogram through distributed shared memory, the leader selects the bin,
+// and every block reads the selection back -- two cluster barriers per digit
+// instead of one block passing over all groups.  Ties at the threshold are
+// kept in group order across the blocks (each block's tie base = the tie
+// counts of the blocks before it); the leader ranks and writes the kept.
+#ifndef ADPS_CAP_CLUSTER
+#define ADPS_CAP_CLUSTER 1
+#endif
+constexpr int kCapCS = 8;                // blocks per cluster (portable maximum)
+constexpr int kCapCT = 1024;             // threads per block
+constexpr int kCapStage = 6144;          // staged keys per block (Gk <= 49152 staged)
+namespace cg = cooperative_groups;
+__global__ void __cluster_dims__(kCapCS, 1, 1) __launch_bounds__(kCapCT) cap_huge_cluster_kernel(MergeArgs a) {
+  pdl_wait();   // programmatic dependent launch: the previous kernel's results are visible
+  constexpr int NT = kCapCT, NW = NT / 32, J = 8, RND = NT * J;
+  cg::cluster_group cl = cg::this_cluster();
+  const int crank = (int)cl.block_rank();
+  __shared__ unsigned skeys_hi[kCapStage];
+  __shared__ unsigned hist[256];
+  // leader-owned state (read and updated by the other blocks through DSMEM)
+  __shared__ unsigned ghist[256];
+  __shared__ unsigned long long s_prefix, s_mask;
+  __shared__ int s_need, s_done, s_nkeep;
+  __shared__ int tie_cnt[kCapCS];
+  __shared__ int keep_g[kSelMax];
+  // block-local
+  __shared__ int huge_k[NT];
+  __shared__ int wtot[NW];
+  __shared__ int s_tie_base;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  unsigned* const L_ghist = cl.map_shared_rank(ghist, 0);
+  unsigned long long* const L_prefix = cl.map_shared_rank(&s_prefix, 0);
+  unsigned long long* const L_mask = cl.map_shared_rank(&s_mask, 0);
+  int* const L_need = cl.map_shared_rank(&s_need, 0);
+  int* const L_done = cl.map_shared_rank(&s_done, 0);
+  int* const L_nkeep = cl.map_shared_rank(&s_nkeep, 0);
+  int* const L_tie = cl.map_shared_rank(tie_cnt, 0);
+  int* const L_keep = cl.map_shared_rank(keep_g, 0);
+  const long long n_split = (long long)a.ctr->n_split;
+  const long long nl = (n_split + NT - 1) / NT;
+  const long long cid = blockIdx.x / kCapCS, ncl = gridDim.x / kCapCS;
+  for (long long i = cid; i < nl; i += ncl) {   // cluster-uniform
+    // this range's huge parents in index order (the same list in every block)
+    const long long kk = i * NT + tid;
+    const bool hp = kk < n_split && a.n_groups[kk] > a.sel_huge;
+    const unsigned bm = __ballot_sync(0xffffffffu, hp);
+    if (lane == 0) wtot[wid] = __popc(bm);
+    __syncthreads();
+    int base = 0, n_here = 0;
+    for (int w = 0; w < NW; ++w) {
+      if (w < wid) base += wtot[w];
+      n_here += wtot[w];
+    }
+    if (hp) huge_k[base + __popc(bm & ((1u << lane) - 1u))] = (int)kk;
+    __syncthreads();
+    for (int hi_ = 0; hi_ < n_here; ++hi_) {
+      const int k = huge_k[hi_];
+      const int Gk = a.n_groups[k];
+      const long long f0 = a.gfirst_of[k];
+      const unsigned long long* key = reinterpret_cast<const unsigned long long*>(a.gext) + f0;
+      const long long per = ((long long)Gk + kCapCS - 1) / kCapCS;
+      const long long lo = min((long long)Gk, per * crank), hi = min((long long)Gk, lo + per);
+      const bool staged = per <= kCapStage;
+      if (staged)
+        for (long long h = lo + tid; h < hi; h += NT) skeys_hi[h - lo] = (unsigned)(__ldg(key + h) >> 32);
+      auto key_at = [&](long long h, unsigned long long m, unsigned long long p) -> unsigned long long {
+        if (!staged) return __ldg(key + h);
+        const unsigned hw = skeys_hi[h - lo];
+        unsigned long long kv = (unsigned long long)hw << 32;
+        if ((m & 0xffffffffull) && (hw & (unsigned)(m >> 32)) == (unsigned)(p >> 32)) kv = __ldg(key + h);
+        return kv;
+      };
+      if (crank == 0) {
+        if (tid < 256) ghist[tid] = 0u;
+        if (tid == 0) {
+          s_prefix = 0ull;
+          s_mask = 0ull;
+          s_need = a.n_max < Gk ? a.n_max : Gk;
+          s_done = Gk <= a.n_max;
+          s_nkeep = 0;
+        }
+      }
+      cl.sync();   // staged keys and the leader's state ready
+      for (int shift = 56; shift >= 0; shift -= 8) {
+        if (*L_done) break;   // cluster-uniform: read after a cluster barrier
+        const unsigned long long pre = *L_prefix, msk = *L_mask;
+        if (tid < 256) hist[tid] = 0u;
+        __syncthreads();
+        for (long long h0 = lo; h0 < hi; h0 += RND) {   // block-uniform trip count
+          unsigned long long kv[J];
+#pragma unroll
+          for (int j = 0; j < J; ++j) {
+            const long long h = h0 + (long long)j * NT + tid;
+            kv[j] = h < hi ? key_at(h, msk | (255ull << shift), pre) : 0ull;
+          }
+#pragma unroll
+          for (int j = 0; j < J; ++j) {
+            const long long h = h0 + (long long)j * NT + tid;
+            const bool hit = h < hi && (kv[j] & msk) == pre;
+            const unsigned bin = hit ? (unsigned)((kv[j] >> shift) & 255u) : 256u;
+            const unsigned peers = __match_any_sync(0xffffffffu, bin);
+            if (hit && lane == __ffs(peers) - 1) atomicAdd(&hist[bin], (unsigned)__popc(peers));
+          }
+        }
+        __syncthreads();
+        if (tid < 256 && hist[tid]) atomicAdd(L_ghist + tid, hist[tid]);
+        cl.sync();   // the cluster's histogram is complete
+        if (crank == 0 && wid == 0) {
+          // the bin holding the need-th largest key (as cap_select_kernel)
+          int hv[8], c = 0;
+#pragma unroll
+          for (int j = 0; j < 8; ++j) c += (hv[j] = (int)ghist[255 - 8 * lane - j]);
+          int x = c;
+#pragma unroll
+          for (int o = 1; o < 32; o <<= 1) {
+            const int t = __shfl_up_sync(0xffffffffu, x, o);
+            if (lane >= o) x += t;
+          }
+          const int need0 = s_need, before = x - c;
+          const unsigned own = __ballot_sync(0xffffffffu, before < need0 && need0 <= x);
+          if (lane == (own ? __ffs(own) - 1 : 31)) {
+            int need = need0 - before, b = 255 - 8 * lane, hb = hv[0];
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+              b = 255 - 8 * lane - j;
+              hb = hv[j];
+              if (b == 0 || hb >= need) break;
+              need -= hb;
+            }
+            s_need = need;
+            s_prefix = pre | ((unsigned long long)b << shift);
+            s_mask = msk | (255ull << shift);
+            if (hb == need || shift == 0) s_done = 1;
+          }
+          __syncwarp();
+#pragma unroll
+          for (int j = 0; j < 8; ++j) ghist[lane * 8 + j] = 0u;   // for the next digit
+        }
+        cl.sync();   // the selection is visible
+      }
+      // kept: keys above the selected prefix range, and the first s_need of the
+      // prefix-matching ones in group order (blocks in rank order, then
+      // threads, then each thread's J consecutive groups)
+      const bool all = Gk <= a.n_max;
+      const unsigned long long pre = *L_prefix, msk = *L_mask;
+      const int need = *L_need;
+      {   // this block's tie count -> the leader
+        int c = 0;
+        for (long long h = lo + tid; h < hi; h += NT) c += !all && (key_at(h, msk, pre) & msk) == pre;
+        for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+        if (lane == 0) wtot[wid] = c;
+        __syncthreads();
+        if (tid == 0) {
+          int t = 0;
+          for (int w = 0; w < NW; ++w) t += wtot[w];
+          L_tie[crank] = t;
+        }
+      }
+      cl.sync();   // every block's tie count is in
+      if (tid == 0) {
+        int t = 0;
+        for (int r = 0; r < crank; ++r) t += L_tie[r];
+        s_tie_base = t;
+      }
+      __syncthreads();
+      for (long long h0 = lo; h0 < hi; h0 += RND) {
+        const long long hb = h0 + (long long)tid * J;   // thread tid owns groups [hb, hb + J)
+        unsigned long long kv[J];
+#pragma unroll
+        for (int j = 0; j < J; ++j) kv[j] = hb + j < hi ? key_at(hb + j, msk, pre) : 0ull;
+        unsigned above = 0u, in = 0u;
+#pragma unroll
+        for (int j = 0; j < J; ++j) {
+          if (hb + j < hi) {
+            if (all || (kv[j] & msk) > pre) above |= 1u << j;
+            else if ((kv[j] & msk) == pre) in |= 1u << j;
+          }
+        }
+        const int cnt = __popc(in);
+        int x = cnt;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const int t = __shfl_up_sync(0xffffffffu, x, o);
+          if (lane >= o) x += t;
+        }
+        if (lane == 31) wtot[wid] = x;
+        __syncthreads();
+        int before = x - cnt, tot = 0;
+        for (int w = 0; w < NW; ++w) {
+          if (w < wid) before += wtot[w];
+          tot += wtot[w];
+        }
+        int tr = s_tie_base + before;
+        for (int j = 0; j < J; ++j) {
+          const bool is_in = (in >> j) & 1u;
+          if (((above >> j) & 1u) || (is_in && tr < need)) L_keep[atomicAdd(L_nkeep, 1)] = (int)(f0 + hb + j);
+          tr += is_in;
+        }
+        __syncthreads();
+        if (tid == 0) s_tie_base += tot;
+        __syncthreads();
+      }
+      cl.sync();   // every kept group is in the leader's list
+      if (crank == 0) {   // rank among the kept by (-extent, group order) and write
+        const int nk = s_nkeep;
+        for (int q = tid; q < nk; q += NT) {
+          const long long g = keep_g[q];
+          const double e = a.gext[g];
+          int rank = 0;
+          for (int j = 0; j < nk; ++j) {
+            const long long h = keep_g[j];
+            const double eh = a.gext[h];
+            rank += (eh > e) || (eh == e && h < g);
+          }
+          cap_write(a, g, k, Gk, rank);
+        }
+      }
+      cl.sync();   // the leader's state is free for the next parent
+    }
+    __syncthreads();   // huge_k / wtot reused by the next range
+  }
+}
+
 cudaError_t launch_merge_cap(const MergeArgs& a, long long cap, cudaStream_t s, cudaStream_t aux,
                              cudaEvent_t fork, cudaEvent_t join) {
   long long b = (cap + 255) / 256;
   if (a.n_max <= kSelMax) {
     // the parents with the most groups (shared-memory selection) on the second
     // stream, concurrently with the thread-per-group ranks and the block selection
-    const int smem = kSelSmemKeys * 4;
-    cudaError_t e = cudaFuncSetAttribute(cap_select_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    if (e != cudaSuccess) return e;
+    cudaError_t e;
     if ((e = cudaEventRecord(fork, s)) != cudaSuccess) return e;
     if ((e = cudaStreamWaitEvent(aux, fork, 0)) != cudaSuccess) return e;
-    launch_k(cap_select_kernel<true>, 16, 1024, smem, aux, a, cap);
+    if (ADPS_CAP_CLUSTER) {
+      launch_k(cap_huge_cluster_kernel, 16 * kCapCS, kCapCT, 0, aux, a);
+    } else {
+      const int smem = kSelSmemKeys * 4;
+      e = cudaFuncSetAttribute(cap_select_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+      if (e != cudaSuccess) return e;
+      launch_k(cap_select_kernel<true>, 16, 1024, smem, aux, a, cap);
+    }
     if ((e = cudaEventRecord(join, aux)) != cudaSuccess) return e;
     launch_k(cap_small_kernel, (unsigned)(b < 1 ? 1 : (b > 65535 ? 65535 : b)), 256, 0, s, a, cap);
     launch_k(cap_select_kernel<false>, a.grid, 256, 0, s, a, cap);

@@ -20,6 +20,10 @@ constexpr int kMortonBits = ADPS_MORTON_BITS;   // per axis (<= 10)
 //
 // Proposal space: valid proposals (t* > 0) gathered in reference order
 // (candidate, view, band, first pixel); candidate k owns [pstart[k], +P_k).
+// default MergeArgs::sel_huge (ADPS_PARAM_CAP_HUGE): parents with more merged
+// groups take the cap's cluster selection
+constexpr int kSelHuge = 4096;
+
 struct MergeArgs {
   // inputs
   const unsigned long long* keys_sorted;   // region sort keys
@@ -36,6 +40,7 @@ struct MergeArgs {
   double gamma_d, gamma_c;
   int n_max;
   int small_max;                           // P <= small_max: warp path for the gates
+  int sel_huge;                            // more groups than this: the cap's cluster selection
   // proposal space
   Proposal* props_s;                       // [cap]
   int* psrc;                               // [cap] proposal q -> region id (gather source)

@@ -145,6 +145,7 @@ struct adps_plan {
   long long launches = 0;
   long long lib_calls = 0;
   int large_threshold = 32;
+  int cap_huge = kSelHuge;   // ADPS_PARAM_CAP_HUGE
   // second stream: small-parent gates and the survivor scan overlap the merge
   cudaStream_t aux = nullptr;
   cudaEvent_t ev_fork = nullptr, ev_small = nullptr, ev_keep = nullptr, ev_nfork = nullptr, ev_norm = nullptr;
@@ -1416,6 +1417,7 @@ static adps_status phase1_merge_part(adps_plan* P, cudaStream_t s) {
   ma.gamma_c = cfg->gamma_c;
   ma.n_max = cfg->n_max;
   ma.small_max = P->large_threshold;
+  ma.sel_huge = P->cap_huge;
   ma.props_s = P->props_s.as<Proposal>();
   ma.psrc = P->psrc.as<int>();
   ma.pcand = P->pcand.as<int>();
@@ -2069,6 +2071,11 @@ extern "C" adps_status adps_set_param(adps_plan* P, int32_t key, int64_t value) 
     P->large_threshold = (int)value;
     return ADPS_OK;
   }
+  if (key == ADPS_PARAM_CAP_HUGE) {
+    if (value < 64 || value > 1000000000) return fail(ADPS_INVALID_ARG, "cap huge threshold must be in [64, 1e9]");
+    P->cap_huge = (int)value;
+    return ADPS_OK;
+  }
   if (key == ADPS_PARAM_PIPELINE_CHUNKS) {
     if (value < 1 || value > adps_plan::kMaxChunks) return fail(ADPS_INVALID_ARG, "pipeline chunks must be in [1,16]");
     P->pipeline_chunks = (int)value;
@@ -2109,6 +2116,7 @@ extern "C" adps_status adps_get_param(adps_plan* P, int32_t key, int64_t* value)
   if (!P || !value) return fail(ADPS_INVALID_ARG, "NULL argument");
   switch (key) {
     case ADPS_PARAM_LARGE_THRESHOLD: *value = P->large_threshold; return ADPS_OK;
+    case ADPS_PARAM_CAP_HUGE: *value = P->cap_huge; return ADPS_OK;
     case ADPS_PARAM_TILE_PATH: *value = P->tile_path; return ADPS_OK;
     case ADPS_PARAM_RAW_CACHE: *value = P->raw_cache; return ADPS_OK;
     case ADPS_PARAM_RENDER_BINNING: *value = P->render_fast; return ADPS_OK;

@@ -36,12 +36,16 @@ def op():
     return operator
 
 
-def _stage_isolated(op, name, views):
+def _stage_isolated(op, name, views, cap_huge=None):
     import torch
+    from paper_2605_06876_b200 import _abi
     from paper_2605_06876_b200 import synth as S
     from paper_2605_06876_b200.types import AdpSplitConfig
     wl = S.CONFIGS[name]
     plan = op.Plan("cuda:0")
+    if cap_huge is not None:
+        plan.set_param(_abi.PARAM_CAP_HUGE, cap_huge)
+        assert plan.get_param(_abi.PARAM_CAP_HUGE) == cap_huge
     d = wl.build_device(plan)
     ini, cams, (ga, den) = d["ini"], d["cams"], d["stats"]
     cams_k = cams[views]
@@ -67,6 +71,7 @@ def _stage_isolated(op, name, views):
     assert c["n_regions"] == sum(len(r) for r in ores.regions.values())
     assert c["n_fallback"] == sum(r.fallback for r in ores.candidates)
     assert c["n_reset"] == len(ores.reset_indices)
+    c["max_groups"] = max((len(v) for v in ores.all_groups.values()), default=0)   # before the cap
     return st, c
 
 
@@ -80,6 +85,16 @@ def test_config3_view_subset_stage_isolated(op):
     st, c = _stage_isolated(op, "config3", [0, 16, 32, 48])
     assert st["mismatched"] == 0, st
     assert c["n_regions"] > 1000 and c["n_children"] > 100, c
+
+
+def test_cap_cluster_selection_stage_isolated(op):
+    """Every parent with more than 64 merged groups through the cap's
+    thread-block-cluster selection (the path of config 3's background parent
+    with thousands of groups at 64 views): same results as the oracle."""
+    st, c = _stage_isolated(op, "config3", [0, 16, 32, 48], cap_huge=64)
+    assert st["mismatched"] == 0, st
+    assert c["max_groups"] > 64, c   # the cluster path ran
+    assert c["n_children"] > 100, c
 
 
 def test_config4_view_subset_stage_isolated(op):

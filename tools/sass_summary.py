@@ -9,7 +9,7 @@ import sys
 
 LIB = "paper_2605_06876_b200/libadps.so"
 CLASSES = ["ACQBULK", "UBLKCP", "SYNCS", "LDGSTS", "REDUX", "MATCH", "VOTE", "SHFL", "ATOMS", "ATOMG", "RED",
-           "BAR", "MUFU", "DFMA", "DADD", "DMUL", "HMMA", "UTCMMA", "UTCHMMA"]
+           "BAR", "MUFU", "DFMA", "DADD", "DMUL", "HMMA", "UTCMMA", "UTCHMMA", "UCGABAR_ARV", "UCGABAR_WAIT", "ATOM"]
 out = subprocess.run(["cuobjdump", "-sass", LIB], capture_output=True, text=True).stdout
 kern, counts = None, collections.OrderedDict()
 for line in out.splitlines():
