@@ -909,13 +909,21 @@ __global__ void __launch_bounds__(kGroupThreads, ADPS_GROUP_MINB) group_small_ke
     }
     if (cnt > kSmallGroup) return false;   // the warp / block reductions (lists built by the scan)
     double acc[12] = {0};
-    for (int m = b; m < e; ++m) {
-      const Proposal& M = a.props_s[a.gval_sorted[m]];
-      for (int t = 0; t < 3; ++t) {
-        acc[t] += M.mu[t];
-        acc[3 + t] += M.rgb[t];
+    // members in ascending order, a fixed trip count with predicated bodies so
+    // the member indices load together
+    int mi[kSmallGroup];
+#pragma unroll
+    for (int u = 0; u < kSmallGroup; ++u) mi[u] = b + u < e ? a.gval_sorted[b + u] : 0;
+#pragma unroll
+    for (int u = 0; u < kSmallGroup; ++u) {
+      if (b + u < e) {
+        const Proposal& M = a.props_s[mi[u]];
+        for (int t = 0; t < 3; ++t) {
+          acc[t] += M.mu[t];
+          acc[3 + t] += M.rgb[t];
+        }
+        for (int t = 0; t < 6; ++t) acc[6 + t] += M.cov[t];
       }
-      for (int t = 0; t < 6; ++t) acc[6 + t] += M.cov[t];
     }
     for (int t = 0; t < 3; ++t) {
       R.mu[t] = acc[t] / cnt;
@@ -929,11 +937,14 @@ __global__ void __launch_bounds__(kGroupThreads, ADPS_GROUP_MINB) group_small_ke
     for (int r = 0; r < 3; ++r) {
       const double ev[3] = {R.evec[r], R.evec[3 + r], R.evec[6 + r]};
       double best = 0.0;
-      for (int m = b; m < e; ++m) {
-        const Proposal& M = a.props_s[a.gval_sorted[m]];
-        const double off = fabs((M.mu[0] - R.mu[0]) * ev[0] + (M.mu[1] - R.mu[1]) * ev[1] +
-                                (M.mu[2] - R.mu[2]) * ev[2]);
-        best = fmax(best, off + sqrt(sym_quad(M.cov, ev)));
+#pragma unroll
+      for (int u = 0; u < kSmallGroup; ++u) {
+        if (b + u < e) {
+          const Proposal& M = a.props_s[mi[u]];
+          const double off = fabs((M.mu[0] - R.mu[0]) * ev[0] + (M.mu[1] - R.mu[1]) * ev[1] +
+                                  (M.mu[2] - R.mu[2]) * ev[2]);
+          best = fmax(best, off + sqrt(sym_quad(M.cov, ev)));
+        }
       }
       R.lam[r] = best * best;
       ext = fmax(ext, R.lam[r]);
@@ -1169,9 +1180,14 @@ __global__ void cap_small_kernel(MergeArgs a, long long cap) {
     const long long f = a.gfirst_of[k];
     const double e = a.gext[g];
     int rank = 0;
-    for (long long h = f; h < f + Gk && rank < a.n_max; ++h) {
-      const double eh = a.gext[h];
-      rank += (eh > e) || (eh == e && h < g);
+    // 8 extents per round, loaded together (one latency per round instead of
+    // one per group); a rank below n_max is exact, larger ones are not written
+    for (long long h0 = f; h0 < f + Gk && rank < a.n_max; h0 += 8) {
+      double eh[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) eh[u] = h0 + u < f + Gk ? a.gext[h0 + u] : -1.0;   // extents are >= 0
+#pragma unroll
+      for (int u = 0; u < 8; ++u) rank += (eh[u] > e) || (eh[u] == e && h0 + u < g);
     }
     if (rank < a.n_max) cap_write(a, g, k, Gk, rank);
   }
