@@ -172,9 +172,13 @@ __global__ void small_pairs_kernel(MergeArgs a) {
 }
 
 // exclusive scans of up to three count arrays (+ total at [n]), a block each
+#ifndef ADPS_TILE_OWNER_FILL
+#define ADPS_TILE_OWNER_FILL 1   // the tile -> parent map written with the offsets, not searched per tile
+#endif
 struct Offsets3 {
   const unsigned long long* in[3];
   unsigned long long* out[3];
+  int* owner;   // optional: owner[t] = i for t in [out[2][i], out[2][i+1]) (the tile -> parent map)
 };
 __global__ void __launch_bounds__(1024) offsets_1block_kernel(Offsets3 io, const unsigned long long* __restrict__ n_dev) {
   pdl_wait();   // programmatic dependent launch: the previous kernel's results are visible
@@ -213,6 +217,13 @@ __global__ void __launch_bounds__(1024) offsets_1block_kernel(Offsets3 io, const
     __syncthreads();
   }
   if (threadIdx.x == 0) out[n] = carry;
+#if ADPS_TILE_OWNER_FILL
+  if (blockIdx.x == 2 && io.owner) {   // the tile -> large parent map (read by the box kernel and the filter)
+    __syncthreads();                   // every offset of this block is written
+    for (long long i = threadIdx.x; i < n; i += blockDim.x)
+      for (unsigned long long t = out[i]; t < out[i + 1]; ++t) io.owner[t] = (int)i;
+  }
+#endif
 }
 
 __global__ void __launch_bounds__(1024) shard_range_kernel(const int* __restrict__ nvalid, long long n, int rank,
@@ -328,6 +339,7 @@ cudaError_t launch_large_offsets(const MergeArgs& a, cudaStream_t s) {
   io.out[1] = a.lp_off;
   io.in[2] = a.tile_cnt;
   io.out[2] = a.tile_off;
+  io.owner = a.tile_owner;
   launch_k(offsets_1block_kernel, 3, 1024, 0, s, io, &a.ctr->n_large);
   return cudaGetLastError();
 }
@@ -407,7 +419,11 @@ __global__ void box_kernel(MergeArgs a) {
   const unsigned long long n_tiles = n_large > 0 ? a.tile_off[n_large] : 0;
   for (long long t = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); t < (long long)n_tiles;
        t += warps) {
+#if ADPS_TILE_OWNER_FILL
+    const long long l = a.tile_owner[t];   // (filled with the tile offsets)
+#else
     const long long l = find_owner(a.tile_off, n_large, (unsigned long long)t);
+#endif
     const long long tl = t - (long long)a.tile_off[l];
     const long long b = (long long)a.lp_off[l] + tl * kMT;
     const long long e = min(b + kMT, (long long)(a.lp_off[l] + a.lp_cnt[l]));
@@ -470,7 +486,7 @@ __global__ void box_kernel(MergeArgs a) {
       B.r = r * (1.0 + 1e-12) + 1e-300;   // rounding guard: the sphere really encloses
       B.inv_s = inv_s;
       a.boxes[t] = B;
-      a.tile_owner[t] = (int)l;
+      if (!ADPS_TILE_OWNER_FILL) a.tile_owner[t] = (int)l;
     }
   }
 }
