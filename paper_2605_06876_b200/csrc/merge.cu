@@ -871,7 +871,10 @@ cudaError_t launch_merge_flatten(const MergeArgs& a, long long cap, cudaStream_t
 }
 
 // ------------------------------------------------------------------ groups
-constexpr int kSmallGroup = 8;
+#ifndef ADPS_SMALL_GROUP
+#define ADPS_SMALL_GROUP 8
+#endif
+constexpr int kSmallGroup = ADPS_SMALL_GROUP;   // groups up to this size: a thread each
 constexpr int kBlockGroup = 512;   // larger groups: a block per group
 
 struct GroupStartPolicy {
