@@ -627,7 +627,10 @@ __device__ __forceinline__ void cp_async4(void* smem, const void* gmem) {
 }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
 
-constexpr int kTwWarps = 8;
+#ifndef ADPS_TW_WARPS
+#define ADPS_TW_WARPS 8
+#endif
+constexpr int kTwWarps = ADPS_TW_WARPS;   // warps (32-pixel word columns) per block of the words pass
 __global__ void __launch_bounds__(kTwWarps * 32) tile_words_t_kernel(const raw16_t* __restrict__ rawf,
                                                                     const float* __restrict__ image,
                                                                     const float* __restrict__ gt,
